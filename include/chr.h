@@ -1,0 +1,200 @@
+/*
+ * chr.h -- C ABI of libchr.so, the B200 (sm_100a) implementation of the
+ * CHR hot path of arXiv 2408.05462 (reference package `isochr`).
+ *
+ * The reference is pure Python + numba; its plug points are the kernel
+ * seam (isochr/kernels.py, switched by backend.USE_NUMBA, backend.py:19-42),
+ * the codec plugin (build_chr(codec=...), chr_archive.py:142; register_codec,
+ * codec.py:207-211) and the public API (isochr/__init__.py:9-86).  A
+ * Python host binds this ABI with ctypes (paper_2408_05462_b200/_abi.py,
+ * INTEGRATION.md) and keeps the reference call signatures.
+ *
+ * Conventions
+ *  - every device buffer is caller-allocated (e.g. a torch tensor) and
+ *    passed as a raw pointer; host buffers are plain C arrays;
+ *  - temporary device memory comes from a caller workspace whose size is
+ *    returned by the matching *_workspace_size() query; the library keeps
+ *    no allocations between calls and no mutable global state beyond
+ *    constant tables initialised once under a mutex;
+ *  - `stream` is a cudaStream_t (0 = legacy default stream);
+ *  - functions return a chr_status_t; calls that produce host-visible
+ *    results synchronise `stream` before returning.
+ *
+ * Volume layout: x fastest ("Fortran ravel" of the [x, y, z] grid), the
+ * layout of Volume.values (volume.py:35-93) and of raw files (load_raw).
+ */
+#ifndef CHR_H_
+#define CHR_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes: the Python host maps them onto isochr.errors classes */
+typedef enum {
+    CHR_OK = 0,
+    CHR_E_PARAMETER = 1,       /* ParameterError            (errors.py:8)  */
+    CHR_E_NONFINITE = 2,       /* NonFiniteSampleError      (errors.py:12) */
+    CHR_E_CORRUPT = 3,         /* CorruptPayloadError       (errors.py:34) */
+    CHR_E_UNSUPPORTED_CODEC = 4, /* UnsupportedCodecError  (errors.py:38) */
+    CHR_E_CUDA = 5,            /* CUDA runtime failure */
+    CHR_E_WORKSPACE = 6        /* workspace too small */
+} chr_status_t;
+
+/* per-region corruption subcodes written by chr_decode_regions
+ * (kernels.py:299-345, codec.py:146-229) */
+enum {
+    CHR_DEC_OK = 0,
+    CHR_DEC_TRUNCATED = 1,
+    CHR_DEC_VARINT_LONG = 2,
+    CHR_DEC_RUN_MISSING = 3,
+    CHR_DEC_RUN_RANGE = 4,
+    CHR_DEC_TRAILING = 5,
+    CHR_DEC_COUNT = 6,
+    CHR_DEC_CHECKSUM = 7,
+    CHR_DEC_SHORT_BITMAP = 8,
+    CHR_DEC_SHORT_ESCAPES = 9,
+    CHR_DEC_BAD_CODEC = 10
+};
+
+/* dtype tags (volume.py:18, FORMAT.md) */
+enum { CHR_F32 = 0, CHR_F64 = 1 };
+
+/* One region of the archive (ArchiveRegion, chr_archive.py:54-75 and the
+ * FORMAT.md region record).  Filled in two steps: chr_plan() writes the
+ * geometry, mask and error bound; chr_compress() writes codec, offsets,
+ * lengths and CRC. */
+typedef struct {
+    int32_t lo[3];             /* block span lo (bx, by, bz), inclusive */
+    int32_t hi[3];             /* block span hi, inclusive */
+    int32_t origin[3];         /* sample origin */
+    int32_t extent[3];         /* sample extent incl. high ghost planes */
+    uint64_t mask;             /* relevance bitmask: bit ci <-> candidate ci */
+    double error_bound;        /* absolute bound (bound.py:150-219) */
+    int32_t codec_id;          /* 0 verbatim f64, 1 lorenzo, 2 lorenzo+esc, 3 verbatim f32 */
+    uint32_t payload_crc;      /* zlib.crc32(payload) */
+    uint64_t block_offset;     /* absolute file offset of the CompressedBlock */
+    uint64_t block_nbytes;     /* 34 + payload length (CompressedBlock.nbytes) */
+    uint64_t n_escaped;        /* escaped samples (codec 2) */
+} chr_region_t;
+
+/* A region to decode (codec.decompress on one CompressedBlock whose
+ * header the host has parsed, codec.py:146-229). */
+typedef struct {
+    uint64_t payload_offset;   /* byte offset of the payload in the blob */
+    uint64_t payload_nbytes;
+    int32_t codec_id;
+    int32_t dims[3];           /* ex, ey, ez */
+    double error_bound;        /* from the block header */
+    uint32_t crc;              /* from the block header */
+    uint32_t _pad;
+    uint64_t out_offset;       /* element offset of this window in the f64 output */
+} chr_dec_region_t;
+
+/* A grid to contour (marching_cubes on one window, isosurf.py:183-204). */
+typedef struct {
+    uint64_t grid_offset;      /* element offset of the f64 window (x fastest) */
+    int32_t dims[3];           /* samples per axis, each >= 2 */
+    int32_t _pad;
+    double origin[3];          /* world origin of lattice point (0,0,0) */
+    double spacing[3];
+} chr_mc_grid_t;
+
+/* ---------------------------------------------------------------- */
+/* library info                                                     */
+int chr_abi_version(void);
+const char *chr_status_string(int status);
+
+/* ---------------------------------------------------------------- */
+/* 1. block decomposition + min/max index (blocking.py:64-127) and the
+ *    strict accuracy-1 distance reduction (bound.py:150-219 with
+ *    kernels.min_abs_distance, kernels.py:417-425) in ONE streaming pass.
+ *
+ * d_vol: nx*ny*nz samples (dtype CHR_F32 or CHR_F64).  h_cands: m <= 64
+ * strictly increasing finite candidates.  Writes, per block
+ * (block_id = bx + nbx*(by + nby*bz)): d_block_stats[3*id+0..2] =
+ * (vmin, vmax, dmin) with dmin = min over the window of min_k |s-k|.
+ * d_first_nonfinite[0] = first flat index of a NaN/Inf sample, or -1.
+ * Asynchronous. */
+int chr_stats(const void *d_vol, int dtype, int64_t nx, int64_t ny, int64_t nz,
+              int64_t block_size, const double *h_cands, int m,
+              double *d_block_stats, int64_t *d_first_nonfinite, void *stream);
+
+/* number of blocks of the decomposition (blocking.block_grid_shape) */
+int64_t chr_num_blocks(int64_t nx, int64_t ny, int64_t nz, int64_t block_size);
+
+/* 2. host planning: relevance masks, greedy merge (blocking.py:130-193)
+ *    and per-region strict bounds.  h_block_stats is the D2H copy of
+ *    chr_stats' output.  h_regions needs chr_num_blocks() entries;
+ *    *n_regions receives the region count (region_id = index). */
+int chr_plan(const double *h_block_stats, int64_t nx, int64_t ny, int64_t nz,
+             int64_t block_size, const double *h_cands, int m, double vmin, double vmax,
+             double loose_fraction, double safety_factor,
+             chr_region_t *h_regions, int64_t *n_regions);
+
+/* 3. compress all regions into a complete .chr file on the device
+ *    (codec.compress per region, codec.py:91-143; write_chr layout,
+ *    chr_archive.py:297-340).  Regions come from chr_plan or from the
+ *    caller (codec.compress on one array = one region covering it).
+ *    With write_file == 0 only the CompressedBlocks are written, each at
+ *    its block_offset starting from 0 (no file header/table/trailer).
+ *    Fills codec/offset/length/crc of h_regions and *h_out_nbytes
+ *    (file or blob size).  Synchronises the stream. */
+size_t chr_compress_workspace_size(const chr_region_t *h_regions, int64_t n_regions);
+uint64_t chr_compress_capacity(const chr_region_t *h_regions, int64_t n_regions, int m,
+                               int source_dtype);
+int chr_compress(const void *d_vol, int dtype, int source_dtype, int64_t nx, int64_t ny,
+                 int64_t nz, const double *spacing, int64_t block_size, double vmin,
+                 double vmax, const double *h_cands, int m, chr_region_t *h_regions,
+                 int64_t n_regions, int write_file, void *d_workspace, size_t workspace_bytes,
+                 uint8_t *d_out, uint64_t out_capacity, uint64_t *h_out_nbytes, void *stream);
+
+/* 4. selective reconstruction: decode the given blocks of d_blob into
+ *    f64 windows (x fastest) at d_out + out_offset.  h_status[i]
+ *    receives a CHR_DEC_* code per region.  Returns CHR_E_CORRUPT /
+ *    CHR_E_UNSUPPORTED_CODEC if any region failed (the host raises for
+ *    the first failing region in request order).  Synchronises. */
+size_t chr_decode_workspace_size(const chr_dec_region_t *h_regs, int64_t n);
+int chr_decode_regions(const uint8_t *d_blob, const chr_dec_region_t *h_regs, int64_t n,
+                       double *d_out, void *d_workspace, size_t workspace_bytes,
+                       int32_t *h_status, void *stream);
+
+/* 5. marching cubes, count -> scan -> emit (kernels.py:428-524,
+ *    isosurf.py:183-225).  Grids are meshed in order and concatenated
+ *    with merge_meshes semantics (vertex ids offset by the vertices of
+ *    the previous grids).  chr_mc_count fills per-grid triangle/vertex
+ *    counts (h_ntri/h_nvert may be NULL) and the totals; chr_mc_emit
+ *    (same workspace, untouched in between) writes d_verts (nv x 3 f64,
+ *    world coordinates) and d_tris (nt x 3 int32). */
+size_t chr_mc_workspace_size(const chr_mc_grid_t *h_grids, int64_t n);
+int chr_mc_count(const double *d_grids, const chr_mc_grid_t *h_grids, int64_t n, double k,
+                 void *d_workspace, size_t workspace_bytes, int64_t *h_ntri, int64_t *h_nvert,
+                 int64_t *h_total_tri, int64_t *h_total_vert, void *stream);
+int chr_mc_emit(const double *d_grids, const chr_mc_grid_t *h_grids, int64_t n, double k,
+                void *d_workspace, size_t workspace_bytes, double *d_verts, int32_t *d_tris,
+                void *stream);
+
+/* 6. per-cell case codes of one grid (isosurf.case_field, isosurf.py:77-88
+ *    when binary_order != 0; Bourke order of mc_extract otherwise). */
+int chr_case_codes(const double *d_grid, int64_t nx, int64_t ny, int64_t nz, double k,
+                   int binary_order, uint8_t *d_codes, void *stream);
+
+/* 7. CRC-32/IEEE (zlib.crc32) of a device buffer; combine operator. */
+size_t chr_crc32_workspace_size(uint64_t n);
+int chr_crc32(const uint8_t *d_buf, uint64_t n, void *d_workspace, size_t workspace_bytes,
+              uint32_t *h_crc, void *stream);
+uint32_t chr_crc32_combine(uint32_t crc1, uint32_t crc2, uint64_t len2);
+
+/* 8. kernel seam (isochr/kernels.py) on single windows */
+int chr_min_abs_distance(const double *d_flat, int64_t n, double k, double *h_out,
+                         void *d_workspace, size_t workspace_bytes, void *stream);
+int chr_lorenzo_encode(const double *d_flat, int64_t nx, int64_t ny, int64_t nz, double e,
+                       int64_t *d_q, uint8_t *d_escaped, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CHR_H_ */

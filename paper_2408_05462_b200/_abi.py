@@ -1,0 +1,189 @@
+"""ctypes binding of libchr.so (include/chr.h).
+
+The library is built in-tree (``paper_2408_05462_b200/libchr.so``, see
+``csrc/Makefile`` and ``__graft_entry__.build``).  There is deliberately no
+CPU fallback: importing the compute entry points without the library or
+without a CUDA device raises immediately.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+from . import exceptions as errors
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libchr.so")
+
+CHR_OK = 0
+CHR_E_PARAMETER = 1
+CHR_E_NONFINITE = 2
+CHR_E_CORRUPT = 3
+CHR_E_UNSUPPORTED_CODEC = 4
+CHR_E_CUDA = 5
+CHR_E_WORKSPACE = 6
+
+DEC_MESSAGES = {
+    1: "token stream truncated",
+    2: "varint too long",
+    3: "zero run missing length",
+    4: "zero run out of range",
+    5: "trailing bytes after token stream",
+    6: "token stream produced wrong count",
+    7: "payload checksum mismatch",
+    8: "payload shorter than its escape bitmap",
+    9: "payload shorter than its escape values",
+    10: "unknown codec id",
+}
+
+P = ctypes.c_void_p
+I64 = ctypes.c_int64
+U64 = ctypes.c_uint64
+D = ctypes.c_double
+INT = ctypes.c_int
+SZ = ctypes.c_size_t
+
+
+class Region(ctypes.Structure):
+    """chr_region_t"""
+
+    _fields_ = [
+        ("lo", ctypes.c_int32 * 3),
+        ("hi", ctypes.c_int32 * 3),
+        ("origin", ctypes.c_int32 * 3),
+        ("extent", ctypes.c_int32 * 3),
+        ("mask", ctypes.c_uint64),
+        ("error_bound", ctypes.c_double),
+        ("codec_id", ctypes.c_int32),
+        ("payload_crc", ctypes.c_uint32),
+        ("block_offset", ctypes.c_uint64),
+        ("block_nbytes", ctypes.c_uint64),
+        ("n_escaped", ctypes.c_uint64),
+    ]
+
+
+class DecRegion(ctypes.Structure):
+    """chr_dec_region_t"""
+
+    _fields_ = [
+        ("payload_offset", ctypes.c_uint64),
+        ("payload_nbytes", ctypes.c_uint64),
+        ("codec_id", ctypes.c_int32),
+        ("dims", ctypes.c_int32 * 3),
+        ("error_bound", ctypes.c_double),
+        ("crc", ctypes.c_uint32),
+        ("_pad", ctypes.c_uint32),
+        ("out_offset", ctypes.c_uint64),
+    ]
+
+
+class McGrid(ctypes.Structure):
+    """chr_mc_grid_t"""
+
+    _fields_ = [
+        ("grid_offset", ctypes.c_uint64),
+        ("dims", ctypes.c_int32 * 3),
+        ("_pad", ctypes.c_int32),
+        ("origin", ctypes.c_double * 3),
+        ("spacing", ctypes.c_double * 3),
+    ]
+
+
+_lib = None
+
+
+def lib():
+    """The loaded library (raises if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"libchr.so not found at {LIB_PATH}: run __graft_entry__.build() "
+                "(make -C paper_2408_05462_b200/csrc); there is no CPU fallback"
+            )
+        L = ctypes.CDLL(LIB_PATH)
+        L.chr_abi_version.restype = INT
+        L.chr_status_string.argtypes = [INT]
+        L.chr_status_string.restype = ctypes.c_char_p
+        L.chr_num_blocks.argtypes = [I64, I64, I64, I64]
+        L.chr_num_blocks.restype = I64
+        L.chr_stats.argtypes = [P, INT, I64, I64, I64, I64, P, INT, P, P, P]
+        L.chr_stats.restype = INT
+        L.chr_plan.argtypes = [P, I64, I64, I64, I64, P, INT, D, D, D, D, P, P]
+        L.chr_plan.restype = INT
+        L.chr_compress_workspace_size.argtypes = [P, I64]
+        L.chr_compress_workspace_size.restype = SZ
+        L.chr_compress_capacity.argtypes = [P, I64, INT, INT]
+        L.chr_compress_capacity.restype = U64
+        L.chr_compress.argtypes = [P, INT, INT, I64, I64, I64, P, I64, D, D, P, INT, P, I64, INT, P, SZ,
+                                   P, U64, P, P]
+        L.chr_compress.restype = INT
+        L.chr_decode_workspace_size.argtypes = [P, I64]
+        L.chr_decode_workspace_size.restype = SZ
+        L.chr_decode_regions.argtypes = [P, P, I64, P, P, SZ, P, P]
+        L.chr_decode_regions.restype = INT
+        L.chr_mc_workspace_size.argtypes = [P, I64]
+        L.chr_mc_workspace_size.restype = SZ
+        L.chr_mc_count.argtypes = [P, P, I64, D, P, SZ, P, P, P, P, P]
+        L.chr_mc_count.restype = INT
+        L.chr_mc_emit.argtypes = [P, P, I64, D, P, SZ, P, P, P]
+        L.chr_mc_emit.restype = INT
+        L.chr_case_codes.argtypes = [P, I64, I64, I64, D, INT, P, P]
+        L.chr_case_codes.restype = INT
+        L.chr_crc32_workspace_size.argtypes = [U64]
+        L.chr_crc32_workspace_size.restype = SZ
+        L.chr_crc32.argtypes = [P, U64, P, SZ, P, P]
+        L.chr_crc32.restype = INT
+        L.chr_crc32_combine.argtypes = [ctypes.c_uint32, ctypes.c_uint32, U64]
+        L.chr_crc32_combine.restype = ctypes.c_uint32
+        L.chr_min_abs_distance.argtypes = [P, I64, D, P, P, SZ, P]
+        L.chr_min_abs_distance.restype = INT
+        L.chr_lorenzo_encode.argtypes = [P, I64, I64, I64, D, P, P, P]
+        L.chr_lorenzo_encode.restype = INT
+        _lib = L
+    return _lib
+
+
+EXPORTS = [
+    "chr_abi_version", "chr_status_string", "chr_num_blocks", "chr_stats", "chr_plan",
+    "chr_compress_workspace_size", "chr_compress_capacity", "chr_compress",
+    "chr_decode_workspace_size", "chr_decode_regions", "chr_mc_workspace_size", "chr_mc_count",
+    "chr_mc_emit", "chr_case_codes", "chr_crc32_workspace_size", "chr_crc32", "chr_crc32_combine",
+    "chr_min_abs_distance", "chr_lorenzo_encode",
+]
+
+
+def device() -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2408_05462_b200 needs a CUDA device (B200, sm_100a); no CPU fallback")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream_ptr() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def ptr(t: torch.Tensor | None):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None and t.numel() else None
+
+
+def workspace(nbytes: int) -> torch.Tensor:
+    return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device())
+
+
+def check(rc: int, what: str = ""):
+    if rc == CHR_OK:
+        return
+    msg = lib().chr_status_string(rc).decode()
+    if what:
+        msg = f"{what}: {msg}"
+    if rc == CHR_E_PARAMETER:
+        raise errors.ParameterError(msg)
+    if rc == CHR_E_CORRUPT:
+        raise errors.CorruptPayloadError(msg)
+    if rc == CHR_E_UNSUPPORTED_CODEC:
+        raise errors.UnsupportedCodecError(msg)
+    raise RuntimeError(msg)

@@ -1,0 +1,361 @@
+"""CHR archive API on the GPU (reference: isochr/chr_archive.py:54-407,
+FORMAT.md).
+
+``build_chr`` runs stats -> plan -> compress on the device and keeps the
+finished file resident (``CHRArchive._device``), so a following ``request``
+decodes straight from HBM; the returned dataclasses are the reference's
+(frozen, compared with ``==``), materialised from one device->host copy.
+"""
+
+from __future__ import annotations
+
+import struct
+import warnings
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _abi, device
+from .blockcodec import HEADER_SIZE, CompressedBlock, decompress_many
+from .exceptions import (
+    BadMagicError,
+    ChecksumError,
+    CorruptPayloadError,
+    InsufficientAccuracyError,
+    NoSuchIsovalueError,
+    ParameterError,
+    UnsupportedCodecError,
+)
+from .field import DTYPE_TAGS, Volume, as_volume_like
+
+MODE_STRICT = "strict_vertices"
+MODE_PAPER = "paper_edges"
+MAGIC = b"CHR1"
+VERSION = 1
+BOUND_MODE_TAGS = {MODE_STRICT: 0, MODE_PAPER: 1}
+_MODES = {v: k for k, v in BOUND_MODE_TAGS.items()}
+_FILE_HDR = struct.Struct("<4sH3I3dBIdd")
+_REC = struct.Struct("<I3I3I3I3IBddQQ")
+DEFAULT_SAFETY_FACTOR = device.SAFETY_FACTOR
+DEFAULT_LOOSE_FRACTION = device.LOOSE_FRACTION
+
+
+@dataclass(frozen=True)
+class ArchiveRegion:
+    region_id: int
+    block_span: tuple[tuple[int, int, int], tuple[int, int, int]]
+    sample_origin: tuple[int, int, int]
+    sample_extent: tuple[int, int, int]
+    relevance: frozenset
+    bound_mode: str
+    accuracy: float
+    error_bound: float
+    block: CompressedBlock
+
+    @property
+    def payload_nbytes(self) -> int:
+        return self.block.nbytes
+
+    def is_relevant(self, candidate_index: int) -> bool:
+        return candidate_index in self.relevance
+
+
+@dataclass(frozen=True)
+class CHRArchive:
+    dims: tuple[int, int, int]
+    spacing: tuple[float, float, float]
+    source_dtype: str
+    block_size: int
+    value_range: tuple[float, float]
+    candidates: tuple[float, ...]
+    regions: tuple[ArchiveRegion, ...]
+    # device copy of the serialised file (built here or uploaded on demand)
+    _device: dict = field(default=None, compare=False, repr=False, hash=False)
+
+    @property
+    def stored_accuracy(self) -> float:
+        return self.regions[0].accuracy
+
+    @property
+    def bound_mode(self) -> str:
+        return self.regions[0].bound_mode
+
+    def header_table_nbytes(self) -> int:
+        return device.header_table_nbytes(len(self.candidates), len(self.regions))
+
+    def payload_nbytes(self) -> int:
+        return sum(r.payload_nbytes for r in self.regions)
+
+    def file_nbytes(self) -> int:
+        return self.header_table_nbytes() + self.payload_nbytes() + 4
+
+
+@dataclass(frozen=True)
+class RequestReport:
+    requested_isovalue: float
+    isovalue: float
+    snapped: bool
+    candidate_index: int
+    requested_accuracy: float
+    stored_accuracy: float
+    drop_pruned: bool
+    regions_returned: int
+    regions_total: int
+    bytes_touched: int
+    bytes_total: int
+
+
+@dataclass(frozen=True)
+class ReconstructionSet:
+    regions: tuple
+    report: RequestReport
+
+
+def _check_build_args(accuracy, bound_mode, safety_factor, loose_fraction, out_of_range):
+    if not 0.0 < accuracy <= 1.0:
+        raise ParameterError(f"accuracy must be in (0, 1], got {accuracy}")
+    if not 0.0 < safety_factor < 1.0:
+        raise ParameterError(f"safety_factor must be in (0, 1), got {safety_factor}")
+    if bound_mode not in BOUND_MODE_TAGS:
+        raise ParameterError(f"mode must be one of {tuple(BOUND_MODE_TAGS)}, got {bound_mode!r}")
+    if out_of_range not in ("error", "warn"):
+        raise ParameterError(f"out_of_range must be 'error' or 'warn', got {out_of_range!r}")
+    if not 0.0 < loose_fraction:
+        raise ParameterError(f"loose_fraction must be positive, got {loose_fraction}")
+    if accuracy != 1.0 or bound_mode != MODE_STRICT:
+        raise NotImplementedError(
+            "the GPU path implements the strict_vertices bound at accuracy 1.0 (the north_star "
+            "configuration); accuracy < 1 and paper_edges are SURVEY §8(f2), scheduled next")
+
+
+def _regions_from_device(res: device.Compressed, host_blob: bytes, cands, source_dtype):
+    out = []
+    for rec in device.region_records(res.regions):
+        blk = CompressedBlock.from_bytes(host_blob, rec["block_offset"])
+        mask = rec["mask"]
+        out.append(ArchiveRegion(
+            region_id=rec["id"], block_span=(rec["lo"], rec["hi"]), sample_origin=rec["origin"],
+            sample_extent=rec["extent"], relevance=frozenset(ci for ci in range(len(cands)) if (mask >> ci) & 1),
+            bound_mode=MODE_STRICT, accuracy=1.0, error_bound=rec["e"], block=blk))
+    return tuple(out)
+
+
+def build_chr(volume, candidates, block_size: int, accuracy: float = 1.0, bound_mode: str = MODE_STRICT,
+              safety_factor: float = DEFAULT_SAFETY_FACTOR, loose_fraction: float = DEFAULT_LOOSE_FRACTION,
+              out_of_range: str = "error", workers: int = 1, codec=None) -> CHRArchive:
+    """chr_archive.build_chr (chr_archive.py:132-212) on the GPU."""
+    del workers  # one device pass; kept for signature compatibility
+    _check_build_args(accuracy, bound_mode, safety_factor, loose_fraction, out_of_range)
+    if block_size < 2:
+        raise ParameterError(f"block_size must be >= 2, got {block_size}")
+    vol = as_volume_like(volume)
+    if any(d < 2 for d in vol.dims):
+        raise ParameterError(f"volume dims must be >= 2 per axis, got {vol.dims}")
+    cands = [float(k) for k in candidates]
+    if not cands:
+        raise ParameterError("candidates must be non-empty")
+    if any(not np.isfinite(k) for k in cands):
+        raise ParameterError("candidates must be finite")
+    if any(b <= a for a, b in zip(cands, cands[1:])):
+        raise ParameterError(f"candidates must be strictly increasing, got {cands}")
+    dvals = vol.device_values()
+    res = device.build_archive(dvals, vol.dims, cands, block_size, spacing=vol.spacing,
+                               source_dtype=vol.source_dtype, loose_fraction=loose_fraction,
+                               safety_factor=safety_factor, vrange=vol.value_range, out_of_range=out_of_range,
+                               on_warn=lambda m: warnings.warn(m, stacklevel=3))
+    if codec is not None:
+        return _rebuild_with_plugin(vol, res, cands, block_size, codec)
+    host = res.blob[: res.nbytes].cpu().numpy().tobytes()
+    regions = _regions_from_device(res, host, cands, vol.source_dtype)
+    dev = {"blob": res.blob[: res.nbytes], "file": host}
+    return CHRArchive(vol.dims, vol.spacing, vol.source_dtype, int(block_size), tuple(res.extra["vrange"]),
+                      tuple(cands), regions, dev)
+
+
+def _rebuild_with_plugin(vol, res, cands, bs, codec):
+    """build_chr(codec=...) seam (chr_archive.py:142,185): GPU bounds, plugin bytes."""
+    grid = vol.grid
+    regions = []
+    for rec in device.region_records(res.regions):
+        (ox, oy, oz), (ex, ey, ez) = rec["origin"], rec["extent"]
+        blk = codec(grid[ox:ox + ex, oy:oy + ey, oz:oz + ez], rec["e"], vol.source_dtype)
+        mask = rec["mask"]
+        regions.append(ArchiveRegion(rec["id"], (rec["lo"], rec["hi"]), rec["origin"], rec["extent"],
+                                     frozenset(ci for ci in range(len(cands)) if (mask >> ci) & 1),
+                                     MODE_STRICT, 1.0, rec["e"], blk))
+    return CHRArchive(vol.dims, vol.spacing, vol.source_dtype, int(bs), tuple(res.extra["vrange"]),
+                      tuple(cands), tuple(regions))
+
+
+def _select_candidate(archive: CHRArchive, k: float, snap: bool):
+    c = np.asarray(archive.candidates)
+    hit = np.flatnonzero(c == k)
+    if hit.size:
+        return int(hit[0]), False
+    if not snap:
+        raise NoSuchIsovalueError(k, archive.candidates)
+    return int(np.argmin(np.abs(c - k))), True
+
+
+def _device_file(archive: CHRArchive):
+    """The archive's serialised bytes on the device (uploading once if needed)."""
+    d = archive._device
+    if d is not None and "blob" in d:
+        return d["blob"]
+    blob = serialize(archive)
+    t = torch.from_numpy(np.frombuffer(blob, dtype=np.uint8).copy()).to(_abi.device())
+    if d is not None:
+        d["blob"] = t
+    return t
+
+
+def _block_offsets(archive: CHRArchive):
+    off = archive.header_table_nbytes()
+    out = []
+    for r in archive.regions:
+        out.append(off)
+        off += r.payload_nbytes
+    return out
+
+
+def request_device(archive: CHRArchive, k: float, accuracy=None, drop_pruned=True, snap=False):
+    """request() keeping the windows on the device: returns
+    (selected regions, f64 device tensor of windows, element offsets, report)."""
+    k = float(k)
+    ci, snapped = _select_candidate(archive, k, snap)
+    stored = archive.stored_accuracy
+    req = stored if accuracy is None else float(accuracy)
+    if req > stored:
+        raise InsufficientAccuracyError(req, stored)
+    offs = _block_offsets(archive)
+    sel = [(r, o) for r, o in zip(archive.regions, offs) if (not drop_pruned) or r.is_relevant(ci)]
+    builtin = all(r.block.codec_id in (0, 1, 2, 3) for r, _ in sel)
+    windows, woffs = None, []
+    if builtin and sel:
+        blob = _device_file(archive)
+        desc = [(o + HEADER_SIZE, len(r.block.payload), r.block.codec_id, r.block.dims, r.block.error_bound,
+                 r.block.checksum) for r, o in sel]
+        windows, woffs, status = device.decode(blob, desc, out=None)
+        for (r, _), st in zip(sel, status):
+            if st == 10:
+                raise UnsupportedCodecError(f"unknown codec id {r.block.codec_id}")
+            if st:
+                raise CorruptPayloadError(_abi.DEC_MESSAGES.get(st, "corrupt payload"))
+    touched = archive.header_table_nbytes() + sum(r.payload_nbytes for r, _ in sel)
+    report = RequestReport(k, archive.candidates[ci], snapped, ci, req, stored, drop_pruned, len(sel),
+                           len(archive.regions), touched, archive.file_nbytes())
+    return [r for r, _ in sel], windows, woffs, report, builtin
+
+
+def request(archive: CHRArchive, k: float, accuracy=None, drop_pruned: bool = True, snap: bool = False,
+            workers: int = 1) -> ReconstructionSet:
+    """chr_archive.request (chr_archive.py:226-274) on the GPU."""
+    del workers
+    regs, windows, woffs, report, builtin = request_device(archive, k, accuracy, drop_pruned, snap)
+    if not builtin:
+        arrays = decompress_many([r.block for r in regs])
+    else:
+        host = windows.cpu().numpy() if regs else None
+        arrays = []
+        for r, o in zip(regs, woffs):
+            d = r.block.dims
+            n = d[0] * d[1] * d[2]
+            arrays.append(host[o:o + n].reshape(d, order="F").copy())
+    return ReconstructionSet(tuple(zip(regs, arrays)), report)
+
+
+def stitch(recon: ReconstructionSet, dims, fill: float = np.nan) -> np.ndarray:
+    """Owner-wins reassembly (chr_archive.py:277-294): lower (z,y,x) origin lands last."""
+    out = np.full(dims, fill, dtype=np.float64, order="F")
+    for region, samples in sorted(recon.regions, key=lambda p: tuple(reversed(p[0].sample_origin)), reverse=True):
+        (ox, oy, oz), (ex, ey, ez) = region.sample_origin, region.sample_extent
+        out[ox:ox + ex, oy:oy + ey, oz:oz + ez] = samples
+    return out
+
+
+def serialize(archive: CHRArchive) -> bytes:
+    """FORMAT.md bytes of an archive (header, candidates, table, blocks, CRC)."""
+    d = archive._device
+    if d is not None and "file" in d:
+        return d["file"]
+    m = len(archive.candidates)
+    mb = (m + 7) // 8
+    parts = [_FILE_HDR.pack(MAGIC, VERSION, *archive.dims, *archive.spacing, DTYPE_TAGS[archive.source_dtype],
+                            archive.block_size, *archive.value_range),
+             struct.pack("<I", m), struct.pack(f"<{m}d", *archive.candidates),
+             struct.pack("<I", len(archive.regions))]
+    off = archive.header_table_nbytes()
+    for r in archive.regions:
+        mask = sum(1 << ci for ci in r.relevance)
+        parts.append(_REC.pack(r.region_id, *r.block_span[0], *r.block_span[1], *r.sample_origin,
+                               *r.sample_extent, BOUND_MODE_TAGS[r.bound_mode], r.accuracy, r.error_bound, off,
+                               r.payload_nbytes))
+        parts.append(mask.to_bytes(mb, "little"))
+        off += r.payload_nbytes
+    parts.extend(r.block.to_bytes() for r in archive.regions)
+    body = b"".join(parts)
+    return body + struct.pack("<I", _gpu_crc(body))
+
+
+def _gpu_crc(b: bytes) -> int:
+    if not b:
+        return 0
+    t = torch.from_numpy(np.frombuffer(b, dtype=np.uint8).copy()).to(_abi.device())
+    return device.crc32(t)
+
+
+def write_chr(archive: CHRArchive, path) -> None:
+    """chr_archive.write_chr (chr_archive.py:297-340)."""
+    with open(path, "wb") as fh:
+        fh.write(serialize(archive))
+
+
+def read_chr(path) -> CHRArchive:
+    """chr_archive.read_chr (chr_archive.py:343-407); the trailer CRC is
+    verified on the GPU."""
+    with open(path, "rb") as fh:
+        blob = fh.read()
+    if len(blob) < _FILE_HDR.size + 4:
+        raise ChecksumError(f"{path}: file too short to be a CHR archive")
+    if blob[:4] != MAGIC:
+        raise BadMagicError(f"{path}: bad magic {blob[:4]!r}, expected {MAGIC!r}")
+    stored = struct.unpack_from("<I", blob, len(blob) - 4)[0]
+    actual = _gpu_crc(blob[:-4])
+    if stored != actual:
+        raise ChecksumError(f"{path}: checksum mismatch (stored {stored:#010x}, computed {actual:#010x})")
+    (_, version, nx, ny, nz, dx, dy, dz, tag, bs, vmin, vmax) = _FILE_HDR.unpack_from(blob, 0)
+    if version != VERSION:
+        from .exceptions import VersionError
+
+        raise VersionError(f"{path}: unsupported CHR version {version}")
+    pos = _FILE_HDR.size
+    (m,) = struct.unpack_from("<I", blob, pos)
+    pos += 4
+    cands = struct.unpack_from(f"<{m}d", blob, pos)
+    pos += 8 * m
+    mb = (m + 7) // 8
+    (nreg,) = struct.unpack_from("<I", blob, pos)
+    pos += 4
+    regions = []
+    for _ in range(nreg):
+        f = _REC.unpack_from(blob, pos)
+        pos += _REC.size
+        mask = int.from_bytes(blob[pos:pos + mb], "little")
+        pos += mb
+        (rid, lx, ly, lz, hx, hy, hz, ox, oy, oz, ex, ey, ez, mode, acc, eb, poff, plen) = f
+        if poff + plen > len(blob) - 4:
+            raise ChecksumError(f"{path}: region {rid} payload exceeds file size")
+        blk = CompressedBlock.from_bytes(blob, poff)
+        if blk.nbytes != plen:
+            raise ChecksumError(f"{path}: region {rid} payload length mismatch (table {plen}, block {blk.nbytes})")
+        regions.append(ArchiveRegion(rid, ((lx, ly, lz), (hx, hy, hz)), (ox, oy, oz), (ex, ey, ez),
+                                     frozenset(ci for ci in range(m) if (mask >> ci) & 1), _MODES[mode], acc, eb,
+                                     blk))
+    dtype = {v: k for k, v in DTYPE_TAGS.items()}[tag]
+    return CHRArchive((nx, ny, nz), (dx, dy, dz), dtype, bs, (vmin, vmax), tuple(cands), tuple(regions),
+                      {"file": blob})
+
+
+__all__ = ["ArchiveRegion", "CHRArchive", "RequestReport", "ReconstructionSet", "build_chr", "request",
+           "request_device", "stitch", "write_chr", "read_chr", "serialize", "MODE_STRICT", "MODE_PAPER", "Volume"]

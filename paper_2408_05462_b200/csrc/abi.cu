@@ -1,0 +1,88 @@
+// abi.cu -- library info + kernel-seam entry points on single windows
+// (isochr/kernels.py: min_abs_distance kernels.py:417-425,
+// lorenzo_encode kernels.py:47-128).
+#include "chr_internal.cuh"
+
+namespace chr {
+
+__global__ void __launch_bounds__(256) k_min_abs(const double *__restrict__ x, int64_t n, double k,
+                                                 unsigned long long *__restrict__ out) {
+    double best = INFINITY;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        best = fmin(best, fabs(__dadd_rn(x[i], -k)));
+    for (int off = 16; off; off >>= 1) best = fmin(best, __shfl_xor_sync(0xFFFFFFFFu, best, off));
+    // non-negative doubles order like their bit patterns
+    if ((threadIdx.x & 31) == 0) atomicMin(out, (unsigned long long)__double_as_longlong(best));
+}
+
+// thread per sample; the 8 lattice values are requantised (exactly as the
+// encoder does), so q matches kernels.lorenzo_encode bit for bit
+__global__ void __launch_bounds__(256) k_lorenzo_seam(const double *__restrict__ x, int64_t nx, int64_t ny,
+                                                      int64_t nz, Quant Q, int64_t *__restrict__ q,
+                                                      uint8_t *__restrict__ esc) {
+    const int64_t n = nx * ny * nz;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t xx = i % nx, yy = (i / nx) % ny, zz = i / (nx * ny);
+        int64_t acc = 0;
+        bool e0 = false;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            const int dx = c & 1, dy = (c >> 1) & 1, dz = (c >> 2) & 1;
+            if (xx - dx < 0 || yy - dy < 0 || zz - dz < 0) continue;
+            bool e;
+            const int32_t u = quantize(Q, x[i - dx - dy * nx - dz * nx * ny], e);
+            if (c == 0) e0 = e;
+            acc += ((dx + dy + dz) & 1) ? -(int64_t)u : (int64_t)u;
+        }
+        q[i] = acc;
+        esc[i] = e0 ? 1 : 0;
+    }
+}
+
+}  // namespace chr
+
+using namespace chr;
+
+extern "C" int chr_abi_version(void) { return 1; }
+
+extern "C" const char *chr_status_string(int s) {
+    switch (s) {
+        case CHR_OK: return "ok";
+        case CHR_E_PARAMETER: return "invalid parameter";
+        case CHR_E_NONFINITE: return "non-finite sample";
+        case CHR_E_CORRUPT: return "corrupt payload";
+        case CHR_E_UNSUPPORTED_CODEC: return "unsupported codec";
+        case CHR_E_CUDA: return "CUDA error";
+        case CHR_E_WORKSPACE: return "workspace too small";
+        default: return "unknown status";
+    }
+}
+
+extern "C" int chr_min_abs_distance(const double *d_flat, int64_t n, double k, double *h_out, void *d_ws,
+                                    size_t ws_bytes, void *stream) {
+    if (!d_flat || n < 1 || !h_out) return CHR_E_PARAMETER;
+    if (!d_ws || ws_bytes < 8) return CHR_E_WORKSPACE;
+    cudaStream_t st = (cudaStream_t)stream;
+    auto *slot = reinterpret_cast<unsigned long long *>(d_ws);
+    CHR_CUDA_TRY(cudaMemsetAsync(slot, 0x7F, 8, st));  // a huge positive double
+    const int64_t blocks = std::min<int64_t>(ceil_div(n, 256), 148 * 16);
+    k_min_abs<<<(unsigned)blocks, 256, 0, st>>>(d_flat, n, k, slot);
+    CHR_CUDA_TRY(cudaGetLastError());
+    unsigned long long bits = 0;
+    CHR_CUDA_TRY(cudaMemcpyAsync(&bits, slot, 8, cudaMemcpyDeviceToHost, st));
+    CHR_CUDA_TRY(cudaStreamSynchronize(st));
+    double v;
+    memcpy(&v, &bits, 8);
+    *h_out = v;
+    return CHR_OK;
+}
+
+extern "C" int chr_lorenzo_encode(const double *d_flat, int64_t nx, int64_t ny, int64_t nz, double e,
+                                  int64_t *d_q, uint8_t *d_escaped, void *stream) {
+    if (!d_flat || !d_q || !d_escaped || nx < 1 || ny < 1 || nz < 1 || !(e > 0.0)) return CHR_E_PARAMETER;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t n = nx * ny * nz;
+    const int64_t blocks = std::min<int64_t>(ceil_div(n, 256), 148 * 32);
+    k_lorenzo_seam<<<(unsigned)blocks, 256, 0, st>>>(d_flat, nx, ny, nz, make_quant(e), d_q, d_escaped);
+    return cudaGetLastError() == cudaSuccess ? CHR_OK : CHR_E_CUDA;
+}

@@ -1,0 +1,41 @@
+// chr_internal.cuh -- declarations shared between libchr translation units.
+#pragma once
+
+#include "chr_common.cuh"
+
+namespace chr {
+
+// ------------------------------------------------------------------ CRC
+constexpr int64_t kCrcScWords = 4096;  // words per superchunk (16 KiB)
+
+struct CrcSeg {
+    uint64_t begin, end;  // byte range
+    int64_t sc_base;      // first superchunk id
+    int64_t n_sc;         // superchunks
+};
+
+int64_t crc_plan_segments(CrcSeg *segs, int64_t nseg);
+int crc_launch(const uint8_t *d_buf, const CrcSeg *d_segs, int64_t nseg, int64_t total_sc,
+               uint32_t *d_seg_raw, cudaStream_t st);
+__global__ void k_crc_segments(const uint8_t *__restrict__ buf, const CrcSeg *__restrict__ segs,
+                               int64_t nseg, const CrcTables *__restrict__ tabs,
+                               uint32_t *__restrict__ seg_raw);
+
+// ------------------------------------------------------------------ workspace
+struct WsCarver {
+    char *base;
+    size_t off, cap;
+    bool ok = true;
+    template <typename T>
+    T *take(size_t count) {
+        off = (off + 255) & ~size_t(255);
+        T *p = reinterpret_cast<T *>(base ? base + off : nullptr);
+        off += count * sizeof(T);
+        if (off > cap) ok = false;
+        return p;
+    }
+};
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+}  // namespace chr

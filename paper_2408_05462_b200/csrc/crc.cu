@@ -1,0 +1,208 @@
+// crc.cu -- CRC-32/IEEE (zlib.crc32) of many byte segments at HBM speed.
+//
+// Reference uses: codec.py:132 (payload checksum), codec.py:220-226
+// (verification in decompress), chr_archive.py:338 / 351-356 (whole-file
+// trailer).  zlib's byte-serial loop is replaced by a lane-interleaved
+// word formulation: lane l of a warp owns words l, l+32, l+64, ... of a
+// superchunk and keeps B = G(B) ^ w (G = multiply by x^1024 mod P, four
+// 256-entry table lookups); the lane's share of the superchunk CRC is then
+// B * x^(32 (W - last)) and the superchunk CRC is the XOR over lanes.
+// Superchunk CRCs are shifted to the segment end and XOR-accumulated, so
+// any number of warps can work on one segment.  Loads are 128-byte
+// coalesced 32-bit words.
+#include <mutex>
+
+#include "chr_common.cuh"
+#include "chr_internal.cuh"
+
+namespace chr {
+
+static CrcTables g_host_tables;
+static CrcTables *g_dev_tables = nullptr;
+static std::once_flag g_host_once;
+static std::mutex g_dev_mu;
+
+void crc_tables_host(CrcTables *t) {
+    // byte table (zlib make_crc_table)
+    for (uint32_t n = 0; n < 256; ++n) {
+        uint32_t c = n;
+        for (int k = 0; k < 8; ++k) c = (c & 1) ? (c >> 1) ^ kCrcPoly : c >> 1;
+        t->t[0][n] = c;
+    }
+    for (uint32_t n = 0; n < 256; ++n)
+        for (int k = 1; k < 4; ++k)
+            t->t[k][n] = (t->t[k - 1][n] >> 8) ^ t->t[0][t->t[k - 1][n] & 0xFF];
+    // x^(2^k) mod P by repeated squaring, starting from x^1 = 0x40000000
+    uint32_t p = 1u << 30;
+    for (int k = 0; k < 64; ++k) {
+        t->x2n[k] = p;
+        p = gf2_mul(p, p);
+    }
+    const uint32_t x1024 = x8n(t->x2n, 128);
+    for (int k = 0; k < 4; ++k)
+        for (uint32_t n = 0; n < 256; ++n) t->g[k][n] = gf2_mul(x1024, n << (8 * k));
+    for (int k = 0; k < 33; ++k) t->xw[k] = x8n(t->x2n, 4ull * k);
+}
+
+const CrcTables &crc_tables_hostref() {
+    std::call_once(g_host_once, [] { crc_tables_host(&g_host_tables); });
+    return g_host_tables;
+}
+
+const CrcTables *crc_tables_device() {
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    if (!g_dev_tables) {
+        const CrcTables &h = crc_tables_hostref();
+        CrcTables *d = nullptr;
+        if (cudaMalloc(&d, sizeof(CrcTables)) != cudaSuccess) return nullptr;
+        if (cudaMemcpy(d, &h, sizeof(CrcTables), cudaMemcpyHostToDevice) != cudaSuccess) {
+            cudaFree(d);
+            return nullptr;
+        }
+        g_dev_tables = d;
+    }
+    return g_dev_tables;
+}
+
+// x^(8n) mod P computed by a whole warp (one bit of n per lane, then a
+// shuffle product tree); every lane returns the result
+__device__ uint32_t warp_x8n(const uint32_t *x2n, uint64_t n) {
+    const int lane = threadIdx.x & 31;
+    uint32_t p = 1u << 31;
+    if ((n >> lane) & 1) p = x2n[lane + 3];
+    if (lane + 32 < 61 && ((n >> (lane + 32)) & 1)) p = gf2_mul(p, x2n[lane + 35]);
+#pragma unroll
+    for (int off = 16; off; off >>= 1) p = gf2_mul(p, __shfl_xor_sync(0xFFFFFFFFu, p, off));
+    return p;
+}
+
+__device__ __forceinline__ uint32_t apply_g(const uint32_t (*g)[256], uint32_t v) {
+    return g[0][v & 0xFF] ^ g[1][(v >> 8) & 0xFF] ^ g[2][(v >> 16) & 0xFF] ^ g[3][v >> 24];
+}
+
+// one warp per superchunk (kCrcScWords words); seg_raw[s] ^= contribution
+__global__ void __launch_bounds__(256) k_crc_segments(const uint8_t *__restrict__ buf,
+                                                      const CrcSeg *__restrict__ segs, int64_t nseg,
+                                                      const CrcTables *__restrict__ tabs,
+                                                      uint32_t *__restrict__ seg_raw) {
+    __shared__ uint32_t g[4][256];
+    __shared__ uint32_t t0[256];
+    __shared__ uint32_t x2n[64];
+    __shared__ uint32_t xw[33];
+    for (int i = threadIdx.x; i < 1024; i += blockDim.x) g[i >> 8][i & 255] = tabs->g[i >> 8][i & 255];
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) t0[i] = tabs->t[0][i];
+    if (threadIdx.x < 64) x2n[threadIdx.x] = tabs->x2n[threadIdx.x];
+    if (threadIdx.x < 33) xw[threadIdx.x] = tabs->xw[threadIdx.x];
+    __syncthreads();
+
+    const int lane = threadIdx.x & 31;
+    const int64_t total_sc = segs[nseg - 1].sc_base + segs[nseg - 1].n_sc;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t sc = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); sc < total_sc;
+         sc += warps) {
+        // segment of this superchunk (segments sorted by sc_base)
+        int64_t lo = 0, hi = nseg - 1;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi + 1) >> 1;
+            if (segs[mid].sc_base <= sc) lo = mid; else hi = mid - 1;
+        }
+        const CrcSeg S = segs[lo];
+        const uint64_t a = S.begin, b = S.end;
+        const uint64_t a4 = (a + 3) & ~3ull, b4 = b & ~3ull;
+        const int64_t isc = sc - S.sc_base;
+        uint32_t contrib = 0;
+        if (a4 < b4) {
+            const uint64_t W = (b4 - a4) >> 2;
+            const uint64_t w0 = (uint64_t)isc * kCrcScWords;
+            const uint64_t w1 = min(W, w0 + kCrcScWords);
+            const uint32_t *wp = reinterpret_cast<const uint32_t *>(buf + a4);
+            uint32_t B = 0;
+            int64_t last = -1;
+            for (uint64_t i = w0 + lane; i < w1; i += 32) {
+                B = apply_g(g, B) ^ __ldg(wp + i);
+                last = (int64_t)(i - w0);
+            }
+            const int64_t Ws = (int64_t)(w1 - w0);
+            uint32_t part = last >= 0 ? gf2_mul(xw[Ws - last], B) : 0;
+#pragma unroll
+            for (int off = 16; off; off >>= 1) part ^= __shfl_xor_sync(0xFFFFFFFFu, part, off);
+            // shift to the segment end
+            const uint64_t after = b - (a4 + 4 * w1);
+            const uint32_t m = warp_x8n(x2n, after);
+            contrib = gf2_mul(m, part);
+            if (isc == 0 && lane == 0) {
+                uint32_t h = crc_raw_bytes(t0, 0, buf + a, (int64_t)(a4 - a));
+                contrib ^= crc_shift(x2n, h, b - a4);
+                contrib ^= crc_raw_bytes(t0, 0, buf + b4, (int64_t)(b - b4));
+            }
+        } else if (lane == 0) {
+            contrib = crc_raw_bytes(t0, 0, buf + a, (int64_t)(b - a));
+        }
+        if (lane == 0 && contrib) atomicXor(seg_raw + lo, contrib);
+    }
+}
+
+// number of superchunks of a segment and their prefix (host side)
+int64_t crc_plan_segments(CrcSeg *segs, int64_t nseg) {
+    int64_t base = 0;
+    for (int64_t s = 0; s < nseg; ++s) {
+        const uint64_t a4 = (segs[s].begin + 3) & ~3ull, b4 = segs[s].end & ~3ull;
+        const uint64_t W = a4 < b4 ? (b4 - a4) >> 2 : 0;
+        segs[s].sc_base = base;
+        segs[s].n_sc = W ? (int64_t)((W + kCrcScWords - 1) / kCrcScWords) : 1;
+        base += segs[s].n_sc;
+    }
+    return base;
+}
+
+int crc_launch(const uint8_t *d_buf, const CrcSeg *d_segs, int64_t nseg, int64_t total_sc,
+               uint32_t *d_seg_raw, cudaStream_t st) {
+    const CrcTables *tabs = crc_tables_device();
+    if (!tabs) return CHR_E_CUDA;
+    if (nseg <= 0) return CHR_OK;
+    // total_sc <= 0: unknown on the host (lives on the device) -> persistent grid
+    const int64_t warps_needed = total_sc > 0 ? total_sc : 148 * 64;
+    int64_t blocks = (warps_needed + 7) / 8;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    if (blocks < 1) blocks = 1;
+    k_crc_segments<<<(unsigned)blocks, 256, 0, st>>>(d_buf, d_segs, nseg, tabs, d_seg_raw);
+    return cudaGetLastError() == cudaSuccess ? CHR_OK : CHR_E_CUDA;
+}
+
+}  // namespace chr
+
+using namespace chr;
+
+extern "C" size_t chr_crc32_workspace_size(uint64_t) { return 256; }
+
+extern "C" int chr_crc32(const uint8_t *d_buf, uint64_t n, void *d_ws, size_t ws_bytes,
+                         uint32_t *h_crc, void *stream) {
+    if (!h_crc || (!d_buf && n)) return CHR_E_PARAMETER;
+    if (ws_bytes < 256 || !d_ws) return CHR_E_WORKSPACE;
+    cudaStream_t st = (cudaStream_t)stream;
+    const CrcTables &H = crc_tables_hostref();
+    if (n == 0) {
+        *h_crc = 0;
+        return CHR_OK;
+    }
+    CrcSeg seg;
+    seg.begin = 0;
+    seg.end = n;
+    crc_plan_segments(&seg, 1);
+    CrcSeg *d_seg = reinterpret_cast<CrcSeg *>(d_ws);
+    uint32_t *d_raw = reinterpret_cast<uint32_t *>(reinterpret_cast<char *>(d_ws) + 128);
+    CHR_CUDA_TRY(cudaMemcpyAsync(d_seg, &seg, sizeof(seg), cudaMemcpyHostToDevice, st));
+    CHR_CUDA_TRY(cudaMemsetAsync(d_raw, 0, 4, st));
+    int rc = crc_launch(d_buf, d_seg, 1, seg.n_sc, d_raw, st);
+    if (rc) return rc;
+    uint32_t raw = 0;
+    CHR_CUDA_TRY(cudaMemcpyAsync(&raw, d_raw, 4, cudaMemcpyDeviceToHost, st));
+    CHR_CUDA_TRY(cudaStreamSynchronize(st));
+    *h_crc = crc_finalize(H.x2n, raw, n);
+    return CHR_OK;
+}
+
+extern "C" uint32_t chr_crc32_combine(uint32_t crc1, uint32_t crc2, uint64_t len2) {
+    const CrcTables &H = crc_tables_hostref();
+    return crc_shift(H.x2n, crc1, len2) ^ crc2;
+}

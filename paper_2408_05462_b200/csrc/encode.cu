@@ -1,0 +1,870 @@
+// encode.cu -- steps 2+3 of the hot path on the device: topology-bounded
+// quantisation + 3D Lorenzo residuals + the zigzag/LEB128/zero-run token
+// stream + codec selection + CompressedBlock / .chr byte layout + CRCs.
+//
+// Reference: kernels.py:47-93 (quantise + Lorenzo), kernels.py:198-234
+// (token stream), codec.py:91-143 (codec 1/2, escape bitmap + values,
+// verbatim fallback 0/3, CRC), codec.py:61-70 (34-byte header),
+// chr_archive.py:297-340 + FORMAT.md (file header, region table,
+// payloads in region order, CRC trailer).
+//
+// Pipeline (all on one stream, no host round trip):
+//   k_tile<COUNT>  per 64-sample row piece: token-byte summary (TokSeg)
+//   k_scan_reduce  chunk aggregates (chunks never straddle regions)
+//   k_scan_regions per region: chunk prefixes, totals, codec decision
+//   k_layout       region offsets in the file, CRC segment plan
+//   k_scan_down    per piece: token offset, zero-run carry, escape offset
+//   k_tile<EMIT>   recompute q, write every token byte at its final offset
+//   k_bitmap       escape bitmaps (codec 2 regions only)
+//   k_write_table  file header + region table
+//   k_crc_segments payload + header-table CRCs (crc.cu)
+//   k_finalize_*   34-byte block headers, file CRC trailer
+//
+// Tiles: a CTA owns 64 columns x 8 rows x 16 planes of one region window
+// and marches z; one warp per row (+1 halo warp for row y0-1), 2 samples
+// per lane + the x0-1 halo sample.  With D = u(z) - u(z-1) shared through
+// shared memory, q = D - D(x-1) - D(y-1) + D(x-1,y-1), so u is computed
+// once per sample (plus the 1/8 + 1/64 + 1/16 halo).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "chr_internal.cuh"
+
+namespace chr {
+
+constexpr int TX = 64, TY = 8, ZC = 16, NW = TY + 1;
+constexpr int64_t CH = 1024;  // pieces per scan chunk
+
+struct RegDev {
+    int32_t ox, oy, oz, ex, ey, ez;
+    int32_t ntx, nty, nzc, mode;  // mode 1: e == 0 (verbatim)
+    double e;
+    int64_t n;
+    int64_t piece_base, npieces, item_base, chunk_base, nchunks;
+    // results
+    int32_t codec, f32ok;
+    int64_t tok_len, nesc, payload_len;
+    uint64_t block_off, payload_off, tok_start;
+    uint32_t crc;
+    uint32_t pad;
+    uint64_t mask;
+    int32_t lo[3], hi[3];
+};
+
+struct EncParams {
+    int64_t NX, NY, NZ;
+    int64_t nreg, nitems, nchunks;
+    int32_t dtype, src_dtype, write_file, m;
+    double spacing[3];
+    double vmin, vmax;
+    int64_t bs;
+    uint64_t header_table;  // bytes before the first block (0 if !write_file)
+    double cands[64];
+};
+
+struct EncScalars {
+    uint64_t file_body;      // bytes before the trailer
+    uint64_t out_nbytes;     // total bytes written
+    uint32_t file_raw;       // raw CRC accumulator of the body
+    uint32_t pad;
+    int64_t n_codec2;
+    int64_t total_sc;
+};
+
+// ------------------------------------------------------------------ helpers
+__device__ __forceinline__ int64_t find_region_by(const RegDev *__restrict__ regs, int64_t nreg,
+                                                  int64_t key, int which) {
+    int64_t lo = 0, hi = nreg - 1;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi + 1) >> 1;
+        const int64_t b = which == 0 ? regs[mid].item_base : regs[mid].chunk_base;
+        if (b <= key) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ uint8_t *put_varint(uint8_t *p, uint64_t u) {
+    while (u >= 0x80) {
+        *p++ = (uint8_t)((u & 0x7F) | 0x80);
+        u >>= 7;
+    }
+    *p++ = (uint8_t)u;
+    return p;
+}
+
+__device__ __forceinline__ uint8_t *put_run(uint8_t *p, int64_t run) {
+    if (run == 1) {
+        *p++ = 1;
+    } else if (run >= 2) {
+        *p++ = 0;
+        p = put_varint(p, (uint64_t)run);
+    }
+    return p;
+}
+
+template <typename V>
+__device__ __forceinline__ void put_le(uint8_t *p, V v) {
+    uint8_t b[sizeof(V)];
+    memcpy(b, &v, sizeof(V));
+#pragma unroll
+    for (int i = 0; i < (int)sizeof(V); ++i) p[i] = b[i];
+}
+
+__device__ __forceinline__ int hibit(uint64_t m) { return 63 - __clzll((long long)m); }
+
+template <typename T>
+__device__ __forceinline__ bool not_f32_exact(T v) {
+    return (double)(float)v != (double)v;
+}
+
+// ------------------------------------------------------------------ tiles
+template <typename T, bool EMIT>
+__global__ void __launch_bounds__(NW * 32) k_tile(const T *__restrict__ vol, const EncParams *__restrict__ P,
+                                                  const RegDev *__restrict__ regs,
+                                                  PieceRec *__restrict__ recs,
+                                                  const PieceOff *__restrict__ poffs,
+                                                  uint8_t *__restrict__ out) {
+    __shared__ int32_t sD[2][NW][TX + 2];
+    __shared__ RegDev R;
+    const int64_t item = blockIdx.x;
+    if (threadIdx.x == 0) R = regs[find_region_by(regs, P->nreg, item, 0)];
+    __syncthreads();
+    const int64_t NX = P->NX, NY = P->NY;
+    const int64_t local = item - R.item_base;
+    const int xt = (int)(local % R.ntx);
+    const int64_t t2 = local / R.ntx;
+    const int yt = (int)(t2 % R.nty);
+    const int zc = (int)(t2 / R.nty);
+    const int x0 = xt * TX, y0 = yt * TY, z0 = zc * ZC;
+    const int z1 = min(z0 + ZC, R.ez);
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int y = y0 - 1 + w;
+    const bool rowok = y >= 0 && y < R.ey;
+    const int xA = x0 + lane, xB = x0 + 32 + lane, xH = x0 - 1;
+    const bool okA = rowok && xA < R.ex, okB = rowok && xB < R.ex;
+    const bool okH = rowok && lane == 0 && xH >= 0;
+    const bool quant = R.mode == 0;
+    const Quant Q = make_quant(R.e);
+    const bool is_last_xt = xt == R.ntx - 1;
+    const int vcount = min(TX, R.ex - x0);
+    // codec decided by the scan (EMIT only)
+    const int codec = EMIT ? R.codec : 0;
+
+    auto vptr = [&](int z) -> const T * {
+        return vol + ((int64_t)(R.oz + z) * NY + (R.oy + y)) * NX + R.ox;
+    };
+    int32_t pA = 0, pB = 0, pH = 0;  // u at the previous plane
+    if (quant && z0 > 0) {
+        const T *row = vptr(z0 - 1);
+        bool e_;
+        if (okA) pA = quantize(Q, (double)__ldg(row + xA), e_);
+        if (okB) pB = quantize(Q, (double)__ldg(row + xB), e_);
+        if (okH) pH = quantize(Q, (double)__ldg(row + xH), e_);
+    }
+    T nA = 0, nB = 0, nH = 0;
+    if (z0 < z1) {
+        const T *row = vptr(z0);
+        if (okA) nA = __ldg(row + xA);
+        if (okB) nB = __ldg(row + xB);
+        if (okH) nH = __ldg(row + xH);
+    }
+    for (int z = z0; z < z1; ++z) {
+        const T vA = nA, vB = nB, vH = nH;
+        if (z + 1 < z1) {  // prefetch the next plane
+            const T *row = vptr(z + 1);
+            if (okA) nA = __ldg(row + xA);
+            if (okB) nB = __ldg(row + xB);
+            if (okH) nH = __ldg(row + xH);
+        }
+        bool eA = false, eB = false, eH = false;
+        int32_t uA = 0, uB = 0, uH = 0;
+        if (quant) {
+            if (okA) uA = quantize(Q, (double)vA, eA);
+            if (okB) uB = quantize(Q, (double)vB, eB);
+            if (okH) uH = quantize(Q, (double)vH, eH);
+        }
+        int32_t(*D)[TX + 2] = sD[z & 1];
+        D[w][lane + 1] = uA - pA;
+        D[w][lane + 33] = uB - pB;
+        if (lane == 0) D[w][0] = uH - pH;
+        pA = uA;
+        pB = uB;
+        pH = uH;
+        __syncthreads();
+        if (w == 0 || !rowok) continue;
+        const int32_t qA = D[w][lane + 1] - D[w][lane] - D[w - 1][lane + 1] + D[w - 1][lane];
+        const int32_t qB = D[w][lane + 33] - D[w][lane + 32] - D[w - 1][lane + 33] + D[w - 1][lane + 32];
+        const bool nzA = okA && qA != 0, nzB = okB && qB != 0;
+        const uint64_t nzm = (uint64_t)__ballot_sync(0xFFFFFFFFu, nzA) |
+                             ((uint64_t)__ballot_sync(0xFFFFFFFFu, nzB) << 32);
+        const uint64_t escm = (uint64_t)__ballot_sync(0xFFFFFFFFu, okA && eA) |
+                              ((uint64_t)__ballot_sync(0xFFFFFFFFu, okB && eB) << 32);
+        const int64_t rec = R.piece_base + ((int64_t)z * R.ey + y) * R.ntx + xt;
+        const uint64_t below_mask_A = (1ull << lane) - 1, below_mask_B = (1ull << (32 + lane)) - 1;
+        if (!EMIT) {
+            int b = 0;
+            if (nzA) {
+                const uint64_t below = nzm & below_mask_A;
+                if (below) b += (int)run_bytes(lane - hibit(below) - 1);
+                b += varint_len(zigzag1(qA));
+            }
+            if (nzB) {
+                const uint64_t below = nzm & below_mask_B;
+                if (below) b += (int)run_bytes(32 + lane - hibit(below) - 1);
+                b += varint_len(zigzag1(qB));
+            }
+            const int bytes = __reduce_add_sync(0xFFFFFFFFu, b);
+            bool inexact = false;
+            if (sizeof(T) == 8 && P->src_dtype == CHR_F32) {
+                inexact = (okA && not_f32_exact(vA)) || (okB && not_f32_exact(vB));
+            }
+            const bool anyinexact = __any_sync(0xFFFFFFFFu, inexact);
+            if (lane == 0) {
+                PieceRec pr;
+                pr.bytes = (uint16_t)bytes;
+                pr.vcount = (uint8_t)vcount;
+                pr.lead = (uint8_t)(nzm ? __ffsll((long long)nzm) - 1 : vcount);
+                pr.trail = (uint8_t)(nzm ? vcount - 1 - hibit(nzm) : vcount);
+                pr.nesc = (uint8_t)__popcll((long long)escm);
+                pr.flags = (uint8_t)((nzm ? 1 : 0) | (anyinexact ? 2 : 0));
+                pr.pad = 0;
+                recs[rec] = pr;
+            }
+        } else {
+            if (codec == 1 || codec == 2) {
+                const PieceOff po = poffs[rec];
+                int64_t runA = 0, runB = 0;
+                int bA = 0, bB = 0;
+                uint64_t zzA = 0, zzB = 0;
+                if (nzA) {
+                    const uint64_t below = nzm & below_mask_A;
+                    runA = below ? lane - hibit(below) - 1 : po.carry + lane;
+                    zzA = zigzag1(qA);
+                    bA = (int)run_bytes(runA) + varint_len(zzA);
+                }
+                if (nzB) {
+                    const uint64_t below = nzm & below_mask_B;
+                    runB = below ? 32 + lane - hibit(below) - 1 : po.carry + 32 + lane;
+                    zzB = zigzag1(qB);
+                    bB = (int)run_bytes(runB) + varint_len(zzB);
+                }
+                // exclusive scans in stream order (elements 0..31 then 32..63)
+                int sA = bA, sB = bB;
+#pragma unroll
+                for (int off = 1; off < 32; off <<= 1) {
+                    const int ta = __shfl_up_sync(0xFFFFFFFFu, sA, off);
+                    const int tb = __shfl_up_sync(0xFFFFFFFFu, sB, off);
+                    if (lane >= off) {
+                        sA += ta;
+                        sB += tb;
+                    }
+                }
+                const int totA = __shfl_sync(0xFFFFFFFFu, sA, 31);
+                const int totB = __shfl_sync(0xFFFFFFFFu, sB, 31);
+                sA -= bA;
+                sB = sB - bB + totA;
+                uint8_t *base = out + R.tok_start + po.tok_off;
+                if (nzA) put_varint(put_run(base + sA, runA), zzA);
+                if (nzB) put_varint(put_run(base + sB, runB), zzB);
+                if (is_last_xt && y == R.ey - 1 && z == R.ez - 1 && lane == 0) {
+                    const int64_t fin = nzm ? vcount - 1 - hibit(nzm) : po.carry + vcount;
+                    put_run(base + totA + totB, fin);
+                }
+                if (codec == 2 && escm) {
+                    const uint64_t vbase = R.payload_off + (uint64_t)((R.n + 7) >> 3);
+                    if (okA && eA) {
+                        const int64_t rank = po.esc_off + __popcll((long long)(escm & below_mask_A));
+                        put_le(out + vbase + 8 * rank, (double)vA);
+                    }
+                    if (okB && eB) {
+                        const int64_t rank = po.esc_off + __popcll((long long)(escm & below_mask_B));
+                        put_le(out + vbase + 8 * rank, (double)vB);
+                    }
+                }
+            } else {
+                // verbatim: codec 3 (f32) or 0 (f64), raster order
+                const int64_t s0 = ((int64_t)z * R.ey + y) * R.ex + x0;
+                if (codec == 3) {
+                    uint8_t *base = out + R.payload_off + 4 * s0;
+                    if (okA) put_le(base + 4 * lane, (float)vA);
+                    if (okB) put_le(base + 4 * (32 + lane), (float)vB);
+                } else {
+                    uint8_t *base = out + R.payload_off + 8 * s0;
+                    if (okA) put_le(base + 8 * lane, (double)vA);
+                    if (okB) put_le(base + 8 * (32 + lane), (double)vB);
+                }
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------ scans
+struct WarpSeg {
+    __device__ static TokSeg shfl_up(const TokSeg &s, int off) {
+        TokSeg r;
+        r.len = __shfl_up_sync(0xFFFFFFFFu, s.len, off);
+        r.lead = __shfl_up_sync(0xFFFFFFFFu, s.lead, off);
+        r.trail = __shfl_up_sync(0xFFFFFFFFu, s.trail, off);
+        r.bytes = __shfl_up_sync(0xFFFFFFFFu, s.bytes, off);
+        r.nesc = __shfl_up_sync(0xFFFFFFFFu, s.nesc, off);
+        r.nz = __shfl_up_sync(0xFFFFFFFFu, s.nz, off);
+        r.f32ok = __shfl_up_sync(0xFFFFFFFFu, s.f32ok, off);
+        return r;
+    }
+};
+
+// inclusive block scan of one TokSeg per thread (256 threads); returns the
+// thread's EXCLUSIVE prefix and writes the block total to *total
+__device__ TokSeg block_excl_scan(TokSeg x, TokSeg *total) {
+    __shared__ TokSeg wsum[8];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    TokSeg inc = x;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const TokSeg o = WarpSeg::shfl_up(inc, off);
+        if (lane >= off) inc = tokseg_combine(o, inc);
+    }
+    if (lane == 31) wsum[warp] = inc;
+    __syncthreads();
+    TokSeg wpre = tokseg_identity();
+    for (int i = 0; i < warp; ++i) wpre = tokseg_combine(wpre, wsum[i]);
+    TokSeg excl = WarpSeg::shfl_up(inc, 1);
+    if (lane == 0) excl = tokseg_identity();
+    if (total) {
+        TokSeg t = tokseg_identity();
+        for (int i = 0; i < 8; ++i) t = tokseg_combine(t, wsum[i]);
+        *total = t;
+    }
+    __syncthreads();
+    return tokseg_combine(wpre, excl);
+}
+
+__global__ void __launch_bounds__(256) k_scan_reduce(const EncParams *__restrict__ P,
+                                                     const RegDev *__restrict__ regs,
+                                                     const PieceRec *__restrict__ recs,
+                                                     TokSeg *__restrict__ chunk_agg) {
+    const int64_t c = blockIdx.x;
+    __shared__ int64_t rlo, rhi;
+    if (threadIdx.x == 0) {
+        const RegDev &R = regs[find_region_by(regs, P->nreg, c, 1)];
+        rlo = R.piece_base;
+        rhi = R.piece_base + R.npieces;
+    }
+    __syncthreads();
+    TokSeg acc = tokseg_identity();
+    const int64_t p0 = c * CH + threadIdx.x * 4;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int64_t p = p0 + k;
+        if (p >= rlo && p < rhi) acc = tokseg_combine(acc, piece_to_seg(recs[p]));
+    }
+    TokSeg total;
+    block_excl_scan(acc, &total);
+    if (threadIdx.x == 0) chunk_agg[c] = total;
+}
+
+__global__ void k_scan_regions(const EncParams *__restrict__ P, RegDev *__restrict__ regs,
+                               TokSeg *__restrict__ chunk_agg, int32_t *__restrict__ codec2_list,
+                               EncScalars *__restrict__ sc) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= P->nreg) return;
+    RegDev &R = regs[r];
+    TokSeg acc = tokseg_identity();
+    for (int64_t c = R.chunk_base; c < R.chunk_base + R.nchunks; ++c) {
+        const TokSeg a = chunk_agg[c];
+        chunk_agg[c] = acc;
+        acc = tokseg_combine(acc, a);
+    }
+    const bool f32ok = P->dtype == CHR_F32 ? true : acc.f32ok != 0;
+    const bool vf32 = P->src_dtype == CHR_F32 && f32ok;
+    const int64_t vlen = R.n * (vf32 ? 4 : 8);
+    const int vcodec = vf32 ? 3 : 0;
+    int codec;
+    int64_t plen, tok = 0, nesc = 0;
+    if (R.mode == 1) {
+        codec = vcodec;
+        plen = vlen;
+    } else {
+        tok = tokseg_stream_bytes(acc);
+        nesc = acc.nesc;
+        if (nesc) {
+            codec = 2;
+            plen = ((R.n + 7) >> 3) + 8 * nesc + tok;
+        } else {
+            codec = 1;
+            plen = tok;
+        }
+        if (plen >= vlen) {
+            codec = vcodec;
+            plen = vlen;
+        }
+    }
+    R.codec = codec;
+    R.f32ok = f32ok;
+    R.tok_len = tok;
+    R.nesc = nesc;
+    R.payload_len = plen;
+    if (codec == 2) {
+        const unsigned long long i = atomicAdd((unsigned long long *)&sc->n_codec2, 1ull);
+        codec2_list[i] = (int32_t)r;
+    }
+}
+
+// single CTA: file offsets of every block (region-id order) + CRC plan
+__global__ void __launch_bounds__(1024) k_layout(const EncParams *__restrict__ P,
+                                                 RegDev *__restrict__ regs, CrcSeg *__restrict__ segs,
+                                                 EncScalars *__restrict__ sc) {
+    __shared__ int64_t wsum[2][32];
+    __shared__ int64_t carry[2];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t nreg = P->nreg;
+    const uint64_t H = P->header_table;
+    const int seg0 = P->write_file ? 1 : 0;  // segment 0 = header+table
+    if (threadIdx.x == 0) {
+        carry[0] = 0;
+        carry[1] = 0;
+    }
+    __syncthreads();
+    auto nsc_of = [](uint64_t a, uint64_t b) -> int64_t {
+        const uint64_t a4 = (a + 3) & ~3ull, b4 = b & ~3ull;
+        const uint64_t W = a4 < b4 ? (b4 - a4) >> 2 : 0;
+        return W ? (int64_t)((W + kCrcScWords - 1) / kCrcScWords) : 1;
+    };
+    int64_t sc_head = 0;
+    if (P->write_file) sc_head = nsc_of(0, H);
+    for (int64_t t0 = 0; t0 < nreg; t0 += 1024) {
+        const int64_t r = t0 + threadIdx.x;
+        int64_t sz = 0, nsc = 0;
+        if (r < nreg) {
+            sz = kBlockHeader + regs[r].payload_len;
+        }
+        // block scan of sz
+        int64_t v = sz;
+        for (int off = 1; off < 32; off <<= 1) {
+            const int64_t o = __shfl_up_sync(0xFFFFFFFFu, v, off);
+            if (lane >= off) v += o;
+        }
+        if (lane == 31) wsum[0][warp] = v;
+        __syncthreads();
+        if (warp == 0) {
+            int64_t s = wsum[0][lane];
+            for (int off = 1; off < 32; off <<= 1) {
+                const int64_t o = __shfl_up_sync(0xFFFFFFFFu, s, off);
+                if (lane >= off) s += o;
+            }
+            wsum[0][lane] = s;
+        }
+        __syncthreads();
+        const int64_t excl = carry[0] + (warp ? wsum[0][warp - 1] : 0) + v - sz;
+        if (r < nreg) {
+            RegDev &R = regs[r];
+            R.block_off = H + (uint64_t)excl;
+            R.payload_off = R.block_off + kBlockHeader;
+            R.tok_start = R.payload_off +
+                          (R.codec == 2 ? (uint64_t)((R.n + 7) >> 3) + 8ull * (uint64_t)R.nesc : 0ull);
+            nsc = nsc_of(R.payload_off, R.payload_off + R.payload_len);
+        }
+        // scan of superchunk counts
+        int64_t u = nsc;
+        for (int off = 1; off < 32; off <<= 1) {
+            const int64_t o = __shfl_up_sync(0xFFFFFFFFu, u, off);
+            if (lane >= off) u += o;
+        }
+        if (lane == 31) wsum[1][warp] = u;
+        __syncthreads();
+        if (warp == 0) {
+            int64_t s = wsum[1][lane];
+            for (int off = 1; off < 32; off <<= 1) {
+                const int64_t o = __shfl_up_sync(0xFFFFFFFFu, s, off);
+                if (lane >= off) s += o;
+            }
+            wsum[1][lane] = s;
+        }
+        __syncthreads();
+        const int64_t uex = carry[1] + (warp ? wsum[1][warp - 1] : 0) + u - nsc;
+        if (r < nreg) {
+            CrcSeg &S = segs[seg0 + r];
+            S.begin = regs[r].payload_off;
+            S.end = regs[r].payload_off + regs[r].payload_len;
+            S.sc_base = sc_head + uex;
+            S.n_sc = nsc;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            carry[0] += wsum[0][31];
+            carry[1] += wsum[1][31];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        const uint64_t body = H + (uint64_t)carry[0];
+        sc->file_body = body;
+        sc->out_nbytes = body + (P->write_file ? 4 : 0);
+        sc->total_sc = sc_head + carry[1];
+        if (P->write_file) {
+            segs[0].begin = 0;
+            segs[0].end = H;
+            segs[0].sc_base = 0;
+            segs[0].n_sc = sc_head;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) k_scan_down(const EncParams *__restrict__ P,
+                                                   const RegDev *__restrict__ regs,
+                                                   const PieceRec *__restrict__ recs,
+                                                   const TokSeg *__restrict__ chunk_pre,
+                                                   PieceOff *__restrict__ poffs) {
+    const int64_t c = blockIdx.x;
+    __shared__ int64_t rlo, rhi;
+    if (threadIdx.x == 0) {
+        const RegDev &R = regs[find_region_by(regs, P->nreg, c, 1)];
+        rlo = R.piece_base;
+        rhi = R.piece_base + R.npieces;
+    }
+    __syncthreads();
+    const int64_t p0 = c * CH + threadIdx.x * 4;
+    TokSeg s[4];
+    TokSeg acc = tokseg_identity();
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int64_t p = p0 + k;
+        s[k] = (p >= rlo && p < rhi) ? piece_to_seg(recs[p]) : tokseg_identity();
+        acc = tokseg_combine(acc, s[k]);
+    }
+    TokSeg pre = tokseg_combine(chunk_pre[c], block_excl_scan(acc, nullptr));
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int64_t p = p0 + k;
+        if (p >= rlo && p < rhi) {
+            PieceOff o;
+            o.tok_off = pre.bytes + (pre.nz ? run_bytes(pre.lead) : 0);
+            o.carry = pre.nz ? pre.trail : pre.len;
+            o.esc_off = pre.nesc;
+            poffs[p] = o;
+        }
+        pre = tokseg_combine(pre, s[k]);
+    }
+}
+
+// escape bitmaps of codec-2 regions: one byte = 8 consecutive stream samples
+template <typename T>
+__global__ void __launch_bounds__(256) k_bitmap(const T *__restrict__ vol, const EncParams *__restrict__ P,
+                                                const RegDev *__restrict__ regs,
+                                                const int32_t *__restrict__ list,
+                                                const EncScalars *__restrict__ sc,
+                                                uint8_t *__restrict__ out) {
+    const int64_t nl = sc->n_codec2;
+    const int64_t NX = P->NX, NY = P->NY;
+    for (int64_t li = 0; li < nl; ++li) {
+        const RegDev &R = regs[list[li]];
+        const Quant Q = make_quant(R.e);
+        const int64_t nbytes = (R.n + 7) >> 3;
+        const int64_t plane = (int64_t)R.ex * R.ey;
+        for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nbytes;
+             b += (int64_t)gridDim.x * blockDim.x) {
+            uint8_t byte = 0;
+            for (int k = 0; k < 8; ++k) {
+                const int64_t s = 8 * b + k;
+                if (s >= R.n) break;
+                const int64_t z = s / plane, rem = s % plane;
+                const int64_t yy = rem / R.ex, xx = rem % R.ex;
+                const T v = vol[((R.oz + z) * NY + (R.oy + yy)) * NX + R.ox + xx];
+                bool esc;
+                quantize(Q, (double)v, esc);
+                if (esc) byte |= (uint8_t)(1u << k);
+            }
+            out[R.payload_off + b] = byte;
+        }
+    }
+}
+
+// file header (FORMAT.md, chr_archive.py:50) + region table (chr_archive.py:51)
+__global__ void __launch_bounds__(256) k_write_table(const EncParams *__restrict__ P,
+                                                     const RegDev *__restrict__ regs,
+                                                     uint8_t *__restrict__ out) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int m = P->m;
+    const int mb = (m + 7) / 8;
+    const int64_t table0 = kFileHeader + 4 + 8 * m + 4;
+    if (r == 0) {
+        uint8_t *p = out;
+        p[0] = 'C'; p[1] = 'H'; p[2] = 'R'; p[3] = '1';
+        put_le(p + 4, (uint16_t)1);
+        put_le(p + 6, (uint32_t)P->NX);
+        put_le(p + 10, (uint32_t)P->NY);
+        put_le(p + 14, (uint32_t)P->NZ);
+        put_le(p + 18, P->spacing[0]);
+        put_le(p + 26, P->spacing[1]);
+        put_le(p + 34, P->spacing[2]);
+        p[42] = (uint8_t)P->src_dtype;
+        put_le(p + 43, (uint32_t)P->bs);
+        put_le(p + 47, P->vmin);
+        put_le(p + 55, P->vmax);
+        put_le(p + 63, (uint32_t)m);
+        for (int i = 0; i < m; ++i) put_le(p + 67 + 8 * i, P->cands[i]);
+        put_le(p + 67 + 8 * m, (uint32_t)P->nreg);
+    }
+    if (r >= P->nreg) return;
+    const RegDev &R = regs[r];
+    uint8_t *p = out + table0 + r * (kRegionFixed + mb);
+    put_le(p, (uint32_t)r);
+    for (int a = 0; a < 3; ++a) {
+        put_le(p + 4 + 4 * a, (uint32_t)R.lo[a]);
+        put_le(p + 16 + 4 * a, (uint32_t)R.hi[a]);
+    }
+    put_le(p + 28, (uint32_t)R.ox);
+    put_le(p + 32, (uint32_t)R.oy);
+    put_le(p + 36, (uint32_t)R.oz);
+    put_le(p + 40, (uint32_t)R.ex);
+    put_le(p + 44, (uint32_t)R.ey);
+    put_le(p + 48, (uint32_t)R.ez);
+    p[52] = 0;                       // bound mode strict_vertices
+    put_le(p + 53, 1.0);             // stored accuracy
+    put_le(p + 61, R.e);
+    put_le(p + 69, (uint64_t)R.block_off);
+    put_le(p + 77, (uint64_t)(kBlockHeader + R.payload_len));
+    for (int i = 0; i < mb; ++i) p[85 + i] = (uint8_t)(R.mask >> (8 * i));
+}
+
+// 34-byte block headers + per-region CRC + file-CRC contributions
+__global__ void __launch_bounds__(128) k_finalize_regions(const EncParams *__restrict__ P,
+                                                          RegDev *__restrict__ regs,
+                                                          const uint32_t *__restrict__ seg_raw,
+                                                          const CrcTables *__restrict__ tabs,
+                                                          EncScalars *__restrict__ sc,
+                                                          uint8_t *__restrict__ out) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int seg0 = P->write_file ? 1 : 0;
+    const uint64_t body = sc->file_body;
+    if (r == 0 && P->write_file) {
+        const uint32_t c = crc_shift(tabs->x2n, seg_raw[0], body - P->header_table);
+        if (c) atomicXor(&sc->file_raw, c);
+    }
+    if (r >= P->nreg) return;
+    RegDev &R = regs[r];
+    const uint32_t praw = seg_raw[seg0 + r];
+    const uint32_t crc = crc_finalize(tabs->x2n, praw, (uint64_t)R.payload_len);
+    R.crc = crc;
+    uint8_t h[kBlockHeader];
+    h[0] = (uint8_t)R.codec;
+    put_le(h + 1, (uint32_t)R.ex);
+    put_le(h + 5, (uint32_t)R.ey);
+    put_le(h + 9, (uint32_t)R.ez);
+    put_le(h + 13, R.e);
+    h[21] = (uint8_t)P->src_dtype;
+    put_le(h + 22, (uint64_t)R.payload_len);
+    put_le(h + 30, crc);
+    uint8_t *dst = out + R.block_off;
+    for (int i = 0; i < kBlockHeader; ++i) dst[i] = h[i];
+    if (P->write_file) {
+        const uint32_t hraw = crc_raw_bytes(tabs->t[0], 0, h, kBlockHeader);
+        uint32_t c = crc_shift(tabs->x2n, hraw, body - (R.block_off + kBlockHeader));
+        c ^= crc_shift(tabs->x2n, praw, body - (R.payload_off + R.payload_len));
+        if (c) atomicXor(&sc->file_raw, c);
+    }
+}
+
+__global__ void k_finalize_file(const CrcTables *__restrict__ tabs, const EncScalars *__restrict__ sc,
+                                uint8_t *__restrict__ out) {
+    const uint32_t crc = crc_finalize(tabs->x2n, sc->file_raw, sc->file_body);
+    put_le(out + sc->file_body, crc);
+}
+
+// ------------------------------------------------------------------ host
+struct EncPlan {
+    std::vector<RegDev> regs;
+    int64_t nitems = 0, npieces_total = 0, nchunks = 0;
+    size_t ws_bytes = 0;
+    // carved pointers
+    EncParams *params;
+    RegDev *d_regs;
+    PieceRec *recs;
+    PieceOff *poffs;
+    TokSeg *chunk;
+    CrcSeg *segs;
+    uint32_t *seg_raw;
+    int32_t *codec2;
+    EncScalars *scal;
+};
+
+static bool build_plan(const chr_region_t *h, int64_t nreg, EncPlan &pl) {
+    pl.regs.resize(nreg);
+    int64_t item = 0, piece = 0, chunk = 0;
+    for (int64_t r = 0; r < nreg; ++r) {
+        RegDev &R = pl.regs[r];
+        std::memset(&R, 0, sizeof(R));
+        R.ox = h[r].origin[0];
+        R.oy = h[r].origin[1];
+        R.oz = h[r].origin[2];
+        R.ex = h[r].extent[0];
+        R.ey = h[r].extent[1];
+        R.ez = h[r].extent[2];
+        if (R.ex < 1 || R.ey < 1 || R.ez < 1) return false;
+        R.e = h[r].error_bound;
+        if (!(R.e >= 0.0) || !std::isfinite(R.e)) return false;
+        R.mode = R.e == 0.0 ? 1 : 0;
+        R.n = (int64_t)R.ex * R.ey * R.ez;
+        R.ntx = (int32_t)ceil_div(R.ex, TX);
+        R.nty = (int32_t)ceil_div(R.ey, TY);
+        R.nzc = (int32_t)ceil_div(R.ez, ZC);
+        R.item_base = item;
+        item += (int64_t)R.ntx * R.nty * R.nzc;
+        R.piece_base = piece;
+        R.npieces = (int64_t)R.ntx * R.ey * R.ez;
+        R.chunk_base = chunk;
+        R.nchunks = ceil_div(R.npieces, CH);
+        chunk += R.nchunks;
+        piece += R.nchunks * CH;
+        R.mask = h[r].mask;
+        for (int a = 0; a < 3; ++a) {
+            R.lo[a] = h[r].lo[a];
+            R.hi[a] = h[r].hi[a];
+        }
+    }
+    pl.nitems = item;
+    pl.npieces_total = piece;
+    pl.nchunks = chunk;
+    return true;
+}
+
+static void carve(EncPlan &pl, void *base, size_t cap) {
+    WsCarver c{reinterpret_cast<char *>(base), 0, cap};
+    const int64_t nreg = (int64_t)pl.regs.size();
+    pl.params = c.take<EncParams>(1);
+    pl.d_regs = c.take<RegDev>(nreg);
+    pl.recs = c.take<PieceRec>(pl.npieces_total);
+    pl.poffs = c.take<PieceOff>(pl.npieces_total);
+    pl.chunk = c.take<TokSeg>(pl.nchunks);
+    pl.segs = c.take<CrcSeg>(nreg + 1);
+    pl.seg_raw = c.take<uint32_t>(nreg + 1);
+    pl.codec2 = c.take<int32_t>(nreg);
+    pl.scal = c.take<EncScalars>(1);
+    pl.ws_bytes = c.off + 256;
+}
+
+}  // namespace chr
+
+using namespace chr;
+
+extern "C" size_t chr_compress_workspace_size(const chr_region_t *h, int64_t nreg) {
+    EncPlan pl;
+    if (!h || nreg < 1 || !build_plan(h, nreg, pl)) return 0;
+    carve(pl, nullptr, ~size_t(0));
+    return pl.ws_bytes;
+}
+
+extern "C" uint64_t chr_compress_capacity(const chr_region_t *h, int64_t nreg, int m, int src_dtype) {
+    (void)src_dtype;
+    uint64_t cap = (uint64_t)kFileHeader + 4 + 8ull * m + 4 + 4;
+    const int mb = (m + 7) / 8;
+    for (int64_t r = 0; r < nreg; ++r) {
+        const uint64_t n = (uint64_t)h[r].extent[0] * h[r].extent[1] * h[r].extent[2];
+        cap += kRegionFixed + mb + kBlockHeader + 8 * n;
+    }
+    return cap;
+}
+
+extern "C" int chr_compress(const void *d_vol, int dtype, int src_dtype, int64_t nx, int64_t ny,
+                            int64_t nz, const double *spacing, int64_t bs, double vmin, double vmax,
+                            const double *h_cands, int m, chr_region_t *h_regions, int64_t nreg,
+                            int write_file, void *d_ws, size_t ws_bytes, uint8_t *d_out,
+                            uint64_t out_cap, uint64_t *h_out_nbytes, void *stream) {
+    if (!d_vol || !h_regions || nreg < 1 || !d_out || !h_out_nbytes) return CHR_E_PARAMETER;
+    if (dtype != CHR_F32 && dtype != CHR_F64) return CHR_E_PARAMETER;
+    if (src_dtype != CHR_F32 && src_dtype != CHR_F64) return CHR_E_PARAMETER;
+    if (write_file && (m < 1 || m > 64 || !h_cands || !spacing)) return CHR_E_PARAMETER;
+    cudaStream_t st = (cudaStream_t)stream;
+    EncPlan pl;
+    if (!build_plan(h_regions, nreg, pl)) return CHR_E_PARAMETER;
+    for (const RegDev &R : pl.regs)
+        if (R.ox < 0 || R.oy < 0 || R.oz < 0 || R.ox + R.ex > nx || R.oy + R.ey > ny || R.oz + R.ez > nz)
+            return CHR_E_PARAMETER;
+    carve(pl, d_ws, ws_bytes);
+    if (!d_ws || pl.ws_bytes > ws_bytes) return CHR_E_WORKSPACE;
+    const CrcTables *tabs = crc_tables_device();
+    if (!tabs) return CHR_E_CUDA;
+
+    EncParams hp;
+    std::memset(&hp, 0, sizeof(hp));
+    hp.NX = nx;
+    hp.NY = ny;
+    hp.NZ = nz;
+    hp.nreg = nreg;
+    hp.nitems = pl.nitems;
+    hp.nchunks = pl.nchunks;
+    hp.dtype = dtype;
+    hp.src_dtype = src_dtype;
+    hp.write_file = write_file ? 1 : 0;
+    hp.m = write_file ? m : 0;
+    for (int a = 0; a < 3; ++a) hp.spacing[a] = spacing ? spacing[a] : 1.0;
+    hp.vmin = vmin;
+    hp.vmax = vmax;
+    hp.bs = bs;
+    for (int i = 0; i < hp.m; ++i) hp.cands[i] = h_cands[i];
+    hp.header_table = write_file ? (uint64_t)(kFileHeader + 4 + 8 * m + 4) +
+                                       (uint64_t)nreg * (kRegionFixed + (m + 7) / 8)
+                                 : 0;
+    // capacity check against the worst case (verbatim f64 everywhere)
+    if (out_cap < chr_compress_capacity(h_regions, nreg, m, src_dtype)) return CHR_E_PARAMETER;
+
+    CHR_CUDA_TRY(cudaMemcpyAsync(pl.params, &hp, sizeof(hp), cudaMemcpyHostToDevice, st));
+    CHR_CUDA_TRY(cudaMemcpyAsync(pl.d_regs, pl.regs.data(), sizeof(RegDev) * nreg,
+                                 cudaMemcpyHostToDevice, st));
+    CHR_CUDA_TRY(cudaMemsetAsync(pl.scal, 0, sizeof(EncScalars), st));
+    CHR_CUDA_TRY(cudaMemsetAsync(pl.seg_raw, 0, sizeof(uint32_t) * (nreg + 1), st));
+
+    const unsigned items = (unsigned)pl.nitems, chunks = (unsigned)pl.nchunks;
+    if (dtype == CHR_F32)
+        k_tile<float, false><<<items, NW * 32, 0, st>>>((const float *)d_vol, pl.params, pl.d_regs,
+                                                        pl.recs, pl.poffs, d_out);
+    else
+        k_tile<double, false><<<items, NW * 32, 0, st>>>((const double *)d_vol, pl.params, pl.d_regs,
+                                                         pl.recs, pl.poffs, d_out);
+    k_scan_reduce<<<chunks, 256, 0, st>>>(pl.params, pl.d_regs, pl.recs, pl.chunk);
+    k_scan_regions<<<(unsigned)ceil_div(nreg, 128), 128, 0, st>>>(pl.params, pl.d_regs, pl.chunk,
+                                                                  pl.codec2, pl.scal);
+    k_layout<<<1, 1024, 0, st>>>(pl.params, pl.d_regs, pl.segs, pl.scal);
+    k_scan_down<<<chunks, 256, 0, st>>>(pl.params, pl.d_regs, pl.recs, pl.chunk, pl.poffs);
+    if (dtype == CHR_F32) {
+        k_tile<float, true><<<items, NW * 32, 0, st>>>((const float *)d_vol, pl.params, pl.d_regs,
+                                                       pl.recs, pl.poffs, d_out);
+        k_bitmap<float><<<148, 256, 0, st>>>((const float *)d_vol, pl.params, pl.d_regs, pl.codec2,
+                                             pl.scal, d_out);
+    } else {
+        k_tile<double, true><<<items, NW * 32, 0, st>>>((const double *)d_vol, pl.params, pl.d_regs,
+                                                        pl.recs, pl.poffs, d_out);
+        k_bitmap<double><<<148, 256, 0, st>>>((const double *)d_vol, pl.params, pl.d_regs, pl.codec2,
+                                              pl.scal, d_out);
+    }
+    if (write_file)
+        k_write_table<<<(unsigned)ceil_div(nreg, 256), 256, 0, st>>>(pl.params, pl.d_regs, d_out);
+    CHR_CUDA_TRY(cudaGetLastError());
+    // CRC segments: the superchunk total lives on the device; a persistent
+    // grid strides over it (no host round trip)
+    EncScalars hs;
+    const int64_t nseg = nreg + (write_file ? 1 : 0);
+    int rc = crc_launch(d_out, pl.segs, nseg, 0, pl.seg_raw, st);
+    if (rc) return rc;
+    k_finalize_regions<<<(unsigned)ceil_div(nreg, 128), 128, 0, st>>>(pl.params, pl.d_regs, pl.seg_raw,
+                                                                      tabs, pl.scal, d_out);
+    if (write_file) k_finalize_file<<<1, 1, 0, st>>>(tabs, pl.scal, d_out);
+    CHR_CUDA_TRY(cudaGetLastError());
+    CHR_CUDA_TRY(cudaMemcpyAsync(pl.regs.data(), pl.d_regs, sizeof(RegDev) * nreg,
+                                 cudaMemcpyDeviceToHost, st));
+    CHR_CUDA_TRY(cudaMemcpyAsync(&hs, pl.scal, sizeof(hs), cudaMemcpyDeviceToHost, st));
+    CHR_CUDA_TRY(cudaStreamSynchronize(st));
+    for (int64_t r = 0; r < nreg; ++r) {
+        const RegDev &R = pl.regs[r];
+        chr_region_t &o = h_regions[r];
+        o.codec_id = R.codec;
+        o.payload_crc = R.crc;
+        o.block_offset = R.block_off;
+        o.block_nbytes = kBlockHeader + (uint64_t)R.payload_len;
+        o.n_escaped = (uint64_t)R.nesc;
+    }
+    *h_out_nbytes = hs.out_nbytes;
+    return CHR_OK;
+}

@@ -1,0 +1,591 @@
+// mc.cu -- step 5 of the hot path: marching cubes as count -> scan -> emit,
+// reproducing the reference mesh exactly (kernels.py:428-524 mc_extract,
+// isosurf.py:183-204 marching_cubes, isosurf.py:207-225 merge_meshes).
+//
+// Reference ordering: cells z-outer / y / x-inner, triangle slots in
+// TRI_TABLE order, a vertex is created the first time its canonical edge
+// (axis, low corner) is touched.  Because every TRI_TABLE row references
+// exactly the crossing edges of its case, the first touch of an edge is by
+// the minimum-index cell containing it, the OWNER:
+//   owner of an axis-a edge at lattice point p = p with every other
+//   coordinate q replaced by max(p_q - 1, 0).
+// So a cell owns the crossing edges whose perpendicular low offsets are 1
+// (or 0 at a grid boundary), the vertex id of an owned edge is
+//   (owned crossing edges in earlier cells) + (its first-appearance rank in
+//   the owner's triangle row), and both come from tables + one scan.
+//
+//   k_mc_count   warp per 64-cell row piece: triangles, owned vertices
+//   k_mc_reduce / k_mc_grids / k_mc_down   chunked exclusive scans
+//   k_mc_emit    CTA = 64 cells x 8 rows, marching z with a halo row, a
+//                halo column and a halo plane in shared memory, so every
+//                owner cell's (code, vertex base) is local.
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "chr_internal.cuh"
+#include "mc_tables.h"
+
+namespace chr {
+
+constexpr int MTX = 64, MTY = 8, MZC = 16, MNW = MTY + 1;
+constexpr int64_t MCH = 1024;
+
+// Bourke corner index of unit offset (x, y, z) (mc_tables.py:8-12)
+#define CHR_CORNER_OF(x, y, z) (4 * (z) + ((2 * (y)) | ((x) ^ (y))))
+
+struct __align__(16) McTables {
+    int8_t tri[256][16];
+    uint8_t ntri[256];
+    uint8_t owncnt[256][8];   // owned crossing edges per (code, boundary flags)
+    int8_t rank[256][8][12];  // first-appearance rank among owned edges, -1 if not owned
+    uint16_t cross[256];      // crossing-edge mask
+    uint8_t edge_axis[12];
+    uint8_t edge_low[12][3];
+    int8_t edge_id[3][2][2][2];  // [axis][lx][ly][lz] -> Bourke edge (l_axis == 0)
+};
+
+static McTables g_mct;
+static McTables *g_dmct = nullptr;
+static std::once_flag g_mct_once;
+static std::mutex g_mct_mu;
+
+// flags bit a set <=> the cell's coordinate along axis a is 0
+static bool owned_by(int e, int flags) {
+    const int a = CHR_EDGE_AXIS[e];
+    for (int q = 0; q < 3; ++q) {
+        if (q == a) continue;
+        if (!(CHR_EDGE_LOW[e][q] == 1 || ((flags >> q) & 1))) return false;
+    }
+    return true;
+}
+
+static void mc_tables_host() {
+    McTables &T = g_mct;
+    std::memset(&T, 0, sizeof(T));
+    std::memcpy(T.tri, CHR_TRI_TABLE, sizeof(T.tri));
+    std::memcpy(T.ntri, CHR_NTRI_TABLE, sizeof(T.ntri));
+    std::memcpy(T.edge_axis, CHR_EDGE_AXIS, sizeof(T.edge_axis));
+    std::memcpy(T.edge_low, CHR_EDGE_LOW, sizeof(T.edge_low));
+    std::memset(T.edge_id, -1, sizeof(T.edge_id));
+    for (int e = 0; e < 12; ++e)
+        T.edge_id[CHR_EDGE_AXIS[e]][CHR_EDGE_LOW[e][0]][CHR_EDGE_LOW[e][1]][CHR_EDGE_LOW[e][2]] = (int8_t)e;
+    for (int c = 0; c < 256; ++c) {
+        uint16_t cm = 0;
+        for (int e = 0; e < 12; ++e) {
+            const int a = CHR_EDGE_CORNERS[e][0], b = CHR_EDGE_CORNERS[e][1];
+            if (((c >> a) & 1) != ((c >> b) & 1)) cm |= (uint16_t)(1u << e);
+        }
+        T.cross[c] = cm;
+        for (int f = 0; f < 8; ++f) {
+            for (int e = 0; e < 12; ++e) T.rank[c][f][e] = -1;
+            int cnt = 0;
+            for (int s = 0; s < 3 * CHR_NTRI_TABLE[c]; ++s) {
+                const int e = CHR_TRI_TABLE[c][s];
+                if (T.rank[c][f][e] < 0 && owned_by(e, f)) T.rank[c][f][e] = (int8_t)cnt++;
+            }
+            T.owncnt[c][f] = (uint8_t)cnt;
+        }
+    }
+}
+
+static const McTables *mc_tables_device() {
+    std::call_once(g_mct_once, mc_tables_host);
+    std::lock_guard<std::mutex> lk(g_mct_mu);
+    if (!g_dmct) {
+        McTables *d = nullptr;
+        if (cudaMalloc(&d, sizeof(McTables)) != cudaSuccess) return nullptr;
+        if (cudaMemcpy(d, &g_mct, sizeof(McTables), cudaMemcpyHostToDevice) != cudaSuccess) {
+            cudaFree(d);
+            return nullptr;
+        }
+        g_dmct = d;
+    }
+    return g_dmct;
+}
+
+struct McGrid {
+    uint64_t goff;
+    int32_t nx, ny, nz, ncx, ncy, ncz, ntx, pad;
+    double origin[3], spacing[3];
+    int64_t piece_base, npieces, chunk_base, nchunks, item_base;
+    int64_t tri_base, vert_base;    // in the merged output (device scan)
+    int64_t ntri, nvert;
+};
+
+struct McPieceCnt {
+    int32_t tri, vert;
+};
+struct McPieceBase {
+    int64_t tri, vert;
+};
+
+__device__ __forceinline__ int64_t find_grid(const McGrid *__restrict__ g, int64_t n, int64_t key, int which) {
+    int64_t lo = 0, hi = n - 1;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi + 1) >> 1;
+        const int64_t b = which == 0 ? g[mid].piece_base : (which == 1 ? g[mid].chunk_base : g[mid].item_base);
+        if (b <= key) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+// Bourke-order case code of cell (cx,cy,cz) (kernels.py:451-467), corner values out
+__device__ __forceinline__ int cell_code(const double *__restrict__ g, int64_t nx, int64_t nxy, int cx, int cy,
+                                         int cz, double k, double c[8]) {
+    const double *p = g + (int64_t)cz * nxy + (int64_t)cy * nx + cx;
+    c[0] = __ldg(p);
+    c[1] = __ldg(p + 1);
+    c[2] = __ldg(p + nx + 1);
+    c[3] = __ldg(p + nx);
+    c[4] = __ldg(p + nxy);
+    c[5] = __ldg(p + nxy + 1);
+    c[6] = __ldg(p + nxy + nx + 1);
+    c[7] = __ldg(p + nxy + nx);
+    int code = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) code |= (c[i] >= k) ? (1 << i) : 0;
+    return code;
+}
+
+__device__ __forceinline__ int bflags(int cx, int cy, int cz) {
+    return (cx == 0 ? 1 : 0) | (cy == 0 ? 2 : 0) | (cz == 0 ? 4 : 0);
+}
+
+// warp per row piece: triangle and owned-vertex counts
+__global__ void __launch_bounds__(256) k_mc_count(const double *__restrict__ grids, const McGrid *__restrict__ G,
+                                                  int64_t ng, int64_t npieces_total, double k,
+                                                  const McTables *__restrict__ T,
+                                                  McPieceCnt *__restrict__ cnt) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t p = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); p < npieces_total; p += warps) {
+        const McGrid &g = G[find_grid(G, ng, p, 0)];
+        const int64_t lp = p - g.piece_base;
+        if (lp >= g.npieces) continue;  // chunk padding
+        const int xt = (int)(lp % g.ntx);
+        const int64_t rr = lp / g.ntx;
+        const int cy = (int)(rr % g.ncy), cz = (int)(rr / g.ncy);
+        const double *gp = grids + g.goff;
+        const int64_t nxy = (int64_t)g.nx * g.ny;
+        int t = 0, v = 0;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int cx = xt * MTX + h * 32 + lane;
+            if (cx < g.ncx) {
+                double c[8];
+                const int code = cell_code(gp, g.nx, nxy, cx, cy, cz, k, c);
+                t += T->ntri[code];
+                v += T->owncnt[code][bflags(cx, cy, cz)];
+            }
+        }
+        t = __reduce_add_sync(0xFFFFFFFFu, t);
+        v = __reduce_add_sync(0xFFFFFFFFu, v);
+        if (lane == 0) {
+            McPieceCnt o;
+            o.tri = t;
+            o.vert = v;
+            cnt[p] = o;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) k_mc_reduce(const McPieceCnt *__restrict__ cnt, McPieceBase *__restrict__ chunk) {
+    const int64_t c = blockIdx.x;
+    int64_t t = 0, v = 0;
+    for (int i = threadIdx.x; i < MCH; i += blockDim.x) {
+        const McPieceCnt x = cnt[c * MCH + i];
+        t += x.tri;
+        v += x.vert;
+    }
+    __shared__ int64_t st[8], sv[8];
+    for (int off = 16; off; off >>= 1) {
+        t += __shfl_xor_sync(0xFFFFFFFFu, t, off);
+        v += __shfl_xor_sync(0xFFFFFFFFu, v, off);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        st[threadIdx.x >> 5] = t;
+        sv[threadIdx.x >> 5] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int64_t a = 0, b = 0;
+        for (int i = 0; i < 8; ++i) {
+            a += st[i];
+            b += sv[i];
+        }
+        chunk[c].tri = a;
+        chunk[c].vert = b;
+    }
+}
+
+// one thread: per grid chunk prefixes + grid totals + merged grid bases
+__global__ void k_mc_grids(McGrid *__restrict__ G, int64_t ng, McPieceBase *__restrict__ chunk,
+                           int64_t *__restrict__ totals) {
+    if (blockIdx.x || threadIdx.x) return;
+    int64_t gt = 0, gv = 0;
+    for (int64_t i = 0; i < ng; ++i) {
+        McGrid &g = G[i];
+        int64_t t = 0, v = 0;
+        for (int64_t c = g.chunk_base; c < g.chunk_base + g.nchunks; ++c) {
+            const McPieceBase x = chunk[c];
+            chunk[c].tri = t;
+            chunk[c].vert = v;
+            t += x.tri;
+            v += x.vert;
+        }
+        g.ntri = t;
+        g.nvert = v;
+        g.tri_base = gt;
+        g.vert_base = gv;
+        gt += t;
+        gv += v;
+    }
+    totals[0] = gt;
+    totals[1] = gv;
+}
+
+__global__ void __launch_bounds__(256) k_mc_down(const McPieceCnt *__restrict__ cnt,
+                                                 const McPieceBase *__restrict__ chunk,
+                                                 McPieceBase *__restrict__ base) {
+    const int64_t c = blockIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // 4 consecutive pieces per thread
+    McPieceCnt x[4];
+    int64_t t = 0, v = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        x[i] = cnt[c * MCH + threadIdx.x * 4 + i];
+        t += x[i].tri;
+        v += x[i].vert;
+    }
+    int64_t it = t, iv = v;
+    for (int off = 1; off < 32; off <<= 1) {
+        const int64_t a = __shfl_up_sync(0xFFFFFFFFu, it, off);
+        const int64_t b = __shfl_up_sync(0xFFFFFFFFu, iv, off);
+        if (lane >= off) {
+            it += a;
+            iv += b;
+        }
+    }
+    __shared__ int64_t st[8], sv[8];
+    if (lane == 31) {
+        st[warp] = it;
+        sv[warp] = iv;
+    }
+    __syncthreads();
+    int64_t pt = chunk[c].tri, pv = chunk[c].vert;
+    for (int i = 0; i < warp; ++i) {
+        pt += st[i];
+        pv += sv[i];
+    }
+    pt += it - t;
+    pv += iv - v;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        McPieceBase b;
+        b.tri = pt;
+        b.vert = pv;
+        base[c * MCH + threadIdx.x * 4 + i] = b;
+        pt += x[i].tri;
+        pv += x[i].vert;
+    }
+}
+
+__device__ __forceinline__ double world(double origin, double lat, double spacing) {
+    return __dadd_rn(origin, __dmul_rn(lat, spacing));
+}
+
+// emit: see header.  sC/sV: (code, vertex base) of cells x0-1 .. x0+63 for
+// rows cy0-1 .. cy0+7 at planes cz-1 and cz (3-deep ring over planes).
+__global__ void __launch_bounds__(MNW * 32) k_mc_emit(const double *__restrict__ grids,
+                                                      const McGrid *__restrict__ G, int64_t ng, double k,
+                                                      const McTables *__restrict__ T,
+                                                      const McPieceBase *__restrict__ base,
+                                                      double *__restrict__ verts, int32_t *__restrict__ tris) {
+    __shared__ uint8_t sC[3][MNW][MTX + 1];
+    __shared__ int64_t sV[3][MNW][MTX + 1];
+    __shared__ McGrid g;
+    __shared__ McTables tb;
+    {
+        const int4 *src = reinterpret_cast<const int4 *>(T);
+        int4 *dst = reinterpret_cast<int4 *>(&tb);
+        for (int i = threadIdx.x; i < (int)(sizeof(McTables) / 16); i += blockDim.x) dst[i] = src[i];
+    }
+    const int64_t item = blockIdx.x;
+    if (threadIdx.x == 0) g = G[find_grid(G, ng, item, 2)];
+    __syncthreads();
+    const int64_t local = item - g.item_base;
+    const int nyt = (g.ncy + MTY - 1) / MTY;
+    const int xt = (int)(local % g.ntx);
+    const int64_t r2 = local / g.ntx;
+    const int yt = (int)(r2 % nyt), zc = (int)(r2 / nyt);
+    const int x0 = xt * MTX, y0 = yt * MTY, z0 = zc * MZC;
+    const int z1 = min(z0 + MZC, g.ncz);
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int cy = y0 - 1 + w;
+    const bool rowok = cy >= 0 && cy < g.ncy;
+    const double *gp = grids + g.goff;
+    const int64_t nxy = (int64_t)g.nx * g.ny;
+    const int cxs[2] = {x0 + lane, x0 + 32 + lane};
+    const int zs = z0 > 0 ? z0 - 1 : z0;
+    for (int cz = zs; cz < z1; ++cz) {
+        const int buf = cz % 3;
+        double cA[8], cB[8], cH[8];
+        int codeA = 0, codeB = 0, codeH = 0, ownA = 0, ownB = 0, ownH = 0, ntA = 0, ntB = 0;
+        const bool okA = rowok && cxs[0] < g.ncx, okB = rowok && cxs[1] < g.ncx;
+        const bool okH = rowok && lane == 0 && x0 > 0;
+        if (okA) {
+            codeA = cell_code(gp, g.nx, nxy, cxs[0], cy, cz, k, cA);
+            ownA = tb.owncnt[codeA][bflags(cxs[0], cy, cz)];
+            ntA = tb.ntri[codeA];
+        }
+        if (okB) {
+            codeB = cell_code(gp, g.nx, nxy, cxs[1], cy, cz, k, cB);
+            ownB = tb.owncnt[codeB][bflags(cxs[1], cy, cz)];
+            ntB = tb.ntri[codeB];
+        }
+        if (okH) {
+            codeH = cell_code(gp, g.nx, nxy, x0 - 1, cy, cz, k, cH);
+            ownH = tb.owncnt[codeH][bflags(x0 - 1, cy, cz)];
+        }
+        // exclusive scans (cells A: 0..31, B: 32..63) of owned vertices and triangles
+        int sA = ownA, sB = ownB, tA = ntA, tB = ntB;
+        for (int off = 1; off < 32; off <<= 1) {
+            const int a = __shfl_up_sync(0xFFFFFFFFu, sA, off), b = __shfl_up_sync(0xFFFFFFFFu, sB, off);
+            const int c = __shfl_up_sync(0xFFFFFFFFu, tA, off), d = __shfl_up_sync(0xFFFFFFFFu, tB, off);
+            if (lane >= off) {
+                sA += a;
+                sB += b;
+                tA += c;
+                tB += d;
+            }
+        }
+        const int totV = __shfl_sync(0xFFFFFFFFu, sA, 31), totT = __shfl_sync(0xFFFFFFFFu, tA, 31);
+        sA -= ownA;
+        sB = sB - ownB + totV;
+        tA -= ntA;
+        tB = tB - ntB + totT;
+        McPieceBase pb;
+        pb.tri = 0;
+        pb.vert = 0;
+        if (rowok) pb = base[g.piece_base + ((int64_t)cz * g.ncy + cy) * g.ntx + xt];
+        sC[buf][w][1 + lane] = (uint8_t)codeA;
+        sC[buf][w][33 + lane] = (uint8_t)codeB;
+        sV[buf][w][1 + lane] = pb.vert + sA;
+        sV[buf][w][33 + lane] = pb.vert + sB;
+        if (lane == 0) {
+            sC[buf][w][0] = (uint8_t)codeH;
+            sV[buf][w][0] = pb.vert - ownH;
+        }
+        __syncthreads();
+        if (cz < z0 || w == 0 || !rowok) continue;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const bool ok = h == 0 ? okA : okB;
+            if (!ok) continue;
+            const int code = h == 0 ? codeA : codeB;
+            const int nt = tb.ntri[code];
+            if (nt == 0) continue;
+            const int cx = cxs[h];
+            const double *c = h == 0 ? cA : cB;
+            const int col = 1 + cx - x0;
+            const int f = bflags(cx, cy, cz);
+            const int64_t vb = sV[buf][w][col];
+            // owned vertices (first-appearance order)
+            const int8_t *rk = tb.rank[code][f];
+            for (int e = 0; e < 12; ++e) {
+                const int r = rk[e];
+                if (r < 0) continue;
+                const int a = tb.edge_axis[e];
+                const int lx = tb.edge_low[e][0], ly = tb.edge_low[e][1], lz = tb.edge_low[e][2];
+                const int c0 = CHR_CORNER_OF(lx, ly, lz);
+                const int c1 = CHR_CORNER_OF(lx + (a == 0), ly + (a == 1), lz + (a == 2));
+                const double s0 = c[c0], s1 = c[c1];
+                const double den = __dadd_rn(s1, -s0);
+                const double t = den == 0.0 ? 0.0 : __ddiv_rn(__dadd_rn(k, -s0), den);
+                double lat[3] = {(double)(cx + lx), (double)(cy + ly), (double)(cz + lz)};
+                lat[a] = __dadd_rn(lat[a], t);
+                double *o = verts + 3 * (g.vert_base + vb + r);
+                o[0] = world(g.origin[0], lat[0], g.spacing[0]);
+                o[1] = world(g.origin[1], lat[1], g.spacing[1]);
+                o[2] = world(g.origin[2], lat[2], g.spacing[2]);
+            }
+            // triangles
+            const int64_t tb0 = g.tri_base + pb.tri + (h == 0 ? tA : tB);
+            int32_t *to = tris + 3 * tb0;
+            for (int s = 0; s < 3 * nt; ++s) {
+                const int e = tb.tri[code][s];
+                const int a = tb.edge_axis[e];
+                int l[3] = {tb.edge_low[e][0], tb.edge_low[e][1], tb.edge_low[e][2]};
+                const int cc[3] = {cx, cy, cz};
+                int d[3] = {0, 0, 0};
+#pragma unroll
+                for (int q = 0; q < 3; ++q) {
+                    if (q == a) continue;
+                    if (l[q] == 0 && cc[q] >= 1) {
+                        d[q] = -1;
+                        l[q] = 1;
+                    }
+                }
+                const int e2 = tb.edge_id[a][l[0]][l[1]][l[2]];
+                const int ob = (cz + d[2]) % 3;
+                const int orow = w + d[1], ocol = col + d[0];
+                const int ocode = sC[ob][orow][ocol];
+                const int of = bflags(cx + d[0], cy + d[1], cz + d[2]);
+                const int64_t vid = sV[ob][orow][ocol] + tb.rank[ocode][of][e2];
+                to[s] = (int32_t)(g.vert_base + vid);
+            }
+        }
+    }
+}
+
+__global__ void k_case_codes(const double *__restrict__ g, int64_t nx, int64_t ny, int64_t nz, double k,
+                             int binary, uint8_t *__restrict__ codes) {
+    const int64_t ncx = nx - 1, ncy = ny - 1, ncz = nz - 1;
+    const int64_t n = ncx * ncy * ncz;
+    const int64_t nxy = nx * ny;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int cx = (int)(i % ncx), cy = (int)((i / ncx) % ncy), cz = (int)(i / (ncx * ncy));
+        double c[8];
+        int code = cell_code(g, nx, nxy, cx, cy, cz, k, c);
+        if (binary) {  // Bourke -> binary: swap bits 2<->3 and 6<->7
+            const int b2 = (code >> 2) & 1, b3 = (code >> 3) & 1, b6 = (code >> 6) & 1, b7 = (code >> 7) & 1;
+            code = (code & 0x33) | (b3 << 2) | (b2 << 3) | (b7 << 6) | (b6 << 7);
+        }
+        codes[i] = (uint8_t)code;
+    }
+}
+
+// ------------------------------------------------------------------ host
+struct McPlan {
+    std::vector<McGrid> grids;
+    int64_t npieces = 0, nchunks = 0, nitems = 0;
+    size_t ws = 0;
+    McGrid *d_grids;
+    McPieceCnt *cnt;
+    McPieceBase *chunk, *base;
+    int64_t *totals;
+};
+
+static bool mc_build(const chr_mc_grid_t *h, int64_t n, McPlan &pl) {
+    pl.grids.resize(n);
+    int64_t piece = 0, chunk = 0, item = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        McGrid &g = pl.grids[i];
+        std::memset(&g, 0, sizeof(g));
+        g.goff = h[i].grid_offset;
+        g.nx = h[i].dims[0];
+        g.ny = h[i].dims[1];
+        g.nz = h[i].dims[2];
+        if (g.nx < 2 || g.ny < 2 || g.nz < 2) return false;
+        g.ncx = g.nx - 1;
+        g.ncy = g.ny - 1;
+        g.ncz = g.nz - 1;
+        g.ntx = (int32_t)ceil_div(g.ncx, MTX);
+        for (int a = 0; a < 3; ++a) {
+            g.origin[a] = h[i].origin[a];
+            g.spacing[a] = h[i].spacing[a];
+        }
+        g.piece_base = piece;
+        g.npieces = (int64_t)g.ntx * g.ncy * g.ncz;
+        g.chunk_base = chunk;
+        g.nchunks = ceil_div(g.npieces, MCH);
+        piece += g.nchunks * MCH;
+        chunk += g.nchunks;
+        g.item_base = item;
+        item += (int64_t)g.ntx * ceil_div(g.ncy, MTY) * ceil_div(g.ncz, MZC);
+    }
+    pl.npieces = piece;
+    pl.nchunks = chunk;
+    pl.nitems = item;
+    return true;
+}
+
+static void mc_carve(McPlan &pl, void *base, size_t cap) {
+    WsCarver c{reinterpret_cast<char *>(base), 0, cap};
+    pl.d_grids = c.take<McGrid>(pl.grids.size());
+    pl.cnt = c.take<McPieceCnt>(pl.npieces);
+    pl.chunk = c.take<McPieceBase>(pl.nchunks);
+    pl.base = c.take<McPieceBase>(pl.npieces);
+    pl.totals = c.take<int64_t>(2);
+    pl.ws = c.off + 256;
+}
+
+}  // namespace chr
+
+using namespace chr;
+
+extern "C" size_t chr_mc_workspace_size(const chr_mc_grid_t *h, int64_t n) {
+    McPlan pl;
+    if (!h || n < 1 || !mc_build(h, n, pl)) return 256;
+    mc_carve(pl, nullptr, ~size_t(0));
+    return pl.ws;
+}
+
+extern "C" int chr_mc_count(const double *d_grids, const chr_mc_grid_t *h, int64_t n, double k, void *d_ws,
+                            size_t ws_bytes, int64_t *h_ntri, int64_t *h_nvert, int64_t *h_total_tri,
+                            int64_t *h_total_vert, void *stream) {
+    if (n == 0) {
+        if (h_total_tri) *h_total_tri = 0;
+        if (h_total_vert) *h_total_vert = 0;
+        return CHR_OK;
+    }
+    if (!d_grids || !h || n < 0) return CHR_E_PARAMETER;
+    cudaStream_t st = (cudaStream_t)stream;
+    McPlan pl;
+    if (!mc_build(h, n, pl)) return CHR_E_PARAMETER;
+    mc_carve(pl, d_ws, ws_bytes);
+    if (!d_ws || pl.ws > ws_bytes) return CHR_E_WORKSPACE;
+    const McTables *T = mc_tables_device();
+    if (!T) return CHR_E_CUDA;
+    CHR_CUDA_TRY(cudaMemcpyAsync(pl.d_grids, pl.grids.data(), sizeof(McGrid) * n, cudaMemcpyHostToDevice, st));
+    CHR_CUDA_TRY(cudaMemsetAsync(pl.cnt, 0, sizeof(McPieceCnt) * pl.npieces, st));
+    const int64_t blocks = std::min<int64_t>(ceil_div(pl.npieces, 8), 148 * 32);
+    k_mc_count<<<(unsigned)blocks, 256, 0, st>>>(d_grids, pl.d_grids, n, pl.npieces, k, T, pl.cnt);
+    k_mc_reduce<<<(unsigned)pl.nchunks, 256, 0, st>>>(pl.cnt, pl.chunk);
+    k_mc_grids<<<1, 1, 0, st>>>(pl.d_grids, n, pl.chunk, pl.totals);
+    k_mc_down<<<(unsigned)pl.nchunks, 256, 0, st>>>(pl.cnt, pl.chunk, pl.base);
+    CHR_CUDA_TRY(cudaGetLastError());
+    CHR_CUDA_TRY(cudaMemcpyAsync(pl.grids.data(), pl.d_grids, sizeof(McGrid) * n, cudaMemcpyDeviceToHost, st));
+    CHR_CUDA_TRY(cudaStreamSynchronize(st));
+    int64_t tt = 0, tv = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        if (h_ntri) h_ntri[i] = pl.grids[i].ntri;
+        if (h_nvert) h_nvert[i] = pl.grids[i].nvert;
+        tt += pl.grids[i].ntri;
+        tv += pl.grids[i].nvert;
+    }
+    if (h_total_tri) *h_total_tri = tt;
+    if (h_total_vert) *h_total_vert = tv;
+    return CHR_OK;
+}
+
+extern "C" int chr_mc_emit(const double *d_grids, const chr_mc_grid_t *h, int64_t n, double k, void *d_ws,
+                           size_t ws_bytes, double *d_verts, int32_t *d_tris, void *stream) {
+    if (n == 0) return CHR_OK;
+    if (!d_grids || !h || n < 0) return CHR_E_PARAMETER;
+    cudaStream_t st = (cudaStream_t)stream;
+    McPlan pl;
+    if (!mc_build(h, n, pl)) return CHR_E_PARAMETER;
+    mc_carve(pl, d_ws, ws_bytes);
+    if (!d_ws || pl.ws > ws_bytes) return CHR_E_WORKSPACE;
+    const McTables *T = mc_tables_device();
+    if (!T) return CHR_E_CUDA;
+    if (pl.nitems > 0)
+        k_mc_emit<<<(unsigned)pl.nitems, MNW * 32, 0, st>>>(d_grids, pl.d_grids, n, k, T, pl.base, d_verts, d_tris);
+    CHR_CUDA_TRY(cudaGetLastError());
+    CHR_CUDA_TRY(cudaStreamSynchronize(st));
+    return CHR_OK;
+}
+
+extern "C" int chr_case_codes(const double *d_grid, int64_t nx, int64_t ny, int64_t nz, double k, int binary,
+                              uint8_t *d_codes, void *stream) {
+    if (!d_grid || !d_codes || nx < 2 || ny < 2 || nz < 2) return CHR_E_PARAMETER;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t n = (nx - 1) * (ny - 1) * (nz - 1);
+    const int64_t blocks = std::min<int64_t>(ceil_div(n, 256), 148 * 32);
+    k_case_codes<<<(unsigned)blocks, 256, 0, st>>>(d_grid, nx, ny, nz, k, binary, d_codes);
+    return cudaGetLastError() == cudaSuccess ? CHR_OK : CHR_E_CUDA;
+}

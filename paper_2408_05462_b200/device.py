@@ -1,0 +1,304 @@
+"""Device-resident CHR pipeline: the hot path as a user of the C-ABI sees it.
+
+Every function takes / returns torch CUDA tensors and calls libchr.so
+(include/chr.h) on the current torch stream.  The reference-shaped API
+(``archive.build_chr`` / ``request`` / ``surface.marching_cubes`` ...) is
+built on these; the benchmark times them directly.
+
+    stats          blocking.decompose + bound distances  (chr_stats)
+    plan           build_index + merge_regions + bounds  (chr_plan)
+    compress       codec.compress per region + write_chr (chr_compress)
+    decode         codec.decompress per selected region  (chr_decode_regions)
+    marching       marching_cubes + merge_meshes         (chr_mc_count/emit)
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _abi
+from ._abi import check, lib, ptr, stream_ptr
+from .exceptions import NonFiniteSampleError, ParameterError
+
+SAFETY_FACTOR = 1.0 - 2.0**-20  # bound.py:38
+LOOSE_FRACTION = 0.01  # bound.py:42
+DTYPE_TAGS = {"f32": 0, "f64": 1}  # volume.py:18
+BLOCK_HEADER = 34  # codec.py:41
+FILE_HEADER = 63  # chr_archive.py:50
+REGION_FIXED = 85  # chr_archive.py:51
+
+
+def _dtype_code(t: torch.Tensor) -> int:
+    if t.dtype == torch.float32:
+        return 0
+    if t.dtype == torch.float64:
+        return 1
+    raise ParameterError(f"volume must be float32 or float64, got {t.dtype}")
+
+
+def _cands_arr(cands) -> np.ndarray:
+    a = np.ascontiguousarray(np.asarray(cands, dtype=np.float64).reshape(-1))
+    if a.size < 1 or a.size > 64:
+        raise ParameterError(f"need 1..64 candidates, got {a.size}")
+    return a
+
+
+def _np_ptr(a: np.ndarray):
+    return ctypes.c_void_p(a.ctypes.data)
+
+
+def num_blocks(dims, bs) -> int:
+    return int(lib().chr_num_blocks(*dims, bs))
+
+
+def stats(vol: torch.Tensor, dims, bs: int, cands) -> tuple[torch.Tensor, torch.Tensor]:
+    """Per-block (vmin, vmax, dmin) f64 [nblocks, 3] + first non-finite index (device)."""
+    cands = _cands_arr(cands)
+    nb = num_blocks(dims, bs)
+    out = torch.empty((nb, 3), dtype=torch.float64, device=vol.device)
+    bad = torch.empty(1, dtype=torch.int64, device=vol.device)
+    check(lib().chr_stats(ptr(vol), _dtype_code(vol), *dims, bs, _np_ptr(cands), cands.size,
+                          ptr(out), ptr(bad), stream_ptr()), "chr_stats")
+    return out, bad
+
+
+def plan(block_stats: np.ndarray, dims, bs, cands, vmin, vmax, loose_fraction=LOOSE_FRACTION,
+         safety_factor=SAFETY_FACTOR):
+    """Regions (ctypes array of chr_region_t) from host block stats."""
+    cands = _cands_arr(cands)
+    bsn = np.ascontiguousarray(block_stats, dtype=np.float64)
+    nb = bsn.shape[0]
+    regs = (_abi.Region * nb)()
+    nreg = ctypes.c_int64(0)
+    check(lib().chr_plan(_np_ptr(bsn), *dims, bs, _np_ptr(cands), cands.size, float(vmin), float(vmax),
+                         float(loose_fraction), float(safety_factor), regs, ctypes.byref(nreg)), "chr_plan")
+    out = (_abi.Region * nreg.value)()
+    ctypes.memmove(out, regs, ctypes.sizeof(_abi.Region) * nreg.value)
+    return out
+
+
+@dataclass
+class Compressed:
+    """Output of :func:`compress`: bytes on the device + the region table."""
+
+    blob: torch.Tensor  # uint8, first `nbytes` valid
+    nbytes: int
+    regions: object  # ctypes array of chr_region_t (codec/offset/crc filled)
+    source_dtype: str
+    extra: dict = field(default_factory=dict)
+
+
+class Workspaces:
+    """Reusable device scratch (grows on demand) so steady-state calls do
+    not hit the caching allocator."""
+
+    def __init__(self):
+        self._bufs: dict[str, torch.Tensor] = {}
+
+    def get(self, name: str, nbytes: int, dtype=torch.uint8) -> torch.Tensor:
+        elem = torch.empty((), dtype=dtype).element_size()
+        n = max(1, -(-int(nbytes) // elem))
+        t = self._bufs.get(name)
+        if t is None or t.numel() < n or t.dtype != dtype or t.device != _abi.device():
+            t = torch.empty(max(n, 64), dtype=dtype, device=_abi.device())
+            self._bufs[name] = t
+        return t
+
+
+_DEFAULT_WS = Workspaces()
+
+
+def compress(vol: torch.Tensor, dims, regions, *, source_dtype="f32", write_file=True, spacing=(1.0, 1.0, 1.0),
+             bs=0, vrange=(0.0, 0.0), cands=(0.0,), ws: Workspaces | None = None,
+             out: torch.Tensor | None = None) -> Compressed:
+    """Run chr_compress on `regions`; returns the device bytes."""
+    ws = ws or _DEFAULT_WS
+    L = lib()
+    nreg = len(regions)
+    cands = _cands_arr(cands)
+    m = cands.size
+    wsz = L.chr_compress_workspace_size(regions, nreg)
+    if wsz == 0:
+        raise ParameterError("invalid regions for compress")
+    work = ws.get("compress", wsz)
+    cap = int(L.chr_compress_capacity(regions, nreg, m, DTYPE_TAGS[source_dtype]))
+    if out is None or out.numel() < cap:
+        out = ws.get("compress_out", cap)
+    nbytes = ctypes.c_uint64(0)
+    sp = (ctypes.c_double * 3)(*[float(s) for s in spacing])
+    check(L.chr_compress(ptr(vol), _dtype_code(vol), DTYPE_TAGS[source_dtype], *dims, sp, int(bs),
+                         float(vrange[0]), float(vrange[1]), _np_ptr(cands), m, regions, nreg,
+                         1 if write_file else 0, ptr(work), work.numel(), ptr(out), out.numel(),
+                         ctypes.byref(nbytes), stream_ptr()), "chr_compress")
+    return Compressed(out, int(nbytes.value), regions, source_dtype)
+
+
+def build_archive(vol: torch.Tensor, dims, cands, bs, *, spacing=(1.0, 1.0, 1.0), source_dtype="f32",
+                  loose_fraction=LOOSE_FRACTION, safety_factor=SAFETY_FACTOR, vrange=None,
+                  out_of_range="error", ws: Workspaces | None = None, on_warn=None) -> Compressed:
+    """stats -> plan -> compress: a complete .chr file on the device
+    (chr_archive.build_chr, strict bound at accuracy 1)."""
+    cands = _cands_arr(cands)
+    if any(b <= a for a, b in zip(cands[:-1], cands[1:])) or not np.isfinite(cands).all():
+        raise ParameterError(f"candidates must be finite and strictly increasing, got {list(cands)}")
+    bst, bad = stats(vol, dims, bs, cands)
+    host = torch.empty(bst.numel() + 1, dtype=torch.float64, pin_memory=True)
+    host[:-1].copy_(bst.reshape(-1), non_blocking=True)
+    host[-1:].copy_(bad.view(torch.float64), non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    hs = host.numpy()
+    badidx = int(hs[-1:].view(np.int64)[0])
+    if badidx >= 0:
+        value = float(vol.reshape(-1)[badidx].item())
+        raise NonFiniteSampleError(badidx, value)
+    bstats = hs[:-1].reshape(-1, 3)
+    if vrange is None:
+        vrange = (float(bstats[:, 0].min()), float(bstats[:, 1].max()))
+    vmin, vmax = vrange
+    outside = [float(k) for k in cands if not vmin <= k <= vmax]
+    if outside:
+        msg = f"candidates outside the volume's value range [{vmin}, {vmax}]: {outside}"
+        if out_of_range == "error":
+            raise ParameterError(msg)
+        if on_warn:
+            on_warn(msg)
+    if not loose_fraction > 0.0:
+        raise ParameterError(f"loose_fraction must be positive, got {loose_fraction}")
+    regions = plan(bstats, dims, bs, cands, vmin, vmax, loose_fraction, safety_factor)
+    res = compress(vol, dims, regions, source_dtype=source_dtype, write_file=True, spacing=spacing, bs=bs,
+                   vrange=(vmin, vmax), cands=cands, ws=ws)
+    res.extra.update(block_stats=bstats, vrange=(vmin, vmax), cands=tuple(float(k) for k in cands))
+    return res
+
+
+def decode(blob: torch.Tensor, sel, ws: Workspaces | None = None, out: torch.Tensor | None = None):
+    """Decode CompressedBlocks of `blob` (device uint8).
+
+    ``sel``: list of (payload_offset, payload_nbytes, codec_id, (ex,ey,ez), e, crc).
+    Returns (f64 device tensor of all windows concatenated, element offsets,
+    per-region status codes)."""
+    ws = ws or _DEFAULT_WS
+    L = lib()
+    n = len(sel)
+    regs = (_abi.DecRegion * max(n, 1))()
+    offs = []
+    total = 0
+    for i, (po, pn, cid, dims, e, crc) in enumerate(sel):
+        r = regs[i]
+        r.payload_offset = int(po)
+        r.payload_nbytes = int(pn)
+        r.codec_id = int(cid)
+        r.dims[0], r.dims[1], r.dims[2] = (int(d) for d in dims)
+        r.error_bound = float(e)
+        r.crc = int(crc) & 0xFFFFFFFF
+        r.out_offset = total
+        offs.append(total)
+        total += int(dims[0]) * int(dims[1]) * int(dims[2])
+    if out is None or out.numel() < total:
+        out = ws.get("decode_out", 8 * max(total, 1), torch.float64)
+    status = (ctypes.c_int32 * max(n, 1))()
+    if n:
+        wsz = L.chr_decode_workspace_size(regs, n)
+        work = ws.get("decode", wsz)
+        rc = L.chr_decode_regions(ptr(blob), regs, n, ptr(out), ptr(work), work.numel(), status, stream_ptr())
+        if rc not in (_abi.CHR_OK, _abi.CHR_E_CORRUPT, _abi.CHR_E_UNSUPPORTED_CODEC):
+            check(rc, "chr_decode_regions")
+    return out, offs, [int(status[i]) for i in range(n)]
+
+
+def marching(grids: torch.Tensor, descs, k: float, ws: Workspaces | None = None):
+    """Marching cubes over several f64 windows of `grids`, merged.
+
+    ``descs``: list of (element_offset, (nx,ny,nz), origin3, spacing3).
+    Returns (verts f64 [nv,3], tris int32 [nt,3], ntri per grid, nvert per grid)."""
+    ws = ws or _DEFAULT_WS
+    L = lib()
+    n = len(descs)
+    dev = _abi.device()
+    if n == 0:
+        return (torch.empty((0, 3), dtype=torch.float64, device=dev),
+                torch.empty((0, 3), dtype=torch.int32, device=dev), [], [])
+    gd = (_abi.McGrid * n)()
+    for i, (off, dims, origin, spacing) in enumerate(descs):
+        g = gd[i]
+        g.grid_offset = int(off)
+        g.dims[0], g.dims[1], g.dims[2] = (int(d) for d in dims)
+        for a in range(3):
+            g.origin[a] = float(origin[a])
+            g.spacing[a] = float(spacing[a])
+    wsz = L.chr_mc_workspace_size(gd, n)
+    work = ws.get("mc", wsz)
+    ntri = (ctypes.c_int64 * n)()
+    nvert = (ctypes.c_int64 * n)()
+    tt = ctypes.c_int64(0)
+    tv = ctypes.c_int64(0)
+    check(L.chr_mc_count(ptr(grids), gd, n, float(k), ptr(work), work.numel(), ntri, nvert, ctypes.byref(tt),
+                         ctypes.byref(tv), stream_ptr()), "chr_mc_count")
+    verts = torch.empty((tv.value, 3), dtype=torch.float64, device=dev)
+    tris = torch.empty((tt.value, 3), dtype=torch.int32, device=dev)
+    check(L.chr_mc_emit(ptr(grids), gd, n, float(k), ptr(work), work.numel(), ptr(verts), ptr(tris),
+                        stream_ptr()), "chr_mc_emit")
+    return verts, tris, list(ntri), list(nvert)
+
+
+def case_codes(grid: torch.Tensor, dims, k: float, binary: bool = True) -> torch.Tensor:
+    nx, ny, nz = dims
+    codes = torch.empty((nx - 1) * (ny - 1) * (nz - 1), dtype=torch.uint8, device=grid.device)
+    check(lib().chr_case_codes(ptr(grid), nx, ny, nz, float(k), 1 if binary else 0, ptr(codes), stream_ptr()),
+          "chr_case_codes")
+    return codes
+
+
+def crc32(buf: torch.Tensor, nbytes: int | None = None) -> int:
+    n = buf.numel() if nbytes is None else int(nbytes)
+    L = lib()
+    work = _DEFAULT_WS.get("crc", L.chr_crc32_workspace_size(n))
+    out = ctypes.c_uint32(0)
+    check(L.chr_crc32(ptr(buf), n, ptr(work), work.numel(), ctypes.byref(out), stream_ptr()), "chr_crc32")
+    return int(out.value)
+
+
+def min_abs_distance(flat: torch.Tensor, k: float) -> float:
+    L = lib()
+    work = _DEFAULT_WS.get("minabs", 256)
+    out = ctypes.c_double(0.0)
+    check(L.chr_min_abs_distance(ptr(flat), flat.numel(), float(k), ctypes.byref(out), ptr(work), work.numel(),
+                                 stream_ptr()), "chr_min_abs_distance")
+    return float(out.value)
+
+
+def lorenzo_encode(flat: torch.Tensor, nx, ny, nz, e):
+    q = torch.empty(nx * ny * nz, dtype=torch.int64, device=flat.device)
+    esc = torch.empty(nx * ny * nz, dtype=torch.uint8, device=flat.device)
+    check(lib().chr_lorenzo_encode(ptr(flat), nx, ny, nz, float(e), ptr(q), ptr(esc), stream_ptr()),
+          "chr_lorenzo_encode")
+    return q, esc
+
+
+def region_records(regions) -> list[dict]:
+    """Plain-Python view of a chr_region_t array."""
+    out = []
+    for i in range(len(regions)):
+        r = regions[i]
+        out.append(dict(
+            id=i, lo=tuple(r.lo), hi=tuple(r.hi), origin=tuple(r.origin), extent=tuple(r.extent),
+            mask=int(r.mask), e=float(r.error_bound), codec=int(r.codec_id), crc=int(r.payload_crc),
+            block_offset=int(r.block_offset), block_nbytes=int(r.block_nbytes), nesc=int(r.n_escaped),
+        ))
+    return out
+
+
+def header_table_nbytes(m: int, nreg: int) -> int:
+    return FILE_HEADER + 4 + 8 * m + 4 + nreg * (REGION_FIXED + (m + 7) // 8)
+
+
+def ceil_div(a, b):
+    return -(-a // b)
+
+
+__all__ = [n for n in dir() if not n.startswith("_") and n not in ("annotations", "ctypes", "math")]

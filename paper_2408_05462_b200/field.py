@@ -1,0 +1,147 @@
+"""Scalar-field container with the reference Volume's interface
+(isochr/volume.py:35-123), able to hold its samples on the GPU.
+
+``values`` (host, read-only f64, x fastest) is what reference code reads;
+``device_values()`` is what the CUDA path reads: f32 when the field is
+f32-sourced and f32-exact (half the HBM traffic), else f64.  A Volume built
+from a CUDA tensor keeps it resident and only copies to the host if
+``values`` is touched.
+"""
+
+from __future__ import annotations
+
+from pathlib import Path
+
+import numpy as np
+import torch
+
+from .exceptions import NonFiniteSampleError, ParameterError, RawSizeMismatchError
+
+DTYPE_TAGS = {"f32": 0, "f64": 1}
+DTYPE_WIDTHS = {"f32": 4, "f64": 8}
+_RAW = {("f32", "little"): "<f4", ("f32", "big"): ">f4", ("f64", "little"): "<f8", ("f64", "big"): ">f8"}
+
+
+def _dims3(dims):
+    if len(dims) != 3 or any(int(d) != d or d < 1 for d in dims):
+        raise ParameterError(f"dims must be three positive integers, got {dims!r}")
+    return tuple(int(d) for d in dims)
+
+
+class Volume:
+    """Immutable 3D scalar field (dims, spacing, values, value_range, source_dtype)."""
+
+    __slots__ = ("dims", "spacing", "source_dtype", "_host", "_dev", "_range")
+
+    def __init__(self, dims, spacing=(1.0, 1.0, 1.0), values=None, source_dtype: str = "f64"):
+        dims = _dims3(dims)
+        sp = tuple(float(s) for s in spacing)
+        if len(sp) != 3 or any(s <= 0 for s in sp):
+            raise ParameterError(f"spacing must be three positive reals, got {spacing!r}")
+        if source_dtype not in DTYPE_TAGS:
+            raise ParameterError(f"unknown dtype tag {source_dtype!r}")
+        n = dims[0] * dims[1] * dims[2]
+        object.__setattr__(self, "dims", dims)
+        object.__setattr__(self, "spacing", sp)
+        object.__setattr__(self, "source_dtype", source_dtype)
+        object.__setattr__(self, "_dev", None)
+        object.__setattr__(self, "_range", None)
+        if isinstance(values, torch.Tensor):
+            t = values.reshape(-1)
+            if t.numel() != n:
+                raise ParameterError(f"values has {t.numel()} samples, dims {dims} require {n}")
+            if t.dtype not in (torch.float32, torch.float64):
+                t = t.to(torch.float64)
+            if not t.is_cuda:
+                t = t.cuda()
+            object.__setattr__(self, "_host", None)
+            object.__setattr__(self, "_dev", t.contiguous())
+        else:
+            a = np.asarray(values, dtype=np.float64).reshape(-1)
+            if a.size != n:
+                raise ParameterError(f"values has {a.size} samples, dims {dims} require {n}")
+            fin = np.isfinite(a)
+            if not fin.all():
+                i = int(np.argmin(fin))
+                raise NonFiniteSampleError(i, float(a[i]))
+            a = a.copy()
+            a.setflags(write=False)
+            object.__setattr__(self, "_host", a)
+            object.__setattr__(self, "_range", (float(a.min()), float(a.max())))
+
+    def __setattr__(self, name, value):
+        raise AttributeError("Volume is immutable")
+
+    # ---- reference-visible attributes
+    @property
+    def values(self) -> np.ndarray:
+        if self._host is None:
+            a = self._dev.to(torch.float64).cpu().numpy()
+            a.setflags(write=False)
+            object.__setattr__(self, "_host", a)
+        return self._host
+
+    @property
+    def value_range(self) -> tuple[float, float]:
+        if self._range is None:
+            t = self._dev
+            fin = torch.isfinite(t)
+            if not bool(fin.all()):
+                i = int(torch.argmin(fin.to(torch.uint8)))
+                raise NonFiniteSampleError(i, float(t[i]))
+            lo, hi = torch.aminmax(t)
+            object.__setattr__(self, "_range", (float(lo), float(hi)))
+        return self._range
+
+    @property
+    def nsamples(self) -> int:
+        return self.dims[0] * self.dims[1] * self.dims[2]
+
+    @property
+    def grid(self) -> np.ndarray:
+        return self.values.reshape(self.dims, order="F")
+
+    @property
+    def nbytes_original(self) -> int:
+        return self.nsamples * DTYPE_WIDTHS[self.source_dtype]
+
+    # ---- device side
+    def device_values(self) -> torch.Tensor:
+        """Samples on the GPU, x fastest (f32 when f32-sourced and exact)."""
+        if self._dev is None:
+            a = self._host
+            if self.source_dtype == "f32":
+                narrow = a.astype(np.float32)
+                if np.array_equal(narrow.astype(np.float64), a):
+                    a = narrow
+            object.__setattr__(self, "_dev", torch.from_numpy(np.ascontiguousarray(a)).cuda())
+        return self._dev
+
+    def __repr__(self):
+        return f"Volume(dims={self.dims}, spacing={self.spacing}, source_dtype={self.source_dtype!r})"
+
+
+def as_volume_like(volume):
+    """Accept our Volume or any object with the reference Volume's attributes."""
+    if isinstance(volume, Volume):
+        return volume
+    return Volume(volume.dims, volume.spacing, np.asarray(volume.values), volume.source_dtype)
+
+
+def load_raw(path, dims, dtype: str = "f32", endianness: str = "little") -> Volume:
+    """Headerless raw volume, x fastest (volume.py:96-112)."""
+    dims = _dims3(dims)
+    if (dtype, endianness) not in _RAW:
+        raise ParameterError(f"unsupported dtype/endianness: {dtype}/{endianness}")
+    path = Path(path)
+    want = dims[0] * dims[1] * dims[2] * DTYPE_WIDTHS[dtype]
+    have = path.stat().st_size
+    if have != want:
+        raise RawSizeMismatchError(path, want, have)
+    return Volume(dims, values=np.fromfile(path, dtype=np.dtype(_RAW[(dtype, endianness)])), source_dtype=dtype)
+
+
+def save_raw(volume: Volume, path, dtype: str = "f32", endianness: str = "little") -> None:
+    if (dtype, endianness) not in _RAW:
+        raise ParameterError(f"unsupported dtype/endianness: {dtype}/{endianness}")
+    volume.values.astype(np.dtype(_RAW[(dtype, endianness)])).tofile(path)

@@ -1,0 +1,259 @@
+"""Parity of the CUDA path (libchr.so through the C-ABI) with the oracle and
+the reference's golden vectors.  Bit-exact for bytes / integers / case codes /
+triangle indices; vertices and reconstructions are bit-exact too (the kernels
+do the reference's f64 operations without FMA), which is stricter than the
+north_star tolerances (1 ulp recon, 1e-5 * spacing vertices)."""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - CPU container
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2408_05462_b200 as G  # noqa: E402
+from oracle import oracle as O  # noqa: E402
+from paper_2408_05462_b200 import device, exceptions, synth  # noqa: E402
+from paper_2408_05462_b200.blockcodec import CompressedBlock  # noqa: E402
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+# ----------------------------------------------------------------- blocks
+def test_codec_md_worked_example(golden):
+    g = golden["codec_example_in"].reshape((2, 2, 2), order="F")
+    blk = G.compress(g, 0.25)
+    assert blk.to_bytes() == golden["codec_example_block"].tobytes()
+    assert blk.payload == bytes.fromhex("0500050908") and blk.checksum == 0xD71089FD
+    assert np.array_equal(G.decompress(blk).ravel(order="F"), [1, 1, 1, 1, 1, 1, 3, 1])
+
+
+def test_random_blocks_bit_exact(golden, golden_meta):
+    for name, shape, e in golden_meta["rand_cases"]:
+        g = golden[name + "_in"].reshape(shape, order="F")
+        blk = G.compress(g, e)
+        assert blk.to_bytes() == golden[name + "_block"].tobytes(), name
+        out = G.decompress(CompressedBlock.from_bytes(golden[name + "_block"].tobytes()))
+        assert np.array_equal(out.ravel(order="F"), golden[name + "_out"]), name
+
+
+def test_verbatim_blocks(golden):
+    g = golden["incompressible_in"].reshape((8, 8, 8), order="F")
+    blk = G.compress(g, 1e-12)
+    assert blk.codec_id == 0 and blk.to_bytes() == golden["incompressible_block"].tobytes()
+    assert np.array_equal(G.decompress(blk), g)
+    g32 = golden["f32src_in"].reshape((5, 4, 3), order="F")
+    for tag, e in (("e0", 0.0), ("tiny", 1e-15), ("1e-2", 1e-2)):
+        blk = G.compress(g32, e, source_dtype="f32")
+        assert blk.to_bytes() == golden[f"f32src_block_{tag}"].tobytes(), tag
+
+
+def test_lorenzo_seam_matches_reference(golden, golden_meta):
+    for name, shape, e in golden_meta["rand_cases"]:
+        flat = torch.from_numpy(golden[name + "_in"]).cuda()
+        q, esc = device.lorenzo_encode(flat, *shape, e)
+        assert np.array_equal(q.cpu().numpy(), golden[name + "_q"]), name
+        assert np.array_equal(esc.cpu().numpy().astype(bool), golden[name + "_esc"]), name
+    for e in (0.25, 0.001):
+        q, esc = device.lorenzo_encode(torch.from_numpy(golden["tie_in"]).cuda(), 4, 2, 2, e)
+        assert np.array_equal(q.cpu().numpy(), golden[f"tie_e{e}_q"])
+
+
+def test_corrupt_and_unknown_codec():
+    g = np.random.default_rng(1).normal(size=(9, 8, 7))
+    blk = G.compress(g, 1e-3)
+    for pos in (0, len(blk.payload) // 2, len(blk.payload) - 1):
+        bad = bytearray(blk.payload)
+        bad[pos] ^= 0x41
+        with pytest.raises(exceptions.CorruptPayloadError):
+            G.decompress(CompressedBlock(blk.codec_id, blk.dims, blk.error_bound, blk.source_dtype, bytes(bad),
+                                         blk.checksum))
+    with pytest.raises(exceptions.UnsupportedCodecError):
+        G.decompress(CompressedBlock(77, blk.dims, blk.error_bound, blk.source_dtype, blk.payload, blk.checksum))
+
+
+def test_crc_valid_malformed_streams(golden_meta):
+    import zlib
+
+    for hexbuf, n, msg in golden_meta["tok_errors"]:
+        payload = bytes.fromhex(hexbuf)
+        blk = CompressedBlock(1, (n, 1, 1), 0.5, "f64", payload, zlib.crc32(payload))
+        with pytest.raises(exceptions.CorruptPayloadError):
+            G.decompress(blk)
+
+
+def test_token_stream_edge_runs(golden):
+    # long runs (multi-byte run lengths) and extreme quanta through a full
+    # compress/decompress: a field whose quanta are exactly tok_vals
+    vals = golden["tok_vals"]
+    n = vals.size
+    q = vals.astype(np.int64)
+    u = np.cumsum(q)  # 1D: x-only Lorenzo
+    e = 0.5
+    g = (u.astype(np.float64) * (2 * e)).reshape((n, 1, 1), order="F")
+    if np.abs(u).max() <= 2**27:
+        blk = G.compress(g, e)
+        ref_cid, ref_payload = O.compress_flat(g.ravel(order="F"), (n, 1, 1), e, "f64")
+        assert blk.payload == ref_payload and blk.codec_id == ref_cid
+        assert np.array_equal(G.decompress(blk).ravel(order="F"), O.decompress_block(blk.to_bytes())[1])
+
+
+# ----------------------------------------------------------------- MC
+def test_mc_all_256_cases(golden):
+    corners = [(0, 0, 0), (1, 0, 0), (1, 1, 0), (0, 1, 0), (0, 0, 1), (1, 0, 1), (1, 1, 1), (0, 1, 1)]
+    for code in range(256):
+        g = np.zeros((2, 2, 2))
+        for i, (ox, oy, oz) in enumerate(corners):
+            g[ox, oy, oz] = 1.0 if (code >> i) & 1 else 0.0
+        m = G.marching_cubes(g, k=0.5)
+        assert np.array_equal(m.vertices, golden[f"mc256_{code}_v"]), code
+        assert np.array_equal(m.triangles, golden[f"mc256_{code}_t"]), code
+
+
+def test_mc_random_grids(golden):
+    for seed in range(5):
+        g = golden[f"mcrand{seed}_in"].reshape((8, 7, 9), order="F")
+        m = G.marching_cubes(g, spacing=(1.0, 2.0, 0.5), origin=(3.0, -1.0, 2.5), k=0.1)
+        assert np.array_equal(m.vertices, golden[f"mcrand{seed}_v"])
+        assert np.array_equal(m.triangles, golden[f"mcrand{seed}_t"])
+        assert np.array_equal(G.case_field(g, 0.1).codes, golden[f"mcrand{seed}_case"])
+    g = golden["mcsmooth_in"].reshape((12, 11, 13), order="F")
+    m = G.marching_cubes(g, k=0.0)
+    assert np.array_equal(m.vertices, golden["mcsmooth_v"]) and np.array_equal(m.triangles, golden["mcsmooth_t"])
+
+
+@pytest.mark.parametrize("shape", [(70, 9, 5), (5, 70, 9), (9, 5, 70), (130, 17, 19), (2, 2, 2), (66, 2, 3)])
+def test_mc_shapes_vs_oracle(shape):
+    g = np.random.default_rng(sum(shape)).normal(size=shape)
+    m = G.marching_cubes(g, k=0.05)
+    v, t = O.marching_cubes(g.ravel(order="F"), shape, 0.05)
+    assert np.array_equal(m.vertices, v) and np.array_equal(m.triangles, t)
+
+
+# ----------------------------------------------------------------- archives
+@pytest.mark.parametrize("name", ["c1", "sphere", "smooth", "exactk", "oor"])
+def test_golden_archives(golden, golden_meta, name, tmp_path):
+    import warnings
+
+    info = golden_meta["archive_" + name]
+    vals = golden[name + "_in"]
+    vol = G.Volume(tuple(info["dims"]), tuple(info["spacing"]), vals.astype(np.float64), info["dtype"])
+    kw = dict(info["kw"])
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        arch = G.build_chr(vol, info["cands"], info["bs"], **kw)
+    p = tmp_path / "a.chr"
+    G.write_chr(arch, p)
+    assert p.read_bytes() == golden[name + "_chr"].tobytes()
+    back = G.read_chr(p)
+    assert back == arch
+    for k in arch.candidates:
+        ref = info["requests"][repr(k)]
+        rs = G.request(arch, k)
+        assert [r.region_id for r, _ in rs.regions] == ref["regions"]
+        assert [sha(np.asarray(w).ravel(order="F")) for _, w in rs.regions] == ref["recon_sha"]
+        assert rs.report.bytes_touched == ref["bytes_touched"]
+        # the same request decoded from the re-read (host) archive
+        rs2 = G.request(back, k)
+        assert all(np.array_equal(a, b) for (_, a), (_, b) in zip(rs.regions, rs2.regions))
+        regs, wins, offs, _, _ = G.request_device(arch, k)
+        v, t, nt, nv = G.extract_device(wins, regs, vol.spacing, k) if regs else (None, None, [], [])
+        if regs:
+            assert sha(v.cpu().numpy()) == ref["merged_v_sha"] and sha(t.cpu().numpy()) == ref["merged_t_sha"]
+            assert nt == ref["ntri"] and nv == ref["nvert"]
+
+
+def _config_parity(name, n, quantile=None, r=None):
+    vals, dims, bs, cands, rr = synth.make_config(name, device="cuda", n=n, quantile=quantile, r=r)
+    host = vals.cpu().numpy()
+    res = device.build_archive(vals, dims, cands, bs, loose_fraction=rr)
+    got = res.blob[: res.nbytes].cpu().numpy().tobytes()
+    ref = O.build_chr(host.astype(np.float64), dims, cands, bs, source_dtype="f32", loose_fraction=rr, workers=8)
+    want = ref.to_bytes()
+    assert len(got) == len(want)
+    assert got == want
+    return res, ref, dims, cands
+
+
+@pytest.mark.parametrize("name,n", [("c1", 64), ("c2", 96), ("c3", 96), ("c4", 80), ("c5", 72)])
+def test_config_recipes_archive_request_mc(name, n):
+    res, ref, dims, cands = _config_parity(name, n)
+    blob = ref.to_bytes()
+    for k in cands[:3]:
+        sel = O.request(ref, k)
+        if not sel:
+            continue
+        desc = []
+        table = _block_offsets(ref)
+        for r, _ in sel:
+            o = table[r["id"]]
+            cid, ex, ey, ez, e, _, plen, crc = O.HEADER_STRUCT.unpack_from(blob, o)
+            desc.append((o + 34, plen, cid, (ex, ey, ez), e, crc))
+        wins, offs, status = device.decode(res.blob, desc)
+        assert not any(status)
+        host = wins.cpu().numpy()
+        for (r, w), o in zip(sel, offs):
+            assert np.array_equal(host[o:o + w.size], w)
+        v, t, nt, nv = device.marching(wins, [(o, r["extent"], tuple(float(a) for a in r["origin"]), (1.0, 1.0, 1.0))
+                                              for (r, _), o in zip(sel, offs)], k)
+        rv, rt = O.extract_regions(sel, (1.0, 1.0, 1.0), k)
+        assert np.array_equal(v.cpu().numpy(), rv) and np.array_equal(t.cpu().numpy(), rt)
+
+
+def _block_offsets(ref):
+    off = ref.header_table_nbytes()
+    out = []
+    for r in ref.regions:
+        out.append(off)
+        off += len(r["block"])
+    return out
+
+
+def test_stats_kernel_vs_oracle():
+    vals, dims, bs, cands, _ = synth.make_config("c5", device="cuda", n=70)
+    st, bad = device.stats(vals, dims, bs, cands)
+    assert int(bad.item()) == -1
+    st = st.cpu().numpy()
+    host = vals.cpu().numpy().astype(np.float64)
+    vmin, vmax = O.block_stats(host, dims, bs)
+    assert np.array_equal(st[:, 0], vmin) and np.array_equal(st[:, 1], vmax)
+    nbx, nby, nbz = O.block_grid_shape(dims, bs)
+    L = O.lib()
+    import ctypes
+
+    for b in range(0, nbx * nby * nbz, 7):
+        bz, rem = divmod(b, nbx * nby)
+        by, bx = divmod(rem, nbx)
+        w = [O._axis_window(c, bs, n) for c, n in zip((bx, by, bz), dims)]
+        d = min(L.or_window_min_abs_distance(ctypes.c_void_p(host.ctypes.data), dims[0], dims[1], w[0][0], w[1][0],
+                                             w[2][0], w[0][1], w[1][1], w[2][1], k) for k in cands)
+        assert st[b, 2] == d
+
+
+def test_nonfinite_detected():
+    vals, dims, bs, cands, _ = synth.make_config("c1", device="cuda", n=32)
+    vals = vals.clone()
+    vals[12345] = float("nan")
+    vals[20000] = float("inf")
+    with pytest.raises(exceptions.NonFiniteSampleError) as ei:
+        device.build_archive(vals, dims, cands, bs)
+    assert ei.value.index == 12345
+
+
+def test_crc_kernel_matches_zlib():
+    import zlib
+
+    rng = np.random.default_rng(3)
+    for n in (1, 3, 4, 5, 1000, 65537, 3 * 2**20 + 7):
+        a = rng.integers(0, 256, size=n, dtype=np.uint8)
+        t = torch.from_numpy(a).cuda()
+        assert device.crc32(t) == zlib.crc32(a.tobytes()), n
+        if n > 8:
+            assert device.crc32(t[3:], n - 3) == zlib.crc32(a[3:].tobytes())
