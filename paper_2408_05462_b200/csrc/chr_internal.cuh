@@ -14,6 +14,13 @@ struct CrcSeg {
     int64_t n_sc;         // superchunks
 };
 
+// superchunks needed for bytes [a, b) whatever the buffer's alignment
+// (one spare word covers the alignment slack; empty superchunks add 0)
+CHR_HD int64_t crc_num_superchunks(uint64_t a, uint64_t b) {
+    const uint64_t Wmax = b > a ? (b - a) / 4 + 1 : 0;
+    return Wmax ? (int64_t)((Wmax + kCrcScWords - 1) / kCrcScWords) : 1;
+}
+
 int64_t crc_plan_segments(CrcSeg *segs, int64_t nseg);
 int crc_launch(const uint8_t *d_buf, const CrcSeg *d_segs, int64_t nseg, int64_t total_sc,
                uint32_t *d_seg_raw, cudaStream_t st);

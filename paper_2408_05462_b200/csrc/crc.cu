@@ -108,7 +108,9 @@ __global__ void __launch_bounds__(256) k_crc_segments(const uint8_t *__restrict_
         }
         const CrcSeg S = segs[lo];
         const uint64_t a = S.begin, b = S.end;
-        const uint64_t a4 = (a + 3) & ~3ull, b4 = b & ~3ull;
+        // word alignment on ABSOLUTE addresses (the buffer may be unaligned)
+        const uint64_t base = (uint64_t)(uintptr_t)buf;
+        const uint64_t a4 = ((base + a + 3) & ~3ull) - base, b4 = ((base + b) & ~3ull) - base;
         const int64_t isc = sc - S.sc_base;
         uint32_t contrib = 0;
         if (a4 < b4) {
@@ -146,10 +148,8 @@ __global__ void __launch_bounds__(256) k_crc_segments(const uint8_t *__restrict_
 int64_t crc_plan_segments(CrcSeg *segs, int64_t nseg) {
     int64_t base = 0;
     for (int64_t s = 0; s < nseg; ++s) {
-        const uint64_t a4 = (segs[s].begin + 3) & ~3ull, b4 = segs[s].end & ~3ull;
-        const uint64_t W = a4 < b4 ? (b4 - a4) >> 2 : 0;
         segs[s].sc_base = base;
-        segs[s].n_sc = W ? (int64_t)((W + kCrcScWords - 1) / kCrcScWords) : 1;
+        segs[s].n_sc = crc_num_superchunks(segs[s].begin, segs[s].end);
         base += segs[s].n_sc;
     }
     return base;

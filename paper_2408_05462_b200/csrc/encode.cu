@@ -427,11 +427,7 @@ __global__ void __launch_bounds__(1024) k_layout(const EncParams *__restrict__ P
         carry[1] = 0;
     }
     __syncthreads();
-    auto nsc_of = [](uint64_t a, uint64_t b) -> int64_t {
-        const uint64_t a4 = (a + 3) & ~3ull, b4 = b & ~3ull;
-        const uint64_t W = a4 < b4 ? (b4 - a4) >> 2 : 0;
-        return W ? (int64_t)((W + kCrcScWords - 1) / kCrcScWords) : 1;
-    };
+    auto nsc_of = [](uint64_t a, uint64_t b) -> int64_t { return crc_num_superchunks(a, b); };
     int64_t sc_head = 0;
     if (P->write_file) sc_head = nsc_of(0, H);
     for (int64_t t0 = 0; t0 < nreg; t0 += 1024) {

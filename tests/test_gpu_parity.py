@@ -164,7 +164,7 @@ def test_golden_archives(golden, golden_meta, name, tmp_path):
         rs2 = G.request(back, k)
         assert all(np.array_equal(a, b) for (_, a), (_, b) in zip(rs.regions, rs2.regions))
         regs, wins, offs, _, _ = G.request_device(arch, k)
-        v, t, nt, nv = G.extract_device(wins, regs, vol.spacing, k) if regs else (None, None, [], [])
+        v, t, nt, nv = G.extract_device(wins, regs, offs, vol.spacing, k) if regs else (None, None, [], [])
         if regs:
             assert sha(v.cpu().numpy()) == ref["merged_v_sha"] and sha(t.cpu().numpy()) == ref["merged_t_sha"]
             assert nt == ref["ntri"] and nv == ref["nvert"]
