@@ -1,0 +1,382 @@
+#!/usr/bin/env python
+"""Benchmark of the CHR hot path on B200 (BASELINE.json metric).
+
+One STEP = the whole north_star path over one synthetic volume:
+    compress  (stats -> plan -> quantise/Lorenzo/tokens -> .chr file, on device)
+ -> request   (selective decode of the regions relevant to k)
+ -> extract   (marching cubes of the selected windows, merged mesh)
+Workload at N=1: BASELINE config c3 (512^3 f32 lognormal exp(1.5 g),
+P(k)~k^-3, bs32, r=1e-3, k = 99th percentile), the config the north_star
+target is stated on.  value = 4*N / t_step (GB/s of f32 input through the
+whole path), inputs resident in HBM; `e2e` is the same metric with the
+input host->device copy and the archive + mesh device->host copies inside
+the timed region.  Stage throughputs follow SURVEY §8(d).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+Under torchrun (N>1) every rank processes its own 512^3 volume (weak
+scaling: independent objects) and the ranks all-gather per-rank archive
+bytes / triangle / vertex counts (NCCL) to place their outputs.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "CHR compress/decompress GB/s + isosurface cells/s, % of HBM roofline, 1–8 GPU"
+FALLBACK_HBM = 6650.0
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[3:7]) if v.strip().lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def make_input(cfg, n, rank, device):
+    from paper_2408_05462_b200 import synth
+
+    vals, dims, bs, cands, r = synth.make_config(cfg, device=device, n=n, seed=rank)
+    return vals, dims, bs, cands, r
+
+
+def sel_desc(res, ci):
+    from paper_2408_05462_b200 import device as D
+
+    recs = D.region_records(res.regions)
+    sel = [q for q in recs if (q["mask"] >> ci) & 1]
+    desc = [(q["block_offset"] + D.BLOCK_HEADER, q["block_nbytes"] - D.BLOCK_HEADER, q["codec"], q["extent"], q["e"],
+             q["crc"]) for q in sel]
+    return sel, desc
+
+
+def run_step(vol, dims, bs, cands, r, ws, spacing=(1.0, 1.0, 1.0), stage_events=None):
+    """compress -> request -> extract, all device resident; returns sizes."""
+    from paper_2408_05462_b200 import device as D
+
+    ev = stage_events
+    if ev:
+        ev[0].record()
+    res = D.build_archive(vol, dims, cands, bs, loose_fraction=r, ws=ws)
+    if ev:
+        ev[1].record()
+    sel, desc = sel_desc(res, 0)
+    wins, offs, status = D.decode(res.blob, desc, ws=ws)
+    assert not any(status), status
+    if ev:
+        ev[2].record()
+    grids = [(o, q["extent"], tuple(float(a) * s for a, s in zip(q["origin"], spacing)), spacing)
+             for q, o in zip(sel, offs)]
+    verts, tris, nt, nv = D.marching(wins, grids, cands[0], ws=ws)
+    if ev:
+        ev[3].record()
+    n_sel = sum(q["extent"][0] * q["extent"][1] * q["extent"][2] for q in sel)
+    cells = sum((q["extent"][0] - 1) * (q["extent"][1] - 1) * (q["extent"][2] - 1) for q in sel)
+    c_sel = sum(q["block_nbytes"] for q in sel)
+    return dict(res=res, wins=wins, verts=verts, tris=tris, n_sel=n_sel, cells=cells, c_sel=c_sel,
+                archive=res.nbytes, nreg=len(res.regions), nsel=len(sel), ntri=int(tris.shape[0]),
+                nvert=int(verts.shape[0]), payload=sum(q["block_nbytes"] for q in D.region_records(res.regions)))
+
+
+def kernel_bytes(name, info, N):
+    """Algorithmic bytes per launch of the main kernels."""
+    c_all = info["payload"]
+    table = {
+        "k_stats<float>": 4 * N,
+        "k_tile<float, false>": 4 * N,
+        "k_tile<float, true>": 4 * N + c_all,
+        "k_crc_segments": None,
+        "k_tok_count": info["c_sel"],
+        "k_locate": info["c_sel"],
+        "k_lorenzo": info["c_sel"] + 8 * info["n_sel"],
+        "k_mc_count": 8 * info["n_sel"],
+        "k_mc_emit": 8 * info["n_sel"] + 24 * info["nvert"] + 12 * info["ntri"],
+    }
+    return table.get(name)
+
+
+def cpu_baseline(vals_host, dims, bs, cands, r, planes, workers):
+    """The oracle port timed on host cores on a bounded z-slab sample."""
+    from oracle import oracle as O
+
+    nx, ny, nz = dims
+    pz = min(planes, nz)
+    sample = np.ascontiguousarray(vals_host[: nx * ny * pz]).astype(np.float64)
+    sdims = (nx, ny, pz)
+    lo, hi = float(sample.min()), float(sample.max())
+    k = float(min(max(cands[0], lo), hi))
+    t0 = time.perf_counter()
+    arch = O.build_chr(sample, sdims, [k], bs, source_dtype="f32", loose_fraction=r, workers=workers,
+                       out_of_range="warn")
+    sel = O.request(arch, k, workers=workers)
+    O.extract_regions(sel, (1.0, 1.0, 1.0), k)
+    t = time.perf_counter() - t0
+    return {"value": 4 * nx * ny * pz / t / 1e9, "unit": "GB/s", "cores": workers, "kind": "port",
+            "sample": f"{nx}x{ny}x{pz} z-slab of the same field (first {pz} planes), same bs/r/k; "
+                      f"build_chr + request + per-region MC, {t:.2f} s"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c3")
+    ap.add_argument("--n", type=int, default=None)
+    ap.add_argument("--cpu-planes", type=int, default=32)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    else:
+        torch.cuda.set_device(0)
+
+    from paper_2408_05462_b200 import _abi, synth
+    from paper_2408_05462_b200 import device as D
+
+    n = args.n or synth.CONFIGS[args.config]["n"]
+    workers = len(os.sched_getaffinity(0))
+
+    if args.impl == "reference":
+        # the reference's CPU path (oracle port of isochr) on host cores
+        if rank != 0:
+            if dist:
+                dist.barrier()
+            return
+        vals, dims, bs, cands, r = make_input(args.config, n, rank, "cuda")
+        host = vals.cpu().numpy()
+        del vals
+        times = []
+        for i in range(args.warmup + args.steps):
+            cb = cpu_baseline(host, dims, bs, cands, r, args.cpu_planes, workers)
+            if i >= args.warmup:
+                times.append(cb)
+        v = statistics.median([t["value"] for t in times])
+        line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": 4 * dims[0] * dims[1] * min(args.cpu_planes, dims[2]) / v / 1e6,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic", "config": {"workload": f"{args.config} {n}^3 bounded z-slab sample"},
+                "cpu_baseline": dict(times[-1], value=v),
+                "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        if dist:
+            dist.barrier()
+        return
+
+    vals, dims, bs, cands, r = make_input(args.config, n, rank, "cuda")
+    N = dims[0] * dims[1] * dims[2]
+    ws = D.Workspaces()
+    host_in = torch.empty(N, dtype=torch.float32, pin_memory=True)
+    host_in.copy_(vals)
+    L = _abi.lib()
+
+    # warm-up (also validates the path once)
+    for _ in range(args.warmup):
+        info = run_step(vals, dims, bs, cands, r, ws)
+    torch.cuda.synchronize()
+
+    # ---- timed, device resident
+    stage = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    start = torch.cuda.Event(enable_timing=True)
+    stop = torch.cuda.Event(enable_timing=True)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    L.chr_prof_enable(1)
+    _abi.prof_report()  # clear
+    l0 = L.chr_launch_count()
+    meta = torch.zeros(3, dtype=torch.int64, device="cuda")
+    gathered = [torch.zeros(3, dtype=torch.int64, device="cuda") for _ in range(world)]
+    with Clocks(local) as clk:
+        start.record()
+        for i in range(args.steps):
+            info = run_step(vals, dims, bs, cands, r, ws, stage_events=stage[i])
+            if dist:  # the exchange step: global offsets of every rank's outputs
+                meta[0], meta[1], meta[2] = info["archive"], info["ntri"], info["nvert"]
+                dist.all_gather(gathered, meta)
+        stop.record()
+        torch.cuda.synchronize()
+    launches = L.chr_launch_count() - l0
+    L.chr_prof_enable(0)
+    kern = _abi.prof_report()
+    ms = start.elapsed_time(stop) / args.steps
+    if dist:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    st = [(s[0].elapsed_time(s[1]), s[1].elapsed_time(s[2]), s[2].elapsed_time(s[3])) for s in stage]
+    t_c = statistics.median(x[0] for x in st)
+    t_d = statistics.median(x[1] for x in st)
+    t_m = statistics.median(x[2] for x in st)
+
+    # ---- e2e through host buffers (pinned input, archive + mesh back to host)
+    out_arch = torch.empty(info["archive"] + 1024, dtype=torch.uint8, pin_memory=True)
+    out_v = torch.empty(info["nvert"] * 3 + 16, dtype=torch.float64, pin_memory=True)
+    out_t = torch.empty(info["ntri"] * 3 + 16, dtype=torch.int32, pin_memory=True)
+    dvol = torch.empty_like(vals)
+    e2e_ms = []
+    h2d = d2h = 0
+    for i in range(args.warmup + args.steps):
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        dvol.copy_(host_in, non_blocking=True)
+        inf = run_step(dvol, dims, bs, cands, r, ws)
+        nb = inf["archive"]
+        out_arch[:nb].copy_(inf["res"].blob[:nb], non_blocking=True)
+        out_v[: inf["nvert"] * 3].copy_(inf["verts"].reshape(-1), non_blocking=True)
+        out_t[: inf["ntri"] * 3].copy_(inf["tris"].reshape(-1), non_blocking=True)
+        b.record()
+        torch.cuda.synchronize()
+        if i >= args.warmup:
+            e2e_ms.append(a.elapsed_time(b))
+            h2d = 4 * N
+            d2h = nb + 24 * inf["nvert"] + 12 * inf["ntri"]
+    e2e = statistics.median(e2e_ms)
+    if dist:
+        t = torch.tensor([e2e], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e = float(t.item())
+
+    # ---- roofline of the dominant kernel
+    peak, peak_src = _peaks()
+    dom = max(kern.items(), key=lambda kv: kv[1][1]) if kern else None
+    roof = None
+    if dom:
+        name, (cnt, tot) = dom
+        alg = kernel_bytes(name, info, N)
+        avg = tot / cnt
+        achieved = alg / (avg * 1e-3) / 1e9 if alg else None
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tp):
+            try:
+                traffic = json.load(open(tp)).get(name)
+            except Exception:
+                traffic = None
+        roof = {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                "algorithmic_bytes": alg, "avg_ms": avg, "launches_per_step": cnt / args.steps,
+                "share_of_step": tot / args.steps / ms, "peak_source": peak_src}
+    kern_tab = {k: {"launches": c, "avg_ms": t / c, "share": t / args.steps / ms,
+                    "gbs": (kernel_bytes(k, info, N) / (t / c * 1e-3) / 1e9) if kernel_bytes(k, info, N) else None}
+                for k, (c, t) in sorted(kern.items(), key=lambda kv: -kv[1][1])}
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(vals.cpu().numpy(), dims, bs, cands, r, args.cpu_planes, workers)
+
+    value = world * 4 * N / (ms * 1e-3) / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded torch GRF; no public dataset)",
+        "config": {
+            "workload": f"{args.config}: {n}^3 f32 " + {
+                "c3": "lognormal exp(1.5 g), g unit-variance GRF P(k)~k^-3", "c4": "GRF P(k)~k^-11/3 [0,1]",
+                "c2": "GRF P(k)~k^-11/3 |k|<=32 [0,1]", "c1": "8 Gaussian blobs + noise",
+                "c5": "GRF + 64 blobs"}.get(args.config, "") +
+            f", bs{bs}, r={r}, k={cands[0]:.6g}; step = compress -> request(k) -> marching cubes",
+            "dims": list(dims), "block_size": bs, "regions": info["nreg"], "regions_selected": info["nsel"],
+            "archive_bytes": info["archive"], "selected_samples": info["n_sel"], "cells": info["cells"],
+            "triangles": info["ntri"], "vertices": info["nvert"],
+            "l2": "no flush: input (4N bytes) and decoded windows (8 N_sel bytes) are each larger than the 126 MB L2",
+            "per_rank": "independent 512^3 volume per rank (seed = rank) + NCCL all_gather of sizes",
+        },
+        "stages": {
+            "compress_ms": t_c, "compress_gbs": 4 * N / (t_c * 1e-3) / 1e9,
+            "request_ms": t_d, "decompress_gbs": 4 * info["n_sel"] / (t_d * 1e-3) / 1e9,
+            "mc_ms": t_m, "mc_cells_per_s": info["cells"] / (t_m * 1e-3),
+        },
+        "kernels": kern_tab,
+        "roofline": roof,
+        "cpu_baseline": cpu,
+        "e2e": {"value": world * 4 * N / (e2e * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": e2e,
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -194,6 +194,12 @@ int chr_min_abs_distance(const double *d_flat, int64_t n, double k, double *h_ou
 int chr_lorenzo_encode(const double *d_flat, int64_t nx, int64_t ny, int64_t nz, double e,
                        int64_t *d_q, uint8_t *d_escaped, void *stream);
 
+/* 9. instrumentation: launch counter and opt-in per-kernel CUDA-event
+ *    timing on the launching stream ("name count total_ms" lines). */
+void chr_prof_enable(int on);
+long long chr_launch_count(void);
+int chr_prof_report(char *buf, size_t cap);
+
 #ifdef __cplusplus
 }
 #endif

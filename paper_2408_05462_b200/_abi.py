@@ -143,6 +143,12 @@ def lib():
         L.chr_min_abs_distance.restype = INT
         L.chr_lorenzo_encode.argtypes = [P, I64, I64, I64, D, P, P, P]
         L.chr_lorenzo_encode.restype = INT
+        L.chr_prof_enable.argtypes = [INT]
+        L.chr_prof_enable.restype = None
+        L.chr_launch_count.argtypes = []
+        L.chr_launch_count.restype = ctypes.c_longlong
+        L.chr_prof_report.argtypes = [ctypes.c_char_p, SZ]
+        L.chr_prof_report.restype = INT
         _lib = L
     return _lib
 
@@ -152,8 +158,20 @@ EXPORTS = [
     "chr_compress_workspace_size", "chr_compress_capacity", "chr_compress",
     "chr_decode_workspace_size", "chr_decode_regions", "chr_mc_workspace_size", "chr_mc_count",
     "chr_mc_emit", "chr_case_codes", "chr_crc32_workspace_size", "chr_crc32", "chr_crc32_combine",
-    "chr_min_abs_distance", "chr_lorenzo_encode",
+    "chr_min_abs_distance", "chr_lorenzo_encode", "chr_prof_enable", "chr_launch_count", "chr_prof_report",
 ]
+
+
+def prof_report() -> dict[str, tuple[int, float]]:
+    """{kernel: (launches, total_ms)} since the last call (CUDA events)."""
+    L = lib()
+    buf = ctypes.create_string_buffer(1 << 16)
+    L.chr_prof_report(buf, 1 << 16)
+    out = {}
+    for line in buf.value.decode().splitlines():
+        name, cnt, ms = line.rsplit(" ", 2)
+        out[name] = (int(cnt), float(ms))
+    return out
 
 
 def device() -> torch.device:

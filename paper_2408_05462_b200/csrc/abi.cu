@@ -66,7 +66,10 @@ extern "C" int chr_min_abs_distance(const double *d_flat, int64_t n, double k, d
     auto *slot = reinterpret_cast<unsigned long long *>(d_ws);
     CHR_CUDA_TRY(cudaMemsetAsync(slot, 0x7F, 8, st));  // a huge positive double
     const int64_t blocks = std::min<int64_t>(ceil_div(n, 256), 148 * 16);
-    k_min_abs<<<(unsigned)blocks, 256, 0, st>>>(d_flat, n, k, slot);
+    {
+        CHR_PROF("k_min_abs", st);
+        k_min_abs<<<(unsigned)blocks, 256, 0, st>>>(d_flat, n, k, slot);
+    }
     CHR_CUDA_TRY(cudaGetLastError());
     unsigned long long bits = 0;
     CHR_CUDA_TRY(cudaMemcpyAsync(&bits, slot, 8, cudaMemcpyDeviceToHost, st));
@@ -83,6 +86,9 @@ extern "C" int chr_lorenzo_encode(const double *d_flat, int64_t nx, int64_t ny, 
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t n = nx * ny * nz;
     const int64_t blocks = std::min<int64_t>(ceil_div(n, 256), 148 * 32);
-    k_lorenzo_seam<<<(unsigned)blocks, 256, 0, st>>>(d_flat, nx, ny, nz, make_quant(e), d_q, d_escaped);
+    {
+        CHR_PROF("k_lorenzo_seam", st);
+        k_lorenzo_seam<<<(unsigned)blocks, 256, 0, st>>>(d_flat, nx, ny, nz, make_quant(e), d_q, d_escaped);
+    }
     return cudaGetLastError() == cudaSuccess ? CHR_OK : CHR_E_CUDA;
 }

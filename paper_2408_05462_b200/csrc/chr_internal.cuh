@@ -28,6 +28,23 @@ __global__ void k_crc_segments(const uint8_t *__restrict__ buf, const CrcSeg *__
                                int64_t nseg, const CrcTables *__restrict__ tabs,
                                uint32_t *__restrict__ seg_raw);
 
+// ------------------------------------------------------------------ profiling
+// RAII: counts a launch; when chr_prof_enable(1), records CUDA events on the
+// launching stream around it (prof.cu)
+class ProfScope {
+  public:
+    ProfScope(const char *name, cudaStream_t st);
+    ~ProfScope();
+
+  private:
+    const char *name_;
+    cudaStream_t st_;
+    cudaEvent_t a_;
+};
+#define CHR_PROF_CAT2(a, b) a##b
+#define CHR_PROF_CAT(a, b) CHR_PROF_CAT2(a, b)
+#define CHR_PROF(name, st) ::chr::ProfScope CHR_PROF_CAT(_chr_prof_, __LINE__)(name, st)
+
 // ------------------------------------------------------------------ workspace
 struct WsCarver {
     char *base;

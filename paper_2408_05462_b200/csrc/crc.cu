@@ -165,7 +165,10 @@ int crc_launch(const uint8_t *d_buf, const CrcSeg *d_segs, int64_t nseg, int64_t
     int64_t blocks = (warps_needed + 7) / 8;
     if (blocks > 148 * 16) blocks = 148 * 16;
     if (blocks < 1) blocks = 1;
-    k_crc_segments<<<(unsigned)blocks, 256, 0, st>>>(d_buf, d_segs, nseg, tabs, d_seg_raw);
+    {
+        CHR_PROF("k_crc_segments", st);
+        k_crc_segments<<<(unsigned)blocks, 256, 0, st>>>(d_buf, d_segs, nseg, tabs, d_seg_raw);
+    }
     return cudaGetLastError() == cudaSuccess ? CHR_OK : CHR_E_CUDA;
 }
 

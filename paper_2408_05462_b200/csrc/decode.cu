@@ -420,8 +420,11 @@ __global__ void __launch_bounds__(DTHREADS) k_lorenzo(const DecReg *__restrict__
         int64_t filled = -seg_skip[k];  // sample position of the next token
         if (threadIdx.x == 0) s_prev_marker = 0;
         __syncthreads();
-        while (filled < seglen && bstart < hi) {
-            const int64_t wlen = min((int64_t)DWIN, hi - bstart);
+        // bytes of this segment: up to the next segment's first token (+ one
+        // run pair, <= 10 bytes, when the next segment starts inside a run)
+        const int64_t seg_hi = (k + 1 < R.seg_base + R.nseg) ? min(hi, seg_byte[k + 1] + 16) : hi;
+        while (filled < seglen && bstart < seg_hi) {
+            const int64_t wlen = min((int64_t)DWIN, seg_hi - bstart);
             for (int64_t i = threadIdx.x; i < wlen; i += DTHREADS) win[i] = blob[bstart + i];
             __syncthreads();
             // window end: stop at the last end byte so no token straddles
@@ -688,23 +691,47 @@ extern "C" int chr_decode_regions(const uint8_t *d_blob, const chr_dec_region_t 
     CHR_CUDA_TRY(cudaMemsetAsync(pl.ticket, 0, sizeof(unsigned long long), st));
     int rc = crc_launch(d_blob, pl.segs, n, total_sc, pl.seg_raw, st);
     if (rc) return rc;
-    k_check<<<(unsigned)ceil_div(n, 128), 128, 0, st>>>(pl.d_regs, n, pl.seg_raw, tabs, d_blob);
-    k_esc_count<<<(unsigned)n, 256, 0, st>>>(pl.d_regs, n, d_blob);
-    k_tok_count<<<(unsigned)pl.nchunks, DTHREADS, 0, st>>>(pl.d_regs, n, d_blob, pl.chunk_samples);
-    k_tok_scan<<<(unsigned)ceil_div(n, 128), 128, 0, st>>>(pl.d_regs, n, pl.chunk_samples);
-    k_locate<<<(unsigned)pl.nchunks, DTHREADS, 0, st>>>(pl.d_regs, n, d_blob, pl.chunk_samples,
-                                                        pl.seg_byte, pl.seg_skip);
-    k_esc_base<<<(unsigned)n, 256, 0, st>>>(pl.d_regs, n, d_blob, pl.esc_base);
+    {
+        CHR_PROF("k_check", st);
+        k_check<<<(unsigned)ceil_div(n, 128), 128, 0, st>>>(pl.d_regs, n, pl.seg_raw, tabs, d_blob);
+    }
+    {
+        CHR_PROF("k_esc_count", st);
+        k_esc_count<<<(unsigned)n, 256, 0, st>>>(pl.d_regs, n, d_blob);
+    }
+    {
+        CHR_PROF("k_tok_count", st);
+        k_tok_count<<<(unsigned)pl.nchunks, DTHREADS, 0, st>>>(pl.d_regs, n, d_blob, pl.chunk_samples);
+    }
+    {
+        CHR_PROF("k_tok_scan", st);
+        k_tok_scan<<<(unsigned)ceil_div(n, 128), 128, 0, st>>>(pl.d_regs, n, pl.chunk_samples);
+    }
+    {
+        CHR_PROF("k_locate", st);
+        k_locate<<<(unsigned)pl.nchunks, DTHREADS, 0, st>>>(pl.d_regs, n, d_blob, pl.chunk_samples,
+                                                            pl.seg_byte, pl.seg_skip);
+    }
+    {
+        CHR_PROF("k_esc_base", st);
+        k_esc_base<<<(unsigned)n, 256, 0, st>>>(pl.d_regs, n, d_blob, pl.esc_base);
+    }
     if (pl.nitems > 0) {
         const size_t smem = (size_t)pl.max_rows_ex * 16 + DWIN;
         CHR_CUDA_TRY(cudaFuncSetAttribute(k_lorenzo, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_lorenzo<<<(unsigned)pl.nitems, DTHREADS, smem, st>>>(pl.d_regs, n, d_blob, pl.seg_byte,
-                                                               pl.seg_skip, pl.esc_base, pl.carry,
-                                                               pl.flags, pl.ticket, d_out);
+        {
+            CHR_PROF("k_lorenzo", st);
+            k_lorenzo<<<(unsigned)pl.nitems, DTHREADS, smem, st>>>(pl.d_regs, n, d_blob, pl.seg_byte,
+                                                                   pl.seg_skip, pl.esc_base, pl.carry,
+                                                                   pl.flags, pl.ticket, d_out);
+        }
     }
     for (int64_t r0 = 0; r0 < n; r0 += 65535) {
         dim3 g(64, (unsigned)std::min<int64_t>(65535, n - r0));
-        k_verbatim<<<g, 256, 0, st>>>(pl.d_regs, r0, d_blob, d_out);
+        {
+            CHR_PROF("k_verbatim", st);
+            k_verbatim<<<g, 256, 0, st>>>(pl.d_regs, r0, d_blob, d_out);
+        }
     }
     CHR_CUDA_TRY(cudaGetLastError());
     CHR_CUDA_TRY(cudaMemcpyAsync(pl.regs.data(), pl.d_regs, sizeof(DecReg) * n, cudaMemcpyDeviceToHost, st));

@@ -814,29 +814,62 @@ extern "C" int chr_compress(const void *d_vol, int dtype, int src_dtype, int64_t
 
     const unsigned items = (unsigned)pl.nitems, chunks = (unsigned)pl.nchunks;
     if (dtype == CHR_F32)
-        k_tile<float, false><<<items, NW * 32, 0, st>>>((const float *)d_vol, pl.params, pl.d_regs,
-                                                        pl.recs, pl.poffs, d_out);
+        {
+            CHR_PROF("k_tile<float, false>", st);
+            k_tile<float, false><<<items, NW * 32, 0, st>>>((const float *)d_vol, pl.params, pl.d_regs,
+                                                            pl.recs, pl.poffs, d_out);
+        }
     else
-        k_tile<double, false><<<items, NW * 32, 0, st>>>((const double *)d_vol, pl.params, pl.d_regs,
-                                                         pl.recs, pl.poffs, d_out);
-    k_scan_reduce<<<chunks, 256, 0, st>>>(pl.params, pl.d_regs, pl.recs, pl.chunk);
-    k_scan_regions<<<(unsigned)ceil_div(nreg, 128), 128, 0, st>>>(pl.params, pl.d_regs, pl.chunk,
-                                                                  pl.codec2, pl.scal);
-    k_layout<<<1, 1024, 0, st>>>(pl.params, pl.d_regs, pl.segs, pl.scal);
-    k_scan_down<<<chunks, 256, 0, st>>>(pl.params, pl.d_regs, pl.recs, pl.chunk, pl.poffs);
+        {
+            CHR_PROF("k_tile<double, false>", st);
+            k_tile<double, false><<<items, NW * 32, 0, st>>>((const double *)d_vol, pl.params, pl.d_regs,
+                                                             pl.recs, pl.poffs, d_out);
+        }
+    {
+        CHR_PROF("k_scan_reduce", st);
+        k_scan_reduce<<<chunks, 256, 0, st>>>(pl.params, pl.d_regs, pl.recs, pl.chunk);
+    }
+    {
+        CHR_PROF("k_scan_regions", st);
+        k_scan_regions<<<(unsigned)ceil_div(nreg, 128), 128, 0, st>>>(pl.params, pl.d_regs, pl.chunk,
+                                                                      pl.codec2, pl.scal);
+    }
+    {
+        CHR_PROF("k_layout", st);
+        k_layout<<<1, 1024, 0, st>>>(pl.params, pl.d_regs, pl.segs, pl.scal);
+    }
+    {
+        CHR_PROF("k_scan_down", st);
+        k_scan_down<<<chunks, 256, 0, st>>>(pl.params, pl.d_regs, pl.recs, pl.chunk, pl.poffs);
+    }
     if (dtype == CHR_F32) {
-        k_tile<float, true><<<items, NW * 32, 0, st>>>((const float *)d_vol, pl.params, pl.d_regs,
-                                                       pl.recs, pl.poffs, d_out);
-        k_bitmap<float><<<148, 256, 0, st>>>((const float *)d_vol, pl.params, pl.d_regs, pl.codec2,
-                                             pl.scal, d_out);
+        {
+            CHR_PROF("k_tile<float, true>", st);
+            k_tile<float, true><<<items, NW * 32, 0, st>>>((const float *)d_vol, pl.params, pl.d_regs,
+                                                           pl.recs, pl.poffs, d_out);
+        }
+        {
+            CHR_PROF("k_bitmap<float>", st);
+            k_bitmap<float><<<148, 256, 0, st>>>((const float *)d_vol, pl.params, pl.d_regs, pl.codec2,
+                                                 pl.scal, d_out);
+        }
     } else {
-        k_tile<double, true><<<items, NW * 32, 0, st>>>((const double *)d_vol, pl.params, pl.d_regs,
-                                                        pl.recs, pl.poffs, d_out);
-        k_bitmap<double><<<148, 256, 0, st>>>((const double *)d_vol, pl.params, pl.d_regs, pl.codec2,
-                                              pl.scal, d_out);
+        {
+            CHR_PROF("k_tile<double, true>", st);
+            k_tile<double, true><<<items, NW * 32, 0, st>>>((const double *)d_vol, pl.params, pl.d_regs,
+                                                            pl.recs, pl.poffs, d_out);
+        }
+        {
+            CHR_PROF("k_bitmap<double>", st);
+            k_bitmap<double><<<148, 256, 0, st>>>((const double *)d_vol, pl.params, pl.d_regs, pl.codec2,
+                                                  pl.scal, d_out);
+        }
     }
     if (write_file)
-        k_write_table<<<(unsigned)ceil_div(nreg, 256), 256, 0, st>>>(pl.params, pl.d_regs, d_out);
+        {
+            CHR_PROF("k_write_table", st);
+            k_write_table<<<(unsigned)ceil_div(nreg, 256), 256, 0, st>>>(pl.params, pl.d_regs, d_out);
+        }
     CHR_CUDA_TRY(cudaGetLastError());
     // CRC segments: the superchunk total lives on the device; a persistent
     // grid strides over it (no host round trip)
@@ -844,9 +877,16 @@ extern "C" int chr_compress(const void *d_vol, int dtype, int src_dtype, int64_t
     const int64_t nseg = nreg + (write_file ? 1 : 0);
     int rc = crc_launch(d_out, pl.segs, nseg, 0, pl.seg_raw, st);
     if (rc) return rc;
-    k_finalize_regions<<<(unsigned)ceil_div(nreg, 128), 128, 0, st>>>(pl.params, pl.d_regs, pl.seg_raw,
-                                                                      tabs, pl.scal, d_out);
-    if (write_file) k_finalize_file<<<1, 1, 0, st>>>(tabs, pl.scal, d_out);
+    {
+        CHR_PROF("k_finalize_regions", st);
+        k_finalize_regions<<<(unsigned)ceil_div(nreg, 128), 128, 0, st>>>(pl.params, pl.d_regs, pl.seg_raw,
+                                                                          tabs, pl.scal, d_out);
+    }
+    if (write_file)
+    {
+        CHR_PROF("k_finalize_file", st);
+            k_finalize_file<<<1, 1, 0, st>>>(tabs, pl.scal, d_out);
+    }
     CHR_CUDA_TRY(cudaGetLastError());
     CHR_CUDA_TRY(cudaMemcpyAsync(pl.regs.data(), pl.d_regs, sizeof(RegDev) * nreg,
                                  cudaMemcpyDeviceToHost, st));

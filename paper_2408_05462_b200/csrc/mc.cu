@@ -543,10 +543,22 @@ extern "C" int chr_mc_count(const double *d_grids, const chr_mc_grid_t *h, int64
     CHR_CUDA_TRY(cudaMemcpyAsync(pl.d_grids, pl.grids.data(), sizeof(McGrid) * n, cudaMemcpyHostToDevice, st));
     CHR_CUDA_TRY(cudaMemsetAsync(pl.cnt, 0, sizeof(McPieceCnt) * pl.npieces, st));
     const int64_t blocks = std::min<int64_t>(ceil_div(pl.npieces, 8), 148 * 32);
-    k_mc_count<<<(unsigned)blocks, 256, 0, st>>>(d_grids, pl.d_grids, n, pl.npieces, k, T, pl.cnt);
-    k_mc_reduce<<<(unsigned)pl.nchunks, 256, 0, st>>>(pl.cnt, pl.chunk);
-    k_mc_grids<<<1, 1, 0, st>>>(pl.d_grids, n, pl.chunk, pl.totals);
-    k_mc_down<<<(unsigned)pl.nchunks, 256, 0, st>>>(pl.cnt, pl.chunk, pl.base);
+    {
+        CHR_PROF("k_mc_count", st);
+        k_mc_count<<<(unsigned)blocks, 256, 0, st>>>(d_grids, pl.d_grids, n, pl.npieces, k, T, pl.cnt);
+    }
+    {
+        CHR_PROF("k_mc_reduce", st);
+        k_mc_reduce<<<(unsigned)pl.nchunks, 256, 0, st>>>(pl.cnt, pl.chunk);
+    }
+    {
+        CHR_PROF("k_mc_grids", st);
+        k_mc_grids<<<1, 1, 0, st>>>(pl.d_grids, n, pl.chunk, pl.totals);
+    }
+    {
+        CHR_PROF("k_mc_down", st);
+        k_mc_down<<<(unsigned)pl.nchunks, 256, 0, st>>>(pl.cnt, pl.chunk, pl.base);
+    }
     CHR_CUDA_TRY(cudaGetLastError());
     CHR_CUDA_TRY(cudaMemcpyAsync(pl.grids.data(), pl.d_grids, sizeof(McGrid) * n, cudaMemcpyDeviceToHost, st));
     CHR_CUDA_TRY(cudaStreamSynchronize(st));
@@ -574,7 +586,10 @@ extern "C" int chr_mc_emit(const double *d_grids, const chr_mc_grid_t *h, int64_
     const McTables *T = mc_tables_device();
     if (!T) return CHR_E_CUDA;
     if (pl.nitems > 0)
-        k_mc_emit<<<(unsigned)pl.nitems, MNW * 32, 0, st>>>(d_grids, pl.d_grids, n, k, T, pl.base, d_verts, d_tris);
+        {
+            CHR_PROF("k_mc_emit", st);
+            k_mc_emit<<<(unsigned)pl.nitems, MNW * 32, 0, st>>>(d_grids, pl.d_grids, n, k, T, pl.base, d_verts, d_tris);
+        }
     CHR_CUDA_TRY(cudaGetLastError());
     CHR_CUDA_TRY(cudaStreamSynchronize(st));
     return CHR_OK;
@@ -586,6 +601,9 @@ extern "C" int chr_case_codes(const double *d_grid, int64_t nx, int64_t ny, int6
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t n = (nx - 1) * (ny - 1) * (nz - 1);
     const int64_t blocks = std::min<int64_t>(ceil_div(n, 256), 148 * 32);
-    k_case_codes<<<(unsigned)blocks, 256, 0, st>>>(d_grid, nx, ny, nz, k, binary, d_codes);
+    {
+        CHR_PROF("k_case_codes", st);
+        k_case_codes<<<(unsigned)blocks, 256, 0, st>>>(d_grid, nx, ny, nz, k, binary, d_codes);
+    }
     return cudaGetLastError() == cudaSuccess ? CHR_OK : CHR_E_CUDA;
 }

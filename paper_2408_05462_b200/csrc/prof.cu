@@ -1,0 +1,94 @@
+// prof.cu -- opt-in per-kernel timing with CUDA events on the launching
+// stream, plus a launch counter.  Used by bench.py to report the dominant
+// kernel's duration (roofline) and the number of kernels launched.
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "chr_internal.cuh"
+
+namespace chr {
+
+namespace {
+std::mutex g_mu;
+bool g_on = false;
+long long g_launches = 0;
+struct Rec {
+    const char *name;
+    cudaEvent_t a, b;
+};
+std::vector<Rec> g_recs;
+std::vector<cudaEvent_t> g_pool;
+
+cudaEvent_t take_event() {
+    if (!g_pool.empty()) {
+        cudaEvent_t e = g_pool.back();
+        g_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+}  // namespace
+
+ProfScope::ProfScope(const char *name, cudaStream_t st) : name_(name), st_(st), a_(nullptr) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    ++g_launches;
+    if (g_on) {
+        a_ = take_event();
+        cudaEventRecord(a_, st_);
+    }
+}
+
+ProfScope::~ProfScope() {
+    if (!a_) return;
+    std::lock_guard<std::mutex> lk(g_mu);
+    cudaEvent_t b = take_event();
+    cudaEventRecord(b, st_);
+    g_recs.push_back({name_, a_, b});
+}
+
+}  // namespace chr
+
+using namespace chr;
+
+extern "C" void chr_prof_enable(int on) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    g_on = on != 0;
+}
+
+extern "C" long long chr_launch_count(void) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    return g_launches;
+}
+
+// "name count total_ms\n" per kernel name since the last report; clears.
+extern "C" int chr_prof_report(char *buf, size_t cap) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    std::map<std::string, std::pair<long long, double>> agg;
+    for (const Rec &r : g_recs) {
+        cudaEventSynchronize(r.b);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, r.a, r.b);
+        auto &x = agg[r.name];
+        x.first += 1;
+        x.second += ms;
+        g_pool.push_back(r.a);
+        g_pool.push_back(r.b);
+    }
+    g_recs.clear();
+    std::string s;
+    for (auto &kv : agg) {
+        char line[256];
+        snprintf(line, sizeof(line), "%s %lld %.6f\n", kv.first.c_str(), kv.second.first, kv.second.second);
+        s += line;
+    }
+    if (buf && cap) {
+        const size_t n = std::min(cap - 1, s.size());
+        memcpy(buf, s.data(), n);
+        buf[n] = 0;
+    }
+    return (int)s.size();
+}

@@ -135,10 +135,16 @@ extern "C" int chr_stats(const void *d_vol, int dtype, int64_t nx, int64_t ny, i
     CHR_CUDA_TRY(cudaMemsetAsync(d_first_nonfinite, 0xFF, sizeof(int64_t), st));
     auto *bad = reinterpret_cast<unsigned long long *>(d_first_nonfinite);
     if (dtype == CHR_F32)
-        k_stats<float><<<(unsigned)nblocks, 256, 0, st>>>((const float *)d_vol, nx, ny, nz, (int)bs,
-                                                          nbx, nby, cp, d_block_stats, bad);
+        {
+            CHR_PROF("k_stats<float>", st);
+            k_stats<float><<<(unsigned)nblocks, 256, 0, st>>>((const float *)d_vol, nx, ny, nz, (int)bs,
+                                                              nbx, nby, cp, d_block_stats, bad);
+        }
     else
-        k_stats<double><<<(unsigned)nblocks, 256, 0, st>>>((const double *)d_vol, nx, ny, nz,
-                                                           (int)bs, nbx, nby, cp, d_block_stats, bad);
+        {
+            CHR_PROF("k_stats<double>", st);
+            k_stats<double><<<(unsigned)nblocks, 256, 0, st>>>((const double *)d_vol, nx, ny, nz,
+                                                               (int)bs, nbx, nby, cp, d_block_stats, bad);
+        }
     return cudaGetLastError() == cudaSuccess ? CHR_OK : CHR_E_CUDA;
 }

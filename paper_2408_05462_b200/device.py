@@ -100,6 +100,13 @@ class Workspaces:
     def __init__(self):
         self._bufs: dict[str, torch.Tensor] = {}
 
+    def pinned(self, name: str, numel: int, dtype=torch.float64) -> torch.Tensor:
+        t = self._bufs.get("pinned:" + name)
+        if t is None or t.numel() < numel or t.dtype != dtype:
+            t = torch.empty(max(int(numel), 64), dtype=dtype, pin_memory=True)
+            self._bufs["pinned:" + name] = t
+        return t[:numel]
+
     def get(self, name: str, nbytes: int, dtype=torch.uint8) -> torch.Tensor:
         elem = torch.empty((), dtype=dtype).element_size()
         n = max(1, -(-int(nbytes) // elem))
@@ -143,11 +150,12 @@ def build_archive(vol: torch.Tensor, dims, cands, bs, *, spacing=(1.0, 1.0, 1.0)
                   out_of_range="error", ws: Workspaces | None = None, on_warn=None) -> Compressed:
     """stats -> plan -> compress: a complete .chr file on the device
     (chr_archive.build_chr, strict bound at accuracy 1)."""
+    ws = ws or _DEFAULT_WS
     cands = _cands_arr(cands)
     if any(b <= a for a, b in zip(cands[:-1], cands[1:])) or not np.isfinite(cands).all():
         raise ParameterError(f"candidates must be finite and strictly increasing, got {list(cands)}")
     bst, bad = stats(vol, dims, bs, cands)
-    host = torch.empty(bst.numel() + 1, dtype=torch.float64, pin_memory=True)
+    host = ws.pinned("block_stats", bst.numel() + 1)
     host[:-1].copy_(bst.reshape(-1), non_blocking=True)
     host[-1:].copy_(bad.view(torch.float64), non_blocking=True)
     torch.cuda.current_stream().synchronize()
