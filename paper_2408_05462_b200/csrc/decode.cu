@@ -36,7 +36,7 @@
 
 namespace chr {
 
-constexpr int64_t DCB = 4096;     // bytes per token chunk
+constexpr int64_t DCB = 16384;    // bytes per token chunk
 constexpr int DTHREADS = 256;
 constexpr int DBYTES_T = DCB / DTHREADS;  // 16 bytes per thread
 constexpr int DWIN = 16384;       // byte window of k_lorenzo (smem)
@@ -67,11 +67,15 @@ struct DecReg {
     int64_t seg_base, nseg;        // decode segments (nyt * ez)
     int64_t item_base;             // k_lorenzo tiles (nyt)
     int64_t carry_base;            // int64 elements of the carry history
+    // fast (canonical-stream) path: 64x8x8 wavefront tiles, row-piece index
+    int64_t abase;                 // 16-byte aligned chunk origin (blob-relative)
+    int32_t ntx, nty3, ntz3, pad3; // row pieces per row; tiles per axis
+    int64_t tile_base, ntiles, rp_base, nrp;
     // device-computed
     uint64_t tok_start;            // absolute offset of the token stream
     int64_t nesc;
     uint32_t err;
-    uint32_t pad2;
+    uint32_t slow;                 // non-canonical varints seen -> generic path
 };
 
 struct DecParams {
@@ -249,10 +253,11 @@ __global__ void __launch_bounds__(DTHREADS) k_tok_count(DecReg *__restrict__ reg
     DecReg &R = regs[ri];
     int64_t cnt = 0;
     uint32_t err = 0;
-    const bool active = (R.codec == 1 || R.codec == 2) && R.err == 0;
+    const bool active = (R.codec == 1 || R.codec == 2) && R.err == 0 && R.slow;
+    if (!((R.codec == 1 || R.codec == 2) && R.slow)) return;  // fast regions: k_tok_fast
     if (active) {
         const int64_t lo = (int64_t)R.tok_start, hi = (int64_t)(R.poff + R.plen);
-        const int64_t b0 = (int64_t)R.poff + (c - R.chunk_base) * DCB + threadIdx.x * DBYTES_T;
+        const int64_t b0 = R.abase + (c - R.chunk_base) * DCB + threadIdx.x * DBYTES_T;
         for (int64_t e = max(b0, lo); e < min(b0 + DBYTES_T, hi); ++e) {
             if (blob[e] >= 0x80) {
                 if (e == hi - 1) err |= EF_TRUNC;
@@ -298,10 +303,10 @@ __global__ void __launch_bounds__(DTHREADS) k_locate(const DecReg *__restrict__ 
     if (threadIdx.x == 0) ri = find_dreg(regs, nreg, c, 0);
     __syncthreads();
     const DecReg &R = regs[ri];
-    const bool active = (R.codec == 1 || R.codec == 2) && R.err == 0;
+    const bool active = (R.codec == 1 || R.codec == 2) && R.err == 0 && R.slow;
     if (!active) return;  // uniform across the block
     const int64_t lo = (int64_t)R.tok_start, hi = (int64_t)(R.poff + R.plen);
-    const int64_t b0 = (int64_t)R.poff + (c - R.chunk_base) * DCB + threadIdx.x * DBYTES_T;
+    const int64_t b0 = R.abase + (c - R.chunk_base) * DCB + threadIdx.x * DBYTES_T;
     uint32_t err = 0;
     int64_t cnt = 0;
     for (int64_t e = max(b0, lo); e < min(b0 + DBYTES_T, hi); ++e)
@@ -341,7 +346,7 @@ __global__ void k_esc_base(const DecReg *__restrict__ regs, int64_t nreg, const 
                            int64_t *__restrict__ esc_base) {
     const int64_t r = blockIdx.x;
     const DecReg &R = regs[r];
-    if (R.codec != 2 || R.err) return;
+    if (R.codec != 2 || R.err || !R.slow) return;
     const int64_t plane = (int64_t)R.ex * R.ey, segl = (int64_t)R.rows * R.ex;
     // per-segment counts by the block, then a serial scan by thread 0
     for (int64_t k = threadIdx.x; k < R.nseg; k += blockDim.x) {
@@ -371,6 +376,14 @@ __device__ __forceinline__ int64_t ld_acquire(const int64_t *p) {
 __device__ __forceinline__ void st_release(int64_t *p, int64_t v) {
     asm volatile("st.release.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+__device__ __forceinline__ int32_t ld_acquire32(const int32_t *p) {
+    int32_t v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release32(int32_t *p, int32_t v) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 
 // the chained 3D prefix decode (see header)
 __global__ void __launch_bounds__(DTHREADS) k_lorenzo(const DecReg *__restrict__ regs, int64_t nreg,
@@ -390,7 +403,7 @@ __global__ void __launch_bounds__(DTHREADS) k_lorenzo(const DecReg *__restrict__
     __syncthreads();
     const int64_t item = s_item;
     const DecReg &R = regs[find_dreg(regs, nreg, item, 2)];
-    if (!((R.codec == 1 || R.codec == 2) && R.err == 0)) return;
+    if (!((R.codec == 1 || R.codec == 2) && R.err == 0 && R.slow)) return;
     const int yt = (int)(item - R.item_base);
     const int rows_full = R.rows;
     const int y0 = yt * rows_full;
@@ -578,17 +591,563 @@ __global__ void k_verbatim(const DecReg *__restrict__ regs, int64_t r0, const ui
     }
 }
 
+// ================================================================== fast path
+// Canonical streams (every varint minimal, as the encoder writes them): a
+// 0x00 byte is always a whole token (a zero-run marker) and a token is a run
+// length iff the byte before it is 0x00.  A 0x00 end byte after a
+// continuation byte (non-minimal varint) marks the region `slow` and the
+// generic path above decodes it, so parity holds for any CRC-valid stream.
+constexpr int LX = 64, LY = 8, LZ = 8;          // wavefront tile
+constexpr int FACE_X = (LZ + 1) * (LY + 1);      // S(x0+63, y0-1..y0+7, z0-1..z0+7)
+constexpr int FACE_Y = (LZ + 1) * LX;            // S(x, y0+7, z0-1..z0+7)
+constexpr int FACE_Z = LY * LX;                  // S(x, y, z0+7)
+constexpr int FACE_ALL = FACE_X + FACE_Y + FACE_Z;
+
+// ---- bit-parallel tokenizer over a 32-byte window {prev 16 | own 16}:
+// bit j <-> byte j.  E = end bytes (< 0x80), Z = zero bytes (markers),
+// C = ~E.  The run-length token after a marker at m ends at the first end
+// byte >= m+1, found for all markers at once by a carry-propagating add:
+//   Lend = (C + (Z << 1)) & ~C.
+__device__ __forceinline__ uint32_t word_end4(uint32_t x) {
+    return ((((~x) >> 7) & 0x01010101u) * 0x10204080u) >> 28;
+}
+__device__ __forceinline__ uint32_t word_zero4(uint32_t x) {
+    const uint32_t nz = ((x & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | x;  // high bit set iff byte != 0
+    return ((((~nz) >> 7) & 0x01010101u) * 0x10204080u) >> 28;
+}
+
+struct UnitMasks {
+    uint32_t lit;    // literal end bytes (own half, in range)
+    uint32_t len;    // run-length end bytes (own half, in range)
+    uint32_t E;      // end bytes (with virtual ends outside the stream)
+    uint32_t err;
+    bool noncanon;
+};
+
+// w[0..3]: previous 16 bytes, w[4..7]: own 16 bytes; bit 16 <-> offset u0.
+// The stream is [lo, hi) (blob offsets).
+__device__ __forceinline__ UnitMasks unit_masks(const uint32_t (&w)[8], int64_t u0, int64_t lo, int64_t hi) {
+    uint32_t E = 0, Z = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        E |= word_end4(w[k]) << (4 * k);
+        Z |= word_zero4(w[k]) << (4 * k);
+    }
+    const int64_t base = u0 - 16;
+    const int64_t nlo = lo - base, nhi = hi - base;  // bits [nlo, nhi) are stream bytes
+    const uint32_t lob = nlo <= 0 ? 0u : (nlo >= 32 ? 0xFFFFFFFFu : ((1u << nlo) - 1u));
+    const uint32_t hib = nhi >= 32 ? 0u : (nhi <= 0 ? 0xFFFFFFFFu : ~((1u << nhi) - 1u));
+    const uint32_t out = lob | hib;
+    E |= out;
+    Z &= ~out;
+    const uint32_t C = ~E;
+    const uint32_t mine = 0xFFFF0000u & ~out;
+    UnitMasks m;
+    m.err = 0;
+    m.noncanon = (Z & (C << 1) & mine) != 0;            // 0x00 after a continuation byte
+    if (Z & (Z << 1) & mine) m.err |= EF_RANGE;          // marker followed by marker: run of 0
+    if (C & (C << 1) & (C << 2) & (C << 3) & (C << 4) & mine) m.err |= EF_LONG;
+    if (nhi >= 17 && nhi <= 32) {                        // last stream byte is mine
+        const uint32_t lb = 1u << (nhi - 1);
+        if (C & lb) m.err |= EF_TRUNC;
+        if (Z & lb) m.err |= EF_MISSING;
+    }
+    const uint32_t Lend = (C + (Z << 1)) & ~C;
+    m.len = Lend & ~Z & mine;
+    m.lit = E & ~Z & ~Lend & mine;
+    m.E = E;
+    return m;
+}
+
+// value of the token ending at bit `e` of a byte window read through `rd`
+template <typename RD>
+__device__ __forceinline__ uint64_t token_value(uint32_t E, int e, RD rd) {
+    const uint32_t below = E & ((1u << e) - 1u);
+    const int s = below ? 32 - __clz(below) : 0;  // first byte after the previous end byte
+    uint64_t v = 0;
+    for (int k = s; k <= e; ++k) v |= (uint64_t)(rd(k) & 0x7Fu) << (7 * (k - s));
+    return v;
+}
+
+__device__ __forceinline__ void load_units(const uint8_t *__restrict__ blob, int64_t u0, uint32_t (&w)[8]) {
+    const uint4 cur = __ldg(reinterpret_cast<const uint4 *>(blob + u0));
+    uint4 prv = make_uint4(0, 0, 0, 0);
+    if (u0 >= 16) prv = __ldg(reinterpret_cast<const uint4 *>(blob + u0 - 16));
+    w[0] = prv.x; w[1] = prv.y; w[2] = prv.z; w[3] = prv.w;
+    w[4] = cur.x; w[5] = cur.y; w[6] = cur.z; w[7] = cur.w;
+}
+
+__device__ __forceinline__ void next_unit(const uint8_t *__restrict__ blob, int64_t u0, uint32_t (&w)[8]) {
+    w[0] = w[4]; w[1] = w[5]; w[2] = w[6]; w[3] = w[7];
+    const uint4 cur = __ldg(reinterpret_cast<const uint4 *>(blob + u0));
+    w[4] = cur.x; w[5] = cur.y; w[6] = cur.z; w[7] = cur.w;
+}
+
+// samples produced by the tokens ending in one unit
+__device__ __forceinline__ int64_t unit_count(const UnitMasks &m, const uint8_t *__restrict__ blob, int64_t u0) {
+    int64_t c = __popc(m.lit);
+    uint32_t L = m.len;
+    while (L) {
+        const int e = __ffs(L) - 1;
+        L &= L - 1;
+        c += (int64_t)token_value(m.E, e, [&](int k) { return (uint32_t)__ldg(blob + u0 - 16 + k); });
+    }
+    return c;
+}
+
+// region of every chunk / tile (filled once per call; replaces per-CTA
+// binary searches whose dependent loads dominated small CTAs)
+__global__ void k_fill_maps(const DecReg *__restrict__ regs, int64_t nreg, int32_t *__restrict__ chunk_reg,
+                            int32_t *__restrict__ tile_reg) {
+    const int64_t r = blockIdx.x;
+    if (r >= nreg) return;
+    const DecReg &R = regs[r];
+    for (int64_t i = threadIdx.x; i < R.nchunks; i += blockDim.x) chunk_reg[R.chunk_base + i] = (int32_t)r;
+    for (int64_t i = threadIdx.x; i < R.ntiles; i += blockDim.x) tile_reg[R.tile_base + i] = (int32_t)r;
+}
+
+constexpr int UPT = (int)(DCB / (16 * DTHREADS));  // 16-byte units per thread
+
+// tile order for k_lorenzo3d: all regions' tiles grouped by wavefront
+// diagonal d = tx + ty + tz (every dependency of a tile lies on d - 1, so
+// taking tiles in this order from a ticket cannot deadlock and keeps every
+// region's wavefront advancing at once).  One thread per (diagonal, region)
+// pair writes its tiles at pair_base.
+__global__ void k_tile_order(const DecReg *__restrict__ regs, const int64_t *__restrict__ pair_base,
+                             int64_t npairs, int64_t nreg, int32_t *__restrict__ order) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= npairs) return;
+    const int64_t d = i / nreg, r = i % nreg;
+    const DecReg &R = regs[r];
+    if (R.ntiles == 0) return;
+    int64_t k = pair_base[i];
+    const int nx = R.ntx, ny = R.nty3, nz = R.ntz3;
+    for (int tz = max(0, (int)d - (nx - 1) - (ny - 1)); tz <= min(nz - 1, (int)d); ++tz) {
+        const int rem = (int)d - tz;
+        for (int ty = max(0, rem - (nx - 1)); ty <= min(ny - 1, rem); ++ty) {
+            const int tx = rem - ty;
+            order[k++] = (int32_t)(R.tile_base + ((int64_t)tz * ny + ty) * nx + tx);
+        }
+    }
+}
+
+// samples per chunk (fast path); flags non-canonical regions
+__global__ void __launch_bounds__(DTHREADS) k_tok_fast(DecReg *__restrict__ regs, const int32_t *__restrict__ chunk_reg,
+                                                       const uint8_t *__restrict__ blob,
+                                                       int64_t *__restrict__ chunk_samples) {
+    const int64_t c = blockIdx.x;
+    DecReg &R = regs[chunk_reg[c]];
+    if (!((R.codec == 1 || R.codec == 2) && R.err == 0)) {
+        if (threadIdx.x == 0) chunk_samples[c] = 0;
+        return;
+    }
+    const int64_t lo = (int64_t)R.tok_start, hi = (int64_t)(R.poff + R.plen);
+    const int64_t ub = R.abase + (c - R.chunk_base) * DCB + (int64_t)threadIdx.x * UPT * 16;
+    int64_t cnt = 0;
+    uint32_t err = 0;
+    bool nc = false;
+    if (ub + UPT * 16 > lo && ub < hi) {
+        uint32_t w[8];
+        load_units(blob, ub, w);
+#pragma unroll 1
+        for (int u = 0; u < UPT; ++u) {
+            const int64_t u0 = ub + 16 * u;
+            if (u) next_unit(blob, u0, w);
+            if (u0 + 16 > lo && u0 < hi) {
+                const UnitMasks m = unit_masks(w, u0, lo, hi);
+                err |= m.err;
+                nc |= m.noncanon;
+                cnt += unit_count(m, blob, u0);
+            }
+        }
+    }
+    const int64_t tot = block_sum64(cnt);
+    if (err) atomicOr(&R.err, err);
+    if (nc) atomicOr(&R.slow, 1u);
+    if (threadIdx.x == 0) chunk_samples[c] = tot;
+}
+
+// row-piece index: for every 64-sample piece of every row, the byte of the
+// token (marker for runs) holding its first sample and the samples to skip
+__global__ void __launch_bounds__(DTHREADS) k_rp_locate(const DecReg *__restrict__ regs,
+                                                        const int32_t *__restrict__ chunk_reg,
+                                                        const uint8_t *__restrict__ blob,
+                                                        const int64_t *__restrict__ chunk_start,
+                                                        int64_t *__restrict__ rp_byte,
+                                                        int64_t *__restrict__ rp_skip) {
+    const int64_t c = blockIdx.x;
+    const DecReg &R = regs[chunk_reg[c]];
+    if (!((R.codec == 1 || R.codec == 2) && R.err == 0 && !R.slow)) return;
+    const int64_t lo = (int64_t)R.tok_start, hi = (int64_t)(R.poff + R.plen);
+    const int64_t ub = R.abase + (c - R.chunk_base) * DCB + (int64_t)threadIdx.x * UPT * 16;
+    const bool mine = ub + UPT * 16 > lo && ub < hi;
+    int64_t cnt = 0;
+    uint32_t w[8];
+    if (mine) {
+        load_units(blob, ub, w);
+#pragma unroll 1
+        for (int u = 0; u < UPT; ++u) {
+            const int64_t u0 = ub + 16 * u;
+            if (u) next_unit(blob, u0, w);
+            if (u0 + 16 > lo && u0 < hi) cnt += unit_count(unit_masks(w, u0, lo, hi), blob, u0);
+        }
+    }
+    int64_t a = chunk_start[c] + block_excl64(cnt, nullptr);
+    if (!mine || cnt == 0) return;
+    const int64_t ex = R.ex;
+    // first row-piece start >= a; nothing to do if it lies beyond the thread's samples
+    int64_t row = a / ex;
+    int64_t x = a - row * ex;
+    {
+        int64_t xs = (x + 63) & ~63ll, r2 = row;
+        if (xs >= ex) {
+            xs = 0;
+            ++r2;
+        }
+        if (r2 * ex + xs >= a + cnt) return;
+    }
+    load_units(blob, ub, w);
+#pragma unroll 1
+    for (int u = 0; u < UPT; ++u) {
+        const int64_t u0 = ub + 16 * u;
+        if (u) next_unit(blob, u0, w);
+        if (!(u0 + 16 > lo && u0 < hi)) continue;
+        const UnitMasks m = unit_masks(w, u0, lo, hi);
+        uint32_t T = m.lit | m.len;
+        while (T) {
+            const int e = __ffs(T) - 1;
+            T &= T - 1;
+            const bool isl = (m.len >> e) & 1u;
+            int64_t tc = 1, sbyte;
+            const uint32_t below = m.E & ((1u << e) - 1u);
+            const int s = below ? 32 - __clz(below) : 0;
+            if (isl) {
+                tc = (int64_t)token_value(m.E, e, [&](int k) { return (uint32_t)__ldg(blob + u0 - 16 + k); });
+                sbyte = u0 - 16 + s - 1;  // the marker
+            } else {
+                sbyte = u0 - 16 + s;
+            }
+            if ((x & 63) == 0 || tc > 1) {
+                int64_t xs = (x + 63) & ~63ll, r2 = row;
+                if (xs >= ex) {
+                    xs = 0;
+                    ++r2;
+                }
+                int64_t pp = r2 * ex + xs;
+                while (pp < a + tc) {
+                    const int64_t k = R.rp_base + r2 * R.ntx + (xs >> 6);
+                    rp_byte[k] = sbyte;
+                    rp_skip[k] = pp - a;
+                    xs += 64;
+                    if (xs >= ex) {
+                        xs = 0;
+                        ++r2;
+                    }
+                    pp = r2 * ex + xs;
+                }
+            }
+            a += tc;
+            x += tc;
+            if (x >= ex) {
+                if (x < 2 * ex) {
+                    x -= ex;
+                    ++row;
+                } else {
+                    row += x / ex;
+                    x %= ex;
+                }
+            }
+        }
+    }
+}
+
+// codec 2: escapes before every row piece (one CTA per region)
+__global__ void __launch_bounds__(256) k_esc_rp(const DecReg *__restrict__ regs, const uint8_t *__restrict__ blob,
+                                                int64_t *__restrict__ esc_rp) {
+    const DecReg &R = regs[blockIdx.x];
+    if (R.codec != 2 || R.err || R.slow) return;
+    const uint8_t *bm = blob + R.poff;
+    int64_t carry = 0;
+    for (int64_t p0 = 0; p0 < R.nrp; p0 += 256) {
+        const int64_t p = p0 + threadIdx.x;
+        int64_t cnt = 0;
+        if (p < R.nrp) {
+            const int64_t row = p / R.ntx, xt = p % R.ntx;
+            const int64_t s0 = row * R.ex + xt * 64, s1 = s0 + min((int64_t)64, (int64_t)R.ex - xt * 64);
+            for (int64_t s = s0; s < s1; ++s) cnt += (bm[s >> 3] >> (s & 7)) & 1;
+        }
+        int64_t total;
+        const int64_t ex = block_excl64(cnt, &total);
+        if (p < R.nrp) esc_rp[R.rp_base + p] = carry + ex;
+        carry += total;
+        __syncthreads();
+    }
+}
+
+__device__ __forceinline__ int64_t ld_cg64(const int64_t *p) { return __ldcg(p); }
+
+// the 3D wavefront: one CTA per 64x8x8 tile, taken in (region, tz, ty, tx)
+// order from an atomic ticket; waits for the x-, y-, z-neighbour's faces.
+constexpr int TBUF = 64 * 352;  // staged token bytes of the tile's 64 row pieces
+__global__ void __launch_bounds__(256) k_lorenzo3d(const DecReg *__restrict__ regs,
+                                                   const int32_t *__restrict__ tile_reg,
+                                                   const uint8_t *__restrict__ blob,
+                                                   const int64_t *__restrict__ rp_byte,
+                                                   const int64_t *__restrict__ rp_skip,
+                                                   const int64_t *__restrict__ esc_rp,
+                                                   int64_t *__restrict__ faces, int32_t *__restrict__ tflag,
+                                                   unsigned long long *__restrict__ ticket,
+                                                   const int32_t *__restrict__ order,
+                                                   double *__restrict__ out) {
+    __shared__ int64_t S[LZ][LY][LX];
+    __shared__ int64_t Fx[LZ + 1][LY + 1];
+    __shared__ int64_t Fy[LZ + 1][LX];
+    __shared__ int64_t Fz[LY][LX];
+    extern __shared__ __align__(16) uint8_t tb[];  // TBUF bytes
+    __shared__ int32_t roff[64], rlen[64];
+    __shared__ int64_t rb0[64];
+    __shared__ int32_t rskip[64];
+    __shared__ int64_t s_item;
+    if (threadIdx.x == 0) s_item = order[atomicAdd(ticket, 1ull)];
+    __syncthreads();
+    const int64_t tile = s_item;
+    const DecReg &R = regs[tile_reg[tile]];
+    if (!((R.codec == 1 || R.codec == 2) && R.err == 0 && !R.slow)) return;
+    const int64_t local = tile - R.tile_base;
+    const int tx = (int)(local % R.ntx);
+    const int64_t l2 = local / R.ntx;
+    const int ty = (int)(l2 % R.nty3), tz = (int)(l2 / R.nty3);
+    const int x0 = tx * LX, y0 = ty * LY, z0 = tz * LZ;
+    const int nxv = min(LX, R.ex - x0), nyv = min(LY, R.ey - y0), nzv = min(LZ, R.ez - z0);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t hi = (int64_t)(R.poff + R.plen);
+    const int64_t rp_end = R.rp_base + R.nrp;
+
+    // ---- 0. stage the bytes of the 64 row pieces (piece j = zz*8 + yy) at
+    //         16-byte aligned shared-memory offsets
+    if (warp == 0) {
+        int32_t len[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int j = lane + 32 * h, zz = j >> 3, yy = j & 7;
+            len[h] = 0;
+            int64_t b0 = 0;
+            if (zz < nzv && yy < nyv) {
+                const int64_t p = R.rp_base + ((int64_t)(z0 + zz) * R.ey + (y0 + yy)) * R.ntx + tx;
+                b0 = rp_byte[p];
+                const int64_t b1 = p + 1 < rp_end ? min(hi, rp_byte[p + 1] + 11) : hi;
+                len[h] = (int32_t)min(b1 - b0, (int64_t)352);
+                rskip[j] = (int32_t)rp_skip[p];
+            }
+            rb0[j] = b0;
+            rlen[j] = len[h];
+        }
+        int32_t a = (len[0] + 15) & ~15, b = (len[1] + 15) & ~15;
+        const int32_t a0 = a, b0v = b;
+        for (int off = 1; off < 32; off <<= 1) {
+            const int32_t oa = __shfl_up_sync(0xFFFFFFFFu, a, off), ob = __shfl_up_sync(0xFFFFFFFFu, b, off);
+            if (lane >= off) {
+                a += oa;
+                b += ob;
+            }
+        }
+        b += __shfl_sync(0xFFFFFFFFu, a, 31);
+        roff[lane] = a - a0;
+        roff[lane + 32] = b - b0v;
+    }
+    int64_t *Sf = &S[0][0][0];
+    for (int i = threadIdx.x; i < LX * LY * LZ; i += 256) Sf[i] = 0;
+    __syncthreads();
+    for (int j = warp; j < 64; j += 8) {
+        const int o = roff[j], L = rlen[j];
+        const int64_t b0 = rb0[j];
+        for (int i = lane; i < ((L + 15) & ~15); i += 32) tb[o + i] = i < L ? __ldg(blob + b0 + i) : 0x80;
+    }
+    __syncthreads();
+    // ---- 1. tokens -> q, bit-parallel per 16-byte unit (one unit per lane)
+    if (warp < nyv) {
+        for (int zz = 0; zz < nzv; ++zz) {
+            const int j = zz * 8 + warp;
+            const uint8_t *bb = tb + roff[j];
+            const int len = rlen[j];
+            const int nunits = (len + 15) >> 4;
+            int64_t cnt = 0;
+            UnitMasks m;
+            m.lit = m.len = 0;
+            m.E = 0;
+            if (lane < nunits) {
+                uint32_t w[8];
+                const uint4 cur = *reinterpret_cast<const uint4 *>(bb + 16 * lane);
+                const uint4 prv = lane ? *reinterpret_cast<const uint4 *>(bb + 16 * (lane - 1)) : make_uint4(0, 0, 0, 0);
+                w[0] = prv.x; w[1] = prv.y; w[2] = prv.z; w[3] = prv.w;
+                w[4] = cur.x; w[5] = cur.y; w[6] = cur.z; w[7] = cur.w;
+                m = unit_masks(w, 16 * lane, 0, len);
+                cnt = __popc(m.lit);
+                uint32_t L = m.len;
+                while (L) {
+                    const int e = __ffs(L) - 1;
+                    L &= L - 1;
+                    cnt += (int64_t)token_value(m.E, e, [&](int k) { return (uint32_t)bb[16 * lane - 16 + k]; });
+                }
+            }
+            int64_t inc = cnt;
+            for (int off = 1; off < 32; off <<= 1) {
+                const int64_t o = __shfl_up_sync(0xFFFFFFFFu, inc, off);
+                if (lane >= off) inc += o;
+            }
+            int64_t at = inc - cnt - rskip[j];
+            uint32_t T = m.lit | m.len;
+            while (T && at < nxv) {
+                const int e = __ffs(T) - 1;
+                T &= T - 1;
+                const uint64_t v = token_value(m.E, e, [&](int k) { return (uint32_t)bb[16 * lane - 16 + k]; });
+                if ((m.len >> e) & 1u) {
+                    at += (int64_t)v;
+                } else {
+                    if (at >= 0) {
+                        const uint64_t zz2 = v - 1;
+                        S[zz][warp][at] = (int64_t)(zz2 >> 1) ^ -(int64_t)(zz2 & 1);
+                    }
+                    ++at;
+                }
+            }
+        }
+    }
+    __syncthreads();
+    // ---- 2. local 3D prefix: x (warp per row), y, z
+    for (int r = warp; r < LZ * LY; r += 8) {
+        int64_t *row = &S[r >> 3][r & 7][0];
+        int64_t a = row[lane], b = row[lane + 32];
+        for (int off = 1; off < 32; off <<= 1) {
+            const int64_t oa = __shfl_up_sync(0xFFFFFFFFu, a, off);
+            const int64_t ob = __shfl_up_sync(0xFFFFFFFFu, b, off);
+            if (lane >= off) {
+                a += oa;
+                b += ob;
+            }
+        }
+        b += __shfl_sync(0xFFFFFFFFu, a, 31);
+        row[lane] = a;
+        row[lane + 32] = b;
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < LZ * LX; t += 256) {
+        const int zz = t >> 6, x = t & 63;
+        int64_t acc = 0;
+#pragma unroll
+        for (int yy = 0; yy < LY; ++yy) {
+            acc += S[zz][yy][x];
+            S[zz][yy][x] = acc;
+        }
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < LY * LX; t += 256) {
+        const int yy = t >> 6, x = t & 63;
+        int64_t acc = 0;
+#pragma unroll
+        for (int zz = 0; zz < LZ; ++zz) {
+            acc += S[zz][yy][x];
+            S[zz][yy][x] = acc;
+        }
+    }
+    // ---- 3. neighbour faces
+    const int64_t nb_x = tx > 0 ? tile - 1 : -1;
+    const int64_t nb_y = ty > 0 ? tile - R.ntx : -1;
+    const int64_t nb_z = tz > 0 ? tile - (int64_t)R.ntx * R.nty3 : -1;
+    if (threadIdx.x == 0) {
+        if (nb_x >= 0) while (ld_acquire32(tflag + nb_x) == 0) __nanosleep(20);
+        if (nb_y >= 0) while (ld_acquire32(tflag + nb_y) == 0) __nanosleep(20);
+        if (nb_z >= 0) while (ld_acquire32(tflag + nb_z) == 0) __nanosleep(20);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < FACE_X; i += 256)
+        (&Fx[0][0])[i] = nb_x >= 0 ? ld_cg64(faces + nb_x * FACE_ALL + i) : 0;
+    for (int i = threadIdx.x; i < FACE_Y; i += 256)
+        (&Fy[0][0])[i] = nb_y >= 0 ? ld_cg64(faces + nb_y * FACE_ALL + FACE_X + i) : 0;
+    for (int i = threadIdx.x; i < FACE_Z; i += 256)
+        (&Fz[0][0])[i] = nb_z >= 0 ? ld_cg64(faces + nb_z * FACE_ALL + FACE_X + FACE_Y + i) : 0;
+    __syncthreads();
+    // ---- 4. S = T + inclusion-exclusion of the low faces
+    for (int i = threadIdx.x; i < LX * LY * LZ; i += 256) {
+        const int zz = i >> 9, yy = (i >> 6) & 7, x = i & 63;
+        Sf[i] += Fx[zz + 1][yy + 1] + Fy[zz + 1][x] + Fz[yy][x] - Fx[zz + 1][0] - Fx[0][yy + 1] - Fy[0][x] +
+                 Fx[0][0];
+    }
+    __syncthreads();
+    // ---- 5. publish this tile's high faces
+    int64_t *my = faces + tile * FACE_ALL;
+    for (int i = threadIdx.x; i < FACE_X; i += 256) {
+        const int zp = i / (LY + 1), yp = i % (LY + 1);
+        int64_t v;
+        if (zp == 0) v = yp == 0 ? Fy[0][LX - 1] : Fz[yp - 1][LX - 1];
+        else if (yp == 0) v = Fy[zp][LX - 1];
+        else v = S[zp - 1][yp - 1][LX - 1];
+        my[i] = v;
+    }
+    for (int i = threadIdx.x; i < FACE_Y; i += 256) {
+        const int zp = i >> 6, x = i & 63;
+        my[FACE_X + i] = zp == 0 ? Fz[LY - 1][x] : S[zp - 1][LY - 1][x];
+    }
+    for (int i = threadIdx.x; i < FACE_Z; i += 256) my[FACE_X + FACE_Y + i] = S[LZ - 1][i >> 6][i & 63];
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) st_release32(tflag + tile, 1);
+    // ---- 6. reconstruction (escapes overwritten in raster order)
+    const double twoe = 2.0 * R.e;
+    const bool esc = R.codec == 2 && R.nesc > 0;
+    const uint8_t *bm = blob + R.poff;
+    const uint8_t *ev = blob + R.poff + ((R.n + 7) >> 3);
+    for (int r = warp; r < LZ * LY; r += 8) {
+        const int zz = r >> 3, yy = r & 7;
+        if (zz >= nzv || yy >= nyv) continue;
+        const int64_t srow = ((int64_t)(z0 + zz) * R.ey + (y0 + yy)) * R.ex + x0;
+        double *o = out + R.out_off + srow;
+        uint64_t em = 0;
+        int64_t ebase = 0;
+        if (esc) {
+            const int sh = (int)(srow & 7);
+            const int64_t byte0 = srow >> 3;
+            uint32_t bt = 0;
+            if (lane < 9 && byte0 + lane < ((R.n + 7) >> 3)) bt = bm[byte0 + lane];
+            uint64_t lo64 = 0;
+            for (int k = 0; k < 8; ++k) lo64 |= (uint64_t)__shfl_sync(0xFFFFFFFFu, bt, k) << (8 * k);
+            const uint64_t b8 = __shfl_sync(0xFFFFFFFFu, bt, 8);
+            em = sh ? (lo64 >> sh) | (b8 << (64 - sh)) : lo64;
+            if (nxv < 64) em &= (1ull << nxv) - 1;
+            ebase = esc_rp[R.rp_base + ((int64_t)(z0 + zz) * R.ey + (y0 + yy)) * R.ntx + tx];
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int x = lane + 32 * h;
+            if (x >= nxv) continue;
+            double v = (double)S[zz][yy][x] * twoe;
+            if (esc && ((em >> x) & 1)) {
+                const int64_t rank = ebase + __popcll((long long)(em & ((1ull << x) - 1)));
+                uint8_t tmp[8];
+                for (int k = 0; k < 8; ++k) tmp[k] = ev[8 * rank + k];
+                memcpy(&v, tmp, 8);
+            }
+            o[x] = v;
+        }
+    }
+}
+
 // ------------------------------------------------------------------ host
 struct DecPlan {
     std::vector<DecReg> regs;
-    int64_t nchunks = 0, nseg = 0, nitems = 0, ncarry = 0;
+    int64_t nchunks = 0, nseg = 0, nitems = 0, ncarry = 0, ntiles = 0, nrp = 0;
     int max_rows_ex = 0;
     size_t ws = 0;
     DecReg *d_regs;
     CrcSeg *segs;
     uint32_t *seg_raw;
     int64_t *chunk_samples, *seg_byte, *seg_skip, *esc_base, *carry, *flags;
-    unsigned long long *ticket;
+    int64_t *rp_byte, *rp_skip, *esc_rp, *faces;
+    int32_t *tflag, *chunk_reg, *tile_reg, *order;
+    int64_t *pair_base;
+    std::vector<int64_t> h_pair_base;
+    int64_t ndiag = 0;
+    unsigned long long *ticket, *ticket3;
 };
 
 static int dec_rows_for(int ex) {
@@ -598,9 +1157,9 @@ static int dec_rows_for(int ex) {
     return rows < 1 ? 0 : rows;
 }
 
-static bool dec_build(const chr_dec_region_t *h, int64_t n, DecPlan &pl) {
+static bool dec_build(const chr_dec_region_t *h, int64_t n, uintptr_t blob, DecPlan &pl) {
     pl.regs.resize(n);
-    int64_t chunk = 0, seg = 0, item = 0, carry = 0;
+    int64_t chunk = 0, seg = 0, item = 0, carry = 0, tile = 0, rp = 0;
     for (int64_t i = 0; i < n; ++i) {
         DecReg &R = pl.regs[i];
         std::memset(&R, 0, sizeof(R));
@@ -618,24 +1177,56 @@ static bool dec_build(const chr_dec_region_t *h, int64_t n, DecPlan &pl) {
         R.rows = dec_rows_for(R.ex);
         if (R.rows < 1) return false;
         R.nyt = (int32_t)ceil_div(R.ey, R.rows);
+        // chunks: 4 KiB over [16-aligned(poff), poff + plen)
+        R.abase = (int64_t)(((blob + R.poff) & ~(uintptr_t)15) - blob);
         R.chunk_base = chunk;
-        R.nchunks = std::max<int64_t>(1, ceil_div((int64_t)R.plen, DCB));
+        R.nchunks = std::max<int64_t>(1, ceil_div((int64_t)(R.poff + R.plen) - R.abase, DCB));
         chunk += R.nchunks;
         R.seg_base = seg;
         R.item_base = item;
         R.carry_base = carry;
+        R.ntx = (int32_t)ceil_div(R.ex, LX);
+        R.nty3 = (int32_t)ceil_div(R.ey, LY);
+        R.ntz3 = (int32_t)ceil_div(R.ez, LZ);
+        R.tile_base = tile;
+        R.rp_base = rp;
         if (R.codec == 1 || R.codec == 2) {
             R.nseg = (int64_t)R.nyt * R.ez;
             seg += R.nseg;
             item += R.nyt;
             carry += (int64_t)R.nyt * R.ez * R.ex;
             pl.max_rows_ex = std::max(pl.max_rows_ex, R.rows * R.ex);
+            R.ntiles = (int64_t)R.ntx * R.nty3 * R.ntz3;
+            tile += R.ntiles;
+            R.nrp = (int64_t)R.ntx * R.ey * R.ez;
+            rp += R.nrp;
         }
     }
     pl.nchunks = chunk;
     pl.nseg = seg;
     pl.nitems = item;
     pl.ncarry = carry;
+    pl.ntiles = tile;
+    pl.nrp = rp;
+    // tiles per (diagonal, region) -> exclusive bases in diagonal-major order
+    int64_t D = 0;
+    for (const DecReg &R : pl.regs)
+        if (R.ntiles) D = std::max<int64_t>(D, (int64_t)R.ntx + R.nty3 + R.ntz3 - 2);
+    pl.ndiag = pl.ntiles ? D + 1 : 0;
+    pl.h_pair_base.assign((size_t)(pl.ndiag * n) + 1, 0);
+    int64_t acc = 0;
+    for (int64_t d = 0; d < pl.ndiag; ++d)
+        for (int64_t i = 0; i < n; ++i) {
+            const DecReg &R = pl.regs[i];
+            pl.h_pair_base[d * n + i] = acc;
+            if (!R.ntiles) continue;
+            const int nx = R.ntx, ny = R.nty3, nz = R.ntz3;
+            for (int tz = std::max<int>(0, (int)d - (nx - 1) - (ny - 1)); tz <= std::min<int>(nz - 1, (int)d); ++tz) {
+                const int rem = (int)d - tz;
+                const int lo = std::max(0, rem - (nx - 1)), hi = std::min(ny - 1, rem);
+                if (hi >= lo) acc += hi - lo + 1;
+            }
+        }
     return true;
 }
 
@@ -651,7 +1242,17 @@ static void dec_carve(DecPlan &pl, void *base, size_t cap) {
     pl.esc_base = c.take<int64_t>(pl.nseg + 1);
     pl.carry = c.take<int64_t>(pl.ncarry + 1);
     pl.flags = c.take<int64_t>(pl.nitems + 1);
+    pl.rp_byte = c.take<int64_t>(pl.nrp + 1);
+    pl.rp_skip = c.take<int64_t>(pl.nrp + 1);
+    pl.esc_rp = c.take<int64_t>(pl.nrp + 1);
+    pl.faces = c.take<int64_t>((size_t)pl.ntiles * FACE_ALL + 1);
+    pl.tflag = c.take<int32_t>(pl.ntiles + 1);
+    pl.chunk_reg = c.take<int32_t>(pl.nchunks + 1);
+    pl.tile_reg = c.take<int32_t>(pl.ntiles + 1);
+    pl.order = c.take<int32_t>(pl.ntiles + 1);
+    pl.pair_base = c.take<int64_t>(pl.h_pair_base.size() + 1);
     pl.ticket = c.take<unsigned long long>(1);
+    pl.ticket3 = c.take<unsigned long long>(1);
     pl.ws = c.off + 256;
 }
 
@@ -661,7 +1262,7 @@ using namespace chr;
 
 extern "C" size_t chr_decode_workspace_size(const chr_dec_region_t *h, int64_t n) {
     DecPlan pl;
-    if (!h || n < 1 || !dec_build(h, n, pl)) return 256;
+    if (!h || n < 1 || !dec_build(h, n, 0, pl)) return 256;
     dec_carve(pl, nullptr, ~size_t(0));
     return pl.ws;
 }
@@ -673,7 +1274,7 @@ extern "C" int chr_decode_regions(const uint8_t *d_blob, const chr_dec_region_t 
     if (!d_blob || !h || n < 0 || !d_out) return CHR_E_PARAMETER;
     cudaStream_t st = (cudaStream_t)stream;
     DecPlan pl;
-    if (!dec_build(h, n, pl)) return CHR_E_PARAMETER;
+    if (!dec_build(h, n, (uintptr_t)d_blob, pl)) return CHR_E_PARAMETER;
     dec_carve(pl, d_ws, ws_bytes);
     if (!d_ws || pl.ws > ws_bytes) return CHR_E_WORKSPACE;
     const CrcTables *tabs = crc_tables_device();
@@ -689,6 +1290,8 @@ extern "C" int chr_decode_regions(const uint8_t *d_blob, const chr_dec_region_t 
     CHR_CUDA_TRY(cudaMemsetAsync(pl.seg_raw, 0, sizeof(uint32_t) * n, st));
     CHR_CUDA_TRY(cudaMemsetAsync(pl.flags, 0, sizeof(int64_t) * (pl.nitems + 1), st));
     CHR_CUDA_TRY(cudaMemsetAsync(pl.ticket, 0, sizeof(unsigned long long), st));
+    CHR_CUDA_TRY(cudaMemsetAsync(pl.ticket3, 0, sizeof(unsigned long long), st));
+    CHR_CUDA_TRY(cudaMemsetAsync(pl.tflag, 0, sizeof(int32_t) * (pl.ntiles + 1), st));
     int rc = crc_launch(d_blob, pl.segs, n, total_sc, pl.seg_raw, st);
     if (rc) return rc;
     {
@@ -700,6 +1303,14 @@ extern "C" int chr_decode_regions(const uint8_t *d_blob, const chr_dec_region_t 
         k_esc_count<<<(unsigned)n, 256, 0, st>>>(pl.d_regs, n, d_blob);
     }
     {
+        CHR_PROF("k_fill_maps", st);
+        k_fill_maps<<<(unsigned)n, 256, 0, st>>>(pl.d_regs, n, pl.chunk_reg, pl.tile_reg);
+    }
+    {
+        CHR_PROF("k_tok_fast", st);
+        k_tok_fast<<<(unsigned)pl.nchunks, DTHREADS, 0, st>>>(pl.d_regs, pl.chunk_reg, d_blob, pl.chunk_samples);
+    }
+    {
         CHR_PROF("k_tok_count", st);
         k_tok_count<<<(unsigned)pl.nchunks, DTHREADS, 0, st>>>(pl.d_regs, n, d_blob, pl.chunk_samples);
     }
@@ -708,13 +1319,35 @@ extern "C" int chr_decode_regions(const uint8_t *d_blob, const chr_dec_region_t 
         k_tok_scan<<<(unsigned)ceil_div(n, 128), 128, 0, st>>>(pl.d_regs, n, pl.chunk_samples);
     }
     {
+        CHR_PROF("k_rp_locate", st);
+        k_rp_locate<<<(unsigned)pl.nchunks, DTHREADS, 0, st>>>(pl.d_regs, pl.chunk_reg, d_blob, pl.chunk_samples,
+                                                               pl.rp_byte, pl.rp_skip);
+    }
+    {
         CHR_PROF("k_locate", st);
         k_locate<<<(unsigned)pl.nchunks, DTHREADS, 0, st>>>(pl.d_regs, n, d_blob, pl.chunk_samples,
                                                             pl.seg_byte, pl.seg_skip);
     }
     {
+        CHR_PROF("k_esc_rp", st);
+        k_esc_rp<<<(unsigned)n, 256, 0, st>>>(pl.d_regs, d_blob, pl.esc_rp);
+    }
+    {
         CHR_PROF("k_esc_base", st);
         k_esc_base<<<(unsigned)n, 256, 0, st>>>(pl.d_regs, n, d_blob, pl.esc_base);
+    }
+    if (pl.ntiles > 0) {
+        const int64_t npairs = pl.ndiag * n;
+        CHR_CUDA_TRY(cudaMemcpyAsync(pl.pair_base, pl.h_pair_base.data(), sizeof(int64_t) * npairs,
+                                     cudaMemcpyHostToDevice, st));
+        {
+            CHR_PROF("k_tile_order", st);
+            k_tile_order<<<(unsigned)ceil_div(npairs, 256), 256, 0, st>>>(pl.d_regs, pl.pair_base, npairs, n, pl.order);
+        }
+        CHR_CUDA_TRY(cudaFuncSetAttribute(k_lorenzo3d, cudaFuncAttributeMaxDynamicSharedMemorySize, TBUF));
+        CHR_PROF("k_lorenzo3d", st);
+        k_lorenzo3d<<<(unsigned)pl.ntiles, 256, TBUF, st>>>(pl.d_regs, pl.tile_reg, d_blob, pl.rp_byte, pl.rp_skip, pl.esc_rp,
+                                                         pl.faces, pl.tflag, pl.ticket3, pl.order, d_out);
     }
     if (pl.nitems > 0) {
         const size_t smem = (size_t)pl.max_rows_ex * 16 + DWIN;

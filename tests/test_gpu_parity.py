@@ -257,3 +257,42 @@ def test_crc_kernel_matches_zlib():
         assert device.crc32(t) == zlib.crc32(a.tobytes()), n
         if n > 8:
             assert device.crc32(t[3:], n - 3) == zlib.crc32(a[3:].tobytes())
+
+
+def test_noncanonical_stream_uses_generic_path():
+    """CRC-valid hand-made streams with non-minimal varints (e.g. 0x81 0x00 for
+    the literal 1) must decode exactly like the reference (kernels.py:304-342);
+    the fast canonical tokenizer hands such regions to the generic path."""
+    import zlib
+
+    g = np.random.default_rng(9).normal(size=(20, 9, 7))
+    blk = G.compress(g, 0.05)
+    assert blk.codec_id == 1
+    tok = blk.payload
+    # rewrite every single-byte literal 0x02..0x7f (end byte, after an end byte)
+    # into a 2-byte non-minimal form b|0x80, 0x00
+    out = bytearray()
+    prev_end = True
+    changed = 0
+    for b in tok:
+        if prev_end and 2 <= b < 0x80 and changed < 40:
+            out += bytes([b | 0x80, 0x00])
+            changed += 1
+        else:
+            out.append(b)
+        prev_end = b < 0x80
+    assert changed
+    crafted = CompressedBlock(1, blk.dims, blk.error_bound, "f64", bytes(out), zlib.crc32(bytes(out)))
+    want = O.decompress_block(crafted.to_bytes())[1]
+    got = G.decompress(crafted).ravel(order="F")
+    assert np.array_equal(got, want)
+    assert np.array_equal(got, G.decompress(blk).ravel(order="F"))
+
+
+@pytest.mark.parametrize("shape", [(64, 8, 8), (65, 9, 17), (130, 3, 2), (1, 1, 300), (200, 1, 1), (3, 70, 40)])
+def test_decode_tile_shapes(shape):
+    g = np.random.default_rng(sum(shape) + 1).normal(size=shape).cumsum(axis=0)
+    for e in (1e-3, 0.3):
+        blk = G.compress(g, e)
+        ref = O.decompress_block(blk.to_bytes())[1]
+        assert np.array_equal(G.decompress(blk).ravel(order="F"), ref), (shape, e)
