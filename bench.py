@@ -150,6 +150,9 @@ def kernel_bytes(name, info, N):
         "k_tok_count": info["c_sel"],
         "k_locate": info["c_sel"],
         "k_lorenzo": info["c_sel"] + 8 * info["n_sel"],
+        "k_lorenzo3d": info["c_sel"] + 8 * info["n_sel"],
+        "k_tok_fast": info["c_sel"],
+        "k_rp_locate": info["c_sel"],
         "k_mc_count": 8 * info["n_sel"],
         "k_mc_emit": 8 * info["n_sel"] + 24 * info["nvert"] + 12 * info["ntri"],
     }

@@ -69,7 +69,7 @@ struct DecReg {
     int64_t carry_base;            // int64 elements of the carry history
     // fast (canonical-stream) path: 64x8x8 wavefront tiles, row-piece index
     int64_t abase;                 // 16-byte aligned chunk origin (blob-relative)
-    int32_t ntx, nty3, ntz3, pad3; // row pieces per row; tiles per axis
+    int32_t ntx, tnx, tny, tnz;    // row pieces per row; wavefront tiles per axis
     int64_t tile_base, ntiles, rp_base, nrp;
     // device-computed
     uint64_t tok_start;            // absolute offset of the token stream
@@ -597,11 +597,6 @@ __global__ void k_verbatim(const DecReg *__restrict__ regs, int64_t r0, const ui
 // length iff the byte before it is 0x00.  A 0x00 end byte after a
 // continuation byte (non-minimal varint) marks the region `slow` and the
 // generic path above decodes it, so parity holds for any CRC-valid stream.
-constexpr int LX = 64, LY = 8, LZ = 8;          // wavefront tile
-constexpr int FACE_X = (LZ + 1) * (LY + 1);      // S(x0+63, y0-1..y0+7, z0-1..z0+7)
-constexpr int FACE_Y = (LZ + 1) * LX;            // S(x, y0+7, z0-1..z0+7)
-constexpr int FACE_Z = LY * LX;                  // S(x, y, z0+7)
-constexpr int FACE_ALL = FACE_X + FACE_Y + FACE_Z;
 
 // ---- bit-parallel tokenizer over a 32-byte window {prev 16 | own 16}:
 // bit j <-> byte j.  E = end bytes (< 0x80), Z = zero bytes (markers),
@@ -721,7 +716,7 @@ __global__ void k_tile_order(const DecReg *__restrict__ regs, const int64_t *__r
     const DecReg &R = regs[r];
     if (R.ntiles == 0) return;
     int64_t k = pair_base[i];
-    const int nx = R.ntx, ny = R.nty3, nz = R.ntz3;
+    const int nx = R.tnx, ny = R.tny, nz = R.tnz;
     for (int tz = max(0, (int)d - (nx - 1) - (ny - 1)); tz <= min(nz - 1, (int)d); ++tz) {
         const int rem = (int)d - tz;
         for (int ty = max(0, rem - (nx - 1)); ty <= min(ny - 1, rem); ++ty) {
@@ -886,9 +881,21 @@ __global__ void __launch_bounds__(256) k_esc_rp(const DecReg *__restrict__ regs,
 
 __device__ __forceinline__ int64_t ld_cg64(const int64_t *p) { return __ldcg(p); }
 
-// the 3D wavefront: one CTA per 64x8x8 tile, taken in (region, tz, ty, tx)
-// order from an atomic ticket; waits for the x-, y-, z-neighbour's faces.
-constexpr int TBUF = 64 * 352;  // staged token bytes of the tile's 64 row pieces
+// the 3D wavefront: one CTA per tile of <= 65 x 9 x 9 samples (64/8/8 plus
+// the region's trailing ghost sample in the last tile of each axis), taken in
+// wavefront-diagonal order from an atomic ticket; waits for the x-, y- and
+// z-neighbour's published faces.
+constexpr int TXM = 65, TYM = 9, TZM = 9;          // tile capacity
+constexpr int FXN = (TZM + 1) * (TYM + 1);         // S(x1-1, y0-1..y1-1, z0-1..z1-1)
+constexpr int FYN = (TZM + 1) * TXM;               // S(x0..x1-1, y1-1, z0-1..z1-1)
+constexpr int FZN = TYM * TXM;                     // S(x0..x1-1, y0..y1-1, z1-1)
+constexpr int FACE_N = FXN + FYN + FZN;
+constexpr int SEGW = 11;                           // row segments per warp (81 / 8)
+constexpr int UNITS_W = 256;                       // units per warp (>= 11 * 22)
+
+__device__ __forceinline__ int tile_lo(int t, int step) { return t * step; }
+__device__ __forceinline__ int tile_hi(int t, int nt, int step, int ext) { return t == nt - 1 ? ext : (t + 1) * step; }
+
 __global__ void __launch_bounds__(256) k_lorenzo3d(const DecReg *__restrict__ regs,
                                                    const int32_t *__restrict__ tile_reg,
                                                    const uint8_t *__restrict__ blob,
@@ -899,14 +906,15 @@ __global__ void __launch_bounds__(256) k_lorenzo3d(const DecReg *__restrict__ re
                                                    unsigned long long *__restrict__ ticket,
                                                    const int32_t *__restrict__ order,
                                                    double *__restrict__ out) {
-    __shared__ int64_t S[LZ][LY][LX];
-    __shared__ int64_t Fx[LZ + 1][LY + 1];
-    __shared__ int64_t Fy[LZ + 1][LX];
-    __shared__ int64_t Fz[LY][LX];
-    extern __shared__ __align__(16) uint8_t tb[];  // TBUF bytes
-    __shared__ int32_t roff[64], rlen[64];
-    __shared__ int64_t rb0[64];
-    __shared__ int32_t rskip[64];
+    extern __shared__ __align__(16) int64_t dyn_s[];  // S[TZM][TYM][TXM]
+    int64_t(*S)[TYM][TXM] = reinterpret_cast<int64_t(*)[TYM][TXM]>(dyn_s);
+    __shared__ int64_t Fx[TZM + 1][TYM + 1];
+    __shared__ int64_t Fy[TZM + 1][TXM];
+    __shared__ int64_t Fz[TYM][TXM];
+    __shared__ int64_t Ayz[TZM][TYM];
+    __shared__ int64_t ucnt[8][UNITS_W];
+    __shared__ int64_t sg_lo[8][SEGW], sg_hi[8][SEGW], sg_ub[8][SEGW], sg_skip[8][SEGW];
+    __shared__ int32_t sg_base[8][SEGW + 1];
     __shared__ int64_t s_item;
     if (threadIdx.x == 0) s_item = order[atomicAdd(ticket, 1ull)];
     __syncthreads();
@@ -914,109 +922,108 @@ __global__ void __launch_bounds__(256) k_lorenzo3d(const DecReg *__restrict__ re
     const DecReg &R = regs[tile_reg[tile]];
     if (!((R.codec == 1 || R.codec == 2) && R.err == 0 && !R.slow)) return;
     const int64_t local = tile - R.tile_base;
-    const int tx = (int)(local % R.ntx);
-    const int64_t l2 = local / R.ntx;
-    const int ty = (int)(l2 % R.nty3), tz = (int)(l2 / R.nty3);
-    const int x0 = tx * LX, y0 = ty * LY, z0 = tz * LZ;
-    const int nxv = min(LX, R.ex - x0), nyv = min(LY, R.ey - y0), nzv = min(LZ, R.ez - z0);
+    const int tx = (int)(local % R.tnx);
+    const int64_t l2 = local / R.tnx;
+    const int ty = (int)(l2 % R.tny), tz = (int)(l2 / R.tny);
+    const int x0 = tile_lo(tx, 64), x1 = tile_hi(tx, R.tnx, 64, R.ex);
+    const int y0 = tile_lo(ty, 8), y1 = tile_hi(ty, R.tny, 8, R.ey);
+    const int z0 = tile_lo(tz, 8), z1 = tile_hi(tz, R.tnz, 8, R.ez);
+    const int nxv = x1 - x0, nyv = y1 - y0, nzv = z1 - z0;
+    const int nrs = nyv * nzv;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t hi = (int64_t)(R.poff + R.plen);
     const int64_t rp_end = R.rp_base + R.nrp;
+    const int64_t nrows = (int64_t)R.ey * R.ez;
 
-    // ---- 0. stage the bytes of the 64 row pieces (piece j = zz*8 + yy) at
-    //         16-byte aligned shared-memory offsets
-    if (warp == 0) {
-        int32_t len[2];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int j = lane + 32 * h, zz = j >> 3, yy = j & 7;
-            len[h] = 0;
-            int64_t b0 = 0;
-            if (zz < nzv && yy < nyv) {
-                const int64_t p = R.rp_base + ((int64_t)(z0 + zz) * R.ey + (y0 + yy)) * R.ntx + tx;
-                b0 = rp_byte[p];
-                const int64_t b1 = p + 1 < rp_end ? min(hi, rp_byte[p + 1] + 11) : hi;
-                len[h] = (int32_t)min(b1 - b0, (int64_t)352);
-                rskip[j] = (int32_t)rp_skip[p];
-            }
-            rb0[j] = b0;
-            rlen[j] = len[h];
-        }
-        int32_t a = (len[0] + 15) & ~15, b = (len[1] + 15) & ~15;
-        const int32_t a0 = a, b0v = b;
-        for (int off = 1; off < 32; off <<= 1) {
-            const int32_t oa = __shfl_up_sync(0xFFFFFFFFu, a, off), ob = __shfl_up_sync(0xFFFFFFFFu, b, off);
-            if (lane >= off) {
-                a += oa;
-                b += ob;
-            }
-        }
-        b += __shfl_sync(0xFFFFFFFFu, a, 31);
-        roff[lane] = a - a0;
-        roff[lane + 32] = b - b0v;
-    }
     int64_t *Sf = &S[0][0][0];
-    for (int i = threadIdx.x; i < LX * LY * LZ; i += 256) Sf[i] = 0;
-    __syncthreads();
-    for (int j = warp; j < 64; j += 8) {
-        const int o = roff[j], L = rlen[j];
-        const int64_t b0 = rb0[j];
-        for (int i = lane; i < ((L + 15) & ~15); i += 32) tb[o + i] = i < L ? __ldg(blob + b0 + i) : 0x80;
+    for (int i = threadIdx.x; i < TZM * TYM * TXM; i += 256) Sf[i] = 0;
+    // ---- 1. tokens -> q.  Warp w owns row segments rs = w, w+8, ... (rs = zz*nyv + yy);
+    //         its units (16 aligned bytes) are spread over all 32 lanes.
+    const int nseg = nrs > warp ? (nrs - warp + 7) >> 3 : 0;
+    {
+        int nun = 0;
+        if (lane < nseg) {
+            const int rs = warp + 8 * lane, zz = rs / nyv, yy = rs - zz * nyv;
+            const int64_t row = (int64_t)(z0 + zz) * R.ey + (y0 + yy);
+            const int64_t p = R.rp_base + row * R.ntx + (x0 >> 6);
+            const int64_t b0 = rp_byte[p];
+            const int64_t pe = x1 < R.ex ? R.rp_base + row * R.ntx + (x1 >> 6)
+                                         : (row + 1 < nrows ? R.rp_base + (row + 1) * R.ntx : rp_end);
+            const int64_t b1 = pe < rp_end ? min(hi, rp_byte[pe] + 11) : hi;
+            const int64_t ub = R.abase + ((b0 - R.abase) & ~15ll);
+            sg_lo[warp][lane] = b0;
+            sg_hi[warp][lane] = b1;
+            sg_ub[warp][lane] = ub;
+            sg_skip[warp][lane] = rp_skip[p];
+            nun = (int)((b1 - ub + 15) >> 4);
+        }
+        int inc = nun;
+        for (int off = 1; off < 32; off <<= 1) {
+            const int o = __shfl_up_sync(0xFFFFFFFFu, inc, off);
+            if (lane >= off) inc += o;
+        }
+        if (lane < nseg) sg_base[warp][lane] = inc - nun;
+        if (lane == 31) sg_base[warp][nseg] = inc;
     }
-    __syncthreads();
-    // ---- 1. tokens -> q, bit-parallel per 16-byte unit (one unit per lane)
-    if (warp < nyv) {
-        for (int zz = 0; zz < nzv; ++zz) {
-            const int j = zz * 8 + warp;
-            const uint8_t *bb = tb + roff[j];
-            const int len = rlen[j];
-            const int nunits = (len + 15) >> 4;
-            int64_t cnt = 0;
-            UnitMasks m;
-            m.lit = m.len = 0;
-            m.E = 0;
-            if (lane < nunits) {
-                uint32_t w[8];
-                const uint4 cur = *reinterpret_cast<const uint4 *>(bb + 16 * lane);
-                const uint4 prv = lane ? *reinterpret_cast<const uint4 *>(bb + 16 * (lane - 1)) : make_uint4(0, 0, 0, 0);
-                w[0] = prv.x; w[1] = prv.y; w[2] = prv.z; w[3] = prv.w;
-                w[4] = cur.x; w[5] = cur.y; w[6] = cur.z; w[7] = cur.w;
-                m = unit_masks(w, 16 * lane, 0, len);
-                cnt = __popc(m.lit);
-                uint32_t L = m.len;
-                while (L) {
-                    const int e = __ffs(L) - 1;
-                    L &= L - 1;
-                    cnt += (int64_t)token_value(m.E, e, [&](int k) { return (uint32_t)bb[16 * lane - 16 + k]; });
-                }
+    __syncwarp();
+    const int U = nseg ? sg_base[warp][nseg] : 0;
+    for (int g = lane; g < U; g += 32) {
+        int i = 0;
+        while (i + 1 < nseg && sg_base[warp][i + 1] <= g) ++i;
+        const int64_t u0 = sg_ub[warp][i] + 16 * (int64_t)(g - sg_base[warp][i]);
+        uint32_t w[8];
+        load_units(blob, u0, w);
+        const UnitMasks m = unit_masks(w, u0, sg_lo[warp][i], sg_hi[warp][i]);
+        ucnt[warp][g] = unit_count(m, blob, u0);
+    }
+    __syncwarp();
+    if (lane < nseg) {  // exclusive scan of the segment's unit counts, minus the skip
+        int64_t acc = -sg_skip[warp][lane];
+        for (int g = sg_base[warp][lane]; g < sg_base[warp][lane + 1]; ++g) {
+            const int64_t t = ucnt[warp][g];
+            ucnt[warp][g] = acc;
+            acc += t;
+        }
+    }
+    __syncwarp();
+    __syncthreads();  // S zeroed
+    for (int g = lane; g < U; g += 32) {
+        int i = 0;
+        while (i + 1 < nseg && sg_base[warp][i + 1] <= g) ++i;
+        int64_t at = ucnt[warp][g];
+        if (at >= nxv) continue;
+        const int rs = warp + 8 * i, zz = rs / nyv, yy = rs - zz * nyv;
+        const int64_t u0 = sg_ub[warp][i] + 16 * (int64_t)(g - sg_base[warp][i]);
+        uint32_t w[8];
+        load_units(blob, u0, w);
+        const UnitMasks m = unit_masks(w, u0, sg_lo[warp][i], sg_hi[warp][i]);
+        uint32_t T = m.lit | m.len;
+        int64_t *srow = &S[zz][yy][0];
+        while (T && at < nxv) {
+            const int e = __ffs(T) - 1;
+            T &= T - 1;
+            uint64_t v;
+            if ((m.E >> (e - 1)) & 1u) {  // one-byte token (the common case)
+                v = __ldg(blob + u0 - 16 + e) & 0x7Fu;
+            } else {
+                v = token_value(m.E, e, [&](int k) { return (uint32_t)__ldg(blob + u0 - 16 + k); });
             }
-            int64_t inc = cnt;
-            for (int off = 1; off < 32; off <<= 1) {
-                const int64_t o = __shfl_up_sync(0xFFFFFFFFu, inc, off);
-                if (lane >= off) inc += o;
-            }
-            int64_t at = inc - cnt - rskip[j];
-            uint32_t T = m.lit | m.len;
-            while (T && at < nxv) {
-                const int e = __ffs(T) - 1;
-                T &= T - 1;
-                const uint64_t v = token_value(m.E, e, [&](int k) { return (uint32_t)bb[16 * lane - 16 + k]; });
-                if ((m.len >> e) & 1u) {
-                    at += (int64_t)v;
-                } else {
-                    if (at >= 0) {
-                        const uint64_t zz2 = v - 1;
-                        S[zz][warp][at] = (int64_t)(zz2 >> 1) ^ -(int64_t)(zz2 & 1);
-                    }
-                    ++at;
+            if ((m.len >> e) & 1u) {
+                at += (int64_t)v;
+            } else {
+                if (at >= 0) {
+                    const uint64_t zz2 = v - 1;
+                    srow[at] = (int64_t)(zz2 >> 1) ^ -(int64_t)(zz2 & 1);
                 }
+                ++at;
             }
         }
     }
     __syncthreads();
-    // ---- 2. local 3D prefix: x (warp per row), y, z
-    for (int r = warp; r < LZ * LY; r += 8) {
-        int64_t *row = &S[r >> 3][r & 7][0];
+    // ---- 2. local 3D prefix: x (warp per row: x = lane, lane+32, 64), y, z
+    for (int r = warp; r < nrs; r += 8) {
+        const int zz = r / nyv, yy = r - zz * nyv;
+        int64_t *row = &S[zz][yy][0];
         int64_t a = row[lane], b = row[lane + 32];
         for (int off = 1; off < 32; off <<= 1) {
             const int64_t oa = __shfl_up_sync(0xFFFFFFFFu, a, off);
@@ -1027,68 +1034,78 @@ __global__ void __launch_bounds__(256) k_lorenzo3d(const DecReg *__restrict__ re
             }
         }
         b += __shfl_sync(0xFFFFFFFFu, a, 31);
+        const int64_t tot = __shfl_sync(0xFFFFFFFFu, b, 31);
         row[lane] = a;
         row[lane + 32] = b;
+        if (lane == 0) row[64] += tot;
     }
     __syncthreads();
-    for (int t = threadIdx.x; t < LZ * LX; t += 256) {
-        const int zz = t >> 6, x = t & 63;
+    for (int t = threadIdx.x; t < nzv * TXM; t += 256) {
+        const int zz = t / TXM, x = t - zz * TXM;
         int64_t acc = 0;
-#pragma unroll
-        for (int yy = 0; yy < LY; ++yy) {
+        for (int yy = 0; yy < nyv; ++yy) {
             acc += S[zz][yy][x];
             S[zz][yy][x] = acc;
         }
     }
     __syncthreads();
-    for (int t = threadIdx.x; t < LY * LX; t += 256) {
-        const int yy = t >> 6, x = t & 63;
+    for (int t = threadIdx.x; t < nyv * TXM; t += 256) {
+        const int yy = t / TXM, x = t - yy * TXM;
         int64_t acc = 0;
-#pragma unroll
-        for (int zz = 0; zz < LZ; ++zz) {
+        for (int zz = 0; zz < nzv; ++zz) {
             acc += S[zz][yy][x];
             S[zz][yy][x] = acc;
         }
     }
     // ---- 3. neighbour faces
     const int64_t nb_x = tx > 0 ? tile - 1 : -1;
-    const int64_t nb_y = ty > 0 ? tile - R.ntx : -1;
-    const int64_t nb_z = tz > 0 ? tile - (int64_t)R.ntx * R.nty3 : -1;
+    const int64_t nb_y = ty > 0 ? tile - R.tnx : -1;
+    const int64_t nb_z = tz > 0 ? tile - (int64_t)R.tnx * R.tny : -1;
     if (threadIdx.x == 0) {
         if (nb_x >= 0) while (ld_acquire32(tflag + nb_x) == 0) __nanosleep(20);
         if (nb_y >= 0) while (ld_acquire32(tflag + nb_y) == 0) __nanosleep(20);
         if (nb_z >= 0) while (ld_acquire32(tflag + nb_z) == 0) __nanosleep(20);
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < FACE_X; i += 256)
-        (&Fx[0][0])[i] = nb_x >= 0 ? ld_cg64(faces + nb_x * FACE_ALL + i) : 0;
-    for (int i = threadIdx.x; i < FACE_Y; i += 256)
-        (&Fy[0][0])[i] = nb_y >= 0 ? ld_cg64(faces + nb_y * FACE_ALL + FACE_X + i) : 0;
-    for (int i = threadIdx.x; i < FACE_Z; i += 256)
-        (&Fz[0][0])[i] = nb_z >= 0 ? ld_cg64(faces + nb_z * FACE_ALL + FACE_X + FACE_Y + i) : 0;
+    for (int i = threadIdx.x; i < FXN; i += 256) (&Fx[0][0])[i] = nb_x >= 0 ? ld_cg64(faces + nb_x * FACE_N + i) : 0;
+    for (int i = threadIdx.x; i < FYN; i += 256)
+        (&Fy[0][0])[i] = nb_y >= 0 ? ld_cg64(faces + nb_y * FACE_N + FXN + i) : 0;
+    for (int i = threadIdx.x; i < FZN; i += 256)
+        (&Fz[0][0])[i] = nb_z >= 0 ? ld_cg64(faces + nb_z * FACE_N + FXN + FYN + i) : 0;
     __syncthreads();
-    // ---- 4. S = T + inclusion-exclusion of the low faces
-    for (int i = threadIdx.x; i < LX * LY * LZ; i += 256) {
-        const int zz = i >> 9, yy = (i >> 6) & 7, x = i & 63;
-        Sf[i] += Fx[zz + 1][yy + 1] + Fy[zz + 1][x] + Fz[yy][x] - Fx[zz + 1][0] - Fx[0][yy + 1] - Fy[0][x] +
-                 Fx[0][0];
+    for (int i = threadIdx.x; i < TZM * TYM; i += 256) {
+        const int zz = i / TYM, yy = i - zz * TYM;
+        Ayz[zz][yy] = Fx[zz + 1][yy + 1] - Fx[zz + 1][0] - Fx[0][yy + 1] + Fx[0][0];
     }
     __syncthreads();
-    // ---- 5. publish this tile's high faces
-    int64_t *my = faces + tile * FACE_ALL;
-    for (int i = threadIdx.x; i < FACE_X; i += 256) {
-        const int zp = i / (LY + 1), yp = i % (LY + 1);
+    // ---- 4. S = T + A(y,z) + [Fy(x,z) - Fy(x,z0-1)] + Fz(x,y)
+    for (int i = threadIdx.x; i < nzv * nyv * TXM; i += 256) {
+        const int zz = i / (nyv * TXM), rem = i - zz * nyv * TXM, yy = rem / TXM, x = rem - yy * TXM;
+        S[zz][yy][x] += Ayz[zz][yy] + (Fy[zz + 1][x] - Fy[0][x]) + Fz[yy][x];
+    }
+    __syncthreads();
+    // ---- 5. publish this tile's high faces (consumers index with their own extents)
+    int64_t *my = faces + tile * FACE_N;
+    const int xl = nxv - 1;
+    for (int i = threadIdx.x; i < FXN; i += 256) {
+        const int zp = i / (TYM + 1), yp = i - zp * (TYM + 1);
+        if (zp > nzv || yp > nyv) continue;
         int64_t v;
-        if (zp == 0) v = yp == 0 ? Fy[0][LX - 1] : Fz[yp - 1][LX - 1];
-        else if (yp == 0) v = Fy[zp][LX - 1];
-        else v = S[zp - 1][yp - 1][LX - 1];
+        if (zp == 0) v = yp == 0 ? Fy[0][xl] : Fz[yp - 1][xl];
+        else if (yp == 0) v = Fy[zp][xl];
+        else v = S[zp - 1][yp - 1][xl];
         my[i] = v;
     }
-    for (int i = threadIdx.x; i < FACE_Y; i += 256) {
-        const int zp = i >> 6, x = i & 63;
-        my[FACE_X + i] = zp == 0 ? Fz[LY - 1][x] : S[zp - 1][LY - 1][x];
+    for (int i = threadIdx.x; i < FYN; i += 256) {
+        const int zp = i / TXM, x = i - zp * TXM;
+        if (zp > nzv || x >= nxv) continue;
+        my[FXN + i] = zp == 0 ? Fz[nyv - 1][x] : S[zp - 1][nyv - 1][x];
     }
-    for (int i = threadIdx.x; i < FACE_Z; i += 256) my[FACE_X + FACE_Y + i] = S[LZ - 1][i >> 6][i & 63];
+    for (int i = threadIdx.x; i < FZN; i += 256) {
+        const int yy = i / TXM, x = i - yy * TXM;
+        if (yy >= nyv || x >= nxv) continue;
+        my[FXN + FYN + i] = S[nzv - 1][yy][x];
+    }
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) st_release32(tflag + tile, 1);
@@ -1097,35 +1114,40 @@ __global__ void __launch_bounds__(256) k_lorenzo3d(const DecReg *__restrict__ re
     const bool esc = R.codec == 2 && R.nesc > 0;
     const uint8_t *bm = blob + R.poff;
     const uint8_t *ev = blob + R.poff + ((R.n + 7) >> 3);
-    for (int r = warp; r < LZ * LY; r += 8) {
-        const int zz = r >> 3, yy = r & 7;
-        if (zz >= nzv || yy >= nyv) continue;
-        const int64_t srow = ((int64_t)(z0 + zz) * R.ey + (y0 + yy)) * R.ex + x0;
+    for (int r = warp; r < nrs; r += 8) {
+        const int zz = r / nyv, yy = r - zz * nyv;
+        const int64_t rowi = (int64_t)(z0 + zz) * R.ey + (y0 + yy);
+        const int64_t srow = rowi * R.ex + x0;
         double *o = out + R.out_off + srow;
         uint64_t em = 0;
+        uint32_t em64 = 0;
         int64_t ebase = 0;
         if (esc) {
             const int sh = (int)(srow & 7);
-            const int64_t byte0 = srow >> 3;
+            const int64_t byte0 = srow >> 3, nbm = (R.n + 7) >> 3;
             uint32_t bt = 0;
-            if (lane < 9 && byte0 + lane < ((R.n + 7) >> 3)) bt = bm[byte0 + lane];
+            if (lane < 10 && byte0 + lane < nbm) bt = bm[byte0 + lane];
             uint64_t lo64 = 0;
             for (int k = 0; k < 8; ++k) lo64 |= (uint64_t)__shfl_sync(0xFFFFFFFFu, bt, k) << (8 * k);
-            const uint64_t b8 = __shfl_sync(0xFFFFFFFFu, bt, 8);
-            em = sh ? (lo64 >> sh) | (b8 << (64 - sh)) : lo64;
+            const uint64_t b8 = __shfl_sync(0xFFFFFFFFu, bt, 8), b9 = __shfl_sync(0xFFFFFFFFu, bt, 9);
+            const uint64_t hi16 = b8 | (b9 << 8);
+            em = sh ? (lo64 >> sh) | (hi16 << (64 - sh)) : lo64;
+            em64 = (uint32_t)((hi16 >> sh) & 1u);
             if (nxv < 64) em &= (1ull << nxv) - 1;
-            ebase = esc_rp[R.rp_base + ((int64_t)(z0 + zz) * R.ey + (y0 + yy)) * R.ntx + tx];
+            if (nxv < 65) em64 = 0;
+            ebase = esc_rp[R.rp_base + rowi * R.ntx + (x0 >> 6)];
         }
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int x = lane + 32 * h;
-            if (x >= nxv) continue;
+        for (int x = lane; x < nxv; x += 32) {
             double v = (double)S[zz][yy][x] * twoe;
-            if (esc && ((em >> x) & 1)) {
-                const int64_t rank = ebase + __popcll((long long)(em & ((1ull << x) - 1)));
-                uint8_t tmp[8];
-                for (int k = 0; k < 8; ++k) tmp[k] = ev[8 * rank + k];
-                memcpy(&v, tmp, 8);
+            if (esc) {
+                const bool isesc = x < 64 ? ((em >> x) & 1) : em64;
+                if (isesc) {
+                    const int64_t rank = ebase + (x < 64 ? __popcll((long long)(em & ((1ull << x) - 1)))
+                                                         : __popcll((long long)em));
+                    uint8_t tmp[8];
+                    for (int k = 0; k < 8; ++k) tmp[k] = ev[8 * rank + k];
+                    memcpy(&v, tmp, 8);
+                }
             }
             o[x] = v;
         }
@@ -1185,9 +1207,12 @@ static bool dec_build(const chr_dec_region_t *h, int64_t n, uintptr_t blob, DecP
         R.seg_base = seg;
         R.item_base = item;
         R.carry_base = carry;
-        R.ntx = (int32_t)ceil_div(R.ex, LX);
-        R.nty3 = (int32_t)ceil_div(R.ey, LY);
-        R.ntz3 = (int32_t)ceil_div(R.ez, LZ);
+        R.ntx = (int32_t)ceil_div(R.ex, 64);
+        // tiles of 64 / 8 / 8 samples; the last one of each axis absorbs the
+        // trailing sample of 32k+1 extents (<= 65 / 9 / 9)
+        R.tnx = (int32_t)std::max<int64_t>(1, ceil_div(R.ex - 1, 64));
+        R.tny = (int32_t)std::max<int64_t>(1, ceil_div(R.ey - 1, 8));
+        R.tnz = (int32_t)std::max<int64_t>(1, ceil_div(R.ez - 1, 8));
         R.tile_base = tile;
         R.rp_base = rp;
         if (R.codec == 1 || R.codec == 2) {
@@ -1196,7 +1221,7 @@ static bool dec_build(const chr_dec_region_t *h, int64_t n, uintptr_t blob, DecP
             item += R.nyt;
             carry += (int64_t)R.nyt * R.ez * R.ex;
             pl.max_rows_ex = std::max(pl.max_rows_ex, R.rows * R.ex);
-            R.ntiles = (int64_t)R.ntx * R.nty3 * R.ntz3;
+            R.ntiles = (int64_t)R.tnx * R.tny * R.tnz;
             tile += R.ntiles;
             R.nrp = (int64_t)R.ntx * R.ey * R.ez;
             rp += R.nrp;
@@ -1211,7 +1236,7 @@ static bool dec_build(const chr_dec_region_t *h, int64_t n, uintptr_t blob, DecP
     // tiles per (diagonal, region) -> exclusive bases in diagonal-major order
     int64_t D = 0;
     for (const DecReg &R : pl.regs)
-        if (R.ntiles) D = std::max<int64_t>(D, (int64_t)R.ntx + R.nty3 + R.ntz3 - 2);
+        if (R.ntiles) D = std::max<int64_t>(D, (int64_t)R.tnx + R.tny + R.tnz - 2);
     pl.ndiag = pl.ntiles ? D + 1 : 0;
     pl.h_pair_base.assign((size_t)(pl.ndiag * n) + 1, 0);
     int64_t acc = 0;
@@ -1220,7 +1245,7 @@ static bool dec_build(const chr_dec_region_t *h, int64_t n, uintptr_t blob, DecP
             const DecReg &R = pl.regs[i];
             pl.h_pair_base[d * n + i] = acc;
             if (!R.ntiles) continue;
-            const int nx = R.ntx, ny = R.nty3, nz = R.ntz3;
+            const int nx = R.tnx, ny = R.tny, nz = R.tnz;
             for (int tz = std::max<int>(0, (int)d - (nx - 1) - (ny - 1)); tz <= std::min<int>(nz - 1, (int)d); ++tz) {
                 const int rem = (int)d - tz;
                 const int lo = std::max(0, rem - (nx - 1)), hi = std::min(ny - 1, rem);
@@ -1245,7 +1270,7 @@ static void dec_carve(DecPlan &pl, void *base, size_t cap) {
     pl.rp_byte = c.take<int64_t>(pl.nrp + 1);
     pl.rp_skip = c.take<int64_t>(pl.nrp + 1);
     pl.esc_rp = c.take<int64_t>(pl.nrp + 1);
-    pl.faces = c.take<int64_t>((size_t)pl.ntiles * FACE_ALL + 1);
+    pl.faces = c.take<int64_t>((size_t)pl.ntiles * FACE_N + 1);
     pl.tflag = c.take<int32_t>(pl.ntiles + 1);
     pl.chunk_reg = c.take<int32_t>(pl.nchunks + 1);
     pl.tile_reg = c.take<int32_t>(pl.ntiles + 1);
@@ -1344,9 +1369,10 @@ extern "C" int chr_decode_regions(const uint8_t *d_blob, const chr_dec_region_t 
             CHR_PROF("k_tile_order", st);
             k_tile_order<<<(unsigned)ceil_div(npairs, 256), 256, 0, st>>>(pl.d_regs, pl.pair_base, npairs, n, pl.order);
         }
-        CHR_CUDA_TRY(cudaFuncSetAttribute(k_lorenzo3d, cudaFuncAttributeMaxDynamicSharedMemorySize, TBUF));
+        const int smem3 = (int)(sizeof(int64_t) * TZM * TYM * TXM);
+        CHR_CUDA_TRY(cudaFuncSetAttribute(k_lorenzo3d, cudaFuncAttributeMaxDynamicSharedMemorySize, smem3));
         CHR_PROF("k_lorenzo3d", st);
-        k_lorenzo3d<<<(unsigned)pl.ntiles, 256, TBUF, st>>>(pl.d_regs, pl.tile_reg, d_blob, pl.rp_byte, pl.rp_skip, pl.esc_rp,
+        k_lorenzo3d<<<(unsigned)pl.ntiles, 256, smem3, st>>>(pl.d_regs, pl.tile_reg, d_blob, pl.rp_byte, pl.rp_skip, pl.esc_rp,
                                                          pl.faces, pl.tflag, pl.ticket3, pl.order, d_out);
     }
     if (pl.nitems > 0) {
