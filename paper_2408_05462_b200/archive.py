@@ -168,7 +168,8 @@ def build_chr(volume, candidates, block_size: int, accuracy: float = 1.0, bound_
         return _rebuild_with_plugin(vol, res, cands, block_size, codec)
     host = res.blob[: res.nbytes].cpu().numpy().tobytes()
     regions = _regions_from_device(res, host, cands, vol.source_dtype)
-    dev = {"blob": res.blob[: res.nbytes], "file": host}
+    # own copy: res.blob is reusable workspace; +16 slack for aligned word reads
+    dev = {"blob": res.blob[: min(res.blob.numel(), res.nbytes + 16)].clone(), "file": host}
     return CHRArchive(vol.dims, vol.spacing, vol.source_dtype, int(block_size), tuple(res.extra["vrange"]),
                       tuple(cands), regions, dev)
 
@@ -203,7 +204,7 @@ def _device_file(archive: CHRArchive):
     d = archive._device
     if d is not None and "blob" in d:
         return d["blob"]
-    blob = serialize(archive)
+    blob = serialize(archive) + bytes(16)  # slack for aligned word reads at the end
     t = torch.from_numpy(np.frombuffer(blob, dtype=np.uint8).copy()).to(_abi.device())
     if d is not None:
         d["blob"] = t

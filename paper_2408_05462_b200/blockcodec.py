@@ -126,9 +126,9 @@ def decompress_many(blocks) -> list[np.ndarray]:
     out: list[np.ndarray | None] = [None] * len(blocks)
     if builtin:
         sizes = [len(blocks[i].payload) for i in builtin]
-        staging = np.frombuffer(b"".join(blocks[i].payload for i in builtin), dtype=np.uint8)
-        dev = torch.from_numpy(staging.copy()).to(_abi.device()) if staging.size else torch.zeros(
-            1, dtype=torch.uint8, device=_abi.device())
+        # +16 bytes: the tokenizer reads whole aligned words around the last token
+        staging = np.frombuffer(b"".join(blocks[i].payload for i in builtin) + bytes(16), dtype=np.uint8)
+        dev = torch.from_numpy(staging.copy()).to(_abi.device())
         sel, off = [], 0
         for i, sz in zip(builtin, sizes):
             b = blocks[i]

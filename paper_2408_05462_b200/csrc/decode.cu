@@ -654,6 +654,25 @@ __device__ __forceinline__ UnitMasks unit_masks(const uint32_t (&w)[8], int64_t 
     return m;
 }
 
+// value of the token [s, e] (<= 5 bytes) at blob offset `p` (start byte):
+// two aligned 32-bit loads, branch-free 7-bit gather
+__device__ __forceinline__ uint64_t varint_at(const uint8_t *__restrict__ blob, int64_t p, int len) {
+    const uint8_t *a = blob + (p & ~3ll);
+    const uint32_t lo = __ldg(reinterpret_cast<const uint32_t *>(a));
+    const uint32_t hi = __ldg(reinterpret_cast<const uint32_t *>(a) + 1);
+    const uint64_t x = (((uint64_t)hi << 32) | lo) >> (8 * (p & 3));
+    uint64_t v = (x & 0x7Full) | ((x >> 1) & (0x7Full << 7)) | ((x >> 2) & (0x7Full << 14)) |
+                 ((x >> 3) & (0x7Full << 21)) | ((x >> 4) & (0x7Full << 28));
+    return v & ((1ull << (7 * len)) - 1);
+}
+
+// value of the token ending at bit `e` of the 32-byte window at u0 - 16
+__device__ __forceinline__ uint64_t unit_token_value(const uint8_t *__restrict__ blob, uint32_t E, int e, int64_t u0) {
+    const uint32_t below = E & ((1u << e) - 1u);
+    const int s = below ? 32 - __clz(below) : 0;
+    return varint_at(blob, u0 - 16 + s, e - s + 1);
+}
+
 // value of the token ending at bit `e` of a byte window read through `rd`
 template <typename RD>
 __device__ __forceinline__ uint64_t token_value(uint32_t E, int e, RD rd) {
@@ -685,7 +704,7 @@ __device__ __forceinline__ int64_t unit_count(const UnitMasks &m, const uint8_t 
     while (L) {
         const int e = __ffs(L) - 1;
         L &= L - 1;
-        c += (int64_t)token_value(m.E, e, [&](int k) { return (uint32_t)__ldg(blob + u0 - 16 + k); });
+        c += (int64_t)unit_token_value(blob, m.E, e, u0);
     }
     return c;
 }
@@ -817,7 +836,7 @@ __global__ void __launch_bounds__(DTHREADS) k_rp_locate(const DecReg *__restrict
             const uint32_t below = m.E & ((1u << e) - 1u);
             const int s = below ? 32 - __clz(below) : 0;
             if (isl) {
-                tc = (int64_t)token_value(m.E, e, [&](int k) { return (uint32_t)__ldg(blob + u0 - 16 + k); });
+                tc = (int64_t)unit_token_value(blob, m.E, e, u0);
                 sbyte = u0 - 16 + s - 1;  // the marker
             } else {
                 sbyte = u0 - 16 + s;
@@ -1006,7 +1025,7 @@ __global__ void __launch_bounds__(256) k_lorenzo3d(const DecReg *__restrict__ re
             if ((m.E >> (e - 1)) & 1u) {  // one-byte token (the common case)
                 v = __ldg(blob + u0 - 16 + e) & 0x7Fu;
             } else {
-                v = token_value(m.E, e, [&](int k) { return (uint32_t)__ldg(blob + u0 - 16 + k); });
+                v = unit_token_value(blob, m.E, e, u0);
             }
             if ((m.len >> e) & 1u) {
                 at += (int64_t)v;
@@ -1021,8 +1040,14 @@ __global__ void __launch_bounds__(256) k_lorenzo3d(const DecReg *__restrict__ re
     }
     __syncthreads();
     // ---- 2. local 3D prefix: x (warp per row: x = lane, lane+32, 64), y, z
+    int zz2 = warp / nyv, yy2 = warp - zz2 * nyv;
     for (int r = warp; r < nrs; r += 8) {
-        const int zz = r / nyv, yy = r - zz * nyv;
+        const int zz = zz2, yy = yy2;
+        yy2 += 8;
+        while (yy2 >= nyv) {
+            yy2 -= nyv;
+            ++zz2;
+        }
         int64_t *row = &S[zz][yy][0];
         int64_t a = row[lane], b = row[lane + 32];
         for (int off = 1; off < 32; off <<= 1) {
@@ -1079,9 +1104,17 @@ __global__ void __launch_bounds__(256) k_lorenzo3d(const DecReg *__restrict__ re
     }
     __syncthreads();
     // ---- 4. S = T + A(y,z) + [Fy(x,z) - Fy(x,z0-1)] + Fz(x,y)
-    for (int i = threadIdx.x; i < nzv * nyv * TXM; i += 256) {
-        const int zz = i / (nyv * TXM), rem = i - zz * nyv * TXM, yy = rem / TXM, x = rem - yy * TXM;
-        S[zz][yy][x] += Ayz[zz][yy] + (Fy[zz + 1][x] - Fy[0][x]) + Fz[yy][x];
+    {
+        int zz = warp / nyv, yy = warp - zz * nyv;
+        for (int r = warp; r < nrs; r += 8) {
+            const int64_t a = Ayz[zz][yy];
+            for (int x = lane; x < nxv; x += 32) S[zz][yy][x] += a + (Fy[zz + 1][x] - Fy[0][x]) + Fz[yy][x];
+            yy += 8;
+            while (yy >= nyv) {
+                yy -= nyv;
+                ++zz;
+            }
+        }
     }
     __syncthreads();
     // ---- 5. publish this tile's high faces (consumers index with their own extents)
@@ -1114,8 +1147,14 @@ __global__ void __launch_bounds__(256) k_lorenzo3d(const DecReg *__restrict__ re
     const bool esc = R.codec == 2 && R.nesc > 0;
     const uint8_t *bm = blob + R.poff;
     const uint8_t *ev = blob + R.poff + ((R.n + 7) >> 3);
+    int zz3 = warp / nyv, yy3 = warp - zz3 * nyv;
     for (int r = warp; r < nrs; r += 8) {
-        const int zz = r / nyv, yy = r - zz * nyv;
+        const int zz = zz3, yy = yy3;
+        yy3 += 8;
+        while (yy3 >= nyv) {
+            yy3 -= nyv;
+            ++zz3;
+        }
         const int64_t rowi = (int64_t)(z0 + zz) * R.ey + (y0 + yy);
         const int64_t srow = rowi * R.ex + x0;
         double *o = out + R.out_off + srow;
@@ -1238,19 +1277,29 @@ static bool dec_build(const chr_dec_region_t *h, int64_t n, uintptr_t blob, DecP
     for (const DecReg &R : pl.regs)
         if (R.ntiles) D = std::max<int64_t>(D, (int64_t)R.tnx + R.tny + R.tnz - 2);
     pl.ndiag = pl.ntiles ? D + 1 : 0;
+    std::vector<int64_t> cnt((size_t)(pl.ndiag * n) + 1, 0);  // [r][d]
+    std::vector<int64_t> diff((size_t)pl.ndiag + 2);
+    for (int64_t i = 0; i < n; ++i) {
+        const DecReg &R = pl.regs[i];
+        if (!R.ntiles) continue;
+        std::fill(diff.begin(), diff.end(), 0);
+        for (int tz = 0; tz < R.tnz; ++tz)
+            for (int ty = 0; ty < R.tny; ++ty) {
+                diff[ty + tz] += 1;
+                diff[ty + tz + R.tnx] -= 1;
+            }
+        int64_t run = 0;
+        for (int64_t d = 0; d < pl.ndiag; ++d) {
+            run += diff[d];
+            cnt[i * pl.ndiag + d] = run;
+        }
+    }
     pl.h_pair_base.assign((size_t)(pl.ndiag * n) + 1, 0);
     int64_t acc = 0;
     for (int64_t d = 0; d < pl.ndiag; ++d)
         for (int64_t i = 0; i < n; ++i) {
-            const DecReg &R = pl.regs[i];
             pl.h_pair_base[d * n + i] = acc;
-            if (!R.ntiles) continue;
-            const int nx = R.tnx, ny = R.tny, nz = R.tnz;
-            for (int tz = std::max<int>(0, (int)d - (nx - 1) - (ny - 1)); tz <= std::min<int>(nz - 1, (int)d); ++tz) {
-                const int rem = (int)d - tz;
-                const int lo = std::max(0, rem - (nx - 1)), hi = std::min(ny - 1, rem);
-                if (hi >= lo) acc += hi - lo + 1;
-            }
+            acc += cnt[i * pl.ndiag + d];
         }
     return true;
 }

@@ -121,7 +121,7 @@ __device__ __forceinline__ bool not_f32_exact(T v) {
 
 // ------------------------------------------------------------------ tiles
 template <typename T, bool EMIT>
-__global__ void __launch_bounds__(NW * 32) k_tile(const T *__restrict__ vol, const EncParams *__restrict__ P,
+__global__ void __launch_bounds__(NW * 32, 5) k_tile(const T *__restrict__ vol, const EncParams *__restrict__ P,
                                                   const RegDev *__restrict__ regs,
                                                   PieceRec *__restrict__ recs,
                                                   const PieceOff *__restrict__ poffs,

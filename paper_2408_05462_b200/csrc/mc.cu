@@ -220,30 +220,66 @@ __global__ void __launch_bounds__(256) k_mc_reduce(const McPieceCnt *__restrict_
     }
 }
 
-// one thread: per grid chunk prefixes + grid totals + merged grid bases
-__global__ void k_mc_grids(McGrid *__restrict__ G, int64_t ng, McPieceBase *__restrict__ chunk,
-                           int64_t *__restrict__ totals) {
-    if (blockIdx.x || threadIdx.x) return;
-    int64_t gt = 0, gv = 0;
-    for (int64_t i = 0; i < ng; ++i) {
-        McGrid &g = G[i];
-        int64_t t = 0, v = 0;
-        for (int64_t c = g.chunk_base; c < g.chunk_base + g.nchunks; ++c) {
-            const McPieceBase x = chunk[c];
-            chunk[c].tri = t;
-            chunk[c].vert = v;
-            t += x.tri;
-            v += x.vert;
-        }
-        g.ntri = t;
-        g.nvert = v;
-        g.tri_base = gt;
-        g.vert_base = gv;
-        gt += t;
-        gv += v;
+// per grid: exclusive chunk prefixes + grid totals (thread per grid)
+__global__ void k_mc_grid_scan(McGrid *__restrict__ G, int64_t ng, McPieceBase *__restrict__ chunk) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= ng) return;
+    McGrid &g = G[i];
+    int64_t t = 0, v = 0;
+    for (int64_t c = g.chunk_base; c < g.chunk_base + g.nchunks; ++c) {
+        const McPieceBase x = chunk[c];
+        chunk[c].tri = t;
+        chunk[c].vert = v;
+        t += x.tri;
+        v += x.vert;
     }
-    totals[0] = gt;
-    totals[1] = gv;
+    g.ntri = t;
+    g.nvert = v;
+}
+
+// one CTA: merged-mesh bases of every grid (exclusive scan over grids)
+__global__ void __launch_bounds__(1024) k_mc_grids(McGrid *__restrict__ G, int64_t ng, int64_t *__restrict__ totals) {
+    __shared__ int64_t st[32], sv[32];
+    __shared__ int64_t ct, cv;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) ct = cv = 0;
+    __syncthreads();
+    for (int64_t b = 0; b < ng; b += 1024) {
+        const int64_t i = b + threadIdx.x;
+        const int64_t t = i < ng ? G[i].ntri : 0, v = i < ng ? G[i].nvert : 0;
+        int64_t it = t, iv = v;
+        for (int off = 1; off < 32; off <<= 1) {
+            const int64_t a = __shfl_up_sync(0xFFFFFFFFu, it, off), c = __shfl_up_sync(0xFFFFFFFFu, iv, off);
+            if (lane >= off) {
+                it += a;
+                iv += c;
+            }
+        }
+        if (lane == 31) {
+            st[warp] = it;
+            sv[warp] = iv;
+        }
+        __syncthreads();
+        int64_t pt = ct, pv = cv;
+        for (int w = 0; w < warp; ++w) {
+            pt += st[w];
+            pv += sv[w];
+        }
+        if (i < ng) {
+            G[i].tri_base = pt + it - t;
+            G[i].vert_base = pv + iv - v;
+        }
+        __syncthreads();
+        if (threadIdx.x == 1023) {
+            ct = pt + it;
+            cv = pv + iv;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        totals[0] = ct;
+        totals[1] = cv;
+    }
 }
 
 __global__ void __launch_bounds__(256) k_mc_down(const McPieceCnt *__restrict__ cnt,
@@ -441,6 +477,325 @@ __global__ void __launch_bounds__(MNW * 32) k_mc_emit(const double *__restrict__
     }
 }
 
+// ------------------------------------------------------------------ v2 tiles
+// CTA = 64 cells x 8 cell rows, marching z over up to MZC cell planes.  Every
+// f64 sample row is loaded once per plane by one warp (coalesced), turned
+// into an inside mask with ballots, and the Bourke code of a cell is
+// assembled from four 64-bit row masks (rows y, y+1 at planes z, z+1).
+__global__ void k_mc_fill_map(const McGrid *__restrict__ G, int64_t ng, int32_t *__restrict__ item_grid) {
+    const int64_t i = blockIdx.x;
+    if (i >= ng) return;
+    const McGrid &g = G[i];
+    const int64_t nit = (int64_t)g.ntx * ((g.ncy + MTY - 1) / MTY) * ((g.ncz + MZC - 1) / MZC);
+    for (int64_t t = threadIdx.x; t < nit; t += blockDim.x) item_grid[g.item_base + t] = (int32_t)i;
+}
+
+// bits c and c+1 of a (lo | hi << 64) mask
+__device__ __forceinline__ uint32_t bit_at(uint64_t lo, uint32_t hi, int c) {
+    return c < 64 ? (uint32_t)(lo >> c) & 1u : (hi >> (c - 64)) & 1u;
+}
+
+// bits (c, c+1) of the 65/66-bit mask (lo | hi << 64) as a 2-bit pair
+__device__ __forceinline__ uint32_t pair_at(uint64_t lo, uint32_t hi, int c) {
+    const uint32_t a = (uint32_t)lo, b = (uint32_t)(lo >> 32);
+    if (c < 32) return __funnelshift_r(a, b, c) & 3u;
+    if (c < 64) return __funnelshift_r(b, hi, c - 32) & 3u;
+    return (hi >> (c - 64)) & 3u;
+}
+__device__ __forceinline__ uint32_t pair_swap(uint32_t p) { return ((p * 5u) >> 1) & 3u; }
+
+// Bourke code from the four row masks: bits (c,c+1) of rows y,z / y+1,z / y,z+1 / y+1,z+1
+__device__ __forceinline__ int code_fast(uint64_t m00, uint32_t h00, uint64_t m10, uint32_t h10, uint64_t m01,
+                                         uint32_t h01, uint64_t m11, uint32_t h11, int c) {
+    return (int)(pair_at(m00, h00, c) | pair_swap(pair_at(m10, h10, c)) << 2 | pair_at(m01, h01, c) << 4 |
+                 pair_swap(pair_at(m11, h11, c)) << 6);
+}
+
+__device__ __forceinline__ int code_from(uint64_t m00, uint32_t h00, uint64_t m10, uint32_t h10, uint64_t m01,
+                                         uint32_t h01, uint64_t m11, uint32_t h11, int c) {
+    // Bourke corners: 0(0,0,0) 1(1,0,0) 2(1,1,0) 3(0,1,0) 4(0,0,1) 5(1,0,1) 6(1,1,1) 7(0,1,1)
+    return (int)(bit_at(m00, h00, c) | bit_at(m00, h00, c + 1) << 1 | bit_at(m10, h10, c + 1) << 2 |
+                 bit_at(m10, h10, c) << 3 | bit_at(m01, h01, c) << 4 | bit_at(m01, h01, c + 1) << 5 |
+                 bit_at(m11, h11, c + 1) << 6 | bit_at(m11, h11, c) << 7);
+}
+
+__global__ void __launch_bounds__(288, 5) k_mc_count2(const double *__restrict__ grids, const McGrid *__restrict__ G,
+                                                   const int32_t *__restrict__ item_grid, double k,
+                                                   const McTables *__restrict__ T, McPieceCnt *__restrict__ cnt) {
+    __shared__ uint64_t mk[3][9];
+    __shared__ uint32_t mkx[3][9];
+    __shared__ uint8_t s_ntri[256];
+    __shared__ uint8_t s_own[256][8];
+    __shared__ McGrid g;
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) s_ntri[i] = T->ntri[i];
+    for (int i = threadIdx.x; i < 2048; i += blockDim.x) (&s_own[0][0])[i] = (&T->owncnt[0][0])[i];
+    const int64_t item = blockIdx.x;
+    if (threadIdx.x == 0) g = G[item_grid[item]];
+    __syncthreads();
+    const int nyt = (g.ncy + MTY - 1) / MTY;
+    const int64_t local = item - g.item_base;
+    const int xt = (int)(local % g.ntx);
+    const int64_t r2 = local / g.ntx;
+    const int yt = (int)(r2 % nyt), zc = (int)(r2 / nyt);
+    const int x0 = xt * MTX, y0 = yt * MTY, z0 = zc * MZC;
+    const int z1 = min(z0 + MZC, g.ncz);
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int sy = y0 + w;
+    const bool rowok = sy < g.ny;
+    const double *gp = grids + g.goff;
+    const int64_t nxy = (int64_t)g.nx * g.ny;
+    const int xa = x0 + lane, xb = x0 + 32 + lane, xe = x0 + 64;
+    const bool oka = rowok && xa < g.nx, okb = rowok && xb < g.nx, oke = rowok && lane == 0 && xe < g.nx;
+    double ca = 0.0, cb2 = 0.0, ce = 0.0;  // plane p (prefetched)
+    {
+        const double *row = gp + (int64_t)z0 * nxy + (int64_t)sy * g.nx;
+        if (oka) ca = __ldg(row + xa);
+        if (okb) cb2 = __ldg(row + xb);
+        if (oke) ce = __ldg(row + xe);
+    }
+    for (int p = z0; p <= z1; ++p) {
+        const bool ia = oka && ca >= k;
+        const bool ib = okb && cb2 >= k;
+        const bool ie = oke && ce >= k;
+        if (p < z1) {  // prefetch plane p+1
+            const double *row = gp + (int64_t)(p + 1) * nxy + (int64_t)sy * g.nx;
+            if (oka) ca = __ldg(row + xa);
+            if (okb) cb2 = __ldg(row + xb);
+            if (oke) ce = __ldg(row + xe);
+        }
+        const uint64_t m = (uint64_t)__ballot_sync(0xFFFFFFFFu, ia) | ((uint64_t)__ballot_sync(0xFFFFFFFFu, ib) << 32);
+        if (lane == 0) {
+            mk[p % 3][w] = m;
+            mkx[p % 3][w] = ie ? 1u : 0u;
+        }
+        __syncthreads();
+        if (p == z0 || w >= MTY) continue;
+        const int cz = p - 1, cy = y0 + w;
+        if (cy >= g.ncy) continue;
+        const int b0 = cz % 3, b1 = p % 3;
+        const uint64_t m00 = mk[b0][w], m10 = mk[b0][w + 1], m01 = mk[b1][w], m11 = mk[b1][w + 1];
+        const uint32_t h00 = mkx[b0][w], h10 = mkx[b0][w + 1], h01 = mkx[b1][w], h11 = mkx[b1][w + 1];
+        int t = 0, v = 0;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int c = lane + 32 * h;
+            if (x0 + c < g.ncx) {
+                const int code = code_fast(m00, h00, m10, h10, m01, h01, m11, h11, c);
+                t += s_ntri[code];
+                v += s_own[code][bflags(x0 + c, cy, cz)];
+            }
+        }
+        t = __reduce_add_sync(0xFFFFFFFFu, t);
+        v = __reduce_add_sync(0xFFFFFFFFu, v);
+        if (lane == 0) {
+            McPieceCnt o;
+            o.tri = t;
+            o.vert = v;
+            cnt[g.piece_base + ((int64_t)cz * g.ncy + cy) * g.ntx + xt] = o;
+        }
+    }
+}
+
+// emit: samples rows y0-1..y0+8 x columns x0-1..x0+64 (66) per plane in a
+// 3-deep ring; cells rows y0-1..y0+7 x columns x0-1..x0+63 (65) with their
+// (code, vertex base) in a 3-deep ring, so every owner is local.
+constexpr int EW = 10;  // warps: sample rows y0-1 .. y0+8
+__global__ void __launch_bounds__(EW * 32, 3) k_mc_emit2(const double *__restrict__ grids, const McGrid *__restrict__ G,
+                                                      const int32_t *__restrict__ item_grid, double k,
+                                                      const McTables *__restrict__ T,
+                                                      const McPieceBase *__restrict__ base,
+                                                      double *__restrict__ verts, int32_t *__restrict__ tris) {
+    __shared__ double sv[3][EW][66];
+    __shared__ uint64_t mk[3][EW];
+    __shared__ uint32_t mkx[3][EW];
+    __shared__ uint8_t sC[3][EW - 1][65];
+    __shared__ int64_t sV[3][EW - 1][65];
+    __shared__ int32_t sT[EW - 1][65];  // triangle offset of each cell within its piece
+    __shared__ int8_t s_tri[256][16];
+    __shared__ uint8_t s_ntri[256];
+    __shared__ uint8_t s_own[256][8];
+    __shared__ uint8_t s_eax[12], s_elow[12][3];
+    __shared__ int8_t s_eid[3][2][2][2];
+    __shared__ McGrid g;
+    for (int i = threadIdx.x; i < 4096; i += blockDim.x) (&s_tri[0][0])[i] = (&T->tri[0][0])[i];
+    if (threadIdx.x < 12) s_eax[threadIdx.x] = T->edge_axis[threadIdx.x];
+    if (threadIdx.x < 36) (&s_elow[0][0])[threadIdx.x] = (&T->edge_low[0][0])[threadIdx.x];
+    if (threadIdx.x < 24) (&s_eid[0][0][0][0])[threadIdx.x] = (&T->edge_id[0][0][0][0])[threadIdx.x];
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) s_ntri[i] = T->ntri[i];
+    for (int i = threadIdx.x; i < 2048; i += blockDim.x) (&s_own[0][0])[i] = (&T->owncnt[0][0])[i];
+    const int64_t item = blockIdx.x;
+    if (threadIdx.x == 0) g = G[item_grid[item]];
+    __syncthreads();
+    const int nyt = (g.ncy + MTY - 1) / MTY;
+    const int64_t local = item - g.item_base;
+    const int xt = (int)(local % g.ntx);
+    const int64_t r2 = local / g.ntx;
+    const int yt = (int)(r2 % nyt), zc = (int)(r2 / nyt);
+    const int x0 = xt * MTX, y0 = yt * MTY, z0 = zc * MZC;
+    const int z1 = min(z0 + MZC, g.ncz);
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const double *gp = grids + g.goff;
+    const int64_t nxy = (int64_t)g.nx * g.ny;
+    // sample row of this warp: y0 - 1 + w ; columns c <-> x = x0 - 1 + c
+    const int sy = y0 - 1 + w;
+    const bool srow = sy >= 0 && sy < g.ny;
+    const int xa = x0 - 1 + lane, xb = x0 + 31 + lane, xe = x0 + 63 + lane;  // c = lane, lane+32, 64+lane
+    const bool oka = srow && xa >= 0 && xa < g.nx, okb = srow && xb < g.nx, oke = srow && lane < 2 && xe < g.nx;
+    // cell row of this warp (w < 9): cy = y0 - 1 + w ; cells c = 1 + lane, 33 + lane, and c = 0 (lane 0)
+    const int cy = y0 - 1 + w;
+    const bool crow = w < EW - 1 && cy >= 0 && cy < g.ncy;
+    const int pstart = z0 > 0 ? z0 - 1 : 0;
+    double na = 0.0, nb = 0.0, ne = 0.0;  // prefetched plane
+    {
+        const double *row = gp + (int64_t)pstart * nxy + (int64_t)sy * g.nx;
+        if (oka) na = __ldg(row + xa);
+        if (okb) nb = __ldg(row + xb);
+        if (oke) ne = __ldg(row + xe);
+    }
+    for (int p = pstart; p <= z1; ++p) {
+        const int pb = p % 3;
+        {
+            const double va = na, vb = nb, ve = ne;
+            if (p < z1) {
+                const double *row = gp + (int64_t)(p + 1) * nxy + (int64_t)sy * g.nx;
+                if (oka) na = __ldg(row + xa);
+                if (okb) nb = __ldg(row + xb);
+                if (oke) ne = __ldg(row + xe);
+            }
+            sv[pb][w][lane] = va;
+            sv[pb][w][lane + 32] = vb;
+            if (lane < 2) sv[pb][w][64 + lane] = ve;
+            const uint64_t m = (uint64_t)__ballot_sync(0xFFFFFFFFu, oka && va >= k) |
+                               ((uint64_t)__ballot_sync(0xFFFFFFFFu, okb && vb >= k) << 32);
+            const uint32_t mx = __ballot_sync(0xFFFFFFFFu, oke && ve >= k) & 3u;
+            if (lane == 0) {
+                mk[pb][w] = m;
+                mkx[pb][w] = mx;
+            }
+        }
+        __syncthreads();
+        if (p == pstart) continue;  // need planes cz and cz+1
+        const int cz = p - 1, cb = cz % 3, qb = p % 3;
+        // ---- codes, owned counts, vertex bases of cell row cy at plane cz
+        int codeA = 0, codeB = 0, ntA = 0, ntB = 0, tA = 0, tB = 0;
+        McPieceBase pbase;
+        pbase.tri = 0;
+        pbase.vert = 0;
+        if (w < EW - 1) {
+            int codeH = 0, ownA = 0, ownB = 0, ownH = 0;
+            if (crow) {
+                const uint64_t m00 = mk[cb][w], m10 = mk[cb][w + 1], m01 = mk[qb][w], m11 = mk[qb][w + 1];
+                const uint32_t h00 = mkx[cb][w], h10 = mkx[cb][w + 1], h01 = mkx[qb][w], h11 = mkx[qb][w + 1];
+                const int xA = x0 + lane, xB = x0 + 32 + lane;
+                if (xA < g.ncx) {
+                    codeA = code_fast(m00, h00, m10, h10, m01, h01, m11, h11, lane + 1);
+                    ownA = s_own[codeA][bflags(xA, cy, cz)];
+                    ntA = s_ntri[codeA];
+                }
+                if (xB < g.ncx) {
+                    codeB = code_fast(m00, h00, m10, h10, m01, h01, m11, h11, lane + 33);
+                    ownB = s_own[codeB][bflags(xB, cy, cz)];
+                    ntB = s_ntri[codeB];
+                }
+                if (lane == 0 && x0 > 0) {
+                    codeH = code_fast(m00, h00, m10, h10, m01, h01, m11, h11, 0);
+                    ownH = s_own[codeH][bflags(x0 - 1, cy, cz)];
+                }
+                pbase = base[g.piece_base + ((int64_t)cz * g.ncy + cy) * g.ntx + xt];
+            }
+            int sA = ownA, sB = ownB;
+            tA = ntA;
+            tB = ntB;
+            for (int off = 1; off < 32; off <<= 1) {
+                const int a = __shfl_up_sync(0xFFFFFFFFu, sA, off), b = __shfl_up_sync(0xFFFFFFFFu, sB, off);
+                const int c = __shfl_up_sync(0xFFFFFFFFu, tA, off), d = __shfl_up_sync(0xFFFFFFFFu, tB, off);
+                if (lane >= off) {
+                    sA += a;
+                    sB += b;
+                    tA += c;
+                    tB += d;
+                }
+            }
+            const int totV = __shfl_sync(0xFFFFFFFFu, sA, 31);
+            const int totT = __shfl_sync(0xFFFFFFFFu, tA, 31);
+            tA -= ntA;
+            tB = tB - ntB + totT;
+            sC[cb][w][1 + lane] = (uint8_t)codeA;
+            sC[cb][w][33 + lane] = (uint8_t)codeB;
+            sV[cb][w][1 + lane] = pbase.vert + sA - ownA;
+            sV[cb][w][33 + lane] = pbase.vert + totV + sB - ownB;
+            if (lane == 0) {
+                sC[cb][w][0] = (uint8_t)codeH;
+                sV[cb][w][0] = pbase.vert - ownH;
+            }
+        }
+        __syncthreads();
+        if (cz < z0 || w == 0 || w >= EW - 1 || !crow) continue;
+        {
+            // ---- emission, warp-cooperative: two active cells per step, lanes
+            //      0..14 / 16..30 take triangle slots, then owned edges
+            sT[w][1 + lane] = tA;
+            sT[w][33 + lane] = tB;
+            __syncwarp();
+            uint64_t act = (uint64_t)__ballot_sync(0xFFFFFFFFu, ntA > 0) |
+                           ((uint64_t)__ballot_sync(0xFFFFFFFFu, ntB > 0) << 32);
+            const int half = lane >> 4, sl = lane & 15;
+            while (act) {
+                const int i0 = __ffsll((long long)act) - 1;
+                act &= act - 1;
+                int i1 = -1;
+                if (act) {
+                    i1 = __ffsll((long long)act) - 1;
+                    act &= act - 1;
+                }
+                const int ci = half ? i1 : i0;
+                if (ci < 0) continue;
+                const int c = ci < 32 ? ci + 1 : ci + 1;  // cell column in the 65-wide ring (1..64)
+                const int cx = x0 + c - 1;
+                const int code = sC[cb][w][c];
+                const int nt = s_ntri[code];
+                const int f = bflags(cx, cy, cz);
+                const int64_t vb = sV[cb][w][c];
+                // triangle slot `sl`
+                if (sl < 3 * nt) {
+                    const int e = s_tri[code][sl];
+                    const int a = s_eax[e];
+                    int l0 = s_elow[e][0], l1 = s_elow[e][1], l2 = s_elow[e][2];
+                    int d0 = 0, d1 = 0, d2 = 0;
+                    if (a != 0 && l0 == 0 && cx >= 1) { d0 = -1; l0 = 1; }
+                    if (a != 1 && l1 == 0 && cy >= 1) { d1 = -1; l1 = 1; }
+                    if (a != 2 && l2 == 0 && cz >= 1) { d2 = -1; l2 = 1; }
+                    const int e2 = s_eid[a][l0][l1][l2];
+                    const int ob = (cz + d2 + 3) % 3;
+                    const int ocode = sC[ob][w + d1][c + d0];
+                    const int of = bflags(cx + d0, cy + d1, cz + d2);
+                    const int64_t vid = sV[ob][w + d1][c + d0] + __ldg(&T->rank[ocode][of][e2]);
+                    tris[3 * (g.tri_base + pbase.tri + sT[w][c]) + sl] = (int32_t)(g.vert_base + vid);
+                }
+                // owned edge `sl` (< 12): vertex
+                if (sl < 12) {
+                    const int e = sl;
+                    const int r = __ldg(&T->rank[code][f][e]);
+                    if (r >= 0) {
+                        const int a = s_eax[e];
+                        const int lx = s_elow[e][0], ly = s_elow[e][1], lz = s_elow[e][2];
+                        const double s0 = sv[(cz + lz) % 3][w + ly][c + lx];
+                        const double s1 = sv[(cz + lz + (a == 2)) % 3][w + ly + (a == 1)][c + lx + (a == 0)];
+                        const double den = __dadd_rn(s1, -s0);
+                        const double t = den == 0.0 ? 0.0 : __ddiv_rn(__dadd_rn(k, -s0), den);
+                        double lat[3] = {(double)(cx + lx), (double)(cy + ly), (double)(cz + lz)};
+                        lat[a] = __dadd_rn(lat[a], t);
+                        double *o = verts + 3 * (g.vert_base + vb + r);
+                        o[0] = world(g.origin[0], lat[0], g.spacing[0]);
+                        o[1] = world(g.origin[1], lat[1], g.spacing[1]);
+                        o[2] = world(g.origin[2], lat[2], g.spacing[2]);
+                    }
+                }
+            }
+        }
+    }
+}
+
 __global__ void k_case_codes(const double *__restrict__ g, int64_t nx, int64_t ny, int64_t nz, double k,
                              int binary, uint8_t *__restrict__ codes) {
     const int64_t ncx = nx - 1, ncy = ny - 1, ncz = nz - 1;
@@ -467,6 +822,7 @@ struct McPlan {
     McPieceCnt *cnt;
     McPieceBase *chunk, *base;
     int64_t *totals;
+    int32_t *item_grid;
 };
 
 static bool mc_build(const chr_mc_grid_t *h, int64_t n, McPlan &pl) {
@@ -510,6 +866,7 @@ static void mc_carve(McPlan &pl, void *base, size_t cap) {
     pl.chunk = c.take<McPieceBase>(pl.nchunks);
     pl.base = c.take<McPieceBase>(pl.npieces);
     pl.totals = c.take<int64_t>(2);
+    pl.item_grid = c.take<int32_t>(pl.nitems + 1);
     pl.ws = c.off + 256;
 }
 
@@ -542,18 +899,25 @@ extern "C" int chr_mc_count(const double *d_grids, const chr_mc_grid_t *h, int64
     if (!T) return CHR_E_CUDA;
     CHR_CUDA_TRY(cudaMemcpyAsync(pl.d_grids, pl.grids.data(), sizeof(McGrid) * n, cudaMemcpyHostToDevice, st));
     CHR_CUDA_TRY(cudaMemsetAsync(pl.cnt, 0, sizeof(McPieceCnt) * pl.npieces, st));
-    const int64_t blocks = std::min<int64_t>(ceil_div(pl.npieces, 8), 148 * 32);
     {
-        CHR_PROF("k_mc_count", st);
-        k_mc_count<<<(unsigned)blocks, 256, 0, st>>>(d_grids, pl.d_grids, n, pl.npieces, k, T, pl.cnt);
+        CHR_PROF("k_mc_fill_map", st);
+        k_mc_fill_map<<<(unsigned)n, 256, 0, st>>>(pl.d_grids, n, pl.item_grid);
+    }
+    if (pl.nitems > 0) {
+        CHR_PROF("k_mc_count2", st);
+        k_mc_count2<<<(unsigned)pl.nitems, 288, 0, st>>>(d_grids, pl.d_grids, pl.item_grid, k, T, pl.cnt);
     }
     {
         CHR_PROF("k_mc_reduce", st);
         k_mc_reduce<<<(unsigned)pl.nchunks, 256, 0, st>>>(pl.cnt, pl.chunk);
     }
     {
+        CHR_PROF("k_mc_grid_scan", st);
+        k_mc_grid_scan<<<(unsigned)ceil_div(n, 128), 128, 0, st>>>(pl.d_grids, n, pl.chunk);
+    }
+    {
         CHR_PROF("k_mc_grids", st);
-        k_mc_grids<<<1, 1, 0, st>>>(pl.d_grids, n, pl.chunk, pl.totals);
+        k_mc_grids<<<1, 1024, 0, st>>>(pl.d_grids, n, pl.totals);
     }
     {
         CHR_PROF("k_mc_down", st);
@@ -587,8 +951,9 @@ extern "C" int chr_mc_emit(const double *d_grids, const chr_mc_grid_t *h, int64_
     if (!T) return CHR_E_CUDA;
     if (pl.nitems > 0)
         {
-            CHR_PROF("k_mc_emit", st);
-            k_mc_emit<<<(unsigned)pl.nitems, MNW * 32, 0, st>>>(d_grids, pl.d_grids, n, k, T, pl.base, d_verts, d_tris);
+            CHR_PROF("k_mc_emit2", st);
+            k_mc_emit2<<<(unsigned)pl.nitems, EW * 32, 0, st>>>(d_grids, pl.d_grids, pl.item_grid, k, T, pl.base,
+                                                                 d_verts, d_tris);
         }
     CHR_CUDA_TRY(cudaGetLastError());
     CHR_CUDA_TRY(cudaStreamSynchronize(st));
