@@ -101,16 +101,6 @@ def make_input(cfg, n, rank, device):
     return vals, dims, bs, cands, r
 
 
-def sel_desc(res, ci):
-    from paper_2408_05462_b200 import device as D
-
-    recs = D.region_records(res.regions)
-    sel = [q for q in recs if (q["mask"] >> ci) & 1]
-    desc = [(q["block_offset"] + D.BLOCK_HEADER, q["block_nbytes"] - D.BLOCK_HEADER, q["codec"], q["extent"], q["e"],
-             q["crc"]) for q in sel]
-    return sel, desc
-
-
 def run_step(vol, dims, bs, cands, r, ws, spacing=(1.0, 1.0, 1.0), stage_events=None):
     """compress -> request -> extract, all device resident; returns sizes."""
     from paper_2408_05462_b200 import device as D
@@ -121,22 +111,23 @@ def run_step(vol, dims, bs, cands, r, ws, spacing=(1.0, 1.0, 1.0), stage_events=
     res = D.build_archive(vol, dims, cands, bs, loose_fraction=r, ws=ws)
     if ev:
         ev[1].record()
-    sel, desc = sel_desc(res, 0)
-    wins, offs, status = D.decode(res.blob, desc, ws=ws)
+    regs = res.regions
+    sel = regs[(regs["mask"] & np.uint64(1)) != 0]  # regions relevant to candidate 0
+    dec = D.dec_table(sel["block_offset"] + D.BLOCK_HEADER, sel["block_nbytes"] - D.BLOCK_HEADER,
+                      sel["codec_id"], sel["extent"], sel["error_bound"], sel["payload_crc"])
+    wins, offs, status = D.decode(res.blob, dec, ws=ws)
     assert not any(status), status
     if ev:
         ev[2].record()
-    grids = [(o, q["extent"], tuple(float(a) * s for a, s in zip(q["origin"], spacing)), spacing)
-             for q, o in zip(sel, offs)]
-    verts, tris, nt, nv = D.marching(wins, grids, cands[0], ws=ws)
+    mct = D.mc_table(dec["out_offset"], sel["extent"], sel["origin"] * np.asarray(spacing), spacing)
+    verts, tris, nt, nv = D.marching(wins, mct, cands[0], ws=ws)
     if ev:
         ev[3].record()
-    n_sel = sum(q["extent"][0] * q["extent"][1] * q["extent"][2] for q in sel)
-    cells = sum((q["extent"][0] - 1) * (q["extent"][1] - 1) * (q["extent"][2] - 1) for q in sel)
-    c_sel = sum(q["block_nbytes"] for q in sel)
-    return dict(res=res, wins=wins, verts=verts, tris=tris, n_sel=n_sel, cells=cells, c_sel=c_sel,
-                archive=res.nbytes, nreg=len(res.regions), nsel=len(sel), ntri=int(tris.shape[0]),
-                nvert=int(verts.shape[0]), payload=sum(q["block_nbytes"] for q in D.region_records(res.regions)))
+    ext = sel["extent"].astype(np.int64)
+    return dict(res=res, wins=wins, verts=verts, tris=tris, n_sel=int(np.prod(ext, axis=1).sum()),
+                cells=int(np.prod(ext - 1, axis=1).sum()), c_sel=int(sel["block_nbytes"].sum()),
+                archive=res.nbytes, nreg=len(regs), nsel=len(sel), ntri=int(tris.shape[0]),
+                nvert=int(verts.shape[0]), payload=int(regs["block_nbytes"].sum()))
 
 
 def kernel_bytes(name, info, N):

@@ -11,6 +11,7 @@ from __future__ import annotations
 import ctypes
 import os
 
+import numpy as np
 import torch
 
 from . import exceptions as errors
@@ -90,6 +91,23 @@ class McGrid(ctypes.Structure):
         ("origin", ctypes.c_double * 3),
         ("spacing", ctypes.c_double * 3),
     ]
+
+
+# numpy mirrors of the ABI structs (vectorised fill / read, no per-field ctypes)
+REGION_DT = np.dtype([("lo", "<i4", 3), ("hi", "<i4", 3), ("origin", "<i4", 3), ("extent", "<i4", 3),
+                      ("mask", "<u8"), ("error_bound", "<f8"), ("codec_id", "<i4"), ("payload_crc", "<u4"),
+                      ("block_offset", "<u8"), ("block_nbytes", "<u8"), ("n_escaped", "<u8")], align=True)
+DEC_DT = np.dtype([("payload_offset", "<u8"), ("payload_nbytes", "<u8"), ("codec_id", "<i4"), ("dims", "<i4", 3),
+                   ("error_bound", "<f8"), ("crc", "<u4"), ("_pad", "<u4"), ("out_offset", "<u8")], align=True)
+MCGRID_DT = np.dtype([("grid_offset", "<u8"), ("dims", "<i4", 3), ("_pad", "<i4"), ("origin", "<f8", 3),
+                      ("spacing", "<f8", 3)], align=True)
+assert REGION_DT.itemsize == ctypes.sizeof(Region)
+assert DEC_DT.itemsize == ctypes.sizeof(DecRegion)
+assert MCGRID_DT.itemsize == ctypes.sizeof(McGrid)
+
+
+def aptr(a: np.ndarray):
+    return ctypes.c_void_p(a.ctypes.data) if a.size else None
 
 
 _lib = None

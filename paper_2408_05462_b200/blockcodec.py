@@ -107,12 +107,9 @@ def compress(samples, error_bound: float, source_dtype: str = "f64") -> Compress
         if not bool(fin.all()):
             i = int(torch.argmin(fin.to(torch.uint8)))
             raise NonFiniteSampleError(i, float(vol[i]))
-    regs = (_abi.Region * 1)()
-    r = regs[0]
-    for a in range(3):
-        r.origin[a] = 0
-        r.extent[a] = dims[a]
-    r.error_bound = e
+    regs = np.zeros(1, dtype=_abi.REGION_DT)
+    regs["extent"][0] = dims
+    regs["error_bound"][0] = e
     res = device.compress(vol, dims, regs, source_dtype=source_dtype, write_file=False)
     blob = res.blob[: res.nbytes].cpu().numpy().tobytes()
     return CompressedBlock.from_bytes(blob, 0)

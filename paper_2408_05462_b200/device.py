@@ -69,17 +69,16 @@ def stats(vol: torch.Tensor, dims, bs: int, cands) -> tuple[torch.Tensor, torch.
 
 def plan(block_stats: np.ndarray, dims, bs, cands, vmin, vmax, loose_fraction=LOOSE_FRACTION,
          safety_factor=SAFETY_FACTOR):
-    """Regions (ctypes array of chr_region_t) from host block stats."""
+    """Regions (numpy array of chr_region_t, ``_abi.REGION_DT``) from host block stats."""
     cands = _cands_arr(cands)
     bsn = np.ascontiguousarray(block_stats, dtype=np.float64)
     nb = bsn.shape[0]
-    regs = (_abi.Region * nb)()
+    regs = np.zeros(nb, dtype=_abi.REGION_DT)
     nreg = ctypes.c_int64(0)
     check(lib().chr_plan(_np_ptr(bsn), *dims, bs, _np_ptr(cands), cands.size, float(vmin), float(vmax),
-                         float(loose_fraction), float(safety_factor), regs, ctypes.byref(nreg)), "chr_plan")
-    out = (_abi.Region * nreg.value)()
-    ctypes.memmove(out, regs, ctypes.sizeof(_abi.Region) * nreg.value)
-    return out
+                         float(loose_fraction), float(safety_factor), _abi.aptr(regs), ctypes.byref(nreg)),
+          "chr_plan")
+    return regs[: nreg.value].copy()
 
 
 @dataclass
@@ -88,7 +87,7 @@ class Compressed:
 
     blob: torch.Tensor  # uint8, first `nbytes` valid
     nbytes: int
-    regions: object  # ctypes array of chr_region_t (codec/offset/crc filled)
+    regions: np.ndarray  # _abi.REGION_DT (codec/offset/crc filled)
     source_dtype: str
     extra: dict = field(default_factory=dict)
 
@@ -126,20 +125,22 @@ def compress(vol: torch.Tensor, dims, regions, *, source_dtype="f32", write_file
     """Run chr_compress on `regions`; returns the device bytes."""
     ws = ws or _DEFAULT_WS
     L = lib()
+    regions = np.ascontiguousarray(regions, dtype=_abi.REGION_DT)
     nreg = len(regions)
+    rp = _abi.aptr(regions)
     cands = _cands_arr(cands)
     m = cands.size
-    wsz = L.chr_compress_workspace_size(regions, nreg)
+    wsz = L.chr_compress_workspace_size(rp, nreg)
     if wsz == 0:
         raise ParameterError("invalid regions for compress")
     work = ws.get("compress", wsz)
-    cap = int(L.chr_compress_capacity(regions, nreg, m, DTYPE_TAGS[source_dtype]))
+    cap = int(L.chr_compress_capacity(rp, nreg, m, DTYPE_TAGS[source_dtype]))
     if out is None or out.numel() < cap:
         out = ws.get("compress_out", cap)
     nbytes = ctypes.c_uint64(0)
     sp = (ctypes.c_double * 3)(*[float(s) for s in spacing])
     check(L.chr_compress(ptr(vol), _dtype_code(vol), DTYPE_TAGS[source_dtype], *dims, sp, int(bs),
-                         float(vrange[0]), float(vrange[1]), _np_ptr(cands), m, regions, nreg,
+                         float(vrange[0]), float(vrange[1]), _np_ptr(cands), m, rp, nreg,
                          1 if write_file else 0, ptr(work), work.numel(), ptr(out), out.numel(),
                          ctypes.byref(nbytes), stream_ptr()), "chr_compress")
     return Compressed(out, int(nbytes.value), regions, source_dtype)
@@ -184,74 +185,92 @@ def build_archive(vol: torch.Tensor, dims, cands, bs, *, spacing=(1.0, 1.0, 1.0)
     return res
 
 
+def dec_table(payload_offset, payload_nbytes, codec, dims, e, crc) -> np.ndarray:
+    """Vectorised chr_dec_region_t table (windows laid out back to back)."""
+    n = len(payload_offset)
+    t = np.zeros(n, dtype=_abi.DEC_DT)
+    t["payload_offset"] = payload_offset
+    t["payload_nbytes"] = payload_nbytes
+    t["codec_id"] = codec
+    t["dims"] = np.asarray(dims, dtype=np.int32).reshape(n, 3)
+    t["error_bound"] = e
+    t["crc"] = np.asarray(crc, dtype=np.uint64) & 0xFFFFFFFF
+    sizes = np.prod(t["dims"].astype(np.int64), axis=1)
+    t["out_offset"] = np.concatenate([[0], np.cumsum(sizes)[:-1]]) if n else []
+    return t
+
+
 def decode(blob: torch.Tensor, sel, ws: Workspaces | None = None, out: torch.Tensor | None = None):
     """Decode CompressedBlocks of `blob` (device uint8).
 
-    ``sel``: list of (payload_offset, payload_nbytes, codec_id, (ex,ey,ez), e, crc).
+    ``sel``: a ``_abi.DEC_DT`` table (see :func:`dec_table`) or a list of
+    (payload_offset, payload_nbytes, codec_id, (ex,ey,ez), e, crc).
     Returns (f64 device tensor of all windows concatenated, element offsets,
     per-region status codes)."""
     ws = ws or _DEFAULT_WS
     L = lib()
+    if not isinstance(sel, np.ndarray):
+        cols = list(zip(*sel)) if sel else [[], [], [], [], [], []]
+        sel = dec_table(*[np.asarray(c) for c in cols]) if sel else np.zeros(0, dtype=_abi.DEC_DT)
     n = len(sel)
-    regs = (_abi.DecRegion * max(n, 1))()
-    offs = []
-    total = 0
-    for i, (po, pn, cid, dims, e, crc) in enumerate(sel):
-        r = regs[i]
-        r.payload_offset = int(po)
-        r.payload_nbytes = int(pn)
-        r.codec_id = int(cid)
-        r.dims[0], r.dims[1], r.dims[2] = (int(d) for d in dims)
-        r.error_bound = float(e)
-        r.crc = int(crc) & 0xFFFFFFFF
-        r.out_offset = total
-        offs.append(total)
-        total += int(dims[0]) * int(dims[1]) * int(dims[2])
+    total = int((np.prod(sel["dims"].astype(np.int64), axis=1)).sum()) if n else 0
     if out is None or out.numel() < total:
         out = ws.get("decode_out", 8 * max(total, 1), torch.float64)
-    status = (ctypes.c_int32 * max(n, 1))()
+    status = np.zeros(max(n, 1), dtype=np.int32)
     if n:
-        wsz = L.chr_decode_workspace_size(regs, n)
+        sp = _abi.aptr(sel)
+        wsz = L.chr_decode_workspace_size(sp, n)
         work = ws.get("decode", wsz)
-        rc = L.chr_decode_regions(ptr(blob), regs, n, ptr(out), ptr(work), work.numel(), status, stream_ptr())
+        rc = L.chr_decode_regions(ptr(blob), sp, n, ptr(out), ptr(work), work.numel(), _abi.aptr(status),
+                                  stream_ptr())
         if rc not in (_abi.CHR_OK, _abi.CHR_E_CORRUPT, _abi.CHR_E_UNSUPPORTED_CODEC):
             check(rc, "chr_decode_regions")
-    return out, offs, [int(status[i]) for i in range(n)]
+    return out, [int(v) for v in sel["out_offset"]] if n else [], [int(v) for v in status[:n]]
+
+
+def mc_table(grid_offset, dims, origin, spacing) -> np.ndarray:
+    n = len(grid_offset)
+    t = np.zeros(n, dtype=_abi.MCGRID_DT)
+    t["grid_offset"] = grid_offset
+    t["dims"] = np.asarray(dims, dtype=np.int32).reshape(n, 3)
+    t["origin"] = np.asarray(origin, dtype=np.float64).reshape(n, 3)
+    t["spacing"] = np.asarray(spacing, dtype=np.float64).reshape(-1, 3)
+    return t
 
 
 def marching(grids: torch.Tensor, descs, k: float, ws: Workspaces | None = None):
     """Marching cubes over several f64 windows of `grids`, merged.
 
-    ``descs``: list of (element_offset, (nx,ny,nz), origin3, spacing3).
+    ``descs``: a ``_abi.MCGRID_DT`` table (:func:`mc_table`) or a list of
+    (element_offset, (nx,ny,nz), origin3, spacing3).
     Returns (verts f64 [nv,3], tris int32 [nt,3], ntri per grid, nvert per grid)."""
     ws = ws or _DEFAULT_WS
     L = lib()
-    n = len(descs)
     dev = _abi.device()
+    if not isinstance(descs, np.ndarray):
+        if not descs:
+            descs = np.zeros(0, dtype=_abi.MCGRID_DT)
+        else:
+            off, dims, org, spc = zip(*descs)
+            descs = mc_table(off, dims, org, spc)
+    n = len(descs)
     if n == 0:
         return (torch.empty((0, 3), dtype=torch.float64, device=dev),
                 torch.empty((0, 3), dtype=torch.int32, device=dev), [], [])
-    gd = (_abi.McGrid * n)()
-    for i, (off, dims, origin, spacing) in enumerate(descs):
-        g = gd[i]
-        g.grid_offset = int(off)
-        g.dims[0], g.dims[1], g.dims[2] = (int(d) for d in dims)
-        for a in range(3):
-            g.origin[a] = float(origin[a])
-            g.spacing[a] = float(spacing[a])
-    wsz = L.chr_mc_workspace_size(gd, n)
+    gp = _abi.aptr(descs)
+    wsz = L.chr_mc_workspace_size(gp, n)
     work = ws.get("mc", wsz)
-    ntri = (ctypes.c_int64 * n)()
-    nvert = (ctypes.c_int64 * n)()
+    ntri = np.zeros(n, dtype=np.int64)
+    nvert = np.zeros(n, dtype=np.int64)
     tt = ctypes.c_int64(0)
     tv = ctypes.c_int64(0)
-    check(L.chr_mc_count(ptr(grids), gd, n, float(k), ptr(work), work.numel(), ntri, nvert, ctypes.byref(tt),
-                         ctypes.byref(tv), stream_ptr()), "chr_mc_count")
+    check(L.chr_mc_count(ptr(grids), gp, n, float(k), ptr(work), work.numel(), _abi.aptr(ntri), _abi.aptr(nvert),
+                         ctypes.byref(tt), ctypes.byref(tv), stream_ptr()), "chr_mc_count")
     verts = torch.empty((tv.value, 3), dtype=torch.float64, device=dev)
     tris = torch.empty((tt.value, 3), dtype=torch.int32, device=dev)
-    check(L.chr_mc_emit(ptr(grids), gd, n, float(k), ptr(work), work.numel(), ptr(verts), ptr(tris),
+    check(L.chr_mc_emit(ptr(grids), gp, n, float(k), ptr(work), work.numel(), ptr(verts), ptr(tris),
                         stream_ptr()), "chr_mc_emit")
-    return verts, tris, list(ntri), list(nvert)
+    return verts, tris, ntri.tolist(), nvert.tolist()
 
 
 def case_codes(grid: torch.Tensor, dims, k: float, binary: bool = True) -> torch.Tensor:
@@ -289,14 +308,16 @@ def lorenzo_encode(flat: torch.Tensor, nx, ny, nz, e):
 
 
 def region_records(regions) -> list[dict]:
-    """Plain-Python view of a chr_region_t array."""
+    """Plain-Python view of a chr_region_t table."""
+    regions = np.asarray(regions)
+    cols = {f: regions[f].tolist() for f in regions.dtype.names}
     out = []
     for i in range(len(regions)):
-        r = regions[i]
         out.append(dict(
-            id=i, lo=tuple(r.lo), hi=tuple(r.hi), origin=tuple(r.origin), extent=tuple(r.extent),
-            mask=int(r.mask), e=float(r.error_bound), codec=int(r.codec_id), crc=int(r.payload_crc),
-            block_offset=int(r.block_offset), block_nbytes=int(r.block_nbytes), nesc=int(r.n_escaped),
+            id=i, lo=tuple(cols["lo"][i]), hi=tuple(cols["hi"][i]), origin=tuple(cols["origin"][i]),
+            extent=tuple(cols["extent"][i]), mask=cols["mask"][i], e=cols["error_bound"][i],
+            codec=cols["codec_id"][i], crc=cols["payload_crc"][i], block_offset=cols["block_offset"][i],
+            block_nbytes=cols["block_nbytes"][i], nesc=cols["n_escaped"][i],
         ))
     return out
 
