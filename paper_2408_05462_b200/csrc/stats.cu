@@ -110,6 +110,100 @@ __global__ void __launch_bounds__(256) k_stats(const T *__restrict__ vol, int64_
     }
 }
 
+// Fast path (f32, block size % 4 == 0, nx % 4 == 0, 16-byte aligned rows):
+// one CTA per (by, bz) block row streams its (bs+1)^2 full-width sample rows
+// with 16-byte loads; thread t owns x-quads t, t + 512, ...  Per-quad
+// partials go through shared memory and one thread per block combines its
+// bs/4 quads plus the x-ghost sample (first sample of the next block).
+constexpr int SQ = 512;  // threads; nx/4 <= SQ quads per row
+__global__ void __launch_bounds__(SQ) k_stats_rows(const float *__restrict__ vol, int64_t nx, int64_t ny,
+                                                   int64_t nz, int bs, int nbx, int nby, CandParams cp,
+                                                   double *__restrict__ stats,
+                                                   unsigned long long *__restrict__ first_bad) {
+    __shared__ double ks[64];
+    // per (row group, quad) partials: index g * nq + q  (rg * nq <= SQ)
+    __shared__ float plo[SQ], phi[SQ], pgl[SQ], pgh[SQ];
+    __shared__ double pdm[SQ], pgd[SQ];
+    if (threadIdx.x < cp.m) ks[threadIdx.x] = cp.k[threadIdx.x];
+    __syncthreads();
+    const int nq = (int)(nx >> 2);
+    const int m = cp.m;
+    const int by = blockIdx.x % nby, bz = blockIdx.x / nby;
+    const int64_t y0 = (int64_t)by * bs, y1 = min((int64_t)(by + 1) * bs, ny - 1);
+    const int64_t z0 = (int64_t)bz * bs, z1 = min((int64_t)(bz + 1) * bs, nz - 1);
+    const int G = bs >> 2;
+    const int rg = SQ / nq;  // row groups
+    const int q = threadIdx.x % nq, g = threadIdx.x / nq;
+    const int nrow_y = (int)(y1 - y0 + 1);
+    const int nrows = nrow_y * (int)(z1 - z0 + 1);
+    if (g < rg) {
+        float lo = INFINITY, hi = -INFINITY, gl = INFINITY, gh = -INFINITY;
+        double dm = INFINITY, gd = INFINITY;
+        unsigned long long bad = ~0ull;
+        const bool ghost = ((4 * q) % bs) == 0 && q > 0;
+        int zr = g / nrow_y, yr = g - (g / nrow_y) * nrow_y;
+        for (int r = g; r < nrows; r += rg) {
+            const int64_t z = z0 + zr, y = y0 + yr;
+            yr += rg;
+            while (yr >= nrow_y) {
+                yr -= nrow_y;
+                ++zr;
+            }
+            const float4 v4 = __ldg(reinterpret_cast<const float4 *>(vol + (z * ny + y) * nx) + q);
+            const float v[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const float f = v[i];
+                if (!isfinite(f)) {
+                    bad = min(bad, (unsigned long long)((z * ny + y) * nx + 4 * q + i));
+                    continue;
+                }
+                lo = fminf(lo, f);
+                hi = fmaxf(hi, f);
+                const double d = min_cand_dist(ks, m, (double)f);
+                dm = fmin(dm, d);
+                if (i == 0 && ghost) {
+                    gl = fminf(gl, f);
+                    gh = fmaxf(gh, f);
+                    gd = fmin(gd, d);
+                }
+            }
+        }
+        if (bad != ~0ull) atomicMin(first_bad, bad);
+        const int k = g * nq + q;
+        plo[k] = lo;
+        phi[k] = hi;
+        pdm[k] = dm;
+        pgl[k] = gl;
+        pgh[k] = gh;
+        pgd[k] = gd;
+    }
+    __syncthreads();
+    for (int bx = threadIdx.x; bx < nbx; bx += SQ) {
+        float l = INFINITY, h = -INFINITY;
+        double d = INFINITY;
+        const int q0 = bx * G, q1 = min(q0 + G, nq);
+        for (int gg = 0; gg < rg; ++gg) {
+            for (int qq = q0; qq < q1; ++qq) {
+                const int k = gg * nq + qq;
+                l = fminf(l, plo[k]);
+                h = fmaxf(h, phi[k]);
+                d = fmin(d, pdm[k]);
+            }
+            if (q1 < nq) {  // x-ghost: first sample of the next block
+                const int k = gg * nq + q1;
+                l = fminf(l, pgl[k]);
+                h = fmaxf(h, pgh[k]);
+                d = fmin(d, pgd[k]);
+            }
+        }
+        const int64_t id = bx + (int64_t)nbx * (by + (int64_t)nby * bz);
+        stats[3 * id + 0] = (double)l;
+        stats[3 * id + 1] = (double)h;
+        stats[3 * id + 2] = d;
+    }
+}
+
 }  // namespace chr
 
 using namespace chr;
@@ -134,7 +228,14 @@ extern "C" int chr_stats(const void *d_vol, int dtype, int64_t nx, int64_t ny, i
     const int64_t nblocks = chr_num_blocks(nx, ny, nz, bs);
     CHR_CUDA_TRY(cudaMemsetAsync(d_first_nonfinite, 0xFF, sizeof(int64_t), st));
     auto *bad = reinterpret_cast<unsigned long long *>(d_first_nonfinite);
-    if (dtype == CHR_F32)
+    const int nbz = (int)((nz - 1 + bs - 1) / bs);
+    const bool rows_ok = dtype == CHR_F32 && bs % 4 == 0 && nx % 4 == 0 && nx <= 4 * SQ &&
+                         ((uintptr_t)d_vol & 15) == 0;
+    if (rows_ok) {
+        CHR_PROF("k_stats_rows", st);
+        k_stats_rows<<<(unsigned)(nby * nbz), SQ, 0, st>>>((const float *)d_vol, nx, ny, nz, (int)bs, nbx, nby, cp,
+                                                           d_block_stats, bad);
+    } else if (dtype == CHR_F32)
         {
             CHR_PROF("k_stats<float>", st);
             k_stats<float><<<(unsigned)nblocks, 256, 0, st>>>((const float *)d_vol, nx, ny, nz, (int)bs,
