@@ -62,4 +62,16 @@ struct WsCarver {
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+#if defined(__CUDACC__)
+// copy a struct from global to shared memory with all threads (parallel
+// 4-byte loads instead of one thread's serialised copy); caller syncs
+template <typename S>
+__device__ __forceinline__ void coop_copy(S *dst, const S *src) {
+    static_assert(sizeof(S) % 4 == 0, "4-byte multiple");
+    const uint32_t *a = reinterpret_cast<const uint32_t *>(src);
+    uint32_t *b = reinterpret_cast<uint32_t *>(dst);
+    for (int i = threadIdx.x; i < (int)(sizeof(S) / 4); i += blockDim.x) b[i] = __ldg(a + i);
+}
+#endif
+
 }  // namespace chr

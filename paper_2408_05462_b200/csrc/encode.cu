@@ -120,18 +120,45 @@ __device__ __forceinline__ bool not_f32_exact(T v) {
 }
 
 // ------------------------------------------------------------------ tiles
+// 32-bit token-size helpers (valid quanta: |q| <= 2^30, zigzag+1 <= 2^31+1)
+__device__ __forceinline__ uint32_t zz1_32(int32_t q) { return (((uint32_t)q << 1) ^ (uint32_t)(q >> 31)) + 1u; }
+__device__ __forceinline__ int vlen32(uint32_t u) {
+    return 1 + (u >= (1u << 7)) + (u >= (1u << 14)) + (u >= (1u << 21)) + (u >= (1u << 28));
+}
+// token bytes of a zero run shorter than 128 (every run inside one 64-sample piece)
+__device__ __forceinline__ int rb_small(int L) { return L <= 0 ? 0 : (L == 1 ? 1 : 2); }
+
+__device__ __forceinline__ uint8_t *put_varint32(uint8_t *p, uint32_t u) {
+    while (u >= 0x80u) {
+        *p++ = (uint8_t)((u & 0x7Fu) | 0x80u);
+        u >>= 7;
+    }
+    *p++ = (uint8_t)u;
+    return p;
+}
+
+// quantiser fast path only; false -> the caller runs the exact sequence
+__device__ __forceinline__ bool quant_fast(const Quant &Q, double v, int32_t &u) {
+    const double qf = __dmul_rn(v, Q.inv);
+    const double t = __dadd_rn(qf, kRoundShift);
+    const double d = __dadd_rn(qf, -__dadd_rn(t, -kRoundShift));
+    u = __double2loint(t);
+    return Q.fast && fabs(qf) < kEscapeUmax && fabs(d) < kTieMargin;
+}
+
 template <typename T, bool EMIT>
-__global__ void __launch_bounds__(NW * 32, 5) k_tile(const T *__restrict__ vol, const EncParams *__restrict__ P,
+__global__ void __launch_bounds__(NW * 32, 4) k_tile(const T *__restrict__ vol, const EncParams *__restrict__ P,
                                                   const RegDev *__restrict__ regs,
+                                                  const int32_t *__restrict__ item_reg,
                                                   PieceRec *__restrict__ recs,
                                                   const PieceOff *__restrict__ poffs,
                                                   uint8_t *__restrict__ out) {
     __shared__ int32_t sD[2][NW][TX + 2];
     __shared__ RegDev R;
     const int64_t item = blockIdx.x;
-    if (threadIdx.x == 0) R = regs[find_region_by(regs, P->nreg, item, 0)];
+    coop_copy(&R, regs + __ldg(item_reg + item));
     __syncthreads();
-    const int64_t NX = P->NX, NY = P->NY;
+    const int64_t NX = P->NX, NY = P->NY, plane = NX * NY;
     const int64_t local = item - R.item_base;
     const int xt = (int)(local % R.ntx);
     const int64_t t2 = local / R.ntx;
@@ -149,42 +176,48 @@ __global__ void __launch_bounds__(NW * 32, 5) k_tile(const T *__restrict__ vol, 
     const Quant Q = make_quant(R.e);
     const bool is_last_xt = xt == R.ntx - 1;
     const int vcount = min(TX, R.ex - x0);
-    // codec decided by the scan (EMIT only)
     const int codec = EMIT ? R.codec : 0;
+    const bool chk32 = sizeof(T) == 8 && P->src_dtype == CHR_F32;
+    const uint32_t lt = (1u << lane) - 1u;
+    const T *row = vol + ((int64_t)(R.oz + z0) * NY + (R.oy + y)) * NX + R.ox;  // plane z0
 
-    auto vptr = [&](int z) -> const T * {
-        return vol + ((int64_t)(R.oz + z) * NY + (R.oy + y)) * NX + R.ox;
+    auto quant3 = [&](T a, T b, T h, int32_t &ua, int32_t &ub, int32_t &uh, bool &ea, bool &eb, bool &eh) {
+        ua = ub = uh = 0;
+        ea = eb = eh = false;
+        bool fa = true, fb = true, fh = true;
+        if (okA) fa = quant_fast(Q, (double)a, ua);
+        if (okB) fb = quant_fast(Q, (double)b, ub);
+        if (okH) fh = quant_fast(Q, (double)h, uh);
+        if (__any_sync(0xFFFFFFFFu, !(fa && fb && fh))) {  // rare: ties, escapes, tiny e
+            if (!fa) ua = quantize(Q, (double)a, ea);
+            if (!fb) ub = quantize(Q, (double)b, eb);
+            if (!fh) uh = quantize(Q, (double)h, eh);
+        }
     };
     int32_t pA = 0, pB = 0, pH = 0;  // u at the previous plane
     if (quant && z0 > 0) {
-        const T *row = vptr(z0 - 1);
-        bool e_;
-        if (okA) pA = quantize(Q, (double)__ldg(row + xA), e_);
-        if (okB) pB = quantize(Q, (double)__ldg(row + xB), e_);
-        if (okH) pH = quantize(Q, (double)__ldg(row + xH), e_);
+        const T *prow = row - plane;
+        bool e0, e1, e2;
+        quant3(okA ? __ldg(prow + xA) : (T)0, okB ? __ldg(prow + xB) : (T)0, okH ? __ldg(prow + xH) : (T)0, pA, pB,
+               pH, e0, e1, e2);
     }
     T nA = 0, nB = 0, nH = 0;
     if (z0 < z1) {
-        const T *row = vptr(z0);
         if (okA) nA = __ldg(row + xA);
         if (okB) nB = __ldg(row + xB);
         if (okH) nH = __ldg(row + xH);
     }
-    for (int z = z0; z < z1; ++z) {
+    for (int z = z0; z < z1; ++z, row += plane) {
         const T vA = nA, vB = nB, vH = nH;
         if (z + 1 < z1) {  // prefetch the next plane
-            const T *row = vptr(z + 1);
-            if (okA) nA = __ldg(row + xA);
-            if (okB) nB = __ldg(row + xB);
-            if (okH) nH = __ldg(row + xH);
+            const T *nrow = row + plane;
+            if (okA) nA = __ldg(nrow + xA);
+            if (okB) nB = __ldg(nrow + xB);
+            if (okH) nH = __ldg(nrow + xH);
         }
         bool eA = false, eB = false, eH = false;
         int32_t uA = 0, uB = 0, uH = 0;
-        if (quant) {
-            if (okA) uA = quantize(Q, (double)vA, eA);
-            if (okB) uB = quantize(Q, (double)vB, eB);
-            if (okH) uH = quantize(Q, (double)vH, eH);
-        }
+        if (quant) quant3(vA, vB, vH, uA, uB, uH, eA, eB, eH);
         int32_t(*D)[TX + 2] = sD[z & 1];
         D[w][lane + 1] = uA - pA;
         D[w][lane + 33] = uB - pB;
@@ -197,38 +230,34 @@ __global__ void __launch_bounds__(NW * 32, 5) k_tile(const T *__restrict__ vol, 
         const int32_t qA = D[w][lane + 1] - D[w][lane] - D[w - 1][lane + 1] + D[w - 1][lane];
         const int32_t qB = D[w][lane + 33] - D[w][lane + 32] - D[w - 1][lane + 33] + D[w - 1][lane + 32];
         const bool nzA = okA && qA != 0, nzB = okB && qB != 0;
-        const uint64_t nzm = (uint64_t)__ballot_sync(0xFFFFFFFFu, nzA) |
-                             ((uint64_t)__ballot_sync(0xFFFFFFFFu, nzB) << 32);
-        const uint64_t escm = (uint64_t)__ballot_sync(0xFFFFFFFFu, okA && eA) |
-                              ((uint64_t)__ballot_sync(0xFFFFFFFFu, okB && eB) << 32);
+        const uint32_t mA = __ballot_sync(0xFFFFFFFFu, nzA), mB = __ballot_sync(0xFFFFFFFFu, nzB);
         const int64_t rec = R.piece_base + ((int64_t)z * R.ey + y) * R.ntx + xt;
-        const uint64_t below_mask_A = (1ull << lane) - 1, below_mask_B = (1ull << (32 + lane)) - 1;
+        // previous nonzero (position in the piece) before element A (= lane) and B (= 32 + lane)
+        const uint32_t bA = mA & lt, bB = mB & lt;
+        const int prevA = bA ? 31 - __clz(bA) : -1;
+        const int prevB = bB ? 63 - __clz(bB) : (mA ? 31 - __clz(mA) : -1);
+        const uint32_t zA = zz1_32(qA), zB = zz1_32(qB);
+        const bool anyesc = __any_sync(0xFFFFFFFFu, (okA && eA) || (okB && eB));
         if (!EMIT) {
             int b = 0;
-            if (nzA) {
-                const uint64_t below = nzm & below_mask_A;
-                if (below) b += (int)run_bytes(lane - hibit(below) - 1);
-                b += varint_len(zigzag1(qA));
-            }
-            if (nzB) {
-                const uint64_t below = nzm & below_mask_B;
-                if (below) b += (int)run_bytes(32 + lane - hibit(below) - 1);
-                b += varint_len(zigzag1(qB));
-            }
+            if (nzA) b += (prevA >= 0 ? rb_small(lane - prevA - 1) : 0) + vlen32(zA);
+            if (nzB) b += (prevB >= 0 ? rb_small(32 + lane - prevB - 1) : 0) + vlen32(zB);
             const int bytes = __reduce_add_sync(0xFFFFFFFFu, b);
-            bool inexact = false;
-            if (sizeof(T) == 8 && P->src_dtype == CHR_F32) {
-                inexact = (okA && not_f32_exact(vA)) || (okB && not_f32_exact(vB));
-            }
-            const bool anyinexact = __any_sync(0xFFFFFFFFu, inexact);
+            int nesc = 0;
+            if (anyesc)
+                nesc = __popc(__ballot_sync(0xFFFFFFFFu, okA && eA)) + __popc(__ballot_sync(0xFFFFFFFFu, okB && eB));
+            bool anyinexact = false;
+            if (chk32) anyinexact = __any_sync(0xFFFFFFFFu, (okA && not_f32_exact(vA)) || (okB && not_f32_exact(vB)));
             if (lane == 0) {
+                const int first = mA ? __ffs(mA) - 1 : (mB ? 31 + __ffs(mB) : vcount);
+                const int lastp = mB ? 63 - __clz(mB) : (mA ? 31 - __clz(mA) : -1);
                 PieceRec pr;
                 pr.bytes = (uint16_t)bytes;
                 pr.vcount = (uint8_t)vcount;
-                pr.lead = (uint8_t)(nzm ? __ffsll((long long)nzm) - 1 : vcount);
-                pr.trail = (uint8_t)(nzm ? vcount - 1 - hibit(nzm) : vcount);
-                pr.nesc = (uint8_t)__popcll((long long)escm);
-                pr.flags = (uint8_t)((nzm ? 1 : 0) | (anyinexact ? 2 : 0));
+                pr.lead = (uint8_t)first;
+                pr.trail = (uint8_t)((mA | mB) ? vcount - 1 - lastp : vcount);
+                pr.nesc = (uint8_t)nesc;
+                pr.flags = (uint8_t)(((mA | mB) ? 1 : 0) | (anyinexact ? 2 : 0));
                 pr.pad = 0;
                 recs[rec] = pr;
             }
@@ -236,22 +265,16 @@ __global__ void __launch_bounds__(NW * 32, 5) k_tile(const T *__restrict__ vol, 
             if (codec == 1 || codec == 2) {
                 const PieceOff po = poffs[rec];
                 int64_t runA = 0, runB = 0;
-                int bA = 0, bB = 0;
-                uint64_t zzA = 0, zzB = 0;
+                int bAy = 0, bBy = 0;
                 if (nzA) {
-                    const uint64_t below = nzm & below_mask_A;
-                    runA = below ? lane - hibit(below) - 1 : po.carry + lane;
-                    zzA = zigzag1(qA);
-                    bA = (int)run_bytes(runA) + varint_len(zzA);
+                    runA = prevA >= 0 ? lane - prevA - 1 : po.carry + lane;
+                    bAy = (prevA >= 0 ? rb_small((int)runA) : (int)run_bytes(runA)) + vlen32(zA);
                 }
                 if (nzB) {
-                    const uint64_t below = nzm & below_mask_B;
-                    runB = below ? 32 + lane - hibit(below) - 1 : po.carry + 32 + lane;
-                    zzB = zigzag1(qB);
-                    bB = (int)run_bytes(runB) + varint_len(zzB);
+                    runB = prevB >= 0 ? 32 + lane - prevB - 1 : po.carry + 32 + lane;
+                    bBy = (prevB >= 0 ? rb_small((int)runB) : (int)run_bytes(runB)) + vlen32(zB);
                 }
-                // exclusive scans in stream order (elements 0..31 then 32..63)
-                int sA = bA, sB = bB;
+                int sA = bAy, sB = bBy;
 #pragma unroll
                 for (int off = 1; off < 32; off <<= 1) {
                     const int ta = __shfl_up_sync(0xFFFFFFFFu, sA, off);
@@ -263,25 +286,23 @@ __global__ void __launch_bounds__(NW * 32, 5) k_tile(const T *__restrict__ vol, 
                 }
                 const int totA = __shfl_sync(0xFFFFFFFFu, sA, 31);
                 const int totB = __shfl_sync(0xFFFFFFFFu, sB, 31);
-                sA -= bA;
-                sB = sB - bB + totA;
+                sA -= bAy;
+                sB = sB - bBy + totA;
                 uint8_t *base = out + R.tok_start + po.tok_off;
-                if (nzA) put_varint(put_run(base + sA, runA), zzA);
-                if (nzB) put_varint(put_run(base + sB, runB), zzB);
+                if (nzA) put_varint32(put_run(base + sA, runA), zA);
+                if (nzB) put_varint32(put_run(base + sB, runB), zB);
                 if (is_last_xt && y == R.ey - 1 && z == R.ez - 1 && lane == 0) {
-                    const int64_t fin = nzm ? vcount - 1 - hibit(nzm) : po.carry + vcount;
+                    const int lastp = mB ? 63 - __clz(mB) : (mA ? 31 - __clz(mA) : -1);
+                    const int64_t fin = (mA | mB) ? vcount - 1 - lastp : po.carry + vcount;
                     put_run(base + totA + totB, fin);
                 }
-                if (codec == 2 && escm) {
+                if (codec == 2 && anyesc) {
+                    const uint32_t eAm = __ballot_sync(0xFFFFFFFFu, okA && eA);
+                    const uint32_t eBm = __ballot_sync(0xFFFFFFFFu, okB && eB);
                     const uint64_t vbase = R.payload_off + (uint64_t)((R.n + 7) >> 3);
-                    if (okA && eA) {
-                        const int64_t rank = po.esc_off + __popcll((long long)(escm & below_mask_A));
-                        put_le(out + vbase + 8 * rank, (double)vA);
-                    }
-                    if (okB && eB) {
-                        const int64_t rank = po.esc_off + __popcll((long long)(escm & below_mask_B));
-                        put_le(out + vbase + 8 * rank, (double)vB);
-                    }
+                    if (okA && eA) put_le(out + vbase + 8 * (po.esc_off + __popc(eAm & lt)), (double)vA);
+                    if (okB && eB)
+                        put_le(out + vbase + 8 * (po.esc_off + __popc(eAm) + __popc(eBm & lt)), (double)vB);
                 }
             } else {
                 // verbatim: codec 3 (f32) or 0 (f64), raster order
@@ -298,6 +319,15 @@ __global__ void __launch_bounds__(NW * 32, 5) k_tile(const T *__restrict__ vol, 
             }
         }
     }
+}
+
+// item -> region map (replaces a per-CTA binary search over the regions)
+__global__ void k_tile_fill_map(const RegDev *__restrict__ regs, int64_t nreg, int32_t *__restrict__ item_reg) {
+    const int64_t r = blockIdx.x;
+    if (r >= nreg) return;
+    const RegDev &R = regs[r];
+    const int64_t nit = (int64_t)R.ntx * R.nty * R.nzc;
+    for (int64_t i = threadIdx.x; i < nit; i += blockDim.x) item_reg[R.item_base + i] = (int32_t)r;
 }
 
 // ------------------------------------------------------------------ scans
@@ -684,6 +714,7 @@ struct EncPlan {
     uint32_t *seg_raw;
     int32_t *codec2;
     EncScalars *scal;
+    int32_t *item_reg;
 };
 
 static bool build_plan(const chr_region_t *h, int64_t nreg, EncPlan &pl) {
@@ -737,6 +768,7 @@ static void carve(EncPlan &pl, void *base, size_t cap) {
     pl.segs = c.take<CrcSeg>(nreg + 1);
     pl.seg_raw = c.take<uint32_t>(nreg + 1);
     pl.codec2 = c.take<int32_t>(nreg);
+    pl.item_reg = c.take<int32_t>(pl.nitems + 1);
     pl.scal = c.take<EncScalars>(1);
     pl.ws_bytes = c.off + 256;
 }
@@ -813,16 +845,20 @@ extern "C" int chr_compress(const void *d_vol, int dtype, int src_dtype, int64_t
     CHR_CUDA_TRY(cudaMemsetAsync(pl.seg_raw, 0, sizeof(uint32_t) * (nreg + 1), st));
 
     const unsigned items = (unsigned)pl.nitems, chunks = (unsigned)pl.nchunks;
+    {
+        CHR_PROF("k_tile_fill_map", st);
+        k_tile_fill_map<<<(unsigned)nreg, 256, 0, st>>>(pl.d_regs, nreg, pl.item_reg);
+    }
     if (dtype == CHR_F32)
         {
             CHR_PROF("k_tile<float, false>", st);
-            k_tile<float, false><<<items, NW * 32, 0, st>>>((const float *)d_vol, pl.params, pl.d_regs,
+            k_tile<float, false><<<items, NW * 32, 0, st>>>((const float *)d_vol, pl.params, pl.d_regs, pl.item_reg,
                                                             pl.recs, pl.poffs, d_out);
         }
     else
         {
             CHR_PROF("k_tile<double, false>", st);
-            k_tile<double, false><<<items, NW * 32, 0, st>>>((const double *)d_vol, pl.params, pl.d_regs,
+            k_tile<double, false><<<items, NW * 32, 0, st>>>((const double *)d_vol, pl.params, pl.d_regs, pl.item_reg,
                                                              pl.recs, pl.poffs, d_out);
         }
     {
@@ -845,7 +881,7 @@ extern "C" int chr_compress(const void *d_vol, int dtype, int src_dtype, int64_t
     if (dtype == CHR_F32) {
         {
             CHR_PROF("k_tile<float, true>", st);
-            k_tile<float, true><<<items, NW * 32, 0, st>>>((const float *)d_vol, pl.params, pl.d_regs,
+            k_tile<float, true><<<items, NW * 32, 0, st>>>((const float *)d_vol, pl.params, pl.d_regs, pl.item_reg,
                                                            pl.recs, pl.poffs, d_out);
         }
         {
@@ -856,7 +892,7 @@ extern "C" int chr_compress(const void *d_vol, int dtype, int src_dtype, int64_t
     } else {
         {
             CHR_PROF("k_tile<double, true>", st);
-            k_tile<double, true><<<items, NW * 32, 0, st>>>((const double *)d_vol, pl.params, pl.d_regs,
+            k_tile<double, true><<<items, NW * 32, 0, st>>>((const double *)d_vol, pl.params, pl.d_regs, pl.item_reg,
                                                             pl.recs, pl.poffs, d_out);
         }
         {

@@ -530,7 +530,7 @@ __global__ void __launch_bounds__(288, 5) k_mc_count2(const double *__restrict__
     for (int i = threadIdx.x; i < 256; i += blockDim.x) s_ntri[i] = T->ntri[i];
     for (int i = threadIdx.x; i < 2048; i += blockDim.x) (&s_own[0][0])[i] = (&T->owncnt[0][0])[i];
     const int64_t item = blockIdx.x;
-    if (threadIdx.x == 0) g = G[item_grid[item]];
+    coop_copy(&g, G + __ldg(item_grid + item));
     __syncthreads();
     const int nyt = (g.ncy + MTY - 1) / MTY;
     const int64_t local = item - g.item_base;
@@ -624,7 +624,7 @@ __global__ void __launch_bounds__(EW * 32, 3) k_mc_emit2(const double *__restric
     for (int i = threadIdx.x; i < 256; i += blockDim.x) s_ntri[i] = T->ntri[i];
     for (int i = threadIdx.x; i < 2048; i += blockDim.x) (&s_own[0][0])[i] = (&T->owncnt[0][0])[i];
     const int64_t item = blockIdx.x;
-    if (threadIdx.x == 0) g = G[item_grid[item]];
+    coop_copy(&g, G + __ldg(item_grid + item));
     __syncthreads();
     const int nyt = (g.ncy + MTY - 1) / MTY;
     const int64_t local = item - g.item_base;
