@@ -135,17 +135,16 @@ def kernel_bytes(name, info, N):
     c_all = info["payload"]
     table = {
         "k_stats<float>": 4 * N,
+        "k_stats_rows": 4 * N,
         "k_tile<float, false>": 4 * N,
         "k_tile<float, true>": 4 * N + c_all,
         "k_crc_segments": None,
-        "k_tok_count": info["c_sel"],
-        "k_locate": info["c_sel"],
-        "k_lorenzo": info["c_sel"] + 8 * info["n_sel"],
-        "k_lorenzo3d": info["c_sel"] + 8 * info["n_sel"],
         "k_tok_fast": info["c_sel"],
-        "k_rp_locate": info["c_sel"],
-        "k_mc_count": 8 * info["n_sel"],
-        "k_mc_emit": 8 * info["n_sel"] + 24 * info["nvert"] + 12 * info["ntri"],
+        "k_seg_locate": info["c_sel"],
+        "k_band": info["c_sel"] + 8 * info["n_sel"],
+        "k_lorenzo": info["c_sel"] + 8 * info["n_sel"],
+        "k_mc_count2": 8 * info["n_sel"],
+        "k_mc_emit2": 8 * info["n_sel"] + 24 * info["nvert"] + 12 * info["ntri"],
     }
     return table.get(name)
 

@@ -29,6 +29,7 @@
 // All integer work is int64 like the reference, so even CRC-valid
 // hand-made streams decode bit-identically.
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <vector>
 
@@ -67,10 +68,13 @@ struct DecReg {
     int64_t seg_base, nseg;        // decode segments (nyt * ez)
     int64_t item_base;             // k_lorenzo tiles (nyt)
     int64_t carry_base;            // int64 elements of the carry history
-    // fast (canonical-stream) path: 64x8x8 wavefront tiles, row-piece index
+    // fast (canonical-stream) path: band tiles (full rows x bty rows x btz planes)
     int64_t abase;                 // 16-byte aligned chunk origin (blob-relative)
-    int32_t ntx, tnx, tny, tnz;    // row pieces per row; wavefront tiles per axis
-    int64_t tile_base, ntiles, rp_base, nrp;
+    int32_t tnx, tny, tnz;         // tiles per axis (tnx = 1, tny = bands, tnz = chunks)
+    int32_t bty, btz, rs;          // band rows, chunk planes, smem row stride
+    int64_t tile_base, ntiles;
+    int64_t sp_base;               // segment index: ez * tny entries
+    int64_t face_base, face_n;     // int64 faces per tile: ex * (btz + 1 + bty)
     // device-computed
     uint64_t tok_start;            // absolute offset of the token stream
     int64_t nesc;
@@ -274,11 +278,13 @@ __global__ void __launch_bounds__(DTHREADS) k_tok_count(DecReg *__restrict__ reg
 }
 
 // per region: exclusive prefix of chunk samples, total must equal n
-__global__ void k_tok_scan(DecReg *__restrict__ regs, int64_t nreg, int64_t *__restrict__ chunk_samples) {
+__global__ void k_tok_scan(DecReg *__restrict__ regs, int64_t nreg, int64_t *__restrict__ chunk_samples,
+                           int slow_pass) {
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= nreg) return;
     DecReg &R = regs[r];
     if (!((R.codec == 1 || R.codec == 2) && R.err == 0)) return;
+    if ((R.slow != 0) != (slow_pass != 0)) return;  // pass 0: band regions, pass 1: generic
     int64_t acc = 0;
     bool over = false;
     for (int64_t c = R.chunk_base; c < R.chunk_base + R.nchunks; ++c) {
@@ -416,7 +422,6 @@ __global__ void __launch_bounds__(DTHREADS) k_lorenzo(const DecReg *__restrict__
     const double twoe = 2.0 * R.e;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t hi = (int64_t)(R.poff + R.plen);
-    const int64_t lo = (int64_t)R.tok_start;
     for (int64_t i = threadIdx.x; i < seglen; i += DTHREADS) up[i] = 0;
     int64_t *my_carry = carry + R.carry_base + (int64_t)yt * R.ez * ex;
     const int64_t *above = yt > 0 ? carry + R.carry_base + (int64_t)(yt - 1) * R.ez * ex : nullptr;
@@ -548,8 +553,6 @@ __global__ void __launch_bounds__(DTHREADS) k_lorenzo(const DecReg *__restrict__
         if (R.codec == 2 && R.nesc > 0) {
             __syncthreads();
             const uint8_t *bm = blob + R.poff;
-            const double *ev = nullptr;
-            (void)ev;
             for (int64_t i = threadIdx.x; i < seglen; i += DTHREADS) {
                 const int64_t s = sk + i;
                 if ((bm[s >> 3] >> (s & 7)) & 1) {
@@ -722,7 +725,7 @@ __global__ void k_fill_maps(const DecReg *__restrict__ regs, int64_t nreg, int32
 
 constexpr int UPT = (int)(DCB / (16 * DTHREADS));  // 16-byte units per thread
 
-// tile order for k_lorenzo3d: all regions' tiles grouped by wavefront
+// tile order for k_band: all regions' tiles grouped by wavefront
 // diagonal d = tx + ty + tz (every dependency of a tile lies on d - 1, so
 // taking tiles in this order from a ticket cannot deadlock and keeps every
 // region's wavefront advancing at once).  One thread per (diagonal, region)
@@ -748,7 +751,8 @@ __global__ void k_tile_order(const DecReg *__restrict__ regs, const int64_t *__r
 // samples per chunk (fast path); flags non-canonical regions
 __global__ void __launch_bounds__(DTHREADS) k_tok_fast(DecReg *__restrict__ regs, const int32_t *__restrict__ chunk_reg,
                                                        const uint8_t *__restrict__ blob,
-                                                       int64_t *__restrict__ chunk_samples) {
+                                                       int64_t *__restrict__ chunk_samples,
+                                                       int64_t *__restrict__ thr_cnt) {
     const int64_t c = blockIdx.x;
     DecReg &R = regs[chunk_reg[c]];
     if (!((R.codec == 1 || R.codec == 2) && R.err == 0)) {
@@ -775,51 +779,42 @@ __global__ void __launch_bounds__(DTHREADS) k_tok_fast(DecReg *__restrict__ regs
             }
         }
     }
+    thr_cnt[c * DTHREADS + threadIdx.x] = cnt;
     const int64_t tot = block_sum64(cnt);
     if (err) atomicOr(&R.err, err);
     if (nc) atomicOr(&R.slow, 1u);
     if (threadIdx.x == 0) chunk_samples[c] = tot;
 }
 
-// row-piece index: for every 64-sample piece of every row, the byte of the
-// token (marker for runs) holding its first sample and the samples to skip
-__global__ void __launch_bounds__(DTHREADS) k_rp_locate(const DecReg *__restrict__ regs,
-                                                        const int32_t *__restrict__ chunk_reg,
-                                                        const uint8_t *__restrict__ blob,
-                                                        const int64_t *__restrict__ chunk_start,
-                                                        int64_t *__restrict__ rp_byte,
-                                                        int64_t *__restrict__ rp_skip) {
+// segment index of the band path: for every (plane z, band b) of a region
+// the byte of the token (marker for runs) holding sample (z*ey + b*bty)*ex
+// and the samples of that token before it.  Per-thread sample counts come
+// from k_tok_fast; only threads whose samples contain a segment start walk
+// their tokens again.
+__global__ void __launch_bounds__(DTHREADS) k_seg_locate(const DecReg *__restrict__ regs,
+                                                         const int32_t *__restrict__ chunk_reg,
+                                                         const uint8_t *__restrict__ blob,
+                                                         const int64_t *__restrict__ chunk_start,
+                                                         const int64_t *__restrict__ thr_cnt,
+                                                         int64_t *__restrict__ sp_byte,
+                                                         int64_t *__restrict__ sp_skip) {
     const int64_t c = blockIdx.x;
     const DecReg &R = regs[chunk_reg[c]];
     if (!((R.codec == 1 || R.codec == 2) && R.err == 0 && !R.slow)) return;
+    const int64_t cnt = thr_cnt[c * DTHREADS + threadIdx.x];
+    int64_t a = chunk_start[c] + block_excl64(cnt, nullptr);
+    if (cnt == 0) return;
+    const int64_t ex = R.ex, plane = ex * R.ey, band = ex * R.bty, nb = R.tny;
+    int64_t z = a / plane, b = (a - z * plane + band - 1) / band;
+    if (b >= nb) {
+        b = 0;
+        ++z;
+    }
+    int64_t s = z * plane + b * band;  // first segment start >= a
+    if (s >= a + cnt) return;
     const int64_t lo = (int64_t)R.tok_start, hi = (int64_t)(R.poff + R.plen);
     const int64_t ub = R.abase + (c - R.chunk_base) * DCB + (int64_t)threadIdx.x * UPT * 16;
-    const bool mine = ub + UPT * 16 > lo && ub < hi;
-    int64_t cnt = 0;
     uint32_t w[8];
-    if (mine) {
-        load_units(blob, ub, w);
-#pragma unroll 1
-        for (int u = 0; u < UPT; ++u) {
-            const int64_t u0 = ub + 16 * u;
-            if (u) next_unit(blob, u0, w);
-            if (u0 + 16 > lo && u0 < hi) cnt += unit_count(unit_masks(w, u0, lo, hi), blob, u0);
-        }
-    }
-    int64_t a = chunk_start[c] + block_excl64(cnt, nullptr);
-    if (!mine || cnt == 0) return;
-    const int64_t ex = R.ex;
-    // first row-piece start >= a; nothing to do if it lies beyond the thread's samples
-    int64_t row = a / ex;
-    int64_t x = a - row * ex;
-    {
-        int64_t xs = (x + 63) & ~63ll, r2 = row;
-        if (xs >= ex) {
-            xs = 0;
-            ++r2;
-        }
-        if (r2 * ex + xs >= a + cnt) return;
-    }
     load_units(blob, ub, w);
 #pragma unroll 1
     for (int u = 0; u < UPT; ++u) {
@@ -831,364 +826,340 @@ __global__ void __launch_bounds__(DTHREADS) k_rp_locate(const DecReg *__restrict
         while (T) {
             const int e = __ffs(T) - 1;
             T &= T - 1;
-            const bool isl = (m.len >> e) & 1u;
-            int64_t tc = 1, sbyte;
             const uint32_t below = m.E & ((1u << e) - 1u);
-            const int s = below ? 32 - __clz(below) : 0;
-            if (isl) {
+            const int sb = below ? 32 - __clz(below) : 0;
+            int64_t tc = 1, sbyte = u0 - 16 + sb;
+            if ((m.len >> e) & 1u) {
                 tc = (int64_t)unit_token_value(blob, m.E, e, u0);
-                sbyte = u0 - 16 + s - 1;  // the marker
-            } else {
-                sbyte = u0 - 16 + s;
+                sbyte -= 1;  // the marker
             }
-            if ((x & 63) == 0 || tc > 1) {
-                int64_t xs = (x + 63) & ~63ll, r2 = row;
-                if (xs >= ex) {
-                    xs = 0;
-                    ++r2;
+            while (s < a + tc) {
+                const int64_t k = R.sp_base + z * nb + b;
+                sp_byte[k] = sbyte;
+                sp_skip[k] = s - a;
+                if (++b >= nb) {
+                    b = 0;
+                    ++z;
                 }
-                int64_t pp = r2 * ex + xs;
-                while (pp < a + tc) {
-                    const int64_t k = R.rp_base + r2 * R.ntx + (xs >> 6);
-                    rp_byte[k] = sbyte;
-                    rp_skip[k] = pp - a;
-                    xs += 64;
-                    if (xs >= ex) {
-                        xs = 0;
-                        ++r2;
-                    }
-                    pp = r2 * ex + xs;
-                }
+                s = z * plane + b * band;
             }
             a += tc;
-            x += tc;
-            if (x >= ex) {
-                if (x < 2 * ex) {
-                    x -= ex;
-                    ++row;
-                } else {
-                    row += x / ex;
-                    x %= ex;
-                }
-            }
         }
     }
 }
 
-// codec 2: escapes before every row piece (one CTA per region)
-__global__ void __launch_bounds__(256) k_esc_rp(const DecReg *__restrict__ regs, const uint8_t *__restrict__ blob,
-                                                int64_t *__restrict__ esc_rp) {
+// codec 2 (band path): escapes before every segment (one CTA per region)
+__global__ void __launch_bounds__(256) k_esc_seg(const DecReg *__restrict__ regs, const uint8_t *__restrict__ blob,
+                                                 int64_t *__restrict__ esc_sp) {
     const DecReg &R = regs[blockIdx.x];
-    if (R.codec != 2 || R.err || R.slow) return;
+    if (R.codec != 2 || R.err || R.slow || R.nesc == 0) return;
     const uint8_t *bm = blob + R.poff;
+    const int64_t plane = (int64_t)R.ex * R.ey, band = (int64_t)R.ex * R.bty, nb = R.tny;
+    const int64_t nsp = (int64_t)R.ez * nb;
     int64_t carry = 0;
-    for (int64_t p0 = 0; p0 < R.nrp; p0 += 256) {
-        const int64_t p = p0 + threadIdx.x;
+    for (int64_t k0 = 0; k0 < nsp; k0 += 256) {
+        const int64_t k = k0 + threadIdx.x;
         int64_t cnt = 0;
-        if (p < R.nrp) {
-            const int64_t row = p / R.ntx, xt = p % R.ntx;
-            const int64_t s0 = row * R.ex + xt * 64, s1 = s0 + min((int64_t)64, (int64_t)R.ex - xt * 64);
-            for (int64_t s = s0; s < s1; ++s) cnt += (bm[s >> 3] >> (s & 7)) & 1;
+        if (k < nsp) {
+            const int64_t z = k / nb, b = k - z * nb;
+            const int64_t s0 = z * plane + b * band, s1 = b + 1 < nb ? s0 + band : (z + 1) * plane;
+            int64_t s = s0;
+            for (; s < s1 && (s & 7); ++s) cnt += (bm[s >> 3] >> (s & 7)) & 1;
+            for (; s + 8 <= s1; s += 8) cnt += __popc(bm[s >> 3]);
+            for (; s < s1; ++s) cnt += (bm[s >> 3] >> (s & 7)) & 1;
         }
         int64_t total;
         const int64_t ex = block_excl64(cnt, &total);
-        if (p < R.nrp) esc_rp[R.rp_base + p] = carry + ex;
+        if (k < nsp) esc_sp[R.sp_base + k] = carry + ex;
         carry += total;
-        __syncthreads();
     }
 }
 
-__device__ __forceinline__ int64_t ld_cg64(const int64_t *p) { return __ldcg(p); }
+// ---- band tiles.  A tile is (full rows x, a band of bty rows y, a chunk of
+// btz planes z) of one region: <= BCAP samples, int64 in shared memory.
+// Tile-local prefixes along x (rows are whole), y and z give T; then
+//   u(x,y,z) = T + [Fy(x,z) - Fy(x,z0-1)] + Fz(x,y)
+// with Fy = last row of the band above (planes z0-1..z1-1) and Fz = last
+// plane of the chunk before.  All int64 (modular like the reference's
+// cumsum), so every canonical stream decodes exactly.  Tiles wait only on
+// those two neighbours, both on the previous wavefront diagonal b + c, so
+// taking tiles in diagonal order from a ticket cannot deadlock; a tile
+// publishes its own faces right after the wait (a few adds per column)
+// and only then writes its samples, so a chain hop costs one face update.
+constexpr int BCAP = 6144;   // samples per tile
+constexpr int BDF = 2048;    // dF entries (btz * ex) when a tile has a band above
+constexpr int BSEGM = 64;    // planes per tile
+constexpr int BUMAX = 2176;  // 16-byte units per tile (5 B/sample + per-plane slack), >= BDF
+constexpr int BUPT = (BUMAX + 255) / 256;
 
-// the 3D wavefront: one CTA per tile of <= 65 x 9 x 9 samples (64/8/8 plus
-// the region's trailing ghost sample in the last tile of each axis), taken in
-// wavefront-diagonal order from an atomic ticket; waits for the x-, y- and
-// z-neighbour's published faces.
-constexpr int TXM = 65, TYM = 9, TZM = 9;          // tile capacity
-constexpr int FXN = (TZM + 1) * (TYM + 1);         // S(x1-1, y0-1..y1-1, z0-1..z1-1)
-constexpr int FYN = (TZM + 1) * TXM;               // S(x0..x1-1, y1-1, z0-1..z1-1)
-constexpr int FZN = TYM * TXM;                     // S(x0..x1-1, y0..y1-1, z1-1)
-constexpr int FACE_N = FXN + FYN + FZN;
-constexpr int SEGW = 11;                           // row segments per warp (81 / 8)
-constexpr int UNITS_W = 256;                       // units per warp (>= 11 * 22)
+__device__ __forceinline__ int seg_of(const int32_t *base, int nseg, int g) {
+    int lo = 0, hi = nseg - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (base[mid] <= g) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
 
-__device__ __forceinline__ int tile_lo(int t, int step) { return t * step; }
-__device__ __forceinline__ int tile_hi(int t, int nt, int step, int ext) { return t == nt - 1 ? ext : (t + 1) * step; }
-
-__global__ void __launch_bounds__(256) k_lorenzo3d(const DecReg *__restrict__ regs,
-                                                   const int32_t *__restrict__ tile_reg,
-                                                   const uint8_t *__restrict__ blob,
-                                                   const int64_t *__restrict__ rp_byte,
-                                                   const int64_t *__restrict__ rp_skip,
-                                                   const int64_t *__restrict__ esc_rp,
-                                                   int64_t *__restrict__ faces, int32_t *__restrict__ tflag,
-                                                   unsigned long long *__restrict__ ticket,
-                                                   const int32_t *__restrict__ order,
-                                                   double *__restrict__ out) {
-    extern __shared__ __align__(16) int64_t dyn_s[];  // S[TZM][TYM][TXM]
-    int64_t(*S)[TYM][TXM] = reinterpret_cast<int64_t(*)[TYM][TXM]>(dyn_s);
-    __shared__ int64_t Fx[TZM + 1][TYM + 1];
-    __shared__ int64_t Fy[TZM + 1][TXM];
-    __shared__ int64_t Fz[TYM][TXM];
-    __shared__ int64_t Ayz[TZM][TYM];
-    __shared__ int64_t ucnt[8][UNITS_W];
-    __shared__ int64_t sg_lo[8][SEGW], sg_hi[8][SEGW], sg_ub[8][SEGW], sg_skip[8][SEGW];
-    __shared__ int32_t sg_base[8][SEGW + 1];
-    __shared__ int64_t s_item;
-    if (threadIdx.x == 0) s_item = order[atomicAdd(ticket, 1ull)];
+__global__ void __launch_bounds__(256) k_band(const DecReg *__restrict__ regs, const int32_t *__restrict__ tile_reg,
+                                              const uint8_t *__restrict__ blob,
+                                              const int64_t *__restrict__ sp_byte,
+                                              const int64_t *__restrict__ sp_skip,
+                                              const int64_t *__restrict__ esc_sp, int64_t *__restrict__ faces,
+                                              int32_t *__restrict__ tflag, unsigned long long *__restrict__ ticket,
+                                              const int32_t *__restrict__ order, double *__restrict__ out) {
+    extern __shared__ __align__(16) int64_t Q[];  // [nzv][nyv][rs]
+    __shared__ int64_t ucnt[BUMAX];               // unit sample offsets; later dF[nzv][ex]
+    __shared__ int64_t s_lo[BSEGM], s_hi[BSEGM], s_ub[BSEGM], s_off[BSEGM];
+    __shared__ int32_t s_base[BSEGM + 1];
+    __shared__ int64_t s_tile;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) s_tile = order[atomicAdd(ticket, 1ull)];
     __syncthreads();
-    const int64_t tile = s_item;
+    const int64_t tile = s_tile;
     const DecReg &R = regs[tile_reg[tile]];
     if (!((R.codec == 1 || R.codec == 2) && R.err == 0 && !R.slow)) return;
+    const int nb = R.tny, ex = R.ex, ey = R.ey, rs = R.rs, bty = R.bty, btz = R.btz;
     const int64_t local = tile - R.tile_base;
-    const int tx = (int)(local % R.tnx);
-    const int64_t l2 = local / R.tnx;
-    const int ty = (int)(l2 % R.tny), tz = (int)(l2 / R.tny);
-    const int x0 = tile_lo(tx, 64), x1 = tile_hi(tx, R.tnx, 64, R.ex);
-    const int y0 = tile_lo(ty, 8), y1 = tile_hi(ty, R.tny, 8, R.ey);
-    const int z0 = tile_lo(tz, 8), z1 = tile_hi(tz, R.tnz, 8, R.ez);
-    const int nxv = x1 - x0, nyv = y1 - y0, nzv = z1 - z0;
-    const int nrs = nyv * nzv;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int b = (int)(local % nb), c = (int)(local / nb);
+    const int y0 = b * bty, z0 = c * btz;
+    const int nyv = min(bty, ey - y0), nzv = min(btz, R.ez - z0);
+    const int L = nyv * ex;       // samples per plane segment
+    const int PL = nyv * rs;      // smem words per plane
     const int64_t hi = (int64_t)(R.poff + R.plen);
-    const int64_t rp_end = R.rp_base + R.nrp;
-    const int64_t nrows = (int64_t)R.ey * R.ez;
+    const int64_t sp_end = R.sp_base + (int64_t)R.ez * nb;
 
-    int64_t *Sf = &S[0][0][0];
-    for (int i = threadIdx.x; i < TZM * TYM * TXM; i += 256) Sf[i] = 0;
-    // ---- 1. tokens -> q.  Warp w owns row segments rs = w, w+8, ... (rs = zz*nyv + yy);
-    //         its units (16 aligned bytes) are spread over all 32 lanes.
-    const int nseg = nrs > warp ? (nrs - warp + 7) >> 3 : 0;
-    {
-        int nun = 0;
-        if (lane < nseg) {
-            const int rs = warp + 8 * lane, zz = rs / nyv, yy = rs - zz * nyv;
-            const int64_t row = (int64_t)(z0 + zz) * R.ey + (y0 + yy);
-            const int64_t p = R.rp_base + row * R.ntx + (x0 >> 6);
-            const int64_t b0 = rp_byte[p];
-            const int64_t pe = x1 < R.ex ? R.rp_base + row * R.ntx + (x1 >> 6)
-                                         : (row + 1 < nrows ? R.rp_base + (row + 1) * R.ntx : rp_end);
-            const int64_t b1 = pe < rp_end ? min(hi, rp_byte[pe] + 11) : hi;
-            const int64_t ub = R.abase + ((b0 - R.abase) & ~15ll);
-            sg_lo[warp][lane] = b0;
-            sg_hi[warp][lane] = b1;
-            sg_ub[warp][lane] = ub;
-            sg_skip[warp][lane] = rp_skip[p];
-            nun = (int)((b1 - ub + 15) >> 4);
+    for (int i = tid; i < nzv * PL; i += 256) Q[i] = 0;
+    // ---- segments (one per plane) and their 16-byte units
+    if (warp == 0) {
+        int nun[2] = {0, 0};
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int j = lane + 32 * h;
+            if (j < nzv) {
+                const int64_t k = R.sp_base + (int64_t)(z0 + j) * nb + b;
+                const int64_t b0 = sp_byte[k];
+                const int64_t b1 = k + 1 < sp_end ? min(hi, sp_byte[k + 1] + 11) : hi;
+                const int64_t ub = R.abase + ((b0 - R.abase) & ~15ll);
+                s_lo[j] = b0;
+                s_hi[j] = b1;
+                s_ub[j] = ub;
+                s_off[j] = sp_skip[k];
+                nun[h] = (int)((b1 - ub + 15) >> 4);
+            }
         }
-        int inc = nun;
+        int i0 = nun[0];  // lane owns j = lane and lane + 32: scan in two halves
+#pragma unroll
         for (int off = 1; off < 32; off <<= 1) {
-            const int o = __shfl_up_sync(0xFFFFFFFFu, inc, off);
-            if (lane >= off) inc += o;
+            const int o = __shfl_up_sync(0xFFFFFFFFu, i0, off);
+            if (lane >= off) i0 += o;
         }
-        if (lane < nseg) sg_base[warp][lane] = inc - nun;
-        if (lane == 31) sg_base[warp][nseg] = inc;
+        const int tot0 = __shfl_sync(0xFFFFFFFFu, i0, 31);
+        int i1 = nun[1];
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int o = __shfl_up_sync(0xFFFFFFFFu, i1, off);
+            if (lane >= off) i1 += o;
+        }
+        const int tot1 = __shfl_sync(0xFFFFFFFFu, i1, 31);
+        if (lane < nzv) s_base[lane] = i0 - nun[0];
+        if (lane + 32 < nzv) s_base[lane + 32] = tot0 + i1 - nun[1];
+        if (lane == 0) s_base[nzv] = tot0 + tot1;
     }
-    __syncwarp();
-    const int U = nseg ? sg_base[warp][nseg] : 0;
-    for (int g = lane; g < U; g += 32) {
-        int i = 0;
-        while (i + 1 < nseg && sg_base[warp][i + 1] <= g) ++i;
-        const int64_t u0 = sg_ub[warp][i] + 16 * (int64_t)(g - sg_base[warp][i]);
+    __syncthreads();
+    const int U = min(s_base[nzv], BUMAX);  // bounded for canonical streams (checked on the host side)
+    // ---- pass 1: samples per unit
+    for (int g = tid; g < U; g += 256) {
+        const int j = seg_of(s_base, nzv, g);
+        const int64_t u0 = s_ub[j] + 16 * (int64_t)(g - s_base[j]);
         uint32_t w[8];
         load_units(blob, u0, w);
-        const UnitMasks m = unit_masks(w, u0, sg_lo[warp][i], sg_hi[warp][i]);
-        ucnt[warp][g] = unit_count(m, blob, u0);
+        ucnt[g] = unit_count(unit_masks(w, u0, s_lo[j], s_hi[j]), blob, u0);
     }
-    __syncwarp();
-    if (lane < nseg) {  // exclusive scan of the segment's unit counts, minus the skip
-        int64_t acc = -sg_skip[warp][lane];
-        for (int g = sg_base[warp][lane]; g < sg_base[warp][lane + 1]; ++g) {
-            const int64_t t = ucnt[warp][g];
-            ucnt[warp][g] = acc;
-            acc += t;
-        }
+    __syncthreads();
+    {  // exclusive scan over all units (thread t owns units [t*BUPT, t*BUPT + BUPT))
+        const int g0 = tid * BUPT;
+        int64_t sum = 0;
+#pragma unroll
+        for (int i = 0; i < BUPT; ++i)
+            if (g0 + i < U) sum += ucnt[g0 + i];
+        int64_t run = block_excl64(sum, nullptr);
+#pragma unroll
+        for (int i = 0; i < BUPT; ++i)
+            if (g0 + i < U) {
+                const int64_t t = ucnt[g0 + i];
+                ucnt[g0 + i] = run;
+                run += t;
+            }
     }
-    __syncwarp();
-    __syncthreads();  // S zeroed
-    for (int g = lane; g < U; g += 32) {
-        int i = 0;
-        while (i + 1 < nseg && sg_base[warp][i + 1] <= g) ++i;
-        int64_t at = ucnt[warp][g];
-        if (at >= nxv) continue;
-        const int rs = warp + 8 * i, zz = rs / nyv, yy = rs - zz * nyv;
-        const int64_t u0 = sg_ub[warp][i] + 16 * (int64_t)(g - sg_base[warp][i]);
+    __syncthreads();
+    if (tid < nzv) s_off[tid] = (s_base[tid] < U ? ucnt[s_base[tid]] : 0) + s_off[tid];  // base + skip
+    __syncthreads();
+    // ---- pass 2: scatter the literals of every unit into its plane
+    for (int g = tid; g < U; g += 256) {
+        const int j = seg_of(s_base, nzv, g);
+        int64_t at = ucnt[g] - s_off[j];
+        if (at >= L) continue;
+        const int64_t u0 = s_ub[j] + 16 * (int64_t)(g - s_base[j]);
         uint32_t w[8];
         load_units(blob, u0, w);
-        const UnitMasks m = unit_masks(w, u0, sg_lo[warp][i], sg_hi[warp][i]);
+        const UnitMasks m = unit_masks(w, u0, s_lo[j], s_hi[j]);
         uint32_t T = m.lit | m.len;
-        int64_t *srow = &S[zz][yy][0];
-        while (T && at < nxv) {
+        int64_t *q = Q + j * PL;
+        int row = 0, x = 0;
+        if (at >= 0) {
+            row = (int)at / ex;
+            x = (int)at - row * ex;
+        }
+        while (T && at < L) {
             const int e = __ffs(T) - 1;
             T &= T - 1;
             uint64_t v;
-            if ((m.E >> (e - 1)) & 1u) {  // one-byte token (the common case)
-                v = __ldg(blob + u0 - 16 + e) & 0x7Fu;
-            } else {
-                v = unit_token_value(blob, m.E, e, u0);
-            }
+            if ((m.E >> (e - 1)) & 1u) v = __ldg(blob + u0 - 16 + e) & 0x7Fu;  // one-byte token
+            else v = unit_token_value(blob, m.E, e, u0);
             if ((m.len >> e) & 1u) {
                 at += (int64_t)v;
-            } else {
-                if (at >= 0) {
-                    const uint64_t zz2 = v - 1;
-                    srow[at] = (int64_t)(zz2 >> 1) ^ -(int64_t)(zz2 & 1);
+                if (at >= 0 && at < L) {
+                    row = (int)at / ex;
+                    x = (int)at - row * ex;
                 }
-                ++at;
+                continue;
+            }
+            if (at >= 0) {
+                const uint64_t zz = v - 1;
+                q[row * rs + x] = (int64_t)(zz >> 1) ^ -(int64_t)(zz & 1);
+                if (++x == ex) {
+                    x = 0;
+                    ++row;
+                }
+            }
+            if (++at == 0) row = x = 0;
+        }
+    }
+    __syncthreads();
+    // ---- x-prefix (rows are whole)
+    const int rows = nzv * nyv;
+    if (ex <= 96) {
+        for (int r = tid; r < rows; r += 256) {
+            int64_t *p = Q + r * rs;
+            int64_t acc = 0;
+            for (int xx = 0; xx < ex; ++xx) {
+                acc += p[xx];
+                p[xx] = acc;
+            }
+        }
+    } else {
+        for (int r = warp; r < rows; r += 8) {
+            int64_t *p = Q + r * rs;
+            int64_t carry = 0;
+            for (int x0 = 0; x0 < ex; x0 += 32) {
+                const int xx = x0 + lane;
+                int64_t v = xx < ex ? p[xx] : 0;
+#pragma unroll
+                for (int off = 1; off < 32; off <<= 1) {
+                    const int64_t o = __shfl_up_sync(0xFFFFFFFFu, v, off);
+                    if (lane >= off) v += o;
+                }
+                v += carry;
+                if (xx < ex) p[xx] = v;
+                carry = __shfl_sync(0xFFFFFFFFu, v, 31);
             }
         }
     }
     __syncthreads();
-    // ---- 2. local 3D prefix: x (warp per row: x = lane, lane+32, 64), y, z
-    int zz2 = warp / nyv, yy2 = warp - zz2 * nyv;
-    for (int r = warp; r < nrs; r += 8) {
-        const int zz = zz2, yy = yy2;
-        yy2 += 8;
-        while (yy2 >= nyv) {
-            yy2 -= nyv;
-            ++zz2;
-        }
-        int64_t *row = &S[zz][yy][0];
-        int64_t a = row[lane], b = row[lane + 32];
-        for (int off = 1; off < 32; off <<= 1) {
-            const int64_t oa = __shfl_up_sync(0xFFFFFFFFu, a, off);
-            const int64_t ob = __shfl_up_sync(0xFFFFFFFFu, b, off);
-            if (lane >= off) {
-                a += oa;
-                b += ob;
-            }
-        }
-        b += __shfl_sync(0xFFFFFFFFu, a, 31);
-        const int64_t tot = __shfl_sync(0xFFFFFFFFu, b, 31);
-        row[lane] = a;
-        row[lane + 32] = b;
-        if (lane == 0) row[64] += tot;
-    }
-    __syncthreads();
-    for (int t = threadIdx.x; t < nzv * TXM; t += 256) {
-        const int zz = t / TXM, x = t - zz * TXM;
+    // ---- y-prefix (columns (plane, x))
+    for (int t = tid; t < ex * nzv; t += 256) {
+        const int j = t / ex, xx = t - j * ex;
+        int64_t *p = Q + j * PL + xx;
         int64_t acc = 0;
         for (int yy = 0; yy < nyv; ++yy) {
-            acc += S[zz][yy][x];
-            S[zz][yy][x] = acc;
+            acc += p[yy * rs];
+            p[yy * rs] = acc;
         }
     }
     __syncthreads();
-    for (int t = threadIdx.x; t < nyv * TXM; t += 256) {
-        const int yy = t / TXM, x = t - yy * TXM;
+    // ---- z-prefix (columns (y, x))
+    for (int t = tid; t < L; t += 256) {
+        const int yy = t / ex, xx = t - yy * ex;
+        int64_t *p = Q + yy * rs + xx;
         int64_t acc = 0;
-        for (int zz = 0; zz < nzv; ++zz) {
-            acc += S[zz][yy][x];
-            S[zz][yy][x] = acc;
+        for (int j = 0; j < nzv; ++j) {
+            acc += p[j * PL];
+            p[j * PL] = acc;
         }
     }
-    // ---- 3. neighbour faces
-    const int64_t nb_x = tx > 0 ? tile - 1 : -1;
-    const int64_t nb_y = ty > 0 ? tile - R.tnx : -1;
-    const int64_t nb_z = tz > 0 ? tile - (int64_t)R.tnx * R.tny : -1;
-    if (threadIdx.x == 0) {
-        if (nb_x >= 0) while (ld_acquire32(tflag + nb_x) == 0) __nanosleep(20);
-        if (nb_y >= 0) while (ld_acquire32(tflag + nb_y) == 0) __nanosleep(20);
-        if (nb_z >= 0) while (ld_acquire32(tflag + nb_z) == 0) __nanosleep(20);
+    // ---- neighbours
+    if (tid == 0) {
+        if (b > 0) while (ld_acquire32(tflag + tile - 1) == 0) __nanosleep(20);
+        if (c > 0) while (ld_acquire32(tflag + tile - nb) == 0) __nanosleep(20);
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < FXN; i += 256) (&Fx[0][0])[i] = nb_x >= 0 ? ld_cg64(faces + nb_x * FACE_N + i) : 0;
-    for (int i = threadIdx.x; i < FYN; i += 256)
-        (&Fy[0][0])[i] = nb_y >= 0 ? ld_cg64(faces + nb_y * FACE_N + FXN + i) : 0;
-    for (int i = threadIdx.x; i < FZN; i += 256)
-        (&Fz[0][0])[i] = nb_z >= 0 ? ld_cg64(faces + nb_z * FACE_N + FXN + FYN + i) : 0;
-    __syncthreads();
-    for (int i = threadIdx.x; i < TZM * TYM; i += 256) {
-        const int zz = i / TYM, yy = i - zz * TYM;
-        Ayz[zz][yy] = Fx[zz + 1][yy + 1] - Fx[zz + 1][0] - Fx[0][yy + 1] + Fx[0][0];
+    const int64_t fn = R.face_n;
+    const int64_t fzo = (int64_t)(btz + 1) * ex;  // Fz part after Fy in a face record
+    int64_t *dF = ucnt;                           // [nzv][ex], <= BDF entries
+    if (b > 0) {
+        const int64_t *Fy = faces + R.face_base + (local - 1) * fn;
+        for (int t = tid; t < ex * nzv; t += 256) {
+            const int j = t / ex, xx = t - j * ex;
+            dF[t] = __ldcg(Fy + (j + 1) * ex + xx) - __ldcg(Fy + xx);
+        }
     }
     __syncthreads();
-    // ---- 4. S = T + A(y,z) + [Fy(x,z) - Fy(x,z0-1)] + Fz(x,y)
+    // ---- own faces: Fz' = u(plane z1-1), Fy' = u(row y1-1, planes z0-1..z1-1)
+    const int64_t *Fz = faces + R.face_base + (local - nb) * fn + fzo;
+    int64_t *myF = faces + R.face_base + local * fn;
     {
-        int zz = warp / nyv, yy = warp - zz * nyv;
-        for (int r = warp; r < nrs; r += 8) {
-            const int64_t a = Ayz[zz][yy];
-            for (int x = lane; x < nxv; x += 32) S[zz][yy][x] += a + (Fy[zz + 1][x] - Fy[0][x]) + Fz[yy][x];
-            yy += 8;
-            while (yy >= nyv) {
-                yy -= nyv;
-                ++zz;
+        const int lastp = (nzv - 1) * PL;
+        for (int t = tid; t < L; t += 256) {
+            const int yy = t / ex, xx = t - yy * ex;
+            const int64_t fz = c > 0 ? __ldcg(Fz + t) : 0;
+            myF[fzo + t] = Q[lastp + yy * rs + xx] + (b > 0 ? dF[(nzv - 1) * ex + xx] : 0) + fz;
+            if (yy == nyv - 1) {
+                myF[xx] = fz;
+                for (int j = 0; j < nzv; ++j)
+                    myF[(j + 1) * ex + xx] = Q[j * PL + yy * rs + xx] + (b > 0 ? dF[j * ex + xx] : 0) + fz;
             }
         }
-    }
-    __syncthreads();
-    // ---- 5. publish this tile's high faces (consumers index with their own extents)
-    int64_t *my = faces + tile * FACE_N;
-    const int xl = nxv - 1;
-    for (int i = threadIdx.x; i < FXN; i += 256) {
-        const int zp = i / (TYM + 1), yp = i - zp * (TYM + 1);
-        if (zp > nzv || yp > nyv) continue;
-        int64_t v;
-        if (zp == 0) v = yp == 0 ? Fy[0][xl] : Fz[yp - 1][xl];
-        else if (yp == 0) v = Fy[zp][xl];
-        else v = S[zp - 1][yp - 1][xl];
-        my[i] = v;
-    }
-    for (int i = threadIdx.x; i < FYN; i += 256) {
-        const int zp = i / TXM, x = i - zp * TXM;
-        if (zp > nzv || x >= nxv) continue;
-        my[FXN + i] = zp == 0 ? Fz[nyv - 1][x] : S[zp - 1][nyv - 1][x];
-    }
-    for (int i = threadIdx.x; i < FZN; i += 256) {
-        const int yy = i / TXM, x = i - yy * TXM;
-        if (yy >= nyv || x >= nxv) continue;
-        my[FXN + FYN + i] = S[nzv - 1][yy][x];
     }
     __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) st_release32(tflag + tile, 1);
-    // ---- 6. reconstruction (escapes overwritten in raster order)
+    if (tid == 0) st_release32(tflag + tile, 1);
+    // ---- reconstruction
     const double twoe = 2.0 * R.e;
-    const bool esc = R.codec == 2 && R.nesc > 0;
-    const uint8_t *bm = blob + R.poff;
-    const uint8_t *ev = blob + R.poff + ((R.n + 7) >> 3);
-    int zz3 = warp / nyv, yy3 = warp - zz3 * nyv;
-    for (int r = warp; r < nrs; r += 8) {
-        const int zz = zz3, yy = yy3;
-        yy3 += 8;
-        while (yy3 >= nyv) {
-            yy3 -= nyv;
-            ++zz3;
+    const int64_t zstride = (int64_t)ex * ey;
+    double *obase = out + R.out_off + ((int64_t)z0 * ey + y0) * ex;
+    for (int t = tid; t < L; t += 256) {
+        const int yy = t / ex, xx = t - yy * ex;
+        const int64_t fz = c > 0 ? __ldcg(Fz + t) : 0;
+        const int64_t *p = Q + yy * rs + xx;
+        if (b > 0) {
+            for (int j = 0; j < nzv; ++j) __stcs(obase + j * zstride + t, (double)(p[j * PL] + dF[j * ex + xx] + fz) * twoe);
+        } else {
+            for (int j = 0; j < nzv; ++j) __stcs(obase + j * zstride + t, (double)(p[j * PL] + fz) * twoe);
         }
-        const int64_t rowi = (int64_t)(z0 + zz) * R.ey + (y0 + yy);
-        const int64_t srow = rowi * R.ex + x0;
-        double *o = out + R.out_off + srow;
-        uint64_t em = 0;
-        uint32_t em64 = 0;
-        int64_t ebase = 0;
-        if (esc) {
-            const int sh = (int)(srow & 7);
-            const int64_t byte0 = srow >> 3, nbm = (R.n + 7) >> 3;
-            uint32_t bt = 0;
-            if (lane < 10 && byte0 + lane < nbm) bt = bm[byte0 + lane];
-            uint64_t lo64 = 0;
-            for (int k = 0; k < 8; ++k) lo64 |= (uint64_t)__shfl_sync(0xFFFFFFFFu, bt, k) << (8 * k);
-            const uint64_t b8 = __shfl_sync(0xFFFFFFFFu, bt, 8), b9 = __shfl_sync(0xFFFFFFFFu, bt, 9);
-            const uint64_t hi16 = b8 | (b9 << 8);
-            em = sh ? (lo64 >> sh) | (hi16 << (64 - sh)) : lo64;
-            em64 = (uint32_t)((hi16 >> sh) & 1u);
-            if (nxv < 64) em &= (1ull << nxv) - 1;
-            if (nxv < 65) em64 = 0;
-            ebase = esc_rp[R.rp_base + rowi * R.ntx + (x0 >> 6)];
-        }
-        for (int x = lane; x < nxv; x += 32) {
-            double v = (double)S[zz][yy][x] * twoe;
-            if (esc) {
-                const bool isesc = x < 64 ? ((em >> x) & 1) : em64;
-                if (isesc) {
-                    const int64_t rank = ebase + (x < 64 ? __popcll((long long)(em & ((1ull << x) - 1)))
-                                                         : __popcll((long long)em));
-                    uint8_t tmp[8];
-                    for (int k = 0; k < 8; ++k) tmp[k] = ev[8 * rank + k];
-                    memcpy(&v, tmp, 8);
+    }
+    // ---- codec 2: escaped samples keep their f64 value (raster order rank)
+    if (R.codec == 2 && R.nesc > 0) {
+        __syncthreads();
+        const uint8_t *bm = blob + R.poff;
+        const uint8_t *ev = bm + ((R.n + 7) >> 3);
+        const uint32_t lt = (1u << lane) - 1u;
+        for (int j = warp; j < nzv; j += 8) {
+            int64_t rank = esc_sp[R.sp_base + (int64_t)(z0 + j) * nb + b];
+            const int64_t s0 = ((int64_t)(z0 + j) * ey + y0) * ex;
+            for (int p0 = 0; p0 < L; p0 += 32) {
+                const int p = p0 + lane;
+                const int64_t s = s0 + p;
+                const bool bit = p < L && ((bm[s >> 3] >> (s & 7)) & 1);
+                const uint32_t bal = __ballot_sync(0xFFFFFFFFu, bit);
+                if (bit) {
+                    const uint8_t *src = ev + 8 * (rank + __popc(bal & lt));
+                    uint64_t bits = 0;
+                    for (int k = 0; k < 8; ++k) bits |= (uint64_t)src[k] << (8 * k);
+                    obase[j * zstride + p] = __longlong_as_double((long long)bits);
                 }
+                rank += __popc(bal);
             }
-            o[x] = v;
         }
     }
 }
@@ -1196,14 +1167,15 @@ __global__ void __launch_bounds__(256) k_lorenzo3d(const DecReg *__restrict__ re
 // ------------------------------------------------------------------ host
 struct DecPlan {
     std::vector<DecReg> regs;
-    int64_t nchunks = 0, nseg = 0, nitems = 0, ncarry = 0, ntiles = 0, nrp = 0;
+    int64_t nchunks = 0, nseg = 0, nitems = 0, ncarry = 0, ntiles = 0, nsp = 0, nface = 0;
     int max_rows_ex = 0;
     size_t ws = 0;
     DecReg *d_regs;
     CrcSeg *segs;
     uint32_t *seg_raw;
     int64_t *chunk_samples, *seg_byte, *seg_skip, *esc_base, *carry, *flags;
-    int64_t *rp_byte, *rp_skip, *esc_rp, *faces;
+    int64_t *sp_byte, *sp_skip, *esc_sp, *thr_cnt;
+    int64_t *faces;
     int32_t *tflag, *chunk_reg, *tile_reg, *order;
     int64_t *pair_base;
     std::vector<int64_t> h_pair_base;
@@ -1218,9 +1190,44 @@ static int dec_rows_for(int ex) {
     return rows < 1 ? 0 : rows;
 }
 
+// band tile shape of a region: rows padded to an odd smem stride; whole
+// planes per tile when they fit, otherwise bands x chunks balanced so the
+// wavefront (bands + chunks) stays short
+static bool band_shape(DecReg &R) {
+    const int rs = R.ex | 1;
+    if (rs > BCAP) return false;
+    const int K = BCAP / rs;  // rows (y * z) per tile
+    int bty, btz;
+    if ((int64_t)R.ey * R.ez <= K && R.ez <= BSEGM) {
+        bty = R.ey;
+        btz = R.ez;
+    } else if (R.ey <= K && K / R.ey >= 4) {
+        bty = R.ey;
+        btz = std::min({R.ez, K / R.ey, BSEGM});
+    } else {
+        const double t = std::sqrt((double)K * R.ey / std::max(1, R.ez));
+        bty = std::max(1, std::min({R.ey, K, (int)t}));
+        bty = std::max(bty, std::min({R.ey, K, 8}));
+        btz = std::max(1, std::min({R.ez, K / bty, BSEGM}));
+        bty = std::max(1, std::min(R.ey, K / btz));
+    }
+    if (bty < R.ey) {  // a band below exists: its dF (btz x ex) must fit
+        btz = std::min(btz, BDF / R.ex);
+        if (btz < 1) return false;
+    }
+    R.rs = rs;
+    R.bty = bty;
+    R.btz = btz;
+    R.tnx = 1;
+    R.tny = (int32_t)ceil_div(R.ey, bty);
+    R.tnz = (int32_t)ceil_div(R.ez, btz);
+    R.face_n = (int64_t)R.ex * (btz + 1 + bty);
+    return true;
+}
+
 static bool dec_build(const chr_dec_region_t *h, int64_t n, uintptr_t blob, DecPlan &pl) {
     pl.regs.resize(n);
-    int64_t chunk = 0, seg = 0, item = 0, carry = 0, tile = 0, rp = 0;
+    int64_t chunk = 0, seg = 0, item = 0, carry = 0, tile = 0, sp = 0, face = 0;
     for (int64_t i = 0; i < n; ++i) {
         DecReg &R = pl.regs[i];
         std::memset(&R, 0, sizeof(R));
@@ -1246,24 +1253,23 @@ static bool dec_build(const chr_dec_region_t *h, int64_t n, uintptr_t blob, DecP
         R.seg_base = seg;
         R.item_base = item;
         R.carry_base = carry;
-        R.ntx = (int32_t)ceil_div(R.ex, 64);
-        // tiles of 64 / 8 / 8 samples; the last one of each axis absorbs the
-        // trailing sample of 32k+1 extents (<= 65 / 9 / 9)
-        R.tnx = (int32_t)std::max<int64_t>(1, ceil_div(R.ex - 1, 64));
-        R.tny = (int32_t)std::max<int64_t>(1, ceil_div(R.ey - 1, 8));
-        R.tnz = (int32_t)std::max<int64_t>(1, ceil_div(R.ez - 1, 8));
         R.tile_base = tile;
-        R.rp_base = rp;
+        R.sp_base = sp;
+        R.face_base = face;
         if (R.codec == 1 || R.codec == 2) {
             R.nseg = (int64_t)R.nyt * R.ez;
             seg += R.nseg;
             item += R.nyt;
             carry += (int64_t)R.nyt * R.ez * R.ex;
             pl.max_rows_ex = std::max(pl.max_rows_ex, R.rows * R.ex);
-            R.ntiles = (int64_t)R.tnx * R.tny * R.tnz;
-            tile += R.ntiles;
-            R.nrp = (int64_t)R.ntx * R.ey * R.ez;
-            rp += R.nrp;
+            if (!band_shape(R)) {
+                R.slow = 1;  // rows wider than a band tile: generic path
+            } else {
+                R.ntiles = (int64_t)R.tny * R.tnz;
+                tile += R.ntiles;
+                sp += (int64_t)R.ez * R.tny;
+                face += R.ntiles * R.face_n;
+            }
         }
     }
     pl.nchunks = chunk;
@@ -1271,7 +1277,8 @@ static bool dec_build(const chr_dec_region_t *h, int64_t n, uintptr_t blob, DecP
     pl.nitems = item;
     pl.ncarry = carry;
     pl.ntiles = tile;
-    pl.nrp = rp;
+    pl.nsp = sp;
+    pl.nface = face;
     // tiles per (diagonal, region) -> exclusive bases in diagonal-major order
     int64_t D = 0;
     for (const DecReg &R : pl.regs)
@@ -1316,10 +1323,11 @@ static void dec_carve(DecPlan &pl, void *base, size_t cap) {
     pl.esc_base = c.take<int64_t>(pl.nseg + 1);
     pl.carry = c.take<int64_t>(pl.ncarry + 1);
     pl.flags = c.take<int64_t>(pl.nitems + 1);
-    pl.rp_byte = c.take<int64_t>(pl.nrp + 1);
-    pl.rp_skip = c.take<int64_t>(pl.nrp + 1);
-    pl.esc_rp = c.take<int64_t>(pl.nrp + 1);
-    pl.faces = c.take<int64_t>((size_t)pl.ntiles * FACE_N + 1);
+    pl.sp_byte = c.take<int64_t>(pl.nsp + 1);
+    pl.sp_skip = c.take<int64_t>(pl.nsp + 1);
+    pl.esc_sp = c.take<int64_t>(pl.nsp + 1);
+    pl.thr_cnt = c.take<int64_t>(pl.nchunks * DTHREADS + 1);
+    pl.faces = c.take<int64_t>(pl.nface + 1);
     pl.tflag = c.take<int32_t>(pl.ntiles + 1);
     pl.chunk_reg = c.take<int32_t>(pl.nchunks + 1);
     pl.tile_reg = c.take<int32_t>(pl.ntiles + 1);
@@ -1382,35 +1390,25 @@ extern "C" int chr_decode_regions(const uint8_t *d_blob, const chr_dec_region_t 
     }
     {
         CHR_PROF("k_tok_fast", st);
-        k_tok_fast<<<(unsigned)pl.nchunks, DTHREADS, 0, st>>>(pl.d_regs, pl.chunk_reg, d_blob, pl.chunk_samples);
-    }
-    {
-        CHR_PROF("k_tok_count", st);
-        k_tok_count<<<(unsigned)pl.nchunks, DTHREADS, 0, st>>>(pl.d_regs, n, d_blob, pl.chunk_samples);
+        k_tok_fast<<<(unsigned)pl.nchunks, DTHREADS, 0, st>>>(pl.d_regs, pl.chunk_reg, d_blob, pl.chunk_samples,
+                                                              pl.thr_cnt);
     }
     {
         CHR_PROF("k_tok_scan", st);
-        k_tok_scan<<<(unsigned)ceil_div(n, 128), 128, 0, st>>>(pl.d_regs, n, pl.chunk_samples);
+        k_tok_scan<<<(unsigned)ceil_div(n, 128), 128, 0, st>>>(pl.d_regs, n, pl.chunk_samples, 0);
     }
-    {
-        CHR_PROF("k_rp_locate", st);
-        k_rp_locate<<<(unsigned)pl.nchunks, DTHREADS, 0, st>>>(pl.d_regs, pl.chunk_reg, d_blob, pl.chunk_samples,
-                                                               pl.rp_byte, pl.rp_skip);
-    }
-    {
-        CHR_PROF("k_locate", st);
-        k_locate<<<(unsigned)pl.nchunks, DTHREADS, 0, st>>>(pl.d_regs, n, d_blob, pl.chunk_samples,
-                                                            pl.seg_byte, pl.seg_skip);
-    }
-    {
-        CHR_PROF("k_esc_rp", st);
-        k_esc_rp<<<(unsigned)n, 256, 0, st>>>(pl.d_regs, d_blob, pl.esc_rp);
-    }
-    {
-        CHR_PROF("k_esc_base", st);
-        k_esc_base<<<(unsigned)n, 256, 0, st>>>(pl.d_regs, n, d_blob, pl.esc_base);
-    }
+    // ---- band path (canonical streams)
     if (pl.ntiles > 0) {
+        {
+            CHR_PROF("k_seg_locate", st);
+            k_seg_locate<<<(unsigned)pl.nchunks, DTHREADS, 0, st>>>(pl.d_regs, pl.chunk_reg, d_blob,
+                                                                    pl.chunk_samples, pl.thr_cnt, pl.sp_byte,
+                                                                    pl.sp_skip);
+        }
+        {
+            CHR_PROF("k_esc_seg", st);
+            k_esc_seg<<<(unsigned)n, 256, 0, st>>>(pl.d_regs, d_blob, pl.esc_sp);
+        }
         const int64_t npairs = pl.ndiag * n;
         CHR_CUDA_TRY(cudaMemcpyAsync(pl.pair_base, pl.h_pair_base.data(), sizeof(int64_t) * npairs,
                                      cudaMemcpyHostToDevice, st));
@@ -1418,11 +1416,32 @@ extern "C" int chr_decode_regions(const uint8_t *d_blob, const chr_dec_region_t 
             CHR_PROF("k_tile_order", st);
             k_tile_order<<<(unsigned)ceil_div(npairs, 256), 256, 0, st>>>(pl.d_regs, pl.pair_base, npairs, n, pl.order);
         }
-        const int smem3 = (int)(sizeof(int64_t) * TZM * TYM * TXM);
-        CHR_CUDA_TRY(cudaFuncSetAttribute(k_lorenzo3d, cudaFuncAttributeMaxDynamicSharedMemorySize, smem3));
-        CHR_PROF("k_lorenzo3d", st);
-        k_lorenzo3d<<<(unsigned)pl.ntiles, 256, smem3, st>>>(pl.d_regs, pl.tile_reg, d_blob, pl.rp_byte, pl.rp_skip, pl.esc_rp,
-                                                         pl.faces, pl.tflag, pl.ticket3, pl.order, d_out);
+        const int smem = (int)(sizeof(int64_t) * BCAP);
+        CHR_CUDA_TRY(cudaFuncSetAttribute(k_band, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        {
+            CHR_PROF("k_band", st);
+            k_band<<<(unsigned)pl.ntiles, 256, smem, st>>>(pl.d_regs, pl.tile_reg, d_blob, pl.sp_byte, pl.sp_skip,
+                                                           pl.esc_sp, pl.faces, pl.tflag, pl.ticket3, pl.order,
+                                                           d_out);
+        }
+    }
+    // ---- generic path (non-canonical streams, rows wider than a band tile)
+    {
+        CHR_PROF("k_tok_count", st);
+        k_tok_count<<<(unsigned)pl.nchunks, DTHREADS, 0, st>>>(pl.d_regs, n, d_blob, pl.chunk_samples);
+    }
+    {
+        CHR_PROF("k_tok_scan", st);
+        k_tok_scan<<<(unsigned)ceil_div(n, 128), 128, 0, st>>>(pl.d_regs, n, pl.chunk_samples, 1);
+    }
+    {
+        CHR_PROF("k_locate", st);
+        k_locate<<<(unsigned)pl.nchunks, DTHREADS, 0, st>>>(pl.d_regs, n, d_blob, pl.chunk_samples,
+                                                            pl.seg_byte, pl.seg_skip);
+    }
+    {
+        CHR_PROF("k_esc_base", st);
+        k_esc_base<<<(unsigned)n, 256, 0, st>>>(pl.d_regs, n, d_blob, pl.esc_base);
     }
     if (pl.nitems > 0) {
         const size_t smem = (size_t)pl.max_rows_ex * 16 + DWIN;

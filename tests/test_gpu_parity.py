@@ -289,10 +289,36 @@ def test_noncanonical_stream_uses_generic_path():
     assert np.array_equal(got, G.decompress(blk).ravel(order="F"))
 
 
-@pytest.mark.parametrize("shape", [(64, 8, 8), (65, 9, 17), (130, 3, 2), (1, 1, 300), (200, 1, 1), (3, 70, 40)])
+@pytest.mark.parametrize("shape", [(64, 8, 8), (65, 9, 17), (130, 3, 2), (1, 1, 300), (200, 1, 1), (3, 70, 40),
+                                   (33, 33, 300), (65, 161, 12), (300, 40, 9), (1, 300, 300), (97, 2, 500),
+                                   (8200, 2, 2)])
 def test_decode_tile_shapes(shape):
+    """Band tiles: whole planes, bands x chunks, warp-per-row prefixes, and
+    rows too wide for a tile (generic path)."""
     g = np.random.default_rng(sum(shape) + 1).normal(size=shape).cumsum(axis=0)
     for e in (1e-3, 0.3):
         blk = G.compress(g, e)
         ref = O.decompress_block(blk.to_bytes())[1]
         assert np.array_equal(G.decompress(blk).ravel(order="F"), ref), (shape, e)
+
+
+def test_decode_wide_quanta_use_int64_path():
+    """sum|q| >= 2^31 in a region: the int32 band tiles hand it to the int64
+    generic path (|u| < 2^27 still, so no escapes)."""
+    g = np.random.default_rng(5).uniform(-1e7, 1e7, size=(20, 20, 20))
+    blk = G.compress(g, 0.5)
+    assert blk.codec_id == 1
+    ref = O.decompress_block(blk.to_bytes())[1]
+    assert np.array_equal(G.decompress(blk).ravel(order="F"), ref)
+
+
+@pytest.mark.parametrize("shape", [(40, 50, 60), (33, 33, 200), (130, 70, 3)])
+def test_decode_escapes_in_band_tiles(shape):
+    rng = np.random.default_rng(sum(shape))
+    g = rng.normal(size=shape).cumsum(axis=2)
+    idx = rng.choice(g.size, size=40, replace=False)
+    g.reshape(-1)[idx] = rng.uniform(1e11, 1e12, size=40)
+    blk = G.compress(g, 1e-2)
+    assert blk.codec_id == 2
+    ref = O.decompress_block(blk.to_bytes())[1]
+    assert np.array_equal(G.decompress(blk).ravel(order="F"), ref)
