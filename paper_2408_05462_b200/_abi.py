@@ -17,7 +17,7 @@ import torch
 from . import exceptions as errors
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libchr.so")
+LIB_PATH = os.environ.get("CHR_LIB_PATH") or os.path.join(_HERE, "libchr.so")
 
 CHR_OK = 0
 CHR_E_PARAMETER = 1

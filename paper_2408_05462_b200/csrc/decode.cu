@@ -71,6 +71,7 @@ struct DecReg {
     // fast (canonical-stream) path: band tiles (full rows x bty rows x btz planes)
     int64_t abase;                 // 16-byte aligned chunk origin (blob-relative)
     int32_t tnx, tny, tnz;         // tiles per axis (tnx = 1, tny = bands, tnz = chunks)
+    int32_t doff, pad2;            // step offset of the region's wavefront (k_tile_order)
     int32_t bty, btz, rs;          // band rows, chunk planes, smem row stride
     int64_t tile_base, ntiles;
     int64_t sp_base;               // segment index: ez * tny entries
@@ -725,27 +726,27 @@ __global__ void k_fill_maps(const DecReg *__restrict__ regs, int64_t nreg, int32
 
 constexpr int UPT = (int)(DCB / (16 * DTHREADS));  // 16-byte units per thread
 
-// tile order for k_band: all regions' tiles grouped by wavefront
-// diagonal d = tx + ty + tz (every dependency of a tile lies on d - 1, so
-// taking tiles in this order from a ticket cannot deadlock and keeps every
-// region's wavefront advancing at once).  One thread per (diagonal, region)
-// pair writes its tiles at pair_base.
+// tile order for k_band: critical path first.  A tile (band b, chunk c)
+// of a region with tny bands and tnz chunks has b + c predecessors on its
+// dependency chain and (tny - 1 - b) + (tnz - 1 - c) successors; tiles are
+// grouped by the global step d = b + c + doff with doff = Dmax - (tny +
+// tnz - 2), so every region's wavefront ENDS on the last step and the
+// longest chains start first.  Every dependency of a tile lies on step
+// d - 1, so taking tiles in this order from a ticket cannot deadlock.  One
+// thread per (step, region) pair writes its tiles at pair_base.
 __global__ void k_tile_order(const DecReg *__restrict__ regs, const int64_t *__restrict__ pair_base,
                              int64_t npairs, int64_t nreg, int32_t *__restrict__ order) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= npairs) return;
-    const int64_t d = i / nreg, r = i % nreg;
+    const int64_t r = i % nreg;
     const DecReg &R = regs[r];
     if (R.ntiles == 0) return;
+    const int d = (int)(i / nreg) - R.doff;
+    if (d < 0) return;
     int64_t k = pair_base[i];
-    const int nx = R.tnx, ny = R.tny, nz = R.tnz;
-    for (int tz = max(0, (int)d - (nx - 1) - (ny - 1)); tz <= min(nz - 1, (int)d); ++tz) {
-        const int rem = (int)d - tz;
-        for (int ty = max(0, rem - (nx - 1)); ty <= min(ny - 1, rem); ++ty) {
-            const int tx = rem - ty;
-            order[k++] = (int32_t)(R.tile_base + ((int64_t)tz * ny + ty) * nx + tx);
-        }
-    }
+    const int ny = R.tny, nz = R.tnz;
+    for (int tz = max(0, d - (ny - 1)); tz <= min(nz - 1, d); ++tz)
+        order[k++] = (int32_t)(R.tile_base + (int64_t)tz * ny + (d - tz));
 }
 
 // samples per chunk (fast path); flags non-canonical regions
@@ -901,6 +902,110 @@ __device__ __forceinline__ int seg_of(const int32_t *base, int nseg, int g) {
     return lo;
 }
 
+// ---- band tokenizer: 24-byte windows {8 look-back | 16 own} held in six
+// registers; bit j <-> byte j, own bytes are bits 8..23.  Canonical streams
+// (validated by k_tok_fast) only, so no error checks here.
+struct Win24 {
+    uint32_t w[6];
+    uint32_t E, lit, len;  // end bytes; literal / run-length token ends (own)
+};
+
+__device__ __forceinline__ Win24 win24(const uint8_t *__restrict__ blob, int64_t u0, int64_t lo, int64_t hi) {
+    Win24 W;
+    const uint4 cur = __ldg(reinterpret_cast<const uint4 *>(blob + u0));
+    uint2 prv = make_uint2(0, 0);
+    if (u0 >= 8) prv = __ldg(reinterpret_cast<const uint2 *>(blob + u0 - 8));
+    W.w[0] = prv.x; W.w[1] = prv.y;
+    W.w[2] = cur.x; W.w[3] = cur.y; W.w[4] = cur.z; W.w[5] = cur.w;
+    uint32_t E = 0, Z = 0;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+        E |= word_end4(W.w[k]) << (4 * k);
+        Z |= word_zero4(W.w[k]) << (4 * k);
+    }
+    const int64_t nlo = lo - (u0 - 8), nhi = hi - (u0 - 8);  // bits [nlo, nhi) are stream bytes
+    const uint32_t lob = nlo <= 0 ? 0u : (nlo >= 24 ? 0xFFFFFFu : ((1u << nlo) - 1u));
+    const uint32_t hib = nhi >= 24 ? 0u : (nhi <= 0 ? 0xFFFFFFu : (0xFFFFFFu & ~((1u << nhi) - 1u)));
+    const uint32_t out = lob | hib;
+    E = (E | out) & 0xFFFFFFu;
+    Z &= ~out & 0xFFFFFFu;
+    const uint32_t C = ~E & 0xFFFFFFu;
+    const uint32_t Lend = (C + (Z << 1)) & ~C;
+    const uint32_t own = 0xFFFF00u & ~out;
+    W.E = E;
+    W.len = Lend & ~Z & own;
+    W.lit = E & ~Z & ~Lend & own;
+    return W;
+}
+
+__device__ __forceinline__ uint32_t win_byte(const Win24 &W, int j) {  // j static after unrolling
+    return (W.w[j >> 2] >> (8 * (j & 3))) & 0xFFu;
+}
+
+// samples of the tokens ending in the unit's own bytes
+__device__ __forceinline__ int64_t win24_count(const Win24 &W) {
+    int64_t c = __popc(W.lit);
+    uint32_t Lm = W.len;
+    while (Lm) {
+        const int e = __ffs(Lm) - 1;
+        Lm &= Lm - 1;
+        const uint32_t below = W.E & ((1u << e) - 1u);
+        const int s = 32 - __clz(below);
+        uint64_t v = 0;
+#pragma unroll
+        for (int j = 3; j < 24; ++j)  // static byte positions; token bytes are s..e
+            if (j >= s && j <= e) v |= (uint64_t)(win_byte(W, j) & 0x7Fu) << (7 * (j - s));
+        c += (int64_t)v;
+    }
+    return c;
+}
+
+// one unit -> literals into the plane `q` (positions count samples from the
+// segment start; PAD planes have row stride ex + 1).  Branch-free over the 16
+// own positions: H holds the LEB128 payload of bytes e-4..e, so the token
+// ending at e has value H >> 7 (5 - len).
+template <bool PAD>
+__device__ __forceinline__ void band_scatter_unit(const Win24 &W, int64_t at64, int L, int ex, uint64_t M,
+                                                  int64_t *__restrict__ q) {
+    int64_t at = at64;
+    int idx = (int)at, x = 0;
+    if (PAD && at >= 0) {
+        const int row = (int)(((uint64_t)at * M) >> 32);
+        x = (int)at - row * ex;
+        idx = row * (ex + 1) + x;
+    }
+    uint64_t H = 0;
+#pragma unroll
+    for (int j = 3; j < 8; ++j) H = (H >> 7) | ((uint64_t)(win_byte(W, j) & 0x7Fu) << 28);
+#pragma unroll
+    for (int e = 8; e < 24; ++e) {
+        H = (H >> 7) | ((uint64_t)(win_byte(W, e) & 0x7Fu) << 28);
+        const bool lit = (W.lit >> e) & 1u, run = (W.len >> e) & 1u;
+        if (!(lit | run)) continue;
+        const uint32_t below = W.E & ((1u << e) - 1u);
+        const int len = e - (32 - __clz(below)) + 1;
+        const uint64_t v = H >> (7 * (5 - len));
+        if (lit) {
+            const uint64_t zz = v - 1;
+            if ((uint64_t)at < (uint64_t)L) q[idx] = (int64_t)(zz >> 1) ^ -(int64_t)(zz & 1);
+            ++at;
+            ++idx;
+            if (PAD && ++x == ex) {
+                x = 0;
+                ++idx;
+            }
+        } else {
+            at += (int64_t)v;
+            idx = (int)min(at, (int64_t)L);
+            if (PAD && at >= 0 && at < L) {
+                const int row = (int)(((uint64_t)at * M) >> 32);
+                x = (int)at - row * ex;
+                idx = row * (ex + 1) + x;
+            }
+        }
+    }
+}
+
 __global__ void __launch_bounds__(256) k_band(const DecReg *__restrict__ regs, const int32_t *__restrict__ tile_reg,
                                               const uint8_t *__restrict__ blob,
                                               const int64_t *__restrict__ sp_byte,
@@ -972,9 +1077,7 @@ __global__ void __launch_bounds__(256) k_band(const DecReg *__restrict__ regs, c
     for (int g = tid; g < U; g += 256) {
         const int j = seg_of(s_base, nzv, g);
         const int64_t u0 = s_ub[j] + 16 * (int64_t)(g - s_base[j]);
-        uint32_t w[8];
-        load_units(blob, u0, w);
-        ucnt[g] = unit_count(unit_masks(w, u0, s_lo[j], s_hi[j]), blob, u0);
+        ucnt[g] = win24_count(win24(blob, u0, s_lo[j], s_hi[j]));
     }
     __syncthreads();
     {  // exclusive scan over all units (thread t owns units [t*BUPT, t*BUPT + BUPT))
@@ -996,50 +1099,20 @@ __global__ void __launch_bounds__(256) k_band(const DecReg *__restrict__ regs, c
     if (tid < nzv) s_off[tid] = (s_base[tid] < U ? ucnt[s_base[tid]] : 0) + s_off[tid];  // base + skip
     __syncthreads();
     // ---- pass 2: scatter the literals of every unit into its plane
+    const uint64_t M = ((1ull << 32) + (uint64_t)ex - 1) / (uint64_t)ex;  // row = (at * M) >> 32
     for (int g = tid; g < U; g += 256) {
         const int j = seg_of(s_base, nzv, g);
-        int64_t at = ucnt[g] - s_off[j];
+        const int64_t at = ucnt[g] - s_off[j];
         if (at >= L) continue;
         const int64_t u0 = s_ub[j] + 16 * (int64_t)(g - s_base[j]);
-        uint32_t w[8];
-        load_units(blob, u0, w);
-        const UnitMasks m = unit_masks(w, u0, s_lo[j], s_hi[j]);
-        uint32_t T = m.lit | m.len;
-        int64_t *q = Q + j * PL;
-        int row = 0, x = 0;
-        if (at >= 0) {
-            row = (int)at / ex;
-            x = (int)at - row * ex;
-        }
-        while (T && at < L) {
-            const int e = __ffs(T) - 1;
-            T &= T - 1;
-            uint64_t v;
-            if ((m.E >> (e - 1)) & 1u) v = __ldg(blob + u0 - 16 + e) & 0x7Fu;  // one-byte token
-            else v = unit_token_value(blob, m.E, e, u0);
-            if ((m.len >> e) & 1u) {
-                at += (int64_t)v;
-                if (at >= 0 && at < L) {
-                    row = (int)at / ex;
-                    x = (int)at - row * ex;
-                }
-                continue;
-            }
-            if (at >= 0) {
-                const uint64_t zz = v - 1;
-                q[row * rs + x] = (int64_t)(zz >> 1) ^ -(int64_t)(zz & 1);
-                if (++x == ex) {
-                    x = 0;
-                    ++row;
-                }
-            }
-            if (++at == 0) row = x = 0;
-        }
+        const Win24 W = win24(blob, u0, s_lo[j], s_hi[j]);
+        if (rs == ex) band_scatter_unit<false>(W, at, L, ex, M, Q + j * PL);
+        else band_scatter_unit<true>(W, at, L, ex, M, Q + j * PL);
     }
     __syncthreads();
     // ---- x-prefix (rows are whole)
     const int rows = nzv * nyv;
-    if (ex <= 96) {
+    if (rows >= 64) {
         for (int r = tid; r < rows; r += 256) {
             int64_t *p = Q + r * rs;
             int64_t acc = 0;
@@ -1068,8 +1141,13 @@ __global__ void __launch_bounds__(256) k_band(const DecReg *__restrict__ regs, c
     }
     __syncthreads();
     // ---- y-prefix (columns (plane, x))
+    auto split = [&](int t, int &hi_, int &lo_) {  // t = hi_ * ex + lo_
+        hi_ = (int)(((uint64_t)t * M) >> 32);
+        lo_ = t - hi_ * ex;
+    };
     for (int t = tid; t < ex * nzv; t += 256) {
-        const int j = t / ex, xx = t - j * ex;
+        int j, xx;
+        split(t, j, xx);
         int64_t *p = Q + j * PL + xx;
         int64_t acc = 0;
         for (int yy = 0; yy < nyv; ++yy) {
@@ -1078,66 +1156,93 @@ __global__ void __launch_bounds__(256) k_band(const DecReg *__restrict__ regs, c
         }
     }
     __syncthreads();
-    // ---- z-prefix (columns (y, x))
+    // ---- z-prefix (columns (y, x); with rs == ex the plane index is t itself)
+    const bool pad = rs != ex;
     for (int t = tid; t < L; t += 256) {
-        const int yy = t / ex, xx = t - yy * ex;
-        int64_t *p = Q + yy * rs + xx;
+        int yy = 0, xx = t;
+        if (pad) split(t, yy, xx);
+        int64_t *p = Q + (pad ? yy * rs + xx : t);
         int64_t acc = 0;
         for (int j = 0; j < nzv; ++j) {
             acc += p[j * PL];
             p[j * PL] = acc;
         }
     }
-    // ---- neighbours
-    if (tid == 0) {
-        if (b > 0) while (ld_acquire32(tflag + tile - 1) == 0) __nanosleep(20);
-        if (c > 0) while (ld_acquire32(tflag + tile - nb) == 0) __nanosleep(20);
-    }
-    __syncthreads();
+    // ---- band above (same chunk): its inclusive faces give dF(z, x) = Fy(z) - Fy(z0 - 1)
+    // Face record of a tile: [Fy' (btz+1) x ex | I (bty x ex)] with
+    // Fy' = u(row y1-1, planes z0-1..z1-1) and I = u(plane z1-1); flag 2 =
+    // published.
     const int64_t fn = R.face_n;
-    const int64_t fzo = (int64_t)(btz + 1) * ex;  // Fz part after Fy in a face record
-    int64_t *dF = ucnt;                           // [nzv][ex], <= BDF entries
-    if (b > 0) {
-        const int64_t *Fy = faces + R.face_base + (local - 1) * fn;
-        for (int t = tid; t < ex * nzv; t += 256) {
-            const int j = t / ex, xx = t - j * ex;
-            dF[t] = __ldcg(Fy + (j + 1) * ex + xx) - __ldcg(Fy + xx);
-        }
-    }
-    __syncthreads();
-    // ---- own faces: Fz' = u(plane z1-1), Fy' = u(row y1-1, planes z0-1..z1-1)
-    const int64_t *Fz = faces + R.face_base + (local - nb) * fn + fzo;
+    const int64_t io = (int64_t)(btz + 1) * ex;
+    int64_t *dF = ucnt;  // [nzv][ex], <= BDF entries
     int64_t *myF = faces + R.face_base + local * fn;
-    {
-        const int lastp = (nzv - 1) * PL;
-        for (int t = tid; t < L; t += 256) {
-            const int yy = t / ex, xx = t - yy * ex;
-            const int64_t fz = c > 0 ? __ldcg(Fz + t) : 0;
-            myF[fzo + t] = Q[lastp + yy * rs + xx] + (b > 0 ? dF[(nzv - 1) * ex + xx] : 0) + fz;
-            if (yy == nyv - 1) {
-                myF[xx] = fz;
-                for (int j = 0; j < nzv; ++j)
-                    myF[(j + 1) * ex + xx] = Q[j * PL + yy * rs + xx] + (b > 0 ? dF[j * ex + xx] : 0) + fz;
-            }
-        }
+    if (b > 0) {
+        if (tid == 0)
+            while (ld_acquire32(tflag + tile - 1) != 2) __nanosleep(20);
+        __syncthreads();
+        const int64_t *Fy = faces + R.face_base + (local - 1) * fn;
+        for (int t = tid; t < ex * nzv; t += 256) dF[t] = __ldcg(Fy + ex + t) - __ldcg(Fy + (t - (t / ex) * ex));
     }
-    __threadfence();
     __syncthreads();
-    if (tid == 0) st_release32(tflag + tile, 1);
-    // ---- reconstruction
+    const int lastp = (nzv - 1) * PL;
+    auto qidx = [&](int t, int &xx) {
+        int yy = 0;
+        xx = t;
+        if (pad || b > 0) split(t, yy, xx);
+        return pad ? yy * rs + xx : t;
+    };
+    auto publish_col = [&](int t, int64_t fz) {
+        int xx;
+        const int qi = qidx(t, xx);
+        myF[io + t] = Q[lastp + qi] + (b > 0 ? dF[(nzv - 1) * ex + xx] : 0) + fz;
+        if (t >= L - ex) {  // last row (xx is the column only when split ran)
+            const int xl = t - (L - ex);
+            myF[xl] = fz;
+            for (int j = 0; j < nzv; ++j) myF[(j + 1) * ex + xl] = Q[j * PL + qi] + (b > 0 ? dF[j * ex + xl] : 0) + fz;
+        }
+    };
     const double twoe = 2.0 * R.e;
     const int64_t zstride = (int64_t)ex * ey;
     double *obase = out + R.out_off + ((int64_t)z0 * ey + y0) * ex;
-    for (int t = tid; t < L; t += 256) {
-        const int yy = t / ex, xx = t - yy * ex;
-        const int64_t fz = c > 0 ? __ldcg(Fz + t) : 0;
-        const int64_t *p = Q + yy * rs + xx;
+    auto recon_col = [&](int t, int64_t fz) {
+        int xx;
+        const int64_t *p = Q + qidx(t, xx);
+        double *o = obase + t;
         if (b > 0) {
-            for (int j = 0; j < nzv; ++j) __stcs(obase + j * zstride + t, (double)(p[j * PL] + dF[j * ex + xx] + fz) * twoe);
+            const int64_t *d = dF + xx;
+            for (int j = 0; j < nzv; ++j) __stcs(o + j * zstride, (double)(p[j * PL] + d[j * ex] + fz) * twoe);
         } else {
-            for (int j = 0; j < nzv; ++j) __stcs(obase + j * zstride + t, (double)(p[j * PL] + fz) * twoe);
+            for (int j = 0; j < nzv; ++j) __stcs(o + j * zstride, (double)(p[j * PL] + fz) * twoe);
+        }
+    };
+    auto release = [&](int f) {  // the barrier orders all face stores before thread 0's fence + flag
+        __syncthreads();
+        if (tid == 0) {
+            __threadfence();
+            st_release32(tflag + tile, f);
+        }
+    };
+    // ---- chunk before (same band): its inclusive faces give the carry Fz
+    const int64_t *Ip = faces + R.face_base + (local - nb) * fn + io;
+    if (c > 0 && tid == 0)
+        while (ld_acquire32(tflag + tile - nb) != 2) __nanosleep(20);
+    __syncthreads();
+    constexpr int FU = 4;  // columns per thread per round: all face loads first
+    for (int t0 = tid; t0 < L; t0 += 256 * FU) {
+        int64_t fzv[FU];
+#pragma unroll
+        for (int k = 0; k < FU; ++k) {
+            const int t = t0 + 256 * k;
+            fzv[k] = (c > 0 && t < L) ? __ldcg(Ip + t) : 0;
+        }
+#pragma unroll
+        for (int k = 0; k < FU; ++k) {
+            const int t = t0 + 256 * k;
+            if (t < L) publish_col(t, fzv[k]);
         }
     }
+    release(2);
+    for (int t = tid; t < L; t += 256) recon_col(t, c > 0 ? __ldcg(Ip + t) : 0);
     // ---- codec 2: escaped samples keep their f64 value (raster order rank)
     if (R.codec == 2 && R.nesc > 0) {
         __syncthreads();
@@ -1279,22 +1384,22 @@ static bool dec_build(const chr_dec_region_t *h, int64_t n, uintptr_t blob, DecP
     pl.ntiles = tile;
     pl.nsp = sp;
     pl.nface = face;
-    // tiles per (diagonal, region) -> exclusive bases in diagonal-major order
+    // tiles per (step, region) -> exclusive bases in step-major order
     int64_t D = 0;
     for (const DecReg &R : pl.regs)
-        if (R.ntiles) D = std::max<int64_t>(D, (int64_t)R.tnx + R.tny + R.tnz - 2);
+        if (R.ntiles) D = std::max<int64_t>(D, (int64_t)R.tny + R.tnz - 2);
     pl.ndiag = pl.ntiles ? D + 1 : 0;
     std::vector<int64_t> cnt((size_t)(pl.ndiag * n) + 1, 0);  // [r][d]
     std::vector<int64_t> diff((size_t)pl.ndiag + 2);
     for (int64_t i = 0; i < n; ++i) {
-        const DecReg &R = pl.regs[i];
+        DecReg &R = pl.regs[i];
         if (!R.ntiles) continue;
+        R.doff = (int32_t)(D - (R.tny + R.tnz - 2));
         std::fill(diff.begin(), diff.end(), 0);
-        for (int tz = 0; tz < R.tnz; ++tz)
-            for (int ty = 0; ty < R.tny; ++ty) {
-                diff[ty + tz] += 1;
-                diff[ty + tz + R.tnx] -= 1;
-            }
+        for (int tz = 0; tz < R.tnz; ++tz) {
+            diff[R.doff + tz] += 1;
+            diff[R.doff + tz + R.tny] -= 1;
+        }
         int64_t run = 0;
         for (int64_t d = 0; d < pl.ndiag; ++d) {
             run += diff[d];

@@ -291,7 +291,7 @@ def test_noncanonical_stream_uses_generic_path():
 
 @pytest.mark.parametrize("shape", [(64, 8, 8), (65, 9, 17), (130, 3, 2), (1, 1, 300), (200, 1, 1), (3, 70, 40),
                                    (33, 33, 300), (65, 161, 12), (300, 40, 9), (1, 300, 300), (97, 2, 500),
-                                   (8200, 2, 2)])
+                                   (8200, 2, 2), (33, 200, 60), (64, 40, 100), (32, 32, 400)])
 def test_decode_tile_shapes(shape):
     """Band tiles: whole planes, bands x chunks, warp-per-row prefixes, and
     rows too wide for a tile (generic path)."""
