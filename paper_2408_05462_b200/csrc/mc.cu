@@ -14,11 +14,12 @@
 //   (owned crossing edges in earlier cells) + (its first-appearance rank in
 //   the owner's triangle row), and both come from tables + one scan.
 //
-//   k_mc_count   warp per 64-cell row piece: triangles, owned vertices
+//   k_mc_count2  CTA = 64 cells x 8 rows x MZC planes: triangles and owned
+//                vertices per 64-cell row piece (ballot row masks)
 //   k_mc_reduce / k_mc_grids / k_mc_down   chunked exclusive scans
-//   k_mc_emit    CTA = 64 cells x 8 rows, marching z with a halo row, a
-//                halo column and a halo plane in shared memory, so every
-//                owner cell's (code, vertex base) is local.
+//   k_mc_emit2   same tiles plus a halo row, column and plane, so every
+//                owner cell's (code, vertex base) is local; the active
+//                cells of a row expand into dense per-lane work items.
 #include <algorithm>
 #include <cstring>
 #include <mutex>
@@ -29,7 +30,7 @@
 
 namespace chr {
 
-constexpr int MTX = 64, MTY = 8, MZC = 16, MNW = MTY + 1;
+constexpr int MTX = 64, MTY = 8, MZC = 16;
 constexpr int64_t MCH = 1024;
 
 // Bourke corner index of unit offset (x, y, z) (mc_tables.py:8-12)
@@ -40,6 +41,7 @@ struct __align__(16) McTables {
     uint8_t ntri[256];
     uint8_t owncnt[256][8];   // owned crossing edges per (code, boundary flags)
     int8_t rank[256][8][12];  // first-appearance rank among owned edges, -1 if not owned
+    int8_t inv[256][8][12];   // owned edge of rank r
     uint16_t cross[256];      // crossing-edge mask
     uint8_t edge_axis[12];
     uint8_t edge_low[12][3];
@@ -86,6 +88,9 @@ static void mc_tables_host() {
                 if (T.rank[c][f][e] < 0 && owned_by(e, f)) T.rank[c][f][e] = (int8_t)cnt++;
             }
             T.owncnt[c][f] = (uint8_t)cnt;
+            std::memset(T.inv[c][f], -1, 12);
+            for (int e = 0; e < 12; ++e)
+                if (T.rank[c][f][e] >= 0) T.inv[c][f][T.rank[c][f][e]] = (int8_t)e;
         }
     }
 }
@@ -151,44 +156,6 @@ __device__ __forceinline__ int cell_code(const double *__restrict__ g, int64_t n
 
 __device__ __forceinline__ int bflags(int cx, int cy, int cz) {
     return (cx == 0 ? 1 : 0) | (cy == 0 ? 2 : 0) | (cz == 0 ? 4 : 0);
-}
-
-// warp per row piece: triangle and owned-vertex counts
-__global__ void __launch_bounds__(256) k_mc_count(const double *__restrict__ grids, const McGrid *__restrict__ G,
-                                                  int64_t ng, int64_t npieces_total, double k,
-                                                  const McTables *__restrict__ T,
-                                                  McPieceCnt *__restrict__ cnt) {
-    const int lane = threadIdx.x & 31;
-    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-    for (int64_t p = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); p < npieces_total; p += warps) {
-        const McGrid &g = G[find_grid(G, ng, p, 0)];
-        const int64_t lp = p - g.piece_base;
-        if (lp >= g.npieces) continue;  // chunk padding
-        const int xt = (int)(lp % g.ntx);
-        const int64_t rr = lp / g.ntx;
-        const int cy = (int)(rr % g.ncy), cz = (int)(rr / g.ncy);
-        const double *gp = grids + g.goff;
-        const int64_t nxy = (int64_t)g.nx * g.ny;
-        int t = 0, v = 0;
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int cx = xt * MTX + h * 32 + lane;
-            if (cx < g.ncx) {
-                double c[8];
-                const int code = cell_code(gp, g.nx, nxy, cx, cy, cz, k, c);
-                t += T->ntri[code];
-                v += T->owncnt[code][bflags(cx, cy, cz)];
-            }
-        }
-        t = __reduce_add_sync(0xFFFFFFFFu, t);
-        v = __reduce_add_sync(0xFFFFFFFFu, v);
-        if (lane == 0) {
-            McPieceCnt o;
-            o.tri = t;
-            o.vert = v;
-            cnt[p] = o;
-        }
-    }
 }
 
 __global__ void __launch_bounds__(256) k_mc_reduce(const McPieceCnt *__restrict__ cnt, McPieceBase *__restrict__ chunk) {
@@ -333,150 +300,6 @@ __device__ __forceinline__ double world(double origin, double lat, double spacin
     return __dadd_rn(origin, __dmul_rn(lat, spacing));
 }
 
-// emit: see header.  sC/sV: (code, vertex base) of cells x0-1 .. x0+63 for
-// rows cy0-1 .. cy0+7 at planes cz-1 and cz (3-deep ring over planes).
-__global__ void __launch_bounds__(MNW * 32) k_mc_emit(const double *__restrict__ grids,
-                                                      const McGrid *__restrict__ G, int64_t ng, double k,
-                                                      const McTables *__restrict__ T,
-                                                      const McPieceBase *__restrict__ base,
-                                                      double *__restrict__ verts, int32_t *__restrict__ tris) {
-    __shared__ uint8_t sC[3][MNW][MTX + 1];
-    __shared__ int64_t sV[3][MNW][MTX + 1];
-    __shared__ McGrid g;
-    __shared__ McTables tb;
-    {
-        const int4 *src = reinterpret_cast<const int4 *>(T);
-        int4 *dst = reinterpret_cast<int4 *>(&tb);
-        for (int i = threadIdx.x; i < (int)(sizeof(McTables) / 16); i += blockDim.x) dst[i] = src[i];
-    }
-    const int64_t item = blockIdx.x;
-    if (threadIdx.x == 0) g = G[find_grid(G, ng, item, 2)];
-    __syncthreads();
-    const int64_t local = item - g.item_base;
-    const int nyt = (g.ncy + MTY - 1) / MTY;
-    const int xt = (int)(local % g.ntx);
-    const int64_t r2 = local / g.ntx;
-    const int yt = (int)(r2 % nyt), zc = (int)(r2 / nyt);
-    const int x0 = xt * MTX, y0 = yt * MTY, z0 = zc * MZC;
-    const int z1 = min(z0 + MZC, g.ncz);
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int cy = y0 - 1 + w;
-    const bool rowok = cy >= 0 && cy < g.ncy;
-    const double *gp = grids + g.goff;
-    const int64_t nxy = (int64_t)g.nx * g.ny;
-    const int cxs[2] = {x0 + lane, x0 + 32 + lane};
-    const int zs = z0 > 0 ? z0 - 1 : z0;
-    for (int cz = zs; cz < z1; ++cz) {
-        const int buf = cz % 3;
-        double cA[8], cB[8], cH[8];
-        int codeA = 0, codeB = 0, codeH = 0, ownA = 0, ownB = 0, ownH = 0, ntA = 0, ntB = 0;
-        const bool okA = rowok && cxs[0] < g.ncx, okB = rowok && cxs[1] < g.ncx;
-        const bool okH = rowok && lane == 0 && x0 > 0;
-        if (okA) {
-            codeA = cell_code(gp, g.nx, nxy, cxs[0], cy, cz, k, cA);
-            ownA = tb.owncnt[codeA][bflags(cxs[0], cy, cz)];
-            ntA = tb.ntri[codeA];
-        }
-        if (okB) {
-            codeB = cell_code(gp, g.nx, nxy, cxs[1], cy, cz, k, cB);
-            ownB = tb.owncnt[codeB][bflags(cxs[1], cy, cz)];
-            ntB = tb.ntri[codeB];
-        }
-        if (okH) {
-            codeH = cell_code(gp, g.nx, nxy, x0 - 1, cy, cz, k, cH);
-            ownH = tb.owncnt[codeH][bflags(x0 - 1, cy, cz)];
-        }
-        // exclusive scans (cells A: 0..31, B: 32..63) of owned vertices and triangles
-        int sA = ownA, sB = ownB, tA = ntA, tB = ntB;
-        for (int off = 1; off < 32; off <<= 1) {
-            const int a = __shfl_up_sync(0xFFFFFFFFu, sA, off), b = __shfl_up_sync(0xFFFFFFFFu, sB, off);
-            const int c = __shfl_up_sync(0xFFFFFFFFu, tA, off), d = __shfl_up_sync(0xFFFFFFFFu, tB, off);
-            if (lane >= off) {
-                sA += a;
-                sB += b;
-                tA += c;
-                tB += d;
-            }
-        }
-        const int totV = __shfl_sync(0xFFFFFFFFu, sA, 31), totT = __shfl_sync(0xFFFFFFFFu, tA, 31);
-        sA -= ownA;
-        sB = sB - ownB + totV;
-        tA -= ntA;
-        tB = tB - ntB + totT;
-        McPieceBase pb;
-        pb.tri = 0;
-        pb.vert = 0;
-        if (rowok) pb = base[g.piece_base + ((int64_t)cz * g.ncy + cy) * g.ntx + xt];
-        sC[buf][w][1 + lane] = (uint8_t)codeA;
-        sC[buf][w][33 + lane] = (uint8_t)codeB;
-        sV[buf][w][1 + lane] = pb.vert + sA;
-        sV[buf][w][33 + lane] = pb.vert + sB;
-        if (lane == 0) {
-            sC[buf][w][0] = (uint8_t)codeH;
-            sV[buf][w][0] = pb.vert - ownH;
-        }
-        __syncthreads();
-        if (cz < z0 || w == 0 || !rowok) continue;
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const bool ok = h == 0 ? okA : okB;
-            if (!ok) continue;
-            const int code = h == 0 ? codeA : codeB;
-            const int nt = tb.ntri[code];
-            if (nt == 0) continue;
-            const int cx = cxs[h];
-            const double *c = h == 0 ? cA : cB;
-            const int col = 1 + cx - x0;
-            const int f = bflags(cx, cy, cz);
-            const int64_t vb = sV[buf][w][col];
-            // owned vertices (first-appearance order)
-            const int8_t *rk = tb.rank[code][f];
-            for (int e = 0; e < 12; ++e) {
-                const int r = rk[e];
-                if (r < 0) continue;
-                const int a = tb.edge_axis[e];
-                const int lx = tb.edge_low[e][0], ly = tb.edge_low[e][1], lz = tb.edge_low[e][2];
-                const int c0 = CHR_CORNER_OF(lx, ly, lz);
-                const int c1 = CHR_CORNER_OF(lx + (a == 0), ly + (a == 1), lz + (a == 2));
-                const double s0 = c[c0], s1 = c[c1];
-                const double den = __dadd_rn(s1, -s0);
-                const double t = den == 0.0 ? 0.0 : __ddiv_rn(__dadd_rn(k, -s0), den);
-                double lat[3] = {(double)(cx + lx), (double)(cy + ly), (double)(cz + lz)};
-                lat[a] = __dadd_rn(lat[a], t);
-                double *o = verts + 3 * (g.vert_base + vb + r);
-                o[0] = world(g.origin[0], lat[0], g.spacing[0]);
-                o[1] = world(g.origin[1], lat[1], g.spacing[1]);
-                o[2] = world(g.origin[2], lat[2], g.spacing[2]);
-            }
-            // triangles
-            const int64_t tb0 = g.tri_base + pb.tri + (h == 0 ? tA : tB);
-            int32_t *to = tris + 3 * tb0;
-            for (int s = 0; s < 3 * nt; ++s) {
-                const int e = tb.tri[code][s];
-                const int a = tb.edge_axis[e];
-                int l[3] = {tb.edge_low[e][0], tb.edge_low[e][1], tb.edge_low[e][2]};
-                const int cc[3] = {cx, cy, cz};
-                int d[3] = {0, 0, 0};
-#pragma unroll
-                for (int q = 0; q < 3; ++q) {
-                    if (q == a) continue;
-                    if (l[q] == 0 && cc[q] >= 1) {
-                        d[q] = -1;
-                        l[q] = 1;
-                    }
-                }
-                const int e2 = tb.edge_id[a][l[0]][l[1]][l[2]];
-                const int ob = (cz + d[2]) % 3;
-                const int orow = w + d[1], ocol = col + d[0];
-                const int ocode = sC[ob][orow][ocol];
-                const int of = bflags(cx + d[0], cy + d[1], cz + d[2]);
-                const int64_t vid = sV[ob][orow][ocol] + tb.rank[ocode][of][e2];
-                to[s] = (int32_t)(g.vert_base + vid);
-            }
-        }
-    }
-}
-
 // ------------------------------------------------------------------ v2 tiles
 // CTA = 64 cells x 8 cell rows, marching z over up to MZC cell planes.  Every
 // f64 sample row is loaded once per plane by one warp (coalesced), turned
@@ -600,6 +423,7 @@ __global__ void __launch_bounds__(288, 5) k_mc_count2(const double *__restrict__
 // 3-deep ring; cells rows y0-1..y0+7 x columns x0-1..x0+63 (65) with their
 // (code, vertex base) in a 3-deep ring, so every owner is local.
 constexpr int EW = 10;  // warps: sample rows y0-1 .. y0+8
+__device__ __forceinline__ int qb_of(int b) { return b == 2 ? 0 : b + 1; }  // next slot of a 3-deep ring
 __global__ void __launch_bounds__(EW * 32, 3) k_mc_emit2(const double *__restrict__ grids, const McGrid *__restrict__ G,
                                                       const int32_t *__restrict__ item_grid, double k,
                                                       const McTables *__restrict__ T,
@@ -611,18 +435,26 @@ __global__ void __launch_bounds__(EW * 32, 3) k_mc_emit2(const double *__restric
     __shared__ uint8_t sC[3][EW - 1][65];
     __shared__ int64_t sV[3][EW - 1][65];
     __shared__ int32_t sT[EW - 1][65];  // triangle offset of each cell within its piece
-    __shared__ int8_t s_tri[256][16];
-    __shared__ uint8_t s_ntri[256];
-    __shared__ uint8_t s_own[256][8];
+    __shared__ __align__(16) int8_t s_tri[256][16];
+    __shared__ __align__(16) uint8_t s_ntri[256];
+    __shared__ __align__(16) uint8_t s_own[256][8];
     __shared__ uint8_t s_eax[12], s_elow[12][3];
     __shared__ int8_t s_eid[3][2][2][2];
     __shared__ McGrid g;
-    for (int i = threadIdx.x; i < 4096; i += blockDim.x) (&s_tri[0][0])[i] = (&T->tri[0][0])[i];
+    {  // tables -> shared memory, 16 bytes per thread
+        const uint4 *src = reinterpret_cast<const uint4 *>(T->tri);
+        uint4 *dst = reinterpret_cast<uint4 *>(&s_tri[0][0]);
+        for (int i = threadIdx.x; i < 256; i += blockDim.x) dst[i] = __ldg(src + i);
+        const uint4 *so = reinterpret_cast<const uint4 *>(T->owncnt);
+        uint4 *d_o = reinterpret_cast<uint4 *>(&s_own[0][0]);
+        for (int i = threadIdx.x; i < 128; i += blockDim.x) d_o[i] = __ldg(so + i);
+        const uint4 *sn = reinterpret_cast<const uint4 *>(T->ntri);
+        uint4 *dn = reinterpret_cast<uint4 *>(s_ntri);
+        if (threadIdx.x < 16) dn[threadIdx.x] = __ldg(sn + threadIdx.x);
+    }
     if (threadIdx.x < 12) s_eax[threadIdx.x] = T->edge_axis[threadIdx.x];
     if (threadIdx.x < 36) (&s_elow[0][0])[threadIdx.x] = (&T->edge_low[0][0])[threadIdx.x];
     if (threadIdx.x < 24) (&s_eid[0][0][0][0])[threadIdx.x] = (&T->edge_id[0][0][0][0])[threadIdx.x];
-    for (int i = threadIdx.x; i < 256; i += blockDim.x) s_ntri[i] = T->ntri[i];
-    for (int i = threadIdx.x; i < 2048; i += blockDim.x) (&s_own[0][0])[i] = (&T->owncnt[0][0])[i];
     const int64_t item = blockIdx.x;
     coop_copy(&g, G + __ldg(item_grid + item));
     __syncthreads();
@@ -645,6 +477,12 @@ __global__ void __launch_bounds__(EW * 32, 3) k_mc_emit2(const double *__restric
     const int cy = y0 - 1 + w;
     const bool crow = w < EW - 1 && cy >= 0 && cy < g.ncy;
     const int pstart = z0 > 0 ? z0 - 1 : 0;
+    const int64_t pb_row = g.piece_base + (int64_t)cy * g.ntx + xt;  // + cz * ncy * ntx
+    const int64_t pb_step = (int64_t)g.ncy * g.ntx;
+    McPieceBase pnext;  // piece base of the next cell plane (prefetched)
+    pnext.tri = 0;
+    pnext.vert = 0;
+    if (crow) pnext = base[pb_row + (int64_t)pstart * pb_step];
     double na = 0.0, nb = 0.0, ne = 0.0;  // prefetched plane
     {
         const double *row = gp + (int64_t)pstart * nxy + (int64_t)sy * g.nx;
@@ -677,12 +515,11 @@ __global__ void __launch_bounds__(EW * 32, 3) k_mc_emit2(const double *__restric
         if (p == pstart) continue;  // need planes cz and cz+1
         const int cz = p - 1, cb = cz % 3, qb = p % 3;
         // ---- codes, owned counts, vertex bases of cell row cy at plane cz
-        int codeA = 0, codeB = 0, ntA = 0, ntB = 0, tA = 0, tB = 0;
-        McPieceBase pbase;
-        pbase.tri = 0;
-        pbase.vert = 0;
+        int codeA = 0, codeB = 0, ntA = 0, ntB = 0, tA = 0, tB = 0, ownA = 0, ownB = 0, exA = 0, exB = 0;
+        const McPieceBase pbase = pnext;
+        if (crow && cz + 1 < z1) pnext = base[pb_row + (int64_t)(cz + 1) * pb_step];
         if (w < EW - 1) {
-            int codeH = 0, ownA = 0, ownB = 0, ownH = 0;
+            int codeH = 0, ownH = 0;
             if (crow) {
                 const uint64_t m00 = mk[cb][w], m10 = mk[cb][w + 1], m01 = mk[qb][w], m11 = mk[qb][w + 1];
                 const uint32_t h00 = mkx[cb][w], h10 = mkx[cb][w + 1], h01 = mkx[qb][w], h11 = mkx[qb][w + 1];
@@ -701,25 +538,26 @@ __global__ void __launch_bounds__(EW * 32, 3) k_mc_emit2(const double *__restric
                     codeH = code_fast(m00, h00, m10, h10, m01, h01, m11, h11, 0);
                     ownH = s_own[codeH][bflags(x0 - 1, cy, cz)];
                 }
-                pbase = base[g.piece_base + ((int64_t)cz * g.ncy + cy) * g.ntx + xt];
             }
-            int sA = ownA, sB = ownB;
-            tA = ntA;
-            tB = ntB;
+            // one scan of packed (owned | triangles << 16) for columns lane and 32 + lane
+            uint32_t pA = (uint32_t)ownA | ((uint32_t)ntA << 16), pB = (uint32_t)ownB | ((uint32_t)ntB << 16);
+#pragma unroll
             for (int off = 1; off < 32; off <<= 1) {
-                const int a = __shfl_up_sync(0xFFFFFFFFu, sA, off), b = __shfl_up_sync(0xFFFFFFFFu, sB, off);
-                const int c = __shfl_up_sync(0xFFFFFFFFu, tA, off), d = __shfl_up_sync(0xFFFFFFFFu, tB, off);
+                const uint32_t a = __shfl_up_sync(0xFFFFFFFFu, pA, off), b = __shfl_up_sync(0xFFFFFFFFu, pB, off);
                 if (lane >= off) {
-                    sA += a;
-                    sB += b;
-                    tA += c;
-                    tB += d;
+                    pA += a;
+                    pB += b;
                 }
             }
-            const int totV = __shfl_sync(0xFFFFFFFFu, sA, 31);
-            const int totT = __shfl_sync(0xFFFFFFFFu, tA, 31);
-            tA -= ntA;
-            tB = tB - ntB + totT;
+            const uint32_t totP = __shfl_sync(0xFFFFFFFFu, pA, 31);
+            pA -= (uint32_t)ownA | ((uint32_t)ntA << 16);  // exclusive
+            pB += totP - ((uint32_t)ownB | ((uint32_t)ntB << 16));
+            const int sA = (int)(pA & 0xFFFFu) + ownA, sB = (int)(pB & 0xFFFFu) + ownB - (int)(totP & 0xFFFFu);
+            const int totV = (int)(totP & 0xFFFFu);
+            tA = (int)(pA >> 16);
+            tB = (int)(pB >> 16);
+            exA = 3 * tA + (int)(pA & 0xFFFFu);  // item offsets (3 per triangle + owned vertices)
+            exB = 3 * tB + (int)(pB & 0xFFFFu);
             sC[cb][w][1 + lane] = (uint8_t)codeA;
             sC[cb][w][33 + lane] = (uint8_t)codeB;
             sV[cb][w][1 + lane] = pbase.vert + sA - ownA;
@@ -732,32 +570,35 @@ __global__ void __launch_bounds__(EW * 32, 3) k_mc_emit2(const double *__restric
         __syncthreads();
         if (cz < z0 || w == 0 || w >= EW - 1 || !crow) continue;
         {
-            // ---- emission, warp-cooperative: two active cells per step, lanes
-            //      0..14 / 16..30 take triangle slots, then owned edges
+            // ---- emission: the row's active cells expand into items (3 per
+            //      triangle, then one per owned vertex), 32 items per step;
+            //      a lane finds its cell by a shuffle binary search over the
+            //      64 exclusive item offsets
             sT[w][1 + lane] = tA;
             sT[w][33 + lane] = tB;
+            const int total = __shfl_sync(0xFFFFFFFFu, exB + 3 * ntB + ownB, 31);
             __syncwarp();
-            uint64_t act = (uint64_t)__ballot_sync(0xFFFFFFFFu, ntA > 0) |
-                           ((uint64_t)__ballot_sync(0xFFFFFFFFu, ntB > 0) << 32);
-            const int half = lane >> 4, sl = lane & 15;
-            while (act) {
-                const int i0 = __ffsll((long long)act) - 1;
-                act &= act - 1;
-                int i1 = -1;
-                if (act) {
-                    i1 = __ffsll((long long)act) - 1;
-                    act &= act - 1;
+            for (int i0 = 0; i0 < total; i0 += 32) {
+                const int i = i0 + lane;
+                int col = 0;
+#pragma unroll
+                for (int step = 32; step; step >>= 1) {
+                    const int cand = col + step;
+                    const int va = __shfl_sync(0xFFFFFFFFu, exA, cand & 31);
+                    const int vb2 = __shfl_sync(0xFFFFFFFFu, exB, cand & 31);
+                    if ((cand < 32 ? va : vb2) <= i) col = cand;
                 }
-                const int ci = half ? i1 : i0;
-                if (ci < 0) continue;
-                const int c = ci < 32 ? ci + 1 : ci + 1;  // cell column in the 65-wide ring (1..64)
-                const int cx = x0 + c - 1;
+                const int qa = __shfl_sync(0xFFFFFFFFu, exA, col & 31);
+                const int qb = __shfl_sync(0xFFFFFFFFu, exB, col & 31);
+                if (i >= total) continue;
+                const int sl = i - (col < 32 ? qa : qb);
+                const int c = col + 1;  // cell column in the 65-wide ring
+                const int cx = x0 + col;
                 const int code = sC[cb][w][c];
                 const int nt = s_ntri[code];
                 const int f = bflags(cx, cy, cz);
-                const int64_t vb = sV[cb][w][c];
-                // triangle slot `sl`
                 if (sl < 3 * nt) {
+                    // triangle corner: vertex id of its edge, held by the owner cell
                     const int e = s_tri[code][sl];
                     const int a = s_eax[e];
                     int l0 = s_elow[e][0], l1 = s_elow[e][1], l2 = s_elow[e][2];
@@ -766,30 +607,29 @@ __global__ void __launch_bounds__(EW * 32, 3) k_mc_emit2(const double *__restric
                     if (a != 1 && l1 == 0 && cy >= 1) { d1 = -1; l1 = 1; }
                     if (a != 2 && l2 == 0 && cz >= 1) { d2 = -1; l2 = 1; }
                     const int e2 = s_eid[a][l0][l1][l2];
-                    const int ob = (cz + d2 + 3) % 3;
+                    const int ob = d2 ? (cb == 0 ? 2 : cb - 1) : cb;
                     const int ocode = sC[ob][w + d1][c + d0];
                     const int of = bflags(cx + d0, cy + d1, cz + d2);
                     const int64_t vid = sV[ob][w + d1][c + d0] + __ldg(&T->rank[ocode][of][e2]);
                     tris[3 * (g.tri_base + pbase.tri + sT[w][c]) + sl] = (int32_t)(g.vert_base + vid);
-                }
-                // owned edge `sl` (< 12): vertex
-                if (sl < 12) {
-                    const int e = sl;
-                    const int r = __ldg(&T->rank[code][f][e]);
-                    if (r >= 0) {
-                        const int a = s_eax[e];
-                        const int lx = s_elow[e][0], ly = s_elow[e][1], lz = s_elow[e][2];
-                        const double s0 = sv[(cz + lz) % 3][w + ly][c + lx];
-                        const double s1 = sv[(cz + lz + (a == 2)) % 3][w + ly + (a == 1)][c + lx + (a == 0)];
-                        const double den = __dadd_rn(s1, -s0);
-                        const double t = den == 0.0 ? 0.0 : __ddiv_rn(__dadd_rn(k, -s0), den);
-                        double lat[3] = {(double)(cx + lx), (double)(cy + ly), (double)(cz + lz)};
-                        lat[a] = __dadd_rn(lat[a], t);
-                        double *o = verts + 3 * (g.vert_base + vb + r);
-                        o[0] = world(g.origin[0], lat[0], g.spacing[0]);
-                        o[1] = world(g.origin[1], lat[1], g.spacing[1]);
-                        o[2] = world(g.origin[2], lat[2], g.spacing[2]);
-                    }
+                } else {
+                    // owned vertex of rank r: interpolate along its edge
+                    const int r = sl - 3 * nt;
+                    const int e = __ldg(&T->inv[code][f][r]);
+                    const int a = s_eax[e];
+                    const int lx = s_elow[e][0], ly = s_elow[e][1], lz = s_elow[e][2];
+                    const int zb = lz ? qb_of(cb) : cb;
+                    const double s0 = sv[zb][w + ly][c + lx];
+                    const double s1 = a == 2 ? sv[qb_of(zb)][w + ly][c + lx]
+                                             : sv[zb][w + ly + (a == 1)][c + lx + (a == 0)];
+                    const double den = __dadd_rn(s1, -s0);
+                    const double t = den == 0.0 ? 0.0 : __ddiv_rn(__dadd_rn(k, -s0), den);
+                    double lat[3] = {(double)(cx + lx), (double)(cy + ly), (double)(cz + lz)};
+                    lat[a] = __dadd_rn(lat[a], t);
+                    double *o = verts + 3 * (g.vert_base + sV[cb][w][c] + r);
+                    o[0] = world(g.origin[0], lat[0], g.spacing[0]);
+                    o[1] = world(g.origin[1], lat[1], g.spacing[1]);
+                    o[2] = world(g.origin[2], lat[2], g.spacing[2]);
                 }
             }
         }
