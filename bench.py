@@ -126,7 +126,7 @@ def run_step(vol, dims, bs, cands, r, ws, spacing=(1.0, 1.0, 1.0), stage_events=
     ext = sel["extent"].astype(np.int64)
     return dict(res=res, wins=wins, verts=verts, tris=tris, n_sel=int(np.prod(ext, axis=1).sum()),
                 cells=int(np.prod(ext - 1, axis=1).sum()), c_sel=int(sel["block_nbytes"].sum()),
-                archive=res.nbytes, nreg=len(regs), nsel=len(sel), ntri=int(tris.shape[0]),
+                archive=res.nbytes, nreg=len(regs), n_all=int(np.prod(regs["extent"].astype(np.int64), axis=1).sum()), nsel=len(sel), ntri=int(tris.shape[0]),
                 nvert=int(verts.shape[0]), payload=int(regs["block_nbytes"].sum()))
 
 
@@ -138,13 +138,15 @@ def kernel_bytes(name, info, N):
         "k_stats_rows": 4 * N,
         "k_tile<float, false>": 4 * N,
         "k_tile<float, true>": 4 * N + c_all,
+        "k_emit_q<float>": 4 * info["n_all"] + c_all,
         "k_crc_segments": None,
         "k_tok_fast": info["c_sel"],
         "k_seg_locate": info["c_sel"],
         "k_band": info["c_sel"] + 8 * info["n_sel"],
         "k_lorenzo": info["c_sel"] + 8 * info["n_sel"],
-        "k_mc_count2": 8 * info["n_sel"],
-        "k_mc_emit2": 8 * info["n_sel"] + 24 * info["nvert"] + 12 * info["ntri"],
+        "k_mc_mask": 8 * info["n_sel"] + info["n_sel"] // 8,
+        "k_mc_count3": info["n_sel"] // 8,
+        "k_mc_emit2": info["n_sel"] // 8 + 16 * info["nvert"] + 24 * info["nvert"] + 12 * info["ntri"],
     }
     return table.get(name)
 

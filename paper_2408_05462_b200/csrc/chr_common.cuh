@@ -63,6 +63,16 @@ CHR_HD uint64_t zigzag1(int64_t v) {  // zigzag(v) + 1
 // ---------------------------------------------------------------- CRC
 // multiplication of two reflected polynomials mod P (zlib multmodp)
 CHR_HD uint32_t gf2_mul(uint32_t a, uint32_t b) {
+#if defined(__CUDA_ARCH__)
+    // branch-free on the device (lanes of a warp never diverge on the bits)
+    uint32_t p = 0;
+#pragma unroll
+    for (int i = 31; i >= 0; --i) {
+        p ^= b & (0u - ((a >> i) & 1u));
+        b = (b >> 1) ^ (kCrcPoly & (0u - (b & 1u)));
+    }
+    return p;
+#else
     uint32_t m = 1u << 31, p = 0;
     for (;;) {
         if (a & m) {
@@ -73,6 +83,7 @@ CHR_HD uint32_t gf2_mul(uint32_t a, uint32_t b) {
         b = (b & 1) ? (b >> 1) ^ kCrcPoly : b >> 1;
     }
     return p;
+#endif
 }
 
 // x^(2^k) mod P for k = 0..63 (zlib x2n_table); filled by crc_tables_init

@@ -6,7 +6,7 @@
 namespace chr {
 
 // ------------------------------------------------------------------ CRC
-constexpr int64_t kCrcScWords = 4096;  // words per superchunk (16 KiB)
+constexpr int64_t kCrcScWords = 1024;  // words per superchunk (4 KiB): short serial chains, many warps
 
 struct CrcSeg {
     uint64_t begin, end;  // byte range
@@ -63,6 +63,19 @@ struct WsCarver {
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 #if defined(__CUDACC__)
+// x^(8n) mod P with the 61 factors spread over the lanes of a warp (all
+// lanes call; every lane gets the product)
+__device__ __forceinline__ uint32_t warp_x8n(const uint32_t *x2n, uint64_t n) {
+    const int lane = threadIdx.x & 31;
+    uint32_t p = 1u << 31;
+    if ((n >> lane) & 1) p = x2n[lane + 3];
+    if (lane + 32 < 61 && ((n >> (lane + 32)) & 1)) p = gf2_mul(p, x2n[lane + 35]);
+#pragma unroll
+    for (int off = 16; off; off >>= 1) p = gf2_mul(p, __shfl_xor_sync(0xFFFFFFFFu, p, off));
+    return p;
+}
+
+
 // copy a struct from global to shared memory with all threads (parallel
 // 4-byte loads instead of one thread's serialised copy); caller syncs
 template <typename S>

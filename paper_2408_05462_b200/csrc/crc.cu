@@ -66,30 +66,28 @@ const CrcTables *crc_tables_device() {
 
 // x^(8n) mod P computed by a whole warp (one bit of n per lane, then a
 // shuffle product tree); every lane returns the result
-__device__ uint32_t warp_x8n(const uint32_t *x2n, uint64_t n) {
-    const int lane = threadIdx.x & 31;
-    uint32_t p = 1u << 31;
-    if ((n >> lane) & 1) p = x2n[lane + 3];
-    if (lane + 32 < 61 && ((n >> (lane + 32)) & 1)) p = gf2_mul(p, x2n[lane + 35]);
-#pragma unroll
-    for (int off = 16; off; off >>= 1) p = gf2_mul(p, __shfl_xor_sync(0xFFFFFFFFu, p, off));
-    return p;
+// G tables replicated 8x (word idx * 8 + (lane & 7)): random byte indices of
+// 32 lanes then spread over all 32 banks (~2-way instead of ~4-way conflicts)
+__device__ __forceinline__ uint32_t apply_g(const uint32_t *g, uint32_t v, int r) {
+    return g[((v & 0xFF) << 3) + r] ^ g[2048 + (((v >> 8) & 0xFF) << 3) + r] ^
+           g[4096 + (((v >> 16) & 0xFF) << 3) + r] ^ g[6144 + ((v >> 24) << 3) + r];
 }
 
-__device__ __forceinline__ uint32_t apply_g(const uint32_t (*g)[256], uint32_t v) {
-    return g[0][v & 0xFF] ^ g[1][(v >> 8) & 0xFF] ^ g[2][(v >> 16) & 0xFF] ^ g[3][v >> 24];
-}
-
+constexpr int kCrcSmemSegs = 1024;
 // one warp per superchunk (kCrcScWords words); seg_raw[s] ^= contribution
 __global__ void __launch_bounds__(256) k_crc_segments(const uint8_t *__restrict__ buf,
                                                       const CrcSeg *__restrict__ segs, int64_t nseg,
                                                       const CrcTables *__restrict__ tabs,
                                                       uint32_t *__restrict__ seg_raw) {
-    __shared__ uint32_t g[4][256];
+    __shared__ uint32_t g[4 * 256 * 8];
     __shared__ uint32_t t0[256];
     __shared__ uint32_t x2n[64];
     __shared__ uint32_t xw[33];
-    for (int i = threadIdx.x; i < 1024; i += blockDim.x) g[i >> 8][i & 255] = tabs->g[i >> 8][i & 255];
+    __shared__ int64_t s_scb[kCrcSmemSegs];  // segment first superchunks (when few segments)
+    const bool seg_smem = nseg <= kCrcSmemSegs;
+    if (seg_smem)
+        for (int64_t i = threadIdx.x; i < nseg; i += blockDim.x) s_scb[i] = segs[i].sc_base;
+    for (int i = threadIdx.x; i < 8192; i += blockDim.x) g[i] = tabs->g[i >> 11][(i >> 3) & 255];
     for (int i = threadIdx.x; i < 256; i += blockDim.x) t0[i] = tabs->t[0][i];
     if (threadIdx.x < 64) x2n[threadIdx.x] = tabs->x2n[threadIdx.x];
     if (threadIdx.x < 33) xw[threadIdx.x] = tabs->xw[threadIdx.x];
@@ -104,7 +102,7 @@ __global__ void __launch_bounds__(256) k_crc_segments(const uint8_t *__restrict_
         int64_t lo = 0, hi = nseg - 1;
         while (lo < hi) {
             const int64_t mid = (lo + hi + 1) >> 1;
-            if (segs[mid].sc_base <= sc) lo = mid; else hi = mid - 1;
+            if ((seg_smem ? s_scb[mid] : segs[mid].sc_base) <= sc) lo = mid; else hi = mid - 1;
         }
         const CrcSeg S = segs[lo];
         const uint64_t a = S.begin, b = S.end;
@@ -121,7 +119,7 @@ __global__ void __launch_bounds__(256) k_crc_segments(const uint8_t *__restrict_
             uint32_t B = 0;
             int64_t last = -1;
             for (uint64_t i = w0 + lane; i < w1; i += 32) {
-                B = apply_g(g, B) ^ __ldg(wp + i);
+                B = apply_g(g, B, lane & 7) ^ __ldg(wp + i);
                 last = (int64_t)(i - w0);
             }
             const int64_t Ws = (int64_t)(w1 - w0);
@@ -161,7 +159,7 @@ int crc_launch(const uint8_t *d_buf, const CrcSeg *d_segs, int64_t nseg, int64_t
     if (!tabs) return CHR_E_CUDA;
     if (nseg <= 0) return CHR_OK;
     // total_sc <= 0: unknown on the host (lives on the device) -> persistent grid
-    const int64_t warps_needed = total_sc > 0 ? total_sc : 148 * 64;
+    const int64_t warps_needed = total_sc > 0 ? total_sc : 148 * 128;
     int64_t blocks = (warps_needed + 7) / 8;
     if (blocks > 148 * 16) blocks = 148 * 16;
     if (blocks < 1) blocks = 1;

@@ -281,19 +281,31 @@ __global__ void __launch_bounds__(DTHREADS) k_tok_count(DecReg *__restrict__ reg
 // per region: exclusive prefix of chunk samples, total must equal n
 __global__ void k_tok_scan(DecReg *__restrict__ regs, int64_t nreg, int64_t *__restrict__ chunk_samples,
                            int slow_pass) {
-    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    // warp per region: 32 chunk counts per step
+    const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
     if (r >= nreg) return;
     DecReg &R = regs[r];
     if (!((R.codec == 1 || R.codec == 2) && R.err == 0)) return;
     if ((R.slow != 0) != (slow_pass != 0)) return;  // pass 0: band regions, pass 1: generic
     int64_t acc = 0;
     bool over = false;
-    for (int64_t c = R.chunk_base; c < R.chunk_base + R.nchunks; ++c) {
-        const int64_t v = chunk_samples[c];
-        chunk_samples[c] = acc;
-        acc += v;
-        if (acc > R.n || v < 0) over = true;
+    for (int64_t c0 = 0; c0 < R.nchunks; c0 += 32) {
+        const int64_t c = R.chunk_base + c0 + lane;
+        const bool ok = c0 + lane < R.nchunks;
+        const int64_t v = ok ? chunk_samples[c] : 0;
+        int64_t inc = v;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int64_t o = __shfl_up_sync(0xFFFFFFFFu, inc, off);
+            if (lane >= off) inc += o;
+        }
+        if (ok) chunk_samples[c] = acc + inc - v;
+        if (ok && (acc + inc > R.n || v < 0)) over = true;
+        acc += __shfl_sync(0xFFFFFFFFu, inc, 31);
     }
+    over = __any_sync(0xFFFFFFFFu, over);
+    if (lane != 0) return;
     if (over) R.err |= EF_RANGE;
     else if (acc < R.n) R.err |= EF_TRUNC;
     if (R.tok_start == R.poff + R.plen && R.n > 0) R.err |= EF_TRUNC;
@@ -753,7 +765,8 @@ __global__ void k_tile_order(const DecReg *__restrict__ regs, const int64_t *__r
 __global__ void __launch_bounds__(DTHREADS) k_tok_fast(DecReg *__restrict__ regs, const int32_t *__restrict__ chunk_reg,
                                                        const uint8_t *__restrict__ blob,
                                                        int64_t *__restrict__ chunk_samples,
-                                                       int64_t *__restrict__ thr_cnt) {
+                                                       int64_t *__restrict__ thr_cnt,
+                                                       int32_t *__restrict__ any_slow) {
     const int64_t c = blockIdx.x;
     DecReg &R = regs[chunk_reg[c]];
     if (!((R.codec == 1 || R.codec == 2) && R.err == 0)) {
@@ -783,7 +796,10 @@ __global__ void __launch_bounds__(DTHREADS) k_tok_fast(DecReg *__restrict__ regs
     thr_cnt[c * DTHREADS + threadIdx.x] = cnt;
     const int64_t tot = block_sum64(cnt);
     if (err) atomicOr(&R.err, err);
-    if (nc) atomicOr(&R.slow, 1u);
+    if (nc) {
+        atomicOr(&R.slow, 1u);
+        atomicOr(any_slow, 1);
+    }
     if (threadIdx.x == 0) chunk_samples[c] = tot;
 }
 
@@ -1286,6 +1302,8 @@ struct DecPlan {
     std::vector<int64_t> h_pair_base;
     int64_t ndiag = 0;
     unsigned long long *ticket, *ticket3;
+    int32_t *any_slow;
+    bool host_slow = false;  // some region needs the generic path whatever the stream
 };
 
 static int dec_rows_for(int ex) {
@@ -1369,6 +1387,7 @@ static bool dec_build(const chr_dec_region_t *h, int64_t n, uintptr_t blob, DecP
             pl.max_rows_ex = std::max(pl.max_rows_ex, R.rows * R.ex);
             if (!band_shape(R)) {
                 R.slow = 1;  // rows wider than a band tile: generic path
+                pl.host_slow = true;
             } else {
                 R.ntiles = (int64_t)R.tny * R.tnz;
                 tile += R.ntiles;
@@ -1440,6 +1459,7 @@ static void dec_carve(DecPlan &pl, void *base, size_t cap) {
     pl.pair_base = c.take<int64_t>(pl.h_pair_base.size() + 1);
     pl.ticket = c.take<unsigned long long>(1);
     pl.ticket3 = c.take<unsigned long long>(1);
+    pl.any_slow = c.take<int32_t>(1);
     pl.ws = c.off + 256;
 }
 
@@ -1478,6 +1498,7 @@ extern "C" int chr_decode_regions(const uint8_t *d_blob, const chr_dec_region_t 
     CHR_CUDA_TRY(cudaMemsetAsync(pl.flags, 0, sizeof(int64_t) * (pl.nitems + 1), st));
     CHR_CUDA_TRY(cudaMemsetAsync(pl.ticket, 0, sizeof(unsigned long long), st));
     CHR_CUDA_TRY(cudaMemsetAsync(pl.ticket3, 0, sizeof(unsigned long long), st));
+    CHR_CUDA_TRY(cudaMemsetAsync(pl.any_slow, 0, sizeof(int32_t), st));
     CHR_CUDA_TRY(cudaMemsetAsync(pl.tflag, 0, sizeof(int32_t) * (pl.ntiles + 1), st));
     int rc = crc_launch(d_blob, pl.segs, n, total_sc, pl.seg_raw, st);
     if (rc) return rc;
@@ -1496,11 +1517,11 @@ extern "C" int chr_decode_regions(const uint8_t *d_blob, const chr_dec_region_t 
     {
         CHR_PROF("k_tok_fast", st);
         k_tok_fast<<<(unsigned)pl.nchunks, DTHREADS, 0, st>>>(pl.d_regs, pl.chunk_reg, d_blob, pl.chunk_samples,
-                                                              pl.thr_cnt);
+                                                              pl.thr_cnt, pl.any_slow);
     }
     {
         CHR_PROF("k_tok_scan", st);
-        k_tok_scan<<<(unsigned)ceil_div(n, 128), 128, 0, st>>>(pl.d_regs, n, pl.chunk_samples, 0);
+        k_tok_scan<<<(unsigned)ceil_div(n, 4), 128, 0, st>>>(pl.d_regs, n, pl.chunk_samples, 0);
     }
     // ---- band path (canonical streams)
     if (pl.ntiles > 0) {
@@ -1530,32 +1551,40 @@ extern "C" int chr_decode_regions(const uint8_t *d_blob, const chr_dec_region_t 
                                                            d_out);
         }
     }
-    // ---- generic path (non-canonical streams, rows wider than a band tile)
-    {
-        CHR_PROF("k_tok_count", st);
-        k_tok_count<<<(unsigned)pl.nchunks, DTHREADS, 0, st>>>(pl.d_regs, n, d_blob, pl.chunk_samples);
+    // ---- generic path (non-canonical streams, rows wider than a band tile):
+    //      skipped unless some region needs it (one 4-byte read-back)
+    int32_t h_any_slow = pl.host_slow ? 1 : 0;
+    if (!h_any_slow) {
+        CHR_CUDA_TRY(cudaMemcpyAsync(&h_any_slow, pl.any_slow, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+        CHR_CUDA_TRY(cudaStreamSynchronize(st));
     }
-    {
-        CHR_PROF("k_tok_scan", st);
-        k_tok_scan<<<(unsigned)ceil_div(n, 128), 128, 0, st>>>(pl.d_regs, n, pl.chunk_samples, 1);
-    }
-    {
-        CHR_PROF("k_locate", st);
-        k_locate<<<(unsigned)pl.nchunks, DTHREADS, 0, st>>>(pl.d_regs, n, d_blob, pl.chunk_samples,
-                                                            pl.seg_byte, pl.seg_skip);
-    }
-    {
-        CHR_PROF("k_esc_base", st);
-        k_esc_base<<<(unsigned)n, 256, 0, st>>>(pl.d_regs, n, d_blob, pl.esc_base);
-    }
-    if (pl.nitems > 0) {
-        const size_t smem = (size_t)pl.max_rows_ex * 16 + DWIN;
-        CHR_CUDA_TRY(cudaFuncSetAttribute(k_lorenzo, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (h_any_slow) {
         {
-            CHR_PROF("k_lorenzo", st);
-            k_lorenzo<<<(unsigned)pl.nitems, DTHREADS, smem, st>>>(pl.d_regs, n, d_blob, pl.seg_byte,
-                                                                   pl.seg_skip, pl.esc_base, pl.carry,
-                                                                   pl.flags, pl.ticket, d_out);
+            CHR_PROF("k_tok_count", st);
+            k_tok_count<<<(unsigned)pl.nchunks, DTHREADS, 0, st>>>(pl.d_regs, n, d_blob, pl.chunk_samples);
+        }
+        {
+            CHR_PROF("k_tok_scan", st);
+            k_tok_scan<<<(unsigned)ceil_div(n, 4), 128, 0, st>>>(pl.d_regs, n, pl.chunk_samples, 1);
+        }
+        {
+            CHR_PROF("k_locate", st);
+            k_locate<<<(unsigned)pl.nchunks, DTHREADS, 0, st>>>(pl.d_regs, n, d_blob, pl.chunk_samples,
+                                                                pl.seg_byte, pl.seg_skip);
+        }
+        {
+            CHR_PROF("k_esc_base", st);
+            k_esc_base<<<(unsigned)n, 256, 0, st>>>(pl.d_regs, n, d_blob, pl.esc_base);
+        }
+        if (pl.nitems > 0) {
+            const size_t smem = (size_t)pl.max_rows_ex * 16 + DWIN;
+            CHR_CUDA_TRY(cudaFuncSetAttribute(k_lorenzo, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            {
+                CHR_PROF("k_lorenzo", st);
+                k_lorenzo<<<(unsigned)pl.nitems, DTHREADS, smem, st>>>(pl.d_regs, n, d_blob, pl.seg_byte,
+                                                                       pl.seg_skip, pl.esc_base, pl.carry,
+                                                                       pl.flags, pl.ticket, d_out);
+            }
         }
     }
     for (int64_t r0 = 0; r0 < n; r0 += 65535) {

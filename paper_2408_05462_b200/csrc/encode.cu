@@ -43,6 +43,7 @@ struct RegDev {
     double e;
     int64_t n;
     int64_t piece_base, npieces, item_base, chunk_base, nchunks;
+    int64_t q_base;               // first token value of the region in the q buffer
     // results
     int32_t codec, f32ok;
     int64_t tok_len, nesc, payload_len;
@@ -122,8 +123,8 @@ __device__ __forceinline__ bool not_f32_exact(T v) {
 // ------------------------------------------------------------------ tiles
 // 32-bit token-size helpers (valid quanta: |q| <= 2^30, zigzag+1 <= 2^31+1)
 __device__ __forceinline__ uint32_t zz1_32(int32_t q) { return (((uint32_t)q << 1) ^ (uint32_t)(q >> 31)) + 1u; }
-__device__ __forceinline__ int vlen32(uint32_t u) {
-    return 1 + (u >= (1u << 7)) + (u >= (1u << 14)) + (u >= (1u << 21)) + (u >= (1u << 28));
+__device__ __forceinline__ int vlen32(uint32_t u) {  // ceil(bits / 7) for u >= 1: ((38 - clz) * 37) >> 8
+    return ((38 - __clz(u)) * 37) >> 8;
 }
 // token bytes of a zero run shorter than 128 (every run inside one 64-sample piece)
 __device__ __forceinline__ int rb_small(int L) { return L <= 0 ? 0 : (L == 1 ? 1 : 2); }
@@ -152,6 +153,7 @@ __global__ void __launch_bounds__(NW * 32, 4) k_tile(const T *__restrict__ vol, 
                                                   const int32_t *__restrict__ item_reg,
                                                   PieceRec *__restrict__ recs,
                                                   const PieceOff *__restrict__ poffs,
+                                                  uint32_t *__restrict__ qz,
                                                   uint8_t *__restrict__ out) {
     __shared__ int32_t sD[2][NW][TX + 2];
     __shared__ RegDev R;
@@ -180,7 +182,9 @@ __global__ void __launch_bounds__(NW * 32, 4) k_tile(const T *__restrict__ vol, 
     const bool chk32 = sizeof(T) == 8 && P->src_dtype == CHR_F32;
     const uint32_t lt = (1u << lane) - 1u;
     const T *row = vol + ((int64_t)(R.oz + z0) * NY + (R.oy + y)) * NX + R.ox;  // plane z0
+    const int64_t rec0 = R.piece_base + (int64_t)y * R.ntx + xt, rec_z = (int64_t)R.ey * R.ntx;
 
+    // returns (warp-uniform) whether the exact sequence ran; escapes only come from it
     auto quant3 = [&](T a, T b, T h, int32_t &ua, int32_t &ub, int32_t &uh, bool &ea, bool &eb, bool &eh) {
         ua = ub = uh = 0;
         ea = eb = eh = false;
@@ -192,7 +196,9 @@ __global__ void __launch_bounds__(NW * 32, 4) k_tile(const T *__restrict__ vol, 
             if (!fa) ua = quantize(Q, (double)a, ea);
             if (!fb) ub = quantize(Q, (double)b, eb);
             if (!fh) uh = quantize(Q, (double)h, eh);
+            return true;
         }
+        return false;
     };
     int32_t pA = 0, pB = 0, pH = 0;  // u at the previous plane
     if (quant && z0 > 0) {
@@ -215,9 +221,9 @@ __global__ void __launch_bounds__(NW * 32, 4) k_tile(const T *__restrict__ vol, 
             if (okB) nB = __ldg(nrow + xB);
             if (okH) nH = __ldg(nrow + xH);
         }
-        bool eA = false, eB = false, eH = false;
+        bool eA = false, eB = false, eH = false, slow = false;
         int32_t uA = 0, uB = 0, uH = 0;
-        if (quant) quant3(vA, vB, vH, uA, uB, uH, eA, eB, eH);
+        if (quant) slow = quant3(vA, vB, vH, uA, uB, uH, eA, eB, eH);
         int32_t(*D)[TX + 2] = sD[z & 1];
         D[w][lane + 1] = uA - pA;
         D[w][lane + 33] = uB - pB;
@@ -231,13 +237,18 @@ __global__ void __launch_bounds__(NW * 32, 4) k_tile(const T *__restrict__ vol, 
         const int32_t qB = D[w][lane + 33] - D[w][lane + 32] - D[w - 1][lane + 33] + D[w - 1][lane + 32];
         const bool nzA = okA && qA != 0, nzB = okB && qB != 0;
         const uint32_t mA = __ballot_sync(0xFFFFFFFFu, nzA), mB = __ballot_sync(0xFFFFFFFFu, nzB);
-        const int64_t rec = R.piece_base + ((int64_t)z * R.ey + y) * R.ntx + xt;
+        const int64_t rec = rec0 + (int64_t)z * rec_z;
         // previous nonzero (position in the piece) before element A (= lane) and B (= 32 + lane)
         const uint32_t bA = mA & lt, bB = mB & lt;
         const int prevA = bA ? 31 - __clz(bA) : -1;
         const int prevB = bB ? 63 - __clz(bB) : (mA ? 31 - __clz(mA) : -1);
         const uint32_t zA = zz1_32(qA), zB = zz1_32(qB);
-        const bool anyesc = __any_sync(0xFFFFFFFFu, (okA && eA) || (okB && eB));
+        if (!EMIT) {  // token values (zigzag + 1) for k_emit_q, raster order of the window
+            uint32_t *qrow = qz + R.q_base + ((int64_t)z * R.ey + y) * R.ex + x0;
+            if (okA) qrow[lane] = zA;
+            if (okB) qrow[32 + lane] = zB;
+        }
+        const bool anyesc = slow && __any_sync(0xFFFFFFFFu, (okA && eA) || (okB && eB));
         if (!EMIT) {
             int b = 0;
             if (nzA) b += (prevA >= 0 ? rb_small(lane - prevA - 1) : 0) + vlen32(zA);
@@ -322,12 +333,132 @@ __global__ void __launch_bounds__(NW * 32, 4) k_tile(const T *__restrict__ vol, 
 }
 
 // item -> region map (replaces a per-CTA binary search over the regions)
-__global__ void k_tile_fill_map(const RegDev *__restrict__ regs, int64_t nreg, int32_t *__restrict__ item_reg) {
+__global__ void k_tile_fill_map(const RegDev *__restrict__ regs, int64_t nreg, int32_t *__restrict__ item_reg,
+                                int32_t *__restrict__ chunk_reg) {
     const int64_t r = blockIdx.x;
     if (r >= nreg) return;
     const RegDev &R = regs[r];
     const int64_t nit = (int64_t)R.ntx * R.nty * R.nzc;
     for (int64_t i = threadIdx.x; i < nit; i += blockDim.x) item_reg[R.item_base + i] = (int32_t)r;
+    for (int64_t i = threadIdx.x; i < R.nchunks; i += blockDim.x) chunk_reg[R.chunk_base + i] = (int32_t)r;
+}
+
+// ------------------------------------------------------------------ emit
+// Token bytes from the stored token values: one warp per 64-sample row
+// piece, a CTA per scan chunk (1024 pieces of one region), no barriers.
+// Escaped samples (codec 2, rare) re-run the exact quantiser for their
+// flag; verbatim regions copy samples.
+template <typename T>
+__global__ void __launch_bounds__(256) k_emit_q(const T *__restrict__ vol, const EncParams *__restrict__ P,
+                                                const RegDev *__restrict__ regs,
+                                                const int32_t *__restrict__ chunk_reg,
+                                                const PieceRec *__restrict__ recs,
+                                                const PieceOff *__restrict__ poffs,
+                                                const uint32_t *__restrict__ qz, uint8_t *__restrict__ out) {
+    __shared__ RegDev R;
+    const int64_t c = blockIdx.x;
+    coop_copy(&R, regs + __ldg(chunk_reg + c));
+    __syncthreads();
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t lt = (1u << lane) - 1u;
+    constexpr int PW = (int)(CH / 8);  // pieces per warp
+    int64_t lp = (c - R.chunk_base) * CH + (int64_t)w * PW;
+    const int64_t lpe = min(lp + PW, R.npieces);
+    if (lp >= lpe) return;
+    const int codec = R.codec;
+    const int64_t NX = P->NX, NY = P->NY;
+    int xt = (int)(lp % R.ntx);
+    const int64_t zy = lp / R.ntx;
+    int y = (int)(zy % R.ey), z = (int)(zy / R.ey);
+    const bool tok = codec == 1 || codec == 2;
+    // software pipeline: the next piece's token values and offsets load
+    // while this piece is written
+    auto fetch = [&](int xt_, int y_, int z_, int64_t lp_, uint32_t &a, uint32_t &b, PieceOff &o) {
+        const int x0_ = xt_ * TX, vc = min(TX, R.ex - x0_);
+        const int64_t s = ((int64_t)z_ * R.ey + y_) * R.ex + x0_;
+        a = lane < vc ? __ldg(qz + R.q_base + s + lane) : 1u;
+        b = 32 + lane < vc ? __ldg(qz + R.q_base + s + 32 + lane) : 1u;
+        o = poffs[R.piece_base + lp_];
+    };
+    uint32_t nA = 1u, nB = 1u;
+    PieceOff npo{};
+    if (tok) fetch(xt, y, z, lp, nA, nB, npo);
+    for (; lp < lpe; ++lp) {
+        const int x0 = xt * TX;
+        const int vcount = min(TX, R.ex - x0);
+        const bool okA = lane < vcount, okB = 32 + lane < vcount;
+        const int64_t s0 = ((int64_t)z * R.ey + y) * R.ex + x0;  // window sample index
+        const int64_t rec = R.piece_base + lp;
+        const T *vrow = vol + ((int64_t)(R.oz + z) * NY + (R.oy + y)) * NX + R.ox + x0;
+        const int cz = z, cy = y;
+        if (++xt == R.ntx) {
+            xt = 0;
+            if (++y == R.ey) {
+                y = 0;
+                ++z;
+            }
+        }
+        if (tok) {
+            const uint32_t zA = nA, zB = nB;
+            const PieceOff po = npo;
+            if (lp + 1 < lpe) fetch(xt, y, z, lp + 1, nA, nB, npo);
+            const bool nzA = zA != 1u, nzB = zB != 1u;
+            const uint32_t mA = __ballot_sync(0xFFFFFFFFu, nzA), mB = __ballot_sync(0xFFFFFFFFu, nzB);
+            const uint32_t bA = mA & lt, bB = mB & lt;
+            const int prevA = bA ? 31 - __clz(bA) : -1;
+            const int prevB = bB ? 63 - __clz(bB) : (mA ? 31 - __clz(mA) : -1);
+            int64_t runA = 0, runB = 0;
+            int bAy = 0, bBy = 0;
+            if (nzA) {
+                runA = prevA >= 0 ? lane - prevA - 1 : po.carry + lane;
+                bAy = (prevA >= 0 ? rb_small((int)runA) : (int)run_bytes(runA)) + vlen32(zA);
+            }
+            if (nzB) {
+                runB = prevB >= 0 ? 32 + lane - prevB - 1 : po.carry + 32 + lane;
+                bBy = (prevB >= 0 ? rb_small((int)runB) : (int)run_bytes(runB)) + vlen32(zB);
+            }
+            // one scan of packed (bytes A | bytes B << 16)
+            uint32_t pk = (uint32_t)bAy | ((uint32_t)bBy << 16);
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, pk, off);
+                if (lane >= off) pk += t;
+            }
+            const uint32_t tot = __shfl_sync(0xFFFFFFFFu, pk, 31);
+            const int totA = (int)(tot & 0xFFFFu), totB = (int)(tot >> 16);
+            const int sA = (int)(pk & 0xFFFFu) - bAy, sB = totA + (int)(pk >> 16) - bBy;
+            uint8_t *base = out + R.tok_start + po.tok_off;
+            if (nzA) put_varint32(put_run(base + sA, runA), zA);
+            if (nzB) put_varint32(put_run(base + sB, runB), zB);
+            if (lp == R.npieces - 1 && lane == 0) {  // the region's final zero run
+                const int lastp = mB ? 63 - __clz(mB) : (mA ? 31 - __clz(mA) : -1);
+                const int64_t fin = (mA | mB) ? vcount - 1 - lastp : po.carry + vcount;
+                put_run(base + totA + totB, fin);
+            }
+            if (codec == 2 && recs[rec].nesc) {
+                const Quant Q = make_quant(R.e);
+                bool eA = false, eB = false;
+                if (okA) quantize(Q, (double)__ldg(vrow + lane), eA);
+                if (okB) quantize(Q, (double)__ldg(vrow + 32 + lane), eB);
+                const uint32_t eAm = __ballot_sync(0xFFFFFFFFu, eA), eBm = __ballot_sync(0xFFFFFFFFu, eB);
+                const uint64_t vbase = R.payload_off + (uint64_t)((R.n + 7) >> 3);
+                if (eA) put_le(out + vbase + 8 * (po.esc_off + __popc(eAm & lt)), (double)__ldg(vrow + lane));
+                if (eB)
+                    put_le(out + vbase + 8 * (po.esc_off + __popc(eAm) + __popc(eBm & lt)),
+                           (double)__ldg(vrow + 32 + lane));
+            }
+        } else if (codec == 3) {  // verbatim f32, raster order
+            uint8_t *b = out + R.payload_off + 4 * s0;
+            if (okA) put_le(b + 4 * lane, (float)__ldg(vrow + lane));
+            if (okB) put_le(b + 4 * (32 + lane), (float)__ldg(vrow + 32 + lane));
+        } else {  // verbatim f64
+            uint8_t *b = out + R.payload_off + 8 * s0;
+            if (okA) put_le(b + 8 * lane, (double)__ldg(vrow + lane));
+            if (okB) put_le(b + 8 * (32 + lane), (double)__ldg(vrow + 32 + lane));
+        }
+        (void)cz;
+        (void)cy;
+    }
 }
 
 // ------------------------------------------------------------------ scans
@@ -398,15 +529,36 @@ __global__ void __launch_bounds__(256) k_scan_reduce(const EncParams *__restrict
 __global__ void k_scan_regions(const EncParams *__restrict__ P, RegDev *__restrict__ regs,
                                TokSeg *__restrict__ chunk_agg, int32_t *__restrict__ codec2_list,
                                EncScalars *__restrict__ sc) {
-    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    // warp per region: 32 chunk aggregates per step, warp scan, carry
+    const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
     if (r >= P->nreg) return;
     RegDev &R = regs[r];
     TokSeg acc = tokseg_identity();
-    for (int64_t c = R.chunk_base; c < R.chunk_base + R.nchunks; ++c) {
-        const TokSeg a = chunk_agg[c];
-        chunk_agg[c] = acc;
-        acc = tokseg_combine(acc, a);
+    for (int64_t c0 = 0; c0 < R.nchunks; c0 += 32) {
+        const int64_t c = R.chunk_base + c0 + lane;
+        const bool ok = c0 + lane < R.nchunks;
+        const TokSeg a = ok ? chunk_agg[c] : tokseg_identity();
+        TokSeg inc = a;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const TokSeg o = WarpSeg::shfl_up(inc, off);
+            if (lane >= off) inc = tokseg_combine(o, inc);
+        }
+        TokSeg ex = WarpSeg::shfl_up(inc, 1);
+        if (lane == 0) ex = tokseg_identity();
+        if (ok) chunk_agg[c] = tokseg_combine(acc, ex);
+        TokSeg tot;
+        tot.len = __shfl_sync(0xFFFFFFFFu, inc.len, 31);
+        tot.lead = __shfl_sync(0xFFFFFFFFu, inc.lead, 31);
+        tot.trail = __shfl_sync(0xFFFFFFFFu, inc.trail, 31);
+        tot.bytes = __shfl_sync(0xFFFFFFFFu, inc.bytes, 31);
+        tot.nesc = __shfl_sync(0xFFFFFFFFu, inc.nesc, 31);
+        tot.nz = __shfl_sync(0xFFFFFFFFu, inc.nz, 31);
+        tot.f32ok = __shfl_sync(0xFFFFFFFFu, inc.f32ok, 31);
+        acc = tokseg_combine(acc, tot);
     }
+    if (lane != 0) return;
     const bool f32ok = P->dtype == CHR_F32 ? true : acc.f32ok != 0;
     const bool vf32 = P->src_dtype == CHR_F32 && f32ok;
     const int64_t vlen = R.n * (vf32 ? 4 : 8);
@@ -656,24 +808,31 @@ __global__ void __launch_bounds__(256) k_write_table(const EncParams *__restrict
 }
 
 // 34-byte block headers + per-region CRC + file-CRC contributions
+// warp per region: payload CRC, block header, and the region's share of
+// the file CRC; the x^(8n) shifts are warp-parallel
 __global__ void __launch_bounds__(128) k_finalize_regions(const EncParams *__restrict__ P,
                                                           RegDev *__restrict__ regs,
                                                           const uint32_t *__restrict__ seg_raw,
                                                           const CrcTables *__restrict__ tabs,
                                                           EncScalars *__restrict__ sc,
                                                           uint8_t *__restrict__ out) {
-    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    __shared__ uint32_t t0[256], x2n[64];
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) t0[i] = tabs->t[0][i];
+    if (threadIdx.x < 64) x2n[threadIdx.x] = tabs->x2n[threadIdx.x];
+    __syncthreads();
+    const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
     const int seg0 = P->write_file ? 1 : 0;
     const uint64_t body = sc->file_body;
     if (r == 0 && P->write_file) {
-        const uint32_t c = crc_shift(tabs->x2n, seg_raw[0], body - P->header_table);
-        if (c) atomicXor(&sc->file_raw, c);
+        const uint32_t c = gf2_mul(warp_x8n(x2n, body - P->header_table), seg_raw[0]);
+        if (lane == 0 && c) atomicXor(&sc->file_raw, c);
     }
     if (r >= P->nreg) return;
     RegDev &R = regs[r];
     const uint32_t praw = seg_raw[seg0 + r];
-    const uint32_t crc = crc_finalize(tabs->x2n, praw, (uint64_t)R.payload_len);
-    R.crc = crc;
+    // zlib crc = raw ^ (0xFFFFFFFF * x^(8 len)) ^ 0xFFFFFFFF
+    const uint32_t crc = gf2_mul(warp_x8n(x2n, (uint64_t)R.payload_len), 0xFFFFFFFFu) ^ praw ^ 0xFFFFFFFFu;
     uint8_t h[kBlockHeader];
     h[0] = (uint8_t)R.codec;
     put_le(h + 1, (uint32_t)R.ex);
@@ -683,13 +842,15 @@ __global__ void __launch_bounds__(128) k_finalize_regions(const EncParams *__res
     h[21] = (uint8_t)P->src_dtype;
     put_le(h + 22, (uint64_t)R.payload_len);
     put_le(h + 30, crc);
+    if (lane == 0) R.crc = crc;
     uint8_t *dst = out + R.block_off;
-    for (int i = 0; i < kBlockHeader; ++i) dst[i] = h[i];
+    if (lane < kBlockHeader) dst[lane] = h[lane];
+    if (lane + 32 < kBlockHeader) dst[lane + 32] = h[lane + 32];
     if (P->write_file) {
-        const uint32_t hraw = crc_raw_bytes(tabs->t[0], 0, h, kBlockHeader);
-        uint32_t c = crc_shift(tabs->x2n, hraw, body - (R.block_off + kBlockHeader));
-        c ^= crc_shift(tabs->x2n, praw, body - (R.payload_off + R.payload_len));
-        if (c) atomicXor(&sc->file_raw, c);
+        const uint32_t hraw = crc_raw_bytes(t0, 0, h, kBlockHeader);
+        uint32_t c = gf2_mul(warp_x8n(x2n, body - (R.block_off + kBlockHeader)), hraw);
+        c ^= gf2_mul(warp_x8n(x2n, body - (R.payload_off + R.payload_len)), praw);
+        if (lane == 0 && c) atomicXor(&sc->file_raw, c);
     }
 }
 
@@ -702,7 +863,7 @@ __global__ void k_finalize_file(const CrcTables *__restrict__ tabs, const EncSca
 // ------------------------------------------------------------------ host
 struct EncPlan {
     std::vector<RegDev> regs;
-    int64_t nitems = 0, npieces_total = 0, nchunks = 0;
+    int64_t nitems = 0, npieces_total = 0, nchunks = 0, qtotal = 0;
     size_t ws_bytes = 0;
     // carved pointers
     EncParams *params;
@@ -714,7 +875,8 @@ struct EncPlan {
     uint32_t *seg_raw;
     int32_t *codec2;
     EncScalars *scal;
-    int32_t *item_reg;
+    int32_t *item_reg, *chunk_reg;
+    uint32_t *qz;
 };
 
 static bool build_plan(const chr_region_t *h, int64_t nreg, EncPlan &pl) {
@@ -745,6 +907,8 @@ static bool build_plan(const chr_region_t *h, int64_t nreg, EncPlan &pl) {
         R.nchunks = ceil_div(R.npieces, CH);
         chunk += R.nchunks;
         piece += R.nchunks * CH;
+        R.q_base = pl.qtotal;
+        pl.qtotal += R.n;
         R.mask = h[r].mask;
         for (int a = 0; a < 3; ++a) {
             R.lo[a] = h[r].lo[a];
@@ -769,6 +933,8 @@ static void carve(EncPlan &pl, void *base, size_t cap) {
     pl.seg_raw = c.take<uint32_t>(nreg + 1);
     pl.codec2 = c.take<int32_t>(nreg);
     pl.item_reg = c.take<int32_t>(pl.nitems + 1);
+    pl.chunk_reg = c.take<int32_t>(pl.nchunks + 1);
+    pl.qz = c.take<uint32_t>(pl.qtotal + 1);
     pl.scal = c.take<EncScalars>(1);
     pl.ws_bytes = c.off + 256;
 }
@@ -847,19 +1013,19 @@ extern "C" int chr_compress(const void *d_vol, int dtype, int src_dtype, int64_t
     const unsigned items = (unsigned)pl.nitems, chunks = (unsigned)pl.nchunks;
     {
         CHR_PROF("k_tile_fill_map", st);
-        k_tile_fill_map<<<(unsigned)nreg, 256, 0, st>>>(pl.d_regs, nreg, pl.item_reg);
+        k_tile_fill_map<<<(unsigned)nreg, 256, 0, st>>>(pl.d_regs, nreg, pl.item_reg, pl.chunk_reg);
     }
     if (dtype == CHR_F32)
         {
             CHR_PROF("k_tile<float, false>", st);
             k_tile<float, false><<<items, NW * 32, 0, st>>>((const float *)d_vol, pl.params, pl.d_regs, pl.item_reg,
-                                                            pl.recs, pl.poffs, d_out);
+                                                            pl.recs, pl.poffs, pl.qz, d_out);
         }
     else
         {
             CHR_PROF("k_tile<double, false>", st);
             k_tile<double, false><<<items, NW * 32, 0, st>>>((const double *)d_vol, pl.params, pl.d_regs, pl.item_reg,
-                                                             pl.recs, pl.poffs, d_out);
+                                                             pl.recs, pl.poffs, pl.qz, d_out);
         }
     {
         CHR_PROF("k_scan_reduce", st);
@@ -867,8 +1033,8 @@ extern "C" int chr_compress(const void *d_vol, int dtype, int src_dtype, int64_t
     }
     {
         CHR_PROF("k_scan_regions", st);
-        k_scan_regions<<<(unsigned)ceil_div(nreg, 128), 128, 0, st>>>(pl.params, pl.d_regs, pl.chunk,
-                                                                      pl.codec2, pl.scal);
+        k_scan_regions<<<(unsigned)ceil_div(nreg, 4), 128, 0, st>>>(pl.params, pl.d_regs, pl.chunk,
+                                                                    pl.codec2, pl.scal);
     }
     {
         CHR_PROF("k_layout", st);
@@ -880,9 +1046,9 @@ extern "C" int chr_compress(const void *d_vol, int dtype, int src_dtype, int64_t
     }
     if (dtype == CHR_F32) {
         {
-            CHR_PROF("k_tile<float, true>", st);
-            k_tile<float, true><<<items, NW * 32, 0, st>>>((const float *)d_vol, pl.params, pl.d_regs, pl.item_reg,
-                                                           pl.recs, pl.poffs, d_out);
+            CHR_PROF("k_emit_q<float>", st);
+            k_emit_q<float><<<chunks, 256, 0, st>>>((const float *)d_vol, pl.params, pl.d_regs, pl.chunk_reg,
+                                                    pl.recs, pl.poffs, pl.qz, d_out);
         }
         {
             CHR_PROF("k_bitmap<float>", st);
@@ -891,9 +1057,9 @@ extern "C" int chr_compress(const void *d_vol, int dtype, int src_dtype, int64_t
         }
     } else {
         {
-            CHR_PROF("k_tile<double, true>", st);
-            k_tile<double, true><<<items, NW * 32, 0, st>>>((const double *)d_vol, pl.params, pl.d_regs, pl.item_reg,
-                                                            pl.recs, pl.poffs, d_out);
+            CHR_PROF("k_emit_q<double>", st);
+            k_emit_q<double><<<chunks, 256, 0, st>>>((const double *)d_vol, pl.params, pl.d_regs, pl.chunk_reg,
+                                                     pl.recs, pl.poffs, pl.qz, d_out);
         }
         {
             CHR_PROF("k_bitmap<double>", st);
@@ -915,7 +1081,7 @@ extern "C" int chr_compress(const void *d_vol, int dtype, int src_dtype, int64_t
     if (rc) return rc;
     {
         CHR_PROF("k_finalize_regions", st);
-        k_finalize_regions<<<(unsigned)ceil_div(nreg, 128), 128, 0, st>>>(pl.params, pl.d_regs, pl.seg_raw,
+        k_finalize_regions<<<(unsigned)ceil_div(nreg, 4), 128, 0, st>>>(pl.params, pl.d_regs, pl.seg_raw,
                                                                           tabs, pl.scal, d_out);
     }
     if (write_file)

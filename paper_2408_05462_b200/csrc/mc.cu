@@ -117,6 +117,9 @@ struct McGrid {
     int64_t piece_base, npieces, chunk_base, nchunks, item_base;
     int64_t tri_base, vert_base;    // in the merged output (device scan)
     int64_t ntri, nvert;
+    int64_t mask_off;               // inside mask (v >= k): word offset, plane-linear bits
+    int64_t mask_item_base;         // k_mc_mask items: planes x ceil(pw / 64)
+    int32_t pw, pad2;               // mask words per plane
 };
 
 struct McPieceCnt {
@@ -305,12 +308,57 @@ __device__ __forceinline__ double world(double origin, double lat, double spacin
 // f64 sample row is loaded once per plane by one warp (coalesced), turned
 // into an inside mask with ballots, and the Bourke code of a cell is
 // assembled from four 64-bit row masks (rows y, y+1 at planes z, z+1).
-__global__ void k_mc_fill_map(const McGrid *__restrict__ G, int64_t ng, int32_t *__restrict__ item_grid) {
+__global__ void k_mc_fill_map(const McGrid *__restrict__ G, int64_t ng, int32_t *__restrict__ item_grid,
+                              int32_t *__restrict__ chunk_grid, int32_t *__restrict__ mask_grid) {
     const int64_t i = blockIdx.x;
     if (i >= ng) return;
     const McGrid &g = G[i];
     const int64_t nit = (int64_t)g.ntx * ((g.ncy + MTY - 1) / MTY) * ((g.ncz + MZC - 1) / MZC);
     for (int64_t t = threadIdx.x; t < nit; t += blockDim.x) item_grid[g.item_base + t] = (int32_t)i;
+    for (int64_t t = threadIdx.x; t < g.nchunks; t += blockDim.x) chunk_grid[g.chunk_base + t] = (int32_t)i;
+    const int64_t nm = (int64_t)g.nz * ((g.pw + 63) / 64);
+    for (int64_t t = threadIdx.x; t < nm; t += blockDim.x) mask_grid[g.mask_item_base + t] = (int32_t)i;
+}
+
+// ------------------------------------------------------------------ inside masks
+// One bit per sample (v >= k), plane-linear (bit y * nx + x of the plane's
+// words): 1/64 of the f64 bytes, so the count and emit passes stream masks
+// and touch f64 samples only to interpolate vertices.  Item = 64 words of
+// one plane; warp = 8 words, all loads issued before the ballots.
+__global__ void __launch_bounds__(256) k_mc_mask(const double *__restrict__ grids, const McGrid *__restrict__ G,
+                                                 const int32_t *__restrict__ mask_grid, double k,
+                                                 uint32_t *__restrict__ mask) {
+    const int64_t item = blockIdx.x;
+    const McGrid &g = G[__ldg(mask_grid + item)];
+    const int64_t local = item - g.mask_item_base;
+    const int wpb = (g.pw + 63) / 64;
+    const int z = (int)(local / wpb), wc = (int)(local - (int64_t)z * wpb);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t nxy = (int64_t)g.nx * g.ny;
+    const double *gp = grids + g.goff + (int64_t)z * nxy;
+    const int w0 = wc * 64 + warp * 8;
+    double v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int64_t t = (int64_t)(w0 + i) * 32 + lane;
+        v[i] = (w0 + i < g.pw && t < nxy) ? __ldg(gp + t) : 0.0;
+    }
+    uint32_t *mp = mask + g.mask_off + (int64_t)z * g.pw;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int64_t t = (int64_t)(w0 + i) * 32 + lane;
+        const uint32_t b = __ballot_sync(0xFFFFFFFFu, t < nxy && v[i] >= k);
+        if (lane == 0 && w0 + i < g.pw) mp[w0 + i] = b;
+    }
+}
+
+// 64 bits of a plane mask from bit `b` (m) and the 2 bits after (h)
+__device__ __forceinline__ void mask_bits66(const uint32_t *__restrict__ mp, int64_t b, uint64_t &m, uint32_t &h) {
+    const uint32_t *w = mp + (b >> 5);
+    const int sh = (int)(b & 31);
+    const uint32_t w0 = __ldg(w), w1 = __ldg(w + 1), w2 = __ldg(w + 2), w3 = __ldg(w + 3);
+    m = (uint64_t)__funnelshift_r(w0, w1, sh) | ((uint64_t)__funnelshift_r(w1, w2, sh) << 32);
+    h = __funnelshift_r(w2, w3, sh) & 3u;
 }
 
 // bits c and c+1 of a (lo | hi << 64) mask
@@ -342,70 +390,103 @@ __device__ __forceinline__ int code_from(uint64_t m00, uint32_t h00, uint64_t m1
                  bit_at(m11, h11, c + 1) << 6 | bit_at(m11, h11, c) << 7);
 }
 
-__global__ void __launch_bounds__(288, 5) k_mc_count2(const double *__restrict__ grids, const McGrid *__restrict__ G,
-                                                   const int32_t *__restrict__ item_grid, double k,
-                                                   const McTables *__restrict__ T, McPieceCnt *__restrict__ cnt) {
-    __shared__ uint64_t mk[3][9];
-    __shared__ uint32_t mkx[3][9];
-    __shared__ uint8_t s_ntri[256];
-    __shared__ uint8_t s_own[256][8];
+// count from the masks: warp per 64-cell row piece, CTA per scan chunk
+__global__ void __launch_bounds__(256) k_mc_count3(const McGrid *__restrict__ G,
+                                                   const int32_t *__restrict__ chunk_grid,
+                                                   const McTables *__restrict__ T,
+                                                   const uint32_t *__restrict__ mask,
+                                                   McPieceCnt *__restrict__ cnt) {
+    __shared__ __align__(16) uint8_t s_ntri[256];
+    __shared__ __align__(16) uint8_t s_own[256][8];
     __shared__ McGrid g;
-    for (int i = threadIdx.x; i < 256; i += blockDim.x) s_ntri[i] = T->ntri[i];
-    for (int i = threadIdx.x; i < 2048; i += blockDim.x) (&s_own[0][0])[i] = (&T->owncnt[0][0])[i];
-    const int64_t item = blockIdx.x;
-    coop_copy(&g, G + __ldg(item_grid + item));
-    __syncthreads();
-    const int nyt = (g.ncy + MTY - 1) / MTY;
-    const int64_t local = item - g.item_base;
-    const int xt = (int)(local % g.ntx);
-    const int64_t r2 = local / g.ntx;
-    const int yt = (int)(r2 % nyt), zc = (int)(r2 / nyt);
-    const int x0 = xt * MTX, y0 = yt * MTY, z0 = zc * MZC;
-    const int z1 = min(z0 + MZC, g.ncz);
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int sy = y0 + w;
-    const bool rowok = sy < g.ny;
-    const double *gp = grids + g.goff;
-    const int64_t nxy = (int64_t)g.nx * g.ny;
-    const int xa = x0 + lane, xb = x0 + 32 + lane, xe = x0 + 64;
-    const bool oka = rowok && xa < g.nx, okb = rowok && xb < g.nx, oke = rowok && lane == 0 && xe < g.nx;
-    double ca = 0.0, cb2 = 0.0, ce = 0.0;  // plane p (prefetched)
     {
-        const double *row = gp + (int64_t)z0 * nxy + (int64_t)sy * g.nx;
-        if (oka) ca = __ldg(row + xa);
-        if (okb) cb2 = __ldg(row + xb);
-        if (oke) ce = __ldg(row + xe);
+        const uint4 *so = reinterpret_cast<const uint4 *>(T->owncnt);
+        uint4 *d_o = reinterpret_cast<uint4 *>(&s_own[0][0]);
+        for (int i = threadIdx.x; i < 128; i += blockDim.x) d_o[i] = __ldg(so + i);
+        if (threadIdx.x < 16)
+            reinterpret_cast<uint4 *>(s_ntri)[threadIdx.x] = __ldg(reinterpret_cast<const uint4 *>(T->ntri) + threadIdx.x);
     }
-    for (int p = z0; p <= z1; ++p) {
-        const bool ia = oka && ca >= k;
-        const bool ib = okb && cb2 >= k;
-        const bool ie = oke && ce >= k;
-        if (p < z1) {  // prefetch plane p+1
-            const double *row = gp + (int64_t)(p + 1) * nxy + (int64_t)sy * g.nx;
-            if (oka) ca = __ldg(row + xa);
-            if (okb) cb2 = __ldg(row + xb);
-            if (oke) ce = __ldg(row + xe);
+    const int64_t c = blockIdx.x;
+    coop_copy(&g, G + __ldg(chunk_grid + c));
+    __syncthreads();
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr int PW = (int)(MCH / 8);
+    int64_t lp = (c - g.chunk_base) * MCH + (int64_t)w * PW;
+    const int64_t lpe = min(lp + PW, g.npieces);
+    if (lp >= lpe) return;
+    int xt = (int)(lp % g.ntx);
+    const int64_t r = lp / g.ntx;
+    int cy = (int)(r % g.ncy), cz = (int)(r / g.ncy);
+    const uint32_t *mbase = mask + g.mask_off;
+    if (g.ntx == 1 && g.ncx <= 32) {
+        // rows of <= 32 cells: two pieces (rows) per step, one per lane
+        const int lane_ok = lane < g.ncx;
+        for (; lp < lpe; lp += 2) {
+            int cy2 = cy + 1, cz2 = cz;
+            if (cy2 == g.ncy) {
+                cy2 = 0;
+                ++cz2;
+            }
+            const bool two = lp + 1 < lpe;
+            int t = 0, v = 0, t2 = 0, v2 = 0;
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const int qy = q ? cy2 : cy, qz = q ? cz2 : cz;
+                if (q && !two) break;
+                const uint32_t *mp0 = mbase + (int64_t)qz * g.pw, *mp1 = mp0 + g.pw;
+                const int64_t b0 = (int64_t)qy * g.nx, b1 = b0 + g.nx;
+                uint64_t m00, m10, m01, m11;
+                uint32_t h00, h10, h01, h11;
+                mask_bits66(mp0, b0, m00, h00);
+                mask_bits66(mp0, b1, m10, h10);
+                mask_bits66(mp1, b0, m01, h01);
+                mask_bits66(mp1, b1, m11, h11);
+                if (lane_ok) {
+                    const int code = code_fast(m00, h00, m10, h10, m01, h01, m11, h11, lane);
+                    (q ? t2 : t) = s_ntri[code];
+                    (q ? v2 : v) = s_own[code][bflags(lane, qy, qz)];
+                }
+            }
+            const uint32_t pa = __reduce_add_sync(0xFFFFFFFFu, (uint32_t)t | ((uint32_t)v << 16));
+            const uint32_t pb = __reduce_add_sync(0xFFFFFFFFu, (uint32_t)t2 | ((uint32_t)v2 << 16));
+            if (lane == 0) {
+                McPieceCnt o;
+                o.tri = (int32_t)(pa & 0xFFFFu);
+                o.vert = (int32_t)(pa >> 16);
+                cnt[g.piece_base + lp] = o;
+                if (two) {
+                    o.tri = (int32_t)(pb & 0xFFFFu);
+                    o.vert = (int32_t)(pb >> 16);
+                    cnt[g.piece_base + lp + 1] = o;
+                }
+            }
+            cy = cy2 + 1;
+            cz = cz2;
+            if (cy == g.ncy) {
+                cy = 0;
+                ++cz;
+            }
         }
-        const uint64_t m = (uint64_t)__ballot_sync(0xFFFFFFFFu, ia) | ((uint64_t)__ballot_sync(0xFFFFFFFFu, ib) << 32);
-        if (lane == 0) {
-            mk[p % 3][w] = m;
-            mkx[p % 3][w] = ie ? 1u : 0u;
-        }
-        __syncthreads();
-        if (p == z0 || w >= MTY) continue;
-        const int cz = p - 1, cy = y0 + w;
-        if (cy >= g.ncy) continue;
-        const int b0 = cz % 3, b1 = p % 3;
-        const uint64_t m00 = mk[b0][w], m10 = mk[b0][w + 1], m01 = mk[b1][w], m11 = mk[b1][w + 1];
-        const uint32_t h00 = mkx[b0][w], h10 = mkx[b0][w + 1], h01 = mkx[b1][w], h11 = mkx[b1][w + 1];
+        return;
+    }
+    for (; lp < lpe; ++lp) {
+        const int x0 = xt * MTX;
+        const uint32_t *mp0 = mbase + (int64_t)cz * g.pw, *mp1 = mp0 + g.pw;
+        const int64_t b0 = (int64_t)cy * g.nx + x0, b1 = b0 + g.nx;
+        uint64_t m00, m10, m01, m11;
+        uint32_t h00, h10, h01, h11;
+        mask_bits66(mp0, b0, m00, h00);
+        mask_bits66(mp0, b1, m10, h10);
+        mask_bits66(mp1, b0, m01, h01);
+        mask_bits66(mp1, b1, m11, h11);
         int t = 0, v = 0;
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int c = lane + 32 * h;
-            if (x0 + c < g.ncx) {
-                const int code = code_fast(m00, h00, m10, h10, m01, h01, m11, h11, c);
+        for (int hh = 0; hh < 2; ++hh) {
+            const int cc = lane + 32 * hh;
+            if (x0 + cc < g.ncx) {
+                const int code = code_fast(m00, h00, m10, h10, m01, h01, m11, h11, cc);
                 t += s_ntri[code];
-                v += s_own[code][bflags(x0 + c, cy, cz)];
+                v += s_own[code][bflags(x0 + cc, cy, cz)];
             }
         }
         t = __reduce_add_sync(0xFFFFFFFFu, t);
@@ -414,7 +495,14 @@ __global__ void __launch_bounds__(288, 5) k_mc_count2(const double *__restrict__
             McPieceCnt o;
             o.tri = t;
             o.vert = v;
-            cnt[g.piece_base + ((int64_t)cz * g.ncy + cy) * g.ntx + xt] = o;
+            cnt[g.piece_base + lp] = o;
+        }
+        if (++xt == g.ntx) {
+            xt = 0;
+            if (++cy == g.ncy) {
+                cy = 0;
+                ++cz;
+            }
         }
     }
 }
@@ -423,13 +511,13 @@ __global__ void __launch_bounds__(288, 5) k_mc_count2(const double *__restrict__
 // 3-deep ring; cells rows y0-1..y0+7 x columns x0-1..x0+63 (65) with their
 // (code, vertex base) in a 3-deep ring, so every owner is local.
 constexpr int EW = 10;  // warps: sample rows y0-1 .. y0+8
-__device__ __forceinline__ int qb_of(int b) { return b == 2 ? 0 : b + 1; }  // next slot of a 3-deep ring
 __global__ void __launch_bounds__(EW * 32, 3) k_mc_emit2(const double *__restrict__ grids, const McGrid *__restrict__ G,
                                                       const int32_t *__restrict__ item_grid, double k,
                                                       const McTables *__restrict__ T,
                                                       const McPieceBase *__restrict__ base,
+                                                      const McPieceCnt *__restrict__ cnt,
+                                                      const uint32_t *__restrict__ mask,
                                                       double *__restrict__ verts, int32_t *__restrict__ tris) {
-    __shared__ double sv[3][EW][66];
     __shared__ uint64_t mk[3][EW];
     __shared__ uint32_t mkx[3][EW];
     __shared__ uint8_t sC[3][EW - 1][65];
@@ -471,8 +559,6 @@ __global__ void __launch_bounds__(EW * 32, 3) k_mc_emit2(const double *__restric
     // sample row of this warp: y0 - 1 + w ; columns c <-> x = x0 - 1 + c
     const int sy = y0 - 1 + w;
     const bool srow = sy >= 0 && sy < g.ny;
-    const int xa = x0 - 1 + lane, xb = x0 + 31 + lane, xe = x0 + 63 + lane;  // c = lane, lane+32, 64+lane
-    const bool oka = srow && xa >= 0 && xa < g.nx, okb = srow && xb < g.nx, oke = srow && lane < 2 && xe < g.nx;
     // cell row of this warp (w < 9): cy = y0 - 1 + w ; cells c = 1 + lane, 33 + lane, and c = 0 (lane 0)
     const int cy = y0 - 1 + w;
     const bool crow = w < EW - 1 && cy >= 0 && cy < g.ncy;
@@ -482,34 +568,41 @@ __global__ void __launch_bounds__(EW * 32, 3) k_mc_emit2(const double *__restric
     McPieceBase pnext;  // piece base of the next cell plane (prefetched)
     pnext.tri = 0;
     pnext.vert = 0;
-    if (crow) pnext = base[pb_row + (int64_t)pstart * pb_step];
-    double na = 0.0, nb = 0.0, ne = 0.0;  // prefetched plane
-    {
-        const double *row = gp + (int64_t)pstart * nxy + (int64_t)sy * g.nx;
-        if (oka) na = __ldg(row + xa);
-        if (okb) nb = __ldg(row + xb);
-        if (oke) ne = __ldg(row + xe);
+    McPieceCnt cnext;
+    cnext.tri = 0;
+    cnext.vert = 0;
+    if (crow) {
+        pnext = base[pb_row + (int64_t)pstart * pb_step];
+        cnext = cnt[pb_row + (int64_t)pstart * pb_step];
     }
+    // row masks of sample row sy, columns x0-1 .. x0+64 (bit c <-> x0 - 1 + c),
+    // read by lane 0 from the plane masks one plane ahead
+    const uint32_t *mbase = mask + g.mask_off;
+    auto row_mask = [&](int p, uint64_t &m, uint32_t &mx) {
+        m = 0;
+        mx = 0;
+        if (!srow) return;
+        const uint32_t *mp = mbase + (int64_t)p * g.pw;
+        const int64_t b = (int64_t)sy * g.nx + x0;
+        if (x0 > 0) {
+            mask_bits66(mp, b - 1, m, mx);
+        } else {
+            uint64_t m1;
+            uint32_t h1;
+            mask_bits66(mp, b, m1, h1);
+            m = m1 << 1;
+            mx = (uint32_t)(m1 >> 63) | ((h1 & 1u) << 1);
+        }
+    };
+    uint64_t nm = 0;
+    uint32_t nmx = 0;
+    if (lane == 0) row_mask(pstart, nm, nmx);
     for (int p = pstart; p <= z1; ++p) {
         const int pb = p % 3;
-        {
-            const double va = na, vb = nb, ve = ne;
-            if (p < z1) {
-                const double *row = gp + (int64_t)(p + 1) * nxy + (int64_t)sy * g.nx;
-                if (oka) na = __ldg(row + xa);
-                if (okb) nb = __ldg(row + xb);
-                if (oke) ne = __ldg(row + xe);
-            }
-            sv[pb][w][lane] = va;
-            sv[pb][w][lane + 32] = vb;
-            if (lane < 2) sv[pb][w][64 + lane] = ve;
-            const uint64_t m = (uint64_t)__ballot_sync(0xFFFFFFFFu, oka && va >= k) |
-                               ((uint64_t)__ballot_sync(0xFFFFFFFFu, okb && vb >= k) << 32);
-            const uint32_t mx = __ballot_sync(0xFFFFFFFFu, oke && ve >= k) & 3u;
-            if (lane == 0) {
-                mk[pb][w] = m;
-                mkx[pb][w] = mx;
-            }
+        if (lane == 0) {
+            mk[pb][w] = nm;
+            mkx[pb][w] = nmx;
+            if (p < z1) row_mask(p + 1, nm, nmx);
         }
         __syncthreads();
         if (p == pstart) continue;  // need planes cz and cz+1
@@ -517,12 +610,28 @@ __global__ void __launch_bounds__(EW * 32, 3) k_mc_emit2(const double *__restric
         // ---- codes, owned counts, vertex bases of cell row cy at plane cz
         int codeA = 0, codeB = 0, ntA = 0, ntB = 0, tA = 0, tB = 0, ownA = 0, ownB = 0, exA = 0, exB = 0;
         const McPieceBase pbase = pnext;
-        if (crow && cz + 1 < z1) pnext = base[pb_row + (int64_t)(cz + 1) * pb_step];
+        const McPieceCnt pcnt = cnext;
+        if (crow && cz + 1 < z1) {
+            pnext = base[pb_row + (int64_t)(cz + 1) * pb_step];
+            cnext = cnt[pb_row + (int64_t)(cz + 1) * pb_step];
+        }
         if (w < EW - 1) {
             int codeH = 0, ownH = 0;
+            uint64_t m00 = 0, m10 = 0, m01 = 0, m11 = 0;
+            uint32_t h00 = 0, h10 = 0, h01 = 0, h11 = 0;
+            bool live = false;
             if (crow) {
-                const uint64_t m00 = mk[cb][w], m10 = mk[cb][w + 1], m01 = mk[qb][w], m11 = mk[qb][w + 1];
-                const uint32_t h00 = mkx[cb][w], h10 = mkx[cb][w + 1], h01 = mkx[qb][w], h11 = mkx[qb][w + 1];
+                m00 = mk[cb][w], m10 = mk[cb][w + 1], m01 = mk[qb][w], m11 = mk[qb][w + 1];
+                h00 = mkx[cb][w], h10 = mkx[cb][w + 1], h01 = mkx[qb][w], h11 = mkx[qb][w + 1];
+                if (x0 > 0) {
+                    codeH = code_fast(m00, h00, m10, h10, m01, h01, m11, h11, 0);
+                    ownH = s_own[codeH][bflags(x0 - 1, cy, cz)];
+                }
+                // a row with no triangles (its halo cell included) is never an
+                // owner of a crossing edge, so nothing of it is looked up
+                live = pcnt.tri > 0 || s_ntri[codeH] > 0;
+            }
+            if (live) {
                 const int xA = x0 + lane, xB = x0 + 32 + lane;
                 if (xA < g.ncx) {
                     codeA = code_fast(m00, h00, m10, h10, m01, h01, m11, h11, lane + 1);
@@ -534,11 +643,6 @@ __global__ void __launch_bounds__(EW * 32, 3) k_mc_emit2(const double *__restric
                     ownB = s_own[codeB][bflags(xB, cy, cz)];
                     ntB = s_ntri[codeB];
                 }
-                if (lane == 0 && x0 > 0) {
-                    codeH = code_fast(m00, h00, m10, h10, m01, h01, m11, h11, 0);
-                    ownH = s_own[codeH][bflags(x0 - 1, cy, cz)];
-                }
-            }
             // one scan of packed (owned | triangles << 16) for columns lane and 32 + lane
             uint32_t pA = (uint32_t)ownA | ((uint32_t)ntA << 16), pB = (uint32_t)ownB | ((uint32_t)ntB << 16);
 #pragma unroll
@@ -565,6 +669,7 @@ __global__ void __launch_bounds__(EW * 32, 3) k_mc_emit2(const double *__restric
             if (lane == 0) {
                 sC[cb][w][0] = (uint8_t)codeH;
                 sV[cb][w][0] = pbase.vert - ownH;
+            }
             }
         }
         __syncthreads();
@@ -618,10 +723,9 @@ __global__ void __launch_bounds__(EW * 32, 3) k_mc_emit2(const double *__restric
                     const int e = __ldg(&T->inv[code][f][r]);
                     const int a = s_eax[e];
                     const int lx = s_elow[e][0], ly = s_elow[e][1], lz = s_elow[e][2];
-                    const int zb = lz ? qb_of(cb) : cb;
-                    const double s0 = sv[zb][w + ly][c + lx];
-                    const double s1 = a == 2 ? sv[qb_of(zb)][w + ly][c + lx]
-                                             : sv[zb][w + ly + (a == 1)][c + lx + (a == 0)];
+                    const double *sp = gp + (int64_t)(cz + lz) * nxy + (int64_t)(cy + ly) * g.nx + (cx + lx);
+                    const double s0 = __ldg(sp);
+                    const double s1 = __ldg(sp + (a == 0 ? 1 : (a == 1 ? (int64_t)g.nx : nxy)));
                     const double den = __dadd_rn(s1, -s0);
                     const double t = den == 0.0 ? 0.0 : __ddiv_rn(__dadd_rn(k, -s0), den);
                     double lat[3] = {(double)(cx + lx), (double)(cy + ly), (double)(cz + lz)};
@@ -656,13 +760,14 @@ __global__ void k_case_codes(const double *__restrict__ g, int64_t nx, int64_t n
 // ------------------------------------------------------------------ host
 struct McPlan {
     std::vector<McGrid> grids;
-    int64_t npieces = 0, nchunks = 0, nitems = 0;
+    int64_t npieces = 0, nchunks = 0, nitems = 0, nmask_items = 0, nmask_words = 0;
     size_t ws = 0;
     McGrid *d_grids;
     McPieceCnt *cnt;
     McPieceBase *chunk, *base;
     int64_t *totals;
-    int32_t *item_grid;
+    int32_t *item_grid, *chunk_grid, *mask_grid;
+    uint32_t *mask;
 };
 
 static bool mc_build(const chr_mc_grid_t *h, int64_t n, McPlan &pl) {
@@ -692,6 +797,11 @@ static bool mc_build(const chr_mc_grid_t *h, int64_t n, McPlan &pl) {
         chunk += g.nchunks;
         g.item_base = item;
         item += (int64_t)g.ntx * ceil_div(g.ncy, MTY) * ceil_div(g.ncz, MZC);
+        g.pw = (int32_t)ceil_div((int64_t)g.nx * g.ny, 32);
+        g.mask_off = pl.nmask_words;
+        pl.nmask_words += (int64_t)g.pw * g.nz;
+        g.mask_item_base = pl.nmask_items;
+        pl.nmask_items += (int64_t)g.nz * ceil_div(g.pw, 64);
     }
     pl.npieces = piece;
     pl.nchunks = chunk;
@@ -707,6 +817,9 @@ static void mc_carve(McPlan &pl, void *base, size_t cap) {
     pl.base = c.take<McPieceBase>(pl.npieces);
     pl.totals = c.take<int64_t>(2);
     pl.item_grid = c.take<int32_t>(pl.nitems + 1);
+    pl.chunk_grid = c.take<int32_t>(pl.nchunks + 1);
+    pl.mask_grid = c.take<int32_t>(pl.nmask_items + 1);
+    pl.mask = c.take<uint32_t>(pl.nmask_words + 8);  // + slack: 4-word reads past a plane
     pl.ws = c.off + 256;
 }
 
@@ -741,11 +854,16 @@ extern "C" int chr_mc_count(const double *d_grids, const chr_mc_grid_t *h, int64
     CHR_CUDA_TRY(cudaMemsetAsync(pl.cnt, 0, sizeof(McPieceCnt) * pl.npieces, st));
     {
         CHR_PROF("k_mc_fill_map", st);
-        k_mc_fill_map<<<(unsigned)n, 256, 0, st>>>(pl.d_grids, n, pl.item_grid);
+        k_mc_fill_map<<<(unsigned)n, 256, 0, st>>>(pl.d_grids, n, pl.item_grid, pl.chunk_grid, pl.mask_grid);
     }
-    if (pl.nitems > 0) {
-        CHR_PROF("k_mc_count2", st);
-        k_mc_count2<<<(unsigned)pl.nitems, 288, 0, st>>>(d_grids, pl.d_grids, pl.item_grid, k, T, pl.cnt);
+    CHR_CUDA_TRY(cudaMemsetAsync(pl.mask + pl.nmask_words, 0, 8 * sizeof(uint32_t), st));
+    if (pl.nmask_items > 0) {
+        CHR_PROF("k_mc_mask", st);
+        k_mc_mask<<<(unsigned)pl.nmask_items, 256, 0, st>>>(d_grids, pl.d_grids, pl.mask_grid, k, pl.mask);
+    }
+    if (pl.nchunks > 0) {
+        CHR_PROF("k_mc_count3", st);
+        k_mc_count3<<<(unsigned)pl.nchunks, 256, 0, st>>>(pl.d_grids, pl.chunk_grid, T, pl.mask, pl.cnt);
     }
     {
         CHR_PROF("k_mc_reduce", st);
@@ -793,7 +911,7 @@ extern "C" int chr_mc_emit(const double *d_grids, const chr_mc_grid_t *h, int64_
         {
             CHR_PROF("k_mc_emit2", st);
             k_mc_emit2<<<(unsigned)pl.nitems, EW * 32, 0, st>>>(d_grids, pl.d_grids, pl.item_grid, k, T, pl.base,
-                                                                 d_verts, d_tris);
+                                                                 pl.cnt, pl.mask, d_verts, d_tris);
         }
     CHR_CUDA_TRY(cudaGetLastError());
     CHR_CUDA_TRY(cudaStreamSynchronize(st));
