@@ -137,6 +137,8 @@ def kernel_bytes(name, info, N):
         "k_stats<float>": 4 * N,
         "k_stats_rows": 4 * N,
         "k_tile<float, false>": 4 * N,
+        "k_quant<float>": 4 * N + 4 * info["n_all"],
+        "k_summarize": 4 * info["n_all"],
         "k_tile<float, true>": 4 * N + c_all,
         "k_emit_q<float>": 4 * info["n_all"] + c_all,
         "k_crc_segments": None,

@@ -9,12 +9,15 @@
 // payloads in region order, CRC trailer).
 //
 // Pipeline (all on one stream, no host round trip):
-//   k_tile<COUNT>  per 64-sample row piece: token-byte summary (TokSeg)
+//   k_quant        quantise + Lorenzo q per sample -> token values (zigzag+1),
+//                  escape bits, f32-exactness flag
+//   k_summarize    per 64-sample piece of a window's stream: token-byte
+//                  summary (TokSeg)
 //   k_scan_reduce  chunk aggregates (chunks never straddle regions)
 //   k_scan_regions per region: chunk prefixes, totals, codec decision
 //   k_layout       region offsets in the file, CRC segment plan
 //   k_scan_down    per piece: token offset, zero-run carry, escape offset
-//   k_tile<EMIT>   recompute q, write every token byte at its final offset
+//   k_emit_q       write every token byte at its final offset
 //   k_bitmap       escape bitmaps (codec 2 regions only)
 //   k_write_table  file header + region table
 //   k_crc_segments payload + header-table CRCs (crc.cu)
@@ -44,6 +47,8 @@ struct RegDev {
     int64_t n;
     int64_t piece_base, npieces, item_base, chunk_base, nchunks;
     int64_t q_base;               // first token value of the region in the q buffer
+    int64_t ebase;                // first escape-bit word of the region
+    int32_t has_esc, f32bad;      // set by k_quant
     // results
     int32_t codec, f32ok;
     int64_t tok_len, nesc, payload_len;
@@ -147,18 +152,21 @@ __device__ __forceinline__ bool quant_fast(const Quant &Q, double v, int32_t &u)
     return Q.fast && fabs(qf) < kEscapeUmax && fabs(d) < kTieMargin;
 }
 
-template <typename T, bool EMIT>
-__global__ void __launch_bounds__(NW * 32, 4) k_tile(const T *__restrict__ vol, const EncParams *__restrict__ P,
-                                                  const RegDev *__restrict__ regs,
-                                                  const int32_t *__restrict__ item_reg,
-                                                  PieceRec *__restrict__ recs,
-                                                  const PieceOff *__restrict__ poffs,
-                                                  uint32_t *__restrict__ qz,
-                                                  uint8_t *__restrict__ out) {
+// Quantiser pass: CTA = 64 columns x 8 rows x 16 planes of one region
+// window (+ a halo row, column and plane), marching z; q = D - D(x-1) -
+// D(y-1) + D(x-1,y-1) with D = u(z) - u(z-1) in shared memory.  Writes the
+// token value zigzag(q) + 1 of every sample in the window's raster order,
+// the escape bits (rare) and the region's f32-inexact flag.
+template <typename T>
+__global__ void __launch_bounds__(NW * 32, 4) k_quant(const T *__restrict__ vol, const EncParams *__restrict__ P,
+                                                   RegDev *__restrict__ regs,
+                                                   const int32_t *__restrict__ item_reg,
+                                                   uint32_t *__restrict__ qz, uint32_t *__restrict__ escbits) {
     __shared__ int32_t sD[2][NW][TX + 2];
     __shared__ RegDev R;
     const int64_t item = blockIdx.x;
-    coop_copy(&R, regs + __ldg(item_reg + item));
+    const int ri = __ldg(item_reg + item);
+    coop_copy(&R, regs + ri);
     __syncthreads();
     const int64_t NX = P->NX, NY = P->NY, plane = NX * NY;
     const int64_t local = item - R.item_base;
@@ -176,13 +184,8 @@ __global__ void __launch_bounds__(NW * 32, 4) k_tile(const T *__restrict__ vol, 
     const bool okH = rowok && lane == 0 && xH >= 0;
     const bool quant = R.mode == 0;
     const Quant Q = make_quant(R.e);
-    const bool is_last_xt = xt == R.ntx - 1;
-    const int vcount = min(TX, R.ex - x0);
-    const int codec = EMIT ? R.codec : 0;
     const bool chk32 = sizeof(T) == 8 && P->src_dtype == CHR_F32;
-    const uint32_t lt = (1u << lane) - 1u;
     const T *row = vol + ((int64_t)(R.oz + z0) * NY + (R.oy + y)) * NX + R.ox;  // plane z0
-    const int64_t rec0 = R.piece_base + (int64_t)y * R.ntx + xt, rec_z = (int64_t)R.ey * R.ntx;
 
     // returns (warp-uniform) whether the exact sequence ran; escapes only come from it
     auto quant3 = [&](T a, T b, T h, int32_t &ua, int32_t &ub, int32_t &uh, bool &ea, bool &eb, bool &eh) {
@@ -213,6 +216,7 @@ __global__ void __launch_bounds__(NW * 32, 4) k_tile(const T *__restrict__ vol, 
         if (okB) nB = __ldg(row + xB);
         if (okH) nH = __ldg(row + xH);
     }
+    bool inexact = false;
     for (int z = z0; z < z1; ++z, row += plane) {
         const T vA = nA, vB = nB, vH = nH;
         if (z + 1 < z1) {  // prefetch the next plane
@@ -235,99 +239,83 @@ __global__ void __launch_bounds__(NW * 32, 4) k_tile(const T *__restrict__ vol, 
         if (w == 0 || !rowok) continue;
         const int32_t qA = D[w][lane + 1] - D[w][lane] - D[w - 1][lane + 1] + D[w - 1][lane];
         const int32_t qB = D[w][lane + 33] - D[w][lane + 32] - D[w - 1][lane + 33] + D[w - 1][lane + 32];
-        const bool nzA = okA && qA != 0, nzB = okB && qB != 0;
+        const int64_t s0 = ((int64_t)z * R.ey + y) * R.ex + x0;  // window sample index of column x0
+        uint32_t *qrow = qz + R.q_base + s0;
+        if (okA) qrow[lane] = zz1_32(qA);
+        if (okB) qrow[32 + lane] = zz1_32(qB);
+        if (slow) {
+            const uint32_t eAm = __ballot_sync(0xFFFFFFFFu, okA && eA), eBm = __ballot_sync(0xFFFFFFFFu, okB && eB);
+            if (lane == 0 && (eAm | eBm)) {  // 64 bits at window bit s0
+                const int64_t bit = (int64_t)R.ebase * 32 + s0;
+                uint32_t *wp = escbits + (bit >> 5);
+                const int sh = (int)(bit & 31);
+                const uint64_t m = (uint64_t)eAm | ((uint64_t)eBm << 32);
+                if (m << sh) {
+                    atomicOr(wp, (uint32_t)(m << sh));
+                    atomicOr(wp + 1, (uint32_t)((m << sh) >> 32));
+                }
+                if (sh && (m >> (64 - sh))) atomicOr(wp + 2, (uint32_t)(m >> (64 - sh)));
+                atomicOr(&regs[ri].has_esc, 1);
+            }
+        }
+        if (chk32) inexact |= (okA && not_f32_exact(vA)) || (okB && not_f32_exact(vB));
+    }
+    if (chk32 && __any_sync(0xFFFFFFFFu, inexact) && lane == 0) atomicOr(&regs[ri].f32bad, 1);
+}
+
+// Piece records: one warp per 64-sample piece of a window's raster stream,
+// a CTA per scan chunk (1024 pieces of one region).  Reads the token values.
+__global__ void __launch_bounds__(256) k_summarize(const RegDev *__restrict__ regs,
+                                                   const int32_t *__restrict__ chunk_reg,
+                                                   const uint32_t *__restrict__ qz,
+                                                   const uint32_t *__restrict__ escbits,
+                                                   PieceRec *__restrict__ recs) {
+    __shared__ RegDev R;
+    const int64_t c = blockIdx.x;
+    coop_copy(&R, regs + __ldg(chunk_reg + c));
+    __syncthreads();
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t lt = (1u << lane) - 1u;
+    constexpr int PW = (int)(CH / 8);
+    int64_t lp = (c - R.chunk_base) * CH + (int64_t)w * PW;
+    const int64_t lpe = min(lp + PW, R.npieces);
+    const uint32_t *q = qz + R.q_base;
+    for (; lp < lpe; ++lp) {
+        const int64_t s0 = lp * TX;
+        const int vcount = (int)min((int64_t)TX, R.n - s0);
+        const uint32_t zA = lane < vcount ? __ldg(q + s0 + lane) : 1u;
+        const uint32_t zB = 32 + lane < vcount ? __ldg(q + s0 + 32 + lane) : 1u;
+        const bool nzA = zA != 1u, nzB = zB != 1u;
         const uint32_t mA = __ballot_sync(0xFFFFFFFFu, nzA), mB = __ballot_sync(0xFFFFFFFFu, nzB);
-        const int64_t rec = rec0 + (int64_t)z * rec_z;
-        // previous nonzero (position in the piece) before element A (= lane) and B (= 32 + lane)
         const uint32_t bA = mA & lt, bB = mB & lt;
         const int prevA = bA ? 31 - __clz(bA) : -1;
         const int prevB = bB ? 63 - __clz(bB) : (mA ? 31 - __clz(mA) : -1);
-        const uint32_t zA = zz1_32(qA), zB = zz1_32(qB);
-        if (!EMIT) {  // token values (zigzag + 1) for k_emit_q, raster order of the window
-            uint32_t *qrow = qz + R.q_base + ((int64_t)z * R.ey + y) * R.ex + x0;
-            if (okA) qrow[lane] = zA;
-            if (okB) qrow[32 + lane] = zB;
-        }
-        const bool anyesc = slow && __any_sync(0xFFFFFFFFu, (okA && eA) || (okB && eB));
-        if (!EMIT) {
-            int b = 0;
-            if (nzA) b += (prevA >= 0 ? rb_small(lane - prevA - 1) : 0) + vlen32(zA);
-            if (nzB) b += (prevB >= 0 ? rb_small(32 + lane - prevB - 1) : 0) + vlen32(zB);
-            const int bytes = __reduce_add_sync(0xFFFFFFFFu, b);
+        int b = 0;
+        if (nzA) b += (prevA >= 0 ? rb_small(lane - prevA - 1) : 0) + vlen32(zA);
+        if (nzB) b += (prevB >= 0 ? rb_small(32 + lane - prevB - 1) : 0) + vlen32(zB);
+        const int bytes = __reduce_add_sync(0xFFFFFFFFu, b);
+        if (lane == 0) {
             int nesc = 0;
-            if (anyesc)
-                nesc = __popc(__ballot_sync(0xFFFFFFFFu, okA && eA)) + __popc(__ballot_sync(0xFFFFFFFFu, okB && eB));
-            bool anyinexact = false;
-            if (chk32) anyinexact = __any_sync(0xFFFFFFFFu, (okA && not_f32_exact(vA)) || (okB && not_f32_exact(vB)));
-            if (lane == 0) {
-                const int first = mA ? __ffs(mA) - 1 : (mB ? 31 + __ffs(mB) : vcount);
-                const int lastp = mB ? 63 - __clz(mB) : (mA ? 31 - __clz(mA) : -1);
-                PieceRec pr;
-                pr.bytes = (uint16_t)bytes;
-                pr.vcount = (uint8_t)vcount;
-                pr.lead = (uint8_t)first;
-                pr.trail = (uint8_t)((mA | mB) ? vcount - 1 - lastp : vcount);
-                pr.nesc = (uint8_t)nesc;
-                pr.flags = (uint8_t)(((mA | mB) ? 1 : 0) | (anyinexact ? 2 : 0));
-                pr.pad = 0;
-                recs[rec] = pr;
+            if (R.has_esc) {
+                const int64_t bit = (int64_t)R.ebase * 32 + s0;
+                const uint32_t *wp = escbits + (bit >> 5);
+                const int sh = (int)(bit & 31);
+                const uint64_t lo = (uint64_t)__funnelshift_r(wp[0], wp[1], sh) |
+                                    ((uint64_t)__funnelshift_r(wp[1], wp[2], sh) << 32);
+                const uint64_t keep = vcount == 64 ? ~0ull : ((1ull << vcount) - 1);
+                nesc = __popcll(lo & keep);
             }
-        } else {
-            if (codec == 1 || codec == 2) {
-                const PieceOff po = poffs[rec];
-                int64_t runA = 0, runB = 0;
-                int bAy = 0, bBy = 0;
-                if (nzA) {
-                    runA = prevA >= 0 ? lane - prevA - 1 : po.carry + lane;
-                    bAy = (prevA >= 0 ? rb_small((int)runA) : (int)run_bytes(runA)) + vlen32(zA);
-                }
-                if (nzB) {
-                    runB = prevB >= 0 ? 32 + lane - prevB - 1 : po.carry + 32 + lane;
-                    bBy = (prevB >= 0 ? rb_small((int)runB) : (int)run_bytes(runB)) + vlen32(zB);
-                }
-                int sA = bAy, sB = bBy;
-#pragma unroll
-                for (int off = 1; off < 32; off <<= 1) {
-                    const int ta = __shfl_up_sync(0xFFFFFFFFu, sA, off);
-                    const int tb = __shfl_up_sync(0xFFFFFFFFu, sB, off);
-                    if (lane >= off) {
-                        sA += ta;
-                        sB += tb;
-                    }
-                }
-                const int totA = __shfl_sync(0xFFFFFFFFu, sA, 31);
-                const int totB = __shfl_sync(0xFFFFFFFFu, sB, 31);
-                sA -= bAy;
-                sB = sB - bBy + totA;
-                uint8_t *base = out + R.tok_start + po.tok_off;
-                if (nzA) put_varint32(put_run(base + sA, runA), zA);
-                if (nzB) put_varint32(put_run(base + sB, runB), zB);
-                if (is_last_xt && y == R.ey - 1 && z == R.ez - 1 && lane == 0) {
-                    const int lastp = mB ? 63 - __clz(mB) : (mA ? 31 - __clz(mA) : -1);
-                    const int64_t fin = (mA | mB) ? vcount - 1 - lastp : po.carry + vcount;
-                    put_run(base + totA + totB, fin);
-                }
-                if (codec == 2 && anyesc) {
-                    const uint32_t eAm = __ballot_sync(0xFFFFFFFFu, okA && eA);
-                    const uint32_t eBm = __ballot_sync(0xFFFFFFFFu, okB && eB);
-                    const uint64_t vbase = R.payload_off + (uint64_t)((R.n + 7) >> 3);
-                    if (okA && eA) put_le(out + vbase + 8 * (po.esc_off + __popc(eAm & lt)), (double)vA);
-                    if (okB && eB)
-                        put_le(out + vbase + 8 * (po.esc_off + __popc(eAm) + __popc(eBm & lt)), (double)vB);
-                }
-            } else {
-                // verbatim: codec 3 (f32) or 0 (f64), raster order
-                const int64_t s0 = ((int64_t)z * R.ey + y) * R.ex + x0;
-                if (codec == 3) {
-                    uint8_t *base = out + R.payload_off + 4 * s0;
-                    if (okA) put_le(base + 4 * lane, (float)vA);
-                    if (okB) put_le(base + 4 * (32 + lane), (float)vB);
-                } else {
-                    uint8_t *base = out + R.payload_off + 8 * s0;
-                    if (okA) put_le(base + 8 * lane, (double)vA);
-                    if (okB) put_le(base + 8 * (32 + lane), (double)vB);
-                }
-            }
+            const int first = mA ? __ffs(mA) - 1 : (mB ? 31 + __ffs(mB) : vcount);
+            const int lastp = mB ? 63 - __clz(mB) : (mA ? 31 - __clz(mA) : -1);
+            PieceRec pr;
+            pr.bytes = (uint16_t)bytes;
+            pr.vcount = (uint8_t)vcount;
+            pr.lead = (uint8_t)first;
+            pr.trail = (uint8_t)((mA | mB) ? vcount - 1 - lastp : vcount);
+            pr.nesc = (uint8_t)nesc;
+            pr.flags = (uint8_t)((mA | mB) ? 1 : 0);
+            pr.pad = 0;
+            recs[R.piece_base + lp] = pr;
         }
     }
 }
@@ -344,17 +332,19 @@ __global__ void k_tile_fill_map(const RegDev *__restrict__ regs, int64_t nreg, i
 }
 
 // ------------------------------------------------------------------ emit
-// Token bytes from the stored token values: one warp per 64-sample row
-// piece, a CTA per scan chunk (1024 pieces of one region), no barriers.
-// Escaped samples (codec 2, rare) re-run the exact quantiser for their
-// flag; verbatim regions copy samples.
+// Token bytes from the stored token values: one warp per 64-sample piece of
+// the window's raster stream, a CTA per scan chunk, no barriers; the next
+// piece's values and offsets load while this one is written.  Escaped
+// samples (codec 2) come from the escape bits; verbatim regions copy
+// samples (raster position -> volume address).
 template <typename T>
 __global__ void __launch_bounds__(256) k_emit_q(const T *__restrict__ vol, const EncParams *__restrict__ P,
                                                 const RegDev *__restrict__ regs,
                                                 const int32_t *__restrict__ chunk_reg,
                                                 const PieceRec *__restrict__ recs,
                                                 const PieceOff *__restrict__ poffs,
-                                                const uint32_t *__restrict__ qz, uint8_t *__restrict__ out) {
+                                                const uint32_t *__restrict__ qz,
+                                                const uint32_t *__restrict__ escbits, uint8_t *__restrict__ out) {
     __shared__ RegDev R;
     const int64_t c = blockIdx.x;
     coop_copy(&R, regs + __ldg(chunk_reg + c));
@@ -367,41 +357,30 @@ __global__ void __launch_bounds__(256) k_emit_q(const T *__restrict__ vol, const
     if (lp >= lpe) return;
     const int codec = R.codec;
     const int64_t NX = P->NX, NY = P->NY;
-    int xt = (int)(lp % R.ntx);
-    const int64_t zy = lp / R.ntx;
-    int y = (int)(zy % R.ey), z = (int)(zy / R.ey);
-    const bool tok = codec == 1 || codec == 2;
-    // software pipeline: the next piece's token values and offsets load
-    // while this piece is written
-    auto fetch = [&](int xt_, int y_, int z_, int64_t lp_, uint32_t &a, uint32_t &b, PieceOff &o) {
-        const int x0_ = xt_ * TX, vc = min(TX, R.ex - x0_);
-        const int64_t s = ((int64_t)z_ * R.ey + y_) * R.ex + x0_;
-        a = lane < vc ? __ldg(qz + R.q_base + s + lane) : 1u;
-        b = 32 + lane < vc ? __ldg(qz + R.q_base + s + 32 + lane) : 1u;
-        o = poffs[R.piece_base + lp_];
+    const int64_t exy = (int64_t)R.ex * R.ey;
+    auto vol_at = [&](int64_t s) {  // window raster index -> sample
+        const int64_t z = s / exy, r = s - z * exy;
+        const int64_t y = r / R.ex, x = r - y * R.ex;
+        return __ldg(vol + ((R.oz + z) * NY + (R.oy + y)) * NX + R.ox + x);
     };
-    uint32_t nA = 1u, nB = 1u;
-    PieceOff npo{};
-    if (tok) fetch(xt, y, z, lp, nA, nB, npo);
-    for (; lp < lpe; ++lp) {
-        const int x0 = xt * TX;
-        const int vcount = min(TX, R.ex - x0);
-        const bool okA = lane < vcount, okB = 32 + lane < vcount;
-        const int64_t s0 = ((int64_t)z * R.ey + y) * R.ex + x0;  // window sample index
-        const int64_t rec = R.piece_base + lp;
-        const T *vrow = vol + ((int64_t)(R.oz + z) * NY + (R.oy + y)) * NX + R.ox + x0;
-        const int cz = z, cy = y;
-        if (++xt == R.ntx) {
-            xt = 0;
-            if (++y == R.ey) {
-                y = 0;
-                ++z;
-            }
-        }
-        if (tok) {
+    const uint32_t *q = qz + R.q_base;
+    if (codec == 1 || codec == 2) {
+        uint32_t nA = 1u, nB = 1u;
+        PieceOff npo{};
+        auto fetch = [&](int64_t p) {
+            const int64_t s = p * TX;
+            const int vc = (int)min((int64_t)TX, R.n - s);
+            nA = lane < vc ? __ldg(q + s + lane) : 1u;
+            nB = 32 + lane < vc ? __ldg(q + s + 32 + lane) : 1u;
+            npo = poffs[R.piece_base + p];
+        };
+        fetch(lp);
+        for (; lp < lpe; ++lp) {
+            const int64_t s0 = lp * TX;
+            const int vcount = (int)min((int64_t)TX, R.n - s0);
             const uint32_t zA = nA, zB = nB;
             const PieceOff po = npo;
-            if (lp + 1 < lpe) fetch(xt, y, z, lp + 1, nA, nB, npo);
+            if (lp + 1 < lpe) fetch(lp + 1);
             const bool nzA = zA != 1u, nzB = zB != 1u;
             const uint32_t mA = __ballot_sync(0xFFFFFFFFu, nzA), mB = __ballot_sync(0xFFFFFFFFu, nzB);
             const uint32_t bA = mA & lt, bB = mB & lt;
@@ -435,29 +414,33 @@ __global__ void __launch_bounds__(256) k_emit_q(const T *__restrict__ vol, const
                 const int64_t fin = (mA | mB) ? vcount - 1 - lastp : po.carry + vcount;
                 put_run(base + totA + totB, fin);
             }
-            if (codec == 2 && recs[rec].nesc) {
-                const Quant Q = make_quant(R.e);
-                bool eA = false, eB = false;
-                if (okA) quantize(Q, (double)__ldg(vrow + lane), eA);
-                if (okB) quantize(Q, (double)__ldg(vrow + 32 + lane), eB);
-                const uint32_t eAm = __ballot_sync(0xFFFFFFFFu, eA), eBm = __ballot_sync(0xFFFFFFFFu, eB);
+            if (codec == 2 && recs[R.piece_base + lp].nesc) {
+                const int64_t bit = (int64_t)R.ebase * 32 + s0;
+                const uint32_t *wp = escbits + (bit >> 5);
+                const int sh = (int)(bit & 31);
+                const uint32_t eAm = __funnelshift_r(wp[0], wp[1], sh), eBm = __funnelshift_r(wp[1], wp[2], sh);
+                const bool eA = lane < vcount && ((eAm >> lane) & 1u);
+                const bool eB = 32 + lane < vcount && ((eBm >> lane) & 1u);
                 const uint64_t vbase = R.payload_off + (uint64_t)((R.n + 7) >> 3);
-                if (eA) put_le(out + vbase + 8 * (po.esc_off + __popc(eAm & lt)), (double)__ldg(vrow + lane));
+                if (eA) put_le(out + vbase + 8 * (po.esc_off + __popc(eAm & lt)), (double)vol_at(s0 + lane));
                 if (eB)
-                    put_le(out + vbase + 8 * (po.esc_off + __popc(eAm) + __popc(eBm & lt)),
-                           (double)__ldg(vrow + 32 + lane));
+                    put_le(out + vbase + 8 * (po.esc_off + __popc(vcount >= 32 ? eAm : 0u) + __popc(eBm & lt)),
+                           (double)vol_at(s0 + 32 + lane));
             }
-        } else if (codec == 3) {  // verbatim f32, raster order
-            uint8_t *b = out + R.payload_off + 4 * s0;
-            if (okA) put_le(b + 4 * lane, (float)__ldg(vrow + lane));
-            if (okB) put_le(b + 4 * (32 + lane), (float)__ldg(vrow + 32 + lane));
-        } else {  // verbatim f64
-            uint8_t *b = out + R.payload_off + 8 * s0;
-            if (okA) put_le(b + 8 * lane, (double)__ldg(vrow + lane));
-            if (okB) put_le(b + 8 * (32 + lane), (double)__ldg(vrow + 32 + lane));
         }
-        (void)cz;
-        (void)cy;
+    } else {  // verbatim (codec 3: f32, codec 0: f64), raster order
+        for (; lp < lpe; ++lp) {
+            const int64_t s0 = lp * TX;
+            const int vcount = (int)min((int64_t)TX, R.n - s0);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int i = lane + 32 * h;
+                if (i >= vcount) continue;
+                const T v = vol_at(s0 + i);
+                if (codec == 3) put_le(out + R.payload_off + 4 * (s0 + i), (float)v);
+                else put_le(out + R.payload_off + 8 * (s0 + i), (double)v);
+            }
+        }
     }
 }
 
@@ -559,7 +542,7 @@ __global__ void k_scan_regions(const EncParams *__restrict__ P, RegDev *__restri
         acc = tokseg_combine(acc, tot);
     }
     if (lane != 0) return;
-    const bool f32ok = P->dtype == CHR_F32 ? true : acc.f32ok != 0;
+    const bool f32ok = P->dtype == CHR_F32 ? true : R.f32bad == 0;
     const bool vf32 = P->src_dtype == CHR_F32 && f32ok;
     const int64_t vlen = R.n * (vf32 ? 4 : 8);
     const int vcodec = vf32 ? 3 : 0;
@@ -728,33 +711,22 @@ __global__ void __launch_bounds__(256) k_scan_down(const EncParams *__restrict__
 }
 
 // escape bitmaps of codec-2 regions: one byte = 8 consecutive stream samples
-template <typename T>
-__global__ void __launch_bounds__(256) k_bitmap(const T *__restrict__ vol, const EncParams *__restrict__ P,
-                                                const RegDev *__restrict__ regs,
+// codec 2: the escape bitmap (np.packbits little-endian) from k_quant's bits
+__global__ void __launch_bounds__(256) k_bitmap(const RegDev *__restrict__ regs,
                                                 const int32_t *__restrict__ list,
                                                 const EncScalars *__restrict__ sc,
+                                                const uint32_t *__restrict__ escbits,
                                                 uint8_t *__restrict__ out) {
     const int64_t nl = sc->n_codec2;
-    const int64_t NX = P->NX, NY = P->NY;
     for (int64_t li = 0; li < nl; ++li) {
         const RegDev &R = regs[list[li]];
-        const Quant Q = make_quant(R.e);
         const int64_t nbytes = (R.n + 7) >> 3;
-        const int64_t plane = (int64_t)R.ex * R.ey;
+        const uint8_t *src = reinterpret_cast<const uint8_t *>(escbits + R.ebase);
         for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nbytes;
              b += (int64_t)gridDim.x * blockDim.x) {
-            uint8_t byte = 0;
-            for (int k = 0; k < 8; ++k) {
-                const int64_t s = 8 * b + k;
-                if (s >= R.n) break;
-                const int64_t z = s / plane, rem = s % plane;
-                const int64_t yy = rem / R.ex, xx = rem % R.ex;
-                const T v = vol[((R.oz + z) * NY + (R.oy + yy)) * NX + R.ox + xx];
-                bool esc;
-                quantize(Q, (double)v, esc);
-                if (esc) byte |= (uint8_t)(1u << k);
-            }
-            out[R.payload_off + b] = byte;
+            uint8_t v = src[b];
+            if (b == nbytes - 1 && (R.n & 7)) v &= (uint8_t)((1u << (R.n & 7)) - 1u);
+            out[R.payload_off + b] = v;
         }
     }
 }
@@ -863,7 +835,7 @@ __global__ void k_finalize_file(const CrcTables *__restrict__ tabs, const EncSca
 // ------------------------------------------------------------------ host
 struct EncPlan {
     std::vector<RegDev> regs;
-    int64_t nitems = 0, npieces_total = 0, nchunks = 0, qtotal = 0;
+    int64_t nitems = 0, npieces_total = 0, nchunks = 0, qtotal = 0, etotal = 0;
     size_t ws_bytes = 0;
     // carved pointers
     EncParams *params;
@@ -876,7 +848,7 @@ struct EncPlan {
     int32_t *codec2;
     EncScalars *scal;
     int32_t *item_reg, *chunk_reg;
-    uint32_t *qz;
+    uint32_t *qz, *escbits;
 };
 
 static bool build_plan(const chr_region_t *h, int64_t nreg, EncPlan &pl) {
@@ -902,13 +874,15 @@ static bool build_plan(const chr_region_t *h, int64_t nreg, EncPlan &pl) {
         R.item_base = item;
         item += (int64_t)R.ntx * R.nty * R.nzc;
         R.piece_base = piece;
-        R.npieces = (int64_t)R.ntx * R.ey * R.ez;
+        R.npieces = ceil_div(R.n, TX);  // 64-sample pieces of the raster stream
         R.chunk_base = chunk;
         R.nchunks = ceil_div(R.npieces, CH);
         chunk += R.nchunks;
         piece += R.nchunks * CH;
         R.q_base = pl.qtotal;
         pl.qtotal += R.n;
+        R.ebase = pl.etotal;
+        pl.etotal += ceil_div(R.n, 32) + 1;
         R.mask = h[r].mask;
         for (int a = 0; a < 3; ++a) {
             R.lo[a] = h[r].lo[a];
@@ -935,6 +909,7 @@ static void carve(EncPlan &pl, void *base, size_t cap) {
     pl.item_reg = c.take<int32_t>(pl.nitems + 1);
     pl.chunk_reg = c.take<int32_t>(pl.nchunks + 1);
     pl.qz = c.take<uint32_t>(pl.qtotal + 1);
+    pl.escbits = c.take<uint32_t>(pl.etotal + 2);
     pl.scal = c.take<EncScalars>(1);
     pl.ws_bytes = c.off + 256;
 }
@@ -1009,24 +984,26 @@ extern "C" int chr_compress(const void *d_vol, int dtype, int src_dtype, int64_t
                                  cudaMemcpyHostToDevice, st));
     CHR_CUDA_TRY(cudaMemsetAsync(pl.scal, 0, sizeof(EncScalars), st));
     CHR_CUDA_TRY(cudaMemsetAsync(pl.seg_raw, 0, sizeof(uint32_t) * (nreg + 1), st));
+    CHR_CUDA_TRY(cudaMemsetAsync(pl.escbits, 0, sizeof(uint32_t) * (pl.etotal + 2), st));
 
     const unsigned items = (unsigned)pl.nitems, chunks = (unsigned)pl.nchunks;
     {
         CHR_PROF("k_tile_fill_map", st);
         k_tile_fill_map<<<(unsigned)nreg, 256, 0, st>>>(pl.d_regs, nreg, pl.item_reg, pl.chunk_reg);
     }
-    if (dtype == CHR_F32)
-        {
-            CHR_PROF("k_tile<float, false>", st);
-            k_tile<float, false><<<items, NW * 32, 0, st>>>((const float *)d_vol, pl.params, pl.d_regs, pl.item_reg,
-                                                            pl.recs, pl.poffs, pl.qz, d_out);
-        }
-    else
-        {
-            CHR_PROF("k_tile<double, false>", st);
-            k_tile<double, false><<<items, NW * 32, 0, st>>>((const double *)d_vol, pl.params, pl.d_regs, pl.item_reg,
-                                                             pl.recs, pl.poffs, pl.qz, d_out);
-        }
+    if (dtype == CHR_F32) {
+        CHR_PROF("k_quant<float>", st);
+        k_quant<float><<<items, NW * 32, 0, st>>>((const float *)d_vol, pl.params, pl.d_regs, pl.item_reg, pl.qz,
+                                                  pl.escbits);
+    } else {
+        CHR_PROF("k_quant<double>", st);
+        k_quant<double><<<items, NW * 32, 0, st>>>((const double *)d_vol, pl.params, pl.d_regs, pl.item_reg, pl.qz,
+                                                   pl.escbits);
+    }
+    {
+        CHR_PROF("k_summarize", st);
+        k_summarize<<<chunks, 256, 0, st>>>(pl.d_regs, pl.chunk_reg, pl.qz, pl.escbits, pl.recs);
+    }
     {
         CHR_PROF("k_scan_reduce", st);
         k_scan_reduce<<<chunks, 256, 0, st>>>(pl.params, pl.d_regs, pl.recs, pl.chunk);
@@ -1048,23 +1025,21 @@ extern "C" int chr_compress(const void *d_vol, int dtype, int src_dtype, int64_t
         {
             CHR_PROF("k_emit_q<float>", st);
             k_emit_q<float><<<chunks, 256, 0, st>>>((const float *)d_vol, pl.params, pl.d_regs, pl.chunk_reg,
-                                                    pl.recs, pl.poffs, pl.qz, d_out);
+                                                    pl.recs, pl.poffs, pl.qz, pl.escbits, d_out);
         }
         {
-            CHR_PROF("k_bitmap<float>", st);
-            k_bitmap<float><<<148, 256, 0, st>>>((const float *)d_vol, pl.params, pl.d_regs, pl.codec2,
-                                                 pl.scal, d_out);
+            CHR_PROF("k_bitmap", st);
+            k_bitmap<<<148, 256, 0, st>>>(pl.d_regs, pl.codec2, pl.scal, pl.escbits, d_out);
         }
     } else {
         {
             CHR_PROF("k_emit_q<double>", st);
             k_emit_q<double><<<chunks, 256, 0, st>>>((const double *)d_vol, pl.params, pl.d_regs, pl.chunk_reg,
-                                                     pl.recs, pl.poffs, pl.qz, d_out);
+                                                     pl.recs, pl.poffs, pl.qz, pl.escbits, d_out);
         }
         {
-            CHR_PROF("k_bitmap<double>", st);
-            k_bitmap<double><<<148, 256, 0, st>>>((const double *)d_vol, pl.params, pl.d_regs, pl.codec2,
-                                                  pl.scal, d_out);
+            CHR_PROF("k_bitmap", st);
+            k_bitmap<<<148, 256, 0, st>>>(pl.d_regs, pl.codec2, pl.scal, pl.escbits, d_out);
         }
     }
     if (write_file)
