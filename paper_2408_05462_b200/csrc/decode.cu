@@ -814,12 +814,14 @@ __global__ void __launch_bounds__(DTHREADS) k_seg_locate(const DecReg *__restric
                                                          const int64_t *__restrict__ chunk_start,
                                                          const int64_t *__restrict__ thr_cnt,
                                                          int64_t *__restrict__ sp_byte,
-                                                         int64_t *__restrict__ sp_skip) {
+                                                         int64_t *__restrict__ sp_skip,
+                                                         int64_t *__restrict__ pos64) {
     const int64_t c = blockIdx.x;
     const DecReg &R = regs[chunk_reg[c]];
     if (!((R.codec == 1 || R.codec == 2) && R.err == 0 && !R.slow)) return;
     const int64_t cnt = thr_cnt[c * DTHREADS + threadIdx.x];
     int64_t a = chunk_start[c] + block_excl64(cnt, nullptr);
+    pos64[c * DTHREADS + threadIdx.x] = a;  // first sample of the tokens ending in this 64-byte group
     if (cnt == 0) return;
     const int64_t ex = R.ex, plane = ex * R.ey, band = ex * R.bty, nb = R.tny;
     int64_t z = a / plane, b = (a - z * plane + band - 1) / band;
@@ -906,8 +908,6 @@ __global__ void __launch_bounds__(256) k_esc_seg(const DecReg *__restrict__ regs
 constexpr int BCAP = 6144;   // samples per tile
 constexpr int BDF = 2048;    // dF entries (btz * ex) when a tile has a band above
 constexpr int BSEGM = 64;    // planes per tile
-constexpr int BUMAX = 2176;  // 16-byte units per tile (5 B/sample + per-plane slack), >= BDF
-constexpr int BUPT = (BUMAX + 255) / 256;
 
 __device__ __forceinline__ int seg_of(const int32_t *base, int nseg, int g) {
     int lo = 0, hi = nseg - 1;
@@ -981,8 +981,8 @@ __device__ __forceinline__ int64_t win24_count(const Win24 &W) {
 // own positions: H holds the LEB128 payload of bytes e-4..e, so the token
 // ending at e has value H >> 7 (5 - len).
 template <bool PAD>
-__device__ __forceinline__ void band_scatter_unit(const Win24 &W, int64_t at64, int L, int ex, uint64_t M,
-                                                  int64_t *__restrict__ q) {
+__device__ __forceinline__ int64_t band_scatter_unit64(const Win24 &W, int64_t at64, int L, int ex, uint64_t M,
+                                                     int64_t *__restrict__ q) {
     int64_t at = at64;
     int idx = (int)at, x = 0;
     if (PAD && at >= 0) {
@@ -1020,17 +1020,79 @@ __device__ __forceinline__ void band_scatter_unit(const Win24 &W, int64_t at64, 
             }
         }
     }
+    return at;
+}
+
+// 32-bit fast path of band_scatter_unit64: tokens <= 4 bytes (H = payload of
+// bytes e-3..e in 28 bits), positions in int32 (runs clamped to 2^31 - 1:
+// every position that matters is < L <= BCAP and a segment starts at
+// -skip >= -2^30).  Returns the position after the unit's tokens.
+template <bool PAD>
+__device__ __forceinline__ int band_scatter_unit32(const Win24 &W, int at, int L, int ex, uint64_t M,
+                                                   int64_t *__restrict__ q) {
+    int idx = at, x = 0;
+    if (PAD && at >= 0) {
+        const int row = (int)(((uint64_t)at * M) >> 32);
+        x = at - row * ex;
+        idx = row * (ex + 1) + x;
+    }
+    uint32_t H = 0;
+#pragma unroll
+    for (int j = 4; j < 8; ++j) H = (H >> 7) | ((win_byte(W, j) & 0x7Fu) << 21);
+#pragma unroll
+    for (int e = 8; e < 24; ++e) {
+        H = (H >> 7) | ((win_byte(W, e) & 0x7Fu) << 21);
+        const bool lit = (W.lit >> e) & 1u, run = (W.len >> e) & 1u;
+        if (!(lit | run)) continue;
+        const uint32_t below = W.E & ((1u << e) - 1u);
+        const int len = e - (32 - __clz(below)) + 1;
+        const uint32_t v = H >> (7 * (4 - len));
+        if (lit) {
+            const uint32_t zz = v - 1u;
+            if ((unsigned)at < (unsigned)L) q[idx] = (int64_t)(int32_t)((zz >> 1) ^ (0u - (zz & 1u)));
+            ++at;
+            ++idx;
+            if (PAD && ++x == ex) {
+                x = 0;
+                ++idx;
+            }
+        } else {
+            at = (int)min((int64_t)at + (int64_t)v, (int64_t)0x7FFFFFFF);
+            idx = min(at, L);
+            if (PAD && at >= 0 && at < L) {
+                const int row = (int)(((uint64_t)at * M) >> 32);
+                x = at - row * ex;
+                idx = row * (ex + 1) + x;
+            }
+        }
+    }
+    return at;
+}
+
+// a unit: 32-bit path unless a 5-byte token ends in it (any lane of the warp)
+// or the position is out of int32 range
+template <bool PAD>
+__device__ __forceinline__ int64_t band_scatter_unit(const Win24 &W, int64_t at, int L, int ex, uint64_t M,
+                                                     int64_t *__restrict__ q, bool active) {
+    const uint32_t C = ~W.E & 0xFFFFFFu;
+    const bool long5 = active && ((C << 1) & (C << 2) & (C << 3) & (C << 4) & (W.lit | W.len)) != 0;
+    const bool wide = active && (long5 || at < -(1ll << 30));
+    if (__any_sync(0xFFFFFFFFu, wide)) {
+        return active ? band_scatter_unit64<PAD>(W, at, L, ex, M, q) : at;
+    }
+    return active ? (int64_t)band_scatter_unit32<PAD>(W, (int)at, L, ex, M, q) : at;
 }
 
 __global__ void __launch_bounds__(256) k_band(const DecReg *__restrict__ regs, const int32_t *__restrict__ tile_reg,
                                               const uint8_t *__restrict__ blob,
                                               const int64_t *__restrict__ sp_byte,
                                               const int64_t *__restrict__ sp_skip,
-                                              const int64_t *__restrict__ esc_sp, int64_t *__restrict__ faces,
+                                              const int64_t *__restrict__ esc_sp, const int64_t *__restrict__ pos64,
+                                              int64_t *__restrict__ faces,
                                               int32_t *__restrict__ tflag, unsigned long long *__restrict__ ticket,
                                               const int32_t *__restrict__ order, double *__restrict__ out) {
     extern __shared__ __align__(16) int64_t Q[];  // [nzv][nyv][rs]
-    __shared__ int64_t ucnt[BUMAX];               // unit sample offsets; later dF[nzv][ex]
+    __shared__ int64_t ucnt[BDF];                 // dF[nzv][ex]
     __shared__ int64_t s_lo[BSEGM], s_hi[BSEGM], s_ub[BSEGM], s_off[BSEGM];
     __shared__ int32_t s_base[BSEGM + 1];
     __shared__ int64_t s_tile;
@@ -1051,9 +1113,12 @@ __global__ void __launch_bounds__(256) k_band(const DecReg *__restrict__ regs, c
     const int64_t sp_end = R.sp_base + (int64_t)R.ez * nb;
 
     for (int i = tid; i < nzv * PL; i += 256) Q[i] = 0;
-    // ---- segments (one per plane) and their 16-byte units
+    // ---- segments (one per plane) and the 64-byte token groups they cover.
+    //      Group g (bytes [G, G+64) from the chunk origin) has its first sample
+    //      in pos64 (k_seg_locate), so a thread walks one group without a count
+    //      pass; the group holding the segment's first byte starts at -skip.
     if (warp == 0) {
-        int nun[2] = {0, 0};
+        int ng[2] = {0, 0};
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const int j = lane + 32 * h;
@@ -1061,69 +1126,59 @@ __global__ void __launch_bounds__(256) k_band(const DecReg *__restrict__ regs, c
                 const int64_t k = R.sp_base + (int64_t)(z0 + j) * nb + b;
                 const int64_t b0 = sp_byte[k];
                 const int64_t b1 = k + 1 < sp_end ? min(hi, sp_byte[k + 1] + 11) : hi;
-                const int64_t ub = R.abase + ((b0 - R.abase) & ~15ll);
+                const int64_t g0 = (b0 - R.abase) >> 6, g1 = (b1 - 1 - R.abase) >> 6;
                 s_lo[j] = b0;
                 s_hi[j] = b1;
-                s_ub[j] = ub;
+                s_ub[j] = g0;
                 s_off[j] = sp_skip[k];
-                nun[h] = (int)((b1 - ub + 15) >> 4);
+                ng[h] = (int)(g1 - g0 + 1);
             }
         }
-        int i0 = nun[0];  // lane owns j = lane and lane + 32: scan in two halves
+        int i0 = ng[0];  // lane owns j = lane and lane + 32: scan in two halves
 #pragma unroll
         for (int off = 1; off < 32; off <<= 1) {
             const int o = __shfl_up_sync(0xFFFFFFFFu, i0, off);
             if (lane >= off) i0 += o;
         }
         const int tot0 = __shfl_sync(0xFFFFFFFFu, i0, 31);
-        int i1 = nun[1];
+        int i1 = ng[1];
 #pragma unroll
         for (int off = 1; off < 32; off <<= 1) {
             const int o = __shfl_up_sync(0xFFFFFFFFu, i1, off);
             if (lane >= off) i1 += o;
         }
         const int tot1 = __shfl_sync(0xFFFFFFFFu, i1, 31);
-        if (lane < nzv) s_base[lane] = i0 - nun[0];
-        if (lane + 32 < nzv) s_base[lane + 32] = tot0 + i1 - nun[1];
+        if (lane < nzv) s_base[lane] = i0 - ng[0];
+        if (lane + 32 < nzv) s_base[lane + 32] = tot0 + i1 - ng[1];
         if (lane == 0) s_base[nzv] = tot0 + tot1;
     }
     __syncthreads();
-    const int U = min(s_base[nzv], BUMAX);  // bounded for canonical streams (checked on the host side)
-    // ---- pass 1: samples per unit
-    for (int g = tid; g < U; g += 256) {
-        const int j = seg_of(s_base, nzv, g);
-        const int64_t u0 = s_ub[j] + 16 * (int64_t)(g - s_base[j]);
-        ucnt[g] = win24_count(win24(blob, u0, s_lo[j], s_hi[j]));
-    }
-    __syncthreads();
-    {  // exclusive scan over all units (thread t owns units [t*BUPT, t*BUPT + BUPT))
-        const int g0 = tid * BUPT;
-        int64_t sum = 0;
-#pragma unroll
-        for (int i = 0; i < BUPT; ++i)
-            if (g0 + i < U) sum += ucnt[g0 + i];
-        int64_t run = block_excl64(sum, nullptr);
-#pragma unroll
-        for (int i = 0; i < BUPT; ++i)
-            if (g0 + i < U) {
-                const int64_t t = ucnt[g0 + i];
-                ucnt[g0 + i] = run;
-                run += t;
-            }
-    }
-    __syncthreads();
-    if (tid < nzv) s_off[tid] = (s_base[tid] < U ? ucnt[s_base[tid]] : 0) + s_off[tid];  // base + skip
-    __syncthreads();
-    // ---- pass 2: scatter the literals of every unit into its plane
+    const int U = s_base[nzv];
     const uint64_t M = ((1ull << 32) + (uint64_t)ex - 1) / (uint64_t)ex;  // row = (at * M) >> 32
-    for (int g = tid; g < U; g += 256) {
-        const int j = seg_of(s_base, nzv, g);
-        const int64_t at = ucnt[g] - s_off[j];
-        if (at >= L) continue;
-        const int64_t u0 = s_ub[j] + 16 * (int64_t)(g - s_base[j]);
-        const Win24 W = win24(blob, u0, s_lo[j], s_hi[j]);
-        if (rs == ex) band_scatter_unit<false>(W, at, L, ex, M, Q + j * PL);
-        else band_scatter_unit<true>(W, at, L, ex, M, Q + j * PL);
+    const int64_t gbase = R.chunk_base * DTHREADS;  // pos64 index of the region's first group
+    for (int g0 = warp * 32; g0 < U; g0 += 256) {  // warp-uniform bounds (the unit walk votes)
+        const int gi = g0 + lane;
+        const bool own = gi < U;
+        int j = 0;
+        int64_t G = 0, at = L;
+        if (own) {
+            j = seg_of(s_base, nzv, gi);
+            const int64_t grp = s_ub[j] + (gi - s_base[j]);
+            G = R.abase + grp * 64;
+            const int64_t segstart = ((int64_t)(z0 + j) * ey + y0) * ex;
+            at = G <= s_lo[j] ? -s_off[j] : __ldg(pos64 + gbase + grp) - segstart;
+        }
+        int64_t *q = Q + j * PL;
+#pragma unroll 1
+        for (int u = 0; u < 4; ++u) {
+            const int64_t u0 = G + 16 * u;
+            const bool act = own && at < L && u0 + 16 > s_lo[j] && u0 < s_hi[j];
+            if (!__any_sync(0xFFFFFFFFu, act)) continue;
+            Win24 W;
+            if (act) W = win24(blob, u0, s_lo[j], s_hi[j]);
+            at = rs == ex ? band_scatter_unit<false>(W, at, L, ex, M, q, act)
+                          : band_scatter_unit<true>(W, at, L, ex, M, q, act);
+        }
     }
     __syncthreads();
     // ---- x-prefix (rows are whole)
@@ -1193,8 +1248,10 @@ __global__ void __launch_bounds__(256) k_band(const DecReg *__restrict__ regs, c
     int64_t *dF = ucnt;  // [nzv][ex], <= BDF entries
     int64_t *myF = faces + R.face_base + local * fn;
     if (b > 0) {
+#ifndef CHR_BAND_NOWAIT
         if (tid == 0)
             while (ld_acquire32(tflag + tile - 1) != 2) __nanosleep(20);
+#endif
         __syncthreads();
         const int64_t *Fy = faces + R.face_base + (local - 1) * fn;
         for (int t = tid; t < ex * nzv; t += 256) dF[t] = __ldcg(Fy + ex + t) - __ldcg(Fy + (t - (t / ex) * ex));
@@ -1240,8 +1297,10 @@ __global__ void __launch_bounds__(256) k_band(const DecReg *__restrict__ regs, c
     };
     // ---- chunk before (same band): its inclusive faces give the carry Fz
     const int64_t *Ip = faces + R.face_base + (local - nb) * fn + io;
+#ifndef CHR_BAND_NOWAIT
     if (c > 0 && tid == 0)
         while (ld_acquire32(tflag + tile - nb) != 2) __nanosleep(20);
+#endif
     __syncthreads();
     constexpr int FU = 4;  // columns per thread per round: all face loads first
     for (int t0 = tid; t0 < L; t0 += 256 * FU) {
@@ -1295,7 +1354,7 @@ struct DecPlan {
     CrcSeg *segs;
     uint32_t *seg_raw;
     int64_t *chunk_samples, *seg_byte, *seg_skip, *esc_base, *carry, *flags;
-    int64_t *sp_byte, *sp_skip, *esc_sp, *thr_cnt;
+    int64_t *sp_byte, *sp_skip, *esc_sp, *thr_cnt, *pos64;
     int64_t *faces;
     int32_t *tflag, *chunk_reg, *tile_reg, *order;
     int64_t *pair_base;
@@ -1451,6 +1510,7 @@ static void dec_carve(DecPlan &pl, void *base, size_t cap) {
     pl.sp_skip = c.take<int64_t>(pl.nsp + 1);
     pl.esc_sp = c.take<int64_t>(pl.nsp + 1);
     pl.thr_cnt = c.take<int64_t>(pl.nchunks * DTHREADS + 1);
+    pl.pos64 = c.take<int64_t>(pl.nchunks * DTHREADS + 1);
     pl.faces = c.take<int64_t>(pl.nface + 1);
     pl.tflag = c.take<int32_t>(pl.ntiles + 1);
     pl.chunk_reg = c.take<int32_t>(pl.nchunks + 1);
@@ -1529,7 +1589,7 @@ extern "C" int chr_decode_regions(const uint8_t *d_blob, const chr_dec_region_t 
             CHR_PROF("k_seg_locate", st);
             k_seg_locate<<<(unsigned)pl.nchunks, DTHREADS, 0, st>>>(pl.d_regs, pl.chunk_reg, d_blob,
                                                                     pl.chunk_samples, pl.thr_cnt, pl.sp_byte,
-                                                                    pl.sp_skip);
+                                                                    pl.sp_skip, pl.pos64);
         }
         {
             CHR_PROF("k_esc_seg", st);
@@ -1547,8 +1607,8 @@ extern "C" int chr_decode_regions(const uint8_t *d_blob, const chr_dec_region_t 
         {
             CHR_PROF("k_band", st);
             k_band<<<(unsigned)pl.ntiles, 256, smem, st>>>(pl.d_regs, pl.tile_reg, d_blob, pl.sp_byte, pl.sp_skip,
-                                                           pl.esc_sp, pl.faces, pl.tflag, pl.ticket3, pl.order,
-                                                           d_out);
+                                                           pl.esc_sp, pl.pos64, pl.faces, pl.tflag, pl.ticket3,
+                                                           pl.order, d_out);
         }
     }
     // ---- generic path (non-canonical streams, rows wider than a band tile):
