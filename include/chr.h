@@ -193,6 +193,14 @@ int chr_min_abs_distance(const double *d_flat, int64_t n, double k, double *h_ou
                          void *d_workspace, size_t workspace_bytes, void *stream);
 int chr_lorenzo_encode(const double *d_flat, int64_t nx, int64_t ny, int64_t nz, double e,
                        int64_t *d_q, uint8_t *d_escaped, void *stream);
+/* rle_varint_encode (kernels.py:198-296, signature kernels.py:292-296):
+ * quanta |q| <= 2^30 -> LEB128 token stream (zero runs >= 2 packed),
+ * *h_nbytes receives its length; out_cap >= 5n + 16.  Synchronises.
+ * (rle_varint_decode and lorenzo_decode are served by chr_decode_regions
+ * on a codec-1 stream, see the Python shims.) */
+size_t chr_rle_encode_workspace_size(int64_t n);
+int chr_rle_encode(const int64_t *d_q, int64_t n, uint8_t *d_out, uint64_t out_cap, void *d_workspace,
+                   size_t workspace_bytes, uint64_t *h_nbytes, void *stream);
 
 /* 9. instrumentation: launch counter and opt-in per-kernel CUDA-event
  *    timing on the launching stream ("name count total_ms" lines). */

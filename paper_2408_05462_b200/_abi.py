@@ -161,6 +161,10 @@ def lib():
         L.chr_min_abs_distance.restype = INT
         L.chr_lorenzo_encode.argtypes = [P, I64, I64, I64, D, P, P, P]
         L.chr_lorenzo_encode.restype = INT
+        L.chr_rle_encode_workspace_size.argtypes = [I64]
+        L.chr_rle_encode_workspace_size.restype = SZ
+        L.chr_rle_encode.argtypes = [P, I64, P, U64, P, SZ, P, P]
+        L.chr_rle_encode.restype = INT
         L.chr_prof_enable.argtypes = [INT]
         L.chr_prof_enable.restype = None
         L.chr_launch_count.argtypes = []
@@ -172,6 +176,7 @@ def lib():
 
 
 EXPORTS = [
+    "chr_rle_encode_workspace_size", "chr_rle_encode",
     "chr_abi_version", "chr_status_string", "chr_num_blocks", "chr_stats", "chr_plan",
     "chr_compress_workspace_size", "chr_compress_capacity", "chr_compress",
     "chr_decode_workspace_size", "chr_decode_regions", "chr_mc_workspace_size", "chr_mc_count",

@@ -1081,3 +1081,106 @@ extern "C" int chr_compress(const void *d_vol, int dtype, int src_dtype, int64_t
     *h_out_nbytes = hs.out_nbytes;
     return CHR_OK;
 }
+
+// ------------------------------------------------------------------ token-stream seam
+// rle_varint_encode (kernels.py:198-296) on a device int64 array: the same
+// summarize -> scan -> emit kernels as the archive path, on one "region"
+// of n samples whose token values come from the caller's quanta.
+namespace chr {
+__global__ void k_q_to_tokens(const int64_t *__restrict__ q, int64_t n, uint32_t *__restrict__ qz,
+                              int32_t *__restrict__ bad) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = q[i];
+        if (v > (1ll << 30) || v < -(1ll << 30)) {  // |q| <= 2^30
+            atomicOr(bad, 1);
+            continue;
+        }
+        qz[i] = zz1_32((int32_t)v);
+    }
+}
+__global__ void k_force_tokens(RegDev *__restrict__ R) {
+    R->codec = 1;
+    R->payload_off = 0;
+    R->tok_start = 0;
+    R->payload_len = R->tok_len;
+}
+}  // namespace chr
+
+static chr_region_t rle_region(int64_t n) {
+    chr_region_t h;
+    std::memset(&h, 0, sizeof(h));
+    h.extent[0] = (int32_t)n;
+    h.extent[1] = 1;
+    h.extent[2] = 1;
+    h.error_bound = 1.0;
+    return h;
+}
+
+extern "C" size_t chr_rle_encode_workspace_size(int64_t n) {
+    if (n < 1 || n > INT32_MAX) return 256;
+    const chr_region_t h = rle_region(n);
+    EncPlan pl;
+    if (!build_plan(&h, 1, pl)) return 256;
+    carve(pl, nullptr, ~size_t(0));
+    return pl.ws_bytes + 256;
+}
+
+extern "C" int chr_rle_encode(const int64_t *d_q, int64_t n, uint8_t *d_out, uint64_t out_cap, void *d_ws,
+                              size_t ws_bytes, uint64_t *h_nbytes, void *stream) {
+    if (!h_nbytes) return CHR_E_PARAMETER;
+    if (n == 0) {
+        *h_nbytes = 0;
+        return CHR_OK;
+    }
+    if (!d_q || !d_out || n < 0 || n > INT32_MAX) return CHR_E_PARAMETER;
+    if (out_cap < 5ull * (uint64_t)n + 16) return CHR_E_PARAMETER;
+    cudaStream_t st = (cudaStream_t)stream;
+    const chr_region_t h = rle_region(n);
+    EncPlan pl;
+    if (!build_plan(&h, 1, pl)) return CHR_E_PARAMETER;
+    carve(pl, d_ws, ws_bytes);
+    if (!d_ws || pl.ws_bytes + 256 > ws_bytes) return CHR_E_WORKSPACE;
+    int32_t *d_bad = reinterpret_cast<int32_t *>(reinterpret_cast<char *>(d_ws) + pl.ws_bytes);
+    EncParams hp;
+    std::memset(&hp, 0, sizeof(hp));
+    hp.NX = n;
+    hp.NY = 1;
+    hp.NZ = 1;
+    hp.nreg = 1;
+    hp.nitems = pl.nitems;
+    hp.nchunks = pl.nchunks;
+    hp.dtype = CHR_F64;
+    hp.src_dtype = CHR_F64;
+    CHR_CUDA_TRY(cudaMemcpyAsync(pl.params, &hp, sizeof(hp), cudaMemcpyHostToDevice, st));
+    CHR_CUDA_TRY(cudaMemcpyAsync(pl.d_regs, pl.regs.data(), sizeof(RegDev), cudaMemcpyHostToDevice, st));
+    CHR_CUDA_TRY(cudaMemsetAsync(pl.scal, 0, sizeof(EncScalars), st));
+    CHR_CUDA_TRY(cudaMemsetAsync(pl.escbits, 0, sizeof(uint32_t) * (pl.etotal + 2), st));
+    CHR_CUDA_TRY(cudaMemsetAsync(d_bad, 0, sizeof(int32_t), st));
+    const unsigned chunks = (unsigned)pl.nchunks;
+    k_tile_fill_map<<<1, 256, 0, st>>>(pl.d_regs, 1, pl.item_reg, pl.chunk_reg);
+    {
+        CHR_PROF("k_q_to_tokens", st);
+        k_q_to_tokens<<<(unsigned)std::min<int64_t>(ceil_div(n, 256), 148 * 16), 256, 0, st>>>(d_q, n, pl.qz, d_bad);
+    }
+    {
+        CHR_PROF("k_summarize", st);
+        k_summarize<<<chunks, 256, 0, st>>>(pl.d_regs, pl.chunk_reg, pl.qz, pl.escbits, pl.recs);
+    }
+    k_scan_reduce<<<chunks, 256, 0, st>>>(pl.params, pl.d_regs, pl.recs, pl.chunk);
+    k_scan_regions<<<1, 128, 0, st>>>(pl.params, pl.d_regs, pl.chunk, pl.codec2, pl.scal);
+    k_force_tokens<<<1, 1, 0, st>>>(pl.d_regs);
+    k_scan_down<<<chunks, 256, 0, st>>>(pl.params, pl.d_regs, pl.recs, pl.chunk, pl.poffs);
+    {
+        CHR_PROF("k_emit_q<double>", st);
+        k_emit_q<double><<<chunks, 256, 0, st>>>(nullptr, pl.params, pl.d_regs, pl.chunk_reg, pl.recs, pl.poffs,
+                                                 pl.qz, pl.escbits, d_out);
+    }
+    CHR_CUDA_TRY(cudaGetLastError());
+    int32_t bad = 0;
+    CHR_CUDA_TRY(cudaMemcpyAsync(&bad, d_bad, sizeof(bad), cudaMemcpyDeviceToHost, st));
+    CHR_CUDA_TRY(cudaMemcpyAsync(pl.regs.data(), pl.d_regs, sizeof(RegDev), cudaMemcpyDeviceToHost, st));
+    CHR_CUDA_TRY(cudaStreamSynchronize(st));
+    if (bad) return CHR_E_PARAMETER;
+    *h_nbytes = (uint64_t)pl.regs[0].tok_len;
+    return CHR_OK;
+}

@@ -307,6 +307,61 @@ def lorenzo_encode(flat: torch.Tensor, nx, ny, nz, e):
     return q, esc
 
 
+def rle_varint_encode(q: torch.Tensor) -> torch.Tensor:
+    """kernels.rle_varint_encode (kernels.py:292-296): int64 quanta -> uint8
+    token stream on the device (|q| <= 2^30, as every valid stream)."""
+    q = q.to(device=_abi.device(), dtype=torch.int64).contiguous()
+    n = q.numel()
+    L = lib()
+    out = torch.empty(5 * n + 16, dtype=torch.uint8, device=q.device)
+    work = _DEFAULT_WS.get("rle", L.chr_rle_encode_workspace_size(n))
+    nb = ctypes.c_uint64(0)
+    check(L.chr_rle_encode(ptr(q), n, ptr(out), out.numel(), ptr(work), work.numel(), ctypes.byref(nb), stream_ptr()),
+          "chr_rle_encode")
+    return out[: nb.value]
+
+
+def rle_varint_decode(buf: torch.Tensor, n: int) -> torch.Tensor:
+    """kernels.rle_varint_decode (kernels.py:407-411): token stream -> int64
+    quanta.  Decoded as a codec-1 stream of a (1,n,1) window with e = 1/2,
+    whose reconstruction is the 1-D prefix u of q (exact in f64 for |u| < 2^53);
+    q = diff(u).  Malformed streams raise ValueError with the reference's
+    reasons (truncated, varint too long, missing/invalid run, trailing, count)."""
+    buf = buf.to(device=_abi.device(), dtype=torch.uint8).contiguous()
+    if n == 0:
+        if buf.numel():
+            raise ValueError("trailing bytes after the last token")
+        return torch.zeros(0, dtype=torch.int64, device=buf.device)
+    staging = torch.zeros(buf.numel() + 16, dtype=torch.uint8, device=buf.device)
+    staging[: buf.numel()] = buf
+    crc = crc32(staging, buf.numel()) if buf.numel() else 0
+    u, _, status = decode(staging, [(0, buf.numel(), 1, (1, n, 1), 0.5, crc)])  # 1-D prefix along y
+    if status[0]:
+        raise ValueError(_abi.DEC_MESSAGES.get(int(status[0]), "corrupt token stream"))
+    u = u[:n].to(torch.int64)
+    return torch.diff(u, prepend=torch.zeros(1, dtype=torch.int64, device=u.device))
+
+
+def lorenzo_decode(q: torch.Tensor, escaped: torch.Tensor, escape_values: torch.Tensor, e: float, nx, ny, nz):
+    """kernels.lorenzo_decode (kernels.py:182-186): u = 3D inclusive prefix of
+    q, recon = u * 2e, escapes overwritten in raster order.  Runs the archive
+    decoder on the device: q -> token stream (rle_varint_encode) -> codec-1
+    block of dims (nx, ny, nz)."""
+    n = nx * ny * nz
+    tok = rle_varint_encode(q)
+    staging = torch.zeros(tok.numel() + 16, dtype=torch.uint8, device=tok.device)
+    staging[: tok.numel()] = tok
+    crc = crc32(staging, tok.numel()) if tok.numel() else 0
+    recon, _, status = decode(staging, [(0, tok.numel(), 1, (nx, ny, nz), float(e), crc)])
+    if status[0]:
+        raise ValueError(_abi.DEC_MESSAGES.get(int(status[0]), "corrupt token stream"))
+    recon = recon[:n].clone()
+    esc = escaped.to(device=recon.device).reshape(-1).bool()
+    if esc.any():
+        recon[esc] = escape_values.to(device=recon.device, dtype=torch.float64).reshape(-1)
+    return recon
+
+
 def region_records(regions) -> list[dict]:
     """Plain-Python view of a chr_region_t table."""
     regions = np.asarray(regions)

@@ -322,3 +322,55 @@ def test_decode_escapes_in_band_tiles(shape):
     assert blk.codec_id == 2
     ref = O.decompress_block(blk.to_bytes())[1]
     assert np.array_equal(G.decompress(blk).ravel(order="F"), ref)
+
+
+@pytest.mark.parametrize("n,kind", [(1, "zeros"), (5, "zeros"), (300, "mixed"), (100000, "mixed"), (64, "ones"),
+                                    (777, "wide"), (4096, "runs")])
+def test_kernel_seam_rle_round_trip(n, kind):
+    """rle_varint_encode / rle_varint_decode shims (kernels.py:292-296,
+    407-411) against the oracle's restatement, byte for byte."""
+    import torch
+
+    rng = np.random.default_rng(n)
+    if kind == "zeros":
+        q = np.zeros(n, dtype=np.int64)
+    elif kind == "ones":
+        q = np.ones(n, dtype=np.int64)
+    elif kind == "wide":
+        q = rng.integers(-(1 << 30), (1 << 30) + 1, size=n).astype(np.int64)
+    elif kind == "runs":
+        q = np.where(rng.random(n) < 0.9, 0, rng.integers(-50, 50, size=n)).astype(np.int64)
+    else:
+        q = np.where(rng.random(n) < 0.4, 0, rng.integers(-70000, 70000, size=n)).astype(np.int64)
+    want = O.rle_encode(q)
+    got = device.rle_varint_encode(torch.from_numpy(q)).cpu().numpy()
+    assert bytes(got) == bytes(want)
+    back = device.rle_varint_decode(torch.from_numpy(np.frombuffer(bytes(want), dtype=np.uint8).copy()), n)
+    assert np.array_equal(back.cpu().numpy(), q)
+
+
+def test_kernel_seam_rle_decode_errors():
+    import torch
+
+    good = O.rle_encode(np.array([0, 0, 0, 5, -3], dtype=np.int64))
+    with pytest.raises(ValueError):  # truncated varint
+        device.rle_varint_decode(torch.tensor(list(good[:-1]) + [0x80], dtype=torch.uint8), 5)
+    with pytest.raises(ValueError):  # wrong count
+        device.rle_varint_decode(torch.tensor(list(good), dtype=torch.uint8), 6)
+    with pytest.raises(ValueError):  # missing run length
+        device.rle_varint_decode(torch.tensor([0x00], dtype=torch.uint8), 3)
+
+
+@pytest.mark.parametrize("dims", [(9, 7, 5), (33, 33, 40), (1, 1, 1)])
+def test_kernel_seam_lorenzo_decode(dims):
+    import torch
+
+    nx, ny, nz = dims
+    g = np.random.default_rng(sum(dims)).normal(size=dims).cumsum(axis=1).ravel(order="F")
+    e = 1e-2
+    q, esc = O.lorenzo_encode(g, nx, ny, nz, e)
+    escv = g[esc.astype(bool)]
+    want = O.lorenzo_decode(q, esc, escv, e, nx, ny, nz)
+    got = device.lorenzo_decode(torch.from_numpy(q), torch.from_numpy(esc.astype(np.uint8)),
+                                torch.from_numpy(escv), e, nx, ny, nz)
+    assert np.array_equal(got.cpu().numpy(), want)
