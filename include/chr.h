@@ -202,6 +202,42 @@ size_t chr_rle_encode_workspace_size(int64_t n);
 int chr_rle_encode(const int64_t *d_q, int64_t n, uint8_t *d_out, uint64_t out_cap, void *d_workspace,
                    size_t workspace_bytes, uint64_t *h_nbytes, void *stream);
 
+/* 10. z-slab multi-GPU protocol.  Rank r holds volume planes
+ *     [z_base, z_base + nz_local) (global z) and encodes planes [zs, ze) of
+ *     every window: its portion, a contiguous piece of the window's raster
+ *     stream.  Phase 1 (chr_dcompress_local) summarises each portion's
+ *     stream; after an allgather of the nreg summaries of every rank,
+ *     phase 2 (chr_dcompress_finish, h_all = [nranks][nreg]) writes this
+ *     rank's bytes at their final file offsets into a zeroed d_out and
+ *     returns h_raw[1 + r] = raw CRC (init 0, no final xor) of its share of
+ *     payload r.  Rank 0 then calls chr_dcompress_headers with the XOR of
+ *     every rank's h_raw to write the file header, region table, block
+ *     headers and trailer.  Slices of all ranks OR together into the file
+ *     that chr_compress writes on one GPU.  The workspace must persist
+ *     from phase 1 to phase 2. */
+typedef struct {              /* token-stream summary of a portion (a monoid) */
+    int64_t len;              /* samples */
+    int64_t lead, trail;      /* zero samples before the first / after the last nonzero */
+    int64_t bytes;            /* literal tokens + runs between them */
+    int64_t nesc;             /* escaped samples */
+    int32_t nz, f32ok;        /* any nonzero quantum; every sample f32-exact */
+} chr_portion_t;
+size_t chr_dcompress_workspace_size(const chr_region_t *h_regions, int64_t n_regions, int64_t z_base,
+                                    int64_t nz_local, int64_t zs, int64_t ze);
+int chr_dcompress_local(const void *d_vol, int dtype, int source_dtype, int64_t nx, int64_t ny, int64_t nz_local,
+                        int64_t z_base, int64_t zs, int64_t ze, const chr_region_t *h_regions, int64_t n_regions,
+                        void *d_workspace, size_t workspace_bytes, chr_portion_t *h_portions, void *stream);
+int chr_dcompress_finish(const void *d_vol, int dtype, int source_dtype, int64_t nx, int64_t ny, int64_t nz_local,
+                         int64_t z_base, int64_t zs, int64_t ze, const double *spacing, int64_t block_size,
+                         double vmin, double vmax, const double *h_cands, int m, chr_region_t *h_regions,
+                         int64_t n_regions, const chr_portion_t *h_all, int nranks, int rank, void *d_workspace,
+                         size_t workspace_bytes, uint8_t *d_out, uint64_t out_cap, uint32_t *h_raw,
+                         uint64_t *h_file_nbytes, void *stream);
+int chr_dcompress_headers(int64_t nx, int64_t ny, int64_t nz, int source_dtype, const double *spacing,
+                          int64_t block_size, double vmin, double vmax, const double *h_cands, int m,
+                          chr_region_t *h_regions, int64_t n_regions, const uint32_t *h_raw_all,
+                          void *d_workspace, size_t workspace_bytes, uint8_t *d_out, void *stream);
+
 /* 9. instrumentation: launch counter and opt-in per-kernel CUDA-event
  *    timing on the launching stream ("name count total_ms" lines). */
 void chr_prof_enable(int on);

@@ -97,6 +97,8 @@ class McGrid(ctypes.Structure):
 REGION_DT = np.dtype([("lo", "<i4", 3), ("hi", "<i4", 3), ("origin", "<i4", 3), ("extent", "<i4", 3),
                       ("mask", "<u8"), ("error_bound", "<f8"), ("codec_id", "<i4"), ("payload_crc", "<u4"),
                       ("block_offset", "<u8"), ("block_nbytes", "<u8"), ("n_escaped", "<u8")], align=True)
+PORTION_DT = np.dtype([("len", "<i8"), ("lead", "<i8"), ("trail", "<i8"), ("bytes", "<i8"), ("nesc", "<i8"),
+                       ("nz", "<i4"), ("f32ok", "<i4")])  # chr_portion_t
 DEC_DT = np.dtype([("payload_offset", "<u8"), ("payload_nbytes", "<u8"), ("codec_id", "<i4"), ("dims", "<i4", 3),
                    ("error_bound", "<f8"), ("crc", "<u4"), ("_pad", "<u4"), ("out_offset", "<u8")], align=True)
 MCGRID_DT = np.dtype([("grid_offset", "<u8"), ("dims", "<i4", 3), ("_pad", "<i4"), ("origin", "<f8", 3),
@@ -161,6 +163,15 @@ def lib():
         L.chr_min_abs_distance.restype = INT
         L.chr_lorenzo_encode.argtypes = [P, I64, I64, I64, D, P, P, P]
         L.chr_lorenzo_encode.restype = INT
+        L.chr_dcompress_workspace_size.argtypes = [P, I64, I64, I64, I64, I64]
+        L.chr_dcompress_workspace_size.restype = SZ
+        L.chr_dcompress_local.argtypes = [P, INT, INT, I64, I64, I64, I64, I64, I64, P, I64, P, SZ, P, P]
+        L.chr_dcompress_local.restype = INT
+        L.chr_dcompress_finish.argtypes = [P, INT, INT, I64, I64, I64, I64, I64, I64, P, I64, D, D, P, INT, P, I64,
+                                           P, INT, INT, P, SZ, P, U64, P, P, P]
+        L.chr_dcompress_finish.restype = INT
+        L.chr_dcompress_headers.argtypes = [I64, I64, I64, INT, P, I64, D, D, P, INT, P, I64, P, P, SZ, P, P]
+        L.chr_dcompress_headers.restype = INT
         L.chr_rle_encode_workspace_size.argtypes = [I64]
         L.chr_rle_encode_workspace_size.restype = SZ
         L.chr_rle_encode.argtypes = [P, I64, P, U64, P, SZ, P, P]
@@ -177,6 +188,7 @@ def lib():
 
 EXPORTS = [
     "chr_rle_encode_workspace_size", "chr_rle_encode",
+    "chr_dcompress_workspace_size", "chr_dcompress_local", "chr_dcompress_finish", "chr_dcompress_headers",
     "chr_abi_version", "chr_status_string", "chr_num_blocks", "chr_stats", "chr_plan",
     "chr_compress_workspace_size", "chr_compress_capacity", "chr_compress",
     "chr_decode_workspace_size", "chr_decode_regions", "chr_mc_workspace_size", "chr_mc_count",

@@ -49,6 +49,13 @@ struct RegDev {
     int64_t q_base;               // first token value of the region in the q buffer
     int64_t ebase;                // first escape-bit word of the region
     int32_t has_esc, f32bad;      // set by k_quant
+    // z-slab portions (multi-GPU): this record encodes window planes
+    // [oz_w, oz_w + ez) of a window of n_win samples, starting at window
+    // sample s_off; zhalo = plane -1 belongs to the window, last = the
+    // portion ends the window, pre = stream summary of the portions before.
+    int64_t s_off, n_win;
+    int32_t zhalo, last;
+    TokSeg pre;
     // results
     int32_t codec, f32ok;
     int64_t tok_len, nesc, payload_len;
@@ -63,6 +70,7 @@ struct EncParams {
     int64_t NX, NY, NZ;
     int64_t nreg, nitems, nchunks;
     int32_t dtype, src_dtype, write_file, m;
+    int32_t dist, pad_;       // dist: codec/length decided on the host from every rank's portions
     double spacing[3];
     double vmin, vmax;
     int64_t bs;
@@ -204,7 +212,7 @@ __global__ void __launch_bounds__(NW * 32, 4) k_quant(const T *__restrict__ vol,
         return false;
     };
     int32_t pA = 0, pB = 0, pH = 0;  // u at the previous plane
-    if (quant && z0 > 0) {
+    if (quant && (z0 > 0 || R.zhalo)) {  // u at the plane before (inside the window)
         const T *prow = row - plane;
         bool e0, e1, e2;
         quant3(okA ? __ldg(prow + xA) : (T)0, okB ? __ldg(prow + xB) : (T)0, okH ? __ldg(prow + xH) : (T)0, pA, pB,
@@ -358,7 +366,7 @@ __global__ void __launch_bounds__(256) k_emit_q(const T *__restrict__ vol, const
     const int codec = R.codec;
     const int64_t NX = P->NX, NY = P->NY;
     const int64_t exy = (int64_t)R.ex * R.ey;
-    auto vol_at = [&](int64_t s) {  // window raster index -> sample
+    auto vol_at = [&](int64_t s) {  // portion raster index -> sample
         const int64_t z = s / exy, r = s - z * exy;
         const int64_t y = r / R.ex, x = r - y * R.ex;
         return __ldg(vol + ((R.oz + z) * NY + (R.oy + y)) * NX + R.ox + x);
@@ -409,7 +417,7 @@ __global__ void __launch_bounds__(256) k_emit_q(const T *__restrict__ vol, const
             uint8_t *base = out + R.tok_start + po.tok_off;
             if (nzA) put_varint32(put_run(base + sA, runA), zA);
             if (nzB) put_varint32(put_run(base + sB, runB), zB);
-            if (lp == R.npieces - 1 && lane == 0) {  // the region's final zero run
+            if (R.last && lp == R.npieces - 1 && lane == 0) {  // the window's final zero run
                 const int lastp = mB ? 63 - __clz(mB) : (mA ? 31 - __clz(mA) : -1);
                 const int64_t fin = (mA | mB) ? vcount - 1 - lastp : po.carry + vcount;
                 put_run(base + totA + totB, fin);
@@ -421,7 +429,7 @@ __global__ void __launch_bounds__(256) k_emit_q(const T *__restrict__ vol, const
                 const uint32_t eAm = __funnelshift_r(wp[0], wp[1], sh), eBm = __funnelshift_r(wp[1], wp[2], sh);
                 const bool eA = lane < vcount && ((eAm >> lane) & 1u);
                 const bool eB = 32 + lane < vcount && ((eBm >> lane) & 1u);
-                const uint64_t vbase = R.payload_off + (uint64_t)((R.n + 7) >> 3);
+                const uint64_t vbase = R.payload_off + (uint64_t)((R.n_win + 7) >> 3);
                 if (eA) put_le(out + vbase + 8 * (po.esc_off + __popc(eAm & lt)), (double)vol_at(s0 + lane));
                 if (eB)
                     put_le(out + vbase + 8 * (po.esc_off + __popc(vcount >= 32 ? eAm : 0u) + __popc(eBm & lt)),
@@ -437,8 +445,8 @@ __global__ void __launch_bounds__(256) k_emit_q(const T *__restrict__ vol, const
                 const int i = lane + 32 * h;
                 if (i >= vcount) continue;
                 const T v = vol_at(s0 + i);
-                if (codec == 3) put_le(out + R.payload_off + 4 * (s0 + i), (float)v);
-                else put_le(out + R.payload_off + 8 * (s0 + i), (double)v);
+                if (codec == 3) put_le(out + R.payload_off + 4 * (R.s_off + s0 + i), (float)v);
+                else put_le(out + R.payload_off + 8 * (R.s_off + s0 + i), (double)v);
             }
         }
     }
@@ -517,7 +525,7 @@ __global__ void k_scan_regions(const EncParams *__restrict__ P, RegDev *__restri
     const int lane = threadIdx.x & 31;
     if (r >= P->nreg) return;
     RegDev &R = regs[r];
-    TokSeg acc = tokseg_identity();
+    TokSeg acc = P->dist ? R.pre : tokseg_identity();  // portions: the stream before this rank's part
     for (int64_t c0 = 0; c0 < R.nchunks; c0 += 32) {
         const int64_t c = R.chunk_base + c0 + lane;
         const bool ok = c0 + lane < R.nchunks;
@@ -541,7 +549,7 @@ __global__ void k_scan_regions(const EncParams *__restrict__ P, RegDev *__restri
         tot.f32ok = __shfl_sync(0xFFFFFFFFu, inc.f32ok, 31);
         acc = tokseg_combine(acc, tot);
     }
-    if (lane != 0) return;
+    if (lane != 0 || P->dist) return;
     const bool f32ok = P->dtype == CHR_F32 ? true : R.f32bad == 0;
     const bool vf32 = P->src_dtype == CHR_F32 && f32ok;
     const int64_t vlen = R.n * (vf32 ? 4 : 8);
@@ -624,7 +632,7 @@ __global__ void __launch_bounds__(1024) k_layout(const EncParams *__restrict__ P
             R.block_off = H + (uint64_t)excl;
             R.payload_off = R.block_off + kBlockHeader;
             R.tok_start = R.payload_off +
-                          (R.codec == 2 ? (uint64_t)((R.n + 7) >> 3) + 8ull * (uint64_t)R.nesc : 0ull);
+                          (R.codec == 2 ? (uint64_t)((R.n_win + 7) >> 3) + 8ull * (uint64_t)R.nesc : 0ull);
             nsc = nsc_of(R.payload_off, R.payload_off + R.payload_len);
         }
         // scan of superchunk counts
@@ -711,7 +719,9 @@ __global__ void __launch_bounds__(256) k_scan_down(const EncParams *__restrict__
 }
 
 // escape bitmaps of codec-2 regions: one byte = 8 consecutive stream samples
-// codec 2: the escape bitmap (np.packbits little-endian) from k_quant's bits
+// codec 2: the escape bitmap (np.packbits little-endian) from k_quant's bits;
+// a portion writes the bytes overlapping window bits [s_off, s_off + n) with
+// its own bits only (other portions' bits stay 0, so slices OR together)
 __global__ void __launch_bounds__(256) k_bitmap(const RegDev *__restrict__ regs,
                                                 const int32_t *__restrict__ list,
                                                 const EncScalars *__restrict__ sc,
@@ -720,13 +730,16 @@ __global__ void __launch_bounds__(256) k_bitmap(const RegDev *__restrict__ regs,
     const int64_t nl = sc->n_codec2;
     for (int64_t li = 0; li < nl; ++li) {
         const RegDev &R = regs[list[li]];
-        const int64_t nbytes = (R.n + 7) >> 3;
-        const uint8_t *src = reinterpret_cast<const uint8_t *>(escbits + R.ebase);
-        for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nbytes;
-             b += (int64_t)gridDim.x * blockDim.x) {
-            uint8_t v = src[b];
-            if (b == nbytes - 1 && (R.n & 7)) v &= (uint8_t)((1u << (R.n & 7)) - 1u);
-            out[R.payload_off + b] = v;
+        const int64_t b0 = R.s_off >> 3, b1 = (R.s_off + R.n + 7) >> 3;  // window bitmap bytes touched
+        for (int64_t B = b0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; B < b1;
+             B += (int64_t)gridDim.x * blockDim.x) {
+            uint32_t v = 0;
+            for (int k = 0; k < 8; ++k) {
+                const int64_t sb = 8 * B + k - R.s_off;  // portion-local bit
+                if (sb < 0 || sb >= R.n) continue;
+                v |= ((escbits[R.ebase + (sb >> 5)] >> (sb & 31)) & 1u) << k;
+            }
+            out[R.payload_off + B] = (uint8_t)v;
         }
     }
 }
@@ -836,6 +849,7 @@ __global__ void k_finalize_file(const CrcTables *__restrict__ tabs, const EncSca
 struct EncPlan {
     std::vector<RegDev> regs;
     int64_t nitems = 0, npieces_total = 0, nchunks = 0, qtotal = 0, etotal = 0;
+    bool portions = false;  // empty windows allowed (z-slab portions)
     size_t ws_bytes = 0;
     // carved pointers
     EncParams *params;
@@ -863,7 +877,7 @@ static bool build_plan(const chr_region_t *h, int64_t nreg, EncPlan &pl) {
         R.ex = h[r].extent[0];
         R.ey = h[r].extent[1];
         R.ez = h[r].extent[2];
-        if (R.ex < 1 || R.ey < 1 || R.ez < 1) return false;
+        if (R.ex < 1 || R.ey < 1 || R.ez < (pl.portions ? 0 : 1)) return false;
         R.e = h[r].error_bound;
         if (!(R.e >= 0.0) || !std::isfinite(R.e)) return false;
         R.mode = R.e == 0.0 ? 1 : 0;
@@ -879,6 +893,11 @@ static bool build_plan(const chr_region_t *h, int64_t nreg, EncPlan &pl) {
         R.nchunks = ceil_div(R.npieces, CH);
         chunk += R.nchunks;
         piece += R.nchunks * CH;
+        R.s_off = 0;
+        R.n_win = R.n;
+        R.zhalo = 0;
+        R.last = 1;
+        R.pre = tokseg_identity();
         R.q_base = pl.qtotal;
         pl.qtotal += R.n;
         R.ebase = pl.etotal;
@@ -1182,5 +1201,375 @@ extern "C" int chr_rle_encode(const int64_t *d_q, int64_t n, uint8_t *d_out, uin
     CHR_CUDA_TRY(cudaStreamSynchronize(st));
     if (bad) return CHR_E_PARAMETER;
     *h_nbytes = (uint64_t)pl.regs[0].tok_len;
+    return CHR_OK;
+}
+
+// ------------------------------------------------------------------ z-slab protocol
+// rank r encodes the planes [zs, ze) of every window (its
+// "portion", a contiguous piece of the window's raster stream) from a local
+// volume holding planes [z_base, z_base + nz_local) (zs - 1 and the block
+// ghost plane included).  Phase 1 summarises each portion's stream (the
+// token-size monoid); after an allgather of those summaries every rank knows
+// each window's codec, length and layout and the summary of the stream
+// before its own portion, writes its bytes at their final offsets (phase 2)
+// and returns the raw CRC of its share of each payload (zeros elsewhere:
+// CRC is linear over GF(2), so the shares XOR to the payload CRC).  Rank 0
+// then writes the block headers and the trailer (phase 3).
+static bool dist_plan(const chr_region_t *h, int64_t nreg, int64_t z_base, int64_t nz_local, int64_t zs,
+                      int64_t ze, EncPlan &pl) {
+    std::vector<chr_region_t> loc(h, h + nreg);
+    std::vector<int64_t> pa(nreg), pb(nreg);
+    for (int64_t r = 0; r < nreg; ++r) {
+        const int64_t oz = h[r].origin[2], ez = h[r].extent[2];
+        pa[r] = std::max(oz, zs);
+        pb[r] = std::max(pa[r], std::min(oz + ez, ze));
+        loc[r].origin[2] = (int32_t)(pa[r] - z_base);
+        loc[r].extent[2] = (int32_t)(pb[r] - pa[r]);
+        if (pb[r] > pa[r] && (pa[r] - (pa[r] > oz ? 1 : 0) < z_base || pb[r] > z_base + nz_local)) return false;
+    }
+    pl.portions = true;
+    if (!build_plan(loc.data(), nreg, pl)) return false;
+    for (int64_t r = 0; r < nreg; ++r) {
+        RegDev &R = pl.regs[r];
+        const int64_t oz = h[r].origin[2];
+        R.s_off = (pa[r] - oz) * (int64_t)R.ex * R.ey;
+        R.n_win = (int64_t)R.ex * R.ey * h[r].extent[2];
+        R.zhalo = pa[r] > oz ? 1 : 0;
+        R.last = pb[r] == oz + h[r].extent[2] ? 1 : 0;
+    }
+    return true;
+}
+
+extern "C" size_t chr_dcompress_workspace_size(const chr_region_t *h, int64_t nreg, int64_t z_base, int64_t nz_local,
+                                               int64_t zs, int64_t ze) {
+    EncPlan pl;
+    if (!h || nreg < 1 || !dist_plan(h, nreg, z_base, nz_local, zs, ze, pl)) return 0;
+    carve(pl, nullptr, ~size_t(0));
+    // + CRC segments of this rank (<= 3 per region) and the header phase's tables
+    return pl.ws_bytes + (sizeof(CrcSeg) + 8) * (size_t)(3 * nreg + 2) + sizeof(RegDev) * (size_t)nreg + 8192;
+}
+
+namespace chr {
+__global__ void k_portion_agg(const RegDev *__restrict__ regs, int64_t nreg, const TokSeg *__restrict__ chunk_agg,
+                              int dtype_f32, TokSeg *__restrict__ out) {
+    const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (r >= nreg) return;
+    const RegDev &R = regs[r];
+    TokSeg acc = tokseg_identity();
+    for (int64_t c0 = 0; c0 < R.nchunks; c0 += 32) {
+        const bool ok = c0 + lane < R.nchunks;
+        TokSeg inc = ok ? chunk_agg[R.chunk_base + c0 + lane] : tokseg_identity();
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const TokSeg o = WarpSeg::shfl_up(inc, off);
+            if (lane >= off) inc = tokseg_combine(o, inc);
+        }
+        TokSeg tot;
+        tot.len = __shfl_sync(0xFFFFFFFFu, inc.len, 31);
+        tot.lead = __shfl_sync(0xFFFFFFFFu, inc.lead, 31);
+        tot.trail = __shfl_sync(0xFFFFFFFFu, inc.trail, 31);
+        tot.bytes = __shfl_sync(0xFFFFFFFFu, inc.bytes, 31);
+        tot.nesc = __shfl_sync(0xFFFFFFFFu, inc.nesc, 31);
+        tot.nz = __shfl_sync(0xFFFFFFFFu, inc.nz, 31);
+        tot.f32ok = __shfl_sync(0xFFFFFFFFu, inc.f32ok, 31);
+        acc = tokseg_combine(acc, tot);
+    }
+    if (lane == 0) {
+        acc.f32ok = dtype_f32 ? 1 : (R.f32bad == 0 ? 1 : 0);
+        out[r] = acc;
+    }
+}
+}  // namespace chr
+
+static void dist_params(EncParams &hp, const EncPlan &pl, int64_t nx, int64_t ny, int64_t nz_local, int dtype,
+                        int src_dtype, int write_file, const double *spacing, int64_t bs, double vmin, double vmax,
+                        const double *h_cands, int m, int64_t nreg) {
+    std::memset(&hp, 0, sizeof(hp));
+    hp.NX = nx;
+    hp.NY = ny;
+    hp.NZ = nz_local;
+    hp.nreg = nreg;
+    hp.nitems = pl.nitems;
+    hp.nchunks = pl.nchunks;
+    hp.dtype = dtype;
+    hp.src_dtype = src_dtype;
+    hp.write_file = write_file;
+    hp.m = m;
+    hp.dist = 1;
+    for (int a = 0; a < 3; ++a) hp.spacing[a] = spacing ? spacing[a] : 1.0;
+    hp.vmin = vmin;
+    hp.vmax = vmax;
+    hp.bs = bs;
+    for (int i = 0; i < m && i < 64; ++i) hp.cands[i] = h_cands[i];
+    hp.header_table = (uint64_t)(kFileHeader + 4 + 8 * m + 4) + (uint64_t)nreg * (kRegionFixed + (m + 7) / 8);
+}
+
+// phase 1: quantise this rank's portions and summarise their streams
+extern "C" int chr_dcompress_local(const void *d_vol, int dtype, int src_dtype, int64_t nx, int64_t ny,
+                                   int64_t nz_local, int64_t z_base, int64_t zs, int64_t ze,
+                                   const chr_region_t *h_regions, int64_t nreg, void *d_ws, size_t ws_bytes,
+                                   chr_portion_t *h_portions, void *stream) {
+    if (!d_vol || !h_regions || nreg < 1 || !h_portions) return CHR_E_PARAMETER;
+    if (dtype != CHR_F32 && dtype != CHR_F64) return CHR_E_PARAMETER;
+    static_assert(sizeof(chr_portion_t) == sizeof(TokSeg), "chr_portion_t mirrors TokSeg");
+    cudaStream_t st = (cudaStream_t)stream;
+    EncPlan pl;
+    if (!dist_plan(h_regions, nreg, z_base, nz_local, zs, ze, pl)) return CHR_E_PARAMETER;
+    for (const RegDev &R : pl.regs)
+        if (R.ox < 0 || R.oy < 0 || R.ox + R.ex > nx || R.oy + R.ey > ny) return CHR_E_PARAMETER;
+    carve(pl, d_ws, ws_bytes);
+    if (!d_ws || pl.ws_bytes > ws_bytes) return CHR_E_WORKSPACE;
+    TokSeg *d_agg = reinterpret_cast<TokSeg *>(reinterpret_cast<char *>(d_ws) + pl.ws_bytes);
+    EncParams hp;
+    dist_params(hp, pl, nx, ny, nz_local, dtype, src_dtype, 0, nullptr, 1, 0, 0, nullptr, 0, nreg);
+    CHR_CUDA_TRY(cudaMemcpyAsync(pl.params, &hp, sizeof(hp), cudaMemcpyHostToDevice, st));
+    CHR_CUDA_TRY(cudaMemcpyAsync(pl.d_regs, pl.regs.data(), sizeof(RegDev) * nreg, cudaMemcpyHostToDevice, st));
+    CHR_CUDA_TRY(cudaMemsetAsync(pl.escbits, 0, sizeof(uint32_t) * (pl.etotal + 2), st));
+    const unsigned items = (unsigned)pl.nitems, chunks = (unsigned)pl.nchunks;
+    k_tile_fill_map<<<(unsigned)nreg, 256, 0, st>>>(pl.d_regs, nreg, pl.item_reg, pl.chunk_reg);
+    if (items) {
+        CHR_PROF(dtype == CHR_F32 ? "k_quant<float>" : "k_quant<double>", st);
+        if (dtype == CHR_F32)
+            k_quant<float><<<items, NW * 32, 0, st>>>((const float *)d_vol, pl.params, pl.d_regs, pl.item_reg,
+                                                      pl.qz, pl.escbits);
+        else
+            k_quant<double><<<items, NW * 32, 0, st>>>((const double *)d_vol, pl.params, pl.d_regs, pl.item_reg,
+                                                       pl.qz, pl.escbits);
+    }
+    if (chunks) {
+        {
+            CHR_PROF("k_summarize", st);
+            k_summarize<<<chunks, 256, 0, st>>>(pl.d_regs, pl.chunk_reg, pl.qz, pl.escbits, pl.recs);
+        }
+        k_scan_reduce<<<chunks, 256, 0, st>>>(pl.params, pl.d_regs, pl.recs, pl.chunk);
+    }
+    k_portion_agg<<<(unsigned)ceil_div(nreg, 4), 128, 0, st>>>(pl.d_regs, nreg, pl.chunk, dtype == CHR_F32, d_agg);
+    CHR_CUDA_TRY(cudaGetLastError());
+    CHR_CUDA_TRY(cudaMemcpyAsync(h_portions, d_agg, sizeof(TokSeg) * nreg, cudaMemcpyDeviceToHost, st));
+    CHR_CUDA_TRY(cudaStreamSynchronize(st));
+    return CHR_OK;
+}
+
+static TokSeg as_seg(const chr_portion_t &p) {
+    TokSeg s;
+    std::memcpy(&s, &p, sizeof(s));
+    return s;
+}
+
+// phase 2: codec / layout from every rank's summaries, this rank's bytes at
+// their final offsets, its raw CRC share of every payload
+extern "C" int chr_dcompress_finish(const void *d_vol, int dtype, int src_dtype, int64_t nx, int64_t ny,
+                                    int64_t nz_local, int64_t z_base, int64_t zs, int64_t ze, const double *spacing,
+                                    int64_t bs, double vmin, double vmax, const double *h_cands, int m,
+                                    chr_region_t *h_regions, int64_t nreg, const chr_portion_t *h_all, int nranks,
+                                    int rank, void *d_ws, size_t ws_bytes, uint8_t *d_out, uint64_t out_cap,
+                                    uint32_t *h_raw, uint64_t *h_file_nbytes, void *stream) {
+    if (!d_vol || !h_regions || nreg < 1 || !h_all || nranks < 1 || rank < 0 || rank >= nranks || !d_out ||
+        !h_raw || !h_file_nbytes || m < 1 || m > 64 || !h_cands)
+        return CHR_E_PARAMETER;
+    cudaStream_t st = (cudaStream_t)stream;
+    EncPlan pl;
+    if (!dist_plan(h_regions, nreg, z_base, nz_local, zs, ze, pl)) return CHR_E_PARAMETER;
+    carve(pl, d_ws, ws_bytes);
+    if (!d_ws || pl.ws_bytes > ws_bytes) return CHR_E_WORKSPACE;
+    if (out_cap < chr_compress_capacity(h_regions, nreg, m, src_dtype)) return CHR_E_PARAMETER;
+    // the device records keep phase 1's flags (has_esc, f32bad, maps)
+    CHR_CUDA_TRY(cudaMemcpyAsync(pl.regs.data(), pl.d_regs, sizeof(RegDev) * nreg, cudaMemcpyDeviceToHost, st));
+    CHR_CUDA_TRY(cudaStreamSynchronize(st));
+    std::vector<int32_t> c2;
+    for (int64_t r = 0; r < nreg; ++r) {
+        RegDev &R = pl.regs[r];
+        TokSeg tot = tokseg_identity(), pre = tokseg_identity();
+        bool f32ok = true;
+        for (int k = 0; k < nranks; ++k) {
+            const TokSeg s = as_seg(h_all[(int64_t)k * nreg + r]);
+            if (k < rank) pre = tokseg_combine(pre, s);
+            tot = tokseg_combine(tot, s);
+            f32ok = f32ok && s.f32ok;
+        }
+        const bool vf32 = src_dtype == CHR_F32 && (dtype == CHR_F32 || f32ok);
+        const int64_t vlen = R.n_win * (vf32 ? 4 : 8);
+        const int vcodec = vf32 ? 3 : 0;
+        int codec;
+        int64_t plen, tok = 0, nesc = 0;
+        if (R.mode == 1) {
+            codec = vcodec;
+            plen = vlen;
+        } else {
+            tok = tokseg_stream_bytes(tot);
+            nesc = tot.nesc;
+            codec = nesc ? 2 : 1;
+            plen = nesc ? ((R.n_win + 7) >> 3) + 8 * nesc + tok : tok;
+            if (plen >= vlen) {
+                codec = vcodec;
+                plen = vlen;
+            }
+        }
+        R.codec = codec;
+        R.f32ok = f32ok;
+        R.tok_len = tok;
+        R.nesc = nesc;
+        R.payload_len = plen;
+        R.pre = pre;
+        if (codec == 2 && R.n > 0) c2.push_back((int32_t)r);
+    }
+    const int write_file = 1;  // every rank lays out the whole file (header/table written by rank 0 in phase 3)
+    EncParams hp;
+    dist_params(hp, pl, nx, ny, nz_local, dtype, src_dtype, write_file, spacing, bs, vmin, vmax, h_cands, m, nreg);
+    EncScalars hs0;
+    std::memset(&hs0, 0, sizeof(hs0));
+    hs0.n_codec2 = (int64_t)c2.size();
+    CHR_CUDA_TRY(cudaMemcpyAsync(pl.params, &hp, sizeof(hp), cudaMemcpyHostToDevice, st));
+    CHR_CUDA_TRY(cudaMemcpyAsync(pl.d_regs, pl.regs.data(), sizeof(RegDev) * nreg, cudaMemcpyHostToDevice, st));
+    CHR_CUDA_TRY(cudaMemcpyAsync(pl.scal, &hs0, sizeof(hs0), cudaMemcpyHostToDevice, st));
+    if (!c2.empty())
+        CHR_CUDA_TRY(cudaMemcpyAsync(pl.codec2, c2.data(), sizeof(int32_t) * c2.size(), cudaMemcpyHostToDevice, st));
+    const unsigned chunks = (unsigned)pl.nchunks;
+    k_scan_regions<<<(unsigned)ceil_div(nreg, 4), 128, 0, st>>>(pl.params, pl.d_regs, pl.chunk, pl.codec2, pl.scal);
+    k_layout<<<1, 1024, 0, st>>>(pl.params, pl.d_regs, pl.segs, pl.scal);
+    if (chunks) {
+        k_scan_down<<<chunks, 256, 0, st>>>(pl.params, pl.d_regs, pl.recs, pl.chunk, pl.poffs);
+        CHR_PROF(dtype == CHR_F32 ? "k_emit_q<float>" : "k_emit_q<double>", st);
+        if (dtype == CHR_F32)
+            k_emit_q<float><<<chunks, 256, 0, st>>>((const float *)d_vol, pl.params, pl.d_regs, pl.chunk_reg,
+                                                    pl.recs, pl.poffs, pl.qz, pl.escbits, d_out);
+        else
+            k_emit_q<double><<<chunks, 256, 0, st>>>((const double *)d_vol, pl.params, pl.d_regs, pl.chunk_reg,
+                                                     pl.recs, pl.poffs, pl.qz, pl.escbits, d_out);
+    }
+    if (!c2.empty()) k_bitmap<<<148, 256, 0, st>>>(pl.d_regs, pl.codec2, pl.scal, pl.escbits, d_out);
+    CHR_CUDA_TRY(cudaGetLastError());
+    EncScalars hs;
+    CHR_CUDA_TRY(cudaMemcpyAsync(pl.regs.data(), pl.d_regs, sizeof(RegDev) * nreg, cudaMemcpyDeviceToHost, st));
+    CHR_CUDA_TRY(cudaMemcpyAsync(&hs, pl.scal, sizeof(hs), cudaMemcpyDeviceToHost, st));
+    CHR_CUDA_TRY(cudaStreamSynchronize(st));
+    // this rank's byte ranges inside every payload (+ the header/table on rank 0)
+    std::vector<CrcSeg> segs;
+    std::vector<int64_t> seg_reg;
+    auto add = [&](uint64_t a, uint64_t b, int64_t r) {
+        if (b <= a) return;
+        CrcSeg sg;
+        std::memset(&sg, 0, sizeof(sg));
+        sg.begin = a;
+        sg.end = b;
+        segs.push_back(sg);
+        seg_reg.push_back(r);
+    };
+    for (int64_t r = 0; r < nreg; ++r) {
+        const RegDev &R = pl.regs[r];
+        if (R.n == 0) continue;
+        if (R.codec == 0 || R.codec == 3) {
+            const int w = R.codec == 3 ? 4 : 8;
+            add(R.payload_off + (uint64_t)(w * R.s_off), R.payload_off + (uint64_t)(w * (R.s_off + R.n)), r);
+            continue;
+        }
+        const TokSeg mine = as_seg(h_all[(int64_t)rank * nreg + r]);
+        const TokSeg upto = tokseg_combine(R.pre, mine);
+        auto tok_off = [](const TokSeg &t) { return t.bytes + (t.nz ? run_bytes(t.lead) : 0); };
+        const int64_t t0 = tok_off(R.pre);
+        const int64_t t1 = R.last ? R.tok_len : tok_off(upto);
+        add(R.tok_start + (uint64_t)t0, R.tok_start + (uint64_t)t1, r);
+        if (R.codec == 2) {
+            const uint64_t vbase = R.payload_off + (uint64_t)((R.n_win + 7) >> 3);
+            add(vbase + 8ull * (uint64_t)R.pre.nesc, vbase + 8ull * (uint64_t)(R.pre.nesc + mine.nesc), r);
+            add(R.payload_off + (uint64_t)(R.s_off >> 3), R.payload_off + (uint64_t)((R.s_off + R.n + 7) >> 3), r);
+        }
+    }
+    for (int64_t r = 0; r <= nreg; ++r) h_raw[r] = 0;
+    if (!segs.empty()) {
+        const int64_t ns = (int64_t)segs.size();
+        const int64_t total_sc = crc_plan_segments(segs.data(), ns);
+        CrcSeg *d_segs = reinterpret_cast<CrcSeg *>(reinterpret_cast<char *>(d_ws) + pl.ws_bytes);
+        uint32_t *d_sraw = reinterpret_cast<uint32_t *>(d_segs + ns);
+        if (pl.ws_bytes + (size_t)ns * (sizeof(CrcSeg) + 4) + 64 > ws_bytes) return CHR_E_WORKSPACE;
+        CHR_CUDA_TRY(cudaMemcpyAsync(d_segs, segs.data(), sizeof(CrcSeg) * ns, cudaMemcpyHostToDevice, st));
+        CHR_CUDA_TRY(cudaMemsetAsync(d_sraw, 0, sizeof(uint32_t) * ns, st));
+        int rc = crc_launch(d_out, d_segs, ns, total_sc, d_sraw, st);
+        if (rc) return rc;
+        std::vector<uint32_t> sraw(ns);
+        CHR_CUDA_TRY(cudaMemcpyAsync(sraw.data(), d_sraw, sizeof(uint32_t) * ns, cudaMemcpyDeviceToHost, st));
+        CHR_CUDA_TRY(cudaStreamSynchronize(st));
+        const CrcTables &H = crc_tables_hostref();
+        for (int64_t i = 0; i < ns; ++i) {
+            const int64_t r = seg_reg[i];
+            const RegDev &R = pl.regs[r];
+            const uint64_t pend = R.payload_off + (uint64_t)R.payload_len;
+            h_raw[1 + r] ^= crc_shift(H.x2n, sraw[i], pend - segs[i].end);  // shift to the payload end
+        }
+    }
+    for (int64_t r = 0; r < nreg; ++r) {
+        const RegDev &R = pl.regs[r];
+        chr_region_t &o = h_regions[r];
+        o.codec_id = R.codec;
+        o.block_offset = R.block_off;
+        o.block_nbytes = kBlockHeader + (uint64_t)R.payload_len;
+        o.n_escaped = (uint64_t)R.nesc;
+    }
+    *h_file_nbytes = hs.out_nbytes;
+    return CHR_OK;
+}
+
+// phase 3 (rank 0): block headers with the combined payload CRCs, trailer
+extern "C" int chr_dcompress_headers(int64_t nx, int64_t ny, int64_t nz, int src_dtype, const double *spacing,
+                                     int64_t bs, double vmin, double vmax, const double *h_cands, int m,
+                                     chr_region_t *h_regions, int64_t nreg, const uint32_t *h_raw_all, void *d_ws,
+                                     size_t ws_bytes, uint8_t *d_out, void *stream) {
+    if (!h_regions || nreg < 1 || !h_raw_all || !d_out || m < 1 || m > 64 || !h_cands) return CHR_E_PARAMETER;
+    cudaStream_t st = (cudaStream_t)stream;
+    EncPlan pl;
+    pl.portions = true;
+    if (!build_plan(h_regions, nreg, pl)) return CHR_E_PARAMETER;
+    {  // only the small tables are needed here
+        WsCarver c{reinterpret_cast<char *>(d_ws), 0, ws_bytes};
+        pl.params = c.take<EncParams>(1);
+        pl.d_regs = c.take<RegDev>(nreg);
+        pl.segs = c.take<CrcSeg>(2);
+        pl.seg_raw = c.take<uint32_t>(nreg + 1);
+        pl.scal = c.take<EncScalars>(1);
+        if (!d_ws || !c.ok) return CHR_E_WORKSPACE;
+    }
+    const CrcTables *tabs = crc_tables_device();
+    if (!tabs) return CHR_E_CUDA;
+    uint64_t body = 0;
+    for (int64_t r = 0; r < nreg; ++r) {
+        RegDev &R = pl.regs[r];
+        R.codec = h_regions[r].codec_id;
+        R.block_off = h_regions[r].block_offset;
+        R.payload_off = R.block_off + kBlockHeader;
+        R.payload_len = (int64_t)h_regions[r].block_nbytes - kBlockHeader;
+        body = std::max<uint64_t>(body, R.block_off + h_regions[r].block_nbytes);
+    }
+    EncParams hp;
+    dist_params(hp, pl, nx, ny, nz, CHR_F32, src_dtype, 1, spacing, bs, vmin, vmax, h_cands, m, nreg);
+    EncScalars hs0;
+    std::memset(&hs0, 0, sizeof(hs0));
+    hs0.file_body = body;
+    hs0.out_nbytes = body + 4;
+    CHR_CUDA_TRY(cudaMemcpyAsync(pl.params, &hp, sizeof(hp), cudaMemcpyHostToDevice, st));
+    CHR_CUDA_TRY(cudaMemcpyAsync(pl.d_regs, pl.regs.data(), sizeof(RegDev) * nreg, cudaMemcpyHostToDevice, st));
+    CHR_CUDA_TRY(cudaMemcpyAsync(pl.scal, &hs0, sizeof(hs0), cudaMemcpyHostToDevice, st));
+    // file header + region table (global windows), then their raw CRC into
+    // seg_raw[0]; seg_raw[1 + r] = payload raw CRCs (XOR of every rank's share)
+    k_write_table<<<(unsigned)ceil_div(nreg, 256), 256, 0, st>>>(pl.params, pl.d_regs, d_out);
+    CHR_CUDA_TRY(cudaMemcpyAsync(pl.seg_raw + 1, h_raw_all + 1, sizeof(uint32_t) * nreg, cudaMemcpyHostToDevice, st));
+    CHR_CUDA_TRY(cudaMemsetAsync(pl.seg_raw, 0, sizeof(uint32_t), st));
+    CrcSeg hseg;
+    std::memset(&hseg, 0, sizeof(hseg));
+    hseg.begin = 0;
+    hseg.end = hp.header_table;
+    const int64_t hsc = crc_plan_segments(&hseg, 1);
+    CHR_CUDA_TRY(cudaMemcpyAsync(pl.segs, &hseg, sizeof(hseg), cudaMemcpyHostToDevice, st));
+    {
+        const int rc = crc_launch(d_out, pl.segs, 1, hsc, pl.seg_raw, st);
+        if (rc) return rc;
+    }
+    k_finalize_regions<<<(unsigned)ceil_div(nreg, 4), 128, 0, st>>>(pl.params, pl.d_regs, pl.seg_raw, tabs, pl.scal,
+                                                                      d_out);
+    k_finalize_file<<<1, 1, 0, st>>>(tabs, pl.scal, d_out);
+    CHR_CUDA_TRY(cudaGetLastError());
+    CHR_CUDA_TRY(cudaMemcpyAsync(pl.regs.data(), pl.d_regs, sizeof(RegDev) * nreg, cudaMemcpyDeviceToHost, st));
+    CHR_CUDA_TRY(cudaStreamSynchronize(st));
+    for (int64_t r = 0; r < nreg; ++r) h_regions[r].payload_crc = pl.regs[r].crc;
     return CHR_OK;
 }

@@ -1,16 +1,34 @@
-"""Multi-GPU placement of per-rank outputs (collective 3).
+"""Multi-GPU path.
 
-One process per GPU; every rank compresses / meshes its own volume (or
-z-slab) and the ranks exchange only sizes: an all-gather of per-rank
-(archive bytes, triangles, vertices) gives each rank the global offsets at
-which its archive bytes and mesh rows land in the concatenated outputs.
+One process per GPU.  Two modes:
+
+* independent volumes (replicas): every rank compresses / meshes its own
+  volume and the ranks exchange only sizes (``place``);
+* one volume in z-slabs of whole blocks (``build_archive_slab``): rank r
+  owns block z-layers [r*B, (r+1)*B) and holds those planes plus a low halo
+  plane and the high ghost plane.  Collectives, each after the step it
+  depends on: (1) all-gather of per-block (vmin, vmax, dmin) -> identical
+  plan on every rank; (2) all-gather of per-(region, rank) stream summaries
+  (chr_portion_t) -> codecs, layout and each rank's stream prefix; (3)
+  all-gather of raw CRC shares -> payload CRCs (rank 0 writes headers).
+  Archive bytes stay distributed (each rank writes its slices at their
+  final offsets); ``assemble`` ORs the slices into the file.
+
 Works with NCCL (CUDA tensors) and gloo (CPU tensors, used by the tests).
 """
 
 from __future__ import annotations
 
+import ctypes
+import math
+from dataclasses import dataclass
+
+import numpy as np
 import torch
 import torch.distributed as dist
+
+from . import _abi, device as D
+from .exceptions import NonFiniteSampleError, ParameterError
 
 
 def gather_sizes(archive_nbytes: int, ntri: int, nvert: int, device=None) -> torch.Tensor:
@@ -34,3 +52,131 @@ def offsets_from_sizes(sizes: torch.Tensor, rank: int) -> dict:
 def place(archive_nbytes: int, ntri: int, nvert: int, device=None) -> dict:
     sizes = gather_sizes(archive_nbytes, ntri, nvert, device)
     return offsets_from_sizes(sizes, dist.get_rank())
+
+
+# ------------------------------------------------------------------ z-slabs
+@dataclass(frozen=True)
+class Slab:
+    """Planes of one rank (global z): encodes [zs, ze), holds [z_base, z_base + nz_local),
+    block stats over [zs, zs + nz_stats) (blocks bz0..bz1-1)."""
+    rank: int
+    world: int
+    bz0: int
+    bz1: int
+    zs: int
+    ze: int
+    z_base: int
+    nz_local: int
+    nz_stats: int
+
+
+def slab_of(nz: int, bs: int, world: int, rank: int) -> Slab:
+    nbz = max(1, math.ceil((nz - 1) / bs))
+    per = math.ceil(nbz / world)
+    bz0, bz1 = min(rank * per, nbz), min((rank + 1) * per, nbz)
+    last = bz1 == nbz
+    if bz0 == bz1:  # more ranks than block layers
+        return Slab(rank, world, bz0, bz1, nz, nz, nz - 1, 1, 0)
+    zs = bz0 * bs
+    ze = nz if last else bz1 * bs
+    ghost = min(bz1 * bs, nz - 1)  # high ghost plane of the last block layer
+    z_base = max(zs - 1, 0)
+    return Slab(rank, world, bz0, bz1, zs, ze, z_base, ghost - z_base + 1, ghost - zs + 1)
+
+
+def _allgather(t: torch.Tensor) -> list[torch.Tensor]:
+    nccl = dist.get_backend() == "nccl"
+    src = t.cuda() if nccl else t.cpu()
+    out = [torch.empty_like(src) for _ in range(dist.get_world_size())]
+    dist.all_gather(out, src)
+    return [o.cpu() for o in out]
+
+
+def build_archive_slab(vol_local: torch.Tensor, dims, slab: Slab, cands, bs, *, spacing=(1.0, 1.0, 1.0),
+                       source_dtype="f32", loose_fraction=D.LOOSE_FRACTION, safety_factor=D.SAFETY_FACTOR,
+                       ws: D.Workspaces | None = None) -> D.Compressed:
+    """build_chr over z-slabs: this rank's slice of the archive (zeros
+    elsewhere), the identical region table on every rank, and the file size.
+    `vol_local`: planes [slab.z_base, slab.z_base + slab.nz_local), x fastest."""
+    ws = ws or D.Workspaces()
+    nx, ny, nz = dims
+    L = _abi.lib()
+    cands = D._cands_arr(cands)
+    m = cands.size
+    nbx, nby = max(1, math.ceil((nx - 1) / bs)), max(1, math.ceil((ny - 1) / bs))
+    # (1) block stats of own layers -> all-gather -> identical plan
+    nb_mine = nbx * nby * (slab.bz1 - slab.bz0)
+    per = math.ceil(max(1, math.ceil((nz - 1) / bs)) / slab.world)
+    nb_max = nbx * nby * per
+    pack = torch.full((nb_max * 3 + 2,), float("nan"), dtype=torch.float64, device=vol_local.device)
+    pack[-2] = float(nb_mine)
+    pack[-1] = -1.0
+    if nb_mine:
+        off = (slab.zs - slab.z_base) * nx * ny
+        view = vol_local.reshape(-1)[off: off + slab.nz_stats * nx * ny]
+        bst, bad = D.stats(view, (nx, ny, slab.nz_stats), bs, cands)
+        pack[: nb_mine * 3] = bst.reshape(-1)
+        pack[-1] = bad.to(torch.float64)[0]
+    parts = _allgather(pack)
+    stats, vmin, vmax = [], math.inf, -math.inf
+    for r, p in enumerate(parts):
+        k = int(p[-2])
+        bad = int(p[-1])
+        if bad >= 0:
+            sr = slab_of(nz, bs, slab.world, r)
+            raise NonFiniteSampleError(sr.zs * nx * ny + bad, float("nan"))
+        stats.append(p[: k * 3].numpy().reshape(k, 3))
+    bstats = np.concatenate(stats)
+    vmin, vmax = float(bstats[:, 0].min()), float(bstats[:, 1].max())
+    outside = [float(k) for k in cands if not vmin <= k <= vmax]
+    if outside:
+        raise ParameterError(f"candidates outside the volume's value range [{vmin}, {vmax}]: {outside}")
+    regions = D.plan(bstats, dims, bs, cands, vmin, vmax, loose_fraction, safety_factor)
+    nreg = len(regions)
+    rp = _abi.aptr(regions)
+    # (2) local portions -> all-gather of stream summaries
+    wsz = L.chr_dcompress_workspace_size(rp, nreg, slab.z_base, slab.nz_local, slab.zs, slab.ze)
+    if wsz == 0:
+        raise ParameterError("slab geometry does not cover its portions")
+    work = ws.get("dcompress", wsz)
+    por = np.zeros(nreg, dtype=_abi.PORTION_DT)
+    dcode = D._dtype_code(vol_local)
+    tag = D.DTYPE_TAGS[source_dtype]
+    D.check(L.chr_dcompress_local(D.ptr(vol_local), dcode, tag, nx, ny, slab.nz_local, slab.z_base, slab.zs, slab.ze,
+                                  rp, nreg, D.ptr(work), work.numel(), _abi.aptr(por), D.stream_ptr()),
+            "chr_dcompress_local")
+    allp = _allgather(torch.from_numpy(por.view(np.uint8).copy()))
+    all_por = np.concatenate([a.numpy().view(_abi.PORTION_DT) for a in allp])
+    cap = int(L.chr_compress_capacity(rp, nreg, m, tag))
+    out = ws.get("dcompress_out", cap)
+    out.zero_()
+    raw = np.zeros(nreg + 1, dtype=np.uint32)
+    fbytes = ctypes.c_uint64(0)
+    sp = (ctypes.c_double * 3)(*[float(s) for s in spacing])
+    D.check(L.chr_dcompress_finish(D.ptr(vol_local), dcode, tag, nx, ny, slab.nz_local, slab.z_base, slab.zs, slab.ze,
+                                   sp, int(bs), vmin, vmax, D._np_ptr(cands), m, rp, nreg, _abi.aptr(all_por),
+                                   slab.world, slab.rank, D.ptr(work), work.numel(), D.ptr(out), out.numel(),
+                                   _abi.aptr(raw), ctypes.byref(fbytes), D.stream_ptr()), "chr_dcompress_finish")
+    # (3) CRC shares -> payload CRCs; rank 0 writes the headers and trailer
+    shares = _allgather(torch.from_numpy(raw.view(np.int32).copy()))
+    tot = np.zeros(nreg + 1, dtype=np.uint32)
+    for sh in shares:
+        tot ^= sh.numpy().view(np.uint32)
+    if slab.rank == 0:
+        hw = ws.get("dheaders", 8192 + 512 * (nreg + 2))
+        D.check(L.chr_dcompress_headers(nx, ny, nz, tag, sp, int(bs), vmin, vmax, D._np_ptr(cands), m, rp, nreg,
+                                        _abi.aptr(tot), D.ptr(hw), hw.numel(), D.ptr(out), D.stream_ptr()),
+                "chr_dcompress_headers")
+    res = D.Compressed(out, int(fbytes.value), regions, source_dtype)
+    res.extra.update(block_stats=bstats, vrange=(vmin, vmax), cands=tuple(float(k) for k in cands))
+    return res
+
+
+def assemble(res: D.Compressed) -> torch.Tensor:
+    """Every rank's slice ORed into the complete file (an all-reduce of
+    disjoint bytes: SUM == OR); returns the file on every rank."""
+    buf = res.blob[: res.nbytes]
+    nccl = dist.get_backend() == "nccl"
+    t = buf.clone() if nccl else buf.cpu().to(torch.int32)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return t.to(torch.uint8).to(buf.device) if not nccl else t

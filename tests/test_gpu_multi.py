@@ -1,0 +1,80 @@
+"""z-slab multi-GPU protocol on one GPU: two processes share
+cuda:0 and exchange only the small records over gloo (no kernel of one rank
+waits on the other).  The slices they write must OR into exactly the file
+the single-GPU path writes."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _field(case):
+    rng = np.random.default_rng(7)
+    if case == "grf":
+        dims, bs = (48, 40, 70), 8
+        g = rng.normal(size=dims[::-1]).cumsum(0).cumsum(1).cumsum(2)
+    elif case == "outliers":
+        dims, bs = (33, 30, 61), 8
+        g = rng.normal(size=dims[::-1]).cumsum(2)
+        idx = rng.choice(g.size, size=25, replace=False)
+        g.reshape(-1)[idx] = rng.uniform(1e11, 1e12, size=25)
+    else:  # "exact": a candidate equal to a sample value (lossless regions)
+        dims, bs = (40, 36, 50), 8
+        g = rng.normal(size=dims[::-1]).cumsum(0)
+    return dims, bs, np.ascontiguousarray(g, dtype=np.float32).reshape(-1)  # [z][y][x] -> x fastest
+
+
+def _worker(rank, world, port, case, out_path):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    from paper_2408_05462_b200 import device as D, multi
+
+    dims, bs, flat = _field(case)
+    nx, ny, nz = dims
+    vals = torch.from_numpy(flat)
+    k = float(np.percentile(flat.astype(np.float64), 60))
+    if case == "exact":
+        k = float(flat[1234])
+    cands = [k]
+    slab = multi.slab_of(nz, bs, world, rank)
+    local = vals[slab.z_base * nx * ny: (slab.z_base + slab.nz_local) * nx * ny].cuda()
+    res = multi.build_archive_slab(local, dims, slab, cands, bs, loose_fraction=1e-3)
+    full = multi.assemble(res)
+    if rank == 0:
+        ref = D.build_archive(vals.cuda(), dims, cands, bs, loose_fraction=1e-3)
+        got = full.cpu().numpy().tobytes()
+        want = ref.blob[: ref.nbytes].cpu().numpy().tobytes()
+        with open(out_path, "w") as f:
+            codecs = "".join(str(int(c)) for c in sorted(set(ref.regions["codec_id"].tolist())))
+            f.write(f"{len(got)} {len(want)} {int(got == want)} {len(ref.regions)} {codecs}\n")
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("case", ["grf", "outliers", "exact"])
+def test_slab_archive_matches_single_gpu(tmp_path, world, case):
+    out = str(tmp_path / "res.txt")
+    mp.spawn(_worker, args=(world, _free_port(), case, out), nprocs=world, join=True)
+    ng, nw, same, nreg, codecs = open(out).read().split()
+    assert int(nreg) >= 1
+    if case == "outliers":
+        assert "2" in codecs  # escapes across slab boundaries
+    assert ng == nw and same == "1", (ng, nw)

@@ -161,3 +161,27 @@ def test_multi_rank_placement_gloo():
     assert out[0]["archive_offset"] == 0 and out[1]["archive_offset"] == 1000
     assert out[1]["tri_offset"] == 10 and out[1]["vert_offset"] == 7
     assert out[0]["archive_total"] == 1250 and out[1]["tri_total"] == 13
+
+
+@pytest.mark.parametrize("nz,bs,world", [(512, 32, 8), (65, 16, 2), (97, 32, 3), (33, 32, 4), (1024, 32, 7), (17, 8, 1)])
+def test_slab_geometry_partitions_planes_and_blocks(nz, bs, world):
+    """z-slabs: encode planes partition [0, nz); each rank holds
+    the plane below its first (Lorenzo z-1) and its blocks' ghost plane; the
+    block layers partition the block grid."""
+    from paper_2408_05462_b200 import multi
+
+    nbz = max(1, -(-(nz - 1) // bs))
+    covered, layers = [], []
+    for r in range(world):
+        s = multi.slab_of(nz, bs, world, r)
+        if s.zs == s.ze:
+            continue
+        covered.append((s.zs, s.ze))
+        layers.extend(range(s.bz0, s.bz1))
+        assert s.z_base <= max(s.zs - 1, 0) and s.ze <= s.z_base + s.nz_local
+        assert s.z_base + s.nz_local - 1 == min(s.bz1 * bs, nz - 1)  # ghost plane of the last layer
+        assert s.nz_stats - 1 == min(s.bz1 * bs, nz - 1) - s.zs
+    covered.sort()
+    assert covered[0][0] == 0 and covered[-1][1] == nz
+    assert all(a[1] == b[0] for a, b in zip(covered, covered[1:]))
+    assert layers == list(range(nbz))
