@@ -162,6 +162,10 @@ def build_archive_slab(vol_local: torch.Tensor, dims, slab: Slab, cands, bs, *, 
     tot = np.zeros(nreg + 1, dtype=np.uint32)
     for sh in shares:
         tot ^= sh.numpy().view(np.uint32)
+    # payload CRC of every region on every rank: zlib crc = shift(~0, len) ^ raw ^ ~0
+    plen = regions["block_nbytes"].astype(np.int64) - D.BLOCK_HEADER
+    regions["payload_crc"] = [L.chr_crc32_combine(0xFFFFFFFF, int(tot[1 + r]), int(plen[r])) ^ 0xFFFFFFFF
+                              for r in range(nreg)]
     if slab.rank == 0:
         hw = ws.get("dheaders", 8192 + 512 * (nreg + 2))
         D.check(L.chr_dcompress_headers(nx, ny, nz, tag, sp, int(bs), vmin, vmax, D._np_ptr(cands), m, rp, nreg,
@@ -180,3 +184,68 @@ def assemble(res: D.Compressed) -> torch.Tensor:
     t = buf.clone() if nccl else buf.cpu().to(torch.int32)
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return t.to(torch.uint8).to(buf.device) if not nccl else t
+
+
+def partition_regions(sizes, world: int) -> list[int]:
+    """Owner rank of every selected region: largest first onto the least
+    loaded rank (deterministic, identical on every rank)."""
+    load = [0] * world
+    owner = [0] * len(sizes)
+    for i in sorted(range(len(sizes)), key=lambda i: (-int(sizes[i]), i)):
+        r = min(range(world), key=lambda r: (load[r], r))
+        owner[i] = r
+        load[r] += int(sizes[i])
+    return owner
+
+
+@dataclass
+class SlabMesh:
+    """This rank's share of the merged mesh: triangles already carry global
+    vertex ids (reference first-touch numbering over all selected regions in
+    archive order); `regions` are indices into the selection, `tri_base` /
+    `vert_base` their rows in the merged mesh."""
+    verts: torch.Tensor
+    tris: torch.Tensor
+    regions: list
+    tri_base: list
+    vert_base: list
+    ntri_total: int
+    nvert_total: int
+
+
+def request_extract_slab(file_dev: torch.Tensor, regions: np.ndarray, k_index: int, k: float, spacing=(1.0, 1.0, 1.0),
+                         ws: D.Workspaces | None = None) -> SlabMesh:
+    """request(k) + marching_cubes over the ranks: the selected regions are
+    split by sample count, each rank decodes and meshes its own, and an
+    all-gather of per-region (triangles, vertices) places every region's rows
+    in the merged mesh (collective (3) of SURVEY §8(e))."""
+    ws = ws or D.Workspaces()
+    rank, world = dist.get_rank(), dist.get_world_size()
+    sel_idx = np.nonzero((regions["mask"] >> np.uint64(k_index)) & np.uint64(1))[0]
+    sel = regions[sel_idx]
+    ext = sel["extent"].astype(np.int64)
+    owner = partition_regions(np.prod(ext, axis=1), world)
+    mine = [i for i in range(len(sel)) if owner[i] == rank]
+    cnt = torch.zeros((len(sel), 2), dtype=torch.int64)
+    verts = torch.empty((0, 3), dtype=torch.float64, device=file_dev.device)
+    tris = torch.empty((0, 3), dtype=torch.int32, device=file_dev.device)
+    if mine:
+        s = sel[mine]
+        dec = D.dec_table(s["block_offset"] + D.BLOCK_HEADER, s["block_nbytes"] - D.BLOCK_HEADER, s["codec_id"],
+                          s["extent"], s["error_bound"], s["payload_crc"])
+        wins, _, status = D.decode(file_dev, dec, ws=ws)
+        if any(status):
+            raise ParameterError(f"decode failed: {status}")
+        mct = D.mc_table(dec["out_offset"], s["extent"], s["origin"] * np.asarray(spacing), spacing)
+        verts, tris, nt, nv = D.marching(wins, mct, k, ws=ws)
+        cnt[mine, 0] = torch.tensor(nt, dtype=torch.int64)
+        cnt[mine, 1] = torch.tensor(nv, dtype=torch.int64)
+    allc = torch.stack(_allgather(cnt)).sum(dim=0)  # [nsel, 2], each row from its owner
+    base = torch.cumsum(allc, dim=0) - allc
+    if mine:  # local vertex ids (merged over my regions) -> global ids
+        nt = allc[mine, 0]
+        loc_v = torch.cumsum(allc[mine, 1], 0) - allc[mine, 1]
+        shift = (base[mine, 1] - loc_v).to(tris.device)
+        tris = tris + torch.repeat_interleave(shift, nt.to(tris.device)).to(torch.int32).unsqueeze(1)
+    return SlabMesh(verts, tris, [int(i) for i in mine], [int(base[i, 0]) for i in mine],
+                    [int(base[i, 1]) for i in mine], int(allc[:, 0].sum()), int(allc[:, 1].sum()))

@@ -78,3 +78,63 @@ def test_slab_archive_matches_single_gpu(tmp_path, world, case):
     if case == "outliers":
         assert "2" in codecs  # escapes across slab boundaries
     assert ng == nw and same == "1", (ng, nw)
+
+
+def _mesh_worker(rank, world, port, out_path):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    from paper_2408_05462_b200 import device as D, multi
+
+    dims, bs, flat = _field("grf")
+    nx, ny, nz = dims
+    vals = torch.from_numpy(flat)
+    k = float(np.percentile(flat.astype(np.float64), 60))
+    slab = multi.slab_of(nz, bs, world, rank)
+    local = vals[slab.z_base * nx * ny: (slab.z_base + slab.nz_local) * nx * ny].cuda()
+    res = multi.build_archive_slab(local, dims, slab, [k], bs, loose_fraction=1e-3)
+    full = multi.assemble(res)
+    m = multi.request_extract_slab(full, res.regions, 0, k)
+    # gather every rank's rows into the merged mesh on rank 0
+    parts = [None] * world
+    dist.all_gather_object(parts, (m.tri_base, m.vert_base, m.regions, m.tris.cpu().numpy(), m.verts.cpu().numpy()))
+    if rank == 0:
+        T = np.zeros((m.ntri_total, 3), np.int32)
+        V = np.zeros((m.nvert_total, 3), np.float64)
+        bases = {}  # selected-region index -> (tri base, vert base) in the merged mesh
+        for tb, vb, regs, _, _ in parts:
+            bases.update({i: (x, y) for i, x, y in zip(regs, tb, vb)})
+        order = sorted(bases)
+        ends = {i: (bases[j][0], bases[j][1]) for i, j in zip(order, order[1:])}
+        ends[order[-1]] = (m.ntri_total, m.nvert_total)
+        for tb, vb, regs, t, v in parts:
+            to = vo = 0
+            for i in regs:  # a rank's rows are its regions in selection order
+                nt_i, nv_i = ends[i][0] - bases[i][0], ends[i][1] - bases[i][1]
+                T[bases[i][0]: bases[i][0] + nt_i] = t[to: to + nt_i]
+                V[bases[i][1]: bases[i][1] + nv_i] = v[vo: vo + nv_i]
+                to += nt_i
+                vo += nv_i
+        ref = D.build_archive(vals.cuda(), dims, [k], bs, loose_fraction=1e-3)
+        sel = ref.regions[(ref.regions["mask"] & np.uint64(1)) != 0]
+        dec = D.dec_table(sel["block_offset"] + D.BLOCK_HEADER, sel["block_nbytes"] - D.BLOCK_HEADER, sel["codec_id"],
+                          sel["extent"], sel["error_bound"], sel["payload_crc"])
+        wins, _, _ = D.decode(ref.blob, dec)
+        mct = D.mc_table(dec["out_offset"], sel["extent"], sel["origin"] * 1.0, (1.0, 1.0, 1.0))
+        rv, rt, _, _ = D.marching(wins, mct, k)
+        ok = np.array_equal(rt.cpu().numpy(), T) and np.array_equal(rv.cpu().numpy(), V)
+        with open(out_path, "w") as f:
+            f.write(f"{int(ok)} {len(T)} {len(V)} {len(sel)}\n")
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_slab_request_extract_matches_single_gpu(tmp_path, world):
+    out = str(tmp_path / "mesh.txt")
+    mp.spawn(_mesh_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    ok, nt, nv, nsel = open(out).read().split()
+    assert int(nsel) >= world and int(nt) > 0
+    assert ok == "1"
