@@ -238,6 +238,11 @@ int chr_dcompress_headers(int64_t nx, int64_t ny, int64_t nz, int source_dtype, 
                           chr_region_t *h_regions, int64_t n_regions, const uint32_t *h_raw_all,
                           void *d_workspace, size_t workspace_bytes, uint8_t *d_out, void *stream);
 
+/* 11. bulk copy by a small grid through UVA (pinned host <-> device):
+ *     keeps the copy engines free for the library's own small copies when
+ *     a caller pipelines its inputs/outputs.  16-byte aligned pointers. */
+int chr_sm_copy(void *dst, const void *src, uint64_t nbytes, int ctas, void *stream);
+
 /* 9. instrumentation: launch counter and opt-in per-kernel CUDA-event
  *    timing on the launching stream ("name count total_ms" lines). */
 void chr_prof_enable(int on);

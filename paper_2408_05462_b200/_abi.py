@@ -172,6 +172,8 @@ def lib():
         L.chr_dcompress_finish.restype = INT
         L.chr_dcompress_headers.argtypes = [I64, I64, I64, INT, P, I64, D, D, P, INT, P, I64, P, P, SZ, P, P]
         L.chr_dcompress_headers.restype = INT
+        L.chr_sm_copy.argtypes = [P, P, U64, INT, P]
+        L.chr_sm_copy.restype = INT
         L.chr_rle_encode_workspace_size.argtypes = [I64]
         L.chr_rle_encode_workspace_size.restype = SZ
         L.chr_rle_encode.argtypes = [P, I64, P, U64, P, SZ, P, P]
@@ -187,7 +189,7 @@ def lib():
 
 
 EXPORTS = [
-    "chr_rle_encode_workspace_size", "chr_rle_encode",
+    "chr_rle_encode_workspace_size", "chr_rle_encode", "chr_sm_copy",
     "chr_dcompress_workspace_size", "chr_dcompress_local", "chr_dcompress_finish", "chr_dcompress_headers",
     "chr_abi_version", "chr_status_string", "chr_num_blocks", "chr_stats", "chr_plan",
     "chr_compress_workspace_size", "chr_compress_capacity", "chr_compress",

@@ -92,3 +92,39 @@ extern "C" int chr_lorenzo_encode(const double *d_flat, int64_t nx, int64_t ny, 
     }
     return cudaGetLastError() == cudaSuccess ? CHR_OK : CHR_E_CUDA;
 }
+
+// ------------------------------------------------------------------ SM copy
+// Bulk host<->device copy through UVA-mapped pinned memory by a small grid
+// (no copy engine): lets a pipelined caller stream inputs/outputs over PCIe
+// while the library's own small DMA copies proceed unqueued.
+namespace chr {
+__global__ void __launch_bounds__(256) k_sm_copy(const uint8_t *__restrict__ src, uint8_t *__restrict__ dst,
+                                                 uint64_t n) {
+    const uint64_t n16 = n >> 4;
+    const uint4 *s = reinterpret_cast<const uint4 *>(src);
+    uint4 *d = reinterpret_cast<uint4 *>(dst);
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; i + 3 * stride < n16; i += 4 * stride) {  // 4 loads in flight per thread
+        const uint4 a = s[i], b = s[i + stride], c = s[i + 2 * stride], e = s[i + 3 * stride];
+        d[i] = a;
+        d[i + stride] = b;
+        d[i + 2 * stride] = c;
+        d[i + 3 * stride] = e;
+    }
+    for (; i < n16; i += stride) d[i] = s[i];
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < (n & 15)) dst[(n16 << 4) + t] = src[(n16 << 4) + t];
+}
+}  // namespace chr
+
+extern "C" int chr_sm_copy(void *dst, const void *src, uint64_t nbytes, int ctas, void *stream) {
+    if (nbytes == 0) return CHR_OK;
+    if (!dst || !src || (((uintptr_t)dst | (uintptr_t)src) & 15)) return CHR_E_PARAMETER;
+    cudaStream_t st = (cudaStream_t)stream;
+    {
+        CHR_PROF("k_sm_copy", st);
+        k_sm_copy<<<(unsigned)std::max(1, ctas), 256, 0, st>>>((const uint8_t *)src, (uint8_t *)dst, nbytes);
+    }
+    return cudaGetLastError() == cudaSuccess ? CHR_OK : CHR_E_CUDA;
+}

@@ -238,7 +238,7 @@ def mc_table(grid_offset, dims, origin, spacing) -> np.ndarray:
     return t
 
 
-def marching(grids: torch.Tensor, descs, k: float, ws: Workspaces | None = None):
+def marching(grids: torch.Tensor, descs, k: float, ws: Workspaces | None = None, reuse_outputs: bool = False):
     """Marching cubes over several f64 windows of `grids`, merged.
 
     ``descs``: a ``_abi.MCGRID_DT`` table (:func:`mc_table`) or a list of
@@ -266,8 +266,12 @@ def marching(grids: torch.Tensor, descs, k: float, ws: Workspaces | None = None)
     tv = ctypes.c_int64(0)
     check(L.chr_mc_count(ptr(grids), gp, n, float(k), ptr(work), work.numel(), _abi.aptr(ntri), _abi.aptr(nvert),
                          ctypes.byref(tt), ctypes.byref(tv), stream_ptr()), "chr_mc_count")
-    verts = torch.empty((tv.value, 3), dtype=torch.float64, device=dev)
-    tris = torch.empty((tt.value, 3), dtype=torch.int32, device=dev)
+    if reuse_outputs:  # outputs in the workspace: valid until the next call with this workspace
+        verts = ws.get("mc_verts", 24 * tv.value, dtype=torch.float64)[: tv.value * 3].view(tv.value, 3)
+        tris = ws.get("mc_tris", 12 * tt.value, dtype=torch.int32)[: tt.value * 3].view(tt.value, 3)
+    else:
+        verts = torch.empty((tv.value, 3), dtype=torch.float64, device=dev)
+        tris = torch.empty((tt.value, 3), dtype=torch.int32, device=dev)
     check(L.chr_mc_emit(ptr(grids), gp, n, float(k), ptr(work), work.numel(), ptr(verts), ptr(tris),
                         stream_ptr()), "chr_mc_emit")
     return verts, tris, ntri.tolist(), nvert.tolist()
