@@ -238,6 +238,22 @@ int chr_dcompress_headers(int64_t nx, int64_t ny, int64_t nz, int source_dtype, 
                           chr_region_t *h_regions, int64_t n_regions, const uint32_t *h_raw_all,
                           void *d_workspace, size_t workspace_bytes, uint8_t *d_out, void *stream);
 
+/* 12. fused request + extract: the decoder also writes each window's
+ *     inside mask (bit y*nx + x of plane z's ceil(nx*ny/32) words is
+ *     v >= iso; windows back to back, chr_mask_words() words in all) and
+ *     the marching cubes passes read those masks instead of recomputing
+ *     them from the f64 windows (same grids, same order). */
+uint64_t chr_mask_words(const int32_t *h_dims, int64_t n);
+int chr_decode_regions_mask(const uint8_t *d_blob, const chr_dec_region_t *h_regions, int64_t n,
+                            double *d_out, void *d_workspace, size_t workspace_bytes, int32_t *h_status,
+                            double iso, uint32_t *d_masks, void *stream);
+int chr_mc_count_masked(const double *d_grids, const chr_mc_grid_t *h_grids, int64_t n, double k,
+                        const uint32_t *d_masks, void *d_workspace, size_t workspace_bytes, int64_t *h_ntri,
+                        int64_t *h_nvert, int64_t *h_total_tri, int64_t *h_total_vert, void *stream);
+int chr_mc_emit_masked(const double *d_grids, const chr_mc_grid_t *h_grids, int64_t n, double k,
+                       const uint32_t *d_masks, void *d_workspace, size_t workspace_bytes, double *d_verts,
+                       int32_t *d_tris, void *stream);
+
 /* 11. bulk copy by a small grid through UVA (pinned host <-> device):
  *     keeps the copy engines free for the library's own small copies when
  *     a caller pipelines its inputs/outputs.  16-byte aligned pointers. */

@@ -172,6 +172,14 @@ def lib():
         L.chr_dcompress_finish.restype = INT
         L.chr_dcompress_headers.argtypes = [I64, I64, I64, INT, P, I64, D, D, P, INT, P, I64, P, P, SZ, P, P]
         L.chr_dcompress_headers.restype = INT
+        L.chr_mask_words.argtypes = [P, I64]
+        L.chr_mask_words.restype = U64
+        L.chr_decode_regions_mask.argtypes = [P, P, I64, P, P, SZ, P, D, P, P]
+        L.chr_decode_regions_mask.restype = INT
+        L.chr_mc_count_masked.argtypes = [P, P, I64, D, P, P, SZ, P, P, P, P, P]
+        L.chr_mc_count_masked.restype = INT
+        L.chr_mc_emit_masked.argtypes = [P, P, I64, D, P, P, SZ, P, P, P]
+        L.chr_mc_emit_masked.restype = INT
         L.chr_sm_copy.argtypes = [P, P, U64, INT, P]
         L.chr_sm_copy.restype = INT
         L.chr_rle_encode_workspace_size.argtypes = [I64]
@@ -190,6 +198,7 @@ def lib():
 
 EXPORTS = [
     "chr_rle_encode_workspace_size", "chr_rle_encode", "chr_sm_copy",
+    "chr_mask_words", "chr_decode_regions_mask", "chr_mc_count_masked", "chr_mc_emit_masked",
     "chr_dcompress_workspace_size", "chr_dcompress_local", "chr_dcompress_finish", "chr_dcompress_headers",
     "chr_abi_version", "chr_status_string", "chr_num_blocks", "chr_stats", "chr_plan",
     "chr_compress_workspace_size", "chr_compress_capacity", "chr_compress",

@@ -76,6 +76,8 @@ struct DecReg {
     int64_t tile_base, ntiles;
     int64_t sp_base;               // segment index: ez * tny entries
     int64_t face_base, face_n;     // int64 faces per tile: ex * (btz + 1 + bty)
+    int64_t mask_off;              // inside-mask words (v >= iso), plane-linear bits (optional output)
+    int32_t pw, pad3;              // mask words per plane
     // device-computed
     uint64_t tok_start;            // absolute offset of the token stream
     int64_t nesc;
@@ -1090,7 +1092,8 @@ __global__ void __launch_bounds__(256) k_band(const DecReg *__restrict__ regs, c
                                               const int64_t *__restrict__ esc_sp, const int64_t *__restrict__ pos64,
                                               int64_t *__restrict__ faces,
                                               int32_t *__restrict__ tflag, unsigned long long *__restrict__ ticket,
-                                              const int32_t *__restrict__ order, double *__restrict__ out) {
+                                              const int32_t *__restrict__ order, double *__restrict__ out,
+                                              uint32_t *__restrict__ mask, double iso) {
     extern __shared__ __align__(16) int64_t Q[];  // [nzv][nyv][rs]
     __shared__ int64_t ucnt[BDF];                 // dF[nzv][ex]
     __shared__ int64_t s_lo[BSEGM], s_hi[BSEGM], s_ub[BSEGM], s_off[BSEGM];
@@ -1317,7 +1320,45 @@ __global__ void __launch_bounds__(256) k_band(const DecReg *__restrict__ regs, c
         }
     }
     release(2);
-    for (int t = tid; t < L; t += 256) recon_col(t, c > 0 ? __ldcg(Ip + t) : 0);
+    if (!mask) {
+        for (int t = tid; t < L; t += 256) recon_col(t, c > 0 ? __ldcg(Ip + t) : 0);
+    } else {
+        // the same reconstruction in warp-uniform 32-column steps, each plane's
+        // inside bits (v >= iso) ballot-packed into the mask (plane-linear bit
+        // y * ex + x; words shared with the band above/below are ORed)
+        uint32_t *mp = mask + R.mask_off;
+        const int64_t bit0 = (int64_t)y0 * ex;
+        for (int t0 = warp * 32; t0 < L; t0 += 256) {
+            const int t = t0 + lane;
+            const bool act = t < L;
+            int xx = 0, qi = 0;
+            int64_t fz = 0;
+            if (act) {
+                qi = qidx(t, xx);
+                fz = c > 0 ? __ldcg(Ip + t) : 0;
+            }
+            const int64_t wb = bit0 + t0;
+            const int sh = (int)(wb & 31);
+            uint32_t *mw = mp + (wb >> 5);
+            for (int j = 0; j < nzv; ++j) {
+                double v = 0.0;
+                if (act) {
+                    v = (double)(Q[j * PL + qi] + (b > 0 ? dF[j * ex + xx] : 0) + fz) * twoe;
+                    __stcs(obase + j * zstride + t, v);
+                }
+                const uint32_t bal = __ballot_sync(0xFFFFFFFFu, act && v >= iso);
+                if (lane == 0) {
+                    uint32_t *w = mw + (int64_t)(z0 + j) * R.pw;
+                    if (nb == 1) {  // whole planes: this warp owns the word
+                        *w = bal;
+                    } else if (bal) {  // band edges share words with the band above / below
+                        atomicOr(w, bal << sh);
+                        if (sh && (bal >> (32 - sh))) atomicOr(w + 1, bal >> (32 - sh));
+                    }
+                }
+            }
+        }
+    }
     // ---- codec 2: escaped samples keep their f64 value (raster order rank)
     if (R.codec == 2 && R.nesc > 0) {
         __syncthreads();
@@ -1336,7 +1377,14 @@ __global__ void __launch_bounds__(256) k_band(const DecReg *__restrict__ regs, c
                     const uint8_t *src = ev + 8 * (rank + __popc(bal & lt));
                     uint64_t bits = 0;
                     for (int k = 0; k < 8; ++k) bits |= (uint64_t)src[k] << (8 * k);
-                    obase[j * zstride + p] = __longlong_as_double((long long)bits);
+                    const double v = __longlong_as_double((long long)bits);
+                    obase[j * zstride + p] = v;
+                    if (mask) {  // the escaped value decides its inside bit
+                        const int64_t pb = (int64_t)y0 * ex + p;
+                        uint32_t *w = mask + R.mask_off + (int64_t)(z0 + j) * R.pw + (pb >> 5);
+                        if (v >= iso) atomicOr(w, 1u << (pb & 31));
+                        else atomicAnd(w, ~(1u << (pb & 31)));
+                    }
                 }
                 rank += __popc(bal);
             }
@@ -1344,10 +1392,29 @@ __global__ void __launch_bounds__(256) k_band(const DecReg *__restrict__ regs, c
     }
 }
 
+// inside masks of the regions k_band did not reconstruct (verbatim codecs,
+// generic path), from their f64 windows: warp per 32-bit word
+__global__ void __launch_bounds__(256) k_mask_rest(const DecReg *__restrict__ regs, int64_t r0,
+                                                   const double *__restrict__ out, uint32_t *__restrict__ mask,
+                                                   double iso) {
+    const DecReg &R = regs[r0 + blockIdx.y];
+    const bool band = (R.codec == 1 || R.codec == 2) && !R.slow;
+    if (band || R.err) return;
+    const int lane = threadIdx.x & 31;
+    const int64_t plane = (int64_t)R.ex * R.ey, words = (int64_t)R.pw * R.ez;
+    for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < words;
+         w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t z = w / R.pw, t = (w - z * R.pw) * 32 + lane;
+        const bool in = t < plane && out[R.out_off + z * plane + t] >= iso;
+        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, in);
+        if (lane == 0) mask[R.mask_off + w] = bal;
+    }
+}
+
 // ------------------------------------------------------------------ host
 struct DecPlan {
     std::vector<DecReg> regs;
-    int64_t nchunks = 0, nseg = 0, nitems = 0, ncarry = 0, ntiles = 0, nsp = 0, nface = 0;
+    int64_t nchunks = 0, nseg = 0, nitems = 0, ncarry = 0, ntiles = 0, nsp = 0, nface = 0, nmask = 0;
     int max_rows_ex = 0;
     size_t ws = 0;
     DecReg *d_regs;
@@ -1425,6 +1492,9 @@ static bool dec_build(const chr_dec_region_t *h, int64_t n, uintptr_t blob, DecP
         R.n = (int64_t)R.ex * R.ey * R.ez;
         R.out_off = h[i].out_offset;
         R.rows = dec_rows_for(R.ex);
+        R.pw = (int32_t)ceil_div((int64_t)R.ex * R.ey, 32);
+        R.mask_off = pl.nmask;
+        pl.nmask += (int64_t)R.pw * R.ez;
         if (R.rows < 1) return false;
         R.nyt = (int32_t)ceil_div(R.ey, R.rows);
         // chunks: 4 KiB over [16-aligned(poff), poff + plen)
@@ -1534,9 +1604,31 @@ extern "C" size_t chr_decode_workspace_size(const chr_dec_region_t *h, int64_t n
     return pl.ws;
 }
 
+static int decode_impl(const uint8_t *d_blob, const chr_dec_region_t *h, int64_t n, double *d_out, void *d_ws,
+                       size_t ws_bytes, int32_t *h_status, double iso, uint32_t *d_mask, void *stream);
+
 extern "C" int chr_decode_regions(const uint8_t *d_blob, const chr_dec_region_t *h, int64_t n,
                                   double *d_out, void *d_ws, size_t ws_bytes, int32_t *h_status,
                                   void *stream) {
+    return decode_impl(d_blob, h, n, d_out, d_ws, ws_bytes, h_status, 0.0, nullptr, stream);
+}
+
+extern "C" uint64_t chr_mask_words(const int32_t *h_dims, int64_t n) {
+    uint64_t w = 0;
+    for (int64_t i = 0; i < n; ++i)
+        w += (uint64_t)ceil_div((int64_t)h_dims[3 * i] * h_dims[3 * i + 1], 32) * (uint64_t)h_dims[3 * i + 2];
+    return w;
+}
+
+extern "C" int chr_decode_regions_mask(const uint8_t *d_blob, const chr_dec_region_t *h, int64_t n, double *d_out,
+                                       void *d_ws, size_t ws_bytes, int32_t *h_status, double iso,
+                                       uint32_t *d_mask, void *stream) {
+    if (!d_mask) return CHR_E_PARAMETER;
+    return decode_impl(d_blob, h, n, d_out, d_ws, ws_bytes, h_status, iso, d_mask, stream);
+}
+
+static int decode_impl(const uint8_t *d_blob, const chr_dec_region_t *h, int64_t n, double *d_out, void *d_ws,
+                       size_t ws_bytes, int32_t *h_status, double iso, uint32_t *d_mask, void *stream) {
     if (n == 0) return CHR_OK;
     if (!d_blob || !h || n < 0 || !d_out) return CHR_E_PARAMETER;
     cudaStream_t st = (cudaStream_t)stream;
@@ -1559,6 +1651,7 @@ extern "C" int chr_decode_regions(const uint8_t *d_blob, const chr_dec_region_t 
     CHR_CUDA_TRY(cudaMemsetAsync(pl.ticket, 0, sizeof(unsigned long long), st));
     CHR_CUDA_TRY(cudaMemsetAsync(pl.ticket3, 0, sizeof(unsigned long long), st));
     CHR_CUDA_TRY(cudaMemsetAsync(pl.any_slow, 0, sizeof(int32_t), st));
+    if (d_mask) CHR_CUDA_TRY(cudaMemsetAsync(d_mask, 0, sizeof(uint32_t) * (pl.nmask + 8), st));
     CHR_CUDA_TRY(cudaMemsetAsync(pl.tflag, 0, sizeof(int32_t) * (pl.ntiles + 1), st));
     int rc = crc_launch(d_blob, pl.segs, n, total_sc, pl.seg_raw, st);
     if (rc) return rc;
@@ -1608,7 +1701,7 @@ extern "C" int chr_decode_regions(const uint8_t *d_blob, const chr_dec_region_t 
             CHR_PROF("k_band", st);
             k_band<<<(unsigned)pl.ntiles, 256, smem, st>>>(pl.d_regs, pl.tile_reg, d_blob, pl.sp_byte, pl.sp_skip,
                                                            pl.esc_sp, pl.pos64, pl.faces, pl.tflag, pl.ticket3,
-                                                           pl.order, d_out);
+                                                           pl.order, d_out, d_mask, iso);
         }
     }
     // ---- generic path (non-canonical streams, rows wider than a band tile):
@@ -1654,6 +1747,12 @@ extern "C" int chr_decode_regions(const uint8_t *d_blob, const chr_dec_region_t 
             k_verbatim<<<g, 256, 0, st>>>(pl.d_regs, r0, d_blob, d_out);
         }
     }
+    if (d_mask)  // regions k_band did not reconstruct
+        for (int64_t r0 = 0; r0 < n; r0 += 65535) {
+            dim3 g(16, (unsigned)std::min<int64_t>(65535, n - r0));
+            CHR_PROF("k_mask_rest", st);
+            k_mask_rest<<<g, 256, 0, st>>>(pl.d_regs, r0, d_out, d_mask, iso);
+        }
     CHR_CUDA_TRY(cudaGetLastError());
     CHR_CUDA_TRY(cudaMemcpyAsync(pl.regs.data(), pl.d_regs, sizeof(DecReg) * n, cudaMemcpyDeviceToHost, st));
     CHR_CUDA_TRY(cudaStreamSynchronize(st));

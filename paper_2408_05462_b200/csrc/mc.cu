@@ -834,9 +834,35 @@ extern "C" size_t chr_mc_workspace_size(const chr_mc_grid_t *h, int64_t n) {
     return pl.ws;
 }
 
+static int mc_count_impl(const double *d_grids, const chr_mc_grid_t *h, int64_t n, double k, const uint32_t *d_masks,
+                         void *d_ws, size_t ws_bytes, int64_t *h_ntri, int64_t *h_nvert, int64_t *h_total_tri,
+                         int64_t *h_total_vert, void *stream);
+static int mc_emit_impl(const double *d_grids, const chr_mc_grid_t *h, int64_t n, double k, const uint32_t *d_masks,
+                        void *d_ws, size_t ws_bytes, double *d_verts, int32_t *d_tris, void *stream);
+
 extern "C" int chr_mc_count(const double *d_grids, const chr_mc_grid_t *h, int64_t n, double k, void *d_ws,
                             size_t ws_bytes, int64_t *h_ntri, int64_t *h_nvert, int64_t *h_total_tri,
                             int64_t *h_total_vert, void *stream) {
+    return mc_count_impl(d_grids, h, n, k, nullptr, d_ws, ws_bytes, h_ntri, h_nvert, h_total_tri, h_total_vert,
+                         stream);
+}
+extern "C" int chr_mc_count_masked(const double *d_grids, const chr_mc_grid_t *h, int64_t n, double k,
+                                   const uint32_t *d_masks, void *d_ws, size_t ws_bytes, int64_t *h_ntri,
+                                   int64_t *h_nvert, int64_t *h_total_tri, int64_t *h_total_vert, void *stream) {
+    if (!d_masks) return CHR_E_PARAMETER;
+    return mc_count_impl(d_grids, h, n, k, d_masks, d_ws, ws_bytes, h_ntri, h_nvert, h_total_tri, h_total_vert,
+                         stream);
+}
+extern "C" int chr_mc_emit_masked(const double *d_grids, const chr_mc_grid_t *h, int64_t n, double k,
+                                  const uint32_t *d_masks, void *d_ws, size_t ws_bytes, double *d_verts,
+                                  int32_t *d_tris, void *stream) {
+    if (!d_masks) return CHR_E_PARAMETER;
+    return mc_emit_impl(d_grids, h, n, k, d_masks, d_ws, ws_bytes, d_verts, d_tris, stream);
+}
+
+static int mc_count_impl(const double *d_grids, const chr_mc_grid_t *h, int64_t n, double k, const uint32_t *d_masks,
+                         void *d_ws, size_t ws_bytes, int64_t *h_ntri, int64_t *h_nvert, int64_t *h_total_tri,
+                         int64_t *h_total_vert, void *stream) {
     if (n == 0) {
         if (h_total_tri) *h_total_tri = 0;
         if (h_total_vert) *h_total_vert = 0;
@@ -856,14 +882,17 @@ extern "C" int chr_mc_count(const double *d_grids, const chr_mc_grid_t *h, int64
         CHR_PROF("k_mc_fill_map", st);
         k_mc_fill_map<<<(unsigned)n, 256, 0, st>>>(pl.d_grids, n, pl.item_grid, pl.chunk_grid, pl.mask_grid);
     }
-    CHR_CUDA_TRY(cudaMemsetAsync(pl.mask + pl.nmask_words, 0, 8 * sizeof(uint32_t), st));
-    if (pl.nmask_items > 0) {
-        CHR_PROF("k_mc_mask", st);
-        k_mc_mask<<<(unsigned)pl.nmask_items, 256, 0, st>>>(d_grids, pl.d_grids, pl.mask_grid, k, pl.mask);
+    const uint32_t *masks = d_masks ? d_masks : pl.mask;  // caller's masks (decoder output) or our own
+    if (!d_masks) {
+        CHR_CUDA_TRY(cudaMemsetAsync(pl.mask + pl.nmask_words, 0, 8 * sizeof(uint32_t), st));
+        if (pl.nmask_items > 0) {
+            CHR_PROF("k_mc_mask", st);
+            k_mc_mask<<<(unsigned)pl.nmask_items, 256, 0, st>>>(d_grids, pl.d_grids, pl.mask_grid, k, pl.mask);
+        }
     }
     if (pl.nchunks > 0) {
         CHR_PROF("k_mc_count3", st);
-        k_mc_count3<<<(unsigned)pl.nchunks, 256, 0, st>>>(pl.d_grids, pl.chunk_grid, T, pl.mask, pl.cnt);
+        k_mc_count3<<<(unsigned)pl.nchunks, 256, 0, st>>>(pl.d_grids, pl.chunk_grid, T, masks, pl.cnt);
     }
     {
         CHR_PROF("k_mc_reduce", st);
@@ -898,6 +927,11 @@ extern "C" int chr_mc_count(const double *d_grids, const chr_mc_grid_t *h, int64
 
 extern "C" int chr_mc_emit(const double *d_grids, const chr_mc_grid_t *h, int64_t n, double k, void *d_ws,
                            size_t ws_bytes, double *d_verts, int32_t *d_tris, void *stream) {
+    return mc_emit_impl(d_grids, h, n, k, nullptr, d_ws, ws_bytes, d_verts, d_tris, stream);
+}
+
+static int mc_emit_impl(const double *d_grids, const chr_mc_grid_t *h, int64_t n, double k, const uint32_t *d_masks,
+                        void *d_ws, size_t ws_bytes, double *d_verts, int32_t *d_tris, void *stream) {
     if (n == 0) return CHR_OK;
     if (!d_grids || !h || n < 0) return CHR_E_PARAMETER;
     cudaStream_t st = (cudaStream_t)stream;
@@ -911,7 +945,8 @@ extern "C" int chr_mc_emit(const double *d_grids, const chr_mc_grid_t *h, int64_
         {
             CHR_PROF("k_mc_emit2", st);
             k_mc_emit2<<<(unsigned)pl.nitems, EW * 32, 0, st>>>(d_grids, pl.d_grids, pl.item_grid, k, T, pl.base,
-                                                                 pl.cnt, pl.mask, d_verts, d_tris);
+                                                                 pl.cnt, d_masks ? d_masks : pl.mask, d_verts,
+                                                                 d_tris);
         }
     CHR_CUDA_TRY(cudaGetLastError());
     CHR_CUDA_TRY(cudaStreamSynchronize(st));

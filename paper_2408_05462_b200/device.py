@@ -200,13 +200,16 @@ def dec_table(payload_offset, payload_nbytes, codec, dims, e, crc) -> np.ndarray
     return t
 
 
-def decode(blob: torch.Tensor, sel, ws: Workspaces | None = None, out: torch.Tensor | None = None):
+def decode(blob: torch.Tensor, sel, ws: Workspaces | None = None, out: torch.Tensor | None = None,
+           iso: float | None = None):
     """Decode CompressedBlocks of `blob` (device uint8).
 
     ``sel``: a ``_abi.DEC_DT`` table (see :func:`dec_table`) or a list of
     (payload_offset, payload_nbytes, codec_id, (ex,ey,ez), e, crc).
     Returns (f64 device tensor of all windows concatenated, element offsets,
-    per-region status codes)."""
+    per-region status codes).  With ``iso`` the decoder also writes every
+    window's inside mask (v >= iso) into ``ws`` ("decode_mask"), which
+    :func:`marching` takes as ``masks`` (fused request + extract)."""
     ws = ws or _DEFAULT_WS
     L = lib()
     if not isinstance(sel, np.ndarray):
@@ -221,8 +224,15 @@ def decode(blob: torch.Tensor, sel, ws: Workspaces | None = None, out: torch.Ten
         sp = _abi.aptr(sel)
         wsz = L.chr_decode_workspace_size(sp, n)
         work = ws.get("decode", wsz)
-        rc = L.chr_decode_regions(ptr(blob), sp, n, ptr(out), ptr(work), work.numel(), _abi.aptr(status),
-                                  stream_ptr())
+        if iso is None:
+            rc = L.chr_decode_regions(ptr(blob), sp, n, ptr(out), ptr(work), work.numel(), _abi.aptr(status),
+                                      stream_ptr())
+        else:
+            dims = np.ascontiguousarray(sel["dims"], dtype=np.int32)
+            mw = int(L.chr_mask_words(_np_ptr(dims), n))
+            mask = ws.get("decode_mask", 4 * (mw + 8), torch.int32)
+            rc = L.chr_decode_regions_mask(ptr(blob), sp, n, ptr(out), ptr(work), work.numel(),
+                                           _abi.aptr(status), float(iso), ptr(mask), stream_ptr())
         if rc not in (_abi.CHR_OK, _abi.CHR_E_CORRUPT, _abi.CHR_E_UNSUPPORTED_CODEC):
             check(rc, "chr_decode_regions")
     return out, [int(v) for v in sel["out_offset"]] if n else [], [int(v) for v in status[:n]]
@@ -238,7 +248,8 @@ def mc_table(grid_offset, dims, origin, spacing) -> np.ndarray:
     return t
 
 
-def marching(grids: torch.Tensor, descs, k: float, ws: Workspaces | None = None, reuse_outputs: bool = False):
+def marching(grids: torch.Tensor, descs, k: float, ws: Workspaces | None = None, reuse_outputs: bool = False,
+             masks: torch.Tensor | None = None):
     """Marching cubes over several f64 windows of `grids`, merged.
 
     ``descs``: a ``_abi.MCGRID_DT`` table (:func:`mc_table`) or a list of
@@ -264,16 +275,25 @@ def marching(grids: torch.Tensor, descs, k: float, ws: Workspaces | None = None,
     nvert = np.zeros(n, dtype=np.int64)
     tt = ctypes.c_int64(0)
     tv = ctypes.c_int64(0)
-    check(L.chr_mc_count(ptr(grids), gp, n, float(k), ptr(work), work.numel(), _abi.aptr(ntri), _abi.aptr(nvert),
-                         ctypes.byref(tt), ctypes.byref(tv), stream_ptr()), "chr_mc_count")
+    if masks is None:
+        check(L.chr_mc_count(ptr(grids), gp, n, float(k), ptr(work), work.numel(), _abi.aptr(ntri),
+                             _abi.aptr(nvert), ctypes.byref(tt), ctypes.byref(tv), stream_ptr()), "chr_mc_count")
+    else:  # inside masks from decode(..., iso=k) of the same windows, same order
+        check(L.chr_mc_count_masked(ptr(grids), gp, n, float(k), ptr(masks), ptr(work), work.numel(),
+                                    _abi.aptr(ntri), _abi.aptr(nvert), ctypes.byref(tt), ctypes.byref(tv),
+                                    stream_ptr()), "chr_mc_count_masked")
     if reuse_outputs:  # outputs in the workspace: valid until the next call with this workspace
         verts = ws.get("mc_verts", 24 * tv.value, dtype=torch.float64)[: tv.value * 3].view(tv.value, 3)
         tris = ws.get("mc_tris", 12 * tt.value, dtype=torch.int32)[: tt.value * 3].view(tt.value, 3)
     else:
         verts = torch.empty((tv.value, 3), dtype=torch.float64, device=dev)
         tris = torch.empty((tt.value, 3), dtype=torch.int32, device=dev)
-    check(L.chr_mc_emit(ptr(grids), gp, n, float(k), ptr(work), work.numel(), ptr(verts), ptr(tris),
-                        stream_ptr()), "chr_mc_emit")
+    if masks is None:
+        check(L.chr_mc_emit(ptr(grids), gp, n, float(k), ptr(work), work.numel(), ptr(verts), ptr(tris),
+                            stream_ptr()), "chr_mc_emit")
+    else:
+        check(L.chr_mc_emit_masked(ptr(grids), gp, n, float(k), ptr(masks), ptr(work), work.numel(), ptr(verts),
+                                   ptr(tris), stream_ptr()), "chr_mc_emit_masked")
     return verts, tris, ntri.tolist(), nvert.tolist()
 
 

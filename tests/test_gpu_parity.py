@@ -374,3 +374,36 @@ def test_kernel_seam_lorenzo_decode(dims):
     got = device.lorenzo_decode(torch.from_numpy(q), torch.from_numpy(esc.astype(np.uint8)),
                                 torch.from_numpy(escv), e, nx, ny, nz)
     assert np.array_equal(got.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("name,n", [("c3", 96), ("c2", 80), ("c1", 64)])
+def test_fused_request_extract_masks(name, n):
+    """decode(..., iso=k) writes the windows' inside masks; marching cubes on
+    those masks gives exactly the mesh of the unfused path, and every mask
+    bit equals (window value >= k)."""
+    import torch
+
+    vals, dims, bs, cands, r = synth.make_config(name, device="cuda", n=n)
+    res = device.build_archive(vals, dims, cands, bs, loose_fraction=r)
+    regs = res.regions
+    sel = regs[(regs["mask"] & np.uint64(1)) != 0]
+    dec = device.dec_table(sel["block_offset"] + device.BLOCK_HEADER, sel["block_nbytes"] - device.BLOCK_HEADER,
+                           sel["codec_id"], sel["extent"], sel["error_bound"], sel["payload_crc"])
+    ws = device.Workspaces()
+    k = cands[0]
+    wins, offs, st = device.decode(res.blob, dec, ws=ws, iso=k)
+    assert not any(st)
+    masks = ws.get("decode_mask", 4, torch.int32).clone()
+    w = wins.cpu().numpy()
+    mw = masks.cpu().numpy().view(np.uint32)
+    base = 0
+    for i, (ex, ey, ez) in enumerate(sel["extent"].tolist()):
+        pw = -(-(ex * ey) // 32)
+        win = w[offs[i]: offs[i] + ex * ey * ez].reshape(ez, ex * ey)
+        bits = np.unpackbits(mw[base: base + pw * ez].view(np.uint8), bitorder="little").reshape(ez, pw * 32)
+        assert np.array_equal(bits[:, : ex * ey].astype(bool), win >= k), i
+        base += pw * ez
+    mct = device.mc_table(dec["out_offset"], sel["extent"], sel["origin"] * 1.0, (1.0, 1.0, 1.0))
+    v0, t0, _, _ = device.marching(wins, mct, k)
+    v1, t1, _, _ = device.marching(wins, mct, k, masks=masks)
+    assert torch.equal(t0, t1) and torch.equal(v0, v1)
