@@ -38,6 +38,8 @@
 namespace chr {
 
 constexpr int TX = 64, TY = 8, ZC = 16, NW = TY + 1;
+constexpr int QB_T = 256, QB_SPT = 4, QB_CAP = QB_T * QB_SPT;  // k_quant_band: threads, slots, samples
+constexpr int CSPLIT = 4;  // k_summarize / k_emit_q CTAs per scan chunk (more warps in flight)
 constexpr int64_t CH = 1024;  // pieces per scan chunk
 
 struct RegDev {
@@ -56,6 +58,7 @@ struct RegDev {
     int64_t s_off, n_win;
     int32_t zhalo, last;
     TokSeg pre;
+    int32_t qband, rb;            // quantiser items are full-row bands of rb rows (k_quant_band)
     // results
     int32_t codec, f32ok;
     int64_t tok_len, nesc, payload_len;
@@ -176,6 +179,7 @@ __global__ void __launch_bounds__(NW * 32, 4) k_quant(const T *__restrict__ vol,
     const int ri = __ldg(item_reg + item);
     coop_copy(&R, regs + ri);
     __syncthreads();
+    if (R.qband) return;  // k_quant_band's item
     const int64_t NX = P->NX, NY = P->NY, plane = NX * NY;
     const int64_t local = item - R.item_base;
     const int xt = (int)(local % R.ntx);
@@ -271,6 +275,112 @@ __global__ void __launch_bounds__(NW * 32, 4) k_quant(const T *__restrict__ vol,
     if (chk32 && __any_sync(0xFFFFFFFFu, inexact) && lane == 0) atomicOr(&regs[ri].f32bad, 1);
 }
 
+// Quantiser pass, full-row bands: CTA = rb whole rows (+ the halo row y0-1)
+// x 16 planes of one window, the band-plane's samples flattened over the
+// threads (QB_SPT slots each) so narrow windows (33 = 32k+1 columns) keep
+// every lane busy; D(z) = u(z) - u(z-1) per slot, q from the band-plane's D
+// in shared memory (x-1 = slot i-1, y-1 = slot i-ex).
+template <typename T>
+__global__ void __launch_bounds__(QB_T, 4) k_quant_band(const T *__restrict__ vol, const EncParams *__restrict__ P,
+                                                    RegDev *__restrict__ regs, const int32_t *__restrict__ item_reg,
+                                                    uint32_t *__restrict__ qz, uint32_t *__restrict__ escbits) {
+    __shared__ int32_t sD[2][QB_CAP];
+    __shared__ RegDev R;
+    const int64_t item = blockIdx.x;
+    const int ri = __ldg(item_reg + item);
+    coop_copy(&R, regs + ri);
+    __syncthreads();
+    if (!R.qband) return;
+    const int64_t NX = P->NX, NY = P->NY, plane = NX * NY;
+    const int64_t local = item - R.item_base;
+    const int yt = (int)(local % R.nty), zc = (int)(local / R.nty);
+    const int ex = R.ex, y0 = yt * R.rb, rows = min(R.rb, R.ey - y0);
+    const int z0 = zc * ZC, z1 = min(z0 + ZC, R.ez);
+    const int span = (rows + 1) * ex;  // halo row first
+    const bool quant = R.mode == 0;
+    const Quant Q = make_quant(R.e);
+    const bool chk32 = sizeof(T) == 8 && P->src_dtype == CHR_F32;
+    const int tid = threadIdx.x;
+    int xs[QB_SPT], ys[QB_SPT];
+    bool ok[QB_SPT], own[QB_SPT];
+    const T *ptr[QB_SPT];
+#pragma unroll
+    for (int k = 0; k < QB_SPT; ++k) {
+        const int i = tid + QB_T * k;
+        const int yy = i / ex;
+        xs[k] = i - yy * ex;
+        ys[k] = y0 - 1 + yy;
+        ok[k] = i < span && ys[k] >= 0;
+        own[k] = i < span && yy >= 1;
+        ptr[k] = vol + ((int64_t)(R.oz + z0) * NY + (R.oy + (ok[k] ? ys[k] : 0))) * NX + R.ox + xs[k];
+    }
+    int32_t up[QB_SPT];
+#pragma unroll
+    for (int k = 0; k < QB_SPT; ++k) up[k] = 0;
+    auto quant_slots = [&](const T (&v)[QB_SPT], int32_t (&u)[QB_SPT], bool (&e)[QB_SPT]) {
+        bool fast = true;
+#pragma unroll
+        for (int k = 0; k < QB_SPT; ++k) {
+            u[k] = 0;
+            e[k] = false;
+            if (ok[k] && quant) fast &= quant_fast(Q, (double)v[k], u[k]);
+        }
+        if (__any_sync(0xFFFFFFFFu, !fast)) {  // rare: ties, escapes, tiny e
+#pragma unroll
+            for (int k = 0; k < QB_SPT; ++k)
+                if (ok[k] && quant) u[k] = quantize(Q, (double)v[k], e[k]);
+        }
+    };
+    if (quant && (z0 > 0 || R.zhalo)) {  // u at the plane before (inside the window)
+        T v[QB_SPT];
+        bool e[QB_SPT];
+#pragma unroll
+        for (int k = 0; k < QB_SPT; ++k) v[k] = ok[k] ? __ldg(ptr[k] - plane) : (T)0;
+        quant_slots(v, up, e);
+    }
+    T nv[QB_SPT];
+#pragma unroll
+    for (int k = 0; k < QB_SPT; ++k) nv[k] = (ok[k] && z0 < z1) ? __ldg(ptr[k]) : (T)0;
+    bool inexact = false;
+    for (int z = z0; z < z1; ++z) {
+        T v[QB_SPT];
+#pragma unroll
+        for (int k = 0; k < QB_SPT; ++k) {
+            v[k] = nv[k];
+            ptr[k] += plane;
+            nv[k] = (ok[k] && z + 1 < z1) ? __ldg(ptr[k]) : (T)0;  // prefetch the next plane
+        }
+        int32_t u[QB_SPT];
+        bool e[QB_SPT];
+        quant_slots(v, u, e);
+        int32_t *D = sD[z & 1];
+#pragma unroll
+        for (int k = 0; k < QB_SPT; ++k) {
+            const int i = tid + QB_T * k;
+            if (i < span) D[i] = u[k] - up[k];  // invalid slots: 0 - 0
+            up[k] = u[k];
+        }
+        __syncthreads();
+        const int64_t zrow = (int64_t)z * R.ey;
+#pragma unroll
+        for (int k = 0; k < QB_SPT; ++k) {
+            if (!own[k]) continue;
+            const int i = tid + QB_T * k;
+            const int x = xs[k];
+            const int32_t q = D[i] - (x > 0 ? D[i - 1] : 0) - D[i - ex] + (x > 0 ? D[i - ex - 1] : 0);
+            const int64_t s = (zrow + ys[k]) * ex + x;  // window raster index
+            qz[R.q_base + s] = zz1_32(q);
+            if (e[k]) {
+                const int64_t bit = (int64_t)R.ebase * 32 + s;
+                atomicOr(escbits + (bit >> 5), 1u << (bit & 31));
+                atomicOr(&regs[ri].has_esc, 1);
+            }
+            if (chk32) inexact |= not_f32_exact(v[k]);
+        }
+    }
+    if (chk32 && __any_sync(0xFFFFFFFFu, inexact) && (tid & 31) == 0) atomicOr(&regs[ri].f32bad, 1);
+}
+
 // Piece records: one warp per 64-sample piece of a window's raster stream,
 // a CTA per scan chunk (1024 pieces of one region).  Reads the token values.
 __global__ void __launch_bounds__(256) k_summarize(const RegDev *__restrict__ regs,
@@ -279,13 +389,13 @@ __global__ void __launch_bounds__(256) k_summarize(const RegDev *__restrict__ re
                                                    const uint32_t *__restrict__ escbits,
                                                    PieceRec *__restrict__ recs) {
     __shared__ RegDev R;
-    const int64_t c = blockIdx.x;
+    const int64_t c = blockIdx.x / CSPLIT;  // CSPLIT CTAs per scan chunk
     coop_copy(&R, regs + __ldg(chunk_reg + c));
     __syncthreads();
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t lt = (1u << lane) - 1u;
-    constexpr int PW = (int)(CH / 8);
-    int64_t lp = (c - R.chunk_base) * CH + (int64_t)w * PW;
+    constexpr int PW = (int)(CH / CSPLIT / 8);
+    int64_t lp = (c - R.chunk_base) * CH + (int64_t)(blockIdx.x % CSPLIT) * (CH / CSPLIT) + (int64_t)w * PW;
     const int64_t lpe = min(lp + PW, R.npieces);
     const uint32_t *q = qz + R.q_base;
     for (; lp < lpe; ++lp) {
@@ -354,13 +464,13 @@ __global__ void __launch_bounds__(256) k_emit_q(const T *__restrict__ vol, const
                                                 const uint32_t *__restrict__ qz,
                                                 const uint32_t *__restrict__ escbits, uint8_t *__restrict__ out) {
     __shared__ RegDev R;
-    const int64_t c = blockIdx.x;
+    const int64_t c = blockIdx.x / CSPLIT;  // CSPLIT CTAs per scan chunk
     coop_copy(&R, regs + __ldg(chunk_reg + c));
     __syncthreads();
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t lt = (1u << lane) - 1u;
-    constexpr int PW = (int)(CH / 8);  // pieces per warp
-    int64_t lp = (c - R.chunk_base) * CH + (int64_t)w * PW;
+    constexpr int PW = (int)(CH / CSPLIT / 8);  // pieces per warp
+    int64_t lp = (c - R.chunk_base) * CH + (int64_t)(blockIdx.x % CSPLIT) * (CH / CSPLIT) + (int64_t)w * PW;
     const int64_t lpe = min(lp + PW, R.npieces);
     if (lp >= lpe) return;
     const int codec = R.codec;
@@ -885,6 +995,14 @@ static bool build_plan(const chr_region_t *h, int64_t nreg, EncPlan &pl) {
         R.ntx = (int32_t)ceil_div(R.ex, TX);
         R.nty = (int32_t)ceil_div(R.ey, TY);
         R.nzc = (int32_t)ceil_div(R.ez, ZC);
+        R.qband = 0;
+        R.rb = 0;
+        if (R.ex <= QB_CAP / 2) {  // full-row bands: rb rows + the halo row fit one CTA's slots
+            R.qband = 1;
+            R.rb = std::max(1, std::min(R.ey, QB_CAP / R.ex - 1));
+            R.ntx = 1;
+            R.nty = (int32_t)ceil_div(R.ey, R.rb);
+        }
         R.item_base = item;
         item += (int64_t)R.ntx * R.nty * R.nzc;
         R.piece_base = piece;
@@ -1014,14 +1132,18 @@ extern "C" int chr_compress(const void *d_vol, int dtype, int src_dtype, int64_t
         CHR_PROF("k_quant<float>", st);
         k_quant<float><<<items, NW * 32, 0, st>>>((const float *)d_vol, pl.params, pl.d_regs, pl.item_reg, pl.qz,
                                                   pl.escbits);
+        k_quant_band<float><<<items, QB_T, 0, st>>>((const float *)d_vol, pl.params, pl.d_regs, pl.item_reg,
+                                                    pl.qz, pl.escbits);
     } else {
         CHR_PROF("k_quant<double>", st);
         k_quant<double><<<items, NW * 32, 0, st>>>((const double *)d_vol, pl.params, pl.d_regs, pl.item_reg, pl.qz,
                                                    pl.escbits);
+        k_quant_band<double><<<items, QB_T, 0, st>>>((const double *)d_vol, pl.params, pl.d_regs, pl.item_reg,
+                                                     pl.qz, pl.escbits);
     }
     {
         CHR_PROF("k_summarize", st);
-        k_summarize<<<chunks, 256, 0, st>>>(pl.d_regs, pl.chunk_reg, pl.qz, pl.escbits, pl.recs);
+        k_summarize<<<chunks * CSPLIT, 256, 0, st>>>(pl.d_regs, pl.chunk_reg, pl.qz, pl.escbits, pl.recs);
     }
     {
         CHR_PROF("k_scan_reduce", st);
@@ -1043,7 +1165,7 @@ extern "C" int chr_compress(const void *d_vol, int dtype, int src_dtype, int64_t
     if (dtype == CHR_F32) {
         {
             CHR_PROF("k_emit_q<float>", st);
-            k_emit_q<float><<<chunks, 256, 0, st>>>((const float *)d_vol, pl.params, pl.d_regs, pl.chunk_reg,
+            k_emit_q<float><<<chunks * CSPLIT, 256, 0, st>>>((const float *)d_vol, pl.params, pl.d_regs, pl.chunk_reg,
                                                     pl.recs, pl.poffs, pl.qz, pl.escbits, d_out);
         }
         {
@@ -1053,7 +1175,7 @@ extern "C" int chr_compress(const void *d_vol, int dtype, int src_dtype, int64_t
     } else {
         {
             CHR_PROF("k_emit_q<double>", st);
-            k_emit_q<double><<<chunks, 256, 0, st>>>((const double *)d_vol, pl.params, pl.d_regs, pl.chunk_reg,
+            k_emit_q<double><<<chunks * CSPLIT, 256, 0, st>>>((const double *)d_vol, pl.params, pl.d_regs, pl.chunk_reg,
                                                      pl.recs, pl.poffs, pl.qz, pl.escbits, d_out);
         }
         {
@@ -1183,7 +1305,7 @@ extern "C" int chr_rle_encode(const int64_t *d_q, int64_t n, uint8_t *d_out, uin
     }
     {
         CHR_PROF("k_summarize", st);
-        k_summarize<<<chunks, 256, 0, st>>>(pl.d_regs, pl.chunk_reg, pl.qz, pl.escbits, pl.recs);
+        k_summarize<<<chunks * CSPLIT, 256, 0, st>>>(pl.d_regs, pl.chunk_reg, pl.qz, pl.escbits, pl.recs);
     }
     k_scan_reduce<<<chunks, 256, 0, st>>>(pl.params, pl.d_regs, pl.recs, pl.chunk);
     k_scan_regions<<<1, 128, 0, st>>>(pl.params, pl.d_regs, pl.chunk, pl.codec2, pl.scal);
@@ -1191,7 +1313,7 @@ extern "C" int chr_rle_encode(const int64_t *d_q, int64_t n, uint8_t *d_out, uin
     k_scan_down<<<chunks, 256, 0, st>>>(pl.params, pl.d_regs, pl.recs, pl.chunk, pl.poffs);
     {
         CHR_PROF("k_emit_q<double>", st);
-        k_emit_q<double><<<chunks, 256, 0, st>>>(nullptr, pl.params, pl.d_regs, pl.chunk_reg, pl.recs, pl.poffs,
+        k_emit_q<double><<<chunks * CSPLIT, 256, 0, st>>>(nullptr, pl.params, pl.d_regs, pl.chunk_reg, pl.recs, pl.poffs,
                                                  pl.qz, pl.escbits, d_out);
     }
     CHR_CUDA_TRY(cudaGetLastError());
@@ -1333,14 +1455,20 @@ extern "C" int chr_dcompress_local(const void *d_vol, int dtype, int src_dtype, 
         if (dtype == CHR_F32)
             k_quant<float><<<items, NW * 32, 0, st>>>((const float *)d_vol, pl.params, pl.d_regs, pl.item_reg,
                                                       pl.qz, pl.escbits);
+        if (dtype == CHR_F32)
+            k_quant_band<float><<<items, QB_T, 0, st>>>((const float *)d_vol, pl.params, pl.d_regs, pl.item_reg,
+                                                        pl.qz, pl.escbits);
         else
             k_quant<double><<<items, NW * 32, 0, st>>>((const double *)d_vol, pl.params, pl.d_regs, pl.item_reg,
                                                        pl.qz, pl.escbits);
+        if (dtype != CHR_F32)
+            k_quant_band<double><<<items, QB_T, 0, st>>>((const double *)d_vol, pl.params, pl.d_regs, pl.item_reg,
+                                                         pl.qz, pl.escbits);
     }
     if (chunks) {
         {
             CHR_PROF("k_summarize", st);
-            k_summarize<<<chunks, 256, 0, st>>>(pl.d_regs, pl.chunk_reg, pl.qz, pl.escbits, pl.recs);
+            k_summarize<<<chunks * CSPLIT, 256, 0, st>>>(pl.d_regs, pl.chunk_reg, pl.qz, pl.escbits, pl.recs);
         }
         k_scan_reduce<<<chunks, 256, 0, st>>>(pl.params, pl.d_regs, pl.recs, pl.chunk);
     }
@@ -1432,10 +1560,10 @@ extern "C" int chr_dcompress_finish(const void *d_vol, int dtype, int src_dtype,
         k_scan_down<<<chunks, 256, 0, st>>>(pl.params, pl.d_regs, pl.recs, pl.chunk, pl.poffs);
         CHR_PROF(dtype == CHR_F32 ? "k_emit_q<float>" : "k_emit_q<double>", st);
         if (dtype == CHR_F32)
-            k_emit_q<float><<<chunks, 256, 0, st>>>((const float *)d_vol, pl.params, pl.d_regs, pl.chunk_reg,
+            k_emit_q<float><<<chunks * CSPLIT, 256, 0, st>>>((const float *)d_vol, pl.params, pl.d_regs, pl.chunk_reg,
                                                     pl.recs, pl.poffs, pl.qz, pl.escbits, d_out);
         else
-            k_emit_q<double><<<chunks, 256, 0, st>>>((const double *)d_vol, pl.params, pl.d_regs, pl.chunk_reg,
+            k_emit_q<double><<<chunks * CSPLIT, 256, 0, st>>>((const double *)d_vol, pl.params, pl.d_regs, pl.chunk_reg,
                                                      pl.recs, pl.poffs, pl.qz, pl.escbits, d_out);
     }
     if (!c2.empty()) k_bitmap<<<148, 256, 0, st>>>(pl.d_regs, pl.codec2, pl.scal, pl.escbits, d_out);
