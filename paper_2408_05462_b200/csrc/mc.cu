@@ -30,7 +30,7 @@
 
 namespace chr {
 
-constexpr int MTX = 64, MTY = 8, MZC = 16;
+constexpr int MTX = 64, MTY = 8, MZC = 32;
 constexpr int64_t MCH = 1024;
 
 // Bourke corner index of unit offset (x, y, z) (mc_tables.py:8-12)
