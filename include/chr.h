@@ -238,6 +238,23 @@ int chr_dcompress_headers(int64_t nx, int64_t ny, int64_t nz, int source_dtype, 
                           chr_region_t *h_regions, int64_t n_regions, const uint32_t *h_raw_all,
                           void *d_workspace, size_t workspace_bytes, uint8_t *d_out, void *stream);
 
+/* 13. SURVEY 8(f2): accuracy < 1 and paper_edges bounds.  For every pair
+ *     (window [ox,oy,oz,ex,ey,ez], candidate k) the n-th smallest of the
+ *     pair's distances (mode 0 strict_vertices: |s-k| over the window;
+ *     mode 1 paper_edges: k-s0, s1-k of straddling edges), n = max(1, 1 +
+ *     floor((1 - accuracy) |D|)) (bound.py:117-219); h_value = -1 when D is
+ *     empty.  chr_compress2 also records the bound mode and accuracy in the
+ *     region table. */
+size_t chr_select_workspace_size(int64_t n_pairs);
+int chr_select_distances(const void *d_vol, int dtype, int64_t nx, int64_t ny, int64_t nz, const int32_t *h_windows,
+                         const double *h_k, int64_t n_pairs, double accuracy, int mode, void *d_workspace,
+                         size_t workspace_bytes, double *h_value, int64_t *h_count, int64_t *h_n, void *stream);
+int chr_compress2(const void *d_vol, int dtype, int source_dtype, int64_t nx, int64_t ny, int64_t nz,
+                  const double *spacing, int64_t block_size, double vmin, double vmax, const double *h_cands, int m,
+                  chr_region_t *h_regions, int64_t n_regions, int write_file, int bound_mode, double accuracy,
+                  void *d_workspace, size_t workspace_bytes, uint8_t *d_out, uint64_t out_cap,
+                  uint64_t *h_out_nbytes, void *stream);
+
 /* 12. fused request + extract: the decoder also writes each window's
  *     inside mask (bit y*nx + x of plane z's ceil(nx*ny/32) words is
  *     v >= iso; windows back to back, chr_mask_words() words in all) and

@@ -13,7 +13,8 @@ the path named by BASELINE.json ``north_star`` (paths below are relative to
 * block decomposition + extrema         blocking.py:64-111
 * span index                            blocking.py:114-127
 * greedy region merge                   blocking.py:130-193  (C: or_merge_regions)
-* strict accuracy-1 region bound        bound.py:150-219, chr_archive.py:168
+* region bound (strict / paper_edges,   bound.py:68-83, 117-219, chr_archive.py:168
+  any accuracy)
 * codec compress / decompress           codec.py:91-229
 * archive build / request / stitch      chr_archive.py:132-294
 * archive serialisation                 chr_archive.py:297-340 (FORMAT.md)
@@ -278,7 +279,8 @@ class OracleArchive:
         off = self.header_table_nbytes()
         for r in self.regions:
             parts.append(REGION_FIXED.pack(r["id"], *r["lo"], *r["hi"], *r["origin"], *r["extent"],
-                                           0, 1.0, r["e"], off, len(r["block"])))
+                                           r.get("bound_mode", 0), r.get("accuracy", 1.0), r["e"], off,
+                                           len(r["block"])))
             parts.append(int(r["mask"]).to_bytes(mb, "little"))
             off += len(r["block"])
         parts.extend(r["block"] for r in self.regions)
@@ -308,9 +310,29 @@ def merge(masks, nb3):
     return out[:nreg]
 
 
+def select_index(nd, accuracy):
+    """n of the n-th-smallest rule (bound.py:117-119)."""
+    return max(1, 1 + int(np.floor((1.0 - accuracy) * nd)))
+
+
+def window_distances(win3, k, paper):
+    """D for one window (bound.py:68-83 / 106-112): |s - k| over every
+    sample, or k - s0, s1 - k over the straddling axis edges."""
+    if not paper:
+        return np.abs(win3.ravel() - k)
+    parts = []
+    for axis in range(3):
+        a = np.moveaxis(win3, axis, 0)
+        s0, s1 = np.minimum(a[:-1], a[1:]), np.maximum(a[:-1], a[1:])
+        m = (s0 < k) & (k < s1)
+        parts += [k - s0[m], s1[m] - k]
+    return np.concatenate(parts) if parts else np.empty(0)
+
+
 def build_chr(values, dims, candidates, bs, spacing=(1.0, 1.0, 1.0), source_dtype="f32",
-              loose_fraction=0.01, out_of_range="error", workers=1):
-    """Strict, accuracy-1 archive build (chr_archive.py:132-212)."""
+              loose_fraction=0.01, out_of_range="error", workers=1, accuracy=1.0, bound_mode="strict_vertices"):
+    """Archive build (chr_archive.py:132-212)."""
+    paper = bound_mode == "paper_edges"
     values = np.ascontiguousarray(values, dtype=np.float64).reshape(-1)
     nx, ny, nz = dims
     if not np.isfinite(values).all():
@@ -339,11 +361,24 @@ def build_chr(values, dims, candidates, bs, spacing=(1.0, 1.0, 1.0), source_dtyp
         served = [cands[ci] for ci in range(len(cands)) if (mask >> ci) & 1]
         unserved = [k for k in cands if k not in served]
         win = (ctypes.c_void_p(values.ctypes.data), nx, ny, *lo_o, *ext)
-        # region_bound strict, accuracy 1 (bound.py:150-219)
+        # region_bound (bound.py:150-219)
         best = None
         lossless = False
+        w3 = None
+        if paper or accuracy != 1.0:
+            w3 = np.empty(ext[0] * ext[1] * ext[2])
+            L.or_gather_window(*win, _p(w3))
+            w3 = w3.reshape(ext[2], ext[1], ext[0])
         for k in served:
-            val = L.or_window_min_abs_distance(*win, k)
+            if w3 is None:
+                val = L.or_window_min_abs_distance(*win, k)
+            else:
+                d = window_distances(w3, k, paper)
+                if d.size == 0:
+                    best = loose if best is None or loose < best else best
+                    continue
+                n = select_index(d.size, accuracy)
+                val = float(np.partition(d, n - 1)[n - 1])
             cand = 0.0 if val == 0.0 else val * SAFETY_FACTOR
             if best is None or cand < best:
                 best = cand
@@ -364,7 +399,7 @@ def build_chr(values, dims, candidates, bs, spacing=(1.0, 1.0, 1.0), source_dtyp
         cid, payload = compress_flat(flat, ext, best, source_dtype)
         return {
             "id": rid, "lo": (bx, by, bz), "hi": (hx, hy, hz), "origin": lo_o, "extent": ext,
-            "mask": mask, "e": best, "codec": cid,
+            "mask": mask, "e": best, "codec": cid, "bound_mode": 1 if paper else 0, "accuracy": float(accuracy),
             "block": block_bytes(cid, ext, best, source_dtype, payload),
         }
 

@@ -172,6 +172,13 @@ def lib():
         L.chr_dcompress_finish.restype = INT
         L.chr_dcompress_headers.argtypes = [I64, I64, I64, INT, P, I64, D, D, P, INT, P, I64, P, P, SZ, P, P]
         L.chr_dcompress_headers.restype = INT
+        L.chr_select_workspace_size.argtypes = [I64]
+        L.chr_select_workspace_size.restype = SZ
+        L.chr_select_distances.argtypes = [P, INT, I64, I64, I64, P, P, I64, D, INT, P, SZ, P, P, P, P]
+        L.chr_select_distances.restype = INT
+        L.chr_compress2.argtypes = [P, INT, INT, I64, I64, I64, P, I64, D, D, P, INT, P, I64, INT, INT, D, P, SZ,
+                                    P, U64, P, P]
+        L.chr_compress2.restype = INT
         L.chr_mask_words.argtypes = [P, I64]
         L.chr_mask_words.restype = U64
         L.chr_decode_regions_mask.argtypes = [P, P, I64, P, P, SZ, P, D, P, P]
@@ -199,6 +206,7 @@ def lib():
 EXPORTS = [
     "chr_rle_encode_workspace_size", "chr_rle_encode", "chr_sm_copy",
     "chr_mask_words", "chr_decode_regions_mask", "chr_mc_count_masked", "chr_mc_emit_masked",
+    "chr_select_workspace_size", "chr_select_distances", "chr_compress2",
     "chr_dcompress_workspace_size", "chr_dcompress_local", "chr_dcompress_finish", "chr_dcompress_headers",
     "chr_abi_version", "chr_status_string", "chr_num_blocks", "chr_stats", "chr_plan",
     "chr_compress_workspace_size", "chr_compress_capacity", "chr_compress",

@@ -123,13 +123,10 @@ def _check_build_args(accuracy, bound_mode, safety_factor, loose_fraction, out_o
         raise ParameterError(f"out_of_range must be 'error' or 'warn', got {out_of_range!r}")
     if not 0.0 < loose_fraction:
         raise ParameterError(f"loose_fraction must be positive, got {loose_fraction}")
-    if accuracy != 1.0 or bound_mode != MODE_STRICT:
-        raise NotImplementedError(
-            "the GPU path implements the strict_vertices bound at accuracy 1.0 (the north_star "
-            "configuration); accuracy < 1 and paper_edges are SURVEY §8(f2), scheduled next")
 
 
-def _regions_from_device(res: device.Compressed, host_blob: bytes, cands, source_dtype):
+def _regions_from_device(res: device.Compressed, host_blob: bytes, cands, source_dtype, bound_mode=MODE_STRICT,
+                         accuracy=1.0):
     out = []
     for rec in device.region_records(res.regions):
         blk = CompressedBlock.from_bytes(host_blob, rec["block_offset"])
@@ -137,7 +134,7 @@ def _regions_from_device(res: device.Compressed, host_blob: bytes, cands, source
         out.append(ArchiveRegion(
             region_id=rec["id"], block_span=(rec["lo"], rec["hi"]), sample_origin=rec["origin"],
             sample_extent=rec["extent"], relevance=frozenset(ci for ci in range(len(cands)) if (mask >> ci) & 1),
-            bound_mode=MODE_STRICT, accuracy=1.0, error_bound=rec["e"], block=blk))
+            bound_mode=bound_mode, accuracy=float(accuracy), error_bound=rec["e"], block=blk))
     return tuple(out)
 
 
@@ -163,18 +160,19 @@ def build_chr(volume, candidates, block_size: int, accuracy: float = 1.0, bound_
     res = device.build_archive(dvals, vol.dims, cands, block_size, spacing=vol.spacing,
                                source_dtype=vol.source_dtype, loose_fraction=loose_fraction,
                                safety_factor=safety_factor, vrange=vol.value_range, out_of_range=out_of_range,
-                               on_warn=lambda m: warnings.warn(m, stacklevel=3))
+                               on_warn=lambda m: warnings.warn(m, stacklevel=3), accuracy=accuracy,
+                               bound_mode=bound_mode)
     if codec is not None:
-        return _rebuild_with_plugin(vol, res, cands, block_size, codec)
+        return _rebuild_with_plugin(vol, res, cands, block_size, codec, bound_mode, accuracy)
     host = res.blob[: res.nbytes].cpu().numpy().tobytes()
-    regions = _regions_from_device(res, host, cands, vol.source_dtype)
+    regions = _regions_from_device(res, host, cands, vol.source_dtype, bound_mode, accuracy)
     # own copy: res.blob is reusable workspace; +16 slack for aligned word reads
     dev = {"blob": res.blob[: min(res.blob.numel(), res.nbytes + 16)].clone(), "file": host}
     return CHRArchive(vol.dims, vol.spacing, vol.source_dtype, int(block_size), tuple(res.extra["vrange"]),
                       tuple(cands), regions, dev)
 
 
-def _rebuild_with_plugin(vol, res, cands, bs, codec):
+def _rebuild_with_plugin(vol, res, cands, bs, codec, bound_mode=MODE_STRICT, accuracy=1.0):
     """build_chr(codec=...) seam (chr_archive.py:142,185): GPU bounds, plugin bytes."""
     grid = vol.grid
     regions = []
@@ -184,7 +182,7 @@ def _rebuild_with_plugin(vol, res, cands, bs, codec):
         mask = rec["mask"]
         regions.append(ArchiveRegion(rec["id"], (rec["lo"], rec["hi"]), rec["origin"], rec["extent"],
                                      frozenset(ci for ci in range(len(cands)) if (mask >> ci) & 1),
-                                     MODE_STRICT, 1.0, rec["e"], blk))
+                                     bound_mode, float(accuracy), rec["e"], blk))
     return CHRArchive(vol.dims, vol.spacing, vol.source_dtype, int(bs), tuple(res.extra["vrange"]),
                       tuple(cands), tuple(regions))
 

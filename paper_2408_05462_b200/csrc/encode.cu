@@ -73,7 +73,8 @@ struct EncParams {
     int64_t NX, NY, NZ;
     int64_t nreg, nitems, nchunks;
     int32_t dtype, src_dtype, write_file, m;
-    int32_t dist, pad_;       // dist: codec/length decided on the host from every rank's portions
+    int32_t dist, bound_mode;  // dist: codec/length decided on the host; bound_mode: table byte (0 strict, 1 paper)
+    double accuracy;           // stored accuracy (region table)
     double spacing[3];
     double vmin, vmax;
     int64_t bs;
@@ -894,8 +895,8 @@ __global__ void __launch_bounds__(256) k_write_table(const EncParams *__restrict
     put_le(p + 40, (uint32_t)R.ex);
     put_le(p + 44, (uint32_t)R.ey);
     put_le(p + 48, (uint32_t)R.ez);
-    p[52] = 0;                       // bound mode strict_vertices
-    put_le(p + 53, 1.0);             // stored accuracy
+    p[52] = (uint8_t)P->bound_mode;  // 0 strict_vertices, 1 paper_edges
+    put_le(p + 53, P->accuracy);     // stored accuracy
     put_le(p + 61, R.e);
     put_le(p + 69, (uint64_t)R.block_off);
     put_le(p + 77, (uint64_t)(kBlockHeader + R.payload_len));
@@ -1073,11 +1074,27 @@ extern "C" uint64_t chr_compress_capacity(const chr_region_t *h, int64_t nreg, i
     return cap;
 }
 
+extern "C" int chr_compress2(const void *d_vol, int dtype, int src_dtype, int64_t nx, int64_t ny, int64_t nz,
+                             const double *spacing, int64_t bs, double vmin, double vmax, const double *h_cands,
+                             int m, chr_region_t *h_regions, int64_t nreg, int write_file, int bound_mode,
+                             double accuracy, void *d_ws, size_t ws_bytes, uint8_t *d_out, uint64_t out_cap,
+                             uint64_t *h_out_nbytes, void *stream);
+
 extern "C" int chr_compress(const void *d_vol, int dtype, int src_dtype, int64_t nx, int64_t ny,
                             int64_t nz, const double *spacing, int64_t bs, double vmin, double vmax,
                             const double *h_cands, int m, chr_region_t *h_regions, int64_t nreg,
                             int write_file, void *d_ws, size_t ws_bytes, uint8_t *d_out,
                             uint64_t out_cap, uint64_t *h_out_nbytes, void *stream) {
+    return chr_compress2(d_vol, dtype, src_dtype, nx, ny, nz, spacing, bs, vmin, vmax, h_cands, m, h_regions, nreg,
+                         write_file, 0, 1.0, d_ws, ws_bytes, d_out, out_cap, h_out_nbytes, stream);
+}
+
+extern "C" int chr_compress2(const void *d_vol, int dtype, int src_dtype, int64_t nx, int64_t ny, int64_t nz,
+                             const double *spacing, int64_t bs, double vmin, double vmax, const double *h_cands,
+                             int m, chr_region_t *h_regions, int64_t nreg, int write_file, int bound_mode,
+                             double accuracy, void *d_ws, size_t ws_bytes, uint8_t *d_out, uint64_t out_cap,
+                             uint64_t *h_out_nbytes, void *stream) {
+    if (bound_mode < 0 || bound_mode > 1 || !(accuracy > 0.0 && accuracy <= 1.0)) return CHR_E_PARAMETER;
     if (!d_vol || !h_regions || nreg < 1 || !d_out || !h_out_nbytes) return CHR_E_PARAMETER;
     if (dtype != CHR_F32 && dtype != CHR_F64) return CHR_E_PARAMETER;
     if (src_dtype != CHR_F32 && src_dtype != CHR_F64) return CHR_E_PARAMETER;
@@ -1113,6 +1130,8 @@ extern "C" int chr_compress(const void *d_vol, int dtype, int src_dtype, int64_t
     hp.header_table = write_file ? (uint64_t)(kFileHeader + 4 + 8 * m + 4) +
                                        (uint64_t)nreg * (kRegionFixed + (m + 7) / 8)
                                  : 0;
+    hp.bound_mode = bound_mode;
+    hp.accuracy = accuracy;
     // capacity check against the worst case (verbatim f64 everywhere)
     if (out_cap < chr_compress_capacity(h_regions, nreg, m, src_dtype)) return CHR_E_PARAMETER;
 
@@ -1425,6 +1444,8 @@ static void dist_params(EncParams &hp, const EncPlan &pl, int64_t nx, int64_t ny
     hp.bs = bs;
     for (int i = 0; i < m && i < 64; ++i) hp.cands[i] = h_cands[i];
     hp.header_table = (uint64_t)(kFileHeader + 4 + 8 * m + 4) + (uint64_t)nreg * (kRegionFixed + (m + 7) / 8);
+    hp.bound_mode = 0;
+    hp.accuracy = 1.0;
 }
 
 // phase 1: quantise this rank's portions and summarise their streams

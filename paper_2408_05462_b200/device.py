@@ -119,9 +119,13 @@ class Workspaces:
 _DEFAULT_WS = Workspaces()
 
 
+BOUND_MODES = {"strict_vertices": 0, "paper_edges": 1}
+
+
 def compress(vol: torch.Tensor, dims, regions, *, source_dtype="f32", write_file=True, spacing=(1.0, 1.0, 1.0),
              bs=0, vrange=(0.0, 0.0), cands=(0.0,), ws: Workspaces | None = None,
-             out: torch.Tensor | None = None) -> Compressed:
+             out: torch.Tensor | None = None, bound_mode: str = "strict_vertices",
+             accuracy: float = 1.0) -> Compressed:
     """Run chr_compress on `regions`; returns the device bytes."""
     ws = ws or _DEFAULT_WS
     L = lib()
@@ -139,16 +143,90 @@ def compress(vol: torch.Tensor, dims, regions, *, source_dtype="f32", write_file
         out = ws.get("compress_out", cap)
     nbytes = ctypes.c_uint64(0)
     sp = (ctypes.c_double * 3)(*[float(s) for s in spacing])
-    check(L.chr_compress(ptr(vol), _dtype_code(vol), DTYPE_TAGS[source_dtype], *dims, sp, int(bs),
-                         float(vrange[0]), float(vrange[1]), _np_ptr(cands), m, rp, nreg,
-                         1 if write_file else 0, ptr(work), work.numel(), ptr(out), out.numel(),
-                         ctypes.byref(nbytes), stream_ptr()), "chr_compress")
+    check(L.chr_compress2(ptr(vol), _dtype_code(vol), DTYPE_TAGS[source_dtype], *dims, sp, int(bs),
+                          float(vrange[0]), float(vrange[1]), _np_ptr(cands), m, rp, nreg,
+                          1 if write_file else 0, BOUND_MODES[bound_mode], float(accuracy), ptr(work),
+                          work.numel(), ptr(out), out.numel(), ctypes.byref(nbytes), stream_ptr()), "chr_compress")
     return Compressed(out, int(nbytes.value), regions, source_dtype)
+
+
+def select_distances(vol: torch.Tensor, dims, windows, ks, accuracy: float, bound_mode: str) -> np.ndarray:
+    """n-th smallest distance D(window, k) per pair (bound.py:117-147),
+    -1.0 where D is empty (paper_edges, no straddling edge)."""
+    npairs = len(windows)
+    val = np.zeros(max(npairs, 1), np.float64)
+    if npairs:
+        L = lib()
+        w = np.ascontiguousarray(windows, dtype=np.int32).reshape(npairs, 6)
+        karr = np.ascontiguousarray(ks, dtype=np.float64)
+        work = _DEFAULT_WS.get("select", L.chr_select_workspace_size(npairs))
+        check(L.chr_select_distances(ptr(vol), _dtype_code(vol), *dims, _np_ptr(w), _np_ptr(karr), npairs,
+                                     float(accuracy), BOUND_MODES[bound_mode], ptr(work), work.numel(),
+                                     _np_ptr(val), None, None, stream_ptr()), "chr_select_distances")
+    return val[:npairs]
+
+
+def select_bounds(vol: torch.Tensor, dims, bs, regions: np.ndarray, block_stats: np.ndarray, cands, accuracy: float,
+                  bound_mode: str, safety_factor: float, loose: float) -> np.ndarray:
+    """bound.region_bound (bound.py:150-219) for accuracy < 1 / paper_edges:
+    n-th smallest distance of every served (region, candidate) pair on the
+    device (chr_select_distances), then per region the minimum spec over its
+    served candidates (a zero distance forces lossless), the loose bound when
+    nothing is served or no edge straddles, and the cap below every unserved
+    candidate's margin (min |s - k|, from the region's block extrema: an
+    unserved k lies outside every one of its blocks' ranges).  Returns the
+    float64 bound per region."""
+    cands = [float(k) for k in cands]
+    nx, ny, nz = dims
+    nb3 = [max(1, -(-(d - 1) // bs)) for d in dims]
+    st = np.asarray(block_stats, dtype=np.float64).reshape(nb3[2], nb3[1], nb3[0], -1)
+    win, kk, owner = [], [], []
+    for r in range(len(regions)):
+        mask = int(regions["mask"][r])
+        for ci, k in enumerate(cands):
+            if (mask >> ci) & 1:
+                win.append(list(regions["origin"][r]) + list(regions["extent"][r]))
+                kk.append(k)
+                owner.append(r)
+    npairs = len(win)
+    val = select_distances(vol, dims, win, kk, accuracy, bound_mode)
+    out = np.empty(len(regions), np.float64)
+    pi = 0
+    for r in range(len(regions)):
+        mask = int(regions["mask"][r])
+        best = None
+        lossless = False
+        while pi < npairs and owner[pi] == r:
+            v = float(val[pi])
+            pi += 1
+            if lossless:
+                continue
+            spec = float(loose) if v < 0 else (0.0 if v == 0.0 else v * safety_factor)
+            if best is None or spec < best:
+                best = spec
+            if v == 0.0:
+                lossless = True
+        if best is None:
+            best = float(loose)
+        if not lossless:
+            lo, hi = regions["lo"][r], regions["hi"][r]
+            sub = st[lo[2]:hi[2] + 1, lo[1]:hi[1] + 1, lo[0]:hi[0] + 1]
+            bmin, bmax = sub[..., 0].ravel(), sub[..., 1].ravel()
+            for ci, k in enumerate(cands):
+                if (mask >> ci) & 1:
+                    continue
+                d = np.where(k < bmin, bmin - k, k - bmax)  # fl(|s - k|) at the nearer extreme
+                margin = float(d.min()) * safety_factor
+                if margin < best:
+                    best = margin
+        out[r] = best
+    return out
 
 
 def build_archive(vol: torch.Tensor, dims, cands, bs, *, spacing=(1.0, 1.0, 1.0), source_dtype="f32",
                   loose_fraction=LOOSE_FRACTION, safety_factor=SAFETY_FACTOR, vrange=None,
-                  out_of_range="error", ws: Workspaces | None = None, on_warn=None) -> Compressed:
+                  out_of_range="error", ws: Workspaces | None = None, on_warn=None, accuracy: float = 1.0,
+                  bound_mode: str = "strict_vertices") -> Compressed:
     """stats -> plan -> compress: a complete .chr file on the device
     (chr_archive.build_chr, strict bound at accuracy 1)."""
     ws = ws or _DEFAULT_WS
@@ -179,8 +257,12 @@ def build_archive(vol: torch.Tensor, dims, cands, bs, *, spacing=(1.0, 1.0, 1.0)
     if not loose_fraction > 0.0:
         raise ParameterError(f"loose_fraction must be positive, got {loose_fraction}")
     regions = plan(bstats, dims, bs, cands, vmin, vmax, loose_fraction, safety_factor)
+    if accuracy != 1.0 or bound_mode != "strict_vertices":
+        loose = loose_fraction * (vmax - vmin)
+        regions["error_bound"] = select_bounds(vol, dims, bs, regions, bstats, cands, accuracy, bound_mode,
+                                               safety_factor, loose)
     res = compress(vol, dims, regions, source_dtype=source_dtype, write_file=True, spacing=spacing, bs=bs,
-                   vrange=(vmin, vmax), cands=cands, ws=ws)
+                   vrange=(vmin, vmax), cands=cands, ws=ws, bound_mode=bound_mode, accuracy=accuracy)
     res.extra.update(block_stats=bstats, vrange=(vmin, vmax), cands=tuple(float(k) for k in cands))
     return res
 

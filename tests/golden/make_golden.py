@@ -160,15 +160,17 @@ put("mcsmooth_t", m.triangles)
 # --- 5. whole archives -------------------------------------------------------
 
 
-def archive_case(name, vol, cands, bs, **kw):
+def archive_case(name, vol, cands, bs, input_from=None, **kw):
     arch = isochr.build_chr(vol, cands, block_size=bs, **kw)
     with tempfile.TemporaryDirectory() as td:
         p = os.path.join(td, "a.chr")
         isochr.write_chr(arch, p)
         blob = open(p, "rb").read()
-    put(name + "_in", vol.values.astype(np.float32) if vol.source_dtype == "f32" else vol.values)
+    if input_from is None:  # else: the same samples as archive ``input_from``
+        put(name + "_in", vol.values.astype(np.float32) if vol.source_dtype == "f32" else vol.values)
     put_bytes(name + "_chr", blob)
     info = {
+        "input": input_from or name,
         "dims": list(vol.dims), "spacing": list(vol.spacing), "dtype": vol.source_dtype,
         "cands": list(arch.candidates), "bs": bs, "kw": kw,
         "codecs": [r.block.codec_id for r in arch.regions],
@@ -229,6 +231,17 @@ with warnings.catch_warnings():
     warnings.simplefilter("ignore")
     archive_case("oor", isochr.Volume(dims=(9, 8, 10), values=np.linspace(0, 1, 720)), [7.0], 4,
                  out_of_range="warn")
+
+# accuracy < 1 and paper_edges bounds (bound.py:68-219)
+archive_case("c1_acc95", vol, [0.5 * vol.value_range[1]], 16, "c1", loose_fraction=1e-3, accuracy=0.95)
+archive_case("sphere_paper", sph, [-4.0, 0.0, 5.0], 8, "sphere", bound_mode="paper_edges")
+archive_case("smooth_paper80", sm, [-1.0, float(np.median(sm.values)), 1.5], 6, "smooth", loose_fraction=0.05,
+             bound_mode="paper_edges", accuracy=0.8)
+archive_case("smooth_acc90", sm, [-1.0, float(np.median(sm.values)), 1.5], 6, "smooth", loose_fraction=0.05,
+             accuracy=0.9)
+# k on a sample: strict -> lossless regions; paper -> edges ending on k do not straddle
+archive_case("exactk_paper", vq, [float(np.sort(vq.values)[vq.values.size // 2])], 5, "exactk",
+             bound_mode="paper_edges", accuracy=0.7)
 
 np.savez_compressed(os.path.join(HERE, "golden.npz"), **G)
 with open(os.path.join(HERE, "golden_meta.json"), "w") as fh:

@@ -138,12 +138,13 @@ def test_mc_shapes_vs_oracle(shape):
 
 
 # ----------------------------------------------------------------- archives
-@pytest.mark.parametrize("name", ["c1", "sphere", "smooth", "exactk", "oor"])
+@pytest.mark.parametrize("name", ["c1", "sphere", "smooth", "exactk", "oor", "c1_acc95", "sphere_paper",
+                                  "smooth_paper80", "smooth_acc90", "exactk_paper"])
 def test_golden_archives(golden, golden_meta, name, tmp_path):
     import warnings
 
     info = golden_meta["archive_" + name]
-    vals = golden[name + "_in"]
+    vals = golden[info["input"] + "_in"]
     vol = G.Volume(tuple(info["dims"]), tuple(info["spacing"]), vals.astype(np.float64), info["dtype"])
     kw = dict(info["kw"])
     with warnings.catch_warnings():
@@ -170,12 +171,13 @@ def test_golden_archives(golden, golden_meta, name, tmp_path):
             assert nt == ref["ntri"] and nv == ref["nvert"]
 
 
-def _config_parity(name, n, quantile=None, r=None):
+def _config_parity(name, n, quantile=None, r=None, accuracy=1.0, bound_mode="strict_vertices"):
     vals, dims, bs, cands, rr = synth.make_config(name, device="cuda", n=n, quantile=quantile, r=r)
     host = vals.cpu().numpy()
-    res = device.build_archive(vals, dims, cands, bs, loose_fraction=rr)
+    res = device.build_archive(vals, dims, cands, bs, loose_fraction=rr, accuracy=accuracy, bound_mode=bound_mode)
     got = res.blob[: res.nbytes].cpu().numpy().tobytes()
-    ref = O.build_chr(host.astype(np.float64), dims, cands, bs, source_dtype="f32", loose_fraction=rr, workers=8)
+    ref = O.build_chr(host.astype(np.float64), dims, cands, bs, source_dtype="f32", loose_fraction=rr, workers=8,
+                      accuracy=accuracy, bound_mode=bound_mode)
     want = ref.to_bytes()
     assert len(got) == len(want)
     assert got == want
@@ -407,3 +409,42 @@ def test_fused_request_extract_masks(name, n):
     v0, t0, _, _ = device.marching(wins, mct, k)
     v1, t1, _, _ = device.marching(wins, mct, k, masks=masks)
     assert torch.equal(t0, t1) and torch.equal(v0, v1)
+
+
+# ----------------------------------------------------------------- SURVEY 8(f2)
+@pytest.mark.parametrize("name,n,acc,mode", [
+    ("c1", 64, 0.95, "strict_vertices"), ("c2", 96, 0.9, "paper_edges"), ("c3", 96, 0.999, "strict_vertices"),
+    ("c4", 80, 1.0, "paper_edges"), ("c5", 72, 0.5, "paper_edges"), ("c2", 96, 1e-9, "strict_vertices")])
+def test_config_accuracy_and_paper_bounds(name, n, acc, mode):
+    """accuracy < 1 / paper_edges archives byte-identical to the oracle's
+    restatement of bound.region_bound (itself pinned by the reference's
+    archives in tests/golden: c1_acc95, sphere_paper, smooth_paper80 ...)."""
+    _config_parity(name, n, accuracy=acc, bound_mode=mode)
+
+
+@pytest.mark.parametrize("mode", ["strict_vertices", "paper_edges"])
+def test_select_distances_vs_numpy(mode):
+    """n-th smallest distance of every (window, k) pair: windows larger than
+    one histogram chunk, duplicated values (ties across the select digits),
+    k on a sample, windows with no straddling edge (|D| = 0 -> -1)."""
+    rng = np.random.default_rng(5)
+    dims = (70, 50, 40)
+    vol = np.round(rng.normal(size=dims[::-1]) * 8) / 8  # many exact ties
+    vol[:, :, :10] = 3.0  # constant slab: no straddles
+    flat = torch.from_numpy(vol.ravel()).cuda()
+    wins, ks = [], []
+    for o, e, k in [((0, 0, 0), (70, 50, 40), 0.0), ((0, 0, 0), (10, 50, 40), 0.0), ((5, 3, 2), (33, 17, 9), 0.25),
+                    ((10, 0, 0), (60, 50, 40), 0.3), ((1, 1, 1), (1, 1, 1), 2.0), ((0, 0, 0), (2, 1, 1), -1.0),
+                    ((20, 20, 20), (50, 30, 20), -0.0625)]:
+        wins.append(list(o) + list(e))
+        ks.append(k)
+    for acc in (1.0, 0.9, 0.5, 0.01):
+        got = device.select_distances(flat, dims, wins, ks, acc, mode)
+        for (ox, oy, oz, ex, ey, ez), k, v in zip(wins, ks, got):
+            w = vol[oz:oz + ez, oy:oy + ey, ox:ox + ex]
+            d = O.window_distances(w, k, mode == "paper_edges")
+            if d.size == 0:
+                assert v == -1.0
+                continue
+            nn = O.select_index(d.size, acc)
+            assert v == np.partition(d, nn - 1)[nn - 1], (acc, k)

@@ -91,14 +91,16 @@ def test_mc_random_grids(golden):
     assert np.array_equal(v, golden["mcsmooth_v"]) and np.array_equal(t, golden["mcsmooth_t"])
 
 
-@pytest.mark.parametrize("name", ["c1", "sphere", "smooth", "exactk", "oor"])
+@pytest.mark.parametrize("name", ["c1", "sphere", "smooth", "exactk", "oor", "c1_acc95", "sphere_paper",
+                                  "smooth_paper80", "smooth_acc90", "exactk_paper"])
 def test_archives_byte_identical(golden, golden_meta, name):
     info = golden_meta["archive_" + name]
-    vals = golden[name + "_in"].astype(np.float64)
+    vals = golden[info["input"] + "_in"].astype(np.float64)
     kw = dict(info["kw"])
     arch = O.build_chr(vals, tuple(info["dims"]), info["cands"], info["bs"], tuple(info["spacing"]),
                        info["dtype"], loose_fraction=kw.get("loose_fraction", 0.01),
-                       out_of_range=kw.get("out_of_range", "error"))
+                       out_of_range=kw.get("out_of_range", "error"), accuracy=kw.get("accuracy", 1.0),
+                       bound_mode=kw.get("bound_mode", "strict_vertices"))
     blob = arch.to_bytes()
     assert blob == golden[name + "_chr"].tobytes()
     for k in arch.candidates:
