@@ -276,6 +276,33 @@ int chr_mc_emit_masked(const double *d_grids, const chr_mc_grid_t *h_grids, int6
  *     a caller pipelines its inputs/outputs.  16-byte aligned pointers. */
 int chr_sm_copy(void *dst, const void *src, uint64_t nbytes, int ctas, void *stream);
 
+/* 14. SURVEY 8(f3): stitch + verify_topology on the device.
+ *     chr_stitch replaces chr_archive.stitch (chr_archive.py:277-294): the
+ *     request windows (f64, each at window_offset samples into d_windows)
+ *     are written into d_out (nx*ny*nz f64, x fastest, prefilled by the
+ *     caller with the fill value), each sample by its owner -- the window
+ *     with the lowest (z, y, x) origin among those covering it.  block_lo /
+ *     block_hi: the region's block span (FORMAT.md record fields).
+ *     chr_topology_compare replaces the case-code comparison of
+ *     verify_topology (isosurf.py:91-114): number of cells whose binary
+ *     case codes differ between a and b at k, and the smallest differing
+ *     cell index (x fastest over the (nx-1)(ny-1)(nz-1) cells; -1 if none).
+ *     Workspace: 16 bytes. */
+typedef struct {
+    uint64_t window_offset;
+    int32_t origin[3];
+    int32_t extent[3];
+    int32_t block_lo[3];
+    int32_t block_hi[3];
+} chr_stitch_t;
+
+size_t chr_stitch_workspace_size(int64_t n_windows, int64_t nx, int64_t ny, int64_t nz, int64_t bs);
+int chr_stitch(const double *d_windows, const chr_stitch_t *h_windows, int64_t n, int64_t nx, int64_t ny,
+               int64_t nz, int64_t bs, void *d_workspace, size_t workspace_bytes, double *d_out, void *stream);
+int chr_topology_compare(const void *d_a, int dtype_a, const void *d_b, int dtype_b, int64_t nx, int64_t ny,
+                         int64_t nz, double k, void *d_workspace, size_t workspace_bytes, uint64_t *h_ndiff,
+                         int64_t *h_first, void *stream);
+
 /* 9. instrumentation: launch counter and opt-in per-kernel CUDA-event
  *    timing on the launching stream ("name count total_ms" lines). */
 void chr_prof_enable(int on);

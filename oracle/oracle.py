@@ -428,6 +428,34 @@ def request(arch: OracleArchive, k, drop_pruned=True, workers=1):
     return list(zip(sel, wins))
 
 
+def stitch(sel, dims, fill=np.nan):
+    """(chr_archive.py:277-294): windows written in descending (z, y, x)
+    origin order, so the lowest origin lands last.  Flat x-fastest f64."""
+    nx, ny, nz = dims
+    out = np.full((nz, ny, nx), fill, dtype=np.float64)
+    for r, w in sorted(sel, key=lambda p: tuple(reversed(p[0]["origin"])), reverse=True):
+        (ox, oy, oz), (ex, ey, ez) = r["origin"], r["extent"]
+        out[oz:oz + ez, oy:oy + ey, ox:ox + ex] = np.asarray(w).reshape(ez, ey, ex)
+    return out.reshape(-1)
+
+
+def verify_topology(a, b, dims, k):
+    """(isosurf.py:91-114): (preserved_fraction, differing, total, first
+    differing cell (cx, cy, cz) or None) from binary case codes."""
+    ca, cb = case_field(a, dims, k), case_field(b, dims, k)
+    diff = ca != cb
+    nd = int(diff.sum())
+    total = ca.size
+    first = None
+    if nd:
+        flat = int(np.argmax(diff))
+        ncx, ncy = dims[0] - 1, dims[1] - 1
+        cz, rem = divmod(flat, ncx * ncy)
+        cy, cx = divmod(rem, ncx)
+        first = [cx, cy, cz]
+    return [(total - nd) / total, nd, total, first]
+
+
 def bytes_touched(arch: OracleArchive, sel):
     return arch.header_table_nbytes() + sum(len(r["block"]) for r, _ in sel)
 

@@ -22,6 +22,7 @@ from .archive import (
     request,
     request_device,
     stitch,
+    stitch_device,
     write_chr,
 )
 from .blockcodec import CompressedBlock, compress, decompress, register_codec
@@ -47,5 +48,5 @@ __all__ = [
     "MODE_STRICT", "ReconstructionSet", "Region", "RequestReport", "TopologyReport", "TriangleMesh", "Volume",
     "build_chr", "build_index", "case_field", "cell_case", "compress", "decompose", "decompress", "export_obj",
     "extract_device", "load_raw", "marching_cubes", "merge_meshes", "merge_regions", "read_chr",
-    "register_codec", "request", "request_device", "save_raw", "stitch", "verify_topology", "write_chr",
+    "register_codec", "request", "request_device", "save_raw", "stitch", "stitch_device", "verify_topology", "write_chr",
 ]

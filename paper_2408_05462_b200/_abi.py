@@ -103,6 +103,9 @@ DEC_DT = np.dtype([("payload_offset", "<u8"), ("payload_nbytes", "<u8"), ("codec
                    ("error_bound", "<f8"), ("crc", "<u4"), ("_pad", "<u4"), ("out_offset", "<u8")], align=True)
 MCGRID_DT = np.dtype([("grid_offset", "<u8"), ("dims", "<i4", 3), ("_pad", "<i4"), ("origin", "<f8", 3),
                       ("spacing", "<f8", 3)], align=True)
+STITCH_DT = np.dtype([("window_offset", "<u8"), ("origin", "<i4", 3), ("extent", "<i4", 3), ("block_lo", "<i4", 3),
+                      ("block_hi", "<i4", 3)])  # chr_stitch_t
+assert STITCH_DT.itemsize == 56
 assert REGION_DT.itemsize == ctypes.sizeof(Region)
 assert DEC_DT.itemsize == ctypes.sizeof(DecRegion)
 assert MCGRID_DT.itemsize == ctypes.sizeof(McGrid)
@@ -179,6 +182,12 @@ def lib():
         L.chr_compress2.argtypes = [P, INT, INT, I64, I64, I64, P, I64, D, D, P, INT, P, I64, INT, INT, D, P, SZ,
                                     P, U64, P, P]
         L.chr_compress2.restype = INT
+        L.chr_stitch_workspace_size.argtypes = [I64, I64, I64, I64, I64]
+        L.chr_stitch_workspace_size.restype = SZ
+        L.chr_stitch.argtypes = [P, P, I64, I64, I64, I64, I64, P, SZ, P, P]
+        L.chr_stitch.restype = INT
+        L.chr_topology_compare.argtypes = [P, INT, P, INT, I64, I64, I64, D, P, SZ, P, P, P]
+        L.chr_topology_compare.restype = INT
         L.chr_mask_words.argtypes = [P, I64]
         L.chr_mask_words.restype = U64
         L.chr_decode_regions_mask.argtypes = [P, P, I64, P, P, SZ, P, D, P, P]
@@ -207,6 +216,7 @@ EXPORTS = [
     "chr_rle_encode_workspace_size", "chr_rle_encode", "chr_sm_copy",
     "chr_mask_words", "chr_decode_regions_mask", "chr_mc_count_masked", "chr_mc_emit_masked",
     "chr_select_workspace_size", "chr_select_distances", "chr_compress2",
+    "chr_stitch_workspace_size", "chr_stitch", "chr_topology_compare",
     "chr_dcompress_workspace_size", "chr_dcompress_local", "chr_dcompress_finish", "chr_dcompress_headers",
     "chr_abi_version", "chr_status_string", "chr_num_blocks", "chr_stats", "chr_plan",
     "chr_compress_workspace_size", "chr_compress_capacity", "chr_compress",

@@ -110,6 +110,9 @@ class RequestReport:
 class ReconstructionSet:
     regions: tuple
     report: RequestReport
+    # the decoded windows still on the device (f64, element offsets) and the
+    # archive's block size, when produced by request(): stitch reuses them
+    _device: tuple | None = field(default=None, compare=False, repr=False)
 
 
 def _check_build_args(accuracy, bound_mode, safety_factor, loose_fraction, out_of_range):
@@ -261,16 +264,49 @@ def request(archive: CHRArchive, k: float, accuracy=None, drop_pruned: bool = Tr
             d = r.block.dims
             n = d[0] * d[1] * d[2]
             arrays.append(host[o:o + n].reshape(d, order="F").copy())
-    return ReconstructionSet(tuple(zip(regs, arrays)), report)
+    dev = (windows, list(woffs), archive.block_size) if builtin and regs else None
+    return ReconstructionSet(tuple(zip(regs, arrays)), report, dev)
+
+
+def _stitch_bs(regions, dims) -> tuple[int, bool]:
+    """Block size from the regions' spans (origin = lo * bs); (max dim, True)
+    when no region starts past block 0 (one region: spans are irrelevant)."""
+    for r in regions:
+        for a in range(3):
+            lo = r.block_span[0][a]
+            if lo > 0:
+                return r.sample_origin[a] // lo, False
+    return max(max(dims) - 1, 1), True
+
+
+def stitch_device(recon: ReconstructionSet, dims, fill: float = np.nan) -> torch.Tensor:
+    """stitch() leaving the volume on the device: a (nx, ny, nz) float64
+    view of an x-fastest buffer (chr_stitch; every sample written once by
+    its owner, the region with the lowest (z, y, x) origin)."""
+    dims = tuple(int(d) for d in dims)
+    regs = [r for r, _ in recon.regions]
+    if recon._device is not None:
+        windows, woffs, bs = recon._device
+        single = False
+    else:
+        arrays = [np.asarray(a, dtype=np.float64) for _, a in recon.regions]
+        woffs = list(np.cumsum([0] + [a.size for a in arrays])[:-1])
+        flat = np.concatenate([a.ravel(order="F") for a in arrays]) if arrays else np.zeros(1)
+        windows = torch.from_numpy(flat).to(_abi.device())
+        bs, single = _stitch_bs(regs, dims)
+    t = np.zeros(len(regs), dtype=_abi.STITCH_DT)
+    for i, (r, o) in enumerate(zip(regs, woffs)):
+        t[i] = (o, r.sample_origin, r.sample_extent, (0, 0, 0) if single else r.block_span[0],
+                (0, 0, 0) if single else r.block_span[1])
+    out = device.stitch(windows, t, dims, bs, fill)
+    return out.view(dims[2], dims[1], dims[0]).permute(2, 1, 0)
 
 
 def stitch(recon: ReconstructionSet, dims, fill: float = np.nan) -> np.ndarray:
-    """Owner-wins reassembly (chr_archive.py:277-294): lower (z,y,x) origin lands last."""
-    out = np.full(dims, fill, dtype=np.float64, order="F")
-    for region, samples in sorted(recon.regions, key=lambda p: tuple(reversed(p[0].sample_origin)), reverse=True):
-        (ox, oy, oz), (ex, ey, ez) = region.sample_origin, region.sample_extent
-        out[ox:ox + ex, oy:oy + ey, oz:oz + ez] = samples
-    return out
+    """chr_archive.stitch (chr_archive.py:277-294) on the GPU: owner-wins
+    reassembly, the lower (z, y, x) origin wins; returns the numpy grid."""
+    v = stitch_device(recon, dims, fill)
+    return v.permute(2, 1, 0).cpu().numpy().reshape(-1).reshape(tuple(int(d) for d in dims), order="F")
 
 
 def serialize(archive: CHRArchive) -> bytes:

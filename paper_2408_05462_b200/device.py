@@ -387,6 +387,39 @@ def case_codes(grid: torch.Tensor, dims, k: float, binary: bool = True) -> torch
     return codes
 
 
+def stitch(windows: torch.Tensor, table: np.ndarray, dims, bs: int, fill: float = float("nan"),
+           out: torch.Tensor | None = None) -> torch.Tensor:
+    """chr_archive.stitch (chr_archive.py:277-294) on the device: f64
+    windows (``table``: ``_abi.STITCH_DT``) -> flat f64 volume, x fastest,
+    every sample written by its owner (lowest (z, y, x) origin)."""
+    nx, ny, nz = dims
+    n = nx * ny * nz
+    if out is None:
+        out = torch.full((n,), fill, dtype=torch.float64, device=_abi.device())
+    else:
+        out[:n].fill_(fill)
+    L = lib()
+    t = np.ascontiguousarray(table, dtype=_abi.STITCH_DT)
+    if t.size:
+        work = _DEFAULT_WS.get("stitch", L.chr_stitch_workspace_size(t.size, nx, ny, nz, int(bs)))
+        check(L.chr_stitch(ptr(windows), _abi.aptr(t), t.size, nx, ny, nz, int(bs), ptr(work), work.numel(),
+                           ptr(out), stream_ptr()), "chr_stitch")
+    return out
+
+
+def topology_compare(a: torch.Tensor, b: torch.Tensor, dims, k: float) -> tuple[int, int]:
+    """Cells whose binary case codes differ at k (isosurf.verify_topology,
+    isosurf.py:91-114): (count, smallest differing cell index or -1)."""
+    nx, ny, nz = dims
+    L = lib()
+    work = _DEFAULT_WS.get("topo", 16)
+    nd, first = ctypes.c_uint64(0), ctypes.c_int64(-1)
+    check(L.chr_topology_compare(ptr(a), _dtype_code(a), ptr(b), _dtype_code(b), nx, ny, nz, float(k), ptr(work),
+                                 work.numel(), ctypes.byref(nd), ctypes.byref(first), stream_ptr()),
+          "chr_topology_compare")
+    return int(nd.value), int(first.value)
+
+
 def crc32(buf: torch.Tensor, nbytes: int | None = None) -> int:
     n = buf.numel() if nbytes is None else int(nbytes)
     L = lib()

@@ -61,7 +61,8 @@ def _grid(samples) -> tuple[torch.Tensor, tuple[int, int, int]]:
     g = np.asarray(samples, dtype=np.float64)
     if g.ndim != 3 or any(n < 2 for n in g.shape):
         raise ParameterError(f"need a 3D grid with >= 2 samples per axis, got {g.shape}")
-    return torch.from_numpy(np.ascontiguousarray(g.ravel(order="F"))).to(_abi.device()), tuple(g.shape)
+    flat = np.require(g.ravel(order="F"), requirements=["C", "W"])
+    return torch.from_numpy(flat).to(_abi.device()), tuple(g.shape)
 
 
 def cell_case(corners, k: float) -> int:
@@ -76,20 +77,29 @@ def case_field(samples, k: float) -> CaseField:
     return CaseField(tuple(d - 1 for d in dims), codes)
 
 
+def _grid_native(samples):
+    """Like _grid, but device tensors keep float32 (the comparison kernel
+    reads f32 or f64 directly): no widening copy of a resident volume."""
+    if isinstance(samples, torch.Tensor) and samples.dtype in (torch.float32, torch.float64) \
+            and samples.device.type == "cuda" and samples.ndim == 3:
+        g = samples
+        if any(n < 2 for n in g.shape):
+            raise ParameterError(f"need a 3D grid with >= 2 samples per axis, got {tuple(g.shape)}")
+        return g.permute(2, 1, 0).contiguous().reshape(-1), tuple(int(d) for d in g.shape)
+    return _grid(samples)
+
+
 def verify_topology(original, reconstructed, k: float) -> TopologyReport:
-    """Fraction of cells whose case codes agree (isosurf.py:91-114)."""
-    a, da = _grid(original)
-    b, db = _grid(reconstructed)
+    """Fraction of cells whose case codes agree (isosurf.py:91-114), one
+    fused comparison kernel (chr_topology_compare)."""
+    a, da = _grid_native(original)
+    b, db = _grid_native(reconstructed)
     if da != db:
         raise ParameterError(f"shape mismatch: {da} vs {db}")
-    ca = device.case_codes(a, da, float(k))
-    cb = device.case_codes(b, db, float(k))
-    diff = ca != cb
-    nd = int(diff.sum())
-    total = ca.numel()
+    nd, flat = device.topology_compare(a, b, da, float(k))
+    total = (da[0] - 1) * (da[1] - 1) * (da[2] - 1)
     first = None
     if nd:
-        flat = int(torch.argmax(diff.to(torch.uint8)))
         ncx, ncy = da[0] - 1, da[1] - 1
         cz, rem = divmod(flat, ncx * ncy)
         cy, cx = divmod(rem, ncx)

@@ -185,7 +185,17 @@ def archive_case(name, vol, cands, bs, input_from=None, **kw):
                                 k=k)
             meshes.append(mm)
         merged = isochr.merge_meshes(meshes)
+        st = isochr.stitch(rs, vol.dims)  # pruned request: NaN outside the selection
+        full = isochr.stitch(isochr.request(arch, k, drop_pruned=False), vol.dims)
+        topo = isochr.verify_topology(vol.grid, full, k)
+        topo_p = isochr.verify_topology(vol.grid, st, k)
         info["requests"][repr(k)] = {
+            "stitch_sha": sha(st.ravel(order="F")),
+            "full_stitch_sha": sha(full.ravel(order="F")),
+            "topo_full": [topo.preserved_fraction, topo.differing_cells, topo.total_cells,
+                          list(topo.first_diff) if topo.first_diff else None],
+            "topo_pruned": [topo_p.preserved_fraction, topo_p.differing_cells, topo_p.total_cells,
+                            list(topo_p.first_diff) if topo_p.first_diff else None],
             "regions": [r.region_id for r, _ in rs.regions],
             "recon_sha": [sha(np.asarray(s).ravel(order="F")) for _, s in rs.regions],
             "bytes_touched": rs.report.bytes_touched,

@@ -164,6 +164,18 @@ def test_golden_archives(golden, golden_meta, name, tmp_path):
         # the same request decoded from the re-read (host) archive
         rs2 = G.request(back, k)
         assert all(np.array_equal(a, b) for (_, a), (_, b) in zip(rs.regions, rs2.regions))
+        # stitch + verify_topology on the device
+        st = G.stitch(rs, vol.dims)
+        assert sha(st.ravel(order="F")) == ref["stitch_sha"]
+        full = G.stitch_device(G.request(arch, k, drop_pruned=False), vol.dims)
+        assert sha(full.permute(2, 1, 0).cpu().numpy()) == ref["full_stitch_sha"]
+        for rep, want in ((G.verify_topology(vol.grid, full, k), ref["topo_full"]),
+                          (G.verify_topology(vol.grid, st, k), ref["topo_pruned"])):
+            assert [rep.preserved_fraction, rep.differing_cells, rep.total_cells,
+                    list(rep.first_diff) if rep.first_diff else None] == want
+        # the host-array path (windows re-uploaded, block size inferred)
+        rs_host = G.ReconstructionSet(rs.regions, rs.report)
+        assert sha(G.stitch(rs_host, vol.dims).ravel(order="F")) == ref["stitch_sha"]
         regs, wins, offs, _, _ = G.request_device(arch, k)
         v, t, nt, nv = G.extract_device(wins, regs, offs, vol.spacing, k) if regs else (None, None, [], [])
         if regs:
@@ -448,3 +460,40 @@ def test_select_distances_vs_numpy(mode):
                 continue
             nn = O.select_index(d.size, acc)
             assert v == np.partition(d, nn - 1)[nn - 1], (acc, k)
+
+
+# ----------------------------------------------------------------- SURVEY 8(f3)
+@pytest.mark.parametrize("shape", [(2, 2, 2), (33, 9, 17), (70, 3, 40), (5, 130, 2), (64, 64, 33)])
+def test_topology_compare_vs_oracle(shape):
+    rng = np.random.default_rng(sum(shape))
+    a = rng.normal(size=shape)
+    b = a.copy()
+    flip = rng.random(size=shape) < 0.01
+    b[flip] = -b[flip]
+    b.reshape(-1)[-1] = np.nan  # NaN is "outside" on both sides of >=
+    want = O.verify_topology(a.ravel(order="F"), b.ravel(order="F"), shape, 0.0)
+    for x, y in ((a, b), (torch.from_numpy(a).cuda().float(), torch.from_numpy(b).cuda())):
+        rep = G.verify_topology(x, y, 0.0) if isinstance(x, np.ndarray) else None
+        if rep is None:  # f32 original resident on the device vs f64 reconstruction
+            rep = G.verify_topology(x, y, 0.0)
+            want = O.verify_topology(a.astype(np.float32).astype(np.float64).ravel(order="F"),
+                                     b.ravel(order="F"), shape, 0.0)
+        assert [rep.preserved_fraction, rep.differing_cells, rep.total_cells,
+                list(rep.first_diff) if rep.first_diff else None] == want
+
+
+@pytest.mark.parametrize("name,n", [("c2", 96), ("c5", 72)])
+def test_stitch_and_topology_at_config(name, n):
+    """Full (unpruned) request stitched on the device == the oracle's
+    stitch, and strict accuracy-1 archives preserve every cell case."""
+    vals, dims, bs, cands, rr = synth.make_config(name, device="cuda", n=n)
+    vol = G.Volume(dims, (1.0, 1.0, 1.0), vals.cpu().numpy().astype(np.float64), "f32")
+    arch = G.build_chr(vol, cands, bs, loose_fraction=rr)
+    ref = O.build_chr(vals.cpu().numpy().astype(np.float64), dims, cands, bs, loose_fraction=rr, workers=8)
+    for k in cands[:2]:
+        full = G.stitch_device(G.request(arch, k, drop_pruned=False), dims)
+        want = O.stitch(O.request(ref, k, drop_pruned=False), dims)
+        assert np.array_equal(full.permute(2, 1, 0).reshape(-1).cpu().numpy(), want)
+        resident = vals.view(dims[2], dims[1], dims[0]).permute(2, 1, 0)  # f32, no widening copy
+        rep = G.verify_topology(resident, full, k)
+        assert rep.preserved_fraction == 1.0 and rep.differing_cells == 0

@@ -111,3 +111,11 @@ def test_archives_byte_identical(golden, golden_meta, name):
         assert O.bytes_touched(arch, sel) == ref["bytes_touched"]
         v, t = O.extract_regions(sel, tuple(info["spacing"]), k)
         assert sha(v) == ref["merged_v_sha"] and sha(t) == ref["merged_t_sha"]
+        # stitch + verify_topology
+        dims = tuple(info["dims"])
+        st = O.stitch(sel, dims)
+        assert sha(st) == ref["stitch_sha"]
+        full = O.stitch(O.request(arch, k, drop_pruned=False), dims)
+        assert sha(full) == ref["full_stitch_sha"]
+        assert O.verify_topology(vals, full, dims, k) == ref["topo_full"]
+        assert O.verify_topology(vals, st, dims, k) == ref["topo_pruned"]
