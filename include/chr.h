@@ -303,6 +303,62 @@ int chr_topology_compare(const void *d_a, int dtype_a, const void *d_b, int dtyp
                          int64_t nz, double k, void *d_workspace, size_t workspace_bytes, uint64_t *h_ndiff,
                          int64_t *h_first, void *stream);
 
+/* 15. SURVEY 8(f1): read_chr on the device (chr_archive.py:343-407).
+ *     Step 1, chr_read_header: the fixed header, m, the region count and
+ *     the stored trailer CRC (small device->host copies); sets
+ *     info.error for a short file / bad magic / a table past the end.
+ *     Step 2, chr_read_archive: whole-file CRC-32 and one thread per region
+ *     record parsing the table entry + the 34-byte block header it points
+ *     at, with the reference's checks (status per entry); the candidates
+ *     and the table come back in one synchronised copy.  The caller raises
+ *     the reference's exceptions in its order: too short, magic, CRC,
+ *     version, then the first region with a nonzero status. */
+enum {
+    CHR_READ_OK = 0,
+    CHR_READ_TOO_SHORT = 1,
+    CHR_READ_BAD_MAGIC = 2,
+    CHR_READ_TABLE_PAST_END = 3,
+    CHR_READ_PAYLOAD_PAST_END = 4,       /* poffset + plen > len(file) - 4 */
+    CHR_READ_BLOCK_HEADER_TRUNCATED = 5, /* < 34 bytes at poffset */
+    CHR_READ_PAYLOAD_TRUNCATED = 6,      /* block header length past the file */
+    CHR_READ_LENGTH_MISMATCH = 7         /* 34 + payload length != table length */
+};
+
+typedef struct {
+    char magic[4];
+    uint32_t version;
+    uint32_t dims[3];
+    double spacing[3];
+    uint32_t dtype;
+    uint32_t block_size;
+    double vmin, vmax;
+    uint32_t m;
+    uint32_t n_regions;
+    uint64_t table_nbytes;     /* header_table_nbytes: first byte after the table */
+    uint32_t stored_crc, actual_crc;
+    int32_t error;             /* CHR_READ_* found by chr_read_header */
+    int32_t _pad;
+} chr_file_info_t;
+
+typedef struct {
+    chr_region_t region;       /* geometry, mask (first 64 candidates), table error bound,
+                                  block offset/length; codec id + payload CRC from the block header */
+    uint32_t region_id;
+    int32_t status;            /* CHR_READ_* */
+    uint32_t bound_mode;
+    uint32_t block_dtype;
+    double accuracy;
+    uint32_t block_dims[3];
+    uint32_t _pad;
+    double block_error_bound;
+    uint64_t payload_len;
+} chr_table_entry_t;
+
+int chr_read_header(const uint8_t *d_file, uint64_t nbytes, chr_file_info_t *h_info, void *stream);
+size_t chr_read_workspace_size(uint64_t nbytes, int64_t n_regions);
+int chr_read_archive(const uint8_t *d_file, uint64_t nbytes, chr_file_info_t *h_info, double *h_cands,
+                     chr_table_entry_t *h_entries, void *d_workspace, size_t workspace_bytes, void *stream);
+
 /* 9. instrumentation: launch counter and opt-in per-kernel CUDA-event
  *    timing on the launching stream ("name count total_ms" lines). */
 void chr_prof_enable(int on);

@@ -106,6 +106,16 @@ MCGRID_DT = np.dtype([("grid_offset", "<u8"), ("dims", "<i4", 3), ("_pad", "<i4"
 STITCH_DT = np.dtype([("window_offset", "<u8"), ("origin", "<i4", 3), ("extent", "<i4", 3), ("block_lo", "<i4", 3),
                       ("block_hi", "<i4", 3)])  # chr_stitch_t
 assert STITCH_DT.itemsize == 56
+FILE_INFO_DT = np.dtype([("magic", "S4"), ("version", "<u4"), ("dims", "<u4", 3), ("spacing", "<f8", 3),
+                         ("dtype", "<u4"), ("block_size", "<u4"), ("vmin", "<f8"), ("vmax", "<f8"), ("m", "<u4"),
+                         ("n_regions", "<u4"), ("table_nbytes", "<u8"), ("stored_crc", "<u4"),
+                         ("actual_crc", "<u4"), ("error", "<i4"), ("_pad", "<i4")], align=True)  # chr_file_info_t
+TABLE_ENTRY_DT = np.dtype([("region", REGION_DT), ("region_id", "<u4"), ("status", "<i4"), ("bound_mode", "<u4"),
+                           ("block_dtype", "<u4"), ("accuracy", "<f8"), ("block_dims", "<u4", 3), ("_pad", "<u4"),
+                           ("block_error_bound", "<f8"), ("payload_len", "<u8")], align=True)  # chr_table_entry_t
+assert FILE_INFO_DT.itemsize == 104 and TABLE_ENTRY_DT.itemsize == 152
+READ_TOO_SHORT, READ_BAD_MAGIC, READ_TABLE_PAST_END, READ_PAYLOAD_PAST_END = 1, 2, 3, 4
+READ_BLOCK_HEADER_TRUNCATED, READ_PAYLOAD_TRUNCATED, READ_LENGTH_MISMATCH = 5, 6, 7
 assert REGION_DT.itemsize == ctypes.sizeof(Region)
 assert DEC_DT.itemsize == ctypes.sizeof(DecRegion)
 assert MCGRID_DT.itemsize == ctypes.sizeof(McGrid)
@@ -188,6 +198,12 @@ def lib():
         L.chr_stitch.restype = INT
         L.chr_topology_compare.argtypes = [P, INT, P, INT, I64, I64, I64, D, P, SZ, P, P, P]
         L.chr_topology_compare.restype = INT
+        L.chr_read_header.argtypes = [P, U64, P, P]
+        L.chr_read_header.restype = INT
+        L.chr_read_workspace_size.argtypes = [U64, I64]
+        L.chr_read_workspace_size.restype = SZ
+        L.chr_read_archive.argtypes = [P, U64, P, P, P, P, SZ, P]
+        L.chr_read_archive.restype = INT
         L.chr_mask_words.argtypes = [P, I64]
         L.chr_mask_words.restype = U64
         L.chr_decode_regions_mask.argtypes = [P, P, I64, P, P, SZ, P, D, P, P]
@@ -217,6 +233,7 @@ EXPORTS = [
     "chr_mask_words", "chr_decode_regions_mask", "chr_mc_count_masked", "chr_mc_emit_masked",
     "chr_select_workspace_size", "chr_select_distances", "chr_compress2",
     "chr_stitch_workspace_size", "chr_stitch", "chr_topology_compare",
+    "chr_read_header", "chr_read_workspace_size", "chr_read_archive",
     "chr_dcompress_workspace_size", "chr_dcompress_local", "chr_dcompress_finish", "chr_dcompress_headers",
     "chr_abi_version", "chr_status_string", "chr_num_blocks", "chr_stats", "chr_plan",
     "chr_compress_workspace_size", "chr_compress_capacity", "chr_compress",

@@ -346,50 +346,78 @@ def write_chr(archive: CHRArchive, path) -> None:
         fh.write(serialize(archive))
 
 
+def _upload_file(blob: bytes) -> torch.Tensor:
+    """The file in HBM (+16 zero bytes of slack for aligned word reads)."""
+    host = torch.empty(len(blob) + 16, dtype=torch.uint8, pin_memory=True)
+    host[: len(blob)].numpy()[:] = np.frombuffer(blob, dtype=np.uint8)
+    host[len(blob):] = 0
+    return host.to(_abi.device(), non_blocking=True)
+
+
 def read_chr(path) -> CHRArchive:
-    """chr_archive.read_chr (chr_archive.py:343-407); the trailer CRC is
-    verified on the GPU."""
+    """chr_archive.read_chr (chr_archive.py:343-407): the file goes to HBM
+    once; the whole-file CRC, the header and every region record + block
+    header are validated there (device.read_table); the same exceptions
+    are raised in the reference's order.  The device copy stays attached,
+    so a following request() decodes without another upload."""
     with open(path, "rb") as fh:
         blob = fh.read()
-    if len(blob) < _FILE_HDR.size + 4:
+    n = len(blob)
+    if n < _FILE_HDR.size + 4:
         raise ChecksumError(f"{path}: file too short to be a CHR archive")
     if blob[:4] != MAGIC:
         raise BadMagicError(f"{path}: bad magic {blob[:4]!r}, expected {MAGIC!r}")
-    stored = struct.unpack_from("<I", blob, len(blob) - 4)[0]
-    actual = _gpu_crc(blob[:-4])
-    if stored != actual:
-        raise ChecksumError(f"{path}: checksum mismatch (stored {stored:#010x}, computed {actual:#010x})")
-    (_, version, nx, ny, nz, dx, dy, dz, tag, bs, vmin, vmax) = _FILE_HDR.unpack_from(blob, 0)
-    if version != VERSION:
+    file_dev = _upload_file(blob)
+    ft = device.read_table(file_dev, n)
+    info = ft.info[0]
+    if int(info["stored_crc"]) != int(info["actual_crc"]):
+        raise ChecksumError(f"{path}: checksum mismatch (stored {int(info['stored_crc']):#010x}, "
+                            f"computed {int(info['actual_crc']):#010x})")
+    if int(info["version"]) != VERSION:
         from .exceptions import VersionError
 
-        raise VersionError(f"{path}: unsupported CHR version {version}")
-    pos = _FILE_HDR.size
-    (m,) = struct.unpack_from("<I", blob, pos)
-    pos += 4
-    cands = struct.unpack_from(f"<{m}d", blob, pos)
-    pos += 8 * m
+        raise VersionError(f"{path}: unsupported CHR version {int(info['version'])}")
+    if int(info["error"]) == _abi.READ_TABLE_PAST_END:
+        raise struct.error(f"{path}: region table extends past the end of the file")
+    m = int(info["m"])
     mb = (m + 7) // 8
-    (nreg,) = struct.unpack_from("<I", blob, pos)
-    pos += 4
-    regions = []
-    for _ in range(nreg):
-        f = _REC.unpack_from(blob, pos)
-        pos += _REC.size
-        mask = int.from_bytes(blob[pos:pos + mb], "little")
-        pos += mb
-        (rid, lx, ly, lz, hx, hy, hz, ox, oy, oz, ex, ey, ez, mode, acc, eb, poff, plen) = f
-        if poff + plen > len(blob) - 4:
+    ent = ft.entries
+    bad = np.nonzero(ent["status"])[0]
+    if bad.size:
+        e = ent[int(bad[0])]
+        rid, st = int(e["region_id"]), int(e["status"])
+        if st == _abi.READ_PAYLOAD_PAST_END:
             raise ChecksumError(f"{path}: region {rid} payload exceeds file size")
-        blk = CompressedBlock.from_bytes(blob, poff)
-        if blk.nbytes != plen:
-            raise ChecksumError(f"{path}: region {rid} payload length mismatch (table {plen}, block {blk.nbytes})")
-        regions.append(ArchiveRegion(rid, ((lx, ly, lz), (hx, hy, hz)), (ox, oy, oz), (ex, ey, ez),
-                                     frozenset(ci for ci in range(m) if (mask >> ci) & 1), _MODES[mode], acc, eb,
-                                     blk))
-    dtype = {v: k for k, v in DTYPE_TAGS.items()}[tag]
-    return CHRArchive((nx, ny, nz), (dx, dy, dz), dtype, bs, (vmin, vmax), tuple(cands), tuple(regions),
-                      {"file": blob})
+        if st == _abi.READ_BLOCK_HEADER_TRUNCATED:
+            raise struct.error(f"{path}: region {rid} block header truncated")
+        if st == _abi.READ_PAYLOAD_TRUNCATED:
+            avail = n - int(e["region"]["block_offset"]) - HEADER_SIZE
+            raise CorruptPayloadError(f"payload truncated: header says {int(e['payload_len'])} bytes, "
+                                      f"{avail} available")
+        raise ChecksumError(f"{path}: region {rid} payload length mismatch (table {int(e['region']['block_nbytes'])}, "
+                            f"block {HEADER_SIZE + int(e['payload_len'])})")
+    names = {0: "f32", 1: "f64"}
+    table0 = int(info["table_nbytes"]) - len(ent) * (_REC.size + mb)
+    regions = []
+    for i, e in enumerate(ent):
+        r = e["region"]
+        if m <= 64:
+            mask = int(r["mask"])
+        else:  # wider masks than the device entry holds: from the record bytes
+            p = table0 + i * (_REC.size + mb) + _REC.size
+            mask = int.from_bytes(blob[p:p + mb], "little")
+        off = int(r["block_offset"]) + HEADER_SIZE
+        blk = CompressedBlock(int(r["codec_id"]), tuple(int(d) for d in e["block_dims"]),
+                              float(e["block_error_bound"]), names[int(e["block_dtype"])],
+                              blob[off:off + int(e["payload_len"])], int(r["payload_crc"]))
+        regions.append(ArchiveRegion(int(e["region_id"]), (tuple(int(v) for v in r["lo"]), tuple(int(v) for v in r["hi"])),
+                                     tuple(int(v) for v in r["origin"]), tuple(int(v) for v in r["extent"]),
+                                     frozenset(ci for ci in range(m) if (mask >> ci) & 1),
+                                     _MODES[int(e["bound_mode"])], float(e["accuracy"]), float(r["error_bound"]), blk))
+    dtype = {v: k for k, v in DTYPE_TAGS.items()}[int(info["dtype"])]
+    return CHRArchive(tuple(int(d) for d in info["dims"]), tuple(float(s) for s in info["spacing"]), dtype,
+                      int(info["block_size"]), (float(info["vmin"]), float(info["vmax"])),
+                      tuple(float(c) for c in ft.candidates), tuple(regions), {"file": blob, "blob": file_dev})
 
 
 __all__ = ["ArchiveRegion", "CHRArchive", "RequestReport", "ReconstructionSet", "build_chr", "request",

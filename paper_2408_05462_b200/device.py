@@ -420,6 +420,43 @@ def topology_compare(a: torch.Tensor, b: torch.Tensor, dims, k: float) -> tuple[
     return int(nd.value), int(first.value)
 
 
+@dataclass
+class FileTable:
+    """read_chr's parse of a device-resident .chr file (chr_read_header +
+    chr_read_archive): header fields, candidates, and the region table as
+    ``_abi.TABLE_ENTRY_DT`` (``entries["region"]`` is a ``REGION_DT`` table
+    the decode / marching entry points take directly)."""
+    info: np.ndarray
+    candidates: np.ndarray
+    entries: np.ndarray
+
+    @property
+    def regions(self) -> np.ndarray:
+        return self.entries["region"]
+
+
+def read_table(file_dev: torch.Tensor, nbytes: int) -> FileTable:
+    """Validate + parse a .chr file already in HBM.  No exception is raised
+    here: ``info["error"]``, the stored/actual CRCs and ``entries["status"]``
+    carry the outcome so the caller can raise in the reference's order."""
+    L = lib()
+    info = np.zeros(1, dtype=_abi.FILE_INFO_DT)
+    check(L.chr_read_header(ptr(file_dev), int(nbytes), _abi.aptr(info), stream_ptr()), "chr_read_header")
+    err = int(info["error"][0])
+    if err in (_abi.READ_TOO_SHORT, _abi.READ_BAD_MAGIC):
+        return FileTable(info, np.zeros(0), np.zeros(0, dtype=_abi.TABLE_ENTRY_DT))
+    nreg = int(info["n_regions"][0]) if err == 0 else 0
+    m = int(info["m"][0])
+    cands = np.zeros(m if 67 + 8 * m <= nbytes else 0, dtype=np.float64)
+    entries = np.zeros(nreg, dtype=_abi.TABLE_ENTRY_DT)
+    work = _DEFAULT_WS.get("read", L.chr_read_workspace_size(int(nbytes), nreg))
+    if err:
+        info["n_regions"] = 0
+    check(L.chr_read_archive(ptr(file_dev), int(nbytes), _abi.aptr(info), _np_ptr(cands) if cands.size else None,
+                             _abi.aptr(entries), ptr(work), work.numel(), stream_ptr()), "chr_read_archive")
+    return FileTable(info, cands, entries)
+
+
 def crc32(buf: torch.Tensor, nbytes: int | None = None) -> int:
     n = buf.numel() if nbytes is None else int(nbytes)
     L = lib()

@@ -497,3 +497,82 @@ def test_stitch_and_topology_at_config(name, n):
         resident = vals.view(dims[2], dims[1], dims[0]).permute(2, 1, 0)  # f32, no widening copy
         rep = G.verify_topology(resident, full, k)
         assert rep.preserved_fraction == 1.0 and rep.differing_cells == 0
+
+
+# ----------------------------------------------------------------- SURVEY 8(f1)
+def _fix_crc(b: bytearray) -> bytes:
+    import struct
+    import zlib
+
+    b[-4:] = struct.pack("<I", zlib.crc32(bytes(b[:-4])))
+    return bytes(b)
+
+
+def test_read_chr_errors_in_reference_order(golden, tmp_path):
+    """read_chr validated on the device raises what chr_archive.read_chr
+    raises (chr_archive.py:343-407; test_chr.py:90-137)."""
+    import struct
+
+    blob = golden["smooth_chr"].tobytes()
+    p = tmp_path / "x.chr"
+    cases = [
+        (blob[:50], exceptions.ChecksumError, "too short"),
+        (b"XHR1" + blob[4:], exceptions.BadMagicError, "bad magic"),
+        (blob[:-1] + bytes([blob[-1] ^ 1]), exceptions.ChecksumError, "checksum mismatch"),
+        (blob[:-100] + blob[-4:], exceptions.ChecksumError, "checksum mismatch"),
+    ]
+    b = bytearray(blob)
+    b[4] = 99
+    cases.append((_fix_crc(b), exceptions.VersionError, "unsupported CHR version 99"))
+    m = struct.unpack_from("<I", blob, 63)[0]
+    rec0 = 63 + 4 + 8 * m + 4
+    b = bytearray(blob)  # region 0: payload offset far past the end
+    struct.pack_into("<Q", b, rec0 + 69, len(blob))
+    cases.append((_fix_crc(b), exceptions.ChecksumError, "region 0 payload exceeds file size"))
+    b = bytearray(blob)  # region 0: table length one byte short of the block
+    plen = struct.unpack_from("<Q", b, rec0 + 77)[0]
+    struct.pack_into("<Q", b, rec0 + 77, plen - 1)
+    cases.append((_fix_crc(b), exceptions.ChecksumError, f"(table {plen - 1}, block {plen})"))
+    for data, exc, msg in cases:
+        p.write_bytes(data)
+        with pytest.raises(exc, match=msg.replace("(", r"\(").replace(")", r"\)")):
+            G.read_chr(p)
+
+
+def test_read_chr_single_byte_corruption(tmp_path):
+    vol = G.Volume((10, 10, 10), (1.0, 1.0, 1.0), np.random.default_rng(3).normal(size=1000), "f64")
+    arch = G.build_chr(vol, [0.0], 4)
+    p = tmp_path / "c.chr"
+    G.write_chr(arch, p)
+    blob = p.read_bytes()
+    rng = np.random.default_rng(0)
+    positions = set(range(0, 64)) | {int(x) for x in rng.integers(0, len(blob), 150)} | set(range(len(blob) - 8, len(blob)))
+    q = tmp_path / "bad.chr"
+    for pos in sorted(positions):
+        t = bytearray(blob)
+        t[pos] ^= 1
+        q.write_bytes(bytes(t))
+        with pytest.raises(exceptions.IsochrError):
+            G.read_chr(q)
+    back = G.read_chr(p)
+    assert back == arch
+    # the device copy from read_chr serves the request without another upload
+    assert back._device["blob"].is_cuda
+    rs = G.request(back, 0.0)
+    rs0 = G.request(arch, 0.0)
+    assert all(np.array_equal(a, b) for (_, a), (_, b) in zip(rs.regions, rs0.regions))
+
+
+def test_read_table_at_config_size(tmp_path):
+    """The device parse of a device-built file matches the builder's table."""
+    vals, dims, bs, cands, rr = synth.make_config("c5", device="cuda", n=96)
+    res = device.build_archive(vals, dims, cands, bs, loose_fraction=rr)
+    ft = device.read_table(res.blob, res.nbytes)
+    info = ft.info[0]
+    assert int(info["stored_crc"]) == int(info["actual_crc"]) and int(info["error"]) == 0
+    assert list(ft.candidates) == list(cands)
+    assert not ft.entries["status"].any()
+    got, want = ft.regions, res.regions
+    for f in ("lo", "hi", "origin", "extent", "mask", "error_bound", "codec_id", "payload_crc", "block_offset",
+              "block_nbytes"):
+        assert np.array_equal(got[f], want[f]), f
