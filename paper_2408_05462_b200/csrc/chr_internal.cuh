@@ -6,7 +6,7 @@
 namespace chr {
 
 // ------------------------------------------------------------------ CRC
-constexpr int64_t kCrcScWords = 1024;  // words per superchunk (4 KiB): short serial chains, many warps
+constexpr int64_t kCrcScWords = 8192;  // words per superchunk (32 KiB): the per-superchunk lane combine + shift (~1600 instr/lane) amortised over 256 words/lane
 
 struct CrcSeg {
     uint64_t begin, end;  // byte range

@@ -556,9 +556,6 @@ __global__ void __launch_bounds__(EW * 32, 3) k_mc_emit2(const double *__restric
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const double *gp = grids + g.goff;
     const int64_t nxy = (int64_t)g.nx * g.ny;
-    // sample row of this warp: y0 - 1 + w ; columns c <-> x = x0 - 1 + c
-    const int sy = y0 - 1 + w;
-    const bool srow = sy >= 0 && sy < g.ny;
     // cell row of this warp (w < 9): cy = y0 - 1 + w ; cells c = 1 + lane, 33 + lane, and c = 0 (lane 0)
     const int cy = y0 - 1 + w;
     const bool crow = w < EW - 1 && cy >= 0 && cy < g.ncy;
@@ -575,15 +572,18 @@ __global__ void __launch_bounds__(EW * 32, 3) k_mc_emit2(const double *__restric
         pnext = base[pb_row + (int64_t)pstart * pb_step];
         cnext = cnt[pb_row + (int64_t)pstart * pb_step];
     }
-    // row masks of sample row sy, columns x0-1 .. x0+64 (bit c <-> x0 - 1 + c),
-    // read by lane 0 from the plane masks one plane ahead
+    // row masks of the EW sample rows, columns x0-1 .. x0+64 (bit c <-> x0 - 1
+    // + c): lane r of warp 0 reads row y0 - 1 + r from the plane masks one
+    // plane ahead (one warp instruction stream for all rows)
     const uint32_t *mbase = mask + g.mask_off;
+    const int my = y0 - 1 + lane;
+    const bool mrow = w == 0 && lane < EW && my >= 0 && my < g.ny;
     auto row_mask = [&](int p, uint64_t &m, uint32_t &mx) {
         m = 0;
         mx = 0;
-        if (!srow) return;
+        if (!mrow) return;
         const uint32_t *mp = mbase + (int64_t)p * g.pw;
-        const int64_t b = (int64_t)sy * g.nx + x0;
+        const int64_t b = (int64_t)my * g.nx + x0;
         if (x0 > 0) {
             mask_bits66(mp, b - 1, m, mx);
         } else {
@@ -594,28 +594,40 @@ __global__ void __launch_bounds__(EW * 32, 3) k_mc_emit2(const double *__restric
             mx = (uint32_t)(m1 >> 63) | ((h1 & 1u) << 1);
         }
     };
+    // One barrier per plane.  Iteration p: (A) warp 0 stores the masks of
+    // plane p+1 (ring slot (p+1)%3, last read in A of p-1, before the
+    // previous barrier); every row computes codes / vertex bases of cell
+    // plane cz = p-1 into ring slot cz%3 (read by B of p-1 only through
+    // slots (p-2)%3 and (p-3)%3); barrier; (B) emission of plane cz.
     uint64_t nm = 0;
     uint32_t nmx = 0;
-    if (lane == 0) row_mask(pstart, nm, nmx);
-    for (int p = pstart; p <= z1; ++p) {
-        const int pb = p % 3;
-        if (lane == 0) {
-            mk[pb][w] = nm;
-            mkx[pb][w] = nmx;
-            if (p < z1) row_mask(p + 1, nm, nmx);
+    if (w == 0) {
+        row_mask(pstart, nm, nmx);
+        if (lane < EW) {
+            mk[pstart % 3][lane] = nm;
+            mkx[pstart % 3][lane] = nmx;
         }
-        __syncthreads();
-        if (p == pstart) continue;  // need planes cz and cz+1
-        const int cz = p - 1, cb = cz % 3, qb = p % 3;
+        if (pstart < z1) row_mask(pstart + 1, nm, nmx);
+    }
+    for (int p = pstart; p <= z1; ++p) {
+        if (w == 0 && p < z1) {
+            if (lane < EW) {
+                mk[(p + 1) % 3][lane] = nm;
+                mkx[(p + 1) % 3][lane] = nmx;
+            }
+            if (p + 1 < z1) row_mask(p + 2, nm, nmx);
+        }
+        const bool codes = p > pstart;  // needs planes cz and cz+1
+        const int cz = p - 1, cb = (cz + 3) % 3, qb = p % 3;
         // ---- codes, owned counts, vertex bases of cell row cy at plane cz
         int codeA = 0, codeB = 0, ntA = 0, ntB = 0, tA = 0, tB = 0, ownA = 0, ownB = 0, exA = 0, exB = 0;
         const McPieceBase pbase = pnext;
         const McPieceCnt pcnt = cnext;
-        if (crow && cz + 1 < z1) {
+        if (codes && crow && cz + 1 < z1) {
             pnext = base[pb_row + (int64_t)(cz + 1) * pb_step];
             cnext = cnt[pb_row + (int64_t)(cz + 1) * pb_step];
         }
-        if (w < EW - 1) {
+        if (codes && w < EW - 1) {
             int codeH = 0, ownH = 0;
             uint64_t m00 = 0, m10 = 0, m01 = 0, m11 = 0;
             uint32_t h00 = 0, h10 = 0, h01 = 0, h11 = 0;
