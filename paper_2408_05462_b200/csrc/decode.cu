@@ -1446,23 +1446,31 @@ static bool band_shape(DecReg &R) {
     const int rs = R.ex | 1;
     if (rs > BCAP) return false;
     const int K = BCAP / rs;  // rows (y * z) per tile
-    int bty, btz;
+    int bty = 0, btz = 0;
     if ((int64_t)R.ey * R.ez <= K && R.ez <= BSEGM) {
         bty = R.ey;
         btz = R.ez;
-    } else if (R.ey <= K && K / R.ey >= 4) {
-        bty = R.ey;
-        btz = std::min({R.ez, K / R.ey, BSEGM});
     } else {
-        const double t = std::sqrt((double)K * R.ey / std::max(1, R.ez));
-        bty = std::max(1, std::min({R.ey, K, (int)t}));
-        bty = std::max(bty, std::min({R.ey, K, 8}));
-        btz = std::max(1, std::min({R.ez, K / bty, BSEGM}));
-        bty = std::max(1, std::min(R.ey, K / btz));
-    }
-    if (bty < R.ey) {  // a band below exists: its dF (btz x ex) must fit
-        btz = std::min(btz, BDF / R.ex);
-        if (btz < 1) return false;
+        // the tiles of a region form a (band, chunk) grid whose dependency
+        // chains are tny + tnz - 1 hops long (band above, chunk before): pick
+        // the shape with the shortest chain, then the fewest tiles
+        int64_t best_chain = INT64_MAX, best_tiles = INT64_MAX;
+        for (int ty = 1; ty <= std::min(R.ey, K); ++ty) {
+            int tz = std::min({R.ez, K / ty, BSEGM});
+            if (ty < R.ey) tz = std::min(tz, BDF / R.ex);  // a band below exists: its dF (tz x ex) must fit
+            if (tz < 1) continue;
+            const int ty2 = std::min(R.ey, K / tz);  // widest band for this chunk depth
+            const int64_t ny = ceil_div(R.ey, ty2), nz = ceil_div(R.ez, tz);
+            if (ty2 < R.ey && tz > BDF / R.ex) continue;
+            const int64_t chain = ny + nz - 1, tiles = ny * nz;
+            if (chain < best_chain || (chain == best_chain && tiles < best_tiles)) {
+                best_chain = chain;
+                best_tiles = tiles;
+                bty = ty2;
+                btz = tz;
+            }
+        }
+        if (bty < 1) return false;
     }
     R.rs = rs;
     R.bty = bty;

@@ -409,10 +409,13 @@ __global__ void __launch_bounds__(256) k_summarize(const RegDev *__restrict__ re
         const uint32_t bA = mA & lt, bB = mB & lt;
         const int prevA = bA ? 31 - __clz(bA) : -1;
         const int prevB = bB ? 63 - __clz(bB) : (mA ? 31 - __clz(mA) : -1);
-        int b = 0;
-        if (nzA) b += (prevA >= 0 ? rb_small(lane - prevA - 1) : 0) + vlen32(zA);
-        if (nzB) b += (prevB >= 0 ? rb_small(32 + lane - prevB - 1) : 0) + vlen32(zB);
-        const int bytes = __reduce_add_sync(0xFFFFFFFFu, b);
+        int bytes = 0;
+        if (mA | mB) {
+            int b = 0;
+            if (nzA) b += (prevA >= 0 ? rb_small(lane - prevA - 1) : 0) + vlen32(zA);
+            if (nzB) b += (prevB >= 0 ? rb_small(32 + lane - prevB - 1) : 0) + vlen32(zB);
+            bytes = __reduce_add_sync(0xFFFFFFFFu, b);
+        }
         if (lane == 0) {
             int nesc = 0;
             if (R.has_esc) {
@@ -502,32 +505,36 @@ __global__ void __launch_bounds__(256) k_emit_q(const T *__restrict__ vol, const
             if (lp + 1 < lpe) fetch(lp + 1);
             const bool nzA = zA != 1u, nzB = zB != 1u;
             const uint32_t mA = __ballot_sync(0xFFFFFFFFu, nzA), mB = __ballot_sync(0xFFFFFFFFu, nzB);
-            const uint32_t bA = mA & lt, bB = mB & lt;
-            const int prevA = bA ? 31 - __clz(bA) : -1;
-            const int prevB = bB ? 63 - __clz(bB) : (mA ? 31 - __clz(mA) : -1);
-            int64_t runA = 0, runB = 0;
-            int bAy = 0, bBy = 0;
-            if (nzA) {
-                runA = prevA >= 0 ? lane - prevA - 1 : po.carry + lane;
-                bAy = (prevA >= 0 ? rb_small((int)runA) : (int)run_bytes(runA)) + vlen32(zA);
-            }
-            if (nzB) {
-                runB = prevB >= 0 ? 32 + lane - prevB - 1 : po.carry + 32 + lane;
-                bBy = (prevB >= 0 ? rb_small((int)runB) : (int)run_bytes(runB)) + vlen32(zB);
-            }
-            // one scan of packed (bytes A | bytes B << 16)
-            uint32_t pk = (uint32_t)bAy | ((uint32_t)bBy << 16);
-#pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {
-                const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, pk, off);
-                if (lane >= off) pk += t;
-            }
-            const uint32_t tot = __shfl_sync(0xFFFFFFFFu, pk, 31);
-            const int totA = (int)(tot & 0xFFFFu), totB = (int)(tot >> 16);
-            const int sA = (int)(pk & 0xFFFFu) - bAy, sB = totA + (int)(pk >> 16) - bBy;
             uint8_t *base = out + R.tok_start + po.tok_off;
-            if (nzA) put_varint32(put_run(base + sA, runA), zA);
-            if (nzB) put_varint32(put_run(base + sB, runB), zB);
+            int totA = 0, totB = 0;
+            if (mA | mB) {  // an all-zero piece only extends the carried run
+                const uint32_t bA = mA & lt, bB = mB & lt;
+                const int prevA = bA ? 31 - __clz(bA) : -1;
+                const int prevB = bB ? 63 - __clz(bB) : (mA ? 31 - __clz(mA) : -1);
+                int64_t runA = 0, runB = 0;
+                int bAy = 0, bBy = 0;
+                if (nzA) {
+                    runA = prevA >= 0 ? lane - prevA - 1 : po.carry + lane;
+                    bAy = (prevA >= 0 ? rb_small((int)runA) : (int)run_bytes(runA)) + vlen32(zA);
+                }
+                if (nzB) {
+                    runB = prevB >= 0 ? 32 + lane - prevB - 1 : po.carry + 32 + lane;
+                    bBy = (prevB >= 0 ? rb_small((int)runB) : (int)run_bytes(runB)) + vlen32(zB);
+                }
+                // one scan of packed (bytes A | bytes B << 16)
+                uint32_t pk = (uint32_t)bAy | ((uint32_t)bBy << 16);
+#pragma unroll
+                for (int off = 1; off < 32; off <<= 1) {
+                    const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, pk, off);
+                    if (lane >= off) pk += t;
+                }
+                const uint32_t tot = __shfl_sync(0xFFFFFFFFu, pk, 31);
+                totA = (int)(tot & 0xFFFFu);
+                totB = (int)(tot >> 16);
+                const int sA = (int)(pk & 0xFFFFu) - bAy, sB = totA + (int)(pk >> 16) - bBy;
+                if (nzA) put_varint32(put_run(base + sA, runA), zA);
+                if (nzB) put_varint32(put_run(base + sB, runB), zB);
+            }
             if (R.last && lp == R.npieces - 1 && lane == 0) {  // the window's final zero run
                 const int lastp = mB ? 63 - __clz(mB) : (mA ? 31 - __clz(mA) : -1);
                 const int64_t fin = (mA | mB) ? vcount - 1 - lastp : po.carry + vcount;

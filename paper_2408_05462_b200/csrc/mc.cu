@@ -480,17 +480,23 @@ __global__ void __launch_bounds__(256) k_mc_count3(const McGrid *__restrict__ G,
         mask_bits66(mp1, b0, m01, h01);
         mask_bits66(mp1, b1, m11, h11);
         int t = 0, v = 0;
+        // all 66 x 4 corner bits equal (the usual case away from the surface):
+        // every cell is case 0 or 255, no triangles, nothing owned
+        const uint64_t a1 = m00 & m10 & m01 & m11, o1 = m00 | m10 | m01 | m11;
+        const uint32_t ah = h00 & h10 & h01 & h11 & 3u, oh = (h00 | h10 | h01 | h11) & 3u;
+        if (!((o1 == 0 && oh == 0) || (a1 == ~0ull && ah == 3u))) {
 #pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-            const int cc = lane + 32 * hh;
-            if (x0 + cc < g.ncx) {
-                const int code = code_fast(m00, h00, m10, h10, m01, h01, m11, h11, cc);
-                t += s_ntri[code];
-                v += s_own[code][bflags(x0 + cc, cy, cz)];
+            for (int hh = 0; hh < 2; ++hh) {
+                const int cc = lane + 32 * hh;
+                if (x0 + cc < g.ncx) {
+                    const int code = code_fast(m00, h00, m10, h10, m01, h01, m11, h11, cc);
+                    t += s_ntri[code];
+                    v += s_own[code][bflags(x0 + cc, cy, cz)];
+                }
             }
+            t = __reduce_add_sync(0xFFFFFFFFu, t);
+            v = __reduce_add_sync(0xFFFFFFFFu, v);
         }
-        t = __reduce_add_sync(0xFFFFFFFFu, t);
-        v = __reduce_add_sync(0xFFFFFFFFu, v);
         if (lane == 0) {
             McPieceCnt o;
             o.tri = t;
