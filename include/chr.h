@@ -364,6 +364,8 @@ int chr_read_archive(const uint8_t *d_file, uint64_t nbytes, chr_file_info_t *h_
 void chr_prof_enable(int on);
 long long chr_launch_count(void);
 int chr_prof_report(char *buf, size_t cap);
+int chr_prof_timeline(char *buf, size_t cap);
+void chr_prof_mark(const char *name, void *stream);
 
 #ifdef __cplusplus
 }

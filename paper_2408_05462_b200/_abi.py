@@ -224,6 +224,10 @@ def lib():
         L.chr_launch_count.restype = ctypes.c_longlong
         L.chr_prof_report.argtypes = [ctypes.c_char_p, SZ]
         L.chr_prof_report.restype = INT
+        L.chr_prof_timeline.argtypes = [ctypes.c_char_p, SZ]
+        L.chr_prof_timeline.restype = INT
+        L.chr_prof_mark.argtypes = [ctypes.c_char_p, P]
+        L.chr_prof_mark.restype = None
         _lib = L
     return _lib
 
@@ -233,7 +237,8 @@ EXPORTS = [
     "chr_mask_words", "chr_decode_regions_mask", "chr_mc_count_masked", "chr_mc_emit_masked",
     "chr_select_workspace_size", "chr_select_distances", "chr_compress2",
     "chr_stitch_workspace_size", "chr_stitch", "chr_topology_compare",
-    "chr_read_header", "chr_read_workspace_size", "chr_read_archive",
+    "chr_read_header", "chr_read_workspace_size", "chr_read_archive", "chr_prof_timeline",
+    "chr_prof_mark",
     "chr_dcompress_workspace_size", "chr_dcompress_local", "chr_dcompress_finish", "chr_dcompress_headers",
     "chr_abi_version", "chr_status_string", "chr_num_blocks", "chr_stats", "chr_plan",
     "chr_compress_workspace_size", "chr_compress_capacity", "chr_compress",

@@ -748,6 +748,40 @@ constexpr int UPT = (int)(DCB / (16 * DTHREADS));  // 16-byte units per thread
 // longest chains start first.  Every dependency of a tile lies on step
 // d - 1, so taking tiles in this order from a ticket cannot deadlock.  One
 // thread per (step, region) pair writes its tiles at pair_base.
+// tiles of region r on step d (pair i = d * nreg + r), in closed form
+__device__ __forceinline__ int64_t pair_tiles(const DecReg &R, int64_t d_glob) {
+    if (R.ntiles == 0) return 0;
+    const int64_t d = d_glob - R.doff;
+    if (d < 0) return 0;
+    const int64_t lo = max((int64_t)0, d - (R.tny - 1)), hi = min((int64_t)R.tnz - 1, d);
+    return hi >= lo ? hi - lo + 1 : 0;
+}
+
+// exclusive prefix of pair_tiles over all pairs in step-major order (one
+// CTA of 1024 threads, 8 consecutive pairs per thread per round)
+__global__ void __launch_bounds__(1024) k_pair_base(const DecReg *__restrict__ regs, int64_t npairs, int64_t nreg,
+                                                     int64_t *__restrict__ pair_base) {
+    int64_t carry = 0;
+    for (int64_t r0 = 0; r0 < npairs; r0 += 1024 * 8) {
+        const int64_t i0 = r0 + (int64_t)threadIdx.x * 8;
+        int64_t c[8], sum = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int64_t i = i0 + j;
+            c[j] = i < npairs ? pair_tiles(regs[i % nreg], i / nreg) : 0;
+            sum += c[j];
+        }
+        int64_t tot;
+        int64_t pre = carry + block_excl64(sum, &tot);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            if (i0 + j < npairs) pair_base[i0 + j] = pre;
+            pre += c[j];
+        }
+        carry += tot;
+    }
+}
+
 __global__ void k_tile_order(const DecReg *__restrict__ regs, const int64_t *__restrict__ pair_base,
                              int64_t npairs, int64_t nreg, int32_t *__restrict__ order) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1425,7 +1459,6 @@ struct DecPlan {
     int64_t *faces;
     int32_t *tflag, *chunk_reg, *tile_reg, *order;
     int64_t *pair_base;
-    std::vector<int64_t> h_pair_base;
     int64_t ndiag = 0;
     unsigned long long *ticket, *ticket3;
     int32_t *any_slow;
@@ -1455,13 +1488,10 @@ static bool band_shape(DecReg &R) {
         // chains are tny + tnz - 1 hops long (band above, chunk before): pick
         // the shape with the shortest chain, then the fewest tiles
         int64_t best_chain = INT64_MAX, best_tiles = INT64_MAX;
-        for (int ty = 1; ty <= std::min(R.ey, K); ++ty) {
-            int tz = std::min({R.ez, K / ty, BSEGM});
-            if (ty < R.ey) tz = std::min(tz, BDF / R.ex);  // a band below exists: its dF (tz x ex) must fit
-            if (tz < 1) continue;
-            const int ty2 = std::min(R.ey, K / tz);  // widest band for this chunk depth
+        for (int tz = 1; tz <= std::min({R.ez, K, BSEGM}); ++tz) {  // chunk depth
+            const int ty2 = std::min(R.ey, K / tz);                     // widest band for it
+            if (ty2 < R.ey && tz > BDF / R.ex) continue;  // a band below exists: its dF (tz x ex) must fit
             const int64_t ny = ceil_div(R.ey, ty2), nz = ceil_div(R.ez, tz);
-            if (ty2 < R.ey && tz > BDF / R.ex) continue;
             const int64_t chain = ny + nz - 1, tiles = ny * nz;
             if (chain < best_chain || (chain == best_chain && tiles < best_tiles)) {
                 best_chain = chain;
@@ -1545,31 +1575,37 @@ static bool dec_build(const chr_dec_region_t *h, int64_t n, uintptr_t blob, DecP
     for (const DecReg &R : pl.regs)
         if (R.ntiles) D = std::max<int64_t>(D, (int64_t)R.tny + R.tnz - 2);
     pl.ndiag = pl.ntiles ? D + 1 : 0;
-    std::vector<int64_t> cnt((size_t)(pl.ndiag * n) + 1, 0);  // [r][d]
-    std::vector<int64_t> diff((size_t)pl.ndiag + 2);
     for (int64_t i = 0; i < n; ++i) {
         DecReg &R = pl.regs[i];
-        if (!R.ntiles) continue;
-        R.doff = (int32_t)(D - (R.tny + R.tnz - 2));
-        std::fill(diff.begin(), diff.end(), 0);
-        for (int tz = 0; tz < R.tnz; ++tz) {
-            diff[R.doff + tz] += 1;
-            diff[R.doff + tz + R.tny] -= 1;
-        }
-        int64_t run = 0;
-        for (int64_t d = 0; d < pl.ndiag; ++d) {
-            run += diff[d];
-            cnt[i * pl.ndiag + d] = run;
-        }
+        if (R.ntiles) R.doff = (int32_t)(D - (R.tny + R.tnz - 2));
     }
-    pl.h_pair_base.assign((size_t)(pl.ndiag * n) + 1, 0);
-    int64_t acc = 0;
-    for (int64_t d = 0; d < pl.ndiag; ++d)
-        for (int64_t i = 0; i < n; ++i) {
-            pl.h_pair_base[d * n + i] = acc;
-            acc += cnt[i * pl.ndiag + d];
-        }
     return true;
+}
+
+// The host plan of the last table this thread built (chr_decode_workspace_size
+// is normally followed by the decode of the same table): reused when the
+// table bytes and the blob's 16-byte alignment match.
+struct DecPlanCache {
+    std::vector<chr_dec_region_t> key;
+    uintptr_t align = ~uintptr_t(0);
+    bool ok = false;
+    DecPlan plan;
+};
+
+static bool dec_build_cached(const chr_dec_region_t *h, int64_t n, uintptr_t blob, DecPlan &pl) {
+    thread_local DecPlanCache C;
+    const uintptr_t al = blob & 15;
+    if (C.align == al && (int64_t)C.key.size() == n && std::memcmp(C.key.data(), h, sizeof(*h) * n) == 0) {
+        if (!C.ok) return false;
+        pl = C.plan;
+        return true;
+    }
+    C.key.assign(h, h + n);
+    C.align = al;
+    C.plan = DecPlan();
+    C.ok = dec_build(h, n, al, C.plan);  // offsets are relative to the blob: only the alignment matters
+    if (C.ok) pl = C.plan;
+    return C.ok;
 }
 
 static void dec_carve(DecPlan &pl, void *base, size_t cap) {
@@ -1594,7 +1630,7 @@ static void dec_carve(DecPlan &pl, void *base, size_t cap) {
     pl.chunk_reg = c.take<int32_t>(pl.nchunks + 1);
     pl.tile_reg = c.take<int32_t>(pl.ntiles + 1);
     pl.order = c.take<int32_t>(pl.ntiles + 1);
-    pl.pair_base = c.take<int64_t>(pl.h_pair_base.size() + 1);
+    pl.pair_base = c.take<int64_t>(pl.ndiag * n + 1);
     pl.ticket = c.take<unsigned long long>(1);
     pl.ticket3 = c.take<unsigned long long>(1);
     pl.any_slow = c.take<int32_t>(1);
@@ -1607,7 +1643,7 @@ using namespace chr;
 
 extern "C" size_t chr_decode_workspace_size(const chr_dec_region_t *h, int64_t n) {
     DecPlan pl;
-    if (!h || n < 1 || !dec_build(h, n, 0, pl)) return 256;
+    if (!h || n < 1 || !dec_build_cached(h, n, 0, pl)) return 256;
     dec_carve(pl, nullptr, ~size_t(0));
     return pl.ws;
 }
@@ -1641,7 +1677,7 @@ static int decode_impl(const uint8_t *d_blob, const chr_dec_region_t *h, int64_t
     if (!d_blob || !h || n < 0 || !d_out) return CHR_E_PARAMETER;
     cudaStream_t st = (cudaStream_t)stream;
     DecPlan pl;
-    if (!dec_build(h, n, (uintptr_t)d_blob, pl)) return CHR_E_PARAMETER;
+    if (!dec_build_cached(h, n, (uintptr_t)d_blob, pl)) return CHR_E_PARAMETER;
     dec_carve(pl, d_ws, ws_bytes);
     if (!d_ws || pl.ws > ws_bytes) return CHR_E_WORKSPACE;
     const CrcTables *tabs = crc_tables_device();
@@ -1697,8 +1733,10 @@ static int decode_impl(const uint8_t *d_blob, const chr_dec_region_t *h, int64_t
             k_esc_seg<<<(unsigned)n, 256, 0, st>>>(pl.d_regs, d_blob, pl.esc_sp);
         }
         const int64_t npairs = pl.ndiag * n;
-        CHR_CUDA_TRY(cudaMemcpyAsync(pl.pair_base, pl.h_pair_base.data(), sizeof(int64_t) * npairs,
-                                     cudaMemcpyHostToDevice, st));
+        {
+            CHR_PROF("k_pair_base", st);
+            k_pair_base<<<1, 1024, 0, st>>>(pl.d_regs, npairs, n, pl.pair_base);
+        }
         {
             CHR_PROF("k_tile_order", st);
             k_tile_order<<<(unsigned)ceil_div(npairs, 256), 256, 0, st>>>(pl.d_regs, pl.pair_base, npairs, n, pl.order);

@@ -92,3 +92,44 @@ extern "C" int chr_prof_report(char *buf, size_t cap) {
     }
     return (int)s.size();
 }
+
+// "name start_ms end_ms\n" per recorded launch (relative to the first
+// record's start), in launch order; clears like chr_prof_report.
+extern "C" int chr_prof_timeline(char *buf, size_t cap) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    std::string s;
+    cudaEvent_t t0 = g_recs.empty() ? nullptr : g_recs.front().a;
+    for (const Rec &r : g_recs) {
+        cudaEventSynchronize(r.b);
+        float a = 0.f, b = 0.f;
+        cudaEventElapsedTime(&a, t0, r.a);
+        cudaEventElapsedTime(&b, t0, r.b);
+        char line[256];
+        snprintf(line, sizeof(line), "%s %.4f %.4f\n", r.name, a, b);
+        s += line;
+    }
+    for (const Rec &r : g_recs) {
+        g_pool.push_back(r.a);
+        g_pool.push_back(r.b);
+    }
+    g_recs.clear();
+    if (buf && cap) {
+        const size_t n = std::min(cap - 1, s.size());
+        memcpy(buf, s.data(), n);
+        buf[n] = 0;
+    }
+    return (int)s.size();
+}
+
+// a named zero-length record on the stream (host-side phase marks in the
+// timeline; not counted as a launch).  The name must outlive the report.
+extern "C" void chr_prof_mark(const char *name, void *stream) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!g_on) return;
+    static std::map<std::string, std::string> names;  // stable storage
+    const char *nm = names.emplace(name, std::string("@") + name).first->second.c_str();
+    cudaEvent_t a = take_event(), b = take_event();
+    cudaEventRecord(a, (cudaStream_t)stream);
+    cudaEventRecord(b, (cudaStream_t)stream);
+    g_recs.push_back({nm, a, b});
+}
