@@ -190,6 +190,8 @@ def main():
     ap.add_argument("--edge", "--size", dest="n", type=int, default=None, help="edge length override (tests)")
     ap.add_argument("--cpu-planes", type=int, default=32)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-copy", default="dma", choices=["dma", "sm"],
+                    help="bulk H2D/D2H of the e2e loop: DMA engines or the UVA copy kernel")
     ap.add_argument("--mode", default="replica", choices=["replica", "slab"],
                     help="N>1: independent volumes per rank, or one volume in z-slabs (SURVEY 8e)")
     ap.add_argument("--backend", default=None, help="torch.distributed backend (default nccl; gloo for 1-GPU tests)")
@@ -306,9 +308,12 @@ def main():
     h2d = d2h = 0
 
     def chunked(dst, src):
-        """bulk copy by a 16-CTA kernel through UVA (chr_sm_copy), not a copy engine: the
-        library's small metadata copies on the compute stream would otherwise queue behind
-        the 500 MB transfers on the DMA engines"""
+        """bulk copy on the DMA engines (full duplex over PCIe); the library's own small
+        transfers bypass the engines (xfer.cu), so they never queue behind these.
+        --e2e-copy sm: a 16-CTA UVA copy kernel (chr_sm_copy) instead"""
+        if args.e2e_copy == "dma":
+            dst.copy_(src, non_blocking=True)
+            return
         nbytes = dst.numel() * dst.element_size()
         rc = L.chr_sm_copy(dst.data_ptr(), src.data_ptr(), nbytes, 16, torch.cuda.current_stream().cuda_stream)
         if rc:

@@ -275,6 +275,9 @@ int chr_mc_emit_masked(const double *d_grids, const chr_mc_grid_t *h_grids, int6
  *     keeps the copy engines free for the library's own small copies when
  *     a caller pipelines its inputs/outputs.  16-byte aligned pointers. */
 int chr_sm_copy(void *dst, const void *src, uint64_t nbytes, int ctas, void *stream);
+/*     the same for small copies at any alignment (the library's own small
+ *     transfers use this path internally, never the copy engines) */
+int chr_copy(void *dst, const void *src, uint64_t nbytes, void *stream);
 
 /* 14. SURVEY 8(f3): stitch + verify_topology on the device.
  *     chr_stitch replaces chr_archive.stitch (chr_archive.py:277-294): the

@@ -228,6 +228,8 @@ def lib():
         L.chr_prof_timeline.restype = INT
         L.chr_prof_mark.argtypes = [ctypes.c_char_p, P]
         L.chr_prof_mark.restype = None
+        L.chr_copy.argtypes = [P, P, U64, P]
+        L.chr_copy.restype = INT
         _lib = L
     return _lib
 
@@ -238,7 +240,7 @@ EXPORTS = [
     "chr_select_workspace_size", "chr_select_distances", "chr_compress2",
     "chr_stitch_workspace_size", "chr_stitch", "chr_topology_compare",
     "chr_read_header", "chr_read_workspace_size", "chr_read_archive", "chr_prof_timeline",
-    "chr_prof_mark",
+    "chr_prof_mark", "chr_copy",
     "chr_dcompress_workspace_size", "chr_dcompress_local", "chr_dcompress_finish", "chr_dcompress_headers",
     "chr_abi_version", "chr_status_string", "chr_num_blocks", "chr_stats", "chr_plan",
     "chr_compress_workspace_size", "chr_compress_capacity", "chr_compress",

@@ -43,9 +43,11 @@ __global__ void __launch_bounds__(256) k_lorenzo_seam(const double *__restrict__
 
 using namespace chr;
 
-extern "C" int chr_abi_version(void) { return 1; }
+extern "C" int chr_abi_version(void) {
+    CHR_XFER_SCOPE; return 1; }
 
 extern "C" const char *chr_status_string(int s) {
+    CHR_XFER_SCOPE;
     switch (s) {
         case CHR_OK: return "ok";
         case CHR_E_PARAMETER: return "invalid parameter";
@@ -60,11 +62,12 @@ extern "C" const char *chr_status_string(int s) {
 
 extern "C" int chr_min_abs_distance(const double *d_flat, int64_t n, double k, double *h_out, void *d_ws,
                                     size_t ws_bytes, void *stream) {
+    CHR_XFER_SCOPE;
     if (!d_flat || n < 1 || !h_out) return CHR_E_PARAMETER;
     if (!d_ws || ws_bytes < 8) return CHR_E_WORKSPACE;
     cudaStream_t st = (cudaStream_t)stream;
     auto *slot = reinterpret_cast<unsigned long long *>(d_ws);
-    CHR_CUDA_TRY(cudaMemsetAsync(slot, 0x7F, 8, st));  // a huge positive double
+    CHR_CUDA_TRY(fill_async(slot, 0x7F, 8, st));  // a huge positive double
     const int64_t blocks = std::min<int64_t>(ceil_div(n, 256), 148 * 16);
     {
         CHR_PROF("k_min_abs", st);
@@ -72,8 +75,8 @@ extern "C" int chr_min_abs_distance(const double *d_flat, int64_t n, double k, d
     }
     CHR_CUDA_TRY(cudaGetLastError());
     unsigned long long bits = 0;
-    CHR_CUDA_TRY(cudaMemcpyAsync(&bits, slot, 8, cudaMemcpyDeviceToHost, st));
-    CHR_CUDA_TRY(cudaStreamSynchronize(st));
+    CHR_CUDA_TRY(d2h(&bits, slot, 8, st));
+    CHR_CUDA_TRY(stream_sync(st));
     double v;
     memcpy(&v, &bits, 8);
     *h_out = v;
@@ -82,6 +85,7 @@ extern "C" int chr_min_abs_distance(const double *d_flat, int64_t n, double k, d
 
 extern "C" int chr_lorenzo_encode(const double *d_flat, int64_t nx, int64_t ny, int64_t nz, double e,
                                   int64_t *d_q, uint8_t *d_escaped, void *stream) {
+    CHR_XFER_SCOPE;
     if (!d_flat || !d_q || !d_escaped || nx < 1 || ny < 1 || nz < 1 || !(e > 0.0)) return CHR_E_PARAMETER;
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t n = nx * ny * nz;
@@ -119,6 +123,7 @@ __global__ void __launch_bounds__(256) k_sm_copy(const uint8_t *__restrict__ src
 }  // namespace chr
 
 extern "C" int chr_sm_copy(void *dst, const void *src, uint64_t nbytes, int ctas, void *stream) {
+    CHR_XFER_SCOPE;
     if (nbytes == 0) return CHR_OK;
     if (!dst || !src || (((uintptr_t)dst | (uintptr_t)src) & 15)) return CHR_E_PARAMETER;
     cudaStream_t st = (cudaStream_t)stream;

@@ -183,6 +183,7 @@ static bool sel_build(const int32_t *h_windows, const double *h_k, int64_t np, s
 }
 
 extern "C" size_t chr_select_workspace_size(int64_t n_pairs) {
+    CHR_XFER_SCOPE;
     return (size_t)n_pairs * (sizeof(SelPair) + 256 * 8) + 1024;
 }
 
@@ -193,6 +194,7 @@ extern "C" int chr_select_distances(const void *d_vol, int dtype, int64_t nx, in
                                     const int32_t *h_windows, const double *h_k, int64_t n_pairs, double accuracy,
                                     int mode, void *d_ws, size_t ws_bytes, double *h_value, int64_t *h_count,
                                     int64_t *h_n, void *stream) {
+    CHR_XFER_SCOPE;
     if (n_pairs == 0) return CHR_OK;
     if (!d_vol || !h_windows || !h_k || !h_value || !(accuracy > 0.0 && accuracy <= 1.0) || mode < 0 || mode > 1)
         return CHR_E_PARAMETER;
@@ -210,8 +212,8 @@ extern "C" int chr_select_distances(const void *d_vol, int dtype, int64_t nx, in
     SelPair *d_pairs = reinterpret_cast<SelPair *>(d_ws);
     unsigned long long *d_hist =
         reinterpret_cast<unsigned long long *>(reinterpret_cast<char *>(d_ws) + (size_t)n_pairs * sizeof(SelPair));
-    CHR_CUDA_TRY(cudaMemcpyAsync(d_pairs, v.data(), sizeof(SelPair) * n_pairs, cudaMemcpyHostToDevice, st));
-    CHR_CUDA_TRY(cudaMemsetAsync(d_hist, 0, sizeof(unsigned long long) * 256 * n_pairs, st));
+    CHR_CUDA_TRY(h2d(d_pairs, v.data(), sizeof(SelPair) * n_pairs, st));
+    CHR_CUDA_TRY(fill_async(d_hist, 0, sizeof(unsigned long long) * 256 * n_pairs, st));
     const unsigned nit = (unsigned)items, pick = (unsigned)ceil_div(n_pairs, 4);
     if (mode == 1) {
         CHR_PROF("k_sel_count", st);
@@ -232,8 +234,8 @@ extern "C" int chr_select_distances(const void *d_vol, int dtype, int64_t nx, in
         k_sel_pick<<<pick, 128, 0, st>>>(d_pairs, n_pairs, shift, d_hist);
     }
     CHR_CUDA_TRY(cudaGetLastError());
-    CHR_CUDA_TRY(cudaMemcpyAsync(v.data(), d_pairs, sizeof(SelPair) * n_pairs, cudaMemcpyDeviceToHost, st));
-    CHR_CUDA_TRY(cudaStreamSynchronize(st));
+    CHR_CUDA_TRY(d2h(v.data(), d_pairs, sizeof(SelPair) * n_pairs, st));
+    CHR_CUDA_TRY(stream_sync(st));
     for (int64_t i = 0; i < n_pairs; ++i) {
         double d;
         std::memcpy(&d, &v[i].prefix, 8);

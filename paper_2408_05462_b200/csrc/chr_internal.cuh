@@ -45,6 +45,26 @@ class ProfScope {
 #define CHR_PROF_CAT(a, b) CHR_PROF_CAT2(a, b)
 #define CHR_PROF(name, st) ::chr::ProfScope CHR_PROF_CAT(_chr_prof_, __LINE__)(name, st)
 
+// ------------------------------------------------------------------ transfers
+// small host<->device copies without the copy engines (xfer.cu): h2d is
+// staged in a pinned ring and pulled by a kernel; d2h is pushed by a kernel
+// and delivered at the next stream_sync of the stream.  Every extern "C"
+// function that calls d2h holds an XferScope.
+cudaError_t h2d(void *dst, const void *src, size_t n, cudaStream_t st);
+cudaError_t d2h(void *dst, const void *src, size_t n, cudaStream_t st);
+cudaError_t stream_sync(cudaStream_t st);
+cudaError_t fill_async(void *dst, int v, size_t n, cudaStream_t st);   // cudaMemsetAsync as a kernel
+cudaError_t copy_async(void *dst, const void *src, size_t n, cudaStream_t st);  // kernel copy, UVA pointers
+class XferScope {
+  public:
+    XferScope();
+    ~XferScope();
+
+  private:
+    size_t mark_;
+};
+#define CHR_XFER_SCOPE ::chr::XferScope CHR_PROF_CAT(_chr_xfer_, __LINE__)
+
 // ------------------------------------------------------------------ workspace
 struct WsCarver {
     char *base;

@@ -174,10 +174,12 @@ int crc_launch(const uint8_t *d_buf, const CrcSeg *d_segs, int64_t nseg, int64_t
 
 using namespace chr;
 
-extern "C" size_t chr_crc32_workspace_size(uint64_t) { return 256; }
+extern "C" size_t chr_crc32_workspace_size(uint64_t) {
+    CHR_XFER_SCOPE; return 256; }
 
 extern "C" int chr_crc32(const uint8_t *d_buf, uint64_t n, void *d_ws, size_t ws_bytes,
                          uint32_t *h_crc, void *stream) {
+    CHR_XFER_SCOPE;
     if (!h_crc || (!d_buf && n)) return CHR_E_PARAMETER;
     if (ws_bytes < 256 || !d_ws) return CHR_E_WORKSPACE;
     cudaStream_t st = (cudaStream_t)stream;
@@ -192,18 +194,19 @@ extern "C" int chr_crc32(const uint8_t *d_buf, uint64_t n, void *d_ws, size_t ws
     crc_plan_segments(&seg, 1);
     CrcSeg *d_seg = reinterpret_cast<CrcSeg *>(d_ws);
     uint32_t *d_raw = reinterpret_cast<uint32_t *>(reinterpret_cast<char *>(d_ws) + 128);
-    CHR_CUDA_TRY(cudaMemcpyAsync(d_seg, &seg, sizeof(seg), cudaMemcpyHostToDevice, st));
-    CHR_CUDA_TRY(cudaMemsetAsync(d_raw, 0, 4, st));
+    CHR_CUDA_TRY(h2d(d_seg, &seg, sizeof(seg), st));
+    CHR_CUDA_TRY(fill_async(d_raw, 0, 4, st));
     int rc = crc_launch(d_buf, d_seg, 1, seg.n_sc, d_raw, st);
     if (rc) return rc;
     uint32_t raw = 0;
-    CHR_CUDA_TRY(cudaMemcpyAsync(&raw, d_raw, 4, cudaMemcpyDeviceToHost, st));
-    CHR_CUDA_TRY(cudaStreamSynchronize(st));
+    CHR_CUDA_TRY(d2h(&raw, d_raw, 4, st));
+    CHR_CUDA_TRY(stream_sync(st));
     *h_crc = crc_finalize(H.x2n, raw, n);
     return CHR_OK;
 }
 
 extern "C" uint32_t chr_crc32_combine(uint32_t crc1, uint32_t crc2, uint64_t len2) {
+    CHR_XFER_SCOPE;
     const CrcTables &H = crc_tables_hostref();
     return crc_shift(H.x2n, crc1, len2) ^ crc2;
 }

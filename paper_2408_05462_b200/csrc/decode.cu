@@ -1642,6 +1642,7 @@ static void dec_carve(DecPlan &pl, void *base, size_t cap) {
 using namespace chr;
 
 extern "C" size_t chr_decode_workspace_size(const chr_dec_region_t *h, int64_t n) {
+    CHR_XFER_SCOPE;
     DecPlan pl;
     if (!h || n < 1 || !dec_build_cached(h, n, 0, pl)) return 256;
     dec_carve(pl, nullptr, ~size_t(0));
@@ -1654,10 +1655,12 @@ static int decode_impl(const uint8_t *d_blob, const chr_dec_region_t *h, int64_t
 extern "C" int chr_decode_regions(const uint8_t *d_blob, const chr_dec_region_t *h, int64_t n,
                                   double *d_out, void *d_ws, size_t ws_bytes, int32_t *h_status,
                                   void *stream) {
+    CHR_XFER_SCOPE;
     return decode_impl(d_blob, h, n, d_out, d_ws, ws_bytes, h_status, 0.0, nullptr, stream);
 }
 
 extern "C" uint64_t chr_mask_words(const int32_t *h_dims, int64_t n) {
+    CHR_XFER_SCOPE;
     uint64_t w = 0;
     for (int64_t i = 0; i < n; ++i)
         w += (uint64_t)ceil_div((int64_t)h_dims[3 * i] * h_dims[3 * i + 1], 32) * (uint64_t)h_dims[3 * i + 2];
@@ -1667,6 +1670,7 @@ extern "C" uint64_t chr_mask_words(const int32_t *h_dims, int64_t n) {
 extern "C" int chr_decode_regions_mask(const uint8_t *d_blob, const chr_dec_region_t *h, int64_t n, double *d_out,
                                        void *d_ws, size_t ws_bytes, int32_t *h_status, double iso,
                                        uint32_t *d_mask, void *stream) {
+    CHR_XFER_SCOPE;
     if (!d_mask) return CHR_E_PARAMETER;
     return decode_impl(d_blob, h, n, d_out, d_ws, ws_bytes, h_status, iso, d_mask, stream);
 }
@@ -1688,15 +1692,15 @@ static int decode_impl(const uint8_t *d_blob, const chr_dec_region_t *h, int64_t
         segs[i].end = pl.regs[i].poff + pl.regs[i].plen;
     }
     const int64_t total_sc = crc_plan_segments(segs.data(), n);
-    CHR_CUDA_TRY(cudaMemcpyAsync(pl.d_regs, pl.regs.data(), sizeof(DecReg) * n, cudaMemcpyHostToDevice, st));
-    CHR_CUDA_TRY(cudaMemcpyAsync(pl.segs, segs.data(), sizeof(CrcSeg) * n, cudaMemcpyHostToDevice, st));
-    CHR_CUDA_TRY(cudaMemsetAsync(pl.seg_raw, 0, sizeof(uint32_t) * n, st));
-    CHR_CUDA_TRY(cudaMemsetAsync(pl.flags, 0, sizeof(int64_t) * (pl.nitems + 1), st));
-    CHR_CUDA_TRY(cudaMemsetAsync(pl.ticket, 0, sizeof(unsigned long long), st));
-    CHR_CUDA_TRY(cudaMemsetAsync(pl.ticket3, 0, sizeof(unsigned long long), st));
-    CHR_CUDA_TRY(cudaMemsetAsync(pl.any_slow, 0, sizeof(int32_t), st));
-    if (d_mask) CHR_CUDA_TRY(cudaMemsetAsync(d_mask, 0, sizeof(uint32_t) * (pl.nmask + 8), st));
-    CHR_CUDA_TRY(cudaMemsetAsync(pl.tflag, 0, sizeof(int32_t) * (pl.ntiles + 1), st));
+    CHR_CUDA_TRY(h2d(pl.d_regs, pl.regs.data(), sizeof(DecReg) * n, st));
+    CHR_CUDA_TRY(h2d(pl.segs, segs.data(), sizeof(CrcSeg) * n, st));
+    CHR_CUDA_TRY(fill_async(pl.seg_raw, 0, sizeof(uint32_t) * n, st));
+    CHR_CUDA_TRY(fill_async(pl.flags, 0, sizeof(int64_t) * (pl.nitems + 1), st));
+    CHR_CUDA_TRY(fill_async(pl.ticket, 0, sizeof(unsigned long long), st));
+    CHR_CUDA_TRY(fill_async(pl.ticket3, 0, sizeof(unsigned long long), st));
+    CHR_CUDA_TRY(fill_async(pl.any_slow, 0, sizeof(int32_t), st));
+    if (d_mask) CHR_CUDA_TRY(fill_async(d_mask, 0, sizeof(uint32_t) * (pl.nmask + 8), st));
+    CHR_CUDA_TRY(fill_async(pl.tflag, 0, sizeof(int32_t) * (pl.ntiles + 1), st));
     int rc = crc_launch(d_blob, pl.segs, n, total_sc, pl.seg_raw, st);
     if (rc) return rc;
     {
@@ -1754,8 +1758,8 @@ static int decode_impl(const uint8_t *d_blob, const chr_dec_region_t *h, int64_t
     //      skipped unless some region needs it (one 4-byte read-back)
     int32_t h_any_slow = pl.host_slow ? 1 : 0;
     if (!h_any_slow) {
-        CHR_CUDA_TRY(cudaMemcpyAsync(&h_any_slow, pl.any_slow, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-        CHR_CUDA_TRY(cudaStreamSynchronize(st));
+        CHR_CUDA_TRY(d2h(&h_any_slow, pl.any_slow, sizeof(int32_t), st));
+        CHR_CUDA_TRY(stream_sync(st));
     }
     if (h_any_slow) {
         {
@@ -1800,8 +1804,8 @@ static int decode_impl(const uint8_t *d_blob, const chr_dec_region_t *h, int64_t
             k_mask_rest<<<g, 256, 0, st>>>(pl.d_regs, r0, d_out, d_mask, iso);
         }
     CHR_CUDA_TRY(cudaGetLastError());
-    CHR_CUDA_TRY(cudaMemcpyAsync(pl.regs.data(), pl.d_regs, sizeof(DecReg) * n, cudaMemcpyDeviceToHost, st));
-    CHR_CUDA_TRY(cudaStreamSynchronize(st));
+    CHR_CUDA_TRY(d2h(pl.regs.data(), pl.d_regs, sizeof(DecReg) * n, st));
+    CHR_CUDA_TRY(stream_sync(st));
     int status = CHR_OK;
     for (int64_t i = 0; i < n; ++i) {
         const uint32_t err = pl.regs[i].err;

@@ -1064,6 +1064,7 @@ static void carve(EncPlan &pl, void *base, size_t cap) {
 using namespace chr;
 
 extern "C" size_t chr_compress_workspace_size(const chr_region_t *h, int64_t nreg) {
+    CHR_XFER_SCOPE;
     EncPlan pl;
     if (!h || nreg < 1 || !build_plan(h, nreg, pl)) return 0;
     carve(pl, nullptr, ~size_t(0));
@@ -1071,6 +1072,7 @@ extern "C" size_t chr_compress_workspace_size(const chr_region_t *h, int64_t nre
 }
 
 extern "C" uint64_t chr_compress_capacity(const chr_region_t *h, int64_t nreg, int m, int src_dtype) {
+    CHR_XFER_SCOPE;
     (void)src_dtype;
     uint64_t cap = (uint64_t)kFileHeader + 4 + 8ull * m + 4 + 4;
     const int mb = (m + 7) / 8;
@@ -1092,6 +1094,7 @@ extern "C" int chr_compress(const void *d_vol, int dtype, int src_dtype, int64_t
                             const double *h_cands, int m, chr_region_t *h_regions, int64_t nreg,
                             int write_file, void *d_ws, size_t ws_bytes, uint8_t *d_out,
                             uint64_t out_cap, uint64_t *h_out_nbytes, void *stream) {
+    CHR_XFER_SCOPE;
     return chr_compress2(d_vol, dtype, src_dtype, nx, ny, nz, spacing, bs, vmin, vmax, h_cands, m, h_regions, nreg,
                          write_file, 0, 1.0, d_ws, ws_bytes, d_out, out_cap, h_out_nbytes, stream);
 }
@@ -1101,6 +1104,7 @@ extern "C" int chr_compress2(const void *d_vol, int dtype, int src_dtype, int64_
                              int m, chr_region_t *h_regions, int64_t nreg, int write_file, int bound_mode,
                              double accuracy, void *d_ws, size_t ws_bytes, uint8_t *d_out, uint64_t out_cap,
                              uint64_t *h_out_nbytes, void *stream) {
+    CHR_XFER_SCOPE;
     if (bound_mode < 0 || bound_mode > 1 || !(accuracy > 0.0 && accuracy <= 1.0)) return CHR_E_PARAMETER;
     if (!d_vol || !h_regions || nreg < 1 || !d_out || !h_out_nbytes) return CHR_E_PARAMETER;
     if (dtype != CHR_F32 && dtype != CHR_F64) return CHR_E_PARAMETER;
@@ -1142,12 +1146,11 @@ extern "C" int chr_compress2(const void *d_vol, int dtype, int src_dtype, int64_
     // capacity check against the worst case (verbatim f64 everywhere)
     if (out_cap < chr_compress_capacity(h_regions, nreg, m, src_dtype)) return CHR_E_PARAMETER;
 
-    CHR_CUDA_TRY(cudaMemcpyAsync(pl.params, &hp, sizeof(hp), cudaMemcpyHostToDevice, st));
-    CHR_CUDA_TRY(cudaMemcpyAsync(pl.d_regs, pl.regs.data(), sizeof(RegDev) * nreg,
-                                 cudaMemcpyHostToDevice, st));
-    CHR_CUDA_TRY(cudaMemsetAsync(pl.scal, 0, sizeof(EncScalars), st));
-    CHR_CUDA_TRY(cudaMemsetAsync(pl.seg_raw, 0, sizeof(uint32_t) * (nreg + 1), st));
-    CHR_CUDA_TRY(cudaMemsetAsync(pl.escbits, 0, sizeof(uint32_t) * (pl.etotal + 2), st));
+    CHR_CUDA_TRY(h2d(pl.params, &hp, sizeof(hp), st));
+    CHR_CUDA_TRY(h2d(pl.d_regs, pl.regs.data(), sizeof(RegDev) * nreg, st));
+    CHR_CUDA_TRY(fill_async(pl.scal, 0, sizeof(EncScalars), st));
+    CHR_CUDA_TRY(fill_async(pl.seg_raw, 0, sizeof(uint32_t) * (nreg + 1), st));
+    CHR_CUDA_TRY(fill_async(pl.escbits, 0, sizeof(uint32_t) * (pl.etotal + 2), st));
 
     const unsigned items = (unsigned)pl.nitems, chunks = (unsigned)pl.nchunks;
     {
@@ -1232,10 +1235,9 @@ extern "C" int chr_compress2(const void *d_vol, int dtype, int src_dtype, int64_
             k_finalize_file<<<1, 1, 0, st>>>(tabs, pl.scal, d_out);
     }
     CHR_CUDA_TRY(cudaGetLastError());
-    CHR_CUDA_TRY(cudaMemcpyAsync(pl.regs.data(), pl.d_regs, sizeof(RegDev) * nreg,
-                                 cudaMemcpyDeviceToHost, st));
-    CHR_CUDA_TRY(cudaMemcpyAsync(&hs, pl.scal, sizeof(hs), cudaMemcpyDeviceToHost, st));
-    CHR_CUDA_TRY(cudaStreamSynchronize(st));
+    CHR_CUDA_TRY(d2h(pl.regs.data(), pl.d_regs, sizeof(RegDev) * nreg, st));
+    CHR_CUDA_TRY(d2h(&hs, pl.scal, sizeof(hs), st));
+    CHR_CUDA_TRY(stream_sync(st));
     for (int64_t r = 0; r < nreg; ++r) {
         const RegDev &R = pl.regs[r];
         chr_region_t &o = h_regions[r];
@@ -1284,6 +1286,7 @@ static chr_region_t rle_region(int64_t n) {
 }
 
 extern "C" size_t chr_rle_encode_workspace_size(int64_t n) {
+    CHR_XFER_SCOPE;
     if (n < 1 || n > INT32_MAX) return 256;
     const chr_region_t h = rle_region(n);
     EncPlan pl;
@@ -1294,6 +1297,7 @@ extern "C" size_t chr_rle_encode_workspace_size(int64_t n) {
 
 extern "C" int chr_rle_encode(const int64_t *d_q, int64_t n, uint8_t *d_out, uint64_t out_cap, void *d_ws,
                               size_t ws_bytes, uint64_t *h_nbytes, void *stream) {
+    CHR_XFER_SCOPE;
     if (!h_nbytes) return CHR_E_PARAMETER;
     if (n == 0) {
         *h_nbytes = 0;
@@ -1318,11 +1322,11 @@ extern "C" int chr_rle_encode(const int64_t *d_q, int64_t n, uint8_t *d_out, uin
     hp.nchunks = pl.nchunks;
     hp.dtype = CHR_F64;
     hp.src_dtype = CHR_F64;
-    CHR_CUDA_TRY(cudaMemcpyAsync(pl.params, &hp, sizeof(hp), cudaMemcpyHostToDevice, st));
-    CHR_CUDA_TRY(cudaMemcpyAsync(pl.d_regs, pl.regs.data(), sizeof(RegDev), cudaMemcpyHostToDevice, st));
-    CHR_CUDA_TRY(cudaMemsetAsync(pl.scal, 0, sizeof(EncScalars), st));
-    CHR_CUDA_TRY(cudaMemsetAsync(pl.escbits, 0, sizeof(uint32_t) * (pl.etotal + 2), st));
-    CHR_CUDA_TRY(cudaMemsetAsync(d_bad, 0, sizeof(int32_t), st));
+    CHR_CUDA_TRY(h2d(pl.params, &hp, sizeof(hp), st));
+    CHR_CUDA_TRY(h2d(pl.d_regs, pl.regs.data(), sizeof(RegDev), st));
+    CHR_CUDA_TRY(fill_async(pl.scal, 0, sizeof(EncScalars), st));
+    CHR_CUDA_TRY(fill_async(pl.escbits, 0, sizeof(uint32_t) * (pl.etotal + 2), st));
+    CHR_CUDA_TRY(fill_async(d_bad, 0, sizeof(int32_t), st));
     const unsigned chunks = (unsigned)pl.nchunks;
     k_tile_fill_map<<<1, 256, 0, st>>>(pl.d_regs, 1, pl.item_reg, pl.chunk_reg);
     {
@@ -1344,9 +1348,9 @@ extern "C" int chr_rle_encode(const int64_t *d_q, int64_t n, uint8_t *d_out, uin
     }
     CHR_CUDA_TRY(cudaGetLastError());
     int32_t bad = 0;
-    CHR_CUDA_TRY(cudaMemcpyAsync(&bad, d_bad, sizeof(bad), cudaMemcpyDeviceToHost, st));
-    CHR_CUDA_TRY(cudaMemcpyAsync(pl.regs.data(), pl.d_regs, sizeof(RegDev), cudaMemcpyDeviceToHost, st));
-    CHR_CUDA_TRY(cudaStreamSynchronize(st));
+    CHR_CUDA_TRY(d2h(&bad, d_bad, sizeof(bad), st));
+    CHR_CUDA_TRY(d2h(pl.regs.data(), pl.d_regs, sizeof(RegDev), st));
+    CHR_CUDA_TRY(stream_sync(st));
     if (bad) return CHR_E_PARAMETER;
     *h_nbytes = (uint64_t)pl.regs[0].tok_len;
     return CHR_OK;
@@ -1390,6 +1394,7 @@ static bool dist_plan(const chr_region_t *h, int64_t nreg, int64_t z_base, int64
 
 extern "C" size_t chr_dcompress_workspace_size(const chr_region_t *h, int64_t nreg, int64_t z_base, int64_t nz_local,
                                                int64_t zs, int64_t ze) {
+    CHR_XFER_SCOPE;
     EncPlan pl;
     if (!h || nreg < 1 || !dist_plan(h, nreg, z_base, nz_local, zs, ze, pl)) return 0;
     carve(pl, nullptr, ~size_t(0));
@@ -1460,6 +1465,7 @@ extern "C" int chr_dcompress_local(const void *d_vol, int dtype, int src_dtype, 
                                    int64_t nz_local, int64_t z_base, int64_t zs, int64_t ze,
                                    const chr_region_t *h_regions, int64_t nreg, void *d_ws, size_t ws_bytes,
                                    chr_portion_t *h_portions, void *stream) {
+    CHR_XFER_SCOPE;
     if (!d_vol || !h_regions || nreg < 1 || !h_portions) return CHR_E_PARAMETER;
     if (dtype != CHR_F32 && dtype != CHR_F64) return CHR_E_PARAMETER;
     static_assert(sizeof(chr_portion_t) == sizeof(TokSeg), "chr_portion_t mirrors TokSeg");
@@ -1473,9 +1479,9 @@ extern "C" int chr_dcompress_local(const void *d_vol, int dtype, int src_dtype, 
     TokSeg *d_agg = reinterpret_cast<TokSeg *>(reinterpret_cast<char *>(d_ws) + pl.ws_bytes);
     EncParams hp;
     dist_params(hp, pl, nx, ny, nz_local, dtype, src_dtype, 0, nullptr, 1, 0, 0, nullptr, 0, nreg);
-    CHR_CUDA_TRY(cudaMemcpyAsync(pl.params, &hp, sizeof(hp), cudaMemcpyHostToDevice, st));
-    CHR_CUDA_TRY(cudaMemcpyAsync(pl.d_regs, pl.regs.data(), sizeof(RegDev) * nreg, cudaMemcpyHostToDevice, st));
-    CHR_CUDA_TRY(cudaMemsetAsync(pl.escbits, 0, sizeof(uint32_t) * (pl.etotal + 2), st));
+    CHR_CUDA_TRY(h2d(pl.params, &hp, sizeof(hp), st));
+    CHR_CUDA_TRY(h2d(pl.d_regs, pl.regs.data(), sizeof(RegDev) * nreg, st));
+    CHR_CUDA_TRY(fill_async(pl.escbits, 0, sizeof(uint32_t) * (pl.etotal + 2), st));
     const unsigned items = (unsigned)pl.nitems, chunks = (unsigned)pl.nchunks;
     k_tile_fill_map<<<(unsigned)nreg, 256, 0, st>>>(pl.d_regs, nreg, pl.item_reg, pl.chunk_reg);
     if (items) {
@@ -1502,8 +1508,8 @@ extern "C" int chr_dcompress_local(const void *d_vol, int dtype, int src_dtype, 
     }
     k_portion_agg<<<(unsigned)ceil_div(nreg, 4), 128, 0, st>>>(pl.d_regs, nreg, pl.chunk, dtype == CHR_F32, d_agg);
     CHR_CUDA_TRY(cudaGetLastError());
-    CHR_CUDA_TRY(cudaMemcpyAsync(h_portions, d_agg, sizeof(TokSeg) * nreg, cudaMemcpyDeviceToHost, st));
-    CHR_CUDA_TRY(cudaStreamSynchronize(st));
+    CHR_CUDA_TRY(d2h(h_portions, d_agg, sizeof(TokSeg) * nreg, st));
+    CHR_CUDA_TRY(stream_sync(st));
     return CHR_OK;
 }
 
@@ -1521,6 +1527,7 @@ extern "C" int chr_dcompress_finish(const void *d_vol, int dtype, int src_dtype,
                                     chr_region_t *h_regions, int64_t nreg, const chr_portion_t *h_all, int nranks,
                                     int rank, void *d_ws, size_t ws_bytes, uint8_t *d_out, uint64_t out_cap,
                                     uint32_t *h_raw, uint64_t *h_file_nbytes, void *stream) {
+    CHR_XFER_SCOPE;
     if (!d_vol || !h_regions || nreg < 1 || !h_all || nranks < 1 || rank < 0 || rank >= nranks || !d_out ||
         !h_raw || !h_file_nbytes || m < 1 || m > 64 || !h_cands)
         return CHR_E_PARAMETER;
@@ -1531,8 +1538,8 @@ extern "C" int chr_dcompress_finish(const void *d_vol, int dtype, int src_dtype,
     if (!d_ws || pl.ws_bytes > ws_bytes) return CHR_E_WORKSPACE;
     if (out_cap < chr_compress_capacity(h_regions, nreg, m, src_dtype)) return CHR_E_PARAMETER;
     // the device records keep phase 1's flags (has_esc, f32bad, maps)
-    CHR_CUDA_TRY(cudaMemcpyAsync(pl.regs.data(), pl.d_regs, sizeof(RegDev) * nreg, cudaMemcpyDeviceToHost, st));
-    CHR_CUDA_TRY(cudaStreamSynchronize(st));
+    CHR_CUDA_TRY(d2h(pl.regs.data(), pl.d_regs, sizeof(RegDev) * nreg, st));
+    CHR_CUDA_TRY(stream_sync(st));
     std::vector<int32_t> c2;
     for (int64_t r = 0; r < nreg; ++r) {
         RegDev &R = pl.regs[r];
@@ -1576,11 +1583,11 @@ extern "C" int chr_dcompress_finish(const void *d_vol, int dtype, int src_dtype,
     EncScalars hs0;
     std::memset(&hs0, 0, sizeof(hs0));
     hs0.n_codec2 = (int64_t)c2.size();
-    CHR_CUDA_TRY(cudaMemcpyAsync(pl.params, &hp, sizeof(hp), cudaMemcpyHostToDevice, st));
-    CHR_CUDA_TRY(cudaMemcpyAsync(pl.d_regs, pl.regs.data(), sizeof(RegDev) * nreg, cudaMemcpyHostToDevice, st));
-    CHR_CUDA_TRY(cudaMemcpyAsync(pl.scal, &hs0, sizeof(hs0), cudaMemcpyHostToDevice, st));
+    CHR_CUDA_TRY(h2d(pl.params, &hp, sizeof(hp), st));
+    CHR_CUDA_TRY(h2d(pl.d_regs, pl.regs.data(), sizeof(RegDev) * nreg, st));
+    CHR_CUDA_TRY(h2d(pl.scal, &hs0, sizeof(hs0), st));
     if (!c2.empty())
-        CHR_CUDA_TRY(cudaMemcpyAsync(pl.codec2, c2.data(), sizeof(int32_t) * c2.size(), cudaMemcpyHostToDevice, st));
+        CHR_CUDA_TRY(h2d(pl.codec2, c2.data(), sizeof(int32_t) * c2.size(), st));
     const unsigned chunks = (unsigned)pl.nchunks;
     k_scan_regions<<<(unsigned)ceil_div(nreg, 4), 128, 0, st>>>(pl.params, pl.d_regs, pl.chunk, pl.codec2, pl.scal);
     k_layout<<<1, 1024, 0, st>>>(pl.params, pl.d_regs, pl.segs, pl.scal);
@@ -1597,9 +1604,9 @@ extern "C" int chr_dcompress_finish(const void *d_vol, int dtype, int src_dtype,
     if (!c2.empty()) k_bitmap<<<148, 256, 0, st>>>(pl.d_regs, pl.codec2, pl.scal, pl.escbits, d_out);
     CHR_CUDA_TRY(cudaGetLastError());
     EncScalars hs;
-    CHR_CUDA_TRY(cudaMemcpyAsync(pl.regs.data(), pl.d_regs, sizeof(RegDev) * nreg, cudaMemcpyDeviceToHost, st));
-    CHR_CUDA_TRY(cudaMemcpyAsync(&hs, pl.scal, sizeof(hs), cudaMemcpyDeviceToHost, st));
-    CHR_CUDA_TRY(cudaStreamSynchronize(st));
+    CHR_CUDA_TRY(d2h(pl.regs.data(), pl.d_regs, sizeof(RegDev) * nreg, st));
+    CHR_CUDA_TRY(d2h(&hs, pl.scal, sizeof(hs), st));
+    CHR_CUDA_TRY(stream_sync(st));
     // this rank's byte ranges inside every payload (+ the header/table on rank 0)
     std::vector<CrcSeg> segs;
     std::vector<int64_t> seg_reg;
@@ -1639,13 +1646,13 @@ extern "C" int chr_dcompress_finish(const void *d_vol, int dtype, int src_dtype,
         CrcSeg *d_segs = reinterpret_cast<CrcSeg *>(reinterpret_cast<char *>(d_ws) + pl.ws_bytes);
         uint32_t *d_sraw = reinterpret_cast<uint32_t *>(d_segs + ns);
         if (pl.ws_bytes + (size_t)ns * (sizeof(CrcSeg) + 4) + 64 > ws_bytes) return CHR_E_WORKSPACE;
-        CHR_CUDA_TRY(cudaMemcpyAsync(d_segs, segs.data(), sizeof(CrcSeg) * ns, cudaMemcpyHostToDevice, st));
-        CHR_CUDA_TRY(cudaMemsetAsync(d_sraw, 0, sizeof(uint32_t) * ns, st));
+        CHR_CUDA_TRY(h2d(d_segs, segs.data(), sizeof(CrcSeg) * ns, st));
+        CHR_CUDA_TRY(fill_async(d_sraw, 0, sizeof(uint32_t) * ns, st));
         int rc = crc_launch(d_out, d_segs, ns, total_sc, d_sraw, st);
         if (rc) return rc;
         std::vector<uint32_t> sraw(ns);
-        CHR_CUDA_TRY(cudaMemcpyAsync(sraw.data(), d_sraw, sizeof(uint32_t) * ns, cudaMemcpyDeviceToHost, st));
-        CHR_CUDA_TRY(cudaStreamSynchronize(st));
+        CHR_CUDA_TRY(d2h(sraw.data(), d_sraw, sizeof(uint32_t) * ns, st));
+        CHR_CUDA_TRY(stream_sync(st));
         const CrcTables &H = crc_tables_hostref();
         for (int64_t i = 0; i < ns; ++i) {
             const int64_t r = seg_reg[i];
@@ -1671,6 +1678,7 @@ extern "C" int chr_dcompress_headers(int64_t nx, int64_t ny, int64_t nz, int src
                                      int64_t bs, double vmin, double vmax, const double *h_cands, int m,
                                      chr_region_t *h_regions, int64_t nreg, const uint32_t *h_raw_all, void *d_ws,
                                      size_t ws_bytes, uint8_t *d_out, void *stream) {
+    CHR_XFER_SCOPE;
     if (!h_regions || nreg < 1 || !h_raw_all || !d_out || m < 1 || m > 64 || !h_cands) return CHR_E_PARAMETER;
     cudaStream_t st = (cudaStream_t)stream;
     EncPlan pl;
@@ -1702,20 +1710,20 @@ extern "C" int chr_dcompress_headers(int64_t nx, int64_t ny, int64_t nz, int src
     std::memset(&hs0, 0, sizeof(hs0));
     hs0.file_body = body;
     hs0.out_nbytes = body + 4;
-    CHR_CUDA_TRY(cudaMemcpyAsync(pl.params, &hp, sizeof(hp), cudaMemcpyHostToDevice, st));
-    CHR_CUDA_TRY(cudaMemcpyAsync(pl.d_regs, pl.regs.data(), sizeof(RegDev) * nreg, cudaMemcpyHostToDevice, st));
-    CHR_CUDA_TRY(cudaMemcpyAsync(pl.scal, &hs0, sizeof(hs0), cudaMemcpyHostToDevice, st));
+    CHR_CUDA_TRY(h2d(pl.params, &hp, sizeof(hp), st));
+    CHR_CUDA_TRY(h2d(pl.d_regs, pl.regs.data(), sizeof(RegDev) * nreg, st));
+    CHR_CUDA_TRY(h2d(pl.scal, &hs0, sizeof(hs0), st));
     // file header + region table (global windows), then their raw CRC into
     // seg_raw[0]; seg_raw[1 + r] = payload raw CRCs (XOR of every rank's share)
     k_write_table<<<(unsigned)ceil_div(nreg, 256), 256, 0, st>>>(pl.params, pl.d_regs, d_out);
-    CHR_CUDA_TRY(cudaMemcpyAsync(pl.seg_raw + 1, h_raw_all + 1, sizeof(uint32_t) * nreg, cudaMemcpyHostToDevice, st));
-    CHR_CUDA_TRY(cudaMemsetAsync(pl.seg_raw, 0, sizeof(uint32_t), st));
+    CHR_CUDA_TRY(h2d(pl.seg_raw + 1, h_raw_all + 1, sizeof(uint32_t) * nreg, st));
+    CHR_CUDA_TRY(fill_async(pl.seg_raw, 0, sizeof(uint32_t), st));
     CrcSeg hseg;
     std::memset(&hseg, 0, sizeof(hseg));
     hseg.begin = 0;
     hseg.end = hp.header_table;
     const int64_t hsc = crc_plan_segments(&hseg, 1);
-    CHR_CUDA_TRY(cudaMemcpyAsync(pl.segs, &hseg, sizeof(hseg), cudaMemcpyHostToDevice, st));
+    CHR_CUDA_TRY(h2d(pl.segs, &hseg, sizeof(hseg), st));
     {
         const int rc = crc_launch(d_out, pl.segs, 1, hsc, pl.seg_raw, st);
         if (rc) return rc;
@@ -1724,8 +1732,8 @@ extern "C" int chr_dcompress_headers(int64_t nx, int64_t ny, int64_t nz, int src
                                                                       d_out);
     k_finalize_file<<<1, 1, 0, st>>>(tabs, pl.scal, d_out);
     CHR_CUDA_TRY(cudaGetLastError());
-    CHR_CUDA_TRY(cudaMemcpyAsync(pl.regs.data(), pl.d_regs, sizeof(RegDev) * nreg, cudaMemcpyDeviceToHost, st));
-    CHR_CUDA_TRY(cudaStreamSynchronize(st));
+    CHR_CUDA_TRY(d2h(pl.regs.data(), pl.d_regs, sizeof(RegDev) * nreg, st));
+    CHR_CUDA_TRY(stream_sync(st));
     for (int64_t r = 0; r < nreg; ++r) h_regions[r].payload_crc = pl.regs[r].crc;
     return CHR_OK;
 }

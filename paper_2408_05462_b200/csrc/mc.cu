@@ -846,6 +846,7 @@ static void mc_carve(McPlan &pl, void *base, size_t cap) {
 using namespace chr;
 
 extern "C" size_t chr_mc_workspace_size(const chr_mc_grid_t *h, int64_t n) {
+    CHR_XFER_SCOPE;
     McPlan pl;
     if (!h || n < 1 || !mc_build(h, n, pl)) return 256;
     mc_carve(pl, nullptr, ~size_t(0));
@@ -861,12 +862,14 @@ static int mc_emit_impl(const double *d_grids, const chr_mc_grid_t *h, int64_t n
 extern "C" int chr_mc_count(const double *d_grids, const chr_mc_grid_t *h, int64_t n, double k, void *d_ws,
                             size_t ws_bytes, int64_t *h_ntri, int64_t *h_nvert, int64_t *h_total_tri,
                             int64_t *h_total_vert, void *stream) {
+    CHR_XFER_SCOPE;
     return mc_count_impl(d_grids, h, n, k, nullptr, d_ws, ws_bytes, h_ntri, h_nvert, h_total_tri, h_total_vert,
                          stream);
 }
 extern "C" int chr_mc_count_masked(const double *d_grids, const chr_mc_grid_t *h, int64_t n, double k,
                                    const uint32_t *d_masks, void *d_ws, size_t ws_bytes, int64_t *h_ntri,
                                    int64_t *h_nvert, int64_t *h_total_tri, int64_t *h_total_vert, void *stream) {
+    CHR_XFER_SCOPE;
     if (!d_masks) return CHR_E_PARAMETER;
     return mc_count_impl(d_grids, h, n, k, d_masks, d_ws, ws_bytes, h_ntri, h_nvert, h_total_tri, h_total_vert,
                          stream);
@@ -874,6 +877,7 @@ extern "C" int chr_mc_count_masked(const double *d_grids, const chr_mc_grid_t *h
 extern "C" int chr_mc_emit_masked(const double *d_grids, const chr_mc_grid_t *h, int64_t n, double k,
                                   const uint32_t *d_masks, void *d_ws, size_t ws_bytes, double *d_verts,
                                   int32_t *d_tris, void *stream) {
+    CHR_XFER_SCOPE;
     if (!d_masks) return CHR_E_PARAMETER;
     return mc_emit_impl(d_grids, h, n, k, d_masks, d_ws, ws_bytes, d_verts, d_tris, stream);
 }
@@ -894,15 +898,15 @@ static int mc_count_impl(const double *d_grids, const chr_mc_grid_t *h, int64_t 
     if (!d_ws || pl.ws > ws_bytes) return CHR_E_WORKSPACE;
     const McTables *T = mc_tables_device();
     if (!T) return CHR_E_CUDA;
-    CHR_CUDA_TRY(cudaMemcpyAsync(pl.d_grids, pl.grids.data(), sizeof(McGrid) * n, cudaMemcpyHostToDevice, st));
-    CHR_CUDA_TRY(cudaMemsetAsync(pl.cnt, 0, sizeof(McPieceCnt) * pl.npieces, st));
+    CHR_CUDA_TRY(h2d(pl.d_grids, pl.grids.data(), sizeof(McGrid) * n, st));
+    CHR_CUDA_TRY(fill_async(pl.cnt, 0, sizeof(McPieceCnt) * pl.npieces, st));
     {
         CHR_PROF("k_mc_fill_map", st);
         k_mc_fill_map<<<(unsigned)n, 256, 0, st>>>(pl.d_grids, n, pl.item_grid, pl.chunk_grid, pl.mask_grid);
     }
     const uint32_t *masks = d_masks ? d_masks : pl.mask;  // caller's masks (decoder output) or our own
     if (!d_masks) {
-        CHR_CUDA_TRY(cudaMemsetAsync(pl.mask + pl.nmask_words, 0, 8 * sizeof(uint32_t), st));
+        CHR_CUDA_TRY(fill_async(pl.mask + pl.nmask_words, 0, 8 * sizeof(uint32_t), st));
         if (pl.nmask_items > 0) {
             CHR_PROF("k_mc_mask", st);
             k_mc_mask<<<(unsigned)pl.nmask_items, 256, 0, st>>>(d_grids, pl.d_grids, pl.mask_grid, k, pl.mask);
@@ -929,8 +933,8 @@ static int mc_count_impl(const double *d_grids, const chr_mc_grid_t *h, int64_t 
         k_mc_down<<<(unsigned)pl.nchunks, 256, 0, st>>>(pl.cnt, pl.chunk, pl.base);
     }
     CHR_CUDA_TRY(cudaGetLastError());
-    CHR_CUDA_TRY(cudaMemcpyAsync(pl.grids.data(), pl.d_grids, sizeof(McGrid) * n, cudaMemcpyDeviceToHost, st));
-    CHR_CUDA_TRY(cudaStreamSynchronize(st));
+    CHR_CUDA_TRY(d2h(pl.grids.data(), pl.d_grids, sizeof(McGrid) * n, st));
+    CHR_CUDA_TRY(stream_sync(st));
     int64_t tt = 0, tv = 0;
     for (int64_t i = 0; i < n; ++i) {
         if (h_ntri) h_ntri[i] = pl.grids[i].ntri;
@@ -945,6 +949,7 @@ static int mc_count_impl(const double *d_grids, const chr_mc_grid_t *h, int64_t 
 
 extern "C" int chr_mc_emit(const double *d_grids, const chr_mc_grid_t *h, int64_t n, double k, void *d_ws,
                            size_t ws_bytes, double *d_verts, int32_t *d_tris, void *stream) {
+    CHR_XFER_SCOPE;
     return mc_emit_impl(d_grids, h, n, k, nullptr, d_ws, ws_bytes, d_verts, d_tris, stream);
 }
 
@@ -967,12 +972,13 @@ static int mc_emit_impl(const double *d_grids, const chr_mc_grid_t *h, int64_t n
                                                                  d_tris);
         }
     CHR_CUDA_TRY(cudaGetLastError());
-    CHR_CUDA_TRY(cudaStreamSynchronize(st));
+    CHR_CUDA_TRY(stream_sync(st));
     return CHR_OK;
 }
 
 extern "C" int chr_case_codes(const double *d_grid, int64_t nx, int64_t ny, int64_t nz, double k, int binary,
                               uint8_t *d_codes, void *stream) {
+    CHR_XFER_SCOPE;
     if (!d_grid || !d_codes || nx < 2 || ny < 2 || nz < 2) return CHR_E_PARAMETER;
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t n = (nx - 1) * (ny - 1) * (nz - 1);

@@ -55,17 +55,20 @@ ProfScope::~ProfScope() {
 using namespace chr;
 
 extern "C" void chr_prof_enable(int on) {
+    CHR_XFER_SCOPE;
     std::lock_guard<std::mutex> lk(g_mu);
     g_on = on != 0;
 }
 
 extern "C" long long chr_launch_count(void) {
+    CHR_XFER_SCOPE;
     std::lock_guard<std::mutex> lk(g_mu);
     return g_launches;
 }
 
 // "name count total_ms\n" per kernel name since the last report; clears.
 extern "C" int chr_prof_report(char *buf, size_t cap) {
+    CHR_XFER_SCOPE;
     std::lock_guard<std::mutex> lk(g_mu);
     std::map<std::string, std::pair<long long, double>> agg;
     for (const Rec &r : g_recs) {
@@ -96,6 +99,7 @@ extern "C" int chr_prof_report(char *buf, size_t cap) {
 // "name start_ms end_ms\n" per recorded launch (relative to the first
 // record's start), in launch order; clears like chr_prof_report.
 extern "C" int chr_prof_timeline(char *buf, size_t cap) {
+    CHR_XFER_SCOPE;
     std::lock_guard<std::mutex> lk(g_mu);
     std::string s;
     cudaEvent_t t0 = g_recs.empty() ? nullptr : g_recs.front().a;
@@ -124,6 +128,7 @@ extern "C" int chr_prof_timeline(char *buf, size_t cap) {
 // a named zero-length record on the stream (host-side phase marks in the
 // timeline; not counted as a launch).  The name must outlive the report.
 extern "C" void chr_prof_mark(const char *name, void *stream) {
+    CHR_XFER_SCOPE;
     std::lock_guard<std::mutex> lk(g_mu);
     if (!g_on) return;
     static std::map<std::string, std::string> names;  // stable storage

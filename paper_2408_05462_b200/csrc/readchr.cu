@@ -78,6 +78,7 @@ __global__ void k_read_table(const uint8_t *__restrict__ f, uint64_t nbytes, uin
 using namespace chr;
 
 extern "C" int chr_read_header(const uint8_t *d_file, uint64_t nbytes, chr_file_info_t *h_info, void *stream) {
+    CHR_XFER_SCOPE;
     if (!h_info || (!d_file && nbytes)) return CHR_E_PARAMETER;
     std::memset(h_info, 0, sizeof(*h_info));
     if (nbytes < kFileHdr + 4) {
@@ -86,8 +87,8 @@ extern "C" int chr_read_header(const uint8_t *d_file, uint64_t nbytes, chr_file_
     }
     cudaStream_t st = (cudaStream_t)stream;
     uint8_t hdr[kFileHdr + 4];
-    CHR_CUDA_TRY(cudaMemcpyAsync(hdr, d_file, kFileHdr + 4, cudaMemcpyDeviceToHost, st));
-    CHR_CUDA_TRY(cudaStreamSynchronize(st));
+    CHR_CUDA_TRY(d2h(hdr, d_file, kFileHdr + 4, st));
+    CHR_CUDA_TRY(stream_sync(st));
     std::memcpy(h_info->magic, hdr, 4);
     if (std::memcmp(hdr, "CHR1", 4) != 0) {
         h_info->error = CHR_READ_BAD_MAGIC;
@@ -106,8 +107,8 @@ extern "C" int chr_read_header(const uint8_t *d_file, uint64_t nbytes, chr_file_
     const uint64_t rpos = kFileHdr + 4 + 8ull * h_info->m;
     if (rpos + 4 <= nbytes) {
         uint32_t nreg = 0;
-        CHR_CUDA_TRY(cudaMemcpyAsync(&nreg, d_file + rpos, 4, cudaMemcpyDeviceToHost, st));
-        CHR_CUDA_TRY(cudaStreamSynchronize(st));
+        CHR_CUDA_TRY(d2h(&nreg, d_file + rpos, 4, st));
+        CHR_CUDA_TRY(stream_sync(st));
         h_info->n_regions = nreg;
     } else {
         h_info->error = CHR_READ_TABLE_PAST_END;
@@ -116,19 +117,21 @@ extern "C" int chr_read_header(const uint8_t *d_file, uint64_t nbytes, chr_file_
     h_info->table_nbytes = tab_end;
     if (!h_info->error && tab_end > nbytes) h_info->error = CHR_READ_TABLE_PAST_END;
     uint32_t stored;
-    CHR_CUDA_TRY(cudaMemcpyAsync(&stored, d_file + nbytes - 4, 4, cudaMemcpyDeviceToHost, st));
-    CHR_CUDA_TRY(cudaStreamSynchronize(st));
+    CHR_CUDA_TRY(d2h(&stored, d_file + nbytes - 4, 4, st));
+    CHR_CUDA_TRY(stream_sync(st));
     h_info->stored_crc = stored;
     return CHR_OK;
 }
 
 extern "C" size_t chr_read_workspace_size(uint64_t nbytes, int64_t n_regions) {
+    CHR_XFER_SCOPE;
     (void)nbytes;
     return 256 + (size_t)n_regions * sizeof(chr_table_entry_t) + 256;
 }
 
 extern "C" int chr_read_archive(const uint8_t *d_file, uint64_t nbytes, chr_file_info_t *h_info, double *h_cands,
                                 chr_table_entry_t *h_entries, void *d_ws, size_t ws_bytes, void *stream) {
+    CHR_XFER_SCOPE;
     if (!h_info || !d_file || nbytes < kFileHdr + 4) return CHR_E_PARAMETER;
     const int64_t nreg = h_info->n_regions;
     if (!d_ws || ws_bytes < chr_read_workspace_size(nbytes, nreg)) return CHR_E_WORKSPACE;
@@ -144,8 +147,8 @@ extern "C" int chr_read_archive(const uint8_t *d_file, uint64_t nbytes, chr_file
     CrcSeg *d_seg = reinterpret_cast<CrcSeg *>(ws);
     uint32_t *d_raw = reinterpret_cast<uint32_t *>(ws + 128);
     chr_table_entry_t *d_ent = reinterpret_cast<chr_table_entry_t *>(ws + 256);
-    CHR_CUDA_TRY(cudaMemcpyAsync(d_seg, &seg, sizeof(seg), cudaMemcpyHostToDevice, st));
-    CHR_CUDA_TRY(cudaMemsetAsync(d_raw, 0, 4, st));
+    CHR_CUDA_TRY(h2d(d_seg, &seg, sizeof(seg), st));
+    CHR_CUDA_TRY(fill_async(d_raw, 0, 4, st));
     {
         CHR_PROF("k_crc_segments", st);
         const int rc = crc_launch(d_file, d_seg, 1, seg.n_sc, d_raw, st);
@@ -158,13 +161,13 @@ extern "C" int chr_read_archive(const uint8_t *d_file, uint64_t nbytes, chr_file
                                                                    (uint64_t)nreg * (kRecFixed + (h_info->m + 7) / 8),
                                                                    (int)h_info->m, nreg, d_ent);
         CHR_CUDA_TRY(cudaGetLastError());
-        CHR_CUDA_TRY(cudaMemcpyAsync(h_entries, d_ent, nreg * sizeof(chr_table_entry_t), cudaMemcpyDeviceToHost, st));
+        CHR_CUDA_TRY(d2h(h_entries, d_ent, nreg * sizeof(chr_table_entry_t), st));
     }
     if (h_cands && h_info->m && kFileHdr + 4 + 8ull * h_info->m <= nbytes)
-        CHR_CUDA_TRY(cudaMemcpyAsync(h_cands, d_file + kFileHdr + 4, 8ull * h_info->m, cudaMemcpyDeviceToHost, st));
+        CHR_CUDA_TRY(d2h(h_cands, d_file + kFileHdr + 4, 8ull * h_info->m, st));
     uint32_t raw = 0;
-    CHR_CUDA_TRY(cudaMemcpyAsync(&raw, d_raw, 4, cudaMemcpyDeviceToHost, st));
-    CHR_CUDA_TRY(cudaStreamSynchronize(st));
+    CHR_CUDA_TRY(d2h(&raw, d_raw, 4, st));
+    CHR_CUDA_TRY(stream_sync(st));
     h_info->actual_crc = crc_finalize(H.x2n, raw, nbytes - 4);
     return CHR_OK;
 }

@@ -209,6 +209,7 @@ __global__ void __launch_bounds__(SQ) k_stats_rows(const float *__restrict__ vol
 using namespace chr;
 
 extern "C" int64_t chr_num_blocks(int64_t nx, int64_t ny, int64_t nz, int64_t bs) {
+    CHR_XFER_SCOPE;
     if (bs < 1) return 0;
     auto nb = [bs](int64_t d) { return d - 1 > 0 ? (d - 1 + bs - 1) / bs : (int64_t)1; };
     return nb(nx) * nb(ny) * nb(nz);
@@ -217,6 +218,7 @@ extern "C" int64_t chr_num_blocks(int64_t nx, int64_t ny, int64_t nz, int64_t bs
 extern "C" int chr_stats(const void *d_vol, int dtype, int64_t nx, int64_t ny, int64_t nz,
                          int64_t bs, const double *h_cands, int m, double *d_block_stats,
                          int64_t *d_first_nonfinite, void *stream) {
+    CHR_XFER_SCOPE;
     if (!d_vol || !d_block_stats || !d_first_nonfinite || !h_cands) return CHR_E_PARAMETER;
     if (bs < 2 || nx < 2 || ny < 2 || nz < 2 || m < 1 || m > 64) return CHR_E_PARAMETER;
     if (dtype != CHR_F32 && dtype != CHR_F64) return CHR_E_PARAMETER;
@@ -226,7 +228,7 @@ extern "C" int chr_stats(const void *d_vol, int dtype, int64_t nx, int64_t ny, i
     for (int i = 0; i < m; ++i) cp.k[i] = h_cands[i];
     const int nbx = (int)((nx - 1 + bs - 1) / bs), nby = (int)((ny - 1 + bs - 1) / bs);
     const int64_t nblocks = chr_num_blocks(nx, ny, nz, bs);
-    CHR_CUDA_TRY(cudaMemsetAsync(d_first_nonfinite, 0xFF, sizeof(int64_t), st));
+    CHR_CUDA_TRY(fill_async(d_first_nonfinite, 0xFF, sizeof(int64_t), st));
     auto *bad = reinterpret_cast<unsigned long long *>(d_first_nonfinite);
     const int nbz = (int)((nz - 1 + bs - 1) / bs);
     const bool rows_ok = dtype == CHR_F32 && bs % 4 == 0 && nx % 4 == 0 && nx <= 4 * SQ &&

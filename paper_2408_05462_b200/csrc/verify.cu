@@ -124,6 +124,7 @@ __global__ void __launch_bounds__(TX *TY) k_topo_compare(const TA *__restrict__ 
 using namespace chr;
 
 extern "C" size_t chr_stitch_workspace_size(int64_t n_windows, int64_t nx, int64_t ny, int64_t nz, int64_t bs) {
+    CHR_XFER_SCOPE;
     if (bs < 1) return 0;
     auto nb = [&](int64_t d) { return std::max<int64_t>(1, (d - 1 + bs - 1) / bs); };
     return (size_t)n_windows * sizeof(StitchDev) + (size_t)nb(nx) * nb(ny) * nb(nz) * 4 + 1024;
@@ -131,6 +132,7 @@ extern "C" size_t chr_stitch_workspace_size(int64_t n_windows, int64_t nx, int64
 
 extern "C" int chr_stitch(const double *d_windows, const chr_stitch_t *h_windows, int64_t n, int64_t nx, int64_t ny,
                           int64_t nz, int64_t bs, void *d_ws, size_t ws_bytes, double *d_out, void *stream) {
+    CHR_XFER_SCOPE;
     if (n == 0) return CHR_OK;
     if (!d_windows || !h_windows || !d_out || bs < 1 || nx < 1 || ny < 1 || nz < 1) return CHR_E_PARAMETER;
     if (!d_ws || ws_bytes < chr_stitch_workspace_size(n, nx, ny, nz, bs)) return CHR_E_WORKSPACE;
@@ -178,8 +180,8 @@ extern "C" int chr_stitch(const double *d_windows, const chr_stitch_t *h_windows
     cudaStream_t st = (cudaStream_t)stream;
     StitchDev *d_tab = reinterpret_cast<StitchDev *>(d_ws);
     int32_t *d_prio = reinterpret_cast<int32_t *>(reinterpret_cast<char *>(d_ws) + n * sizeof(StitchDev));
-    CHR_CUDA_TRY(cudaMemcpyAsync(d_tab, tab.data(), n * sizeof(StitchDev), cudaMemcpyHostToDevice, st));
-    CHR_CUDA_TRY(cudaMemcpyAsync(d_prio, prio.data(), prio.size() * 4, cudaMemcpyHostToDevice, st));
+    CHR_CUDA_TRY(h2d(d_tab, tab.data(), n * sizeof(StitchDev), st));
+    CHR_CUDA_TRY(h2d(d_prio, prio.data(), prio.size() * 4, st));
     {
         CHR_PROF("k_stitch", st);
         k_stitch<<<(unsigned)ceil_div(rows, 8), 256, 0, st>>>(d_windows, d_tab, n, rows, d_prio, nx, ny, (int)bs,
@@ -192,6 +194,7 @@ extern "C" int chr_stitch(const double *d_windows, const chr_stitch_t *h_windows
 extern "C" int chr_topology_compare(const void *d_a, int dtype_a, const void *d_b, int dtype_b, int64_t nx,
                                     int64_t ny, int64_t nz, double k, void *d_ws, size_t ws_bytes,
                                     uint64_t *h_ndiff, int64_t *h_first, void *stream) {
+    CHR_XFER_SCOPE;
     if (!d_a || !d_b || !h_ndiff || !h_first || nx < 2 || ny < 2 || nz < 2) return CHR_E_PARAMETER;
     if ((dtype_a != CHR_F32 && dtype_a != CHR_F64) || (dtype_b != CHR_F32 && dtype_b != CHR_F64))
         return CHR_E_PARAMETER;
@@ -199,7 +202,7 @@ extern "C" int chr_topology_compare(const void *d_a, int dtype_a, const void *d_
     cudaStream_t st = (cudaStream_t)stream;
     unsigned long long *d_res = reinterpret_cast<unsigned long long *>(d_ws);
     const unsigned long long init[2] = {0ull, ~0ull};
-    CHR_CUDA_TRY(cudaMemcpyAsync(d_res, init, 16, cudaMemcpyHostToDevice, st));
+    CHR_CUDA_TRY(h2d(d_res, init, 16, st));
     const dim3 grid((unsigned)ceil_div(nx - 1, TX), (unsigned)ceil_div(ny - 1, TY), (unsigned)ceil_div(nz - 1, TZ));
     {
         CHR_PROF("k_topo_compare", st);
@@ -213,8 +216,8 @@ extern "C" int chr_topology_compare(const void *d_a, int dtype_a, const void *d_
     }
     CHR_CUDA_TRY(cudaGetLastError());
     unsigned long long res[2];
-    CHR_CUDA_TRY(cudaMemcpyAsync(res, d_res, 16, cudaMemcpyDeviceToHost, st));
-    CHR_CUDA_TRY(cudaStreamSynchronize(st));
+    CHR_CUDA_TRY(d2h(res, d_res, 16, st));
+    CHR_CUDA_TRY(stream_sync(st));
     *h_ndiff = res[0];
     *h_first = res[0] ? (int64_t)res[1] : -1;
     return CHR_OK;

@@ -1,0 +1,172 @@
+// xfer.cu -- the library's small host<->device transfers without the copy
+// engines.  A caller pipelining bulk transfers (hundreds of MB on the DMA
+// engines, other streams) would otherwise hold every small plan/size copy
+// of the library behind them in the engines' queues.  Small transfers go
+// through a thread-local pinned, mapped ring instead: host->device copies
+// are staged there and pulled by a tiny kernel on the caller's stream;
+// device->host copies are pushed into it by a kernel and delivered to the
+// destination at the next chr::stream_sync() of that stream.  Transfers
+// above kXferBig keep cudaMemcpyAsync.
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "chr_internal.cuh"
+
+namespace chr {
+
+namespace {
+constexpr size_t kXferBig = 4u << 20;
+
+struct Pending {
+    const uint8_t *src;
+    void *dst;
+    size_t n;
+    cudaStream_t st;
+};
+
+struct Ring {
+    uint8_t *buf = nullptr;
+    size_t cap = 0, head = 0;
+    std::vector<Pending> pend;
+    std::vector<cudaStream_t> users;  // streams with ring traffic since the last reset
+};
+
+thread_local Ring g_ring;
+
+__global__ void k_xfer(const uint8_t *__restrict__ src, uint8_t *__restrict__ dst, size_t n) {
+    const size_t i0 = (size_t)blockIdx.x * blockDim.x + threadIdx.x, stride = (size_t)gridDim.x * blockDim.x;
+    if ((((uintptr_t)src | (uintptr_t)dst) & 15) == 0) {
+        const size_t n16 = n >> 4;
+        for (size_t i = i0; i < n16; i += stride)
+            reinterpret_cast<uint4 *>(dst)[i] = reinterpret_cast<const uint4 *>(src)[i];
+        for (size_t i = (n16 << 4) + i0; i < n; i += stride) dst[i] = src[i];
+    } else {
+        for (size_t i = i0; i < n; i += stride) dst[i] = src[i];
+    }
+}
+
+cudaError_t launch_xfer(const void *src, void *dst, size_t n, cudaStream_t st) {
+    const unsigned blocks = (unsigned)std::min<size_t>(64, (n + 4095) / 4096 + 1);
+    CHR_PROF("k_xfer", st);
+    k_xfer<<<blocks, 256, 0, st>>>((const uint8_t *)src, (uint8_t *)dst, n);
+    return cudaGetLastError();
+}
+
+void deliver(cudaStream_t st) {
+    Ring &R = g_ring;
+    size_t k = 0;
+    for (const Pending &p : R.pend) {
+        if (p.st == st) std::memcpy(p.dst, p.src, p.n);
+        else R.pend[k++] = p;
+    }
+    R.pend.resize(k);
+}
+
+cudaError_t reserve(size_t n, cudaStream_t st, uint8_t **out) {
+    Ring &R = g_ring;
+    n = (n + 255) & ~size_t(255);
+    if (R.head + n > R.cap) {  // wait for every stream using the ring, then reuse (or grow) it
+        for (cudaStream_t s : R.users) {
+            const cudaError_t e = cudaStreamSynchronize(s);
+            if (e != cudaSuccess) return e;
+            deliver(s);
+        }
+        R.users.clear();
+        R.head = 0;
+        if (n > R.cap) {
+            if (R.buf) cudaFreeHost(R.buf);
+            R.buf = nullptr;
+            R.cap = std::max({n, R.cap * 2, size_t(8) << 20});
+            const cudaError_t e = cudaHostAlloc(reinterpret_cast<void **>(&R.buf), R.cap,
+                                                cudaHostAllocMapped | cudaHostAllocPortable);
+            if (e != cudaSuccess) {
+                R.cap = 0;
+                return e;
+            }
+        }
+    }
+    *out = R.buf + R.head;
+    R.head += n;
+    if (std::find(R.users.begin(), R.users.end(), st) == R.users.end()) R.users.push_back(st);
+    return cudaSuccess;
+}
+}  // namespace
+
+cudaError_t h2d(void *dst, const void *src, size_t n, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    if (n > kXferBig) return cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, st);
+    uint8_t *p = nullptr;
+    cudaError_t e = reserve(n, st, &p);
+    if (e != cudaSuccess) return e;
+    std::memcpy(p, src, n);
+    return launch_xfer(p, dst, n, st);
+}
+
+cudaError_t d2h(void *dst, const void *src, size_t n, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    if (n > kXferBig) return cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToHost, st);
+    uint8_t *p = nullptr;
+    cudaError_t e = reserve(n, st, &p);
+    if (e != cudaSuccess) return e;
+    e = launch_xfer(src, p, n, st);
+    if (e == cudaSuccess) g_ring.pend.push_back({p, dst, n, st});
+    return e;
+}
+
+namespace {
+__global__ void k_fill(uint8_t *__restrict__ dst, int v, size_t n) {
+    const size_t i0 = (size_t)blockIdx.x * blockDim.x + threadIdx.x, stride = (size_t)gridDim.x * blockDim.x;
+    const uint32_t w = 0x01010101u * (uint32_t)(v & 0xFF);
+    if (((uintptr_t)dst & 15) == 0) {
+        const size_t n16 = n >> 4;
+        for (size_t i = i0; i < n16; i += stride) reinterpret_cast<uint4 *>(dst)[i] = make_uint4(w, w, w, w);
+        for (size_t i = (n16 << 4) + i0; i < n; i += stride) dst[i] = (uint8_t)v;
+    } else {
+        for (size_t i = i0; i < n; i += stride) dst[i] = (uint8_t)v;
+    }
+}
+}  // namespace
+
+// cudaMemsetAsync as a kernel (no copy engine)
+cudaError_t fill_async(void *dst, int v, size_t n, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    const unsigned blocks = (unsigned)std::min<size_t>(1184, (n + 16383) / 16384 + 1);
+    CHR_PROF("k_fill", st);
+    k_fill<<<blocks, 256, 0, st>>>((uint8_t *)dst, v, n);
+    return cudaGetLastError();
+}
+
+// device-accessible pointers (device or mapped pinned host), any alignment
+cudaError_t copy_async(void *dst, const void *src, size_t n, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    return launch_xfer(src, dst, n, st);
+}
+
+cudaError_t stream_sync(cudaStream_t st) {
+    const cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return e;
+    Ring &R = g_ring;
+    deliver(st);
+    if (R.users.size() == 1 && R.users[0] == st) {  // nothing else in flight in the ring
+        R.users.clear();
+        R.head = 0;
+    }
+    return cudaSuccess;
+}
+
+XferScope::XferScope() : mark_(g_ring.pend.size()) {}
+XferScope::~XferScope() {  // undelivered copies of this call (an error path) must not outlive its buffers
+    if (g_ring.pend.size() > mark_) g_ring.pend.resize(mark_);
+}
+
+}  // namespace chr
+
+using namespace chr;
+
+// copy between device-accessible pointers (device memory or pinned host
+// memory) with a kernel on `stream`: no copy engine, any alignment
+extern "C" int chr_copy(void *dst, const void *src, uint64_t nbytes, void *stream) {
+    if (nbytes && (!dst || !src)) return CHR_E_PARAMETER;
+    return copy_async(dst, src, nbytes, (cudaStream_t)stream) == cudaSuccess ? CHR_OK : CHR_E_CUDA;
+}

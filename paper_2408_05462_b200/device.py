@@ -235,8 +235,9 @@ def build_archive(vol: torch.Tensor, dims, cands, bs, *, spacing=(1.0, 1.0, 1.0)
         raise ParameterError(f"candidates must be finite and strictly increasing, got {list(cands)}")
     bst, bad = stats(vol, dims, bs, cands)
     host = ws.pinned("block_stats", bst.numel() + 1)
-    host[:-1].copy_(bst.reshape(-1), non_blocking=True)
-    host[-1:].copy_(bad.view(torch.float64), non_blocking=True)
+    L = lib()  # kernel copies into pinned memory: never queued behind a caller's bulk DMA
+    check(L.chr_copy(host.data_ptr(), bst.data_ptr(), 8 * bst.numel(), stream_ptr()), "chr_copy")
+    check(L.chr_copy(host.data_ptr() + 8 * bst.numel(), bad.data_ptr(), 8, stream_ptr()), "chr_copy")
     torch.cuda.current_stream().synchronize()
     hs = host.numpy()
     badidx = int(hs[-1:].view(np.int64)[0])
