@@ -159,12 +159,20 @@ def kernel_bytes(name, info, N):
     return table.get(name)
 
 
+def workload_name(config, n, bs, r, cands):
+    return (f"{config}: {n}^3 f32 " + {
+        "c3": "lognormal exp(1.5 g), g unit-variance GRF P(k)~k^-3", "c4": "GRF P(k)~k^-11/3 [0,1]",
+        "c2": "GRF P(k)~k^-11/3 |k|<=32 [0,1]", "c1": "8 Gaussian blobs + noise",
+        "c5": "GRF + 64 blobs"}.get(config, "") +
+        f", bs{bs}, r={r}, k={cands[0]:.6g}; step = compress -> request(k) -> marching cubes")
+
+
 def cpu_baseline(vals_host, dims, bs, cands, r, planes, workers):
     """The oracle port timed on host cores on a bounded z-slab sample."""
     from oracle import oracle as O
 
     nx, ny, nz = dims
-    pz = min(planes, nz)
+    pz = min(planes, nz) if planes > 0 else nz
     sample = np.ascontiguousarray(vals_host[: nx * ny * pz]).astype(np.float64)
     sdims = (nx, ny, pz)
     lo, hi = float(sample.min()), float(sample.max())
@@ -176,8 +184,9 @@ def cpu_baseline(vals_host, dims, bs, cands, r, planes, workers):
     O.extract_regions(sel, (1.0, 1.0, 1.0), k)
     t = time.perf_counter() - t0
     return {"value": 4 * nx * ny * pz / t / 1e9, "unit": "GB/s", "cores": workers, "kind": "port",
-            "sample": f"{nx}x{ny}x{pz} z-slab of the same field (first {pz} planes), same bs/r/k; "
-                      f"build_chr + request + per-region MC, {t:.2f} s"}
+            "sample": (f"{nx}x{ny}x{pz} z-slab of the same field (first {pz} planes), same bs/r/k; "
+                       if pz < nz else "the whole workload (same volume, bs, r, k); ") +
+                      f"build_chr + request + per-region MC, {t:.2f} s wall on {workers} threads"}
 
 
 def main():
@@ -188,7 +197,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c3")
     ap.add_argument("--edge", "--size", dest="n", type=int, default=None, help="edge length override (tests)")
-    ap.add_argument("--cpu-planes", type=int, default=32)
+    ap.add_argument("--cpu-planes", type=int, default=0,
+                    help="CPU baseline sample: first P z-planes of the volume (0 = the whole volume)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-copy", default="dma", choices=["dma", "sm"],
                     help="bulk H2D/D2H of the e2e loop: DMA engines or the UVA copy kernel")
@@ -231,11 +241,14 @@ def main():
             if i >= args.warmup:
                 times.append(cb)
         v = statistics.median([t["value"] for t in times])
+        pz = min(args.cpu_planes, dims[2]) if args.cpu_planes > 0 else dims[2]
         line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": args.gpus,
                 "steps": args.steps, "warmup": args.warmup,
-                "ms_per_step": 4 * dims[0] * dims[1] * min(args.cpu_planes, dims[2]) / v / 1e6,
+                "ms_per_step": 4 * dims[0] * dims[1] * pz / v / 1e6,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic", "config": {"workload": f"{args.config} {n}^3 bounded z-slab sample"},
+                "data": "synthetic (seeded torch GRF; no public dataset)",
+                "config": {"workload": workload_name(args.config, n, bs, r, cands), "dims": list(dims),
+                           "block_size": bs},
                 "cpu_baseline": dict(times[-1], value=v),
                 "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
@@ -402,11 +415,7 @@ def main():
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded torch GRF; no public dataset)",
         "config": {
-            "workload": f"{args.config}: {n}^3 f32 " + {
-                "c3": "lognormal exp(1.5 g), g unit-variance GRF P(k)~k^-3", "c4": "GRF P(k)~k^-11/3 [0,1]",
-                "c2": "GRF P(k)~k^-11/3 |k|<=32 [0,1]", "c1": "8 Gaussian blobs + noise",
-                "c5": "GRF + 64 blobs"}.get(args.config, "") +
-            f", bs{bs}, r={r}, k={cands[0]:.6g}; step = compress -> request(k) -> marching cubes",
+            "workload": workload_name(args.config, n, bs, r, cands),
             "dims": list(dims), "block_size": bs, "regions": info["nreg"], "regions_selected": info["nsel"],
             "archive_bytes": info["archive"], "selected_samples": info["n_sel"], "cells": info["cells"],
             "triangles": info["ntri"], "vertices": info["nvert"],
