@@ -517,7 +517,7 @@ __global__ void __launch_bounds__(256) k_mc_count3(const McGrid *__restrict__ G,
 // 3-deep ring; cells rows y0-1..y0+7 x columns x0-1..x0+63 (65) with their
 // (code, vertex base) in a 3-deep ring, so every owner is local.
 constexpr int EW = 10;  // warps: sample rows y0-1 .. y0+8
-__global__ void __launch_bounds__(EW * 32, 3) k_mc_emit2(const double *__restrict__ grids, const McGrid *__restrict__ G,
+__global__ void __launch_bounds__(EW * 32, 4) k_mc_emit2(const double *__restrict__ grids, const McGrid *__restrict__ G,
                                                       const int32_t *__restrict__ item_grid, double k,
                                                       const McTables *__restrict__ T,
                                                       const McPieceBase *__restrict__ base,
