@@ -941,8 +941,8 @@ __global__ void __launch_bounds__(256) k_esc_seg(const DecReg *__restrict__ regs
 // taking tiles in diagonal order from a ticket cannot deadlock; a tile
 // publishes its own faces right after the wait (a few adds per column)
 // and only then writes its samples, so a chain hop costs one face update.
-constexpr int BCAP = 6144;   // samples per tile
-constexpr int BDF = 2048;    // dF entries (btz * ex) when a tile has a band above
+constexpr int BCAP = 5632;   // samples per tile (44 KB of int64 + 8 KB dF: 4 CTAs per SM)
+constexpr int BDF = 1024;    // dF entries (btz * ex) when a tile has a band above
 constexpr int BSEGM = 64;    // planes per tile
 
 __device__ __forceinline__ int seg_of(const int32_t *base, int nseg, int g) {
