@@ -576,3 +576,46 @@ def test_read_table_at_config_size(tmp_path):
     for f in ("lo", "hi", "origin", "extent", "mask", "error_bound", "codec_id", "payload_crc", "block_offset",
               "block_nbytes"):
         assert np.array_equal(got[f], want[f]), f
+
+
+# ----------------------------------------------------------------- reentrancy (no global mutable state)
+def test_concurrent_threads_on_separate_streams():
+    """Two host threads, each on its own stream and workspaces, run compress ->
+    request -> marching cubes at the same time (ctypes drops the GIL inside
+    the library): results identical to a sequential run.  Exercises the
+    thread-local transfer ring and decoder plan cache."""
+    import threading
+
+    jobs = []
+    for name, n in (("c2", 80), ("c5", 64)):
+        vals, dims, bs, cands, r = synth.make_config(name, device="cuda", n=n)
+        jobs.append((vals, dims, bs, cands, r))
+
+    def run(job, ws, stream):
+        vals, dims, bs, cands, r = job
+        with torch.cuda.stream(stream):
+            res = device.build_archive(vals, dims, cands, bs, loose_fraction=r, ws=ws)
+            regs = res.regions
+            sel = regs[(regs["mask"] & np.uint64(1)) != 0]
+            dec = device.dec_table(sel["block_offset"] + device.BLOCK_HEADER, sel["block_nbytes"] - device.BLOCK_HEADER,
+                                   sel["codec_id"], sel["extent"], sel["error_bound"], sel["payload_crc"])
+            wins, offs, st = device.decode(res.blob, dec, ws=ws, iso=cands[0])
+            mct = device.mc_table(dec["out_offset"], sel["extent"], sel["origin"].astype(np.float64), (1.0, 1.0, 1.0))
+            v, t, _, _ = device.marching(wins, mct, cands[0], ws=ws, masks=ws.get("decode_mask", 4, torch.int32))
+            stream.synchronize()
+            return (res.blob[: res.nbytes].cpu().numpy().tobytes(), sha(wins[: int(np.prod(sel["extent"].astype(np.int64), axis=1).sum())].cpu().numpy()),
+                    sha(v.cpu().numpy()), sha(t.cpu().numpy()), list(st))
+
+    want = [run(j, device.Workspaces(), torch.cuda.Stream()) for j in jobs]
+    for _ in range(3):
+        got = [None, None]
+
+        def worker(i):
+            got[i] = run(jobs[i], device.Workspaces(), torch.cuda.Stream())
+
+        th = [threading.Thread(target=worker, args=(i,)) for i in range(2)]
+        for x in th:
+            x.start()
+        for x in th:
+            x.join()
+        assert got == want
