@@ -141,31 +141,40 @@ __global__ void __launch_bounds__(SQ) k_stats_rows(const float *__restrict__ vol
         double dm = INFINITY, gd = INFINITY;
         unsigned long long bad = ~0ull;
         const bool ghost = ((4 * q) % bs) == 0 && q > 0;
-        int zr = g / nrow_y, yr = g - (g / nrow_y) * nrow_y;
-        for (int r = g; r < nrows; r += rg) {
-            const int64_t z = z0 + zr, y = y0 + yr;
-            yr += rg;
-            while (yr >= nrow_y) {
-                yr -= nrow_y;
-                ++zr;
-            }
-            const float4 v4 = __ldg(reinterpret_cast<const float4 *>(vol + (z * ny + y) * nx) + q);
-            const float v[4] = {v4.x, v4.y, v4.z, v4.w};
+        // RU rows per step: their 16-byte loads are all in flight before any is
+        // used (one outstanding load per thread left HBM at ~35 % of peak)
+        constexpr int RU = 4;
+        for (int r0 = g; r0 < nrows; r0 += RU * rg) {
+            float4 v4[RU];
+            int64_t rowoff[RU];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const float f = v[i];
-                if (!isfinite(f)) {
-                    bad = min(bad, (unsigned long long)((z * ny + y) * nx + 4 * q + i));
-                    continue;
-                }
-                lo = fminf(lo, f);
-                hi = fmaxf(hi, f);
-                const double d = min_cand_dist(ks, m, (double)f);
-                dm = fmin(dm, d);
-                if (i == 0 && ghost) {
-                    gl = fminf(gl, f);
-                    gh = fmaxf(gh, f);
-                    gd = fmin(gd, d);
+            for (int u = 0; u < RU; ++u) {
+                const int r = r0 + u * rg;
+                const int zr = r / nrow_y, yr = r - zr * nrow_y;
+                rowoff[u] = ((z0 + zr) * ny + (y0 + yr)) * nx;
+                v4[u] = r < nrows ? __ldg(reinterpret_cast<const float4 *>(vol + rowoff[u]) + q)
+                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int u = 0; u < RU; ++u) {
+                if (r0 + u * rg >= nrows) break;
+                const float v[4] = {v4[u].x, v4[u].y, v4[u].z, v4[u].w};
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const float f = v[i];
+                    if (!isfinite(f)) {
+                        bad = min(bad, (unsigned long long)(rowoff[u] + 4 * q + i));
+                        continue;
+                    }
+                    lo = fminf(lo, f);
+                    hi = fmaxf(hi, f);
+                    const double d = min_cand_dist(ks, m, (double)f);
+                    dm = fmin(dm, d);
+                    if (i == 0 && ghost) {
+                        gl = fminf(gl, f);
+                        gh = fmaxf(gh, f);
+                        gd = fmin(gd, d);
+                    }
                 }
             }
         }
