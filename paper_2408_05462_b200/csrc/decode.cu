@@ -1066,12 +1066,9 @@ __device__ __forceinline__ int64_t band_scatter_unit64(const Win24 &W, int64_t a
 template <bool PAD>
 __device__ __forceinline__ int band_scatter_unit32(const Win24 &W, int at, int L, int ex, uint64_t M,
                                                    int64_t *__restrict__ q) {
-    int idx = at, x = 0;
-    if (PAD && at >= 0) {
-        const int row = (int)(((uint64_t)at * M) >> 32);
-        x = at - row * ex;
-        idx = row * (ex + 1) + x;
-    }
+    // branch-free over the 16 own positions: a literal ending at e is stored
+    // at its position (predicated), every token advances `at` (1 or the run
+    // length); PAD planes place position t at t + t / ex
     uint32_t H = 0;
 #pragma unroll
     for (int j = 4; j < 8; ++j) H = (H >> 7) | ((win_byte(W, j) & 0x7Fu) << 21);
@@ -1079,28 +1076,16 @@ __device__ __forceinline__ int band_scatter_unit32(const Win24 &W, int at, int L
     for (int e = 8; e < 24; ++e) {
         H = (H >> 7) | ((win_byte(W, e) & 0x7Fu) << 21);
         const bool lit = (W.lit >> e) & 1u, run = (W.len >> e) & 1u;
-        if (!(lit | run)) continue;
         const uint32_t below = W.E & ((1u << e) - 1u);
         const int len = e - (32 - __clz(below)) + 1;
         const uint32_t v = H >> (7 * (4 - len));
-        if (lit) {
+        if (lit && (unsigned)at < (unsigned)L) {
             const uint32_t zz = v - 1u;
-            if ((unsigned)at < (unsigned)L) q[idx] = (int64_t)(int32_t)((zz >> 1) ^ (0u - (zz & 1u)));
-            ++at;
-            ++idx;
-            if (PAD && ++x == ex) {
-                x = 0;
-                ++idx;
-            }
-        } else {
-            at = (int)min((int64_t)at + (int64_t)v, (int64_t)0x7FFFFFFF);
-            idx = min(at, L);
-            if (PAD && at >= 0 && at < L) {
-                const int row = (int)(((uint64_t)at * M) >> 32);
-                x = at - row * ex;
-                idx = row * (ex + 1) + x;
-            }
+            const int idx = PAD ? at + (int)(((uint64_t)(unsigned)at * M) >> 32) : at;
+            q[idx] = (int64_t)(int32_t)((zz >> 1) ^ (0u - (zz & 1u)));
         }
+        const int64_t adv = lit ? 1 : (run ? (int64_t)v : 0);
+        at = (int)min((int64_t)at + adv, (int64_t)0x7FFFFFFF);
     }
     return at;
 }
