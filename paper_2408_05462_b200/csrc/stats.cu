@@ -11,14 +11,33 @@
 // Closed form used for the bound (verified against the
 // oracle in tests): per sample, min_k |s - k| is attained at one of the two
 // candidates bracketing s, because fl(s - k) is monotone in k.
+#include <cmath>
+
 #include "chr_internal.cuh"
 
 namespace chr {
 
 struct CandParams {
     double k[64];
+    float thr[64];  // smallest float >= k[j]: for a float s, k[j] <= s  <=>  s >= thr[j]
     int m;
 };
+
+// min_k |s - k| for a float sample: the bracketing index by single-precision
+// compares against thr (exact, see CandParams), the two distances in f64
+__device__ __forceinline__ double min_cand_dist_f32(const double *k, const float *thr, int m, float s) {
+    if (m == 1) return fabs(__dadd_rn((double)s, -k[0]));
+    // #{j : k[j] <= s} = first candidate > s: branch-free binary search over
+    // the thresholds padded with +inf to 128 (a finite s is never >= +inf)
+    int lo = 0;
+#pragma unroll
+    for (int step = 64; step; step >>= 1)
+        if (step < 2 * m && s >= thr[lo + step - 1]) lo += step;
+    double d = INFINITY;
+    if (lo > 0) d = fabs(__dadd_rn((double)s, -k[lo - 1]));
+    if (lo < m) d = fmin(d, fabs(__dadd_rn((double)s, -k[lo])));
+    return d;
+}
 
 __device__ __forceinline__ double min_cand_dist(const double *k, int m, double s) {
     if (m == 1) return fabs(__dadd_rn(s, -k[0]));
@@ -116,15 +135,43 @@ __global__ void __launch_bounds__(256) k_stats(const T *__restrict__ vol, int64_
 // partials go through shared memory and one thread per block combines its
 // bs/4 quads plus the x-ghost sample (first sample of the next block).
 constexpr int SQ = 512;  // threads; nx/4 <= SQ quads per row
+constexpr int SB = 4096;  // candidate buckets (k_stats_rows, m > 1)
 __global__ void __launch_bounds__(SQ) k_stats_rows(const float *__restrict__ vol, int64_t nx, int64_t ny,
                                                    int64_t nz, int bs, int nbx, int nby, CandParams cp,
                                                    double *__restrict__ stats,
                                                    unsigned long long *__restrict__ first_bad) {
-    __shared__ double ks[64];
+    __shared__ double ks[128];
+    __shared__ float kt[128];  // thresholds, +inf padded (the search may probe up to 2m - 2)
     // per (row group, quad) partials: index g * nq + q  (rg * nq <= SQ)
     __shared__ float plo[SQ], phi[SQ], pgl[SQ], pgh[SQ];
     __shared__ double pdm[SQ], pgd[SQ];
-    if (threadIdx.x < cp.m) ks[threadIdx.x] = cp.k[threadIdx.x];
+    if (threadIdx.x < 128) ks[threadIdx.x] = threadIdx.x < cp.m ? cp.k[threadIdx.x] : INFINITY;
+    if (threadIdx.x < 128) kt[threadIdx.x] = threadIdx.x < cp.m ? cp.thr[threadIdx.x] : INFINITY;
+    __syncthreads();
+    // bucket table: a sample f in [thr[0], thr[m-1]) maps to bucket
+    // b(f) = min(SB-1, int((f - lo_e) * invw)), monotone in f.  A bucket no
+    // threshold maps to has one answer, #{j : b(thr[j]) < b}; a bucket some
+    // threshold maps to is flagged (0x80) and resolved by exact compares.
+    __shared__ uint8_t kb[SB];
+    const float lo_e = kt[0], hi_e = cp.m > 1 ? kt[cp.m - 1] : kt[0];
+    const float invw = hi_e > lo_e ? (float)SB / (hi_e - lo_e) : 0.f;
+    auto bucket = [&](float f) { return min(SB - 1, (int)((f - lo_e) * invw)); };
+    if (cp.m > 1) {
+        for (int b = threadIdx.x; b < SB; b += blockDim.x) {
+            int c = 0, hit = 0;
+            for (int j = 0; j < cp.m; ++j) {
+                const float t = kt[j];
+                if (!(t >= lo_e) || !(t < hi_e)) {  // outside the bucketed range
+                    c += t < lo_e ? 1 : 0;
+                    continue;
+                }
+                const int bt = bucket(t);
+                c += bt < b ? 1 : 0;
+                hit |= bt == b ? 1 : 0;
+            }
+            kb[b] = (uint8_t)(c | (hit << 7));
+        }
+    }
     __syncthreads();
     const int nq = (int)(nx >> 2);
     const int m = cp.m;
@@ -168,7 +215,28 @@ __global__ void __launch_bounds__(SQ) k_stats_rows(const float *__restrict__ vol
                     }
                     lo = fminf(lo, f);
                     hi = fmaxf(hi, f);
-                    const double d = min_cand_dist(ks, m, (double)f);
+                    // min |s - k| over the two candidates bracketing s
+                    const double sd = (double)f;
+                    double d;
+                    if (m == 1) {
+                        d = fabs(__dadd_rn(sd, -ks[0]));
+                    } else {
+                        int c;  // #{j : k[j] <= s}
+                        if (!(f >= lo_e)) {
+                            c = 0;
+                        } else if (f >= hi_e) {
+                            c = m;
+                        } else {
+                            const int v = kb[min(SB - 1, (int)((f - lo_e) * invw))];
+                            c = v & 0x7F;
+                            if (v & 0x80) {  // a threshold falls in this bucket: exact compares
+                                while (c < m && f >= kt[c]) ++c;
+                                while (c > 0 && f < kt[c - 1]) --c;
+                            }
+                        }
+                        const double kl = c > 0 ? ks[c - 1] : -INFINITY;
+                        d = fmin(fabs(__dadd_rn(sd, -kl)), fabs(__dadd_rn(sd, -ks[c])));  // ks[m] = +inf
+                    }
                     dm = fmin(dm, d);
                     if (i == 0 && ghost) {
                         gl = fminf(gl, f);
@@ -234,7 +302,13 @@ extern "C" int chr_stats(const void *d_vol, int dtype, int64_t nx, int64_t ny, i
     cudaStream_t st = (cudaStream_t)stream;
     CandParams cp;
     cp.m = m;
-    for (int i = 0; i < m; ++i) cp.k[i] = h_cands[i];
+    for (int i = 0; i < m; ++i) {
+        cp.k[i] = h_cands[i];
+        float f = (float)h_cands[i];  // round to nearest, then up to the smallest float >= k
+        if (std::isnan(h_cands[i])) f = INFINITY;
+        else if ((double)f < h_cands[i]) f = std::nextafter(f, INFINITY);
+        cp.thr[i] = f;
+    }
     const int nbx = (int)((nx - 1 + bs - 1) / bs), nby = (int)((ny - 1 + bs - 1) / bs);
     const int64_t nblocks = chr_num_blocks(nx, ny, nz, bs);
     CHR_CUDA_TRY(fill_async(d_first_nonfinite, 0xFF, sizeof(int64_t), st));
