@@ -117,14 +117,12 @@ def run_step(vol, dims, bs, cands, r, ws, spacing=(1.0, 1.0, 1.0), stage_events=
     if ev:
         ev[1].record()
     regs = res.regions
-    sel = regs[(regs["mask"] & np.uint64(1)) != 0]  # regions relevant to candidate 0
-    dec = D.dec_table(sel["block_offset"] + D.BLOCK_HEADER, sel["block_nbytes"] - D.BLOCK_HEADER,
-                      sel["codec_id"], sel["extent"], sel["error_bound"], sel["payload_crc"])
+    dec, mct, sel_idx, _ = D.request_tables(regs, 0, spacing)  # regions relevant to candidate 0
+    sel = regs[sel_idx]
     wins, offs, status = D.decode(res.blob, dec, ws=ws, iso=cands[0])  # + inside masks for MC
     assert not any(status), status
     if ev:
         ev[2].record()
-    mct = D.mc_table(dec["out_offset"], sel["extent"], sel["origin"] * np.asarray(spacing), spacing)
     verts, tris, nt, nv = D.marching(wins, mct, cands[0], ws=ws, reuse_outputs=True,
                                      masks=ws.get("decode_mask", 4, torch.int32))
     if ev:

@@ -362,6 +362,14 @@ size_t chr_read_workspace_size(uint64_t nbytes, int64_t n_regions);
 int chr_read_archive(const uint8_t *d_file, uint64_t nbytes, chr_file_info_t *h_info, double *h_cands,
                      chr_table_entry_t *h_entries, void *d_workspace, size_t workspace_bytes, void *stream);
 
+/* 16. request(k) tables from a region table, host only (chr_archive.py:249-259):
+ *     regions whose mask has bit k_index (all when k_index < 0) as decode and
+ *     marching tables with back-to-back windows; returns the count (-1 on a
+ *     bad argument).  Output arrays need n entries. */
+int64_t chr_request_tables(const chr_region_t *h_regions, int64_t n, int k_index, const double *spacing,
+                           chr_dec_region_t *h_dec, chr_mc_grid_t *h_mc, int64_t *h_sel,
+                           uint64_t *h_total_samples);
+
 /* 9. instrumentation: launch counter and opt-in per-kernel CUDA-event
  *    timing on the launching stream ("name count total_ms" lines). */
 void chr_prof_enable(int on);

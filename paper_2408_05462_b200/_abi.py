@@ -230,6 +230,8 @@ def lib():
         L.chr_prof_mark.restype = None
         L.chr_copy.argtypes = [P, P, U64, P]
         L.chr_copy.restype = INT
+        L.chr_request_tables.argtypes = [P, I64, INT, P, P, P, P, P]
+        L.chr_request_tables.restype = I64
         _lib = L
     return _lib
 
@@ -240,7 +242,7 @@ EXPORTS = [
     "chr_select_workspace_size", "chr_select_distances", "chr_compress2",
     "chr_stitch_workspace_size", "chr_stitch", "chr_topology_compare",
     "chr_read_header", "chr_read_workspace_size", "chr_read_archive", "chr_prof_timeline",
-    "chr_prof_mark", "chr_copy",
+    "chr_prof_mark", "chr_copy", "chr_request_tables",
     "chr_dcompress_workspace_size", "chr_dcompress_local", "chr_dcompress_finish", "chr_dcompress_headers",
     "chr_abi_version", "chr_status_string", "chr_num_blocks", "chr_stats", "chr_plan",
     "chr_compress_workspace_size", "chr_compress_capacity", "chr_compress",

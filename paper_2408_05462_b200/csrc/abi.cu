@@ -1,6 +1,8 @@
 // abi.cu -- library info + kernel-seam entry points on single windows
 // (isochr/kernels.py: min_abs_distance kernels.py:417-425,
 // lorenzo_encode kernels.py:47-128).
+#include <cstring>
+
 #include "chr_internal.cuh"
 
 namespace chr {
@@ -132,4 +134,50 @@ extern "C" int chr_sm_copy(void *dst, const void *src, uint64_t nbytes, int ctas
         k_sm_copy<<<(unsigned)std::max(1, ctas), 256, 0, st>>>((const uint8_t *)src, (uint8_t *)dst, nbytes);
     }
     return cudaGetLastError() == cudaSuccess ? CHR_OK : CHR_E_CUDA;
+}
+
+// request(k) tables from an archive's region table (chr_archive.py:249-259
+// selection; host only): the regions whose relevance mask has bit
+// k_index (all regions when k_index < 0), as chr_dec_region_t (payload
+// after the 34-byte block header, windows back to back) and chr_mc_grid_t
+// (world origin = sample origin * spacing).  Returns the selected count;
+// h_sel receives their region indices, *h_total_samples the window sum.
+extern "C" int64_t chr_request_tables(const chr_region_t *h_regions, int64_t n, int k_index, const double *spacing,
+                                      chr_dec_region_t *h_dec, chr_mc_grid_t *h_mc, int64_t *h_sel,
+                                      uint64_t *h_total_samples) {
+    if (!h_regions || n < 0 || k_index > 63) return -1;
+    int64_t m = 0;
+    uint64_t off = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        const chr_region_t &r = h_regions[i];
+        if (k_index >= 0 && !((r.mask >> k_index) & 1ull)) continue;
+        const uint64_t ns = (uint64_t)r.extent[0] * r.extent[1] * r.extent[2];
+        if (h_dec) {
+            chr_dec_region_t &d = h_dec[m];
+            std::memset(&d, 0, sizeof(d));
+            d.payload_offset = r.block_offset + 34;
+            d.payload_nbytes = r.block_nbytes - 34;
+            d.codec_id = r.codec_id;
+            for (int a = 0; a < 3; ++a) d.dims[a] = r.extent[a];
+            d.error_bound = r.error_bound;
+            d.crc = r.payload_crc;
+            d.out_offset = off;
+        }
+        if (h_mc) {
+            chr_mc_grid_t &g = h_mc[m];
+            std::memset(&g, 0, sizeof(g));
+            g.grid_offset = off;
+            for (int a = 0; a < 3; ++a) {
+                g.dims[a] = r.extent[a];
+                const double sp = spacing ? spacing[a] : 1.0;
+                g.origin[a] = (double)r.origin[a] * sp;
+                g.spacing[a] = sp;
+            }
+        }
+        if (h_sel) h_sel[m] = i;
+        off += ns;
+        ++m;
+    }
+    if (h_total_samples) *h_total_samples = off;
+    return m;
 }

@@ -268,6 +268,24 @@ def build_archive(vol: torch.Tensor, dims, cands, bs, *, spacing=(1.0, 1.0, 1.0)
     return res
 
 
+def request_tables(regions: np.ndarray, k_index: int, spacing=(1.0, 1.0, 1.0)):
+    """(decode table, marching table, selected region indices, total window
+    samples) for request(k) over a ``REGION_DT`` table, built in C
+    (chr_request_tables); ``k_index`` < 0 selects every region."""
+    regions = np.ascontiguousarray(regions, dtype=_abi.REGION_DT)
+    n = len(regions)
+    dec = np.empty(n, dtype=_abi.DEC_DT)
+    mct = np.empty(n, dtype=_abi.MCGRID_DT)
+    sel = np.empty(n, dtype=np.int64)
+    total = ctypes.c_uint64(0)
+    sp = (ctypes.c_double * 3)(*[float(v) for v in spacing])
+    m = lib().chr_request_tables(_abi.aptr(regions), n, int(k_index), sp, _abi.aptr(dec), _abi.aptr(mct),
+                                 _np_ptr(sel), ctypes.byref(total))
+    if m < 0:
+        raise ParameterError("chr_request_tables: bad arguments")
+    return dec[:m], mct[:m], sel[:m], int(total.value)
+
+
 def dec_table(payload_offset, payload_nbytes, codec, dims, e, crc) -> np.ndarray:
     """Vectorised chr_dec_region_t table (windows laid out back to back)."""
     n = len(payload_offset)

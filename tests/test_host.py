@@ -185,3 +185,33 @@ def test_slab_geometry_partitions_planes_and_blocks(nz, bs, world):
     assert covered[0][0] == 0 and covered[-1][1] == nz
     assert all(a[1] == b[0] for a, b in zip(covered, covered[1:]))
     assert layers == list(range(nbz))
+
+
+def test_request_tables_match_selection():
+    """chr_request_tables (host C) == the numpy selection + table build of
+    request(k) (chr_archive.py:249-259)."""
+    from paper_2408_05462_b200 import _abi, device
+
+    rng = np.random.default_rng(4)
+    n = 57
+    regs = np.zeros(n, dtype=_abi.REGION_DT)
+    regs["extent"] = rng.integers(2, 40, size=(n, 3))
+    regs["origin"] = rng.integers(0, 500, size=(n, 3))
+    regs["mask"] = rng.integers(0, 8, size=n).astype(np.uint64)
+    regs["block_offset"] = np.cumsum(rng.integers(40, 4000, size=n))
+    regs["block_nbytes"] = rng.integers(34, 3000, size=n)
+    regs["codec_id"] = rng.integers(0, 4, size=n)
+    regs["error_bound"] = rng.random(n)
+    regs["payload_crc"] = rng.integers(0, 2**32, size=n, dtype=np.uint64).astype(np.uint32)
+    spacing = (0.5, 2.0, 1.25)
+    for ki in (-1, 0, 1, 2):
+        dec, mct, sel_idx, total = device.request_tables(regs, ki, spacing)
+        want = np.arange(n) if ki < 0 else np.nonzero((regs["mask"] >> np.uint64(ki)) & np.uint64(1))[0]
+        assert np.array_equal(sel_idx, want)
+        s = regs[want]
+        ref = device.dec_table(s["block_offset"] + device.BLOCK_HEADER, s["block_nbytes"] - device.BLOCK_HEADER,
+                               s["codec_id"], s["extent"], s["error_bound"], s["payload_crc"])
+        assert dec.tobytes() == ref.tobytes()
+        mref = device.mc_table(ref["out_offset"], s["extent"], s["origin"] * np.asarray(spacing), spacing)
+        assert mct.tobytes() == mref.tobytes()
+        assert total == int(np.prod(s["extent"].astype(np.int64), axis=1).sum())
