@@ -471,14 +471,24 @@ __global__ void __launch_bounds__(256) k_mc_count3(const McGrid *__restrict__ G,
     }
     for (; lp < lpe; ++lp) {
         const int x0 = xt * MTX;
-        const uint32_t *mp0 = mbase + (int64_t)cz * g.pw, *mp1 = mp0 + g.pw;
-        const int64_t b0 = (int64_t)cy * g.nx + x0, b1 = b0 + g.nx;
+        // lane r < 4 reads row (cy + (r & 1)) of plane (cz + (r >> 1)); shuffles share them
+        uint64_t mr = 0;
+        uint32_t hr = 0;
+        if (lane < 4) {
+            const uint32_t *mp = mbase + (int64_t)(cz + (lane >> 1)) * g.pw;
+            mask_bits66(mp, (int64_t)(cy + (lane & 1)) * g.nx + x0, mr, hr);
+        }
+        const uint32_t mlo = (uint32_t)mr, mhi = (uint32_t)(mr >> 32);
+        auto row = [&](int r, uint64_t &m, uint32_t &h) {
+            m = (uint64_t)__shfl_sync(0xFFFFFFFFu, mlo, r) | ((uint64_t)__shfl_sync(0xFFFFFFFFu, mhi, r) << 32);
+            h = __shfl_sync(0xFFFFFFFFu, hr, r);
+        };
         uint64_t m00, m10, m01, m11;
         uint32_t h00, h10, h01, h11;
-        mask_bits66(mp0, b0, m00, h00);
-        mask_bits66(mp0, b1, m10, h10);
-        mask_bits66(mp1, b0, m01, h01);
-        mask_bits66(mp1, b1, m11, h11);
+        row(0, m00, h00);
+        row(1, m10, h10);
+        row(2, m01, h01);
+        row(3, m11, h11);
         int t = 0, v = 0;
         // all 66 x 4 corner bits equal (the usual case away from the surface):
         // every cell is case 0 or 255, no triangles, nothing owned
