@@ -91,7 +91,7 @@ def _grid_to_device(samples) -> tuple[torch.Tensor, tuple[int, int, int]]:
     if not fin.all():
         i = int(np.argmin(fin))
         raise NonFiniteSampleError(i, float(flat[i]))
-    return torch.from_numpy(np.ascontiguousarray(flat)).to(_abi.device()), tuple(int(d) for d in g.shape)
+    return torch.from_numpy(np.require(flat, requirements=["C", "W"])).to(_abi.device()), tuple(int(d) for d in g.shape)
 
 
 def compress(samples, error_bound: float, source_dtype: str = "f64") -> CompressedBlock:
