@@ -114,7 +114,7 @@ class Volume:
                 narrow = a.astype(np.float32)
                 if np.array_equal(narrow.astype(np.float64), a):
                     a = narrow
-            object.__setattr__(self, "_dev", torch.from_numpy(np.ascontiguousarray(a)).cuda())
+            object.__setattr__(self, "_dev", torch.from_numpy(np.array(a, copy=True)).cuda())
         return self._dev
 
     def __repr__(self):

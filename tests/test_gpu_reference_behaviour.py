@@ -373,3 +373,46 @@ def test_verify_topology_and_merge():
     merged = G.merge_meshes([m1, m1])
     assert merged.num_triangles == 2 * m1.num_triangles
     assert np.array_equal(merged.triangles[m1.num_triangles:], m1.triangles + m1.num_vertices)
+
+
+# ------------------------------------------------------------------ acceptance criteria (test_acceptance.py)
+def _fields():
+    from paper_2408_05462_b200 import synth
+
+    out = [("sphere", sphere((40, 40, 40), 12.0), 0.0)]
+    for name, n in (("c2", 64), ("c3", 64), ("c5", 48)):
+        vals, dims, bs, cands, r = synth.make_config(name, device="cuda", n=n)
+        out.append((name, G.Volume(dims, (1.0, 1.0, 1.0), vals.cpu().numpy().astype(np.float64), "f32"), cands[0]))
+    return out
+
+
+def test_acceptance_strict_topology_and_relaxation_monotone():
+    """test_acceptance.py:61-75 (criterion 1) and 130-158 (criterion 4):
+    strict accuracy 1 preserves every cell case; relaxing the accuracy
+    never shrinks the bounds and never grows the bytes a request touches"""
+    for name, vol, k in _fields():
+        bounds, touched, kept = [], [], {}
+        for acc in (0.80, 0.95, 0.99, 1.0):
+            arch = G.build_chr(vol, [k], block_size=16, accuracy=acc)
+            bounds.append(max(r.error_bound for r in arch.regions if r.relevance))
+            touched.append(G.request(arch, k, accuracy=acc, drop_pruned=True).report.bytes_touched)
+            full = G.stitch_device(G.request(arch, k, accuracy=acc, drop_pruned=False), vol.dims)
+            kept[acc] = G.verify_topology(vol.grid, full, k).preserved_fraction
+        assert all(a >= b for a, b in zip(bounds, bounds[1:])), (name, bounds)
+        assert all(a <= b for a, b in zip(touched, touched[1:])), (name, touched)
+        assert kept[1.0] == 1.0, (name, kept)
+        paper = G.build_chr(vol, [k], block_size=16, bound_mode="paper_edges")
+        full = G.stitch(G.request(paper, k, drop_pruned=False), vol.dims)
+        assert 0.0 <= G.verify_topology(vol.grid, full, k).preserved_fraction <= 1.0
+
+
+def test_acceptance_codec_bound_exhaustive():
+    """test_acceptance.py:106-127 (criterion 3): no sample ever outside the
+    bound, 20 random 32^3 fields x 3 bounds"""
+    violations = 0
+    for seed in range(20):
+        g = np.random.default_rng(seed).normal(size=(32, 32, 32))
+        for frac in (1e-1, 1e-2, 1e-3):
+            e = frac * (g.max() - g.min())
+            violations += int((np.abs(G.decompress(G.compress(g, e)) - g) > e).sum())
+    assert violations == 0
