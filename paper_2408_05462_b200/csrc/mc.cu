@@ -542,8 +542,6 @@ __global__ void __launch_bounds__(EW * 32, 4) k_mc_emit2(const double *__restric
     __shared__ __align__(16) int8_t s_tri[256][16];
     __shared__ __align__(16) uint8_t s_ntri[256];
     __shared__ __align__(16) uint8_t s_own[256][8];
-    __shared__ uint8_t s_eax[12], s_elow[12][3];
-    __shared__ int8_t s_eid[3][2][2][2];
     __shared__ McGrid g;
     {  // tables -> shared memory, 16 bytes per thread
         const uint4 *src = reinterpret_cast<const uint4 *>(T->tri);
@@ -556,9 +554,22 @@ __global__ void __launch_bounds__(EW * 32, 4) k_mc_emit2(const double *__restric
         uint4 *dn = reinterpret_cast<uint4 *>(s_ntri);
         if (threadIdx.x < 16) dn[threadIdx.x] = __ldg(sn + threadIdx.x);
     }
-    if (threadIdx.x < 12) s_eax[threadIdx.x] = T->edge_axis[threadIdx.x];
-    if (threadIdx.x < 36) (&s_elow[0][0])[threadIdx.x] = (&T->edge_low[0][0])[threadIdx.x];
-    if (threadIdx.x < 24) (&s_eid[0][0][0][0])[threadIdx.x] = (&T->edge_id[0][0][0][0])[threadIdx.x];
+    // per (edge, boundary flags): the owner cell's offset (bit d set: -1 along
+    // d) and the edge's id in the owner; per edge: axis + low corner
+    __shared__ uint8_t s_cinfo[12][8], s_vinfo[12];
+    if (threadIdx.x < 96) {
+        const int e = threadIdx.x >> 3, f = threadIdx.x & 7;
+        const int a = T->edge_axis[e];
+        int l[3] = {T->edge_low[e][0], T->edge_low[e][1], T->edge_low[e][2]};
+        int d = 0;
+        for (int k = 0; k < 3; ++k)
+            if (k != a && l[k] == 0 && !((f >> k) & 1)) {
+                d |= 1 << k;
+                l[k] = 1;
+            }
+        s_cinfo[e][f] = (uint8_t)(d | (T->edge_id[a][l[0]][l[1]][l[2]] << 3));
+        if (f == 0) s_vinfo[e] = (uint8_t)(a | (T->edge_low[e][0] << 2) | (T->edge_low[e][1] << 3) | (T->edge_low[e][2] << 4));
+    }
     const int64_t item = blockIdx.x;
     coop_copy(&g, G + __ldg(item_grid + item));
     __syncthreads();
@@ -732,14 +743,9 @@ __global__ void __launch_bounds__(EW * 32, 4) k_mc_emit2(const double *__restric
                 const int f = bflags(cx, cy, cz);
                 if (sl < 3 * nt) {
                     // triangle corner: vertex id of its edge, held by the owner cell
-                    const int e = s_tri[code][sl];
-                    const int a = s_eax[e];
-                    int l0 = s_elow[e][0], l1 = s_elow[e][1], l2 = s_elow[e][2];
-                    int d0 = 0, d1 = 0, d2 = 0;
-                    if (a != 0 && l0 == 0 && cx >= 1) { d0 = -1; l0 = 1; }
-                    if (a != 1 && l1 == 0 && cy >= 1) { d1 = -1; l1 = 1; }
-                    if (a != 2 && l2 == 0 && cz >= 1) { d2 = -1; l2 = 1; }
-                    const int e2 = s_eid[a][l0][l1][l2];
+                    const int info = s_cinfo[s_tri[code][sl]][f];
+                    const int d0 = -(info & 1), d1 = -((info >> 1) & 1), d2 = -((info >> 2) & 1);
+                    const int e2 = info >> 3;
                     const int ob = d2 ? (cb == 0 ? 2 : cb - 1) : cb;
                     const int ocode = sC[ob][w + d1][c + d0];
                     const int of = bflags(cx + d0, cy + d1, cz + d2);
@@ -748,9 +754,8 @@ __global__ void __launch_bounds__(EW * 32, 4) k_mc_emit2(const double *__restric
                 } else {
                     // owned vertex of rank r: interpolate along its edge
                     const int r = sl - 3 * nt;
-                    const int e = __ldg(&T->inv[code][f][r]);
-                    const int a = s_eax[e];
-                    const int lx = s_elow[e][0], ly = s_elow[e][1], lz = s_elow[e][2];
+                    const int vi = s_vinfo[__ldg(&T->inv[code][f][r])];
+                    const int a = vi & 3, lx = (vi >> 2) & 1, ly = (vi >> 3) & 1, lz = (vi >> 4) & 1;
                     const double *sp = gp + (int64_t)(cz + lz) * nxy + (int64_t)(cy + ly) * g.nx + (cx + lx);
                     const double s0 = __ldg(sp);
                     const double s1 = __ldg(sp + (a == 0 ? 1 : (a == 1 ? (int64_t)g.nx : nxy)));
