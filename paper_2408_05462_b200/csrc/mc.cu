@@ -538,7 +538,11 @@ __global__ void __launch_bounds__(EW * 32, 4) k_mc_emit2(const double *__restric
     __shared__ uint32_t mkx[3][EW];
     __shared__ uint8_t sC[3][EW - 1][65];
     __shared__ int64_t sV[3][EW - 1][65];
-    __shared__ int32_t sT[EW - 1][65];  // triangle offset of each cell within its piece
+    // per cell row, double-buffered by plane parity (written in A, read in B):
+    __shared__ int32_t sT[2][EW - 1][64];   // triangle offset of each cell within its piece
+    __shared__ int32_t sEx[2][EW - 1][64];  // exclusive item offset of each cell within its row
+    __shared__ int32_t sTot[2][EW];         // items per emitting row (index 0 unused)
+    __shared__ int64_t sPT[2][EW - 1];      // triangle base of the row's piece
     __shared__ __align__(16) int8_t s_tri[256][16];
     __shared__ __align__(16) uint8_t s_ntri[256];
     __shared__ __align__(16) uint8_t s_own[256][8];
@@ -645,9 +649,10 @@ __global__ void __launch_bounds__(EW * 32, 4) k_mc_emit2(const double *__restric
             if (p + 1 < z1) row_mask(p + 2, nm, nmx);
         }
         const bool codes = p > pstart;  // needs planes cz and cz+1
-        const int cz = p - 1, cb = (cz + 3) % 3, qb = p % 3;
+        const int cz = p - 1, cb = (cz + 3) % 3, qb = p % 3, pp = cz & 1;
         // ---- codes, owned counts, vertex bases of cell row cy at plane cz
         int codeA = 0, codeB = 0, ntA = 0, ntB = 0, tA = 0, tB = 0, ownA = 0, ownB = 0, exA = 0, exB = 0;
+        int rowtot = 0;
         const McPieceBase pbase = pnext;
         const McPieceCnt pcnt = cnext;
         if (codes && crow && cz + 1 < z1) {
@@ -701,73 +706,83 @@ __global__ void __launch_bounds__(EW * 32, 4) k_mc_emit2(const double *__restric
             tB = (int)(pB >> 16);
             exA = 3 * tA + (int)(pA & 0xFFFFu);  // item offsets (3 per triangle + owned vertices)
             exB = 3 * tB + (int)(pB & 0xFFFFu);
+            rowtot = __shfl_sync(0xFFFFFFFFu, exB + 3 * ntB + ownB, 31);
             sC[cb][w][1 + lane] = (uint8_t)codeA;
             sC[cb][w][33 + lane] = (uint8_t)codeB;
             sV[cb][w][1 + lane] = pbase.vert + sA - ownA;
             sV[cb][w][33 + lane] = pbase.vert + totV + sB - ownB;
+            sT[pp][w][lane] = tA;
+            sT[pp][w][32 + lane] = tB;
+            sEx[pp][w][lane] = exA;
+            sEx[pp][w][32 + lane] = exB;
             if (lane == 0) {
                 sC[cb][w][0] = (uint8_t)codeH;
                 sV[cb][w][0] = pbase.vert - ownH;
             }
             }
+            if (lane == 0) {  // only rows y0 .. y0+7 of planes z0 .. z1-1 emit
+                sTot[pp][w] = (w >= 1 && crow && cz >= z0) ? rowtot : 0;
+                sPT[pp][w] = pbase.tri;
+            }
         }
         __syncthreads();
-        if (cz < z0 || w == 0 || w >= EW - 1 || !crow) continue;
-        {
-            // ---- emission: the row's active cells expand into items (3 per
-            //      triangle, then one per owned vertex), 32 items per step;
-            //      a lane finds its cell by a shuffle binary search over the
-            //      64 exclusive item offsets
-            sT[w][1 + lane] = tA;
-            sT[w][33 + lane] = tB;
-            const int total = __shfl_sync(0xFFFFFFFFu, exB + 3 * ntB + ownB, 31);
-            __syncwarp();
-            for (int i0 = 0; i0 < total; i0 += 32) {
-                const int i = i0 + lane;
-                int col = 0;
+        if (!codes || cz < z0) continue;
+        // ---- emission, balanced over ALL warps of the CTA (a dense surface
+        //      makes rows very unequal; a per-row warp left the others at the
+        //      next barrier): the plane's items (3 per triangle, then one per
+        //      owned vertex, row after row) are dealt out 32 per warp step; an
+        //      item finds its row in the 8 row totals and its cell by a binary
+        //      search over the row's 64 offsets
+        int rowpre[EW - 1];
+        int total = 0;
 #pragma unroll
-                for (int step = 32; step; step >>= 1) {
-                    const int cand = col + step;
-                    const int va = __shfl_sync(0xFFFFFFFFu, exA, cand & 31);
-                    const int vb2 = __shfl_sync(0xFFFFFFFFu, exB, cand & 31);
-                    if ((cand < 32 ? va : vb2) <= i) col = cand;
-                }
-                const int qa = __shfl_sync(0xFFFFFFFFu, exA, col & 31);
-                const int qb = __shfl_sync(0xFFFFFFFFu, exB, col & 31);
-                if (i >= total) continue;
-                const int sl = i - (col < 32 ? qa : qb);
-                const int c = col + 1;  // cell column in the 65-wide ring
-                const int cx = x0 + col;
-                const int code = sC[cb][w][c];
-                const int nt = s_ntri[code];
-                const int f = bflags(cx, cy, cz);
-                if (sl < 3 * nt) {
-                    // triangle corner: vertex id of its edge, held by the owner cell
-                    const int info = s_cinfo[s_tri[code][sl]][f];
-                    const int d0 = -(info & 1), d1 = -((info >> 1) & 1), d2 = -((info >> 2) & 1);
-                    const int e2 = info >> 3;
-                    const int ob = d2 ? (cb == 0 ? 2 : cb - 1) : cb;
-                    const int ocode = sC[ob][w + d1][c + d0];
-                    const int of = bflags(cx + d0, cy + d1, cz + d2);
-                    const int64_t vid = sV[ob][w + d1][c + d0] + __ldg(&T->rank[ocode][of][e2]);
-                    tris[3 * (g.tri_base + pbase.tri + sT[w][c]) + sl] = (int32_t)(g.vert_base + vid);
-                } else {
-                    // owned vertex of rank r: interpolate along its edge
-                    const int r = sl - 3 * nt;
-                    const int vi = s_vinfo[__ldg(&T->inv[code][f][r])];
-                    const int a = vi & 3, lx = (vi >> 2) & 1, ly = (vi >> 3) & 1, lz = (vi >> 4) & 1;
-                    const double *sp = gp + (int64_t)(cz + lz) * nxy + (int64_t)(cy + ly) * g.nx + (cx + lx);
-                    const double s0 = __ldg(sp);
-                    const double s1 = __ldg(sp + (a == 0 ? 1 : (a == 1 ? (int64_t)g.nx : nxy)));
-                    const double den = __dadd_rn(s1, -s0);
-                    const double t = den == 0.0 ? 0.0 : __ddiv_rn(__dadd_rn(k, -s0), den);
-                    double lat[3] = {(double)(cx + lx), (double)(cy + ly), (double)(cz + lz)};
-                    lat[a] = __dadd_rn(lat[a], t);
-                    double *o = verts + 3 * (g.vert_base + sV[cb][w][c] + r);
-                    o[0] = world(g.origin[0], lat[0], g.spacing[0]);
-                    o[1] = world(g.origin[1], lat[1], g.spacing[1]);
-                    o[2] = world(g.origin[2], lat[2], g.spacing[2]);
-                }
+        for (int r = 1; r < EW - 1; ++r) {
+            rowpre[r] = total;
+            total += sTot[pp][r];
+        }
+        for (int i = w * 32 + lane; i < total; i += EW * 32) {
+            int rw = 1;
+#pragma unroll
+            for (int r = 2; r < EW - 1; ++r)
+                if (rowpre[r] <= i) rw = r;
+            const int li = i - rowpre[rw];
+            const int32_t *exr = sEx[pp][rw];
+            int col = 0;
+#pragma unroll
+            for (int step = 32; step; step >>= 1)
+                if (col + step < 64 && exr[col + step] <= li) col += step;
+            const int sl = li - exr[col];
+            const int c = col + 1;  // cell column in the 65-wide ring
+            const int cx = x0 + col, ry = y0 - 1 + rw;
+            const int code = sC[cb][rw][c];
+            const int nt = s_ntri[code];
+            const int f = bflags(cx, ry, cz);
+            if (sl < 3 * nt) {
+                // triangle corner: vertex id of its edge, held by the owner cell
+                const int info = s_cinfo[s_tri[code][sl]][f];
+                const int d0 = -(info & 1), d1 = -((info >> 1) & 1), d2 = -((info >> 2) & 1);
+                const int e2 = info >> 3;
+                const int ob = d2 ? (cb == 0 ? 2 : cb - 1) : cb;
+                const int ocode = sC[ob][rw + d1][c + d0];
+                const int of = bflags(cx + d0, ry + d1, cz + d2);
+                const int64_t vid = sV[ob][rw + d1][c + d0] + __ldg(&T->rank[ocode][of][e2]);
+                tris[3 * (g.tri_base + sPT[pp][rw] + sT[pp][rw][col]) + sl] = (int32_t)(g.vert_base + vid);
+            } else {
+                // owned vertex of rank r: interpolate along its edge
+                const int r = sl - 3 * nt;
+                const int vi = s_vinfo[__ldg(&T->inv[code][f][r])];
+                const int a = vi & 3, lx = (vi >> 2) & 1, ly = (vi >> 3) & 1, lz = (vi >> 4) & 1;
+                const double *sp = gp + (int64_t)(cz + lz) * nxy + (int64_t)(ry + ly) * g.nx + (cx + lx);
+                const double s0 = __ldg(sp);
+                const double s1 = __ldg(sp + (a == 0 ? 1 : (a == 1 ? (int64_t)g.nx : nxy)));
+                const double den = __dadd_rn(s1, -s0);
+                const double t = den == 0.0 ? 0.0 : __ddiv_rn(__dadd_rn(k, -s0), den);
+                double lat[3] = {(double)(cx + lx), (double)(ry + ly), (double)(cz + lz)};
+                lat[a] = __dadd_rn(lat[a], t);
+                double *o = verts + 3 * (g.vert_base + sV[cb][rw][c] + r);
+                o[0] = world(g.origin[0], lat[0], g.spacing[0]);
+                o[1] = world(g.origin[1], lat[1], g.spacing[1]);
+                o[2] = world(g.origin[2], lat[2], g.spacing[2]);
             }
         }
     }
