@@ -336,7 +336,9 @@ def decode(blob: torch.Tensor, sel, ws: Workspaces | None = None, out: torch.Ten
                                            _abi.aptr(status), float(iso), ptr(mask), stream_ptr())
         if rc not in (_abi.CHR_OK, _abi.CHR_E_CORRUPT, _abi.CHR_E_UNSUPPORTED_CODEC):
             check(rc, "chr_decode_regions")
-    return out, [int(v) for v in sel["out_offset"]] if n else [], [int(v) for v in status[:n]]
+    # the windows only (the workspace may be far larger: a caller copying the
+    # result to the host must not drag the whole buffer along)
+    return out[:total], [int(v) for v in sel["out_offset"]] if n else [], [int(v) for v in status[:n]]
 
 
 def mc_table(grid_offset, dims, origin, spacing) -> np.ndarray:

@@ -5,6 +5,7 @@ do the reference's f64 operations without FMA), which is stricter than the
 north_star tolerances (1 ulp recon, 1e-5 * spacing vertices)."""
 
 import hashlib
+import struct
 
 import numpy as np
 import pytest
@@ -619,3 +620,18 @@ def test_concurrent_threads_on_separate_streams():
         for x in th:
             x.join()
         assert got == want
+
+
+def test_decode_returns_only_the_windows():
+    """decode() hands back a view of exactly the decoded samples, never the
+    (possibly much larger) workspace buffer: a small decompress after a big
+    request must not copy the big buffer to the host."""
+    ws = device.Workspaces()
+    big = torch.zeros(1 << 24, dtype=torch.float64, device="cuda")
+    ws._bufs["decode_out"] = big
+    g = np.random.default_rng(3).normal(size=(6, 5, 4))
+    b = G.compress(g, 0.01).to_bytes()
+    blob = torch.from_numpy(np.frombuffer(b + bytes(16), dtype=np.uint8).copy()).cuda()
+    cid, ex, ey, ez, e, _, plen, crc = struct.unpack_from("<B3IdBQI", b, 0)
+    wins, offs, st = device.decode(blob, [(34, plen, cid, (ex, ey, ez), e, crc)], ws=ws)
+    assert not any(st) and wins.numel() == 6 * 5 * 4 and wins.data_ptr() == big.data_ptr()
