@@ -443,9 +443,10 @@ def main():
 def slab_main(args, dist, rank, world, local, n, workers):
     """N>1, one volume of n x n x (n * world) samples in z-slabs (weak
     scaling): distributed compress (block-stats / stream-summary
-    / CRC-share all-gathers), the slices assembled into the file (all-reduce
-    of disjoint bytes), request + marching cubes split by region with the
-    per-region count all-gather.  Times are the max over ranks."""
+    / CRC-share all-gathers), every rank keeping its slice of the file;
+    request + marching cubes split by region, the owned payloads gathered by
+    one all-to-all, with the per-region count all-gather.  Times are the max
+    over ranks."""
     from paper_2408_05462_b200 import _abi, multi, synth
     from paper_2408_05462_b200 import device as D
 
@@ -465,13 +466,14 @@ def slab_main(args, dist, rank, world, local, n, workers):
         res = multi.build_archive_slab(vol, dims, slab, cands, bs, loose_fraction=r, ws=ws)
         if ev:
             ev[1].record()
-        f = multi.assemble(res)
+        # each rank keeps its slice of the archive (it writes those bytes to the
+        # file); the owned payloads of the request come from one all-to-all
         if ev:
             ev[2].record()
-        m = multi.request_extract_slab(f, res.regions, 0, k, ws=ws)
+        m = multi.request_extract_slab(res, res.regions, 0, k, ws=ws, dims=dims, bs=bs)
         if ev:
             ev[3].record()
-        return res, f, m
+        return res, None, m
 
     for _ in range(args.warmup):
         res, f, m = step()
@@ -519,7 +521,13 @@ def slab_main(args, dist, rank, world, local, n, workers):
         vol = saved
         hv = m.verts.cpu()
         ht = m.tris.cpu()
-        hf = f.cpu() if rank == 0 else None
+        # this rank's share of the file: the payloads it wrote (+ header/table on rank 0)
+        contrib = multi.contributors(res.regions, dims, bs, world)[:, rank]
+        rs = res.regions[contrib]
+        parts = [res.blob[int(o): int(o) + int(b)] for o, b in zip(rs["block_offset"], rs["block_nbytes"])]
+        if rank == 0:
+            parts.append(res.blob[: D.header_table_nbytes(len(cands), len(res.regions))])
+        hf = torch.cat(parts).cpu() if parts else None
         eb.record()
         torch.cuda.synchronize()
         if i >= args.warmup:
@@ -538,12 +546,12 @@ def slab_main(args, dist, rank, world, local, n, workers):
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded torch GRF; no public dataset)",
         "config": {"workload": f"{args.config} recipe on {nx}x{ny}x{nz} f32 ({n}^3 per GPU) in z-slabs; step = "
-                               "slab compress -> file assembly -> request(k) + marching cubes split by region",
+                               "slab compress -> request(k) + marching cubes split by region (payloads by all-to-all)",
                    "dims": list(dims), "block_size": bs, "k": k, "regions": int(len(res.regions)),
                    "regions_selected": int(len(sel)), "archive_bytes": int(res.nbytes),
                    "triangles": m.ntri_total, "vertices": m.nvert_total, "parallelism": f"zslab{world}",
                    "l2": "no flush: per-rank input and outputs exceed the 126 MB L2"},
-        "stages": {"compress_ms": t_c, "assemble_ms": t_a, "request_mc_ms": t_rm,
+        "stages": {"compress_ms": t_c, "request_mc_ms": t_rm,
                    "compress_gbs": 4 * Ntot / (t_c * 1e-3) / 1e9, "cells": ncell},
         "kernels": kern_tab,
         "roofline": {"bound": "hbm", "kernel": dom[0] if dom else None, "achieved": None, "peak": peak,

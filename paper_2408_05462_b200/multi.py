@@ -198,6 +198,58 @@ def partition_regions(sizes, world: int) -> list[int]:
     return owner
 
 
+def contributors(regions: np.ndarray, dims, bs: int, world: int) -> np.ndarray:
+    """[nreg, world] bool: rank p wrote bytes of region r's payload (its
+    encode planes [zs, ze) meet the region window's planes)."""
+    nz = dims[2]
+    oz = regions["origin"][:, 2].astype(np.int64)
+    ez = regions["extent"][:, 2].astype(np.int64)
+    out = np.zeros((len(regions), world), dtype=bool)
+    for p in range(world):
+        sl = slab_of(nz, bs, world, p)
+        if sl.zs < sl.ze:
+            out[:, p] = (sl.zs < oz + ez) & (sl.ze > oz)
+    return out
+
+
+def gather_payloads(res: D.Compressed, regions: np.ndarray, sel_idx, owner, dims, bs: int):
+    """The payloads of this rank's regions, assembled from every rank's
+    slice with one all-to-all: rank p sends to rank q the
+    payload ranges of q's regions out of its own slice (zero where another
+    rank wrote), q adds the world copies (disjoint bytes, and disjoint bits
+    in shared escape-bitmap bytes, so the sum is the file's bytes).  No rank
+    ever holds the whole file.  Returns (uint8 device buffer with 16 bytes of
+    slack, byte offset of each owned region's payload in it, owned indices)."""
+    rank, world = dist.get_rank(), dist.get_world_size()
+    sel_idx = np.asarray(sel_idx, dtype=np.int64)
+    owner = np.asarray(owner, dtype=np.int64)
+    poff = regions["block_offset"].astype(np.int64) + D.BLOCK_HEADER
+    plen = regions["block_nbytes"].astype(np.int64) - D.BLOCK_HEADER
+    blob = res.blob
+    nccl = dist.get_backend() == "nccl"
+    send, in_split = [], []
+    for q in range(world):
+        mine = sel_idx[owner == q]
+        parts = [blob[poff[r]: poff[r] + plen[r]] for r in mine]
+        send.extend(parts)
+        in_split.append(int(plen[mine].sum()) if len(mine) else 0)
+    own = sel_idx[owner == rank]
+    L = int(plen[own].sum()) if len(own) else 0
+    inp = torch.cat(send) if send else torch.zeros(0, dtype=torch.uint8, device=blob.device)
+    out = torch.empty(world * L, dtype=torch.uint8, device=blob.device)
+    if nccl:
+        dist.all_to_all_single(out, inp, [L] * world, in_split)
+    else:  # gloo: host tensors
+        o = out.cpu()
+        dist.all_to_all_single(o, inp.cpu(), [L] * world, in_split)
+        out = o.to(blob.device)
+    buf = torch.zeros(L + 16, dtype=torch.uint8, device=blob.device)
+    if L:
+        buf[:L] = out.view(world, L).sum(dim=0, dtype=torch.int32).to(torch.uint8)
+    offs = np.concatenate([[0], np.cumsum(plen[own])[:-1]]).astype(np.int64) if len(own) else np.zeros(0, np.int64)
+    return buf, offs, own
+
+
 @dataclass
 class SlabMesh:
     """This rank's share of the merged mesh: triangles already carry global
@@ -213,12 +265,15 @@ class SlabMesh:
     nvert_total: int
 
 
-def request_extract_slab(file_dev: torch.Tensor, regions: np.ndarray, k_index: int, k: float, spacing=(1.0, 1.0, 1.0),
-                         ws: D.Workspaces | None = None) -> SlabMesh:
+def request_extract_slab(src, regions: np.ndarray, k_index: int, k: float, spacing=(1.0, 1.0, 1.0),
+                         ws: D.Workspaces | None = None, dims=None, bs: int | None = None) -> SlabMesh:
     """request(k) + marching_cubes over the ranks: the selected regions are
     split by sample count, each rank decodes and meshes its own, and an
     all-gather of per-region (triangles, vertices) places every region's rows
-    in the merged mesh (collective (3) of SURVEY §8(e))."""
+    in the merged mesh (collective (3) of SURVEY §8(e)).  ``src``: this
+    rank's slab archive (``build_archive_slab``; needs ``dims``, ``bs``) --
+    the owned payloads then come from one all-to-all (gather_payloads) -- or
+    an assembled file on the device."""
     ws = ws or D.Workspaces()
     rank, world = dist.get_rank(), dist.get_world_size()
     sel_idx = np.nonzero((regions["mask"] >> np.uint64(k_index)) & np.uint64(1))[0]
@@ -226,14 +281,22 @@ def request_extract_slab(file_dev: torch.Tensor, regions: np.ndarray, k_index: i
     ext = sel["extent"].astype(np.int64)
     owner = partition_regions(np.prod(ext, axis=1), world)
     mine = [i for i in range(len(sel)) if owner[i] == rank]
+    if isinstance(src, D.Compressed):
+        if dims is None or bs is None:
+            raise ParameterError("request_extract_slab on a slab archive needs dims and bs")
+        buf, local_off, _ = gather_payloads(src, regions, sel_idx, owner, dims, bs)
+    else:
+        buf, local_off = src, None
+    dev = buf.device
     cnt = torch.zeros((len(sel), 2), dtype=torch.int64)
-    verts = torch.empty((0, 3), dtype=torch.float64, device=file_dev.device)
-    tris = torch.empty((0, 3), dtype=torch.int32, device=file_dev.device)
+    verts = torch.empty((0, 3), dtype=torch.float64, device=dev)
+    tris = torch.empty((0, 3), dtype=torch.int32, device=dev)
     if mine:
         s = sel[mine]
-        dec = D.dec_table(s["block_offset"] + D.BLOCK_HEADER, s["block_nbytes"] - D.BLOCK_HEADER, s["codec_id"],
+        payload_off = local_off if local_off is not None else s["block_offset"] + D.BLOCK_HEADER
+        dec = D.dec_table(payload_off, s["block_nbytes"] - D.BLOCK_HEADER, s["codec_id"],
                           s["extent"], s["error_bound"], s["payload_crc"])
-        wins, _, status = D.decode(file_dev, dec, ws=ws)
+        wins, _, status = D.decode(buf, dec, ws=ws)
         if any(status):
             raise ParameterError(f"decode failed: {status}")
         mct = D.mc_table(dec["out_offset"], s["extent"], s["origin"] * np.asarray(spacing), spacing)

@@ -97,6 +97,12 @@ def _mesh_worker(rank, world, port, out_path):
     res = multi.build_archive_slab(local, dims, slab, [k], bs, loose_fraction=1e-3)
     full = multi.assemble(res)
     m = multi.request_extract_slab(full, res.regions, 0, k)
+    # the same request from the slices alone (owned payloads by one all-to-all, no file assembly)
+    m2 = multi.request_extract_slab(res, res.regions, 0, k, dims=dims, bs=bs)
+    same_local = (m2.regions == m.regions and m2.tri_base == m.tri_base and m2.vert_base == m.vert_base
+                  and torch.equal(m2.tris, m.tris) and torch.equal(m2.verts, m.verts))
+    flags = [None] * world
+    dist.all_gather_object(flags, bool(same_local))
     # gather every rank's rows into the merged mesh on rank 0
     parts = [None] * world
     dist.all_gather_object(parts, (m.tri_base, m.vert_base, m.regions, m.tris.cpu().numpy(), m.verts.cpu().numpy()))
@@ -124,7 +130,7 @@ def _mesh_worker(rank, world, port, out_path):
         wins, _, _ = D.decode(ref.blob, dec)
         mct = D.mc_table(dec["out_offset"], sel["extent"], sel["origin"] * 1.0, (1.0, 1.0, 1.0))
         rv, rt, _, _ = D.marching(wins, mct, k)
-        ok = np.array_equal(rt.cpu().numpy(), T) and np.array_equal(rv.cpu().numpy(), V)
+        ok = np.array_equal(rt.cpu().numpy(), T) and np.array_equal(rv.cpu().numpy(), V) and all(flags)
         with open(out_path, "w") as f:
             f.write(f"{int(ok)} {len(T)} {len(V)} {len(sel)}\n")
     dist.barrier()
