@@ -1060,7 +1060,7 @@ __device__ __forceinline__ int64_t band_scatter_unit64(const Win24 &W, int64_t a
 }
 
 // 32-bit fast path of band_scatter_unit64: tokens <= 4 bytes (H = payload of
-// bytes e-3..e in 28 bits), positions in int32 (runs clamped to 2^31 - 1:
+// bytes e-3..e in 28 bits), positions in int32 (clamped to 2^30 past L:
 // every position that matters is < L <= BCAP and a segment starts at
 // -skip >= -2^30).  Returns the position after the unit's tokens.
 template <bool PAD>
@@ -1084,8 +1084,9 @@ __device__ __forceinline__ int band_scatter_unit32(const Win24 &W, int at, int L
             const int idx = PAD ? at + (int)(((uint64_t)(unsigned)at * M) >> 32) : at;
             q[idx] = (int64_t)(int32_t)((zz >> 1) ^ (0u - (zz & 1u)));
         }
-        const int64_t adv = lit ? 1 : (run ? (int64_t)v : 0);
-        at = (int)min((int64_t)at + adv, (int64_t)0x7FFFFFFF);
+        // positions past L only need to stay past L: clamping at 2^30 keeps
+        // at + v (< 2^28 here) inside int32
+        at = min(at + (lit ? 1 : (run ? (int)v : 0)), 1 << 30);
     }
     return at;
 }
