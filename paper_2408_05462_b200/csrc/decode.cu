@@ -1359,8 +1359,9 @@ __global__ void __launch_bounds__(256) k_band(const DecReg *__restrict__ regs, c
             }
             const int64_t wb = bit0 + t0;
             const int sh = (int)(wb & 31);
-            uint32_t *mw = mp + (wb >> 5);
-            for (int j = 0; j < nzv; ++j) {
+            const int64_t pw = R.pw;
+            uint32_t *w = mp + (wb >> 5) + (int64_t)z0 * pw;
+            for (int j = 0; j < nzv; ++j, w += pw) {
                 double v = 0.0;
                 if (act) {
                     v = (double)(Q[j * PL + qi] + (b > 0 ? dF[j * ex + xx] : 0) + fz) * twoe;
@@ -1368,7 +1369,6 @@ __global__ void __launch_bounds__(256) k_band(const DecReg *__restrict__ regs, c
                 }
                 const uint32_t bal = __ballot_sync(0xFFFFFFFFu, act && v >= iso);
                 if (lane == 0) {
-                    uint32_t *w = mw + (int64_t)(z0 + j) * R.pw;
                     if (nb == 1) {  // whole planes: this warp owns the word
                         *w = bal;
                     } else if (bal) {  // band edges share words with the band above / below
