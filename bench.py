@@ -106,14 +106,18 @@ def make_input(cfg, n, rank, device):
     return vals, dims, bs, cands, r
 
 
-def run_step(vol, dims, bs, cands, r, ws, spacing=(1.0, 1.0, 1.0), stage_events=None):
-    """compress -> request -> extract, all device resident; returns sizes."""
+def run_step(vol, dims, bs, cands, r, ws, spacing=(1.0, 1.0, 1.0), stage_events=None, after_compress=None):
+    """compress -> request -> extract, all device resident; returns sizes.
+    ``after_compress(res)`` runs as soon as the archive exists (the e2e loop
+    starts its device->host copy there, overlapping request + extract)."""
     from paper_2408_05462_b200 import device as D
 
     ev = stage_events
     if ev:
         ev[0].record()
     res = D.build_archive(vol, dims, cands, bs, loose_fraction=r, ws=ws)
+    if after_compress is not None:
+        after_compress(res)
     if ev:
         ev[1].record()
     regs = res.regions
@@ -350,17 +354,25 @@ def main():
                         s_in.wait_event(ev_used[nb])
                     chunked(dvols[nb], host_in)
                     ev_in[nb].record()
+            ha, hv, ht = hout[bi]
+
+            def archive_out(res, bi=bi, ha=ha):
+                # the archive leaves while request + extract run
+                ev_arch = torch.cuda.Event()
+                ev_arch.record(s_cmp)
+                with torch.cuda.stream(s_out):
+                    s_out.wait_event(ev_arch)
+                    chunked(ha[: res.nbytes], res.blob[: res.nbytes])
+
             with torch.cuda.stream(s_cmp):
                 s_cmp.wait_event(ev_in[bi])
                 if i >= 2:
                     s_cmp.wait_event(ev_out[bi])  # step i-2's outputs have left workspace bi
-                inf = run_step(dvols[bi], dims, bs, cands, r, wss[bi])
+                inf = run_step(dvols[bi], dims, bs, cands, r, wss[bi], after_compress=archive_out)
                 ev_used[bi].record()
             with torch.cuda.stream(s_out):
                 s_out.wait_event(ev_used[bi])
                 nbytes = inf["archive"]
-                ha, hv, ht = hout[bi]
-                chunked(ha[:nbytes], inf["res"].blob[:nbytes])
                 chunked(hv[: inf["nvert"] * 3], inf["verts"].reshape(-1))
                 chunked(ht[: inf["ntri"] * 3], inf["tris"].reshape(-1))
                 ev_out[bi].record()
