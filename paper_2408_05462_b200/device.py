@@ -61,7 +61,7 @@ def stats(vol: torch.Tensor, dims, bs: int, cands) -> tuple[torch.Tensor, torch.
     cands = _cands_arr(cands)
     nb = num_blocks(dims, bs)
     out = torch.empty((nb, 3), dtype=torch.float64, device=vol.device)
-    bad = torch.empty(1, dtype=torch.int64, device=vol.device)
+    bad = torch.empty(1, dtype=torch.int64, device=vol.device)  # (both small: the caching allocator serves them)
     check(lib().chr_stats(ptr(vol), _dtype_code(vol), *dims, bs, _np_ptr(cands), cands.size,
                           ptr(out), ptr(bad), stream_ptr()), "chr_stats")
     return out, bad
@@ -73,7 +73,7 @@ def plan(block_stats: np.ndarray, dims, bs, cands, vmin, vmax, loose_fraction=LO
     cands = _cands_arr(cands)
     bsn = np.ascontiguousarray(block_stats, dtype=np.float64)
     nb = bsn.shape[0]
-    regs = np.zeros(nb, dtype=_abi.REGION_DT)
+    regs = np.empty(nb, dtype=_abi.REGION_DT)  # chr_plan zero-fills every record it writes
     nreg = ctypes.c_int64(0)
     check(lib().chr_plan(_np_ptr(bsn), *dims, bs, _np_ptr(cands), cands.size, float(vmin), float(vmax),
                          float(loose_fraction), float(safety_factor), _abi.aptr(regs), ctypes.byref(nreg)),
