@@ -635,3 +635,39 @@ def test_decode_returns_only_the_windows():
     cid, ex, ey, ez, e, _, plen, crc = struct.unpack_from("<B3IdBQI", b, 0)
     wins, offs, st = device.decode(blob, [(34, plen, cid, (ex, ey, ez), e, crc)], ws=ws)
     assert not any(st) and wins.numel() == 6 * 5 * 4 and wins.data_ptr() == big.data_ptr()
+
+
+@pytest.mark.parametrize("case", ["dense64", "close_pairs", "wide_range", "on_samples"])
+def test_stats_rows_many_candidates_exact(case):
+    """The row-streaming stats kernel (f32, nx % 4 == 0) finds each sample's
+    bracketing candidates from a bucket table: exact against the oracle for
+    candidate sets that defeat the buckets (pairs closer than a bucket, two
+    doubles rounding to one float, extreme ranges, candidates on samples)."""
+    rng = np.random.default_rng(11)
+    dims, bs = (64, 40, 36), 8
+    vals = (rng.normal(size=dims[::-1]) * 3.0).astype(np.float32).reshape(-1)
+    if case == "dense64":
+        cands = np.sort(rng.normal(size=64) * 3.0)
+    elif case == "close_pairs":
+        base = np.sort(rng.normal(size=20) * 3.0)
+        f = np.float32(1.2345)
+        cands = np.concatenate([base, [float(f), float(f) + 1e-12, float(f) + 2e-12, 0.5, 0.5 + 1e-9]])
+    elif case == "wide_range":
+        cands = np.array([-1e30, -1e3, -1.0, -1e-7, 1e-30, 0.3, 2.0, 1e5, 1e30])
+    else:
+        cands = np.sort(vals[rng.choice(vals.size, size=24, replace=False)].astype(np.float64))
+    cands = np.unique(cands)
+    st, bad = device.stats(torch.from_numpy(vals).cuda(), dims, bs, list(cands))
+    st = st.cpu().numpy()
+    host = vals.astype(np.float64)
+    nbx, nby, nbz = O.block_grid_shape(dims, bs)
+    L = O.lib()
+    import ctypes
+
+    for b in range(nbx * nby * nbz):
+        bz, rem = divmod(b, nbx * nby)
+        by, bx = divmod(rem, nbx)
+        w = [O._axis_window(c, bs, n) for c, n in zip((bx, by, bz), dims)]
+        d = min(L.or_window_min_abs_distance(ctypes.c_void_p(host.ctypes.data), dims[0], dims[1], w[0][0], w[1][0],
+                                             w[2][0], w[0][1], w[1][1], w[2][1], float(k)) for k in cands)
+        assert st[b, 2] == d, (case, b)
