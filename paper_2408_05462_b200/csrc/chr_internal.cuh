@@ -1,6 +1,9 @@
 // chr_internal.cuh -- declarations shared between libchr translation units.
 #pragma once
 
+#include <initializer_list>
+#include <utility>
+
 #include "chr_common.cuh"
 
 namespace chr {
@@ -54,6 +57,8 @@ cudaError_t h2d(void *dst, const void *src, size_t n, cudaStream_t st);
 cudaError_t d2h(void *dst, const void *src, size_t n, cudaStream_t st);
 cudaError_t stream_sync(cudaStream_t st);
 cudaError_t fill_async(void *dst, int v, size_t n, cudaStream_t st);   // cudaMemsetAsync as a kernel
+constexpr int kFillMax = 8;
+cudaError_t zero_async(std::initializer_list<std::pair<void *, size_t>> ranges, cudaStream_t st);  // one launch
 cudaError_t copy_async(void *dst, const void *src, size_t n, cudaStream_t st);  // kernel copy, UVA pointers
 class XferScope {
   public:

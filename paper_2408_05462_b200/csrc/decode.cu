@@ -1680,13 +1680,14 @@ static int decode_impl(const uint8_t *d_blob, const chr_dec_region_t *h, int64_t
     const int64_t total_sc = crc_plan_segments(segs.data(), n);
     CHR_CUDA_TRY(h2d(pl.d_regs, pl.regs.data(), sizeof(DecReg) * n, st));
     CHR_CUDA_TRY(h2d(pl.segs, segs.data(), sizeof(CrcSeg) * n, st));
-    CHR_CUDA_TRY(fill_async(pl.seg_raw, 0, sizeof(uint32_t) * n, st));
-    CHR_CUDA_TRY(fill_async(pl.flags, 0, sizeof(int64_t) * (pl.nitems + 1), st));
-    CHR_CUDA_TRY(fill_async(pl.ticket, 0, sizeof(unsigned long long), st));
-    CHR_CUDA_TRY(fill_async(pl.ticket3, 0, sizeof(unsigned long long), st));
-    CHR_CUDA_TRY(fill_async(pl.any_slow, 0, sizeof(int32_t), st));
-    if (d_mask) CHR_CUDA_TRY(fill_async(d_mask, 0, sizeof(uint32_t) * (pl.nmask + 8), st));
-    CHR_CUDA_TRY(fill_async(pl.tflag, 0, sizeof(int32_t) * (pl.ntiles + 1), st));
+    CHR_CUDA_TRY(zero_async({{pl.seg_raw, sizeof(uint32_t) * n},
+                             {pl.flags, sizeof(int64_t) * (pl.nitems + 1)},
+                             {pl.ticket, sizeof(unsigned long long)},
+                             {pl.ticket3, sizeof(unsigned long long)},
+                             {pl.any_slow, sizeof(int32_t)},
+                             {d_mask, d_mask ? sizeof(uint32_t) * (pl.nmask + 8) : 0},
+                             {pl.tflag, sizeof(int32_t) * (pl.ntiles + 1)}},
+                            st));
     int rc = crc_launch(d_blob, pl.segs, n, total_sc, pl.seg_raw, st);
     if (rc) return rc;
     {

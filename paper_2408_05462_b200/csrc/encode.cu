@@ -1148,9 +1148,10 @@ extern "C" int chr_compress2(const void *d_vol, int dtype, int src_dtype, int64_
 
     CHR_CUDA_TRY(h2d(pl.params, &hp, sizeof(hp), st));
     CHR_CUDA_TRY(h2d(pl.d_regs, pl.regs.data(), sizeof(RegDev) * nreg, st));
-    CHR_CUDA_TRY(fill_async(pl.scal, 0, sizeof(EncScalars), st));
-    CHR_CUDA_TRY(fill_async(pl.seg_raw, 0, sizeof(uint32_t) * (nreg + 1), st));
-    CHR_CUDA_TRY(fill_async(pl.escbits, 0, sizeof(uint32_t) * (pl.etotal + 2), st));
+    CHR_CUDA_TRY(zero_async({{pl.scal, sizeof(EncScalars)},
+                             {pl.seg_raw, sizeof(uint32_t) * (nreg + 1)},
+                             {pl.escbits, sizeof(uint32_t) * (pl.etotal + 2)}},
+                            st));
 
     const unsigned items = (unsigned)pl.nitems, chunks = (unsigned)pl.nchunks;
     {

@@ -137,6 +137,47 @@ cudaError_t fill_async(void *dst, int v, size_t n, cudaStream_t st) {
     return cudaGetLastError();
 }
 
+namespace {
+struct FillSet {
+    uint8_t *ptr[kFillMax];
+    size_t n[kFillMax];
+    int count;
+};
+
+// one launch zero-fills up to kFillMax ranges: blockIdx.y picks the range
+__global__ void k_fill_multi(FillSet set) {
+    uint8_t *dst = set.ptr[blockIdx.y];
+    const size_t n = set.n[blockIdx.y];
+    const size_t i0 = (size_t)blockIdx.x * blockDim.x + threadIdx.x, stride = (size_t)gridDim.x * blockDim.x;
+    if (((uintptr_t)dst & 15) == 0) {
+        const size_t n16 = n >> 4;
+        for (size_t i = i0; i < n16; i += stride) reinterpret_cast<uint4 *>(dst)[i] = make_uint4(0, 0, 0, 0);
+        for (size_t i = (n16 << 4) + i0; i < n; i += stride) dst[i] = 0;
+    } else {
+        for (size_t i = i0; i < n; i += stride) dst[i] = 0;
+    }
+}
+}  // namespace
+
+cudaError_t zero_async(std::initializer_list<std::pair<void *, size_t>> ranges, cudaStream_t st) {
+    FillSet set;
+    set.count = 0;
+    size_t most = 0;
+    for (const auto &r : ranges) {
+        if (!r.first || r.second == 0) continue;
+        if (set.count == kFillMax) return cudaErrorInvalidValue;
+        set.ptr[set.count] = (uint8_t *)r.first;
+        set.n[set.count] = r.second;
+        most = std::max(most, r.second);
+        ++set.count;
+    }
+    if (set.count == 0) return cudaSuccess;
+    const unsigned bx = (unsigned)std::min<size_t>(1184, (most + 16383) / 16384 + 1);
+    CHR_PROF("k_fill", st);
+    k_fill_multi<<<dim3(bx, set.count), 256, 0, st>>>(set);
+    return cudaGetLastError();
+}
+
 // device-accessible pointers (device or mapped pinned host), any alignment
 cudaError_t copy_async(void *dst, const void *src, size_t n, cudaStream_t st) {
     if (n == 0) return cudaSuccess;
