@@ -58,6 +58,13 @@ cudaError_t d2h(void *dst, const void *src, size_t n, cudaStream_t st);
 cudaError_t stream_sync(cudaStream_t st);
 cudaError_t fill_async(void *dst, int v, size_t n, cudaStream_t st);   // cudaMemsetAsync as a kernel
 constexpr int kFillMax = 8;
+struct Xfer {
+    void *dst;
+    const void *src;
+    size_t n;
+};
+cudaError_t h2d_multi(std::initializer_list<Xfer> xs, cudaStream_t st);  // one pull launch
+cudaError_t d2h_multi(std::initializer_list<Xfer> xs, cudaStream_t st);  // one push launch
 cudaError_t zero_async(std::initializer_list<std::pair<void *, size_t>> ranges, cudaStream_t st);  // one launch
 cudaError_t copy_async(void *dst, const void *src, size_t n, cudaStream_t st);  // kernel copy, UVA pointers
 class XferScope {

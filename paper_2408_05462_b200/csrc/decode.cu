@@ -1678,8 +1678,8 @@ static int decode_impl(const uint8_t *d_blob, const chr_dec_region_t *h, int64_t
         segs[i].end = pl.regs[i].poff + pl.regs[i].plen;
     }
     const int64_t total_sc = crc_plan_segments(segs.data(), n);
-    CHR_CUDA_TRY(h2d(pl.d_regs, pl.regs.data(), sizeof(DecReg) * n, st));
-    CHR_CUDA_TRY(h2d(pl.segs, segs.data(), sizeof(CrcSeg) * n, st));
+    CHR_CUDA_TRY(h2d_multi({{pl.d_regs, pl.regs.data(), sizeof(DecReg) * n}, {pl.segs, segs.data(), sizeof(CrcSeg) * n}},
+                           st));
     CHR_CUDA_TRY(zero_async({{pl.seg_raw, sizeof(uint32_t) * n},
                              {pl.flags, sizeof(int64_t) * (pl.nitems + 1)},
                              {pl.ticket, sizeof(unsigned long long)},

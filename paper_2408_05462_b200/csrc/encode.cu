@@ -1146,8 +1146,7 @@ extern "C" int chr_compress2(const void *d_vol, int dtype, int src_dtype, int64_
     // capacity check against the worst case (verbatim f64 everywhere)
     if (out_cap < chr_compress_capacity(h_regions, nreg, m, src_dtype)) return CHR_E_PARAMETER;
 
-    CHR_CUDA_TRY(h2d(pl.params, &hp, sizeof(hp), st));
-    CHR_CUDA_TRY(h2d(pl.d_regs, pl.regs.data(), sizeof(RegDev) * nreg, st));
+    CHR_CUDA_TRY(h2d_multi({{pl.params, &hp, sizeof(hp)}, {pl.d_regs, pl.regs.data(), sizeof(RegDev) * nreg}}, st));
     CHR_CUDA_TRY(zero_async({{pl.scal, sizeof(EncScalars)},
                              {pl.seg_raw, sizeof(uint32_t) * (nreg + 1)},
                              {pl.escbits, sizeof(uint32_t) * (pl.etotal + 2)}},
@@ -1236,8 +1235,7 @@ extern "C" int chr_compress2(const void *d_vol, int dtype, int src_dtype, int64_
             k_finalize_file<<<1, 1, 0, st>>>(tabs, pl.scal, d_out);
     }
     CHR_CUDA_TRY(cudaGetLastError());
-    CHR_CUDA_TRY(d2h(pl.regs.data(), pl.d_regs, sizeof(RegDev) * nreg, st));
-    CHR_CUDA_TRY(d2h(&hs, pl.scal, sizeof(hs), st));
+    CHR_CUDA_TRY(d2h_multi({{pl.regs.data(), pl.d_regs, sizeof(RegDev) * nreg}, {&hs, pl.scal, sizeof(hs)}}, st));
     CHR_CUDA_TRY(stream_sync(st));
     for (int64_t r = 0; r < nreg; ++r) {
         const RegDev &R = pl.regs[r];
@@ -1605,8 +1603,7 @@ extern "C" int chr_dcompress_finish(const void *d_vol, int dtype, int src_dtype,
     if (!c2.empty()) k_bitmap<<<148, 256, 0, st>>>(pl.d_regs, pl.codec2, pl.scal, pl.escbits, d_out);
     CHR_CUDA_TRY(cudaGetLastError());
     EncScalars hs;
-    CHR_CUDA_TRY(d2h(pl.regs.data(), pl.d_regs, sizeof(RegDev) * nreg, st));
-    CHR_CUDA_TRY(d2h(&hs, pl.scal, sizeof(hs), st));
+    CHR_CUDA_TRY(d2h_multi({{pl.regs.data(), pl.d_regs, sizeof(RegDev) * nreg}, {&hs, pl.scal, sizeof(hs)}}, st));
     CHR_CUDA_TRY(stream_sync(st));
     // this rank's byte ranges inside every payload (+ the header/table on rank 0)
     std::vector<CrcSeg> segs;

@@ -93,6 +93,87 @@ cudaError_t reserve(size_t n, cudaStream_t st, uint8_t **out) {
 }
 }  // namespace
 
+namespace {
+struct CopySet {
+    const uint8_t *src[kFillMax];
+    uint8_t *dst[kFillMax];
+    size_t n[kFillMax];
+};
+
+__global__ void k_xfer_multi(CopySet set) {
+    const uint8_t *src = set.src[blockIdx.y];
+    uint8_t *dst = set.dst[blockIdx.y];
+    const size_t n = set.n[blockIdx.y];
+    const size_t i0 = (size_t)blockIdx.x * blockDim.x + threadIdx.x, stride = (size_t)gridDim.x * blockDim.x;
+    if ((((uintptr_t)src | (uintptr_t)dst) & 15) == 0) {
+        const size_t n16 = n >> 4;
+        for (size_t i = i0; i < n16; i += stride)
+            reinterpret_cast<uint4 *>(dst)[i] = reinterpret_cast<const uint4 *>(src)[i];
+        for (size_t i = (n16 << 4) + i0; i < n; i += stride) dst[i] = src[i];
+    } else {
+        for (size_t i = i0; i < n; i += stride) dst[i] = src[i];
+    }
+}
+
+cudaError_t launch_multi(const CopySet &set, int count, size_t most, cudaStream_t st) {
+    if (count == 0) return cudaSuccess;
+    const unsigned bx = (unsigned)std::min<size_t>(64, (most + 4095) / 4096 + 1);
+    CHR_PROF("k_xfer", st);
+    k_xfer_multi<<<dim3(bx, count), 256, 0, st>>>(set);
+    return cudaGetLastError();
+}
+}  // namespace
+
+// several small host->device copies staged in the ring and pulled by one launch
+cudaError_t h2d_multi(std::initializer_list<Xfer> xs, cudaStream_t st) {
+    CopySet set;
+    int count = 0;
+    size_t most = 0;
+    for (const Xfer &x : xs) {
+        if (x.n == 0) continue;
+        if (x.n > kXferBig || count == kFillMax) {
+            const cudaError_t e = h2d(x.dst, x.src, x.n, st);
+            if (e != cudaSuccess) return e;
+            continue;
+        }
+        uint8_t *p = nullptr;
+        const cudaError_t e = reserve(x.n, st, &p);
+        if (e != cudaSuccess) return e;
+        std::memcpy(p, x.src, x.n);
+        set.src[count] = p;
+        set.dst[count] = (uint8_t *)x.dst;
+        set.n[count] = x.n;
+        most = std::max(most, x.n);
+        ++count;
+    }
+    return launch_multi(set, count, most, st);
+}
+
+// several small device->host copies pushed by one launch, delivered at stream_sync
+cudaError_t d2h_multi(std::initializer_list<Xfer> xs, cudaStream_t st) {
+    CopySet set;
+    int count = 0;
+    size_t most = 0;
+    for (const Xfer &x : xs) {
+        if (x.n == 0) continue;
+        if (x.n > kXferBig || count == kFillMax) {
+            const cudaError_t e = d2h(x.dst, x.src, x.n, st);
+            if (e != cudaSuccess) return e;
+            continue;
+        }
+        uint8_t *p = nullptr;
+        const cudaError_t e = reserve(x.n, st, &p);
+        if (e != cudaSuccess) return e;
+        set.src[count] = (const uint8_t *)x.src;
+        set.dst[count] = p;
+        set.n[count] = x.n;
+        most = std::max(most, x.n);
+        g_ring.pend.push_back({p, x.dst, x.n, st});
+        ++count;
+    }
+    return launch_multi(set, count, most, st);
+}
+
 cudaError_t h2d(void *dst, const void *src, size_t n, cudaStream_t st) {
     if (n == 0) return cudaSuccess;
     if (n > kXferBig) return cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, st);
