@@ -191,20 +191,40 @@ __global__ void __launch_bounds__(256) k_mc_reduce(const McPieceCnt *__restrict_
 }
 
 // per grid: exclusive chunk prefixes + grid totals (thread per grid)
+// warp per grid: exclusive scan of its chunk totals, 32 chunks per step
 __global__ void k_mc_grid_scan(McGrid *__restrict__ G, int64_t ng, McPieceBase *__restrict__ chunk) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
     if (i >= ng) return;
     McGrid &g = G[i];
-    int64_t t = 0, v = 0;
-    for (int64_t c = g.chunk_base; c < g.chunk_base + g.nchunks; ++c) {
-        const McPieceBase x = chunk[c];
-        chunk[c].tri = t;
-        chunk[c].vert = v;
-        t += x.tri;
-        v += x.vert;
+    int64_t t = 0, v = 0;  // running totals before this step
+    for (int64_t c0 = g.chunk_base; c0 < g.chunk_base + g.nchunks; c0 += 32) {
+        const int64_t c = c0 + lane;
+        const bool ok = c < g.chunk_base + g.nchunks;
+        McPieceBase x;
+        x.tri = 0;
+        x.vert = 0;
+        if (ok) x = chunk[c];
+        int64_t it = x.tri, iv = x.vert;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int64_t a = __shfl_up_sync(0xFFFFFFFFu, it, off), b = __shfl_up_sync(0xFFFFFFFFu, iv, off);
+            if (lane >= off) {
+                it += a;
+                iv += b;
+            }
+        }
+        if (ok) {
+            chunk[c].tri = t + it - x.tri;
+            chunk[c].vert = v + iv - x.vert;
+        }
+        t += __shfl_sync(0xFFFFFFFFu, it, 31);
+        v += __shfl_sync(0xFFFFFFFFu, iv, 31);
     }
-    g.ntri = t;
-    g.nvert = v;
+    if (lane == 0) {
+        g.ntri = t;
+        g.nvert = v;
+    }
 }
 
 // one CTA: merged-mesh bases of every grid (exclusive scan over grids)
@@ -952,7 +972,7 @@ static int mc_count_impl(const double *d_grids, const chr_mc_grid_t *h, int64_t 
     }
     {
         CHR_PROF("k_mc_grid_scan", st);
-        k_mc_grid_scan<<<(unsigned)ceil_div(n, 128), 128, 0, st>>>(pl.d_grids, n, pl.chunk);
+        k_mc_grid_scan<<<(unsigned)ceil_div(n, 4), 128, 0, st>>>(pl.d_grids, n, pl.chunk);
     }
     {
         CHR_PROF("k_mc_grids", st);
