@@ -308,7 +308,7 @@ def decode(blob: torch.Tensor, sel, ws: Workspaces | None = None, out: torch.Ten
     ``sel``: a ``_abi.DEC_DT`` table (see :func:`dec_table`) or a list of
     (payload_offset, payload_nbytes, codec_id, (ex,ey,ez), e, crc).
     Returns (f64 device tensor of all windows concatenated, element offsets,
-    per-region status codes).  With ``iso`` the decoder also writes every
+    per-region status codes) -- the last two as numpy arrays.  With ``iso`` the decoder also writes every
     window's inside mask (v >= iso) into ``ws`` ("decode_mask"), which
     :func:`marching` takes as ``masks`` (fused request + extract)."""
     ws = ws or _DEFAULT_WS
@@ -338,7 +338,9 @@ def decode(blob: torch.Tensor, sel, ws: Workspaces | None = None, out: torch.Ten
             check(rc, "chr_decode_regions")
     # the windows only (the workspace may be far larger: a caller copying the
     # result to the host must not drag the whole buffer along)
-    return out[:total], [int(v) for v in sel["out_offset"]] if n else [], [int(v) for v in status[:n]]
+    # offsets and status as numpy arrays (a Python list of ints costs ~0.1 us per region)
+    offs = sel["out_offset"].astype(np.int64) if n else np.zeros(0, np.int64)
+    return out[:total], offs, status[:n]
 
 
 def mc_table(grid_offset, dims, origin, spacing) -> np.ndarray:
