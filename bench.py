@@ -182,10 +182,14 @@ def cpu_baseline(vals_host, dims, bs, cands, r, planes, workers):
     t0 = time.perf_counter()
     arch = O.build_chr(sample, sdims, [k], bs, source_dtype="f32", loose_fraction=r, workers=workers,
                        out_of_range="warn")
+    t1 = time.perf_counter()
     sel = O.request(arch, k, workers=workers)
+    t2 = time.perf_counter()
     O.extract_regions(sel, (1.0, 1.0, 1.0), k)
-    t = time.perf_counter() - t0
+    t3 = time.perf_counter()
+    t = t3 - t0
     return {"value": 4 * nx * ny * pz / t / 1e9, "unit": "GB/s", "cores": workers, "kind": "port",
+            "stages_s": {"build_chr": t1 - t0, "request": t2 - t1, "marching_cubes": t3 - t2},
             "sample": (f"{nx}x{ny}x{pz} z-slab of the same field (first {pz} planes), same bs/r/k; "
                        if pz < nz else "the whole workload (same volume, bs, r, k); ") +
                       f"build_chr + request + per-region MC, {t:.2f} s wall on {workers} threads"}
