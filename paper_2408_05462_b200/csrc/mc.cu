@@ -449,18 +449,30 @@ __global__ void __launch_bounds__(256) k_mc_count3(const McGrid *__restrict__ G,
             }
             const bool two = lp + 1 < lpe;
             int t = 0, v = 0, t2 = 0, v2 = 0;
+            // lane 4q + r reads row mask r (y + (r & 1), z + (r >> 1)) of piece q; shuffles share them
+            uint64_t mr = 0;
+            uint32_t hr = 0;
+            if (lane < (two ? 8 : 4)) {
+                const int q = lane >> 2, rr = lane & 3;
+                const int qy = q ? cy2 : cy, qz = q ? cz2 : cz;
+                mask_bits66(mbase + (int64_t)(qz + (rr >> 1)) * g.pw, (int64_t)(qy + (rr & 1)) * g.nx, mr, hr);
+            }
+            const uint32_t mlo = (uint32_t)mr, mhi = (uint32_t)(mr >> 32);
 #pragma unroll
             for (int q = 0; q < 2; ++q) {
                 const int qy = q ? cy2 : cy, qz = q ? cz2 : cz;
                 if (q && !two) break;
-                const uint32_t *mp0 = mbase + (int64_t)qz * g.pw, *mp1 = mp0 + g.pw;
-                const int64_t b0 = (int64_t)qy * g.nx, b1 = b0 + g.nx;
+                auto row = [&](int r, uint64_t &m, uint32_t &h) {
+                    m = (uint64_t)__shfl_sync(0xFFFFFFFFu, mlo, 4 * q + r) |
+                        ((uint64_t)__shfl_sync(0xFFFFFFFFu, mhi, 4 * q + r) << 32);
+                    h = __shfl_sync(0xFFFFFFFFu, hr, 4 * q + r);
+                };
                 uint64_t m00, m10, m01, m11;
                 uint32_t h00, h10, h01, h11;
-                mask_bits66(mp0, b0, m00, h00);
-                mask_bits66(mp0, b1, m10, h10);
-                mask_bits66(mp1, b0, m01, h01);
-                mask_bits66(mp1, b1, m11, h11);
+                row(0, m00, h00);
+                row(1, m10, h10);
+                row(2, m01, h01);
+                row(3, m11, h11);
                 if (lane_ok) {
                     const int code = code_fast(m00, h00, m10, h10, m01, h01, m11, h11, lane);
                     (q ? t2 : t) = s_ntri[code];
