@@ -283,31 +283,27 @@ __global__ void __launch_bounds__(DTHREADS) k_tok_count(DecReg *__restrict__ reg
 // per region: exclusive prefix of chunk samples, total must equal n
 __global__ void k_tok_scan(DecReg *__restrict__ regs, int64_t nreg, int64_t *__restrict__ chunk_samples,
                            int slow_pass) {
-    // warp per region: 32 chunk counts per step
-    const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
+    // CTA per region: blockDim chunk counts per step (a region can span
+    // thousands of 4 KiB chunks; a warp-wide scan left a long serial chain)
+    const int64_t r = blockIdx.x;
     if (r >= nreg) return;
     DecReg &R = regs[r];
     if (!((R.codec == 1 || R.codec == 2) && R.err == 0)) return;
     if ((R.slow != 0) != (slow_pass != 0)) return;  // pass 0: band regions, pass 1: generic
     int64_t acc = 0;
-    bool over = false;
-    for (int64_t c0 = 0; c0 < R.nchunks; c0 += 32) {
-        const int64_t c = R.chunk_base + c0 + lane;
-        const bool ok = c0 + lane < R.nchunks;
+    int over = 0;
+    for (int64_t c0 = 0; c0 < R.nchunks; c0 += blockDim.x) {
+        const int64_t c = R.chunk_base + c0 + threadIdx.x;
+        const bool ok = c0 + threadIdx.x < R.nchunks;
         const int64_t v = ok ? chunk_samples[c] : 0;
-        int64_t inc = v;
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-            const int64_t o = __shfl_up_sync(0xFFFFFFFFu, inc, off);
-            if (lane >= off) inc += o;
-        }
-        if (ok) chunk_samples[c] = acc + inc - v;
-        if (ok && (acc + inc > R.n || v < 0)) over = true;
-        acc += __shfl_sync(0xFFFFFFFFu, inc, 31);
+        int64_t tot;
+        const int64_t ex = block_excl64(v, &tot);
+        if (ok) chunk_samples[c] = acc + ex;
+        if (ok && (acc + ex + v > R.n || v < 0)) over = 1;
+        acc += tot;
     }
-    over = __any_sync(0xFFFFFFFFu, over);
-    if (lane != 0) return;
+    over = __syncthreads_or(over);
+    if (threadIdx.x != 0) return;
     if (over) R.err |= EF_RANGE;
     else if (acc < R.n) R.err |= EF_TRUNC;
     if (R.tok_start == R.poff + R.plen && R.n > 0) R.err |= EF_TRUNC;
@@ -1709,7 +1705,7 @@ static int decode_impl(const uint8_t *d_blob, const chr_dec_region_t *h, int64_t
     }
     {
         CHR_PROF("k_tok_scan", st);
-        k_tok_scan<<<(unsigned)ceil_div(n, 4), 128, 0, st>>>(pl.d_regs, n, pl.chunk_samples, 0);
+        k_tok_scan<<<(unsigned)n, 512, 0, st>>>(pl.d_regs, n, pl.chunk_samples, 0);
     }
     // ---- band path (canonical streams)
     if (pl.ntiles > 0) {
@@ -1755,7 +1751,7 @@ static int decode_impl(const uint8_t *d_blob, const chr_dec_region_t *h, int64_t
         }
         {
             CHR_PROF("k_tok_scan", st);
-            k_tok_scan<<<(unsigned)ceil_div(n, 4), 128, 0, st>>>(pl.d_regs, n, pl.chunk_samples, 1);
+            k_tok_scan<<<(unsigned)n, 512, 0, st>>>(pl.d_regs, n, pl.chunk_samples, 1);
         }
         {
             CHR_PROF("k_locate", st);
