@@ -107,35 +107,25 @@ def make_input(cfg, n, rank, device):
 
 
 def run_step(vol, dims, bs, cands, r, ws, spacing=(1.0, 1.0, 1.0), stage_events=None, after_compress=None):
-    """compress -> request -> extract, all device resident; returns sizes.
-    ``after_compress(res)`` runs as soon as the archive exists (the e2e loop
-    starts its device->host copy there, overlapping request + extract)."""
+    """compress -> request(k) -> marching cubes, all device resident, in one
+    library call (device.pipeline -> chr_pipeline: the same bytes, windows
+    and mesh as build_archive + decode + marching, without host round trips
+    between the phases); returns sizes.  ``after_compress(archive)`` runs as
+    soon as the archive exists (the e2e loop starts its device->host copy
+    there, overlapping request + extract).  stage_events: 4 CUDA events
+    recorded at the start, after compress, after decode, after the mesh."""
     from paper_2408_05462_b200 import device as D
 
-    ev = stage_events
-    if ev:
-        ev[0].record()
-    res = D.build_archive(vol, dims, cands, bs, loose_fraction=r, ws=ws)
-    if after_compress is not None:
-        after_compress(res)
-    if ev:
-        ev[1].record()
-    regs = res.regions
-    dec, mct, sel_idx, _ = D.request_tables(regs, 0, spacing)  # regions relevant to candidate 0
-    sel = regs[sel_idx]
-    wins, offs, status = D.decode(res.blob, dec, ws=ws, iso=cands[0])  # + inside masks for MC
-    assert not any(status), status
-    if ev:
-        ev[2].record()
-    verts, tris, nt, nv = D.marching(wins, mct, cands[0], ws=ws, reuse_outputs=True,
-                                     masks=ws.get("decode_mask", 4, torch.int32))
-    if ev:
-        ev[3].record()
+    p = D.pipeline(vol, dims, cands, bs, loose_fraction=r, k_index=0, spacing=spacing, ws=ws,
+                   stage_events=stage_events, after_compress=after_compress)
+    regs = p.regions
+    sel = regs[(regs["mask"] & np.uint64(1)) != 0]  # regions relevant to candidate 0
     ext = sel["extent"].astype(np.int64)
-    return dict(res=res, wins=wins, verts=verts, tris=tris, n_sel=int(np.prod(ext, axis=1).sum()),
-                cells=int(np.prod(ext - 1, axis=1).sum()), c_sel=int(sel["block_nbytes"].sum()),
-                archive=res.nbytes, nreg=len(regs), n_all=int(np.prod(regs["extent"].astype(np.int64), axis=1).sum()), nsel=len(sel), ntri=int(tris.shape[0]),
-                nvert=int(verts.shape[0]), payload=int(regs["block_nbytes"].sum()))
+    return dict(archive_view=p.archive, wins=p.windows, verts=p.verts, tris=p.tris,
+                n_sel=int(np.prod(ext, axis=1).sum()), cells=int(np.prod(ext - 1, axis=1).sum()),
+                c_sel=int(sel["block_nbytes"].sum()), archive=int(p.archive.numel()), nreg=len(regs),
+                n_all=int(np.prod(regs["extent"].astype(np.int64), axis=1).sum()), nsel=len(sel),
+                ntri=int(p.tris.shape[0]), nvert=int(p.verts.shape[0]), payload=int(regs["block_nbytes"].sum()))
 
 
 def kernel_bytes(name, info, N):
@@ -360,13 +350,13 @@ def main():
                     ev_in[nb].record()
             ha, hv, ht = hout[bi]
 
-            def archive_out(res, bi=bi, ha=ha):
+            def archive_out(archive, bi=bi, ha=ha):
                 # the archive leaves while request + extract run
                 ev_arch = torch.cuda.Event()
                 ev_arch.record(s_cmp)
                 with torch.cuda.stream(s_out):
                     s_out.wait_event(ev_arch)
-                    chunked(ha[: res.nbytes], res.blob[: res.nbytes])
+                    chunked(ha[: archive.numel()], archive)
 
             with torch.cuda.stream(s_cmp):
                 s_cmp.wait_event(ev_in[bi])

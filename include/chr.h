@@ -370,6 +370,38 @@ int64_t chr_request_tables(const chr_region_t *h_regions, int64_t n, int k_index
                            chr_dec_region_t *h_dec, chr_mc_grid_t *h_mc, int64_t *h_sel,
                            uint64_t *h_total_samples);
 
+/* 17. the whole step in one call (stats -> plan -> compress -> request(k) ->
+ *     decode + inside masks -> marching cubes), results identical to the
+ *     separate entry points; no host round trips in between.  Strict bound,
+ *     accuracy 1, out_of_range="error".  The archive goes to d_archive, the
+ *     mesh to d_verts / d_tris (capacities in vertices / triangles), the f64
+ *     windows and masks stay in the workspace at the offsets reported.
+ *     CHR_E_WORKSPACE: grow to ws_needed / archive_needed / n_tri / n_vert
+ *     and call again.  stage_events (may be NULL): 4 cudaEvent_t recorded at
+ *     the start, after compress, after decode and after the mesh. */
+typedef struct {
+    int64_t n_regions, n_selected;
+    uint64_t archive_nbytes, archive_needed;
+    int64_t n_tri, n_vert;
+    uint64_t window_samples;     /* f64 samples of the selected windows */
+    uint64_t windows_offset;     /* byte offsets in the workspace */
+    uint64_t masks_offset;
+    uint64_t ws_needed;
+    int64_t first_nonfinite;     /* CHR_E_NONFINITE: flat index */
+    double vmin, vmax;
+} chr_pipeline_result_t;
+
+/* called (host thread, between compress and request) with the archive size:
+ * lets a caller start copying the archive out while the rest runs */
+typedef void (*chr_after_compress_fn)(uint64_t archive_nbytes, void *user);
+
+int chr_pipeline(const void *d_vol, int dtype, int src_dtype, int64_t nx, int64_t ny, int64_t nz,
+                 const double *spacing, int64_t block_size, const double *h_cands, int m, double loose_fraction,
+                 double safety_factor, int k_index, void *d_workspace, size_t workspace_bytes, uint8_t *d_archive,
+                 uint64_t archive_cap, double *d_verts, int64_t verts_cap, int32_t *d_tris, int64_t tris_cap,
+                 chr_region_t *h_regions, void *const *stage_events, chr_after_compress_fn after_compress,
+                 void *user, chr_pipeline_result_t *h_res, void *stream);
+
 /* 9. instrumentation: launch counter and opt-in per-kernel CUDA-event
  *    timing on the launching stream ("name count total_ms" lines). */
 void chr_prof_enable(int on);

@@ -103,6 +103,7 @@ DEC_DT = np.dtype([("payload_offset", "<u8"), ("payload_nbytes", "<u8"), ("codec
                    ("error_bound", "<f8"), ("crc", "<u4"), ("_pad", "<u4"), ("out_offset", "<u8")], align=True)
 MCGRID_DT = np.dtype([("grid_offset", "<u8"), ("dims", "<i4", 3), ("_pad", "<i4"), ("origin", "<f8", 3),
                       ("spacing", "<f8", 3)], align=True)
+AFTER_COMPRESS = ctypes.CFUNCTYPE(None, ctypes.c_uint64, ctypes.c_void_p)  # chr_after_compress_fn
 STITCH_DT = np.dtype([("window_offset", "<u8"), ("origin", "<i4", 3), ("extent", "<i4", 3), ("block_lo", "<i4", 3),
                       ("block_hi", "<i4", 3)])  # chr_stitch_t
 assert STITCH_DT.itemsize == 56
@@ -114,6 +115,10 @@ TABLE_ENTRY_DT = np.dtype([("region", REGION_DT), ("region_id", "<u4"), ("status
                            ("block_dtype", "<u4"), ("accuracy", "<f8"), ("block_dims", "<u4", 3), ("_pad", "<u4"),
                            ("block_error_bound", "<f8"), ("payload_len", "<u8")], align=True)  # chr_table_entry_t
 assert FILE_INFO_DT.itemsize == 104 and TABLE_ENTRY_DT.itemsize == 152
+PIPE_RES_DT = np.dtype([("n_regions", "<i8"), ("n_selected", "<i8"), ("archive_nbytes", "<u8"),
+                        ("archive_needed", "<u8"), ("n_tri", "<i8"), ("n_vert", "<i8"), ("window_samples", "<u8"),
+                        ("windows_offset", "<u8"), ("masks_offset", "<u8"), ("ws_needed", "<u8"),
+                        ("first_nonfinite", "<i8"), ("vmin", "<f8"), ("vmax", "<f8")])  # chr_pipeline_result_t
 READ_TOO_SHORT, READ_BAD_MAGIC, READ_TABLE_PAST_END, READ_PAYLOAD_PAST_END = 1, 2, 3, 4
 READ_BLOCK_HEADER_TRUNCATED, READ_PAYLOAD_TRUNCATED, READ_LENGTH_MISMATCH = 5, 6, 7
 assert REGION_DT.itemsize == ctypes.sizeof(Region)
@@ -232,6 +237,9 @@ def lib():
         L.chr_copy.restype = INT
         L.chr_request_tables.argtypes = [P, I64, INT, P, P, P, P, P]
         L.chr_request_tables.restype = I64
+        L.chr_pipeline.argtypes = [P, INT, INT, I64, I64, I64, P, I64, P, INT, D, D, INT, P, SZ, P, U64, P, I64, P,
+                                   I64, P, P, AFTER_COMPRESS, P, P, P]
+        L.chr_pipeline.restype = INT
         _lib = L
     return _lib
 
@@ -242,7 +250,7 @@ EXPORTS = [
     "chr_select_workspace_size", "chr_select_distances", "chr_compress2",
     "chr_stitch_workspace_size", "chr_stitch", "chr_topology_compare",
     "chr_read_header", "chr_read_workspace_size", "chr_read_archive", "chr_prof_timeline",
-    "chr_prof_mark", "chr_copy", "chr_request_tables",
+    "chr_prof_mark", "chr_copy", "chr_request_tables", "chr_pipeline",
     "chr_dcompress_workspace_size", "chr_dcompress_local", "chr_dcompress_finish", "chr_dcompress_headers",
     "chr_abi_version", "chr_status_string", "chr_num_blocks", "chr_stats", "chr_plan",
     "chr_compress_workspace_size", "chr_compress_capacity", "chr_compress",

@@ -99,6 +99,13 @@ class Workspaces:
     def __init__(self):
         self._bufs: dict[str, torch.Tensor] = {}
 
+    def host(self, name: str, n: int, dtype) -> np.ndarray:
+        a = self._bufs.get("host:" + name)
+        if a is None or a.size < n or a.dtype != dtype:
+            a = np.zeros(max(int(n), 1), dtype=dtype)
+            self._bufs["host:" + name] = a
+        return a
+
     def pinned(self, name: str, numel: int, dtype=torch.float64) -> torch.Tensor:
         t = self._bufs.get("pinned:" + name)
         if t is None or t.numel() < numel or t.dtype != dtype:
@@ -284,6 +291,85 @@ def request_tables(regions: np.ndarray, k_index: int, spacing=(1.0, 1.0, 1.0)):
     if m < 0:
         raise ParameterError("chr_request_tables: bad arguments")
     return dec[:m], mct[:m], sel[:m], int(total.value)
+
+
+@dataclass
+class PipelineResult:
+    """chr_pipeline's outputs; the tensors are views into ``ws`` buffers
+    (valid until the next pipeline call with the same workspaces)."""
+    archive: torch.Tensor   # uint8 .chr file
+    regions: np.ndarray     # REGION_DT (codec / offsets / CRCs filled)
+    windows: torch.Tensor   # f64 selected windows, back to back
+    verts: torch.Tensor     # (nv, 3) f64 world coordinates
+    tris: torch.Tensor      # (nt, 3) int32
+    n_selected: int
+    vrange: tuple
+
+
+def pipeline(vol: torch.Tensor, dims, cands, bs, *, loose_fraction=LOOSE_FRACTION, safety_factor=SAFETY_FACTOR,
+             k_index: int = 0, spacing=(1.0, 1.0, 1.0), source_dtype="f32", ws: Workspaces | None = None,
+             stage_events=None, after_compress=None) -> PipelineResult:
+    """build_archive + request(candidate k_index) + marching cubes in one
+    C call (chr_pipeline): the same bytes, windows and mesh as the separate
+    calls, without the host round trips between them.  Strict bound at
+    accuracy 1; candidates must lie inside the volume's range.
+    ``after_compress(archive_view)`` runs as soon as the archive exists
+    (the mesh is still being computed)."""
+    ws = ws or _DEFAULT_WS
+    L = lib()
+    cands = _cands_arr(cands)
+    sp = (ctypes.c_double * 3)(*[float(v) for v in spacing])
+    nb = num_blocks(dims, bs)
+    regions = ws.host("pipe_regions", nb, _abi.REGION_DT)
+    res = np.zeros(1, dtype=_abi.PIPE_RES_DT)
+    need = dict(ws=1 << 20, arch=1 << 20, tri=1 << 16, vert=1 << 16)
+    for key, name in (("ws", "pipe_ws"), ("arch", "pipe_archive")):
+        b = ws._bufs.get(name)
+        if b is not None:
+            need[key] = max(need[key], b.numel())
+    for key, name, el in (("tri", "pipe_tris", 12), ("vert", "pipe_verts", 24)):
+        b = ws._bufs.get(name)
+        if b is not None:
+            need[key] = max(need[key], b.numel() * b.element_size() // el)
+    cb = _abi.AFTER_COMPRESS(0)  # NULL
+    if after_compress is not None:
+        def _cb(nbytes, _user):
+            after_compress(ws._bufs["pipe_archive"][: int(nbytes)])
+        cb = _abi.AFTER_COMPRESS(_cb)
+    evs = None
+    if stage_events is not None:
+        for e in stage_events:
+            if not e.cuda_event:  # torch creates the CUDA event lazily, on its first record
+                e.record()
+        evs = (ctypes.c_void_p * 4)(*[ctypes.c_void_p(e.cuda_event) for e in stage_events])
+    for _ in range(6):
+        work = ws.get("pipe_ws", need["ws"])
+        arch = ws.get("pipe_archive", need["arch"])
+        verts = ws.get("pipe_verts", 24 * need["vert"], torch.float64)
+        tris = ws.get("pipe_tris", 12 * need["tri"], torch.int32)
+        rc = L.chr_pipeline(ptr(vol), _dtype_code(vol), DTYPE_TAGS[source_dtype], *dims, sp, int(bs), _np_ptr(cands),
+                            cands.size, float(loose_fraction), float(safety_factor), int(k_index), ptr(work),
+                            work.numel(), ptr(arch), arch.numel(), ptr(verts), verts.numel() // 3, ptr(tris),
+                            tris.numel() // 3, _abi.aptr(regions), evs, cb, None, _abi.aptr(res), stream_ptr())
+        r = res[0]
+        if rc == _abi.CHR_E_WORKSPACE:
+            need["ws"] = max(need["ws"], int(r["ws_needed"]))
+            need["arch"] = max(need["arch"], int(r["archive_needed"]))
+            need["tri"] = max(need["tri"], int(r["n_tri"]))
+            need["vert"] = max(need["vert"], int(r["n_vert"]))
+            continue
+        if rc == _abi.CHR_E_NONFINITE:
+            i = int(r["first_nonfinite"])
+            raise NonFiniteSampleError(i, float(vol.reshape(-1)[i].item()))
+        check(rc, "chr_pipeline")
+        nreg, nsel = int(r["n_regions"]), int(r["n_selected"])
+        nt, nv = int(r["n_tri"]), int(r["n_vert"])
+        wo, tot = int(r["windows_offset"]), int(r["window_samples"])
+        windows = work[wo: wo + 8 * tot].view(torch.float64)
+        return PipelineResult(arch[: int(r["archive_nbytes"])], regions[:nreg].copy(), windows,
+                              verts[: 3 * nv].view(nv, 3), tris[: 3 * nt].view(nt, 3), nsel,
+                              (float(r["vmin"]), float(r["vmax"])))
+    raise ParameterError("chr_pipeline: workspace negotiation did not converge")
 
 
 def dec_table(payload_offset, payload_nbytes, codec, dims, e, crc) -> np.ndarray:

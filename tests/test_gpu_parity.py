@@ -671,3 +671,28 @@ def test_stats_rows_many_candidates_exact(case):
         d = min(L.or_window_min_abs_distance(ctypes.c_void_p(host.ctypes.data), dims[0], dims[1], w[0][0], w[1][0],
                                              w[2][0], w[0][1], w[1][1], w[2][1], float(k)) for k in cands)
         assert st[b, 2] == d, (case, b)
+
+
+@pytest.mark.parametrize("name,n", [("c1", 64), ("c3", 96), ("c5", 72)])
+def test_pipeline_one_call_matches_separate_calls(name, n):
+    """chr_pipeline (stats -> plan -> compress -> request -> decode -> MC in
+    one call) produces the same archive, windows and mesh as the separate
+    entry points; the after-compress hook sees the finished archive."""
+    vals, dims, bs, cands, r = synth.make_config(name, device="cuda", n=n)
+    seen = {}
+    ws = device.Workspaces()
+    p = device.pipeline(vals, dims, cands, bs, loose_fraction=r, ws=ws,
+                        after_compress=lambda a: seen.setdefault("a", a.cpu().numpy().tobytes()))
+    ref = device.build_archive(vals, dims, cands, bs, loose_fraction=r)
+    want = ref.blob[: ref.nbytes].cpu().numpy().tobytes()
+    assert p.archive.cpu().numpy().tobytes() == want and seen["a"] == want
+    assert np.array_equal(p.regions.view(np.uint8), ref.regions.view(np.uint8))
+    dec, mct, sel_idx, total = device.request_tables(ref.regions, 0)
+    wins, offs, st = device.decode(ref.blob, dec, iso=cands[0])
+    assert not any(st) and p.n_selected == len(sel_idx)
+    assert torch.equal(p.windows, wins)
+    v, t, _, _ = device.marching(wins, mct, cands[0])
+    assert torch.equal(p.verts, v) and torch.equal(p.tris, t)
+    # a second call reuses the negotiated buffers
+    p2 = device.pipeline(vals, dims, cands, bs, loose_fraction=r, ws=ws)
+    assert torch.equal(p2.tris, t)
