@@ -820,6 +820,236 @@ __global__ void __launch_bounds__(EW * 32, 4) k_mc_emit2(const double *__restric
     }
 }
 
+// emit v3: warp per LIVE row piece (triangles > 0), CTA per scan chunk.  The
+// surface touches ~3 % of the cells (c3: a third of the row pieces), so the
+// work is proportional to live pieces, not to the tile volume.  A piece
+// needs the (code, vertex base) of its own cell row and of the three rows an
+// owner can sit in, (y-1, z), (y, z-1), (y-1, z-1), each with the halo cell
+// x0-1: nine row masks (rows y-1..y+1 x planes z-1..z+1) give all of them.
+// Row slot r = (owner offset bits >> 1) & 3: bit 0 = y-1, bit 1 = z-1.
+constexpr int E3W = 8;  // warps per CTA
+struct E3Warp {
+    uint64_t m[9];        // row masks, bit c <-> x0 - 1 + c; index 3 * (dz + 1) + (dy + 1)
+    uint32_t h[9];
+    int64_t vb[4][66];    // vertex base of cell column c (c = 0: halo x0 - 1)
+    int32_t tofs[64];     // own row: triangle offset of each cell within the piece
+    int32_t ex[64];       // own row: exclusive item offset (3 per triangle + owned)
+    uint8_t code[4][66];
+};
+__global__ void __launch_bounds__(E3W * 32, 4) k_mc_emit3(const double *__restrict__ grids, const McGrid *__restrict__ G,
+                                                       const int32_t *__restrict__ chunk_grid, double k,
+                                                       const McTables *__restrict__ T,
+                                                       const McPieceBase *__restrict__ base,
+                                                       const McPieceCnt *__restrict__ cnt,
+                                                       const uint32_t *__restrict__ mask,
+                                                       double *__restrict__ verts, int32_t *__restrict__ tris) {
+    __shared__ __align__(16) int8_t s_tri[256][16];
+    __shared__ __align__(16) uint8_t s_ntri[256];
+    __shared__ __align__(16) uint8_t s_own[256][8];
+    __shared__ uint8_t s_cinfo[12][8], s_vinfo[12];
+    __shared__ E3Warp sw[E3W];
+    __shared__ McGrid g;
+    {
+        const uint4 *src = reinterpret_cast<const uint4 *>(T->tri);
+        uint4 *dst = reinterpret_cast<uint4 *>(&s_tri[0][0]);
+        for (int i = threadIdx.x; i < 256; i += blockDim.x) dst[i] = __ldg(src + i);
+        const uint4 *so = reinterpret_cast<const uint4 *>(T->owncnt);
+        uint4 *d_o = reinterpret_cast<uint4 *>(&s_own[0][0]);
+        for (int i = threadIdx.x; i < 128; i += blockDim.x) d_o[i] = __ldg(so + i);
+        if (threadIdx.x < 16)
+            reinterpret_cast<uint4 *>(s_ntri)[threadIdx.x] = __ldg(reinterpret_cast<const uint4 *>(T->ntri) + threadIdx.x);
+    }
+    if (threadIdx.x < 96) {
+        const int e = threadIdx.x >> 3, f = threadIdx.x & 7;
+        const int a = T->edge_axis[e];
+        int l[3] = {T->edge_low[e][0], T->edge_low[e][1], T->edge_low[e][2]};
+        int d = 0;
+        for (int q = 0; q < 3; ++q)
+            if (q != a && l[q] == 0 && !((f >> q) & 1)) {
+                d |= 1 << q;
+                l[q] = 1;
+            }
+        s_cinfo[e][f] = (uint8_t)(d | (T->edge_id[a][l[0]][l[1]][l[2]] << 3));
+        if (f == 0) s_vinfo[e] = (uint8_t)(a | (T->edge_low[e][0] << 2) | (T->edge_low[e][1] << 3) | (T->edge_low[e][2] << 4));
+    }
+    const int64_t c = blockIdx.x;
+    coop_copy(&g, G + __ldg(chunk_grid + c));
+    __syncthreads();
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    E3Warp &S = sw[w];
+    const uint32_t *mbase = mask + g.mask_off;
+    const double *gp = grids + g.goff;
+    const int64_t nxy = (int64_t)g.nx * g.ny;
+    const int64_t pstep = (int64_t)g.ncy * g.ntx;
+    for (int b = 0; b < (int)(MCH / (32 * E3W)); ++b) {
+        const int64_t p0 = c * MCH + (int64_t)(b * E3W + w) * 32;  // global piece index of lane 0
+        const McPieceCnt mine = cnt[p0 + lane];
+        uint32_t live = __ballot_sync(0xFFFFFFFFu, mine.tri > 0);
+        while (live) {
+            const int src = __ffs(live) - 1;
+            live &= live - 1;
+            const int64_t gpiece = p0 + src;
+            const int ptri = __shfl_sync(0xFFFFFFFFu, mine.tri, src);
+            const int pvert = __shfl_sync(0xFFFFFFFFu, mine.vert, src);
+            const int lp = (int)(gpiece - g.piece_base);  // < 2^31 (McGrid dims are int32 products checked on the host)
+            const int rr = lp / g.ntx;
+            const int xt = lp - rr * g.ntx;
+            const int cz = rr / g.ncy, cy = rr - cz * g.ncy;
+            const int x0 = xt * MTX;
+            // ---- nine row masks (lanes 0..8) and four piece bases (lanes 9..12)
+            __syncwarp();  // previous piece's readers of S are done
+            if (lane < 9) {
+                const int dy = lane % 3 - 1, dz = lane / 3 - 1;
+                const int my = cy + dy, mz = cz + dz;
+                uint64_t m = 0;
+                uint32_t mx = 0;
+                if (my >= 0 && my < g.ny && mz >= 0 && mz < g.nz) {
+                    const uint32_t *mp = mbase + (int64_t)mz * g.pw;
+                    const int64_t bb = (int64_t)my * g.nx + x0;
+                    if (x0 > 0) {
+                        mask_bits66(mp, bb - 1, m, mx);
+                    } else {
+                        uint64_t m1;
+                        uint32_t h1;
+                        mask_bits66(mp, bb, m1, h1);
+                        m = m1 << 1;
+                        mx = (uint32_t)(m1 >> 63) | ((h1 & 1u) << 1);
+                    }
+                }
+                S.m[lane] = m;
+                S.h[lane] = mx;
+            }
+            int64_t rb = 0;  // lanes 0..3: vertex base of row slot r's piece; lane 4: own triangle base
+            if (lane < 5) {
+                const int r = lane & 3;
+                const int dy = -(r & 1), dz = -(r >> 1);
+                if (cy + dy >= 0 && cz + dz >= 0) {
+                    const McPieceBase pb = base[gpiece + dy * g.ntx + dz * pstep];
+                    rb = lane < 4 ? pb.vert : pb.tri;
+                }
+            }
+            __syncwarp();
+            int64_t rbr[5];
+#pragma unroll
+            for (int r = 0; r < 5; ++r) rbr[r] = __shfl_sync(0xFFFFFFFFu, rb, r);
+            // ---- codes of the four row slots: lane owns columns c = 1 + 2 lane, 2 + 2 lane.
+            //      Bits c..c+2 of each of the nine row masks, taken once with
+            //      fixed shifts, give both cells' corner pairs.
+            const int cA = 1 + 2 * lane, xA = x0 + 2 * lane;
+            const bool okA = xA < g.ncx, okB = xA + 1 < g.ncx;
+            uint32_t P0[9], P1[9], H0[9];
+#pragma unroll
+            for (int i = 0; i < 9; ++i) {
+                const uint64_t m = S.m[i];
+                const uint32_t t = (uint32_t)((m >> cA) | ((uint64_t)S.h[i] << (64 - cA)));
+                P0[i] = t & 3u;
+                P1[i] = (t >> 1) & 3u;
+                H0[i] = (uint32_t)m & 3u;  // halo cell (bits 0, 1)
+            }
+            auto mk_code = [](uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+                return (int)(a | pair_swap(b) << 2 | c << 4 | pair_swap(d) << 6);
+            };
+            int own[4][2], ntA = 0, ntB = 0;
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const int dy = -(r & 1), dz = -(r >> 1);
+                const int i00 = 3 * (dz + 1) + (dy + 1);
+                const bool rowok = cy + dy >= 0 && cz + dz >= 0;
+                const int fyz = (cy + dy == 0 ? 2 : 0) | (cz + dz == 0 ? 4 : 0);
+                const int a = (rowok && okA) ? mk_code(P0[i00], P0[i00 + 1], P0[i00 + 3], P0[i00 + 4]) : 0;
+                const int bcode = (rowok && okB) ? mk_code(P1[i00], P1[i00 + 1], P1[i00 + 3], P1[i00 + 4]) : 0;
+                own[r][0] = s_own[a][fyz | (xA == 0 ? 1 : 0)];
+                own[r][1] = s_own[bcode][fyz];
+                S.code[r][cA] = (uint8_t)a;
+                S.code[r][cA + 1] = (uint8_t)bcode;
+                if (r == 0) {
+                    ntA = s_ntri[a];
+                    ntB = s_ntri[bcode];
+                }
+                if (lane == 0) {
+                    const int h = (rowok && x0 > 0) ? mk_code(H0[i00], H0[i00 + 1], H0[i00 + 3], H0[i00 + 4]) : 0;
+                    S.code[r][0] = (uint8_t)h;
+                    S.vb[r][0] = rbr[r] - s_own[h][fyz];
+                }
+            }
+            // ---- scans: owned counts of slots (0,1) and (2,3) packed, triangles of slot 0
+            const uint32_t v01 = (uint32_t)(own[0][0] + own[0][1]) | ((uint32_t)(own[1][0] + own[1][1]) << 16);
+            const uint32_t v23 = (uint32_t)(own[2][0] + own[2][1]) | ((uint32_t)(own[3][0] + own[3][1]) << 16);
+            const uint32_t vt = (uint32_t)(ntA + ntB);
+            uint32_t s01 = v01, s23 = v23, st = vt;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const uint32_t a = __shfl_up_sync(0xFFFFFFFFu, s01, off), bq = __shfl_up_sync(0xFFFFFFFFu, s23, off),
+                               cq = __shfl_up_sync(0xFFFFFFFFu, st, off);
+                if (lane >= off) {
+                    s01 += a;
+                    s23 += bq;
+                    st += cq;
+                }
+            }
+            s01 -= v01;
+            s23 -= v23;
+            st -= vt;
+            const int64_t rb0 = rbr[0], rb1 = rbr[1], rb2 = rbr[2], rb3 = rbr[3], tbase = rbr[4];
+            {
+                const int e0 = (int)(s01 & 0xFFFFu), e1 = (int)(s01 >> 16), e2 = (int)(s23 & 0xFFFFu),
+                          e3 = (int)(s23 >> 16);
+                S.vb[0][cA] = rb0 + e0;
+                S.vb[0][cA + 1] = rb0 + e0 + own[0][0];
+                S.vb[1][cA] = rb1 + e1;
+                S.vb[1][cA + 1] = rb1 + e1 + own[1][0];
+                S.vb[2][cA] = rb2 + e2;
+                S.vb[2][cA + 1] = rb2 + e2 + own[2][0];
+                S.vb[3][cA] = rb3 + e3;
+                S.vb[3][cA + 1] = rb3 + e3 + own[3][0];
+                const int t0 = (int)st;
+                S.tofs[2 * lane] = t0;
+                S.tofs[2 * lane + 1] = t0 + ntA;
+                S.ex[2 * lane] = 3 * t0 + e0;
+                S.ex[2 * lane + 1] = 3 * (t0 + ntA) + e0 + own[0][0];
+            }
+            __syncwarp();
+            // ---- emission: 3 items per triangle corner, then one per owned vertex
+            const int total = 3 * ptri + pvert;
+            for (int i = lane; i < total; i += 32) {
+                int col = 0;
+#pragma unroll
+                for (int step = 32; step; step >>= 1)
+                    if (col + step < 64 && S.ex[col + step] <= i) col += step;
+                const int sl = i - S.ex[col];
+                const int cc = col + 1;
+                const int cx = x0 + col;
+                const int code = S.code[0][cc];
+                const int nt = s_ntri[code];
+                const int f = bflags(cx, cy, cz);
+                if (sl < 3 * nt) {
+                    const int info = s_cinfo[s_tri[code][sl]][f];
+                    const int dx = info & 1, r = (info >> 1) & 3, e2 = info >> 3;
+                    const int ocode = S.code[r][cc - dx];
+                    const int of = bflags(cx - dx, cy - (r & 1), cz - (r >> 1));
+                    const int64_t vid = S.vb[r][cc - dx] + __ldg(&T->rank[ocode][of][e2]);
+                    tris[3 * (g.tri_base + tbase + S.tofs[col]) + sl] = (int32_t)(g.vert_base + vid);
+                } else {
+                    const int rk = sl - 3 * nt;
+                    const int vi = s_vinfo[__ldg(&T->inv[code][f][rk])];
+                    const int a = vi & 3, lx = (vi >> 2) & 1, ly = (vi >> 3) & 1, lz = (vi >> 4) & 1;
+                    const double *sp = gp + (int64_t)(cz + lz) * nxy + (int64_t)(cy + ly) * g.nx + (cx + lx);
+                    const double s0 = __ldg(sp);
+                    const double s1 = __ldg(sp + (a == 0 ? 1 : (a == 1 ? (int64_t)g.nx : nxy)));
+                    const double den = __dadd_rn(s1, -s0);
+                    const double t = den == 0.0 ? 0.0 : __ddiv_rn(__dadd_rn(k, -s0), den);
+                    double lat[3] = {(double)(cx + lx), (double)(cy + ly), (double)(cz + lz)};
+                    lat[a] = __dadd_rn(lat[a], t);
+                    double *o = verts + 3 * (g.vert_base + S.vb[0][cc] + rk);
+                    o[0] = world(g.origin[0], lat[0], g.spacing[0]);
+                    o[1] = world(g.origin[1], lat[1], g.spacing[1]);
+                    o[2] = world(g.origin[2], lat[2], g.spacing[2]);
+                }
+            }
+        }
+    }
+}
+
 __global__ void k_case_codes(const double *__restrict__ g, int64_t nx, int64_t ny, int64_t nz, double k,
                              int binary, uint8_t *__restrict__ codes) {
     const int64_t ncx = nx - 1, ncy = ny - 1, ncz = nz - 1;
@@ -871,6 +1101,7 @@ static bool mc_build(const chr_mc_grid_t *h, int64_t n, McPlan &pl) {
         }
         g.piece_base = piece;
         g.npieces = (int64_t)g.ntx * g.ncy * g.ncz;
+        if (g.npieces >= (int64_t(1) << 31)) return false;  // piece indices are int32 in the kernels
         g.chunk_base = chunk;
         g.nchunks = ceil_div(g.npieces, MCH);
         piece += g.nchunks * MCH;
@@ -1026,13 +1257,11 @@ static int mc_emit_impl(const double *d_grids, const chr_mc_grid_t *h, int64_t n
     if (!d_ws || pl.ws > ws_bytes) return CHR_E_WORKSPACE;
     const McTables *T = mc_tables_device();
     if (!T) return CHR_E_CUDA;
-    if (pl.nitems > 0)
-        {
-            CHR_PROF("k_mc_emit2", st);
-            k_mc_emit2<<<(unsigned)pl.nitems, EW * 32, 0, st>>>(d_grids, pl.d_grids, pl.item_grid, k, T, pl.base,
-                                                                 pl.cnt, d_masks ? d_masks : pl.mask, d_verts,
-                                                                 d_tris);
-        }
+    if (pl.nchunks > 0) {
+        CHR_PROF("k_mc_emit3", st);
+        k_mc_emit3<<<(unsigned)pl.nchunks, E3W * 32, 0, st>>>(d_grids, pl.d_grids, pl.chunk_grid, k, T, pl.base,
+                                                              pl.cnt, d_masks ? d_masks : pl.mask, d_verts, d_tris);
+    }
     CHR_CUDA_TRY(cudaGetLastError());
     CHR_CUDA_TRY(stream_sync(st));
     return CHR_OK;
