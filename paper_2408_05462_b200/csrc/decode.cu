@@ -1114,9 +1114,12 @@ __global__ void __launch_bounds__(256) k_band(const DecReg *__restrict__ regs, c
     __shared__ int64_t ucnt[BDF];                 // dF[nzv][ex]
     __shared__ int64_t s_lo[BSEGM], s_hi[BSEGM], s_ub[BSEGM], s_off[BSEGM];
     __shared__ int32_t s_base[BSEGM + 1];
-    __shared__ int64_t s_tile;
+    __shared__ int64_t s_tile, s_zero;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) s_tile = order[atomicAdd(ticket, 1ull)];
+    if (tid == 0) {
+        s_tile = order[atomicAdd(ticket, 1ull)];
+        s_zero = 0;
+    }
     __syncthreads();
     const int64_t tile = s_tile;
     const DecReg &R = regs[tile_reg[tile]];
@@ -1357,12 +1360,15 @@ __global__ void __launch_bounds__(256) k_band(const DecReg *__restrict__ regs, c
             const int sh = (int)(wb & 31);
             const int64_t pw = R.pw;
             uint32_t *w = mp + (wb >> 5) + (int64_t)z0 * pw;
-            for (int j = 0; j < nzv; ++j, w += pw) {
-                double v = 0.0;
-                if (act) {
-                    v = (double)(Q[j * PL + qi] + (b > 0 ? dF[j * ex + xx] : 0) + fz) * twoe;
-                    __stcs(obase + j * zstride + t, v);
-                }
+            // inactive lanes read valid shared words (index 0) and store nothing
+            const int64_t *qp = Q + qi;
+            const int64_t *dp = dF + xx;
+            double *op = obase + t;
+            const int dstep = b > 0 ? ex : 0;
+            if (b == 0) dp = &s_zero;
+            for (int j = 0; j < nzv; ++j, w += pw, qp += PL, dp += dstep, op += zstride) {
+                const double v = (double)(*qp + *dp + fz) * twoe;
+                if (act) __stcs(op, v);
                 const uint32_t bal = __ballot_sync(0xFFFFFFFFu, act && v >= iso);
                 if (lane == 0) {
                     if (nb == 1) {  // whole planes: this warp owns the word

@@ -881,53 +881,79 @@ __global__ void __launch_bounds__(E3W * 32, 4) k_mc_emit3(const double *__restri
     const double *gp = grids + g.goff;
     const int64_t nxy = (int64_t)g.nx * g.ny;
     const int64_t pstep = (int64_t)g.ncy * g.ntx;
-    for (int b = 0; b < (int)(MCH / (32 * E3W)); ++b) {
+    // The next live piece's row masks (lanes 0..8) and piece bases (lanes
+    // 0..4) are loaded while the current one is computed and emitted.
+    struct Fetch {
+        uint64_t m;
+        uint32_t mx;
+        int64_t rb;
+    };
+    auto coords = [&](int64_t gpiece, int &cy, int &cz, int &x0) {
+        const int lp = (int)(gpiece - g.piece_base);  // < 2^31 (checked on the host)
+        const int rr = lp / g.ntx;
+        const int xt = lp - rr * g.ntx;
+        cz = rr / g.ncy;
+        cy = rr - cz * g.ncy;
+        x0 = xt * MTX;
+    };
+    auto fetch = [&](int64_t gpiece) {
+        Fetch f{0, 0, 0};
+        int cy, cz, x0;
+        coords(gpiece, cy, cz, x0);
+        if (lane < 9) {
+            const int dy = lane % 3 - 1, dz = lane / 3 - 1;
+            const int my = cy + dy, mz = cz + dz;
+            if (my >= 0 && my < g.ny && mz >= 0 && mz < g.nz) {
+                const uint32_t *mp = mbase + (int64_t)mz * g.pw;
+                const int64_t bb = (int64_t)my * g.nx + x0;
+                if (x0 > 0) {
+                    mask_bits66(mp, bb - 1, f.m, f.mx);
+                } else {
+                    uint64_t m1;
+                    uint32_t h1;
+                    mask_bits66(mp, bb, m1, h1);
+                    f.m = m1 << 1;
+                    f.mx = (uint32_t)(m1 >> 63) | ((h1 & 1u) << 1);
+                }
+            }
+        }
+        if (lane < 5) {  // lanes 0..3: vertex base of row slot r's piece; lane 4: own triangle base
+            const int r = lane & 3;
+            const int dy = -(r & 1), dz = -(r >> 1);
+            if (cy + dy >= 0 && cz + dz >= 0) {
+                const McPieceBase pb = base[gpiece + dy * g.ntx + dz * pstep];
+                f.rb = lane < 4 ? pb.vert : pb.tri;
+            }
+        }
+        return f;
+    };
+    constexpr int NB = (int)(MCH / (32 * E3W));
+    McPieceCnt mine = cnt[c * MCH + (int64_t)w * 32 + lane];
+    for (int b = 0; b < NB; ++b) {
         const int64_t p0 = c * MCH + (int64_t)(b * E3W + w) * 32;  // global piece index of lane 0
-        const McPieceCnt mine = cnt[p0 + lane];
         uint32_t live = __ballot_sync(0xFFFFFFFFu, mine.tri > 0);
-        while (live) {
-            const int src = __ffs(live) - 1;
-            live &= live - 1;
+        const McPieceCnt cur_cnt = mine;
+        if (b + 1 < NB) mine = cnt[p0 + E3W * 32 + lane];  // next batch, in flight meanwhile
+        if (!live) continue;
+        int src = __ffs(live) - 1;
+        live &= live - 1;
+        Fetch nf = fetch(p0 + src);
+        while (src >= 0) {
+            const Fetch f = nf;
             const int64_t gpiece = p0 + src;
-            const int ptri = __shfl_sync(0xFFFFFFFFu, mine.tri, src);
-            const int pvert = __shfl_sync(0xFFFFFFFFu, mine.vert, src);
-            const int lp = (int)(gpiece - g.piece_base);  // < 2^31 (McGrid dims are int32 products checked on the host)
-            const int rr = lp / g.ntx;
-            const int xt = lp - rr * g.ntx;
-            const int cz = rr / g.ncy, cy = rr - cz * g.ncy;
-            const int x0 = xt * MTX;
-            // ---- nine row masks (lanes 0..8) and four piece bases (lanes 9..12)
+            const int ptri = __shfl_sync(0xFFFFFFFFu, cur_cnt.tri, src);
+            const int pvert = __shfl_sync(0xFFFFFFFFu, cur_cnt.vert, src);
+            int cy, cz, x0;
+            coords(gpiece, cy, cz, x0);
+            src = live ? __ffs(live) - 1 : -1;
+            live &= live - 1;
             __syncwarp();  // previous piece's readers of S are done
             if (lane < 9) {
-                const int dy = lane % 3 - 1, dz = lane / 3 - 1;
-                const int my = cy + dy, mz = cz + dz;
-                uint64_t m = 0;
-                uint32_t mx = 0;
-                if (my >= 0 && my < g.ny && mz >= 0 && mz < g.nz) {
-                    const uint32_t *mp = mbase + (int64_t)mz * g.pw;
-                    const int64_t bb = (int64_t)my * g.nx + x0;
-                    if (x0 > 0) {
-                        mask_bits66(mp, bb - 1, m, mx);
-                    } else {
-                        uint64_t m1;
-                        uint32_t h1;
-                        mask_bits66(mp, bb, m1, h1);
-                        m = m1 << 1;
-                        mx = (uint32_t)(m1 >> 63) | ((h1 & 1u) << 1);
-                    }
-                }
-                S.m[lane] = m;
-                S.h[lane] = mx;
+                S.m[lane] = f.m;
+                S.h[lane] = f.mx;
             }
-            int64_t rb = 0;  // lanes 0..3: vertex base of row slot r's piece; lane 4: own triangle base
-            if (lane < 5) {
-                const int r = lane & 3;
-                const int dy = -(r & 1), dz = -(r >> 1);
-                if (cy + dy >= 0 && cz + dz >= 0) {
-                    const McPieceBase pb = base[gpiece + dy * g.ntx + dz * pstep];
-                    rb = lane < 4 ? pb.vert : pb.tri;
-                }
-            }
+            if (src >= 0) nf = fetch(p0 + src);
+            const int64_t rb = f.rb;
             __syncwarp();
             int64_t rbr[5];
 #pragma unroll
@@ -937,14 +963,12 @@ __global__ void __launch_bounds__(E3W * 32, 4) k_mc_emit3(const double *__restri
             //      fixed shifts, give both cells' corner pairs.
             const int cA = 1 + 2 * lane, xA = x0 + 2 * lane;
             const bool okA = xA < g.ncx, okB = xA + 1 < g.ncx;
-            uint32_t P0[9], P1[9], H0[9];
+            uint32_t P0[9], P1[9];
 #pragma unroll
             for (int i = 0; i < 9; ++i) {
-                const uint64_t m = S.m[i];
-                const uint32_t t = (uint32_t)((m >> cA) | ((uint64_t)S.h[i] << (64 - cA)));
+                const uint32_t t = (uint32_t)((S.m[i] >> cA) | ((uint64_t)S.h[i] << (64 - cA)));
                 P0[i] = t & 3u;
                 P1[i] = (t >> 1) & 3u;
-                H0[i] = (uint32_t)m & 3u;  // halo cell (bits 0, 1)
             }
             auto mk_code = [](uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
                 return (int)(a | pair_swap(b) << 2 | c << 4 | pair_swap(d) << 6);
@@ -966,11 +990,17 @@ __global__ void __launch_bounds__(E3W * 32, 4) k_mc_emit3(const double *__restri
                     ntA = s_ntri[a];
                     ntB = s_ntri[bcode];
                 }
-                if (lane == 0) {
-                    const int h = (rowok && x0 > 0) ? mk_code(H0[i00], H0[i00 + 1], H0[i00 + 3], H0[i00 + 4]) : 0;
-                    S.code[r][0] = (uint8_t)h;
-                    S.vb[r][0] = rbr[r] - s_own[h][fyz];
-                }
+            }
+            if (lane < 4) {  // halo cell x0 - 1 of slot r = lane (bits 0, 1 of its masks)
+                const int dy = -(lane & 1), dz = -(lane >> 1);
+                const int i00 = 3 * (dz + 1) + (dy + 1);
+                const bool rowok = cy + dy >= 0 && cz + dz >= 0;
+                const int fyz = (cy + dy == 0 ? 2 : 0) | (cz + dz == 0 ? 4 : 0);
+                const int h = (rowok && x0 > 0) ? mk_code((uint32_t)S.m[i00] & 3u, (uint32_t)S.m[i00 + 1] & 3u,
+                                                          (uint32_t)S.m[i00 + 3] & 3u, (uint32_t)S.m[i00 + 4] & 3u)
+                                                : 0;
+                S.code[lane][0] = (uint8_t)h;
+                S.vb[lane][0] = rb - s_own[h][fyz];
             }
             // ---- scans: owned counts of slots (0,1) and (2,3) packed, triangles of slot 0
             const uint32_t v01 = (uint32_t)(own[0][0] + own[0][1]) | ((uint32_t)(own[1][0] + own[1][1]) << 16);
