@@ -761,11 +761,15 @@ __global__ void __launch_bounds__(1024) k_pair_base(const DecReg *__restrict__ r
     for (int64_t r0 = 0; r0 < npairs; r0 += 1024 * 8) {
         const int64_t i0 = r0 + (int64_t)threadIdx.x * 8;
         int64_t c[8], sum = 0;
+        int64_t st = i0 / nreg, r = i0 - st * nreg;  // one division; (step, region) advance by increments
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-            const int64_t i = i0 + j;
-            c[j] = i < npairs ? pair_tiles(regs[i % nreg], i / nreg) : 0;
+            c[j] = i0 + j < npairs ? pair_tiles(regs[r], st) : 0;
             sum += c[j];
+            if (++r == nreg) {
+                r = 0;
+                ++st;
+            }
         }
         int64_t tot;
         int64_t pre = carry + block_excl64(sum, &tot);
@@ -862,7 +866,8 @@ __global__ void __launch_bounds__(DTHREADS) k_seg_locate(const DecReg *__restric
         ++z;
     }
     int64_t s = z * plane + b * band;  // first segment start >= a
-    if (s >= a + cnt) return;
+    const int64_t a_end = a + cnt;
+    if (s >= a_end) return;
     const int64_t lo = (int64_t)R.tok_start, hi = (int64_t)(R.poff + R.plen);
     const int64_t ub = R.abase + (c - R.chunk_base) * DCB + (int64_t)threadIdx.x * UPT * 16;
     uint32_t w[8];
@@ -873,6 +878,25 @@ __global__ void __launch_bounds__(DTHREADS) k_seg_locate(const DecReg *__restric
         if (u) next_unit(blob, u0, w);
         if (!(u0 + 16 > lo && u0 < hi)) continue;
         const UnitMasks m = unit_masks(w, u0, lo, hi);
+        if (m.len == 0) {  // literals only: one sample per token, starts found by rank
+            const int n = __popc(m.lit);
+            while (s < a + n) {
+                const int e = (int)__fns(m.lit, 0, (int)(s - a) + 1);
+                const uint32_t below = m.E & ((1u << e) - 1u);
+                const int sb = below ? 32 - __clz(below) : 0;
+                const int64_t k = R.sp_base + z * nb + b;
+                sp_byte[k] = u0 - 16 + sb;
+                sp_skip[k] = 0;
+                if (++b >= nb) {
+                    b = 0;
+                    ++z;
+                }
+                s = z * plane + b * band;
+            }
+            a += n;
+            if (s >= a_end) return;
+            continue;
+        }
         uint32_t T = m.lit | m.len;
         while (T) {
             const int e = __ffs(T) - 1;
@@ -896,6 +920,7 @@ __global__ void __launch_bounds__(DTHREADS) k_seg_locate(const DecReg *__restric
             }
             a += tc;
         }
+        if (s >= a_end) return;  // no segment start left in this thread's samples
     }
 }
 

@@ -527,13 +527,20 @@ __global__ void __launch_bounds__(256) k_mc_count3(const McGrid *__restrict__ G,
         const uint64_t a1 = m00 & m10 & m01 & m11, o1 = m00 | m10 | m01 | m11;
         const uint32_t ah = h00 & h10 & h01 & h11 & 3u, oh = (h00 | h10 | h01 | h11) & 3u;
         if (!((o1 == 0 && oh == 0) || (a1 == ~0ull && ah == 3u))) {
+            // lane owns cells 2 lane, 2 lane + 1: bits 2 lane .. 2 lane + 2 of each row
+            const int cA = 2 * lane;
+            auto trip = [&](uint64_t m, uint32_t h) {
+                return (uint32_t)(m >> cA) | (uint32_t)(((uint64_t)h << 2) << (62 - cA));
+            };
+            const uint32_t t00 = trip(m00, h00), t10 = trip(m10, h10), t01 = trip(m01, h01), t11 = trip(m11, h11);
+            const int fyz = (cy == 0 ? 2 : 0) | (cz == 0 ? 4 : 0);
 #pragma unroll
             for (int hh = 0; hh < 2; ++hh) {
-                const int cc = lane + 32 * hh;
-                if (x0 + cc < g.ncx) {
-                    const int code = code_fast(m00, h00, m10, h10, m01, h01, m11, h11, cc);
+                if (x0 + cA + hh < g.ncx) {
+                    const int code = (int)(((t00 >> hh) & 3u) | pair_swap((t10 >> hh) & 3u) << 2 |
+                                           ((t01 >> hh) & 3u) << 4 | pair_swap((t11 >> hh) & 3u) << 6);
                     t += s_ntri[code];
-                    v += s_own[code][bflags(x0 + cc, cy, cz)];
+                    v += s_own[code][fyz | (x0 + cA + hh == 0 ? 1 : 0)];
                 }
             }
             t = __reduce_add_sync(0xFFFFFFFFu, t);
