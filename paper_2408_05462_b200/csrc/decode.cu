@@ -753,37 +753,41 @@ __device__ __forceinline__ int64_t pair_tiles(const DecReg &R, int64_t d_glob) {
     return hi >= lo ? hi - lo + 1 : 0;
 }
 
-// exclusive prefix of pair_tiles over all pairs in step-major order (one
-// CTA of 1024 threads, 8 consecutive pairs per thread per round)
-__global__ void __launch_bounds__(1024) k_pair_base(const DecReg *__restrict__ regs, int64_t npairs, int64_t nreg,
-                                                     int64_t *__restrict__ pair_base) {
+// exclusive prefix of pair_tiles over all pairs in step-major order, in two
+// parts: k_step_pairs (CTA per step) = prefix over the regions of one step +
+// the step's total; k_step_scan (one CTA) = exclusive prefix over the steps,
+// added by k_tile_order.
+__global__ void __launch_bounds__(256) k_step_pairs(const DecReg *__restrict__ regs, int64_t nreg,
+                                                    int64_t *__restrict__ pair_base, int64_t *__restrict__ step_tot) {
+    const int64_t st = blockIdx.x;
     int64_t carry = 0;
-    for (int64_t r0 = 0; r0 < npairs; r0 += 1024 * 8) {
-        const int64_t i0 = r0 + (int64_t)threadIdx.x * 8;
-        int64_t c[8], sum = 0;
-        int64_t st = i0 / nreg, r = i0 - st * nreg;  // one division; (step, region) advance by increments
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            c[j] = i0 + j < npairs ? pair_tiles(regs[r], st) : 0;
-            sum += c[j];
-            if (++r == nreg) {
-                r = 0;
-                ++st;
-            }
-        }
+    for (int64_t r0 = 0; r0 < nreg; r0 += 256) {
+        const int64_t r = r0 + threadIdx.x;
+        const int64_t c = r < nreg ? pair_tiles(regs[r], st) : 0;
         int64_t tot;
-        int64_t pre = carry + block_excl64(sum, &tot);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            if (i0 + j < npairs) pair_base[i0 + j] = pre;
-            pre += c[j];
-        }
+        const int64_t pre = block_excl64(c, &tot);
+        if (r < nreg) pair_base[st * nreg + r] = carry + pre;
+        carry += tot;
+    }
+    if (threadIdx.x == 0) step_tot[st] = carry;
+}
+
+__global__ void __launch_bounds__(1024) k_step_scan(int64_t nsteps, int64_t *__restrict__ step_tot) {
+    int64_t carry = 0;
+    for (int64_t s0 = 0; s0 < nsteps; s0 += 1024) {
+        const int64_t i = s0 + threadIdx.x;
+        const int64_t v = i < nsteps ? step_tot[i] : 0;
+        int64_t tot;
+        const int64_t pre = block_excl64(v, &tot);
+        __syncthreads();  // every thread has read its total before it is overwritten
+        if (i < nsteps) step_tot[i] = carry + pre;
         carry += tot;
     }
 }
 
 __global__ void k_tile_order(const DecReg *__restrict__ regs, const int64_t *__restrict__ pair_base,
-                             int64_t npairs, int64_t nreg, int32_t *__restrict__ order) {
+                             const int64_t *__restrict__ step_base, int64_t npairs, int64_t nreg,
+                             int32_t *__restrict__ order) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= npairs) return;
     const int64_t r = i % nreg;
@@ -791,7 +795,7 @@ __global__ void k_tile_order(const DecReg *__restrict__ regs, const int64_t *__r
     if (R.ntiles == 0) return;
     const int d = (int)(i / nreg) - R.doff;
     if (d < 0) return;
-    int64_t k = pair_base[i];
+    int64_t k = step_base[i / nreg] + pair_base[i];
     const int ny = R.tny, nz = R.tnz;
     for (int tz = max(0, d - (ny - 1)); tz <= min(nz - 1, d); ++tz)
         order[k++] = (int32_t)(R.tile_base + (int64_t)tz * ny + (d - tz));
@@ -1471,7 +1475,7 @@ struct DecPlan {
     int64_t *sp_byte, *sp_skip, *esc_sp, *thr_cnt, *pos64;
     int64_t *faces;
     int32_t *tflag, *chunk_reg, *tile_reg, *order;
-    int64_t *pair_base;
+    int64_t *pair_base, *step_base;
     int64_t ndiag = 0;
     unsigned long long *ticket, *ticket3;
     int32_t *any_slow;
@@ -1644,6 +1648,7 @@ static void dec_carve(DecPlan &pl, void *base, size_t cap) {
     pl.tile_reg = c.take<int32_t>(pl.ntiles + 1);
     pl.order = c.take<int32_t>(pl.ntiles + 1);
     pl.pair_base = c.take<int64_t>(pl.ndiag * n + 1);
+    pl.step_base = c.take<int64_t>(pl.ndiag + 1);
     pl.ticket = c.take<unsigned long long>(1);
     pl.ticket3 = c.take<unsigned long long>(1);
     pl.any_slow = c.take<int32_t>(1);
@@ -1752,12 +1757,17 @@ static int decode_impl(const uint8_t *d_blob, const chr_dec_region_t *h, int64_t
         }
         const int64_t npairs = pl.ndiag * n;
         {
-            CHR_PROF("k_pair_base", st);
-            k_pair_base<<<1, 1024, 0, st>>>(pl.d_regs, npairs, n, pl.pair_base);
+            CHR_PROF("k_step_pairs", st);
+            k_step_pairs<<<(unsigned)pl.ndiag, 256, 0, st>>>(pl.d_regs, n, pl.pair_base, pl.step_base);
+        }
+        {
+            CHR_PROF("k_step_scan", st);
+            k_step_scan<<<1, 1024, 0, st>>>(pl.ndiag, pl.step_base);
         }
         {
             CHR_PROF("k_tile_order", st);
-            k_tile_order<<<(unsigned)ceil_div(npairs, 256), 256, 0, st>>>(pl.d_regs, pl.pair_base, npairs, n, pl.order);
+            k_tile_order<<<(unsigned)ceil_div(npairs, 256), 256, 0, st>>>(pl.d_regs, pl.pair_base, pl.step_base,
+                                                                         npairs, n, pl.order);
         }
         const int smem = (int)(sizeof(int64_t) * BCAP);
         CHR_CUDA_TRY(cudaFuncSetAttribute(k_band, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
