@@ -836,6 +836,7 @@ __global__ void __launch_bounds__(EW * 32, 4) k_mc_emit2(const double *__restric
 // Row slot r = (owner offset bits >> 1) & 3: bit 0 = y-1, bit 1 = z-1.
 constexpr int E3W = 8;  // warps per CTA
 struct E3Warp {
+    McGrid g;             // grid of the warp's current batch
     uint64_t m[9];        // row masks, bit c <-> x0 - 1 + c; index 3 * (dz + 1) + (dy + 1)
     uint32_t h[9];
     int64_t vb[4][66];    // vertex base of cell column c (c = 0: halo x0 - 1)
@@ -849,13 +850,13 @@ __global__ void __launch_bounds__(E3W * 32, 4) k_mc_emit3(const double *__restri
                                                        const McPieceBase *__restrict__ base,
                                                        const McPieceCnt *__restrict__ cnt,
                                                        const uint32_t *__restrict__ mask,
+                                                       unsigned long long *__restrict__ queue, int64_t nbatch,
                                                        double *__restrict__ verts, int32_t *__restrict__ tris) {
     __shared__ __align__(16) int8_t s_tri[256][16];
     __shared__ __align__(16) uint8_t s_ntri[256];
     __shared__ __align__(16) uint8_t s_own[256][8];
     __shared__ uint8_t s_cinfo[12][8], s_vinfo[12];
     __shared__ E3Warp sw[E3W];
-    __shared__ McGrid g;
     {
         const uint4 *src = reinterpret_cast<const uint4 *>(T->tri);
         uint4 *dst = reinterpret_cast<uint4 *>(&s_tri[0][0]);
@@ -879,15 +880,14 @@ __global__ void __launch_bounds__(E3W * 32, 4) k_mc_emit3(const double *__restri
         s_cinfo[e][f] = (uint8_t)(d | (T->edge_id[a][l[0]][l[1]][l[2]] << 3));
         if (f == 0) s_vinfo[e] = (uint8_t)(a | (T->edge_low[e][0] << 2) | (T->edge_low[e][1] << 3) | (T->edge_low[e][2] << 4));
     }
-    const int64_t c = blockIdx.x;
-    coop_copy(&g, G + __ldg(chunk_grid + c));
     __syncthreads();
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     E3Warp &S = sw[w];
-    const uint32_t *mbase = mask + g.mask_off;
-    const double *gp = grids + g.goff;
-    const int64_t nxy = (int64_t)g.nx * g.ny;
-    const int64_t pstep = (int64_t)g.ncy * g.ntx;
+    McGrid &g = S.g;
+    const uint32_t *mbase = nullptr;
+    const double *gp = nullptr;
+    int64_t nxy = 0, pstep = 0;
+    int cur_grid = -1;
     // The next live piece's row masks (lanes 0..8) and piece bases (lanes
     // 0..4) are loaded while the current one is computed and emitted.
     struct Fetch {
@@ -934,13 +934,32 @@ __global__ void __launch_bounds__(E3W * 32, 4) k_mc_emit3(const double *__restri
         }
         return f;
     };
-    constexpr int NB = (int)(MCH / (32 * E3W));
-    McPieceCnt mine = cnt[c * MCH + (int64_t)w * 32 + lane];
-    for (int b = 0; b < NB; ++b) {
-        const int64_t p0 = c * MCH + (int64_t)(b * E3W + w) * 32;  // global piece index of lane 0
-        uint32_t live = __ballot_sync(0xFFFFFFFFu, mine.tri > 0);
-        const McPieceCnt cur_cnt = mine;
-        if (b + 1 < NB) mine = cnt[p0 + E3W * 32 + lane];  // next batch, in flight meanwhile
+    // Persistent warps take batches of 32 consecutive pieces from a global
+    // queue (dense surface patches make batches very unequal; a fixed split
+    // left warps idle while their CTA's slowest warp finished).
+    constexpr int NB = (int)(MCH / 32);  // batches per scan chunk
+    for (;;) {
+        unsigned long long bq = 0;
+        if (lane == 0) bq = atomicAdd(queue, 1ull);
+        const int64_t bi = (int64_t)__shfl_sync(0xFFFFFFFFu, bq, 0);
+        if (bi >= nbatch) break;
+        const int64_t c = bi / NB;
+        const int gi = __ldg(chunk_grid + c);
+        if (gi != cur_grid) {
+            __syncwarp();
+            const uint32_t *src = reinterpret_cast<const uint32_t *>(G + gi);
+            uint32_t *dst = reinterpret_cast<uint32_t *>(&S.g);
+            for (int i = lane; i < (int)(sizeof(McGrid) / 4); i += 32) dst[i] = src[i];
+            __syncwarp();
+            cur_grid = gi;
+            mbase = mask + g.mask_off;
+            gp = grids + g.goff;
+            nxy = (int64_t)g.nx * g.ny;
+            pstep = (int64_t)g.ncy * g.ntx;
+        }
+        const int64_t p0 = c * MCH + (bi - c * NB) * 32;  // global piece index of lane 0
+        const McPieceCnt cur_cnt = cnt[p0 + lane];
+        uint32_t live = __ballot_sync(0xFFFFFFFFu, cur_cnt.tri > 0);
         if (!live) continue;
         int src = __ffs(live) - 1;
         live &= live - 1;
@@ -1157,10 +1176,14 @@ static bool mc_build(const chr_mc_grid_t *h, int64_t n, McPlan &pl) {
     return true;
 }
 
+static unsigned long long *mc_queue(const McPlan &pl) {
+    return reinterpret_cast<unsigned long long *>(pl.cnt + pl.npieces);
+}
+
 static void mc_carve(McPlan &pl, void *base, size_t cap) {
     WsCarver c{reinterpret_cast<char *>(base), 0, cap};
     pl.d_grids = c.take<McGrid>(pl.grids.size());
-    pl.cnt = c.take<McPieceCnt>(pl.npieces);
+    pl.cnt = c.take<McPieceCnt>(pl.npieces + 1);  // last entry: k_mc_emit3's batch queue
     pl.chunk = c.take<McPieceBase>(pl.nchunks);
     pl.base = c.take<McPieceBase>(pl.npieces);
     pl.totals = c.take<int64_t>(2);
@@ -1229,7 +1252,7 @@ static int mc_count_impl(const double *d_grids, const chr_mc_grid_t *h, int64_t 
     const McTables *T = mc_tables_device();
     if (!T) return CHR_E_CUDA;
     CHR_CUDA_TRY(h2d(pl.d_grids, pl.grids.data(), sizeof(McGrid) * n, st));
-    CHR_CUDA_TRY(fill_async(pl.cnt, 0, sizeof(McPieceCnt) * pl.npieces, st));
+    CHR_CUDA_TRY(fill_async(pl.cnt, 0, sizeof(McPieceCnt) * (pl.npieces + 1), st));  // + the emit queue
     {
         CHR_PROF("k_mc_fill_map", st);
         k_mc_fill_map<<<(unsigned)n, 256, 0, st>>>(pl.d_grids, n, pl.item_grid, pl.chunk_grid, pl.mask_grid);
@@ -1295,9 +1318,18 @@ static int mc_emit_impl(const double *d_grids, const chr_mc_grid_t *h, int64_t n
     const McTables *T = mc_tables_device();
     if (!T) return CHR_E_CUDA;
     if (pl.nchunks > 0) {
+        static int n_sm = 0;
+        if (!n_sm) {
+            int dev = 0;
+            CHR_CUDA_TRY(cudaGetDevice(&dev));
+            CHR_CUDA_TRY(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
+        }
+        const int64_t nbatch = pl.nchunks * (MCH / 32);
+        const int64_t ctas = std::min<int64_t>(ceil_div(nbatch, E3W), (int64_t)n_sm * 4);
         CHR_PROF("k_mc_emit3", st);
-        k_mc_emit3<<<(unsigned)pl.nchunks, E3W * 32, 0, st>>>(d_grids, pl.d_grids, pl.chunk_grid, k, T, pl.base,
-                                                              pl.cnt, d_masks ? d_masks : pl.mask, d_verts, d_tris);
+        k_mc_emit3<<<(unsigned)ctas, E3W * 32, 0, st>>>(d_grids, pl.d_grids, pl.chunk_grid, k, T, pl.base, pl.cnt,
+                                                        d_masks ? d_masks : pl.mask, mc_queue(pl), nbatch, d_verts,
+                                                        d_tris);
     }
     CHR_CUDA_TRY(cudaGetLastError());
     CHR_CUDA_TRY(stream_sync(st));
