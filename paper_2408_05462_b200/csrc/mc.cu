@@ -415,10 +415,11 @@ __global__ void __launch_bounds__(256) k_mc_count3(const McGrid *__restrict__ G,
                                                    const int32_t *__restrict__ chunk_grid,
                                                    const McTables *__restrict__ T,
                                                    const uint32_t *__restrict__ mask,
-                                                   McPieceCnt *__restrict__ cnt) {
+                                                   McPieceCnt *__restrict__ cnt,
+                                                   unsigned long long *__restrict__ queue, int64_t nbatch) {
     __shared__ __align__(16) uint8_t s_ntri[256];
     __shared__ __align__(16) uint8_t s_own[256][8];
-    __shared__ McGrid g;
+    __shared__ McGrid sg[8];
     {
         const uint4 *so = reinterpret_cast<const uint4 *>(T->owncnt);
         uint4 *d_o = reinterpret_cast<uint4 *>(&s_own[0][0]);
@@ -426,14 +427,13 @@ __global__ void __launch_bounds__(256) k_mc_count3(const McGrid *__restrict__ G,
         if (threadIdx.x < 16)
             reinterpret_cast<uint4 *>(s_ntri)[threadIdx.x] = __ldg(reinterpret_cast<const uint4 *>(T->ntri) + threadIdx.x);
     }
-    const int64_t c = blockIdx.x;
-    coop_copy(&g, G + __ldg(chunk_grid + c));
     __syncthreads();
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    constexpr int PW = (int)(MCH / 8);
-    int64_t lp = (c - g.chunk_base) * MCH + (int64_t)w * PW;
-    const int64_t lpe = min(lp + PW, g.npieces);
-    if (lp >= lpe) return;
+    McGrid &g = sg[w];
+    int cur_grid = -1;
+    // persistent warps: batches of 32 pieces from a global queue (live and
+    // dead pieces cost very differently; a fixed split left warps idle)
+    auto run = [&](int64_t lp, const int64_t lpe) {
     int xt = (int)(lp % g.ntx);
     const int64_t r = lp / g.ntx;
     int cy = (int)(r % g.ncy), cz = (int)(r / g.ncy);
@@ -559,6 +559,27 @@ __global__ void __launch_bounds__(256) k_mc_count3(const McGrid *__restrict__ G,
                 ++cz;
             }
         }
+    }
+    };
+    constexpr int NB = (int)(MCH / 32);
+    for (;;) {
+        unsigned long long bq = 0;
+        if (lane == 0) bq = atomicAdd(queue, 1ull);
+        const int64_t bi = (int64_t)__shfl_sync(0xFFFFFFFFu, bq, 0);
+        if (bi >= nbatch) break;
+        const int64_t c = bi / NB;
+        const int gi = __ldg(chunk_grid + c);
+        if (gi != cur_grid) {
+            __syncwarp();
+            const uint32_t *src = reinterpret_cast<const uint32_t *>(G + gi);
+            uint32_t *dst = reinterpret_cast<uint32_t *>(&g);
+            for (int i = lane; i < (int)(sizeof(McGrid) / 4); i += 32) dst[i] = src[i];
+            __syncwarp();
+            cur_grid = gi;
+        }
+        const int64_t lp = (c - g.chunk_base) * MCH + (bi - c * NB) * 32;
+        const int64_t lpe = min(lp + 32, g.npieces);
+        if (lp < lpe) run(lp, lpe);
     }
 }
 
@@ -1176,6 +1197,20 @@ static bool mc_build(const chr_mc_grid_t *h, int64_t n, McPlan &pl) {
     return true;
 }
 
+static int mc_num_sms() {
+    static int n_sm = 0;
+    if (!n_sm) {
+        int dev = 0, n = 0;
+        if (cudaGetDevice(&dev) == cudaSuccess &&
+            cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess)
+            n_sm = n;
+        else
+            return 148;
+    }
+    return n_sm;
+}
+
+// two zeroed counters after the piece counts: [0] k_mc_emit3's batch queue, [1] k_mc_count3's
 static unsigned long long *mc_queue(const McPlan &pl) {
     return reinterpret_cast<unsigned long long *>(pl.cnt + pl.npieces);
 }
@@ -1183,7 +1218,7 @@ static unsigned long long *mc_queue(const McPlan &pl) {
 static void mc_carve(McPlan &pl, void *base, size_t cap) {
     WsCarver c{reinterpret_cast<char *>(base), 0, cap};
     pl.d_grids = c.take<McGrid>(pl.grids.size());
-    pl.cnt = c.take<McPieceCnt>(pl.npieces + 1);  // last entry: k_mc_emit3's batch queue
+    pl.cnt = c.take<McPieceCnt>(pl.npieces + 2);  // + the two batch queues (mc_queue)
     pl.chunk = c.take<McPieceBase>(pl.nchunks);
     pl.base = c.take<McPieceBase>(pl.npieces);
     pl.totals = c.take<int64_t>(2);
@@ -1252,7 +1287,7 @@ static int mc_count_impl(const double *d_grids, const chr_mc_grid_t *h, int64_t 
     const McTables *T = mc_tables_device();
     if (!T) return CHR_E_CUDA;
     CHR_CUDA_TRY(h2d(pl.d_grids, pl.grids.data(), sizeof(McGrid) * n, st));
-    CHR_CUDA_TRY(fill_async(pl.cnt, 0, sizeof(McPieceCnt) * (pl.npieces + 1), st));  // + the emit queue
+    CHR_CUDA_TRY(fill_async(pl.cnt, 0, sizeof(McPieceCnt) * (pl.npieces + 2), st));  // + the batch queues
     {
         CHR_PROF("k_mc_fill_map", st);
         k_mc_fill_map<<<(unsigned)n, 256, 0, st>>>(pl.d_grids, n, pl.item_grid, pl.chunk_grid, pl.mask_grid);
@@ -1267,7 +1302,9 @@ static int mc_count_impl(const double *d_grids, const chr_mc_grid_t *h, int64_t 
     }
     if (pl.nchunks > 0) {
         CHR_PROF("k_mc_count3", st);
-        k_mc_count3<<<(unsigned)pl.nchunks, 256, 0, st>>>(pl.d_grids, pl.chunk_grid, T, masks, pl.cnt);
+        const int64_t nbatch = pl.nchunks * (MCH / 32);
+        k_mc_count3<<<(unsigned)std::min<int64_t>(ceil_div(nbatch, 8), (int64_t)mc_num_sms() * 8), 256, 0, st>>>(
+            pl.d_grids, pl.chunk_grid, T, masks, pl.cnt, mc_queue(pl) + 1, nbatch);
     }
     {
         CHR_PROF("k_mc_reduce", st);
@@ -1318,14 +1355,8 @@ static int mc_emit_impl(const double *d_grids, const chr_mc_grid_t *h, int64_t n
     const McTables *T = mc_tables_device();
     if (!T) return CHR_E_CUDA;
     if (pl.nchunks > 0) {
-        static int n_sm = 0;
-        if (!n_sm) {
-            int dev = 0;
-            CHR_CUDA_TRY(cudaGetDevice(&dev));
-            CHR_CUDA_TRY(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
-        }
         const int64_t nbatch = pl.nchunks * (MCH / 32);
-        const int64_t ctas = std::min<int64_t>(ceil_div(nbatch, E3W), (int64_t)n_sm * 4);
+        const int64_t ctas = std::min<int64_t>(ceil_div(nbatch, E3W), (int64_t)mc_num_sms() * 4);
         CHR_PROF("k_mc_emit3", st);
         k_mc_emit3<<<(unsigned)ctas, E3W * 32, 0, st>>>(d_grids, pl.d_grids, pl.chunk_grid, k, T, pl.base, pl.cnt,
                                                         d_masks ? d_masks : pl.mask, mc_queue(pl), nbatch, d_verts,
