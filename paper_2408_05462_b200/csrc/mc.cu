@@ -862,7 +862,7 @@ struct E3Warp {
     uint32_t h[9];
     int64_t vb[4][66];    // vertex base of cell column c (c = 0: halo x0 - 1)
     int32_t tofs[64];     // own row: triangle offset of each cell within the piece
-    int32_t ex[64];       // own row: exclusive item offset (3 per triangle + owned)
+    int32_t ex[64];       // own row: exclusive owned-vertex offset of each cell within the piece
     uint8_t code[4][66];
 };
 __global__ void __launch_bounds__(E3W * 32, 4) k_mc_emit3(const double *__restrict__ grids, const McGrid *__restrict__ G,
@@ -915,19 +915,23 @@ __global__ void __launch_bounds__(E3W * 32, 4) k_mc_emit3(const double *__restri
         uint64_t m;
         uint32_t mx;
         int64_t rb;
+        int cy, cz, x0;
     };
     auto coords = [&](int64_t gpiece, int &cy, int &cz, int &x0) {
         const int lp = (int)(gpiece - g.piece_base);  // < 2^31 (checked on the host)
-        const int rr = lp / g.ntx;
+        const int rr = g.ntx == 1 ? lp : lp / g.ntx;
         const int xt = lp - rr * g.ntx;
         cz = rr / g.ncy;
         cy = rr - cz * g.ncy;
         x0 = xt * MTX;
     };
     auto fetch = [&](int64_t gpiece) {
-        Fetch f{0, 0, 0};
+        Fetch f{0, 0, 0, 0, 0, 0};
         int cy, cz, x0;
         coords(gpiece, cy, cz, x0);
+        f.cy = cy;
+        f.cz = cz;
+        f.x0 = x0;
         if (lane < 9) {
             const int dy = lane % 3 - 1, dz = lane / 3 - 1;
             const int my = cy + dy, mz = cz + dz;
@@ -990,8 +994,7 @@ __global__ void __launch_bounds__(E3W * 32, 4) k_mc_emit3(const double *__restri
             const int64_t gpiece = p0 + src;
             const int ptri = __shfl_sync(0xFFFFFFFFu, cur_cnt.tri, src);
             const int pvert = __shfl_sync(0xFFFFFFFFu, cur_cnt.vert, src);
-            int cy, cz, x0;
-            coords(gpiece, cy, cz, x0);
+            const int cy = f.cy, cz = f.cz, x0 = f.x0;
             src = live ? __ffs(live) - 1 : -1;
             live &= live - 1;
             __syncwarp();  // previous piece's readers of S are done
@@ -1082,46 +1085,53 @@ __global__ void __launch_bounds__(E3W * 32, 4) k_mc_emit3(const double *__restri
                 const int t0 = (int)st;
                 S.tofs[2 * lane] = t0;
                 S.tofs[2 * lane + 1] = t0 + ntA;
-                S.ex[2 * lane] = 3 * t0 + e0;
-                S.ex[2 * lane + 1] = 3 * (t0 + ntA) + e0 + own[0][0];
+                S.ex[2 * lane] = e0;  // owned-vertex prefix of the own row
+                S.ex[2 * lane + 1] = e0 + own[0][0];
             }
             __syncwarp();
-            // ---- emission: 3 items per triangle corner, then one per owned vertex
-            const int total = 3 * ptri + pvert;
-            for (int i = lane; i < total; i += 32) {
+            // ---- emission in two uniform passes (no divergence between the
+            //      kinds): triangle corners in output order, then owned vertices
+            auto find = [&](const int32_t *pre, int i) {  // last column with pre[col] <= i
                 int col = 0;
 #pragma unroll
                 for (int step = 32; step; step >>= 1)
-                    if (col + step < 64 && S.ex[col + step] <= i) col += step;
-                const int sl = i - S.ex[col];
+                    if (col + step < 64 && pre[col + step] <= i) col += step;
+                return col;
+            };
+            const int64_t tout = 3 * (g.tri_base + tbase);
+            for (int i = lane; i < 3 * ptri; i += 32) {
+                const int ti = i / 3;
+                const int col = find(S.tofs, ti);
+                const int sl = i - 3 * S.tofs[col];
                 const int cc = col + 1;
                 const int cx = x0 + col;
                 const int code = S.code[0][cc];
-                const int nt = s_ntri[code];
-                const int f = bflags(cx, cy, cz);
-                if (sl < 3 * nt) {
-                    const int info = s_cinfo[s_tri[code][sl]][f];
-                    const int dx = info & 1, r = (info >> 1) & 3, e2 = info >> 3;
-                    const int ocode = S.code[r][cc - dx];
-                    const int of = bflags(cx - dx, cy - (r & 1), cz - (r >> 1));
-                    const int64_t vid = S.vb[r][cc - dx] + __ldg(&T->rank[ocode][of][e2]);
-                    tris[3 * (g.tri_base + tbase + S.tofs[col]) + sl] = (int32_t)(g.vert_base + vid);
-                } else {
-                    const int rk = sl - 3 * nt;
-                    const int vi = s_vinfo[__ldg(&T->inv[code][f][rk])];
-                    const int a = vi & 3, lx = (vi >> 2) & 1, ly = (vi >> 3) & 1, lz = (vi >> 4) & 1;
-                    const double *sp = gp + (int64_t)(cz + lz) * nxy + (int64_t)(cy + ly) * g.nx + (cx + lx);
-                    const double s0 = __ldg(sp);
-                    const double s1 = __ldg(sp + (a == 0 ? 1 : (a == 1 ? (int64_t)g.nx : nxy)));
-                    const double den = __dadd_rn(s1, -s0);
-                    const double t = den == 0.0 ? 0.0 : __ddiv_rn(__dadd_rn(k, -s0), den);
-                    double lat[3] = {(double)(cx + lx), (double)(cy + ly), (double)(cz + lz)};
-                    lat[a] = __dadd_rn(lat[a], t);
-                    double *o = verts + 3 * (g.vert_base + S.vb[0][cc] + rk);
-                    o[0] = world(g.origin[0], lat[0], g.spacing[0]);
-                    o[1] = world(g.origin[1], lat[1], g.spacing[1]);
-                    o[2] = world(g.origin[2], lat[2], g.spacing[2]);
-                }
+                const int info = s_cinfo[s_tri[code][sl]][bflags(cx, cy, cz)];
+                const int dx = info & 1, r = (info >> 1) & 3, e2 = info >> 3;
+                const int ocode = S.code[r][cc - dx];
+                const int of = bflags(cx - dx, cy - (r & 1), cz - (r >> 1));
+                const int64_t vid = S.vb[r][cc - dx] + __ldg(&T->rank[ocode][of][e2]);
+                tris[tout + i] = (int32_t)(g.vert_base + vid);
+            }
+            for (int j = lane; j < pvert; j += 32) {
+                const int col = find(S.ex, j);
+                const int rk = j - S.ex[col];
+                const int cc = col + 1;
+                const int cx = x0 + col;
+                const int code = S.code[0][cc];
+                const int vi = s_vinfo[__ldg(&T->inv[code][bflags(cx, cy, cz)][rk])];
+                const int a = vi & 3, lx = (vi >> 2) & 1, ly = (vi >> 3) & 1, lz = (vi >> 4) & 1;
+                const double *sp = gp + (int64_t)(cz + lz) * nxy + (int64_t)(cy + ly) * g.nx + (cx + lx);
+                const double s0 = __ldg(sp);
+                const double s1 = __ldg(sp + (a == 0 ? 1 : (a == 1 ? (int64_t)g.nx : nxy)));
+                const double den = __dadd_rn(s1, -s0);
+                const double t = den == 0.0 ? 0.0 : __ddiv_rn(__dadd_rn(k, -s0), den);
+                double lat[3] = {(double)(cx + lx), (double)(cy + ly), (double)(cz + lz)};
+                lat[a] = __dadd_rn(lat[a], t);
+                double *o = verts + 3 * (g.vert_base + S.vb[0][cc] + rk);
+                o[0] = world(g.origin[0], lat[0], g.spacing[0]);
+                o[1] = world(g.origin[1], lat[1], g.spacing[1]);
+                o[2] = world(g.origin[2], lat[2], g.spacing[2]);
             }
         }
     }
