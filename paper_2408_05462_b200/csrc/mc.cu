@@ -1099,19 +1099,27 @@ __global__ void __launch_bounds__(E3W * 32, 4) k_mc_emit3(const double *__restri
                 return col;
             };
             const int64_t tout = 3 * (g.tri_base + tbase);
-            for (int i = lane; i < 3 * ptri; i += 32) {
-                const int ti = i / 3;
+            for (int ti = lane; ti < ptri; ti += 32) {  // lane per triangle, its three corners
                 const int col = find(S.tofs, ti);
-                const int sl = i - 3 * S.tofs[col];
                 const int cc = col + 1;
                 const int cx = x0 + col;
                 const int code = S.code[0][cc];
-                const int info = s_cinfo[s_tri[code][sl]][bflags(cx, cy, cz)];
-                const int dx = info & 1, r = (info >> 1) & 3, e2 = info >> 3;
-                const int ocode = S.code[r][cc - dx];
-                const int of = bflags(cx - dx, cy - (r & 1), cz - (r >> 1));
-                const int64_t vid = S.vb[r][cc - dx] + __ldg(&T->rank[ocode][of][e2]);
-                tris[tout + i] = (int32_t)(g.vert_base + vid);
+                const int f = bflags(cx, cy, cz);
+                const int8_t *trow = s_tri[code] + 3 * (ti - S.tofs[col]);
+                int32_t out3[3];
+#pragma unroll
+                for (int q = 0; q < 3; ++q) {
+                    const int info = s_cinfo[trow[q]][f];
+                    const int dx = info & 1, r = (info >> 1) & 3, e2 = info >> 3;
+                    const int ocode = S.code[r][cc - dx];
+                    const int of = bflags(cx - dx, cy - (r & 1), cz - (r >> 1));
+                    const int64_t vid = S.vb[r][cc - dx] + __ldg(&T->rank[ocode][of][e2]);
+                    out3[q] = (int32_t)(g.vert_base + vid);
+                }
+                int32_t *o = tris + tout + 3 * (int64_t)ti;
+                o[0] = out3[0];
+                o[1] = out3[1];
+                o[2] = out3[2];
             }
             for (int j = lane; j < pvert; j += 32) {
                 const int col = find(S.ex, j);
