@@ -146,7 +146,7 @@ def kernel_bytes(name, info, N):
         "k_lorenzo": info["c_sel"] + 8 * info["n_sel"],
         "k_mc_mask": 8 * info["n_sel"] + info["n_sel"] // 8,
         "k_mc_count3": info["n_sel"] // 8,
-        "k_mc_emit2": info["n_sel"] // 8 + 16 * info["nvert"] + 24 * info["nvert"] + 12 * info["ntri"],
+        "k_mc_emit3": info["n_sel"] // 8 + 16 * info["nvert"] + 24 * info["nvert"] + 12 * info["ntri"],
     }
     return table.get(name)
 
