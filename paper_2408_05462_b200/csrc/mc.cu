@@ -112,7 +112,8 @@ static const McTables *mc_tables_device() {
 
 struct McGrid {
     uint64_t goff;
-    int32_t nx, ny, nz, ncx, ncy, ncz, ntx, pad;
+    int32_t nx, ny, nz, ncx, ncy, ncz, ntx;
+    uint32_t ncy_magic;             // ceil(2^32 / ncy): rr / ncy by __umulhi (+ one correction)
     double origin[3], spacing[3];
     int64_t piece_base, npieces, chunk_base, nchunks, item_base;
     int64_t tri_base, vert_base;    // in the merged output (device scan)
@@ -859,6 +860,7 @@ constexpr int E3W = 8;  // warps per CTA
 struct E3Warp {
     McGrid g;             // grid of the warp's current batch
     uint64_t m[9];        // row masks, bit c <-> x0 - 1 + c; index 3 * (dz + 1) + (dy + 1)
+    int64_t rb[5];        // vertex base of slot r's piece (r < 4), own triangle base (4)
     uint32_t h[9];
     int64_t vb[4][66];    // vertex base of cell column c (c = 0: halo x0 - 1)
     int32_t tofs[64];     // own row: triangle offset of each cell within the piece
@@ -921,7 +923,9 @@ __global__ void __launch_bounds__(E3W * 32, 4) k_mc_emit3(const double *__restri
         const int lp = (int)(gpiece - g.piece_base);  // < 2^31 (checked on the host)
         const int rr = g.ntx == 1 ? lp : lp / g.ntx;
         const int xt = lp - rr * g.ntx;
-        cz = rr / g.ncy;
+        int q = g.ncy == 1 ? rr : (int)__umulhi((uint32_t)rr, g.ncy_magic);  // rr / ncy
+        if (q * g.ncy > rr) --q;  // the estimate is exact or one too high
+        cz = q;
         cy = rr - cz * g.ncy;
         x0 = xt * MTX;
     };
@@ -1002,12 +1006,11 @@ __global__ void __launch_bounds__(E3W * 32, 4) k_mc_emit3(const double *__restri
                 S.m[lane] = f.m;
                 S.h[lane] = f.mx;
             }
+            if (lane < 5) S.rb[lane] = f.rb;
             if (src >= 0) nf = fetch(p0 + src);
             const int64_t rb = f.rb;
             __syncwarp();
-            int64_t rbr[5];
-#pragma unroll
-            for (int r = 0; r < 5; ++r) rbr[r] = __shfl_sync(0xFFFFFFFFu, rb, r);
+            const int64_t *rbr = S.rb;  // broadcast reads
             // ---- codes of the four row slots: lane owns columns c = 1 + 2 lane, 2 + 2 lane.
             //      Bits c..c+2 of each of the nine row masks, taken once with
             //      fixed shifts, give both cells' corner pairs.
@@ -1190,6 +1193,7 @@ static bool mc_build(const chr_mc_grid_t *h, int64_t n, McPlan &pl) {
         g.ncy = g.ny - 1;
         g.ncz = g.nz - 1;
         g.ntx = (int32_t)ceil_div(g.ncx, MTX);
+        g.ncy_magic = g.ncy > 1 ? (uint32_t)(((uint64_t(1) << 32) + (uint64_t)g.ncy - 1) / (uint64_t)g.ncy) : 0u;
         for (int a = 0; a < 3; ++a) {
             g.origin[a] = h[i].origin[a];
             g.spacing[a] = h[i].spacing[a];
