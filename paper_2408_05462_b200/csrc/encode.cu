@@ -983,7 +983,7 @@ struct EncPlan {
     uint32_t *qz, *escbits;
 };
 
-static bool build_plan(const chr_region_t *h, int64_t nreg, EncPlan &pl) {
+static bool build_plan_uncached(const chr_region_t *h, int64_t nreg, EncPlan &pl) {
     pl.regs.resize(nreg);
     int64_t item = 0, piece = 0, chunk = 0;
     for (int64_t r = 0; r < nreg; ++r) {
@@ -1037,6 +1037,30 @@ static bool build_plan(const chr_region_t *h, int64_t nreg, EncPlan &pl) {
     pl.nitems = item;
     pl.npieces_total = piece;
     pl.nchunks = chunk;
+    return true;
+}
+
+// The pipeline asks for the workspace size and then compresses with the same
+// region table: the host plan of the last table is kept per thread (the table
+// is compared byte for byte, ~3 us, instead of rebuilt, ~25 us at 426 regions).
+static bool build_plan(const chr_region_t *h, int64_t nreg, EncPlan &pl) {
+    struct Cache {
+        std::vector<chr_region_t> key;
+        EncPlan plan;
+        bool valid = false;
+    };
+    thread_local Cache C;
+    if (pl.portions) return build_plan_uncached(h, nreg, pl);
+    if (C.valid && (int64_t)C.key.size() == nreg &&
+        std::memcmp(C.key.data(), h, sizeof(chr_region_t) * (size_t)nreg) == 0) {
+        pl = C.plan;
+        return true;
+    }
+    C.valid = false;
+    if (!build_plan_uncached(h, nreg, pl)) return false;
+    C.key.assign(h, h + nreg);
+    C.plan = pl;
+    C.valid = true;
     return true;
 }
 
