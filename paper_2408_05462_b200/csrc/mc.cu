@@ -14,12 +14,12 @@
 //   (owned crossing edges in earlier cells) + (its first-appearance rank in
 //   the owner's triangle row), and both come from tables + one scan.
 //
-//   k_mc_count2  CTA = 64 cells x 8 rows x MZC planes: triangles and owned
-//                vertices per 64-cell row piece (ballot row masks)
-//   k_mc_reduce / k_mc_grids / k_mc_down   chunked exclusive scans
-//   k_mc_emit2   same tiles plus a halo row, column and plane, so every
-//                owner cell's (code, vertex base) is local; the active
-//                cells of a row expand into dense per-lane work items.
+//   k_mc_count3  warp per 64-cell row piece (persistent warps on a batch
+//                queue): triangles and owned vertices from the inside masks
+//   k_mc_reduce / k_mc_grid_scan / k_mc_grids / k_mc_down   chunked scans
+//   k_mc_emit3   warp per LIVE row piece: codes + vertex bases of the own row
+//                and the three owner rows from nine row masks, then a lane per
+//                triangle and a lane per owned vertex
 #include <algorithm>
 #include <cstring>
 #include <mutex>
@@ -584,271 +584,6 @@ __global__ void __launch_bounds__(256) k_mc_count3(const McGrid *__restrict__ G,
     }
 }
 
-// emit: samples rows y0-1..y0+8 x columns x0-1..x0+64 (66) per plane in a
-// 3-deep ring; cells rows y0-1..y0+7 x columns x0-1..x0+63 (65) with their
-// (code, vertex base) in a 3-deep ring, so every owner is local.
-constexpr int EW = 10;  // warps: sample rows y0-1 .. y0+8
-__global__ void __launch_bounds__(EW * 32, 4) k_mc_emit2(const double *__restrict__ grids, const McGrid *__restrict__ G,
-                                                      const int32_t *__restrict__ item_grid, double k,
-                                                      const McTables *__restrict__ T,
-                                                      const McPieceBase *__restrict__ base,
-                                                      const McPieceCnt *__restrict__ cnt,
-                                                      const uint32_t *__restrict__ mask,
-                                                      double *__restrict__ verts, int32_t *__restrict__ tris) {
-    __shared__ uint64_t mk[3][EW];
-    __shared__ uint32_t mkx[3][EW];
-    __shared__ uint8_t sC[3][EW - 1][65];
-    __shared__ int64_t sV[3][EW - 1][65];
-    // per cell row, double-buffered by plane parity (written in A, read in B):
-    __shared__ int32_t sT[2][EW - 1][64];   // triangle offset of each cell within its piece
-    __shared__ int32_t sEx[2][EW - 1][64];  // exclusive item offset of each cell within its row
-    __shared__ int32_t sTot[2][EW];         // items per emitting row (index 0 unused)
-    __shared__ int64_t sPT[2][EW - 1];      // triangle base of the row's piece
-    __shared__ __align__(16) int8_t s_tri[256][16];
-    __shared__ __align__(16) uint8_t s_ntri[256];
-    __shared__ __align__(16) uint8_t s_own[256][8];
-    __shared__ McGrid g;
-    {  // tables -> shared memory, 16 bytes per thread
-        const uint4 *src = reinterpret_cast<const uint4 *>(T->tri);
-        uint4 *dst = reinterpret_cast<uint4 *>(&s_tri[0][0]);
-        for (int i = threadIdx.x; i < 256; i += blockDim.x) dst[i] = __ldg(src + i);
-        const uint4 *so = reinterpret_cast<const uint4 *>(T->owncnt);
-        uint4 *d_o = reinterpret_cast<uint4 *>(&s_own[0][0]);
-        for (int i = threadIdx.x; i < 128; i += blockDim.x) d_o[i] = __ldg(so + i);
-        const uint4 *sn = reinterpret_cast<const uint4 *>(T->ntri);
-        uint4 *dn = reinterpret_cast<uint4 *>(s_ntri);
-        if (threadIdx.x < 16) dn[threadIdx.x] = __ldg(sn + threadIdx.x);
-    }
-    // per (edge, boundary flags): the owner cell's offset (bit d set: -1 along
-    // d) and the edge's id in the owner; per edge: axis + low corner
-    __shared__ uint8_t s_cinfo[12][8], s_vinfo[12];
-    if (threadIdx.x < 96) {
-        const int e = threadIdx.x >> 3, f = threadIdx.x & 7;
-        const int a = T->edge_axis[e];
-        int l[3] = {T->edge_low[e][0], T->edge_low[e][1], T->edge_low[e][2]};
-        int d = 0;
-        for (int k = 0; k < 3; ++k)
-            if (k != a && l[k] == 0 && !((f >> k) & 1)) {
-                d |= 1 << k;
-                l[k] = 1;
-            }
-        s_cinfo[e][f] = (uint8_t)(d | (T->edge_id[a][l[0]][l[1]][l[2]] << 3));
-        if (f == 0) s_vinfo[e] = (uint8_t)(a | (T->edge_low[e][0] << 2) | (T->edge_low[e][1] << 3) | (T->edge_low[e][2] << 4));
-    }
-    const int64_t item = blockIdx.x;
-    coop_copy(&g, G + __ldg(item_grid + item));
-    __syncthreads();
-    const int nyt = (g.ncy + MTY - 1) / MTY;
-    const int64_t local = item - g.item_base;
-    const int xt = (int)(local % g.ntx);
-    const int64_t r2 = local / g.ntx;
-    const int yt = (int)(r2 % nyt), zc = (int)(r2 / nyt);
-    const int x0 = xt * MTX, y0 = yt * MTY, z0 = zc * MZC;
-    const int z1 = min(z0 + MZC, g.ncz);
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const double *gp = grids + g.goff;
-    const int64_t nxy = (int64_t)g.nx * g.ny;
-    // cell row of this warp (w < 9): cy = y0 - 1 + w ; cells c = 1 + lane, 33 + lane, and c = 0 (lane 0)
-    const int cy = y0 - 1 + w;
-    const bool crow = w < EW - 1 && cy >= 0 && cy < g.ncy;
-    const int pstart = z0 > 0 ? z0 - 1 : 0;
-    const int64_t pb_row = g.piece_base + (int64_t)cy * g.ntx + xt;  // + cz * ncy * ntx
-    const int64_t pb_step = (int64_t)g.ncy * g.ntx;
-    McPieceBase pnext;  // piece base of the next cell plane (prefetched)
-    pnext.tri = 0;
-    pnext.vert = 0;
-    McPieceCnt cnext;
-    cnext.tri = 0;
-    cnext.vert = 0;
-    if (crow) {
-        pnext = base[pb_row + (int64_t)pstart * pb_step];
-        cnext = cnt[pb_row + (int64_t)pstart * pb_step];
-    }
-    // row masks of the EW sample rows, columns x0-1 .. x0+64 (bit c <-> x0 - 1
-    // + c): lane r of warp 0 reads row y0 - 1 + r from the plane masks one
-    // plane ahead (one warp instruction stream for all rows)
-    const uint32_t *mbase = mask + g.mask_off;
-    const int my = y0 - 1 + lane;
-    const bool mrow = w == 0 && lane < EW && my >= 0 && my < g.ny;
-    auto row_mask = [&](int p, uint64_t &m, uint32_t &mx) {
-        m = 0;
-        mx = 0;
-        if (!mrow) return;
-        const uint32_t *mp = mbase + (int64_t)p * g.pw;
-        const int64_t b = (int64_t)my * g.nx + x0;
-        if (x0 > 0) {
-            mask_bits66(mp, b - 1, m, mx);
-        } else {
-            uint64_t m1;
-            uint32_t h1;
-            mask_bits66(mp, b, m1, h1);
-            m = m1 << 1;
-            mx = (uint32_t)(m1 >> 63) | ((h1 & 1u) << 1);
-        }
-    };
-    // One barrier per plane.  Iteration p: (A) warp 0 stores the masks of
-    // plane p+1 (ring slot (p+1)%3, last read in A of p-1, before the
-    // previous barrier); every row computes codes / vertex bases of cell
-    // plane cz = p-1 into ring slot cz%3 (read by B of p-1 only through
-    // slots (p-2)%3 and (p-3)%3); barrier; (B) emission of plane cz.
-    uint64_t nm = 0;
-    uint32_t nmx = 0;
-    if (w == 0) {
-        row_mask(pstart, nm, nmx);
-        if (lane < EW) {
-            mk[pstart % 3][lane] = nm;
-            mkx[pstart % 3][lane] = nmx;
-        }
-        if (pstart < z1) row_mask(pstart + 1, nm, nmx);
-    }
-    for (int p = pstart; p <= z1; ++p) {
-        if (w == 0 && p < z1) {
-            if (lane < EW) {
-                mk[(p + 1) % 3][lane] = nm;
-                mkx[(p + 1) % 3][lane] = nmx;
-            }
-            if (p + 1 < z1) row_mask(p + 2, nm, nmx);
-        }
-        const bool codes = p > pstart;  // needs planes cz and cz+1
-        const int cz = p - 1, cb = (cz + 3) % 3, qb = p % 3, pp = cz & 1;
-        // ---- codes, owned counts, vertex bases of cell row cy at plane cz
-        int codeA = 0, codeB = 0, ntA = 0, ntB = 0, tA = 0, tB = 0, ownA = 0, ownB = 0, exA = 0, exB = 0;
-        int rowtot = 0;
-        const McPieceBase pbase = pnext;
-        const McPieceCnt pcnt = cnext;
-        if (codes && crow && cz + 1 < z1) {
-            pnext = base[pb_row + (int64_t)(cz + 1) * pb_step];
-            cnext = cnt[pb_row + (int64_t)(cz + 1) * pb_step];
-        }
-        if (codes && w < EW - 1) {
-            int codeH = 0, ownH = 0;
-            uint64_t m00 = 0, m10 = 0, m01 = 0, m11 = 0;
-            uint32_t h00 = 0, h10 = 0, h01 = 0, h11 = 0;
-            bool live = false;
-            if (crow) {
-                m00 = mk[cb][w], m10 = mk[cb][w + 1], m01 = mk[qb][w], m11 = mk[qb][w + 1];
-                h00 = mkx[cb][w], h10 = mkx[cb][w + 1], h01 = mkx[qb][w], h11 = mkx[qb][w + 1];
-                if (x0 > 0) {
-                    codeH = code_fast(m00, h00, m10, h10, m01, h01, m11, h11, 0);
-                    ownH = s_own[codeH][bflags(x0 - 1, cy, cz)];
-                }
-                // a row with no triangles (its halo cell included) is never an
-                // owner of a crossing edge, so nothing of it is looked up
-                live = pcnt.tri > 0 || s_ntri[codeH] > 0;
-            }
-            if (live) {
-                const int xA = x0 + lane, xB = x0 + 32 + lane;
-                if (xA < g.ncx) {
-                    codeA = code_fast(m00, h00, m10, h10, m01, h01, m11, h11, lane + 1);
-                    ownA = s_own[codeA][bflags(xA, cy, cz)];
-                    ntA = s_ntri[codeA];
-                }
-                if (xB < g.ncx) {
-                    codeB = code_fast(m00, h00, m10, h10, m01, h01, m11, h11, lane + 33);
-                    ownB = s_own[codeB][bflags(xB, cy, cz)];
-                    ntB = s_ntri[codeB];
-                }
-            // one scan of packed (owned | triangles << 16) for columns lane and 32 + lane
-            uint32_t pA = (uint32_t)ownA | ((uint32_t)ntA << 16), pB = (uint32_t)ownB | ((uint32_t)ntB << 16);
-#pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {
-                const uint32_t a = __shfl_up_sync(0xFFFFFFFFu, pA, off), b = __shfl_up_sync(0xFFFFFFFFu, pB, off);
-                if (lane >= off) {
-                    pA += a;
-                    pB += b;
-                }
-            }
-            const uint32_t totP = __shfl_sync(0xFFFFFFFFu, pA, 31);
-            pA -= (uint32_t)ownA | ((uint32_t)ntA << 16);  // exclusive
-            pB += totP - ((uint32_t)ownB | ((uint32_t)ntB << 16));
-            const int sA = (int)(pA & 0xFFFFu) + ownA, sB = (int)(pB & 0xFFFFu) + ownB - (int)(totP & 0xFFFFu);
-            const int totV = (int)(totP & 0xFFFFu);
-            tA = (int)(pA >> 16);
-            tB = (int)(pB >> 16);
-            exA = 3 * tA + (int)(pA & 0xFFFFu);  // item offsets (3 per triangle + owned vertices)
-            exB = 3 * tB + (int)(pB & 0xFFFFu);
-            rowtot = __shfl_sync(0xFFFFFFFFu, exB + 3 * ntB + ownB, 31);
-            sC[cb][w][1 + lane] = (uint8_t)codeA;
-            sC[cb][w][33 + lane] = (uint8_t)codeB;
-            sV[cb][w][1 + lane] = pbase.vert + sA - ownA;
-            sV[cb][w][33 + lane] = pbase.vert + totV + sB - ownB;
-            sT[pp][w][lane] = tA;
-            sT[pp][w][32 + lane] = tB;
-            sEx[pp][w][lane] = exA;
-            sEx[pp][w][32 + lane] = exB;
-            if (lane == 0) {
-                sC[cb][w][0] = (uint8_t)codeH;
-                sV[cb][w][0] = pbase.vert - ownH;
-            }
-            }
-            if (lane == 0) {  // only rows y0 .. y0+7 of planes z0 .. z1-1 emit
-                sTot[pp][w] = (w >= 1 && crow && cz >= z0) ? rowtot : 0;
-                sPT[pp][w] = pbase.tri;
-            }
-        }
-        __syncthreads();
-        if (!codes || cz < z0) continue;
-        // ---- emission, balanced over ALL warps of the CTA (a dense surface
-        //      makes rows very unequal; a per-row warp left the others at the
-        //      next barrier): the plane's items (3 per triangle, then one per
-        //      owned vertex, row after row) are dealt out 32 per warp step; an
-        //      item finds its row in the 8 row totals and its cell by a binary
-        //      search over the row's 64 offsets
-        int rowpre[EW - 1];
-        int total = 0;
-#pragma unroll
-        for (int r = 1; r < EW - 1; ++r) {
-            rowpre[r] = total;
-            total += sTot[pp][r];
-        }
-        for (int i = w * 32 + lane; i < total; i += EW * 32) {
-            int rw = 1;
-#pragma unroll
-            for (int r = 2; r < EW - 1; ++r)
-                if (rowpre[r] <= i) rw = r;
-            const int li = i - rowpre[rw];
-            const int32_t *exr = sEx[pp][rw];
-            int col = 0;
-#pragma unroll
-            for (int step = 32; step; step >>= 1)
-                if (col + step < 64 && exr[col + step] <= li) col += step;
-            const int sl = li - exr[col];
-            const int c = col + 1;  // cell column in the 65-wide ring
-            const int cx = x0 + col, ry = y0 - 1 + rw;
-            const int code = sC[cb][rw][c];
-            const int nt = s_ntri[code];
-            const int f = bflags(cx, ry, cz);
-            if (sl < 3 * nt) {
-                // triangle corner: vertex id of its edge, held by the owner cell
-                const int info = s_cinfo[s_tri[code][sl]][f];
-                const int d0 = -(info & 1), d1 = -((info >> 1) & 1), d2 = -((info >> 2) & 1);
-                const int e2 = info >> 3;
-                const int ob = d2 ? (cb == 0 ? 2 : cb - 1) : cb;
-                const int ocode = sC[ob][rw + d1][c + d0];
-                const int of = bflags(cx + d0, ry + d1, cz + d2);
-                const int64_t vid = sV[ob][rw + d1][c + d0] + __ldg(&T->rank[ocode][of][e2]);
-                tris[3 * (g.tri_base + sPT[pp][rw] + sT[pp][rw][col]) + sl] = (int32_t)(g.vert_base + vid);
-            } else {
-                // owned vertex of rank r: interpolate along its edge
-                const int r = sl - 3 * nt;
-                const int vi = s_vinfo[__ldg(&T->inv[code][f][r])];
-                const int a = vi & 3, lx = (vi >> 2) & 1, ly = (vi >> 3) & 1, lz = (vi >> 4) & 1;
-                const double *sp = gp + (int64_t)(cz + lz) * nxy + (int64_t)(ry + ly) * g.nx + (cx + lx);
-                const double s0 = __ldg(sp);
-                const double s1 = __ldg(sp + (a == 0 ? 1 : (a == 1 ? (int64_t)g.nx : nxy)));
-                const double den = __dadd_rn(s1, -s0);
-                const double t = den == 0.0 ? 0.0 : __ddiv_rn(__dadd_rn(k, -s0), den);
-                double lat[3] = {(double)(cx + lx), (double)(ry + ly), (double)(cz + lz)};
-                lat[a] = __dadd_rn(lat[a], t);
-                double *o = verts + 3 * (g.vert_base + sV[cb][rw][c] + r);
-                o[0] = world(g.origin[0], lat[0], g.spacing[0]);
-                o[1] = world(g.origin[1], lat[1], g.spacing[1]);
-                o[2] = world(g.origin[2], lat[2], g.spacing[2]);
-            }
-        }
-    }
-}
-
 // emit v3: warp per LIVE row piece (triangles > 0), CTA per scan chunk.  The
 // surface touches ~3 % of the cells (c3: a third of the row pieces), so the
 // work is proportional to live pieces, not to the tile volume.  A piece
@@ -995,7 +730,6 @@ __global__ void __launch_bounds__(E3W * 32, 4) k_mc_emit3(const double *__restri
         Fetch nf = fetch(p0 + src);
         while (src >= 0) {
             const Fetch f = nf;
-            const int64_t gpiece = p0 + src;
             const int ptri = __shfl_sync(0xFFFFFFFFu, cur_cnt.tri, src);
             const int pvert = __shfl_sync(0xFFFFFFFFu, cur_cnt.vert, src);
             const int cy = f.cy, cz = f.cz, x0 = f.x0;
