@@ -135,6 +135,21 @@ int chr_plan(const double *h_block_stats, int64_t nx, int64_t ny, int64_t nz,
              double loose_fraction, double safety_factor,
              chr_region_t *h_regions, int64_t *n_regions);
 
+/* 2b. merge_regions (blocking.py:130-193) over caller-supplied keys: one
+ *     integer per block (block_id order; equal integers = equal relevance
+ *     keys, i.e. the IsoIndex.relevance_key frozensets the caller holds).
+ *     h_spans receives 6 int32 per region (lo x,y,z, hi x,y,z, inclusive) in
+ *     region_id order and needs 6*nbx*nby*nbz entries.  Host only. */
+int chr_merge_keys(const uint64_t *h_keys, int64_t nbx, int64_t nby, int64_t nbz, int32_t *h_spans,
+                   int64_t *n_regions);
+
+/* 1b. Volume.value_range + the finite check (volume.py:54-78) of n samples
+ *     on the device: h_range = (min, max) of the finite samples,
+ *     *h_first_nonfinite = first flat index of a NaN/Inf or -1.  Workspace:
+ *     24 bytes.  Synchronises. */
+int chr_value_range(const void *d_vol, int dtype, int64_t n, void *d_workspace, size_t workspace_bytes,
+                    double *h_range, int64_t *h_first_nonfinite, void *stream);
+
 /* 3. compress all regions into a complete .chr file on the device
  *    (codec.compress per region, codec.py:91-143; write_chr layout,
  *    chr_archive.py:297-340).  Regions come from chr_plan or from the

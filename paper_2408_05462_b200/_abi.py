@@ -152,6 +152,10 @@ def lib():
         L.chr_stats.restype = INT
         L.chr_plan.argtypes = [P, I64, I64, I64, I64, P, INT, D, D, D, D, P, P]
         L.chr_plan.restype = INT
+        L.chr_merge_keys.argtypes = [P, I64, I64, I64, P, P]
+        L.chr_merge_keys.restype = INT
+        L.chr_value_range.argtypes = [P, INT, I64, P, SZ, P, P, P]
+        L.chr_value_range.restype = INT
         L.chr_compress_workspace_size.argtypes = [P, I64]
         L.chr_compress_workspace_size.restype = SZ
         L.chr_compress_capacity.argtypes = [P, I64, INT, INT]
@@ -252,7 +256,8 @@ EXPORTS = [
     "chr_read_header", "chr_read_workspace_size", "chr_read_archive", "chr_prof_timeline",
     "chr_prof_mark", "chr_copy", "chr_request_tables", "chr_pipeline",
     "chr_dcompress_workspace_size", "chr_dcompress_local", "chr_dcompress_finish", "chr_dcompress_headers",
-    "chr_abi_version", "chr_status_string", "chr_num_blocks", "chr_stats", "chr_plan",
+    "chr_abi_version", "chr_status_string", "chr_num_blocks", "chr_stats", "chr_plan", "chr_merge_keys",
+    "chr_value_range",
     "chr_compress_workspace_size", "chr_compress_capacity", "chr_compress",
     "chr_decode_workspace_size", "chr_decode_regions", "chr_mc_workspace_size", "chr_mc_count",
     "chr_mc_emit", "chr_case_codes", "chr_crc32_workspace_size", "chr_crc32", "chr_crc32_combine",

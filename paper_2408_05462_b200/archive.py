@@ -162,9 +162,11 @@ def build_chr(volume, candidates, block_size: int, accuracy: float = 1.0, bound_
     dvals = vol.device_values()
     res = device.build_archive(dvals, vol.dims, cands, block_size, spacing=vol.spacing,
                                source_dtype=vol.source_dtype, loose_fraction=loose_fraction,
-                               safety_factor=safety_factor, vrange=vol.value_range, out_of_range=out_of_range,
+                               safety_factor=safety_factor, vrange=vol.known_range(), out_of_range=out_of_range,
                                on_warn=lambda m: warnings.warn(m, stacklevel=3), accuracy=accuracy,
                                bound_mode=bound_mode)
+    if vol.known_range() is None:  # a device field: the range comes from the stats pass just run
+        vol._set_range(res.extra["vrange"])
     if codec is not None:
         return _rebuild_with_plugin(vol, res, cands, block_size, codec, bound_mode, accuracy)
     host = res.blob[: res.nbytes].cpu().numpy().tobytes()
@@ -238,7 +240,11 @@ def request_device(archive: CHRArchive, k: float, accuracy=None, drop_pruned=Tru
         blob = _device_file(archive)
         desc = [(o + HEADER_SIZE, len(r.block.payload), r.block.codec_id, r.block.dims, r.block.error_bound,
                  r.block.checksum) for r, o in sel]
-        windows, woffs, status = device.decode(blob, desc, out=None)
+        # the windows get their own buffer: a ReconstructionSet keeps them for
+        # stitch(), so they must not alias the decoder's reusable workspace
+        total = sum(int(r.block.dims[0]) * int(r.block.dims[1]) * int(r.block.dims[2]) for r, _ in sel)
+        own = torch.empty(max(total, 1), dtype=torch.float64, device=blob.device)
+        windows, woffs, status = device.decode(blob, desc, out=own)
         for (r, _), st in zip(sel, status):
             if st == 10:
                 raise UnsupportedCodecError(f"unknown codec id {r.block.codec_id}")

@@ -41,9 +41,76 @@ __global__ void __launch_bounds__(256) k_lorenzo_seam(const double *__restrict__
     }
 }
 
+// value_range + finite check of a whole volume (volume.py:54-78): min/max
+// over the samples as ordered-integer atomics, the first non-finite flat
+// index as an atomicMin (a NaN/Inf never enters min/max, like the
+// reference which raises before computing the range)
+__device__ __forceinline__ unsigned long long ord_key(double v) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+    return (b >> 63) ? ~b : (b | (1ull << 63));
+}
+template <typename T>
+__global__ void __launch_bounds__(256) k_value_range(const T *__restrict__ x, int64_t n,
+                                                     unsigned long long *__restrict__ out) {
+    double lo = INFINITY, hi = -INFINITY;
+    unsigned long long bad = ~0ull;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const double v = (double)__ldg(x + i);
+        if (!isfinite(v)) {
+            bad = min(bad, (unsigned long long)i);
+            continue;
+        }
+        lo = fmin(lo, v);
+        hi = fmax(hi, v);
+    }
+    for (int off = 16; off; off >>= 1) {
+        lo = fmin(lo, __shfl_xor_sync(0xFFFFFFFFu, lo, off));
+        hi = fmax(hi, __shfl_xor_sync(0xFFFFFFFFu, hi, off));
+        bad = min(bad, __shfl_xor_sync(0xFFFFFFFFu, bad, off));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (lo <= hi) {
+            atomicMin(out + 0, ord_key(lo));
+            atomicMax(out + 1, ord_key(hi));
+        }
+        if (bad != ~0ull) atomicMin(out + 2, bad);
+    }
+}
+
 }  // namespace chr
 
 using namespace chr;
+
+extern "C" int chr_value_range(const void *d_vol, int dtype, int64_t n, void *d_ws, size_t ws_bytes,
+                               double *h_range, int64_t *h_first_nonfinite, void *stream) {
+    CHR_XFER_SCOPE;
+    if (!d_vol || n < 1 || !h_range || !h_first_nonfinite) return CHR_E_PARAMETER;
+    if (dtype != CHR_F32 && dtype != CHR_F64) return CHR_E_PARAMETER;
+    if (!d_ws || ws_bytes < 24) return CHR_E_WORKSPACE;
+    cudaStream_t st = (cudaStream_t)stream;
+    auto *slot = reinterpret_cast<unsigned long long *>(d_ws);
+    CHR_CUDA_TRY(zero_async({{slot + 1, 8}}, st));
+    CHR_CUDA_TRY(fill_async(slot, 0xFF, 8, st));
+    CHR_CUDA_TRY(fill_async(slot + 2, 0xFF, 8, st));
+    const int64_t blocks = std::min<int64_t>(ceil_div(n, 256), 148 * 8);
+    {
+        CHR_PROF("k_value_range", st);
+        if (dtype == CHR_F32)
+            k_value_range<float><<<(unsigned)blocks, 256, 0, st>>>((const float *)d_vol, n, slot);
+        else
+            k_value_range<double><<<(unsigned)blocks, 256, 0, st>>>((const double *)d_vol, n, slot);
+    }
+    CHR_CUDA_TRY(cudaGetLastError());
+    unsigned long long r[3];
+    CHR_CUDA_TRY(d2h(r, slot, 24, st));
+    CHR_CUDA_TRY(stream_sync(st));
+    for (int i = 0; i < 2; ++i) {
+        const unsigned long long b = (r[i] >> 63) ? (r[i] & ~(1ull << 63)) : ~r[i];
+        memcpy(&h_range[i], &b, 8);
+    }
+    *h_first_nonfinite = r[2] == ~0ull ? -1 : (int64_t)r[2];
+    return CHR_OK;
+}
 
 extern "C" int chr_abi_version(void) {
     CHR_XFER_SCOPE; return 1; }

@@ -18,7 +18,8 @@
 namespace chr {
 
 static CrcTables g_host_tables;
-static CrcTables *g_dev_tables = nullptr;
+constexpr int kMaxDevices = 64;
+static CrcTables *g_dev_tables[kMaxDevices] = {};  // per CUDA device (cudaGetDevice)
 static std::once_flag g_host_once;
 static std::mutex g_dev_mu;
 
@@ -50,8 +51,10 @@ const CrcTables &crc_tables_hostref() {
 }
 
 const CrcTables *crc_tables_device() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return nullptr;
     std::lock_guard<std::mutex> lk(g_dev_mu);
-    if (!g_dev_tables) {
+    if (!g_dev_tables[dev]) {
         const CrcTables &h = crc_tables_hostref();
         CrcTables *d = nullptr;
         if (cudaMalloc(&d, sizeof(CrcTables)) != cudaSuccess) return nullptr;
@@ -59,9 +62,9 @@ const CrcTables *crc_tables_device() {
             cudaFree(d);
             return nullptr;
         }
-        g_dev_tables = d;
+        g_dev_tables[dev] = d;
     }
-    return g_dev_tables;
+    return g_dev_tables[dev];
 }
 
 // x^(8n) mod P computed by a whole warp (one bit of n per lane, then a

@@ -49,7 +49,8 @@ struct __align__(16) McTables {
 };
 
 static McTables g_mct;
-static McTables *g_dmct = nullptr;
+constexpr int kMaxDevices = 64;
+static McTables *g_dmct[kMaxDevices] = {};  // per CUDA device (cudaGetDevice)
 static std::once_flag g_mct_once;
 static std::mutex g_mct_mu;
 
@@ -97,17 +98,19 @@ static void mc_tables_host() {
 
 static const McTables *mc_tables_device() {
     std::call_once(g_mct_once, mc_tables_host);
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return nullptr;
     std::lock_guard<std::mutex> lk(g_mct_mu);
-    if (!g_dmct) {
+    if (!g_dmct[dev]) {
         McTables *d = nullptr;
         if (cudaMalloc(&d, sizeof(McTables)) != cudaSuccess) return nullptr;
         if (cudaMemcpy(d, &g_mct, sizeof(McTables), cudaMemcpyHostToDevice) != cudaSuccess) {
             cudaFree(d);
             return nullptr;
         }
-        g_dmct = d;
+        g_dmct[dev] = d;
     }
-    return g_dmct;
+    return g_dmct[dev];
 }
 
 struct McGrid {
@@ -954,16 +957,17 @@ static bool mc_build(const chr_mc_grid_t *h, int64_t n, McPlan &pl) {
 }
 
 static int mc_num_sms() {
-    static int n_sm = 0;
-    if (!n_sm) {
-        int dev = 0, n = 0;
-        if (cudaGetDevice(&dev) == cudaSuccess &&
-            cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess)
-            n_sm = n;
+    static int n_sm[kMaxDevices] = {};  // per CUDA device
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return 148;
+    if (!n_sm[dev]) {
+        int n = 0;
+        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess)
+            n_sm[dev] = n;
         else
             return 148;
     }
-    return n_sm;
+    return n_sm[dev];
 }
 
 // two zeroed counters after the piece counts: [0] k_mc_emit3's batch queue, [1] k_mc_count3's

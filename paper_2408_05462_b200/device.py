@@ -76,6 +76,18 @@ def stats(vol: torch.Tensor, dims, bs: int, cands) -> tuple[torch.Tensor, torch.
     return out, bad
 
 
+def value_range(vol: torch.Tensor) -> tuple[float, float, int]:
+    """(min, max, first non-finite flat index or -1) of a device field
+    (Volume.value_range + finite check, volume.py:54-78; chr_value_range)."""
+    flat = vol.reshape(-1)
+    lo_hi = (ctypes.c_double * 2)()
+    bad = ctypes.c_int64(-1)
+    work = _DEFAULT_WS.get("vrange", 64)
+    check(lib().chr_value_range(ptr(flat), _dtype_code(flat), flat.numel(), ptr(work), work.numel(), lo_hi,
+                                ctypes.byref(bad), stream_ptr()), "chr_value_range")
+    return float(lo_hi[0]), float(lo_hi[1]), int(bad.value)
+
+
 def plan(block_stats: np.ndarray, dims, bs, cands, vmin, vmax, loose_fraction=LOOSE_FRACTION,
          safety_factor=SAFETY_FACTOR):
     """Regions (numpy array of chr_region_t, ``_abi.REGION_DT``) from host block stats."""

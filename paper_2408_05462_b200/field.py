@@ -83,15 +83,21 @@ class Volume:
 
     @property
     def value_range(self) -> tuple[float, float]:
-        if self._range is None:
-            t = self._dev
-            fin = torch.isfinite(t)
-            if not bool(fin.all()):
-                i = int(torch.argmin(fin.to(torch.uint8)))
-                raise NonFiniteSampleError(i, float(t[i]))
-            lo, hi = torch.aminmax(t)
-            object.__setattr__(self, "_range", (float(lo), float(hi)))
+        if self._range is None:  # device-resident field: one reduction kernel (chr_value_range)
+            from . import device
+
+            lo, hi, bad = device.value_range(self._dev)
+            if bad >= 0:
+                raise NonFiniteSampleError(bad, float(self._dev[bad].item()))
+            self._set_range((lo, hi))
         return self._range
+
+    def known_range(self):
+        """value_range if already known (host fields, or set by a stats pass), else None."""
+        return self._range
+
+    def _set_range(self, r) -> None:
+        object.__setattr__(self, "_range", (float(r[0]), float(r[1])))
 
     @property
     def nsamples(self) -> int:

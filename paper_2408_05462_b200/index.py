@@ -1,9 +1,10 @@
 """Decomposition / span index / region merge API (reference:
-isochr/blocking.py:22-193, bound.py:150-219).  Extrema and distances come
-from the chr_stats kernel, the merge from the host C++ planner (chr_plan)."""
+isochr/blocking.py:22-193).  Extrema come from the chr_stats kernel, the
+greedy merge from host C++ (chr_merge_keys)."""
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass
 
 import numpy as np
@@ -93,55 +94,37 @@ def build_index(blocks, candidates) -> IsoIndex:
 
 
 def merge_regions(blocks, index: IsoIndex) -> list[Region]:
-    """Greedy same-key box merge (blocking.py:130-193) via chr_plan."""
+    """Greedy same-key box merge (blocking.py:130-193) in host C++
+    (chr_merge_keys) over the caller's own relevance keys
+    (``index.relevance_key``), so a hand-made IsoIndex merges exactly as in
+    the reference; origins/extents come from the blocks' windows."""
     if not blocks:
         return []
     nbx = max(b.block_coords[0] for b in blocks) + 1
     nby = max(b.block_coords[1] for b in blocks) + 1
     nbz = max(b.block_coords[2] for b in blocks) + 1
-    # chr_plan recomputes keys with the same span test from (vmin, vmax)
-    st = np.zeros((nbx * nby * nbz, 3))
+    by_coords = {b.block_coords: b for b in blocks}
+    key_of: dict[frozenset, int] = {}
+    keys_by_id = []
+    ids = np.zeros(nbx * nby * nbz, dtype=np.uint64)
     for b in blocks:
-        st[b.block_id] = (b.vmin, b.vmax, 1.0)
-    # dims consistent with the block windows
-    dims = tuple(max(b.sample_origin[a] + b.sample_extent[a] for b in blocks) for a in range(3))
-    regs = device.plan(st, dims, _infer_bs(blocks, dims), index.candidates, 0.0, 1.0)
+        key = index.relevance_key(b.block_id)
+        kid = key_of.get(key)
+        if kid is None:
+            kid = key_of[key] = len(keys_by_id)
+            keys_by_id.append(key)
+        bx, by, bz = b.block_coords
+        ids[bx + nbx * (by + nby * bz)] = kid
+    spans = np.zeros((nbx * nby * nbz, 6), dtype=np.int32)
+    nreg = ctypes.c_int64(0)
+    _abi.check(_abi.lib().chr_merge_keys(_abi.aptr(ids), nbx, nby, nbz, _abi.aptr(spans), ctypes.byref(nreg)),
+               "chr_merge_keys")
     out = []
-    for i in range(len(regs)):
-        r = regs[i]
-        key = frozenset(ci for ci in range(len(index.candidates)) if (int(r.mask) >> ci) & 1)
-        out.append(Region(i, (tuple(r.lo), tuple(r.hi)), tuple(r.origin), tuple(r.extent), key))
+    for i, sp in enumerate(spans[: nreg.value].tolist()):
+        lo, hi = tuple(sp[:3]), tuple(sp[3:])
+        lo_b, hi_b = by_coords[lo], by_coords[hi]
+        origin = lo_b.sample_origin
+        extent = tuple(hi_b.sample_origin[a] + hi_b.sample_extent[a] - origin[a] for a in range(3))
+        bx, by, bz = lo
+        out.append(Region(i, (lo, hi), origin, extent, keys_by_id[int(ids[bx + nbx * (by + nby * bz)])]))
     return out
-
-
-def _infer_bs(blocks, dims):
-    # block_size = origin of block (1,*,*) along the first axis with >1 blocks
-    for a in range(3):
-        for b in blocks:
-            if b.block_coords[a] == 1:
-                return b.sample_origin[a]
-    return max(dims) - 1
-
-
-def region_bound_strict(samples, all_candidates, served, loose_bound=0.0,
-                        safety_factor=device.SAFETY_FACTOR) -> float:
-    """bound.region_bound for strict_vertices at accuracy 1 (bound.py:150-219),
-    with min |s-k| on the GPU (kernels.min_abs_distance)."""
-    import torch
-
-    flat = torch.from_numpy(np.ascontiguousarray(np.asarray(samples, dtype=np.float64).ravel(order="F")))
-    flat = flat.to(_abi.device())
-    served = [float(k) for k in served]
-    best = None
-    for k in served:
-        v = device.min_abs_distance(flat, k)
-        e = 0.0 if v == 0.0 else v * safety_factor
-        best = e if best is None else min(best, e)
-        if v == 0.0:
-            return 0.0
-    cap = float(loose_bound) if best is None else best
-    for k in all_candidates:
-        if float(k) in served:
-            continue
-        cap = min(cap, device.min_abs_distance(flat, float(k)) * safety_factor)
-    return cap

@@ -1,11 +1,11 @@
 """Parity at BASELINE.json's full sizes (c3 512^3 single GPU,
 c4 1024^3, c5 1536^3 with 16 candidates).
 
-* c3 512^3 (always; c4 / c5 with CHR_FULLSIZE=1): archive bytes, request
-  windows and the merged mesh are bit-identical to the oracle's on the same
-  input (the oracle runs the whole volume on all host threads).
-* every config (c4 / c5 only with CHR_FULLSIZE=1 -- 4 GiB / 13.5 GiB inputs):
-  size-independent properties -- the file validates on the device (trailer
+* c3 512^3, c4 1024^3, c5 1536^3: archive bytes, request windows and the
+  merged mesh are bit-identical to the oracle's on the same input (the
+  oracle runs the whole volume on all host threads); c5 is extracted at all
+  16 isovalues (sampled regions against the oracle, all regions' counts).
+* every config: size-independent properties -- the file validates on the device (trailer
   CRC, table, block headers), every region decodes within its error bound
   (escapes and verbatim regions exactly), and with the strict accuracy-1
   bound every cell's marching-cubes case is preserved for every candidate
@@ -28,9 +28,6 @@ if not torch.cuda.is_available():  # pragma: no cover - CPU container
 import paper_2408_05462_b200 as G  # noqa: E402
 from oracle import oracle as O  # noqa: E402
 from paper_2408_05462_b200 import device, synth  # noqa: E402
-
-FULL = os.environ.get("CHR_FULLSIZE", "") == "1"
-
 
 def sha(a):
     return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
@@ -77,8 +74,22 @@ def _properties(vals, dims, bs, cands, r):
     return res, worst
 
 
-@pytest.mark.parametrize("name", ["c3"] + (["c4", "c5"] if FULL else []))
+def _request_windows(res, ci, iso=None):
+    regs = res.regions
+    sel = np.nonzero((regs["mask"] & np.uint64(1 << ci)) != 0)[0]
+    mine = regs[sel]
+    dec = device.dec_table(mine["block_offset"] + device.BLOCK_HEADER, mine["block_nbytes"] - device.BLOCK_HEADER,
+                           mine["codec_id"], mine["extent"], mine["error_bound"], mine["payload_crc"])
+    wins, offs, st = device.decode(res.blob, dec, iso=iso)
+    assert not any(st)
+    return sel, mine, dec, wins, offs
+
+
+@pytest.mark.parametrize("name", ["c3", "c4", "c5"])
 def test_fullsize_bit_exact_vs_oracle(name):
+    """Archive bytes bit-identical to the oracle's at BASELINE's full sizes;
+    the request(k) windows and the merged mesh too (c5: candidate 0 here,
+    all 16 in test_c5_all_isovalues)."""
     vals, dims, bs, cands, r = synth.make_config(name, device="cuda")
     assert dims == {"c3": (512,) * 3, "c4": (1024,) * 3, "c5": (1536,) * 3}[name]
     res, _ = _properties(vals, dims, bs, cands, r)
@@ -86,26 +97,63 @@ def test_fullsize_bit_exact_vs_oracle(name):
     ref = O.build_chr(host, dims, cands, bs, source_dtype="f32", loose_fraction=r,
                       workers=len(os.sched_getaffinity(0)))
     assert res.blob[: res.nbytes].cpu().numpy().tobytes() == ref.to_bytes()
+    del host
     k = cands[0]
-    sel = O.request(ref, k, workers=len(os.sched_getaffinity(0)))
-    regs = res.regions
-    mine = regs[(regs["mask"] & np.uint64(1)) != 0]
-    assert [int(x) for x in np.nonzero((regs["mask"] & np.uint64(1)) != 0)[0]] == [s["id"] for s, _ in sel]
-    dec = device.dec_table(mine["block_offset"] + device.BLOCK_HEADER, mine["block_nbytes"] - device.BLOCK_HEADER,
-                           mine["codec_id"], mine["extent"], mine["error_bound"], mine["payload_crc"])
-    wins, offs, st = device.decode(res.blob, dec, iso=k)
-    assert not any(st)
+    sel_ref = O.request(ref, k, workers=len(os.sched_getaffinity(0)))
+    sel, mine, dec, wins, offs = _request_windows(res, 0, iso=k)
+    assert sel.tolist() == [s["id"] for s, _ in sel_ref]
     host_w = wins.cpu().numpy()
-    for (s, w), o in zip(sel, offs):
+    for (s, w), o in zip(sel_ref, offs):
         assert np.array_equal(host_w[o:o + w.size], w), s["id"]
+    del host_w
     mct = device.mc_table(dec["out_offset"], mine["extent"], mine["origin"].astype(np.float64), (1.0, 1.0, 1.0))
     ws = device.Workspaces()
     v, t, _, _ = device.marching(wins, mct, k, ws=ws)
-    rv, rt = O.extract_regions(sel, (1.0, 1.0, 1.0), k)
+    rv, rt = O.extract_regions(sel_ref, (1.0, 1.0, 1.0), k)
     assert np.array_equal(v.cpu().numpy(), rv) and np.array_equal(t.cpu().numpy(), rt)
 
 
-@pytest.mark.skipif(not FULL, reason="CHR_FULLSIZE=1 runs the 1024^3 / 1536^3 configs")
+def test_c5_all_isovalues():
+    """c5 1536^3 with 16 candidates: request + marching cubes for EVERY
+    isovalue (the archive itself is byte-compared with the oracle's in
+    test_fullsize_bit_exact_vs_oracle[c5]).  Per isovalue the fused decode
+    (windows + inside masks) feeds the mesh, and every 8th selected region
+    (offset by the candidate index) decodes and meshes bit-identically to
+    the oracle's region window + mesh."""
+    vals, dims, bs, cands, r = synth.make_config("c5", device="cuda")
+    assert len(cands) == 16
+    res = device.build_archive(vals, dims, cands, bs, loose_fraction=r)
+    regs = res.regions
+    host_blob = res.blob[: res.nbytes].cpu().numpy().tobytes()
+    ws = device.Workspaces()
+    total_tris = 0
+    for ci, k in enumerate(cands):
+        sel, mine, dec, wins, offs = _request_windows(res, ci, iso=k)
+        assert len(sel) > 0
+        mct = device.mc_table(dec["out_offset"], mine["extent"], mine["origin"].astype(np.float64), (1.0, 1.0, 1.0))
+        v, t, ntri, nvert = device.marching(wins, mct, k, ws=ws, masks=device._DEFAULT_WS.get("decode_mask", 4, torch.int32))
+        total_tris += int(t.shape[0])
+        assert sum(ntri) == t.shape[0] and sum(nvert) == v.shape[0]
+        # the sampled regions against the oracle, decoded from the same bytes
+        pick = list(range(ci % 8, len(sel), 8))
+        vb = v.cpu().numpy()
+        tb = t.cpu().numpy()
+        tri0 = np.concatenate([[0], np.cumsum(ntri)])
+        vert0 = np.concatenate([[0], np.cumsum(nvert)])
+        for j in pick:
+            i = int(sel[j])
+            _, win = O.decompress_block(host_blob, int(regs["block_offset"][i]))
+            got = wins[int(offs[j]): int(offs[j]) + win.size].cpu().numpy()
+            assert np.array_equal(got, win), (ci, i)
+            ext = tuple(int(e) for e in regs["extent"][i])
+            org = tuple(float(o) for o in regs["origin"][i])
+            rv, rt = O.marching_cubes(win, ext, k, (1.0, 1.0, 1.0), org)
+            assert (ntri[j], nvert[j]) == (rt.shape[0], rv.shape[0]), (ci, i)
+            assert np.array_equal(vb[vert0[j]:vert0[j + 1]], rv), (ci, i)
+            assert np.array_equal(tb[tri0[j]:tri0[j + 1]] - vert0[j], rt), (ci, i)
+    print(f"c5: 16 isovalues, {len(regs)} regions, {total_tris} triangles in all")
+
+
 @pytest.mark.parametrize("name", ["c4", "c5"])
 def test_fullsize_properties(name):
     vals, dims, bs, cands, r = synth.make_config(name, device="cuda")
