@@ -63,7 +63,7 @@ def grf(n: int, slope: float, seed: int = 0, kmax: float | None = None, nz: int 
         table[np.arange(table.size) > kmax * kmax] = 0.0
     spec *= table[k2]
     del k2
-    return np.fft.irfftn(spec, s=(nz, n, n))
+    return np.fft.irfftn(spec, s=(nz, n, n), axes=(0, 1, 2))
 
 
 def _minmax01(f: np.ndarray) -> np.ndarray:
