@@ -197,6 +197,25 @@ CHR_HD TokSeg piece_to_seg(const PieceRec &p) {
     return s;
 }
 
+// 16-byte record of a wider stream piece (segment encoder: <= 65535 samples)
+struct PieceRec2 {
+    uint16_t len, lead, trail, nesc;
+    uint32_t bytes;   // literal + internal run bytes
+    uint32_t nz;
+};
+
+CHR_HD TokSeg piece_to_seg(const PieceRec2 &p) {
+    TokSeg s;
+    s.len = p.len;
+    s.lead = p.lead;
+    s.trail = p.trail;
+    s.bytes = p.bytes;
+    s.nesc = p.nesc;
+    s.nz = (int32_t)p.nz;
+    s.f32ok = 1;
+    return s;
+}
+
 // where piece j starts: exclusive-prefix consequences
 struct PieceOff {
     int64_t tok_off;  // token bytes owned by earlier pieces of the region

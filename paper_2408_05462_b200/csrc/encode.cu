@@ -59,6 +59,7 @@ struct RegDev {
     int32_t zhalo, last;
     TokSeg pre;
     int32_t qband, rb;            // quantiser items are full-row bands of rb rows (k_quant_band)
+    int32_t zl, pad_zl;           // segment path: planes per item (k_qseg / k_qemit)
     // results
     int32_t codec, f32ok;
     int64_t tok_len, nesc, payload_len;
@@ -611,9 +612,10 @@ __device__ TokSeg block_excl_scan(TokSeg x, TokSeg *total) {
     return tokseg_combine(wpre, excl);
 }
 
+template <typename Rec>
 __global__ void __launch_bounds__(256) k_scan_reduce(const EncParams *__restrict__ P,
                                                      const RegDev *__restrict__ regs,
-                                                     const PieceRec *__restrict__ recs,
+                                                     const Rec *__restrict__ recs,
                                                      TokSeg *__restrict__ chunk_agg) {
     const int64_t c = blockIdx.x;
     __shared__ int64_t rlo, rhi;
@@ -799,9 +801,10 @@ __global__ void __launch_bounds__(1024) k_layout(const EncParams *__restrict__ P
     }
 }
 
+template <typename Rec>
 __global__ void __launch_bounds__(256) k_scan_down(const EncParams *__restrict__ P,
                                                    const RegDev *__restrict__ regs,
-                                                   const PieceRec *__restrict__ recs,
+                                                   const Rec *__restrict__ recs,
                                                    const TokSeg *__restrict__ chunk_pre,
                                                    PieceOff *__restrict__ poffs) {
     const int64_t c = blockIdx.x;
@@ -963,11 +966,496 @@ __global__ void k_finalize_file(const CrcTables *__restrict__ tabs, const EncSca
     put_le(out + sc->file_body, crc);
 }
 
+// ------------------------------------------------------------------ segment encoder
+// Single-read encoder path (no quantum intermediate in HBM).  An item is a
+// band of whole rows (rb rows + the halo row y0-1) x up to SG_ZMAX planes of
+// one region window, marching z.  The band's rows of one plane are a
+// contiguous piece of the window's raster stream (a segment); warp w owns
+// the slots [w W, (w + 1) W) of it -- a PIECE of the stream:
+//   k_qseg   quantise + Lorenzo q and reduce each piece's token stream to
+//            its summary (the token-size monoid, PieceRec2); nothing per
+//            sample leaves the SM but (rare) escape bits
+//   k_scan_reduce / k_scan_regions / k_scan_down
+//            exclusive prefix of every piece in its region's stream order
+//            (plane, band, warp), codec decision, file layout
+//   k_qemit  recomputes q from the input (the second and last read) and
+//            writes every token byte at its final offset
+// Per plane, phase 1 runs over the band-plane's slots with a block stride
+// (coalesced loads): u, D = u - u(z-1) into shared memory (u(z-1) kept per
+// slot in sU).  Phase 2 gives each lane SG_L consecutive slots: it reads D,
+// forms q = D - D(x-1) - D(y-1) + D(x-1,y-1) and folds its samples into a
+// 32-bit token summary sequentially (a few instructions per sample); lanes
+// combine by one ordered warp reduction (k_qseg) or scan (k_qemit, which
+// then writes its samples' tokens sequentially).  Shared arrays are padded
+// (index i + i/8) so both access patterns are bank-conflict free; D and the
+// escape flags are double-buffered by plane: one barrier per plane.
+constexpr int SG_T = 256;                // threads per item
+constexpr int SG_NW = SG_T / 32;
+constexpr int SG_L = 8;                  // consecutive slots per lane in phase 2
+constexpr int SG_SPAN = 4096;            // max band-plane slots incl. the halo row
+constexpr int SG_TARGET = 2048;          // band height target: (rb + 1) * ex <= SG_TARGET
+constexpr int SG_ZMAX = 16;              // planes per item
+static_assert(SG_SPAN / SG_T <= 32, "phase-1 slot masks are 32-bit");
+
+__device__ __forceinline__ int sp_idx(int i) { return i + (i >> 3); }  // padded shared index
+
+// 32-bit token-size monoid inside one piece (<= SG_SPAN samples)
+struct TS32 {
+    int32_t len, lead, trail, bytes, nesc, nz;
+};
+__device__ __forceinline__ TS32 ts32_identity() { return TS32{0, 0, 0, 0, 0, 0}; }
+__device__ __forceinline__ int rb32(int L) { return L <= 0 ? 0 : (L == 1 ? 1 : 1 + vlen32((uint32_t)L)); }
+__device__ __forceinline__ TS32 ts32_combine(const TS32 &a, const TS32 &b) {
+    TS32 r;
+    r.len = a.len + b.len;
+    r.nesc = a.nesc + b.nesc;
+    r.nz = a.nz | b.nz;
+    r.lead = a.nz ? a.lead : a.len + b.lead;
+    r.trail = b.nz ? b.trail : (a.nz ? a.trail + b.len : r.len);
+    r.bytes = a.bytes + b.bytes + ((a.nz && b.nz) ? rb32(a.trail + b.lead) : 0);
+    return r;
+}
+__device__ __forceinline__ TS32 ts32_shfl(const TS32 &s, int off, bool up) {
+    TS32 r;
+    if (up) {
+        r.len = __shfl_up_sync(0xFFFFFFFFu, s.len, off);
+        r.lead = __shfl_up_sync(0xFFFFFFFFu, s.lead, off);
+        r.trail = __shfl_up_sync(0xFFFFFFFFu, s.trail, off);
+        r.bytes = __shfl_up_sync(0xFFFFFFFFu, s.bytes, off);
+        r.nesc = __shfl_up_sync(0xFFFFFFFFu, s.nesc, off);
+        r.nz = __shfl_up_sync(0xFFFFFFFFu, s.nz, off);
+    } else {
+        r.len = __shfl_down_sync(0xFFFFFFFFu, s.len, off);
+        r.lead = __shfl_down_sync(0xFFFFFFFFu, s.lead, off);
+        r.trail = __shfl_down_sync(0xFFFFFFFFu, s.trail, off);
+        r.bytes = __shfl_down_sync(0xFFFFFFFFu, s.bytes, off);
+        r.nesc = __shfl_down_sync(0xFFFFFFFFu, s.nesc, off);
+        r.nz = __shfl_down_sync(0xFFFFFFFFu, s.nz, off);
+    }
+    return r;
+}
+
+__device__ __forceinline__ TS32 ts32_bcast(const TS32 &s, int src) {
+    TS32 r;
+    r.len = __shfl_sync(0xFFFFFFFFu, s.len, src);
+    r.lead = __shfl_sync(0xFFFFFFFFu, s.lead, src);
+    r.trail = __shfl_sync(0xFFFFFFFFu, s.trail, src);
+    r.bytes = __shfl_sync(0xFFFFFFFFu, s.bytes, src);
+    r.nesc = __shfl_sync(0xFFFFFFFFu, s.nesc, src);
+    r.nz = __shfl_sync(0xFFFFFFFFu, s.nz, src);
+    return r;
+}
+
+struct SegGeom {
+    int band, y0, rows, z0, z1, ex, span, W;
+    uint32_t M;  // row = umulhi(slot, M) for slot < SG_SPAN (M = ceil(2^32 / ex); ex == 1 special)
+};
+
+__device__ __forceinline__ SegGeom seg_geom(const RegDev &R, int64_t item) {
+    SegGeom g;
+    const int64_t local = item - R.item_base;
+    g.band = (int)(local % R.nty);
+    const int zc = (int)(local / R.nty);
+    g.ex = R.ex;
+    g.y0 = g.band * R.rb;
+    g.rows = min(R.rb, R.ey - g.y0);
+    g.z0 = zc * R.zl;
+    g.z1 = min(g.z0 + R.zl, R.ez);
+    g.span = (g.rows + 1) * g.ex;
+    // slots per warp: whole 256-slot chunks (lanes full in phase 2; a small
+    // band-plane leaves the last warps idle rather than every lane half-used)
+    g.W = 32 * SG_L * ((g.span + SG_T * SG_L - 1) / (SG_T * SG_L));
+    g.M = (uint32_t)((0x100000000ull + (uint64_t)g.ex - 1) / (uint64_t)g.ex);
+    return g;
+}
+
+__device__ __forceinline__ int seg_row(const SegGeom &G, int i) {
+    return G.ex == 1 ? i : (int)__umulhi((uint32_t)i, G.M);
+}
+
+// piece (warp range of one band-plane) index in the region's stream order
+__device__ __forceinline__ int64_t seg_piece(const RegDev &R, int z, int band, int warp) {
+    return R.piece_base + ((int64_t)z * R.nty + band) * SG_NW + warp;
+}
+
+// Shared memory of an item: one dynamic array (int32 words), addressed by
+// integer offsets so every access compiles to LDS/STS: D x 2 (by plane
+// parity) and U, each padded (sp_idx), then the escape flags x 2 (bytes).
+extern __shared__ __align__(16) int32_t sg_w[];
+struct SegSmem {
+    int ps;                  // padded words per array
+    int d0, d1, u;           // word offsets
+};
+__device__ __forceinline__ SegSmem seg_smem(int span_cap) {
+    SegSmem s;
+    s.ps = sp_idx(span_cap) + 16;  // + lookahead of a lane's SG_L slots
+    s.d0 = 0;
+    s.d1 = s.ps;
+    s.u = 2 * s.ps;
+    return s;
+}
+__device__ __forceinline__ uint8_t *seg_flags(const SegSmem &S, int par, int span_cap) {
+    return reinterpret_cast<uint8_t *>(sg_w + 3 * S.ps) + par * (span_cap + 16);
+}
+// staged input of plane parity par (cp.async, one element per slot)
+template <typename T>
+__device__ __forceinline__ T *seg_stage(const SegSmem &S, int par, int span_cap) {
+    unsigned char *b = reinterpret_cast<unsigned char *>(sg_w + 3 * S.ps) + 2 * (span_cap + 16);
+    b = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(b) + 15) & ~uintptr_t(15));
+    return reinterpret_cast<T *>(b) + par * span_cap;
+}
+
+// asynchronous copy of the thread's strided slots of one plane into the
+// staging buffer (rows above the window are not copied: their u is 0)
+template <typename T>
+__device__ __forceinline__ void seg_issue(const SegGeom &G, const T *base, int64_t NX, T *stage) {
+    for (int i = threadIdx.x; i < G.span; i += SG_T) {
+        const int row = seg_row(G, i);
+        if (G.y0 - 1 + row >= 0) {
+            const T *src = base + (int64_t)row * NX + (i - row * G.ex);
+            const unsigned dst = (unsigned)__cvta_generic_to_shared(stage + i);
+            if (sizeof(T) == 4)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dst), "l"(src) : "memory");
+            else
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(src) : "memory");
+        }
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+__device__ __forceinline__ void seg_wait_prev() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+
+// u at plane z0 - 1 of the thread's slots (0 outside the window); escape
+// flags cleared
+template <typename T>
+__device__ __forceinline__ void seg_init(const RegDev &R, const SegGeom &G, const Quant &Q, bool quant,
+                                         const T *base, int64_t NX, int64_t plane, const SegSmem &S,
+                                         int span_cap) {
+    uint8_t *e0 = seg_flags(S, 0, span_cap), *e1 = seg_flags(S, 1, span_cap);
+    for (int i = threadIdx.x; i < S.ps; i += SG_T) {  // D zero past the span (lookahead reads)
+        sg_w[S.d0 + i] = 0;
+        sg_w[S.d1 + i] = 0;
+    }
+    for (int i = threadIdx.x; i < G.span; i += SG_T) {
+        int32_t u = 0;
+        const int row = seg_row(G, i);
+        if (quant && (G.z0 > 0 || R.zhalo) && G.y0 - 1 + row >= 0) {
+            bool e;
+            u = quantize(Q, (double)__ldg(base - plane + (int64_t)row * NX + (i - row * G.ex)), e);
+        }
+        sg_w[S.u + sp_idx(i)] = u;
+        e0[i] = 0;
+        e1[i] = 0;
+    }
+}
+
+// phase 1 of one plane: D = u - u(z-1) for the thread's strided slots; the
+// (rare) lanes whose fast quantiser path failed run the exact sequence
+// afterwards; returns the thread's escape mask (bit k = slot tid + SG_T k)
+template <typename T, bool CHK32>
+__device__ __forceinline__ uint32_t seg_phase1(const SegGeom &G, const Quant &Q, bool quant, const T *base,
+                                               int64_t NX, const SegSmem &S, int par, int span_cap,
+                                               uint32_t clear_escm, bool &inexact) {
+    const int dofs = par ? S.d1 : S.d0, uofs = S.u;
+    const T *stage = seg_stage<T>(S, par, span_cap);
+    uint8_t *sE = seg_flags(S, par, span_cap);
+    while (clear_escm) {  // flags this thread set two planes ago in this buffer
+        const int k = __ffs(clear_escm) - 1;
+        clear_escm &= clear_escm - 1;
+        sE[threadIdx.x + SG_T * k] = 0;
+    }
+    uint32_t slowm = 0;
+    int k = 0;
+#pragma unroll 4
+    for (int i = threadIdx.x; i < G.span; i += SG_T, ++k) {
+        const int row = seg_row(G, i);
+        int32_t u = 0;
+        if (G.y0 - 1 + row >= 0) {
+            const T tv = stage[i];
+            if (CHK32 && row >= 1) inexact |= not_f32_exact(tv);
+            if (quant && !quant_fast(Q, (double)tv, u)) slowm |= 1u << k;
+        }
+        const int p = sp_idx(i);
+        sg_w[dofs + p] = u - sg_w[uofs + p];
+        sg_w[uofs + p] = u;
+    }
+    uint32_t escm = 0;
+    while (slowm) {  // exact sequence; prev = u_fast - D keeps D = u - prev exact
+        const int kk = __ffs(slowm) - 1;
+        slowm &= slowm - 1;
+        const int i = threadIdx.x + SG_T * kk;
+        const int row = seg_row(G, i);
+        bool e;
+        const int32_t u = quantize(Q, (double)stage[i], e);
+        const int p = sp_idx(i);
+        const int32_t prev = sg_w[uofs + p] - sg_w[dofs + p];
+        sg_w[dofs + p] = u - prev;
+        sg_w[uofs + p] = u;
+        if (e && row >= 1) {
+            escm |= 1u << kk;
+            sE[i] = 1;
+        }
+    }
+    return escm;
+}
+
+// phase 2 helper: the lane's SG_L consecutive slots [i0, i0 + SG_L) (i0 a
+// multiple of SG_L) below lim: token values (zigzag + 1; 1 = zero or not own)
+// and bit masks of own / nonzero / escaped slots (own slots are contiguous).
+// Straight-line: own range and row starts as masks, reads clamped in-bounds.
+struct LaneQ {
+    uint32_t z1[SG_L];
+    uint32_t own, nz, esc;  // bit j
+};
+__device__ __forceinline__ LaneQ seg_lane_q(const SegGeom &G, const SegSmem &S, int par, int span_cap, int i0,
+                                            int lim, bool any_esc) {
+    LaneQ L;
+    if (i0 >= lim) {  // no slot of this lane (its reads would leave the arrays)
+#pragma unroll
+        for (int j = 0; j < SG_L; ++j) L.z1[j] = 1u;
+        L.own = L.nz = L.esc = 0;
+        return L;
+    }
+    const int dofs = par ? S.d1 : S.d0;
+    const int lo = min(max(G.ex - i0, 0), SG_L), hi = min(lim - i0, SG_L);  // own slots [lo, hi)
+    L.own = (hi > lo) ? (((1u << hi) - 1u) & ~((1u << lo) - 1u)) : 0u;
+    const int x0 = i0 - seg_row(G, i0) * G.ex;
+    uint32_t rs = 0;  // slots j with x == 0
+    for (int t = x0 == 0 ? 0 : G.ex - x0; t < SG_L; t += G.ex) rs |= 1u << t;
+    const int pb = dofs + sp_idx(i0);  // slot i0 + j sits at pb + j (i0 % 8 == 0)
+    const int pu = i0 - G.ex;          // up-row slot of j = 0 (negative only when not own)
+    int32_t dl = sg_w[dofs + sp_idx(max(i0 - 1, 0))];
+    int32_t ul = sg_w[dofs + sp_idx(max(pu - 1, 0))];
+    uint32_t nzm = 0;
+#pragma unroll
+    for (int j = 0; j < SG_L; ++j) {
+        const int32_t d = sg_w[pb + j];
+        const int32_t du = sg_w[dofs + sp_idx(max(pu + j, 0))];
+        const int32_t q = d - du - (((rs >> j) & 1u) ? 0 : dl - ul);
+        const uint32_t z1v = ((L.own >> j) & 1u) ? zz1_32(q) : 1u;
+        L.z1[j] = z1v;
+        nzm |= (z1v != 1u ? 1u : 0u) << j;
+        dl = d;
+        ul = du;
+    }
+    L.nz = nzm;
+    uint32_t em = 0;
+    if (any_esc) {
+        const uint8_t *sE = seg_flags(S, par, span_cap);
+#pragma unroll
+        for (int j = 0; j < SG_L; ++j)
+            if ((L.own >> j) & 1u) em |= (sE[i0 + j] ? 1u : 0u) << j;
+    }
+    L.esc = em;
+    return L;
+}
+
+// the lane's summary from its masks: bytes = sum of literal varint sizes +
+// run tokens between literals (gaps < SG_L: rb = [gap >= 1] + [gap >= 2])
+__device__ __forceinline__ TS32 lane_summary(const LaneQ &L) {
+    TS32 t;
+    const uint32_t own = L.own, m = L.nz;
+    t.len = __popc(own);
+    t.nesc = __popc(L.esc);
+    t.nz = m != 0;
+    int vb = 0;
+#pragma unroll
+    for (int j = 0; j < SG_L; ++j) vb += ((m >> j) & 1u) ? vlen32(L.z1[j]) : 0;
+    const uint32_t later = m & (m - 1);                 // nonzeros after the first
+    const uint32_t g1 = later & ~(m << 1);              // ... whose previous slot is zero
+    const uint32_t g2 = g1 & ~(m << 2);                 // ... and the one before it too
+    t.bytes = vb + __popc(g1) + __popc(g2);
+    const int a = own ? __ffs(own) - 1 : 0, b = own ? 32 - __clz(own) : 0;  // own slots [a, b)
+    t.lead = m ? (__ffs(m) - 1) - a : t.len;
+    t.trail = m ? (b - 1) - (31 - __clz(m)) : t.len;
+    return t;
+}
+
+// pass 1: the summary of every piece (warp range of a band-plane)
+template <typename T>
+__global__ void __launch_bounds__(SG_T, 3) k_qseg(const T *__restrict__ vol, const EncParams *__restrict__ P,
+                                                  RegDev *__restrict__ regs, const int32_t *__restrict__ item_reg,
+                                                  PieceRec2 *__restrict__ recs, uint32_t *__restrict__ escbits,
+                                                  int span_cap) {
+    __shared__ RegDev R;
+    const int64_t item = blockIdx.x;
+    const int ri = __ldg(item_reg + item);
+    coop_copy(&R, regs + ri);
+    __syncthreads();
+    const SegGeom G = seg_geom(R, item);
+    const SegSmem S = seg_smem(span_cap);
+    const int64_t NX = P->NX, NY = P->NY, plane = NX * NY;
+    const bool quant = R.mode == 0;
+    const Quant Q = make_quant(R.e);
+    const bool chk32 = sizeof(T) == 8 && P->src_dtype == CHR_F32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const T *base = vol + ((int64_t)(R.oz + G.z0) * NY + R.oy + G.y0 - 1) * NX + R.ox;  // halo row, plane z0
+    seg_init(R, G, Q, quant, base, NX, plane, S, span_cap);
+    seg_issue(G, base, NX, seg_stage<T>(S, G.z0 & 1, span_cap));
+    __syncthreads();
+    bool inexact = false;
+    uint32_t hist0 = 0u, hist1 = 0u;  // escape masks of the last two planes (by parity)
+    const int wlo = warp * G.W, whi = min(wlo + G.W, G.span);
+    for (int z = G.z0; z < G.z1; ++z, base += plane) {
+        const int par = z & 1;
+        if (z + 1 < G.z1) seg_issue(G, base + plane, NX, seg_stage<T>(S, par ^ 1, span_cap));
+        else asm volatile("cp.async.commit_group;\n" ::: "memory");
+        seg_wait_prev();
+        const uint32_t clr = par ? hist1 : hist0;
+        const uint32_t escm = chk32 ? seg_phase1<T, true>(G, Q, quant, base, NX, S, par, span_cap, clr, inexact)
+                                    : seg_phase1<T, false>(G, Q, quant, base, NX, S, par, span_cap, clr, inexact);
+        if (par) hist1 = escm; else hist0 = escm;
+        const bool any_esc = __syncthreads_or(escm != 0);
+        if (escm) {  // rare: escape bits at the window's raster index
+            uint32_t m = escm;
+            while (m) {
+                const int kk = __ffs(m) - 1;
+                m &= m - 1;
+                const int i = threadIdx.x + SG_T * kk;
+                const int64_t bit = (int64_t)R.ebase * 32 + ((int64_t)z * R.ey + G.y0) * G.ex + (i - G.ex);
+                atomicOr(escbits + (bit >> 5), 1u << (bit & 31));
+            }
+            atomicOr(&regs[ri].has_esc, 1);
+        }
+        TS32 acc = ts32_identity();
+        for (int c0 = wlo; c0 < whi; c0 += 32 * SG_L) {  // warp-uniform
+            const LaneQ L = seg_lane_q(G, S, par, span_cap, c0 + SG_L * lane, whi, any_esc);
+            TS32 t = lane_summary(L);
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {  // ordered tree: lane 0 ends with the chunk
+                const TS32 o = ts32_shfl(t, off, false);
+                if ((lane & (2 * off - 1)) == 0) t = ts32_combine(t, o);
+            }
+            acc = ts32_combine(acc, t);  // lane 0's value is the one used
+        }
+        if (lane == 0) {
+            PieceRec2 pr;
+            pr.len = (uint16_t)acc.len;
+            pr.lead = (uint16_t)acc.lead;
+            pr.trail = (uint16_t)acc.trail;
+            pr.nesc = (uint16_t)acc.nesc;
+            pr.bytes = (uint32_t)acc.bytes;
+            pr.nz = (uint32_t)acc.nz;
+            recs[seg_piece(R, z, G.band, warp)] = pr;
+        }
+    }
+    if (chk32 && __any_sync(0xFFFFFFFFu, inexact) && lane == 0) atomicOr(&regs[ri].f32bad, 1);
+}
+
+// pass 2: recompute q, place and write every token byte (codec 1 / 2),
+// escape values (codec 2), or the samples themselves (codec 3 / 0).  The
+// warp's stream offset comes from its piece's exclusive prefix (PieceOff);
+// lanes get theirs from one ordered warp scan per chunk, then write their
+// samples' tokens sequentially.
+template <typename T>
+__global__ void __launch_bounds__(SG_T, 3) k_qemit(const T *__restrict__ vol, const EncParams *__restrict__ P,
+                                                   const RegDev *__restrict__ regs,
+                                                   const int32_t *__restrict__ item_reg,
+                                                   const PieceOff *__restrict__ poffs, uint8_t *__restrict__ out,
+                                                   int span_cap) {
+    __shared__ RegDev R;
+    const int64_t item = blockIdx.x;
+    const int ri = __ldg(item_reg + item);
+    coop_copy(&R, regs + ri);
+    __syncthreads();
+    const SegGeom G = seg_geom(R, item);
+    const int64_t NX = P->NX, NY = P->NY, plane = NX * NY;
+    const int codec = R.codec;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const T *base = vol + ((int64_t)(R.oz + G.z0) * NY + R.oy + G.y0 - 1) * NX + R.ox;  // halo row, plane z0
+    if (codec == 0 || codec == 3) {  // verbatim: the samples in raster order
+        for (int z = G.z0; z < G.z1; ++z, base += plane) {
+            const int64_t s0 = R.s_off + ((int64_t)z * R.ey + G.y0) * G.ex - G.ex;  // stream index of slot 0
+            for (int i = G.ex + threadIdx.x; i < G.span; i += SG_T) {
+                const int row = seg_row(G, i);
+                const T v = __ldg(base + (int64_t)row * NX + (i - row * G.ex));
+                if (codec == 3) put_le(out + R.payload_off + 4 * (s0 + i), (float)v);
+                else put_le(out + R.payload_off + 8 * (s0 + i), (double)v);
+            }
+        }
+        return;
+    }
+    const SegSmem S = seg_smem(span_cap);
+    const Quant Q = make_quant(R.e);
+    seg_init(R, G, Q, true, base, NX, plane, S, span_cap);
+    seg_issue(G, base, NX, seg_stage<T>(S, G.z0 & 1, span_cap));
+    __syncthreads();
+    const uint64_t vbase = R.payload_off + (uint64_t)((R.n_win + 7) >> 3);
+    uint8_t *const tok = out + R.tok_start;
+    const int wlo = warp * G.W, whi = min(wlo + G.W, G.span);
+    const bool ends_window = R.last && G.band == R.nty - 1 && wlo < G.span && whi == G.span;
+    uint32_t hist0 = 0u, hist1 = 0u;  // escape masks of the last two planes (by parity)
+    bool unused = false;
+    for (int z = G.z0; z < G.z1; ++z, base += plane) {
+        const int par = z & 1;
+        if (z + 1 < G.z1) seg_issue(G, base + plane, NX, seg_stage<T>(S, par ^ 1, span_cap));
+        else asm volatile("cp.async.commit_group;\n" ::: "memory");
+        const PieceOff po = poffs[seg_piece(R, z, G.band, warp)];
+        seg_wait_prev();
+        const uint32_t escm =
+            seg_phase1<T, false>(G, Q, true, base, NX, S, par, span_cap, par ? hist1 : hist0, unused);
+        if (par) hist1 = escm; else hist0 = escm;
+        const bool any_esc = __syncthreads_or(escm != 0);
+        // placement after (piece prefix) ++ r (r: this warp's samples so far):
+        //   token offset = r.nz ? tok_off + r.bytes + run_bytes(carry + r.lead) : tok_off
+        //   zero carry   = r.nz ? r.trail : carry + r.len
+        TS32 r = ts32_identity();
+        for (int c0 = wlo; c0 < whi; c0 += 32 * SG_L) {  // warp-uniform
+            const int i0 = c0 + SG_L * lane;
+            const LaneQ L = seg_lane_q(G, S, par, span_cap, i0, whi, any_esc);
+            const TS32 t = lane_summary(L);
+            TS32 inc = t;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const TS32 o = ts32_shfl(inc, off, true);
+                if (lane >= off) inc = ts32_combine(o, inc);
+            }
+            TS32 ex = ts32_shfl(inc, 1, true);
+            if (lane == 0) ex = ts32_identity();
+            const TS32 pre = ts32_combine(r, ex);  // samples of this piece before the lane's
+            if (t.nz || t.nesc) {
+                int64_t off = pre.nz ? po.tok_off + pre.bytes + run_bytes(po.carry + pre.lead) : po.tok_off;
+                int64_t zc = pre.nz ? (int64_t)pre.trail : po.carry + pre.len;  // zeros since the last literal
+                int64_t nesc = po.esc_off + pre.nesc;
+#pragma unroll
+                for (int j = 0; j < SG_L; ++j) {
+                    if (!((L.own >> j) & 1u)) continue;
+                    const uint32_t z1v = L.z1[j];
+                    if (z1v != 1u) {
+                        uint8_t *p = tok + off;
+                        uint8_t *e = put_varint32(put_run(p, zc), z1v);
+                        off += e - p;
+                        zc = 0;
+                    } else {
+                        ++zc;
+                    }
+                    if ((L.esc >> j) & 1u) {
+                        const int i = i0 + j;
+                        const int row = seg_row(G, i);
+                        const double v = (double)__ldg(base + (int64_t)row * NX + (i - row * G.ex));
+                        put_le(out + vbase + 8 * nesc, v);
+                        ++nesc;
+                    }
+                }
+            }
+            r = ts32_combine(r, ts32_bcast(inc, 31));
+        }
+        // the window's final zero run, after its last sample
+        if (ends_window && z == R.ez - 1 && lane == 0) {
+            const int64_t off = r.nz ? po.tok_off + r.bytes + run_bytes(po.carry + r.lead) : po.tok_off;
+            const int64_t fin = r.nz ? (int64_t)r.trail : po.carry + r.len;
+            put_run(tok + off, fin);
+        }
+    }
+}
+
 // ------------------------------------------------------------------ host
 struct EncPlan {
     std::vector<RegDev> regs;
     int64_t nitems = 0, npieces_total = 0, nchunks = 0, qtotal = 0, etotal = 0;
     bool portions = false;  // empty windows allowed (z-slab portions)
+    bool segmode = false;   // single-read segment path (k_qseg / k_qemit)
+    int span_cap = 0;       // segment path: max band-plane slots (multiple of 32)
+    PieceRec2 *recs2 = nullptr;  // segment path: piece summaries (k_qseg)
     size_t ws_bytes = 0;
     // carved pointers
     EncParams *params;
@@ -1040,26 +1528,75 @@ static bool build_plan_uncached(const chr_region_t *h, int64_t nreg, EncPlan &pl
     return true;
 }
 
+// Segment-path geometry (k_qseg / k_qemit): bands of rb whole rows with
+// (rb + 1) * ex <= SG_TARGET (at least one row: (1 + 1) * ex <= SG_SPAN),
+// z-chunks of <= SG_ZMAX planes balanced over the window; a segment per
+// (plane, band) in stream order; scan chunks of CH segments.  Returns false
+// when a window is too wide for the path (the caller keeps the piece path).
+static bool plan_segments(EncPlan &pl) {
+    int64_t item = 0, seg = 0, chunk = 0, span_cap = 32;
+    for (const RegDev &R : pl.regs)
+        if (2 * (int64_t)R.ex > SG_SPAN) return false;
+    for (RegDev &R : pl.regs) {
+        R.rb = (int32_t)std::max<int64_t>(1, std::min<int64_t>(R.ey, SG_TARGET / R.ex - 1));
+        R.ntx = 1;
+        R.nty = (int32_t)ceil_div(R.ey, R.rb);
+        R.nzc = (int32_t)std::max<int64_t>(1, ceil_div(R.ez, SG_ZMAX));
+        R.zl = (int32_t)std::max<int64_t>(1, ceil_div(R.ez, R.nzc));
+        R.nzc = (int32_t)std::max<int64_t>(1, ceil_div(R.ez, R.zl));
+        R.qband = 0;
+        R.item_base = item;
+        item += (int64_t)R.nty * R.nzc;
+        R.piece_base = seg;
+        R.npieces = (int64_t)R.ez * R.nty * SG_NW;  // pieces: (plane, band, warp) in stream order
+        R.chunk_base = chunk;
+        R.nchunks = std::max<int64_t>(1, ceil_div(R.npieces, CH));
+        chunk += R.nchunks;
+        seg += R.nchunks * CH;
+        span_cap = std::max<int64_t>(span_cap, (int64_t)(std::min(R.rb, R.ey) + 1) * R.ex);
+    }
+    pl.nitems = item;
+    pl.npieces_total = seg;
+    pl.nchunks = chunk;
+    pl.span_cap = (int)((span_cap + 31) & ~int64_t(31));
+    pl.qtotal = 0;  // no quantum intermediate
+    pl.segmode = true;
+    return true;
+}
+
+// SegSmem: D x 2 + U (padded int32, + lookahead) + escape flags x 2 (bytes)
+// + staged input x 2 (elem bytes each)
+static size_t seg_smem_bytes(int span_cap, size_t elem) {
+    return 3 * sizeof(int32_t) * (size_t)(span_cap + span_cap / 8 + 16) + 2 * (size_t)(span_cap + 16) + 16 +
+           2 * elem * (size_t)span_cap + 16;
+}
+
 // The pipeline asks for the workspace size and then compresses with the same
 // region table: the host plan of the last table is kept per thread (the table
 // is compared byte for byte, ~3 us, instead of rebuilt, ~25 us at 426 regions).
-static bool build_plan(const chr_region_t *h, int64_t nreg, EncPlan &pl) {
+static bool build_plan(const chr_region_t *h, int64_t nreg, EncPlan &pl, bool allow_seg = true) {
     struct Cache {
         std::vector<chr_region_t> key;
         EncPlan plan;
+        bool allow_seg = true;
         bool valid = false;
     };
     thread_local Cache C;
+    // the piece path stays the default: the segment path reads the input once
+    // less but issues ~1.5x the instructions; CHR_ENC_SEG=1
+    allow_seg = allow_seg && getenv("CHR_ENC_SEG") != nullptr;
     if (pl.portions) return build_plan_uncached(h, nreg, pl);
-    if (C.valid && (int64_t)C.key.size() == nreg &&
+    if (C.valid && C.allow_seg == allow_seg && (int64_t)C.key.size() == nreg &&
         std::memcmp(C.key.data(), h, sizeof(chr_region_t) * (size_t)nreg) == 0) {
         pl = C.plan;
         return true;
     }
     C.valid = false;
     if (!build_plan_uncached(h, nreg, pl)) return false;
+    if (allow_seg) plan_segments(pl);  // false (a window too wide): the piece path
     C.key.assign(h, h + nreg);
     C.plan = pl;
+    C.allow_seg = allow_seg;
     C.valid = true;
     return true;
 }
@@ -1069,7 +1606,7 @@ static void carve(EncPlan &pl, void *base, size_t cap) {
     const int64_t nreg = (int64_t)pl.regs.size();
     pl.params = c.take<EncParams>(1);
     pl.d_regs = c.take<RegDev>(nreg);
-    pl.recs = c.take<PieceRec>(pl.npieces_total);
+    pl.recs = c.take<PieceRec>(pl.segmode ? 0 : pl.npieces_total);
     pl.poffs = c.take<PieceOff>(pl.npieces_total);
     pl.chunk = c.take<TokSeg>(pl.nchunks);
     pl.segs = c.take<CrcSeg>(nreg + 1);
@@ -1078,6 +1615,9 @@ static void carve(EncPlan &pl, void *base, size_t cap) {
     pl.item_reg = c.take<int32_t>(pl.nitems + 1);
     pl.chunk_reg = c.take<int32_t>(pl.nchunks + 1);
     pl.qz = c.take<uint32_t>(pl.qtotal + 1);
+    if (pl.segmode) {
+        pl.recs2 = c.take<PieceRec2>(pl.npieces_total);
+    }
     pl.escbits = c.take<uint32_t>(pl.etotal + 2);
     pl.scal = c.take<EncScalars>(1);
     pl.ws_bytes = c.off + 256;
@@ -1181,26 +1721,49 @@ extern "C" int chr_compress2(const void *d_vol, int dtype, int src_dtype, int64_
         CHR_PROF("k_tile_fill_map", st);
         k_tile_fill_map<<<(unsigned)nreg, 256, 0, st>>>(pl.d_regs, nreg, pl.item_reg, pl.chunk_reg);
     }
-    if (dtype == CHR_F32) {
-        CHR_PROF("k_quant<float>", st);
-        k_quant<float><<<items, NW * 32, 0, st>>>((const float *)d_vol, pl.params, pl.d_regs, pl.item_reg, pl.qz,
-                                                  pl.escbits);
-        k_quant_band<float><<<items, QB_T, 0, st>>>((const float *)d_vol, pl.params, pl.d_regs, pl.item_reg,
-                                                    pl.qz, pl.escbits);
+    if (pl.segmode) {
+        const size_t smem = seg_smem_bytes(pl.span_cap, dtype == CHR_F32 ? 4 : 8);
+        if (smem > 48 * 1024) {
+            CHR_CUDA_TRY(cudaFuncSetAttribute(k_qseg<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            CHR_CUDA_TRY(cudaFuncSetAttribute(k_qseg<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            CHR_CUDA_TRY(cudaFuncSetAttribute(k_qemit<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            CHR_CUDA_TRY(cudaFuncSetAttribute(k_qemit<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        }
+        if (dtype == CHR_F32) {
+            CHR_PROF("k_qseg<float>", st);
+            k_qseg<float><<<items, SG_T, smem, st>>>((const float *)d_vol, pl.params, pl.d_regs, pl.item_reg,
+                                                     pl.recs2, pl.escbits, pl.span_cap);
+        } else {
+            CHR_PROF("k_qseg<double>", st);
+            k_qseg<double><<<items, SG_T, smem, st>>>((const double *)d_vol, pl.params, pl.d_regs, pl.item_reg,
+                                                      pl.recs2, pl.escbits, pl.span_cap);
+        }
+        {
+            CHR_PROF("k_scan_reduce", st);
+            k_scan_reduce<<<chunks, 256, 0, st>>>(pl.params, pl.d_regs, pl.recs2, pl.chunk);
+        }
     } else {
-        CHR_PROF("k_quant<double>", st);
-        k_quant<double><<<items, NW * 32, 0, st>>>((const double *)d_vol, pl.params, pl.d_regs, pl.item_reg, pl.qz,
-                                                   pl.escbits);
-        k_quant_band<double><<<items, QB_T, 0, st>>>((const double *)d_vol, pl.params, pl.d_regs, pl.item_reg,
-                                                     pl.qz, pl.escbits);
-    }
-    {
-        CHR_PROF("k_summarize", st);
-        k_summarize<<<chunks * CSPLIT, 256, 0, st>>>(pl.d_regs, pl.chunk_reg, pl.qz, pl.escbits, pl.recs);
-    }
-    {
-        CHR_PROF("k_scan_reduce", st);
-        k_scan_reduce<<<chunks, 256, 0, st>>>(pl.params, pl.d_regs, pl.recs, pl.chunk);
+        if (dtype == CHR_F32) {
+            CHR_PROF("k_quant<float>", st);
+            k_quant<float><<<items, NW * 32, 0, st>>>((const float *)d_vol, pl.params, pl.d_regs, pl.item_reg,
+                                                      pl.qz, pl.escbits);
+            k_quant_band<float><<<items, QB_T, 0, st>>>((const float *)d_vol, pl.params, pl.d_regs, pl.item_reg,
+                                                        pl.qz, pl.escbits);
+        } else {
+            CHR_PROF("k_quant<double>", st);
+            k_quant<double><<<items, NW * 32, 0, st>>>((const double *)d_vol, pl.params, pl.d_regs, pl.item_reg,
+                                                       pl.qz, pl.escbits);
+            k_quant_band<double><<<items, QB_T, 0, st>>>((const double *)d_vol, pl.params, pl.d_regs,
+                                                         pl.item_reg, pl.qz, pl.escbits);
+        }
+        {
+            CHR_PROF("k_summarize", st);
+            k_summarize<<<chunks * CSPLIT, 256, 0, st>>>(pl.d_regs, pl.chunk_reg, pl.qz, pl.escbits, pl.recs);
+        }
+        {
+            CHR_PROF("k_scan_reduce", st);
+            k_scan_reduce<<<chunks, 256, 0, st>>>(pl.params, pl.d_regs, pl.recs, pl.chunk);
+        }
     }
     {
         CHR_PROF("k_scan_regions", st);
@@ -1211,30 +1774,41 @@ extern "C" int chr_compress2(const void *d_vol, int dtype, int src_dtype, int64_
         CHR_PROF("k_layout", st);
         k_layout<<<1, 1024, 0, st>>>(pl.params, pl.d_regs, pl.segs, pl.scal);
     }
-    {
-        CHR_PROF("k_scan_down", st);
-        k_scan_down<<<chunks, 256, 0, st>>>(pl.params, pl.d_regs, pl.recs, pl.chunk, pl.poffs);
-    }
-    if (dtype == CHR_F32) {
+    if (pl.segmode) {
+        const size_t smem = seg_smem_bytes(pl.span_cap, dtype == CHR_F32 ? 4 : 8);
         {
-            CHR_PROF("k_emit_q<float>", st);
-            k_emit_q<float><<<chunks * CSPLIT, 256, 0, st>>>((const float *)d_vol, pl.params, pl.d_regs, pl.chunk_reg,
-                                                    pl.recs, pl.poffs, pl.qz, pl.escbits, d_out);
+            CHR_PROF("k_scan_down", st);
+            k_scan_down<<<chunks, 256, 0, st>>>(pl.params, pl.d_regs, pl.recs2, pl.chunk, pl.poffs);
         }
-        {
-            CHR_PROF("k_bitmap", st);
-            k_bitmap<<<148, 256, 0, st>>>(pl.d_regs, pl.codec2, pl.scal, pl.escbits, d_out);
+        if (dtype == CHR_F32) {
+            CHR_PROF("k_qemit<float>", st);
+            k_qemit<float><<<items, SG_T, smem, st>>>((const float *)d_vol, pl.params, pl.d_regs, pl.item_reg,
+                                                      pl.poffs, d_out, pl.span_cap);
+        } else {
+            CHR_PROF("k_qemit<double>", st);
+            k_qemit<double><<<items, SG_T, smem, st>>>((const double *)d_vol, pl.params, pl.d_regs, pl.item_reg,
+                                                       pl.poffs, d_out, pl.span_cap);
         }
     } else {
         {
+            CHR_PROF("k_scan_down", st);
+            k_scan_down<<<chunks, 256, 0, st>>>(pl.params, pl.d_regs, pl.recs, pl.chunk, pl.poffs);
+        }
+        if (dtype == CHR_F32) {
+            CHR_PROF("k_emit_q<float>", st);
+            k_emit_q<float><<<chunks * CSPLIT, 256, 0, st>>>((const float *)d_vol, pl.params, pl.d_regs,
+                                                             pl.chunk_reg, pl.recs, pl.poffs, pl.qz, pl.escbits,
+                                                             d_out);
+        } else {
             CHR_PROF("k_emit_q<double>", st);
-            k_emit_q<double><<<chunks * CSPLIT, 256, 0, st>>>((const double *)d_vol, pl.params, pl.d_regs, pl.chunk_reg,
-                                                     pl.recs, pl.poffs, pl.qz, pl.escbits, d_out);
+            k_emit_q<double><<<chunks * CSPLIT, 256, 0, st>>>((const double *)d_vol, pl.params, pl.d_regs,
+                                                              pl.chunk_reg, pl.recs, pl.poffs, pl.qz, pl.escbits,
+                                                              d_out);
         }
-        {
-            CHR_PROF("k_bitmap", st);
-            k_bitmap<<<148, 256, 0, st>>>(pl.d_regs, pl.codec2, pl.scal, pl.escbits, d_out);
-        }
+    }
+    {
+        CHR_PROF("k_bitmap", st);
+        k_bitmap<<<148, 256, 0, st>>>(pl.d_regs, pl.codec2, pl.scal, pl.escbits, d_out);
     }
     if (write_file)
         {
@@ -1313,7 +1887,7 @@ extern "C" size_t chr_rle_encode_workspace_size(int64_t n) {
     if (n < 1 || n > INT32_MAX) return 256;
     const chr_region_t h = rle_region(n);
     EncPlan pl;
-    if (!build_plan(&h, 1, pl)) return 256;
+    if (!build_plan(&h, 1, pl, false)) return 256;
     carve(pl, nullptr, ~size_t(0));
     return pl.ws_bytes + 256;
 }
@@ -1331,7 +1905,7 @@ extern "C" int chr_rle_encode(const int64_t *d_q, int64_t n, uint8_t *d_out, uin
     cudaStream_t st = (cudaStream_t)stream;
     const chr_region_t h = rle_region(n);
     EncPlan pl;
-    if (!build_plan(&h, 1, pl)) return CHR_E_PARAMETER;
+    if (!build_plan(&h, 1, pl, false)) return CHR_E_PARAMETER;
     carve(pl, d_ws, ws_bytes);
     if (!d_ws || pl.ws_bytes + 256 > ws_bytes) return CHR_E_WORKSPACE;
     int32_t *d_bad = reinterpret_cast<int32_t *>(reinterpret_cast<char *>(d_ws) + pl.ws_bytes);
