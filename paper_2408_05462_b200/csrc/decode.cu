@@ -956,7 +956,7 @@ __global__ void __launch_bounds__(256) k_esc_seg(const DecReg *__restrict__ regs
 }
 
 // ---- band tiles.  A tile is (full rows x, a band of bty rows y, a chunk of
-// btz planes z) of one region: <= BCAP samples, int64 in shared memory.
+// btz planes z) of one region: <= BCAP samples, int32 in shared memory.
 // Tile-local prefixes along x (rows are whole), y and z give T; then
 //   u(x,y,z) = T + [Fy(x,z) - Fy(x,z0-1)] + Fz(x,y)
 // with Fy = last row of the band above (planes z0-1..z1-1) and Fz = last
@@ -966,8 +966,15 @@ __global__ void __launch_bounds__(256) k_esc_seg(const DecReg *__restrict__ regs
 // taking tiles in diagonal order from a ticket cannot deadlock; a tile
 // publishes its own faces right after the wait (a few adds per column)
 // and only then writes its samples, so a chain hop costs one face update.
-constexpr int BCAP = 5632;   // samples per tile (44 KB of int64 + 8 KB dF: 4 CTAs per SM)
-constexpr int BDF = 1024;    // dF entries (btz * ex) when a tile has a band above
+// The tile holds q and its tile-local prefixes T as int32: every T is a sum
+// of the tile's q, so int32 is exact when the tile's sum |q| < 2^31 (k_band
+// checks it right after tokenising; a tile at or above it -- rare, and only
+// from extreme quanta -- sends its region to the generic int64 path via
+// k_asum_check).  Faces (u at tile boundaries) and u = T + faces are int64,
+// exact like the reference's int64 cumsum.
+using BV = int32_t;
+constexpr int BCAP = 10240;  // samples per tile (40 KB of int32 + 12 KB dF: 4 CTAs per SM)
+constexpr int BDF = 1536;    // dF entries (btz * ex) when a tile has a band above
 constexpr int BSEGM = 64;    // planes per tile
 
 __device__ __forceinline__ int seg_of(const int32_t *base, int nseg, int g) {
@@ -1040,10 +1047,13 @@ __device__ __forceinline__ int64_t win24_count(const Win24 &W) {
 // one unit -> literals into the plane `q` (positions count samples from the
 // segment start; PAD planes have row stride ex + 1).  Branch-free over the 16
 // own positions: H holds the LEB128 payload of bytes e-4..e, so the token
-// ending at e has value H >> 7 (5 - len).
-template <bool PAD>
+// ending at e has value H >> 7 (5 - len).  Only for positions below -2^30
+// (a segment starting deep inside a zero run) or a 5-byte token in the
+// warp.  A literal too wide for int32 (never from a valid encoder) adds 2^31
+// to asum, which sends its region to the generic int64 path.
+template <bool PAD, typename QV>
 __device__ __forceinline__ int64_t band_scatter_unit64(const Win24 &W, int64_t at64, int L, int ex, uint64_t M,
-                                                     int64_t *__restrict__ q) {
+                                                     QV *__restrict__ q, uint64_t &asum) {
     int64_t at = at64;
     int idx = (int)at, x = 0;
     if (PAD && at >= 0) {
@@ -1064,7 +1074,10 @@ __device__ __forceinline__ int64_t band_scatter_unit64(const Win24 &W, int64_t a
         const uint64_t v = H >> (7 * (5 - len));
         if (lit) {
             const uint64_t zz = v - 1;
-            if ((uint64_t)at < (uint64_t)L) q[idx] = (int64_t)(zz >> 1) ^ -(int64_t)(zz & 1);
+            if ((uint64_t)at < (uint64_t)L) {
+                q[idx] = (QV)((int64_t)(zz >> 1) ^ -(int64_t)(zz & 1));
+                asum += (zz >> 1) + (zz & 1);
+            }
             ++at;
             ++idx;
             if (PAD && ++x == ex) {
@@ -1084,16 +1097,14 @@ __device__ __forceinline__ int64_t band_scatter_unit64(const Win24 &W, int64_t a
     return at;
 }
 
-// 32-bit fast path of band_scatter_unit64: tokens <= 4 bytes (H = payload of
-// bytes e-3..e in 28 bits), positions in int32 (clamped to 2^30 past L:
-// every position that matters is < L <= BCAP and a segment starts at
-// -skip >= -2^30).  Returns the position after the unit's tokens.
-template <bool PAD>
+// 32-bit path: tokens <= 4 bytes (H = payload of bytes e-3..e in 28 bits),
+// positions in int32 (clamped to 2^30 past L: every position that matters
+// is < L <= BCAP and a segment starts at -skip >= -2^30).  Stored literals
+// add |q| to asum (the region's sum |q| bounds |u|: int32 tiles are exact
+// when it stays below 2^31).  Returns the position after the unit's tokens.
+template <bool PAD, typename QV>
 __device__ __forceinline__ int band_scatter_unit32(const Win24 &W, int at, int L, int ex, uint64_t M,
-                                                   int64_t *__restrict__ q) {
-    // branch-free over the 16 own positions: a literal ending at e is stored
-    // at its position (predicated), every token advances `at` (1 or the run
-    // length); PAD planes place position t at t + t / ex
+                                                   QV *__restrict__ q, uint64_t &asum) {
     uint32_t H = 0;
 #pragma unroll
     for (int j = 4; j < 8; ++j) H = (H >> 7) | ((win_byte(W, j) & 0x7Fu) << 21);
@@ -1107,7 +1118,8 @@ __device__ __forceinline__ int band_scatter_unit32(const Win24 &W, int at, int L
         if (lit && (unsigned)at < (unsigned)L) {
             const uint32_t zz = v - 1u;
             const int idx = PAD ? at + (int)(((uint64_t)(unsigned)at * M) >> 32) : at;
-            q[idx] = (int64_t)(int32_t)((zz >> 1) ^ (0u - (zz & 1u)));
+            q[idx] = (QV)(int32_t)((zz >> 1) ^ (0u - (zz & 1u)));
+            asum += (zz >> 1) + (zz & 1u);
         }
         // positions past L only need to stay past L: clamping at 2^30 keeps
         // at + v (< 2^28 here) inside int32
@@ -1116,20 +1128,21 @@ __device__ __forceinline__ int band_scatter_unit32(const Win24 &W, int at, int L
     return at;
 }
 
-// a unit: 32-bit path unless a 5-byte token ends in it (any lane of the warp)
-// or the position is out of int32 range
-template <bool PAD>
+template <bool PAD, typename QV>
 __device__ __forceinline__ int64_t band_scatter_unit(const Win24 &W, int64_t at, int L, int ex, uint64_t M,
-                                                     int64_t *__restrict__ q, bool active) {
+                                                     QV *__restrict__ q, bool active, uint64_t &asum) {
     const uint32_t C = ~W.E & 0xFFFFFFu;
     const bool long5 = active && ((C << 1) & (C << 2) & (C << 3) & (C << 4) & (W.lit | W.len)) != 0;
     const bool wide = active && (long5 || at < -(1ll << 30));
     if (__any_sync(0xFFFFFFFFu, wide)) {
-        return active ? band_scatter_unit64<PAD>(W, at, L, ex, M, q) : at;
+        return active ? band_scatter_unit64<PAD, QV>(W, at, L, ex, M, q, asum) : at;
     }
-    return active ? (int64_t)band_scatter_unit32<PAD>(W, (int)at, L, ex, M, q) : at;
+    return active ? (int64_t)band_scatter_unit32<PAD, QV>(W, (int)at, L, ex, M, q, asum) : at;
 }
 
+// QV = int32_t: the fast pass (checks the tile's sum |q|); QV = int64_t: the
+// pass over the regions some int32 tile could not hold (asum_reg >= 2^31)
+template <typename QV>
 __global__ void __launch_bounds__(256) k_band(const DecReg *__restrict__ regs, const int32_t *__restrict__ tile_reg,
                                               const uint8_t *__restrict__ blob,
                                               const int64_t *__restrict__ sp_byte,
@@ -1138,21 +1151,26 @@ __global__ void __launch_bounds__(256) k_band(const DecReg *__restrict__ regs, c
                                               int64_t *__restrict__ faces,
                                               int32_t *__restrict__ tflag, unsigned long long *__restrict__ ticket,
                                               const int32_t *__restrict__ order, double *__restrict__ out,
-                                              uint32_t *__restrict__ mask, double iso) {
-    extern __shared__ __align__(16) int64_t Q[];  // [nzv][nyv][rs]
+                                              uint32_t *__restrict__ mask, double iso,
+                                              unsigned long long *__restrict__ asum_reg) {
+    extern __shared__ __align__(16) unsigned char kb_raw[];
+    QV *const Q = reinterpret_cast<QV *>(kb_raw);  // [nzv][nyv][rs]
     __shared__ int64_t ucnt[BDF];                 // dF[nzv][ex]
     __shared__ int64_t s_lo[BSEGM], s_hi[BSEGM], s_ub[BSEGM], s_off[BSEGM];
     __shared__ int32_t s_base[BSEGM + 1];
     __shared__ int64_t s_tile, s_zero;
+    __shared__ unsigned long long s_asum;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid == 0) {
         s_tile = order[atomicAdd(ticket, 1ull)];
         s_zero = 0;
+        s_asum = 0;
     }
     __syncthreads();
     const int64_t tile = s_tile;
     const DecReg &R = regs[tile_reg[tile]];
     if (!((R.codec == 1 || R.codec == 2) && R.err == 0 && !R.slow)) return;
+    if (sizeof(QV) == 8 && asum_reg[tile_reg[tile]] < (1ull << 31)) return;  // done by the int32 pass
     const int nb = R.tny, ex = R.ex, ey = R.ey, rs = R.rs, bty = R.bty, btz = R.btz;
     const int64_t local = tile - R.tile_base;
     const int b = (int)(local % nb), c = (int)(local / nb);
@@ -1207,6 +1225,7 @@ __global__ void __launch_bounds__(256) k_band(const DecReg *__restrict__ regs, c
     const int U = s_base[nzv];
     const uint64_t M = ((1ull << 32) + (uint64_t)ex - 1) / (uint64_t)ex;  // row = (at * M) >> 32
     const int64_t gbase = R.chunk_base * DTHREADS;  // pos64 index of the region's first group
+    uint64_t asum = 0;  // sum |q| of the literals this thread stored
     for (int g0 = warp * 32; g0 < U; g0 += 256) {  // warp-uniform bounds (the unit walk votes)
         const int gi = g0 + lane;
         const bool own = gi < U;
@@ -1219,7 +1238,7 @@ __global__ void __launch_bounds__(256) k_band(const DecReg *__restrict__ regs, c
             const int64_t segstart = ((int64_t)(z0 + j) * ey + y0) * ex;
             at = G <= s_lo[j] ? -s_off[j] : __ldg(pos64 + gbase + grp) - segstart;
         }
-        int64_t *q = Q + j * PL;
+        QV *q = Q + j * PL;
 #pragma unroll 1
         for (int u = 0; u < 4; ++u) {
             const int64_t u0 = G + 16 * u;
@@ -1227,17 +1246,25 @@ __global__ void __launch_bounds__(256) k_band(const DecReg *__restrict__ regs, c
             if (!__any_sync(0xFFFFFFFFu, act)) continue;
             Win24 W;
             if (act) W = win24(blob, u0, s_lo[j], s_hi[j]);
-            at = rs == ex ? band_scatter_unit<false>(W, at, L, ex, M, q, act)
-                          : band_scatter_unit<true>(W, at, L, ex, M, q, act);
+            at = rs == ex ? band_scatter_unit<false, QV>(W, at, L, ex, M, q, act, asum)
+                          : band_scatter_unit<true, QV>(W, at, L, ex, M, q, act, asum);
         }
     }
+#pragma unroll
+    for (int off = 16; off; off >>= 1) asum += __shfl_xor_sync(0xFFFFFFFFu, asum, off);
+    if (lane == 0 && asum) atomicAdd(&s_asum, (unsigned long long)asum);
     __syncthreads();
+    // int32 tile prefixes are exact below 2^31 of sum |q|; else the region is
+    // decoded again by the generic int64 path (this tile still publishes its
+    // faces so the rest of the region's chain completes)
+    if (sizeof(QV) == 4 && tid == 0 && s_asum >= (1ull << 31))
+        atomicMax(asum_reg + tile_reg[tile], (unsigned long long)s_asum);
     // ---- x-prefix (rows are whole)
     const int rows = nzv * nyv;
     if (rows >= 64) {
         for (int r = tid; r < rows; r += 256) {
-            int64_t *p = Q + r * rs;
-            int64_t acc = 0;
+            QV *p = Q + r * rs;
+            QV acc = 0;
             for (int xx = 0; xx < ex; ++xx) {
                 acc += p[xx];
                 p[xx] = acc;
@@ -1245,14 +1272,14 @@ __global__ void __launch_bounds__(256) k_band(const DecReg *__restrict__ regs, c
         }
     } else {
         for (int r = warp; r < rows; r += 8) {
-            int64_t *p = Q + r * rs;
-            int64_t carry = 0;
+            QV *p = Q + r * rs;
+            QV carry = 0;
             for (int x0 = 0; x0 < ex; x0 += 32) {
                 const int xx = x0 + lane;
-                int64_t v = xx < ex ? p[xx] : 0;
+                QV v = xx < ex ? p[xx] : 0;
 #pragma unroll
                 for (int off = 1; off < 32; off <<= 1) {
-                    const int64_t o = __shfl_up_sync(0xFFFFFFFFu, v, off);
+                    const QV o = __shfl_up_sync(0xFFFFFFFFu, v, off);
                     if (lane >= off) v += o;
                 }
                 v += carry;
@@ -1270,8 +1297,8 @@ __global__ void __launch_bounds__(256) k_band(const DecReg *__restrict__ regs, c
     for (int t = tid; t < ex * nzv; t += 256) {
         int j, xx;
         split(t, j, xx);
-        int64_t *p = Q + j * PL + xx;
-        int64_t acc = 0;
+        QV *p = Q + j * PL + xx;
+        QV acc = 0;
         for (int yy = 0; yy < nyv; ++yy) {
             acc += p[yy * rs];
             p[yy * rs] = acc;
@@ -1283,8 +1310,8 @@ __global__ void __launch_bounds__(256) k_band(const DecReg *__restrict__ regs, c
     for (int t = tid; t < L; t += 256) {
         int yy = 0, xx = t;
         if (pad) split(t, yy, xx);
-        int64_t *p = Q + (pad ? yy * rs + xx : t);
-        int64_t acc = 0;
+        QV *p = Q + (pad ? yy * rs + xx : t);
+        QV acc = 0;
         for (int j = 0; j < nzv; ++j) {
             acc += p[j * PL];
             p[j * PL] = acc;
@@ -1330,7 +1357,7 @@ __global__ void __launch_bounds__(256) k_band(const DecReg *__restrict__ regs, c
     double *obase = out + R.out_off + ((int64_t)z0 * ey + y0) * ex;
     auto recon_col = [&](int t, int64_t fz) {
         int xx;
-        const int64_t *p = Q + qidx(t, xx);
+        const QV *p = Q + qidx(t, xx);
         double *o = obase + t;
         if (b > 0) {
             const int64_t *d = dF + xx;
@@ -1390,7 +1417,7 @@ __global__ void __launch_bounds__(256) k_band(const DecReg *__restrict__ regs, c
             const int64_t pw = R.pw;
             uint32_t *w = mp + (wb >> 5) + (int64_t)z0 * pw;
             // inactive lanes read valid shared words (index 0) and store nothing
-            const int64_t *qp = Q + qi;
+            const QV *qp = Q + qi;
             const int64_t *dp = dF + xx;
             double *op = obase + t;
             const int dstep = b > 0 ? ex : 0;
@@ -1443,6 +1470,29 @@ __global__ void __launch_bounds__(256) k_band(const DecReg *__restrict__ regs, c
     }
 }
 
+// regions with a tile whose sum |q| reached 2^31 (its int32 prefixes may
+// have wrapped): k_band<int64_t> decodes them again, overwriting the output
+__global__ void k_asum_check(const DecReg *__restrict__ regs, int64_t nreg,
+                             const unsigned long long *__restrict__ asum, int32_t *__restrict__ any_redo) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= nreg) return;
+    const DecReg &R = regs[r];
+    if ((R.codec == 1 || R.codec == 2) && !R.slow && R.err == 0 && asum[r] >= (1ull << 31)) *any_redo = 1;
+}
+
+// inside-mask words of the regions the int64 pass redoes (its band edges OR
+// into words the int32 pass already wrote)
+__global__ void k_mask_clear(const DecReg *__restrict__ regs, int64_t nreg, const unsigned long long *__restrict__ asum,
+                             uint32_t *__restrict__ mask) {
+    for (int64_t r = blockIdx.y; r < nreg; r += gridDim.y) {
+        if (asum[r] < (1ull << 31)) continue;
+        const DecReg &R = regs[r];
+        const int64_t nw = (int64_t)R.pw * R.ez;
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nw; i += (int64_t)gridDim.x * blockDim.x)
+            mask[R.mask_off + i] = 0;
+    }
+}
+
 // inside masks of the regions k_band did not reconstruct (verbatim codecs,
 // generic path), from their f64 windows: warp per 32-bit word
 __global__ void __launch_bounds__(256) k_mask_rest(const DecReg *__restrict__ regs, int64_t r0,
@@ -1474,6 +1524,7 @@ struct DecPlan {
     int64_t *chunk_samples, *seg_byte, *seg_skip, *esc_base, *carry, *flags;
     int64_t *sp_byte, *sp_skip, *esc_sp, *thr_cnt, *pos64;
     int64_t *faces;
+    unsigned long long *asum;  // per region: max tile sum |q| >= 2^31 (else 0)
     int32_t *tflag, *chunk_reg, *tile_reg, *order;
     int64_t *pair_base, *step_base;
     int64_t ndiag = 0;
@@ -1643,6 +1694,7 @@ static void dec_carve(DecPlan &pl, void *base, size_t cap) {
     pl.thr_cnt = c.take<int64_t>(pl.nchunks * DTHREADS + 1);
     pl.pos64 = c.take<int64_t>(pl.nchunks * DTHREADS + 1);
     pl.faces = c.take<int64_t>(pl.nface + 1);
+    pl.asum = c.take<unsigned long long>(pl.regs.size() + 1);
     pl.tflag = c.take<int32_t>(pl.ntiles + 1);
     pl.chunk_reg = c.take<int32_t>(pl.nchunks + 1);
     pl.tile_reg = c.take<int32_t>(pl.ntiles + 1);
@@ -1651,7 +1703,7 @@ static void dec_carve(DecPlan &pl, void *base, size_t cap) {
     pl.step_base = c.take<int64_t>(pl.ndiag + 1);
     pl.ticket = c.take<unsigned long long>(1);
     pl.ticket3 = c.take<unsigned long long>(1);
-    pl.any_slow = c.take<int32_t>(1);
+    pl.any_slow = c.take<int32_t>(2);  // [0] generic path needed, [1] int64 band pass needed
     pl.ws = c.off + 256;
 }
 
@@ -1716,7 +1768,8 @@ static int decode_impl(const uint8_t *d_blob, const chr_dec_region_t *h, int64_t
                              {pl.flags, sizeof(int64_t) * (pl.nitems + 1)},
                              {pl.ticket, sizeof(unsigned long long)},
                              {pl.ticket3, sizeof(unsigned long long)},
-                             {pl.any_slow, sizeof(int32_t)},
+                             {pl.any_slow, 2 * sizeof(int32_t)},
+                             {pl.asum, sizeof(unsigned long long) * (size_t)(n + 1)},
                              {d_mask, d_mask ? sizeof(uint32_t) * (pl.nmask + 8) : 0},
                              {pl.tflag, sizeof(int32_t) * (pl.ntiles + 1)}},
                             st));
@@ -1769,23 +1822,40 @@ static int decode_impl(const uint8_t *d_blob, const chr_dec_region_t *h, int64_t
             k_tile_order<<<(unsigned)ceil_div(npairs, 256), 256, 0, st>>>(pl.d_regs, pl.pair_base, pl.step_base,
                                                                          npairs, n, pl.order);
         }
-        const int smem = (int)(sizeof(int64_t) * BCAP);
-        CHR_CUDA_TRY(cudaFuncSetAttribute(k_band, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        const int smem = (int)(sizeof(int32_t) * BCAP);
+        CHR_CUDA_TRY(cudaFuncSetAttribute(k_band<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         {
             CHR_PROF("k_band", st);
-            k_band<<<(unsigned)pl.ntiles, 256, smem, st>>>(pl.d_regs, pl.tile_reg, d_blob, pl.sp_byte, pl.sp_skip,
-                                                           pl.esc_sp, pl.pos64, pl.faces, pl.tflag, pl.ticket3,
-                                                           pl.order, d_out, d_mask, iso);
+            k_band<int32_t><<<(unsigned)pl.ntiles, 256, smem, st>>>(
+                pl.d_regs, pl.tile_reg, d_blob, pl.sp_byte, pl.sp_skip, pl.esc_sp, pl.pos64, pl.faces, pl.tflag,
+                pl.ticket3, pl.order, d_out, d_mask, iso, pl.asum);
+        }
+        {
+            CHR_PROF("k_asum_check", st);
+            k_asum_check<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(pl.d_regs, n, pl.asum, pl.any_slow + 1);
         }
     }
-    // ---- generic path (non-canonical streams, rows wider than a band tile):
-    //      skipped unless some region needs it (one 4-byte read-back)
-    int32_t h_any_slow = pl.host_slow ? 1 : 0;
-    if (!h_any_slow) {
-        CHR_CUDA_TRY(d2h(&h_any_slow, pl.any_slow, sizeof(int32_t), st));
-        CHR_CUDA_TRY(stream_sync(st));
+    // ---- generic path (non-canonical streams, rows wider than a band tile)
+    //      and the int64 band pass: skipped unless some region needs them
+    //      (one 8-byte read-back)
+    int32_t h_flags[2] = {0, 0};
+    CHR_CUDA_TRY(d2h(h_flags, pl.any_slow, sizeof(h_flags), st));
+    CHR_CUDA_TRY(stream_sync(st));
+    if (h_flags[1] && pl.ntiles > 0) {  // int64 tiles for the regions an int32 tile could not hold
+        CHR_CUDA_TRY(zero_async({{pl.tflag, sizeof(int32_t) * (pl.ntiles + 1)}, {pl.ticket3, sizeof(unsigned long long)}},
+                                st));
+        if (d_mask) {
+            CHR_PROF("k_mask_clear", st);
+            k_mask_clear<<<dim3(16, (unsigned)std::min<int64_t>(n, 1024)), 256, 0, st>>>(pl.d_regs, n, pl.asum, d_mask);
+        }
+        const int smem = (int)(sizeof(int64_t) * BCAP);
+        CHR_CUDA_TRY(cudaFuncSetAttribute(k_band<int64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        CHR_PROF("k_band64", st);
+        k_band<int64_t><<<(unsigned)pl.ntiles, 256, smem, st>>>(
+            pl.d_regs, pl.tile_reg, d_blob, pl.sp_byte, pl.sp_skip, pl.esc_sp, pl.pos64, pl.faces, pl.tflag,
+            pl.ticket3, pl.order, d_out, d_mask, iso, pl.asum);
     }
-    if (h_any_slow) {
+    if (pl.host_slow || h_flags[0]) {
         {
             CHR_PROF("k_tok_count", st);
             k_tok_count<<<(unsigned)pl.nchunks, DTHREADS, 0, st>>>(pl.d_regs, n, d_blob, pl.chunk_samples);

@@ -318,8 +318,9 @@ def test_decode_tile_shapes(shape):
 
 
 def test_decode_wide_quanta_use_int64_path():
-    """sum|q| >= 2^31 in a region: the int32 band tiles hand it to the int64
-    generic path (|u| < 2^27 still, so no escapes)."""
+    """A tile whose sum |q| >= 2^31: the int32 band pass flags its region and
+    the int64 band pass (k_band<int64_t>) decodes it again (|u| < 2^27
+    still, so no escapes)."""
     g = np.random.default_rng(5).uniform(-1e7, 1e7, size=(20, 20, 20))
     blk = G.compress(g, 0.5)
     assert blk.codec_id == 1
