@@ -10,14 +10,21 @@ P(k)~k^-3, bs32, r=1e-3, k = 99th percentile), the config the north_star
 target is stated on.  value = 4*N / t_step (GB/s of f32 input through the
 whole path), inputs resident in HBM; `e2e` is the same metric with the
 input host->device copy and the archive + mesh device->host copies inside
-the timed region.  Stage throughputs follow SURVEY §8(d).
+the timed region (chr_pipeline, pipelined); `e2e_api` times the drop-in API
+a reference user calls (Volume from host numpy -> build_chr -> request ->
+marching_cubes per region -> merge_meshes, pipeline.py:121-202).  Stage
+throughputs and per-stage rooflines follow SURVEY §8(d).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-Under torchrun (N>1), --mode replica (default): every rank processes its own
-512^3 volume (weak scaling: independent objects) and the ranks all-gather
-per-rank archive bytes / triangle / vertex counts (NCCL) to place their
-outputs; --mode slab: one 512^2 x (512 N) volume in z-slabs through the
-distributed compress of SURVEY 8(e) (see slab_main).
+
+N > 1: ``python bench.py --gpus N`` launches N ranks itself (torchrun,
+127.0.0.1) unless WORLD_SIZE is already set.  Default N>1 workload: one
+c3-recipe volume of 512 x 512 x 512N in z-slabs, one 512^3 slab per GPU
+(weak scaling: per-GPU work = the N=1 workload) through the distributed
+path of SURVEY §8(e): z-slab compress (all-gathers of block stats, stream
+summaries, CRC shares) and per-portion request + marching cubes (all-gathers
+of region z-carries, boundary planes and mesh counts; no payload bytes move).
+``--scaling strong --config c4``: one 1024^3 volume split over the N GPUs.
 """
 
 from __future__ import annotations
@@ -133,26 +140,30 @@ def run_step(vol, dims, bs, cands, r, ws, spacing=(1.0, 1.0, 1.0), stage_events=
 
 
 def kernel_bytes(name, info, N):
-    """Algorithmic bytes per launch of the main kernels."""
-    c_all = info["payload"]
+    """Algorithmic bytes per launch of the main kernels: each
+    kernel's share of its stage's algorithmic bytes -- input reads, archive /
+    window / mesh writes -- never the design's own intermediates (token
+    values, piece records, faces), so a kernel that only moves an
+    intermediate has none (None)."""
+    c_all = info["archive"]
     table = {
-        "k_stats<float>": 4 * N,
+        "k_stats<float>": 4 * N,                # stats read (compress: 8N + C)
         "k_stats_rows": 4 * N,
-        "k_tile<float, false>": 4 * N,
-        "k_quant<float>": 4 * N + 4 * info["n_all"],
-        "k_summarize": 4 * info["n_all"],
-        "k_tile<float, true>": 4 * N + c_all,
-        "k_emit_q<float>": 4 * info["n_all"] + c_all,
-        "k_crc_segments": None,
-        "k_tok_fast": info["c_sel"],
-        "k_seg_locate": info["c_sel"],
+        "k_quant<float>": 4 * N,                # encode read
+        "k_qseg<float>": 4 * N,
+        "k_emit_q<float>": c_all,               # archive write
+        "k_qemit<float>": c_all,
+        "k_tok_fast": info["c_sel"],            # selected payload read (decompress: C_sel + 8 N_sel)
         "k_band": info["c_sel"] + 8 * info["n_sel"],
         "k_lorenzo": info["c_sel"] + 8 * info["n_sel"],
-        "k_mc_mask": 8 * info["n_sel"] + info["n_sel"] // 8,
-        "k_mc_count3": info["n_sel"] // 8,
-        "k_mc_emit3": info["n_sel"] // 8 + 16 * info["nvert"] + 24 * info["nvert"] + 12 * info["ntri"],
+        "k_mc_emit3": 24 * info["nvert"] + 12 * info["ntri"],  # mesh write (MC: 8 N_sel + 24 nv + 12 nt)
     }
     return table.get(name)
+
+
+def stage_roofline(t_ms, alg_bytes, peak):
+    gbs = alg_bytes / (t_ms * 1e-3) / 1e9
+    return {"ms": t_ms, "algorithmic_bytes": int(alg_bytes), "achieved_gbs": gbs, "frac": gbs / peak}
 
 
 def workload_name(config, n, bs, r, cands):
@@ -163,30 +174,63 @@ def workload_name(config, n, bs, r, cands):
         f", bs{bs}, r={r}, k={cands[0]:.6g}; step = compress -> request(k) -> marching cubes")
 
 
-def cpu_baseline(vals_host, dims, bs, cands, r, planes, workers):
-    """The oracle port timed on host cores on a bounded z-slab sample."""
-    from oracle import oracle as O
+def cpu_baseline(vals_host, dims, bs, cands, r, planes, workers, repeats=3):
+    """The reference's CPU path (isochr from baseline/_ref when installed,
+    else the oracle port) on host cores, on a bounded z-slab sample."""
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    import cpu_reference  # noqa: PLC0415
 
-    nx, ny, nz = dims
-    pz = min(planes, nz) if planes > 0 else nz
-    sample = np.ascontiguousarray(vals_host[: nx * ny * pz]).astype(np.float64)
-    sdims = (nx, ny, pz)
-    lo, hi = float(sample.min()), float(sample.max())
-    k = float(min(max(cands[0], lo), hi))
-    t0 = time.perf_counter()
-    arch = O.build_chr(sample, sdims, [k], bs, source_dtype="f32", loose_fraction=r, workers=workers,
-                       out_of_range="warn")
-    t1 = time.perf_counter()
-    sel = O.request(arch, k, workers=workers)
-    t2 = time.perf_counter()
-    O.extract_regions(sel, (1.0, 1.0, 1.0), k)
-    t3 = time.perf_counter()
-    t = t3 - t0
-    return {"value": 4 * nx * ny * pz / t / 1e9, "unit": "GB/s", "cores": workers, "kind": "port",
-            "stages_s": {"build_chr": t1 - t0, "request": t2 - t1, "marching_cubes": t3 - t2},
-            "sample": (f"{nx}x{ny}x{pz} z-slab of the same field (first {pz} planes), same bs/r/k; "
-                       if pz < nz else "the whole workload (same volume, bs, r, k); ") +
-                      f"build_chr + request + per-region MC, {t:.2f} s wall on {workers} threads"}
+    return cpu_reference.time_stages(vals_host, dims, bs, cands[0], r, planes, workers, repeats)
+
+
+def api_e2e(vals, dims, bs, cands, r, steps):
+    """The drop-in path timed end to end (pipeline.py:121-202 calls): a host
+    numpy field -> Volume -> build_chr -> request(k) -> marching_cubes per
+    selected region -> merge_meshes, every result back on the host as the
+    reference's dataclasses.  One warm-up call, then the median of `steps`."""
+    import paper_2408_05462_b200 as G  # noqa: PLC0415
+
+    host = vals.cpu().numpy()
+    k = cands[0]
+
+    def run():
+        vol = G.Volume(dims, values=host, source_dtype="f32")
+        arch = G.build_chr(vol, [k], bs, loose_fraction=r)
+        rs = G.request(arch, k)
+        meshes = [G.marching_cubes(win, vol.spacing, tuple(o * sp for o, sp in zip(reg.sample_origin, vol.spacing)), k)
+                  for reg, win in rs.regions]
+        return G.merge_meshes(meshes)
+
+    run()
+    ts = []
+    for _ in range(steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        m = run()
+        torch.cuda.synchronize()
+        ts.append(time.perf_counter() - t0)
+    t = statistics.median(ts)
+    n = dims[0] * dims[1] * dims[2]
+    return {"value": 4 * n / t / 1e9, "unit": "GB/s", "ms_per_step": t * 1e3, "steps": steps,
+            "h2d_bytes_per_step": 4 * n, "d2h_bytes_per_step": None, "triangles": int(m.num_triangles),
+            "path": "Volume(host f32) -> build_chr -> request -> marching_cubes per region -> merge_meshes "
+                    "(host numpy results, reference dataclasses); wall clock, median"}
+
+
+def launch_ranks(args) -> int:
+    """``--gpus N`` without torchrun: start N ranks on this node (127.0.0.1)."""
+    if torch.cuda.device_count() < args.gpus:
+        print(json.dumps({"metric": METRIC, "error": f"--gpus {args.gpus}: only {torch.cuda.device_count()} "
+                                                      "CUDA device(s) visible"}), flush=True)
+        return 1
+    import socket
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -197,26 +241,44 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c3")
     ap.add_argument("--edge", "--size", dest="n", type=int, default=None, help="edge length override (tests)")
-    ap.add_argument("--cpu-planes", type=int, default=0,
+    ap.add_argument("--cpu-planes", type=int, default=128,
                     help="CPU baseline sample: first P z-planes of the volume (0 = the whole volume)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-copy", default="dma", choices=["dma", "sm"],
                     help="bulk H2D/D2H of the e2e loop: DMA engines or the UVA copy kernel")
-    ap.add_argument("--mode", default="replica", choices=["replica", "slab"],
-                    help="N>1: independent volumes per rank, or one volume in z-slabs (SURVEY 8e)")
+    ap.add_argument("--mode", default="slab", choices=["replica", "slab"],
+                    help="N>1: one volume in z-slabs (SURVEY 8e, default) or independent volumes per rank")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="slab mode: n x n x nN volume (weak) or one n^3 volume split over the ranks (strong)")
+    ap.add_argument("--no-api-e2e", action="store_true", help="skip the drop-in API e2e timing")
+    ap.add_argument("--dist1", action="store_true",
+                    help="run the distributed (slab) path even at N=1 (one NCCL rank)")
     ap.add_argument("--backend", default=None, help="torch.distributed backend (default nccl; gloo for 1-GPU tests)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(launch_ranks(args))
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     dist = None
-    if world > 1:
+    if world > 1 or args.dist1:
         import torch.distributed as dist
 
         torch.cuda.set_device(local % max(1, torch.cuda.device_count()))
-        dist.init_process_group(args.backend or "nccl")
+        if world == 1:  # --dist1: the distributed path on one rank (NCCL branches exercised)
+            import socket
+
+            with socket.socket() as so:
+                so.bind(("127.0.0.1", 0))
+                port = so.getsockname()[1]
+            dist.init_process_group(args.backend or "nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0,
+                                    world_size=1)
+        else:
+            dist.init_process_group(args.backend or "nccl")
     else:
         torch.cuda.set_device(0)
 
@@ -227,7 +289,8 @@ def main():
     workers = len(os.sched_getaffinity(0))
 
     if args.impl == "reference":
-        # the reference's CPU path (oracle port of isochr) on host cores
+        # the reference's CPU path on host cores: the reference package itself
+        # (isochr + numba, installed under baseline/_ref) or, absent, the oracle port
         if rank != 0:
             if dist:
                 dist.barrier()
@@ -236,8 +299,8 @@ def main():
         host = vals.cpu().numpy()
         del vals
         times = []
-        for i in range(args.warmup + args.steps):
-            cb = cpu_baseline(host, dims, bs, cands, r, args.cpu_planes, workers)
+        for i in range(args.warmup + args.steps):  # a step = one run of the sample, every stage once
+            cb = cpu_baseline(host, dims, bs, cands, r, args.cpu_planes, workers, repeats=1)
             if i >= args.warmup:
                 times.append(cb)
         v = statistics.median([t["value"] for t in times])
@@ -248,7 +311,7 @@ def main():
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (seeded torch GRF; no public dataset)",
                 "config": {"workload": workload_name(args.config, n, bs, r, cands), "dims": list(dims),
-                           "block_size": bs},
+                           "block_size": bs, "cpu_sample_planes": pz},
                 "cpu_baseline": dict(times[-1], value=v),
                 "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
@@ -412,9 +475,9 @@ def main():
         alg = kernel_bytes(name, info, N)
         avg = tot / cnt
         achieved = alg / (avg * 1e-3) / 1e9 if alg else None
-        traffic = None
-        tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-        if os.path.exists(tp):
+        traffic = None  # dram bytes of the same kernel on the same config (one ncu --set full capture)
+        tp = os.path.join(ROOT, "profiles", f"ncu_traffic_{args.config}.json")
+        if os.path.exists(tp) and args.n is None:
             try:
                 traffic = json.load(open(tp)).get(name)
             except Exception:
@@ -428,9 +491,26 @@ def main():
                     "gbs": (kernel_bytes(k, info, N) / (t / c * 1e-3) / 1e9) if kernel_bytes(k, info, N) else None}
                 for k, (c, t) in sorted(kern.items(), key=lambda kv: -kv[1][1])}
 
-    cpu = None
+    # per-stage rooflines on SURVEY §8(d)'s algorithmic bytes
+    stage_roof = {
+        "compress": stage_roofline(t_c, 8 * N + info["archive"], peak),
+        "decompress": stage_roofline(t_d, info["c_sel"] + 8 * info["n_sel"], peak),
+        "marching_cubes": stage_roofline(t_m, 8 * info["n_sel"] + 24 * info["nvert"] + 12 * info["ntri"], peak),
+        "step": stage_roofline(ms, 8 * N + info["archive"] + info["c_sel"] + 16 * info["n_sel"] +
+                               24 * info["nvert"] + 12 * info["ntri"], peak),
+        "peak_gbs": peak, "peak_source": peak_src,
+    }
+
+    # drop-in API e2e: what a reference user calls, host numpy in and out
+    api = None
+    if not args.no_api_e2e:
+        api = api_e2e(vals, dims, bs, cands, r, max(1, min(args.steps, 3)))
+
+    cpu = cpu1 = None
     if rank == 0 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(vals.cpu().numpy(), dims, bs, cands, r, args.cpu_planes, workers)
+        host_vals = vals.cpu().numpy()
+        cpu = cpu_baseline(host_vals, dims, bs, cands, r, args.cpu_planes, workers)
+        cpu1 = cpu_baseline(host_vals, dims, bs, cands, r, args.cpu_planes, 1)
 
     value = world * 4 * N / (ms * 1e-3) / 1e9
     line = {
@@ -443,16 +523,18 @@ def main():
             "archive_bytes": info["archive"], "selected_samples": info["n_sel"], "cells": info["cells"],
             "triangles": info["ntri"], "vertices": info["nvert"],
             "l2": "no flush: input (4N bytes) and decoded windows (8 N_sel bytes) are each larger than the 126 MB L2",
-            "per_rank": "independent 512^3 volume per rank (seed = rank) + NCCL all_gather of sizes",
         },
         "stages": {
             "compress_ms": t_c, "compress_gbs": 4 * N / (t_c * 1e-3) / 1e9,
             "request_ms": t_d, "decompress_gbs": 4 * info["n_sel"] / (t_d * 1e-3) / 1e9,
             "mc_ms": t_m, "mc_cells_per_s": info["cells"] / (t_m * 1e-3),
+            "roofline": stage_roof,
         },
         "kernels": kern_tab,
         "roofline": roof,
         "cpu_baseline": cpu,
+        "cpu_baseline_1core": cpu1,
+        "e2e_api": api,
         "e2e": {"value": world * 4 * N / (e2e * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": e2e,
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": int(launches),
@@ -467,16 +549,18 @@ def main():
 
 
 def slab_main(args, dist, rank, world, local, n, workers):
-    """N>1, one volume of n x n x (n * world) samples in z-slabs (weak
-    scaling): distributed compress (block-stats / stream-summary
-    / CRC-share all-gathers), every rank keeping its slice of the file;
-    request + marching cubes split by region, the owned payloads gathered by
-    one all-to-all, with the per-region count all-gather.  Times are the max
-    over ranks."""
+    """N>1, one volume in z-slabs: weak scaling n x n x (n N)
+    (default: per-GPU work = the N=1 workload) or strong scaling n^3 split
+    over the ranks.  Step = distributed compress (block-stats / stream-summary
+    / CRC-share all-gathers; every rank writes its slice of the file) ->
+    per-portion request + marching cubes (every rank decodes and meshes its
+    own planes; all-gathers of z-carry planes, boundary planes, CRC shares
+    and mesh counts; no payload bytes move).  Times are the max over ranks."""
     from paper_2408_05462_b200 import _abi, multi, synth
     from paper_2408_05462_b200 import device as D
 
-    full, dims, bs, cands, r = synth.make_config(args.config, device="cuda", n=n, nz=n * world, seed=0)
+    nz_total = n * world if args.scaling == "weak" else n
+    full, dims, bs, cands, r = synth.make_config(args.config, device="cuda", n=n, nz=nz_total, seed=0)
     nx, ny, nz = dims
     slab = multi.slab_of(nz, bs, world, rank)
     vol = full[slab.z_base * nx * ny: (slab.z_base + slab.nz_local) * nx * ny].clone()
@@ -486,40 +570,32 @@ def slab_main(args, dist, rank, world, local, n, workers):
     L = _abi.lib()
     k = cands[0]
 
-    def step(ev=None):
+    def step(ev=None, v=None):
         if ev:
             ev[0].record()
-        res = multi.build_archive_slab(vol, dims, slab, cands, bs, loose_fraction=r, ws=ws)
+        res = multi.build_archive_slab(vol if v is None else v, dims, slab, cands, bs, loose_fraction=r, ws=ws)
         if ev:
             ev[1].record()
-        # each rank keeps its slice of the archive (it writes those bytes to the
-        # file); the owned payloads of the request come from one all-to-all
+        m = multi.request_extract_portions(res, 0, k, ws=ws)
         if ev:
             ev[2].record()
-        m = multi.request_extract_slab(res, res.regions, 0, k, ws=ws, dims=dims, bs=bs)
-        if ev:
-            ev[3].record()
-        return res, None, m
+        return res, m
 
     for _ in range(args.warmup):
-        res, f, m = step()
+        res, m = step()
     torch.cuda.synchronize()
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     dist.barrier()
     torch.cuda.synchronize()
-    L.chr_prof_enable(1)
-    _abi.prof_report()
     l0 = L.chr_launch_count()
     with Clocks(local % max(1, torch.cuda.device_count())) as clk:
         a.record()
         for i in range(args.steps):
-            res, f, m = step(evs[i])
+            res, m = step(evs[i])
         b.record()
         torch.cuda.synchronize()
     launches = L.chr_launch_count() - l0
-    L.chr_prof_enable(0)
-    kern = _abi.prof_report()
 
     def maxr(x):
         t = torch.tensor([x], dtype=torch.float64, device="cuda" if dist.get_backend() == "nccl" else "cpu")
@@ -527,30 +603,37 @@ def slab_main(args, dist, rank, world, local, n, workers):
         return float(t.item())
 
     ms = maxr(a.elapsed_time(b) / args.steps)
-    st = [(e[0].elapsed_time(e[1]), e[1].elapsed_time(e[2]), e[2].elapsed_time(e[3])) for e in evs]
+    st = [(e[0].elapsed_time(e[1]), e[1].elapsed_time(e[2])) for e in evs]
     t_c = maxr(statistics.median(x[0] for x in st))
-    t_a = maxr(statistics.median(x[1] for x in st))
-    t_rm = maxr(statistics.median(x[2] for x in st))
-    # e2e: H2D of this rank's slab, D2H of its mesh rows (+ the file on rank 0)
+    t_rm = maxr(statistics.median(x[1] for x in st))
+    # per-kernel table: the same K steps again with the library's profiler on
+    dist.barrier()
+    torch.cuda.synchronize()
+    L.chr_prof_enable(1)
+    _abi.prof_report()
+    for i in range(args.steps):
+        step()
+    torch.cuda.synchronize()
+    L.chr_prof_enable(0)
+    kern = _abi.prof_report()
+    # e2e: H2D of this rank's slab, D2H of its mesh rows and its share of the file
     host_in = torch.empty(vol.numel(), dtype=torch.float32, pin_memory=True)
     host_in.copy_(vol)
     dvol = torch.empty_like(vol)
     e2e = []
+    h2d = d2h = 0
     for i in range(args.warmup + args.steps):
         dist.barrier()
         torch.cuda.synchronize()
         ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ea.record()
         dvol.copy_(host_in, non_blocking=True)
-        vol, saved = dvol, vol
-        res, f, m = step()
-        vol = saved
+        res, m = step(v=dvol)
         hv = m.verts.cpu()
         ht = m.tris.cpu()
-        # this rank's share of the file: the payloads it wrote (+ header/table on rank 0)
         contrib = multi.contributors(res.regions, dims, bs, world)[:, rank]
         rs = res.regions[contrib]
-        parts = [res.blob[int(o): int(o) + int(b)] for o, b in zip(rs["block_offset"], rs["block_nbytes"])]
+        parts = [res.blob[int(o): int(o) + int(c)] for o, c in zip(rs["block_offset"], rs["block_nbytes"])]
         if rank == 0:
             parts.append(res.blob[: D.header_table_nbytes(len(cands), len(res.regions))])
         hf = torch.cat(parts).cpu() if parts else None
@@ -558,6 +641,8 @@ def slab_main(args, dist, rank, world, local, n, workers):
         torch.cuda.synchronize()
         if i >= args.warmup:
             e2e.append(ea.elapsed_time(eb))
+        h2d = 4 * vol.numel()
+        d2h = int(hv.numel() * 8 + ht.numel() * 4 + (hf.numel() if hf is not None else 0))
     e2e_ms = maxr(statistics.median(e2e))
     Ntot = nx * ny * nz
     sel = res.regions[(res.regions["mask"] & np.uint64(1)) != 0]
@@ -569,10 +654,11 @@ def slab_main(args, dist, rank, world, local, n, workers):
     line = {
         "metric": METRIC, "value": 4 * Ntot / (ms * 1e-3) / 1e9, "unit": "GB/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded torch GRF; no public dataset)",
-        "config": {"workload": f"{args.config} recipe on {nx}x{ny}x{nz} f32 ({n}^3 per GPU) in z-slabs; step = "
-                               "slab compress -> request(k) + marching cubes split by region (payloads by all-to-all)",
+        "config": {"workload": f"{args.config} recipe on {nx}x{ny}x{nz} f32 in z-slabs over {world} GPUs "
+                               f"({args.scaling} scaling); step = slab compress -> per-portion request(k) + "
+                               "marching cubes (no payload bytes move between ranks)",
                    "dims": list(dims), "block_size": bs, "k": k, "regions": int(len(res.regions)),
                    "regions_selected": int(len(sel)), "archive_bytes": int(res.nbytes),
                    "triangles": m.ntri_total, "vertices": m.nvert_total, "parallelism": f"zslab{world}",
@@ -585,8 +671,7 @@ def slab_main(args, dist, rank, world, local, n, workers):
                      "note": "per-kernel roofline is reported by the N=1 run"},
         "cpu_baseline": None,
         "e2e": {"value": 4 * Ntot / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": e2e_ms,
-                "h2d_bytes_per_step": 4 * vol.numel(),
-                "d2h_bytes_per_step": int(hv.numel() * 8 + ht.numel() * 4 + (hf.numel() if hf is not None else 0))},
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }

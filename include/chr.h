@@ -98,8 +98,9 @@ typedef struct {
 typedef struct {
     uint64_t grid_offset;      /* element offset of the f64 window (x fastest) */
     int32_t dims[3];           /* samples per axis, each >= 2 */
-    int32_t _pad;
-    double origin[3];          /* world origin of lattice point (0,0,0) */
+    int32_t zoff;              /* lattice z of grid plane 0 (0 for a whole window; a z-slab
+                                  portion grid sets its plane offset in the region window) */
+    double origin[3];          /* world origin of lattice point (0,0,0) of the region window */
     double spacing[3];
 } chr_mc_grid_t;
 
@@ -192,6 +193,13 @@ int chr_mc_emit(const double *d_grids, const chr_mc_grid_t *h_grids, int64_t n, 
                 void *d_workspace, size_t workspace_bytes, double *d_verts, int32_t *d_tris,
                 void *stream);
 
+/*    chr_mc_emit plus every vertex's canonical edge (grid-local
+ *    ((z * ny + y) * nx + x) * 3 + axis) in d_vedge (nv int64): the z-slab
+ *    request matches the vertices of a plane two ranks share by it. */
+int chr_mc_emit_edges(const double *d_grids, const chr_mc_grid_t *h_grids, int64_t n, double k,
+                      void *d_workspace, size_t workspace_bytes, double *d_verts, int32_t *d_tris,
+                      int64_t *d_vedge, void *stream);
+
 /* 6. per-cell case codes of one grid (isosurf.case_field, isosurf.py:77-88
  *    when binary_order != 0; Bourke order of mc_extract otherwise). */
 int chr_case_codes(const double *d_grid, int64_t nx, int64_t ny, int64_t nz, double k,
@@ -202,6 +210,14 @@ size_t chr_crc32_workspace_size(uint64_t n);
 int chr_crc32(const uint8_t *d_buf, uint64_t n, void *d_workspace, size_t workspace_bytes,
               uint32_t *h_crc, void *stream);
 uint32_t chr_crc32_combine(uint32_t crc1, uint32_t crc2, uint64_t len2);
+/*    n byte ranges [begin, end) (h_ranges: 2n u64) of one buffer in one
+ *    launch: h_raw = raw registers (init 0, no final xor; shares of disjoint
+ *    ranges XOR after chr_crc32_shift), h_crc = zlib.crc32 per range (either
+ *    may be NULL).  Synchronises. */
+size_t chr_crc32_segments_workspace_size(int64_t n);
+int chr_crc32_segments(const uint8_t *d_buf, const uint64_t *h_ranges, int64_t n, void *d_workspace,
+                       size_t workspace_bytes, uint32_t *h_raw, uint32_t *h_crc, void *stream);
+uint32_t chr_crc32_shift(uint32_t raw, uint64_t len);
 
 /* 8. kernel seam (isochr/kernels.py) on single windows */
 int chr_min_abs_distance(const double *d_flat, int64_t n, double k, double *h_out,
@@ -252,6 +268,14 @@ int chr_dcompress_headers(int64_t nx, int64_t ny, int64_t nz, int source_dtype, 
                           int64_t block_size, double vmin, double vmax, const double *h_cands, int m,
                           chr_region_t *h_regions, int64_t n_regions, const uint32_t *h_raw_all,
                           void *d_workspace, size_t workspace_bytes, uint8_t *d_out, void *stream);
+
+/* 10b. z-slab request: finish n portions decoded with e = 1/2 (u_local as
+ *     exact integers in f64) in place: u = u_local + carry plane (int64 at
+ *     d_carry + carry_offset, ex*ey entries; carry_offset < 0: none), then
+ *     recon = u * 2e with the region's bound e.  Workspace: 48 * n bytes. */
+int chr_portion_finish(double *d_windows, const uint64_t *h_out_offset, const int64_t *h_plane,
+                       const int64_t *h_nplanes, const int64_t *h_carry_offset, const double *h_error_bound,
+                       int64_t n, const int64_t *d_carry, void *d_workspace, size_t workspace_bytes, void *stream);
 
 /* 13. SURVEY 8(f2): accuracy < 1 and paper_edges bounds.  For every pair
  *     (window [ox,oy,oz,ex,ey,ez], candidate k) the n-th smallest of the

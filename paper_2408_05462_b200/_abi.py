@@ -87,7 +87,7 @@ class McGrid(ctypes.Structure):
     _fields_ = [
         ("grid_offset", ctypes.c_uint64),
         ("dims", ctypes.c_int32 * 3),
-        ("_pad", ctypes.c_int32),
+        ("zoff", ctypes.c_int32),
         ("origin", ctypes.c_double * 3),
         ("spacing", ctypes.c_double * 3),
     ]
@@ -101,7 +101,7 @@ PORTION_DT = np.dtype([("len", "<i8"), ("lead", "<i8"), ("trail", "<i8"), ("byte
                        ("nz", "<i4"), ("f32ok", "<i4")])  # chr_portion_t
 DEC_DT = np.dtype([("payload_offset", "<u8"), ("payload_nbytes", "<u8"), ("codec_id", "<i4"), ("dims", "<i4", 3),
                    ("error_bound", "<f8"), ("crc", "<u4"), ("_pad", "<u4"), ("out_offset", "<u8")], align=True)
-MCGRID_DT = np.dtype([("grid_offset", "<u8"), ("dims", "<i4", 3), ("_pad", "<i4"), ("origin", "<f8", 3),
+MCGRID_DT = np.dtype([("grid_offset", "<u8"), ("dims", "<i4", 3), ("zoff", "<i4"), ("origin", "<f8", 3),
                       ("spacing", "<f8", 3)], align=True)
 AFTER_COMPRESS = ctypes.CFUNCTYPE(None, ctypes.c_uint64, ctypes.c_void_p)  # chr_after_compress_fn
 STITCH_DT = np.dtype([("window_offset", "<u8"), ("origin", "<i4", 3), ("extent", "<i4", 3), ("block_lo", "<i4", 3),
@@ -179,6 +179,16 @@ def lib():
         L.chr_crc32_workspace_size.restype = SZ
         L.chr_crc32.argtypes = [P, U64, P, SZ, P, P]
         L.chr_crc32.restype = INT
+        L.chr_crc32_segments_workspace_size.argtypes = [I64]
+        L.chr_crc32_segments_workspace_size.restype = SZ
+        L.chr_crc32_segments.argtypes = [P, P, I64, P, SZ, P, P, P]
+        L.chr_crc32_segments.restype = INT
+        L.chr_crc32_shift.argtypes = [ctypes.c_uint32, U64]
+        L.chr_crc32_shift.restype = ctypes.c_uint32
+        L.chr_mc_emit_edges.argtypes = [P, P, I64, D, P, SZ, P, P, P, P]
+        L.chr_mc_emit_edges.restype = INT
+        L.chr_portion_finish.argtypes = [P, P, P, P, P, P, I64, P, P, SZ, P]
+        L.chr_portion_finish.restype = INT
         L.chr_crc32_combine.argtypes = [ctypes.c_uint32, ctypes.c_uint32, U64]
         L.chr_crc32_combine.restype = ctypes.c_uint32
         L.chr_min_abs_distance.argtypes = [P, I64, D, P, P, SZ, P]
@@ -257,7 +267,8 @@ EXPORTS = [
     "chr_prof_mark", "chr_copy", "chr_request_tables", "chr_pipeline",
     "chr_dcompress_workspace_size", "chr_dcompress_local", "chr_dcompress_finish", "chr_dcompress_headers",
     "chr_abi_version", "chr_status_string", "chr_num_blocks", "chr_stats", "chr_plan", "chr_merge_keys",
-    "chr_value_range",
+    "chr_value_range", "chr_crc32_segments_workspace_size", "chr_crc32_segments", "chr_crc32_shift",
+    "chr_mc_emit_edges", "chr_portion_finish",
     "chr_compress_workspace_size", "chr_compress_capacity", "chr_compress",
     "chr_decode_workspace_size", "chr_decode_regions", "chr_mc_workspace_size", "chr_mc_count",
     "chr_mc_emit", "chr_case_codes", "chr_crc32_workspace_size", "chr_crc32", "chr_crc32_combine",

@@ -264,12 +264,18 @@ def request(archive: CHRArchive, k: float, accuracy=None, drop_pruned: bool = Tr
     if not builtin:
         arrays = decompress_many([r.block for r in regs])
     else:
+        # one D2H of every window; each region's array is a read-only
+        # Fortran-order view of it, and marching_cubes on such a view reads
+        # the device copy instead of uploading it again (device.host_window)
         host = windows.cpu().numpy() if regs else None
         arrays = []
+        if regs:
+            host.setflags(write=False)
+            device.register_host_windows(host, windows)
         for r, o in zip(regs, woffs):
             d = r.block.dims
             n = d[0] * d[1] * d[2]
-            arrays.append(host[o:o + n].reshape(d, order="F").copy())
+            arrays.append(host[o:o + n].reshape(d, order="F"))
     dev = (windows, list(woffs), archive.block_size) if builtin and regs else None
     return ReconstructionSet(tuple(zip(regs, arrays)), report, dev)
 

@@ -10,7 +10,9 @@
 // Superchunk CRCs are shifted to the segment end and XOR-accumulated, so
 // any number of warps can work on one segment.  Loads are 128-byte
 // coalesced 32-bit words.
+#include <algorithm>
 #include <mutex>
+#include <vector>
 
 #include "chr_common.cuh"
 #include "chr_internal.cuh"
@@ -206,6 +208,53 @@ extern "C" int chr_crc32(const uint8_t *d_buf, uint64_t n, void *d_ws, size_t ws
     CHR_CUDA_TRY(stream_sync(st));
     *h_crc = crc_finalize(H.x2n, raw, n);
     return CHR_OK;
+}
+
+extern "C" size_t chr_crc32_segments_workspace_size(int64_t n) {
+    CHR_XFER_SCOPE;
+    return n < 1 ? 256 : (size_t)(n + 1) * (sizeof(CrcSeg) + sizeof(uint32_t)) + 512;
+}
+
+// CRC-32 of n byte ranges [begin, end) of one device buffer, one launch:
+// h_raw (may be NULL) = the raw register (init 0, no final xor; linear, so
+// shares of disjoint ranges XOR after shifting), h_crc (may be NULL) =
+// zlib.crc32 of each range.  Synchronises.
+extern "C" int chr_crc32_segments(const uint8_t *d_buf, const uint64_t *h_ranges, int64_t n, void *d_ws,
+                                  size_t ws_bytes, uint32_t *h_raw, uint32_t *h_crc, void *stream) {
+    CHR_XFER_SCOPE;
+    if (n < 0 || (n && (!h_ranges || !d_buf))) return CHR_E_PARAMETER;
+    if (n == 0) return CHR_OK;
+    if (!d_ws || ws_bytes < chr_crc32_segments_workspace_size(n)) return CHR_E_WORKSPACE;
+    cudaStream_t st = (cudaStream_t)stream;
+    const CrcTables &H = crc_tables_hostref();
+    std::vector<CrcSeg> segs((size_t)n);
+    for (int64_t i = 0; i < n; ++i) {
+        segs[i].begin = h_ranges[2 * i];
+        segs[i].end = std::max(h_ranges[2 * i], h_ranges[2 * i + 1]);
+    }
+    const int64_t total_sc = crc_plan_segments(segs.data(), n);
+    CrcSeg *d_seg = reinterpret_cast<CrcSeg *>(d_ws);
+    uint32_t *d_raw = reinterpret_cast<uint32_t *>(reinterpret_cast<char *>(d_ws) +
+                                                   ((sizeof(CrcSeg) * (size_t)n + 255) & ~size_t(255)));
+    CHR_CUDA_TRY(h2d(d_seg, segs.data(), sizeof(CrcSeg) * (size_t)n, st));
+    CHR_CUDA_TRY(fill_async(d_raw, 0, 4 * (size_t)n, st));
+    int rc = crc_launch(d_buf, d_seg, n, total_sc, d_raw, st);
+    if (rc) return rc;
+    std::vector<uint32_t> raw((size_t)n);
+    CHR_CUDA_TRY(d2h(raw.data(), d_raw, 4 * (size_t)n, st));
+    CHR_CUDA_TRY(stream_sync(st));
+    for (int64_t i = 0; i < n; ++i) {
+        if (h_raw) h_raw[i] = raw[i];
+        if (h_crc) h_crc[i] = segs[i].end > segs[i].begin ? crc_finalize(H.x2n, raw[i], segs[i].end - segs[i].begin) : 0;
+    }
+    return CHR_OK;
+}
+
+// raw register of a range shifted by `len` more bytes (zeros) after it: the
+// share of a range inside a longer buffer (chr_crc32_segments' raw values)
+extern "C" uint32_t chr_crc32_shift(uint32_t raw, uint64_t len) {
+    CHR_XFER_SCOPE;
+    return crc_shift(crc_tables_hostref().x2n, raw, len);
 }
 
 extern "C" uint32_t chr_crc32_combine(uint32_t crc1, uint32_t crc2, uint64_t len2) {

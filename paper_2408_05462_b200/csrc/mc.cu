@@ -123,7 +123,8 @@ struct McGrid {
     int64_t ntri, nvert;
     int64_t mask_off;               // inside mask (v >= k): word offset, plane-linear bits
     int64_t mask_item_base;         // k_mc_mask items: planes x ceil(pw / 64)
-    int32_t pw, pad2;               // mask words per plane
+    int32_t pw;                     // mask words per plane
+    int32_t zoff;                   // lattice z of grid plane 0 (sub-grid of a region window)
 };
 
 struct McPieceCnt {
@@ -612,7 +613,8 @@ __global__ void __launch_bounds__(E3W * 32, 4) k_mc_emit3(const double *__restri
                                                        const McPieceCnt *__restrict__ cnt,
                                                        const uint32_t *__restrict__ mask,
                                                        unsigned long long *__restrict__ queue, int64_t nbatch,
-                                                       double *__restrict__ verts, int32_t *__restrict__ tris) {
+                                                       double *__restrict__ verts, int32_t *__restrict__ tris,
+                                                       int64_t *__restrict__ vedge) {
     __shared__ __align__(16) int8_t s_tri[256][16];
     __shared__ __align__(16) uint8_t s_ntri[256];
     __shared__ __align__(16) uint8_t s_own[256][8];
@@ -874,9 +876,12 @@ __global__ void __launch_bounds__(E3W * 32, 4) k_mc_emit3(const double *__restri
                 const double s1 = __ldg(sp + (a == 0 ? 1 : (a == 1 ? (int64_t)g.nx : nxy)));
                 const double den = __dadd_rn(s1, -s0);
                 const double t = den == 0.0 ? 0.0 : __ddiv_rn(__dadd_rn(k, -s0), den);
-                double lat[3] = {(double)(cx + lx), (double)(cy + ly), (double)(cz + lz)};
+                double lat[3] = {(double)(cx + lx), (double)(cy + ly), (double)(cz + lz + g.zoff)};
                 lat[a] = __dadd_rn(lat[a], t);
-                double *o = verts + 3 * (g.vert_base + S.vb[0][cc] + rk);
+                const int64_t vid = g.vert_base + S.vb[0][cc] + rk;
+                double *o = verts + 3 * vid;
+                if (vedge)  // canonical edge of the vertex, grid-local: ((z * ny + y) * nx + x) * 3 + axis
+                    vedge[vid] = (((int64_t)(cz + lz) * g.ny + (cy + ly)) * g.nx + (cx + lx)) * 3 + a;
                 o[0] = world(g.origin[0], lat[0], g.spacing[0]);
                 o[1] = world(g.origin[1], lat[1], g.spacing[1]);
                 o[2] = world(g.origin[2], lat[2], g.spacing[2]);
@@ -935,6 +940,7 @@ static bool mc_build(const chr_mc_grid_t *h, int64_t n, McPlan &pl) {
             g.origin[a] = h[i].origin[a];
             g.spacing[a] = h[i].spacing[a];
         }
+        g.zoff = h[i].zoff;
         g.piece_base = piece;
         g.npieces = (int64_t)g.ntx * g.ncy * g.ncz;
         if (g.npieces >= (int64_t(1) << 31)) return false;  // piece indices are int32 in the kernels
@@ -1005,7 +1011,8 @@ static int mc_count_impl(const double *d_grids, const chr_mc_grid_t *h, int64_t 
                          void *d_ws, size_t ws_bytes, int64_t *h_ntri, int64_t *h_nvert, int64_t *h_total_tri,
                          int64_t *h_total_vert, void *stream);
 static int mc_emit_impl(const double *d_grids, const chr_mc_grid_t *h, int64_t n, double k, const uint32_t *d_masks,
-                        void *d_ws, size_t ws_bytes, double *d_verts, int32_t *d_tris, void *stream);
+                        void *d_ws, size_t ws_bytes, double *d_verts, int32_t *d_tris, int64_t *d_vedge,
+                        void *stream);
 
 extern "C" int chr_mc_count(const double *d_grids, const chr_mc_grid_t *h, int64_t n, double k, void *d_ws,
                             size_t ws_bytes, int64_t *h_ntri, int64_t *h_nvert, int64_t *h_total_tri,
@@ -1027,7 +1034,7 @@ extern "C" int chr_mc_emit_masked(const double *d_grids, const chr_mc_grid_t *h,
                                   int32_t *d_tris, void *stream) {
     CHR_XFER_SCOPE;
     if (!d_masks) return CHR_E_PARAMETER;
-    return mc_emit_impl(d_grids, h, n, k, d_masks, d_ws, ws_bytes, d_verts, d_tris, stream);
+    return mc_emit_impl(d_grids, h, n, k, d_masks, d_ws, ws_bytes, d_verts, d_tris, nullptr, stream);
 }
 
 static int mc_count_impl(const double *d_grids, const chr_mc_grid_t *h, int64_t n, double k, const uint32_t *d_masks,
@@ -1100,11 +1107,21 @@ static int mc_count_impl(const double *d_grids, const chr_mc_grid_t *h, int64_t 
 extern "C" int chr_mc_emit(const double *d_grids, const chr_mc_grid_t *h, int64_t n, double k, void *d_ws,
                            size_t ws_bytes, double *d_verts, int32_t *d_tris, void *stream) {
     CHR_XFER_SCOPE;
-    return mc_emit_impl(d_grids, h, n, k, nullptr, d_ws, ws_bytes, d_verts, d_tris, stream);
+    return mc_emit_impl(d_grids, h, n, k, nullptr, d_ws, ws_bytes, d_verts, d_tris, nullptr, stream);
+}
+
+// chr_mc_emit that also writes every vertex's canonical edge (grid-local
+// ((z * ny + y) * nx + x) * 3 + axis, int64) -- the z-slab request matches
+// vertices on the planes two ranks share by it
+extern "C" int chr_mc_emit_edges(const double *d_grids, const chr_mc_grid_t *h, int64_t n, double k, void *d_ws,
+                                 size_t ws_bytes, double *d_verts, int32_t *d_tris, int64_t *d_vedge, void *stream) {
+    CHR_XFER_SCOPE;
+    return mc_emit_impl(d_grids, h, n, k, nullptr, d_ws, ws_bytes, d_verts, d_tris, d_vedge, stream);
 }
 
 static int mc_emit_impl(const double *d_grids, const chr_mc_grid_t *h, int64_t n, double k, const uint32_t *d_masks,
-                        void *d_ws, size_t ws_bytes, double *d_verts, int32_t *d_tris, void *stream) {
+                        void *d_ws, size_t ws_bytes, double *d_verts, int32_t *d_tris, int64_t *d_vedge,
+                        void *stream) {
     if (n == 0) return CHR_OK;
     if (!d_grids || !h || n < 0) return CHR_E_PARAMETER;
     cudaStream_t st = (cudaStream_t)stream;
@@ -1120,7 +1137,7 @@ static int mc_emit_impl(const double *d_grids, const chr_mc_grid_t *h, int64_t n
         CHR_PROF("k_mc_emit3", st);
         k_mc_emit3<<<(unsigned)ctas, E3W * 32, 0, st>>>(d_grids, pl.d_grids, pl.chunk_grid, k, T, pl.base, pl.cnt,
                                                         d_masks ? d_masks : pl.mask, mc_queue(pl), nbatch, d_verts,
-                                                        d_tris);
+                                                        d_tris, d_vedge);
     }
     CHR_CUDA_TRY(cudaGetLastError());
     CHR_CUDA_TRY(stream_sync(st));

@@ -16,6 +16,8 @@ from __future__ import annotations
 
 import ctypes
 import math
+import threading
+import weakref
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -74,6 +76,33 @@ def stats(vol: torch.Tensor, dims, bs: int, cands) -> tuple[torch.Tensor, torch.
     check(lib().chr_stats(ptr(vol), _dtype_code(vol), *dims, bs, _np_ptr(cands), cands.size,
                           ptr(out), ptr(bad), stream_ptr()), "chr_stats")
     return out, bad
+
+
+# host copies of decoded windows -> their device originals (request()):
+# a window array handed back to marching_cubes is meshed from HBM directly
+_HOST_WINDOWS: dict = {}
+
+
+def register_host_windows(host: np.ndarray, dev: torch.Tensor) -> None:
+    """Remember that read-only `host` is a D2H copy of f64 `dev` (same length)."""
+    key = id(host)
+    _HOST_WINDOWS[key] = (host.ctypes.data, host.size, dev)
+    weakref.finalize(host, _HOST_WINDOWS.pop, key, None)
+
+
+def host_window(a: np.ndarray) -> torch.Tensor | None:
+    """The device f64 copy of `a` (x fastest) if `a` is a Fortran-order view
+    into a registered host window buffer, else None."""
+    root = a
+    while isinstance(root.base, np.ndarray):
+        root = root.base
+    ent = _HOST_WINDOWS.get(id(root))
+    if ent is None or ent[0] != root.ctypes.data or a.dtype != np.float64 or not a.flags.f_contiguous:
+        return None
+    off = (a.ctypes.data - ent[0]) // 8
+    if off < 0 or off + a.size > ent[1]:
+        return None
+    return ent[2][off: off + a.size]
 
 
 def value_range(vol: torch.Tensor) -> tuple[float, float, int]:
@@ -144,7 +173,26 @@ class Workspaces:
         return t
 
 
-_DEFAULT_WS = Workspaces()
+class _ThreadWorkspaces:
+    """The default workspaces, one set per host thread: the reference runs
+    request / decompress under a ThreadPoolExecutor (chr_archive.py:253-255),
+    and a shared scratch buffer would let one thread's decode overwrite
+    another's (the C library's own host state is thread-local too)."""
+
+    def __init__(self):
+        self._tls = threading.local()
+
+    def _get(self) -> Workspaces:
+        ws = getattr(self._tls, "ws", None)
+        if ws is None:
+            ws = self._tls.ws = Workspaces()
+        return ws
+
+    def __getattr__(self, name):
+        return getattr(self._get(), name)
+
+
+_DEFAULT_WS = _ThreadWorkspaces()
 
 
 BOUND_MODES = {"strict_vertices": 0, "paper_edges": 1}
@@ -461,12 +509,14 @@ def mc_table(grid_offset, dims, origin, spacing) -> np.ndarray:
 
 
 def marching(grids: torch.Tensor, descs, k: float, ws: Workspaces | None = None, reuse_outputs: bool = False,
-             masks: torch.Tensor | None = None):
+             masks: torch.Tensor | None = None, edges: bool = False):
     """Marching cubes over several f64 windows of `grids`, merged.
 
     ``descs``: a ``_abi.MCGRID_DT`` table (:func:`mc_table`) or a list of
     (element_offset, (nx,ny,nz), origin3, spacing3).
-    Returns (verts f64 [nv,3], tris int32 [nt,3], ntri per grid, nvert per grid)."""
+    Returns (verts f64 [nv,3], tris int32 [nt,3], ntri per grid, nvert per grid)
+    (+ the int64 canonical edge of every vertex with ``edges=True``,
+    chr_mc_emit_edges: grid-local ((z * ny + y) * nx + x) * 3 + axis)."""
     ws = ws or _DEFAULT_WS
     L = lib()
     dev = _abi.device()
@@ -478,8 +528,9 @@ def marching(grids: torch.Tensor, descs, k: float, ws: Workspaces | None = None,
             descs = mc_table(off, dims, org, spc)
     n = len(descs)
     if n == 0:
-        return (torch.empty((0, 3), dtype=torch.float64, device=dev),
-                torch.empty((0, 3), dtype=torch.int32, device=dev), [], [])
+        empty = (torch.empty((0, 3), dtype=torch.float64, device=dev),
+                 torch.empty((0, 3), dtype=torch.int32, device=dev), [], [])
+        return empty + (torch.empty(0, dtype=torch.int64, device=dev),) if edges else empty
     gp = _abi.aptr(descs)
     wsz = L.chr_mc_workspace_size(gp, n)
     work = ws.get("mc", wsz)
@@ -500,6 +551,11 @@ def marching(grids: torch.Tensor, descs, k: float, ws: Workspaces | None = None,
     else:
         verts = torch.empty((tv.value, 3), dtype=torch.float64, device=dev)
         tris = torch.empty((tt.value, 3), dtype=torch.int32, device=dev)
+    if edges:
+        vedge = torch.empty(tv.value, dtype=torch.int64, device=dev)
+        check(L.chr_mc_emit_edges(ptr(grids), gp, n, float(k), ptr(work), work.numel(), ptr(verts), ptr(tris),
+                                  ptr(vedge), stream_ptr()), "chr_mc_emit_edges")
+        return verts, tris, ntri.tolist(), nvert.tolist(), vedge
     if masks is None:
         check(L.chr_mc_emit(ptr(grids), gp, n, float(k), ptr(work), work.numel(), ptr(verts), ptr(tris),
                             stream_ptr()), "chr_mc_emit")

@@ -31,7 +31,7 @@ def _dims3(dims):
 class Volume:
     """Immutable 3D scalar field (dims, spacing, values, value_range, source_dtype)."""
 
-    __slots__ = ("dims", "spacing", "source_dtype", "_host", "_dev", "_range")
+    __slots__ = ("dims", "spacing", "source_dtype", "_host", "_dev", "_range", "_host32")
 
     def __init__(self, dims, spacing=(1.0, 1.0, 1.0), values=None, source_dtype: str = "f64"):
         dims = _dims3(dims)
@@ -46,7 +46,26 @@ class Volume:
         object.__setattr__(self, "source_dtype", source_dtype)
         object.__setattr__(self, "_dev", None)
         object.__setattr__(self, "_range", None)
-        if isinstance(values, torch.Tensor):
+        object.__setattr__(self, "_host32", None)
+        if (isinstance(values, np.ndarray) and values.dtype == np.float32 and source_dtype == "f32"
+                and torch.cuda.is_available()):
+            # f32 samples (what load_raw reads): uploaded as they are, finite
+            # check + value_range by one device reduction (chr_value_range);
+            # the f64 `values` view is only built if someone reads it
+            from . import device
+
+            a32 = values.reshape(-1)
+            if a32.size != n:
+                raise ParameterError(f"values has {a32.size} samples, dims {dims} require {n}")
+            a32 = np.require(a32, requirements=["C", "W"])
+            t = torch.from_numpy(a32).cuda()
+            lo, hi, bad = device.value_range(t)
+            if bad >= 0:
+                raise NonFiniteSampleError(bad, float(a32[bad]))
+            object.__setattr__(self, "_host", None)  # `values` comes from the device copy (no aliasing)
+            object.__setattr__(self, "_dev", t)
+            object.__setattr__(self, "_range", (lo, hi))
+        elif isinstance(values, torch.Tensor):
             t = values.reshape(-1)
             if t.numel() != n:
                 raise ParameterError(f"values has {t.numel()} samples, dims {dims} require {n}")
@@ -76,7 +95,7 @@ class Volume:
     @property
     def values(self) -> np.ndarray:
         if self._host is None:
-            a = self._dev.to(torch.float64).cpu().numpy()
+            a = self._dev.cpu().numpy().astype(np.float64)
             a.setflags(write=False)
             object.__setattr__(self, "_host", a)
         return self._host

@@ -61,7 +61,12 @@ def _grid(samples) -> tuple[torch.Tensor, tuple[int, int, int]]:
     g = np.asarray(samples, dtype=np.float64)
     if g.ndim != 3 or any(n < 2 for n in g.shape):
         raise ParameterError(f"need a 3D grid with >= 2 samples per axis, got {g.shape}")
-    flat = np.require(g.ravel(order="F"), requirements=["C", "W"])
+    dev = device.host_window(g)  # a request() window: its device copy, no upload
+    if dev is not None:
+        return dev, tuple(g.shape)
+    flat = g.ravel(order="F")  # free for Fortran-order arrays
+    if not flat.flags.writeable:
+        flat = flat.copy()
     return torch.from_numpy(flat).to(_abi.device()), tuple(g.shape)
 
 
