@@ -277,6 +277,14 @@ int chr_portion_finish(double *d_windows, const uint64_t *h_out_offset, const in
                        const int64_t *h_nplanes, const int64_t *h_carry_offset, const double *h_error_bound,
                        int64_t n, const int64_t *d_carry, void *d_workspace, size_t workspace_bytes, void *stream);
 
+/*     n segments (h_table: 4 u64 each = dst offset, src offset, length,
+ *     source 0 / 1) from d_src0 / d_src1 into d_dst in one launch (the
+ *     z-slab request's re-framed token streams and packed planes); elem = 1:
+ *     byte copies; elem = 8: int64 elements ADDED into d_dst (segments may
+ *     share a destination; z-carry sums).  Workspace: 32 * n bytes. */
+int chr_copy_segments(void *d_dst, const void *d_src0, const void *d_src1, const uint64_t *h_table, int64_t n,
+                      int elem, void *d_workspace, size_t workspace_bytes, void *stream);
+
 /* 13. SURVEY 8(f2): accuracy < 1 and paper_edges bounds.  For every pair
  *     (window [ox,oy,oz,ex,ey,ez], candidate k) the n-th smallest of the
  *     pair's distances (mode 0 strict_vertices: |s-k| over the window;

@@ -966,12 +966,12 @@ __global__ void __launch_bounds__(256) k_esc_seg(const DecReg *__restrict__ regs
 // taking tiles in diagonal order from a ticket cannot deadlock; a tile
 // publishes its own faces right after the wait (a few adds per column)
 // and only then writes its samples, so a chain hop costs one face update.
-// The tile holds q and its tile-local prefixes T as int32: every T is a sum
-// of the tile's q, so int32 is exact when the tile's sum |q| < 2^31 (k_band
-// checks it right after tokenising; a tile at or above it -- rare, and only
-// from extreme quanta -- sends its region to the generic int64 path via
-// k_asum_check).  Faces (u at tile boundaries) and u = T + faces are int64,
-// exact like the reference's int64 cumsum.
+// The tile holds q and its x / y prefixes as int32: those sums stay inside
+// one plane segment of the tile, so int32 is exact when the segment's sum |q|
+// < 2^31 (k_band checks it right after tokenising; a segment at or above it
+// -- rare, only from extreme quanta -- sends its region to the int64 pass via
+// k_asum_check).  The z prefix, the faces (u at tile boundaries) and u =
+// prefix + faces are int64, exact like the reference's int64 cumsum.
 using BV = int32_t;
 constexpr int BCAP = 10240;  // samples per tile (40 KB of int32 + 12 KB dF: 4 CTAs per SM)
 constexpr int BDF = 1536;    // dF entries (btz * ex) when a tile has a band above
@@ -1159,12 +1159,11 @@ __global__ void __launch_bounds__(256) k_band(const DecReg *__restrict__ regs, c
     __shared__ int64_t s_lo[BSEGM], s_hi[BSEGM], s_ub[BSEGM], s_off[BSEGM];
     __shared__ int32_t s_base[BSEGM + 1];
     __shared__ int64_t s_tile, s_zero;
-    __shared__ unsigned long long s_asum;
+    __shared__ unsigned long long s_asum[BSEGM];  // sum |q| per plane segment
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid == 0) {
         s_tile = order[atomicAdd(ticket, 1ull)];
         s_zero = 0;
-        s_asum = 0;
     }
     __syncthreads();
     const int64_t tile = s_tile;
@@ -1182,6 +1181,7 @@ __global__ void __launch_bounds__(256) k_band(const DecReg *__restrict__ regs, c
     const int64_t sp_end = R.sp_base + (int64_t)R.ez * nb;
 
     for (int i = tid; i < nzv * PL; i += 256) Q[i] = 0;
+    if (tid < BSEGM) s_asum[tid] = 0;
     // ---- segments (one per plane) and the 64-byte token groups they cover.
     //      Group g (bytes [G, G+64) from the chunk origin) has its first sample
     //      in pos64 (k_seg_locate), so a thread walks one group without a count
@@ -1225,8 +1225,8 @@ __global__ void __launch_bounds__(256) k_band(const DecReg *__restrict__ regs, c
     const int U = s_base[nzv];
     const uint64_t M = ((1ull << 32) + (uint64_t)ex - 1) / (uint64_t)ex;  // row = (at * M) >> 32
     const int64_t gbase = R.chunk_base * DTHREADS;  // pos64 index of the region's first group
-    uint64_t asum = 0;  // sum |q| of the literals this thread stored
     for (int g0 = warp * 32; g0 < U; g0 += 256) {  // warp-uniform bounds (the unit walk votes)
+        uint64_t asum = 0;  // sum |q| of the literals this thread stores (segment j)
         const int gi = g0 + lane;
         const bool own = gi < U;
         int j = 0;
@@ -1249,16 +1249,20 @@ __global__ void __launch_bounds__(256) k_band(const DecReg *__restrict__ regs, c
             at = rs == ex ? band_scatter_unit<false, QV>(W, at, L, ex, M, q, act, asum)
                           : band_scatter_unit<true, QV>(W, at, L, ex, M, q, act, asum);
         }
+        if (asum) atomicAdd(&s_asum[j], (unsigned long long)asum);
     }
-#pragma unroll
-    for (int off = 16; off; off >>= 1) asum += __shfl_xor_sync(0xFFFFFFFFu, asum, off);
-    if (lane == 0 && asum) atomicAdd(&s_asum, (unsigned long long)asum);
     __syncthreads();
-    // int32 tile prefixes are exact below 2^31 of sum |q|; else the region is
-    // decoded again by the generic int64 path (this tile still publishes its
-    // faces so the rest of the region's chain completes)
-    if (sizeof(QV) == 4 && tid == 0 && s_asum >= (1ull << 31))
-        atomicMax(asum_reg + tile_reg[tile], (unsigned long long)s_asum);
+    // The x / y prefixes stay inside one plane segment, so int32 holds them
+    // exactly when the segment's sum |q| < 2^31 (the z prefix is summed in
+    // int64 below).  Otherwise the region is decoded again by the int64 pass
+    // (this tile still publishes its faces so the region's chain completes).
+    if (sizeof(QV) == 4 && warp == 0) {
+        unsigned long long mx = 0;
+        for (int j = lane; j < nzv; j += 32) mx = max(mx, s_asum[j]);
+#pragma unroll
+        for (int off = 16; off; off >>= 1) mx = max(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, off));
+        if (lane == 0 && mx >= (1ull << 31)) atomicMax(asum_reg + tile_reg[tile], mx);
+    }
     // ---- x-prefix (rows are whole)
     const int rows = nzv * nyv;
     if (rows >= 64) {
@@ -1304,19 +1308,8 @@ __global__ void __launch_bounds__(256) k_band(const DecReg *__restrict__ regs, c
             p[yy * rs] = acc;
         }
     }
-    __syncthreads();
-    // ---- z-prefix (columns (y, x); with rs == ex the plane index is t itself)
+    // ---- the z prefix runs in int64 inside the face / reconstruction loops
     const bool pad = rs != ex;
-    for (int t = tid; t < L; t += 256) {
-        int yy = 0, xx = t;
-        if (pad) split(t, yy, xx);
-        QV *p = Q + (pad ? yy * rs + xx : t);
-        QV acc = 0;
-        for (int j = 0; j < nzv; ++j) {
-            acc += p[j * PL];
-            p[j * PL] = acc;
-        }
-    }
     // ---- band above (same chunk): its inclusive faces give dF(z, x) = Fy(z) - Fy(z0 - 1)
     // Face record of a tile: [Fy' (btz+1) x ex | I (bty x ex)] with
     // Fy' = u(row y1-1, planes z0-1..z1-1) and I = u(plane z1-1); flag 2 =
@@ -1335,7 +1328,6 @@ __global__ void __launch_bounds__(256) k_band(const DecReg *__restrict__ regs, c
         for (int t = tid; t < ex * nzv; t += 256) dF[t] = __ldcg(Fy + ex + t) - __ldcg(Fy + (t - (t / ex) * ex));
     }
     __syncthreads();
-    const int lastp = (nzv - 1) * PL;
     auto qidx = [&](int t, int &xx) {
         int yy = 0;
         xx = t;
@@ -1345,12 +1337,18 @@ __global__ void __launch_bounds__(256) k_band(const DecReg *__restrict__ regs, c
     auto publish_col = [&](int t, int64_t fz) {
         int xx;
         const int qi = qidx(t, xx);
-        myF[io + t] = Q[lastp + qi] + (b > 0 ? dF[(nzv - 1) * ex + xx] : 0) + fz;
+        int64_t acc = 0;  // z prefix of the column
         if (t >= L - ex) {  // last row (xx is the column only when split ran)
             const int xl = t - (L - ex);
             myF[xl] = fz;
-            for (int j = 0; j < nzv; ++j) myF[(j + 1) * ex + xl] = Q[j * PL + qi] + (b > 0 ? dF[j * ex + xl] : 0) + fz;
+            for (int j = 0; j < nzv; ++j) {
+                acc += Q[j * PL + qi];
+                myF[(j + 1) * ex + xl] = acc + (b > 0 ? dF[j * ex + xl] : 0) + fz;
+            }
+        } else {
+            for (int j = 0; j < nzv; ++j) acc += Q[j * PL + qi];
         }
+        myF[io + t] = acc + (b > 0 ? dF[(nzv - 1) * ex + xx] : 0) + fz;
     };
     const double twoe = 2.0 * R.e;
     const int64_t zstride = (int64_t)ex * ey;
@@ -1359,11 +1357,18 @@ __global__ void __launch_bounds__(256) k_band(const DecReg *__restrict__ regs, c
         int xx;
         const QV *p = Q + qidx(t, xx);
         double *o = obase + t;
+        int64_t acc = fz;
         if (b > 0) {
             const int64_t *d = dF + xx;
-            for (int j = 0; j < nzv; ++j) __stcs(o + j * zstride, (double)(p[j * PL] + d[j * ex] + fz) * twoe);
+            for (int j = 0; j < nzv; ++j) {
+                acc += p[j * PL];
+                __stcs(o + j * zstride, (double)(acc + d[j * ex]) * twoe);
+            }
         } else {
-            for (int j = 0; j < nzv; ++j) __stcs(o + j * zstride, (double)(p[j * PL] + fz) * twoe);
+            for (int j = 0; j < nzv; ++j) {
+                acc += p[j * PL];
+                __stcs(o + j * zstride, (double)acc * twoe);
+            }
         }
     };
     auto release = [&](int f) {  // the barrier orders all face stores before thread 0's fence + flag
@@ -1422,8 +1427,10 @@ __global__ void __launch_bounds__(256) k_band(const DecReg *__restrict__ regs, c
             double *op = obase + t;
             const int dstep = b > 0 ? ex : 0;
             if (b == 0) dp = &s_zero;
+            int64_t acc = fz;  // z prefix
             for (int j = 0; j < nzv; ++j, w += pw, qp += PL, dp += dstep, op += zstride) {
-                const double v = (double)(*qp + *dp + fz) * twoe;
+                acc += *qp;
+                const double v = (double)(acc + *dp) * twoe;
                 if (act) __stcs(op, v);
                 const uint32_t bal = __ballot_sync(0xFFFFFFFFu, act && v >= iso);
                 if (lane == 0) {

@@ -478,6 +478,11 @@ __global__ void __launch_bounds__(256) k_mc_count3(const McGrid *__restrict__ G,
                 row(1, m10, h10);
                 row(2, m01, h01);
                 row(3, m11, h11);
+                // the row's ncx + 1 <= 33 corner bits of all four rows equal (warp-uniform):
+                // every cell is case 0 or 255 -- no triangles, nothing owned
+                const uint64_t live = (1ull << (g.ncx + 1)) - 1;
+                const uint64_t a4 = m00 & m10 & m01 & m11 & live, o4 = (m00 | m10 | m01 | m11) & live;
+                if (o4 == 0 || a4 == live) continue;
                 if (lane_ok) {
                     const int code = code_fast(m00, h00, m10, h10, m01, h01, m11, h11, lane);
                     (q ? t2 : t) = s_ntri[code];

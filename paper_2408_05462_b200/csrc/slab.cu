@@ -66,3 +66,120 @@ extern "C" int chr_portion_finish(double *d_windows, const uint64_t *h_out_offse
     }
     return cudaGetLastError() == cudaSuccess ? CHR_OK : CHR_E_CUDA;
 }
+
+namespace chr {
+
+// segment table entry: dst[dst_off, +len) <- src_k[src_off, +len) (k = src)
+struct CopySeg {
+    uint64_t dst_off, src_off, len;
+    uint64_t src;
+};
+
+// bytes; one CTA per segment (grid-stride over long ones)
+__global__ void __launch_bounds__(256) k_copy_segments(uint8_t *__restrict__ dst, const uint8_t *__restrict__ s0,
+                                                       const uint8_t *__restrict__ s1, const CopySeg *__restrict__ t,
+                                                       int64_t n) {
+    for (int64_t i = blockIdx.y; i < n; i += gridDim.y) {
+        const CopySeg S = t[i];
+        const uint8_t *src = (S.src ? s1 : s0) + S.src_off;
+        uint8_t *d = dst + S.dst_off;
+        if ((((uintptr_t)src | (uintptr_t)d | S.len) & 7) == 0) {  // f64 planes: 8-byte moves
+            const uint64_t *s8 = reinterpret_cast<const uint64_t *>(src);
+            uint64_t *d8 = reinterpret_cast<uint64_t *>(d);
+            for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < S.len / 8;
+                 j += (uint64_t)gridDim.x * blockDim.x)
+                d8[j] = __ldg(s8 + j);
+            continue;
+        }
+        for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < S.len; j += (uint64_t)gridDim.x * blockDim.x)
+            d[j] = __ldg(src + j);
+    }
+}
+
+// bytes, word-granular: thread per aligned 4-byte word of the destination
+// range covered by the (sorted, adjacent) segments; each byte is looked up
+// in its segment (binary search over the segment starts) -- one aligned store
+// per word, no two threads touch the same word
+__global__ void __launch_bounds__(256) k_gather_words(uint8_t *__restrict__ dst, const uint8_t *__restrict__ s0,
+                                                      const uint8_t *__restrict__ s1, const CopySeg *__restrict__ t,
+                                                      int64_t n, uint64_t lo, uint64_t hi) {
+    const uint64_t w0 = lo >> 2, w1 = (hi + 3) >> 2;
+    for (uint64_t w = w0 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; w < w1;
+         w += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t word = 0, keep = 0;
+        int64_t a = 0, b = n - 1;
+        const uint64_t first = w << 2;
+        while (a < b) {  // last segment starting at or before the word's first byte
+            const int64_t m = (a + b + 1) >> 1;
+            if (t[m].dst_off <= first) a = m; else b = m - 1;
+        }
+        int64_t si = a;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint64_t d = first + k;
+            while (si + 1 < n && t[si + 1].dst_off <= d) ++si;
+            const CopySeg S = t[si];
+            if (d >= S.dst_off && d < S.dst_off + S.len) {
+                const uint8_t v = __ldg((S.src ? s1 : s0) + S.src_off + (d - S.dst_off));
+                word |= (uint32_t)v << (8 * k);
+                keep |= 0xFFu << (8 * k);
+            }
+        }
+        uint32_t *p = reinterpret_cast<uint32_t *>(dst) + w;
+        if (keep == 0xFFFFFFFFu) *p = word;
+        else if (keep) *p = (*p & ~keep) | word;  // the range's edge words: bytes outside it keep their value
+    }
+}
+
+// int64 elements: dst[dst_off + j] += src[src_off + j] (segments may share a
+// destination: 64-bit atomic adds, two's complement wraps like int64 sums)
+__global__ void __launch_bounds__(256) k_add_segments(long long *__restrict__ dst, const long long *__restrict__ src,
+                                                      const CopySeg *__restrict__ t, int64_t n) {
+    for (int64_t i = blockIdx.y; i < n; i += gridDim.y) {
+        const CopySeg S = t[i];
+        for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < S.len; j += (uint64_t)gridDim.x * blockDim.x)
+            atomicAdd(reinterpret_cast<unsigned long long *>(dst + S.dst_off + j),
+                      (unsigned long long)__ldg(src + S.src_off + j));
+    }
+}
+
+}  // namespace chr
+
+// n segments (h_table: 4 u64 each = dst offset, src offset, length, source
+// 0/1) copied from d_src0 / d_src1 into d_dst, one launch (z-slab request:
+// re-framed token streams, packed planes).  elem = 1: bytes; elem = 8: the
+// offsets and lengths count int64 elements and the segments ADD into d_dst.
+extern "C" int chr_copy_segments(void *d_dst, const void *d_src0, const void *d_src1, const uint64_t *h_table,
+                                 int64_t n, int elem, void *d_ws, size_t ws_bytes, void *stream) {
+    CHR_XFER_SCOPE;
+    if (n == 0) return CHR_OK;
+    if (!d_dst || !h_table || n < 0 || (elem != 1 && elem != 8)) return CHR_E_PARAMETER;
+    if (!d_ws || ws_bytes < sizeof(CopySeg) * (size_t)n) return CHR_E_WORKSPACE;
+    cudaStream_t st = (cudaStream_t)stream;
+    CopySeg *d_t = reinterpret_cast<CopySeg *>(d_ws);
+    CHR_CUDA_TRY(h2d(d_t, h_table, sizeof(CopySeg) * (size_t)n, st));
+    const dim3 grid(16, (unsigned)std::min<int64_t>(n, 65535));
+    bool gather = elem == 1 && ((uintptr_t)d_dst & 3) == 0;
+    uint64_t lo = ~0ull, hi = 0, tot = 0;
+    for (int64_t i = 0; gather && i < n; ++i) {  // sorted, non-overlapping destinations: word gather
+        const uint64_t a = h_table[4 * i], b = a + h_table[4 * i + 2];
+        if (i && a < h_table[4 * (i - 1)] + h_table[4 * (i - 1) + 2]) gather = false;
+        lo = std::min(lo, a);
+        hi = std::max(hi, b);
+        tot += b - a;
+    }
+    if (gather && hi > lo && 2 * tot >= hi - lo) {  // dense (re-framed streams): word gather
+        CHR_PROF("k_gather_words", st);
+        const uint64_t words = ((hi + 3) >> 2) - (lo >> 2);
+        k_gather_words<<<(unsigned)std::min<uint64_t>((words + 255) / 256, 148 * 16), 256, 0, st>>>(
+            (uint8_t *)d_dst, (const uint8_t *)d_src0, (const uint8_t *)d_src1, d_t, n, lo, hi);
+    } else if (elem == 1) {
+        CHR_PROF("k_copy_segments", st);
+        k_copy_segments<<<grid, 256, 0, st>>>((uint8_t *)d_dst, (const uint8_t *)d_src0, (const uint8_t *)d_src1, d_t,
+                                              n);
+    } else {
+        CHR_PROF("k_add_segments", st);
+        k_add_segments<<<grid, 256, 0, st>>>((long long *)d_dst, (const long long *)d_src0, d_t, n);
+    }
+    return cudaGetLastError() == cudaSuccess ? CHR_OK : CHR_E_CUDA;
+}

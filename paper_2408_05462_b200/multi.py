@@ -411,327 +411,356 @@ def _allgather_var(t: torch.Tensor, sizes: list[int]) -> list[torch.Tensor]:
     return [o[:n].to(t.device) for o, n in zip(out, sizes)]
 
 
+def _rb_np(L):
+    """run_bytes over an int64 array."""
+    L = np.asarray(L, dtype=np.int64)
+    vl = np.ones_like(L)
+    for b in (7, 14, 21, 28, 35, 42, 49, 56):
+        vl += L >= (1 << b)
+    return np.where(L <= 0, 0, np.where(L == 1, 1, 1 + vl))
+
+
+def _combine_np(a: dict, b: dict) -> dict:
+    """TokSeg monoid over arrays (tokseg_combine, elementwise)."""
+    both = (a["nz"] != 0) & (b["nz"] != 0)
+    r = {"len": a["len"] + b["len"], "nesc": a["nesc"] + b["nesc"], "nz": ((a["nz"] != 0) | (b["nz"] != 0)).astype(np.int64)}
+    r["lead"] = np.where(a["nz"] != 0, a["lead"], a["len"] + b["lead"])
+    r["trail"] = np.where(b["nz"] != 0, b["trail"], np.where(a["nz"] != 0, a["trail"] + b["len"], r["len"]))
+    r["bytes"] = a["bytes"] + b["bytes"] + np.where(both, _rb_np(a["trail"] + b["lead"]), 0)
+    return r
+
+
+def _tok_off_np(s: dict):
+    return s["bytes"] + np.where(s["nz"] != 0, _rb_np(s["lead"]), 0)
+
+
+def _seg_np(p) -> dict:
+    return {f: np.asarray(p[f], dtype=np.int64) for f in ("len", "lead", "trail", "bytes", "nesc", "nz")}
+
+
+def _copy_segments(dst, src0, src1, table: np.ndarray, elem: int, ws: D.Workspaces):
+    if len(table) == 0:
+        return
+    t = np.ascontiguousarray(table, dtype=np.uint64)
+    wk = ws.get("cpseg", 32 * len(t) + 64)
+    D.check(_abi.lib().chr_copy_segments(D.ptr(dst), D.ptr(src0), D.ptr(src1) if src1 is not None else None,
+                                         _abi.aptr(t), len(t), elem, D.ptr(wk), wk.numel(), D.stream_ptr()),
+            "chr_copy_segments")
+
+
 def request_extract_portions(res: D.Compressed, k_index: int, k: float, spacing=(1.0, 1.0, 1.0),
-                             ws: D.Workspaces | None = None) -> "SlabMesh":
+                             ws: D.Workspaces | None = None) -> SlabMesh:
     """request(k) + marching cubes on a z-slab archive without moving payload
     bytes: every rank decodes ITS planes of every selected
     window from the bytes it wrote and meshes the cells between them.
 
       * its token bytes are re-framed into a stand-alone stream for its
-        planes (the zero runs crossing the slab boundaries re-split at them,
-        from the compress step's all-gathered stream summaries) and decoded
-        with e = 1/2, which yields u_local (the portion's own 3D prefix) as
-        exact integers; verbatim windows are decoded as they are;
+        planes (the zero runs crossing the slab boundaries re-split there,
+        from the compress step's all-gathered stream summaries; one
+        chr_copy_segments launch) and decoded with e = 1/2, which yields
+        u_local (the portion's own 3D prefix) as exact integers; verbatim
+        windows are decoded as they are;
       * all-gather of each portion's last-plane u_local -> the z-carry plane
-        of every later portion (u = u_local + carry), then recon = u * 2e
-        (chr_portion_finish) and the escapes of codec-2 windows;
+        of every later portion (u = u_local + carry, chr_copy_segments in
+        add mode), then recon = u * 2e (chr_portion_finish) and the escapes
+        of codec-2 windows;
       * all-gather of raw CRC shares -> every selected payload's CRC checked
         (codec.decompress's check, codec.py:220-226) without assembling it;
       * all-gather of each portion's last reconstructed plane -> the halo
         plane of the next portion, so the cells between two ranks' planes are
-        meshed by the later rank (lattice z offset per grid keeps vertices
+        meshed by the later rank (a lattice z offset per grid keeps vertices
         bit-identical to the whole-window mesh);
-      * all-gather of per-portion (triangles, new vertices) -> the rows of the
-        merged mesh, and of each portion's top-plane vertex ids -> the next
-        rank's triangles refer to them (first-touch numbering of merge_meshes,
-        isosurf.py:207-225, identical to one GPU).
+      * all-gather of per-portion (triangles, new vertices, exported ids) ->
+        the rows of the merged mesh, and of each portion's top-plane vertex
+        ids -> the next rank's triangles refer to them (first-touch numbering
+        of merge_meshes, isosurf.py:207-225, identical to one GPU).
     Every collective carries sizes, counts or one plane per window boundary;
-    no rank ever holds another rank's payload bytes."""
+    no rank ever holds another rank's payload bytes.  Host bookkeeping is
+    vectorised over the portions (numpy), device work is a fixed number of
+    launches independent of the region count."""
     ws = ws or D.Workspaces()
     rank, world = dist.get_rank(), dist.get_world_size()
     L = _abi.lib()
     regions = res.regions
     dims, bs, all_por = res.extra["dims"], res.extra["bs"], res.extra["portions"]
-    nx, ny, _ = dims
+    nz = dims[2]
     sel_idx = np.nonzero((regions["mask"] >> np.uint64(k_index)) & np.uint64(1))[0]
     nsel = len(sel_idx)
     blob = res.blob
     dev = blob.device
-    ports_all = [_portions_of(regions, sel_idx, all_por, dims, bs, world, r) for r in range(world)]
-    mine = ports_all[rank]
-    poff = regions["block_offset"].astype(np.int64) + D.BLOCK_HEADER
-    plen = regions["block_nbytes"].astype(np.int64) - D.BLOCK_HEADER
+    R = regions[sel_idx]
+    ex = R["extent"][:, 0].astype(np.int64)
+    ey = R["extent"][:, 1].astype(np.int64)
+    ez = R["extent"][:, 2].astype(np.int64)
+    oz = R["origin"][:, 2].astype(np.int64)
+    plane = ex * ey
+    codec = R["codec_id"].astype(np.int64)
+    lor = (codec == 1) | (codec == 2)
+    poff = R["block_offset"].astype(np.int64) + D.BLOCK_HEADER
+    plen = R["block_nbytes"].astype(np.int64) - D.BLOCK_HEADER
+    ebound = R["error_bound"].astype(np.float64)
+    # portions of every rank (vectorised over the selection)
+    pa_r, pb_r, has_r, pre_r = [], [], [], []
+    pre = {f: np.zeros(nsel, np.int64) for f in ("len", "lead", "trail", "bytes", "nesc", "nz")}
+    for r in range(world):
+        sl = slab_of(nz, bs, world, r)
+        pa, pb = np.maximum(oz, sl.zs), np.minimum(oz + ez, sl.ze)
+        pa_r.append(pa)
+        pb_r.append(pb)
+        has_r.append(pb > pa)
+        pre_r.append(pre)
+        pre = _combine_np(pre, _seg_np(all_por[r][sel_idx]))
+    has = np.stack(has_r)                      # [world, nsel]
+    gz_r = np.stack([np.where(has[r], pb_r[r] - pa_r[r] + (pa_r[r] > oz), 0) for r in range(world)])
+    J = np.nonzero(has[rank])[0]               # my portions, in selection order
+    pa, pb = pa_r[rank][J], pb_r[rank][J]
+    nzp = pb - pa
+    first = pa == oz[J]
+    last = pb == oz[J] + ez[J]
+    halo = (~first).astype(np.int64)
+    pl = plane[J]
+    mine = _seg_np(all_por[rank][sel_idx[J]])
+    prem = {f: v[J] for f, v in pre_r[rank].items()}
+    np_ = len(J)
+    # window buffer: [halo plane][own planes] per portion
+    wsz = pl * (nzp + halo)
+    woff = np.concatenate([[0], np.cumsum(wsz)[:-1]]).astype(np.int64) if np_ else np.zeros(0, np.int64)
+    own_off = woff + halo * pl
 
-    # ---- CRC shares of the byte ranges this rank wrote, and the re-framed payloads
-    ranges, range_reg = [], []
-    pieces, dec_rows = [], []
-    synth_off = 0
-    w_off = 0
-    win_off = []  # sample offset of each portion's buffer (halo plane first when not `first`)
-    esc_fix = []  # codec-2 portions: (portion index, bitmap range, values range)
-    for pi, P in enumerate(mine):
-        i = P.reg
-        cid = int(regions["codec_id"][i])
-        ex, ey, ez = (int(v) for v in regions["extent"][i])
-        plane = ex * ey
-        nzp = P.pb - P.pa
-        n_win = plane * ez
-        s0 = P.pre["len"]  # stream index of the portion's first sample
-        base = int(poff[i])
-        win_off.append(w_off)
-        halo = 0 if P.first else 1
-        if cid in (0, 3):
-            wdt = 4 if cid == 3 else 8
-            a, b = wdt * s0, wdt * (s0 + P.mine["len"])
-            ranges += [base + a, base + b]
-            range_reg.append((i, b))
-            pieces.append(blob[base + a: base + b])
-            dec_rows.append((synth_off, b - a, cid, (ex, ey, nzp), float(regions["error_bound"][i]), w_off + halo * plane))
-            synth_off += b - a
-        else:
-            tok0 = 0
-            if cid == 2:
-                bm = (n_win + 7) >> 3
-                nesc_tot = int(regions["n_escaped"][i])
-                tok0 = bm + 8 * nesc_tot
-                ba, bb = s0 >> 3, (s0 + P.mine["len"] + 7) >> 3
-                va, vb = bm + 8 * P.pre["nesc"], bm + 8 * (P.pre["nesc"] + P.mine["nesc"])
-                for a, b in ((ba, bb), (va, vb)):
-                    if b > a:
-                        ranges += [base + a, base + b]
-                        range_reg.append((i, b))
-                esc_fix.append((pi, base + ba, base + va, s0, P.mine["len"], P.mine["nesc"]))
-            t0 = _tok_off(P.pre)
-            t1 = int(plen[i]) - tok0 if P.last else _tok_off(_seg_combine(P.pre, P.mine))
-            if t1 > t0:
-                ranges += [base + tok0 + t0, base + tok0 + t1]
-                range_reg.append((i, tok0 + t1))
-            carry_in = P.pre["trail"] if P.pre["nz"] else P.pre["len"]
-            if P.mine["nz"]:
-                skip = _run_bytes(carry_in + P.mine["lead"])
-                head = _run_token(P.mine["lead"])
-                body = blob[base + tok0 + t0 + skip: base + tok0 + t1]
-                tail = b"" if P.last else _run_token(P.mine["trail"])
-            else:
-                head, body, tail = _run_token(P.mine["len"]), blob[0:0], b""
-            parts = [torch.tensor(list(head), dtype=torch.uint8, device=dev), body,
-                     torch.tensor(list(tail), dtype=torch.uint8, device=dev)]
-            nbytes = sum(int(p.numel()) for p in parts)
-            pieces.extend(parts)
-            dec_rows.append((synth_off, nbytes, 1, (ex, ey, nzp), 0.5, w_off + halo * plane))
-            synth_off += nbytes
-        w_off += plane * (nzp + halo)
-    # raw CRC shares -> all-gather -> every selected payload checked
+    # ---- byte ranges this rank wrote (CRC shares) and the re-framed streams
+    s0 = prem["len"]
+    n_win = plane[J] * ez[J]
+    cj = codec[J]
+    bm = (n_win + 7) >> 3
+    tok0 = np.where(cj == 2, bm + 8 * R["n_escaped"][J].astype(np.int64), 0)
+    t0 = _tok_off_np(prem)
+    t1 = np.where(last, plen[J] - tok0, _tok_off_np(_combine_np(prem, mine)))
+    carry_in = np.where(prem["nz"] != 0, prem["trail"], prem["len"])
+    skip = np.where(mine["nz"] != 0, _rb_np(carry_in + mine["lead"]), 0)
+    wdt = np.where(cj == 3, 4, 8)
+    base = poff[J]
+    rng = []  # (abs begin, abs end, selection index, payload-relative end)
+    for q in range(np_):
+        b0 = int(base[q])
+        if cj[q] in (0, 3):
+            a_, b_ = int(wdt[q] * s0[q]), int(wdt[q] * (s0[q] + mine["len"][q]))
+            if b_ > a_:
+                rng.append((b0 + a_, b0 + b_, J[q], b_))
+            continue
+        if cj[q] == 2:
+            ba, bb = int(s0[q]) >> 3, (int(s0[q] + mine["len"][q]) + 7) >> 3
+            va, vb = int(bm[q] + 8 * prem["nesc"][q]), int(bm[q] + 8 * (prem["nesc"][q] + mine["nesc"][q]))
+            for a_, b_ in ((ba, bb), (va, vb)):
+                if b_ > a_:
+                    rng.append((b0 + a_, b0 + b_, J[q], b_))
+        if t1[q] > t0[q]:
+            rng.append((b0 + int(tok0[q] + t0[q]), b0 + int(tok0[q] + t1[q]), J[q], int(tok0[q] + t1[q])))
     share = np.zeros(nsel, dtype=np.uint32)
-    if ranges:
-        rr = np.asarray(ranges, dtype=np.uint64)
-        raw = np.zeros(len(range_reg), dtype=np.uint32)
-        wk = ws.get("crcseg", L.chr_crc32_segments_workspace_size(len(range_reg)))
-        D.check(L.chr_crc32_segments(D.ptr(blob), _abi.aptr(rr), len(range_reg), D.ptr(wk), wk.numel(), _abi.aptr(raw),
-                                     None, D.stream_ptr()), "chr_crc32_segments")
-        where = {int(i): j for j, i in enumerate(sel_idx)}
-        for (i, end), rv in zip(range_reg, raw):
-            share[where[i]] ^= L.chr_crc32_shift(int(rv), int(plen[i]) - int(end))
+    if rng:
+        rr = np.asarray([(a_, b_) for a_, b_, _, _ in rng], dtype=np.uint64).reshape(-1)
+        raw = np.zeros(len(rng), dtype=np.uint32)
+        wk = ws.get("crcseg", L.chr_crc32_segments_workspace_size(len(rng)))
+        D.check(L.chr_crc32_segments(D.ptr(blob), _abi.aptr(rr), len(rng), D.ptr(wk), wk.numel(), _abi.aptr(raw), None,
+                                     D.stream_ptr()), "chr_crc32_segments")
+        for (_, _, j, end), rv in zip(rng, raw):
+            share[j] ^= L.chr_crc32_shift(int(rv), int(plen[j]) - int(end))
     tot = np.zeros(nsel, dtype=np.uint32)
     for sh in _allgather(torch.from_numpy(share.view(np.int32).copy())):
         tot ^= sh.numpy().view(np.uint32)
-    for j, i in enumerate(sel_idx):
-        crc = L.chr_crc32_combine(0xFFFFFFFF, int(tot[j]), int(plen[i])) ^ 0xFFFFFFFF
-        if crc != int(regions["payload_crc"][i]):
+    for j in range(nsel):
+        if (L.chr_crc32_combine(0xFFFFFFFF, int(tot[j]), int(plen[j])) ^ 0xFFFFFFFF) != int(R["payload_crc"][j]):
             from .exceptions import CorruptPayloadError
 
             raise CorruptPayloadError("payload checksum mismatch")
+    # re-framed payloads: [run(lead)] + tokens after the boundary run + [run(trail)]
+    extra = bytearray()
+    segs, dec_off, dec_len = [], [], []
+    at = 0
+    for q in range(np_):
+        start = at
+        b0 = int(base[q])
+        if cj[q] in (0, 3):
+            a_, b_ = int(wdt[q] * s0[q]), int(wdt[q] * (s0[q] + mine["len"][q]))
+            segs.append((at, b0 + a_, b_ - a_, 0))
+            at += b_ - a_
+        else:
+            if mine["nz"][q]:
+                head = _run_token(int(mine["lead"][q]))
+                body = (b0 + int(tok0[q] + t0[q] + skip[q]), int(t1[q] - t0[q] - skip[q]))
+                tail = b"" if last[q] else _run_token(int(mine["trail"][q]))
+            else:
+                head, body, tail = _run_token(int(mine["len"][q])), (0, 0), b""
+            for piece in (head, body, tail):
+                if isinstance(piece, bytes):
+                    if piece:
+                        segs.append((at, len(extra), len(piece), 1))
+                        extra += piece
+                        at += len(piece)
+                elif piece[1] > 0:
+                    segs.append((at, piece[0], piece[1], 0))
+                    at += piece[1]
+        dec_off.append(start)
+        dec_len.append(at - start)
+    sblob = torch.zeros(at + 16, dtype=torch.uint8, device=dev)
+    xb = torch.tensor(list(extra) or [0], dtype=torch.uint8).to(dev)
+    _copy_segments(sblob, blob, xb, np.asarray(segs, dtype=np.uint64).reshape(-1, 4), 1, ws)
 
-    # ---- decode the re-framed portions (e = 1/2 -> u_local exact)
-    windows = torch.zeros(max(w_off, 1), dtype=torch.float64, device=dev)
-    if mine:
-        sblob = torch.cat([p.reshape(-1) for p in pieces] + [torch.zeros(16, dtype=torch.uint8, device=dev)])
-        offs = np.asarray([r[0] for r in dec_rows], dtype=np.uint64)
-        lens = np.asarray([r[1] for r in dec_rows], dtype=np.uint64)
+    # ---- decode (e = 1/2 for Lorenzo portions: u_local exact)
+    windows = torch.zeros(max(int(wsz.sum()) if np_ else 0, 1), dtype=torch.float64, device=dev)
+    if np_:
+        offs = np.asarray(dec_off, dtype=np.uint64)
+        lens = np.asarray(dec_len, dtype=np.uint64)
         rr = np.stack([offs, offs + lens], axis=1).reshape(-1)
-        crcs = np.zeros(len(dec_rows), dtype=np.uint32)
-        wk = ws.get("crcseg", L.chr_crc32_segments_workspace_size(len(dec_rows)))
-        D.check(L.chr_crc32_segments(D.ptr(sblob), _abi.aptr(rr), len(dec_rows), D.ptr(wk), wk.numel(), None,
-                                     _abi.aptr(crcs), D.stream_ptr()), "chr_crc32_segments")
-        tab = D.dec_table(offs, lens, [r[2] for r in dec_rows], [r[3] for r in dec_rows], [r[4] for r in dec_rows],
-                          crcs)
-        tab["out_offset"] = [r[5] for r in dec_rows]
+        crcs = np.zeros(np_, dtype=np.uint32)
+        wk = ws.get("crcseg", L.chr_crc32_segments_workspace_size(np_))
+        D.check(L.chr_crc32_segments(D.ptr(sblob), _abi.aptr(rr), np_, D.ptr(wk), wk.numel(), None, _abi.aptr(crcs),
+                                     D.stream_ptr()), "chr_crc32_segments")
+        dcodec = np.where(lor[J], 1, cj)
+        tab = D.dec_table(offs, lens, dcodec, np.stack([ex[J], ey[J], nzp], 1), np.where(lor[J], 0.5, ebound[J]), crcs)
+        tab["out_offset"] = own_off
         _, _, status = D.decode(sblob, tab, ws=ws, out=windows)
         if any(status):
             raise ParameterError(f"portion decode failed: {list(status)}")
 
-    # ---- z-carries: all-gather every portion's last-plane u_local
-    def plane_of(P):
-        e = regions["extent"][P.reg]
-        return int(e[0]) * int(e[1])
+    # ---- z-carries: all-gather of every Lorenzo portion's last-plane u_local
+    def last_planes(r):  # (selection indices, plane sizes) in pack order
+        jj = np.nonzero(has[r] & lor)[0]
+        return jj, plane[jj]
 
-    def lorenzo(P):
-        return int(regions["codec_id"][P.reg]) in (1, 2)
-
-    sizes = [sum(plane_of(P) for P in ports_all[r] if lorenzo(P)) for r in range(world)]
-    mine_last = [windows[win_off[pi] + (0 if P.first else plane_of(P)) + (P.pb - P.pa - 1) * plane_of(P):][: plane_of(P)]
-                 for pi, P in enumerate(mine) if lorenzo(P)]
-    packed = torch.cat(mine_last).to(torch.int64) if mine_last else torch.zeros(0, dtype=torch.int64, device=dev)
-    lasts = _allgather_var(packed, sizes)
-    last_of = {}  # (rank, region) -> int64 plane
+    sizes = [int(last_planes(r)[1].sum()) for r in range(world)]
+    lj = np.nonzero(lor[J])[0]  # my Lorenzo portions (positions in J)
+    pk_off = np.concatenate([[0], np.cumsum(pl[lj])[:-1]]).astype(np.int64) if len(lj) else np.zeros(0, np.int64)
+    pack = torch.zeros(max(int(pl[lj].sum()) if len(lj) else 0, 1), dtype=torch.float64, device=dev)
+    tb = np.stack([pk_off * 8, (own_off[lj] + (nzp[lj] - 1) * pl[lj]) * 8, pl[lj] * 8, np.zeros(len(lj), np.int64)],
+                  1) if len(lj) else np.zeros((0, 4))
+    _copy_segments(pack, windows, None, tb, 1, ws)
+    lasts = _allgather_var(pack[: sizes[rank]].to(torch.int64), sizes)
+    gath = torch.cat(lasts) if sum(sizes) else torch.zeros(1, dtype=torch.int64, device=dev)
+    gbase = np.concatenate([[0], np.cumsum(sizes)[:-1]]).astype(np.int64)
+    loc_in = {}  # (rank, selection) -> element offset in gath
     for r in range(world):
-        o = 0
-        for P in ports_all[r]:
-            if lorenzo(P):
-                last_of[(r, P.reg)] = lasts[r][o: o + plane_of(P)]
-                o += plane_of(P)
-    carries, c_off = [], []
+        jj, pp = last_planes(r)
+        o = gbase[r] + np.concatenate([[0], np.cumsum(pp)[:-1]]) if len(jj) else []
+        loc_in.update({(r, int(j)): int(x) for j, x in zip(jj, o)})
+    cq = [q for q in lj if not first[q]]  # portions needing a carry
+    c_off = np.full(np_, -1, np.int64)
     c_at = 0
-    fin = []
-    for pi, P in enumerate(mine):
-        if not lorenzo(P):
-            continue
-        co = -1
-        if not P.first:
-            c = sum(last_of[(r, P.reg)] for r in range(rank) if (r, P.reg) in last_of)
-            carries.append(c)
-            co = c_at
-            c_at += plane_of(P)
-        e = regions["extent"][P.reg]
-        fin.append((win_off[pi] + (0 if P.first else plane_of(P)), plane_of(P), P.pb - P.pa, co,
-                    float(regions["error_bound"][P.reg])))
-    if fin:
-        cbuf = torch.cat(carries) if carries else torch.zeros(1, dtype=torch.int64, device=dev)
-        cols = (np.asarray([x[0] for x in fin], dtype=np.uint64), np.asarray([x[1] for x in fin], dtype=np.int64),
-                np.asarray([x[2] for x in fin], dtype=np.int64), np.asarray([x[3] for x in fin], dtype=np.int64),
-                np.asarray([x[4] for x in fin], dtype=np.float64))  # kept alive across the call
-        wk = ws.get("pfin", 64 * len(fin))
-        D.check(L.chr_portion_finish(D.ptr(windows), *[_abi.aptr(c) for c in cols], len(fin), D.ptr(cbuf),
-                                     D.ptr(wk), wk.numel(), D.stream_ptr()), "chr_portion_finish")
-    for pi, bmo, vo, s0, n, ne in esc_fix:  # codec 2: escaped samples keep their f64 value
+    add = []
+    for q in cq:
+        c_off[q] = c_at
+        for r in range(rank):
+            key = (r, int(J[q]))
+            if key in loc_in:
+                add.append((c_at, loc_in[key], int(pl[q]), 0))
+        c_at += int(pl[q])
+    carry = torch.zeros(max(c_at, 1), dtype=torch.int64, device=dev)
+    _copy_segments(carry, gath, None, np.asarray(add, dtype=np.uint64).reshape(-1, 4), 8, ws)
+    if len(lj):
+        cols = (own_off[lj].astype(np.uint64), pl[lj].astype(np.int64), nzp[lj].astype(np.int64),
+                c_off[lj].astype(np.int64), ebound[J][lj].astype(np.float64))  # alive across the call
+        wk = ws.get("pfin", 64 * len(lj))
+        D.check(L.chr_portion_finish(D.ptr(windows), *[_abi.aptr(c) for c in cols], len(lj), D.ptr(carry), D.ptr(wk),
+                                     wk.numel(), D.stream_ptr()), "chr_portion_finish")
+    for q in np.nonzero(cj == 2)[0]:  # codec 2 (rare): escaped samples keep their f64 value
+        ne, n0, st0 = int(mine["nesc"][q]), int(mine["len"][q]), int(s0[q])
         if ne == 0:
             continue
-        P = mine[pi]
-        nb = ((s0 + n + 7) >> 3) - (s0 >> 3)
-        bits = torch.stack([(blob[bmo: bmo + nb] >> b) & 1 for b in range(8)], dim=1).reshape(-1)
-        bits = bits[(s0 & 7): (s0 & 7) + n].bool()
-        vals = blob[vo: vo + 8 * ne].clone().view(torch.float64)
-        dst = windows[win_off[pi] + (0 if P.first else plane_of(P)):][:n]
+        b0 = int(base[q])
+        nb = ((st0 + n0 + 7) >> 3) - (st0 >> 3)
+        bits = torch.stack([(blob[b0 + (st0 >> 3): b0 + (st0 >> 3) + nb] >> b) & 1 for b in range(8)], 1).reshape(-1)
+        bits = bits[(st0 & 7): (st0 & 7) + n0].bool()
+        va = int(b0 + bm[q] + 8 * prem["nesc"][q])
+        vals = blob[va: va + 8 * ne].clone().view(torch.float64)
+        dst = windows[int(own_off[q]): int(own_off[q]) + n0]
         dst[bits] = vals
 
     # ---- halo planes: all-gather of every non-final portion's last plane
-    hsizes = [sum(plane_of(P) for P in ports_all[r] if not P.last) for r in range(world)]
-    mine_top = [windows[win_off[pi] + (0 if P.first else plane_of(P)) + (P.pb - P.pa - 1) * plane_of(P):][: plane_of(P)]
-                for pi, P in enumerate(mine) if not P.last]
-    hp = torch.cat(mine_top) if mine_top else torch.zeros(0, dtype=torch.float64, device=dev)
-    tops = _allgather_var(hp, hsizes)
-    top_of = {}
-    for r in range(world):
-        o = 0
-        for P in ports_all[r]:
-            if not P.last:
-                top_of[(r, P.reg)] = tops[r][o: o + plane_of(P)]
-                o += plane_of(P)
-    for pi, P in enumerate(mine):
-        if not P.first:
-            windows[win_off[pi]: win_off[pi] + plane_of(P)] = top_of[(rank - 1, P.reg)]
+    def top_planes(r):
+        jj = np.nonzero(has[r] & (pb_r[r] < oz + ez))[0]
+        return jj, plane[jj]
+
+    hsz = [int(top_planes(r)[1].sum()) for r in range(world)]
+    tq = np.nonzero(~last)[0]
+    hp = torch.zeros(max(int(pl[tq].sum()) if len(tq) else 0, 1), dtype=torch.float64, device=dev)
+    hoff = np.concatenate([[0], np.cumsum(pl[tq])[:-1]]).astype(np.int64) if len(tq) else np.zeros(0, np.int64)
+    tb = np.stack([hoff * 8, (own_off[tq] + (nzp[tq] - 1) * pl[tq]) * 8, pl[tq] * 8, np.zeros(len(tq), np.int64)],
+                  1) if len(tq) else np.zeros((0, 4))
+    _copy_segments(hp, windows, None, tb, 1, ws)
+    tops = _allgather_var(hp[: hsz[rank]], hsz)
+    if rank > 0 and np.any(~first):
+        prev_j, prev_p = top_planes(rank - 1)
+        prev_o = np.concatenate([[0], np.cumsum(prev_p)[:-1]]).astype(np.int64)
+        where = {int(j): int(o) for j, o in zip(prev_j, prev_o)}
+        hq = np.nonzero(~first)[0]
+        tb = np.asarray([(woff[q] * 8, where[int(J[q])] * 8, pl[q] * 8, 0) for q in hq], dtype=np.uint64)
+        _copy_segments(windows, tops[rank - 1], None, tb, 1, ws)
 
     # ---- marching cubes of each portion's cells (halo plane first)
+    gzm = nzp + halo
+    gq = np.nonzero(gzm >= 2)[0]  # a one-plane first portion has no cells
     verts = torch.empty((0, 3), dtype=torch.float64, device=dev)
     tris = torch.empty((0, 3), dtype=torch.int32, device=dev)
     vedge = torch.empty(0, dtype=torch.int64, device=dev)
-    nt = nv = []
-    grids = []
-    for pi, P in enumerate(mine):
-        ex, ey, _ = (int(v) for v in regions["extent"][P.reg])
-        oz = int(regions["origin"][P.reg][2])
-        gz = P.pb - P.pa + (0 if P.first else 1)
-        grids.append((pi, win_off[pi], (ex, ey, gz), P.pa - oz - (0 if P.first else 1)))
-    keep = [g for g in grids if g[2][2] >= 2]  # a one-plane portion has no cells of its own
-    if keep:
-        org = np.stack([regions["origin"][mine[g[0]].reg].astype(np.float64) * np.asarray(spacing) for g in keep])
-        mct = D.mc_table([g[1] for g in keep], [g[2] for g in keep], org, spacing)
-        mct["zoff"] = [g[3] for g in keep]
-        verts, tris, nt, nv, vedge = D.marching(windows, mct, k, ws=ws, edges=True)
-    cnt_t = {g[0]: c for g, c in zip(keep, nt)}
-    cnt_v = {g[0]: c for g, c in zip(keep, nv)}
-
-    # drop halo-plane x/y vertices (first touched by the previous rank), count the rest
-    vbase = np.concatenate([[0], np.cumsum(nv)]).astype(np.int64) if keep else np.zeros(1, np.int64)
-    drop = torch.zeros(verts.shape[0], dtype=torch.bool, device=dev)
-    gi = {g[0]: j for j, g in enumerate(keep)}
-    def prev_has_cells(P):
-        for Q in ports_all[rank - 1]:
-            if Q.reg == P.reg:
-                return (Q.pb - Q.pa) + (0 if Q.first else 1) >= 2
-        return False
-
-    for pi, P in enumerate(mine):
-        if P.first or pi not in gi or not prev_has_cells(P):
-            continue
-        j = gi[pi]
-        e = vedge[vbase[j]: vbase[j + 1]]
-        ex, ey = (int(v) for v in regions["extent"][P.reg][:2])
-        drop[vbase[j]: vbase[j + 1]] = (e // 3 < ex * ey) & (e % 3 != 2)
-    kept = torch.zeros(len(mine), dtype=torch.int64)
-    for pi in range(len(mine)):
-        if pi in gi:
-            j = gi[pi]
-            kept[pi] = int(cnt_v[pi]) - int(drop[vbase[j]: vbase[j + 1]].sum())
-    # all-gather of (triangles, kept vertices) of every (selected region, rank)
-    cnt = torch.zeros((nsel, 2), dtype=torch.int64)
-    for pi, P in enumerate(mine):
-        cnt[P.sel, 0] = int(cnt_t.get(pi, 0))
-        cnt[P.sel, 1] = int(kept[pi])
-    allc = torch.stack(_allgather(cnt))  # [world, nsel, 2]
-    per_reg = allc.sum(dim=0)
-    reg_base = torch.cumsum(per_reg, 0) - per_reg  # [nsel, 2] rows of each region
-    rank_pre = torch.cumsum(allc, 0) - allc        # [world, nsel, 2] earlier ranks inside the region
-    # global ids of this rank's kept vertices; export the top-plane x/y ones
-    gid = torch.full((verts.shape[0],), -1, dtype=torch.int64, device=dev)
-    exp_keys, exp_ids = [], []
-    for pi, P in enumerate(mine):
-        if pi not in gi:
-            continue
-        j = gi[pi]
-        sl = slice(int(vbase[j]), int(vbase[j + 1]))
-        d = drop[sl]
-        b0 = int(reg_base[P.sel, 1] + rank_pre[rank, P.sel, 1])
-        ids = torch.cumsum((~d).to(torch.int64), 0) - 1 + b0
-        gid[sl] = torch.where(d, torch.full_like(ids, -1), ids)
-        if not P.last:
-            ex, ey, gz = (int(v) for v in keep[j][2])
-            e = vedge[sl]
-            top = (e // 3 >= (gz - 1) * ex * ey) & (e % 3 != 2) & ~d
-            exp_keys.append(e[top] - (gz - 1) * ex * ey * 3)
-            exp_ids.append(gid[sl][top])
-    # exchange top-plane vertex ids (sizes first)
-    my_exp = [(P, kk, ii) for P, kk, ii in zip([P for pi, P in enumerate(mine) if pi in gi and not P.last],
-                                               exp_keys, exp_ids)]
-    lens_local = torch.tensor([len(kk) for _, kk, _ in my_exp], dtype=torch.int64)
-    nexp = torch.zeros(nsel, dtype=torch.int64)
-    for (P, kk, _), n in zip(my_exp, lens_local):
-        nexp[P.sel] = int(n)
-    alln = torch.stack(_allgather(nexp))  # [world, nsel]
-    esz = [int(alln[r].sum()) * 2 for r in range(world)]
-    pack = torch.cat([torch.stack([kk, ii], 1).reshape(-1) for _, kk, ii in my_exp]) if my_exp else \
+    nt_g = np.zeros(len(gq), np.int64)
+    nv_g = np.zeros(len(gq), np.int64)
+    if len(gq):
+        org = R["origin"][J[gq]].astype(np.float64) * np.asarray(spacing)
+        mct = D.mc_table(woff[gq], np.stack([ex[J[gq]], ey[J[gq]], gzm[gq]], 1), org, spacing)
+        mct["zoff"] = (pa[gq] - oz[J[gq]] - halo[gq]).astype(np.int32)
+        verts, tris, nt_l, nv_l, vedge = D.marching(windows, mct, k, ws=ws, edges=True)
+        nt_g, nv_g = np.asarray(nt_l, np.int64), np.asarray(nv_l, np.int64)
+    ng = len(gq)
+    # renumbering, vectorised over vertices: drop the halo-plane x/y vertices
+    # (first touched by the previous rank's last cell layer), number the rest
+    prev_cells = np.zeros(np_, bool)
+    if rank > 0:
+        prev_cells = gz_r[rank - 1][J] >= 2
+    drop_grid = torch.from_numpy((halo[gq].astype(bool) & prev_cells[gq]).astype(np.int64)).to(dev)
+    gvid = torch.repeat_interleave(torch.arange(ng, device=dev), torch.from_numpy(nv_g).to(dev)) if ng else \
         torch.zeros(0, dtype=torch.int64, device=dev)
-    allexp = _allgather_var(pack, esz)
-    imp = {}
-    for r in range(world):
-        o = 0
-        for s in range(nsel):
-            n = int(alln[r, s])
-            if n:
-                kv = allexp[r][o: o + 2 * n].view(n, 2)
-                imp[(r, s)] = (kv[:, 0], kv[:, 1])
-                o += 2 * n
-    # resolve the dropped (halo-plane) vertices from the previous rank's export
-    for pi, P in enumerate(mine):
-        if P.first or pi not in gi:
-            continue
-        j = gi[pi]
-        sl = slice(int(vbase[j]), int(vbase[j + 1]))
-        d = drop[sl]
-        if not bool(d.any()):
-            continue
-        keys, ids = imp[(rank - 1, P.sel)]
-        order = torch.argsort(keys)
-        keys, ids = keys[order], ids[order]
-        want = vedge[sl][d]
-        pos = torch.searchsorted(keys, want)
-        g = gid[sl]
-        g[d] = ids[pos.clamp_max(max(len(ids) - 1, 0))]
-        gid[sl] = g
+    pl_g = torch.from_numpy(pl[gq]).to(dev)
+    gz_g = torch.from_numpy(gzm[gq]).to(dev)
+    axis = vedge % 3
+    drop = (drop_grid[gvid] != 0) & (vedge < 3 * pl_g[gvid]) & (axis != 2)
+    keepv = (~drop).to(torch.int64)
+    kept_g = torch.zeros(ng, dtype=torch.int64, device=dev).index_add_(0, gvid, keepv).cpu().numpy() if ng else nv_g
+    topm = (torch.from_numpy((~last[gq]).astype(np.int64)).to(dev)[gvid] != 0) & \
+        (vedge >= 3 * (gz_g[gvid] - 1) * pl_g[gvid]) & (axis != 2) & ~drop
+    exp_g = torch.zeros(ng, dtype=torch.int64, device=dev).index_add_(0, gvid, topm.to(torch.int64)).cpu().numpy() \
+        if ng else nv_g
+    cnt = torch.zeros((nsel, 3), dtype=torch.int64)
+    cnt[J[gq], 0] = torch.from_numpy(nt_g)
+    cnt[J[gq], 1] = torch.from_numpy(kept_g)
+    cnt[J[gq], 2] = torch.from_numpy(exp_g)
+    allc = torch.stack(_allgather(cnt)).numpy()  # [world, nsel, 3]
+    per_reg = allc[:, :, :2].sum(axis=0)
+    reg_base = np.cumsum(per_reg, axis=0) - per_reg
+    rank_pre = np.cumsum(allc[:, :, :2], axis=0) - allc[:, :, :2]
+    vb_g = reg_base[J[gq], 1] + rank_pre[rank, J[gq], 1]  # global id of each grid's first kept vertex
+    kstart = np.concatenate([[0], np.cumsum(kept_g)[:-1]]).astype(np.int64)
+    kc = torch.cumsum(keepv, 0) - 1
+    gid = torch.from_numpy(vb_g - kstart).to(dev)[gvid] + kc if ng else torch.zeros(0, dtype=torch.int64, device=dev)
+    # exports: (selection, in-plane key) -> global id of every top-plane x/y vertex
+    keymul = 3 * int(plane.max()) if nsel else 1
+    jsel = torch.from_numpy(J[gq]).to(dev)[gvid] if ng else gvid
+    kexp = jsel[topm] * keymul + (vedge[topm] - 3 * (gz_g[gvid][topm] - 1) * pl_g[gvid][topm])
+    epack = torch.stack([kexp, gid[topm]], 1).reshape(-1) if ng else torch.zeros(0, dtype=torch.int64, device=dev)
+    esz = [int(allc[r, :, 2].sum()) * 2 for r in range(world)]
+    allexp = _allgather_var(epack, esz)
+    if rank > 0 and bool(drop.any()):
+        kv = allexp[rank - 1].view(-1, 2)
+        order = torch.argsort(kv[:, 0])
+        keys, ids = kv[order, 0], kv[order, 1]
+        want = jsel[drop] * keymul + vedge[drop]
+        pos = torch.searchsorted(keys, want).clamp_max(max(len(keys) - 1, 0))
+        gid[drop] = ids[pos]
     tris_g = gid[tris.reshape(-1).to(torch.int64)].reshape(-1, 3).to(torch.int32) if tris.numel() else tris
     verts_k = verts[~drop] if verts.numel() else verts
-    tri_base = [int(reg_base[P.sel, 0] + rank_pre[rank, P.sel, 0]) for P in mine]
-    vert_base = [int(reg_base[P.sel, 1] + rank_pre[rank, P.sel, 1]) for P in mine]
-    return SlabMesh(verts_k, tris_g, [P.sel for P in mine], tri_base, vert_base, int(per_reg[:, 0].sum()),
-                    int(per_reg[:, 1].sum()), [int(cnt_t.get(pi, 0)) for pi in range(len(mine))],
-                    [int(kept[pi]) for pi in range(len(mine))])
+    nt_p = np.zeros(np_, np.int64)
+    nv_p = np.zeros(np_, np.int64)
+    nt_p[gq] = nt_g
+    nv_p[gq] = kept_g
+    tri_base = (reg_base[J, 0] + rank_pre[rank, J, 0]).tolist()
+    vert_base = (reg_base[J, 1] + rank_pre[rank, J, 1]).tolist()
+    return SlabMesh(verts_k, tris_g, J.tolist(), [int(x) for x in tri_base], [int(x) for x in vert_base],
+                    int(per_reg[:, 0].sum()), int(per_reg[:, 1].sum()), nt_p.tolist(), nv_p.tolist())
