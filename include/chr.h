@@ -218,6 +218,7 @@ size_t chr_crc32_segments_workspace_size(int64_t n);
 int chr_crc32_segments(const uint8_t *d_buf, const uint64_t *h_ranges, int64_t n, void *d_workspace,
                        size_t workspace_bytes, uint32_t *h_raw, uint32_t *h_crc, void *stream);
 uint32_t chr_crc32_shift(uint32_t raw, uint64_t len);
+void chr_crc32_shift_many(const uint32_t *h_raw, const uint64_t *h_len, int64_t n, uint32_t *h_out);
 
 /* 8. kernel seam (isochr/kernels.py) on single windows */
 int chr_min_abs_distance(const double *d_flat, int64_t n, double k, double *h_out,
@@ -284,6 +285,17 @@ int chr_portion_finish(double *d_windows, const uint64_t *h_out_offset, const in
  *     share a destination; z-carry sums).  Workspace: 32 * n bytes. */
 int chr_copy_segments(void *d_dst, const void *d_src0, const void *d_src1, const uint64_t *h_table, int64_t n,
                       int elem, void *d_workspace, size_t workspace_bytes, void *stream);
+
+/*     z-slab request, vertex bookkeeping: h_grids = ng x 6 int64 (vertex
+ *     base, vertex end, halo limit, top-plane edge id, key base, id base).
+ *     chr_slab_classify: per vertex flags (1 dropped halo-plane x/y vertex,
+ *     2 exported top-plane x/y vertex) + key, per-grid (dropped, exported)
+ *     counts in h_counts (2 ng u64; synchronises).  chr_slab_gid: global id
+ *     = id base + inclusive kept count - 1.  Workspace: 64 ng + 512 bytes. */
+int chr_slab_classify(const int64_t *d_vedge, int64_t nv, const int64_t *h_grids, int ng, int8_t *d_flags,
+                      int64_t *d_key, uint64_t *h_counts, void *d_workspace, size_t workspace_bytes, void *stream);
+int chr_slab_gid(const int64_t *d_kept_incl, int64_t nv, const int64_t *h_grids, int ng, int64_t *d_gid,
+                 void *d_workspace, size_t workspace_bytes, void *stream);
 
 /* 13. SURVEY 8(f2): accuracy < 1 and paper_edges bounds.  For every pair
  *     (window [ox,oy,oz,ex,ey,ez], candidate k) the n-th smallest of the

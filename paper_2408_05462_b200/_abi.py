@@ -185,12 +185,18 @@ def lib():
         L.chr_crc32_segments.restype = INT
         L.chr_crc32_shift.argtypes = [ctypes.c_uint32, U64]
         L.chr_crc32_shift.restype = ctypes.c_uint32
+        L.chr_crc32_shift_many.argtypes = [P, P, I64, P]
+        L.chr_crc32_shift_many.restype = None
         L.chr_mc_emit_edges.argtypes = [P, P, I64, D, P, SZ, P, P, P, P]
         L.chr_mc_emit_edges.restype = INT
         L.chr_portion_finish.argtypes = [P, P, P, P, P, P, I64, P, P, SZ, P]
         L.chr_portion_finish.restype = INT
         L.chr_copy_segments.argtypes = [P, P, P, P, I64, INT, P, SZ, P]
         L.chr_copy_segments.restype = INT
+        L.chr_slab_classify.argtypes = [P, I64, P, INT, P, P, P, P, SZ, P]
+        L.chr_slab_classify.restype = INT
+        L.chr_slab_gid.argtypes = [P, I64, P, INT, P, P, SZ, P]
+        L.chr_slab_gid.restype = INT
         L.chr_crc32_combine.argtypes = [ctypes.c_uint32, ctypes.c_uint32, U64]
         L.chr_crc32_combine.restype = ctypes.c_uint32
         L.chr_min_abs_distance.argtypes = [P, I64, D, P, P, SZ, P]
@@ -269,8 +275,8 @@ EXPORTS = [
     "chr_prof_mark", "chr_copy", "chr_request_tables", "chr_pipeline",
     "chr_dcompress_workspace_size", "chr_dcompress_local", "chr_dcompress_finish", "chr_dcompress_headers",
     "chr_abi_version", "chr_status_string", "chr_num_blocks", "chr_stats", "chr_plan", "chr_merge_keys",
-    "chr_value_range", "chr_crc32_segments_workspace_size", "chr_crc32_segments", "chr_crc32_shift",
-    "chr_mc_emit_edges", "chr_portion_finish", "chr_copy_segments",
+    "chr_value_range", "chr_crc32_segments_workspace_size", "chr_crc32_segments", "chr_crc32_shift", "chr_crc32_shift_many",
+    "chr_mc_emit_edges", "chr_portion_finish", "chr_copy_segments", "chr_slab_classify", "chr_slab_gid",
     "chr_compress_workspace_size", "chr_compress_capacity", "chr_compress",
     "chr_decode_workspace_size", "chr_decode_regions", "chr_mc_workspace_size", "chr_mc_count",
     "chr_mc_emit", "chr_case_codes", "chr_crc32_workspace_size", "chr_crc32", "chr_crc32_combine",

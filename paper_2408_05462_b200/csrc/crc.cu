@@ -257,6 +257,13 @@ extern "C" uint32_t chr_crc32_shift(uint32_t raw, uint64_t len) {
     return crc_shift(crc_tables_hostref().x2n, raw, len);
 }
 
+// h_out[i] = chr_crc32_shift(h_raw[i], h_len[i]) for n values (host)
+extern "C" void chr_crc32_shift_many(const uint32_t *h_raw, const uint64_t *h_len, int64_t n, uint32_t *h_out) {
+    CHR_XFER_SCOPE;
+    const CrcTables &H = crc_tables_hostref();
+    for (int64_t i = 0; i < n; ++i) h_out[i] = crc_shift(H.x2n, h_raw[i], h_len[i]);
+}
+
 extern "C" uint32_t chr_crc32_combine(uint32_t crc1, uint32_t crc2, uint64_t len2) {
     CHR_XFER_SCOPE;
     const CrcTables &H = crc_tables_hostref();

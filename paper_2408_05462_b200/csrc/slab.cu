@@ -183,3 +183,93 @@ extern "C" int chr_copy_segments(void *d_dst, const void *d_src0, const void *d_
     }
     return cudaGetLastError() == cudaSuccess ? CHR_OK : CHR_E_CUDA;
 }
+
+namespace chr {
+
+// one marching-cubes grid of the z-slab request (request_extract_portions)
+struct SlabGrid {
+    int64_t vbase, vend;     // its vertices in the merged local arrays
+    int64_t halo_lim;        // drop x/y vertices with edge id < halo_lim (3 * plane on a halo grid, else 0)
+    int64_t top_lo;          // export x/y vertices with edge id >= top_lo (top plane; INT64_MAX if none)
+    int64_t key_base;        // selection index * key multiplier
+    int64_t gid_base;        // global id of the grid's first kept vertex - its kept-prefix start
+};
+
+__device__ __forceinline__ int slab_grid_of(const SlabGrid *__restrict__ g, int ng, int64_t v) {
+    int a = 0, b = ng - 1;
+    while (a < b) {
+        const int m = (a + b + 1) >> 1;
+        if (g[m].vbase <= v) a = m; else b = m - 1;
+    }
+    return a;
+}
+
+// flags: bit 0 = dropped (a halo-plane x/y vertex the previous rank created),
+// bit 1 = exported (a top-plane x/y vertex the next rank refers to); key =
+// (selection, in-plane edge) of either kind; per-grid drop / export counts
+__global__ void __launch_bounds__(256) k_slab_classify(const int64_t *__restrict__ vedge, int64_t nv,
+                                                       const SlabGrid *__restrict__ g, int ng,
+                                                       int8_t *__restrict__ flags, int64_t *__restrict__ key,
+                                                       unsigned long long *__restrict__ counts) {
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += (int64_t)gridDim.x * blockDim.x) {
+        const int gi = slab_grid_of(g, ng, v);
+        const SlabGrid G = g[gi];
+        const int64_t e = vedge[v];
+        const bool xy = e % 3 != 2;
+        const bool drop = xy && e < G.halo_lim;
+        const bool top = xy && !drop && e >= G.top_lo;
+        flags[v] = (int8_t)((drop ? 1 : 0) | (top ? 2 : 0));
+        key[v] = drop ? G.key_base + e : (top ? G.key_base + e - G.top_lo : -1);
+        if (drop) atomicAdd(counts + 2 * gi, 1ull);
+        if (top) atomicAdd(counts + 2 * gi + 1, 1ull);
+    }
+}
+
+// global ids of the kept vertices: gid = grid base + (kept vertices before v)
+__global__ void __launch_bounds__(256) k_slab_gid(const int64_t *__restrict__ kept_incl, int64_t nv,
+                                                  const SlabGrid *__restrict__ g, int ng, int64_t *__restrict__ gid) {
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += (int64_t)gridDim.x * blockDim.x)
+        gid[v] = g[slab_grid_of(g, ng, v)].gid_base + kept_incl[v] - 1;
+}
+
+}  // namespace chr
+
+extern "C" int chr_slab_classify(const int64_t *d_vedge, int64_t nv, const int64_t *h_grids, int ng,
+                                 int8_t *d_flags, int64_t *d_key, uint64_t *h_counts, void *d_ws, size_t ws_bytes,
+                                 void *stream) {
+    CHR_XFER_SCOPE;
+    if (ng < 1 || nv < 0 || !h_grids || !h_counts) return CHR_E_PARAMETER;
+    const size_t tb = sizeof(SlabGrid) * (size_t)ng, cb = 16 * (size_t)ng;
+    if (!d_ws || ws_bytes < tb + cb + 256) return CHR_E_WORKSPACE;
+    cudaStream_t st = (cudaStream_t)stream;
+    SlabGrid *d_g = reinterpret_cast<SlabGrid *>(d_ws);
+    unsigned long long *d_c = reinterpret_cast<unsigned long long *>(reinterpret_cast<char *>(d_ws) + ((tb + 255) & ~size_t(255)));
+    CHR_CUDA_TRY(h2d(d_g, h_grids, tb, st));
+    CHR_CUDA_TRY(zero_async({{d_c, cb}}, st));
+    if (nv > 0) {
+        CHR_PROF("k_slab_classify", st);
+        k_slab_classify<<<(unsigned)std::min<int64_t>((nv + 255) / 256, 148 * 16), 256, 0, st>>>(d_vedge, nv, d_g, ng,
+                                                                                                d_flags, d_key, d_c);
+    }
+    CHR_CUDA_TRY(cudaGetLastError());
+    CHR_CUDA_TRY(d2h(h_counts, d_c, cb, st));
+    CHR_CUDA_TRY(stream_sync(st));
+    return CHR_OK;
+}
+
+extern "C" int chr_slab_gid(const int64_t *d_kept_incl, int64_t nv, const int64_t *h_grids, int ng, int64_t *d_gid,
+                            void *d_ws, size_t ws_bytes, void *stream) {
+    CHR_XFER_SCOPE;
+    if (ng < 1 || nv < 0 || !h_grids) return CHR_E_PARAMETER;
+    const size_t tb = sizeof(SlabGrid) * (size_t)ng;
+    if (!d_ws || ws_bytes < tb) return CHR_E_WORKSPACE;
+    cudaStream_t st = (cudaStream_t)stream;
+    SlabGrid *d_g = reinterpret_cast<SlabGrid *>(d_ws);
+    CHR_CUDA_TRY(h2d(d_g, h_grids, tb, st));
+    if (nv > 0) {
+        CHR_PROF("k_slab_gid", st);
+        k_slab_gid<<<(unsigned)std::min<int64_t>((nv + 255) / 256, 148 * 16), 256, 0, st>>>(d_kept_incl, nv, d_g, ng,
+                                                                                           d_gid);
+    }
+    return cudaGetLastError() == cudaSuccess ? CHR_OK : CHR_E_CUDA;
+}

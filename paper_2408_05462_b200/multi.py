@@ -411,6 +411,25 @@ def _allgather_var(t: torch.Tensor, sizes: list[int]) -> list[torch.Tensor]:
     return [o[:n].to(t.device) for o, n in zip(out, sizes)]
 
 
+def _ticker():
+    """CHR_SLAB_TIMES=1: host time of each phase of request_extract_portions (stderr)."""
+    import os
+    import sys
+    import time
+
+    if not os.environ.get("CHR_SLAB_TIMES"):
+        return lambda name: None
+    t = [time.perf_counter()]
+
+    def tick(name):
+        torch.cuda.synchronize()
+        now = time.perf_counter()
+        print(f"[slab] {name}: {1e3 * (now - t[0]):.2f} ms", file=sys.stderr)
+        t[0] = now
+
+    return tick
+
+
 def _rb_np(L):
     """run_bytes over an int64 array."""
     L = np.asarray(L, dtype=np.int64)
@@ -418,6 +437,26 @@ def _rb_np(L):
     for b in (7, 14, 21, 28, 35, 42, 49, 56):
         vl += L >= (1 << b)
     return np.where(L <= 0, 0, np.where(L == 1, 1, 1 + vl))
+
+
+def _run_tokens_np(L):
+    """Token bytes of zero runs (kernels.py:205-218) for an array of lengths:
+    (concatenated uint8 bytes, bytes per run)."""
+    L = np.asarray(L, dtype=np.int64)
+    n = _rb_np(L)
+    out = np.zeros(int(n.sum()), dtype=np.uint8)
+    st = np.concatenate([[0], np.cumsum(n)[:-1]]).astype(np.int64) if len(L) else np.zeros(0, np.int64)
+    one = L == 1
+    out[st[one]] = 1
+    big = L >= 2
+    sb, Lb, nb = st[big], L[big], n[big]
+    out[sb] = 0
+    for k in range(10):  # LEB128 bytes after the 0x00 marker
+        has = nb - 1 > k
+        v = (Lb[has] >> (7 * k)) & 0x7F
+        cont = (Lb[has] >> (7 * (k + 1))) > 0
+        out[sb[has] + 1 + k] = (v | np.where(cont, 0x80, 0)).astype(np.uint8)
+    return out, n
 
 
 def _combine_np(a: dict, b: dict) -> dict:
@@ -479,6 +518,7 @@ def request_extract_portions(res: D.Compressed, k_index: int, k: float, spacing=
     vectorised over the portions (numpy), device work is a fixed number of
     launches independent of the region count."""
     ws = ws or D.Workspaces()
+    _tick = _ticker()
     rank, world = dist.get_rank(), dist.get_world_size()
     L = _abi.lib()
     regions = res.regions
@@ -527,6 +567,7 @@ def request_extract_portions(res: D.Compressed, k_index: int, k: float, spacing=
     woff = np.concatenate([[0], np.cumsum(wsz)[:-1]]).astype(np.int64) if np_ else np.zeros(0, np.int64)
     own_off = woff + halo * pl
 
+    _tick("# ---- byte ranges this rank w")
     # ---- byte ranges this rank wrote (CRC shares) and the re-framed streams
     s0 = prem["len"]
     n_win = plane[J] * ez[J]
@@ -539,72 +580,66 @@ def request_extract_portions(res: D.Compressed, k_index: int, k: float, spacing=
     skip = np.where(mine["nz"] != 0, _rb_np(carry_in + mine["lead"]), 0)
     wdt = np.where(cj == 3, 4, 8)
     base = poff[J]
-    rng = []  # (abs begin, abs end, selection index, payload-relative end)
-    for q in range(np_):
-        b0 = int(base[q])
-        if cj[q] in (0, 3):
-            a_, b_ = int(wdt[q] * s0[q]), int(wdt[q] * (s0[q] + mine["len"][q]))
-            if b_ > a_:
-                rng.append((b0 + a_, b0 + b_, J[q], b_))
-            continue
-        if cj[q] == 2:
-            ba, bb = int(s0[q]) >> 3, (int(s0[q] + mine["len"][q]) + 7) >> 3
-            va, vb = int(bm[q] + 8 * prem["nesc"][q]), int(bm[q] + 8 * (prem["nesc"][q] + mine["nesc"][q]))
-            for a_, b_ in ((ba, bb), (va, vb)):
-                if b_ > a_:
-                    rng.append((b0 + a_, b0 + b_, J[q], b_))
-        if t1[q] > t0[q]:
-            rng.append((b0 + int(tok0[q] + t0[q]), b0 + int(tok0[q] + t1[q]), J[q], int(tok0[q] + t1[q])))
+    # ranges (payload-relative [a, b)) this rank wrote, vectorised over the portions
+    vb_ = (cj == 0) | (cj == 3)
+    c2 = cj == 2
+    ra = [np.where(vb_, wdt * s0, 0), np.where(c2, s0 >> 3, 0), np.where(c2, bm + 8 * prem["nesc"], 0),
+          np.where(vb_, 0, tok0 + t0)]
+    rb_ = [np.where(vb_, wdt * (s0 + mine["len"]), 0), np.where(c2, (s0 + mine["len"] + 7) >> 3, 0),
+           np.where(c2, bm + 8 * (prem["nesc"] + mine["nesc"]), 0), np.where(vb_, 0, tok0 + t1)]
+    ra, rb_ = np.concatenate(ra), np.concatenate(rb_)
+    rj = np.tile(J, 4)
+    ok = rb_ > ra
+    ra, rb_, rj = ra[ok], rb_[ok], rj[ok]
+    base4 = poff[rj]
     share = np.zeros(nsel, dtype=np.uint32)
-    if rng:
-        rr = np.asarray([(a_, b_) for a_, b_, _, _ in rng], dtype=np.uint64).reshape(-1)
-        raw = np.zeros(len(rng), dtype=np.uint32)
-        wk = ws.get("crcseg", L.chr_crc32_segments_workspace_size(len(rng)))
-        D.check(L.chr_crc32_segments(D.ptr(blob), _abi.aptr(rr), len(rng), D.ptr(wk), wk.numel(), _abi.aptr(raw), None,
+    if len(ra):
+        rr = np.stack([base4 + ra, base4 + rb_], 1).astype(np.uint64).reshape(-1)
+        raw = np.zeros(len(ra), dtype=np.uint32)
+        wk = ws.get("crcseg", L.chr_crc32_segments_workspace_size(len(ra)))
+        D.check(L.chr_crc32_segments(D.ptr(blob), _abi.aptr(rr), len(ra), D.ptr(wk), wk.numel(), _abi.aptr(raw), None,
                                      D.stream_ptr()), "chr_crc32_segments")
-        for (_, _, j, end), rv in zip(rng, raw):
-            share[j] ^= L.chr_crc32_shift(int(rv), int(plen[j]) - int(end))
+        after = (plen[rj] - rb_).astype(np.uint64)
+        shifted = np.zeros(len(ra), dtype=np.uint32)
+        L.chr_crc32_shift_many(_abi.aptr(raw), _abi.aptr(after), len(ra), _abi.aptr(shifted))
+        np.bitwise_xor.at(share, rj, shifted)
     tot = np.zeros(nsel, dtype=np.uint32)
     for sh in _allgather(torch.from_numpy(share.view(np.int32).copy())):
         tot ^= sh.numpy().view(np.uint32)
-    for j in range(nsel):
-        if (L.chr_crc32_combine(0xFFFFFFFF, int(tot[j]), int(plen[j])) ^ 0xFFFFFFFF) != int(R["payload_crc"][j]):
-            from .exceptions import CorruptPayloadError
+    init = np.full(nsel, 0xFFFFFFFF, dtype=np.uint32)
+    crc = np.zeros(nsel, dtype=np.uint32)
+    pl64 = plen.astype(np.uint64)
+    L.chr_crc32_shift_many(_abi.aptr(init), _abi.aptr(pl64), nsel, _abi.aptr(crc))
+    crc ^= tot ^ np.uint32(0xFFFFFFFF)
+    if not np.array_equal(crc, R["payload_crc"].astype(np.uint32)):
+        from .exceptions import CorruptPayloadError
 
-            raise CorruptPayloadError("payload checksum mismatch")
-    # re-framed payloads: [run(lead)] + tokens after the boundary run + [run(trail)]
-    extra = bytearray()
-    segs, dec_off, dec_len = [], [], []
-    at = 0
-    for q in range(np_):
-        start = at
-        b0 = int(base[q])
-        if cj[q] in (0, 3):
-            a_, b_ = int(wdt[q] * s0[q]), int(wdt[q] * (s0[q] + mine["len"][q]))
-            segs.append((at, b0 + a_, b_ - a_, 0))
-            at += b_ - a_
-        else:
-            if mine["nz"][q]:
-                head = _run_token(int(mine["lead"][q]))
-                body = (b0 + int(tok0[q] + t0[q] + skip[q]), int(t1[q] - t0[q] - skip[q]))
-                tail = b"" if last[q] else _run_token(int(mine["trail"][q]))
-            else:
-                head, body, tail = _run_token(int(mine["len"][q])), (0, 0), b""
-            for piece in (head, body, tail):
-                if isinstance(piece, bytes):
-                    if piece:
-                        segs.append((at, len(extra), len(piece), 1))
-                        extra += piece
-                        at += len(piece)
-                elif piece[1] > 0:
-                    segs.append((at, piece[0], piece[1], 0))
-                    at += piece[1]
-        dec_off.append(start)
-        dec_len.append(at - start)
+        raise CorruptPayloadError("payload checksum mismatch")
+    # re-framed payloads: per portion [run(lead)] [tokens after the boundary run] [run(trail)]
+    lor_q = lor[J]
+    hl = np.where(lor_q, np.where(mine["nz"] != 0, mine["lead"], mine["len"]), 0)  # head run lengths
+    tl = np.where(lor_q & (mine["nz"] != 0) & ~last, mine["trail"], 0)            # tail run lengths
+    hbytes, hlen = _run_tokens_np(hl)
+    tbytes, tlen = _run_tokens_np(tl)
+    extra = np.concatenate([hbytes, tbytes])
+    hsrc = np.concatenate([[0], np.cumsum(hlen)[:-1]]).astype(np.int64) if np_ else np.zeros(0, np.int64)
+    tsrc = len(hbytes) + (np.concatenate([[0], np.cumsum(tlen)[:-1]]).astype(np.int64) if np_ else np.zeros(0, np.int64))
+    body_src = np.where(vb_, base + wdt * s0, base + tok0 + t0 + skip)
+    body_len = np.where(vb_, wdt * mine["len"], np.where(mine["nz"] != 0, t1 - t0 - skip, 0))
+    seg_len = np.stack([hlen, body_len, tlen], 1).reshape(-1)
+    seg_src = np.stack([hsrc, body_src, tsrc], 1).reshape(-1)
+    seg_kind = np.tile(np.asarray([1, 0, 1], np.int64), np_)
+    seg_dst = np.concatenate([[0], np.cumsum(seg_len)[:-1]]).astype(np.int64) if np_ else np.zeros(0, np.int64)
+    at = int(seg_len.sum()) if np_ else 0
+    dec_off = seg_dst[0::3] if np_ else np.zeros(0, np.int64)
+    dec_len = (hlen + body_len + tlen) if np_ else np.zeros(0, np.int64)
+    keep = seg_len > 0
+    segs = np.stack([seg_dst[keep], seg_src[keep], seg_len[keep], seg_kind[keep]], 1)
     sblob = torch.zeros(at + 16, dtype=torch.uint8, device=dev)
-    xb = torch.tensor(list(extra) or [0], dtype=torch.uint8).to(dev)
-    _copy_segments(sblob, blob, xb, np.asarray(segs, dtype=np.uint64).reshape(-1, 4), 1, ws)
+    xb = torch.from_numpy(extra if len(extra) else np.zeros(1, np.uint8)).to(dev)
+    _copy_segments(sblob, blob, xb, segs, 1, ws)
 
+    _tick("# ---- decode (e = 1/2")
     # ---- decode (e = 1/2 for Lorenzo portions: u_local exact)
     windows = torch.zeros(max(int(wsz.sum()) if np_ else 0, 1), dtype=torch.float64, device=dev)
     if np_:
@@ -622,6 +657,7 @@ def request_extract_portions(res: D.Compressed, k_index: int, k: float, spacing=
         if any(status):
             raise ParameterError(f"portion decode failed: {list(status)}")
 
+    _tick("# ---- z-carries:")
     # ---- z-carries: all-gather of every Lorenzo portion's last-plane u_local
     def last_planes(r):  # (selection indices, plane sizes) in pack order
         jj = np.nonzero(has[r] & lor)[0]
@@ -674,6 +710,7 @@ def request_extract_portions(res: D.Compressed, k_index: int, k: float, spacing=
         dst = windows[int(own_off[q]): int(own_off[q]) + n0]
         dst[bits] = vals
 
+    _tick("# ---- halo planes:")
     # ---- halo planes: all-gather of every non-final portion's last plane
     def top_planes(r):
         jj = np.nonzero(has[r] & (pb_r[r] < oz + ez))[0]
@@ -695,6 +732,7 @@ def request_extract_portions(res: D.Compressed, k_index: int, k: float, spacing=
         tb = np.asarray([(woff[q] * 8, where[int(J[q])] * 8, pl[q] * 8, 0) for q in hq], dtype=np.uint64)
         _copy_segments(windows, tops[rank - 1], None, tb, 1, ws)
 
+    _tick("# ---- marching cubes of each ")
     # ---- marching cubes of each portion's cells (halo plane first)
     gzm = nzp + halo
     gq = np.nonzero(gzm >= 2)[0]  # a one-plane first portion has no cells
@@ -710,24 +748,33 @@ def request_extract_portions(res: D.Compressed, k_index: int, k: float, spacing=
         verts, tris, nt_l, nv_l, vedge = D.marching(windows, mct, k, ws=ws, edges=True)
         nt_g, nv_g = np.asarray(nt_l, np.int64), np.asarray(nv_l, np.int64)
     ng = len(gq)
-    # renumbering, vectorised over vertices: drop the halo-plane x/y vertices
-    # (first touched by the previous rank's last cell layer), number the rest
+    _tick("# renumbering")
+    # renumbering: drop the halo-plane x/y vertices (first touched by the
+    # previous rank's last cell layer), number the rest, export the top-plane
+    # x/y vertex ids (chr_slab_classify / chr_slab_gid, one pass each)
     prev_cells = np.zeros(np_, bool)
     if rank > 0:
         prev_cells = gz_r[rank - 1][J] >= 2
-    drop_grid = torch.from_numpy((halo[gq].astype(bool) & prev_cells[gq]).astype(np.int64)).to(dev)
-    gvid = torch.repeat_interleave(torch.arange(ng, device=dev), torch.from_numpy(nv_g).to(dev)) if ng else \
-        torch.zeros(0, dtype=torch.int64, device=dev)
-    pl_g = torch.from_numpy(pl[gq]).to(dev)
-    gz_g = torch.from_numpy(gzm[gq]).to(dev)
-    axis = vedge % 3
-    drop = (drop_grid[gvid] != 0) & (vedge < 3 * pl_g[gvid]) & (axis != 2)
-    keepv = (~drop).to(torch.int64)
-    kept_g = torch.zeros(ng, dtype=torch.int64, device=dev).index_add_(0, gvid, keepv).cpu().numpy() if ng else nv_g
-    topm = (torch.from_numpy((~last[gq]).astype(np.int64)).to(dev)[gvid] != 0) & \
-        (vedge >= 3 * (gz_g[gvid] - 1) * pl_g[gvid]) & (axis != 2) & ~drop
-    exp_g = torch.zeros(ng, dtype=torch.int64, device=dev).index_add_(0, gvid, topm.to(torch.int64)).cpu().numpy() \
-        if ng else nv_g
+    keymul = 3 * int(plane.max()) if nsel else 1
+    nvt = int(verts.shape[0])
+    vbg = np.concatenate([[0], np.cumsum(nv_g)]).astype(np.int64)
+    gtab = np.zeros((max(ng, 1), 6), dtype=np.int64)
+    if ng:
+        gtab[:, 0] = vbg[:-1]
+        gtab[:, 1] = vbg[1:]
+        gtab[:, 2] = np.where(halo[gq].astype(bool) & prev_cells[gq], 3 * pl[gq], 0)
+        gtab[:, 3] = np.where(~last[gq], 3 * (gzm[gq] - 1) * pl[gq], np.iinfo(np.int64).max)
+        gtab[:, 4] = J[gq] * keymul
+    flags = torch.zeros(max(nvt, 1), dtype=torch.int8, device=dev)
+    vkey = torch.empty(max(nvt, 1), dtype=torch.int64, device=dev)
+    counts = np.zeros(2 * max(ng, 1), dtype=np.uint64)
+    wk = ws.get("slabcls", 64 * max(ng, 1) + 1024)
+    if ng:
+        D.check(L.chr_slab_classify(D.ptr(vedge), nvt, _abi.aptr(gtab), ng, D.ptr(flags), D.ptr(vkey),
+                                    _abi.aptr(counts), D.ptr(wk), wk.numel(), D.stream_ptr()), "chr_slab_classify")
+    dropped_g = counts[0::2][:ng].astype(np.int64)
+    exp_g = counts[1::2][:ng].astype(np.int64)
+    kept_g = nv_g - dropped_g
     cnt = torch.zeros((nsel, 3), dtype=torch.int64)
     cnt[J[gq], 0] = torch.from_numpy(nt_g)
     cnt[J[gq], 1] = torch.from_numpy(kept_g)
@@ -736,30 +783,37 @@ def request_extract_portions(res: D.Compressed, k_index: int, k: float, spacing=
     per_reg = allc[:, :, :2].sum(axis=0)
     reg_base = np.cumsum(per_reg, axis=0) - per_reg
     rank_pre = np.cumsum(allc[:, :, :2], axis=0) - allc[:, :, :2]
-    vb_g = reg_base[J[gq], 1] + rank_pre[rank, J[gq], 1]  # global id of each grid's first kept vertex
-    kstart = np.concatenate([[0], np.cumsum(kept_g)[:-1]]).astype(np.int64)
-    kc = torch.cumsum(keepv, 0) - 1
-    gid = torch.from_numpy(vb_g - kstart).to(dev)[gvid] + kc if ng else torch.zeros(0, dtype=torch.int64, device=dev)
-    # exports: (selection, in-plane key) -> global id of every top-plane x/y vertex
-    keymul = 3 * int(plane.max()) if nsel else 1
-    jsel = torch.from_numpy(J[gq]).to(dev)[gvid] if ng else gvid
-    kexp = jsel[topm] * keymul + (vedge[topm] - 3 * (gz_g[gvid][topm] - 1) * pl_g[gvid][topm])
-    epack = torch.stack([kexp, gid[topm]], 1).reshape(-1) if ng else torch.zeros(0, dtype=torch.int64, device=dev)
+    gid = torch.zeros(max(nvt, 1), dtype=torch.int64, device=dev)
+    drop = (flags[:nvt] & 1) != 0
+    if ng:
+        kstart = np.concatenate([[0], np.cumsum(kept_g)[:-1]]).astype(np.int64)
+        gtab[:, 5] = reg_base[J[gq], 1] + rank_pre[rank, J[gq], 1] - kstart
+        kept_incl = torch.cumsum((~drop).to(torch.int64), 0)
+        D.check(L.chr_slab_gid(D.ptr(kept_incl), nvt, _abi.aptr(gtab), ng, D.ptr(gid), D.ptr(wk), wk.numel(),
+                               D.stream_ptr()), "chr_slab_gid")
+    # exports: (key, global id) of this rank's top-plane x/y vertices
+    if int(exp_g.sum()):
+        top_i = torch.nonzero((flags[:nvt] & 2) != 0).reshape(-1)
+        epack = torch.stack([vkey[top_i], gid[top_i]], 1).reshape(-1)
+    else:
+        epack = torch.zeros(0, dtype=torch.int64, device=dev)
     esz = [int(allc[r, :, 2].sum()) * 2 for r in range(world)]
     allexp = _allgather_var(epack, esz)
-    if rank > 0 and bool(drop.any()):
+    if rank > 0 and int(dropped_g.sum()):
         kv = allexp[rank - 1].view(-1, 2)
         order = torch.argsort(kv[:, 0])
         keys, ids = kv[order, 0], kv[order, 1]
-        want = jsel[drop] * keymul + vedge[drop]
-        pos = torch.searchsorted(keys, want).clamp_max(max(len(keys) - 1, 0))
-        gid[drop] = ids[pos]
+        di = torch.nonzero(drop).reshape(-1)
+        pos = torch.searchsorted(keys, vkey[di]).clamp_max(max(len(keys) - 1, 0))
+        gid[di] = ids[pos]
+    _tick("tris_g")
     tris_g = gid[tris.reshape(-1).to(torch.int64)].reshape(-1, 3).to(torch.int32) if tris.numel() else tris
-    verts_k = verts[~drop] if verts.numel() else verts
+    verts_k = verts[~drop] if (nvt and int(dropped_g.sum())) else verts
     nt_p = np.zeros(np_, np.int64)
     nv_p = np.zeros(np_, np.int64)
     nt_p[gq] = nt_g
     nv_p[gq] = kept_g
+    _tick("end")
     tri_base = (reg_base[J, 0] + rank_pre[rank, J, 0]).tolist()
     vert_base = (reg_base[J, 1] + rank_pre[rank, J, 1]).tolist()
     return SlabMesh(verts_k, tris_g, J.tolist(), [int(x) for x in tri_base], [int(x) for x in vert_base],
