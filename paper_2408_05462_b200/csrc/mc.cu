@@ -593,6 +593,83 @@ __global__ void __launch_bounds__(256) k_mc_count3(const McGrid *__restrict__ G,
     }
 }
 
+// count v4: a LANE per 64-cell row piece (a warp takes 32 consecutive pieces
+// of a batch).  The lane loads its piece's four 66-bit row masks (rows y, y+1
+// x planes z, z+1), finds the live cells -- some corner inside and some
+// outside: (OR of the 8 corners) & ~(AND of the 8 corners), with the x+1
+// corners by a one-bit shift -- and looks up triangles / owned vertices only
+// for those (c3: 3 % of the cells), so a dead piece costs a few dozen
+// instructions of one lane instead of a warp's step.
+__global__ void __launch_bounds__(256) k_mc_count4(const McGrid *__restrict__ G,
+                                                   const int32_t *__restrict__ chunk_grid,
+                                                   const McTables *__restrict__ T,
+                                                   const uint32_t *__restrict__ mask,
+                                                   McPieceCnt *__restrict__ cnt,
+                                                   unsigned long long *__restrict__ queue, int64_t nbatch) {
+    __shared__ __align__(16) uint8_t s_ntri[256];
+    __shared__ __align__(16) uint8_t s_own[256][8];
+    __shared__ McGrid sg[8];
+    {
+        const uint4 *so = reinterpret_cast<const uint4 *>(T->owncnt);
+        uint4 *d_o = reinterpret_cast<uint4 *>(&s_own[0][0]);
+        for (int i = threadIdx.x; i < 128; i += blockDim.x) d_o[i] = __ldg(so + i);
+        if (threadIdx.x < 16)
+            reinterpret_cast<uint4 *>(s_ntri)[threadIdx.x] = __ldg(reinterpret_cast<const uint4 *>(T->ntri) + threadIdx.x);
+    }
+    __syncthreads();
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    McGrid &g = sg[w];
+    int cur_grid = -1;
+    constexpr int NB = (int)(MCH / 32);
+    for (;;) {
+        unsigned long long bq = 0;
+        if (lane == 0) bq = atomicAdd(queue, 1ull);
+        const int64_t bi = (int64_t)__shfl_sync(0xFFFFFFFFu, bq, 0);
+        if (bi >= nbatch) break;
+        const int64_t c = bi / NB;
+        const int gi = __ldg(chunk_grid + c);
+        if (gi != cur_grid) {
+            __syncwarp();
+            const uint32_t *src = reinterpret_cast<const uint32_t *>(G + gi);
+            uint32_t *dst = reinterpret_cast<uint32_t *>(&g);
+            for (int i = lane; i < (int)(sizeof(McGrid) / 4); i += 32) dst[i] = src[i];
+            __syncwarp();
+            cur_grid = gi;
+        }
+        const int64_t lp = (c - g.chunk_base) * MCH + (bi - c * NB) * 32 + lane;
+        if (lp >= g.npieces) continue;
+        const int xt = (int)(lp % g.ntx);
+        const int64_t rr = lp / g.ntx;
+        const int cy = (int)(rr % g.ncy), cz = (int)(rr / g.ncy);
+        const int x0 = xt * MTX;
+        const int ncell = min(MTX, g.ncx - x0);
+        const uint32_t *mbase = mask + g.mask_off;
+        uint64_t m[4];
+        uint32_t h[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+            mask_bits66(mbase + (int64_t)(cz + (r >> 1)) * g.pw, (int64_t)(cy + (r & 1)) * g.nx + x0, m[r], h[r]);
+        const uint64_t a = m[0] & m[1] & m[2] & m[3], o = m[0] | m[1] | m[2] | m[3];
+        const uint32_t ah = h[0] & h[1] & h[2] & h[3], oh = h[0] | h[1] | h[2] | h[3];
+        const uint64_t o1 = (o >> 1) | ((uint64_t)(oh & 1u) << 63), a1 = (a >> 1) | ((uint64_t)(ah & 1u) << 63);
+        const uint64_t cells = ncell >= 64 ? ~0ull : ((1ull << ncell) - 1);
+        uint64_t live = (o | o1) & ~(a & a1) & cells;
+        int t = 0, v = 0;
+        const int fyz = (cy == 0 ? 2 : 0) | (cz == 0 ? 4 : 0);
+        while (live) {
+            const int cc = __ffsll((long long)live) - 1;
+            live &= live - 1;
+            const int code = code_fast(m[0], h[0], m[1], h[1], m[2], h[2], m[3], h[3], cc);
+            t += s_ntri[code];
+            v += s_own[code][fyz | (x0 + cc == 0 ? 1 : 0)];
+        }
+        McPieceCnt out;
+        out.tri = t;
+        out.vert = v;
+        cnt[g.piece_base + lp] = out;
+    }
+}
+
 // emit v3: warp per LIVE row piece (triangles > 0), CTA per scan chunk.  The
 // surface touches ~3 % of the cells (c3: a third of the row pieces), so the
 // work is proportional to live pieces, not to the tile volume.  A piece
@@ -1073,9 +1150,9 @@ static int mc_count_impl(const double *d_grids, const chr_mc_grid_t *h, int64_t 
         }
     }
     if (pl.nchunks > 0) {
-        CHR_PROF("k_mc_count3", st);
+        CHR_PROF("k_mc_count4", st);
         const int64_t nbatch = pl.nchunks * (MCH / 32);
-        k_mc_count3<<<(unsigned)std::min<int64_t>(ceil_div(nbatch, 8), (int64_t)mc_num_sms() * 8), 256, 0, st>>>(
+        k_mc_count4<<<(unsigned)std::min<int64_t>(ceil_div(nbatch, 8), (int64_t)mc_num_sms() * 8), 256, 0, st>>>(
             pl.d_grids, pl.chunk_grid, T, masks, pl.cnt, mc_queue(pl) + 1, nbatch);
     }
     {
