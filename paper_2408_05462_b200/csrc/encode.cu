@@ -443,6 +443,67 @@ __global__ void __launch_bounds__(256) k_summarize(const RegDev *__restrict__ re
     }
 }
 
+// Piece records, a THREAD per 64-sample piece (CSPLIT CTAs of 256 threads per
+// scan chunk): the piece's 64 token values in 16 vector loads (regions start
+// 16-byte aligned in the token-value buffer), then a sequential branch-free
+// fold of the token-size summary -- the warp-per-piece ballot version spent
+// its issue slots on 32 lanes' worth of mask bookkeeping per piece.
+__global__ void __launch_bounds__(256) k_summarize2(const RegDev *__restrict__ regs,
+                                                    const int32_t *__restrict__ chunk_reg,
+                                                    const uint32_t *__restrict__ qz,
+                                                    const uint32_t *__restrict__ escbits,
+                                                    PieceRec *__restrict__ recs) {
+    __shared__ RegDev R;
+    const int64_t c = blockIdx.x / CSPLIT;
+    coop_copy(&R, regs + __ldg(chunk_reg + c));
+    __syncthreads();
+    const int64_t lp = (c - R.chunk_base) * CH + (int64_t)(blockIdx.x % CSPLIT) * (CH / CSPLIT) + threadIdx.x;
+    if (lp >= R.npieces) return;
+    const int64_t s0 = lp * TX;
+    const int vcount = (int)min((int64_t)TX, R.n - s0);
+    const uint32_t *q = qz + R.q_base + s0;
+    int bytes = 0, lead = -1, run = 0;
+    auto fold = [&](uint32_t z, int i) {
+        const bool nz = z != 1u && i < vcount;
+        const int add = (lead >= 0 ? rb_small(run) : 0) + vlen32(z);
+        bytes += nz ? add : 0;
+        lead = (nz && lead < 0) ? i : lead;
+        run = nz ? 0 : run + (i < vcount ? 1 : 0);
+    };
+    if (vcount == TX) {
+        const uint4 *q4 = reinterpret_cast<const uint4 *>(q);
+#pragma unroll 4
+        for (int k = 0; k < TX / 4; ++k) {
+            const uint4 v = __ldg(q4 + k);
+            fold(v.x, 4 * k);
+            fold(v.y, 4 * k + 1);
+            fold(v.z, 4 * k + 2);
+            fold(v.w, 4 * k + 3);
+        }
+    } else {
+        for (int i = 0; i < vcount; ++i) fold(__ldg(q + i), i);
+    }
+    int nesc = 0;
+    if (R.has_esc) {
+        const int64_t bit = (int64_t)R.ebase * 32 + s0;
+        const uint32_t *wp = escbits + (bit >> 5);
+        const int sh = (int)(bit & 31);
+        const uint64_t lo = (uint64_t)__funnelshift_r(wp[0], wp[1], sh) |
+                            ((uint64_t)__funnelshift_r(wp[1], wp[2], sh) << 32);
+        const uint64_t keep = vcount == 64 ? ~0ull : ((1ull << vcount) - 1);
+        nesc = __popcll(lo & keep);
+    }
+    PieceRec pr;
+    pr.bytes = (uint16_t)bytes;
+    pr.vcount = (uint8_t)vcount;
+    pr.lead = (uint8_t)(lead >= 0 ? lead : vcount);
+    pr.trail = (uint8_t)(lead >= 0 ? run : vcount);
+    pr.nesc = (uint8_t)nesc;
+    pr.flags = (uint8_t)(lead >= 0 ? 1 : 0);
+    pr.pad = 0;
+    recs[R.piece_base + lp] = pr;
+}
+
 // item -> region map (replaces a per-CTA binary search over the regions)
 __global__ void k_tile_fill_map(const RegDev *__restrict__ regs, int64_t nreg, int32_t *__restrict__ item_reg,
                                 int32_t *__restrict__ chunk_reg) {
@@ -1513,7 +1574,7 @@ static bool build_plan_uncached(const chr_region_t *h, int64_t nreg, EncPlan &pl
         R.last = 1;
         R.pre = tokseg_identity();
         R.q_base = pl.qtotal;
-        pl.qtotal += R.n;
+        pl.qtotal += (R.n + 3) & ~int64_t(3);  // 16-byte aligned token values per region (k_summarize2)
         R.ebase = pl.etotal;
         pl.etotal += ceil_div(R.n, 32) + 1;
         R.mask = h[r].mask;
@@ -1758,7 +1819,7 @@ extern "C" int chr_compress2(const void *d_vol, int dtype, int src_dtype, int64_
         }
         {
             CHR_PROF("k_summarize", st);
-            k_summarize<<<chunks * CSPLIT, 256, 0, st>>>(pl.d_regs, pl.chunk_reg, pl.qz, pl.escbits, pl.recs);
+            k_summarize2<<<chunks * CSPLIT, 256, 0, st>>>(pl.d_regs, pl.chunk_reg, pl.qz, pl.escbits, pl.recs);
         }
         {
             CHR_PROF("k_scan_reduce", st);
@@ -1932,7 +1993,7 @@ extern "C" int chr_rle_encode(const int64_t *d_q, int64_t n, uint8_t *d_out, uin
     }
     {
         CHR_PROF("k_summarize", st);
-        k_summarize<<<chunks * CSPLIT, 256, 0, st>>>(pl.d_regs, pl.chunk_reg, pl.qz, pl.escbits, pl.recs);
+        k_summarize2<<<chunks * CSPLIT, 256, 0, st>>>(pl.d_regs, pl.chunk_reg, pl.qz, pl.escbits, pl.recs);
     }
     k_scan_reduce<<<chunks, 256, 0, st>>>(pl.params, pl.d_regs, pl.recs, pl.chunk);
     k_scan_regions<<<1, 128, 0, st>>>(pl.params, pl.d_regs, pl.chunk, pl.codec2, pl.scal);
@@ -2099,7 +2160,7 @@ extern "C" int chr_dcompress_local(const void *d_vol, int dtype, int src_dtype, 
     if (chunks) {
         {
             CHR_PROF("k_summarize", st);
-            k_summarize<<<chunks * CSPLIT, 256, 0, st>>>(pl.d_regs, pl.chunk_reg, pl.qz, pl.escbits, pl.recs);
+            k_summarize2<<<chunks * CSPLIT, 256, 0, st>>>(pl.d_regs, pl.chunk_reg, pl.qz, pl.escbits, pl.recs);
         }
         k_scan_reduce<<<chunks, 256, 0, st>>>(pl.params, pl.d_regs, pl.recs, pl.chunk);
     }
