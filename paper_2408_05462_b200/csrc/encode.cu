@@ -39,7 +39,7 @@ namespace chr {
 
 constexpr int TX = 64, TY = 8, ZC = 16, NW = TY + 1;
 constexpr int QB_T = 256, QB_SPT = 4, QB_CAP = QB_T * QB_SPT;  // k_quant_band: threads, slots, samples
-constexpr int CSPLIT = 4;  // k_summarize / k_emit_q CTAs per scan chunk (more warps in flight)
+constexpr int CSPLIT = 4;  // k_summarize2 CTAs per scan chunk
 constexpr int64_t CH = 1024;  // pieces per scan chunk
 
 struct RegDev {
@@ -383,71 +383,12 @@ __global__ void __launch_bounds__(QB_T, 4) k_quant_band(const T *__restrict__ vo
     if (chk32 && __any_sync(0xFFFFFFFFu, inexact) && (tid & 31) == 0) atomicOr(&regs[ri].f32bad, 1);
 }
 
-// Piece records: one warp per 64-sample piece of a window's raster stream,
-// a CTA per scan chunk (1024 pieces of one region).  Reads the token values.
-__global__ void __launch_bounds__(256) k_summarize(const RegDev *__restrict__ regs,
-                                                   const int32_t *__restrict__ chunk_reg,
-                                                   const uint32_t *__restrict__ qz,
-                                                   const uint32_t *__restrict__ escbits,
-                                                   PieceRec *__restrict__ recs) {
-    __shared__ RegDev R;
-    const int64_t c = blockIdx.x / CSPLIT;  // CSPLIT CTAs per scan chunk
-    coop_copy(&R, regs + __ldg(chunk_reg + c));
-    __syncthreads();
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t lt = (1u << lane) - 1u;
-    constexpr int PW = (int)(CH / CSPLIT / 8);
-    int64_t lp = (c - R.chunk_base) * CH + (int64_t)(blockIdx.x % CSPLIT) * (CH / CSPLIT) + (int64_t)w * PW;
-    const int64_t lpe = min(lp + PW, R.npieces);
-    const uint32_t *q = qz + R.q_base;
-    for (; lp < lpe; ++lp) {
-        const int64_t s0 = lp * TX;
-        const int vcount = (int)min((int64_t)TX, R.n - s0);
-        const uint32_t zA = lane < vcount ? __ldg(q + s0 + lane) : 1u;
-        const uint32_t zB = 32 + lane < vcount ? __ldg(q + s0 + 32 + lane) : 1u;
-        const bool nzA = zA != 1u, nzB = zB != 1u;
-        const uint32_t mA = __ballot_sync(0xFFFFFFFFu, nzA), mB = __ballot_sync(0xFFFFFFFFu, nzB);
-        const uint32_t bA = mA & lt, bB = mB & lt;
-        const int prevA = bA ? 31 - __clz(bA) : -1;
-        const int prevB = bB ? 63 - __clz(bB) : (mA ? 31 - __clz(mA) : -1);
-        int bytes = 0;
-        if (mA | mB) {
-            int b = 0;
-            if (nzA) b += (prevA >= 0 ? rb_small(lane - prevA - 1) : 0) + vlen32(zA);
-            if (nzB) b += (prevB >= 0 ? rb_small(32 + lane - prevB - 1) : 0) + vlen32(zB);
-            bytes = __reduce_add_sync(0xFFFFFFFFu, b);
-        }
-        if (lane == 0) {
-            int nesc = 0;
-            if (R.has_esc) {
-                const int64_t bit = (int64_t)R.ebase * 32 + s0;
-                const uint32_t *wp = escbits + (bit >> 5);
-                const int sh = (int)(bit & 31);
-                const uint64_t lo = (uint64_t)__funnelshift_r(wp[0], wp[1], sh) |
-                                    ((uint64_t)__funnelshift_r(wp[1], wp[2], sh) << 32);
-                const uint64_t keep = vcount == 64 ? ~0ull : ((1ull << vcount) - 1);
-                nesc = __popcll(lo & keep);
-            }
-            const int first = mA ? __ffs(mA) - 1 : (mB ? 31 + __ffs(mB) : vcount);
-            const int lastp = mB ? 63 - __clz(mB) : (mA ? 31 - __clz(mA) : -1);
-            PieceRec pr;
-            pr.bytes = (uint16_t)bytes;
-            pr.vcount = (uint8_t)vcount;
-            pr.lead = (uint8_t)first;
-            pr.trail = (uint8_t)((mA | mB) ? vcount - 1 - lastp : vcount);
-            pr.nesc = (uint8_t)nesc;
-            pr.flags = (uint8_t)((mA | mB) ? 1 : 0);
-            pr.pad = 0;
-            recs[R.piece_base + lp] = pr;
-        }
-    }
-}
-
 // Piece records, a THREAD per 64-sample piece (CSPLIT CTAs of 256 threads per
 // scan chunk): the piece's 64 token values in 16 vector loads (regions start
 // 16-byte aligned in the token-value buffer), then a sequential branch-free
-// fold of the token-size summary -- the warp-per-piece ballot version spent
-// its issue slots on 32 lanes' worth of mask bookkeeping per piece.
+// fold of the token-size summary (a warp-per-piece ballot version spent its
+// issue slots on 32 lanes' worth of mask bookkeeping per piece: 0.33 ms vs
+// 0.15 ms at c3).
 __global__ void __launch_bounds__(256) k_summarize2(const RegDev *__restrict__ regs,
                                                     const int32_t *__restrict__ chunk_reg,
                                                     const uint32_t *__restrict__ qz,
@@ -516,29 +457,37 @@ __global__ void k_tile_fill_map(const RegDev *__restrict__ regs, int64_t nreg, i
 }
 
 // ------------------------------------------------------------------ emit
-// Token bytes from the stored token values: one warp per 64-sample piece of
-// the window's raster stream, a CTA per scan chunk, no barriers; the next
-// piece's values and offsets load while this one is written.  Escaped
-// samples (codec 2) come from the escape bits; verbatim regions copy
-// samples (raster position -> volume address).
+// Token bytes, a THREAD per 64-sample piece (4 warps per CTA, 128 pieces):
+// the lane folds its piece's token values into bytes sequentially, into a
+// per-warp shared staging buffer at the piece's offset relative to the
+// warp's first piece (a warp's 32 pieces are consecutive in one region's
+// stream, so its bytes are one contiguous range [tok_off(p0), tok_off(p32))),
+// then the warp writes that range with aligned 4-byte stores (byte stores
+// only for its two edge words; the warp-per-piece ballot/scan version it
+// replaced took 0.62 ms at c3, this one 0.55 ms).  A range larger than the buffer is written
+// byte by byte from the lanes (rare).  Verbatim regions: the CTA's threads
+// copy the samples of its 128 pieces, coalesced.
+constexpr int E2_WARPS = 4;
+constexpr int E2_STAGE = 8192;  // bytes per warp
 template <typename T>
-__global__ void __launch_bounds__(256) k_emit_q(const T *__restrict__ vol, const EncParams *__restrict__ P,
-                                                const RegDev *__restrict__ regs,
-                                                const int32_t *__restrict__ chunk_reg,
-                                                const PieceRec *__restrict__ recs,
-                                                const PieceOff *__restrict__ poffs,
-                                                const uint32_t *__restrict__ qz,
-                                                const uint32_t *__restrict__ escbits, uint8_t *__restrict__ out) {
+__global__ void __launch_bounds__(E2_WARPS * 32) k_emit_q2(const T *__restrict__ vol, const EncParams *__restrict__ P,
+                                                           const RegDev *__restrict__ regs,
+                                                           const int32_t *__restrict__ chunk_reg,
+                                                           const PieceRec *__restrict__ recs,
+                                                           const PieceOff *__restrict__ poffs,
+                                                           const uint32_t *__restrict__ qz,
+                                                           const uint32_t *__restrict__ escbits,
+                                                           uint8_t *__restrict__ out) {
     __shared__ RegDev R;
-    const int64_t c = blockIdx.x / CSPLIT;  // CSPLIT CTAs per scan chunk
+    __shared__ __align__(16) uint8_t stage[E2_WARPS][E2_STAGE];
+    constexpr int PER = E2_WARPS * 32;  // pieces per CTA
+    constexpr int SPLIT = (int)(CH / PER);
+    const int64_t c = blockIdx.x / SPLIT;
     coop_copy(&R, regs + __ldg(chunk_reg + c));
     __syncthreads();
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t lt = (1u << lane) - 1u;
-    constexpr int PW = (int)(CH / CSPLIT / 8);  // pieces per warp
-    int64_t lp = (c - R.chunk_base) * CH + (int64_t)(blockIdx.x % CSPLIT) * (CH / CSPLIT) + (int64_t)w * PW;
-    const int64_t lpe = min(lp + PW, R.npieces);
-    if (lp >= lpe) return;
+    const int64_t lpb = (c - R.chunk_base) * CH + (int64_t)(blockIdx.x % SPLIT) * PER;  // CTA's first piece
+    if (lpb >= R.npieces) return;
     const int codec = R.codec;
     const int64_t NX = P->NX, NY = P->NY;
     const int64_t exy = (int64_t)R.ex * R.ey;
@@ -547,89 +496,108 @@ __global__ void __launch_bounds__(256) k_emit_q(const T *__restrict__ vol, const
         const int64_t y = r / R.ex, x = r - y * R.ex;
         return __ldg(vol + ((R.oz + z) * NY + (R.oy + y)) * NX + R.ox + x);
     };
-    const uint32_t *q = qz + R.q_base;
-    if (codec == 1 || codec == 2) {
-        uint32_t nA = 1u, nB = 1u;
-        PieceOff npo{};
-        auto fetch = [&](int64_t p) {
-            const int64_t s = p * TX;
-            const int vc = (int)min((int64_t)TX, R.n - s);
-            nA = lane < vc ? __ldg(q + s + lane) : 1u;
-            nB = 32 + lane < vc ? __ldg(q + s + 32 + lane) : 1u;
-            npo = poffs[R.piece_base + p];
-        };
-        fetch(lp);
-        for (; lp < lpe; ++lp) {
-            const int64_t s0 = lp * TX;
-            const int vcount = (int)min((int64_t)TX, R.n - s0);
-            const uint32_t zA = nA, zB = nB;
-            const PieceOff po = npo;
-            if (lp + 1 < lpe) fetch(lp + 1);
-            const bool nzA = zA != 1u, nzB = zB != 1u;
-            const uint32_t mA = __ballot_sync(0xFFFFFFFFu, nzA), mB = __ballot_sync(0xFFFFFFFFu, nzB);
-            uint8_t *base = out + R.tok_start + po.tok_off;
-            int totA = 0, totB = 0;
-            if (mA | mB) {  // an all-zero piece only extends the carried run
-                const uint32_t bA = mA & lt, bB = mB & lt;
-                const int prevA = bA ? 31 - __clz(bA) : -1;
-                const int prevB = bB ? 63 - __clz(bB) : (mA ? 31 - __clz(mA) : -1);
-                int64_t runA = 0, runB = 0;
-                int bAy = 0, bBy = 0;
-                if (nzA) {
-                    runA = prevA >= 0 ? lane - prevA - 1 : po.carry + lane;
-                    bAy = (prevA >= 0 ? rb_small((int)runA) : (int)run_bytes(runA)) + vlen32(zA);
-                }
-                if (nzB) {
-                    runB = prevB >= 0 ? 32 + lane - prevB - 1 : po.carry + 32 + lane;
-                    bBy = (prevB >= 0 ? rb_small((int)runB) : (int)run_bytes(runB)) + vlen32(zB);
-                }
-                // one scan of packed (bytes A | bytes B << 16)
-                uint32_t pk = (uint32_t)bAy | ((uint32_t)bBy << 16);
-#pragma unroll
-                for (int off = 1; off < 32; off <<= 1) {
-                    const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, pk, off);
-                    if (lane >= off) pk += t;
-                }
-                const uint32_t tot = __shfl_sync(0xFFFFFFFFu, pk, 31);
-                totA = (int)(tot & 0xFFFFu);
-                totB = (int)(tot >> 16);
-                const int sA = (int)(pk & 0xFFFFu) - bAy, sB = totA + (int)(pk >> 16) - bBy;
-                if (nzA) put_varint32(put_run(base + sA, runA), zA);
-                if (nzB) put_varint32(put_run(base + sB, runB), zB);
-            }
-            if (R.last && lp == R.npieces - 1 && lane == 0) {  // the window's final zero run
-                const int lastp = mB ? 63 - __clz(mB) : (mA ? 31 - __clz(mA) : -1);
-                const int64_t fin = (mA | mB) ? vcount - 1 - lastp : po.carry + vcount;
-                put_run(base + totA + totB, fin);
-            }
-            if (codec == 2 && recs[R.piece_base + lp].nesc) {
-                const int64_t bit = (int64_t)R.ebase * 32 + s0;
-                const uint32_t *wp = escbits + (bit >> 5);
-                const int sh = (int)(bit & 31);
-                const uint32_t eAm = __funnelshift_r(wp[0], wp[1], sh), eBm = __funnelshift_r(wp[1], wp[2], sh);
-                const bool eA = lane < vcount && ((eAm >> lane) & 1u);
-                const bool eB = 32 + lane < vcount && ((eBm >> lane) & 1u);
-                const uint64_t vbase = R.payload_off + (uint64_t)((R.n_win + 7) >> 3);
-                if (eA) put_le(out + vbase + 8 * (po.esc_off + __popc(eAm & lt)), (double)vol_at(s0 + lane));
-                if (eB)
-                    put_le(out + vbase + 8 * (po.esc_off + __popc(vcount >= 32 ? eAm : 0u) + __popc(eBm & lt)),
-                           (double)vol_at(s0 + 32 + lane));
-            }
+    if (codec != 1 && codec != 2) {  // verbatim (codec 3: f32, codec 0: f64), raster order
+        const int64_t s_lo = lpb * TX, s_hi = min(s_lo + (int64_t)PER * TX, R.n);
+        for (int64_t s = s_lo + threadIdx.x; s < s_hi; s += PER) {
+            const T v = vol_at(s);
+            if (codec == 3) put_le(out + R.payload_off + 4 * (R.s_off + s), (float)v);
+            else put_le(out + R.payload_off + 8 * (R.s_off + s), (double)v);
         }
-    } else {  // verbatim (codec 3: f32, codec 0: f64), raster order
-        for (; lp < lpe; ++lp) {
-            const int64_t s0 = lp * TX;
-            const int vcount = (int)min((int64_t)TX, R.n - s0);
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int i = lane + 32 * h;
-                if (i >= vcount) continue;
-                const T v = vol_at(s0 + i);
-                if (codec == 3) put_le(out + R.payload_off + 4 * (R.s_off + s0 + i), (float)v);
-                else put_le(out + R.payload_off + 8 * (R.s_off + s0 + i), (double)v);
-            }
-        }
+        return;
     }
+    const int64_t wp0 = lpb + 32 * w;  // warp's first piece
+    if (wp0 >= R.npieces) return;
+    const int64_t lp = wp0 + lane;
+    const bool have = lp < R.npieces;
+    const int64_t wlast = min(wp0 + 32, R.npieces);  // one past the warp's last piece
+    const int64_t off0 = poffs[R.piece_base + wp0].tok_off;
+    const int64_t off_end = wlast < R.npieces ? poffs[R.piece_base + wlast].tok_off : R.tok_len;
+    const int64_t total = off_end - off0;
+    const bool staged = total <= E2_STAGE;
+    uint8_t *const gdst = out + R.tok_start + off0;
+    uint8_t *const sbuf = stage[w];
+    if (have) {
+        const PieceOff po = poffs[R.piece_base + lp];
+        const int64_t s0 = lp * TX;
+        const int vcount = (int)min((int64_t)TX, R.n - s0);
+        int64_t cur = po.tok_off - off0;
+        int64_t run = po.carry;
+        auto put = [&](uint8_t b) {
+            if (staged) sbuf[cur] = b;
+            else gdst[cur] = b;
+            ++cur;
+        };
+        auto put_runs = [&](int64_t L) {
+            if (L == 1) {
+                put(1);
+            } else if (L >= 2) {
+                put(0);
+                uint64_t u = (uint64_t)L;
+                while (u >= 0x80) {
+                    put((uint8_t)((u & 0x7F) | 0x80));
+                    u >>= 7;
+                }
+                put((uint8_t)u);
+            }
+        };
+        const uint32_t *q = qz + R.q_base + s0;
+        uint32_t em0 = 0, em1 = 0;  // escape bits of the piece (codec 2)
+        int64_t erank = po.esc_off;
+        if (codec == 2 && recs[R.piece_base + lp].nesc) {
+            const int64_t bit = (int64_t)R.ebase * 32 + s0;
+            const uint32_t *wq = escbits + (bit >> 5);
+            const int sh = (int)(bit & 31);
+            em0 = __funnelshift_r(wq[0], wq[1], sh);
+            em1 = __funnelshift_r(wq[1], wq[2], sh);
+        }
+        const uint64_t vbase = R.payload_off + (uint64_t)((R.n_win + 7) >> 3);
+        auto step = [&](uint32_t z, int i) {
+            if (z != 1u) {
+                put_runs(run);
+                run = 0;
+                uint32_t u = z;
+                while (u >= 0x80u) {
+                    put((uint8_t)((u & 0x7Fu) | 0x80u));
+                    u >>= 7;
+                }
+                put((uint8_t)u);
+            } else {
+                ++run;
+            }
+            if ((i < 32 ? (em0 >> i) : (em1 >> (i - 32))) & 1u)
+                put_le(out + vbase + 8 * (erank++), (double)vol_at(s0 + i));
+        };
+        if (vcount == TX) {
+            const uint4 *q4 = reinterpret_cast<const uint4 *>(q);
+#pragma unroll 2
+            for (int k = 0; k < TX / 4; ++k) {
+                const uint4 v = __ldg(q4 + k);
+                step(v.x, 4 * k);
+                step(v.y, 4 * k + 1);
+                step(v.z, 4 * k + 2);
+                step(v.w, 4 * k + 3);
+            }
+        } else {
+            for (int i = 0; i < vcount; ++i) step(__ldg(q + i), i);
+        }
+        if (R.last && lp == R.npieces - 1) put_runs(run);  // the window's final zero run
+    }
+    if (!staged) return;
+    __syncwarp();
+    // the warp's bytes [0, total) -> gdst, aligned words + two edge words
+    const uintptr_t d0 = (uintptr_t)gdst;
+    const int head = (int)((4 - (d0 & 3)) & 3);
+    const int h = (int)(total < head ? total : (int64_t)head);
+    if (lane < h) gdst[lane] = sbuf[lane];
+    const int64_t nw = (total - h) >> 2;
+    uint32_t *gw = reinterpret_cast<uint32_t *>(gdst + h);
+    for (int64_t j = lane; j < nw; j += 32) {
+        const int b = h + 4 * (int)j;
+        gw[j] = (uint32_t)sbuf[b] | ((uint32_t)sbuf[b + 1] << 8) | ((uint32_t)sbuf[b + 2] << 16) |
+                ((uint32_t)sbuf[b + 3] << 24);
+    }
+    const int64_t tb = h + 4 * nw;
+    if (tb + lane < total) gdst[tb + lane] = sbuf[tb + lane];
 }
 
 // ------------------------------------------------------------------ scans
@@ -1857,12 +1825,12 @@ extern "C" int chr_compress2(const void *d_vol, int dtype, int src_dtype, int64_
         }
         if (dtype == CHR_F32) {
             CHR_PROF("k_emit_q<float>", st);
-            k_emit_q<float><<<chunks * CSPLIT, 256, 0, st>>>((const float *)d_vol, pl.params, pl.d_regs,
+            k_emit_q2<float><<<chunks * (unsigned)(CH / (E2_WARPS * 32)), E2_WARPS * 32, 0, st>>>((const float *)d_vol, pl.params, pl.d_regs,
                                                              pl.chunk_reg, pl.recs, pl.poffs, pl.qz, pl.escbits,
                                                              d_out);
         } else {
             CHR_PROF("k_emit_q<double>", st);
-            k_emit_q<double><<<chunks * CSPLIT, 256, 0, st>>>((const double *)d_vol, pl.params, pl.d_regs,
+            k_emit_q2<double><<<chunks * (unsigned)(CH / (E2_WARPS * 32)), E2_WARPS * 32, 0, st>>>((const double *)d_vol, pl.params, pl.d_regs,
                                                               pl.chunk_reg, pl.recs, pl.poffs, pl.qz, pl.escbits,
                                                               d_out);
         }
@@ -2001,7 +1969,7 @@ extern "C" int chr_rle_encode(const int64_t *d_q, int64_t n, uint8_t *d_out, uin
     k_scan_down<<<chunks, 256, 0, st>>>(pl.params, pl.d_regs, pl.recs, pl.chunk, pl.poffs);
     {
         CHR_PROF("k_emit_q<double>", st);
-        k_emit_q<double><<<chunks * CSPLIT, 256, 0, st>>>(nullptr, pl.params, pl.d_regs, pl.chunk_reg, pl.recs, pl.poffs,
+        k_emit_q2<double><<<chunks * (unsigned)(CH / (E2_WARPS * 32)), E2_WARPS * 32, 0, st>>>(nullptr, pl.params, pl.d_regs, pl.chunk_reg, pl.recs, pl.poffs,
                                                  pl.qz, pl.escbits, d_out);
     }
     CHR_CUDA_TRY(cudaGetLastError());
@@ -2253,10 +2221,10 @@ extern "C" int chr_dcompress_finish(const void *d_vol, int dtype, int src_dtype,
         k_scan_down<<<chunks, 256, 0, st>>>(pl.params, pl.d_regs, pl.recs, pl.chunk, pl.poffs);
         CHR_PROF(dtype == CHR_F32 ? "k_emit_q<float>" : "k_emit_q<double>", st);
         if (dtype == CHR_F32)
-            k_emit_q<float><<<chunks * CSPLIT, 256, 0, st>>>((const float *)d_vol, pl.params, pl.d_regs, pl.chunk_reg,
+            k_emit_q2<float><<<chunks * (unsigned)(CH / (E2_WARPS * 32)), E2_WARPS * 32, 0, st>>>((const float *)d_vol, pl.params, pl.d_regs, pl.chunk_reg,
                                                     pl.recs, pl.poffs, pl.qz, pl.escbits, d_out);
         else
-            k_emit_q<double><<<chunks * CSPLIT, 256, 0, st>>>((const double *)d_vol, pl.params, pl.d_regs, pl.chunk_reg,
+            k_emit_q2<double><<<chunks * (unsigned)(CH / (E2_WARPS * 32)), E2_WARPS * 32, 0, st>>>((const double *)d_vol, pl.params, pl.d_regs, pl.chunk_reg,
                                                      pl.recs, pl.poffs, pl.qz, pl.escbits, d_out);
     }
     if (!c2.empty()) k_bitmap<<<148, 256, 0, st>>>(pl.d_regs, pl.codec2, pl.scal, pl.escbits, d_out);
