@@ -156,7 +156,7 @@ def kernel_bytes(name, info, N):
         "k_tok_fast": info["c_sel"],            # selected payload read (decompress: C_sel + 8 N_sel)
         "k_band": info["c_sel"] + 8 * info["n_sel"],
         "k_lorenzo": info["c_sel"] + 8 * info["n_sel"],
-        "k_mc_emit3": 24 * info["nvert"] + 12 * info["ntri"],  # mesh write (MC: 8 N_sel + 24 nv + 12 nt)
+        "k_mc_emit4": 24 * info["nvert"] + 12 * info["ntri"],  # mesh write (MC: 8 N_sel + 24 nv + 12 nt)
     }
     return table.get(name)
 

@@ -511,9 +511,11 @@ __global__ void __launch_bounds__(E2_WARPS * 32) k_emit_q2(const T *__restrict__
     const bool have = lp < R.npieces;
     const int64_t wlast = min(wp0 + 32, R.npieces);  // one past the warp's last piece
     const int64_t off0 = poffs[R.piece_base + wp0].tok_off;
+    // upper bound of the warp's bytes (a z-slab portion that does not end its
+    // window stops short of tok_len: its trailing run belongs to the next one)
     const int64_t off_end = wlast < R.npieces ? poffs[R.piece_base + wlast].tok_off : R.tok_len;
-    const int64_t total = off_end - off0;
-    const bool staged = total <= E2_STAGE;
+    const bool staged = off_end - off0 <= E2_STAGE;
+    int64_t cur_end = 0;  // end of this lane's bytes (relative to off0)
     uint8_t *const gdst = out + R.tok_start + off0;
     uint8_t *const sbuf = stage[w];
     if (have) {
@@ -581,9 +583,11 @@ __global__ void __launch_bounds__(E2_WARPS * 32) k_emit_q2(const T *__restrict__
             for (int i = 0; i < vcount; ++i) step(__ldg(q + i), i);
         }
         if (R.last && lp == R.npieces - 1) put_runs(run);  // the window's final zero run
+        cur_end = cur;
     }
     if (!staged) return;
     __syncwarp();
+    const int64_t total = (int64_t)__reduce_max_sync(0xFFFFFFFFu, (unsigned)cur_end);
     // the warp's bytes [0, total) -> gdst, aligned words + two edge words
     const uintptr_t d0 = (uintptr_t)gdst;
     const int head = (int)((4 - (d0 & 3)) & 3);

@@ -14,12 +14,13 @@
 //   (owned crossing edges in earlier cells) + (its first-appearance rank in
 //   the owner's triangle row), and both come from tables + one scan.
 //
-//   k_mc_count3  warp per 64-cell row piece (persistent warps on a batch
-//                queue): triangles and owned vertices from the inside masks
+//   k_mc_count4  lane per 64-cell row piece (persistent warps on a batch
+//                queue): live cells, triangles and owned vertices from the
+//                inside masks; per live piece the owned-vertex prefix of each
+//                live cell (u16) and 4-bit triangle counts
 //   k_mc_reduce / k_mc_grid_scan / k_mc_grids / k_mc_down   chunked scans
-//   k_mc_emit3   warp per LIVE row piece: codes + vertex bases of the own row
-//                and the three owner rows from nine row masks, then a lane per
-//                triangle and a lane per owned vertex
+//   k_mc_emit4   lane per LIVE CELL: its code and its owners' codes from nine
+//                3-bit row windows, owner vertex ids from piece base + prefix
 #include <algorithm>
 #include <cstring>
 #include <mutex>
@@ -415,184 +416,6 @@ __device__ __forceinline__ int code_from(uint64_t m00, uint32_t h00, uint64_t m1
                  bit_at(m11, h11, c + 1) << 6 | bit_at(m11, h11, c) << 7);
 }
 
-// count from the masks: warp per 64-cell row piece, CTA per scan chunk
-__global__ void __launch_bounds__(256) k_mc_count3(const McGrid *__restrict__ G,
-                                                   const int32_t *__restrict__ chunk_grid,
-                                                   const McTables *__restrict__ T,
-                                                   const uint32_t *__restrict__ mask,
-                                                   McPieceCnt *__restrict__ cnt,
-                                                   unsigned long long *__restrict__ queue, int64_t nbatch) {
-    __shared__ __align__(16) uint8_t s_ntri[256];
-    __shared__ __align__(16) uint8_t s_own[256][8];
-    __shared__ McGrid sg[8];
-    {
-        const uint4 *so = reinterpret_cast<const uint4 *>(T->owncnt);
-        uint4 *d_o = reinterpret_cast<uint4 *>(&s_own[0][0]);
-        for (int i = threadIdx.x; i < 128; i += blockDim.x) d_o[i] = __ldg(so + i);
-        if (threadIdx.x < 16)
-            reinterpret_cast<uint4 *>(s_ntri)[threadIdx.x] = __ldg(reinterpret_cast<const uint4 *>(T->ntri) + threadIdx.x);
-    }
-    __syncthreads();
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    McGrid &g = sg[w];
-    int cur_grid = -1;
-    // persistent warps: batches of 32 pieces from a global queue (live and
-    // dead pieces cost very differently; a fixed split left warps idle)
-    auto run = [&](int64_t lp, const int64_t lpe) {
-    int xt = (int)(lp % g.ntx);
-    const int64_t r = lp / g.ntx;
-    int cy = (int)(r % g.ncy), cz = (int)(r / g.ncy);
-    const uint32_t *mbase = mask + g.mask_off;
-    if (g.ntx == 1 && g.ncx <= 32) {
-        // rows of <= 32 cells: two pieces (rows) per step, one per lane
-        const int lane_ok = lane < g.ncx;
-        for (; lp < lpe; lp += 2) {
-            int cy2 = cy + 1, cz2 = cz;
-            if (cy2 == g.ncy) {
-                cy2 = 0;
-                ++cz2;
-            }
-            const bool two = lp + 1 < lpe;
-            int t = 0, v = 0, t2 = 0, v2 = 0;
-            // lane 4q + r reads row mask r (y + (r & 1), z + (r >> 1)) of piece q; shuffles share them
-            uint64_t mr = 0;
-            uint32_t hr = 0;
-            if (lane < (two ? 8 : 4)) {
-                const int q = lane >> 2, rr = lane & 3;
-                const int qy = q ? cy2 : cy, qz = q ? cz2 : cz;
-                mask_bits66(mbase + (int64_t)(qz + (rr >> 1)) * g.pw, (int64_t)(qy + (rr & 1)) * g.nx, mr, hr);
-            }
-            const uint32_t mlo = (uint32_t)mr, mhi = (uint32_t)(mr >> 32);
-#pragma unroll
-            for (int q = 0; q < 2; ++q) {
-                const int qy = q ? cy2 : cy, qz = q ? cz2 : cz;
-                if (q && !two) break;
-                auto row = [&](int r, uint64_t &m, uint32_t &h) {
-                    m = (uint64_t)__shfl_sync(0xFFFFFFFFu, mlo, 4 * q + r) |
-                        ((uint64_t)__shfl_sync(0xFFFFFFFFu, mhi, 4 * q + r) << 32);
-                    h = __shfl_sync(0xFFFFFFFFu, hr, 4 * q + r);
-                };
-                uint64_t m00, m10, m01, m11;
-                uint32_t h00, h10, h01, h11;
-                row(0, m00, h00);
-                row(1, m10, h10);
-                row(2, m01, h01);
-                row(3, m11, h11);
-                // the row's ncx + 1 <= 33 corner bits of all four rows equal (warp-uniform):
-                // every cell is case 0 or 255 -- no triangles, nothing owned
-                const uint64_t live = (1ull << (g.ncx + 1)) - 1;
-                const uint64_t a4 = m00 & m10 & m01 & m11 & live, o4 = (m00 | m10 | m01 | m11) & live;
-                if (o4 == 0 || a4 == live) continue;
-                if (lane_ok) {
-                    const int code = code_fast(m00, h00, m10, h10, m01, h01, m11, h11, lane);
-                    (q ? t2 : t) = s_ntri[code];
-                    (q ? v2 : v) = s_own[code][bflags(lane, qy, qz)];
-                }
-            }
-            const uint32_t pa = __reduce_add_sync(0xFFFFFFFFu, (uint32_t)t | ((uint32_t)v << 16));
-            const uint32_t pb = __reduce_add_sync(0xFFFFFFFFu, (uint32_t)t2 | ((uint32_t)v2 << 16));
-            if (lane == 0) {
-                McPieceCnt o;
-                o.tri = (int32_t)(pa & 0xFFFFu);
-                o.vert = (int32_t)(pa >> 16);
-                cnt[g.piece_base + lp] = o;
-                if (two) {
-                    o.tri = (int32_t)(pb & 0xFFFFu);
-                    o.vert = (int32_t)(pb >> 16);
-                    cnt[g.piece_base + lp + 1] = o;
-                }
-            }
-            cy = cy2 + 1;
-            cz = cz2;
-            if (cy == g.ncy) {
-                cy = 0;
-                ++cz;
-            }
-        }
-        return;
-    }
-    for (; lp < lpe; ++lp) {
-        const int x0 = xt * MTX;
-        // lane r < 4 reads row (cy + (r & 1)) of plane (cz + (r >> 1)); shuffles share them
-        uint64_t mr = 0;
-        uint32_t hr = 0;
-        if (lane < 4) {
-            const uint32_t *mp = mbase + (int64_t)(cz + (lane >> 1)) * g.pw;
-            mask_bits66(mp, (int64_t)(cy + (lane & 1)) * g.nx + x0, mr, hr);
-        }
-        const uint32_t mlo = (uint32_t)mr, mhi = (uint32_t)(mr >> 32);
-        auto row = [&](int r, uint64_t &m, uint32_t &h) {
-            m = (uint64_t)__shfl_sync(0xFFFFFFFFu, mlo, r) | ((uint64_t)__shfl_sync(0xFFFFFFFFu, mhi, r) << 32);
-            h = __shfl_sync(0xFFFFFFFFu, hr, r);
-        };
-        uint64_t m00, m10, m01, m11;
-        uint32_t h00, h10, h01, h11;
-        row(0, m00, h00);
-        row(1, m10, h10);
-        row(2, m01, h01);
-        row(3, m11, h11);
-        int t = 0, v = 0;
-        // all 66 x 4 corner bits equal (the usual case away from the surface):
-        // every cell is case 0 or 255, no triangles, nothing owned
-        const uint64_t a1 = m00 & m10 & m01 & m11, o1 = m00 | m10 | m01 | m11;
-        const uint32_t ah = h00 & h10 & h01 & h11 & 3u, oh = (h00 | h10 | h01 | h11) & 3u;
-        if (!((o1 == 0 && oh == 0) || (a1 == ~0ull && ah == 3u))) {
-            // lane owns cells 2 lane, 2 lane + 1: bits 2 lane .. 2 lane + 2 of each row
-            const int cA = 2 * lane;
-            auto trip = [&](uint64_t m, uint32_t h) {
-                return (uint32_t)(m >> cA) | (uint32_t)(((uint64_t)h << 2) << (62 - cA));
-            };
-            const uint32_t t00 = trip(m00, h00), t10 = trip(m10, h10), t01 = trip(m01, h01), t11 = trip(m11, h11);
-            const int fyz = (cy == 0 ? 2 : 0) | (cz == 0 ? 4 : 0);
-#pragma unroll
-            for (int hh = 0; hh < 2; ++hh) {
-                if (x0 + cA + hh < g.ncx) {
-                    const int code = (int)(((t00 >> hh) & 3u) | pair_swap((t10 >> hh) & 3u) << 2 |
-                                           ((t01 >> hh) & 3u) << 4 | pair_swap((t11 >> hh) & 3u) << 6);
-                    t += s_ntri[code];
-                    v += s_own[code][fyz | (x0 + cA + hh == 0 ? 1 : 0)];
-                }
-            }
-            t = __reduce_add_sync(0xFFFFFFFFu, t);
-            v = __reduce_add_sync(0xFFFFFFFFu, v);
-        }
-        if (lane == 0) {
-            McPieceCnt o;
-            o.tri = t;
-            o.vert = v;
-            cnt[g.piece_base + lp] = o;
-        }
-        if (++xt == g.ntx) {
-            xt = 0;
-            if (++cy == g.ncy) {
-                cy = 0;
-                ++cz;
-            }
-        }
-    }
-    };
-    constexpr int NB = (int)(MCH / 32);
-    for (;;) {
-        unsigned long long bq = 0;
-        if (lane == 0) bq = atomicAdd(queue, 1ull);
-        const int64_t bi = (int64_t)__shfl_sync(0xFFFFFFFFu, bq, 0);
-        if (bi >= nbatch) break;
-        const int64_t c = bi / NB;
-        const int gi = __ldg(chunk_grid + c);
-        if (gi != cur_grid) {
-            __syncwarp();
-            const uint32_t *src = reinterpret_cast<const uint32_t *>(G + gi);
-            uint32_t *dst = reinterpret_cast<uint32_t *>(&g);
-            for (int i = lane; i < (int)(sizeof(McGrid) / 4); i += 32) dst[i] = src[i];
-            __syncwarp();
-            cur_grid = gi;
-        }
-        const int64_t lp = (c - g.chunk_base) * MCH + (bi - c * NB) * 32;
-        const int64_t lpe = min(lp + 32, g.npieces);
-        if (lp < lpe) run(lp, lpe);
-    }
-}
-
 // count v4: a LANE per 64-cell row piece (a warp takes 32 consecutive pieces
 // of a batch).  The lane loads its piece's four 66-bit row masks (rows y, y+1
 // x planes z, z+1), finds the live cells -- some corner inside and some
@@ -604,7 +427,8 @@ __global__ void __launch_bounds__(256) k_mc_count4(const McGrid *__restrict__ G,
                                                    const int32_t *__restrict__ chunk_grid,
                                                    const McTables *__restrict__ T,
                                                    const uint32_t *__restrict__ mask,
-                                                   McPieceCnt *__restrict__ cnt,
+                                                   McPieceCnt *__restrict__ cnt, uint64_t *__restrict__ lmask,
+                                                   uint4 *__restrict__ tnib, uint16_t *__restrict__ vpre,
                                                    unsigned long long *__restrict__ queue, int64_t nbatch) {
     __shared__ __align__(16) uint8_t s_ntri[256];
     __shared__ __align__(16) uint8_t s_own[256][8];
@@ -653,64 +477,91 @@ __global__ void __launch_bounds__(256) k_mc_count4(const McGrid *__restrict__ G,
         const uint32_t ah = h[0] & h[1] & h[2] & h[3], oh = h[0] | h[1] | h[2] | h[3];
         const uint64_t o1 = (o >> 1) | ((uint64_t)(oh & 1u) << 63), a1 = (a >> 1) | ((uint64_t)(ah & 1u) << 63);
         const uint64_t cells = ncell >= 64 ? ~0ull : ((1ull << ncell) - 1);
-        uint64_t live = (o | o1) & ~(a & a1) & cells;
+        const uint64_t live0 = (o | o1) & ~(a & a1) & cells;
+        uint64_t live = live0;
         int t = 0, v = 0;
         const int fyz = (cy == 0 ? 2 : 0) | (cz == 0 ? 4 : 0);
+        uint64_t tn0 = 0, tn1 = 0, tn2 = 0, tn3 = 0;
+        const int64_t gp = g.piece_base + lp;
+        uint16_t *vp = vpre + 64 * gp;
         while (live) {
             const int cc = __ffsll((long long)live) - 1;
             live &= live - 1;
             const int code = code_fast(m[0], h[0], m[1], h[1], m[2], h[2], m[3], h[3], cc);
-            t += s_ntri[code];
-            v += s_own[code][fyz | (x0 + cc == 0 ? 1 : 0)];
+            const uint32_t nt = s_ntri[code], no = s_own[code][fyz | (x0 + cc == 0 ? 1 : 0)];
+            vp[cc] = (uint16_t)v;  // owned vertices of the piece's earlier cells
+            t += nt;
+            v += no;
+            const int sh = 4 * (cc & 15), q = cc >> 4;
+            const uint64_t tb = (uint64_t)nt << sh;
+            tn0 |= q == 0 ? tb : 0;
+            tn1 |= q == 1 ? tb : 0;
+            tn2 |= q == 2 ? tb : 0;
+            tn3 |= q == 3 ? tb : 0;
         }
         McPieceCnt out;
         out.tri = t;
         out.vert = v;
-        cnt[g.piece_base + lp] = out;
+        cnt[gp] = out;
+        lmask[gp] = live0;
+        if (live0) {  // per-cell triangle counts, 4 bits each (k_mc_emit4's triangle offsets)
+            uint4 *np = tnib + 2 * gp;
+            np[0] = make_uint4((uint32_t)tn0, (uint32_t)(tn0 >> 32), (uint32_t)tn1, (uint32_t)(tn1 >> 32));
+            np[1] = make_uint4((uint32_t)tn2, (uint32_t)(tn2 >> 32), (uint32_t)tn3, (uint32_t)(tn3 >> 32));
+        }
     }
 }
 
-// emit v3: warp per LIVE row piece (triangles > 0), CTA per scan chunk.  The
-// surface touches ~3 % of the cells (c3: a third of the row pieces), so the
-// work is proportional to live pieces, not to the tile volume.  A piece
-// needs the (code, vertex base) of its own cell row and of the three rows an
-// owner can sit in, (y-1, z), (y, z-1), (y-1, z-1), each with the halo cell
-// x0-1: nine row masks (rows y-1..y+1 x planes z-1..z+1) give all of them.
-// Row slot r = (owner offset bits >> 1) & 3: bit 0 = y-1, bit 1 = z-1.
-constexpr int E3W = 8;  // warps per CTA
-struct E3Warp {
-    McGrid g;             // grid of the warp's current batch
-    uint64_t m[9];        // row masks, bit c <-> x0 - 1 + c; index 3 * (dz + 1) + (dy + 1)
-    int64_t rb[5];        // vertex base of slot r's piece (r < 4), own triangle base (4)
-    uint32_t h[9];
-    int64_t vb[4][66];    // vertex base of cell column c (c = 0: halo x0 - 1)
-    int32_t tofs[64];     // own row: triangle offset of each cell within the piece
-    int32_t ex[64];       // own row: exclusive owned-vertex offset of each cell within the piece
-    uint8_t code[4][66];
-};
-__global__ void __launch_bounds__(E3W * 32, 4) k_mc_emit3(const double *__restrict__ grids, const McGrid *__restrict__ G,
+// Sum of the 4-bit fields of the four words below field b (b in 0..63).
+__device__ __forceinline__ uint32_t nib_prefix(uint4 A, uint4 B, int b) {
+    const int q = b >> 4;
+    const uint64_t part = (1ull << (4 * (b & 15))) - 1;
+    uint64_t w0 = (uint64_t)A.x | ((uint64_t)A.y << 32), w1 = (uint64_t)A.z | ((uint64_t)A.w << 32);
+    uint64_t w2 = (uint64_t)B.x | ((uint64_t)B.y << 32), w3 = (uint64_t)B.z | ((uint64_t)B.w << 32);
+    w0 = q > 0 ? w0 : (q == 0 ? w0 & part : 0);
+    w1 = q > 1 ? w1 : (q == 1 ? w1 & part : 0);
+    w2 = q > 2 ? w2 : (q == 2 ? w2 & part : 0);
+    w3 = q == 3 ? w3 & part : 0;
+    constexpr uint64_t N4 = 0x0F0F0F0F0F0F0F0Full, B8 = 0x00FF00FF00FF00FFull;
+    auto bytes = [](uint64_t x) { return (x & N4) + ((x >> 4) & N4); };  // 8 bytes <= 24 each
+    uint64_t y = bytes(w0) + bytes(w1) + bytes(w2) + bytes(w3);       // bytes <= 96
+    y = (y & B8) + ((y >> 8) & B8);                                   // 4 halves <= 192
+    return (uint32_t)((y * 0x0001000100010001ull) >> 48);
+}
+
+// emit v4: a LANE per LIVE CELL.  A warp takes 32 consecutive pieces of a
+// batch, scans their live-cell counts (k_mc_count4's live masks) and deals
+// the batch's live cells to its lanes 32 at a time, so every lane does one
+// cell's work whatever the pieces' densities.  A cell's vertex base is its
+// piece's base + the 4-bit owned-vertex counts of the cells before it in
+// the piece (k_mc_count4's per-piece fields, a SWAR sum); the same holds for
+// its triangle offset and for any owner cell, so a triangle corner costs
+// the owner's code (from nine 3-bit row windows around the cell), its piece
+// base and fields, and one rank lookup -- no per-piece code arrays, no
+// warp-wide scans over the piece's 64 cells.
+constexpr int E4W = 8;  // warps per CTA
+__global__ void __launch_bounds__(E4W * 32) k_mc_emit4(const double *__restrict__ grids, const McGrid *__restrict__ G,
                                                        const int32_t *__restrict__ chunk_grid, double k,
                                                        const McTables *__restrict__ T,
                                                        const McPieceBase *__restrict__ base,
-                                                       const McPieceCnt *__restrict__ cnt,
+                                                       const uint64_t *__restrict__ lmask,
+                                                       const uint4 *__restrict__ tnib,
+                                                       const uint16_t *__restrict__ vpre,
                                                        const uint32_t *__restrict__ mask,
                                                        unsigned long long *__restrict__ queue, int64_t nbatch,
                                                        double *__restrict__ verts, int32_t *__restrict__ tris,
                                                        int64_t *__restrict__ vedge) {
     __shared__ __align__(16) int8_t s_tri[256][16];
-    __shared__ __align__(16) uint8_t s_ntri[256];
-    __shared__ __align__(16) uint8_t s_own[256][8];
+    __shared__ __align__(16) int8_t s_rank[256][8][12];
     __shared__ uint8_t s_cinfo[12][8], s_vinfo[12];
-    __shared__ E3Warp sw[E3W];
+    __shared__ McGrid sg[E4W];
     {
         const uint4 *src = reinterpret_cast<const uint4 *>(T->tri);
         uint4 *dst = reinterpret_cast<uint4 *>(&s_tri[0][0]);
         for (int i = threadIdx.x; i < 256; i += blockDim.x) dst[i] = __ldg(src + i);
-        const uint4 *so = reinterpret_cast<const uint4 *>(T->owncnt);
-        uint4 *d_o = reinterpret_cast<uint4 *>(&s_own[0][0]);
-        for (int i = threadIdx.x; i < 128; i += blockDim.x) d_o[i] = __ldg(so + i);
-        if (threadIdx.x < 16)
-            reinterpret_cast<uint4 *>(s_ntri)[threadIdx.x] = __ldg(reinterpret_cast<const uint4 *>(T->ntri) + threadIdx.x);
+        const uint4 *sr = reinterpret_cast<const uint4 *>(T->rank);
+        uint4 *dr = reinterpret_cast<uint4 *>(&s_rank[0][0][0]);
+        for (int i = threadIdx.x; i < (int)(sizeof(s_rank) / 16); i += blockDim.x) dr[i] = __ldg(sr + i);
     }
     if (threadIdx.x < 96) {
         const int e = threadIdx.x >> 3, f = threadIdx.x & 7;
@@ -727,68 +578,9 @@ __global__ void __launch_bounds__(E3W * 32, 4) k_mc_emit3(const double *__restri
     }
     __syncthreads();
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    E3Warp &S = sw[w];
-    McGrid &g = S.g;
-    const uint32_t *mbase = nullptr;
-    const double *gp = nullptr;
-    int64_t nxy = 0, pstep = 0;
+    McGrid &g = sg[w];
     int cur_grid = -1;
-    // The next live piece's row masks (lanes 0..8) and piece bases (lanes
-    // 0..4) are loaded while the current one is computed and emitted.
-    struct Fetch {
-        uint64_t m;
-        uint32_t mx;
-        int64_t rb;
-        int cy, cz, x0;
-    };
-    auto coords = [&](int64_t gpiece, int &cy, int &cz, int &x0) {
-        const int lp = (int)(gpiece - g.piece_base);  // < 2^31 (checked on the host)
-        const int rr = g.ntx == 1 ? lp : lp / g.ntx;
-        const int xt = lp - rr * g.ntx;
-        int q = g.ncy == 1 ? rr : (int)__umulhi((uint32_t)rr, g.ncy_magic);  // rr / ncy
-        if (q * g.ncy > rr) --q;  // the estimate is exact or one too high
-        cz = q;
-        cy = rr - cz * g.ncy;
-        x0 = xt * MTX;
-    };
-    auto fetch = [&](int64_t gpiece) {
-        Fetch f{0, 0, 0, 0, 0, 0};
-        int cy, cz, x0;
-        coords(gpiece, cy, cz, x0);
-        f.cy = cy;
-        f.cz = cz;
-        f.x0 = x0;
-        if (lane < 9) {
-            const int dy = lane % 3 - 1, dz = lane / 3 - 1;
-            const int my = cy + dy, mz = cz + dz;
-            if (my >= 0 && my < g.ny && mz >= 0 && mz < g.nz) {
-                const uint32_t *mp = mbase + (int64_t)mz * g.pw;
-                const int64_t bb = (int64_t)my * g.nx + x0;
-                if (x0 > 0) {
-                    mask_bits66(mp, bb - 1, f.m, f.mx);
-                } else {
-                    uint64_t m1;
-                    uint32_t h1;
-                    mask_bits66(mp, bb, m1, h1);
-                    f.m = m1 << 1;
-                    f.mx = (uint32_t)(m1 >> 63) | ((h1 & 1u) << 1);
-                }
-            }
-        }
-        if (lane < 5) {  // lanes 0..3: vertex base of row slot r's piece; lane 4: own triangle base
-            const int r = lane & 3;
-            const int dy = -(r & 1), dz = -(r >> 1);
-            if (cy + dy >= 0 && cz + dz >= 0) {
-                const McPieceBase pb = base[gpiece + dy * g.ntx + dz * pstep];
-                f.rb = lane < 4 ? pb.vert : pb.tri;
-            }
-        }
-        return f;
-    };
-    // Persistent warps take batches of 32 consecutive pieces from a global
-    // queue (dense surface patches make batches very unequal; a fixed split
-    // left warps idle while their CTA's slowest warp finished).
-    constexpr int NB = (int)(MCH / 32);  // batches per scan chunk
+    constexpr int NB = (int)(MCH / 32);
     for (;;) {
         unsigned long long bq = 0;
         if (lane == 0) bq = atomicAdd(queue, 1ull);
@@ -799,174 +591,126 @@ __global__ void __launch_bounds__(E3W * 32, 4) k_mc_emit3(const double *__restri
         if (gi != cur_grid) {
             __syncwarp();
             const uint32_t *src = reinterpret_cast<const uint32_t *>(G + gi);
-            uint32_t *dst = reinterpret_cast<uint32_t *>(&S.g);
+            uint32_t *dst = reinterpret_cast<uint32_t *>(&g);
             for (int i = lane; i < (int)(sizeof(McGrid) / 4); i += 32) dst[i] = src[i];
             __syncwarp();
             cur_grid = gi;
-            mbase = mask + g.mask_off;
-            gp = grids + g.goff;
-            nxy = (int64_t)g.nx * g.ny;
-            pstep = (int64_t)g.ncy * g.ntx;
         }
-        const int64_t p0 = c * MCH + (bi - c * NB) * 32;  // global piece index of lane 0
-        const McPieceCnt cur_cnt = cnt[p0 + lane];
-        uint32_t live = __ballot_sync(0xFFFFFFFFu, cur_cnt.tri > 0);
-        if (!live) continue;
-        int src = __ffs(live) - 1;
-        live &= live - 1;
-        Fetch nf = fetch(p0 + src);
-        while (src >= 0) {
-            const Fetch f = nf;
-            const int ptri = __shfl_sync(0xFFFFFFFFu, cur_cnt.tri, src);
-            const int pvert = __shfl_sync(0xFFFFFFFFu, cur_cnt.vert, src);
-            const int cy = f.cy, cz = f.cz, x0 = f.x0;
-            src = live ? __ffs(live) - 1 : -1;
-            live &= live - 1;
-            __syncwarp();  // previous piece's readers of S are done
-            if (lane < 9) {
-                S.m[lane] = f.m;
-                S.h[lane] = f.mx;
-            }
-            if (lane < 5) S.rb[lane] = f.rb;
-            if (src >= 0) nf = fetch(p0 + src);
-            const int64_t rb = f.rb;
-            __syncwarp();
-            const int64_t *rbr = S.rb;  // broadcast reads
-            // ---- codes of the four row slots: lane owns columns c = 1 + 2 lane, 2 + 2 lane.
-            //      Bits c..c+2 of each of the nine row masks, taken once with
-            //      fixed shifts, give both cells' corner pairs.
-            const int cA = 1 + 2 * lane, xA = x0 + 2 * lane;
-            const bool okA = xA < g.ncx, okB = xA + 1 < g.ncx;
-            uint32_t P0[9], P1[9];
+        const int64_t lp0 = (c - g.chunk_base) * MCH + (bi - c * NB) * 32;  // batch's first piece (grid-local)
+        const uint64_t live = lp0 + lane < g.npieces ? __ldg(lmask + g.piece_base + lp0 + lane) : 0ull;
+        const int n = __popcll(live);
+        int incl = n;
 #pragma unroll
-            for (int i = 0; i < 9; ++i) {
-                const uint32_t t = (uint32_t)((S.m[i] >> cA) | ((uint64_t)S.h[i] << (64 - cA)));
-                P0[i] = t & 3u;
-                P1[i] = (t >> 1) & 3u;
-            }
-            auto mk_code = [](uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
-                return (int)(a | pair_swap(b) << 2 | c << 4 | pair_swap(d) << 6);
-            };
-            int own[4][2], ntA = 0, ntB = 0;
+        for (int off = 1; off < 32; off <<= 1) {
+            const int t = __shfl_up_sync(0xFFFFFFFFu, incl, off);
+            if (lane >= off) incl += t;
+        }
+        const int total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+        if (total == 0) continue;
+        const int excl = incl - n;
+        const uint32_t llo = (uint32_t)live, lhi = (uint32_t)(live >> 32);
+        const uint32_t *mbase = mask + g.mask_off;
+        const double *gp = grids + g.goff;
+        const int64_t nxy = (int64_t)g.nx * g.ny;
+        for (int i0 = 0; i0 < total; i0 += 32) {
+            const int i = i0 + lane;
+            int q = 0;  // the lane (piece) holding live cell i: last q with excl_q <= i
 #pragma unroll
-            for (int r = 0; r < 4; ++r) {
-                const int dy = -(r & 1), dz = -(r >> 1);
-                const int i00 = 3 * (dz + 1) + (dy + 1);
-                const bool rowok = cy + dy >= 0 && cz + dz >= 0;
-                const int fyz = (cy + dy == 0 ? 2 : 0) | (cz + dz == 0 ? 4 : 0);
-                const int a = (rowok && okA) ? mk_code(P0[i00], P0[i00 + 1], P0[i00 + 3], P0[i00 + 4]) : 0;
-                const int bcode = (rowok && okB) ? mk_code(P1[i00], P1[i00 + 1], P1[i00 + 3], P1[i00 + 4]) : 0;
-                own[r][0] = s_own[a][fyz | (xA == 0 ? 1 : 0)];
-                own[r][1] = s_own[bcode][fyz];
-                S.code[r][cA] = (uint8_t)a;
-                S.code[r][cA + 1] = (uint8_t)bcode;
-                if (r == 0) {
-                    ntA = s_ntri[a];
-                    ntB = s_ntri[bcode];
+            for (int step = 16; step; step >>= 1) {
+                const int e = __shfl_sync(0xFFFFFFFFu, excl, q + step);
+                if (e <= i) q += step;
+            }
+            const int r = i - __shfl_sync(0xFFFFFFFFu, excl, q);
+            const uint32_t lo = __shfl_sync(0xFFFFFFFFu, llo, q), hi = __shfl_sync(0xFFFFFFFFu, lhi, q);
+            if (i >= total) continue;
+            const int clo = __popc(lo);
+            const int b = r < clo ? (int)__fns(lo, 0, r + 1) : 32 + (int)__fns(hi, 0, r - clo + 1);
+            const int lp = (int)(lp0 + q);
+            const int rr = g.ntx == 1 ? lp : lp / g.ntx;
+            const int xt = lp - rr * g.ntx;
+            int cz = g.ncy == 1 ? rr : (int)__umulhi((uint32_t)rr, g.ncy_magic);
+            if (cz * g.ncy > rr) --cz;
+            const int cy = rr - cz * g.ncy;
+            const int cx = xt * MTX + b;
+            // nine 3-bit windows: bits x-1, x, x+1 of rows (cy + dy, cz + dz), dy, dz in -1..1
+            uint32_t W[9];
+#pragma unroll
+            for (int j = 0; j < 9; ++j) {
+                const int dy = j % 3 - 1, dz = j / 3 - 1;
+                const int y = cy + dy, z = cz + dz;
+                uint32_t wv = 0;
+                if (y >= 0 && z >= 0) {
+                    const uint32_t *mp = mbase + (int64_t)z * g.pw;
+                    const int64_t pos = (int64_t)y * g.nx + cx - (cx > 0 ? 1 : 0);
+                    const uint32_t *wp = mp + (pos >> 5);
+                    wv = __funnelshift_r(__ldg(wp), __ldg(wp + 1), (int)(pos & 31)) & 7u;
+                    if (cx == 0) wv = (wv << 1) & 7u;
                 }
+                W[j] = wv;
             }
-            if (lane < 4) {  // halo cell x0 - 1 of slot r = lane (bits 0, 1 of its masks)
-                const int dy = -(lane & 1), dz = -(lane >> 1);
-                const int i00 = 3 * (dz + 1) + (dy + 1);
-                const bool rowok = cy + dy >= 0 && cz + dz >= 0;
-                const int fyz = (cy + dy == 0 ? 2 : 0) | (cz + dz == 0 ? 4 : 0);
-                const int h = (rowok && x0 > 0) ? mk_code((uint32_t)S.m[i00] & 3u, (uint32_t)S.m[i00 + 1] & 3u,
-                                                          (uint32_t)S.m[i00 + 3] & 3u, (uint32_t)S.m[i00 + 4] & 3u)
-                                                : 0;
-                S.code[lane][0] = (uint8_t)h;
-                S.vb[lane][0] = rb - s_own[h][fyz];
-            }
-            // ---- scans: owned counts of slots (0,1) and (2,3) packed, triangles of slot 0
-            const uint32_t v01 = (uint32_t)(own[0][0] + own[0][1]) | ((uint32_t)(own[1][0] + own[1][1]) << 16);
-            const uint32_t v23 = (uint32_t)(own[2][0] + own[2][1]) | ((uint32_t)(own[3][0] + own[3][1]) << 16);
-            const uint32_t vt = (uint32_t)(ntA + ntB);
-            uint32_t s01 = v01, s23 = v23, st = vt;
+            // Bourke codes of the 8 possible owners (dx, slot r): byte r of ocode[dx]
+            uint32_t ocode[2];
 #pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {
-                const uint32_t a = __shfl_up_sync(0xFFFFFFFFu, s01, off), bq = __shfl_up_sync(0xFFFFFFFFu, s23, off),
-                               cq = __shfl_up_sync(0xFFFFFFFFu, st, off);
-                if (lane >= off) {
-                    s01 += a;
-                    s23 += bq;
-                    st += cq;
+            for (int dx = 0; dx < 2; ++dx) {
+                uint32_t acc = 0;
+#pragma unroll
+                for (int rs = 0; rs < 4; ++rs) {
+                    const int i00 = 3 * (1 - (rs >> 1)) + (1 - (rs & 1));
+                    const uint32_t p0 = (W[i00] >> (1 - dx)) & 3u, p1 = (W[i00 + 1] >> (1 - dx)) & 3u;
+                    const uint32_t p3 = (W[i00 + 3] >> (1 - dx)) & 3u, p4 = (W[i00 + 4] >> (1 - dx)) & 3u;
+                    acc |= (p0 | pair_swap(p1) << 2 | p3 << 4 | pair_swap(p4) << 6) << (8 * rs);
                 }
+                ocode[dx] = acc;
             }
-            s01 -= v01;
-            s23 -= v23;
-            st -= vt;
-            const int64_t rb0 = rbr[0], rb1 = rbr[1], rb2 = rbr[2], rb3 = rbr[3], tbase = rbr[4];
-            {
-                const int e0 = (int)(s01 & 0xFFFFu), e1 = (int)(s01 >> 16), e2 = (int)(s23 & 0xFFFFu),
-                          e3 = (int)(s23 >> 16);
-                S.vb[0][cA] = rb0 + e0;
-                S.vb[0][cA + 1] = rb0 + e0 + own[0][0];
-                S.vb[1][cA] = rb1 + e1;
-                S.vb[1][cA + 1] = rb1 + e1 + own[1][0];
-                S.vb[2][cA] = rb2 + e2;
-                S.vb[2][cA + 1] = rb2 + e2 + own[2][0];
-                S.vb[3][cA] = rb3 + e3;
-                S.vb[3][cA + 1] = rb3 + e3 + own[3][0];
-                const int t0 = (int)st;
-                S.tofs[2 * lane] = t0;
-                S.tofs[2 * lane + 1] = t0 + ntA;
-                S.ex[2 * lane] = e0;  // owned-vertex prefix of the own row
-                S.ex[2 * lane + 1] = e0 + own[0][0];
-            }
-            __syncwarp();
-            // ---- emission in two uniform passes (no divergence between the
-            //      kinds): triangle corners in output order, then owned vertices
-            auto find = [&](const int32_t *pre, int i) {  // last column with pre[col] <= i
-                int col = 0;
-#pragma unroll
-                for (int step = 32; step; step >>= 1)
-                    if (col + step < 64 && pre[col + step] <= i) col += step;
-                return col;
-            };
-            const int64_t tout = 3 * (g.tri_base + tbase);
-            for (int ti = lane; ti < ptri; ti += 32) {  // lane per triangle, its three corners
-                const int col = find(S.tofs, ti);
-                const int cc = col + 1;
-                const int cx = x0 + col;
-                const int code = S.code[0][cc];
-                const int f = bflags(cx, cy, cz);
-                const int8_t *trow = s_tri[code] + 3 * (ti - S.tofs[col]);
+            const int code = (int)(ocode[0] & 0xFFu);
+            const int f = bflags(cx, cy, cz);
+            const int64_t pg = g.piece_base + lp;
+            const uint4 *np = tnib + 2 * pg;
+            const McPieceBase pb = base[pg];
+            const int64_t vbase = pb.vert + vpre[64 * pg + b];
+            const int64_t tofs = pb.tri + nib_prefix(np[0], np[1], b);
+            const int nt = (int)T->ntri[code];
+            int32_t *to = tris + 3 * (g.tri_base + tofs);
+            const int pstep = g.ncy * g.ntx;  // pieces per cell plane (< 2^31)
+            for (int t = 0; t < nt; ++t) {
                 int32_t out3[3];
 #pragma unroll
-                for (int q = 0; q < 3; ++q) {
-                    const int info = s_cinfo[trow[q]][f];
-                    const int dx = info & 1, r = (info >> 1) & 3, e2 = info >> 3;
-                    const int ocode = S.code[r][cc - dx];
-                    const int of = bflags(cx - dx, cy - (r & 1), cz - (r >> 1));
-                    const int64_t vid = S.vb[r][cc - dx] + __ldg(&T->rank[ocode][of][e2]);
-                    out3[q] = (int32_t)(g.vert_base + vid);
+                for (int qq = 0; qq < 3; ++qq) {
+                    // owner cell (the cell itself when info & 7 == 0): its piece's
+                    // vertex base + its prefix inside the piece + the edge's rank
+                    const int info = s_cinfo[s_tri[code][3 * t + qq]][f];
+                    const int dx = info & 1, rs = (info >> 1) & 3, e2 = info >> 3;
+                    const int ox = cx - dx, oy = cy - (rs & 1), oz = cz - (rs >> 1);
+                    const int oc = (int)((ocode[dx] >> (8 * rs)) & 0xFFu);
+                    const int64_t op = pg - (rs & 1) * g.ntx - (rs >> 1) * pstep - ((dx & (b == 0)) ? 1 : 0);
+                    const int64_t vid = __ldg(&base[op].vert) + __ldg(vpre + 64 * op + (ox & 63)) +
+                                        s_rank[oc][bflags(ox, oy, oz)][e2];
+                    out3[qq] = (int32_t)(g.vert_base + vid);
                 }
-                int32_t *o = tris + tout + 3 * (int64_t)ti;
-                o[0] = out3[0];
-                o[1] = out3[1];
-                o[2] = out3[2];
+                to[3 * t] = out3[0];
+                to[3 * t + 1] = out3[1];
+                to[3 * t + 2] = out3[2];
             }
-            for (int j = lane; j < pvert; j += 32) {
-                const int col = find(S.ex, j);
-                const int rk = j - S.ex[col];
-                const int cc = col + 1;
-                const int cx = x0 + col;
-                const int code = S.code[0][cc];
-                const int vi = s_vinfo[__ldg(&T->inv[code][bflags(cx, cy, cz)][rk])];
+            const int nown = (int)T->owncnt[code][f];
+            for (int rk = 0; rk < nown; ++rk) {
+                const int vi = s_vinfo[__ldg(&T->inv[code][f][rk])];
                 const int a = vi & 3, lx = (vi >> 2) & 1, ly = (vi >> 3) & 1, lz = (vi >> 4) & 1;
                 const double *sp = gp + (int64_t)(cz + lz) * nxy + (int64_t)(cy + ly) * g.nx + (cx + lx);
                 const double s0 = __ldg(sp);
                 const double s1 = __ldg(sp + (a == 0 ? 1 : (a == 1 ? (int64_t)g.nx : nxy)));
                 const double den = __dadd_rn(s1, -s0);
-                const double t = den == 0.0 ? 0.0 : __ddiv_rn(__dadd_rn(k, -s0), den);
-                double lat[3] = {(double)(cx + lx), (double)(cy + ly), (double)(cz + lz + g.zoff)};
-                lat[a] = __dadd_rn(lat[a], t);
-                const int64_t vid = g.vert_base + S.vb[0][cc] + rk;
+                const double tt = den == 0.0 ? 0.0 : __ddiv_rn(__dadd_rn(k, -s0), den);
+                double lx_ = (double)(cx + lx), ly_ = (double)(cy + ly), lz_ = (double)(cz + lz + g.zoff);
+                if (a == 0) lx_ = __dadd_rn(lx_, tt);
+                else if (a == 1) ly_ = __dadd_rn(ly_, tt);
+                else lz_ = __dadd_rn(lz_, tt);
+                const int64_t vid = g.vert_base + vbase + rk;
                 double *o = verts + 3 * vid;
-                if (vedge)  // canonical edge of the vertex, grid-local: ((z * ny + y) * nx + x) * 3 + axis
+                if (vedge)
                     vedge[vid] = (((int64_t)(cz + lz) * g.ny + (cy + ly)) * g.nx + (cx + lx)) * 3 + a;
-                o[0] = world(g.origin[0], lat[0], g.spacing[0]);
-                o[1] = world(g.origin[1], lat[1], g.spacing[1]);
-                o[2] = world(g.origin[2], lat[2], g.spacing[2]);
+                o[0] = world(g.origin[0], lx_, g.spacing[0]);
+                o[1] = world(g.origin[1], ly_, g.spacing[1]);
+                o[2] = world(g.origin[2], lz_, g.spacing[2]);
             }
         }
     }
@@ -997,6 +741,9 @@ struct McPlan {
     McGrid *d_grids;
     McPieceCnt *cnt;
     McPieceBase *chunk, *base;
+    uint64_t *lmask;  // live cells of every piece (k_mc_count4)
+    uint4 *tnib;      // per live piece: 4-bit triangle counts of its cells (2 x 16 B)
+    uint16_t *vpre;   // per live piece: owned vertices of the piece's cells before each live cell
     int64_t *totals;
     int32_t *item_grid, *chunk_grid, *mask_grid;
     uint32_t *mask;
@@ -1058,7 +805,7 @@ static int mc_num_sms() {
     return n_sm[dev];
 }
 
-// two zeroed counters after the piece counts: [0] k_mc_emit3's batch queue, [1] k_mc_count3's
+// two zeroed counters after the piece counts: [0] k_mc_emit4's batch queue, [1] k_mc_count4's
 static unsigned long long *mc_queue(const McPlan &pl) {
     return reinterpret_cast<unsigned long long *>(pl.cnt + pl.npieces);
 }
@@ -1069,6 +816,9 @@ static void mc_carve(McPlan &pl, void *base, size_t cap) {
     pl.cnt = c.take<McPieceCnt>(pl.npieces + 2);  // + the two batch queues (mc_queue)
     pl.chunk = c.take<McPieceBase>(pl.nchunks);
     pl.base = c.take<McPieceBase>(pl.npieces);
+    pl.lmask = c.take<uint64_t>(pl.npieces);
+    pl.tnib = c.take<uint4>(2 * pl.npieces);
+    pl.vpre = c.take<uint16_t>(64 * pl.npieces);
     pl.totals = c.take<int64_t>(2);
     pl.item_grid = c.take<int32_t>(pl.nitems + 1);
     pl.chunk_grid = c.take<int32_t>(pl.nchunks + 1);
@@ -1153,7 +903,7 @@ static int mc_count_impl(const double *d_grids, const chr_mc_grid_t *h, int64_t 
         CHR_PROF("k_mc_count4", st);
         const int64_t nbatch = pl.nchunks * (MCH / 32);
         k_mc_count4<<<(unsigned)std::min<int64_t>(ceil_div(nbatch, 8), (int64_t)mc_num_sms() * 8), 256, 0, st>>>(
-            pl.d_grids, pl.chunk_grid, T, masks, pl.cnt, mc_queue(pl) + 1, nbatch);
+            pl.d_grids, pl.chunk_grid, T, masks, pl.cnt, pl.lmask, pl.tnib, pl.vpre, mc_queue(pl) + 1, nbatch);
     }
     {
         CHR_PROF("k_mc_reduce", st);
@@ -1215,11 +965,11 @@ static int mc_emit_impl(const double *d_grids, const chr_mc_grid_t *h, int64_t n
     if (!T) return CHR_E_CUDA;
     if (pl.nchunks > 0) {
         const int64_t nbatch = pl.nchunks * (MCH / 32);
-        const int64_t ctas = std::min<int64_t>(ceil_div(nbatch, E3W), (int64_t)mc_num_sms() * 4);
-        CHR_PROF("k_mc_emit3", st);
-        k_mc_emit3<<<(unsigned)ctas, E3W * 32, 0, st>>>(d_grids, pl.d_grids, pl.chunk_grid, k, T, pl.base, pl.cnt,
-                                                        d_masks ? d_masks : pl.mask, mc_queue(pl), nbatch, d_verts,
-                                                        d_tris, d_vedge);
+        const int64_t ctas = std::min<int64_t>(ceil_div(nbatch, E4W), (int64_t)mc_num_sms() * 6);
+        CHR_PROF("k_mc_emit4", st);
+        k_mc_emit4<<<(unsigned)ctas, E4W * 32, 0, st>>>(d_grids, pl.d_grids, pl.chunk_grid, k, T, pl.base, pl.lmask,
+                                                        pl.tnib, pl.vpre, d_masks ? d_masks : pl.mask, mc_queue(pl), nbatch,
+                                                        d_verts, d_tris, d_vedge);
     }
     CHR_CUDA_TRY(cudaGetLastError());
     CHR_CUDA_TRY(stream_sync(st));
