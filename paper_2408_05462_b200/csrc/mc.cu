@@ -428,7 +428,7 @@ __global__ void __launch_bounds__(256) k_mc_count4(const McGrid *__restrict__ G,
                                                    const McTables *__restrict__ T,
                                                    const uint32_t *__restrict__ mask,
                                                    McPieceCnt *__restrict__ cnt, uint64_t *__restrict__ lmask,
-                                                   uint4 *__restrict__ tnib, uint16_t *__restrict__ vpre,
+                                                   uint32_t *__restrict__ cellw,
                                                    unsigned long long *__restrict__ queue, int64_t nbatch) {
     __shared__ __align__(16) uint8_t s_ntri[256];
     __shared__ __align__(16) uint8_t s_own[256][8];
@@ -481,73 +481,42 @@ __global__ void __launch_bounds__(256) k_mc_count4(const McGrid *__restrict__ G,
         uint64_t live = live0;
         int t = 0, v = 0;
         const int fyz = (cy == 0 ? 2 : 0) | (cz == 0 ? 4 : 0);
-        uint64_t tn0 = 0, tn1 = 0, tn2 = 0, tn3 = 0;
         const int64_t gp = g.piece_base + lp;
-        uint16_t *vp = vpre + 64 * gp;
+        uint32_t *cw = cellw + 64 * gp;
         while (live) {
             const int cc = __ffsll((long long)live) - 1;
             live &= live - 1;
             const int code = code_fast(m[0], h[0], m[1], h[1], m[2], h[2], m[3], h[3], cc);
             const uint32_t nt = s_ntri[code], no = s_own[code][fyz | (x0 + cc == 0 ? 1 : 0)];
-            vp[cc] = (uint16_t)v;  // owned vertices of the piece's earlier cells
+            // the cell's word: owned vertices (<= 516) and triangles (<= 320) of
+            // the piece's earlier cells, and its code
+            cw[cc] = (uint32_t)v | ((uint32_t)t << 10) | ((uint32_t)code << 19);
             t += nt;
             v += no;
-            const int sh = 4 * (cc & 15), q = cc >> 4;
-            const uint64_t tb = (uint64_t)nt << sh;
-            tn0 |= q == 0 ? tb : 0;
-            tn1 |= q == 1 ? tb : 0;
-            tn2 |= q == 2 ? tb : 0;
-            tn3 |= q == 3 ? tb : 0;
         }
         McPieceCnt out;
         out.tri = t;
         out.vert = v;
         cnt[gp] = out;
         lmask[gp] = live0;
-        if (live0) {  // per-cell triangle counts, 4 bits each (k_mc_emit4's triangle offsets)
-            uint4 *np = tnib + 2 * gp;
-            np[0] = make_uint4((uint32_t)tn0, (uint32_t)(tn0 >> 32), (uint32_t)tn1, (uint32_t)(tn1 >> 32));
-            np[1] = make_uint4((uint32_t)tn2, (uint32_t)(tn2 >> 32), (uint32_t)tn3, (uint32_t)(tn3 >> 32));
-        }
     }
-}
-
-// Sum of the 4-bit fields of the four words below field b (b in 0..63).
-__device__ __forceinline__ uint32_t nib_prefix(uint4 A, uint4 B, int b) {
-    const int q = b >> 4;
-    const uint64_t part = (1ull << (4 * (b & 15))) - 1;
-    uint64_t w0 = (uint64_t)A.x | ((uint64_t)A.y << 32), w1 = (uint64_t)A.z | ((uint64_t)A.w << 32);
-    uint64_t w2 = (uint64_t)B.x | ((uint64_t)B.y << 32), w3 = (uint64_t)B.z | ((uint64_t)B.w << 32);
-    w0 = q > 0 ? w0 : (q == 0 ? w0 & part : 0);
-    w1 = q > 1 ? w1 : (q == 1 ? w1 & part : 0);
-    w2 = q > 2 ? w2 : (q == 2 ? w2 & part : 0);
-    w3 = q == 3 ? w3 & part : 0;
-    constexpr uint64_t N4 = 0x0F0F0F0F0F0F0F0Full, B8 = 0x00FF00FF00FF00FFull;
-    auto bytes = [](uint64_t x) { return (x & N4) + ((x >> 4) & N4); };  // 8 bytes <= 24 each
-    uint64_t y = bytes(w0) + bytes(w1) + bytes(w2) + bytes(w3);       // bytes <= 96
-    y = (y & B8) + ((y >> 8) & B8);                                   // 4 halves <= 192
-    return (uint32_t)((y * 0x0001000100010001ull) >> 48);
 }
 
 // emit v4: a LANE per LIVE CELL.  A warp takes 32 consecutive pieces of a
 // batch, scans their live-cell counts (k_mc_count4's live masks) and deals
 // the batch's live cells to its lanes 32 at a time, so every lane does one
-// cell's work whatever the pieces' densities.  A cell's vertex base is its
-// piece's base + the 4-bit owned-vertex counts of the cells before it in
-// the piece (k_mc_count4's per-piece fields, a SWAR sum); the same holds for
-// its triangle offset and for any owner cell, so a triangle corner costs
-// the owner's code (from nine 3-bit row windows around the cell), its piece
-// base and fields, and one rank lookup -- no per-piece code arrays, no
-// warp-wide scans over the piece's 64 cells.
+// cell's work whatever the pieces' densities.  k_mc_count4 left one word per
+// live cell (code, owned vertices and triangles of the piece's earlier
+// cells), so a cell's triangle offset and vertex base are its piece's bases
+// + its word, and a triangle corner owned by another cell costs that cell's
+// word and its piece's vertex base (two loads) + one rank lookup.
 constexpr int E4W = 8;  // warps per CTA
 __global__ void __launch_bounds__(E4W * 32) k_mc_emit4(const double *__restrict__ grids, const McGrid *__restrict__ G,
                                                        const int32_t *__restrict__ chunk_grid, double k,
                                                        const McTables *__restrict__ T,
                                                        const McPieceBase *__restrict__ base,
                                                        const uint64_t *__restrict__ lmask,
-                                                       const uint4 *__restrict__ tnib,
-                                                       const uint16_t *__restrict__ vpre,
-                                                       const uint32_t *__restrict__ mask,
+                                                       const uint32_t *__restrict__ cellw,
                                                        unsigned long long *__restrict__ queue, int64_t nbatch,
                                                        double *__restrict__ verts, int32_t *__restrict__ tris,
                                                        int64_t *__restrict__ vedge) {
@@ -609,7 +578,6 @@ __global__ void __launch_bounds__(E4W * 32) k_mc_emit4(const double *__restrict_
         if (total == 0) continue;
         const int excl = incl - n;
         const uint32_t llo = (uint32_t)live, lhi = (uint32_t)(live >> 32);
-        const uint32_t *mbase = mask + g.mask_off;
         const double *gp = grids + g.goff;
         const int64_t nxy = (int64_t)g.nx * g.ny;
         for (int i0 = 0; i0 < total; i0 += 32) {
@@ -632,43 +600,13 @@ __global__ void __launch_bounds__(E4W * 32) k_mc_emit4(const double *__restrict_
             if (cz * g.ncy > rr) --cz;
             const int cy = rr - cz * g.ncy;
             const int cx = xt * MTX + b;
-            // nine 3-bit windows: bits x-1, x, x+1 of rows (cy + dy, cz + dz), dy, dz in -1..1
-            uint32_t W[9];
-#pragma unroll
-            for (int j = 0; j < 9; ++j) {
-                const int dy = j % 3 - 1, dz = j / 3 - 1;
-                const int y = cy + dy, z = cz + dz;
-                uint32_t wv = 0;
-                if (y >= 0 && z >= 0) {
-                    const uint32_t *mp = mbase + (int64_t)z * g.pw;
-                    const int64_t pos = (int64_t)y * g.nx + cx - (cx > 0 ? 1 : 0);
-                    const uint32_t *wp = mp + (pos >> 5);
-                    wv = __funnelshift_r(__ldg(wp), __ldg(wp + 1), (int)(pos & 31)) & 7u;
-                    if (cx == 0) wv = (wv << 1) & 7u;
-                }
-                W[j] = wv;
-            }
-            // Bourke codes of the 8 possible owners (dx, slot r): byte r of ocode[dx]
-            uint32_t ocode[2];
-#pragma unroll
-            for (int dx = 0; dx < 2; ++dx) {
-                uint32_t acc = 0;
-#pragma unroll
-                for (int rs = 0; rs < 4; ++rs) {
-                    const int i00 = 3 * (1 - (rs >> 1)) + (1 - (rs & 1));
-                    const uint32_t p0 = (W[i00] >> (1 - dx)) & 3u, p1 = (W[i00 + 1] >> (1 - dx)) & 3u;
-                    const uint32_t p3 = (W[i00 + 3] >> (1 - dx)) & 3u, p4 = (W[i00 + 4] >> (1 - dx)) & 3u;
-                    acc |= (p0 | pair_swap(p1) << 2 | p3 << 4 | pair_swap(p4) << 6) << (8 * rs);
-                }
-                ocode[dx] = acc;
-            }
-            const int code = (int)(ocode[0] & 0xFFu);
             const int f = bflags(cx, cy, cz);
             const int64_t pg = g.piece_base + lp;
-            const uint4 *np = tnib + 2 * pg;
             const McPieceBase pb = base[pg];
-            const int64_t vbase = pb.vert + vpre[64 * pg + b];
-            const int64_t tofs = pb.tri + nib_prefix(np[0], np[1], b);
+            const uint32_t cwd = __ldg(cellw + 64 * pg + b);
+            const int code = (int)(cwd >> 19);
+            const int64_t vbase = pb.vert + (cwd & 1023u);
+            const int64_t tofs = pb.tri + ((cwd >> 10) & 511u);
             const int nt = (int)T->ntri[code];
             int32_t *to = tris + 3 * (g.tri_base + tofs);
             const int pstep = g.ncy * g.ntx;  // pieces per cell plane (< 2^31)
@@ -681,10 +619,9 @@ __global__ void __launch_bounds__(E4W * 32) k_mc_emit4(const double *__restrict_
                     const int info = s_cinfo[s_tri[code][3 * t + qq]][f];
                     const int dx = info & 1, rs = (info >> 1) & 3, e2 = info >> 3;
                     const int ox = cx - dx, oy = cy - (rs & 1), oz = cz - (rs >> 1);
-                    const int oc = (int)((ocode[dx] >> (8 * rs)) & 0xFFu);
                     const int64_t op = pg - (rs & 1) * g.ntx - (rs >> 1) * pstep - ((dx & (b == 0)) ? 1 : 0);
-                    const int64_t vid = __ldg(&base[op].vert) + __ldg(vpre + 64 * op + (ox & 63)) +
-                                        s_rank[oc][bflags(ox, oy, oz)][e2];
+                    const uint32_t ow = __ldg(cellw + 64 * op + (ox & 63));
+                    const int64_t vid = __ldg(&base[op].vert) + (ow & 1023u) + s_rank[ow >> 19][bflags(ox, oy, oz)][e2];
                     out3[qq] = (int32_t)(g.vert_base + vid);
                 }
                 to[3 * t] = out3[0];
@@ -742,8 +679,7 @@ struct McPlan {
     McPieceCnt *cnt;
     McPieceBase *chunk, *base;
     uint64_t *lmask;  // live cells of every piece (k_mc_count4)
-    uint4 *tnib;      // per live piece: 4-bit triangle counts of its cells (2 x 16 B)
-    uint16_t *vpre;   // per live piece: owned vertices of the piece's cells before each live cell
+    uint32_t *cellw;  // per live cell of a live piece: vertex / triangle prefix in the piece + code
     int64_t *totals;
     int32_t *item_grid, *chunk_grid, *mask_grid;
     uint32_t *mask;
@@ -817,8 +753,7 @@ static void mc_carve(McPlan &pl, void *base, size_t cap) {
     pl.chunk = c.take<McPieceBase>(pl.nchunks);
     pl.base = c.take<McPieceBase>(pl.npieces);
     pl.lmask = c.take<uint64_t>(pl.npieces);
-    pl.tnib = c.take<uint4>(2 * pl.npieces);
-    pl.vpre = c.take<uint16_t>(64 * pl.npieces);
+    pl.cellw = c.take<uint32_t>(64 * pl.npieces);
     pl.totals = c.take<int64_t>(2);
     pl.item_grid = c.take<int32_t>(pl.nitems + 1);
     pl.chunk_grid = c.take<int32_t>(pl.nchunks + 1);
@@ -903,7 +838,7 @@ static int mc_count_impl(const double *d_grids, const chr_mc_grid_t *h, int64_t 
         CHR_PROF("k_mc_count4", st);
         const int64_t nbatch = pl.nchunks * (MCH / 32);
         k_mc_count4<<<(unsigned)std::min<int64_t>(ceil_div(nbatch, 8), (int64_t)mc_num_sms() * 8), 256, 0, st>>>(
-            pl.d_grids, pl.chunk_grid, T, masks, pl.cnt, pl.lmask, pl.tnib, pl.vpre, mc_queue(pl) + 1, nbatch);
+            pl.d_grids, pl.chunk_grid, T, masks, pl.cnt, pl.lmask, pl.cellw, mc_queue(pl) + 1, nbatch);
     }
     {
         CHR_PROF("k_mc_reduce", st);
@@ -968,7 +903,7 @@ static int mc_emit_impl(const double *d_grids, const chr_mc_grid_t *h, int64_t n
         const int64_t ctas = std::min<int64_t>(ceil_div(nbatch, E4W), (int64_t)mc_num_sms() * 6);
         CHR_PROF("k_mc_emit4", st);
         k_mc_emit4<<<(unsigned)ctas, E4W * 32, 0, st>>>(d_grids, pl.d_grids, pl.chunk_grid, k, T, pl.base, pl.lmask,
-                                                        pl.tnib, pl.vpre, d_masks ? d_masks : pl.mask, mc_queue(pl), nbatch,
+                                                        pl.cellw, mc_queue(pl), nbatch,
                                                         d_verts, d_tris, d_vedge);
     }
     CHR_CUDA_TRY(cudaGetLastError());

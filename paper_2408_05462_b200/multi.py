@@ -21,6 +21,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -117,6 +118,7 @@ def build_archive_slab(vol_local: torch.Tensor, dims, slab: Slab, cands, bs, *, 
         bst, bad = D.stats(view, (nx, ny, slab.nz_stats), bs, cands)
         pack[: nb_mine * 3] = bst.reshape(-1)
         pack[-1] = bad.to(torch.float64)[0]
+    _dbg("stats_local", pack)
     parts = _allgather(pack)
     stats, vmin, vmax = [], math.inf, -math.inf
     for r, p in enumerate(parts):
@@ -411,6 +413,20 @@ def _allgather_var(t: torch.Tensor, sizes: list[int]) -> list[torch.Tensor]:
     return [o[:n].to(t.device) for o, n in zip(out, sizes)]
 
 
+DEBUG_SUMS: dict = {}  # stage -> checksum (CHR_SLAB_DEBUG=1; stress tests)
+
+
+def _dbg(name, t):
+    if os.environ.get("CHR_SLAB_DEBUG") == "1":
+        torch.cuda.synchronize()
+        x = t.reshape(-1)
+        if x.dtype == torch.float64:
+            x = x.view(torch.int64)
+        elif x.dtype == torch.float32:
+            x = x.view(torch.int32)
+        DEBUG_SUMS[name] = int(x.to(torch.int64).sum())
+
+
 def _ticker():
     """CHR_SLAB_TIMES=1: host time of each phase of request_extract_portions (stderr)."""
     import os
@@ -638,6 +654,7 @@ def request_extract_portions(res: D.Compressed, k_index: int, k: float, spacing=
     sblob = torch.zeros(at + 16, dtype=torch.uint8, device=dev)
     xb = torch.from_numpy(extra if len(extra) else np.zeros(1, np.uint8)).to(dev)
     _copy_segments(sblob, blob, xb, segs, 1, ws)
+    _dbg("sblob", sblob)
 
     _tick("# ---- decode (e = 1/2")
     # ---- decode (e = 1/2 for Lorenzo portions: u_local exact)
@@ -656,6 +673,7 @@ def request_extract_portions(res: D.Compressed, k_index: int, k: float, spacing=
         _, _, status = D.decode(sblob, tab, ws=ws, out=windows)
         if any(status):
             raise ParameterError(f"portion decode failed: {list(status)}")
+        _dbg("decoded", windows)
 
     _tick("# ---- z-carries:")
     # ---- z-carries: all-gather of every Lorenzo portion's last-plane u_local
@@ -690,7 +708,9 @@ def request_extract_portions(res: D.Compressed, k_index: int, k: float, spacing=
                 add.append((c_at, loc_in[key], int(pl[q]), 0))
         c_at += int(pl[q])
     carry = torch.zeros(max(c_at, 1), dtype=torch.int64, device=dev)
+    _dbg("gath", gath)
     _copy_segments(carry, gath, None, np.asarray(add, dtype=np.uint64).reshape(-1, 4), 8, ws)
+    _dbg("carry", carry)
     if len(lj):
         cols = (own_off[lj].astype(np.uint64), pl[lj].astype(np.int64), nzp[lj].astype(np.int64),
                 c_off[lj].astype(np.int64), ebound[J][lj].astype(np.float64))  # alive across the call
@@ -710,6 +730,7 @@ def request_extract_portions(res: D.Compressed, k_index: int, k: float, spacing=
         dst = windows[int(own_off[q]): int(own_off[q]) + n0]
         dst[bits] = vals
 
+    _dbg("finished", windows)
     _tick("# ---- halo planes:")
     # ---- halo planes: all-gather of every non-final portion's last plane
     def top_planes(r):
@@ -732,6 +753,7 @@ def request_extract_portions(res: D.Compressed, k_index: int, k: float, spacing=
         tb = np.asarray([(woff[q] * 8, where[int(J[q])] * 8, pl[q] * 8, 0) for q in hq], dtype=np.uint64)
         _copy_segments(windows, tops[rank - 1], None, tb, 1, ws)
 
+    _dbg("halo", windows)
     _tick("# ---- marching cubes of each ")
     # ---- marching cubes of each portion's cells (halo plane first)
     gzm = nzp + halo
@@ -747,6 +769,8 @@ def request_extract_portions(res: D.Compressed, k_index: int, k: float, spacing=
         mct["zoff"] = (pa[gq] - oz[J[gq]] - halo[gq]).astype(np.int32)
         verts, tris, nt_l, nv_l, vedge = D.marching(windows, mct, k, ws=ws, edges=True)
         nt_g, nv_g = np.asarray(nt_l, np.int64), np.asarray(nv_l, np.int64)
+        _dbg("tris", tris)
+        _dbg("verts", verts)
     ng = len(gq)
     _tick("# renumbering")
     # renumbering: drop the halo-plane x/y vertices (first touched by the

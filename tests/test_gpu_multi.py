@@ -146,7 +146,18 @@ def test_slab_request_extract_matches_single_gpu(tmp_path, world):
     assert ok == "1"
 
 
-def _portion_worker(rank, world, port, case, out_path):
+def _c4_field():
+    """BASELINE c4 recipe (GRF k^-11/3 in [0,1], bs32, r=1e-4, k=0.5) at 96^3,
+    generated ONCE by the test process and handed to every rank (torch's CPU
+    FFT under three competing processes is not bit-reproducible, so ranks
+    generating it themselves could disagree about the input)."""
+    from paper_2408_05462_b200 import synth
+
+    v, dims, bs, cands, r = synth.make_config("c4", device="cpu", n=96)
+    return v.numpy().copy(), dims, bs, float(cands[0]), r
+
+
+def _portion_worker(rank, world, port, case, out_path, c4=None):
     """z-slab compress, then the per-portion request + marching cubes
     (request_extract_portions: no payload bytes leave their rank); rank 0
     reassembles the merged mesh from every rank's rows and compares it with
@@ -158,12 +169,10 @@ def _portion_worker(rank, world, port, case, out_path):
 
     dist.init_process_group("gloo", rank=rank, world_size=world)
     torch.cuda.set_device(0)
-    from paper_2408_05462_b200 import multi, synth
+    from paper_2408_05462_b200 import multi
 
-    if case == "c4":  # BASELINE c4 recipe (GRF k^-11/3 in [0,1], bs32, r=1e-4, k=0.5) at 96^3
-        v, dims, bs, cands, r = synth.make_config("c4", device="cpu", n=96)
-        flat = v.numpy()
-        k = cands[0]
+    if case == "c4":
+        flat, dims, bs, k, r = c4
     else:
         dims, bs, flat = _field(case)
         r = 1e-3
@@ -205,7 +214,8 @@ def _portion_worker(rank, world, port, case, out_path):
 @pytest.mark.parametrize("case", ["grf", "outliers", "c4"])
 def test_slab_portion_request_matches_oracle(tmp_path, world, case):
     out = str(tmp_path / "mesh.txt")
-    mp.spawn(_portion_worker, args=(world, _free_port(), case, out), nprocs=world, join=True)
+    c4 = _c4_field() if case == "c4" else None
+    mp.spawn(_portion_worker, args=(world, _free_port(), case, out, c4), nprocs=world, join=True)
     ok, nt, ntr, nv, nvr, codecs = open(out).read().split()
     assert int(ntr) > 0 and (nt, nv) == (ntr, nvr)
     if case == "outliers":
