@@ -1049,11 +1049,10 @@ __device__ __forceinline__ int64_t win24_count(const Win24 &W) {
 // own positions: H holds the LEB128 payload of bytes e-4..e, so the token
 // ending at e has value H >> 7 (5 - len).  Only for positions below -2^30
 // (a segment starting deep inside a zero run) or a 5-byte token in the
-// warp.  A literal too wide for int32 (never from a valid encoder) adds 2^31
-// to asum, which sends its region to the generic int64 path.
+// warp, in the int64 pass (the int32 pass sends such regions there).
 template <bool PAD, typename QV>
 __device__ __forceinline__ int64_t band_scatter_unit64(const Win24 &W, int64_t at64, int L, int ex, uint64_t M,
-                                                     QV *__restrict__ q, uint64_t &asum) {
+                                                     QV *__restrict__ q) {
     int64_t at = at64;
     int idx = (int)at, x = 0;
     if (PAD && at >= 0) {
@@ -1076,7 +1075,6 @@ __device__ __forceinline__ int64_t band_scatter_unit64(const Win24 &W, int64_t a
             const uint64_t zz = v - 1;
             if ((uint64_t)at < (uint64_t)L) {
                 q[idx] = (QV)((int64_t)(zz >> 1) ^ -(int64_t)(zz & 1));
-                asum += (zz >> 1) + (zz & 1);
             }
             ++at;
             ++idx;
@@ -1099,12 +1097,11 @@ __device__ __forceinline__ int64_t band_scatter_unit64(const Win24 &W, int64_t a
 
 // 32-bit path: tokens <= 4 bytes (H = payload of bytes e-3..e in 28 bits),
 // positions in int32 (clamped to 2^30 past L: every position that matters
-// is < L <= BCAP and a segment starts at -skip >= -2^30).  Stored literals
-// add |q| to asum (the region's sum |q| bounds |u|: int32 tiles are exact
-// when it stays below 2^31).  Returns the position after the unit's tokens.
+// is < L <= BCAP and a segment starts at -skip >= -2^30).  Returns the
+// position after the unit's tokens.
 template <bool PAD, typename QV>
 __device__ __forceinline__ int band_scatter_unit32(const Win24 &W, int at, int L, int ex, uint64_t M,
-                                                   QV *__restrict__ q, uint64_t &asum) {
+                                                   QV *__restrict__ q, uint32_t &asum) {
     uint32_t H = 0;
 #pragma unroll
     for (int j = 4; j < 8; ++j) H = (H >> 7) | ((win_byte(W, j) & 0x7Fu) << 21);
@@ -1119,7 +1116,7 @@ __device__ __forceinline__ int band_scatter_unit32(const Win24 &W, int at, int L
             const uint32_t zz = v - 1u;
             const int idx = PAD ? at + (int)(((uint64_t)(unsigned)at * M) >> 32) : at;
             q[idx] = (QV)(int32_t)((zz >> 1) ^ (0u - (zz & 1u)));
-            asum += (zz >> 1) + (zz & 1u);
+            asum += v >> 1;  // |q| (v = zigzag + 1)
         }
         // positions past L only need to stay past L: clamping at 2^30 keeps
         // at + v (< 2^28 here) inside int32
@@ -1128,16 +1125,30 @@ __device__ __forceinline__ int band_scatter_unit32(const Win24 &W, int at, int L
     return at;
 }
 
+// QV = int64_t: tokens of any width.  QV = int32_t (the fast pass): a unit
+// with a 5-byte token or a position below -2^30 in the warp flags its region
+// for the int64 pass (`wide_out`) and is skipped; otherwise the stored
+// literals' |q| add to `asum` (<= 2^31 over a 64-byte group: at most 2^25
+// per byte).
 template <bool PAD, typename QV>
 __device__ __forceinline__ int64_t band_scatter_unit(const Win24 &W, int64_t at, int L, int ex, uint64_t M,
-                                                     QV *__restrict__ q, bool active, uint64_t &asum) {
+                                                     QV *__restrict__ q, bool active, uint32_t &asum,
+                                                     bool &wide_out) {
     const uint32_t C = ~W.E & 0xFFFFFFu;
     const bool long5 = active && ((C << 1) & (C << 2) & (C << 3) & (C << 4) & (W.lit | W.len)) != 0;
     const bool wide = active && (long5 || at < -(1ll << 30));
-    if (__any_sync(0xFFFFFFFFu, wide)) {
-        return active ? band_scatter_unit64<PAD, QV>(W, at, L, ex, M, q, asum) : at;
+    if (sizeof(QV) == 4) {
+        if (__any_sync(0xFFFFFFFFu, wide)) {
+            wide_out |= wide;
+            return at;  // the region is decoded again by the int64 pass
+        }
+        return active ? (int64_t)band_scatter_unit32<PAD, QV>(W, (int)at, L, ex, M, q, asum) : at;
     }
-    return active ? (int64_t)band_scatter_unit32<PAD, QV>(W, (int)at, L, ex, M, q, asum) : at;
+    uint32_t unused = 0;
+    if (__any_sync(0xFFFFFFFFu, wide)) {
+        return active ? band_scatter_unit64<PAD, QV>(W, at, L, ex, M, q) : at;
+    }
+    return active ? (int64_t)band_scatter_unit32<PAD, QV>(W, (int)at, L, ex, M, q, unused) : at;
 }
 
 // QV = int32_t: the fast pass (checks the tile's sum |q|); QV = int64_t: the
@@ -1225,8 +1236,9 @@ __global__ void __launch_bounds__(256) k_band(const DecReg *__restrict__ regs, c
     const int U = s_base[nzv];
     const uint64_t M = ((1ull << 32) + (uint64_t)ex - 1) / (uint64_t)ex;  // row = (at * M) >> 32
     const int64_t gbase = R.chunk_base * DTHREADS;  // pos64 index of the region's first group
+    bool wide = false;  // a token the int32 pass does not take (5 bytes / deep negative start)
     for (int g0 = warp * 32; g0 < U; g0 += 256) {  // warp-uniform bounds (the unit walk votes)
-        uint64_t asum = 0;  // sum |q| of the literals this thread stores (segment j)
+        uint32_t asum = 0;  // sum |q| of the literals this thread stores (segment j; <= 2^31)
         const int gi = g0 + lane;
         const bool own = gi < U;
         int j = 0;
@@ -1246,11 +1258,22 @@ __global__ void __launch_bounds__(256) k_band(const DecReg *__restrict__ regs, c
             if (!__any_sync(0xFFFFFFFFu, act)) continue;
             Win24 W;
             if (act) W = win24(blob, u0, s_lo[j], s_hi[j]);
-            at = rs == ex ? band_scatter_unit<false, QV>(W, at, L, ex, M, q, act, asum)
-                          : band_scatter_unit<true, QV>(W, at, L, ex, M, q, act, asum);
+            at = rs == ex ? band_scatter_unit<false, QV>(W, at, L, ex, M, q, act, asum, wide)
+                          : band_scatter_unit<true, QV>(W, at, L, ex, M, q, act, asum, wide);
         }
-        if (asum) atomicAdd(&s_asum[j], (unsigned long long)asum);
+        if (sizeof(QV) == 4) {
+            // one shared atomic per warp when its lanes' groups are in one
+            // segment and their sum fits 32 bits (the usual case)
+            const int j0 = __shfl_sync(0xFFFFFFFFu, j, 0);
+            if (__all_sync(0xFFFFFFFFu, (j == j0 || !own) && asum < (1u << 26))) {
+                const uint32_t tot = __reduce_add_sync(0xFFFFFFFFu, asum);
+                if (lane == 0 && tot) atomicAdd(&s_asum[j0], (unsigned long long)tot);
+            } else if (asum) {
+                atomicAdd(&s_asum[j], (unsigned long long)asum);
+            }
+        }
     }
+    if (sizeof(QV) == 4 && wide) atomicMax(&s_asum[0], 1ull << 31);
     __syncthreads();
     // The x / y prefixes stay inside one plane segment, so int32 holds them
     // exactly when the segment's sum |q| < 2^31 (the z prefix is summed in
