@@ -29,6 +29,8 @@
 // All integer work is int64 like the reference, so even CRC-valid
 // hand-made streams decode bit-identically.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <vector>
@@ -974,7 +976,11 @@ __global__ void __launch_bounds__(256) k_esc_seg(const DecReg *__restrict__ regs
 // prefix + faces are int64, exact like the reference's int64 cumsum.
 using BV = int32_t;
 constexpr int BCAP = 10240;  // samples per tile (40 KB of int32 + 12 KB dF: 4 CTAs per SM)
-constexpr int BDF = 1536;    // dF entries (btz * ex) when a tile has a band above
+constexpr int BDF = 1536;
+#ifndef CHR_KBT
+#define CHR_KBT 384
+#endif
+constexpr int KBT = CHR_KBT, KBW = KBT / 32;  // k_band threads / warps per CTA    // dF entries (btz * ex) when a tile has a band above
 constexpr int BSEGM = 64;    // planes per tile
 
 __device__ __forceinline__ int seg_of(const int32_t *base, int nseg, int g) {
@@ -994,11 +1000,9 @@ struct Win24 {
     uint32_t E, lit, len;  // end bytes; literal / run-length token ends (own)
 };
 
-__device__ __forceinline__ Win24 win24(const uint8_t *__restrict__ blob, int64_t u0, int64_t lo, int64_t hi) {
+// the window from its 8 context bytes (prv) and 16 own bytes (cur) at u0
+__device__ __forceinline__ Win24 win24_of(uint2 prv, uint4 cur, int64_t u0, int64_t lo, int64_t hi) {
     Win24 W;
-    const uint4 cur = __ldg(reinterpret_cast<const uint4 *>(blob + u0));
-    uint2 prv = make_uint2(0, 0);
-    if (u0 >= 8) prv = __ldg(reinterpret_cast<const uint2 *>(blob + u0 - 8));
     W.w[0] = prv.x; W.w[1] = prv.y;
     W.w[2] = cur.x; W.w[3] = cur.y; W.w[4] = cur.z; W.w[5] = cur.w;
     uint32_t E = 0, Z = 0;
@@ -1153,8 +1157,27 @@ __device__ __forceinline__ int64_t band_scatter_unit(const Win24 &W, int64_t at,
 
 // QV = int32_t: the fast pass (checks the tile's sum |q|); QV = int64_t: the
 // pass over the regions some int32 tile could not hold (asum_reg >= 2^31)
+#ifdef CHR_BAND_TRACE
+// diagnostic build only: per tile (smid, start, after scatter, after x/y
+// prefix, band-above face in, chunk-before face in, published, end) in ns
+__device__ unsigned long long *g_band_trace;
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define BAND_TR(k)                                                                      \
+    do {                                                                                \
+        if (g_band_trace && sizeof(QV) == 4 && tid == 0) g_band_trace[tile * 8 + (k)] = gtime(); \
+    } while (0)
+#else
+#define BAND_TR(k) \
+    do {           \
+    } while (0)
+#endif
+
 template <typename QV>
-__global__ void __launch_bounds__(256) k_band(const DecReg *__restrict__ regs, const int32_t *__restrict__ tile_reg,
+__global__ void __launch_bounds__(KBT) k_band(const DecReg *__restrict__ regs, const int32_t *__restrict__ tile_reg,
                                               const uint8_t *__restrict__ blob,
                                               const int64_t *__restrict__ sp_byte,
                                               const int64_t *__restrict__ sp_skip,
@@ -1190,8 +1213,16 @@ __global__ void __launch_bounds__(256) k_band(const DecReg *__restrict__ regs, c
     const int PL = nyv * rs;      // smem words per plane
     const int64_t hi = (int64_t)(R.poff + R.plen);
     const int64_t sp_end = R.sp_base + (int64_t)R.ez * nb;
+#ifdef CHR_BAND_TRACE
+    if (g_band_trace && sizeof(QV) == 4 && tid == 0) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        g_band_trace[tile * 8] = smid;
+    }
+#endif
+    BAND_TR(1);
 
-    for (int i = tid; i < nzv * PL; i += 256) Q[i] = 0;
+    for (int i = tid; i < nzv * PL; i += KBT) Q[i] = 0;
     if (tid < BSEGM) s_asum[tid] = 0;
     // ---- segments (one per plane) and the 64-byte token groups they cover.
     //      Group g (bytes [G, G+64) from the chunk origin) has its first sample
@@ -1237,29 +1268,41 @@ __global__ void __launch_bounds__(256) k_band(const DecReg *__restrict__ regs, c
     const uint64_t M = ((1ull << 32) + (uint64_t)ex - 1) / (uint64_t)ex;  // row = (at * M) >> 32
     const int64_t gbase = R.chunk_base * DTHREADS;  // pos64 index of the region's first group
     bool wide = false;  // a token the int32 pass does not take (5 bytes / deep negative start)
-    for (int g0 = warp * 32; g0 < U; g0 += 256) {  // warp-uniform bounds (the unit walk votes)
+    for (int g0 = warp * 32; g0 < U; g0 += KBT) {  // warp-uniform bounds (the unit walk votes)
         uint32_t asum = 0;  // sum |q| of the literals this thread stores (segment j; <= 2^31)
         const int gi = g0 + lane;
         const bool own = gi < U;
         int j = 0;
         int64_t G = 0, at = L;
+        uint4 cur = make_uint4(0, 0, 0, 0);  // the unit's 16 bytes, loaded one unit ahead
+        uint2 prv = make_uint2(0, 0);        // the 8 bytes before it
+        int64_t slo = 0, shi = 0;
         if (own) {
             j = seg_of(s_base, nzv, gi);
             const int64_t grp = s_ub[j] + (gi - s_base[j]);
             G = R.abase + grp * 64;
+            slo = s_lo[j];
+            shi = s_hi[j];
+            cur = __ldg(reinterpret_cast<const uint4 *>(blob + G));  // G < shi: inside the file
+            if (G >= 8) prv = __ldg(reinterpret_cast<const uint2 *>(blob + G - 8));
             const int64_t segstart = ((int64_t)(z0 + j) * ey + y0) * ex;
-            at = G <= s_lo[j] ? -s_off[j] : __ldg(pos64 + gbase + grp) - segstart;
+            at = G <= slo ? -s_off[j] : __ldg(pos64 + gbase + grp) - segstart;
         }
         QV *q = Q + j * PL;
 #pragma unroll 1
         for (int u = 0; u < 4; ++u) {
             const int64_t u0 = G + 16 * u;
-            const bool act = own && at < L && u0 + 16 > s_lo[j] && u0 < s_hi[j];
-            if (!__any_sync(0xFFFFFFFFu, act)) continue;
-            Win24 W;
-            if (act) W = win24(blob, u0, s_lo[j], s_hi[j]);
-            at = rs == ex ? band_scatter_unit<false, QV>(W, at, L, ex, M, q, act, asum, wide)
-                          : band_scatter_unit<true, QV>(W, at, L, ex, M, q, act, asum, wide);
+            const bool act = own && at < L && u0 + 16 > slo && u0 < shi;
+            uint4 nxt = make_uint4(0, 0, 0, 0);
+            if (own && u < 3 && u0 + 16 < shi) nxt = __ldg(reinterpret_cast<const uint4 *>(blob + u0 + 16));
+            if (__any_sync(0xFFFFFFFFu, act)) {
+                Win24 W;
+                if (act) W = win24_of(prv, cur, u0, slo, shi);
+                at = rs == ex ? band_scatter_unit<false, QV>(W, at, L, ex, M, q, act, asum, wide)
+                              : band_scatter_unit<true, QV>(W, at, L, ex, M, q, act, asum, wide);
+            }
+            prv = make_uint2(cur.z, cur.w);
+            cur = nxt;
         }
         if (sizeof(QV) == 4) {
             // one shared atomic per warp when its lanes' groups are in one
@@ -1275,6 +1318,7 @@ __global__ void __launch_bounds__(256) k_band(const DecReg *__restrict__ regs, c
     }
     if (sizeof(QV) == 4 && wide) atomicMax(&s_asum[0], 1ull << 31);
     __syncthreads();
+    BAND_TR(2);
     // The x / y prefixes stay inside one plane segment, so int32 holds them
     // exactly when the segment's sum |q| < 2^31 (the z prefix is summed in
     // int64 below).  Otherwise the region is decoded again by the int64 pass
@@ -1289,7 +1333,7 @@ __global__ void __launch_bounds__(256) k_band(const DecReg *__restrict__ regs, c
     // ---- x-prefix (rows are whole)
     const int rows = nzv * nyv;
     if (rows >= 64) {
-        for (int r = tid; r < rows; r += 256) {
+        for (int r = tid; r < rows; r += KBT) {
             QV *p = Q + r * rs;
             QV acc = 0;
             for (int xx = 0; xx < ex; ++xx) {
@@ -1298,7 +1342,7 @@ __global__ void __launch_bounds__(256) k_band(const DecReg *__restrict__ regs, c
             }
         }
     } else {
-        for (int r = warp; r < rows; r += 8) {
+        for (int r = warp; r < rows; r += KBW) {
             QV *p = Q + r * rs;
             QV carry = 0;
             for (int x0 = 0; x0 < ex; x0 += 32) {
@@ -1321,7 +1365,7 @@ __global__ void __launch_bounds__(256) k_band(const DecReg *__restrict__ regs, c
         hi_ = (int)(((uint64_t)t * M) >> 32);
         lo_ = t - hi_ * ex;
     };
-    for (int t = tid; t < ex * nzv; t += 256) {
+    for (int t = tid; t < ex * nzv; t += KBT) {
         int j, xx;
         split(t, j, xx);
         QV *p = Q + j * PL + xx;
@@ -1341,14 +1385,16 @@ __global__ void __launch_bounds__(256) k_band(const DecReg *__restrict__ regs, c
     const int64_t io = (int64_t)(btz + 1) * ex;
     int64_t *dF = ucnt;  // [nzv][ex], <= BDF entries
     int64_t *myF = faces + R.face_base + local * fn;
+    BAND_TR(3);
     if (b > 0) {
 #ifndef CHR_BAND_NOWAIT
         if (tid == 0)
             while (ld_acquire32(tflag + tile - 1) != 2) __nanosleep(20);
 #endif
         __syncthreads();
+        BAND_TR(4);
         const int64_t *Fy = faces + R.face_base + (local - 1) * fn;
-        for (int t = tid; t < ex * nzv; t += 256) dF[t] = __ldcg(Fy + ex + t) - __ldcg(Fy + (t - (t / ex) * ex));
+        for (int t = tid; t < ex * nzv; t += KBT) dF[t] = __ldcg(Fy + ex + t) - __ldcg(Fy + (t - (t / ex) * ex));
     }
     __syncthreads();
     auto qidx = [&](int t, int &xx) {
@@ -1408,30 +1454,32 @@ __global__ void __launch_bounds__(256) k_band(const DecReg *__restrict__ regs, c
         while (ld_acquire32(tflag + tile - nb) != 2) __nanosleep(20);
 #endif
     __syncthreads();
+    BAND_TR(5);
     constexpr int FU = 4;  // columns per thread per round: all face loads first
-    for (int t0 = tid; t0 < L; t0 += 256 * FU) {
+    for (int t0 = tid; t0 < L; t0 += KBT * FU) {
         int64_t fzv[FU];
 #pragma unroll
         for (int k = 0; k < FU; ++k) {
-            const int t = t0 + 256 * k;
+            const int t = t0 + KBT * k;
             fzv[k] = (c > 0 && t < L) ? __ldcg(Ip + t) : 0;
         }
 #pragma unroll
         for (int k = 0; k < FU; ++k) {
-            const int t = t0 + 256 * k;
+            const int t = t0 + KBT * k;
             if (t < L) publish_col(t, fzv[k]);
         }
     }
     release(2);
+    BAND_TR(6);
     if (!mask) {
-        for (int t = tid; t < L; t += 256) recon_col(t, c > 0 ? __ldcg(Ip + t) : 0);
+        for (int t = tid; t < L; t += KBT) recon_col(t, c > 0 ? __ldcg(Ip + t) : 0);
     } else {
         // the same reconstruction in warp-uniform 32-column steps, each plane's
         // inside bits (v >= iso) ballot-packed into the mask (plane-linear bit
         // y * ex + x; words shared with the band above/below are ORed)
         uint32_t *mp = mask + R.mask_off;
         const int64_t bit0 = (int64_t)y0 * ex;
-        for (int t0 = warp * 32; t0 < L; t0 += 256) {
+        for (int t0 = warp * 32; t0 < L; t0 += KBT) {
             const int t = t0 + lane;
             const bool act = t < L;
             int xx = 0, qi = 0;
@@ -1467,13 +1515,14 @@ __global__ void __launch_bounds__(256) k_band(const DecReg *__restrict__ regs, c
             }
         }
     }
+    BAND_TR(7);
     // ---- codec 2: escaped samples keep their f64 value (raster order rank)
     if (R.codec == 2 && R.nesc > 0) {
         __syncthreads();
         const uint8_t *bm = blob + R.poff;
         const uint8_t *ev = bm + ((R.n + 7) >> 3);
         const uint32_t lt = (1u << lane) - 1u;
-        for (int j = warp; j < nzv; j += 8) {
+        for (int j = warp; j < nzv; j += KBW) {
             int64_t rank = esc_sp[R.sp_base + (int64_t)(z0 + j) * nb + b];
             const int64_t s0 = ((int64_t)(z0 + j) * ey + y0) * ex;
             for (int p0 = 0; p0 < L; p0 += 32) {
@@ -1854,12 +1903,34 @@ static int decode_impl(const uint8_t *d_blob, const chr_dec_region_t *h, int64_t
         }
         const int smem = (int)(sizeof(int32_t) * BCAP);
         CHR_CUDA_TRY(cudaFuncSetAttribute(k_band<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+#ifdef CHR_BAND_TRACE
+        unsigned long long *d_tr = nullptr;
+        const char *trf = std::getenv("CHR_BAND_TRACE_FILE");
+        if (trf) {
+            CHR_CUDA_TRY(cudaMalloc(&d_tr, sizeof(unsigned long long) * 8 * (size_t)pl.ntiles));
+            CHR_CUDA_TRY(cudaMemcpyToSymbol(g_band_trace, &d_tr, sizeof(d_tr)));
+        }
+#endif
         {
             CHR_PROF("k_band", st);
-            k_band<int32_t><<<(unsigned)pl.ntiles, 256, smem, st>>>(
+            k_band<int32_t><<<(unsigned)pl.ntiles, KBT, smem, st>>>(
                 pl.d_regs, pl.tile_reg, d_blob, pl.sp_byte, pl.sp_skip, pl.esc_sp, pl.pos64, pl.faces, pl.tflag,
                 pl.ticket3, pl.order, d_out, d_mask, iso, pl.asum);
         }
+#ifdef CHR_BAND_TRACE
+        if (d_tr) {
+            std::vector<unsigned long long> h((size_t)8 * pl.ntiles);
+            CHR_CUDA_TRY(cudaStreamSynchronize(st));
+            CHR_CUDA_TRY(cudaMemcpy(h.data(), d_tr, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost));
+            unsigned long long *z = nullptr;
+            CHR_CUDA_TRY(cudaMemcpyToSymbol(g_band_trace, &z, sizeof(z)));
+            cudaFree(d_tr);
+            if (FILE *f = std::fopen(trf, "wb")) {
+                std::fwrite(h.data(), sizeof(unsigned long long), h.size(), f);
+                std::fclose(f);
+            }
+        }
+#endif
         {
             CHR_PROF("k_asum_check", st);
             k_asum_check<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(pl.d_regs, n, pl.asum, pl.any_slow + 1);
@@ -1881,7 +1952,7 @@ static int decode_impl(const uint8_t *d_blob, const chr_dec_region_t *h, int64_t
         const int smem = (int)(sizeof(int64_t) * BCAP);
         CHR_CUDA_TRY(cudaFuncSetAttribute(k_band<int64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         CHR_PROF("k_band64", st);
-        k_band<int64_t><<<(unsigned)pl.ntiles, 256, smem, st>>>(
+        k_band<int64_t><<<(unsigned)pl.ntiles, KBT, smem, st>>>(
             pl.d_regs, pl.tile_reg, d_blob, pl.sp_byte, pl.sp_skip, pl.esc_sp, pl.pos64, pl.faces, pl.tflag,
             pl.ticket3, pl.order, d_out, d_mask, iso, pl.asum);
     }
