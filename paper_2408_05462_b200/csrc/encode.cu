@@ -468,7 +468,7 @@ __global__ void k_tile_fill_map(const RegDev *__restrict__ regs, int64_t nreg, i
 // byte by byte from the lanes (rare).  Verbatim regions: the CTA's threads
 // copy the samples of its 128 pieces, coalesced.
 constexpr int E2_WARPS = 4;
-constexpr int E2_STAGE = 8192;  // bytes per warp
+constexpr int E2_STAGE = 8188;  // bytes per warp (+ up to 3 alignment bytes)
 template <typename T>
 __global__ void __launch_bounds__(E2_WARPS * 32) k_emit_q2(const T *__restrict__ vol, const EncParams *__restrict__ P,
                                                            const RegDev *__restrict__ regs,
@@ -479,7 +479,7 @@ __global__ void __launch_bounds__(E2_WARPS * 32) k_emit_q2(const T *__restrict__
                                                            const uint32_t *__restrict__ escbits,
                                                            uint8_t *__restrict__ out) {
     __shared__ RegDev R;
-    __shared__ __align__(16) uint8_t stage[E2_WARPS][E2_STAGE];
+    __shared__ __align__(16) uint8_t stage[E2_WARPS][E2_STAGE + 4];
     constexpr int PER = E2_WARPS * 32;  // pieces per CTA
     constexpr int SPLIT = (int)(CH / PER);
     const int64_t c = blockIdx.x / SPLIT;
@@ -518,90 +518,133 @@ __global__ void __launch_bounds__(E2_WARPS * 32) k_emit_q2(const T *__restrict__
     int64_t cur_end = 0;  // end of this lane's bytes (relative to off0)
     uint8_t *const gdst = out + R.tok_start + off0;
     uint8_t *const sbuf = stage[w];
+    // staging index = byte address mod 4 + offset: word k of the stage is an
+    // aligned word of the archive, for the lanes' packed stores and the copy-out
+    const int base = (int)((uintptr_t)gdst & 3);
     if (have) {
         const PieceOff po = poffs[R.piece_base + lp];
         const int64_t s0 = lp * TX;
         const int vcount = (int)min((int64_t)TX, R.n - s0);
-        int64_t cur = po.tok_off - off0;
-        int64_t run = po.carry;
-        auto put = [&](uint8_t b) {
-            if (staged) sbuf[cur] = b;
-            else gdst[cur] = b;
-            ++cur;
-        };
-        auto put_runs = [&](int64_t L) {
-            if (L == 1) {
-                put(1);
-            } else if (L >= 2) {
-                put(0);
-                uint64_t u = (uint64_t)L;
-                while (u >= 0x80) {
-                    put((uint8_t)((u & 0x7F) | 0x80));
-                    u >>= 7;
-                }
-                put((uint8_t)u);
-            }
-        };
         const uint32_t *q = qz + R.q_base + s0;
-        uint32_t em0 = 0, em1 = 0;  // escape bits of the piece (codec 2)
-        int64_t erank = po.esc_off;
+        const int64_t p0 = base + po.tok_off - off0;
+        int64_t run = po.carry;
+        // run the piece's tokens through a byte packer (bytes collect in a
+        // 64-bit register and leave as aligned 4-byte stores; the lane's first
+        // and last partial words as byte stores: the neighbours own the rest)
+        auto emit = [&](auto st8, auto st32) {
+            uint64_t acc = 0;
+            int n = 0, need = (int)((4 - (p0 & 3)) & 3);
+            int64_t pos = p0;
+            auto add = [&](uint64_t v, int len) {  // len <= 5, n <= 3 on entry
+                acc |= v << (8 * n);
+                n += len;
+                while (need > 0 && n > 0) {  // head bytes up to the first word boundary
+                    st8(pos++, (uint8_t)acc);
+                    acc >>= 8;
+                    --n;
+                    --need;
+                }
+                if (n >= 4) {
+                    st32(pos, (uint32_t)acc);
+                    acc >>= 32;
+                    n -= 4;
+                    pos += 4;
+                }
+                if (n >= 4) {
+                    st32(pos, (uint32_t)acc);
+                    acc >>= 32;
+                    n -= 4;
+                    pos += 4;
+                }
+            };
+            auto leb = [](uint64_t u, int &len) {  // u < 2^35: LEB128 bytes, low byte first
+                len = 1 + (u >= (1ull << 7)) + (u >= (1ull << 14)) + (u >= (1ull << 21)) + (u >= (1ull << 28));
+                const uint64_t v = (u & 0x7Full) | ((u & 0x3F80ull) << 1) | ((u & 0x1FC000ull) << 2) |
+                                   ((u & 0xFE00000ull) << 3) | ((u & 0x7F0000000ull) << 4);
+                return v | (0x80808080ull & ((1ull << (8 * (len - 1))) - 1));
+            };
+            auto runs = [&](int64_t L) {  // the zero-run token before a literal (or the stream end)
+                if (L == 1) {
+                    add(1, 1);
+                } else if (L >= 2) {
+                    int len;
+                    const uint64_t v = leb((uint64_t)L, len);
+                    add(0, 1);
+                    add(v, len);
+                }
+            };
+            auto step = [&](uint32_t z) {
+                if (z != 1u) {
+                    runs(run);
+                    run = 0;
+                    int len;
+                    const uint64_t v = leb(z, len);
+                    add(v, len);
+                } else {
+                    ++run;
+                }
+            };
+            if (vcount == TX) {
+                const uint4 *q4 = reinterpret_cast<const uint4 *>(q);
+#pragma unroll 2
+                for (int k = 0; k < TX / 4; ++k) {
+                    const uint4 v = __ldg(q4 + k);
+                    step(v.x);
+                    step(v.y);
+                    step(v.z);
+                    step(v.w);
+                }
+            } else {
+                for (int i = 0; i < vcount; ++i) step(__ldg(q + i));
+            }
+            if (R.last && lp == R.npieces - 1) runs(run);  // the window's final zero run
+            while (n > 0) {  // the last partial word
+                st8(pos++, (uint8_t)acc);
+                acc >>= 8;
+                --n;
+            }
+            return pos;
+        };
+        if (staged) {
+            cur_end = emit([&](int64_t i, uint8_t v) { sbuf[i] = v; },
+                           [&](int64_t i, uint32_t v) { *reinterpret_cast<uint32_t *>(sbuf + i) = v; });
+        } else {
+            uint8_t *g = gdst - base;  // 4-aligned
+            cur_end = emit([&](int64_t i, uint8_t v) { g[i] = v; },
+                           [&](int64_t i, uint32_t v) { *reinterpret_cast<uint32_t *>(g + i) = v; });
+        }
+        // codec 2: escaped samples' f64 values at their escape rank
         if (codec == 2 && recs[R.piece_base + lp].nesc) {
             const int64_t bit = (int64_t)R.ebase * 32 + s0;
             const uint32_t *wq = escbits + (bit >> 5);
             const int sh = (int)(bit & 31);
-            em0 = __funnelshift_r(wq[0], wq[1], sh);
-            em1 = __funnelshift_r(wq[1], wq[2], sh);
-        }
-        const uint64_t vbase = R.payload_off + (uint64_t)((R.n_win + 7) >> 3);
-        auto step = [&](uint32_t z, int i) {
-            if (z != 1u) {
-                put_runs(run);
-                run = 0;
-                uint32_t u = z;
-                while (u >= 0x80u) {
-                    put((uint8_t)((u & 0x7Fu) | 0x80u));
-                    u >>= 7;
-                }
-                put((uint8_t)u);
-            } else {
-                ++run;
-            }
-            if ((i < 32 ? (em0 >> i) : (em1 >> (i - 32))) & 1u)
+            uint64_t em = (uint64_t)__funnelshift_r(wq[0], wq[1], sh) |
+                          ((uint64_t)__funnelshift_r(wq[1], wq[2], sh) << 32);
+            if (vcount < 64) em &= (1ull << vcount) - 1;
+            const uint64_t vbase = R.payload_off + (uint64_t)((R.n_win + 7) >> 3);
+            int64_t erank = po.esc_off;
+            while (em) {
+                const int i = __ffsll((long long)em) - 1;
+                em &= em - 1;
                 put_le(out + vbase + 8 * (erank++), (double)vol_at(s0 + i));
-        };
-        if (vcount == TX) {
-            const uint4 *q4 = reinterpret_cast<const uint4 *>(q);
-#pragma unroll 2
-            for (int k = 0; k < TX / 4; ++k) {
-                const uint4 v = __ldg(q4 + k);
-                step(v.x, 4 * k);
-                step(v.y, 4 * k + 1);
-                step(v.z, 4 * k + 2);
-                step(v.w, 4 * k + 3);
             }
-        } else {
-            for (int i = 0; i < vcount; ++i) step(__ldg(q + i), i);
         }
-        if (R.last && lp == R.npieces - 1) put_runs(run);  // the window's final zero run
-        cur_end = cur;
     }
     if (!staged) return;
     __syncwarp();
-    const int64_t total = (int64_t)__reduce_max_sync(0xFFFFFFFFu, (unsigned)cur_end);
-    // the warp's bytes [0, total) -> gdst, aligned words + two edge words
-    const uintptr_t d0 = (uintptr_t)gdst;
-    const int head = (int)((4 - (d0 & 3)) & 3);
-    const int h = (int)(total < head ? total : (int64_t)head);
-    if (lane < h) gdst[lane] = sbuf[lane];
-    const int64_t nw = (total - h) >> 2;
-    uint32_t *gw = reinterpret_cast<uint32_t *>(gdst + h);
-    for (int64_t j = lane; j < nw; j += 32) {
-        const int b = h + 4 * (int)j;
-        gw[j] = (uint32_t)sbuf[b] | ((uint32_t)sbuf[b + 1] << 8) | ((uint32_t)sbuf[b + 2] << 16) |
-                ((uint32_t)sbuf[b + 3] << 24);
+    // the warp's bytes: stage [base, end) -> gdst - base + [base, end)
+    const int end = (int)__reduce_max_sync(0xFFFFFFFFu, (unsigned)(have ? cur_end : (int64_t)base));
+    uint8_t *const g = gdst - base;
+    const int w0 = (base + 3) >> 2, w1 = end >> 2;  // whole words [w0, w1)
+    if (w0 > w1) {  // all inside one word
+        if (lane >= base && lane < end) g[lane] = sbuf[lane];
+        return;
     }
-    const int64_t tb = h + 4 * nw;
-    if (tb + lane < total) gdst[tb + lane] = sbuf[tb + lane];
+    if (lane >= base && lane < 4 * w0) g[lane] = sbuf[lane];
+    const uint32_t *sw = reinterpret_cast<const uint32_t *>(sbuf);
+    uint32_t *gw = reinterpret_cast<uint32_t *>(g);
+    for (int j = w0 + lane; j < w1; j += 32) gw[j] = sw[j];
+    if (4 * w1 + lane < end) g[4 * w1 + lane] = sbuf[4 * w1 + lane];
 }
 
 // ------------------------------------------------------------------ scans
