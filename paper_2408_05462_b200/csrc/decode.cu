@@ -637,13 +637,20 @@ struct UnitMasks {
 
 // w[0..3]: previous 16 bytes, w[4..7]: own 16 bytes; bit 16 <-> offset u0.
 // The stream is [lo, hi) (blob offsets).
-__device__ __forceinline__ UnitMasks unit_masks(const uint32_t (&w)[8], int64_t u0, int64_t lo, int64_t hi) {
-    uint32_t E = 0, Z = 0;
+// end / zero bits of 16 bytes (4 words)
+__device__ __forceinline__ void ez16(const uint32_t *w, uint32_t &E, uint32_t &Z) {
+    E = 0;
+    Z = 0;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
+    for (int k = 0; k < 4; ++k) {
         E |= word_end4(w[k]) << (4 * k);
         Z |= word_zero4(w[k]) << (4 * k);
     }
+}
+
+// from the raw end / zero bits of the 32-byte window (consecutive units of
+// a thread pass their own half on as the next unit's context half)
+__device__ __forceinline__ UnitMasks unit_masks_ez(uint32_t E, uint32_t Z, int64_t u0, int64_t lo, int64_t hi) {
     const int64_t base = u0 - 16;
     const int64_t nlo = lo - base, nhi = hi - base;  // bits [nlo, nhi) are stream bytes
     const uint32_t lob = nlo <= 0 ? 0u : (nlo >= 32 ? 0xFFFFFFFFu : ((1u << nlo) - 1u));
@@ -668,6 +675,13 @@ __device__ __forceinline__ UnitMasks unit_masks(const uint32_t (&w)[8], int64_t 
     m.lit = E & ~Z & ~Lend & mine;
     m.E = E;
     return m;
+}
+
+__device__ __forceinline__ UnitMasks unit_masks(const uint32_t (&w)[8], int64_t u0, int64_t lo, int64_t hi) {
+    uint32_t E0, Z0, E1, Z1;
+    ez16(w, E0, Z0);
+    ez16(w + 4, E1, Z1);
+    return unit_masks_ez(E0 | (E1 << 16), Z0 | (Z1 << 16), u0, lo, hi);
 }
 
 // value of the token [s, e] (<= 5 bytes) at blob offset `p` (start byte):
@@ -823,12 +837,19 @@ __global__ void __launch_bounds__(DTHREADS) k_tok_fast(DecReg *__restrict__ regs
     if (ub + UPT * 16 > lo && ub < hi) {
         uint32_t w[8];
         load_units(blob, ub, w);
+        uint32_t Ec, Zc;  // raw end / zero bits of the context half
+        ez16(w, Ec, Zc);
 #pragma unroll 1
         for (int u = 0; u < UPT; ++u) {
             const int64_t u0 = ub + 16 * u;
             if (u) next_unit(blob, u0, w);
+            uint32_t Eo, Zo;
+            ez16(w + 4, Eo, Zo);
+            const uint32_t Ew = Ec | (Eo << 16), Zw = Zc | (Zo << 16);
+            Ec = Eo;
+            Zc = Zo;
             if (u0 + 16 > lo && u0 < hi) {
-                const UnitMasks m = unit_masks(w, u0, lo, hi);
+                const UnitMasks m = unit_masks_ez(Ew, Zw, u0, lo, hi);
                 err |= m.err;
                 nc |= m.noncanon;
                 cnt += unit_count(m, blob, u0);
@@ -878,12 +899,19 @@ __global__ void __launch_bounds__(DTHREADS) k_seg_locate(const DecReg *__restric
     const int64_t ub = R.abase + (c - R.chunk_base) * DCB + (int64_t)threadIdx.x * UPT * 16;
     uint32_t w[8];
     load_units(blob, ub, w);
+    uint32_t Ec, Zc;  // raw end / zero bits of the context half
+    ez16(w, Ec, Zc);
 #pragma unroll 1
     for (int u = 0; u < UPT; ++u) {
         const int64_t u0 = ub + 16 * u;
         if (u) next_unit(blob, u0, w);
+        uint32_t Eo, Zo;
+        ez16(w + 4, Eo, Zo);
+        const uint32_t Ew = Ec | (Eo << 16), Zw = Zc | (Zo << 16);
+        Ec = Eo;
+        Zc = Zo;
         if (!(u0 + 16 > lo && u0 < hi)) continue;
-        const UnitMasks m = unit_masks(w, u0, lo, hi);
+        const UnitMasks m = unit_masks_ez(Ew, Zw, u0, lo, hi);
         if (m.len == 0) {  // literals only: one sample per token, starts found by rank
             const int n = __popc(m.lit);
             while (s < a + n) {
