@@ -186,6 +186,12 @@ __global__ void __launch_bounds__(SQ) k_stats_rows(const float *__restrict__ vol
     if (g < rg) {
         float lo = INFINITY, hi = -INFINITY, gl = INFINITY, gh = -INFINITY;
         double dm = INFINITY, gd = INFINITY;
+        // m == 1: fl(s - k) is monotone in s, so min |fl(s - k)| over a block
+        // is attained at the smallest sample >= k or the largest sample < k:
+        // track those two in f32 (exact compares against thr = the smallest
+        // float >= k) and form the f64 distances once at the end
+        float ab = INFINITY, bl = -INFINITY, gab = INFINITY, gbl = -INFINITY;
+        const float thr0 = kt[0];
         unsigned long long bad = ~0ull;
         const bool ghost = ((4 * q) % bs) == 0 && q > 0;
         // RU rows per step: their 16-byte loads are all in flight before any is
@@ -215,12 +221,22 @@ __global__ void __launch_bounds__(SQ) k_stats_rows(const float *__restrict__ vol
                     }
                     lo = fminf(lo, f);
                     hi = fmaxf(hi, f);
+                    if (m == 1) {
+                        const bool up = f >= thr0;
+                        ab = fminf(ab, up ? f : INFINITY);
+                        bl = fmaxf(bl, up ? -INFINITY : f);
+                        if (i == 0 && ghost) {
+                            gl = fminf(gl, f);
+                            gh = fmaxf(gh, f);
+                            gab = fminf(gab, up ? f : INFINITY);
+                            gbl = fmaxf(gbl, up ? -INFINITY : f);
+                        }
+                        continue;
+                    }
                     // min |s - k| over the two candidates bracketing s
                     const double sd = (double)f;
                     double d;
-                    if (m == 1) {
-                        d = fabs(__dadd_rn(sd, -ks[0]));
-                    } else {
+                    {
                         int c;  // #{j : k[j] <= s}
                         if (!(f >= lo_e)) {
                             c = 0;
@@ -245,6 +261,11 @@ __global__ void __launch_bounds__(SQ) k_stats_rows(const float *__restrict__ vol
                     }
                 }
             }
+        }
+        if (m == 1 && !isnan(ks[0])) {  // (a NaN candidate leaves the distances at +inf, like fmin)
+            const double k0 = ks[0];
+            dm = fmin(__dadd_rn((double)ab, -k0), __dadd_rn(k0, -(double)bl));
+            gd = fmin(__dadd_rn((double)gab, -k0), __dadd_rn(k0, -(double)gbl));
         }
         if (bad != ~0ull) atomicMin(first_bad, bad);
         const int k = g * nq + q;
