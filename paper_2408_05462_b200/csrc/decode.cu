@@ -400,6 +400,17 @@ __device__ __forceinline__ int32_t ld_acquire32(const int32_t *p) {
     asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+__device__ __forceinline__ int32_t ld_relaxed32(const int32_t *p) {
+    int32_t v;
+    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+// spin on a tile flag with relaxed loads (an acquire load invalidates the
+// SM's L1 on every poll), then one acquire load orders the reads after it
+__device__ __forceinline__ void wait_flag(const int32_t *p, int32_t v) {
+    while (ld_relaxed32(p) != v) __nanosleep(20);
+    (void)ld_acquire32(p);
+}
 __device__ __forceinline__ void st_release32(int32_t *p, int32_t v) {
     asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -1417,7 +1428,7 @@ __global__ void __launch_bounds__(KBT) k_band(const DecReg *__restrict__ regs, c
     if (b > 0) {
 #ifndef CHR_BAND_NOWAIT
         if (tid == 0)
-            while (ld_acquire32(tflag + tile - 1) != 2) __nanosleep(20);
+            wait_flag(tflag + tile - 1, 2);
 #endif
         __syncthreads();
         BAND_TR(4);
@@ -1479,7 +1490,7 @@ __global__ void __launch_bounds__(KBT) k_band(const DecReg *__restrict__ regs, c
     const int64_t *Ip = faces + R.face_base + (local - nb) * fn + io;
 #ifndef CHR_BAND_NOWAIT
     if (c > 0 && tid == 0)
-        while (ld_acquire32(tflag + tile - nb) != 2) __nanosleep(20);
+        wait_flag(tflag + tile - nb, 2);
 #endif
     __syncthreads();
     BAND_TR(5);
