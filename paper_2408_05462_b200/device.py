@@ -168,9 +168,16 @@ class Workspaces:
         n = max(1, -(-int(nbytes) // elem))
         t = self._bufs.get(name)
         if t is None or t.numel() < n or t.dtype != dtype or t.device != _abi.device():
+            # drop the old buffer first: at c5 sizes old + new may not fit together
+            self._bufs.pop(name, None)
+            del t
             t = torch.empty(max(n, 64), dtype=dtype, device=_abi.device())
             self._bufs[name] = t
         return t
+
+    def clear(self) -> None:
+        """Drop every buffer (device, pinned and host)."""
+        self._bufs.clear()
 
 
 class _ThreadWorkspaces:
@@ -190,6 +197,24 @@ class _ThreadWorkspaces:
 
     def __getattr__(self, name):
         return getattr(self._get(), name)
+
+    def release(self) -> None:
+        """Drop this thread's default workspaces."""
+        ws = getattr(self._tls, "ws", None)
+        if ws is not None:
+            ws.clear()
+
+
+def release_workspaces() -> None:
+    """Free the calling thread's default scratch and the caching allocator's
+    unused blocks (between full-size runs that each need most of the HBM)."""
+    import gc
+
+    _DEFAULT_WS.release()
+    gc.collect()
+    if torch.cuda.is_available():
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
 
 
 _DEFAULT_WS = _ThreadWorkspaces()

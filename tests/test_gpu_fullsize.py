@@ -29,6 +29,15 @@ import paper_2408_05462_b200 as G  # noqa: E402
 from oracle import oracle as O  # noqa: E402
 from paper_2408_05462_b200 import device, synth  # noqa: E402
 
+
+@pytest.fixture(autouse=True)
+def _free_hbm():
+    """Each full-size test needs most of the 180 GB: start from empty scratch."""
+    device.release_workspaces()
+    yield
+    device.release_workspaces()
+
+
 def sha(a):
     return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
 
@@ -151,6 +160,7 @@ def test_c5_all_isovalues():
             assert (ntri[j], nvert[j]) == (rt.shape[0], rv.shape[0]), (ci, i)
             assert np.array_equal(vb[vert0[j]:vert0[j + 1]], rv), (ci, i)
             assert np.array_equal(tb[tri0[j]:tri0[j + 1]] - vert0[j], rt), (ci, i)
+        del wins, v, t, vb, tb  # the next candidate's windows may need a larger buffer
     print(f"c5: 16 isovalues, {len(regs)} regions, {total_tris} triangles in all")
 
 

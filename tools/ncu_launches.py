@@ -14,7 +14,7 @@ for r in rows[h + 1:]:
     if len(r) < len(hdr) or r[mn] != "gpu__time_duration.sum":
         continue
     name = r[kn].split("(")[0].replace("void ", "")
-    if not name.startswith("chr::"):
+    if not (name.startswith("chr::") or "::k_" in name or name.startswith("k_")):
         continue  # synthetic-input generation, torch kernels
     a = agg.setdefault(name, [0, 0.0])
     a[0] += 1
