@@ -25,8 +25,9 @@ CHR_HD int64_t crc_num_superchunks(uint64_t a, uint64_t b) {
 }
 
 int64_t crc_plan_segments(CrcSeg *segs, int64_t nseg);
+// max_blocks > 0 caps the grid (a CRC overlapping other kernels on a side stream)
 int crc_launch(const uint8_t *d_buf, const CrcSeg *d_segs, int64_t nseg, int64_t total_sc,
-               uint32_t *d_seg_raw, cudaStream_t st);
+               uint32_t *d_seg_raw, cudaStream_t st, int64_t max_blocks = 0);
 __global__ void k_crc_segments(const uint8_t *__restrict__ buf, const CrcSeg *__restrict__ segs,
                                int64_t nseg, const CrcTables *__restrict__ tabs,
                                uint32_t *__restrict__ seg_raw);
@@ -76,6 +77,35 @@ class XferScope {
     size_t mark_;
 };
 #define CHR_XFER_SCOPE ::chr::XferScope CHR_PROF_CAT(_chr_xfer_, __LINE__)
+
+// ------------------------------------------------------------------ side stream
+// Per host thread and device: a second (non-blocking) stream and events for
+// work that overlaps the caller's stream inside one library call -- the
+// payload CRC-32s, which nothing on the caller's stream reads until the
+// call's final status.  nullptr when CHR_NO_SIDE=1 (serial A/B runs) or on
+// a CUDA error; callers then run everything on their own stream.
+struct Side {
+    cudaStream_t st = nullptr;
+    cudaEvent_t ev[4] = {};
+};
+Side *side_stream();
+
+// compress with the CRC tail (payload CRCs, block headers, file trailer) on
+// `side` (encode.cu): returns after the host knows the layout; the archive
+// is complete once side->ev[1] fires.  The control arrays the tail reads are
+// carved first in the workspace (`keep_bytes`), so a caller may reuse the
+// rest of the workspace right away.  compress_crcs() then copies the
+// finished payload CRCs into a device array (after side->ev[1]).
+int compress_with_side(const void *d_vol, int dtype, int src_dtype, int64_t nx, int64_t ny, int64_t nz,
+                       const double *spacing, int64_t bs, double vmin, double vmax, const double *h_cands, int m,
+                       chr_region_t *h_regions, int64_t nreg, void *d_ws, size_t ws_bytes, uint8_t *d_out,
+                       uint64_t out_cap, uint64_t *h_out_nbytes, Side *side, size_t *keep_bytes, void **d_regs,
+                       cudaStream_t st);
+int compress_crcs(const void *d_regs, int64_t nreg, uint32_t *d_crc, cudaStream_t st);
+// chr_decode_regions_mask with the expected payload CRCs read from the block
+// headers in d_blob (the pipeline: the host has not seen them yet)
+int decode_mask_hdrcrc(const uint8_t *d_blob, const chr_dec_region_t *h, int64_t n, double *d_out, void *d_ws,
+                       size_t ws_bytes, int32_t *h_status, double iso, uint32_t *d_mask, cudaStream_t st);
 
 // ------------------------------------------------------------------ workspace
 struct WsCarver {

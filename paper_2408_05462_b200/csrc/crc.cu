@@ -159,7 +159,7 @@ int64_t crc_plan_segments(CrcSeg *segs, int64_t nseg) {
 }
 
 int crc_launch(const uint8_t *d_buf, const CrcSeg *d_segs, int64_t nseg, int64_t total_sc,
-               uint32_t *d_seg_raw, cudaStream_t st) {
+               uint32_t *d_seg_raw, cudaStream_t st, int64_t max_blocks) {
     const CrcTables *tabs = crc_tables_device();
     if (!tabs) return CHR_E_CUDA;
     if (nseg <= 0) return CHR_OK;
@@ -167,6 +167,7 @@ int crc_launch(const uint8_t *d_buf, const CrcSeg *d_segs, int64_t nseg, int64_t
     const int64_t warps_needed = total_sc > 0 ? total_sc : 148 * 128;
     int64_t blocks = (warps_needed + 7) / 8;
     if (blocks > 148 * 16) blocks = 148 * 16;
+    if (max_blocks > 0 && blocks > max_blocks) blocks = max_blocks;
     if (blocks < 1) blocks = 1;
     {
         CHR_PROF("k_crc_segments", st);

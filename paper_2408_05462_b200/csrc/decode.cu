@@ -103,15 +103,15 @@ __device__ __forceinline__ int64_t find_dreg(const DecReg *__restrict__ r, int64
     return lo;
 }
 
-__global__ void k_check(DecReg *__restrict__ regs, int64_t nreg, const uint32_t *__restrict__ seg_raw,
-                        const CrcTables *__restrict__ tabs, const uint8_t *__restrict__ blob) {
+// per-region checks that need no payload pass (the CRC is k_crc_flag's, on
+// the side stream: decoding proceeds and the call's status reports a
+// mismatch first, as decompress() raises it before decoding, codec.py:220)
+__global__ void k_check(DecReg *__restrict__ regs, int64_t nreg) {
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= nreg) return;
     DecReg &R = regs[r];
-    const uint32_t crc = crc_finalize(tabs->x2n, seg_raw[r], R.plen);
     uint32_t err = 0;
-    if (crc != R.crc) err |= EF_CRC;
-    else if (R.codec < 0 || R.codec > 3) err |= EF_CODEC;
+    if (R.codec < 0 || R.codec > 3) err |= EF_CODEC;
     R.tok_start = R.poff;
     R.nesc = 0;
     if (!err) {
@@ -120,6 +120,24 @@ __global__ void k_check(DecReg *__restrict__ regs, int64_t nreg, const uint32_t 
         if (R.codec == 2 && R.plen < (uint64_t)((R.n + 7) >> 3)) err |= EF_SHORTBM;
     }
     R.err = err;
+}
+
+// payload CRC vs the expected one: the host's (R.crc) or, with `hdr`, the
+// block header's last four bytes (just before the payload).  Writes only
+// crc_bad, which no decode kernel reads (R.err stays the decoders' own).
+__global__ void k_crc_flag(const DecReg *__restrict__ regs, int64_t nreg, const uint32_t *__restrict__ seg_raw,
+                           const CrcTables *__restrict__ tabs, const uint8_t *__restrict__ blob, int hdr,
+                           int32_t *__restrict__ crc_bad) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= nreg) return;
+    const DecReg &R = regs[r];
+    const uint32_t crc = crc_finalize(tabs->x2n, seg_raw[r], R.plen);
+    uint32_t want = R.crc;
+    if (hdr) {
+        const uint8_t *p = blob + R.poff - 4;
+        want = (uint32_t)p[0] | ((uint32_t)p[1] << 8) | ((uint32_t)p[2] << 16) | ((uint32_t)p[3] << 24);
+    }
+    crc_bad[r] = crc != want ? 1 : 0;
 }
 
 // codec 2: count escapes (popcount of the bitmap) -> token start
@@ -1639,6 +1657,7 @@ struct DecPlan {
     DecReg *d_regs;
     CrcSeg *segs;
     uint32_t *seg_raw;
+    int32_t *crc_bad;
     int64_t *chunk_samples, *seg_byte, *seg_skip, *esc_base, *carry, *flags;
     int64_t *sp_byte, *sp_skip, *esc_sp, *thr_cnt, *pos64;
     int64_t *faces;
@@ -1799,7 +1818,8 @@ static void dec_carve(DecPlan &pl, void *base, size_t cap) {
     const int64_t n = (int64_t)pl.regs.size();
     pl.d_regs = c.take<DecReg>(n);
     pl.segs = c.take<CrcSeg>(n);
-    pl.seg_raw = c.take<uint32_t>(n);
+    pl.seg_raw = c.take<uint32_t>(2 * n);  // + crc_bad (one zero range)
+    pl.crc_bad = base ? reinterpret_cast<int32_t *>(pl.seg_raw + n) : nullptr;
     pl.chunk_samples = c.take<int64_t>(pl.nchunks);
     pl.seg_byte = c.take<int64_t>(pl.nseg + 1);
     pl.seg_skip = c.take<int64_t>(pl.nseg + 1);
@@ -1838,7 +1858,8 @@ extern "C" size_t chr_decode_workspace_size(const chr_dec_region_t *h, int64_t n
 }
 
 static int decode_impl(const uint8_t *d_blob, const chr_dec_region_t *h, int64_t n, double *d_out, void *d_ws,
-                       size_t ws_bytes, int32_t *h_status, double iso, uint32_t *d_mask, void *stream);
+                       size_t ws_bytes, int32_t *h_status, double iso, uint32_t *d_mask, void *stream,
+                       int crc_hdr = 0);
 
 extern "C" int chr_decode_regions(const uint8_t *d_blob, const chr_dec_region_t *h, int64_t n,
                                   double *d_out, void *d_ws, size_t ws_bytes, int32_t *h_status,
@@ -1863,8 +1884,16 @@ extern "C" int chr_decode_regions_mask(const uint8_t *d_blob, const chr_dec_regi
     return decode_impl(d_blob, h, n, d_out, d_ws, ws_bytes, h_status, iso, d_mask, stream);
 }
 
+namespace chr {
+int decode_mask_hdrcrc(const uint8_t *d_blob, const chr_dec_region_t *h, int64_t n, double *d_out, void *d_ws,
+                       size_t ws_bytes, int32_t *h_status, double iso, uint32_t *d_mask, cudaStream_t st) {
+    return decode_impl(d_blob, h, n, d_out, d_ws, ws_bytes, h_status, iso, d_mask, st, 1);
+}
+}  // namespace chr
+
 static int decode_impl(const uint8_t *d_blob, const chr_dec_region_t *h, int64_t n, double *d_out, void *d_ws,
-                       size_t ws_bytes, int32_t *h_status, double iso, uint32_t *d_mask, void *stream) {
+                       size_t ws_bytes, int32_t *h_status, double iso, uint32_t *d_mask, void *stream,
+                       int crc_hdr) {
     if (n == 0) return CHR_OK;
     if (!d_blob || !h || n < 0 || !d_out) return CHR_E_PARAMETER;
     cudaStream_t st = (cudaStream_t)stream;
@@ -1882,7 +1911,7 @@ static int decode_impl(const uint8_t *d_blob, const chr_dec_region_t *h, int64_t
     const int64_t total_sc = crc_plan_segments(segs.data(), n);
     CHR_CUDA_TRY(h2d_multi({{pl.d_regs, pl.regs.data(), sizeof(DecReg) * n}, {pl.segs, segs.data(), sizeof(CrcSeg) * n}},
                            st));
-    CHR_CUDA_TRY(zero_async({{pl.seg_raw, sizeof(uint32_t) * n},
+    CHR_CUDA_TRY(zero_async({{pl.seg_raw, 2 * sizeof(uint32_t) * n},  // + crc_bad
                              {pl.flags, sizeof(int64_t) * (pl.nitems + 1)},
                              {pl.ticket, sizeof(unsigned long long)},
                              {pl.ticket3, sizeof(unsigned long long)},
@@ -1891,12 +1920,28 @@ static int decode_impl(const uint8_t *d_blob, const chr_dec_region_t *h, int64_t
                              {d_mask, d_mask ? sizeof(uint32_t) * (pl.nmask + 8) : 0},
                              {pl.tflag, sizeof(int32_t) * (pl.ntiles + 1)}},
                             st));
-    int rc = crc_launch(d_blob, pl.segs, n, total_sc, pl.seg_raw, st);
-    if (rc) return rc;
     {
         CHR_PROF("k_check", st);
-        k_check<<<(unsigned)ceil_div(n, 128), 128, 0, st>>>(pl.d_regs, n, pl.seg_raw, tabs, d_blob);
+        k_check<<<(unsigned)ceil_div(n, 128), 128, 0, st>>>(pl.d_regs, n);
     }
+    // payload CRCs: on the side stream (overlapping the decode), joined
+    // before the status read-back
+    Side *side = side_stream();
+    cudaStream_t ct = st;
+    if (side) {
+        CHR_CUDA_TRY(cudaEventRecord(side->ev[2], st));
+        CHR_CUDA_TRY(cudaStreamWaitEvent(side->st, side->ev[2], 0));
+        ct = side->st;
+    }
+    int rc = crc_launch(d_blob, pl.segs, n, total_sc, pl.seg_raw, ct, side ? 148 * 2 : 0);
+    if (rc) return rc;
+    {
+        CHR_PROF("k_crc_flag", ct);
+        k_crc_flag<<<(unsigned)ceil_div(n, 128), 128, 0, ct>>>(pl.d_regs, n, pl.seg_raw, tabs, d_blob, crc_hdr,
+                                                               pl.crc_bad);
+    }
+    CHR_CUDA_TRY(cudaGetLastError());
+    if (side) CHR_CUDA_TRY(cudaEventRecord(side->ev[3], side->st));
     {
         CHR_PROF("k_esc_count", st);
         k_esc_count<<<(unsigned)n, 256, 0, st>>>(pl.d_regs, n, d_blob);
@@ -2038,11 +2083,14 @@ static int decode_impl(const uint8_t *d_blob, const chr_dec_region_t *h, int64_t
             k_mask_rest<<<g, 256, 0, st>>>(pl.d_regs, r0, d_out, d_mask, iso);
         }
     CHR_CUDA_TRY(cudaGetLastError());
-    CHR_CUDA_TRY(d2h(pl.regs.data(), pl.d_regs, sizeof(DecReg) * n, st));
+    if (side) CHR_CUDA_TRY(cudaStreamWaitEvent(st, side->ev[3], 0));
+    std::vector<int32_t> crc_bad((size_t)n);
+    CHR_CUDA_TRY(d2h_multi({{pl.regs.data(), pl.d_regs, sizeof(DecReg) * n},
+                            {crc_bad.data(), pl.crc_bad, sizeof(int32_t) * n}}, st));
     CHR_CUDA_TRY(stream_sync(st));
     int status = CHR_OK;
     for (int64_t i = 0; i < n; ++i) {
-        const uint32_t err = pl.regs[i].err;
+        const uint32_t err = pl.regs[i].err | (crc_bad[i] ? (uint32_t)EF_CRC : 0u);
         int code = CHR_DEC_OK;
         if (err) {
             code = __builtin_ctz(err);

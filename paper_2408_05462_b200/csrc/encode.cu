@@ -521,6 +521,12 @@ __global__ void __launch_bounds__(E2_WARPS * 32) k_emit_q2(const T *__restrict__
     // staging index = byte address mod 4 + offset: word k of the stage is an
     // aligned word of the archive, for the lanes' packed stores and the copy-out
     const int base = (int)((uintptr_t)gdst & 3);
+    if (staged) {  // the lanes OR their words into a zeroed stage (edge words are shared)
+        const int nw = (base + (int)(off_end - off0) + 3) >> 2;
+        uint32_t *sw = reinterpret_cast<uint32_t *>(sbuf);
+        for (int j = lane; j < nw; j += 32) sw[j] = 0;
+        __syncwarp();
+    }
     if (have) {
         const PieceOff po = poffs[R.piece_base + lp];
         const int64_t s0 = lp * TX;
@@ -605,9 +611,84 @@ __global__ void __launch_bounds__(E2_WARPS * 32) k_emit_q2(const T *__restrict__
             }
             return pos;
         };
+        // staged: a lean packer -- every word leaves by a shared atomicOr, so
+        // a lane needs no byte stores for the words it shares with its
+        // neighbours (acc starts with p0 & 3 zero bytes)
+        auto emit_smem = [&]() -> int64_t {
+            uint32_t *sw = reinterpret_cast<uint32_t *>(sbuf);
+            int pw = (int)(p0 >> 2);
+            uint64_t acc = 0;
+            int n = (int)(p0 & 3);
+            auto add = [&](uint64_t v, int len) {  // n <= 3 on entry, len <= 5
+                acc |= v << (8 * n);
+                n += len;
+                if (n >= 4) {
+                    atomicOr(sw + pw, (uint32_t)acc);
+                    acc >>= 32;
+                    n -= 4;
+                    ++pw;
+                }
+                if (n >= 4) {
+                    atomicOr(sw + pw, (uint32_t)acc);
+                    acc >>= 32;
+                    n -= 4;
+                    ++pw;
+                }
+            };
+            auto leb = [](uint64_t u, int &len) {  // u < 2^35: LEB128 bytes, low byte first
+                len = 1 + (u >= (1ull << 7)) + (u >= (1ull << 14)) + (u >= (1ull << 21)) + (u >= (1ull << 28));
+                const uint64_t v = (u & 0x7Full) | ((u & 0x3F80ull) << 1) | ((u & 0x1FC000ull) << 2) |
+                                   ((u & 0xFE00000ull) << 3) | ((u & 0x7F0000000ull) << 4);
+                return v | (0x80808080ull & ((1ull << (8 * (len - 1))) - 1));
+            };
+            auto runs = [&](int64_t L) {  // the zero-run token before a literal (or the stream end)
+                if (L == 1) {
+                    add(1, 1);
+                } else if (L >= 2) {
+                    int len;
+                    const uint64_t v = leb((uint64_t)L, len);
+                    if (len <= 3) {
+                        add(v << 8, len + 1);  // the 0x00 marker and the length in one add
+                    } else {
+                        add(0, 1);
+                        add(v, len);
+                    }
+                }
+            };
+            auto step = [&](uint32_t z) {
+                if (z != 1u) {
+                    if (run) runs(run);
+                    run = 0;
+                    // LEB128 of a 32-bit token value in 32-bit ops: 7-bit groups
+                    // spread to bytes, continuation bits on all but the last
+                    const int len = vlen32(z);
+                    const uint32_t lo = (z & 0x7Fu) | ((z << 1) & 0x7F00u) | ((z << 2) & 0x7F0000u) |
+                                        ((z << 3) & 0x7F000000u);
+                    const uint32_t cont = __funnelshift_rc(0x80808080u, 0u, 8 * (5 - len));
+                    add(((uint64_t)(z >> 28) << 32) | (lo | cont), len);
+                } else {
+                    ++run;
+                }
+            };
+            if (vcount == TX) {
+                const uint4 *q4 = reinterpret_cast<const uint4 *>(q);
+#pragma unroll 2
+                for (int k = 0; k < TX / 4; ++k) {
+                    const uint4 v = __ldg(q4 + k);
+                    step(v.x);
+                    step(v.y);
+                    step(v.z);
+                    step(v.w);
+                }
+            } else {
+                for (int i = 0; i < vcount; ++i) step(__ldg(q + i));
+            }
+            if (R.last && lp == R.npieces - 1) runs(run);  // the window's final zero run
+            if (n > 0) atomicOr(sw + pw, (uint32_t)acc);
+            return 4 * (int64_t)pw + n;
+        };
         if (staged) {
-            cur_end = emit([&](int64_t i, uint8_t v) { sbuf[i] = v; },
-                           [&](int64_t i, uint32_t v) { *reinterpret_cast<uint32_t *>(sbuf + i) = v; });
+            cur_end = emit_smem();
         } else {
             uint8_t *g = gdst - base;  // 4-aligned
             cur_end = emit([&](int64_t i, uint8_t v) { g[i] = v; },
@@ -1532,7 +1613,7 @@ struct EncPlan {
     bool segmode = false;   // single-read segment path (k_qseg / k_qemit)
     int span_cap = 0;       // segment path: max band-plane slots (multiple of 32)
     PieceRec2 *recs2 = nullptr;  // segment path: piece summaries (k_qseg)
-    size_t ws_bytes = 0;
+    size_t ws_bytes = 0, keep_bytes = 0;
     // carved pointers
     EncParams *params;
     RegDev *d_regs;
@@ -1680,13 +1761,17 @@ static bool build_plan(const chr_region_t *h, int64_t nreg, EncPlan &pl, bool al
 static void carve(EncPlan &pl, void *base, size_t cap) {
     WsCarver c{reinterpret_cast<char *>(base), 0, cap};
     const int64_t nreg = (int64_t)pl.regs.size();
+    // what the CRC tail (crc_launch, k_finalize_*) reads comes first: a
+    // caller overlapping that tail reuses the workspace past keep_bytes
     pl.params = c.take<EncParams>(1);
     pl.d_regs = c.take<RegDev>(nreg);
+    pl.segs = c.take<CrcSeg>(nreg + 1);
+    pl.seg_raw = c.take<uint32_t>(nreg + 1);
+    pl.scal = c.take<EncScalars>(1);
+    pl.keep_bytes = (c.off + 255) & ~size_t(255);
     pl.recs = c.take<PieceRec>(pl.segmode ? 0 : pl.npieces_total);
     pl.poffs = c.take<PieceOff>(pl.npieces_total);
     pl.chunk = c.take<TokSeg>(pl.nchunks);
-    pl.segs = c.take<CrcSeg>(nreg + 1);
-    pl.seg_raw = c.take<uint32_t>(nreg + 1);
     pl.codec2 = c.take<int32_t>(nreg);
     pl.item_reg = c.take<int32_t>(pl.nitems + 1);
     pl.chunk_reg = c.take<int32_t>(pl.nchunks + 1);
@@ -1695,7 +1780,6 @@ static void carve(EncPlan &pl, void *base, size_t cap) {
         pl.recs2 = c.take<PieceRec2>(pl.npieces_total);
     }
     pl.escbits = c.take<uint32_t>(pl.etotal + 2);
-    pl.scal = c.take<EncScalars>(1);
     pl.ws_bytes = c.off + 256;
 }
 
@@ -1739,18 +1823,56 @@ extern "C" int chr_compress(const void *d_vol, int dtype, int src_dtype, int64_t
                          write_file, 0, 1.0, d_ws, ws_bytes, d_out, out_cap, h_out_nbytes, stream);
 }
 
+static int compress_impl(const void *d_vol, int dtype, int src_dtype, int64_t nx, int64_t ny, int64_t nz,
+                         const double *spacing, int64_t bs, double vmin, double vmax, const double *h_cands, int m,
+                         chr_region_t *h_regions, int64_t nreg, int write_file, int bound_mode, double accuracy,
+                         void *d_ws, size_t ws_bytes, uint8_t *d_out, uint64_t out_cap, uint64_t *h_out_nbytes,
+                         Side *side, size_t *keep_bytes, void **d_regs_out, cudaStream_t st);
+
 extern "C" int chr_compress2(const void *d_vol, int dtype, int src_dtype, int64_t nx, int64_t ny, int64_t nz,
                              const double *spacing, int64_t bs, double vmin, double vmax, const double *h_cands,
                              int m, chr_region_t *h_regions, int64_t nreg, int write_file, int bound_mode,
                              double accuracy, void *d_ws, size_t ws_bytes, uint8_t *d_out, uint64_t out_cap,
                              uint64_t *h_out_nbytes, void *stream) {
     CHR_XFER_SCOPE;
+    return compress_impl(d_vol, dtype, src_dtype, nx, ny, nz, spacing, bs, vmin, vmax, h_cands, m, h_regions, nreg,
+                         write_file, bound_mode, accuracy, d_ws, ws_bytes, d_out, out_cap, h_out_nbytes, nullptr,
+                         nullptr, nullptr, (cudaStream_t)stream);
+}
+
+namespace chr {
+int compress_with_side(const void *d_vol, int dtype, int src_dtype, int64_t nx, int64_t ny, int64_t nz,
+                       const double *spacing, int64_t bs, double vmin, double vmax, const double *h_cands, int m,
+                       chr_region_t *h_regions, int64_t nreg, void *d_ws, size_t ws_bytes, uint8_t *d_out,
+                       uint64_t out_cap, uint64_t *h_out_nbytes, Side *side, size_t *keep_bytes, void **d_regs,
+                       cudaStream_t st) {
+    return compress_impl(d_vol, dtype, src_dtype, nx, ny, nz, spacing, bs, vmin, vmax, h_cands, m, h_regions, nreg, 1,
+                         0, 1.0, d_ws, ws_bytes, d_out, out_cap, h_out_nbytes, side, keep_bytes, d_regs, st);
+}
+
+__global__ void k_crc_out(const RegDev *__restrict__ regs, int64_t nreg, uint32_t *__restrict__ crc) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r < nreg) crc[r] = regs[r].crc;
+}
+
+int compress_crcs(const void *d_regs, int64_t nreg, uint32_t *d_crc, cudaStream_t st) {
+    if (nreg < 1) return CHR_OK;
+    CHR_PROF("k_crc_out", st);
+    k_crc_out<<<(unsigned)ceil_div(nreg, 256), 256, 0, st>>>(reinterpret_cast<const RegDev *>(d_regs), nreg, d_crc);
+    return cudaGetLastError() == cudaSuccess ? CHR_OK : CHR_E_CUDA;
+}
+}  // namespace chr
+
+static int compress_impl(const void *d_vol, int dtype, int src_dtype, int64_t nx, int64_t ny, int64_t nz,
+                         const double *spacing, int64_t bs, double vmin, double vmax, const double *h_cands, int m,
+                         chr_region_t *h_regions, int64_t nreg, int write_file, int bound_mode, double accuracy,
+                         void *d_ws, size_t ws_bytes, uint8_t *d_out, uint64_t out_cap, uint64_t *h_out_nbytes,
+                         Side *side, size_t *keep_bytes, void **d_regs_out, cudaStream_t st) {
     if (bound_mode < 0 || bound_mode > 1 || !(accuracy > 0.0 && accuracy <= 1.0)) return CHR_E_PARAMETER;
     if (!d_vol || !h_regions || nreg < 1 || !d_out || !h_out_nbytes) return CHR_E_PARAMETER;
     if (dtype != CHR_F32 && dtype != CHR_F64) return CHR_E_PARAMETER;
     if (src_dtype != CHR_F32 && src_dtype != CHR_F64) return CHR_E_PARAMETER;
     if (write_file && (m < 1 || m > 64 || !h_cands || !spacing)) return CHR_E_PARAMETER;
-    cudaStream_t st = (cudaStream_t)stream;
     EncPlan pl;
     if (!build_plan(h_regions, nreg, pl)) return CHR_E_PARAMETER;
     for (const RegDev &R : pl.regs)
@@ -1892,30 +2014,45 @@ extern "C" int chr_compress2(const void *d_vol, int dtype, int src_dtype, int64_
             k_write_table<<<(unsigned)ceil_div(nreg, 256), 256, 0, st>>>(pl.params, pl.d_regs, d_out);
         }
     CHR_CUDA_TRY(cudaGetLastError());
+    // the host needs the layout (codecs, offsets, lengths: known since
+    // k_layout), not the CRCs: with a side stream the CRC tail runs there
+    EncScalars hs;
+    if (side) CHR_CUDA_TRY(d2h_multi({{pl.regs.data(), pl.d_regs, sizeof(RegDev) * nreg}, {&hs, pl.scal, sizeof(hs)}}, st));
+    cudaStream_t ct = st;
+    if (side) {
+        CHR_CUDA_TRY(cudaEventRecord(side->ev[0], st));
+        CHR_CUDA_TRY(cudaStreamWaitEvent(side->st, side->ev[0], 0));
+        ct = side->st;
+    }
     // CRC segments: the superchunk total lives on the device; a persistent
     // grid strides over it (no host round trip)
-    EncScalars hs;
     const int64_t nseg = nreg + (write_file ? 1 : 0);
-    int rc = crc_launch(d_out, pl.segs, nseg, 0, pl.seg_raw, st);
+    int rc = crc_launch(d_out, pl.segs, nseg, 0, pl.seg_raw, ct);
     if (rc) return rc;
     {
-        CHR_PROF("k_finalize_regions", st);
-        k_finalize_regions<<<(unsigned)ceil_div(nreg, 4), 128, 0, st>>>(pl.params, pl.d_regs, pl.seg_raw,
+        CHR_PROF("k_finalize_regions", ct);
+        k_finalize_regions<<<(unsigned)ceil_div(nreg, 4), 128, 0, ct>>>(pl.params, pl.d_regs, pl.seg_raw,
                                                                           tabs, pl.scal, d_out);
     }
     if (write_file)
     {
-        CHR_PROF("k_finalize_file", st);
-            k_finalize_file<<<1, 1, 0, st>>>(tabs, pl.scal, d_out);
+        CHR_PROF("k_finalize_file", ct);
+            k_finalize_file<<<1, 1, 0, ct>>>(tabs, pl.scal, d_out);
     }
     CHR_CUDA_TRY(cudaGetLastError());
-    CHR_CUDA_TRY(d2h_multi({{pl.regs.data(), pl.d_regs, sizeof(RegDev) * nreg}, {&hs, pl.scal, sizeof(hs)}}, st));
+    if (side) {
+        CHR_CUDA_TRY(cudaEventRecord(side->ev[1], side->st));
+        if (keep_bytes) *keep_bytes = pl.keep_bytes;
+        if (d_regs_out) *d_regs_out = pl.d_regs;
+    } else {
+        CHR_CUDA_TRY(d2h_multi({{pl.regs.data(), pl.d_regs, sizeof(RegDev) * nreg}, {&hs, pl.scal, sizeof(hs)}}, st));
+    }
     CHR_CUDA_TRY(stream_sync(st));
     for (int64_t r = 0; r < nreg; ++r) {
         const RegDev &R = pl.regs[r];
         chr_region_t &o = h_regions[r];
         o.codec_id = R.codec;
-        o.payload_crc = R.crc;
+        o.payload_crc = side ? 0u : R.crc;  // side: compress_crcs() after side->ev[1]
         o.block_offset = R.block_off;
         o.block_nbytes = kBlockHeader + (uint64_t)R.payload_len;
         o.n_escaped = (uint64_t)R.nesc;

@@ -82,13 +82,42 @@ extern "C" int chr_pipeline(const void *d_vol, int dtype, int src_dtype, int64_t
         h_res->ws_needed = std::max(cws, stats_bytes);
         return CHR_E_WORKSPACE;
     }
+    // The CRC tail of the compress (payload CRCs, block headers, trailer)
+    // runs on a side stream, overlapping the request; the decoder takes the
+    // expected payload CRCs from the block headers and joins the side stream
+    // before its status read-back.  The tail's control arrays stay at the
+    // front of the workspace (keep), the windows start after them.
+    Side *side = side_stream();
     uint64_t nbytes = 0;
-    rc = chr_compress2(d_vol, dtype, src_dtype, nx, ny, nz, spacing, bs, vmin, vmax, h_cands, m, h_regions, nreg, 1, 0,
-                       1.0, d_ws, ws_bytes, d_archive, archive_cap, &nbytes, stream);
+    size_t keep = 0;
+    void *enc_regs = nullptr;
+    if (side) {
+        rc = compress_with_side(d_vol, dtype, src_dtype, nx, ny, nz, spacing, bs, vmin, vmax, h_cands, m, h_regions,
+                                nreg, d_ws, ws_bytes, d_archive, archive_cap, &nbytes, side, &keep, &enc_regs, st);
+    } else {
+        rc = chr_compress2(d_vol, dtype, src_dtype, nx, ny, nz, spacing, bs, vmin, vmax, h_cands, m, h_regions, nreg,
+                           1, 0, 1.0, d_ws, ws_bytes, d_archive, archive_cap, &nbytes, stream);
+    }
     if (rc) return rc;
     h_res->archive_nbytes = nbytes;
     CHR_CUDA_TRY(mark(1));
-    if (after_compress) after_compress(nbytes, user);  // e.g. start the archive's device->host copy
+    if (after_compress) {  // e.g. start the archive's device->host copy: the archive must be final
+        if (side) CHR_CUDA_TRY(cudaStreamWaitEvent(st, side->ev[1], 0));
+        after_compress(nbytes, user);
+    }
+    // the finished payload CRCs go back into h_regions at the next sync
+    const size_t crc_off = al(keep), pre = side ? al(crc_off + sizeof(uint32_t) * (size_t)(nreg + 1)) : 0;
+    uint32_t *d_crc = reinterpret_cast<uint32_t *>(ws + crc_off);
+    std::vector<uint32_t> hcrc(side ? (size_t)nreg : 0);
+    auto fetch_crcs = [&]() -> int {  // after the decoder joined the side stream (or after waiting here)
+        if (!side) return CHR_OK;
+        int r2 = compress_crcs(enc_regs, nreg, d_crc, st);
+        if (r2) return r2;
+        return d2h(hcrc.data(), d_crc, sizeof(uint32_t) * (size_t)nreg, st) == cudaSuccess ? CHR_OK : CHR_E_CUDA;
+    };
+    auto store_crcs = [&]() {
+        for (int64_t r = 0; r < (int64_t)hcrc.size(); ++r) h_regions[r].payload_crc = hcrc[r];
+    };
 
     // ---- request(k): decode the selected windows (+ inside masks)
     std::vector<chr_dec_region_t> dec((size_t)nreg);
@@ -100,6 +129,11 @@ extern "C" int chr_pipeline(const void *d_vol, int dtype, int src_dtype, int64_t
     h_res->n_selected = ns;
     h_res->window_samples = total;
     if (ns == 0) {
+        if (side) CHR_CUDA_TRY(cudaStreamWaitEvent(st, side->ev[1], 0));
+        rc = fetch_crcs();
+        if (rc) return rc;
+        CHR_CUDA_TRY(stream_sync(st));
+        store_crcs();
         CHR_CUDA_TRY(mark(2));
         CHR_CUDA_TRY(mark(3));
         return CHR_OK;
@@ -110,29 +144,32 @@ extern "C" int chr_pipeline(const void *d_vol, int dtype, int src_dtype, int64_t
     const uint64_t mw = chr_mask_words(dims3.data(), ns);
     const size_t win_bytes = al(total * sizeof(double) + 16), mask_bytes = al((mw + 8) * sizeof(uint32_t));
     const size_t dws = chr_decode_workspace_size(dec.data(), ns), mws = chr_mc_workspace_size(mcg.data(), ns);
-    const size_t need = win_bytes + mask_bytes + std::max(dws, mws);
+    const size_t need = pre + win_bytes + mask_bytes + std::max(dws, mws);
     if (ws_bytes < need) {
         h_res->ws_needed = std::max(need, cws);
         return CHR_E_WORKSPACE;
     }
-    double *d_win = reinterpret_cast<double *>(ws);
-    uint32_t *d_masks = reinterpret_cast<uint32_t *>(ws + win_bytes);
-    char *tail = ws + win_bytes + mask_bytes;
-    const size_t tail_bytes = ws_bytes - win_bytes - mask_bytes;
-    h_res->windows_offset = 0;
-    h_res->masks_offset = win_bytes;
+    double *d_win = reinterpret_cast<double *>(ws + pre);
+    uint32_t *d_masks = reinterpret_cast<uint32_t *>(ws + pre + win_bytes);
+    char *tail = ws + pre + win_bytes + mask_bytes;
+    const size_t tail_bytes = ws_bytes - pre - win_bytes - mask_bytes;
+    h_res->windows_offset = pre;
+    h_res->masks_offset = pre + win_bytes;
     std::vector<int32_t> status((size_t)ns);
     const double iso = h_cands[k_index];
-    rc = chr_decode_regions_mask(d_archive, dec.data(), ns, d_win, tail, tail_bytes, status.data(), iso, d_masks,
-                                 stream);
+    rc = decode_mask_hdrcrc(d_archive, dec.data(), ns, d_win, tail, tail_bytes, status.data(), iso, d_masks, st);
     if (rc) return rc;
     CHR_CUDA_TRY(mark(2));
+    if (side) CHR_CUDA_TRY(cudaStreamWaitEvent(st, side->ev[1], 0));  // (the decoder already joined it)
+    rc = fetch_crcs();  // delivered by the marching-cubes count's sync
+    if (rc) return rc;
 
     // ---- marching cubes on the windows (masks from the decoder)
     int64_t ntri = 0, nvert = 0;
     rc = chr_mc_count_masked(d_win, mcg.data(), ns, iso, d_masks, tail, tail_bytes, nullptr, nullptr, &ntri, &nvert,
                              stream);
     if (rc) return rc;
+    store_crcs();
     h_res->n_tri = ntri;
     h_res->n_vert = nvert;
     if (ntri > tris_cap || nvert > verts_cap || (ntri && (!d_tris || !d_verts))) {

@@ -8,6 +8,7 @@
 // destination at the next chr::stream_sync() of that stream.  Transfers
 // above kXferBig keep cudaMemcpyAsync.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -275,6 +276,28 @@ cudaError_t stream_sync(cudaStream_t st) {
         R.head = 0;
     }
     return cudaSuccess;
+}
+
+Side *side_stream() {
+    static const bool off = [] {
+        const char *e = std::getenv("CHR_NO_SIDE");
+        return e && e[0] == '1';
+    }();
+    if (off) return nullptr;
+    constexpr int kMaxDev = 64;
+    thread_local Side sides[kMaxDev];
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) return nullptr;
+    Side &S = sides[dev];
+    if (!S.st) {
+        if (cudaStreamCreateWithFlags(&S.st, cudaStreamNonBlocking) != cudaSuccess) {
+            S.st = nullptr;
+            return nullptr;
+        }
+        for (cudaEvent_t &e : S.ev)
+            if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+    }
+    return &S;
 }
 
 XferScope::XferScope() : mark_(g_ring.pend.size()) {}
