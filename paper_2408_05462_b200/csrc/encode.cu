@@ -30,6 +30,7 @@
 // once per sample (plus the 1/8 + 1/64 + 1/16 halo).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -38,7 +39,8 @@
 namespace chr {
 
 constexpr int TX = 64, TY = 8, ZC = 16, NW = TY + 1;
-constexpr int QB_T = 256, QB_SPT = 4, QB_CAP = QB_T * QB_SPT;  // k_quant_band: threads, slots, samples
+constexpr int QB_T = 320, QB_SPT = 4, QB_CAP = QB_T * QB_SPT;  // k_quant_band: threads, slots, samples
+constexpr int QB_ZMAX = 33;  // k_quant_band: planes per item at most (balanced chunks)
 constexpr int CSPLIT = 4;  // k_summarize2 CTAs per scan chunk
 constexpr int64_t CH = 1024;  // pieces per scan chunk
 
@@ -59,7 +61,7 @@ struct RegDev {
     int32_t zhalo, last;
     TokSeg pre;
     int32_t qband, rb;            // quantiser items are full-row bands of rb rows (k_quant_band)
-    int32_t zl, pad_zl;           // segment path: planes per item (k_qseg / k_qemit)
+    int32_t zl, qzch;             // planes per item: segment path (k_qseg / k_qemit) / k_quant_band
     // results
     int32_t codec, f32ok;
     int64_t tok_len, nesc, payload_len;
@@ -281,12 +283,17 @@ __global__ void __launch_bounds__(NW * 32, 4) k_quant(const T *__restrict__ vol,
 // x 16 planes of one window, the band-plane's samples flattened over the
 // threads (QB_SPT slots each) so narrow windows (33 = 32k+1 columns) keep
 // every lane busy; D(z) = u(z) - u(z-1) per slot, q from the band-plane's D
-// in shared memory (x-1 = slot i-1, y-1 = slot i-ex).
+// in shared memory.  Slot i = row yy (0 = halo) * ex + x; its volume offset
+// (yy * NX + x), its window offset (i, from row y0-1 of the plane) and its
+// shared index (a zero column at x = -1: yy * (ex+1) + x + 1, so the x-1 /
+// y-1 / (x-1, y-1) neighbours need no edge selects) are 32-bit and fixed;
+// only the per-plane base pointers move.
+constexpr int QB_SD = 2 * QB_CAP + 64;  // padded band-plane: (rows + 1) * (ex + 1) <= 2 * QB_CAP
 template <typename T>
-__global__ void __launch_bounds__(QB_T, 4) k_quant_band(const T *__restrict__ vol, const EncParams *__restrict__ P,
+__global__ void __launch_bounds__(QB_T, 3) k_quant_band(const T *__restrict__ vol, const EncParams *__restrict__ P,
                                                     RegDev *__restrict__ regs, const int32_t *__restrict__ item_reg,
                                                     uint32_t *__restrict__ qz, uint32_t *__restrict__ escbits) {
-    __shared__ int32_t sD[2][QB_CAP];
+    __shared__ int32_t sD[2][QB_SD];
     __shared__ RegDev R;
     const int64_t item = blockIdx.x;
     const int ri = __ldg(item_reg + item);
@@ -297,82 +304,92 @@ __global__ void __launch_bounds__(QB_T, 4) k_quant_band(const T *__restrict__ vo
     const int64_t local = item - R.item_base;
     const int yt = (int)(local % R.nty), zc = (int)(local / R.nty);
     const int ex = R.ex, y0 = yt * R.rb, rows = min(R.rb, R.ey - y0);
-    const int z0 = zc * ZC, z1 = min(z0 + ZC, R.ez);
+    const int z0 = zc * R.qzch, z1 = min(z0 + R.qzch, R.ez);
     const int span = (rows + 1) * ex;  // halo row first
     const bool quant = R.mode == 0;
     const Quant Q = make_quant(R.e);
     const bool chk32 = sizeof(T) == 8 && P->src_dtype == CHR_F32;
     const int tid = threadIdx.x;
-    int xs[QB_SPT], ys[QB_SPT];
-    bool ok[QB_SPT], own[QB_SPT];
-    const T *ptr[QB_SPT];
+    int voff[QB_SPT], sj[QB_SPT];
+    unsigned okm = 0, ownm = 0;  // slot bits: a sample of the window / an own (non-halo) sample
 #pragma unroll
     for (int k = 0; k < QB_SPT; ++k) {
         const int i = tid + QB_T * k;
-        const int yy = i / ex;
-        xs[k] = i - yy * ex;
-        ys[k] = y0 - 1 + yy;
-        ok[k] = i < span && ys[k] >= 0;
-        own[k] = i < span && yy >= 1;
-        ptr[k] = vol + ((int64_t)(R.oz + z0) * NY + (R.oy + (ok[k] ? ys[k] : 0))) * NX + R.ox + xs[k];
+        const int yy = i / ex, x = i - yy * ex;
+        voff[k] = yy * (int)NX + x;
+        sj[k] = yy * (ex + 1) + x + 1;
+        if (i < span && y0 - 1 + yy >= 0) okm |= 1u << k;
+        if (i < span && yy >= 1) ownm |= 1u << k;
     }
+    // zero columns (x = -1) of both buffers; slots never write them
+    for (int t = tid; t <= rows; t += QB_T) {
+        sD[0][t * (ex + 1)] = 0;
+        sD[1][t * (ex + 1)] = 0;
+    }
+    // row y0-1 of plane z: slot offsets are added to these
+    const T *vrow = vol + ((int64_t)(R.oz + z0) * NY + (R.oy + y0 - 1)) * NX + R.ox;
+    const int64_t plane_w = (int64_t)ex * R.ey;
+    uint32_t *qrow = qz + R.q_base + (int64_t)z0 * plane_w + (int64_t)(y0 - 1) * ex;
     int32_t up[QB_SPT];
 #pragma unroll
     for (int k = 0; k < QB_SPT; ++k) up[k] = 0;
-    auto quant_slots = [&](const T (&v)[QB_SPT], int32_t (&u)[QB_SPT], bool (&e)[QB_SPT]) {
+    // returns the slots' escape bits (only the exact sequence escapes)
+    auto quant_slots = [&](const T (&v)[QB_SPT], int32_t (&u)[QB_SPT]) -> unsigned {
         bool fast = true;
 #pragma unroll
         for (int k = 0; k < QB_SPT; ++k) {
             u[k] = 0;
-            e[k] = false;
-            if (ok[k] && quant) fast &= quant_fast(Q, (double)v[k], u[k]);
+            if (((okm >> k) & 1u) && quant) fast &= quant_fast(Q, (double)v[k], u[k]);
         }
+        unsigned em = 0;
         if (__any_sync(0xFFFFFFFFu, !fast)) {  // rare: ties, escapes, tiny e
 #pragma unroll
             for (int k = 0; k < QB_SPT; ++k)
-                if (ok[k] && quant) u[k] = quantize(Q, (double)v[k], e[k]);
+                if (((okm >> k) & 1u) && quant) {
+                    bool e = false;
+                    u[k] = quantize(Q, (double)v[k], e);
+                    em |= e ? 1u << k : 0u;
+                }
         }
+        return em;
     };
     if (quant && (z0 > 0 || R.zhalo)) {  // u at the plane before (inside the window)
         T v[QB_SPT];
-        bool e[QB_SPT];
 #pragma unroll
-        for (int k = 0; k < QB_SPT; ++k) v[k] = ok[k] ? __ldg(ptr[k] - plane) : (T)0;
-        quant_slots(v, up, e);
+        for (int k = 0; k < QB_SPT; ++k) v[k] = ((okm >> k) & 1u) ? __ldg(vrow - plane + voff[k]) : (T)0;
+        quant_slots(v, up);
     }
     T nv[QB_SPT];
 #pragma unroll
-    for (int k = 0; k < QB_SPT; ++k) nv[k] = (ok[k] && z0 < z1) ? __ldg(ptr[k]) : (T)0;
+    for (int k = 0; k < QB_SPT; ++k) nv[k] = (((okm >> k) & 1u) && z0 < z1) ? __ldg(vrow + voff[k]) : (T)0;
     bool inexact = false;
-    for (int z = z0; z < z1; ++z) {
+    for (int z = z0; z < z1; ++z, vrow += plane, qrow += plane_w) {
         T v[QB_SPT];
+        const bool more = z + 1 < z1;
 #pragma unroll
         for (int k = 0; k < QB_SPT; ++k) {
             v[k] = nv[k];
-            ptr[k] += plane;
-            nv[k] = (ok[k] && z + 1 < z1) ? __ldg(ptr[k]) : (T)0;  // prefetch the next plane
+            nv[k] = (((okm >> k) & 1u) && more) ? __ldg(vrow + plane + voff[k]) : (T)0;  // prefetch the next plane
         }
         int32_t u[QB_SPT];
-        bool e[QB_SPT];
-        quant_slots(v, u, e);
+        const unsigned em = quant_slots(v, u);
         int32_t *D = sD[z & 1];
 #pragma unroll
         for (int k = 0; k < QB_SPT; ++k) {
-            const int i = tid + QB_T * k;
-            if (i < span) D[i] = u[k] - up[k];  // invalid slots: 0 - 0
+            if (tid + QB_T * k < span) D[sj[k]] = u[k] - up[k];  // invalid slots: 0 - 0
             up[k] = u[k];
         }
         __syncthreads();
-        const int64_t zrow = (int64_t)z * R.ey;
+        const int rs = ex + 1;
 #pragma unroll
         for (int k = 0; k < QB_SPT; ++k) {
-            if (!own[k]) continue;
+            if (!((ownm >> k) & 1u)) continue;
+            const int j = sj[k];
+            const int32_t q = D[j] - D[j - 1] - D[j - rs] + D[j - rs - 1];
             const int i = tid + QB_T * k;
-            const int x = xs[k];
-            const int32_t q = D[i] - (x > 0 ? D[i - 1] : 0) - D[i - ex] + (x > 0 ? D[i - ex - 1] : 0);
-            const int64_t s = (zrow + ys[k]) * ex + x;  // window raster index
-            qz[R.q_base + s] = zz1_32(q);
-            if (e[k]) {
+            qrow[i] = zz1_32(q);
+            if ((em >> k) & 1u) {
+                const int64_t s = (int64_t)z * plane_w + (int64_t)(y0 - 1) * ex + i;  // window raster index
                 const int64_t bit = (int64_t)R.ebase * 32 + s;
                 atomicOr(escbits + (bit >> 5), 1u << (bit & 31));
                 atomicOr(&regs[ri].has_esc, 1);
@@ -1650,11 +1667,21 @@ static bool build_plan_uncached(const chr_region_t *h, int64_t nreg, EncPlan &pl
         R.nzc = (int32_t)ceil_div(R.ez, ZC);
         R.qband = 0;
         R.rb = 0;
+        R.qzch = ZC;
         if (R.ex <= QB_CAP / 2) {  // full-row bands: rb rows + the halo row fit one CTA's slots
+            // balanced bands and plane chunks (a 33-row window is one band
+            // of 33 rows, not 30 + 3; 33 planes one chunk, not 16 + 16 + 1)
             R.qband = 1;
-            R.rb = std::max(1, std::min(R.ey, QB_CAP / R.ex - 1));
-            R.ntx = 1;
+            const int rbmax = std::max(1, std::min(R.ey, QB_CAP / R.ex - 1));
+            R.nty = (int32_t)ceil_div(R.ey, rbmax);
+            R.rb = (int32_t)ceil_div(R.ey, R.nty);
             R.nty = (int32_t)ceil_div(R.ey, R.rb);
+            R.ntx = 1;
+            if (R.ez > 0) {  // (an empty z-slab portion has no items)
+                R.nzc = (int32_t)ceil_div(R.ez, QB_ZMAX);
+                R.qzch = (int32_t)ceil_div(R.ez, R.nzc);
+                R.nzc = (int32_t)ceil_div(R.ez, R.qzch);
+            }
         }
         R.item_base = item;
         item += (int64_t)R.ntx * R.nty * R.nzc;
@@ -1952,7 +1979,7 @@ static int compress_impl(const void *d_vol, int dtype, int src_dtype, int64_t nx
             k_quant<double><<<items, NW * 32, 0, st>>>((const double *)d_vol, pl.params, pl.d_regs, pl.item_reg,
                                                        pl.qz, pl.escbits);
             k_quant_band<double><<<items, QB_T, 0, st>>>((const double *)d_vol, pl.params, pl.d_regs,
-                                                         pl.item_reg, pl.qz, pl.escbits);
+                                                            pl.item_reg, pl.qz, pl.escbits);
         }
         {
             CHR_PROF("k_summarize", st);
