@@ -335,8 +335,14 @@ int chr_mc_emit_masked(const double *d_grids, const chr_mc_grid_t *h_grids, int6
  *     a caller pipelines its inputs/outputs.  16-byte aligned pointers. */
 int chr_sm_copy(void *dst, const void *src, uint64_t nbytes, int ctas, void *stream);
 /*     the same for small copies at any alignment (the library's own small
- *     transfers use this path internally, never the copy engines) */
+ *     transfers use this path internally by default) */
 int chr_copy(void *dst, const void *src, uint64_t nbytes, void *stream);
+/*     the library's own small host<->device transfers (plans, sizes, status):
+ *     dma = 0 (default) by kernels through a pinned mapped ring, so they never
+ *     queue behind a caller's bulk copies on the copy engines; dma = 1 on the
+ *     copy engines (cheaper when the caller keeps them idle).  Process-wide;
+ *     returns the previous mode.  Env CHR_XFER=dma sets 1 at load. */
+int chr_set_xfer_mode(int dma);
 
 /* 14. SURVEY 8(f3): stitch + verify_topology on the device.
  *     chr_stitch replaces chr_archive.stitch (chr_archive.py:277-294): the

@@ -47,7 +47,16 @@ __global__ void k_xfer(const uint8_t *__restrict__ src, uint8_t *__restrict__ ds
     }
 }
 
+// small copies through the copy engines (1) or by kernels (0): a caller that
+// keeps the engines busy with bulk transfers wants kernels (the default);
+// CHR_XFER=dma / chr_set_xfer_mode(1) for callers that do not
+int g_xfer_dma = [] {
+    const char *e = std::getenv("CHR_XFER");
+    return e && std::strcmp(e, "dma") == 0 ? 1 : 0;
+}();
+
 cudaError_t launch_xfer(const void *src, void *dst, size_t n, cudaStream_t st) {
+    if (g_xfer_dma) return cudaMemcpyAsync(dst, src, n, cudaMemcpyDefault, st);
     const unsigned blocks = (unsigned)std::min<size_t>(64, (n + 4095) / 4096 + 1);
     CHR_PROF("k_xfer", st);
     k_xfer<<<blocks, 256, 0, st>>>((const uint8_t *)src, (uint8_t *)dst, n);
@@ -118,6 +127,13 @@ __global__ void k_xfer_multi(CopySet set) {
 
 cudaError_t launch_multi(const CopySet &set, int count, size_t most, cudaStream_t st) {
     if (count == 0) return cudaSuccess;
+    if (g_xfer_dma) {
+        for (int i = 0; i < count; ++i) {
+            const cudaError_t e = cudaMemcpyAsync(set.dst[i], set.src[i], set.n[i], cudaMemcpyDefault, st);
+            if (e != cudaSuccess) return e;
+        }
+        return cudaSuccess;
+    }
     const unsigned bx = (unsigned)std::min<size_t>(64, (most + 4095) / 4096 + 1);
     CHR_PROF("k_xfer", st);
     k_xfer_multi<<<dim3(bx, count), 256, 0, st>>>(set);
@@ -311,6 +327,12 @@ using namespace chr;
 
 // copy between device-accessible pointers (device memory or pinned host
 // memory) with a kernel on `stream`: no copy engine, any alignment
+extern "C" int chr_set_xfer_mode(int dma) {
+    const int old = g_xfer_dma;
+    g_xfer_dma = dma ? 1 : 0;
+    return old;
+}
+
 extern "C" int chr_copy(void *dst, const void *src, uint64_t nbytes, void *stream) {
     if (nbytes && (!dst || !src)) return CHR_E_PARAMETER;
     return copy_async(dst, src, nbytes, (cudaStream_t)stream) == cudaSuccess ? CHR_OK : CHR_E_CUDA;
