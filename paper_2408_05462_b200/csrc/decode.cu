@@ -1460,11 +1460,14 @@ __global__ void __launch_bounds__(KBT) k_band(const DecReg *__restrict__ regs, c
         if (pad || b > 0) split(t, yy, xx);
         return pad ? yy * rs + xx : t;
     };
+    // a tile publishes only what its successors read: Fy' (last row, every
+    // plane) when a band below exists, I (last plane) when a chunk follows
+    const bool need_fy = b + 1 < nb, need_i = c + 1 < R.tnz;
     auto publish_col = [&](int t, int64_t fz) {
         int xx;
         const int qi = qidx(t, xx);
         int64_t acc = 0;  // z prefix of the column
-        if (t >= L - ex) {  // last row (xx is the column only when split ran)
+        if (need_fy && t >= L - ex) {  // last row (xx is the column only when split ran)
             const int xl = t - (L - ex);
             myF[xl] = fz;
             for (int j = 0; j < nzv; ++j) {
@@ -1474,7 +1477,7 @@ __global__ void __launch_bounds__(KBT) k_band(const DecReg *__restrict__ regs, c
         } else {
             for (int j = 0; j < nzv; ++j) acc += Q[j * PL + qi];
         }
-        myF[io + t] = acc + (b > 0 ? dF[(nzv - 1) * ex + xx] : 0) + fz;
+        if (need_i) myF[io + t] = acc + (b > 0 ? dF[(nzv - 1) * ex + xx] : 0) + fz;
     };
     const double twoe = 2.0 * R.e;
     const int64_t zstride = (int64_t)ex * ey;
@@ -1513,7 +1516,8 @@ __global__ void __launch_bounds__(KBT) k_band(const DecReg *__restrict__ regs, c
     __syncthreads();
     BAND_TR(5);
     constexpr int FU = 4;  // columns per thread per round: all face loads first
-    for (int t0 = tid; t0 < L; t0 += KBT * FU) {
+    const int tpub = need_i ? 0 : (need_fy ? L - ex : L);  // columns whose faces are read
+    for (int t0 = tpub + tid; t0 < L; t0 += KBT * FU) {
         int64_t fzv[FU];
 #pragma unroll
         for (int k = 0; k < FU; ++k) {
@@ -1526,7 +1530,7 @@ __global__ void __launch_bounds__(KBT) k_band(const DecReg *__restrict__ regs, c
             if (t < L) publish_col(t, fzv[k]);
         }
     }
-    release(2);
+    if (need_fy || need_i) release(2);  // (no successor waits on a tile that publishes nothing)
     BAND_TR(6);
     if (!mask) {
         for (int t = tid; t < L; t += KBT) recon_col(t, c > 0 ? __ldcg(Ip + t) : 0);
@@ -1842,7 +1846,7 @@ static void dec_carve(DecPlan &pl, void *base, size_t cap) {
     pl.ticket = c.take<unsigned long long>(1);
     pl.ticket3 = c.take<unsigned long long>(1);
     pl.any_slow = c.take<int32_t>(2);  // [0] generic path needed, [1] int64 band pass needed
-    pl.ws = c.off + 256;
+    pl.ws = ((c.off + 255) & ~size_t(255)) + 256;
 }
 
 }  // namespace chr

@@ -1807,7 +1807,7 @@ static void carve(EncPlan &pl, void *base, size_t cap) {
         pl.recs2 = c.take<PieceRec2>(pl.npieces_total);
     }
     pl.escbits = c.take<uint32_t>(pl.etotal + 2);
-    pl.ws_bytes = c.off + 256;
+    pl.ws_bytes = ((c.off + 255) & ~size_t(255)) + 256;  // 256-aligned: callers carve past it
 }
 
 }  // namespace chr

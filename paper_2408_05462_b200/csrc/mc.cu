@@ -759,7 +759,7 @@ static void mc_carve(McPlan &pl, void *base, size_t cap) {
     pl.chunk_grid = c.take<int32_t>(pl.nchunks + 1);
     pl.mask_grid = c.take<int32_t>(pl.nmask_items + 1);
     pl.mask = c.take<uint32_t>(pl.nmask_words + 8);  // + slack: 4-word reads past a plane
-    pl.ws = c.off + 256;
+    pl.ws = ((c.off + 255) & ~size_t(255)) + 256;
 }
 
 }  // namespace chr

@@ -1,6 +1,8 @@
 // prof.cu -- opt-in per-kernel timing with CUDA events on the launching
 // stream, plus a launch counter.  Used by bench.py to report the dominant
 // kernel's duration (roofline) and the number of kernels launched.
+#include <cstdio>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <string>
@@ -42,7 +44,20 @@ ProfScope::ProfScope(const char *name, cudaStream_t st) : name_(name), st_(st), 
     }
 }
 
+// CHR_DEBUG_SYNC=1: synchronise after every profiled launch and name the
+// kernel that failed (debugging only: serialises the library)
+static const bool g_debug_sync = [] {
+    const char *e = std::getenv("CHR_DEBUG_SYNC");
+    return e && e[0] == '1';
+}();
+
 ProfScope::~ProfScope() {
+    if (g_debug_sync) {
+        const cudaError_t e = cudaStreamSynchronize(st_);
+        const cudaError_t l = cudaGetLastError();
+        if (e != cudaSuccess || l != cudaSuccess)
+            std::fprintf(stderr, "chr: %s failed: %s / %s\n", name_, cudaGetErrorString(e), cudaGetErrorString(l));
+    }
     if (!a_) return;
     std::lock_guard<std::mutex> lk(g_mu);
     cudaEvent_t b = take_event();

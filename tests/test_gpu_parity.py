@@ -697,3 +697,49 @@ def test_pipeline_one_call_matches_separate_calls(name, n):
     # a second call reuses the negotiated buffers
     p2 = device.pipeline(vals, dims, cands, bs, loose_fraction=r, ws=ws)
     assert torch.equal(p2.tris, t)
+
+
+def test_decode_payload_crc_mismatch_per_region():
+    """Payload CRCs are checked on a side stream while the band decoder runs:
+    a region whose payload bytes were flipped reports the checksum status
+    (before any token error, as decompress() checks the CRC first,
+    codec.py:220-226), an unknown codec with a bad CRC reports the checksum
+    too, and every intact region still decodes bit-identically to the oracle."""
+    import torch
+
+    vals, dims, bs, cands, r = synth.make_config("c2", device="cuda", n=160)
+    res = device.build_archive(vals, dims, cands, bs, loose_fraction=r)
+    regs = res.regions
+    host = res.blob[: res.nbytes].cpu().numpy().tobytes()
+    sel = regs[(regs["mask"] & np.uint64(1)) != 0]
+    assert len(sel) >= 6, len(sel)
+    codec = sel["codec_id"].copy()
+    blob = bytearray(host)
+    hit = [1, 3, len(sel) - 1]  # flip a payload byte in these regions
+    for j in hit:
+        o = int(sel["block_offset"][j]) + device.BLOCK_HEADER
+        ln = int(sel["block_nbytes"][j]) - device.BLOCK_HEADER
+        blob[o + ln // 2] ^= 0x5A
+    codec[4] = 77  # unknown codec, intact CRC
+    dev = torch.tensor(np.frombuffer(bytes(blob), np.uint8), device="cuda")
+    dec = device.dec_table(sel["block_offset"] + device.BLOCK_HEADER, sel["block_nbytes"] - device.BLOCK_HEADER,
+                           codec, sel["extent"], sel["error_bound"], sel["payload_crc"])
+    for iso in (None, cands[0]):
+        wins, offs, st = device.decode(dev, dec, iso=iso)
+        w = wins.cpu().numpy()
+        for j in range(len(sel)):
+            if j in hit:
+                assert st[j] == 7, (j, st[j])  # CHR_DEC_CHECKSUM
+            elif j == 4:
+                assert st[j] == 10, st[j]  # unknown codec
+            else:
+                assert st[j] == 0, (j, st[j])
+                _, ref = O.decompress_block(host, int(sel["block_offset"][j]))
+                assert np.array_equal(w[int(offs[j]): int(offs[j]) + ref.size], ref), j
+    # an unknown codec whose payload CRC is also wrong: the checksum wins
+    codec2 = sel["codec_id"].copy()
+    codec2[hit[0]] = 77
+    dec2 = device.dec_table(sel["block_offset"] + device.BLOCK_HEADER, sel["block_nbytes"] - device.BLOCK_HEADER,
+                            codec2, sel["extent"], sel["error_bound"], sel["payload_crc"])
+    _, _, st2 = device.decode(dev, dec2)
+    assert st2[hit[0]] == 7

@@ -1,9 +1,10 @@
 #!/bin/bash
-# Round-2 GPU evidence run: smoke, bench (ours + reference arm), full gpu tests, ncu launch list + full capture.
-set -x
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/smi.txt
-python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke=$?
-python bench.py > gpurun_out/bench_a.json 2> gpurun_out/bench_a.err; echo bench=$?
-python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo ref=$?
-timeout 2400 python -m pytest tests -m gpu -q -x --durations=25 > gpurun_out/gputest.log 2>&1; echo tests=$?
-bash tools/prof_r02.sh r02a
+# Round-2 GPU evidence run (tag $1): smoke, bench as the driver runs it (ours + reference arm),
+# full gpu tests, ncu launch list + --set full of the top kernels (tools/prof_r02.sh).
+tag=${1:-r02}
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/smi_$tag.txt
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_$tag.log 2>&1; echo smoke=$?
+python bench.py --gpus 1 --steps 20 --warmup 5 > gpurun_out/bench_$tag.json 2> gpurun_out/bench_$tag.err; echo bench=$?
+python bench.py --impl reference --gpus 1 --steps 3 --warmup 3 > gpurun_out/bench_ref_$tag.json 2> gpurun_out/bench_ref_$tag.err; echo ref=$?
+timeout 2400 python -m pytest tests -m gpu -q -x --durations=15 > gpurun_out/gputest_$tag.log 2>&1; echo tests=$? | tee -a gpurun_out/gputest_$tag.log
+bash tools/prof_r02.sh $tag

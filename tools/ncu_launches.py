@@ -29,6 +29,6 @@ print(txt)
 if len(sys.argv) > 2:
     open(sys.argv[2], "w").write(
         f"# ncu launch list (`gpu__time_duration.sum`, --clock-control none, serialised, cold caches)\n\n"
-        f"Source: `{sys.argv[1]}`; {steps} steps (warm-up + timed) of `python bench.py --steps 2 --warmup 1`.\n"
+        f"Source: `{sys.argv[1]}`; {steps} pipeline step(s) captured (`tools/prof_r02.sh`: one warm c3 step of `tools/one_step.py` between cudaProfilerStart/Stop).\n"
         f"Per-launch times are cold-cache and serialised, so compare SHARES with the bench's CUDA-event table.\n\n"
         + txt + "\n")
