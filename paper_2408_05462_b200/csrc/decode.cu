@@ -1032,7 +1032,13 @@ __global__ void __launch_bounds__(256) k_esc_seg(const DecReg *__restrict__ regs
 // k_asum_check).  The z prefix, the faces (u at tile boundaries) and u =
 // prefix + faces are int64, exact like the reference's int64 cumsum.
 using BV = int32_t;
-constexpr int BCAP = 10240;  // samples per tile (40 KB of int32 + 12 KB dF: 4 CTAs per SM)
+#ifndef CHR_BCAP
+#define CHR_BCAP 15360
+#endif
+// samples per tile: the largest that keeps 3 CTAs per SM (60 KB of int32 +
+// 12 KB dF + the segment tables; measured at c3: 10240 -> 1.167 ms,
+// 12288 -> 1.118, 14336 -> 1.100, 15360 -> 1.077, 16384 -> 1.284 at 2 CTAs/SM)
+constexpr int BCAP = CHR_BCAP;
 constexpr int BDF = 1536;
 #ifndef CHR_KBT
 #define CHR_KBT 384
