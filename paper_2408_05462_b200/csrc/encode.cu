@@ -39,8 +39,14 @@
 namespace chr {
 
 constexpr int TX = 64, TY = 8, ZC = 16, NW = TY + 1;
-constexpr int QB_T = 320, QB_SPT = 4, QB_CAP = QB_T * QB_SPT;  // k_quant_band: threads, slots, samples
-constexpr int QB_ZMAX = 33;  // k_quant_band: planes per item at most (balanced chunks)
+#ifndef CHR_QB_T
+#define CHR_QB_T 320
+#endif
+#ifndef CHR_QB_ZMAX
+#define CHR_QB_ZMAX 33
+#endif
+constexpr int QB_T = CHR_QB_T, QB_SPT = 4, QB_CAP = QB_T * QB_SPT;  // k_quant_band: threads, slots, samples
+constexpr int QB_ZMAX = CHR_QB_ZMAX;  // k_quant_band: planes per item at most (balanced chunks)
 constexpr int CSPLIT = 4;  // k_summarize2 CTAs per scan chunk
 constexpr int64_t CH = 1024;  // pieces per scan chunk
 
