@@ -116,7 +116,14 @@ def marching_cubes(samples, spacing=(1.0, 1.0, 1.0), origin=(0.0, 0.0, 0.0), k: 
     """isosurf.marching_cubes (isosurf.py:183-204) on the GPU."""
     t, dims = _grid(samples)
     v, tr, _, _ = device.marching(t, [(0, dims, origin, spacing)], float(k))
-    return TriangleMesh(v.cpu().numpy(), tr.cpu().numpy())
+    return TriangleMesh(_to_host(v), _to_host(tr))
+
+
+def _to_host(t: torch.Tensor) -> np.ndarray:
+    """D2H into page-locked memory (recycled by torch's caching host allocator)."""
+    h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    h.copy_(t)
+    return h.numpy()
 
 
 def extract_device(windows: torch.Tensor, regions, offsets, spacing, k: float):
@@ -132,9 +139,15 @@ def merge_meshes(meshes) -> TriangleMesh:
     meshes = list(meshes)
     if not meshes:
         return TriangleMesh(np.empty((0, 3), np.float64), np.empty((0, 3), np.int32))
-    off = np.cumsum([0] + [m.num_vertices for m in meshes[:-1]])
-    return TriangleMesh(np.concatenate([m.vertices for m in meshes], axis=0),
-                        np.concatenate([m.triangles + o for m, o in zip(meshes, off)], axis=0).astype(np.int32))
+    nt = sum(m.num_triangles for m in meshes)
+    tris = np.empty((nt, 3), np.int32)
+    t0 = v0 = 0
+    for m in meshes:  # one pass: each mesh's triangles + its vertex offset, straight into place
+        n = m.num_triangles
+        np.add(m.triangles, v0, out=tris[t0:t0 + n], casting="unsafe")
+        t0 += n
+        v0 += m.num_vertices
+    return TriangleMesh(np.concatenate([m.vertices for m in meshes], axis=0), tris)
 
 
 def export_obj(mesh: TriangleMesh, path) -> None:
