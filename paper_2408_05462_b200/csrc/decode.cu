@@ -1015,7 +1015,7 @@ __global__ void __launch_bounds__(256) k_esc_seg(const DecReg *__restrict__ regs
 }
 
 // ---- band tiles.  A tile is (full rows x, a band of bty rows y, a chunk of
-// btz planes z) of one region: <= BCAP samples, int32 in shared memory.
+// btz planes z) of one region in SMB bytes of shared memory (int32).
 // Tile-local prefixes along x (rows are whole), y and z give T; then
 //   u(x,y,z) = T + [Fy(x,z) - Fy(x,z0-1)] + Fz(x,y)
 // with Fy = last row of the band above (planes z0-1..z1-1) and Fz = last
@@ -1032,14 +1032,16 @@ __global__ void __launch_bounds__(256) k_esc_seg(const DecReg *__restrict__ regs
 // k_asum_check).  The z prefix, the faces (u at tile boundaries) and u =
 // prefix + faces are int64, exact like the reference's int64 cumsum.
 using BV = int32_t;
-#ifndef CHR_BCAP
-#define CHR_BCAP 15360
+// Dynamic shared memory per band tile (int32 pass): the int32 tile and, for
+// a region with more than one band, its dF (btz x ex int64) behind it.  The
+// largest budget that keeps 3 CTAs per SM next to the ~3 KB of segment
+// tables (72 KB: 18432 int32 samples without dF).  Measured at c3 with a
+// fixed 12 KB dF array beside the tile: 10240 samples -> 1.167 ms, 12288 ->
+// 1.118, 14336 -> 1.100, 15360 -> 1.077, 16384 -> 1.284 (2 CTAs/SM).
+#ifndef CHR_BAND_SMEM
+#define CHR_BAND_SMEM 73728
 #endif
-// samples per tile: the largest that keeps 3 CTAs per SM (60 KB of int32 +
-// 12 KB dF + the segment tables; measured at c3: 10240 -> 1.167 ms,
-// 12288 -> 1.118, 14336 -> 1.100, 15360 -> 1.077, 16384 -> 1.284 at 2 CTAs/SM)
-constexpr int BCAP = CHR_BCAP;
-constexpr int BDF = 1536;
+constexpr int64_t SMB = CHR_BAND_SMEM;
 #ifndef CHR_KBT
 #define CHR_KBT 384
 #endif
@@ -1164,7 +1166,7 @@ __device__ __forceinline__ int64_t band_scatter_unit64(const Win24 &W, int64_t a
 
 // 32-bit path: tokens <= 4 bytes (H = payload of bytes e-3..e in 28 bits),
 // positions in int32 (clamped to 2^30 past L: every position that matters
-// is < L <= BCAP and a segment starts at -skip >= -2^30).  Returns the
+// is < L <= SMB / 4 and a segment starts at -skip >= -2^30).  Returns the
 // position after the unit's tokens.
 template <bool PAD, typename QV>
 __device__ __forceinline__ int band_scatter_unit32(const Win24 &W, int at, int L, int ex, uint64_t M,
@@ -1252,7 +1254,6 @@ __global__ void __launch_bounds__(KBT) k_band(const DecReg *__restrict__ regs, c
                                               unsigned long long *__restrict__ asum_reg) {
     extern __shared__ __align__(16) unsigned char kb_raw[];
     QV *const Q = reinterpret_cast<QV *>(kb_raw);  // [nzv][nyv][rs]
-    __shared__ int64_t ucnt[BDF];                 // dF[nzv][ex]
     __shared__ int64_t s_lo[BSEGM], s_hi[BSEGM], s_ub[BSEGM], s_off[BSEGM];
     __shared__ int32_t s_base[BSEGM + 1];
     __shared__ int64_t s_tile, s_zero;
@@ -1446,7 +1447,8 @@ __global__ void __launch_bounds__(KBT) k_band(const DecReg *__restrict__ regs, c
     // published.
     const int64_t fn = R.face_n;
     const int64_t io = (int64_t)(btz + 1) * ex;
-    int64_t *dF = ucnt;  // [nzv][ex], <= BDF entries
+    // [nzv][ex] behind the tile (band_shape budgets both when a band below exists)
+    int64_t *dF = reinterpret_cast<int64_t *>(kb_raw + (((size_t)nzv * PL * sizeof(QV) + 15) & ~size_t(15)));
     int64_t *myF = faces + R.face_base + local * fn;
     BAND_TR(3);
     if (b > 0) {
@@ -1692,8 +1694,9 @@ static int dec_rows_for(int ex) {
 // wavefront (bands + chunks) stays short
 static bool band_shape(DecReg &R) {
     const int rs = R.ex | 1;
-    if (rs > BCAP) return false;
-    const int K = BCAP / rs;  // rows (y * z) per tile
+    const int64_t rowb = 4ll * rs;  // int32 bytes per tile row
+    if (rowb > SMB) return false;
+    const int64_t K = SMB / rowb;   // rows (y * z) per tile when no dF is needed
     int bty = 0, btz = 0;
     if ((int64_t)R.ey * R.ez <= K && R.ez <= BSEGM) {
         bty = R.ey;
@@ -1703,19 +1706,25 @@ static bool band_shape(DecReg &R) {
         // chains are tny + tnz - 1 hops long (band above, chunk before): pick
         // the shape with the shortest chain, then the fewest tiles
         int64_t best_chain = INT64_MAX, best_tiles = INT64_MAX;
-        for (int tz = 1; tz <= std::min({R.ez, K, BSEGM}); ++tz) {  // chunk depth
-            const int ty2 = std::min(R.ey, K / tz);                     // widest band for it
-            if (ty2 < R.ey && tz > BDF / R.ex) continue;  // a band below exists: its dF (tz x ex) must fit
+        for (int tz = 1; tz <= (int)std::min<int64_t>({(int64_t)R.ez, K, (int64_t)BSEGM}); ++tz) {  // chunk depth
+            int64_t ty2 = std::min<int64_t>(R.ey, K / tz);  // widest band for it
+            if (ty2 < R.ey) {  // bands below exist: their dF (tz x ex int64) shares the budget
+                ty2 = std::min<int64_t>(R.ey, (SMB - 8ll * tz * R.ex) / (rowb * tz));
+                if (ty2 < 1) continue;
+            }
             const int64_t ny = ceil_div(R.ey, ty2), nz = ceil_div(R.ez, tz);
             const int64_t chain = ny + nz - 1, tiles = ny * nz;
             if (chain < best_chain || (chain == best_chain && tiles < best_tiles)) {
                 best_chain = chain;
                 best_tiles = tiles;
-                bty = ty2;
+                bty = (int)ty2;
                 btz = tz;
             }
         }
         if (bty < 1) return false;
+        // the same grid with balanced bands and chunks (33 + 32 rows, not 40 + 25)
+        bty = (int)ceil_div(R.ey, ceil_div(R.ey, bty));
+        btz = (int)ceil_div(R.ez, ceil_div(R.ez, btz));
     }
     R.rs = rs;
     R.bty = bty;
@@ -1995,7 +2004,7 @@ static int decode_impl(const uint8_t *d_blob, const chr_dec_region_t *h, int64_t
             k_tile_order<<<(unsigned)ceil_div(npairs, 256), 256, 0, st>>>(pl.d_regs, pl.pair_base, pl.step_base,
                                                                          npairs, n, pl.order);
         }
-        const int smem = (int)(sizeof(int32_t) * BCAP);
+        const int smem = (int)SMB;
         CHR_CUDA_TRY(cudaFuncSetAttribute(k_band<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
 #ifdef CHR_BAND_TRACE
         unsigned long long *d_tr = nullptr;
@@ -2043,7 +2052,7 @@ static int decode_impl(const uint8_t *d_blob, const chr_dec_region_t *h, int64_t
             CHR_PROF("k_mask_clear", st);
             k_mask_clear<<<dim3(16, (unsigned)std::min<int64_t>(n, 1024)), 256, 0, st>>>(pl.d_regs, n, pl.asum, d_mask);
         }
-        const int smem = (int)(sizeof(int64_t) * BCAP);
+        const int smem = (int)(2 * SMB);  // int64 tile + dF
         CHR_CUDA_TRY(cudaFuncSetAttribute(k_band<int64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         CHR_PROF("k_band64", st);
         k_band<int64_t><<<(unsigned)pl.ntiles, KBT, smem, st>>>(
