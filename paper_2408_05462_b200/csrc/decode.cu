@@ -916,7 +916,16 @@ __global__ void __launch_bounds__(DTHREADS) k_seg_locate(const DecReg *__restric
     pos64[c * DTHREADS + threadIdx.x] = a;  // first sample of the tokens ending in this 64-byte group
     if (cnt == 0) return;
     const int64_t ex = R.ex, plane = ex * R.ey, band = ex * R.bty, nb = R.tny;
-    int64_t z = a / plane, b = (a - z * plane + band - 1) / band;
+    int64_t z, b;
+    if (a < (1ll << 32) && plane < (1ll << 31)) {  // 32-bit divisions (a 64-bit one is a long software routine)
+        const uint32_t a32 = (uint32_t)a, p32 = (uint32_t)plane, b32 = (uint32_t)band;
+        const uint32_t zz = a32 / p32;
+        z = zz;
+        b = (a32 - zz * p32 + b32 - 1) / b32;
+    } else {
+        z = a / plane;
+        b = (a - z * plane + band - 1) / band;
+    }
     if (b >= nb) {
         b = 0;
         ++z;

@@ -490,7 +490,10 @@ __global__ void k_tile_fill_map(const RegDev *__restrict__ regs, int64_t nreg, i
 // replaced took 0.62 ms at c3, this one 0.55 ms).  A range larger than the buffer is written
 // byte by byte from the lanes (rare).  Verbatim regions: the CTA's threads
 // copy the samples of its 128 pieces, coalesced.
-constexpr int E2_WARPS = 4;
+#ifndef CHR_E2_WARPS
+#define CHR_E2_WARPS 4
+#endif
+constexpr int E2_WARPS = CHR_E2_WARPS;
 constexpr int E2_STAGE = 8188;  // bytes per warp (+ up to 3 alignment bytes)
 template <typename T>
 __global__ void __launch_bounds__(E2_WARPS * 32) k_emit_q2(const T *__restrict__ vol, const EncParams *__restrict__ P,

@@ -510,7 +510,10 @@ __global__ void __launch_bounds__(256) k_mc_count4(const McGrid *__restrict__ G,
 // cells), so a cell's triangle offset and vertex base are its piece's bases
 // + its word, and a triangle corner owned by another cell costs that cell's
 // word and its piece's vertex base (two loads) + one rank lookup.
-constexpr int E4W = 8;  // warps per CTA
+#ifndef CHR_E4W
+#define CHR_E4W 8
+#endif
+constexpr int E4W = CHR_E4W;  // warps per CTA
 __global__ void __launch_bounds__(E4W * 32) k_mc_emit4(const double *__restrict__ grids, const McGrid *__restrict__ G,
                                                        const int32_t *__restrict__ chunk_grid, double k,
                                                        const McTables *__restrict__ T,

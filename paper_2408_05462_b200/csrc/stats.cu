@@ -15,6 +15,10 @@
 
 #include "chr_internal.cuh"
 
+#ifndef CHR_STATS_RU
+#define CHR_STATS_RU 4
+#endif
+
 namespace chr {
 
 struct CandParams {
@@ -196,7 +200,7 @@ __global__ void __launch_bounds__(SQ) k_stats_rows(const float *__restrict__ vol
         const bool ghost = ((4 * q) % bs) == 0 && q > 0;
         // RU rows per step: their 16-byte loads are all in flight before any is
         // used (one outstanding load per thread left HBM at ~35 % of peak)
-        constexpr int RU = 4;
+        constexpr int RU = CHR_STATS_RU;
         for (int r0 = g; r0 < nrows; r0 += RU * rg) {
             float4 v4[RU];
             int64_t rowoff[RU];

@@ -8,10 +8,13 @@ SRC=$ROOT/paper_2408_05462_b200/csrc
 OUT=$ROOT/build/variants/$name
 mkdir -p $OUT
 FLAGS="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -fmad=false -Xcompiler -fPIC --expt-relaxed-constexpr"
+rm -f $OUT/*.o
+pids=()
 for f in $SRC/*.cu; do
   nvcc $FLAGS "$@" -c $f -o $OUT/$(basename $f .cu).o &
+  pids+=($!)
 done
 g++ -O2 -fPIC -std=c++17 -ffp-contract=off -c $SRC/plan.cpp -o $OUT/plan.o
-wait
+for p in "${pids[@]}"; do wait $p || { echo "variant $name: compile failed" >&2; exit 1; }; done
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $ROOT/build/variants/$name.so $OUT/*.o -lcudart
 echo built $ROOT/build/variants/$name.so
