@@ -491,7 +491,7 @@ __global__ void k_tile_fill_map(const RegDev *__restrict__ regs, int64_t nreg, i
 // byte by byte from the lanes (rare).  Verbatim regions: the CTA's threads
 // copy the samples of its 128 pieces, coalesced.
 #ifndef CHR_E2_WARPS
-#define CHR_E2_WARPS 4
+#define CHR_E2_WARPS 2
 #endif
 constexpr int E2_WARPS = CHR_E2_WARPS;
 constexpr int E2_STAGE = 8188;  // bytes per warp (+ up to 3 alignment bytes)
