@@ -29,6 +29,7 @@
 // All integer work is int64 like the reference, so even CRC-valid
 // hand-made streams decode bit-identically.
 #include <algorithm>
+#include <memory>
 #include <cstdio>
 #include <cstdlib>
 #include <cmath>
@@ -73,7 +74,7 @@ struct DecReg {
     // fast (canonical-stream) path: band tiles (full rows x bty rows x btz planes)
     int64_t abase;                 // 16-byte aligned chunk origin (blob-relative)
     int32_t tnx, tny, tnz;         // tiles per axis (tnx = 1, tny = bands, tnz = chunks)
-    int32_t doff, pad2;            // step offset of the region's wavefront (k_tile_order)
+    int32_t doff, pad2;            // step offset of the region's wavefront (host tile order, dec_build)
     int32_t bty, btz, rs;          // band rows, chunk planes, smem row stride
     int64_t tile_base, ntiles;
     int64_t sp_base;               // segment index: ez * tny entries
@@ -768,83 +769,7 @@ __device__ __forceinline__ int64_t unit_count(const UnitMasks &m, const uint8_t 
     return c;
 }
 
-// region of every chunk / tile (filled once per call; replaces per-CTA
-// binary searches whose dependent loads dominated small CTAs)
-__global__ void k_fill_maps(const DecReg *__restrict__ regs, int64_t nreg, int32_t *__restrict__ chunk_reg,
-                            int32_t *__restrict__ tile_reg) {
-    const int64_t r = blockIdx.x;
-    if (r >= nreg) return;
-    const DecReg &R = regs[r];
-    for (int64_t i = threadIdx.x; i < R.nchunks; i += blockDim.x) chunk_reg[R.chunk_base + i] = (int32_t)r;
-    for (int64_t i = threadIdx.x; i < R.ntiles; i += blockDim.x) tile_reg[R.tile_base + i] = (int32_t)r;
-}
-
 constexpr int UPT = (int)(DCB / (16 * DTHREADS));  // 16-byte units per thread
-
-// tile order for k_band: critical path first.  A tile (band b, chunk c)
-// of a region with tny bands and tnz chunks has b + c predecessors on its
-// dependency chain and (tny - 1 - b) + (tnz - 1 - c) successors; tiles are
-// grouped by the global step d = b + c + doff with doff = Dmax - (tny +
-// tnz - 2), so every region's wavefront ENDS on the last step and the
-// longest chains start first.  Every dependency of a tile lies on step
-// d - 1, so taking tiles in this order from a ticket cannot deadlock.  One
-// thread per (step, region) pair writes its tiles at pair_base.
-// tiles of region r on step d (pair i = d * nreg + r), in closed form
-__device__ __forceinline__ int64_t pair_tiles(const DecReg &R, int64_t d_glob) {
-    if (R.ntiles == 0) return 0;
-    const int64_t d = d_glob - R.doff;
-    if (d < 0) return 0;
-    const int64_t lo = max((int64_t)0, d - (R.tny - 1)), hi = min((int64_t)R.tnz - 1, d);
-    return hi >= lo ? hi - lo + 1 : 0;
-}
-
-// exclusive prefix of pair_tiles over all pairs in step-major order, in two
-// parts: k_step_pairs (CTA per step) = prefix over the regions of one step +
-// the step's total; k_step_scan (one CTA) = exclusive prefix over the steps,
-// added by k_tile_order.
-__global__ void __launch_bounds__(256) k_step_pairs(const DecReg *__restrict__ regs, int64_t nreg,
-                                                    int64_t *__restrict__ pair_base, int64_t *__restrict__ step_tot) {
-    const int64_t st = blockIdx.x;
-    int64_t carry = 0;
-    for (int64_t r0 = 0; r0 < nreg; r0 += 256) {
-        const int64_t r = r0 + threadIdx.x;
-        const int64_t c = r < nreg ? pair_tiles(regs[r], st) : 0;
-        int64_t tot;
-        const int64_t pre = block_excl64(c, &tot);
-        if (r < nreg) pair_base[st * nreg + r] = carry + pre;
-        carry += tot;
-    }
-    if (threadIdx.x == 0) step_tot[st] = carry;
-}
-
-__global__ void __launch_bounds__(1024) k_step_scan(int64_t nsteps, int64_t *__restrict__ step_tot) {
-    int64_t carry = 0;
-    for (int64_t s0 = 0; s0 < nsteps; s0 += 1024) {
-        const int64_t i = s0 + threadIdx.x;
-        const int64_t v = i < nsteps ? step_tot[i] : 0;
-        int64_t tot;
-        const int64_t pre = block_excl64(v, &tot);
-        __syncthreads();  // every thread has read its total before it is overwritten
-        if (i < nsteps) step_tot[i] = carry + pre;
-        carry += tot;
-    }
-}
-
-__global__ void k_tile_order(const DecReg *__restrict__ regs, const int64_t *__restrict__ pair_base,
-                             const int64_t *__restrict__ step_base, int64_t npairs, int64_t nreg,
-                             int32_t *__restrict__ order) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= npairs) return;
-    const int64_t r = i % nreg;
-    const DecReg &R = regs[r];
-    if (R.ntiles == 0) return;
-    const int d = (int)(i / nreg) - R.doff;
-    if (d < 0) return;
-    int64_t k = step_base[i / nreg] + pair_base[i];
-    const int ny = R.tny, nz = R.tnz;
-    for (int tz = max(0, d - (ny - 1)); tz <= min(nz - 1, d); ++tz)
-        order[k++] = (int32_t)(R.tile_base + (int64_t)tz * ny + (d - tz));
-}
 
 // samples per chunk (fast path); flags non-canonical regions
 __global__ void __launch_bounds__(DTHREADS) k_tok_fast(DecReg *__restrict__ regs, const int32_t *__restrict__ chunk_reg,
@@ -1684,8 +1609,11 @@ struct DecPlan {
     int64_t *faces;
     unsigned long long *asum;  // per region: max tile sum |q| >= 2^31 (else 0)
     int32_t *tflag, *chunk_reg, *tile_reg, *order;
-    int64_t *pair_base, *step_base;
     int64_t ndiag = 0;
+    // host-built [chunk -> region | tile -> region | tile order], uploaded with
+    // the region records (built once per region table, shared by the cache)
+    std::shared_ptr<const std::vector<int32_t>> hmaps;
+    int32_t *maps;
     unsigned long long *ticket, *ticket3;
     int32_t *any_slow;
     bool host_slow = false;  // some region needs the generic path whatever the stream
@@ -1812,6 +1740,29 @@ static bool dec_build(const chr_dec_region_t *h, int64_t n, uintptr_t blob, DecP
         DecReg &R = pl.regs[i];
         if (R.ntiles) R.doff = (int32_t)(D - (R.tny + R.tnz - 2));
     }
+    // chunk / tile -> region maps and the critical-path tile order (step d of
+    // a region's wavefront = band + chunk + doff; every region ends on the last
+    // step; a tile's two predecessors lie on step d - 1, so taking tiles in
+    // this order from a ticket cannot deadlock)
+    auto m = std::make_shared<std::vector<int32_t>>((size_t)(pl.nchunks + 2 * pl.ntiles + 3), 0);
+    int32_t *creg = m->data(), *treg = creg + pl.nchunks + 1, *ord = treg + pl.ntiles + 1;
+    for (int64_t r = 0; r < n; ++r) {
+        const DecReg &R = pl.regs[r];
+        for (int64_t i = 0; i < R.nchunks; ++i) creg[R.chunk_base + i] = (int32_t)r;
+        for (int64_t i = 0; i < R.ntiles; ++i) treg[R.tile_base + i] = (int32_t)r;
+    }
+    int64_t k = 0;
+    for (int64_t d = 0; d < pl.ndiag; ++d)
+        for (int64_t r = 0; r < n; ++r) {
+            const DecReg &R = pl.regs[r];
+            if (!R.ntiles) continue;
+            const int64_t dl = d - R.doff;
+            if (dl < 0) continue;
+            for (int64_t tz = std::max<int64_t>(0, dl - (R.tny - 1)); tz <= std::min<int64_t>(R.tnz - 1, dl); ++tz)
+                ord[k++] = (int32_t)(R.tile_base + tz * R.tny + (dl - tz));
+        }
+    if (k != pl.ntiles) return false;
+    pl.hmaps = m;
     return true;
 }
 
@@ -1862,11 +1813,10 @@ static void dec_carve(DecPlan &pl, void *base, size_t cap) {
     pl.faces = c.take<int64_t>(pl.nface + 1);
     pl.asum = c.take<unsigned long long>(pl.regs.size() + 1);
     pl.tflag = c.take<int32_t>(pl.ntiles + 1);
-    pl.chunk_reg = c.take<int32_t>(pl.nchunks + 1);
-    pl.tile_reg = c.take<int32_t>(pl.ntiles + 1);
-    pl.order = c.take<int32_t>(pl.ntiles + 1);
-    pl.pair_base = c.take<int64_t>(pl.ndiag * n + 1);
-    pl.step_base = c.take<int64_t>(pl.ndiag + 1);
+    pl.maps = c.take<int32_t>(pl.nchunks + 2 * pl.ntiles + 3);  // layout of hmaps
+    pl.chunk_reg = pl.maps;
+    pl.tile_reg = base ? pl.maps + pl.nchunks + 1 : nullptr;
+    pl.order = base ? pl.tile_reg + pl.ntiles + 1 : nullptr;
     pl.ticket = c.take<unsigned long long>(1);
     pl.ticket3 = c.take<unsigned long long>(1);
     pl.any_slow = c.take<int32_t>(2);  // [0] generic path needed, [1] int64 band pass needed
@@ -1937,7 +1887,9 @@ static int decode_impl(const uint8_t *d_blob, const chr_dec_region_t *h, int64_t
         segs[i].end = pl.regs[i].poff + pl.regs[i].plen;
     }
     const int64_t total_sc = crc_plan_segments(segs.data(), n);
-    CHR_CUDA_TRY(h2d_multi({{pl.d_regs, pl.regs.data(), sizeof(DecReg) * n}, {pl.segs, segs.data(), sizeof(CrcSeg) * n}},
+    CHR_CUDA_TRY(h2d_multi({{pl.d_regs, pl.regs.data(), sizeof(DecReg) * n},
+                            {pl.segs, segs.data(), sizeof(CrcSeg) * n},
+                            {pl.maps, pl.hmaps->data(), sizeof(int32_t) * pl.hmaps->size()}},
                            st));
     CHR_CUDA_TRY(zero_async({{pl.seg_raw, 2 * sizeof(uint32_t) * n},  // + crc_bad
                              {pl.flags, sizeof(int64_t) * (pl.nitems + 1)},
@@ -1975,10 +1927,6 @@ static int decode_impl(const uint8_t *d_blob, const chr_dec_region_t *h, int64_t
         k_esc_count<<<(unsigned)n, 256, 0, st>>>(pl.d_regs, n, d_blob);
     }
     {
-        CHR_PROF("k_fill_maps", st);
-        k_fill_maps<<<(unsigned)n, 256, 0, st>>>(pl.d_regs, n, pl.chunk_reg, pl.tile_reg);
-    }
-    {
         CHR_PROF("k_tok_fast", st);
         k_tok_fast<<<(unsigned)pl.nchunks, DTHREADS, 0, st>>>(pl.d_regs, pl.chunk_reg, d_blob, pl.chunk_samples,
                                                               pl.thr_cnt, pl.any_slow);
@@ -1998,20 +1946,6 @@ static int decode_impl(const uint8_t *d_blob, const chr_dec_region_t *h, int64_t
         {
             CHR_PROF("k_esc_seg", st);
             k_esc_seg<<<(unsigned)n, 256, 0, st>>>(pl.d_regs, d_blob, pl.esc_sp);
-        }
-        const int64_t npairs = pl.ndiag * n;
-        {
-            CHR_PROF("k_step_pairs", st);
-            k_step_pairs<<<(unsigned)pl.ndiag, 256, 0, st>>>(pl.d_regs, n, pl.pair_base, pl.step_base);
-        }
-        {
-            CHR_PROF("k_step_scan", st);
-            k_step_scan<<<1, 1024, 0, st>>>(pl.ndiag, pl.step_base);
-        }
-        {
-            CHR_PROF("k_tile_order", st);
-            k_tile_order<<<(unsigned)ceil_div(npairs, 256), 256, 0, st>>>(pl.d_regs, pl.pair_base, pl.step_base,
-                                                                         npairs, n, pl.order);
         }
         const int smem = (int)SMB;
         CHR_CUDA_TRY(cudaFuncSetAttribute(k_band<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));

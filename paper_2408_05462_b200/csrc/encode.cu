@@ -32,6 +32,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <vector>
 
 #include "chr_internal.cuh"
@@ -1652,7 +1653,23 @@ struct EncPlan {
     EncScalars *scal;
     int32_t *item_reg, *chunk_reg;
     uint32_t *qz, *escbits;
+    // host-built item -> region and chunk -> region maps (uploaded with the
+    // region records; shared by the per-thread plan cache)
+    std::shared_ptr<const std::vector<int32_t>> hitem, hchunk;
 };
+
+static void host_maps(EncPlan &pl) {
+    auto it = std::make_shared<std::vector<int32_t>>((size_t)pl.nitems + 1, 0);
+    auto ch = std::make_shared<std::vector<int32_t>>((size_t)pl.nchunks + 1, 0);
+    for (size_t r = 0; r < pl.regs.size(); ++r) {
+        const RegDev &R = pl.regs[r];
+        const int64_t nit = pl.segmode ? (int64_t)R.nty * R.nzc : (int64_t)R.ntx * R.nty * R.nzc;
+        for (int64_t i = 0; i < nit; ++i) (*it)[R.item_base + i] = (int32_t)r;
+        for (int64_t i = 0; i < R.nchunks; ++i) (*ch)[R.chunk_base + i] = (int32_t)r;
+    }
+    pl.hitem = it;
+    pl.hchunk = ch;
+}
 
 static bool build_plan_uncached(const chr_region_t *h, int64_t nreg, EncPlan &pl) {
     pl.regs.resize(nreg);
@@ -1778,7 +1795,11 @@ static bool build_plan(const chr_region_t *h, int64_t nreg, EncPlan &pl, bool al
     // the piece path stays the default: the segment path reads the input once
     // less but issues ~1.5x the instructions; CHR_ENC_SEG=1
     allow_seg = allow_seg && getenv("CHR_ENC_SEG") != nullptr;
-    if (pl.portions) return build_plan_uncached(h, nreg, pl);
+    if (pl.portions) {
+        if (!build_plan_uncached(h, nreg, pl)) return false;
+        host_maps(pl);
+        return true;
+    }
     if (C.valid && C.allow_seg == allow_seg && (int64_t)C.key.size() == nreg &&
         std::memcmp(C.key.data(), h, sizeof(chr_region_t) * (size_t)nreg) == 0) {
         pl = C.plan;
@@ -1787,6 +1808,7 @@ static bool build_plan(const chr_region_t *h, int64_t nreg, EncPlan &pl, bool al
     C.valid = false;
     if (!build_plan_uncached(h, nreg, pl)) return false;
     if (allow_seg) plan_segments(pl);  // false (a window too wide): the piece path
+    host_maps(pl);
     C.key.assign(h, h + nreg);
     C.plan = pl;
     C.allow_seg = allow_seg;
@@ -1944,17 +1966,17 @@ static int compress_impl(const void *d_vol, int dtype, int src_dtype, int64_t nx
     // capacity check against the worst case (verbatim f64 everywhere)
     if (out_cap < chr_compress_capacity(h_regions, nreg, m, src_dtype)) return CHR_E_PARAMETER;
 
-    CHR_CUDA_TRY(h2d_multi({{pl.params, &hp, sizeof(hp)}, {pl.d_regs, pl.regs.data(), sizeof(RegDev) * nreg}}, st));
+    CHR_CUDA_TRY(h2d_multi({{pl.params, &hp, sizeof(hp)},
+                            {pl.d_regs, pl.regs.data(), sizeof(RegDev) * nreg},
+                            {pl.item_reg, pl.hitem->data(), sizeof(int32_t) * pl.hitem->size()},
+                            {pl.chunk_reg, pl.hchunk->data(), sizeof(int32_t) * pl.hchunk->size()}},
+                           st));
     CHR_CUDA_TRY(zero_async({{pl.scal, sizeof(EncScalars)},
                              {pl.seg_raw, sizeof(uint32_t) * (nreg + 1)},
                              {pl.escbits, sizeof(uint32_t) * (pl.etotal + 2)}},
                             st));
 
     const unsigned items = (unsigned)pl.nitems, chunks = (unsigned)pl.nchunks;
-    {
-        CHR_PROF("k_tile_fill_map", st);
-        k_tile_fill_map<<<(unsigned)nreg, 256, 0, st>>>(pl.d_regs, nreg, pl.item_reg, pl.chunk_reg);
-    }
     if (pl.segmode) {
         const size_t smem = seg_smem_bytes(pl.span_cap, dtype == CHR_F32 ? 4 : 8);
         if (smem > 48 * 1024) {
