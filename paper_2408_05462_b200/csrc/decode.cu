@@ -1499,9 +1499,19 @@ __global__ void __launch_bounds__(KBT) k_band(const DecReg *__restrict__ regs, c
             const QV *qp = Q + qi;
             const int64_t *dp = dF + xx;
             double *op = obase + t;
+            int64_t acc = fz;  // z prefix
+            if (nb == 1) {  // one band (most windows): no band above, this warp owns its mask words
+                for (int j = 0; j < nzv; ++j, w += pw, qp += PL, op += zstride) {
+                    acc += *qp;
+                    const double v = (double)acc * twoe;
+                    if (act) __stcs(op, v);
+                    const uint32_t bal = __ballot_sync(0xFFFFFFFFu, act && v >= iso);
+                    if (lane == 0) *w = bal;
+                }
+                continue;
+            }
             const int dstep = b > 0 ? ex : 0;
             if (b == 0) dp = &s_zero;
-            int64_t acc = fz;  // z prefix
             for (int j = 0; j < nzv; ++j, w += pw, qp += PL, dp += dstep, op += zstride) {
                 acc += *qp;
                 const double v = (double)(acc + *dp) * twoe;
