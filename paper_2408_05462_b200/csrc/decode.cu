@@ -1923,7 +1923,11 @@ static int decode_impl(const uint8_t *d_blob, const chr_dec_region_t *h, int64_t
         CHR_CUDA_TRY(cudaStreamWaitEvent(side->st, side->ev[2], 0));
         ct = side->st;
     }
-    int rc = crc_launch(d_blob, pl.segs, n, total_sc, pl.seg_raw, ct, side ? 148 * 2 : 0);
+    static const int crc_ctas = [] {  // side-stream CRC grid (it shares the SMs with the tokenizer passes)
+        const char *e = std::getenv("CHR_CRC_CTAS");
+        return e ? std::atoi(e) : 148 * 4;
+    }();
+    int rc = crc_launch(d_blob, pl.segs, n, total_sc, pl.seg_raw, ct, side ? crc_ctas : 0);
     if (rc) return rc;
     {
         CHR_PROF("k_crc_flag", ct);
