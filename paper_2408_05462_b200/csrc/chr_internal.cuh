@@ -56,6 +56,7 @@ class ProfScope {
 // function that calls d2h holds an XferScope.
 cudaError_t h2d(void *dst, const void *src, size_t n, cudaStream_t st);
 cudaError_t d2h(void *dst, const void *src, size_t n, cudaStream_t st);
+const void *d2h_view(const void *src, size_t n, cudaStream_t st, cudaError_t *err);  // zero-copy read-back
 cudaError_t stream_sync(cudaStream_t st);
 cudaError_t fill_async(void *dst, int v, size_t n, cudaStream_t st);   // cudaMemsetAsync as a kernel
 constexpr int kFillMax = 8;

@@ -30,6 +30,7 @@
 // once per sample (plus the 1/8 + 1/64 + 1/16 halo).
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <memory>

@@ -11,6 +11,9 @@
 // When a buffer is too small the call returns CHR_E_WORKSPACE with the
 // sizes it needs (the caller grows them and calls again).
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <vector>
@@ -27,6 +30,17 @@ extern "C" int chr_pipeline(const void *d_vol, int dtype, int src_dtype, int64_t
                             chr_after_compress_fn after_compress, void *user, chr_pipeline_result_t *h_res,
                             void *stream) {
     CHR_XFER_SCOPE;
+    // CHR_TRACE_HOST=1: host-side phase times of the call on stderr (diagnostics)
+    static const bool trace = [] {
+        const char *e = std::getenv("CHR_TRACE_HOST");
+        return e && e[0] == '1';
+    }();
+    auto t_start = std::chrono::steady_clock::now();
+    auto tmark = [&](const char *what) {
+        if (!trace) return;
+        const double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t_start).count();
+        std::fprintf(stderr, "chr_pipeline %8.1f us  %s\n", us, what);
+    };
     if (!d_vol || !h_cands || !h_regions || !h_res || !spacing) return CHR_E_PARAMETER;
     if (m < 1 || m > 64 || k_index < 0 || k_index >= m) return CHR_E_PARAMETER;
     std::memset(h_res, 0, sizeof(*h_res));
@@ -51,10 +65,30 @@ extern "C" int chr_pipeline(const void *d_vol, int dtype, int src_dtype, int64_t
     int64_t *d_bad = reinterpret_cast<int64_t *>(ws + al((size_t)nb * 3 * sizeof(double)));
     int rc = chr_stats(d_vol, dtype, nx, ny, nz, bs, h_cands, m, d_stats, d_bad, stream);
     if (rc) return rc;
-    std::vector<double> hs((size_t)nb * 3);
+    // the block stats are read straight from the pinned transfer ring (no
+    // copy-out: 786 KB at c3); they are consumed by the plan below, before
+    // the next transfer reuses the ring
+    std::vector<double> hs_copy;
+    const double *hs = nullptr;
     int64_t bad = -1;
-    CHR_CUDA_TRY(d2h_multi({{hs.data(), d_stats, hs.size() * sizeof(double)}, {&bad, d_bad, sizeof(bad)}}, st));
+    cudaError_t ve = cudaSuccess;
+    const size_t sbytes = al((size_t)nb * 3 * sizeof(double)) + sizeof(int64_t);  // stats, then d_bad
+    const void *view = d2h_view(d_stats, sbytes, st, &ve);
+    CHR_CUDA_TRY(ve);
+    if (!view) {
+        hs_copy.resize((size_t)nb * 3);
+        CHR_CUDA_TRY(d2h_multi({{hs_copy.data(), d_stats, hs_copy.size() * sizeof(double)}, {&bad, d_bad, sizeof(bad)}},
+                               st));
+    }
+    tmark("stats launched");
     CHR_CUDA_TRY(stream_sync(st));
+    tmark("stats synced");
+    if (view) {
+        hs = reinterpret_cast<const double *>(view);
+        std::memcpy(&bad, reinterpret_cast<const char *>(view) + (sbytes - sizeof(int64_t)), sizeof(bad));
+    } else {
+        hs = hs_copy.data();
+    }
     if (bad >= 0) {
         h_res->first_nonfinite = bad;
         return CHR_E_NONFINITE;
@@ -68,15 +102,18 @@ extern "C" int chr_pipeline(const void *d_vol, int dtype, int src_dtype, int64_t
     h_res->vmax = vmax;
     for (int i = 0; i < m; ++i)
         if (!(vmin <= h_cands[i] && h_cands[i] <= vmax)) return CHR_E_PARAMETER;  // out_of_range="error"
+    tmark("value range");
     int64_t nreg = 0;
-    rc = chr_plan(hs.data(), nx, ny, nz, bs, h_cands, m, vmin, vmax, loose_fraction, safety_factor, h_regions, &nreg);
+    rc = chr_plan(hs, nx, ny, nz, bs, h_cands, m, vmin, vmax, loose_fraction, safety_factor, h_regions, &nreg);
     if (rc) return rc;
     h_res->n_regions = nreg;
+    tmark("plan");
 
     // ---- compress into the caller's archive buffer
     const size_t cws = chr_compress_workspace_size(h_regions, nreg);
     const uint64_t cap = chr_compress_capacity(h_regions, nreg, m, src_dtype);
     h_res->archive_needed = cap;
+    tmark("compress sizes");
     if (cws == 0) return CHR_E_PARAMETER;
     if (ws_bytes < cws || archive_cap < cap || !d_archive) {
         h_res->ws_needed = std::max(cws, stats_bytes);
@@ -99,6 +136,7 @@ extern "C" int chr_pipeline(const void *d_vol, int dtype, int src_dtype, int64_t
                            1, 0, 1.0, d_ws, ws_bytes, d_archive, archive_cap, &nbytes, stream);
     }
     if (rc) return rc;
+    tmark("compress returned");
     h_res->archive_nbytes = nbytes;
     CHR_CUDA_TRY(mark(1));
     if (after_compress) {  // e.g. start the archive's device->host copy: the archive must be final

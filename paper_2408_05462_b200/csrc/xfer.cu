@@ -201,6 +201,19 @@ cudaError_t h2d(void *dst, const void *src, size_t n, cudaStream_t st) {
     return launch_xfer(p, dst, n, st);
 }
 
+// device -> host into the pinned ring without the copy-out at stream_sync:
+// the returned pointer is readable after the next stream_sync(st) and valid
+// until the next transfer of this thread (nullptr: too large for the ring)
+const void *d2h_view(const void *src, size_t n, cudaStream_t st, cudaError_t *err) {
+    *err = cudaSuccess;
+    if (n == 0 || n > kXferBig) return nullptr;
+    uint8_t *p = nullptr;
+    *err = reserve(n, st, &p);
+    if (*err != cudaSuccess) return nullptr;
+    *err = launch_xfer(src, p, n, st);
+    return *err == cudaSuccess ? p : nullptr;
+}
+
 cudaError_t d2h(void *dst, const void *src, size_t n, cudaStream_t st) {
     if (n == 0) return cudaSuccess;
     if (n > kXferBig) return cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToHost, st);
