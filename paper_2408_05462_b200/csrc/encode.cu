@@ -492,6 +492,9 @@ __global__ void k_tile_fill_map(const RegDev *__restrict__ regs, int64_t nreg, i
 // replaced took 0.62 ms at c3, this one 0.55 ms).  A range larger than the buffer is written
 // byte by byte from the lanes (rare).  Verbatim regions: the CTA's threads
 // copy the samples of its 128 pieces, coalesced.
+#ifndef CHR_EMIT_PF
+#define CHR_EMIT_PF 2
+#endif
 #ifndef CHR_E2_WARPS
 #define CHR_E2_WARPS 2
 #endif
@@ -700,6 +703,27 @@ __global__ void __launch_bounds__(E2_WARPS * 32) k_emit_q2(const T *__restrict__
             };
             if (vcount == TX) {
                 const uint4 *q4 = reinterpret_cast<const uint4 *>(q);
+#if CHR_EMIT_PF
+                constexpr int EP = CHR_EMIT_PF;  // token values EP uint4 ahead of their use
+                uint4 a[EP];
+#pragma unroll
+                for (int j = 0; j < EP; ++j) a[j] = __ldg(q4 + j);
+#pragma unroll 1
+                for (int k = 0; k < TX / 4; k += EP) {
+                    uint4 b[EP];
+#pragma unroll
+                    for (int j = 0; j < EP; ++j) b[j] = k + EP < TX / 4 ? __ldg(q4 + k + EP + j) : a[j];
+#pragma unroll
+                    for (int j = 0; j < EP; ++j) {
+                        step(a[j].x);
+                        step(a[j].y);
+                        step(a[j].z);
+                        step(a[j].w);
+                    }
+#pragma unroll
+                    for (int j = 0; j < EP; ++j) a[j] = b[j];
+                }
+#else
 #pragma unroll 2
                 for (int k = 0; k < TX / 4; ++k) {
                     const uint4 v = __ldg(q4 + k);
@@ -708,6 +732,7 @@ __global__ void __launch_bounds__(E2_WARPS * 32) k_emit_q2(const T *__restrict__
                     step(v.z);
                     step(v.w);
                 }
+#endif
             } else {
                 for (int i = 0; i < vcount; ++i) step(__ldg(q + i));
             }
