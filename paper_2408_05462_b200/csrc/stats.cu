@@ -12,6 +12,8 @@
 // oracle in tests): per sample, min_k |s - k| is attained at one of the two
 // candidates bracketing s, because fl(s - k) is monotone in k.
 #include <cmath>
+#include <cstdlib>
+#include <algorithm>
 
 #include "chr_internal.cuh"
 
@@ -140,10 +142,40 @@ __global__ void __launch_bounds__(256) k_stats(const T *__restrict__ vol, int64_
 // bs/4 quads plus the x-ghost sample (first sample of the next block).
 constexpr int SQ = 512;  // threads; nx/4 <= SQ quads per row
 constexpr int SB = 4096;  // candidate buckets (k_stats_rows, m > 1)
+constexpr int NSTG = 4;   // bulk-copy stages in flight per CTA (TMA variant)
+constexpr int STG_BYTES = 16384;  // bytes per stage
+
+// mbarrier / bulk-copy primitives (PTX; sm_90+)
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void async_proxy_fence() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+template <bool TMA>
 __global__ void __launch_bounds__(SQ) k_stats_rows(const float *__restrict__ vol, int64_t nx, int64_t ny,
                                                    int64_t nz, int bs, int nbx, int nby, CandParams cp,
                                                    double *__restrict__ stats,
-                                                   unsigned long long *__restrict__ first_bad) {
+                                                   unsigned long long *__restrict__ first_bad, int srows) {
     __shared__ double ks[128];
     __shared__ float kt[128];  // thresholds, +inf padded (the search may probe up to 2m - 2)
     // per (row group, quad) partials: index g * nq + q  (rg * nq <= SQ)
@@ -187,85 +219,135 @@ __global__ void __launch_bounds__(SQ) k_stats_rows(const float *__restrict__ vol
     const int q = threadIdx.x % nq, g = threadIdx.x / nq;
     const int nrow_y = (int)(y1 - y0 + 1);
     const int nrows = nrow_y * (int)(z1 - z0 + 1);
-    if (g < rg) {
-        float lo = INFINITY, hi = -INFINITY, gl = INFINITY, gh = -INFINITY;
-        double dm = INFINITY, gd = INFINITY;
-        // m == 1: fl(s - k) is monotone in s, so min |fl(s - k)| over a block
-        // is attained at the smallest sample >= k or the largest sample < k:
-        // track those two in f32 (exact compares against thr = the smallest
-        // float >= k) and form the f64 distances once at the end
-        float ab = INFINITY, bl = -INFINITY, gab = INFINITY, gbl = -INFINITY;
-        const float thr0 = kt[0];
-        unsigned long long bad = ~0ull;
-        const bool ghost = ((4 * q) % bs) == 0 && q > 0;
-        // RU rows per step: their 16-byte loads are all in flight before any is
-        // used (one outstanding load per thread left HBM at ~35 % of peak)
-        constexpr int RU = CHR_STATS_RU;
-        for (int r0 = g; r0 < nrows; r0 += RU * rg) {
-            float4 v4[RU];
-            int64_t rowoff[RU];
+    float lo = INFINITY, hi = -INFINITY, gl = INFINITY, gh = -INFINITY;
+    double dm = INFINITY, gd = INFINITY;
+    // m == 1: fl(s - k) is monotone in s, so min |fl(s - k)| over a block
+    // is attained at the smallest sample >= k or the largest sample < k:
+    // track those two in f32 (exact compares against thr = the smallest
+    // float >= k) and form the f64 distances once at the end
+    float ab = INFINITY, bl = -INFINITY, gab = INFINITY, gbl = -INFINITY;
+    const float thr0 = kt[0];
+    unsigned long long bad = ~0ull;
+    const bool ghost = ((4 * q) % bs) == 0 && q > 0;
+    auto row_off = [&](int r) {  // flat index of row r's first sample
+        const int zr = r / nrow_y, yr = r - zr * nrow_y;
+        return ((z0 + zr) * ny + (y0 + yr)) * nx;
+    };
+    auto proc = [&](const float4 v4, int r) {  // this thread's quad of row r
+        const float v[4] = {v4.x, v4.y, v4.z, v4.w};
 #pragma unroll
-            for (int u = 0; u < RU; ++u) {
-                const int r = r0 + u * rg;
-                const int zr = r / nrow_y, yr = r - zr * nrow_y;
-                rowoff[u] = ((z0 + zr) * ny + (y0 + yr)) * nx;
-                v4[u] = r < nrows ? __ldg(reinterpret_cast<const float4 *>(vol + rowoff[u]) + q)
-                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int i = 0; i < 4; ++i) {
+            const float f = v[i];
+            if (!isfinite(f)) {
+                bad = min(bad, (unsigned long long)(row_off(r) + 4 * q + i));
+                continue;
             }
+            lo = fminf(lo, f);
+            hi = fmaxf(hi, f);
+            if (m == 1) {
+                const bool up = f >= thr0;
+                ab = fminf(ab, up ? f : INFINITY);
+                bl = fmaxf(bl, up ? -INFINITY : f);
+                if (i == 0 && ghost) {
+                    gl = fminf(gl, f);
+                    gh = fmaxf(gh, f);
+                    gab = fminf(gab, up ? f : INFINITY);
+                    gbl = fmaxf(gbl, up ? -INFINITY : f);
+                }
+                continue;
+            }
+            // min |s - k| over the two candidates bracketing s
+            const double sd = (double)f;
+            double d;
+            {
+                int c;  // #{j : k[j] <= s}
+                if (!(f >= lo_e)) {
+                    c = 0;
+                } else if (f >= hi_e) {
+                    c = m;
+                } else {
+                    const int vv = kb[min(SB - 1, (int)((f - lo_e) * invw))];
+                    c = vv & 0x7F;
+                    if (vv & 0x80) {  // a threshold falls in this bucket: exact compares
+                        while (c < m && f >= kt[c]) ++c;
+                        while (c > 0 && f < kt[c - 1]) --c;
+                    }
+                }
+                const double kl = c > 0 ? ks[c - 1] : -INFINITY;
+                d = fmin(fabs(__dadd_rn(sd, -kl)), fabs(__dadd_rn(sd, -ks[c])));  // ks[m] = +inf
+            }
+            dm = fmin(dm, d);
+            if (i == 0 && ghost) {
+                gl = fminf(gl, f);
+                gh = fmaxf(gh, f);
+                gd = fmin(gd, d);
+            }
+        }
+    };
+    if constexpr (!TMA) {
+        if (g < rg) {
+            // RU rows per step: their 16-byte loads are all in flight before any is
+            // used (one outstanding load per thread left HBM at ~35 % of peak)
+            constexpr int RU = CHR_STATS_RU;
+            for (int r0 = g; r0 < nrows; r0 += RU * rg) {
+                float4 v4[RU];
 #pragma unroll
-            for (int u = 0; u < RU; ++u) {
-                if (r0 + u * rg >= nrows) break;
-                const float v[4] = {v4[u].x, v4[u].y, v4[u].z, v4[u].w};
+                for (int u = 0; u < RU; ++u) {
+                    const int r = r0 + u * rg;
+                    v4[u] = r < nrows ? __ldg(reinterpret_cast<const float4 *>(vol + row_off(r)) + q)
+                                      : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
 #pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const float f = v[i];
-                    if (!isfinite(f)) {
-                        bad = min(bad, (unsigned long long)(rowoff[u] + 4 * q + i));
-                        continue;
-                    }
-                    lo = fminf(lo, f);
-                    hi = fmaxf(hi, f);
-                    if (m == 1) {
-                        const bool up = f >= thr0;
-                        ab = fminf(ab, up ? f : INFINITY);
-                        bl = fmaxf(bl, up ? -INFINITY : f);
-                        if (i == 0 && ghost) {
-                            gl = fminf(gl, f);
-                            gh = fmaxf(gh, f);
-                            gab = fminf(gab, up ? f : INFINITY);
-                            gbl = fmaxf(gbl, up ? -INFINITY : f);
-                        }
-                        continue;
-                    }
-                    // min |s - k| over the two candidates bracketing s
-                    const double sd = (double)f;
-                    double d;
-                    {
-                        int c;  // #{j : k[j] <= s}
-                        if (!(f >= lo_e)) {
-                            c = 0;
-                        } else if (f >= hi_e) {
-                            c = m;
-                        } else {
-                            const int v = kb[min(SB - 1, (int)((f - lo_e) * invw))];
-                            c = v & 0x7F;
-                            if (v & 0x80) {  // a threshold falls in this bucket: exact compares
-                                while (c < m && f >= kt[c]) ++c;
-                                while (c > 0 && f < kt[c - 1]) --c;
-                            }
-                        }
-                        const double kl = c > 0 ? ks[c - 1] : -INFINITY;
-                        d = fmin(fabs(__dadd_rn(sd, -kl)), fabs(__dadd_rn(sd, -ks[c])));  // ks[m] = +inf
-                    }
-                    dm = fmin(dm, d);
-                    if (i == 0 && ghost) {
-                        gl = fminf(gl, f);
-                        gh = fmaxf(gh, f);
-                        gd = fmin(gd, d);
-                    }
+                for (int u = 0; u < RU; ++u) {
+                    if (r0 + u * rg >= nrows) break;
+                    proc(v4[u], r0 + u * rg);
                 }
             }
         }
+    } else {
+        // Bulk-copy (TMA) row streaming: thread 0 keeps NSTG stages of `srows`
+        // rows in flight (cp.async.bulk into shared memory, completion counted
+        // on one mbarrier per stage; rows of one plane are contiguous in HBM,
+        // so a stage is one or two copies); every thread reduces its quad of
+        // the stage's rows from shared memory.
+        extern __shared__ __align__(128) unsigned char st_raw[];
+        __shared__ __align__(8) uint64_t full[NSTG];
+        const int64_t rowb = nx * 4;
+        const int nst = (nrows + srows - 1) / srows;
+        auto issue = [&](int s) {  // thread 0: stage s into buffer s % NSTG
+            const int r0 = s * srows, r1 = min(nrows, r0 + srows);
+            uint64_t *bar = &full[s % NSTG];
+            unsigned char *dst = st_raw + (size_t)(s % NSTG) * srows * rowb;
+            mbar_expect_tx(bar, (uint32_t)((r1 - r0) * rowb));
+            for (int r = r0; r < r1;) {
+                const int zr = r / nrow_y, yr = r - zr * nrow_y;
+                const int cnt = min(r1 - r, nrow_y - yr);  // rows left in this plane
+                bulk_g2s(dst + (size_t)(r - r0) * rowb, vol + row_off(r), (uint32_t)(cnt * rowb), bar);
+                r += cnt;
+            }
+        };
+        if (threadIdx.x == 0) {
+            for (int i = 0; i < NSTG; ++i) mbar_init(&full[i], 1);
+            mbar_fence_init();
+            for (int s = 0; s < NSTG && s < nst; ++s) issue(s);
+        }
+        __syncthreads();
+        for (int s = 0; s < nst; ++s) {
+            const int buf = s % NSTG;
+            mbar_wait(&full[buf], (uint32_t)((s / NSTG) & 1));
+            if (g < rg) {
+                const int r0 = s * srows, rn = min(nrows - r0, srows);
+                const float4 *sb = reinterpret_cast<const float4 *>(st_raw + (size_t)buf * srows * rowb);
+                for (int rr = g; rr < rn; rr += rg) proc(sb[(size_t)rr * nq + q], r0 + rr);
+            }
+            __syncthreads();  // every thread is done with the buffer
+            if (threadIdx.x == 0 && s + NSTG < nst) {
+                async_proxy_fence();
+                issue(s + NSTG);
+            }
+        }
+    }
+    if (g < rg) {
         if (m == 1 && !isnan(ks[0])) {  // (a NaN candidate leaves the distances at +inf, like fmin)
             const double k0 = ks[0];
             dm = fmin(__dadd_rn((double)ab, -k0), __dadd_rn(k0, -(double)bl));
@@ -342,9 +424,22 @@ extern "C" int chr_stats(const void *d_vol, int dtype, int64_t nx, int64_t ny, i
     const bool rows_ok = dtype == CHR_F32 && bs % 4 == 0 && nx % 4 == 0 && nx <= 4 * SQ &&
                          ((uintptr_t)d_vol & 15) == 0;
     if (rows_ok) {
+        // bulk-copy (TMA) row staging unless CHR_STATS_TMA=0; rows per stage: 16 KB
+        static const bool tma = [] {
+            const char *e = std::getenv("CHR_STATS_TMA");
+            return !(e && e[0] == '0');
+        }();
+        const int srows = (int)std::max<int64_t>(1, STG_BYTES / (4 * nx));
+        const int smem = NSTG * srows * (int)(4 * nx);
         CHR_PROF("k_stats_rows", st);
-        k_stats_rows<<<(unsigned)(nby * nbz), SQ, 0, st>>>((const float *)d_vol, nx, ny, nz, (int)bs, nbx, nby, cp,
-                                                           d_block_stats, bad);
+        if (tma) {
+            CHR_CUDA_TRY(cudaFuncSetAttribute(k_stats_rows<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            k_stats_rows<true><<<(unsigned)(nby * nbz), SQ, smem, st>>>((const float *)d_vol, nx, ny, nz, (int)bs, nbx,
+                                                                       nby, cp, d_block_stats, bad, srows);
+        } else {
+            k_stats_rows<false><<<(unsigned)(nby * nbz), SQ, 0, st>>>((const float *)d_vol, nx, ny, nz, (int)bs, nbx,
+                                                                     nby, cp, d_block_stats, bad, srows);
+        }
     } else if (dtype == CHR_F32)
         {
             CHR_PROF("k_stats<float>", st);
