@@ -22,6 +22,42 @@ DTYPE_WIDTHS = {"f32": 4, "f64": 8}
 _RAW = {("f32", "little"): "<f4", ("f32", "big"): ">f4", ("f64", "little"): "<f8", ("f64", "big"): ">f8"}
 
 
+_UPLOAD_POOL = None
+
+
+def upload_pool():
+    """A small thread pool for large host copies (numpy releases the GIL)."""
+    global _UPLOAD_POOL
+    if _UPLOAD_POOL is None:
+        from concurrent.futures import ThreadPoolExecutor
+
+        _UPLOAD_POOL = ThreadPoolExecutor(max_workers=8, thread_name_prefix="chr-host-copy")
+    return _UPLOAD_POOL
+
+
+def _upload(a: np.ndarray) -> torch.Tensor:
+    """Host array -> new device tensor.  Large arrays go through page-locked
+    staging filled by a few host threads (np.copyto releases the GIL), chunk
+    by chunk, each chunk's DMA queued as soon as it is staged: the pageable
+    .cuda() of a c3 field ran at ~11 GB/s (48 ms for 537 MB)."""
+    a = np.ascontiguousarray(a)
+    if a.nbytes < (64 << 20):
+        return torch.from_numpy(np.array(a, copy=True)).cuda()
+    pool = upload_pool()
+    flat = a.reshape(-1)
+    t_flat = torch.from_numpy(flat[:1].copy())  # dtype probe
+    stage = torch.empty(flat.size, dtype=t_flat.dtype, pin_memory=True)  # torch's caching host allocator
+    sn = stage.numpy()
+    dev = torch.empty(flat.size, dtype=t_flat.dtype, device="cuda")
+    nch = 16
+    bounds = [(flat.size * i // nch, flat.size * (i + 1) // nch) for i in range(nch)]
+    futs = [pool.submit(np.copyto, sn[lo:hi], flat[lo:hi]) for lo, hi in bounds]
+    for (lo, hi), f in zip(bounds, futs):
+        f.result()
+        dev[lo:hi].copy_(stage[lo:hi], non_blocking=True)  # the allocator keeps `stage` until these finish
+    return dev.reshape(a.shape)
+
+
 def _dims3(dims):
     if len(dims) != 3 or any(int(d) != d or d < 1 for d in dims):
         raise ParameterError(f"dims must be three positive integers, got {dims!r}")
@@ -57,8 +93,7 @@ class Volume:
             a32 = values.reshape(-1)
             if a32.size != n:
                 raise ParameterError(f"values has {a32.size} samples, dims {dims} require {n}")
-            a32 = np.require(a32, requirements=["C", "W"])
-            t = torch.from_numpy(a32).cuda()
+            t = _upload(a32)
             lo, hi, bad = device.value_range(t)
             if bad >= 0:
                 raise NonFiniteSampleError(bad, float(a32[bad]))
@@ -139,7 +174,7 @@ class Volume:
                 narrow = a.astype(np.float32)
                 if np.array_equal(narrow.astype(np.float64), a):
                     a = narrow
-            object.__setattr__(self, "_dev", torch.from_numpy(np.array(a, copy=True)).cuda())
+            object.__setattr__(self, "_dev", _upload(a))
         return self._dev
 
     def __repr__(self):

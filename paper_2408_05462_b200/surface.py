@@ -140,14 +140,29 @@ def merge_meshes(meshes) -> TriangleMesh:
     if not meshes:
         return TriangleMesh(np.empty((0, 3), np.float64), np.empty((0, 3), np.int32))
     nt = sum(m.num_triangles for m in meshes)
+    nv = sum(m.num_vertices for m in meshes)
     tris = np.empty((nt, 3), np.int32)
+    verts = np.empty((nv, 3), np.float64)
+    jobs = []
     t0 = v0 = 0
-    for m in meshes:  # one pass: each mesh's triangles + its vertex offset, straight into place
-        n = m.num_triangles
-        np.add(m.triangles, v0, out=tris[t0:t0 + n], casting="unsafe")
-        t0 += n
+    for m in meshes:  # one pass: each mesh's vertices, and triangles + its vertex offset, straight into place
+        jobs.append((m, t0, v0))
+        t0 += m.num_triangles
         v0 += m.num_vertices
-    return TriangleMesh(np.concatenate([m.vertices for m in meshes], axis=0), tris)
+
+    def place(job):
+        m, t, v = job
+        np.copyto(verts[v:v + m.num_vertices], m.vertices)
+        np.add(m.triangles, v, out=tris[t:t + m.num_triangles], casting="unsafe")
+
+    if nt + nv > (1 << 20):  # large meshes: a few host threads (numpy releases the GIL while copying)
+        from .field import upload_pool
+
+        list(upload_pool().map(place, jobs))
+    else:
+        for job in jobs:
+            place(job)
+    return TriangleMesh(verts, tris)
 
 
 def export_obj(mesh: TriangleMesh, path) -> None:
