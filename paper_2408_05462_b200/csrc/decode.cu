@@ -1106,6 +1106,7 @@ template <bool PAD, typename QV>
 __device__ __forceinline__ int band_scatter_unit32(const Win24 &W, int at, int L, int ex, uint64_t M,
                                                    QV *__restrict__ q, uint32_t &asum) {
     uint32_t H = 0;
+    const uint32_t qs = (uint32_t)__cvta_generic_to_shared(q);
 #pragma unroll
     for (int j = 4; j < 8; ++j) H = (H >> 7) | ((win_byte(W, j) & 0x7Fu) << 21);
 #pragma unroll
@@ -1118,7 +1119,12 @@ __device__ __forceinline__ int band_scatter_unit32(const Win24 &W, int at, int L
         if (lit && (unsigned)at < (unsigned)L) {
             const uint32_t zz = v - 1u;
             const int idx = PAD ? at + (int)(((uint64_t)(unsigned)at * M) >> 32) : at;
-            q[idx] = (QV)(int32_t)((zz >> 1) ^ (0u - (zz & 1u)));
+            const int32_t qv = (int32_t)((zz >> 1) ^ (0u - (zz & 1u)));
+            if (sizeof(QV) == 4) {  // a shared-window store from the hoisted 32-bit address
+                asm volatile("st.shared.b32 [%0], %1;" ::"r"(qs + 4u * (uint32_t)idx), "r"(qv) : "memory");
+            } else {
+                q[idx] = (QV)qv;
+            }
             asum += v >> 1;  // |q| (v = zigzag + 1)
         }
         // positions past L only need to stay past L: clamping at 2^30 keeps
