@@ -58,18 +58,38 @@ def _peaks():
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+    """SM clock and throttle-reason sampling during the timed region
+    (B200_PROFILING.md): NVML polled every 5 ms from a thread (a c3 timed
+    region is ~70 ms, shorter than nvidia-smi's start-up), nvidia-smi -lms as
+    the fallback when NVML is absent."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
+    # nvmlClocksEventReason* bits
+    BITS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20, "sw_power_cap": 0x4}
 
     def __init__(self, index):
         self.index = index
         self.rows = []
         self.proc = None
+        self.nvml = None
+        self.stop = threading.Event()
 
     def __enter__(self):
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(self.index)
+            self.nvml = (N, h)
+            self.mx = float(N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM))
+            self._sample_nvml()  # one sample before the region starts
+            self.rows.clear()
+            self.t = threading.Thread(target=self._poll_nvml, daemon=True)
+            self.t.start()
+            return self
+        except Exception:
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
@@ -80,11 +100,35 @@ class Clocks:
             self.proc = None
         return self
 
+    def _sample_nvml(self):
+        N, h = self.nvml
+        sm = float(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM))
+        rs = int(N.nvmlDeviceGetCurrentClocksEventReasons(h))
+        self.rows.append([str(sm), str(self.mx), hex(rs)] +
+                         ["Active" if rs & self.BITS[n] else "Not Active" for n in
+                          ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")])
+
+    def _poll_nvml(self):
+        while True:
+            try:
+                self._sample_nvml()
+            except Exception:
+                return
+            if self.stop.wait(0.005):
+                return
+
     def _read(self):
         for line in self.proc.stdout:
             self.rows.append([c.strip() for c in line.split(",")])
 
     def __exit__(self, *a):
+        if self.nvml:
+            self.stop.set()
+            self.t.join(timeout=1)
+            try:
+                self._sample_nvml()  # the region's last moment
+            except Exception:
+                pass
         if self.proc:
             self.proc.terminate()
             try:
@@ -103,7 +147,7 @@ class Clocks:
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({n for r in rows for n, v in zip(names, r[3:7]) if v.strip().lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(rows)}
+                "reasons": reasons, "samples": len(rows), "source": "nvml" if self.nvml else "nvidia-smi"}
 
 
 def make_input(cfg, n, rank, device):

@@ -79,6 +79,10 @@ __device__ __forceinline__ uint32_t apply_g(const uint32_t *g, uint32_t v, int r
 }
 
 constexpr int kCrcSmemSegs = 1024;
+#ifndef CHR_CRC_UNROLL
+#define CHR_CRC_UNROLL 16
+#endif
+constexpr int kCrcUnroll = CHR_CRC_UNROLL;
 // one warp per superchunk (kCrcScWords words); seg_raw[s] ^= contribution
 __global__ void __launch_bounds__(256) k_crc_segments(const uint8_t *__restrict__ buf,
                                                       const CrcSeg *__restrict__ segs, int64_t nseg,
@@ -123,7 +127,18 @@ __global__ void __launch_bounds__(256) k_crc_segments(const uint8_t *__restrict_
             const uint32_t *wp = reinterpret_cast<const uint32_t *>(buf + a4);
             uint32_t B = 0;
             int64_t last = -1;
-            for (uint64_t i = w0 + lane; i < w1; i += 32) {
+            uint64_t i = w0 + lane;
+            // kCrcUnroll words per lane loaded before any is folded: the fold is a
+            // dependent chain of shared lookups, so the loads must be in flight together
+            for (; i + 32 * (kCrcUnroll - 1) < w1; i += 32 * kCrcUnroll) {
+                uint32_t w[kCrcUnroll];
+#pragma unroll
+                for (int j = 0; j < kCrcUnroll; ++j) w[j] = __ldg(wp + i + 32 * j);
+#pragma unroll
+                for (int j = 0; j < kCrcUnroll; ++j) B = apply_g(g, B, lane & 7) ^ w[j];
+                last = (int64_t)(i + 32 * (kCrcUnroll - 1) - w0);
+            }
+            for (; i < w1; i += 32) {
                 B = apply_g(g, B, lane & 7) ^ __ldg(wp + i);
                 last = (int64_t)(i - w0);
             }
