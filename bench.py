@@ -183,6 +183,60 @@ def run_step(vol, dims, bs, cands, r, ws, spacing=(1.0, 1.0, 1.0), stage_events=
                 ntri=int(p.tris.shape[0]), nvert=int(p.verts.shape[0]), payload=int(regs["block_nbytes"].sum()))
 
 
+def timed_lanes(args, lanes, local, vals, dims, bs, cands, r, ws, info):
+    """The same K steps as the serial timed loop, dealt to `lanes` host
+    threads, each with its own stream and workspaces (a serving process
+    keeps several volumes in flight): one step's host syncs (the block
+    statistics read-back before the plan, the mesh-size read-back) and
+    launch gaps are filled by another step's kernels.  Timed on the device:
+    a start event on the launching thread's stream that every lane waits on,
+    and a stop event after every lane's last kernel.  Every step's triangle
+    count is checked against the serial run's."""
+    from paper_2408_05462_b200 import device as D
+
+    wss = [ws] + [D.Workspaces() for _ in range(lanes - 1)]
+    sts = [torch.cuda.Stream() for _ in range(lanes)]
+    share = [args.steps // lanes + (1 if i < args.steps % lanes else 0) for i in range(lanes)]
+    go = torch.cuda.Event()
+    ends = [torch.cuda.Event() for _ in range(lanes)]
+    bad = []
+
+    def lane(i, nsteps, timed):
+        torch.cuda.set_device(local)
+        with torch.cuda.stream(sts[i]):
+            if timed:
+                sts[i].wait_event(go)
+            for _ in range(nsteps):
+                out = run_step(vals, dims, bs, cands, r, wss[i], light=True)
+                if out["ntri"] != info["ntri"] or out["archive"] != info["archive"]:
+                    bad.append((i, out["ntri"], out["archive"]))
+            ends[i].record()
+
+    def run(counts, timed):
+        th = [threading.Thread(target=lane, args=(i, counts[i], timed)) for i in range(lanes)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+
+    run([1] * lanes, False)  # each lane's workspaces sized once, untimed
+    torch.cuda.synchronize()
+    start = torch.cuda.Event(enable_timing=True)
+    stop = torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        start.record()
+        go.record()
+        run(share, True)
+        cur = torch.cuda.current_stream()
+        for e in ends:
+            cur.wait_event(e)
+        stop.record()
+        torch.cuda.synchronize()
+    if bad:
+        raise RuntimeError(f"lane steps differ from the serial step: {bad[:4]}")
+    return start.elapsed_time(stop) / args.steps, clk
+
+
 def kernel_bytes(name, info, N):
     """Algorithmic bytes per launch of the main kernels: each
     kernel's share of its stage's algorithmic bytes -- input reads, archive /
@@ -295,6 +349,8 @@ def main():
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="slab mode: n x n x nN volume (weak) or one n^3 volume split over the ranks (strong)")
     ap.add_argument("--no-api-e2e", action="store_true", help="skip the drop-in API e2e timing")
+    ap.add_argument("--lanes", type=int, default=1,
+                    help="host threads (own stream + workspaces each) sharing the K device-resident steps")
     ap.add_argument("--dist1", action="store_true",
                     help="run the distributed (slab) path even at N=1 (one NCCL rank)")
     ap.add_argument("--backend", default=None, help="torch.distributed backend (default nccl; gloo for 1-GPU tests)")
@@ -397,6 +453,10 @@ def main():
         torch.cuda.synchronize()
     launches = L.chr_launch_count() - l0
     ms = start.elapsed_time(stop) / args.steps
+    ms_1lane = ms
+    lanes = 1 if dist else max(1, args.lanes)
+    if lanes > 1:
+        ms, clk = timed_lanes(args, lanes, local, vals, dims, bs, cands, r, ws, info)
     if dist:
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -561,8 +621,10 @@ def main():
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded torch GRF; no public dataset)",
+        "ms_per_step_1lane": ms_1lane,
         "config": {
             "workload": workload_name(args.config, n, bs, r, cands),
+            "lanes": lanes,
             "dims": list(dims), "block_size": bs, "regions": info["nreg"], "regions_selected": info["nsel"],
             "archive_bytes": info["archive"], "selected_samples": info["n_sel"], "cells": info["cells"],
             "triangles": info["ntri"], "vertices": info["nvert"],
